@@ -1,0 +1,212 @@
+/* kvc.h -- C-ABI of the B200-native cluster-level KV-cache hot path (Mosaic, arXiv 2604.10060).
+ *
+ * Drop-in boundary for the reference's `kvclust::core` hot path. The
+ * reference has no FFI; its boundary is the C++ API of HierIndex / TieredStore / Maintainer /
+ * retrieve driven by StreamEngine. Each entry point below names the reference interface it
+ * replaces (paths relative to /root/reference/proj/core). Conventions:
+ *   - plain pointers and sizes only; no C++ or torch types cross this ABI;
+ *   - every call returns an int status (KVC_OK or a negative KVC_E_* code); C++ exceptions of
+ *     the reference's kvclust::Error hierarchy (include/kvclust/error.hpp:9-82) map one-to-one
+ *     onto the codes, and kvc_last_error() returns the message;
+ *   - `mem` arguments say where a buffer lives: KVC_MEM_HOST (pageable or pinned host memory;
+ *     the call copies it in/out on the context's stream) or KVC_MEM_DEVICE (device pointer on
+ *     the context's GPU, consumed/produced in stream order);
+ *   - a context is single-threaded like the reference: one writer.
+ */
+#ifndef KVC_H
+#define KVC_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ------------------------------------------------------------------ status codes */
+#define KVC_OK 0
+#define KVC_E_GENERIC -1
+#define KVC_E_DEGENERATE -2      /* DegenerateVector   error.hpp:15 */
+#define KVC_E_DIM -3             /* DimMismatch        error.hpp:20 */
+#define KVC_E_EMPTY_INPUT -4     /* EmptyInput         error.hpp:26 */
+#define KVC_E_EMPTY_CLUSTER -5   /* EmptyCluster       error.hpp:31 */
+#define KVC_E_TOO_FEW -6         /* TooFewPoints       error.hpp:36 */
+#define KVC_E_BAD_LAYER -7       /* BadLayer           error.hpp:41 */
+#define KVC_E_UNKNOWN_CLUSTER -8 /* UnknownCluster     error.hpp:46 */
+#define KVC_E_EMPTY_INDEX -9     /* EmptyIndex         error.hpp:51 */
+#define KVC_E_CONFIG -10         /* ConfigError        error.hpp:57 */
+#define KVC_E_INVARIANT -11      /* InvariantViolation error.hpp:69 */
+#define KVC_E_CUDA -20           /* CUDA runtime failure (no reference counterpart) */
+#define KVC_E_CAPACITY -21       /* a device table/page pool is full (raise the kvc_cfg limit) */
+#define KVC_E_NO_DEVICE -22      /* no CUDA device: the product has no CPU fallback */
+
+#define KVC_MEM_HOST 0
+#define KVC_MEM_DEVICE 1
+
+#define KVC_DTYPE_F32 0
+#define KVC_DTYPE_BF16 1
+
+/* TransferCause (store.hpp:33) */
+#define KVC_CAUSE_RETRIEVAL 0
+#define KVC_CAUSE_MAINTENANCE 1
+#define KVC_CAUSE_PREFETCH 2
+#define KVC_CAUSE_COMPLETION 3
+#define KVC_CAUSE_OFFLOAD 4
+
+#if defined(__GNUC__)
+#define KVC_API __attribute__((visibility("default")))
+#else
+#define KVC_API
+#endif
+
+typedef struct kvc_ctx kvc_ctx;
+
+/* ------------------------------------------------------------------ configuration
+ * The first block is EngineConfig flattened (engine.hpp:21-33 with RetrievalConfig
+ * retrieval.hpp:20-32, MaintainerConfig maintainer.hpp:18-34, BuildConfig index.hpp:76-82,
+ * CostModel store.hpp:17-31), field-for-field, same defaults (kvc_cfg_default). The second
+ * block sizes the device data plane (no reference counterpart). */
+typedef struct {
+  int32_t k_v, k_s, window_frames, prefetch_k, prefetch_enabled, token_mode;
+  int64_t token_budget;
+  double lookup_cost_per_candidate_us, compute_cost_per_token_us;
+  double tau_min, tau_max, n0;
+  int32_t defer_host_splits, max_split_depth;
+  double visual_floor;
+  int32_t target_visual_cluster_size, target_semantic_cluster_size, kmeans_max_iters;
+  double kmeans_tol;
+  double alpha_us, beta_us_per_byte;
+  int64_t bytes_per_entry, device_capacity_entries;
+  int32_t build_batch_frames, batched_ingest;
+  double ingest_overhead_us;
+  int32_t offload_horizon_frames;
+  uint64_t seed;
+  /* ---- device data plane ---- */
+  int32_t kv_dtype;            /* KVC_DTYPE_F32 (bit-exact fp32 keys) or KVC_DTYPE_BF16 */
+  int32_t page_tokens;         /* tokens per K/V page (cluster-contiguous store), default 64 */
+  int64_t max_pages;           /* page-pool size (0 = derive from pool_bytes) */
+  int64_t pool_bytes;          /* page-pool bytes when max_pages == 0, default 1 GiB */
+  int32_t max_slots;           /* live-cluster table capacity, default 65536 */
+  int32_t max_cluster_pages;   /* member pages per cluster, default 256 */
+  int32_t max_buffer_pages;    /* pending-split buffer pages per cluster, default 64 */
+  int32_t max_partitions;      /* visual partitions, default 4096 */
+  int32_t max_candidates;      /* clusters (+ buffers) scored per domain per call, default 1024 */
+  int32_t max_tokens;          /* tokens per frame, default 256 */
+  int32_t parity_mode;         /* materialise attended (frame, token) sets on the host */
+  int32_t check_invariants;    /* run the structural self-check after build/query (engine.cpp:91,235) */
+} kvc_cfg;
+
+KVC_API void kvc_cfg_default(kvc_cfg* cfg);
+
+/* ------------------------------------------------------------------ lifetime
+ * StreamEngine(const EngineConfig&, int d, int L)  (engine.hpp:64, engine.cpp:37-44).
+ * L is the number of clustering domains (the reference's layer_id space; on a GQA model one
+ * domain per (layer, KV head)). Binds the calling thread's current CUDA device. */
+KVC_API int kvc_create(const kvc_cfg* cfg, int32_t d, int32_t L, kvc_ctx** out);
+KVC_API void kvc_destroy(kvc_ctx* ctx);
+KVC_API const char* kvc_last_error(void);
+/* The context's compute stream (cudaStream_t as void*), for event timing / interop. */
+KVC_API void* kvc_stream(kvc_ctx* ctx);
+
+/* ------------------------------------------------------------------ hot path
+ * Frame ingest: StreamEngine::process(Frame) (engine.cpp:134-174) = build buffering
+ * (engine.cpp:161-166 -> build_index index.cpp:364-450), Maintainer::place_frame
+ * (maintainer.cpp:37-53), Maintainer::on_insert for every (layer, token) in layer-major order
+ * (maintainer.cpp:88-176), push_window / repin / apply_cadence (engine.cpp:54-132).
+ * visual: [d] f32 host. keys/values: [L][T][d] in cfg.kv_dtype, host or device (`mem`).
+ * assigned (optional, host [L*T]): routed cluster id per entry, the return value of
+ * on_insert (-1 while the frame waits for the batch build). partition (optional): placed id. */
+KVC_API int kvc_ingest_frame(kvc_ctx* ctx, int64_t frame_id, const float* visual, const void* keys,
+                     const void* values, int32_t T, int32_t mem, int64_t* assigned,
+                     int64_t* partition);
+
+/* Decode step: StreamEngine::process(Query) (engine.cpp:176-237) -> retrieve()
+ * (retrieval.cpp:45-143), then attention over each domain's attended set (members of the
+ * selected clusters U the local window; no reference counterpart):
+ * out[l] = sum_t softmax(q_l . k_t / sqrt(d)) v_t, fp32.
+ * q: [L][d] f32 (`q_mem`); out: [L][d] f32 (`out_mem`), may be NULL. gt: ground-truth frames
+ * for recall (host, may be NULL). */
+KVC_API int kvc_decode_step(kvc_ctx* ctx, int64_t query_id, const float* q, int32_t q_mem, float* out,
+                    int32_t out_mem, const int64_t* gt, int32_t n_gt);
+
+/* Views of the last decode step's RetrievalResult (retrieval.hpp:49-71). Each returns the
+ * element count and copies at most `cap` elements. */
+KVC_API int kvc_last_ranked(kvc_ctx* ctx, int32_t layer, int64_t* ids, int32_t* is_buffer, int32_t cap);
+KVC_API int kvc_last_selected(kvc_ctx* ctx, int32_t layer, int64_t* ids, int32_t cap);
+/* attended (frame, token), sorted; needs cfg.parity_mode */
+KVC_API int kvc_last_attended(kvc_ctx* ctx, int32_t layer, int64_t* frames, int32_t* tokens, int32_t cap);
+/* lat[5] = lookup, transfer, stall, completion, compute (retrieval.hpp:39-47);
+ * ints[5] = verified_clusters, prefetch_hits, rep_count, n_predicted, attended_count */
+KVC_API int kvc_last_layer_meta(kvc_ctx* ctx, int32_t layer, double* lat, int64_t* ints);
+/* dd[2] = ttft_us, recall */
+KVC_API int kvc_last_query_meta(kvc_ctx* ctx, double* dd);
+/* FNV-1a attended digest (engine.cpp:18-35); needs cfg.parity_mode */
+KVC_API uint64_t kvc_last_digest(kvc_ctx* ctx);
+
+/* oracle_flat_topk (retrieval.cpp:145-164) computed on the device: k best candidates of
+ * rep_set(layer) for q ([d] f32 host). Returns the count. */
+KVC_API int kvc_flat_topk(kvc_ctx* ctx, const float* q, int32_t layer, int32_t k, int64_t* ids,
+                  int32_t* is_buffer);
+
+/* Forces the batch build of buffered frames (engine.cpp:202 "a query cannot wait"). */
+KVC_API int kvc_build_now(kvc_ctx* ctx);
+
+/* Bulk construction: HierIndex::add_partition (index.cpp:59-69) + add_cluster
+ * (index.cpp:97-120) for every cluster of one partition + TieredStore::adopt (store.cpp:82-86).
+ * Installs, for each domain l, n_clusters[l] clusters whose members are the rows of
+ * keys/values [L][N][d] (kv dtype, `mem`) with cluster index assign[l*N + i] in [0,C);
+ * member (frame, token) = (frame_ids[i], token_ids[i]). Representatives / variances are the
+ * exact Eq. 1/2 statistics (compute_representative / compute_variance, index.cpp:345-362).
+ * Clusters are created layer by layer, cluster index ascending. Returns the partition id. */
+KVC_API int kvc_bulk_load(kvc_ctx* ctx, const float* visual, const void* keys, const void* values,
+                  int32_t N, int32_t C, const int32_t* assign, const int64_t* frame_ids,
+                  const int32_t* token_ids, int32_t mem, int64_t* partition);
+
+/* ------------------------------------------------------------------ index / store views */
+KVC_API int kvc_n_clusters(kvc_ctx* ctx);
+KVC_API int kvc_cluster_ids(kvc_ctx* ctx, int64_t* ids, int32_t cap);
+/* info[10] = layer, parent, n_members, n_buffer, stat_count, lazy, residence (0 device,
+ * 1 host), device_tail, first_frame, last_touch; var; rep[d]; buffer_rep[d] (fp64, read
+ * back from the device masters). Mirrors ClusterRecord (index.hpp:29-50). */
+KVC_API int kvc_cluster(kvc_ctx* ctx, int64_t id, int64_t* info, double* var, double* rep,
+                double* buffer_rep);
+/* members (which=0) or buffer (which=1) as (frame, token) in stored order */
+KVC_API int kvc_cluster_entries(kvc_ctx* ctx, int64_t id, int32_t which, int64_t* frames,
+                        int32_t* tokens, int32_t cap);
+/* member / buffer payload rows read back from the device store: keys/values [n][d] f32 */
+KVC_API int kvc_cluster_payload(kvc_ctx* ctx, int64_t id, int32_t which, float* keys, float* values,
+                        int32_t cap);
+KVC_API int kvc_n_partitions(kvc_ctx* ctx);
+KVC_API int kvc_partition(kvc_ctx* ctx, int32_t p, double* visual_rep, int64_t* frames, int32_t cap);
+KVC_API int kvc_partition_layer(kvc_ctx* ctx, int32_t p, int32_t layer, int64_t* ids, int32_t cap);
+/* MaintainerStats (maintainer.hpp:36-46) -> out[9] */
+KVC_API int kvc_maint_stats(kvc_ctx* ctx, int64_t* out);
+/* TransferLedger totals per cause (store.cpp:21-65): ops[5], bytes[5], cost_us[5];
+ * returns TieredStore::device_entries (store.hpp:97) */
+KVC_API int64_t kvc_ledger(kvc_ctx* ctx, int64_t* ops, int64_t* bytes, double* cost_us);
+KVC_API int kvc_ledger_log_size(kvc_ctx* ctx);
+/* op i: ints[4] = cause, to_device, cluster_id, bytes */
+KVC_API int kvc_ledger_op(kvc_ctx* ctx, int32_t i, int64_t* ints);
+/* HierIndex::check_invariants (index.cpp:263-343) + TieredStore::audit (store.cpp:183-189),
+ * including device-vs-host agreement of counts and page tables. */
+KVC_API int kvc_check(kvc_ctx* ctx);
+
+/* TieredStore::offload / fetch (store.cpp:95-130) for one cluster. Returns the simulated cost
+ * in *cost_us (the reference's ledger arithmetic). */
+KVC_API int kvc_offload(kvc_ctx* ctx, int64_t id, double* cost_us);
+KVC_API int kvc_fetch(kvc_ctx* ctx, int64_t id, int32_t cause, double* cost_us);
+
+/* ------------------------------------------------------------------ instrumentation */
+/* Kernel launches issued by this context since creation (for bench gpu_launches). */
+KVC_API int64_t kvc_launch_count(kvc_ctx* ctx);
+/* Timing of the last decode step's device phases in microseconds (CUDA events):
+ * t[0]=score/select, t[1]=attention, t[2]=combine, t[3]=whole step; and the algorithmic
+ * bytes of the attention launch (t[4]) */
+KVC_API int kvc_last_step_timing(kvc_ctx* ctx, double* t);
+/* Enables per-phase CUDA-event timing (off by default: it adds event records). */
+KVC_API void kvc_set_timing(kvc_ctx* ctx, int32_t on);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KVC_H */

@@ -1,0 +1,73 @@
+"""Builds the sm_100a shared library of the hot path: paper_2604_10060_b200/_lib/libkvc.so.
+
+Plain nvcc / g++ invocations (no torch extension machinery): the library exposes the C-ABI of
+include/kvc.h and links only the CUDA runtime. Objects are rebuilt when a source is newer.
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+CSRC = os.path.join(HERE, "csrc")
+OUT = os.path.join(HERE, "_lib")
+LIB = os.path.join(OUT, "libkvc.so")
+
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+# -ffp-contract=off / --fmad=false: the fp64 statistics must reproduce the reference's
+# sequential, uncontracted arithmetic (reference CMakeLists.txt:11-13).
+CXXFLAGS = ["-std=c++17", "-O3", "-fPIC", "-ffp-contract=off", "-fvisibility=hidden", "-Wall",
+            "-Wextra", "-Wno-unused-parameter"]
+NVFLAGS = ["-std=c++17", "-O3", "-lineinfo", "--fmad=false", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
+           "-Xcompiler", "-ffp-contract=off", "-Xptxas", "-v"] + ARCH
+
+SOURCES = ["kmeans.cpp", "context.cpp", "context_query.cpp", "abi.cpp", "kernels.cu"]
+HEADERS = ["kvc_core.hpp", "kmeans.hpp", "context.hpp", os.path.join("..", "..", "include", "kvc.h")]
+
+
+def _stale(obj: str, src: str) -> bool:
+    if not os.path.exists(obj):
+        return True
+    t = os.path.getmtime(obj)
+    deps = [src] + [os.path.join(CSRC, h) for h in HEADERS]
+    return any(os.path.getmtime(p) > t for p in deps if os.path.exists(p))
+
+
+def build(verbose: bool = False) -> str:
+    os.makedirs(OUT, exist_ok=True)
+    objs = []
+    procs = []
+    for s in SOURCES:
+        src = os.path.join(CSRC, s)
+        obj = os.path.join(OUT, s + ".o")
+        objs.append(obj)
+        if not _stale(obj, src):
+            continue
+        if s.endswith(".cu"):
+            cmd = [NVCC, *NVFLAGS, "-I", os.path.join(ROOT, "include"), "-c", src, "-o", obj]
+        else:
+            cmd = ["g++", *CXXFLAGS, "-I", "/usr/local/cuda/include", "-I", os.path.join(ROOT, "include"),
+                   "-c", src, "-o", obj]
+        procs.append((cmd, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT,
+                                            text=True)))
+    for cmd, p in procs:
+        out, _ = p.communicate()
+        if p.returncode != 0:
+            sys.stderr.write(out)
+            raise RuntimeError("compile failed: " + " ".join(cmd))
+        if verbose and out:
+            sys.stderr.write(out)
+        with open(os.path.join(OUT, os.path.basename(cmd[-1]) + ".log"), "w") as f:
+            f.write(out)
+    if procs or not os.path.exists(LIB):
+        cmd = ["g++", "-shared", "-o", LIB, *objs, "-L/usr/local/cuda/lib64", "-lcudart",
+               "-Wl,-rpath,/usr/local/cuda/lib64"]
+        subprocess.run(cmd, check=True)
+    return LIB
+
+
+if __name__ == "__main__":
+    print(build(verbose="-v" in sys.argv))

@@ -1,0 +1,326 @@
+// abi.cpp -- the extern "C" boundary (include/kvc.h). Every entry point catches kvc::Error and
+// returns its code; no exception crosses the ABI (SURVEY.md §8(b) "Errors").
+#include <cstring>
+#include <memory>
+#include <string>
+
+#include "../../include/kvc.h"
+#include "context.hpp"
+
+using kvc::Context;
+
+struct kvc_ctx {
+  std::unique_ptr<Context> impl;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return KVC_OK;
+  } catch (const kvc::Error& e) {
+    g_err = e.what();
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_err = "host allocation failed";
+    return KVC_E_GENERIC;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return KVC_E_GENERIC;
+  }
+}
+
+template <class T>
+int copy_out(const std::vector<T>& v, T* dst, int cap) {
+  const int n = static_cast<int>(v.size());
+  if (dst)
+    for (int i = 0; i < n && i < cap; ++i) dst[i] = v[static_cast<std::size_t>(i)];
+  return n;
+}
+
+}  // namespace
+
+extern "C" {
+
+void kvc_cfg_default(kvc_cfg* c) {
+  std::memset(c, 0, sizeof(*c));
+  // EngineConfig defaults (engine.hpp:21-33 and the nested structs)
+  c->k_v = 4;
+  c->k_s = 4;
+  c->window_frames = 4;
+  c->prefetch_k = 4;
+  c->prefetch_enabled = 0;
+  c->token_mode = 0;
+  c->token_budget = 256;
+  c->lookup_cost_per_candidate_us = 0.02;
+  c->compute_cost_per_token_us = 0.6;
+  c->tau_min = 0.05;
+  c->tau_max = 0.3;
+  c->n0 = 32.0;
+  c->defer_host_splits = 1;
+  c->max_split_depth = 4;
+  c->visual_floor = 0.75;
+  c->target_visual_cluster_size = 8;
+  c->target_semantic_cluster_size = 32;
+  c->kmeans_max_iters = 50;
+  c->kmeans_tol = 1e-6;
+  c->alpha_us = 10.0;
+  c->beta_us_per_byte = 0.001;
+  c->bytes_per_entry = 0;
+  c->device_capacity_entries = 1 << 20;
+  c->build_batch_frames = 32;
+  c->batched_ingest = 0;
+  c->ingest_overhead_us = 10.0;
+  c->offload_horizon_frames = 16;
+  c->seed = 0;
+  // device data plane
+  c->kv_dtype = KVC_DTYPE_F32;
+  c->page_tokens = 64;
+  c->max_pages = 0;
+  c->pool_bytes = 1LL << 30;
+  c->max_slots = 65536;
+  c->max_cluster_pages = 256;
+  c->max_buffer_pages = 64;
+  c->max_partitions = 4096;
+  c->max_candidates = 1024;
+  c->max_tokens = 256;
+  c->parity_mode = 0;
+  c->check_invariants = 0;
+}
+
+const char* kvc_last_error(void) { return g_err.c_str(); }
+
+int kvc_create(const kvc_cfg* cfg, int32_t d, int32_t L, kvc_ctx** out) {
+  return guard([&] {
+    if (!cfg || !out) kvc::fail(KVC_E_CONFIG, "null argument");
+    auto* h = new kvc_ctx;
+    try {
+      h->impl = std::make_unique<Context>(*cfg, d, L);
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+
+void kvc_destroy(kvc_ctx* ctx) { delete ctx; }
+
+void* kvc_stream(kvc_ctx* ctx) { return ctx ? static_cast<void*>(ctx->impl->stream()) : nullptr; }
+
+int kvc_ingest_frame(kvc_ctx* ctx, int64_t frame_id, const float* visual, const void* keys,
+                     const void* values, int32_t T, int32_t mem, int64_t* assigned,
+                     int64_t* partition) {
+  return guard([&] { ctx->impl->ingest_frame(frame_id, visual, keys, values, T, mem, assigned, partition); });
+}
+
+int kvc_decode_step(kvc_ctx* ctx, int64_t query_id, const float* q, int32_t q_mem, float* out,
+                    int32_t out_mem, const int64_t* gt, int32_t n_gt) {
+  return guard([&] { ctx->impl->decode_step(query_id, q, q_mem, out, out_mem, gt, n_gt); });
+}
+
+int kvc_last_ranked(kvc_ctx* ctx, int32_t layer, int64_t* ids, int32_t* is_buffer, int32_t cap) {
+  const auto& ls = ctx->impl->last_layers();
+  if (layer < 0 || layer >= static_cast<int>(ls.size())) return KVC_E_BAD_LAYER;
+  const auto& r = ls[static_cast<std::size_t>(layer)].ranked;
+  for (int i = 0; i < static_cast<int>(r.size()) && i < cap; ++i) {
+    ids[i] = r[static_cast<std::size_t>(i)].first;
+    is_buffer[i] = r[static_cast<std::size_t>(i)].second;
+  }
+  return static_cast<int>(r.size());
+}
+
+int kvc_last_selected(kvc_ctx* ctx, int32_t layer, int64_t* ids, int32_t cap) {
+  const auto& ls = ctx->impl->last_layers();
+  if (layer < 0 || layer >= static_cast<int>(ls.size())) return KVC_E_BAD_LAYER;
+  return copy_out(ls[static_cast<std::size_t>(layer)].selected, ids, cap);
+}
+
+int kvc_last_attended(kvc_ctx* ctx, int32_t layer, int64_t* frames, int32_t* tokens, int32_t cap) {
+  const auto& ls = ctx->impl->last_layers();
+  if (layer < 0 || layer >= static_cast<int>(ls.size())) return KVC_E_BAD_LAYER;
+  const auto& a = ls[static_cast<std::size_t>(layer)].attended;
+  for (int i = 0; i < static_cast<int>(a.size()) && i < cap; ++i) {
+    frames[i] = a[static_cast<std::size_t>(i)].first;
+    tokens[i] = a[static_cast<std::size_t>(i)].second;
+  }
+  return static_cast<int>(a.size());
+}
+
+int kvc_last_layer_meta(kvc_ctx* ctx, int32_t layer, double* lat, int64_t* ints) {
+  const auto& ls = ctx->impl->last_layers();
+  if (layer < 0 || layer >= static_cast<int>(ls.size())) return KVC_E_BAD_LAYER;
+  const auto& lo = ls[static_cast<std::size_t>(layer)];
+  for (int i = 0; i < 5; ++i) lat[i] = lo.lat[i];
+  ints[0] = lo.verified;
+  ints[1] = lo.prefetch_hits;
+  ints[2] = lo.rep_count;
+  ints[3] = static_cast<int64_t>(lo.predicted.size());
+  ints[4] = lo.attended_count;
+  return KVC_OK;
+}
+
+int kvc_last_query_meta(kvc_ctx* ctx, double* dd) {
+  dd[0] = ctx->impl->last_ttft();
+  dd[1] = ctx->impl->last_recall();
+  return KVC_OK;
+}
+
+uint64_t kvc_last_digest(kvc_ctx* ctx) { return ctx->impl->last_digest(); }
+
+int kvc_flat_topk(kvc_ctx* ctx, const float* q, int32_t layer, int32_t k, int64_t* ids,
+                  int32_t* is_buffer) {
+  int n = 0;
+  const int rc = guard([&] {
+    auto r = ctx->impl->flat_topk(q, layer, k);
+    n = static_cast<int>(r.size());
+    for (int i = 0; i < n; ++i) {
+      ids[i] = r[static_cast<std::size_t>(i)].first;
+      is_buffer[i] = r[static_cast<std::size_t>(i)].second;
+    }
+  });
+  return rc != KVC_OK ? rc : n;
+}
+
+int kvc_build_now(kvc_ctx* ctx) {
+  return guard([&] { ctx->impl->build_now(); });
+}
+
+int kvc_bulk_load(kvc_ctx* ctx, const float* visual, const void* keys, const void* values,
+                  int32_t N, int32_t C, const int32_t* assign, const int64_t* frame_ids,
+                  const int32_t* token_ids, int32_t mem, int64_t* partition) {
+  return guard([&] {
+    const int64_t p = ctx->impl->bulk_load(visual, keys, values, N, C, assign, frame_ids, token_ids, mem);
+    if (partition) *partition = p;
+  });
+}
+
+int kvc_n_clusters(kvc_ctx* ctx) { return static_cast<int>(ctx->impl->cluster_ids().size()); }
+
+int kvc_cluster_ids(kvc_ctx* ctx, int64_t* ids, int32_t cap) {
+  return copy_out(ctx->impl->cluster_ids(), ids, cap);
+}
+
+int kvc_cluster(kvc_ctx* ctx, int64_t id, int64_t* info, double* var, double* rep,
+                double* buffer_rep) {
+  return guard([&] {
+    const kvc::Cluster* c = ctx->impl->cluster(id);
+    if (!c) kvc::fail(KVC_E_UNKNOWN_CLUSTER, "unknown cluster id: " + std::to_string(id));
+    info[0] = c->layer;
+    info[1] = c->parent;
+    info[2] = static_cast<int64_t>(c->members.size());
+    info[3] = static_cast<int64_t>(c->buffer.size());
+    info[4] = c->stat_count;
+    info[5] = c->lazy ? 1 : 0;
+    info[6] = c->host ? 1 : 0;
+    info[7] = c->device_tail;
+    info[8] = c->first_frame;
+    info[9] = c->last_touch;
+    double v = 0.0;
+    ctx->impl->cluster_stats(id, &v, rep, buffer_rep);
+    if (var) *var = v;
+  });
+}
+
+int kvc_cluster_entries(kvc_ctx* ctx, int64_t id, int32_t which, int64_t* frames, int32_t* tokens,
+                        int32_t cap) {
+  const kvc::Cluster* c = ctx->impl->cluster(id);
+  if (!c) return KVC_E_UNKNOWN_CLUSTER;
+  const auto& v = which == 0 ? c->members : c->buffer;
+  for (int i = 0; i < static_cast<int>(v.size()) && i < cap; ++i) {
+    frames[i] = v[static_cast<std::size_t>(i)].frame;
+    tokens[i] = v[static_cast<std::size_t>(i)].token;
+  }
+  return static_cast<int>(v.size());
+}
+
+int kvc_cluster_payload(kvc_ctx* ctx, int64_t id, int32_t which, float* keys, float* values,
+                        int32_t cap) {
+  int n = 0;
+  const int rc = guard([&] { n = ctx->impl->cluster_payload(id, which, keys, values, cap); });
+  return rc != KVC_OK ? rc : n;
+}
+
+int kvc_n_partitions(kvc_ctx* ctx) { return static_cast<int>(ctx->impl->partitions().size()); }
+
+int kvc_partition(kvc_ctx* ctx, int32_t p, double* visual_rep, int64_t* frames, int32_t cap) {
+  const auto& ps = ctx->impl->partitions();
+  if (p < 0 || p >= static_cast<int>(ps.size())) return KVC_E_UNKNOWN_CLUSTER;
+  const auto& part = ps[static_cast<std::size_t>(p)];
+  if (visual_rep) std::memcpy(visual_rep, part.vrep.data(), part.vrep.size() * sizeof(double));
+  return copy_out(part.frames, frames, cap);
+}
+
+int kvc_partition_layer(kvc_ctx* ctx, int32_t p, int32_t layer, int64_t* ids, int32_t cap) {
+  const auto& ps = ctx->impl->partitions();
+  if (p < 0 || p >= static_cast<int>(ps.size())) return KVC_E_UNKNOWN_CLUSTER;
+  if (layer < 0 || layer >= ctx->impl->L()) return KVC_E_BAD_LAYER;
+  return copy_out(ps[static_cast<std::size_t>(p)].per_layer[static_cast<std::size_t>(layer)], ids, cap);
+}
+
+int kvc_maint_stats(kvc_ctx* ctx, int64_t* out) {
+  std::memcpy(out, ctx->impl->maint_stats(), 9 * sizeof(int64_t));
+  return KVC_OK;
+}
+
+int64_t kvc_ledger(kvc_ctx* ctx, int64_t* ops, int64_t* bytes, double* cost_us) {
+  for (int i = 0; i < 5; ++i) {
+    ops[i] = 0;
+    bytes[i] = 0;
+    cost_us[i] = 0.0;
+  }
+  for (const auto& op : ctx->impl->ledger()) {  // TransferLedger::record (store.cpp:21-27)
+    ops[op.cause] += op.n_ops;
+    bytes[op.cause] += op.bytes;
+    cost_us[op.cause] += op.cost_us;
+  }
+  return ctx->impl->device_entries();
+}
+
+int kvc_ledger_log_size(kvc_ctx* ctx) { return static_cast<int>(ctx->impl->ledger().size()); }
+
+int kvc_ledger_op(kvc_ctx* ctx, int32_t i, int64_t* ints) {
+  const auto& lg = ctx->impl->ledger();
+  if (i < 0 || i >= static_cast<int>(lg.size())) return KVC_E_CONFIG;
+  const auto& op = lg[static_cast<std::size_t>(i)];
+  ints[0] = op.cause;
+  ints[1] = op.to_device ? 1 : 0;
+  ints[2] = op.cluster_id;
+  ints[3] = op.bytes;
+  return KVC_OK;
+}
+
+int kvc_check(kvc_ctx* ctx) {
+  return guard([&] { ctx->impl->check(); });
+}
+
+int kvc_offload(kvc_ctx* ctx, int64_t id, double* cost_us) {
+  return guard([&] {
+    const double c = ctx->impl->offload(id);
+    if (cost_us) *cost_us = c;
+  });
+}
+
+int kvc_fetch(kvc_ctx* ctx, int64_t id, int32_t cause, double* cost_us) {
+  return guard([&] {
+    if (cause < 0 || cause > 4) kvc::fail(KVC_E_CONFIG, "unknown transfer cause");
+    const double c = ctx->impl->fetch(id, cause);
+    if (cost_us) *cost_us = c;
+  });
+}
+
+int64_t kvc_launch_count(kvc_ctx* ctx) { return ctx->impl->launches(); }
+
+int kvc_last_step_timing(kvc_ctx* ctx, double* t) {
+  const double* s = ctx->impl->step_timing();
+  for (int i = 0; i < 5; ++i) t[i] = s[i];
+  return KVC_OK;
+}
+
+void kvc_set_timing(kvc_ctx* ctx, int32_t on) { ctx->impl->set_timing(on != 0); }
+
+}  // extern "C"

@@ -1,0 +1,1150 @@
+// context.cpp -- host control plane of one stream (see context.hpp).
+//
+// Reference semantics followed (paths under /root/reference/proj/core):
+//   engine.cpp:54-174     window / repin / build / cadence / ingest order
+//   engine.cpp:176-237    query path
+//   maintainer.cpp:37-242 placement, insert branches (decided on the GPU, replayed here),
+//                         split_members / materialize (host slow path)
+//   store.cpp:67-189      residency state machine and ledger arithmetic
+//   retrieval.cpp:45-143  per-layer bookkeeping around the GPU rankings
+//   index.cpp:97-190      cluster registration, frame -> cluster map, buffers
+#include "context.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+#include <string>
+
+#include "kmeans.hpp"
+
+namespace kvc {
+
+namespace {
+
+inline double tau_of(std::int64_t n, const kvc_cfg& c) {  // maintainer.cpp:11-14
+  return c.tau_min + (c.tau_max - c.tau_min) * std::exp(-static_cast<double>(n) / c.n0);
+}
+
+inline float bf16_to_f32(std::uint16_t h) {
+  std::uint32_t u = static_cast<std::uint32_t>(h) << 16;
+  float f;
+  std::memcpy(&f, &u, 4);
+  return f;
+}
+
+void rows_to_f32(const void* src, int bf16, std::size_t n, float* dst) {
+  if (!bf16) {
+    std::memcpy(dst, src, n * sizeof(float));
+    return;
+  }
+  const auto* h = static_cast<const std::uint16_t*>(src);
+  for (std::size_t i = 0; i < n; ++i) dst[i] = bf16_to_f32(h[i]);
+}
+
+}  // namespace
+
+// ============================================================================ lifetime
+
+Context::Context(const kvc_cfg& cfg, int d, int L) : cfg_(cfg), d_(d), L_(L) {
+  // EngineConfig::validate (engine.cpp:9-14), RetrievalConfig::validate (retrieval.cpp:10-16)
+  if (cfg_.k_v <= 0 || cfg_.k_s <= 0 || cfg_.window_frames <= 0 || cfg_.prefetch_k <= 0)
+    fail(-10, "retrieval budgets must be positive");
+  if (cfg_.token_budget < 1) fail(-10, "token budget must be at least 1");
+  if (cfg_.lookup_cost_per_candidate_us < 0.0 || cfg_.compute_cost_per_token_us < 0.0)
+    fail(-10, "cost constants must be non-negative");
+  if (cfg_.build_batch_frames < 1) fail(-10, "build batch must be at least 1 frame");
+  if (cfg_.ingest_overhead_us < 0.0) fail(-10, "ingestion overhead must be non-negative");
+  if (cfg_.offload_horizon_frames < 1) fail(-10, "offload horizon must be at least 1 frame");
+  if (d < 1 || L < 1) fail(-10, "stream dimensions must be positive");
+  // TieredStore / Maintainer constructor checks (store.cpp:67-74, maintainer.cpp:27-35)
+  if (cfg_.alpha_us < 0.0 || cfg_.beta_us_per_byte < 0.0) fail(-10, "transfer costs must be non-negative");
+  if (cfg_.device_capacity_entries <= 0) fail(-10, "device capacity must be positive");
+  if (cfg_.tau_min < 0.0 || cfg_.tau_max < cfg_.tau_min)
+    fail(-10, "variance thresholds must satisfy 0 <= tau_min <= tau_max");
+  if (cfg_.n0 <= 0.0) fail(-10, "threshold horizon must be positive");
+  if (cfg_.max_split_depth < 1) fail(-10, "split depth must be at least 1");
+  if (cfg_.visual_floor < -1.0 || cfg_.visual_floor > 1.0) fail(-10, "visual floor must be a cosine value");
+  if (cfg_.token_mode) fail(-10, "token-baseline mode is served by the token ablation entry points");
+  if (cfg_.kv_dtype != KVC_DTYPE_F32 && cfg_.kv_dtype != KVC_DTYPE_BF16) fail(-10, "kv_dtype");
+  if (cfg_.page_tokens < 8 || cfg_.page_tokens > 256 || cfg_.page_tokens % 8) fail(-10, "page_tokens");
+  if (d % 8 != 0 || d > 256) fail(-10, "the device path supports d % 8 == 0 and d <= 256");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    fail(-22, "no CUDA device: the B200 path has no CPU fallback");
+  es_ = cfg_.kv_dtype == KVC_DTYPE_BF16 ? 2 : 4;
+  KVC_CUDA(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
+  for (auto& e : ev_) KVC_CUDA(cudaEventCreate(&e));
+  alloc_device();
+  upload_tau();
+  mstats_[0] = 0;
+  last_.resize(static_cast<std::size_t>(L_));
+}
+
+Context::~Context() {
+  if (st_) cudaStreamSynchronize(st_);
+  for (void* p : dev_allocs_) cudaFree(p);
+  for (void* p : host_allocs_) cudaFreeHost(p);
+  for (auto& e : ev_) cudaEventDestroy(e);
+  if (st_) cudaStreamDestroy(st_);
+}
+
+void* Context::dalloc(std::size_t bytes) {
+  void* p = nullptr;
+  KVC_CUDA(cudaMalloc(&p, std::max<std::size_t>(bytes, 16)));
+  KVC_CUDA(cudaMemsetAsync(p, 0, std::max<std::size_t>(bytes, 16), st_));
+  dev_allocs_.push_back(p);
+  return p;
+}
+
+void* Context::halloc(std::size_t bytes) {
+  void* p = nullptr;
+  KVC_CUDA(cudaMallocHost(&p, std::max<std::size_t>(bytes, 16)));
+  std::memset(p, 0, std::max<std::size_t>(bytes, 16));
+  host_allocs_.push_back(p);
+  return p;
+}
+
+void Context::alloc_device() {
+  const std::int64_t S = cfg_.max_slots, d = d_, L = L_;
+  t_.d = d_;
+  t_.L = L_;
+  t_.P = cfg_.page_tokens;
+  t_.es = es_;
+  t_.kv_bf16 = cfg_.kv_dtype == KVC_DTYPE_BF16;
+  t_.max_slots = cfg_.max_slots;
+  t_.maxp = cfg_.max_cluster_pages;
+  t_.maxbp = cfg_.max_buffer_pages;
+  t_.max_parts = cfg_.max_partitions;
+  t_.cmax = cfg_.max_candidates;
+  t_.tmax = cfg_.max_tokens;
+  t_.W = cfg_.window_frames;
+  t_.page_bytes = 2LL * t_.P * d * es_;
+  t_.rpp = (t_.tmax + t_.P - 1) / t_.P;
+  const std::int64_t ring_pages = L * t_.W * t_.rpp;
+  t_.max_pages = cfg_.max_pages > 0 ? cfg_.max_pages : cfg_.pool_bytes / t_.page_bytes;
+  if (t_.max_pages <= ring_pages + 16) fail(-21, "page pool too small for the window ring");
+
+  t_.rep64 = static_cast<double*>(dalloc(S * d * 8));
+  t_.rep32 = static_cast<float*>(dalloc(S * d * 4));
+  t_.rnorm = static_cast<double*>(dalloc(S * 8));
+  t_.brep64 = static_cast<double*>(dalloc(S * d * 8));
+  t_.brep32 = static_cast<float*>(dalloc(S * d * 4));
+  t_.bnorm = static_cast<double*>(dalloc(S * 8));
+  t_.var = static_cast<double*>(dalloc(S * 8));
+  t_.stat = static_cast<std::int64_t*>(dalloc(S * 8));
+  t_.nmem = static_cast<std::int64_t*>(dalloc(S * 8));
+  t_.nbuf = static_cast<std::int32_t*>(dalloc(S * 4));
+  t_.lazy = static_cast<std::uint8_t*>(dalloc(S));
+  t_.resid = static_cast<std::uint8_t*>(dalloc(S));
+  t_.cid = static_cast<std::int64_t*>(dalloc(S * 8));
+  t_.npages = static_cast<std::int32_t*>(dalloc(S * 4));
+  t_.pages = static_cast<std::int32_t*>(dalloc(S * t_.maxp * 4));
+  t_.nbpages = static_cast<std::int32_t*>(dalloc(S * 4));
+  t_.bpages = static_cast<std::int32_t*>(dalloc(S * t_.maxbp * 4));
+  t_.pg_fill = static_cast<std::int32_t*>(dalloc(t_.max_pages * 4));
+  t_.free_stack = static_cast<std::int32_t*>(dalloc(t_.max_pages * 4));
+  t_.free_top = static_cast<std::int32_t*>(dalloc(16));
+  t_.pool = static_cast<std::uint8_t*>(dalloc(static_cast<std::size_t>(t_.max_pages) * t_.page_bytes));
+  t_.ring_pages = static_cast<std::int32_t*>(dalloc(ring_pages * 4));
+  t_.ring_owner = static_cast<std::int32_t*>(dalloc(L * t_.W * t_.tmax * 4));
+  t_.ring_count = static_cast<std::int32_t*>(dalloc(t_.W * 4));
+  t_.vrep = static_cast<double*>(dalloc(static_cast<std::int64_t>(t_.max_parts) * d * 8));
+  t_.vnorm = static_cast<double*>(dalloc(static_cast<std::int64_t>(t_.max_parts) * 8));
+  t_.n_parts = static_cast<std::int32_t*>(dalloc(16));
+  t_.pl_off = static_cast<std::int32_t*>(dalloc(static_cast<std::int64_t>(t_.max_parts) * L * 4));
+  t_.pl_cnt = static_cast<std::int32_t*>(dalloc(static_cast<std::int64_t>(t_.max_parts) * L * 4));
+  t_.pl_pool_cap = S * 4 + 1024;
+  t_.pl_pool = static_cast<std::int32_t*>(dalloc(t_.pl_pool_cap * 4));
+  t_.err = static_cast<std::int32_t*>(dalloc(16));
+
+  // page stack: ring pages are [0, ring_pages); the stack holds the rest
+  {
+    std::vector<std::int32_t> stack(static_cast<std::size_t>(t_.max_pages - ring_pages));
+    for (std::size_t i = 0; i < stack.size(); ++i)
+      stack[i] = static_cast<std::int32_t>(t_.max_pages - 1 - static_cast<std::int64_t>(i));
+    KVC_CUDA(cudaMemcpy(t_.free_stack, stack.data(), stack.size() * 4, cudaMemcpyHostToDevice));
+    std::int32_t top = static_cast<std::int32_t>(stack.size());
+    KVC_CUDA(cudaMemcpy(t_.free_top, &top, 4, cudaMemcpyHostToDevice));
+    std::vector<std::int32_t> rp(static_cast<std::size_t>(ring_pages));
+    std::iota(rp.begin(), rp.end(), 0);
+    KVC_CUDA(cudaMemcpy(t_.ring_pages, rp.data(), rp.size() * 4, cudaMemcpyHostToDevice));
+    ring_owner_h_.assign(static_cast<std::size_t>(L * t_.W * t_.tmax), -1);
+    ring_frame_.assign(static_cast<std::size_t>(t_.W), RingFrame{});
+    KVC_CUDA(cudaMemcpy(t_.ring_owner, ring_owner_h_.data(), ring_owner_h_.size() * 4, cudaMemcpyHostToDevice));
+  }
+  slot_id_.assign(static_cast<std::size_t>(S), -1);
+  free_slots_.resize(static_cast<std::size_t>(S));
+  for (std::int64_t i = 0; i < S; ++i) free_slots_[static_cast<std::size_t>(i)] = static_cast<std::int32_t>(S - 1 - i);
+  resid_h_.assign(static_cast<std::size_t>(S), 0);
+  layer_live_count_.assign(static_cast<std::size_t>(L), 0);
+
+  // frame input (kv dtype, [L][tmax][d])
+  const std::size_t frame_bytes = static_cast<std::size_t>(L) * t_.tmax * d * es_;
+  d_fk_ = dalloc(frame_bytes);
+  d_fv_ = dalloc(frame_bytes);
+  ensure_stage(static_cast<std::int64_t>(t_.maxp + t_.maxbp) * t_.P + 1);
+  ensure_idx(1 << 16, 1 << 12);
+
+  // ingest arrays
+  ia_.cand_n = static_cast<std::int32_t*>(dalloc(L * 4));
+  ia_.cand_slot = static_cast<std::int32_t*>(dalloc(L * t_.cmax * 4));
+  ia_.cand_buf = static_cast<std::uint8_t*>(dalloc(L * t_.cmax));
+  ia_.approx = static_cast<float*>(dalloc(L * t_.tmax * t_.cmax * 4));
+  ia_.ev_kind = static_cast<std::int32_t*>(dalloc(L * t_.tmax * 4));
+  ia_.ev_slot = static_cast<std::int32_t*>(dalloc(L * t_.tmax * 4));
+  ia_.stop_t = static_cast<std::int32_t*>(dalloc(L * 4 * 3 + 16));
+  ia_.stop_kind = ia_.stop_t + L;
+  ia_.stop_slot = ia_.stop_t + 2 * L;
+  ia_.n_exact = static_cast<std::int32_t*>(dalloc(L * 4));
+  d_active_ = static_cast<std::int32_t*>(dalloc(L * 4 * 2));
+  d_cursor_ = d_active_ + L;
+  h_active_ = static_cast<std::int32_t*>(halloc(L * 4 * 2));
+  h_cursor_ = h_active_ + L;
+  h_evk_ = static_cast<std::int32_t*>(halloc(L * t_.tmax * 4 * 2));
+  h_evs_ = h_evk_ + L * t_.tmax;
+  h_stop_ = static_cast<std::int32_t*>(halloc(L * 4 * 3 + 16));
+  ia_.active = d_active_;
+  ia_.cursor = d_cursor_;
+  ia_.fk = d_fk_;
+  ia_.fv = d_fv_;
+  ia_.defer = cfg_.defer_host_splits;
+
+  // decode result block
+  const int kv = cfg_.k_v, ks = cfg_.k_s, kp = cfg_.prefetch_k;
+  da_.max_items = 512;
+  da_.chunk_pages = 4;
+  std::size_t off = 0;
+  auto carve = [&](std::size_t bytes) {
+    std::size_t o = off;
+    off += (bytes + 15) & ~std::size_t(15);
+    return o;
+  };
+  const std::size_t o_parts = carve(L * kv * 4), o_nps = carve(L * 4), o_rs = carve(L * ks * 4),
+                    o_rb = carve(L * ks), o_nr = carve(L * 4), o_ps = carve(L * kp * 4),
+                    o_pb = carve(L * kp), o_np = carve(L * 4), o_vs = carve(L * ks * 4),
+                    o_nv = carve(L * 4), o_att = carve(L * 8), o_nc = carve(L * 4);
+  dec_bytes_ = off;
+  d_dec_ = dalloc(dec_bytes_);
+  h_dec_ = halloc(dec_bytes_);
+  auto* base = static_cast<std::uint8_t*>(d_dec_);
+  da_.parts = reinterpret_cast<std::int32_t*>(base + o_parts);
+  da_.n_parts_sel = reinterpret_cast<std::int32_t*>(base + o_nps);
+  da_.ranked_slot = reinterpret_cast<std::int32_t*>(base + o_rs);
+  da_.ranked_buf = base + o_rb;
+  da_.n_ranked = reinterpret_cast<std::int32_t*>(base + o_nr);
+  da_.pf_slot = reinterpret_cast<std::int32_t*>(base + o_ps);
+  da_.pf_buf = base + o_pb;
+  da_.n_pf = reinterpret_cast<std::int32_t*>(base + o_np);
+  da_.ver_slot = reinterpret_cast<std::int32_t*>(base + o_vs);
+  da_.n_ver = reinterpret_cast<std::int32_t*>(base + o_nv);
+  da_.attended = reinterpret_cast<std::int64_t*>(base + o_att);
+  da_.n_cand = reinterpret_cast<std::int32_t*>(base + o_nc);
+  da_.items = static_cast<int4*>(dalloc(L * da_.max_items * sizeof(int4)));
+  da_.n_items = static_cast<std::int32_t*>(dalloc(L * 4));
+  da_.part_ml = static_cast<float*>(dalloc(L * da_.max_items * 2 * 4));
+  da_.part_o = static_cast<float*>(dalloc(L * da_.max_items * d * 4));
+  da_.dom_done = static_cast<std::int32_t*>(dalloc(L * 4));
+  da_.k_v = kv;
+  da_.k_s = ks;
+  da_.prefetch_k = kp;
+  da_.prefetch = cfg_.prefetch_enabled;
+  da_.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(d)));
+  d_q_ = static_cast<float*>(dalloc(L * d * 4));
+  d_out_ = static_cast<float*>(dalloc(L * d * 4));
+  KVC_CUDA(cudaStreamSynchronize(st_));
+}
+
+void Context::upload_tau() {
+  const std::int64_t len = static_cast<std::int64_t>(t_.maxp) * t_.P + 2;
+  tau_host_.resize(static_cast<std::size_t>(len));
+  for (std::int64_t n = 0; n < len; ++n) tau_host_[static_cast<std::size_t>(n)] = tau_of(n, cfg_);
+  t_.tau_tab = static_cast<double*>(dalloc(len * 8));
+  t_.tau_len = static_cast<std::int32_t>(len);
+  KVC_CUDA(cudaMemcpy(t_.tau_tab, tau_host_.data(), len * 8, cudaMemcpyHostToDevice));
+}
+
+void Context::ensure_stage(std::int64_t rows) {
+  if (rows <= stage_rows_) return;
+  const std::size_t rb = static_cast<std::size_t>(d_) * es_;
+  stage_rows_ = std::max<std::int64_t>(rows, stage_rows_ * 2);
+  // old buffers stay allocated until destruction (rare growth)
+  d_stage_k_ = dalloc(stage_rows_ * rb);
+  d_stage_v_ = dalloc(stage_rows_ * rb);
+  d_stage_f32_ = static_cast<float*>(dalloc(stage_rows_ * d_ * 4));
+  h_stage_f32_ = static_cast<float*>(halloc(stage_rows_ * d_ * 4));
+}
+
+void Context::ensure_idx(std::int64_t n, std::int64_t runs) {
+  if (n > idx_cap_) {
+    idx_cap_ = std::max(n, idx_cap_ * 2);
+    d_idx_ = static_cast<std::int32_t*>(dalloc(idx_cap_ * 4));
+    h_idx_ = static_cast<std::int32_t*>(halloc(idx_cap_ * 4));
+  }
+  if (runs > runs_cap_) {
+    runs_cap_ = std::max(runs, runs_cap_ * 2);
+    d_runs_ = static_cast<AppendRun*>(dalloc(runs_cap_ * sizeof(AppendRun)));
+    h_runs_ = static_cast<AppendRun*>(halloc(runs_cap_ * sizeof(AppendRun)));
+  }
+}
+
+void Context::sync() { KVC_CUDA(cudaStreamSynchronize(st_)); }
+
+void Context::check_dev_err() {
+  std::int32_t e = 0;
+  KVC_CUDA(cudaMemcpy(&e, t_.err, 4, cudaMemcpyDeviceToHost));
+  if (!e) return;
+  std::int32_t z = 0;
+  KVC_CUDA(cudaMemcpy(t_.err, &z, 4, cudaMemcpyHostToDevice));
+  if (e & DERR_DEGENERATE) fail(-2, "cosine of zero vector");
+  if (e & DERR_PAGES) fail(-21, "page pool exhausted (raise kvc_cfg.pool_bytes)");
+  if (e & DERR_CLUSTER_PAGES) fail(-21, "cluster exceeds max_cluster_pages / max_buffer_pages");
+  if (e & DERR_CANDIDATES) fail(-21, "more candidates than max_candidates");
+  if (e & DERR_ITEMS) fail(-21, "attention work list overflow");
+  fail(-1, "device error");
+}
+
+// ============================================================================ index (host)
+
+Cluster& Context::C(std::int64_t id) {
+  if (id < 0 || id >= static_cast<std::int64_t>(clusters_.size()) || !clusters_[static_cast<std::size_t>(id)])
+    fail(-8, "unknown cluster id: " + std::to_string(id));
+  return *clusters_[static_cast<std::size_t>(id)];
+}
+
+const Cluster* Context::cluster(std::int64_t id) const {
+  if (id < 0 || id >= static_cast<std::int64_t>(clusters_.size())) return nullptr;
+  return clusters_[static_cast<std::size_t>(id)].get();
+}
+
+std::vector<std::int64_t> Context::cluster_ids() const {
+  std::vector<std::int64_t> out;
+  out.reserve(static_cast<std::size_t>(n_live_));
+  for (std::size_t i = 0; i < clusters_.size(); ++i)
+    if (clusters_[i]) out.push_back(static_cast<std::int64_t>(i));
+  return out;
+}
+
+std::int32_t Context::take_slot() {
+  if (free_slots_.empty()) fail(-21, "cluster table full (raise kvc_cfg.max_slots)");
+  std::int32_t s = free_slots_.back();
+  free_slots_.pop_back();
+  return s;
+}
+
+void Context::frame_add(std::int64_t frame, std::int64_t cid) {
+  auto& v = frame_clusters_[frame];
+  auto it = std::lower_bound(v.begin(), v.end(), cid);
+  if (it == v.end() || *it != cid) v.insert(it, cid);
+}
+
+void Context::frame_del(std::int64_t frame, std::int64_t cid) {
+  auto f = frame_clusters_.find(frame);
+  if (f == frame_clusters_.end()) return;
+  auto it = std::lower_bound(f->second.begin(), f->second.end(), cid);
+  if (it != f->second.end() && *it == cid) f->second.erase(it);
+  if (f->second.empty()) frame_clusters_.erase(f);
+}
+
+// HierIndex::add_cluster (index.cpp:97-120) for a cluster whose statistics the caller
+// installs on the device. Returns the id; assigns a device slot.
+std::int64_t Context::new_cluster(std::int32_t layer, std::int64_t parent,
+                                  std::vector<Member>&& members, bool host) {
+  if (members.empty()) fail(-5, "cluster with no members");
+  if (layer < 0 || layer >= L_) fail(-7, "layer out of range: " + std::to_string(layer));
+  auto c = std::make_unique<Cluster>();
+  c->id = static_cast<std::int64_t>(clusters_.size());
+  c->layer = layer;
+  c->parent = parent;
+  c->members = std::move(members);
+  c->stat_count = static_cast<std::int64_t>(c->members.size());
+  c->host = host;
+  c->first_frame = c->members.front().frame;
+  c->last_touch = c->members.front().frame;
+  for (const Member& m : c->members) {
+    c->first_frame = std::min(c->first_frame, m.frame);
+    c->last_touch = std::max(c->last_touch, m.frame);
+    frame_add(m.frame, c->id);
+  }
+  c->slot = take_slot();
+  slot_id_[static_cast<std::size_t>(c->slot)] = c->id;
+  resid_h_[static_cast<std::size_t>(c->slot)] = host ? 1 : 0;
+  parts_[static_cast<std::size_t>(parent)].per_layer[static_cast<std::size_t>(layer)].push_back(c->id);
+  layer_live_count_[static_cast<std::size_t>(layer)] += 1;
+  n_live_ += 1;
+  std::int64_t id = c->id;
+  clusters_.push_back(std::move(c));
+  return id;
+}
+
+// HierIndex::remove_cluster (index.cpp:122-145); device pages are released by the caller.
+void Context::drop_cluster(std::int64_t id) {
+  Cluster& c = C(id);
+  auto& sib = parts_[static_cast<std::size_t>(c.parent)].per_layer[static_cast<std::size_t>(c.layer)];
+  sib.erase(std::remove(sib.begin(), sib.end(), id), sib.end());
+  for (const Member& m : c.members) frame_del(m.frame, id);
+  for (const Member& m : c.buffer) frame_del(m.frame, id);
+  layer_live_count_[static_cast<std::size_t>(c.layer)] -= 1;
+  n_live_ -= 1;
+  std::int32_t s = c.slot;
+  launches_ += launch_free_slot_pages(t_, s, st_);
+  slot_id_[static_cast<std::size_t>(s)] = -1;
+  free_slots_.push_back(s);
+  clusters_[static_cast<std::size_t>(id)].reset();
+}
+
+// Device copy of per_layer_clusters[layer] of a partition, as slots.
+void Context::pl_upload(std::int64_t pid, int layer) {
+  Partition& p = parts_[static_cast<std::size_t>(pid)];
+  const auto& ids = p.per_layer[static_cast<std::size_t>(layer)];
+  const std::int32_t n = static_cast<std::int32_t>(ids.size());
+  std::int32_t& off = p.dev_off[static_cast<std::size_t>(layer)];
+  std::int32_t& cap = p.dev_cap[static_cast<std::size_t>(layer)];
+  if (n > cap) {
+    std::int32_t ncap = std::max<std::int32_t>(16, std::max(n, cap * 2));
+    if (pl_bump_ + ncap > t_.pl_pool_cap) {
+      // compact: re-lay every list contiguously
+      pl_bump_ = 0;
+      for (std::size_t q = 0; q < parts_.size(); ++q)
+        for (int l = 0; l < L_; ++l) {
+          parts_[q].dev_cap[static_cast<std::size_t>(l)] = 0;
+        }
+      for (std::size_t q = 0; q < parts_.size(); ++q)
+        for (int l = 0; l < L_; ++l) {
+          const std::int32_t m = static_cast<std::int32_t>(parts_[q].per_layer[static_cast<std::size_t>(l)].size());
+          const std::int32_t c2 = (static_cast<std::int64_t>(q) == pid && l == layer) ? ncap : m;
+          if (pl_bump_ + c2 > t_.pl_pool_cap) fail(-21, "partition-list pool full");
+          parts_[q].dev_off[static_cast<std::size_t>(l)] = static_cast<std::int32_t>(pl_bump_);
+          parts_[q].dev_cap[static_cast<std::size_t>(l)] = c2;
+          pl_bump_ += c2;
+          if (!(static_cast<std::int64_t>(q) == pid && l == layer) && m > 0) pl_upload(static_cast<std::int64_t>(q), l);
+        }
+    } else {
+      off = static_cast<std::int32_t>(pl_bump_);
+      cap = ncap;
+      pl_bump_ += ncap;
+    }
+  }
+  std::vector<std::int32_t> tmp(static_cast<std::size_t>(n));
+  for (std::int32_t i = 0; i < n; ++i) tmp[static_cast<std::size_t>(i)] = C(ids[static_cast<std::size_t>(i)]).slot;
+  // the stream is synchronised below, so pageable sources may be locals
+  if (n > 0) KVC_CUDA(cudaMemcpyAsync(t_.pl_pool + off, tmp.data(), n * 4, cudaMemcpyHostToDevice, st_));
+  const std::int64_t k = pid * L_ + layer;
+  KVC_CUDA(cudaMemcpyAsync(t_.pl_off + k, &off, 4, cudaMemcpyHostToDevice, st_));
+  KVC_CUDA(cudaMemcpyAsync(t_.pl_cnt + k, &n, 4, cudaMemcpyHostToDevice, st_));
+  KVC_CUDA(cudaStreamSynchronize(st_));
+}
+
+void Context::upload_partition(std::int64_t pid) {
+  const Partition& p = parts_[static_cast<std::size_t>(pid)];
+  double nrm = norm_d(p.vrep.data(), d_);
+  KVC_CUDA(cudaMemcpyAsync(t_.vrep + pid * d_, p.vrep.data(), d_ * 8, cudaMemcpyHostToDevice, st_));
+  KVC_CUDA(cudaMemcpyAsync(t_.vnorm + pid, &nrm, 8, cudaMemcpyHostToDevice, st_));
+  std::int32_t np = static_cast<std::int32_t>(parts_.size());
+  KVC_CUDA(cudaMemcpyAsync(t_.n_parts, &np, 4, cudaMemcpyHostToDevice, st_));
+  KVC_CUDA(cudaStreamSynchronize(st_));
+}
+
+void Context::flush_resid() {
+  if (!resid_dirty_) return;
+  KVC_CUDA(cudaMemcpyAsync(t_.resid, resid_h_.data(), resid_h_.size(), cudaMemcpyHostToDevice, st_));
+  KVC_CUDA(cudaStreamSynchronize(st_));
+  resid_dirty_ = false;
+}
+
+// ============================================================================ store (host)
+
+std::int64_t Context::entry_bytes() const {  // CostModel::entry_bytes (store.hpp:27-30)
+  return cfg_.bytes_per_entry > 0 ? cfg_.bytes_per_entry
+                                  : static_cast<std::int64_t>(d_) * 2 * static_cast<std::int64_t>(sizeof(float));
+}
+
+std::int64_t Context::side_entries(const Cluster& c) const {  // store.cpp:76-80
+  const std::int64_t buffered = static_cast<std::int64_t>(c.buffer.size());
+  if (!c.host) return static_cast<std::int64_t>(c.members.size()) + buffered;
+  return c.device_tail + buffered;
+}
+
+void Context::adopt(std::int64_t id) {  // store.cpp:82-86
+  Cluster& c = C(id);
+  device_entries_ += side_entries(c);
+  std::int64_t tk = tick_++;
+  if (!c.tracked) {
+    c.tracked = true;
+    c.last_use = tk;
+  }
+}
+
+void Context::forget(std::int64_t id) {  // store.cpp:88-93
+  Cluster& c = C(id);
+  device_entries_ -= side_entries(c);
+  c.tracked = false;
+  if (c.pinned) {
+    c.pinned = false;
+    pinned_ids_.erase(std::remove(pinned_ids_.begin(), pinned_ids_.end(), id), pinned_ids_.end());
+  }
+}
+
+void Context::touch(std::int64_t id) {  // store.cpp:139-141
+  Cluster& c = C(id);
+  c.tracked = true;
+  c.last_use = tick_++;
+}
+
+void Context::record(int cause, bool to_dev, std::int64_t id, std::int64_t bytes) {
+  LedgerOp op{cause, to_dev, id, 1, bytes,
+              1.0 * cfg_.alpha_us + static_cast<double>(bytes) * cfg_.beta_us_per_byte};
+  ledger_.push_back(op);
+}
+
+double Context::fetch(std::int64_t id, int cause) {  // store.cpp:95-113
+  Cluster& c = C(id);
+  touch(id);
+  if (!c.host) return 0.0;
+  const std::int64_t moved = static_cast<std::int64_t>(c.members.size()) - c.device_tail;
+  if (moved < 0) fail(-11, "device tail exceeds member count");
+  double paid = 0.0;
+  if (moved > 0) {
+    const std::int64_t bytes = moved * entry_bytes();
+    record(cause, true, id, bytes);
+    paid = ledger_.back().cost_us;
+    device_entries_ += moved;
+  }
+  c.host = false;
+  c.device_tail = 0;
+  resid_h_[static_cast<std::size_t>(c.slot)] = 0;
+  resid_dirty_ = true;
+  paid += enforce_capacity();
+  return paid;
+}
+
+double Context::offload(std::int64_t id) {  // store.cpp:115-130
+  Cluster& c = C(id);
+  const std::int64_t moved = !c.host ? static_cast<std::int64_t>(c.members.size()) : c.device_tail;
+  double paid = 0.0;
+  if (moved > 0) {
+    const std::int64_t bytes = moved * entry_bytes();
+    record(KVC_CAUSE_OFFLOAD, false, id, bytes);
+    paid = ledger_.back().cost_us;
+    device_entries_ -= moved;
+  }
+  c.host = true;
+  c.device_tail = 0;
+  resid_h_[static_cast<std::size_t>(c.slot)] = 1;
+  resid_dirty_ = true;
+  return paid;
+}
+
+double Context::enforce_capacity() {  // store.cpp:156-164
+  double paid = 0.0;
+  while (device_entries_ > cfg_.device_capacity_entries) {
+    const double cost = evict_one();
+    if (cost < 0.0) break;
+    paid += cost;
+  }
+  return paid;
+}
+
+double Context::evict_one() {  // store.cpp:166-181
+  std::int64_t victim = -1, vt = 0;
+  for (const auto& up : clusters_) {
+    if (!up || !up->tracked || up->pinned) continue;
+    if (side_entries(*up) == 0) continue;
+    if (!up->buffer.empty()) continue;
+    if (victim < 0 || up->last_use < vt) {
+      victim = up->id;
+      vt = up->last_use;
+    }
+  }
+  if (victim < 0) return -1.0;
+  return offload(victim);
+}
+
+// ============================================================================ engine (host)
+
+void Context::push_window(std::int64_t frame_id, int T) {  // engine.cpp:54-57
+  const int slot = static_cast<int>(frames_seen_ % t_.W);
+  window_.push_back({frame_id, slot, T});
+  while (static_cast<int>(window_.size()) > t_.W) window_.pop_front();
+}
+
+std::vector<std::int64_t> Context::window_owner_ids() const {
+  std::vector<std::int64_t> out;
+  for (const WinFrame& w : window_) {
+    auto it = frame_clusters_.find(w.frame_id);
+    if (it != frame_clusters_.end()) out.insert(out.end(), it->second.begin(), it->second.end());
+  }
+  std::sort(out.begin(), out.end());
+  out.erase(std::unique(out.begin(), out.end()), out.end());
+  return out;
+}
+
+void Context::repin() {  // engine.cpp:67-75 + TieredStore::pin (store.cpp:143-145)
+  for (std::int64_t id : pinned_ids_)
+    if (auto* c = clusters_[static_cast<std::size_t>(id)].get()) c->pinned = false;
+  pinned_ids_ = window_owner_ids();
+  for (std::int64_t id : pinned_ids_) C(id).pinned = true;
+}
+
+void Context::apply_cadence(std::int64_t frame_id, std::int64_t pid) {  // engine.cpp:95-132
+  if (last_partition_ >= 0 && pid >= 0 && pid != last_partition_) {
+    const Partition& closed = parts_[static_cast<std::size_t>(last_partition_)];
+    std::vector<std::int64_t> ids;
+    for (const auto& list : closed.per_layer) ids.insert(ids.end(), list.begin(), list.end());
+    for (std::int64_t cid : ids) {
+      const Cluster& c = C(cid);
+      if (!c.host && !c.lazy) {
+        const auto owners = window_owner_ids();
+        if (!std::binary_search(owners.begin(), owners.end(), cid)) offload(cid);
+      }
+    }
+  }
+  if (pid >= 0) last_partition_ = pid;
+  std::vector<std::int64_t> stale;
+  for (const auto& up : clusters_)
+    if (up && !up->host && !up->lazy && up->last_touch + cfg_.offload_horizon_frames < frame_id)
+      stale.push_back(up->id);
+  if (!stale.empty()) {
+    const auto owners = window_owner_ids();
+    for (std::int64_t cid : stale)
+      if (!std::binary_search(owners.begin(), owners.end(), cid)) offload(cid);
+  }
+  enforce_capacity();
+}
+
+std::int64_t Context::place_frame(std::int64_t frame_id, const float* visual) {
+  // maintainer.cpp:37-53
+  std::int64_t best = -1;
+  double best_sim = -2.0;
+  for (std::size_t p = 0; p < parts_.size(); ++p) {
+    const double sim = cosine_fd(visual, parts_[p].vrep.data(), d_);
+    if (sim > best_sim) {
+      best_sim = sim;
+      best = static_cast<std::int64_t>(p);
+    }
+  }
+  if (best >= 0 && best_sim >= cfg_.visual_floor) {  // HierIndex::append_frame (index.cpp:71-79)
+    Partition& p = parts_[static_cast<std::size_t>(best)];
+    p.frames.push_back(frame_id);
+    const double n = static_cast<double>(p.stat);
+    for (int i = 0; i < d_; ++i) p.vrep[static_cast<std::size_t>(i)] = (n * p.vrep[static_cast<std::size_t>(i)] + visual[i]) / (n + 1.0);
+    p.stat += 1;
+    upload_partition(best);
+    return best;
+  }
+  mstats_[8] += 1;  // partitions_opened
+  if (static_cast<std::int32_t>(parts_.size()) >= t_.max_parts) fail(-21, "too many partitions (raise max_partitions)");
+  Partition p;  // HierIndex::add_partition (index.cpp:59-69)
+  p.frames.push_back(frame_id);
+  p.vrep.assign(visual, visual + d_);
+  p.stat = 1;
+  p.per_layer.resize(static_cast<std::size_t>(L_));
+  p.dev_off.assign(static_cast<std::size_t>(L_), 0);
+  p.dev_cap.assign(static_cast<std::size_t>(L_), 0);
+  parts_.push_back(std::move(p));
+  const std::int64_t pid = static_cast<std::int64_t>(parts_.size()) - 1;
+  upload_partition(pid);
+  // empty device lists
+  std::vector<std::int32_t> z(static_cast<std::size_t>(L_), 0);
+  KVC_CUDA(cudaMemcpyAsync(t_.pl_cnt + pid * L_, z.data(), L_ * 4, cudaMemcpyHostToDevice, st_));
+  KVC_CUDA(cudaStreamSynchronize(st_));
+  return pid;
+}
+
+void Context::ingest_frame(std::int64_t frame_id, const float* visual, const void* keys,
+                           const void* values, int T, int mem, std::int64_t* assigned,
+                           std::int64_t* partition) {
+  if (T < 1 || T > t_.tmax) fail(-10, "tokens per frame outside [1, max_tokens]");
+  if (!visual || !keys || !values) fail(-10, "null frame buffer");
+  if (assigned) std::fill(assigned, assigned + static_cast<std::int64_t>(L_) * T, -1);
+  if (partition) *partition = -1;
+  // payload -> device frame buffer [L][tmax][d]
+  const std::size_t row = static_cast<std::size_t>(T) * d_ * es_;
+  const std::size_t pitch = static_cast<std::size_t>(t_.tmax) * d_ * es_;
+  const cudaMemcpyKind kind = mem == KVC_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  KVC_CUDA(cudaMemcpy2DAsync(d_fk_, pitch, keys, row, row, L_, kind, st_));
+  KVC_CUDA(cudaMemcpy2DAsync(d_fv_, pitch, values, row, row, L_, kind, st_));
+  const int ring_slot = static_cast<int>(frames_seen_ % t_.W);
+  launches_ += launch_ring_write(t_, d_fk_, d_fv_, T, ring_slot, st_);
+  for (int l = 0; l < L_; ++l)
+    std::fill_n(&ring_owner_h_[(static_cast<std::size_t>(l) * t_.W + ring_slot) * t_.tmax], t_.tmax, -1);
+  ring_frame_[static_cast<std::size_t>(ring_slot)] = RingFrame{frame_id, T};
+
+  if (!built_) {  // engine.cpp:161-166
+    PendingFrame pf;
+    pf.frame_id = frame_id;
+    pf.visual.assign(visual, visual + d_);
+    pf.T = T;
+    const std::size_t n = static_cast<std::size_t>(L_) * T * d_;
+    pf.keys_raw.resize(n * es_);
+    pf.vals_raw.resize(n * es_);
+    if (mem == KVC_MEM_DEVICE) {
+      KVC_CUDA(cudaMemcpyAsync(pf.keys_raw.data(), keys, n * es_, cudaMemcpyDeviceToHost, st_));
+      KVC_CUDA(cudaMemcpyAsync(pf.vals_raw.data(), values, n * es_, cudaMemcpyDeviceToHost, st_));
+      sync();
+    } else {
+      std::memcpy(pf.keys_raw.data(), keys, n * es_);
+      std::memcpy(pf.vals_raw.data(), values, n * es_);
+    }
+    pf.keys_f32.resize(n);
+    rows_to_f32(pf.keys_raw.data(), es_ == 2, n, pf.keys_f32.data());
+    pending_.push_back(std::move(pf));
+    push_window(frame_id, T);
+    frames_seen_ += 1;
+    if (static_cast<int>(pending_.size()) >= cfg_.build_batch_frames) build_now();
+    return;
+  }
+
+  const std::int64_t pid = place_frame(frame_id, visual);
+  if (partition) *partition = pid;
+  run_inserts(frame_id, pid, T, assigned);
+  push_window(frame_id, T);
+  frames_seen_ += 1;
+  repin();
+  apply_cadence(frame_id, pid);
+}
+
+// Runs on_insert for every (layer, token) of the frame in layer-major order
+// (engine.cpp:169-170). The GPU resolves every domain in parallel until a host event; the
+// host replays the outcomes in reference order and settles host events domain by domain so
+// ids, split seeds and LRU ticks are assigned exactly as the sequential reference does.
+void Context::run_inserts(std::int64_t frame_id, std::int64_t pid, int T, std::int64_t* assigned) {
+  const int ring_slot = static_cast<int>(frames_seen_ % t_.W);
+  const bool eager = !cfg_.defer_host_splits;
+  std::vector<int> cursor(static_cast<std::size_t>(L_), 0), replayed(static_cast<std::size_t>(L_), 0);
+  std::vector<int> active;
+  if (eager)
+    active.push_back(0);
+  else
+    for (int l = 0; l < L_; ++l) active.push_back(l);
+  int frontier = 0;
+  bool launch = true;
+  ia_.T = T;
+  ia_.pid = static_cast<std::int32_t>(pid);
+  ia_.ring_slot = ring_slot;
+  ia_.margin = 1e-4f;
+  while (frontier < L_) {
+    if (launch) {
+      flush_resid();
+      ia_.n_active = static_cast<std::int32_t>(active.size());
+      for (std::size_t i = 0; i < active.size(); ++i) {
+        h_active_[i] = active[i];
+      }
+      for (int l = 0; l < L_; ++l) h_cursor_[l] = cursor[static_cast<std::size_t>(l)];
+      KVC_CUDA(cudaMemcpyAsync(d_active_, h_active_, L_ * 8, cudaMemcpyHostToDevice, st_));
+      launches_ += launch_build_cands(t_, ia_, st_);
+      launches_ += launch_approx(t_, ia_, st_);
+      launches_ += launch_resolve(t_, ia_, st_);
+      KVC_CUDA(cudaMemcpyAsync(h_evk_, ia_.ev_kind, static_cast<std::size_t>(L_) * t_.tmax * 4, cudaMemcpyDeviceToHost, st_));
+      KVC_CUDA(cudaMemcpyAsync(h_evs_, ia_.ev_slot, static_cast<std::size_t>(L_) * t_.tmax * 4, cudaMemcpyDeviceToHost, st_));
+      KVC_CUDA(cudaMemcpyAsync(h_stop_, ia_.stop_t, static_cast<std::size_t>(L_) * 12, cudaMemcpyDeviceToHost, st_));
+      sync();
+      check_dev_err();
+      launch = false;
+    }
+    const int l = frontier;
+    const int stop = h_stop_[l];
+    const std::int32_t* evk = h_evk_ + static_cast<std::size_t>(l) * t_.tmax;
+    const std::int32_t* evs = h_evs_ + static_cast<std::size_t>(l) * t_.tmax;
+    std::int32_t* owner = &ring_owner_h_[(static_cast<std::size_t>(l) * t_.W + ring_slot) * t_.tmax];
+    for (int t = replayed[static_cast<std::size_t>(l)]; t < stop; ++t) {
+      const std::int32_t slot = evs[t];
+      const std::int64_t cid = slot_id_[static_cast<std::size_t>(slot)];
+      Cluster& c = C(cid);
+      mstats_[0] += 1;  // inserts
+      c.stat_count += 1;
+      c.last_touch = std::max(c.last_touch, frame_id);
+      frame_add(frame_id, cid);
+      owner[t] = slot;
+      switch (evk[t]) {
+        case EV_ABSORB:  // add_member + note_device_append (index.cpp:170-175, store.cpp:132-137)
+          c.members.push_back({frame_id, t});
+          if (c.host) c.device_tail += 1;
+          device_entries_ += 1;
+          touch(cid);
+          mstats_[1] += 1;
+          break;
+        case EV_BUFJOIN:  // add_to_buffer + note_device_buffer_append
+          c.buffer.push_back({frame_id, t});
+          device_entries_ += 1;
+          touch(cid);
+          mstats_[3] += 1;
+          break;
+        case EV_DEFER:  // lazy mark + buffer + register (maintainer.cpp:170-175)
+          mstats_[6] += 1;
+          c.lazy = true;
+          c.buffer.push_back({frame_id, t});
+          device_entries_ += 1;
+          touch(cid);
+          mstats_[3] += 1;
+          break;
+        default:
+          fail(-11, "unexpected device event kind");
+      }
+      if (assigned) assigned[static_cast<std::size_t>(l) * T + t] = cid;
+    }
+    replayed[static_cast<std::size_t>(l)] = stop;
+    if (stop >= T) {
+      frontier += 1;
+      if (eager && frontier < L_) {
+        active.assign(1, frontier);
+        launch = true;
+      }
+      continue;
+    }
+    const std::int64_t id = handle_host_event(frame_id, pid, l, stop, h_stop_[L_ + l], h_stop_[2 * L_ + l]);
+    if (assigned) assigned[static_cast<std::size_t>(l) * T + stop] = id;
+    cursor[static_cast<std::size_t>(l)] = stop + 1;
+    replayed[static_cast<std::size_t>(l)] = stop + 1;
+    if (stop + 1 < T) {
+      active.assign(1, l);
+      launch = true;
+    } else {
+      frontier += 1;
+      if (eager && frontier < L_) {
+        active.assign(1, frontier);
+        launch = true;
+      }
+    }
+  }
+}
+
+// ============================================================================ slow path
+
+std::int64_t Context::stage_cluster(std::int32_t slot, bool with_buffer) {
+  const Cluster& c = C(slot_id_[static_cast<std::size_t>(slot)]);
+  const std::int64_t rows = static_cast<std::int64_t>(c.members.size()) + (with_buffer ? static_cast<std::int64_t>(c.buffer.size()) : 0);
+  ensure_stage(rows + 1);
+  launches_ += launch_gather_cluster(t_, slot, with_buffer ? 1 : 0, d_stage_k_, d_stage_v_, 0, st_);
+  return rows;
+}
+
+void Context::stage_download(std::int64_t rows) {
+  launches_ += launch_to_f32(t_, d_stage_k_, d_stage_f32_, rows * d_, st_);
+  KVC_CUDA(cudaMemcpyAsync(h_stage_f32_, d_stage_f32_, static_cast<std::size_t>(rows) * d_ * 4, cudaMemcpyDeviceToHost, st_));
+  sync();
+}
+
+void Context::init_slots(const std::vector<std::int32_t>& slots,
+                         const std::vector<std::vector<double>>& reps,
+                         const std::vector<double>& vars, const std::vector<std::int64_t>& stats,
+                         const std::vector<std::int64_t>& nmem, const std::vector<std::int64_t>& cids,
+                         const std::vector<std::uint8_t>& resid, const std::vector<std::int32_t>* nbuf,
+                         const std::vector<std::vector<double>>* breps) {
+  // Host-computed exact statistics -> device tables. Few rows (split children / seeds):
+  // plain async copies from pinned staging, then the fp32 mirrors are refreshed on device.
+  const std::size_t n = slots.size();
+  if (n == 0) return;
+  for (std::size_t i = 0; i < n; ++i) {
+    const std::int64_t s = slots[i];
+    const double rn = norm_d(reps[i].data(), d_);
+    KVC_CUDA(cudaMemcpyAsync(t_.rep64 + s * d_, reps[i].data(), d_ * 8, cudaMemcpyHostToDevice, st_));
+    KVC_CUDA(cudaMemcpyAsync(t_.rnorm + s, &rn, 8, cudaMemcpyHostToDevice, st_));
+    KVC_CUDA(cudaMemcpyAsync(t_.var + s, &vars[i], 8, cudaMemcpyHostToDevice, st_));
+    KVC_CUDA(cudaMemcpyAsync(t_.stat + s, &stats[i], 8, cudaMemcpyHostToDevice, st_));
+    KVC_CUDA(cudaMemcpyAsync(t_.nmem + s, &nmem[i], 8, cudaMemcpyHostToDevice, st_));
+    KVC_CUDA(cudaMemcpyAsync(t_.cid + s, &cids[i], 8, cudaMemcpyHostToDevice, st_));
+    KVC_CUDA(cudaMemcpyAsync(t_.resid + s, &resid[i], 1, cudaMemcpyHostToDevice, st_));
+    const std::int32_t nb = nbuf ? (*nbuf)[i] : 0;
+    const std::uint8_t lz = nb > 0 ? 1 : 0;
+    KVC_CUDA(cudaMemcpyAsync(t_.nbuf + s, &nb, 4, cudaMemcpyHostToDevice, st_));
+    KVC_CUDA(cudaMemcpyAsync(t_.lazy + s, &lz, 1, cudaMemcpyHostToDevice, st_));
+    if (breps && nb > 0) {
+      const double bn = norm_d((*breps)[i].data(), d_);
+      KVC_CUDA(cudaMemcpyAsync(t_.brep64 + s * d_, (*breps)[i].data(), d_ * 8, cudaMemcpyHostToDevice, st_));
+      KVC_CUDA(cudaMemcpyAsync(t_.bnorm + s, &bn, 8, cudaMemcpyHostToDevice, st_));
+    }
+    // the pageable sources must stay alive until the copies complete
+    KVC_CUDA(cudaStreamSynchronize(st_));
+  }
+  std::vector<std::int32_t> sl(slots.begin(), slots.end());
+  ensure_idx(static_cast<std::int64_t>(n), 1);
+  std::memcpy(h_idx_, sl.data(), n * 4);
+  KVC_CUDA(cudaMemcpyAsync(d_idx_, h_idx_, n * 4, cudaMemcpyHostToDevice, st_));
+  launches_ += launch_refresh_mirror(t_, d_idx_, static_cast<std::int32_t>(n), st_);
+}
+
+// Appends staged rows idx[run.first .. run.first + run.n) to each run's slot, in order.
+void Context::append_runs_idx(const std::vector<AppendRun>& runs, const std::vector<std::int32_t>& idx,
+                              const void* src_k, const void* src_v) {
+  if (runs.empty()) return;
+  ensure_idx(static_cast<std::int64_t>(idx.size()), static_cast<std::int64_t>(runs.size()));
+  std::memcpy(h_idx_, idx.data(), idx.size() * 4);
+  std::memcpy(h_runs_, runs.data(), runs.size() * sizeof(AppendRun));
+  KVC_CUDA(cudaMemcpyAsync(d_idx_, h_idx_, idx.size() * 4, cudaMemcpyHostToDevice, st_));
+  KVC_CUDA(cudaMemcpyAsync(d_runs_, h_runs_, runs.size() * sizeof(AppendRun), cudaMemcpyHostToDevice, st_));
+  launches_ += launch_append_runs(t_, d_runs_, static_cast<std::int32_t>(runs.size()), d_idx_,
+                                  src_k ? src_k : d_stage_k_, src_v ? src_v : d_stage_v_, st_);
+  sync();
+}
+
+// Points the ring entries of the given tokens at `slot`. The ring holds the frames of the
+// device view (including a frame being ingested, whose slot already replaced the oldest window
+// frame), so lookups go through ring_frame_, not the reference-order window_.
+void Context::ring_owner_patch(int layer, const std::vector<Member>& ids, std::int32_t slot) {
+  for (const Member& m : ids)
+    for (int rs = 0; rs < t_.W; ++rs) {
+      const RingFrame& rf = ring_frame_[static_cast<std::size_t>(rs)];
+      if (rf.frame_id == m.frame && m.token < rf.T)
+        ring_owner_h_[(static_cast<std::size_t>(layer) * t_.W + rs) * t_.tmax + m.token] = slot;
+    }
+}
+
+void Context::ring_owner_upload(int layer) {
+  const std::size_t off = static_cast<std::size_t>(layer) * t_.W * t_.tmax;
+  KVC_CUDA(cudaMemcpyAsync(t_.ring_owner + off, &ring_owner_h_[off], static_cast<std::size_t>(t_.W) * t_.tmax * 4,
+                           cudaMemcpyHostToDevice, st_));
+  sync();
+}
+
+// Maintainer::split_members (maintainer.cpp:195-242) over the staged pool rows
+// [0, ids.size()). Emits children in reference order; installs their exact statistics and
+// repacks their payload rows into fresh pages. Returns the new ids.
+std::vector<std::int64_t> Context::split_pool(std::int64_t pid, int layer, bool host,
+                                              std::vector<Member>&& ids, std::int64_t rows, int) {
+  if (static_cast<std::int64_t>(ids.size()) != rows) fail(-11, "pool size mismatch");
+  stage_download(rows);
+  const float* keys = h_stage_f32_;
+  std::vector<std::int64_t> out;
+  std::vector<std::int32_t> slots;
+  std::vector<std::vector<double>> reps;
+  std::vector<double> vars;
+  std::vector<std::int64_t> stats, nmem, cids;
+  std::vector<std::uint8_t> res;
+  std::vector<AppendRun> runs;
+  std::vector<std::int32_t> idx;
+
+  auto emit = [&](const std::vector<int>& g, std::vector<double>&& rep, double var) {
+    std::vector<Member> m;
+    m.reserve(g.size());
+    for (int r : g) m.push_back(ids[static_cast<std::size_t>(r)]);
+    const std::int64_t id = new_cluster(layer, pid, std::move(m), host);
+    Cluster& c = C(id);
+    adopt(id);
+    out.push_back(id);
+    slots.push_back(c.slot);
+    reps.push_back(std::move(rep));
+    vars.push_back(var);
+    stats.push_back(static_cast<std::int64_t>(g.size()));
+    nmem.push_back(static_cast<std::int64_t>(g.size()));
+    cids.push_back(id);
+    res.push_back(host ? 1 : 0);
+    runs.push_back({c.slot, static_cast<std::int32_t>(idx.size()), static_cast<std::int32_t>(g.size()), 0});
+    idx.insert(idx.end(), g.begin(), g.end());
+  };
+
+  std::vector<double> tmp(static_cast<std::size_t>(d_));
+  std::vector<float> sub;
+  auto rec = [&](auto&& self, std::vector<int> grp, int depth) -> void {
+    if (grp.size() < 2) {
+      std::vector<double> rep(static_cast<std::size_t>(d_));
+      representative(keys, grp.data(), static_cast<int>(grp.size()), d_, rep.data());
+      const double var = variance(keys, grp.data(), static_cast<int>(grp.size()), d_, rep.data());
+      emit(grp, std::move(rep), var);
+      return;
+    }
+    sub.resize(grp.size() * static_cast<std::size_t>(d_));
+    for (std::size_t i = 0; i < grp.size(); ++i)
+      std::memcpy(&sub[i * d_], keys + static_cast<std::size_t>(grp[i]) * d_, d_ * 4);
+    const KMeansOut halves = split_two(sub.data(), static_cast<int>(grp.size()), d_,
+                                       mix_seed(maint_seed_, static_cast<std::uint64_t>(split_counter_++)));
+    mstats_[5] += 1;  // split_ops_total
+    std::vector<int> g2[2];
+    for (std::size_t i = 0; i < grp.size(); ++i) g2[halves.assign[i]].push_back(grp[i]);
+    for (auto& g : g2) {
+      if (g.empty()) continue;
+      std::vector<double> rep(static_cast<std::size_t>(d_));
+      representative(keys, g.data(), static_cast<int>(g.size()), d_, rep.data());
+      const double var = variance(keys, g.data(), static_cast<int>(g.size()), d_, rep.data());
+      if (depth + 1 < cfg_.max_split_depth && g.size() >= 2 &&
+          var > tau_of(static_cast<std::int64_t>(g.size()), cfg_)) {
+        self(self, std::move(g), depth + 1);
+      } else {
+        emit(g, std::move(rep), var);
+      }
+    }
+  };
+  std::vector<int> all(static_cast<std::size_t>(rows));
+  std::iota(all.begin(), all.end(), 0);
+  rec(rec, std::move(all), 0);
+
+  init_slots(slots, reps, vars, stats, nmem, cids, res, nullptr, nullptr);
+  append_runs_idx(runs, idx);
+  pl_upload(pid, layer);
+  for (std::size_t i = 0; i < out.size(); ++i) ring_owner_patch(layer, C(out[i]).members, slots[i]);
+  ring_owner_upload(layer);
+  return out;
+}
+
+std::int64_t Context::handle_host_event(std::int64_t frame_id, std::int64_t pid, int layer, int tok,
+                                        int kind, std::int32_t slot) {
+  mstats_[0] += 1;  // inserts (maintainer.cpp:89)
+  const std::size_t frow = static_cast<std::size_t>(layer) * t_.tmax + tok;
+  const std::size_t rb = static_cast<std::size_t>(d_) * es_;
+  if (kind == EV_SEED) {  // seed_cluster (maintainer.cpp:74-86)
+    ensure_stage(2);
+    KVC_CUDA(cudaMemcpyAsync(d_stage_k_, static_cast<std::uint8_t*>(d_fk_) + frow * rb, rb, cudaMemcpyDeviceToDevice, st_));
+    KVC_CUDA(cudaMemcpyAsync(d_stage_v_, static_cast<std::uint8_t*>(d_fv_) + frow * rb, rb, cudaMemcpyDeviceToDevice, st_));
+    stage_download(1);
+    std::vector<Member> m{{frame_id, tok}};
+    const std::int64_t id = new_cluster(layer, pid, std::move(m), false);
+    Cluster& c = C(id);
+    std::vector<double> rep(h_stage_f32_, h_stage_f32_ + d_);
+    init_slots({c.slot}, {rep}, {0.0}, {1}, {1}, {id}, {0}, nullptr, nullptr);
+    append_runs_idx({{c.slot, 0, 1, 0}}, {0});
+    adopt(id);
+    pl_upload(pid, layer);
+    ring_owner_patch(layer, c.members, c.slot);
+    ring_owner_upload(layer);
+    return id;
+  }
+  const std::int64_t cid = slot_id_[static_cast<std::size_t>(slot)];
+  Cluster& c = C(cid);
+  if (kind == EV_EAGER) {  // maintainer.cpp:151-158
+    mstats_[6] += 1;
+    fetch(cid, KVC_CAUSE_MAINTENANCE);
+    mstats_[7] += 1;
+  } else if (kind != EV_SPLIT) {
+    fail(-11, "unknown host event");
+  }
+  mstats_[2] += 1;  // immediate_splits
+  const std::int64_t rows = stage_cluster(c.slot, true);
+  KVC_CUDA(cudaMemcpyAsync(static_cast<std::uint8_t*>(d_stage_k_) + rows * rb,
+                           static_cast<std::uint8_t*>(d_fk_) + frow * rb, rb, cudaMemcpyDeviceToDevice, st_));
+  KVC_CUDA(cudaMemcpyAsync(static_cast<std::uint8_t*>(d_stage_v_) + rows * rb,
+                           static_cast<std::uint8_t*>(d_fv_) + frow * rb, rb, cudaMemcpyDeviceToDevice, st_));
+  std::vector<Member> ids = c.members;
+  ids.insert(ids.end(), c.buffer.begin(), c.buffer.end());
+  ids.push_back({frame_id, tok});
+  forget(cid);
+  drop_cluster(cid);
+  const std::vector<std::int64_t> kids = split_pool(pid, layer, false, std::move(ids), rows + 1, 0);
+  for (std::int64_t k : kids)  // home_of (maintainer.cpp:62-70)
+    for (const Member& m : C(k).members)
+      if (m.frame == frame_id && m.token == tok) return k;
+  return kids.front();
+}
+
+std::vector<std::int64_t> Context::materialize(std::int64_t id) {  // maintainer.cpp:178-193
+  Cluster& c = C(id);
+  if (!c.lazy) return {id};
+  if (c.host) fail(-11, "pending split settled without fetching the payload first");
+  mstats_[4] += 1;  // settled_splits
+  const std::int64_t rows = stage_cluster(c.slot, true);
+  std::vector<Member> ids = c.members;
+  ids.insert(ids.end(), c.buffer.begin(), c.buffer.end());
+  const std::int64_t pid = c.parent;
+  const int layer = c.layer;
+  const bool host = c.host;
+  forget(id);
+  drop_cluster(id);
+  return split_pool(pid, layer, host, std::move(ids), rows, 0);
+}
+
+// ============================================================================ build
+
+void Context::build_now() {  // engine.cpp:77-93 + build_index (index.cpp:364-450)
+  if (built_) return;
+  if (pending_.empty()) fail(-9, "no frames available to build from");
+  const std::uint64_t bseed = mix_seed(cfg_.seed, 1);
+  maint_seed_ = mix_seed(cfg_.seed, 2);
+  const int n = static_cast<int>(pending_.size());
+  std::vector<float> vis(static_cast<std::size_t>(n) * d_);
+  for (int i = 0; i < n; ++i) std::memcpy(&vis[static_cast<std::size_t>(i) * d_], pending_[static_cast<std::size_t>(i)].visual.data(), d_ * 4);
+  const int kv = (n + cfg_.target_visual_cluster_size - 1) / cfg_.target_visual_cluster_size;
+  const KMeansOut vk = spherical_kmeans(vis.data(), n, d_, kv, cfg_.kmeans_max_iters, cfg_.kmeans_tol, bseed);
+  std::vector<std::vector<int>> pf(static_cast<std::size_t>(vk.k_live));
+  for (int i = 0; i < n; ++i) pf[static_cast<std::size_t>(vk.assign[static_cast<std::size_t>(i)])].push_back(i);
+  for (std::size_t p = 0; p < pf.size(); ++p) {
+    Partition part;
+    std::vector<double> acc(static_cast<std::size_t>(d_), 0.0);  // dmean (vecmath.hpp:80-92)
+    for (int fi : pf[p]) {
+      part.frames.push_back(pending_[static_cast<std::size_t>(fi)].frame_id);
+      for (int c = 0; c < d_; ++c) acc[static_cast<std::size_t>(c)] += static_cast<double>(pending_[static_cast<std::size_t>(fi)].visual[static_cast<std::size_t>(c)]);
+    }
+    const double inv = 1.0 / static_cast<double>(pf[p].size());
+    for (double& x : acc) x *= inv;
+    part.vrep = std::move(acc);
+    part.stat = static_cast<std::int64_t>(pf[p].size());
+    part.per_layer.resize(static_cast<std::size_t>(L_));
+    part.dev_off.assign(static_cast<std::size_t>(L_), 0);
+    part.dev_cap.assign(static_cast<std::size_t>(L_), 0);
+    if (static_cast<std::int32_t>(parts_.size()) >= t_.max_parts) fail(-21, "too many partitions");
+    parts_.push_back(std::move(part));
+    upload_partition(static_cast<std::int64_t>(parts_.size()) - 1);
+  }
+  const std::size_t rb = static_cast<std::size_t>(d_) * es_;
+  for (std::size_t p = 0; p < pf.size(); ++p) {
+    for (int layer = 0; layer < L_; ++layer) {
+      // pool = frames of the partition in order, tokens in order (index.cpp:405-409)
+      std::vector<Member> ids;
+      std::int64_t rows = 0;
+      for (int fi : pf[p]) rows += pending_[static_cast<std::size_t>(fi)].T;
+      if (rows == 0) continue;
+      ensure_stage(rows + 1);
+      std::vector<float> keys(static_cast<std::size_t>(rows) * d_);
+      std::vector<std::uint8_t> kraw(static_cast<std::size_t>(rows) * rb), vraw(static_cast<std::size_t>(rows) * rb);
+      std::int64_t r = 0;
+      for (int fi : pf[p]) {
+        const PendingFrame& f = pending_[static_cast<std::size_t>(fi)];
+        const std::size_t base = static_cast<std::size_t>(layer) * f.T;
+        std::memcpy(&keys[static_cast<std::size_t>(r) * d_], &f.keys_f32[base * d_], static_cast<std::size_t>(f.T) * d_ * 4);
+        std::memcpy(&kraw[static_cast<std::size_t>(r) * rb], &f.keys_raw[base * rb], static_cast<std::size_t>(f.T) * rb);
+        std::memcpy(&vraw[static_cast<std::size_t>(r) * rb], &f.vals_raw[base * rb], static_cast<std::size_t>(f.T) * rb);
+        for (int t = 0; t < f.T; ++t) ids.push_back({f.frame_id, t});
+        r += f.T;
+      }
+      KVC_CUDA(cudaMemcpyAsync(d_stage_k_, kraw.data(), kraw.size(), cudaMemcpyHostToDevice, st_));
+      KVC_CUDA(cudaMemcpyAsync(d_stage_v_, vraw.data(), vraw.size(), cudaMemcpyHostToDevice, st_));
+      const int ks = static_cast<int>((rows + cfg_.target_semantic_cluster_size - 1) / cfg_.target_semantic_cluster_size);
+      const std::uint64_t sseed = mix_seed(bseed, (static_cast<std::uint64_t>(p) << 8) | static_cast<std::uint64_t>(layer) | 0x100u);
+      const KMeansOut sk = spherical_kmeans(keys.data(), static_cast<int>(rows), d_, ks, cfg_.kmeans_max_iters, cfg_.kmeans_tol, sseed);
+      std::vector<std::vector<int>> groups(static_cast<std::size_t>(sk.k_live));
+      for (std::int64_t i = 0; i < rows; ++i) groups[static_cast<std::size_t>(sk.assign[static_cast<std::size_t>(i)])].push_back(static_cast<int>(i));
+      std::vector<std::int32_t> slots;
+      std::vector<std::vector<double>> reps;
+      std::vector<double> vars;
+      std::vector<std::int64_t> stats, nmem, cids;
+      std::vector<std::uint8_t> res;
+      std::vector<AppendRun> runs;
+      std::vector<std::int32_t> idx;
+      for (auto& g : groups) {
+        std::vector<double> rep(static_cast<std::size_t>(d_));
+        representative(keys.data(), g.data(), static_cast<int>(g.size()), d_, rep.data());
+        const double var = variance(keys.data(), g.data(), static_cast<int>(g.size()), d_, rep.data());
+        std::vector<Member> m;
+        for (int i : g) m.push_back(ids[static_cast<std::size_t>(i)]);
+        const std::int64_t id = new_cluster(layer, static_cast<std::int64_t>(p), std::move(m), false);
+        const Cluster& c = C(id);
+        slots.push_back(c.slot);
+        reps.push_back(std::move(rep));
+        vars.push_back(var);
+        stats.push_back(static_cast<std::int64_t>(g.size()));
+        nmem.push_back(static_cast<std::int64_t>(g.size()));
+        cids.push_back(id);
+        res.push_back(0);
+        runs.push_back({c.slot, static_cast<std::int32_t>(idx.size()), static_cast<std::int32_t>(g.size()), 0});
+        idx.insert(idx.end(), g.begin(), g.end());
+      }
+      init_slots(slots, reps, vars, stats, nmem, cids, res, nullptr, nullptr);
+      append_runs_idx(runs, idx);
+      pl_upload(static_cast<std::int64_t>(p), layer);
+    }
+  }
+  // TieredStore(index, cost) adopts every cluster in id order (store.cpp:67-74)
+  for (std::int64_t id : cluster_ids()) adopt(id);
+  built_ = true;
+  const std::int64_t last = pending_.back().frame_id;
+  pending_.clear();
+  // ring owners of the window frames
+  for (int layer = 0; layer < L_; ++layer) {
+    for (const auto& up : clusters_)
+      if (up && up->layer == layer) ring_owner_patch(layer, up->members, up->slot);
+    ring_owner_upload(layer);
+  }
+  repin();
+  apply_cadence(last, -1);
+  if (cfg_.check_invariants) check();
+}
+
+}  // namespace kvc

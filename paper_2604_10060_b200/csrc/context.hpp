@@ -1,0 +1,256 @@
+// context.hpp -- one stream's cluster-level KV cache: host control plane + device data plane.
+//
+// The host side keeps what the reference keeps in HierIndex / TieredStore / Maintainer /
+// StreamEngine *except* the payloads and the statistics: ids, partitions, member identities
+// (frame, token) in stored order, residency, LRU ticks, the transfer ledger, split counters
+// (index.hpp:84-166, store.hpp:73-125, maintainer.hpp:48-80, engine.hpp:62-100). K/V payloads,
+// fp64 representatives / variances and page tables live on the GPU and are only read back on
+// the split slow path or through debug accessors.
+#pragma once
+
+#include <cstdint>
+#include <deque>
+#include <memory>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/kvc.h"
+#include "kvc_core.hpp"
+
+namespace kvc {
+
+struct Member {
+  std::int64_t frame;
+  std::int32_t token;
+};
+
+struct Cluster {  // ClusterRecord (index.hpp:29-50) minus payload and statistics
+  std::int64_t id = 0;
+  std::int32_t layer = 0;
+  std::int64_t parent = 0;
+  std::int32_t slot = -1;
+  std::vector<Member> members, buffer;
+  std::int64_t stat_count = 0;
+  bool lazy = false;
+  bool host = false;  // Residence::Host
+  std::int64_t device_tail = 0;
+  std::int64_t first_frame = 0, last_touch = 0;
+  // TieredStore::last_use_ entry (store.hpp:118)
+  bool tracked = false;
+  std::int64_t last_use = 0;
+  bool pinned = false;
+};
+
+struct Partition {  // VisualPartition (index.hpp:52-58)
+  std::vector<std::int64_t> frames;
+  std::vector<double> vrep;
+  std::int64_t stat = 0;
+  std::vector<std::vector<std::int64_t>> per_layer;  // [L] cluster ids, stored order
+  std::vector<std::int32_t> dev_off, dev_cap;        // [L] region of the device slot list
+};
+
+struct LedgerOp {  // TransferOp (store.hpp:35-42)
+  int cause;
+  bool to_device;
+  std::int64_t cluster_id, n_ops, bytes;
+  double cost_us;
+};
+
+struct LayerOut {  // LayerResult (retrieval.hpp:49-59)
+  std::vector<std::pair<std::int64_t, int>> ranked;
+  std::vector<std::int64_t> selected, predicted;
+  std::int64_t prefetch_hits = 0, verified = 0, rep_count = 0, attended_count = 0;
+  double lat[5] = {0, 0, 0, 0, 0};
+  std::vector<std::pair<std::int64_t, std::int32_t>> attended;  // parity mode
+};
+
+struct PendingFrame {
+  std::int64_t frame_id;
+  std::vector<float> visual;
+  std::vector<float> keys_f32;  // [L][T][d] (exact values of the kv dtype)
+  std::vector<std::uint8_t> keys_raw, vals_raw;  // kv dtype
+  int T;
+};
+
+class Context {
+ public:
+  Context(const kvc_cfg& cfg, int d, int L);
+  ~Context();
+
+  void ingest_frame(std::int64_t frame_id, const float* visual, const void* keys,
+                    const void* values, int T, int mem, std::int64_t* assigned,
+                    std::int64_t* partition);
+  void decode_step(std::int64_t qid, const float* q, int q_mem, float* out, int out_mem,
+                   const std::int64_t* gt, int n_gt);
+  void build_now();
+  std::int64_t bulk_load(const float* visual, const void* keys, const void* values, int N, int C,
+                         const std::int32_t* assign, const std::int64_t* frame_ids,
+                         const std::int32_t* token_ids, int mem);
+  std::vector<std::pair<std::int64_t, int>> flat_topk(const float* q, int layer, int k);
+
+  // views
+  const kvc_cfg& cfg() const { return cfg_; }
+  int d() const { return d_; }
+  int L() const { return L_; }
+  const Cluster* cluster(std::int64_t id) const;
+  std::vector<std::int64_t> cluster_ids() const;
+  void cluster_stats(std::int64_t id, double* var, double* rep, double* brep);
+  int cluster_payload(std::int64_t id, int which, float* k, float* v, int cap);
+  const std::vector<Partition>& partitions() const { return parts_; }
+  const std::vector<LayerOut>& last_layers() const { return last_; }
+  double last_ttft() const { return last_ttft_; }
+  double last_recall() const { return last_recall_; }
+  std::uint64_t last_digest() const { return last_digest_; }
+  const std::int64_t* maint_stats() const { return mstats_; }
+  const std::vector<LedgerOp>& ledger() const { return ledger_; }
+  std::int64_t device_entries() const { return device_entries_; }
+  void check();
+  double offload(std::int64_t id);
+  double fetch(std::int64_t id, int cause);
+  cudaStream_t stream() const { return st_; }
+  std::int64_t launches() const { return launches_; }
+  void set_timing(bool on) { timing_ = on; }
+  const double* step_timing() const { return step_t_; }
+
+ private:
+  // ---- configuration
+  kvc_cfg cfg_;
+  int d_, L_, es_;
+  // ---- device
+  DevTables t_{};
+  cudaStream_t st_ = nullptr;
+  std::vector<void*> dev_allocs_;
+  void* dalloc(std::size_t bytes);
+  void* halloc(std::size_t bytes);  // pinned
+  std::vector<void*> host_allocs_;
+  // frame input + staging
+  void* d_fk_ = nullptr;
+  void* d_fv_ = nullptr;
+  void* d_stage_k_ = nullptr;
+  void* d_stage_v_ = nullptr;
+  float* d_stage_f32_ = nullptr;
+  std::int64_t stage_rows_ = 0;
+  float* h_stage_f32_ = nullptr;
+  std::int32_t* d_idx_ = nullptr;
+  std::int32_t* h_idx_ = nullptr;
+  std::int64_t idx_cap_ = 0;
+  AppendRun* d_runs_ = nullptr;
+  AppendRun* h_runs_ = nullptr;
+  std::int64_t runs_cap_ = 0;
+  // slot-init staging
+  void* d_init_ = nullptr;
+  void* h_init_ = nullptr;
+  std::int64_t init_cap_ = 0;
+  // ingest buffers
+  IngestArgs ia_{};
+  std::int32_t *d_active_ = nullptr, *h_active_ = nullptr, *d_cursor_ = nullptr, *h_cursor_ = nullptr;
+  std::int32_t* h_evk_ = nullptr;
+  std::int32_t* h_evs_ = nullptr;
+  std::int32_t* h_stop_ = nullptr;  // [3][L]: stop_t, stop_kind, stop_slot
+  // decode buffers
+  DecodeArgs da_{};
+  void* d_dec_ = nullptr;  // packed result block
+  void* h_dec_ = nullptr;
+  std::size_t dec_bytes_ = 0;
+  float* d_q_ = nullptr;
+  float* d_out_ = nullptr;
+  cudaEvent_t ev_[8];
+  bool timing_ = false;
+  double step_t_[8] = {0};
+  std::int64_t launches_ = 0;
+
+  // ---- host control plane
+  std::vector<std::unique_ptr<Cluster>> clusters_;  // by id (dense, null when removed)
+  std::int64_t n_live_ = 0;
+  std::vector<std::int64_t> slot_id_;               // slot -> cluster id (-1 free)
+  std::vector<std::int32_t> free_slots_;
+  std::vector<Partition> parts_;
+  std::vector<std::int64_t> layer_live_count_;      // rep_timeline sizes
+  std::unordered_map<std::int64_t, std::vector<std::int64_t>> frame_clusters_;
+  std::vector<std::uint8_t> resid_h_;               // device residence mirror
+  bool resid_dirty_ = false;
+  std::int64_t pl_bump_ = 0;
+  // store
+  std::int64_t device_entries_ = 0, tick_ = 0;
+  std::vector<std::int64_t> pinned_ids_;
+  std::vector<LedgerOp> ledger_;
+  // maintainer
+  std::int64_t mstats_[9] = {0};
+  std::int64_t split_counter_ = 0;
+  std::uint64_t maint_seed_ = 0;
+  std::vector<double> tau_host_;
+  // engine
+  bool built_ = false;
+  std::vector<PendingFrame> pending_;
+  struct WinFrame {
+    std::int64_t frame_id;
+    int ring_slot;
+    int T;
+  };
+  std::deque<WinFrame> window_;
+  std::int64_t frames_seen_ = 0;
+  std::int64_t last_partition_ = -1;
+  std::vector<std::int32_t> ring_owner_h_;  // [L][W][tmax] mirror
+  struct RingFrame {
+    std::int64_t frame_id = -1;
+    int T = 0;
+  };
+  std::vector<RingFrame> ring_frame_;  // [W] frame held by each ring slot (device view)
+  // last query
+  std::vector<LayerOut> last_;
+  double last_ttft_ = 0.0, last_recall_ = -1.0;
+  std::uint64_t last_digest_ = 0;
+
+  // ---- helpers
+  void alloc_device();
+  void upload_tau();
+  Cluster& C(std::int64_t id);
+  std::int32_t take_slot();
+  std::int64_t new_cluster(std::int32_t layer, std::int64_t parent, std::vector<Member>&& members,
+                           bool host);
+  void drop_cluster(std::int64_t id);  // HierIndex::remove_cluster (host side)
+  void frame_add(std::int64_t frame, std::int64_t cid);
+  void frame_del(std::int64_t frame, std::int64_t cid);
+  void pl_upload(std::int64_t pid, int layer);
+  void upload_partition(std::int64_t pid);
+  void flush_resid();
+  // store (store.cpp:67-189)
+  std::int64_t side_entries(const Cluster& c) const;
+  void adopt(std::int64_t id);
+  void forget(std::int64_t id);
+  void touch(std::int64_t id);
+  double enforce_capacity();
+  double evict_one();
+  void record(int cause, bool to_dev, std::int64_t id, std::int64_t bytes);
+  std::int64_t entry_bytes() const;
+  // engine (engine.cpp)
+  void push_window(std::int64_t frame_id, int T);
+  void repin();
+  std::vector<std::int64_t> window_owner_ids() const;
+  void apply_cadence(std::int64_t frame_id, std::int64_t pid);
+  std::int64_t place_frame(std::int64_t frame_id, const float* visual);
+  void run_inserts(std::int64_t frame_id, std::int64_t pid, int T, std::int64_t* assigned);
+  // split slow path
+  std::vector<std::int64_t> split_pool(std::int64_t pid, int layer, bool host,
+                                       std::vector<Member>&& ids, std::int64_t rows, int depth_unused);
+  std::int64_t stage_cluster(std::int32_t slot, bool with_buffer);
+  void stage_download(std::int64_t rows);
+  void init_slots(const std::vector<std::int32_t>& slots, const std::vector<std::vector<double>>& reps,
+                  const std::vector<double>& vars, const std::vector<std::int64_t>& stats,
+                  const std::vector<std::int64_t>& nmem, const std::vector<std::int64_t>& cids,
+                  const std::vector<std::uint8_t>& resid, const std::vector<std::int32_t>* nbuf,
+                  const std::vector<std::vector<double>>* breps);
+  void append_runs_idx(const std::vector<AppendRun>& runs, const std::vector<std::int32_t>& idx,
+                       const void* src_k = nullptr, const void* src_v = nullptr);
+  void ring_owner_patch(int layer, const std::vector<Member>& ids, std::int32_t slot);
+  void ring_owner_upload(int layer);
+  std::int64_t handle_host_event(std::int64_t frame_id, std::int64_t pid, int layer, int tok,
+                                 int kind, std::int32_t slot);
+  std::vector<std::int64_t> materialize(std::int64_t id);
+  void ensure_stage(std::int64_t rows);
+  void ensure_idx(std::int64_t n, std::int64_t runs);
+  void sync();
+  void check_dev_err();
+};
+
+}  // namespace kvc

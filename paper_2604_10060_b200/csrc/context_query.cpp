@@ -1,0 +1,420 @@
+// context_query.cpp -- decode step (retrieve + attend), bulk load, views and self-checks.
+//
+// Reference semantics (paths under /root/reference/proj/core):
+//   retrieval.cpp:45-143  retrieve(): per-layer rankings (computed on the GPU for all layers at
+//                         once -- rankings depend only on representatives, which nothing in the
+//                         per-layer loop changes for a later layer), then fetch / materialize /
+//                         touch / latency bookkeeping replayed here in layer order.
+//   retrieval.cpp:145-164 oracle_flat_topk
+//   engine.cpp:176-237    answer_query: repin + checks after the query
+//   index.cpp:263-343     check_invariants;  store.cpp:183-189 audit
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+#include <string>
+
+#include "context.hpp"
+#include "kmeans.hpp"
+
+namespace kvc {
+
+namespace {
+
+std::uint64_t fnv1a(std::uint64_t h, std::uint64_t x) {  // engine.cpp:18-24
+  for (int i = 0; i < 8; ++i) {
+    h ^= (x >> (8 * i)) & 0xffu;
+    h *= 1099511628211ull;
+  }
+  return h;
+}
+
+}  // namespace
+
+void Context::decode_step(std::int64_t qid, const float* q, int q_mem, float* out, int out_mem,
+                          const std::int64_t* gt, int n_gt) {
+  (void)qid;
+  if (!built_) build_now();  // engine.cpp:202
+  if (parts_.empty()) fail(-9, "retrieve before any index was built");
+  if (!q) fail(-10, "null query");
+  flush_resid();
+  const float* dq = q;
+  if (q_mem != KVC_MEM_DEVICE) {
+    KVC_CUDA(cudaMemcpyAsync(d_q_, q, static_cast<std::size_t>(L_) * d_ * 4, cudaMemcpyHostToDevice, st_));
+    dq = d_q_;
+  }
+  da_.q = dq;
+  da_.out = (out && out_mem == KVC_MEM_DEVICE) ? out : d_out_;
+  da_.n_parts_host = static_cast<std::int32_t>(parts_.size());
+  launches_ += launch_decode(t_, da_, st_, timing_ ? ev_ : nullptr);
+  KVC_CUDA(cudaMemcpyAsync(h_dec_, d_dec_, dec_bytes_, cudaMemcpyDeviceToHost, st_));
+  if (out && out_mem != KVC_MEM_DEVICE)
+    KVC_CUDA(cudaMemcpyAsync(out, d_out_, static_cast<std::size_t>(L_) * d_ * 4, cudaMemcpyDeviceToHost, st_));
+  sync();
+  check_dev_err();
+  if (timing_) {
+    float ms = 0.f;
+    for (int i = 0; i < 3; ++i) {
+      KVC_CUDA(cudaEventElapsedTime(&ms, ev_[i], ev_[i + 1]));
+      step_t_[i] = ms * 1e3;
+    }
+    KVC_CUDA(cudaEventElapsedTime(&ms, ev_[0], ev_[3]));
+    step_t_[3] = ms * 1e3;
+  }
+
+  // host copies of the device rankings (same carve offsets as alloc_device)
+  auto hp = [&](const void* dptr) {
+    return static_cast<const std::uint8_t*>(h_dec_) +
+           (static_cast<const std::uint8_t*>(dptr) - static_cast<const std::uint8_t*>(d_dec_));
+  };
+  const auto* h_parts = reinterpret_cast<const std::int32_t*>(hp(da_.parts));
+  const auto* h_nps = reinterpret_cast<const std::int32_t*>(hp(da_.n_parts_sel));
+  const auto* h_rs = reinterpret_cast<const std::int32_t*>(hp(da_.ranked_slot));
+  const auto* h_rb = hp(da_.ranked_buf);
+  const auto* h_nr = reinterpret_cast<const std::int32_t*>(hp(da_.n_ranked));
+  const auto* h_ps = reinterpret_cast<const std::int32_t*>(hp(da_.pf_slot));
+  const auto* h_pb = hp(da_.pf_buf);
+  const auto* h_np = reinterpret_cast<const std::int32_t*>(hp(da_.n_pf));
+  const auto* h_att = reinterpret_cast<const std::int64_t*>(hp(da_.attended));
+  const auto* h_nc = reinterpret_cast<const std::int32_t*>(hp(da_.n_cand));
+  (void)h_parts;
+  (void)h_nps;
+
+  // Translate every layer's slots to ids before any settle frees / reuses a slot.
+  std::vector<std::vector<std::pair<std::int64_t, int>>> ranked(static_cast<std::size_t>(L_)), pf(static_cast<std::size_t>(L_));
+  for (int l = 0; l < L_; ++l) {
+    for (int i = 0; i < h_nr[l]; ++i)
+      ranked[static_cast<std::size_t>(l)].push_back({slot_id_[static_cast<std::size_t>(h_rs[l * da_.k_s + i])], h_rb[l * da_.k_s + i]});
+    for (int i = 0; i < h_np[l]; ++i)
+      pf[static_cast<std::size_t>(l)].push_back({slot_id_[static_cast<std::size_t>(h_ps[l * da_.prefetch_k + i])], h_pb[l * da_.prefetch_k + i]});
+  }
+
+  // retrieval.cpp:58-128, layer by layer
+  const bool parity = cfg_.parity_mode != 0 || (gt && n_gt > 0);
+  std::vector<std::int64_t> predicted_next;
+  double stall_next = 0.0;
+  std::vector<std::int64_t> context_frames;
+  last_ttft_ = 0.0;
+  for (int l = 0; l < L_; ++l) {
+    LayerOut& lo = last_[static_cast<std::size_t>(l)];
+    lo = LayerOut{};
+    const std::int64_t compared = static_cast<std::int64_t>(parts_.size()) + h_nc[l];
+    lo.lat[0] = cfg_.lookup_cost_per_candidate_us * static_cast<double>(compared);
+    lo.ranked = ranked[static_cast<std::size_t>(l)];
+    std::vector<std::int64_t> verified;
+    for (const auto& r : lo.ranked)
+      if (std::find(verified.begin(), verified.end(), r.first) == verified.end()) verified.push_back(r.first);
+    lo.verified = static_cast<std::int64_t>(verified.size());
+    if (cfg_.prefetch_enabled && l > 0) {
+      lo.predicted = predicted_next;
+      lo.lat[2] = stall_next;
+      for (std::int64_t cid : verified) {
+        if (std::find(lo.predicted.begin(), lo.predicted.end(), cid) != lo.predicted.end()) lo.prefetch_hits += 1;
+        lo.lat[3] += fetch(cid, KVC_CAUSE_COMPLETION);
+      }
+    } else {
+      for (std::int64_t cid : verified) lo.lat[1] += fetch(cid, KVC_CAUSE_RETRIEVAL);
+    }
+    predicted_next.clear();
+    stall_next = 0.0;
+    for (std::int64_t cid : verified) {
+      std::vector<std::int64_t> s = materialize(cid);
+      lo.selected.insert(lo.selected.end(), s.begin(), s.end());
+    }
+    std::sort(lo.selected.begin(), lo.selected.end());
+    for (std::int64_t cid : lo.selected) touch(cid);
+    lo.attended_count = h_att[l];
+    if (parity) {
+      auto& att = lo.attended;
+      for (std::int64_t cid : lo.selected)
+        for (const Member& m : C(cid).members) att.push_back({m.frame, m.token});
+      for (const WinFrame& w : window_)
+        for (int t = 0; t < w.T; ++t) att.push_back({w.frame_id, t});
+      std::sort(att.begin(), att.end());
+      att.erase(std::unique(att.begin(), att.end()), att.end());
+      if (static_cast<std::int64_t>(att.size()) != lo.attended_count) {
+        std::int64_t members = 0;
+        for (std::int64_t cid : lo.selected) members += static_cast<std::int64_t>(C(cid).members.size());
+        fail(-11, "device attended count disagrees with the attended set: layer " + std::to_string(l) +
+                      " device " + std::to_string(lo.attended_count) + " host " + std::to_string(att.size()) +
+                      " selected members " + std::to_string(members) + " window frames " +
+                      std::to_string(window_.size()));
+      }
+      for (const auto& a : att) context_frames.push_back(a.first);
+    }
+    lo.rep_count = layer_live_count_[static_cast<std::size_t>(l)];
+    lo.lat[4] = cfg_.compute_cost_per_token_us * static_cast<double>(lo.attended_count + lo.rep_count);
+    if (cfg_.prefetch_enabled && l + 1 < L_) {
+      for (const auto& r : pf[static_cast<std::size_t>(l)])
+        if (std::find(predicted_next.begin(), predicted_next.end(), r.first) == predicted_next.end())
+          predicted_next.push_back(r.first);
+      double pf_cost = 0.0;
+      for (std::int64_t cid : predicted_next) pf_cost += fetch(cid, KVC_CAUSE_PREFETCH);
+      stall_next = std::max(0.0, pf_cost - lo.lat[4]);
+    }
+  }
+  for (const LayerOut& lo : last_) last_ttft_ += lo.lat[0] + lo.lat[1] + lo.lat[2] + lo.lat[3] + lo.lat[4];
+  last_recall_ = -1.0;
+  if (parity) {
+    std::sort(context_frames.begin(), context_frames.end());
+    context_frames.erase(std::unique(context_frames.begin(), context_frames.end()), context_frames.end());
+    if (gt && n_gt > 0) {
+      std::int64_t hit = 0;
+      for (int i = 0; i < n_gt; ++i)
+        if (std::binary_search(context_frames.begin(), context_frames.end(), gt[i])) hit += 1;
+      last_recall_ = static_cast<double>(hit) / static_cast<double>(n_gt);
+    }
+    std::uint64_t h = 1469598103934665603ull;
+    for (int l = 0; l < L_; ++l)
+      for (const auto& a : last_[static_cast<std::size_t>(l)].attended) {
+        h = fnv1a(h, static_cast<std::uint64_t>(l));
+        h = fnv1a(h, static_cast<std::uint64_t>(a.first));
+        h = fnv1a(h, static_cast<std::uint64_t>(a.second));
+      }
+    last_digest_ = h;
+  }
+  repin();  // engine.cpp:234
+  if (cfg_.check_invariants) check();
+}
+
+// ---------------------------------------------------------------------------- bulk load
+
+std::int64_t Context::bulk_load(const float* visual, const void* keys, const void* values, int N,
+                                int C_, const std::int32_t* assign, const std::int64_t* frame_ids,
+                                const std::int32_t* token_ids, int mem) {
+  if (!pending_.empty()) fail(-10, "bulk load after frames are pending the batch build");
+  if (N < 1 || C_ < 1) fail(-4, "bulk load needs members and clusters");
+  if (!built_) {
+    built_ = true;
+    maint_seed_ = mix_seed(cfg_.seed, 2);
+  }
+  if (static_cast<std::int32_t>(parts_.size()) >= t_.max_parts) fail(-21, "too many partitions");
+  Partition p;
+  std::vector<std::int64_t> fr(frame_ids, frame_ids + N);
+  std::sort(fr.begin(), fr.end());
+  fr.erase(std::unique(fr.begin(), fr.end()), fr.end());
+  p.frames = fr;
+  p.vrep.assign(visual, visual + d_);
+  p.stat = static_cast<std::int64_t>(fr.size());
+  p.per_layer.resize(static_cast<std::size_t>(L_));
+  p.dev_off.assign(static_cast<std::size_t>(L_), 0);
+  p.dev_cap.assign(static_cast<std::size_t>(L_), 0);
+  parts_.push_back(std::move(p));
+  const std::int64_t pid = static_cast<std::int64_t>(parts_.size()) - 1;
+  upload_partition(pid);
+  std::vector<std::int32_t> z(static_cast<std::size_t>(L_), 0);
+  KVC_CUDA(cudaMemcpyAsync(t_.pl_cnt + pid * L_, z.data(), L_ * 4, cudaMemcpyHostToDevice, st_));
+  sync();
+
+  const std::size_t rb = static_cast<std::size_t>(d_) * es_;
+  ensure_stage(N + 1);
+  std::vector<std::int64_t> new_ids;
+  for (int l = 0; l < L_; ++l) {
+    const auto* kb = static_cast<const std::uint8_t*>(keys) + static_cast<std::size_t>(l) * N * rb;
+    const auto* vb = static_cast<const std::uint8_t*>(values) + static_cast<std::size_t>(l) * N * rb;
+    const cudaMemcpyKind kind = mem == KVC_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    KVC_CUDA(cudaMemcpyAsync(d_stage_k_, kb, static_cast<std::size_t>(N) * rb, kind, st_));
+    KVC_CUDA(cudaMemcpyAsync(d_stage_v_, vb, static_cast<std::size_t>(N) * rb, kind, st_));
+    // stable grouping by cluster index (members keep row order)
+    const std::int32_t* a = assign + static_cast<std::size_t>(l) * N;
+    std::vector<std::int32_t> cnt(static_cast<std::size_t>(C_) + 1, 0);
+    for (int i = 0; i < N; ++i) {
+      if (a[i] < 0 || a[i] >= C_) fail(-10, "cluster index out of range");
+      cnt[static_cast<std::size_t>(a[i]) + 1] += 1;
+    }
+    for (int c = 0; c < C_; ++c) cnt[static_cast<std::size_t>(c) + 1] += cnt[static_cast<std::size_t>(c)];
+    std::vector<std::int32_t> idx(static_cast<std::size_t>(N));
+    {
+      std::vector<std::int32_t> pos(cnt.begin(), cnt.end() - 1);
+      for (int i = 0; i < N; ++i) idx[static_cast<std::size_t>(pos[static_cast<std::size_t>(a[i])]++)] = i;
+    }
+    std::vector<AppendRun> runs;
+    std::vector<std::int32_t> slots;
+    std::vector<std::int64_t> cids;
+    for (int c = 0; c < C_; ++c) {
+      const std::int32_t b = cnt[static_cast<std::size_t>(c)], e = cnt[static_cast<std::size_t>(c) + 1];
+      if (b == e) continue;
+      std::vector<Member> m;
+      m.reserve(static_cast<std::size_t>(e - b));
+      for (std::int32_t j = b; j < e; ++j) {
+        const std::int32_t i = idx[static_cast<std::size_t>(j)];
+        m.push_back({frame_ids[i], token_ids[i]});
+      }
+      const std::int64_t id = new_cluster(l, pid, std::move(m), false);
+      const Cluster& cl = C(id);
+      runs.push_back({cl.slot, b, e - b, 0});
+      slots.push_back(cl.slot);
+      cids.push_back(id);
+      new_ids.push_back(id);
+    }
+    // headers (counts / ids / residence); statistics are computed exactly on the device
+    for (std::size_t i = 0; i < slots.size(); ++i) {
+      const Cluster& cl = C(cids[i]);
+      const std::int64_t n = static_cast<std::int64_t>(cl.members.size());
+      const std::int64_t s = slots[i];
+      std::int32_t zero = 0;
+      std::uint8_t z8 = 0;
+      KVC_CUDA(cudaMemcpyAsync(t_.stat + s, &n, 8, cudaMemcpyHostToDevice, st_));
+      KVC_CUDA(cudaMemcpyAsync(t_.nmem + s, &n, 8, cudaMemcpyHostToDevice, st_));
+      KVC_CUDA(cudaMemcpyAsync(t_.cid + s, &cids[i], 8, cudaMemcpyHostToDevice, st_));
+      KVC_CUDA(cudaMemcpyAsync(t_.nbuf + s, &zero, 4, cudaMemcpyHostToDevice, st_));
+      KVC_CUDA(cudaMemcpyAsync(t_.lazy + s, &z8, 1, cudaMemcpyHostToDevice, st_));
+      KVC_CUDA(cudaMemcpyAsync(t_.resid + s, &z8, 1, cudaMemcpyHostToDevice, st_));
+      sync();
+    }
+    ensure_idx(N, static_cast<std::int64_t>(runs.size()));
+    std::memcpy(h_idx_, idx.data(), idx.size() * 4);
+    std::memcpy(h_runs_, runs.data(), runs.size() * sizeof(AppendRun));
+    KVC_CUDA(cudaMemcpyAsync(d_idx_, h_idx_, idx.size() * 4, cudaMemcpyHostToDevice, st_));
+    KVC_CUDA(cudaMemcpyAsync(d_runs_, h_runs_, runs.size() * sizeof(AppendRun), cudaMemcpyHostToDevice, st_));
+    launches_ += launch_exact_stats(t_, d_runs_, static_cast<std::int32_t>(runs.size()), d_idx_, d_stage_k_, st_);
+    launches_ += launch_append_runs(t_, d_runs_, static_cast<std::int32_t>(runs.size()), d_idx_, d_stage_k_, d_stage_v_, st_);
+    sync();
+    check_dev_err();
+    pl_upload(pid, l);
+  }
+  for (std::int64_t id : new_ids) adopt(id);
+  return pid;
+}
+
+// ---------------------------------------------------------------------------- flat top-k
+
+std::vector<std::pair<std::int64_t, int>> Context::flat_topk(const float* q, int layer, int k) {
+  if (k <= 0) fail(-10, "oracle top-k must be positive");
+  if (layer < 0 || layer >= L_) fail(-7, "layer out of range: " + std::to_string(layer));
+  std::vector<std::int32_t> slots;
+  std::vector<std::uint8_t> bufs;
+  for (const auto& up : clusters_) {
+    if (!up || up->layer != layer) continue;
+    slots.push_back(up->slot);
+    bufs.push_back(0);
+    if (up->lazy) {
+      slots.push_back(up->slot);
+      bufs.push_back(1);
+    }
+  }
+  const int n = static_cast<int>(slots.size());
+  std::vector<std::pair<std::int64_t, int>> out;
+  if (n == 0) return out;
+  ensure_idx(static_cast<std::int64_t>(n) * 2 + k + d_, 1);
+  std::memcpy(h_idx_, slots.data(), n * 4);
+  auto* hb = reinterpret_cast<std::uint8_t*>(h_idx_ + n);
+  std::memcpy(hb, bufs.data(), n);
+  KVC_CUDA(cudaMemcpyAsync(d_idx_, h_idx_, static_cast<std::size_t>(n) * 8, cudaMemcpyHostToDevice, st_));
+  KVC_CUDA(cudaMemcpyAsync(d_q_, q, d_ * 4, cudaMemcpyHostToDevice, st_));
+  std::int32_t* d_out = d_idx_ + 2 * n;
+  launches_ += launch_flat_topk(t_, d_q_, d_idx_, reinterpret_cast<std::uint8_t*>(d_idx_ + n), n, k, d_out, st_);
+  const int take = std::min(n, k);
+  std::vector<std::int32_t> order(static_cast<std::size_t>(take));
+  KVC_CUDA(cudaMemcpyAsync(order.data(), d_out, take * 4, cudaMemcpyDeviceToHost, st_));
+  sync();
+  check_dev_err();
+  for (int i = 0; i < take; ++i) {
+    const int j = order[static_cast<std::size_t>(i)];
+    out.push_back({slot_id_[static_cast<std::size_t>(slots[static_cast<std::size_t>(j)])], bufs[static_cast<std::size_t>(j)]});
+  }
+  return out;
+}
+
+// ---------------------------------------------------------------------------- views
+
+void Context::cluster_stats(std::int64_t id, double* var, double* rep, double* brep) {
+  const Cluster& c = C(id);
+  const std::int64_t s = c.slot;
+  KVC_CUDA(cudaMemcpyAsync(var, t_.var + s, 8, cudaMemcpyDeviceToHost, st_));
+  if (rep) KVC_CUDA(cudaMemcpyAsync(rep, t_.rep64 + s * d_, d_ * 8, cudaMemcpyDeviceToHost, st_));
+  if (brep && !c.buffer.empty())
+    KVC_CUDA(cudaMemcpyAsync(brep, t_.brep64 + s * d_, d_ * 8, cudaMemcpyDeviceToHost, st_));
+  sync();
+}
+
+int Context::cluster_payload(std::int64_t id, int which, float* k, float* v, int cap) {
+  const Cluster& c = C(id);
+  const std::int64_t nm = static_cast<std::int64_t>(c.members.size());
+  const std::int64_t nb = static_cast<std::int64_t>(c.buffer.size());
+  const std::int64_t rows = stage_cluster(c.slot, true);
+  const std::int64_t first = which == 0 ? 0 : nm;
+  const std::int64_t n = which == 0 ? nm : nb;
+  (void)rows;
+  const std::size_t rb = static_cast<std::size_t>(d_) * es_;
+  const int take = static_cast<int>(std::min<std::int64_t>(n, cap));
+  if (take > 0) {
+    launches_ += launch_to_f32(t_, static_cast<std::uint8_t*>(d_stage_k_) + first * rb, d_stage_f32_, static_cast<std::int64_t>(take) * d_, st_);
+    KVC_CUDA(cudaMemcpyAsync(k, d_stage_f32_, static_cast<std::size_t>(take) * d_ * 4, cudaMemcpyDeviceToHost, st_));
+    sync();
+    launches_ += launch_to_f32(t_, static_cast<std::uint8_t*>(d_stage_v_) + first * rb, d_stage_f32_, static_cast<std::int64_t>(take) * d_, st_);
+    KVC_CUDA(cudaMemcpyAsync(v, d_stage_f32_, static_cast<std::size_t>(take) * d_ * 4, cudaMemcpyDeviceToHost, st_));
+    sync();
+  }
+  return static_cast<int>(n);
+}
+
+// ---------------------------------------------------------------------------- self-check
+
+void Context::check() {
+  auto bad = [](const std::string& w) { fail(-11, w); };
+  // index.cpp:266-282: partitions
+  for (std::size_t p = 0; p < parts_.size(); ++p) {
+    const Partition& part = parts_[p];
+    if (!std::is_sorted(part.frames.begin(), part.frames.end())) bad("partition frame list not in temporal order");
+    for (int l = 0; l < L_; ++l)
+      for (std::int64_t cid : part.per_layer[static_cast<std::size_t>(l)]) {
+        const Cluster* c = cluster(cid);
+        if (!c) bad("partition lists a cluster that does not exist");
+        if (c->parent != static_cast<std::int64_t>(p)) bad("cluster parent does not match the partition listing it");
+        if (c->layer != l) bad("cluster filed under the wrong layer");
+      }
+  }
+  // index.cpp:284-307 + device agreement
+  std::vector<std::int64_t> live(static_cast<std::size_t>(L_), 0);
+  std::unordered_map<std::int64_t, std::vector<std::int64_t>> frames;
+  std::vector<std::int64_t> dstat(static_cast<std::size_t>(t_.max_slots)), dnmem(static_cast<std::size_t>(t_.max_slots));
+  std::vector<std::int32_t> dnbuf(static_cast<std::size_t>(t_.max_slots));
+  std::vector<std::uint8_t> dlazy(static_cast<std::size_t>(t_.max_slots));
+  KVC_CUDA(cudaMemcpyAsync(dstat.data(), t_.stat, dstat.size() * 8, cudaMemcpyDeviceToHost, st_));
+  KVC_CUDA(cudaMemcpyAsync(dnmem.data(), t_.nmem, dnmem.size() * 8, cudaMemcpyDeviceToHost, st_));
+  KVC_CUDA(cudaMemcpyAsync(dnbuf.data(), t_.nbuf, dnbuf.size() * 4, cudaMemcpyDeviceToHost, st_));
+  KVC_CUDA(cudaMemcpyAsync(dlazy.data(), t_.lazy, dlazy.size(), cudaMemcpyDeviceToHost, st_));
+  sync();
+  std::int64_t recount = 0;
+  for (const auto& up : clusters_) {
+    if (!up) continue;
+    const Cluster& c = *up;
+    const std::size_t s = static_cast<std::size_t>(c.slot);
+    if (slot_id_[s] != c.id) bad("slot map out of step");
+    if (c.members.empty()) bad("cluster with no members");
+    if (c.stat_count != static_cast<std::int64_t>(c.members.size() + c.buffer.size()))
+      bad("statistics count out of step with held entries");
+    if (c.lazy != !c.buffer.empty()) bad("deferred-split flag out of step with buffer");
+    if (!c.host && c.device_tail != 0) bad("device-resident cluster with a device tail");
+    if (c.device_tail < 0 || c.device_tail > static_cast<std::int64_t>(c.members.size()))
+      bad("device tail outside the member count");
+    if (dstat[s] != c.stat_count || dnmem[s] != static_cast<std::int64_t>(c.members.size()) ||
+        dnbuf[s] != static_cast<std::int32_t>(c.buffer.size()) || (dlazy[s] != 0) != c.lazy)
+      bad("device cluster table out of step with the host control plane");
+    std::int64_t first = c.members.front().frame;
+    for (const Member& m : c.members) {
+      first = std::min(first, m.frame);
+      frames[m.frame].push_back(c.id);
+    }
+    for (const Member& m : c.buffer) frames[m.frame].push_back(c.id);
+    if (first != c.first_frame) bad("first-frame marker out of step with members");
+    live[static_cast<std::size_t>(c.layer)] += 1;
+    recount += side_entries(c);
+  }
+  for (auto& kv : frames) {
+    std::sort(kv.second.begin(), kv.second.end());
+    kv.second.erase(std::unique(kv.second.begin(), kv.second.end()), kv.second.end());
+    auto it = frame_clusters_.find(kv.first);
+    if (it == frame_clusters_.end() || it->second != kv.second) bad("frame lookup map out of step with cluster contents");
+  }
+  if (frames.size() != frame_clusters_.size()) bad("frame lookup map out of step with cluster contents");
+  for (int l = 0; l < L_; ++l)
+    if (live[static_cast<std::size_t>(l)] != layer_live_count_[static_cast<std::size_t>(l)])
+      bad("timeline length out of step with live clusters");
+  // store.cpp:183-189 + ledger replay (store.cpp:44-60 is trivially consistent here: totals are
+  // always derived from the op log)
+  if (recount != device_entries_) bad("device occupancy out of step with residency");
+}
+
+}  // namespace kvc

@@ -1,0 +1,1334 @@
+// kernels.cu -- sm_100a kernels of the cluster-level KV-cache hot path.
+//
+//   K0 build_cands     candidate list of the frame's partition per domain (maintainer.cpp:91-109)
+//   K1 approx          approximate cosine tile S~[t][c] for every token x candidate (fp32)
+//   K2 resolve         exact sequential on_insert per domain: fp64 re-score of the candidates the
+//                      approximate tile cannot rule out, Eq. 3/4 update, Eq. 5 test, branch
+//                      (maintainer.cpp:88-176); appends K/V into cluster-contiguous pages
+//   K4 score_select    visual_topk + semantic_topk (+ prefetch ranking) per domain with exact fp64
+//                      cosines and the reference tie-breaks (index.cpp:192-240); attended count and
+//                      the attention work list
+//   K6 attend          split-KV attention over the selected clusters' pages and the window ring,
+//                      TMA bulk copies (cp.async.bulk) into a shared-memory page pipeline, online
+//                      softmax, in-kernel combine by the last CTA of each domain
+// plus store maintenance (append / gather / free / exact stats / mirrors).
+//
+// Exactness: every fp64 operation that must reproduce the reference bit-for-bit is written with
+// explicit round-to-nearest intrinsics (__dmul_rn/__dadd_rn/__ddiv_rn/__dsqrt_rn) so no FMA
+// contraction can occur (the reference builds with -ffp-contract=off, CMakeLists.txt:11-13),
+// and every sum runs in the reference's sequential order.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cfloat>
+#include <cstdint>
+
+#include "kvc_core.hpp"
+
+namespace kvc {
+
+namespace {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double ddiv(double a, double b) { return __ddiv_rn(a, b); }
+__device__ __forceinline__ double clamp1(double x) { return x < -1.0 ? -1.0 : (x > 1.0 ? 1.0 : x); }
+
+__device__ __forceinline__ float ld_kv(const void* base, int64_t i, int bf16) {
+  if (bf16) return __bfloat162float(static_cast<const __nv_bfloat16*>(base)[i]);
+  return static_cast<const float*>(base)[i];
+}
+
+__device__ __forceinline__ void set_err(const DevTables& t, int bit) { atomicOr(t.err, bit); }
+
+// (sim desc, key asc) "a better than b"
+__device__ __forceinline__ bool better(double sa, long long ka, double sb, long long kb) {
+  return sa > sb || (sa == sb && ka < kb);
+}
+
+// Warp arg-best over (sim, key, payload).
+__device__ __forceinline__ void warp_best(double& s, long long& k, int& p) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    double so = __shfl_xor_sync(kFull, s, o);
+    long long ko = __shfl_xor_sync(kFull, k, o);
+    int po = __shfl_xor_sync(kFull, p, o);
+    if (better(so, ko, s, k)) {
+      s = so;
+      k = ko;
+      p = po;
+    }
+  }
+}
+
+// One warp appends one K/V row (kv dtype) to a slot's member or buffer page list.
+__device__ bool warp_append(const DevTables& t, int slot, bool to_buf, const uint8_t* src_k,
+                            const uint8_t* src_v) {
+  const int lane = threadIdx.x & 31;
+  int page = -1, row = -1;
+  if (lane == 0) {
+    int* np = to_buf ? &t.nbpages[slot] : &t.npages[slot];
+    int* list = to_buf ? t.bpages + static_cast<int64_t>(slot) * t.maxbp
+                       : t.pages + static_cast<int64_t>(slot) * t.maxp;
+    const int cap = to_buf ? t.maxbp : t.maxp;
+    const int n = *np;
+    page = n > 0 ? list[n - 1] : -1;
+    if (page < 0 || t.pg_fill[page] >= t.P) {
+      if (n >= cap) {
+        set_err(t, DERR_CLUSTER_PAGES);
+        page = -1;
+      } else {
+        const int top = atomicSub(t.free_top, 1) - 1;
+        if (top < 0) {
+          atomicAdd(t.free_top, 1);
+          set_err(t, DERR_PAGES);
+          page = -1;
+        } else {
+          page = t.free_stack[top];
+          list[n] = page;
+          *np = n + 1;
+          t.pg_fill[page] = 0;
+        }
+      }
+    }
+    if (page >= 0) row = t.pg_fill[page]++;
+  }
+  page = __shfl_sync(kFull, page, 0);
+  row = __shfl_sync(kFull, row, 0);
+  if (page < 0) return false;
+  const int rb = t.d * t.es;
+  uint8_t* dk = page_k(t, page) + static_cast<int64_t>(row) * rb;
+  uint8_t* dv = page_v(t, page) + static_cast<int64_t>(row) * rb;
+  for (int o = lane * 16; o < rb; o += 32 * 16) {
+    *reinterpret_cast<uint4*>(dk + o) = *reinterpret_cast<const uint4*>(src_k + o);
+    *reinterpret_cast<uint4*>(dv + o) = *reinterpret_cast<const uint4*>(src_v + o);
+  }
+  return true;
+}
+
+// ============================================================================ K0
+__global__ void k_build_cands(DevTables t, IngestArgs a) {
+  const int dom = a.active[blockIdx.x];
+  __shared__ int cnt_s;
+  if (threadIdx.x == 0) cnt_s = 0;
+  __syncthreads();
+  const int64_t key = static_cast<int64_t>(a.pid) * t.L + dom;
+  const int off = t.pl_off[key], cnt = t.pl_cnt[key];
+  int32_t* cs = a.cand_slot + static_cast<int64_t>(dom) * t.cmax;
+  uint8_t* cb = a.cand_buf + static_cast<int64_t>(dom) * t.cmax;
+  for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+    const int s = t.pl_pool[off + i];
+    const int k = atomicAdd(&cnt_s, t.lazy[s] ? 2 : 1);
+    if (k + (t.lazy[s] ? 2 : 1) > t.cmax) {
+      set_err(t, DERR_CANDIDATES);
+      continue;
+    }
+    cs[k] = s;
+    cb[k] = 0;
+    if (t.lazy[s]) {
+      cs[k + 1] = s;
+      cb[k + 1] = 1;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) a.cand_n[dom] = min(cnt_s, t.cmax);
+}
+
+// ============================================================================ K1
+// S~[t][c] = <k_t, r32_c> / (|k_t| |r_c|) in fp32 (CUDA cores). |S~ - S| is bounded by a few
+// 1e-6 for unit-scale data; the resolve kernel uses margin = 1e-4.
+constexpr int AT = 32;  // tokens per CTA
+constexpr int AC = 64;  // candidates per tile
+__global__ void __launch_bounds__(256) k_approx(DevTables t, IngestArgs a) {
+  extern __shared__ float sm[];
+  const int d = t.d, dp = d + 1;
+  float* kt = sm;                  // [AT][d+1]
+  float* rt = kt + AT * dp;        // [AC][d+1]
+  float* ink = rt + AC * dp;       // [AT]
+  float* inr = ink + AT;           // [AC]
+  const int dom = a.active[blockIdx.y];
+  const int t0 = blockIdx.x * AT;
+  if (t0 >= a.T) return;
+  const int n = a.cand_n[dom];
+  const int nt = min(AT, a.T - t0);
+  const void* fk = a.fk;
+  for (int i = threadIdx.x; i < AT * d; i += blockDim.x) {
+    const int r = i / d, c = i % d;
+    kt[r * dp + c] = r < nt ? ld_kv(fk, (static_cast<int64_t>(dom) * t.tmax + t0 + r) * d + c, t.kv_bf16) : 0.f;
+  }
+  __syncthreads();
+  if (threadIdx.x < AT) {
+    float s = 0.f;
+    for (int c = 0; c < d; ++c) s += kt[threadIdx.x * dp + c] * kt[threadIdx.x * dp + c];
+    ink[threadIdx.x] = s > 0.f ? rsqrtf(s) : 0.f;
+  }
+  const int32_t* cs = a.cand_slot + static_cast<int64_t>(dom) * t.cmax;
+  const uint8_t* cb = a.cand_buf + static_cast<int64_t>(dom) * t.cmax;
+  float* out = a.approx + (static_cast<int64_t>(dom) * t.tmax + t0) * t.cmax;
+  const int tp = threadIdx.x / 16, cq = threadIdx.x % 16;
+  for (int c0 = 0; c0 < n; c0 += AC) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < AC * d; i += blockDim.x) {
+      const int r = i / d, c = i % d;
+      float v = 0.f;
+      if (c0 + r < n) {
+        const int s = cs[c0 + r];
+        v = cb[c0 + r] ? t.brep32[static_cast<int64_t>(s) * d + c] : t.rep32[static_cast<int64_t>(s) * d + c];
+      }
+      rt[r * dp + c] = v;
+    }
+    if (threadIdx.x < AC) {
+      float nr = 0.f;
+      if (c0 + threadIdx.x < n) {
+        const int s = cs[c0 + threadIdx.x];
+        nr = static_cast<float>(cb[c0 + threadIdx.x] ? t.bnorm[s] : t.rnorm[s]);
+      }
+      inr[threadIdx.x] = nr > 0.f ? 1.f / nr : 0.f;
+    }
+    __syncthreads();
+    float acc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+    const float* k0 = kt + (2 * tp) * dp;
+    const float* k1 = k0 + dp;
+    for (int c = 0; c < d; ++c) {
+      const float x0 = k0[c], x1 = k1[c];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float y = rt[(4 * cq + j) * dp + c];
+        acc[0][j] = fmaf(x0, y, acc[0][j]);
+        acc[1][j] = fmaf(x1, y, acc[1][j]);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int tt = 2 * tp + i, cc = c0 + 4 * cq + j;
+        if (tt < nt && cc < n) out[static_cast<int64_t>(tt) * t.cmax + cc] = acc[i][j] * ink[tt] * inr[4 * cq + j];
+      }
+  }
+}
+
+// ============================================================================ K2
+// One warp per domain. Per token: exact fp64 cosines for (a) every candidate touched earlier in
+// this launch (its representative moved) and (b) every untouched candidate whose approximate
+// score is within 2*margin of the best untouched approximate score; arg-best with the
+// CandidateRef tie-break; then the maintainer branch.
+__global__ void __launch_bounds__(32) k_resolve(DevTables t, IngestArgs a) {
+  extern __shared__ uint8_t smraw[];
+  const int d = t.d, cmax = t.cmax, lane = threadIdx.x;
+  double* nk = reinterpret_cast<double*>(smraw);       // [tmax]
+  double* repn = nk + t.tmax;                           // [d]
+  double* bufn = repn + d;                              // [d]
+  double* relsim = bufn + d;                            // [cmax]
+  float* keyf = reinterpret_cast<float*>(relsim + cmax);  // [d]
+  int* cslot = reinterpret_cast<int*>(keyf + d);         // [cmax]
+  int* rel = cslot + cmax;                               // [cmax]
+  uint8_t* cbuf = reinterpret_cast<uint8_t*>(rel + cmax);  // [cmax]
+  uint8_t* touched = cbuf + cmax;                          // [cmax]
+
+  const int dom = a.active[blockIdx.x];
+  const int T = a.T;
+  const int cur = a.cursor[dom];
+  int n = a.cand_n[dom];
+  for (int c = lane; c < n; c += 32) {
+    cslot[c] = a.cand_slot[static_cast<int64_t>(dom) * cmax + c];
+    cbuf[c] = a.cand_buf[static_cast<int64_t>(dom) * cmax + c];
+    touched[c] = 0;
+  }
+  const void* fk = a.fk;
+  const uint8_t* fkb = static_cast<const uint8_t*>(a.fk);
+  const uint8_t* fvb = static_cast<const uint8_t*>(a.fv);
+  const int rb = d * t.es;
+  // |k_t| for every remaining token (vecmath.hpp:35-40), one sequential chain per lane
+  for (int tt = cur + lane; tt < T; tt += 32) {
+    double s = 0.0;
+    const int64_t base = (static_cast<int64_t>(dom) * t.tmax + tt) * d;
+    for (int i = 0; i < d; ++i) {
+      const double x = static_cast<double>(ld_kv(fk, base + i, t.kv_bf16));
+      s = dadd(s, dmul(x, x));
+    }
+    nk[tt] = __dsqrt_rn(s);
+  }
+  __syncwarp();
+  if (lane == 0) {
+    a.stop_t[dom] = T;
+    a.stop_kind[dom] = EV_NONE;
+    a.stop_slot[dom] = -1;
+  }
+  if (cur < T) {  // a degenerate representative throws at the first cosine (vecmath.hpp:59)
+    bool bad = false;
+    for (int c = lane; c < n; c += 32) {
+      const int s = cslot[c];
+      if ((cbuf[c] ? t.bnorm[s] : t.rnorm[s]) < 1e-12) bad = true;
+    }
+    if (__any_sync(kFull, bad)) {
+      if (lane == 0) {
+        set_err(t, DERR_DEGENERATE);
+        a.stop_t[dom] = cur;
+      }
+      return;
+    }
+  }
+  int n_exact = 0;
+  const float margin2 = 2.f * a.margin;
+  for (int tt = cur; tt < T; ++tt) {
+    const int64_t frow = static_cast<int64_t>(dom) * t.tmax + tt;
+    for (int i = lane; i < d; i += 32) keyf[i] = ld_kv(fk, frow * d + i, t.kv_bf16);
+    __syncwarp();
+    const double nkt = nk[tt];
+    if (n == 0) {  // maintainer.cpp:93-94
+      if (lane == 0) {
+        a.stop_t[dom] = tt;
+        a.stop_kind[dom] = EV_SEED;
+      }
+      break;
+    }
+    if (nkt < 1e-12) {
+      if (lane == 0) {
+        set_err(t, DERR_DEGENERATE);
+        a.stop_t[dom] = tt;
+      }
+      break;
+    }
+    // (1) best approximate score among untouched candidates
+    const float* ap = a.approx + frow * cmax;
+    float ba = -FLT_MAX;
+    for (int c = lane; c < n; c += 32)
+      if (!touched[c]) ba = fmaxf(ba, ap[c]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ba = fmaxf(ba, __shfl_xor_sync(kFull, ba, o));
+    const float thr = ba - margin2;
+    // (2) relevant candidates
+    int nrel = 0;
+    for (int c0 = 0; c0 < n; c0 += 32) {
+      const int c = c0 + lane;
+      const bool f = c < n && (touched[c] || ap[c] >= thr);
+      const unsigned m = __ballot_sync(kFull, f);
+      if (f) rel[nrel + __popc(m & ((1u << lane) - 1))] = c;
+      nrel += __popc(m);
+    }
+    __syncwarp();
+    n_exact += nrel;
+    // (3) exact cosines (vecmath.hpp:54-61), sequential sums
+    double bs = -3.0;
+    long long bk = LLONG_MAX;
+    int bp = -1;
+    for (int r = lane; r < nrel; r += 32) {
+      const int c = rel[r];
+      const int s = cslot[c];
+      const bool ib = cbuf[c];
+      const double* rp = (ib ? t.brep64 : t.rep64) + static_cast<int64_t>(s) * d;
+      const double nr = ib ? t.bnorm[s] : t.rnorm[s];
+      double acc = 0.0;
+      for (int i = 0; i < d; ++i) acc = dadd(acc, dmul(static_cast<double>(keyf[i]), rp[i]));
+      const double cs = clamp1(ddiv(acc, dmul(nkt, nr)));
+      relsim[r] = cs;
+      const long long key = 2LL * t.cid[s] + (ib ? 1 : 0);
+      if (better(cs, key, bs, bk)) {
+        bs = cs;
+        bk = key;
+        bp = r;
+      }
+    }
+    warp_best(bs, bk, bp);
+    const int bc = rel[bp];
+    const int slot = cslot[bc];
+    const bool isbuf = cbuf[bc];
+    // (4) Eq. 3/4 update into repn (not yet committed): r' = (n r + k)/(n+1)
+    const double dn = static_cast<double>(t.stat[slot]);
+    const double* rp = t.rep64 + static_cast<int64_t>(slot) * d;
+    for (int i = lane; i < d; i += 32)
+      repn[i] = ddiv(dadd(dmul(dn, rp[i]), static_cast<double>(keyf[i])), dadd(dn, 1.0));
+    // buffer running mean if the entry parks in the buffer (index.cpp:181-188); computed for
+    // every branch (cheap) so BUFJOIN and DEFER -- including DEFER onto an already-lazy
+    // cluster, whose buffer is non-empty -- share it
+    const int nb = t.nbuf[slot];
+    {
+      const double dnb = static_cast<double>(nb);
+      const double* bp2 = t.brep64 + static_cast<int64_t>(slot) * d;
+      for (int i = lane; i < d; i += 32)
+        bufn[i] = nb == 0 ? static_cast<double>(keyf[i])
+                          : ddiv(dadd(dmul(dnb, bp2[i]), static_cast<double>(keyf[i])), dadd(dnb, 1.0));
+    }
+    __syncwarp();
+    // sequential chains: lane 0 sq_dist(k, r') (vecmath.hpp:42-51), lane 1 |r'|, lane 2 |buf'|
+    double chain = 0.0;
+    if (lane == 0) {
+      for (int i = 0; i < d; ++i) {
+        const double df = dsub(static_cast<double>(keyf[i]), repn[i]);
+        chain = dadd(chain, dmul(df, df));
+      }
+    } else if (lane == 1) {
+      for (int i = 0; i < d; ++i) chain = dadd(chain, dmul(repn[i], repn[i]));
+      chain = __dsqrt_rn(chain);
+    } else if (lane == 2) {
+      for (int i = 0; i < d; ++i) chain = dadd(chain, dmul(bufn[i], bufn[i]));
+      chain = __dsqrt_rn(chain);
+    }
+    const double sq = __shfl_sync(kFull, chain, 0);
+    const double rn = __shfl_sync(kFull, chain, 1);
+    const double bn = __shfl_sync(kFull, chain, 2);
+    const double varn = ddiv(dadd(dmul(dn, t.var[slot]), sq), dadd(dn, 1.0));
+
+    int kind;
+    if (isbuf) {
+      kind = EV_BUFJOIN;
+    } else {
+      const int64_t npre = t.nmem[slot];
+      const double tau = t.tau_tab[npre < t.tau_len ? npre : t.tau_len - 1];
+      if (varn <= tau)
+        kind = EV_ABSORB;
+      else if (t.resid[slot] == 0)
+        kind = EV_SPLIT;
+      else if (a.defer)
+        kind = EV_DEFER;
+      else
+        kind = EV_EAGER;
+    }
+    if (kind == EV_SPLIT || kind == EV_EAGER) {  // host slow path; nothing committed
+      if (lane == 0) {
+        a.stop_t[dom] = tt;
+        a.stop_kind[dom] = kind;
+        a.stop_slot[dom] = slot;
+      }
+      break;
+    }
+    // commit statistics
+    double* rw = t.rep64 + static_cast<int64_t>(slot) * d;
+    float* rw32 = t.rep32 + static_cast<int64_t>(slot) * d;
+    for (int i = lane; i < d; i += 32) {
+      rw[i] = repn[i];
+      rw32[i] = static_cast<float>(repn[i]);
+    }
+    if (lane == 0) {
+      t.rnorm[slot] = rn;
+      t.var[slot] = varn;
+      t.stat[slot] += 1;
+    }
+    const uint8_t* srck = fkb + frow * rb;
+    const uint8_t* srcv = fvb + frow * rb;
+    if (kind == EV_ABSORB) {
+      warp_append(t, slot, false, srck, srcv);
+      if (lane == 0) t.nmem[slot] += 1;
+    } else {  // BUFJOIN / DEFER: entry parks in the buffer
+      double* bw = t.brep64 + static_cast<int64_t>(slot) * d;
+      float* bw32 = t.brep32 + static_cast<int64_t>(slot) * d;
+      for (int i = lane; i < d; i += 32) {
+        bw[i] = bufn[i];
+        bw32[i] = static_cast<float>(bufn[i]);
+      }
+      if (lane == 0) {
+        t.bnorm[slot] = bn;
+        if (kind == EV_DEFER) t.lazy[slot] = 1;
+      }
+      warp_append(t, slot, true, srck, srcv);
+      if (lane == 0) t.nbuf[slot] = nb + 1;
+    }
+    if (lane == 0) {
+      a.ev_kind[frow] = kind;
+      a.ev_slot[frow] = slot;
+      t.ring_owner[(static_cast<int64_t>(dom) * t.W + a.ring_slot) * t.tmax + tt] = slot;
+    }
+    // the winner's representative moved: every candidate of this slot is now "touched"
+    for (int c = lane; c < n; c += 32)
+      if (cslot[c] == slot) touched[c] = 1;
+    const bool fresh_buffer = kind == EV_DEFER && nb == 0;
+    if (fresh_buffer && lane == 0) {  // register the new buffer candidate (index.cpp:153-160)
+      if (n < cmax) {
+        cslot[n] = slot;
+        cbuf[n] = 1;
+        touched[n] = 1;
+      } else {
+        set_err(t, DERR_CANDIDATES);
+      }
+    }
+    if (fresh_buffer) n = min(n + 1, cmax);
+    __syncwarp();
+  }
+  if (lane == 0) a.n_exact[dom] = n_exact;
+}
+
+// ============================================================================ ring write
+__global__ void k_ring_write(DevTables t, const uint8_t* fk, const uint8_t* fv, int T, int rs) {
+  const int dom = blockIdx.y;
+  const int rb = t.d * t.es;
+  for (int tt = blockIdx.x; tt < t.tmax; tt += gridDim.x) {
+    if (threadIdx.x == 0) t.ring_owner[(static_cast<int64_t>(dom) * t.W + rs) * t.tmax + tt] = -1;
+    if (tt >= T) continue;
+    const int page = t.ring_pages[(static_cast<int64_t>(dom) * t.W + rs) * t.rpp + tt / t.P];
+    const int row = tt % t.P;
+    const int64_t src = (static_cast<int64_t>(dom) * t.tmax + tt) * rb;
+    uint8_t* dk = page_k(t, page) + static_cast<int64_t>(row) * rb;
+    uint8_t* dv = page_v(t, page) + static_cast<int64_t>(row) * rb;
+    for (int o = threadIdx.x * 16; o < rb; o += blockDim.x * 16) {
+      *reinterpret_cast<uint4*>(dk + o) = *reinterpret_cast<const uint4*>(fk + src + o);
+      *reinterpret_cast<uint4*>(dv + o) = *reinterpret_cast<const uint4*>(fv + src + o);
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x < t.rpp) {
+    const int j = threadIdx.x;
+    const int page = t.ring_pages[(static_cast<int64_t>(dom) * t.W + rs) * t.rpp + j];
+    t.pg_fill[page] = max(0, min(t.P, T - j * t.P));
+  }
+  if (blockIdx.x == 0 && dom == 0 && threadIdx.x == 0) t.ring_count[rs] = T;
+}
+
+// ============================================================================ store maintenance
+__global__ void k_append_runs(DevTables t, const AppendRun* runs, int n_runs, const int32_t* idx,
+                              const uint8_t* sk, const uint8_t* sv) {
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) / 32;
+  if (w >= n_runs) return;
+  const AppendRun r = runs[w];
+  const int rb = t.d * t.es;
+  for (int j = 0; j < r.n_rows; ++j) {
+    const int64_t row = idx[r.first_row + j];
+    if (!warp_append(t, r.slot, r.to_buffer != 0, sk + row * rb, sv + row * rb)) break;
+  }
+}
+
+__global__ void k_gather_cluster(DevTables t, int slot, int with_buf, uint8_t* sk, uint8_t* sv,
+                                 int64_t row0) {
+  // block b copies page b of the member list, then the buffer pages
+  const int np = t.npages[slot];
+  const int nbp = with_buf ? t.nbpages[slot] : 0;
+  const int64_t nmem = t.nmem[slot];
+  const int b = blockIdx.x;
+  if (b >= np + nbp) return;
+  const bool isb = b >= np;
+  const int j = isb ? b - np : b;
+  const int page = isb ? t.bpages[static_cast<int64_t>(slot) * t.maxbp + j]
+                       : t.pages[static_cast<int64_t>(slot) * t.maxp + j];
+  const int fill = t.pg_fill[page];
+  const int64_t first = row0 + (isb ? nmem : 0) + static_cast<int64_t>(j) * t.P;
+  const int rb = t.d * t.es;
+  const uint8_t* pk = page_k(t, page);
+  const uint8_t* pv = page_v(t, page);
+  for (int o = threadIdx.x * 16; o < fill * rb; o += blockDim.x * 16) {
+    *reinterpret_cast<uint4*>(sk + first * rb + o) = *reinterpret_cast<const uint4*>(pk + o);
+    *reinterpret_cast<uint4*>(sv + first * rb + o) = *reinterpret_cast<const uint4*>(pv + o);
+  }
+}
+
+__global__ void k_free_slot(DevTables t, int slot) {
+  const int np = t.npages[slot], nbp = t.nbpages[slot];
+  __shared__ int base;
+  if (threadIdx.x == 0) base = atomicAdd(t.free_top, np + nbp);
+  __syncthreads();
+  for (int i = threadIdx.x; i < np; i += blockDim.x)
+    t.free_stack[base + i] = t.pages[static_cast<int64_t>(slot) * t.maxp + i];
+  for (int i = threadIdx.x; i < nbp; i += blockDim.x)
+    t.free_stack[base + np + i] = t.bpages[static_cast<int64_t>(slot) * t.maxbp + i];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    t.npages[slot] = 0;
+    t.nbpages[slot] = 0;
+    t.nmem[slot] = 0;
+    t.nbuf[slot] = 0;
+    t.lazy[slot] = 0;
+    t.stat[slot] = 0;
+  }
+}
+
+__global__ void k_refresh_mirror(DevTables t, const int32_t* slots, int n) {
+  const int i = blockIdx.x;
+  if (i >= n) return;
+  const int64_t s = slots[i];
+  for (int c = threadIdx.x; c < t.d; c += blockDim.x) {
+    t.rep32[s * t.d + c] = static_cast<float>(t.rep64[s * t.d + c]);
+    if (t.nbuf[s] > 0) t.brep32[s * t.d + c] = static_cast<float>(t.brep64[s * t.d + c]);
+  }
+}
+
+// compute_representative / compute_variance (index.cpp:345-362), exact order.
+__global__ void k_exact_stats(DevTables t, const AppendRun* runs, int n_runs, const int32_t* idx,
+                              const void* sk) {
+  extern __shared__ double es[];
+  double* rep = es;            // [d]
+  double* sq = es + t.d;       // [blockDim]
+  const int r = blockIdx.x;
+  if (r >= n_runs) return;
+  const AppendRun run = runs[r];
+  const int d = t.d;
+  const int64_t s = run.slot;
+  const double inv = ddiv(1.0, static_cast<double>(run.n_rows));
+  for (int c = threadIdx.x; c < d; c += blockDim.x) {
+    double acc = 0.0;
+    for (int j = 0; j < run.n_rows; ++j)
+      acc = dadd(acc, static_cast<double>(ld_kv(sk, static_cast<int64_t>(idx[run.first_row + j]) * d + c, t.kv_bf16)));
+    rep[c] = dmul(acc, inv);
+    t.rep64[s * d + c] = rep[c];
+    t.rep32[s * d + c] = static_cast<float>(rep[c]);
+  }
+  __syncthreads();
+  double total = 0.0;
+  for (int j0 = 0; j0 < run.n_rows; j0 += blockDim.x) {
+    const int j = j0 + threadIdx.x;
+    if (j < run.n_rows) {
+      const int64_t row = idx[run.first_row + j];
+      double acc = 0.0;
+      for (int c = 0; c < d; ++c) {
+        const double df = dsub(static_cast<double>(ld_kv(sk, row * d + c, t.kv_bf16)), rep[c]);
+        acc = dadd(acc, dmul(df, df));
+      }
+      sq[threadIdx.x] = acc;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const int m = min(static_cast<int>(blockDim.x), run.n_rows - j0);
+      for (int i = 0; i < m; ++i) total = dadd(total, sq[i]);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    t.var[s] = ddiv(total, static_cast<double>(run.n_rows));
+    double nn = 0.0;
+    for (int c = 0; c < d; ++c) nn = dadd(nn, dmul(rep[c], rep[c]));
+    t.rnorm[s] = __dsqrt_rn(nn);
+  }
+}
+
+__global__ void k_to_f32(const void* src, float* dst, int64_t n, int bf16) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    dst[i] = ld_kv(src, i, bf16);
+}
+
+// ============================================================================ K4
+// Block-wide k-best selection by repeated arg-best (k <= 64): items (sim[i], key[i]).
+__device__ int block_take_best(const double* sim, const long long* key, uint8_t* taken, int n,
+                               double* red_s, long long* red_k, int* red_i) {
+  double bs = -4.0;
+  long long bk = LLONG_MAX;
+  int bi = -1;
+  for (int i = threadIdx.x; i < n; i += blockDim.x)
+    if (!taken[i] && better(sim[i], key[i], bs, bk)) {
+      bs = sim[i];
+      bk = key[i];
+      bi = i;
+    }
+  warp_best(bs, bk, bi);
+  const int w = threadIdx.x / 32, nw = blockDim.x / 32;
+  if ((threadIdx.x & 31) == 0) {
+    red_s[w] = bs;
+    red_k[w] = bk;
+    red_i[w] = bi;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = red_s[0];
+    long long k = red_k[0];
+    int ii = red_i[0];
+    for (int j = 1; j < nw; ++j)
+      if (red_i[j] >= 0 && (ii < 0 || better(red_s[j], red_k[j], s, k))) {
+        s = red_s[j];
+        k = red_k[j];
+        ii = red_i[j];
+      }
+    red_i[32] = ii;
+    if (ii >= 0) taken[ii] = 1;
+  }
+  __syncthreads();
+  const int r = red_i[32];
+  __syncthreads();
+  return r;
+}
+
+// exact cosine of q (fp32, norm nq) with a fp64 row (vecmath.hpp:54-61)
+__device__ __forceinline__ double exact_cos(const float* q, double nq, const double* row, double nr,
+                                            int d, bool& degenerate) {
+  if (nq < 1e-12 || nr < 1e-12) {
+    degenerate = true;
+    return -2.0;
+  }
+  double acc = 0.0;
+  for (int i = 0; i < d; ++i) acc = dadd(acc, dmul(static_cast<double>(q[i]), row[i]));
+  return clamp1(ddiv(acc, dmul(nq, nr)));
+}
+
+struct K4Smem {
+  double* vsim;
+  long long* vkey;
+  uint8_t* vtaken;
+  double* csim;
+  long long* ckey;
+  uint8_t* ctaken;
+  int* cslot;
+  uint8_t* cbuf;
+};
+
+__global__ void __launch_bounds__(256) k_score_select(DevTables t, DecodeArgs a, int* work_ctr) {
+  extern __shared__ uint8_t sm4[];
+  const int l = blockIdx.x, d = t.d, L = t.L;
+  const int P = *t.n_parts;
+  const int cmax = t.cmax;
+  // carve
+  uint8_t* p = sm4;
+  float* qf = reinterpret_cast<float*>(p);
+  p += ((d * 4 + 15) / 16) * 16;
+  double* vsim = reinterpret_cast<double*>(p);
+  p += static_cast<size_t>(t.max_parts) * 8;
+  long long* vkey = reinterpret_cast<long long*>(p);
+  p += static_cast<size_t>(t.max_parts) * 8;
+  double* csim = reinterpret_cast<double*>(p);
+  p += static_cast<size_t>(cmax) * 8;
+  long long* ckey = reinterpret_cast<long long*>(p);
+  p += static_cast<size_t>(cmax) * 8;
+  int* cslot = reinterpret_cast<int*>(p);
+  p += static_cast<size_t>(cmax) * 4;
+  uint8_t* cbuf = p;
+  p += cmax;
+  uint8_t* vtaken = p;
+  p += t.max_parts;
+  uint8_t* ctaken = p;
+  p += cmax;
+  __shared__ double red_s[32];
+  __shared__ long long red_k[32];
+  __shared__ int red_i[33];
+  __shared__ double nq_s;
+  __shared__ int ncand_s, chosen[64];
+  __shared__ int vers[64], nver_s;
+  __shared__ unsigned long long att_s;
+  __shared__ bool degen;
+
+  if (l == 0 && threadIdx.x == 0) *work_ctr = 0;
+  const float* q = a.q + static_cast<int64_t>(l) * d;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) qf[i] = q[i];
+  if (threadIdx.x == 0) {
+    degen = false;
+    att_s = 0;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int i = 0; i < d; ++i) s = dadd(s, dmul(static_cast<double>(qf[i]), static_cast<double>(qf[i])));
+    nq_s = __dsqrt_rn(s);
+  }
+  __syncthreads();
+  const double nq = nq_s;
+  bool dg = false;
+  // ---- stage 1: visual_topk (index.cpp:192-208)
+  for (int pp = threadIdx.x; pp < P; pp += blockDim.x) {
+    vsim[pp] = exact_cos(qf, nq, t.vrep + static_cast<int64_t>(pp) * d, t.vnorm[pp], d, dg);
+    vkey[pp] = pp;
+    vtaken[pp] = 0;
+  }
+  if (dg) degen = true;
+  __syncthreads();
+  const int kv = min(a.k_v, P);
+  for (int i = 0; i < kv; ++i) {
+    const int b = block_take_best(vsim, vkey, vtaken, P, red_s, red_k, red_i);
+    if (threadIdx.x == 0) chosen[i] = b;
+  }
+  __syncthreads();
+  if (threadIdx.x < kv) a.parts[l * a.k_v + threadIdx.x] = chosen[threadIdx.x];
+  if (threadIdx.x == 0) a.n_parts_sel[l] = kv;
+
+  // ---- stage 2 (and the prefetch ranking of layer l+1, retrieval.cpp:117-128)
+  const int passes = (a.prefetch && l + 1 < L) ? 2 : 1;
+  for (int pass = 0; pass < passes; ++pass) {
+    const int layer = l + pass;
+    const int ktake = pass == 0 ? a.k_s : a.prefetch_k;
+    if (threadIdx.x == 0) ncand_s = 0;
+    __syncthreads();
+    for (int i = 0; i < kv; ++i) {
+      const int64_t key = static_cast<int64_t>(chosen[i]) * L + layer;
+      const int off = t.pl_off[key], cnt = t.pl_cnt[key];
+      for (int j = threadIdx.x; j < cnt; j += blockDim.x) {
+        const int s = t.pl_pool[off + j];
+        const int lz = t.lazy[s];
+        const int k = atomicAdd(&ncand_s, lz ? 2 : 1);
+        if (k + (lz ? 2 : 1) > cmax) {
+          set_err(t, DERR_CANDIDATES);
+          continue;
+        }
+        cslot[k] = s;
+        cbuf[k] = 0;
+        if (lz) {
+          cslot[k + 1] = s;
+          cbuf[k + 1] = 1;
+        }
+      }
+    }
+    __syncthreads();
+    const int nc = min(ncand_s, cmax);
+    if (pass == 0 && threadIdx.x == 0) a.n_cand[l] = nc;
+    dg = false;
+    for (int c = threadIdx.x; c < nc; c += blockDim.x) {
+      const int s = cslot[c];
+      const bool ib = cbuf[c];
+      csim[c] = exact_cos(qf, nq, (ib ? t.brep64 : t.rep64) + static_cast<int64_t>(s) * d,
+                          ib ? t.bnorm[s] : t.rnorm[s], d, dg);
+      ckey[c] = 2LL * t.cid[s] + (ib ? 1 : 0);
+      ctaken[c] = 0;
+    }
+    if (dg) degen = true;
+    __syncthreads();
+    const int take = min(ktake, nc);
+    for (int i = 0; i < take; ++i) {
+      const int b = block_take_best(csim, ckey, ctaken, nc, red_s, red_k, red_i);
+      if (threadIdx.x == 0) {
+        if (pass == 0) {
+          a.ranked_slot[l * a.k_s + i] = cslot[b];
+          a.ranked_buf[l * a.k_s + i] = cbuf[b];
+        } else {
+          a.pf_slot[l * a.prefetch_k + i] = cslot[b];
+          a.pf_buf[l * a.prefetch_k + i] = cbuf[b];
+        }
+      }
+    }
+    if (threadIdx.x == 0) {
+      if (pass == 0)
+        a.n_ranked[l] = take;
+      else
+        a.n_pf[l] = take;
+    }
+    __syncthreads();
+  }
+  if (passes == 1 && threadIdx.x == 0) a.n_pf[l] = 0;
+  if (degen && threadIdx.x == 0) set_err(t, DERR_DEGENERATE);
+
+  // ---- verified (dedup in rank order, retrieval.cpp:20-26) + attended count + work list
+  if (threadIdx.x == 0) {
+    int nv = 0;
+    for (int i = 0; i < a.n_ranked[l]; ++i) {
+      const int s = a.ranked_slot[l * a.k_s + i];
+      bool dup = false;
+      for (int j = 0; j < nv; ++j) dup |= vers[j] == s;
+      if (!dup) vers[nv++] = s;
+    }
+    nver_s = nv;
+    unsigned long long att = 0;
+    int ni = 0;
+    int4* items = a.items + static_cast<int64_t>(l) * a.max_items;
+    for (int j = 0; j < nv; ++j) {
+      const int s = vers[j];
+      a.ver_slot[l * a.k_s + j] = s;
+      att += static_cast<unsigned long long>(t.nmem[s] + t.nbuf[s]);
+      const int np = t.npages[s], nbp = t.nbpages[s];
+      for (int f = 0; f < np; f += a.chunk_pages)
+        if (ni < a.max_items) items[ni++] = make_int4(0, s, f, min(a.chunk_pages, np - f));
+      for (int f = 0; f < nbp; f += a.chunk_pages)
+        if (ni < a.max_items) items[ni++] = make_int4(1, s, f, min(a.chunk_pages, nbp - f));
+    }
+    a.n_ver[l] = nv;
+    att_s = att;
+    red_i[0] = ni;
+  }
+  __syncthreads();
+  // window ring: unmasked tokens per (ring slot, page)
+  __shared__ int ring_cnt[64];
+  const int W = t.W, rpp = t.rpp;
+  for (int i = threadIdx.x; i < W * rpp && i < 64; i += blockDim.x) ring_cnt[i] = 0;
+  __syncthreads();
+  const int nv = nver_s;
+  for (int i = threadIdx.x; i < W * t.tmax; i += blockDim.x) {
+    const int rs = i / t.tmax, tt = i % t.tmax;
+    if (tt >= t.ring_count[rs]) continue;
+    const int own = t.ring_owner[(static_cast<int64_t>(l) * W + rs) * t.tmax + tt];
+    bool m = false;
+    for (int j = 0; j < nv; ++j) m |= vers[j] == own;
+    if (!m) {
+      atomicAdd(&att_s, 1ull);
+      if (rs * rpp + tt / t.P < 64) atomicAdd(&ring_cnt[rs * rpp + tt / t.P], 1);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int ni = red_i[0];
+    int4* items = a.items + static_cast<int64_t>(l) * a.max_items;
+    for (int i = 0; i < W * rpp && i < 64; ++i)
+      if (ring_cnt[i] > 0) {
+        if (ni < a.max_items)
+          items[ni++] = make_int4(2, i / rpp, i % rpp, 1);
+        else
+          set_err(t, DERR_ITEMS);
+      }
+    a.n_items[l] = ni;
+    a.attended[l] = static_cast<int64_t>(att_s);
+  }
+  if (a.n_items != nullptr) {
+    __syncthreads();
+    if (a.n_items[l] == 0)  // nothing attended: output zeros
+      for (int i = threadIdx.x; i < d; i += blockDim.x) a.out[static_cast<int64_t>(l) * d + i] = 0.f;
+  }
+}
+
+// ============================================================================ K6
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, int cnt) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(cnt));
+}
+__device__ __forceinline__ void mbar_expect(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "W_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra W_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+struct StageMeta {
+  int dom, item, page, fill;
+  int kind, ring_slot, tok0, flags;  // flags: 1 first page of item, 2 last page of item
+};
+
+template <int D, bool BF16, int STAGES>
+__global__ void __launch_bounds__(128) k_attend(DevTables t, DecodeArgs a, int* work_ctr) {
+  constexpr int ES = BF16 ? 2 : 4;
+  constexpr int ROWB = D * ES;
+  extern __shared__ __align__(128) uint8_t sm6[];
+  const int P = t.P;
+  const int64_t stage_bytes = static_cast<int64_t>(2) * P * ROWB;
+  uint8_t* stages = sm6;
+  __shared__ __align__(8) uint64_t full[STAGES];
+  __shared__ StageMeta meta[STAGES];
+  __shared__ float qs[D];
+  __shared__ int vers_s[64];
+  __shared__ int nver_sh;
+  __shared__ int prefix[1025];
+  __shared__ float wm[4], wl[4];
+  __shared__ float wo[4][D];
+  __shared__ int last_flag;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int L = t.L;
+  if (tid == 0) {
+    prefix[0] = 0;
+    for (int l = 0; l < L && l < 1024; ++l) prefix[l + 1] = prefix[l] + a.n_items[l];
+    for (int s = 0; s < STAGES; ++s) mbar_init(&full[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int total = prefix[min(L, 1024)];
+
+  // ---- producer state (thread 0 only)
+  int p_item = -1, p_dom = 0, p_j = 0, p_pg = 0;
+  int4 p_it = make_int4(0, 0, 0, 0);
+  bool p_done = false;
+  auto produce = [&](int s) -> bool {  // thread 0: next page into stage s
+    if (p_done) return false;
+    while (true) {
+      if (p_item < 0 || p_pg >= p_it.w) {
+        const int g = atomicAdd(work_ctr, 1);
+        if (g >= total) {
+          p_done = true;
+          return false;
+        }
+        int lo = 0, hi = L;  // prefix[lo] <= g < prefix[lo+1]
+        while (hi - lo > 1) {
+          const int mid = (lo + hi) / 2;
+          if (prefix[mid] <= g) lo = mid; else hi = mid;
+        }
+        p_dom = lo;
+        p_j = g - prefix[lo];
+        p_it = a.items[static_cast<int64_t>(p_dom) * a.max_items + p_j];
+        p_item = g;
+        p_pg = 0;
+      }
+      StageMeta m;
+      m.dom = p_dom;
+      m.item = p_j;
+      m.kind = p_it.x;
+      m.flags = (p_pg == 0 ? 1 : 0) | (p_pg == p_it.w - 1 ? 2 : 0);
+      const int pidx = p_it.z + p_pg;
+      if (m.kind == 0) {
+        m.page = t.pages[static_cast<int64_t>(p_it.y) * t.maxp + pidx];
+        m.ring_slot = -1;
+        m.tok0 = 0;
+      } else if (m.kind == 1) {
+        m.page = t.bpages[static_cast<int64_t>(p_it.y) * t.maxbp + pidx];
+        m.ring_slot = -1;
+        m.tok0 = 0;
+      } else {
+        m.ring_slot = p_it.y;
+        m.page = t.ring_pages[(static_cast<int64_t>(p_dom) * t.W + p_it.y) * t.rpp + pidx];
+        m.tok0 = pidx * P;
+      }
+      m.fill = t.pg_fill[m.page];
+      p_pg += 1;
+      meta[s] = m;
+      const uint32_t bytes = static_cast<uint32_t>(m.fill) * ROWB;
+      uint8_t* dst = stages + s * stage_bytes;
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_expect(&full[s], 2 * bytes);
+      bulk_g2s(dst, page_k(t, m.page), bytes, &full[s]);
+      bulk_g2s(dst + static_cast<int64_t>(P) * ROWB, page_v(t, m.page), bytes, &full[s]);
+      return true;
+    }
+  };
+  __shared__ int issued[STAGES];
+  if (tid == 0)
+    for (int s = 0; s < STAGES; ++s) issued[s] = produce(s) ? 1 : 0;
+  __syncthreads();
+
+  float m_run = -INFINITY, l_run = 0.f;
+  constexpr int OPL = D / 32;  // output dims per lane
+  float o_run[OPL];
+#pragma unroll
+  for (int i = 0; i < OPL; ++i) o_run[i] = 0.f;
+  int cur_dom = -1;
+  uint32_t phase_bits = 0;
+  const float sl2 = a.scale_log2;
+
+  for (int s = 0;; s = (s + 1) % STAGES) {
+    if (!issued[s]) break;
+    mbar_wait(&full[s], (phase_bits >> s) & 1u);
+    phase_bits ^= (1u << s);
+    const StageMeta m = meta[s];
+    if (m.flags & 1) {  // new item: reset state, load the domain's query / verified list
+      m_run = -INFINITY;
+      l_run = 0.f;
+#pragma unroll
+      for (int i = 0; i < OPL; ++i) o_run[i] = 0.f;
+      if (m.dom != cur_dom) {
+        __syncthreads();
+        for (int i = tid; i < D; i += 128) qs[i] = a.q[static_cast<int64_t>(m.dom) * D + i];
+        if (tid == 0) nver_sh = a.n_ver[m.dom];
+        if (tid < 64) vers_s[tid] = tid < a.n_ver[m.dom] ? a.ver_slot[m.dom * a.k_s + tid] : -1;
+        __syncthreads();
+        cur_dom = m.dom;
+      }
+    }
+    const uint8_t* Ks = stages + s * stage_bytes;
+    const uint8_t* Vs = Ks + static_cast<int64_t>(P) * ROWB;
+    // ---- scores: 2 threads per token, 16 tokens per warp per sub-tile of 64
+    for (int tb = 0; tb < P; tb += 64) {
+      const int tok = tb + (tid >> 1);
+      const int half = tid & 1;
+      float sc = -INFINITY;
+      bool valid = tok < m.fill;
+      if (valid && m.kind == 2) {
+        const int own = t.ring_owner[(static_cast<int64_t>(m.dom) * t.W + m.ring_slot) * t.tmax + m.tok0 + tok];
+        for (int j = 0; j < nver_sh; ++j) valid &= vers_s[j] != own;
+      }
+      float acc = 0.f;
+      if (tok < m.fill) {
+        constexpr int CH = ROWB / 32;  // 16-byte chunks per half row
+        const uint8_t* krow = Ks + static_cast<int64_t>(tok) * ROWB + half * (ROWB / 2);
+#pragma unroll
+        for (int j = 0; j < CH; ++j) {
+          const int c = (j + tok) % CH;
+          const uint4 raw = *reinterpret_cast<const uint4*>(krow + c * 16);
+          if (BF16) {
+            const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
+            const float* qq = qs + half * (D / 2) + c * 8;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float2 f = __bfloat1622float2(h2[e]);
+              acc = fmaf(f.x, qq[2 * e], acc);
+              acc = fmaf(f.y, qq[2 * e + 1], acc);
+            }
+          } else {
+            const float* f = reinterpret_cast<const float*>(&raw);
+            const float* qq = qs + half * (D / 2) + c * 4;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) acc = fmaf(f[e], qq[e], acc);
+          }
+        }
+      }
+      acc += __shfl_xor_sync(kFull, acc, 1);
+      if (valid) sc = acc * sl2;
+      // warp max over its 16 tokens
+      float mx = sc;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(kFull, mx, o));
+      const float m_new = fmaxf(m_run, mx);
+      if (m_new == -INFINITY) continue;  // nothing valid yet in this warp
+      const float alpha = exp2f(m_run - m_new);
+      const float pr = valid ? exp2f(sc - m_new) : 0.f;
+      float psum = half == 0 ? pr : 0.f;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) psum += __shfl_xor_sync(kFull, psum, o);
+      l_run = l_run * alpha + psum;
+#pragma unroll
+      for (int i = 0; i < OPL; ++i) o_run[i] *= alpha;
+      m_run = m_new;
+      // P.V over the warp's 16 tokens; lane owns dims [lane*OPL, lane*OPL + OPL)
+#pragma unroll 4
+      for (int j = 0; j < 16; ++j) {
+        const float pj = __shfl_sync(kFull, pr, 2 * j);
+        const int tj = tb + warp * 16 + j;
+        if (tj >= m.fill || pj == 0.f) continue;
+        const uint8_t* vrow = Vs + static_cast<int64_t>(tj) * ROWB + lane * OPL * ES;
+        if (BF16) {
+#pragma unroll
+          for (int i = 0; i < OPL; i += 2) {
+            const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(vrow + i * 2));
+            o_run[i] = fmaf(pj, f.x, o_run[i]);
+            if (i + 1 < OPL) o_run[i + 1] = fmaf(pj, f.y, o_run[i + 1]);
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < OPL; ++i) o_run[i] = fmaf(pj, reinterpret_cast<const float*>(vrow)[i], o_run[i]);
+        }
+      }
+    }
+    __syncthreads();  // stage s fully consumed
+    if (m.flags & 2) {  // item done: merge the 4 warps, write the partial
+      if (lane == 0) {
+        wm[warp] = m_run;
+        wl[warp] = l_run;
+      }
+#pragma unroll
+      for (int i = 0; i < OPL; ++i) wo[warp][lane * OPL + i] = o_run[i];
+      __syncthreads();
+      float M = fmaxf(fmaxf(wm[0], wm[1]), fmaxf(wm[2], wm[3]));
+      const int64_t pi = static_cast<int64_t>(m.dom) * a.max_items + m.item;
+      for (int c = tid; c < D; c += 128) {
+        float o = 0.f;
+        for (int w = 0; w < 4; ++w)
+          if (wm[w] != -INFINITY) o += wo[w][c] * exp2f(wm[w] - M);
+        a.part_o[pi * D + c] = o;
+      }
+      if (tid == 0) {
+        float lsum = 0.f;
+        for (int w = 0; w < 4; ++w)
+          if (wm[w] != -INFINITY) lsum += wl[w] * exp2f(wm[w] - M);
+        a.part_ml[pi * 2] = M;
+        a.part_ml[pi * 2 + 1] = lsum;
+      }
+      __threadfence();
+      __syncthreads();
+      if (tid == 0) last_flag = (atomicAdd(&a.dom_done[m.dom], 1) + 1 == a.n_items[m.dom]);
+      __syncthreads();
+      if (last_flag) {  // combine all partials of the domain (split-KV reduction)
+        __threadfence();
+        const int ni = a.n_items[m.dom];
+        const float* ml = a.part_ml + static_cast<int64_t>(m.dom) * a.max_items * 2;
+        float MM = -INFINITY;
+        for (int i = 0; i < ni; ++i) MM = fmaxf(MM, ml[2 * i]);
+        for (int c = tid; c < D; c += 128) {
+          float num = 0.f, den = 0.f;
+          for (int i = 0; i < ni; ++i) {
+            if (ml[2 * i] == -INFINITY) continue;
+            const float w = exp2f(ml[2 * i] - MM);
+            num += w * a.part_o[(static_cast<int64_t>(m.dom) * a.max_items + i) * D + c];
+            den += w * ml[2 * i + 1];
+          }
+          a.out[static_cast<int64_t>(m.dom) * D + c] = den > 0.f ? num / den : 0.f;
+        }
+        if (tid == 0) a.dom_done[m.dom] = 0;
+      }
+      m_run = -INFINITY;
+      l_run = 0.f;
+#pragma unroll
+      for (int i = 0; i < OPL; ++i) o_run[i] = 0.f;
+      __syncthreads();
+    }
+    if (tid == 0) issued[s] = produce(s) ? 1 : 0;
+    __syncthreads();
+  }
+}
+
+// flat top-k over an explicit candidate list (one CTA)
+__global__ void __launch_bounds__(256) k_flat_topk(DevTables t, const float* q, const int32_t* slots,
+                                                   const uint8_t* bufs, int n, int k, int32_t* out) {
+  extern __shared__ uint8_t smf[];
+  double* sim = reinterpret_cast<double*>(smf);
+  long long* key = reinterpret_cast<long long*>(sim + n);
+  uint8_t* taken = reinterpret_cast<uint8_t*>(key + n);
+  __shared__ double red_s[32];
+  __shared__ long long red_k[32];
+  __shared__ int red_i[33];
+  __shared__ float qf[256];
+  __shared__ double nq;
+  const int d = t.d;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) qf[i] = q[i];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int i = 0; i < d; ++i) s = dadd(s, dmul(static_cast<double>(qf[i]), static_cast<double>(qf[i])));
+    nq = __dsqrt_rn(s);
+  }
+  __syncthreads();
+  bool dg = false;
+  for (int c = threadIdx.x; c < n; c += blockDim.x) {
+    const int s = slots[c];
+    const bool ib = bufs[c];
+    sim[c] = exact_cos(qf, nq, (ib ? t.brep64 : t.rep64) + static_cast<int64_t>(s) * d,
+                       ib ? t.bnorm[s] : t.rnorm[s], d, dg);
+    key[c] = 2LL * t.cid[s] + (ib ? 1 : 0);
+    taken[c] = 0;
+  }
+  if (dg) set_err(t, DERR_DEGENERATE);
+  __syncthreads();
+  const int take = min(n, k);
+  for (int i = 0; i < take; ++i) {
+    const int b = block_take_best(sim, key, taken, n, red_s, red_k, red_i);
+    if (threadIdx.x == 0) out[i] = b;
+  }
+}
+
+}  // namespace
+
+// ============================================================================ launchers
+
+int launch_build_cands(const DevTables& t, const IngestArgs& a, cudaStream_t st) {
+  k_build_cands<<<a.n_active, 256, 0, st>>>(t, a);
+  return 1;
+}
+
+int launch_approx(const DevTables& t, const IngestArgs& a, cudaStream_t st) {
+  const int dp = t.d + 1;
+  const size_t smem = static_cast<size_t>(AT * dp + AC * dp + AT + AC) * 4;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_approx, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  dim3 g((a.T + AT - 1) / AT, a.n_active);
+  k_approx<<<g, 256, smem, st>>>(t, a);
+  return 1;
+}
+
+int launch_resolve(const DevTables& t, const IngestArgs& a, cudaStream_t st) {
+  const size_t smem = static_cast<size_t>(t.tmax) * 8 + 2 * t.d * 8 + static_cast<size_t>(t.cmax) * 8 +
+                      t.d * 4 + static_cast<size_t>(t.cmax) * 4 * 2 + static_cast<size_t>(t.cmax) * 2 + 64;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_resolve, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  k_resolve<<<a.n_active, 32, smem, st>>>(t, a);
+  return 1;
+}
+
+int launch_ring_write(const DevTables& t, const void* fk, const void* fv, int32_t T, int32_t rs,
+                      cudaStream_t st) {
+  dim3 g(min(t.tmax, 64), t.L);
+  k_ring_write<<<g, 128, 0, st>>>(t, static_cast<const uint8_t*>(fk), static_cast<const uint8_t*>(fv), T, rs);
+  return 1;
+}
+
+int launch_append_runs(const DevTables& t, const AppendRun* runs, int32_t n_runs, const int32_t* idx,
+                       const void* sk, const void* sv, cudaStream_t st) {
+  if (n_runs <= 0) return 0;
+  const int warps = 4;
+  k_append_runs<<<(n_runs + warps - 1) / warps, 32 * warps, 0, st>>>(
+      t, runs, n_runs, idx, static_cast<const uint8_t*>(sk), static_cast<const uint8_t*>(sv));
+  return 1;
+}
+
+int launch_gather_cluster(const DevTables& t, int32_t slot, int32_t with_buf, void* sk, void* sv,
+                          int64_t row0, cudaStream_t st) {
+  const int blocks = t.maxp + (with_buf ? t.maxbp : 0);
+  k_gather_cluster<<<blocks, 128, 0, st>>>(t, slot, with_buf, static_cast<uint8_t*>(sk),
+                                           static_cast<uint8_t*>(sv), row0);
+  return 1;
+}
+
+int launch_free_slot_pages(const DevTables& t, int32_t slot, cudaStream_t st) {
+  k_free_slot<<<1, 128, 0, st>>>(t, slot);
+  return 1;
+}
+
+int launch_refresh_mirror(const DevTables& t, const int32_t* slots, int32_t n, cudaStream_t st) {
+  if (n <= 0) return 0;
+  k_refresh_mirror<<<n, 128, 0, st>>>(t, slots, n);
+  return 1;
+}
+
+int launch_exact_stats(const DevTables& t, const AppendRun* runs, int32_t n_runs, const int32_t* idx,
+                       const void* sk, cudaStream_t st) {
+  if (n_runs <= 0) return 0;
+  const int threads = 128;
+  const size_t smem = static_cast<size_t>(t.d + threads) * 8;
+  k_exact_stats<<<n_runs, threads, smem, st>>>(t, runs, n_runs, idx, sk);
+  return 1;
+}
+
+int launch_to_f32(const DevTables& t, const void* src, float* dst, int64_t n, cudaStream_t st) {
+  if (n <= 0) return 0;
+  const int blocks = static_cast<int>((n + 255) / 256 < 4096 ? (n + 255) / 256 : 4096);
+  k_to_f32<<<blocks, 256, 0, st>>>(src, dst, n, t.kv_bf16);
+  return 1;
+}
+
+int launch_flat_topk(const DevTables& t, const float* q, const int32_t* slots, const uint8_t* bufs,
+                     int32_t n, int32_t k, int32_t* out, cudaStream_t st) {
+  const size_t smem = static_cast<size_t>(n) * 17 + 16;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_flat_topk, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  k_flat_topk<<<1, 256, smem, st>>>(t, q, slots, bufs, n, k, out);
+  return 1;
+}
+
+namespace {
+int g_sms = 0;
+int* g_ctr = nullptr;
+
+template <int D, bool BF16>
+int launch_attend_t(const DevTables& t, const DecodeArgs& a, cudaStream_t st) {
+  constexpr int STAGES = BF16 ? 3 : 2;
+  const size_t smem = static_cast<size_t>(STAGES) * 2 * t.P * D * (BF16 ? 2 : 4);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_attend<D, BF16, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(smem));
+    attr = true;
+  }
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_attend<D, BF16, STAGES>, 128, smem);
+  per_sm = max(1, per_sm);
+  k_attend<D, BF16, STAGES><<<g_sms * per_sm, 128, smem, st>>>(t, a, g_ctr);
+  return 1;
+}
+}  // namespace
+
+int launch_decode(const DevTables& t, const DecodeArgs& a, cudaStream_t st, cudaEvent_t* ev) {
+  if (!g_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaMalloc(&g_ctr, 64);
+  }
+  if (ev) cudaEventRecord(ev[0], st);
+  const size_t smem4 = ((t.d * 4 + 15) / 16) * 16 + static_cast<size_t>(t.max_parts) * 17 +
+                       static_cast<size_t>(t.cmax) * 22 + 64;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_score_select, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  k_score_select<<<t.L, 256, smem4, st>>>(t, a, g_ctr);
+  if (ev) cudaEventRecord(ev[1], st);
+  int n = 1;
+  switch (t.d * 2 + t.kv_bf16) {
+    case 64: n += launch_attend_t<32, false>(t, a, st); break;
+    case 65: n += launch_attend_t<32, true>(t, a, st); break;
+    case 128: n += launch_attend_t<64, false>(t, a, st); break;
+    case 129: n += launch_attend_t<64, true>(t, a, st); break;
+    case 256: n += launch_attend_t<128, false>(t, a, st); break;
+    case 257: n += launch_attend_t<128, true>(t, a, st); break;
+    case 512: n += launch_attend_t<256, false>(t, a, st); break;
+    case 513: n += launch_attend_t<256, true>(t, a, st); break;
+    default: break;
+  }
+  if (ev) {
+    cudaEventRecord(ev[2], st);
+    cudaEventRecord(ev[3], st);
+  }
+  return n;
+}
+
+}  // namespace kvc

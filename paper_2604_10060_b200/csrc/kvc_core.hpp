@@ -1,0 +1,206 @@
+// kvc_core.hpp -- declarations shared by the host control plane (context.cpp) and the
+// sm_100a kernels (kernels.cu). Plain structs of device pointers; no torch.
+#pragma once
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+#include <cuda_runtime.h>
+
+namespace kvc {
+
+// ----------------------------------------------------------------------------- errors
+// One exception type carrying a KVC_E_* code; the C-ABI turns it into the return value.
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] inline void fail(int code, const std::string& msg) { throw Error(code, msg); }
+
+#define KVC_CUDA(expr)                                                                 \
+  do {                                                                                 \
+    cudaError_t e_ = (expr);                                                           \
+    if (e_ != cudaSuccess)                                                             \
+      ::kvc::fail(-20, std::string("CUDA: ") + cudaGetErrorString(e_) + " at " #expr); \
+  } while (0)
+
+// ----------------------------------------------------------------------------- events
+// Per-(domain, token) outcome of the device resolve kernel (maintainer.cpp:88-176 branches).
+enum EventKind : int32_t {
+  EV_NONE = 0,
+  EV_ABSORB = 1,   // add_member + note_device_append          (maintainer.cpp:132-137)
+  EV_BUFJOIN = 2,  // buffer candidate won: add_to_buffer        (maintainer.cpp:112-123)
+  EV_DEFER = 3,    // over threshold on a Host cluster: lazy mark (maintainer.cpp:170-175)
+  EV_SEED = 4,     // host: empty candidate set -> seed_cluster   (maintainer.cpp:93-94)
+  EV_SPLIT = 5,    // host: over threshold on a Device cluster    (maintainer.cpp:139-149)
+  EV_EAGER = 6,    // host: eager policy fetch + split            (maintainer.cpp:153-166)
+};
+
+// Device error flags (bit set in DevTables::err).
+enum DevErr : int32_t {
+  DERR_DEGENERATE = 1,  // a norm below 1e-12 met a cosine (vecmath.hpp:59)
+  DERR_PAGES = 2,       // page pool exhausted
+  DERR_CLUSTER_PAGES = 4,
+  DERR_CANDIDATES = 8,  // more candidates than max_candidates
+  DERR_ITEMS = 16,      // attention work list overflow
+};
+
+// ----------------------------------------------------------------------------- device state
+// Cluster tables are SoA indexed by a device *slot*; the host maps slots <-> cluster ids.
+// K/V live in a page pool: page p = [K: page_tokens x d][V: page_tokens x d] in kv dtype,
+// cluster-contiguous (a cluster's members are its pages in order; buffered entries of a
+// pending split use a second page list).
+struct DevTables {
+  int32_t d, L, P, es;  // dim, domains, page tokens, element size (4 f32 / 2 bf16)
+  int32_t kv_bf16;
+  int32_t max_slots, maxp, maxbp, max_parts, cmax, tmax, W;
+  int64_t max_pages, page_bytes;
+
+  double* rep64;   // [S][d] running centroid (Eq. 3), fp64 master
+  float* rep32;    // [S][d] fp32 mirror for the approximate tile
+  double* rnorm;   // [S]    norm(rep) (vecmath.hpp:35-40), cached bit-exactly
+  double* brep64;  // [S][d] pending-buffer running mean (index.cpp:177-190)
+  float* brep32;
+  double* bnorm;
+  double* var;     // [S]    running variance (Eq. 4)
+  int64_t* stat;   // [S]    stat_count
+  int64_t* nmem;   // [S]    members
+  int32_t* nbuf;   // [S]    buffered entries
+  uint8_t* lazy;   // [S]    lazy_split (== buffer registered)
+  uint8_t* resid;  // [S]    0 Device, 1 Host
+  int64_t* cid;    // [S]    cluster id (tie-break key)
+  int32_t* npages; // [S]
+  int32_t* pages;  // [S][maxp]
+  int32_t* nbpages;
+  int32_t* bpages; // [S][maxbp]
+  int32_t* pg_fill;     // [max_pages] rows used in each page
+  int32_t* free_stack;  // [max_pages]
+  int32_t* free_top;    // [1]
+  uint8_t* pool;        // page pool
+  // window ring (engine.cpp:54-65): W frame slots per domain, each ceil(tmax/P) pages
+  int32_t* ring_pages;  // [L][W][rpp]
+  int32_t* ring_owner;  // [L][W][tmax] owning slot of each window token (-1 none)
+  int32_t* ring_count;  // [W] tokens in the frame held by each ring slot (0 empty)
+  int32_t rpp;          // ring pages per frame slot
+  // visual partitions (index.hpp:52-58)
+  double* vrep;   // [max_parts][d]
+  double* vnorm;  // [max_parts]
+  int32_t* n_parts;  // [1]
+  // per (partition, domain) live-cluster slot lists (per_layer_clusters order)
+  int32_t* pl_off;   // [max_parts * L]
+  int32_t* pl_cnt;   // [max_parts * L]
+  int32_t* pl_pool;
+  int64_t pl_pool_cap;
+  // Eq. 5 threshold table tau[n] computed on the host with libm exp (maintainer.cpp:11-14)
+  double* tau_tab;
+  int32_t tau_len;
+  int32_t* err;  // [1] DevErr bits
+};
+
+inline __host__ __device__ uint8_t* page_k(const DevTables& t, int32_t page) {
+  return t.pool + static_cast<int64_t>(page) * t.page_bytes;
+}
+inline __host__ __device__ uint8_t* page_v(const DevTables& t, int32_t page) {
+  return t.pool + static_cast<int64_t>(page) * t.page_bytes +
+         static_cast<int64_t>(t.P) * t.d * t.es;
+}
+
+// ----------------------------------------------------------------------------- ingest
+struct IngestArgs {
+  int32_t T, pid, ring_slot, n_active;
+  const int32_t* active;   // [n_active] domains to run (device)
+  const int32_t* cursor;   // [L] first token to process per domain (device)
+  const void* fk;          // [L][tmax][d] frame keys (kv dtype)
+  const void* fv;
+  // candidate lists (built per launch)
+  int32_t* cand_n;         // [L]
+  int32_t* cand_slot;      // [L][cmax]
+  uint8_t* cand_buf;       // [L][cmax]
+  float* approx;           // [L][tmax][cmax] approximate cosines (K1)
+  float margin;            // certified bound on |approx - exact| (cosine units)
+  int32_t defer;           // MaintainerConfig::defer_host_splits
+  // outputs
+  int32_t* ev_kind;        // [L][tmax]
+  int32_t* ev_slot;        // [L][tmax]
+  int32_t* stop_t;         // [L] token index of the host event (T when done)
+  int32_t* stop_kind;      // [L]
+  int32_t* stop_slot;      // [L]
+  int32_t* n_exact;        // [L] exact re-scores performed (instrumentation)
+};
+
+// ----------------------------------------------------------------------------- decode
+struct DecodeArgs {
+  const float* q;          // [L][d]
+  int32_t k_v, k_s, prefetch_k, prefetch;
+  int32_t n_parts_host;    // partitions known to the host (== device count)
+  // outputs (device)
+  int32_t* parts;          // [L][k_v]    visual_topk partition ids
+  int32_t* n_parts_sel;    // [L]
+  int32_t* ranked_slot;    // [L][k_s]
+  uint8_t* ranked_buf;     // [L][k_s]
+  int32_t* n_ranked;       // [L]
+  int32_t* pf_slot;        // [L][prefetch_k] ranking of layer l+1 candidates with q_l
+  uint8_t* pf_buf;
+  int32_t* n_pf;           // [L]
+  int32_t* ver_slot;       // [L][k_s]    verified (dedup, rank order)
+  int32_t* n_ver;          // [L]
+  int64_t* attended;       // [L]        attended-set size (members+buffers of verified U window)
+  int32_t* n_cand;         // [L]        candidates compared (count_candidates)
+  // attention work list: item = (domain, kind, ref, first page, n pages)
+  int4* items;             // [L][max_items]
+  int32_t* n_items;        // [L]
+  int32_t max_items, chunk_pages;
+  // attention partials / output
+  float* part_ml;          // [L][max_items][2]
+  float* part_o;           // [L][max_items][d]
+  int32_t* dom_done;       // [L] completion counters (reset by the combine)
+  float* out;              // [L][d]
+  float scale_log2;        // log2(e) / sqrt(d)
+};
+
+// ----------------------------------------------------------------------------- launchers
+// Implemented in kernels.cu. All launch on `st`; each returns the number of kernel launches.
+int launch_build_cands(const DevTables& t, const IngestArgs& a, cudaStream_t st);
+int launch_approx(const DevTables& t, const IngestArgs& a, cudaStream_t st);
+int launch_resolve(const DevTables& t, const IngestArgs& a, cudaStream_t st);
+int launch_ring_write(const DevTables& t, const void* fk, const void* fv, int32_t T,
+                      int32_t ring_slot, cudaStream_t st);
+int launch_decode(const DevTables& t, const DecodeArgs& a, cudaStream_t st, cudaEvent_t* ev);
+
+// Slot initialisation from host-computed exact statistics: rep64 rows (rep, norm, var,
+// counts) uploaded by the host; this kernel fills the fp32 mirrors.
+int launch_refresh_mirror(const DevTables& t, const int32_t* slots, int32_t n, cudaStream_t st);
+
+// Appends staged rows (kv dtype, [rows][d] K and V) to slots: run r appends rows
+// idx[first .. first + n_rows) in order to the member (or buffer) pages of run.slot.
+// One warp per run (runs must name distinct slots).
+struct AppendRun {
+  int32_t slot, first_row, n_rows, to_buffer;
+};
+int launch_append_runs(const DevTables& t, const AppendRun* runs, int32_t n_runs,
+                       const int32_t* idx, const void* stage_k, const void* stage_v,
+                       cudaStream_t st);
+
+// Gathers a cluster's members (then its buffer) into staging rows [n][d] K and V.
+int launch_gather_cluster(const DevTables& t, int32_t slot, int32_t include_buffer,
+                          void* stage_k, void* stage_v, int64_t row0, cudaStream_t st);
+// Returns a slot's member and buffer pages to the free stack and clears its page lists.
+int launch_free_slot_pages(const DevTables& t, int32_t slot, cudaStream_t st);
+
+// Exact compute_representative / compute_variance (index.cpp:345-362) over staged rows
+// idx[first .. first+n) for each run; writes rep64/rep32/rnorm/var of run.slot.
+int launch_exact_stats(const DevTables& t, const AppendRun* runs, int32_t n_runs,
+                       const int32_t* idx, const void* stage_k, cudaStream_t st);
+
+// Flat top-k (oracle_flat_topk) of one query over an explicit candidate list.
+int launch_flat_topk(const DevTables& t, const float* q, const int32_t* slots,
+                     const uint8_t* bufs, int32_t n, int32_t k, int32_t* out_idx,
+                     cudaStream_t st);
+
+// Converts staged kv-dtype rows to fp32 (for host read-back).
+int launch_to_f32(const DevTables& t, const void* src, float* dst, int64_t n_elems,
+                  cudaStream_t st);
+
+}  // namespace kvc

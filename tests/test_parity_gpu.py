@@ -1,0 +1,122 @@
+"""GPU parity against the compiled reference (or golden fixtures) on the config-1 stream.
+
+Bar (BASELINE.json north_star): routed cluster ids, ranked / selected cluster-id lists and the
+attended-set digest bit-exact; attention within 1e-3 max relative error (normwise: max|out-ref|
+/ max|ref|, fp32 vs the fp64 restatement over the reference's attended set).
+"""
+import numpy as np
+import pytest
+
+from oracle import pyoracle as po
+from tests.harness import Replay
+
+pytestmark = pytest.mark.gpu
+
+ATT_TOL = 1e-3
+
+
+@pytest.fixture(scope="module")
+def stream1():
+    return po.gen_stream_restated(po.config1_stream())
+
+
+def _run(stream, ecfg, ref_lib_present=True, dev_kw=None, check_attention=True, max_events=None):
+    ref = po.RefDriver(ecfg, stream.d, stream.L, checks=False) if po.reference() is not None else None
+    r = Replay(stream, ecfg, ref, dev_kw).run(check_attention=check_attention, max_events=max_events)
+    r.final_compare()
+    return r
+
+
+def test_config1_full_stream(stream1, ref_lib):
+    """64 frames (16 build + 48 online with ~360 splits) and 32 queries, top-4."""
+    r = _run(stream1, po.config1_engine())
+    assert r.mismatches == [], r.mismatches[:5]
+    assert r.att_err < ATT_TOL, r.att_err
+
+
+def test_config1_bf16(stream1, ref_lib):
+    """Keys/values rounded to bf16 before either side sees them (SURVEY §7 hard part 5)."""
+    import torch
+
+    s = po.Stream(stream1.d, stream1.L, stream1.T, stream1.kinds, stream1.visual,
+                  torch.from_numpy(stream1.keys).bfloat16().float().numpy(),
+                  torch.from_numpy(stream1.values).bfloat16().float().numpy(), stream1.q, stream1.gt)
+    from paper_2604_10060_b200 import ClusterKVCache  # noqa: F401
+
+    ecfg = po.config1_engine()
+    ref = po.RefDriver(ecfg, s.d, s.L, checks=False)
+    from tests.harness import product_config
+    from paper_2604_10060_b200 import ClusterKVCache as KV
+
+    kv = KV(product_config(ecfg, kv_dtype=1), s.d, s.L)
+    kbf = torch.from_numpy(s.keys).bfloat16()
+    vbf = torch.from_numpy(s.values).bfloat16()
+    mism = []
+    for kind, i in s.events():
+        if kind == "frame":
+            kk = kbf[i].contiguous().view(torch.int16).numpy()
+            vv = vbf[i].contiguous().view(torch.int16).numpy()
+            pid, asg = kv.process_frame(i, s.visual[i], kk, vv)
+            rpid, rasg = ref.frame(i, s.visual[i], s.keys[i], s.values[i])
+            if pid != rpid or not np.array_equal(asg, rasg):
+                mism.append(("frame", i))
+        else:
+            kv.query(i, s.q[i], gt=s.gt[i])
+            ref.query(i, s.q[i], s.gt[i])
+            for l in range(s.L):
+                if kv.ranked(l) != ref.ranked(l) or kv.selected(l) != ref.selected(l):
+                    mism.append(("query", i, l))
+            if kv.digest() != ref.digest():
+                mism.append(("digest", i))
+    assert mism == [], mism[:5]
+
+
+def test_decode_only_config1b(ref_lib):
+    """Config 1b: build over all 64 frames (4 partitions x 4 clusters), k_v = 4, k_s = 4."""
+    s = po.gen_stream_restated(po.config1_stream())
+    ecfg = po.config1_engine(build_batch_frames=64, target_semantic_cluster_size=784, k_v=4, k_s=4)
+    r = _run(s, ecfg)
+    assert r.mismatches == [], r.mismatches[:5]
+    assert r.att_err < ATT_TOL
+
+
+def test_flat_topk_matches_reference(stream1, ref_lib):
+    ecfg = po.config1_engine()
+    ref = po.RefDriver(ecfg, stream1.d, stream1.L, checks=False)
+    r = Replay(stream1, ecfg, ref)
+    n = 0
+    for kind, i in stream1.events():
+        if kind != "frame":
+            continue
+        r.frame(i)
+        n += 1
+        if n in (16, 30, 64):
+            for l in range(stream1.L):
+                for k in (1, 4, 1000):
+                    q = stream1.q[(n + l) % len(stream1.q), l]
+                    assert r.kv.flat_topk(q, l, k) == ref.flat_topk(q, l, k)
+    assert r.mismatches == []
+
+
+def test_eager_policy(ref_lib):
+    """defer_host_splits = false: eager fetch + split, domains resolved one at a time."""
+    s = po.gen_stream_restated(po.StreamCfg.make(n_scenes=3, frames_per_scene=12, tokens_per_frame=32,
+                                                 d=32, L=3, n_queries=6, semantic_noise=0.05, seed=5))
+    ecfg = po.EngineCfg.make(build_batch_frames=8, defer_host_splits=0, offload_horizon_frames=2)
+    r = _run(s, ecfg)
+    assert r.mismatches == [], r.mismatches[:5]
+    assert r.att_err < ATT_TOL
+
+
+def test_deferred_and_prefetch_drift(ref_lib):
+    """Drift preset (workload.cpp:337-346) scaled down: deferred splits, buffers, settles, prefetch."""
+    s = po.gen_stream_restated(po.StreamCfg.make(n_scenes=6, frames_per_scene=16, tokens_per_frame=16,
+                                                 d=32, L=4, scene_cycle=2, drift_rate=0.06,
+                                                 semantic_noise=0.05, n_queries=12, seed=7))
+    ecfg = po.EngineCfg.make(build_batch_frames=8, offload_horizon_frames=4, prefetch_enabled=1,
+                             device_capacity_entries=1500)
+    r = _run(s, ecfg)
+    assert r.mismatches == [], r.mismatches[:5]
+    st = r.kv.maint_stats()
+    assert st[3] > 0, "stream must exercise the deferred path"
+    assert r.att_err < ATT_TOL
