@@ -1,0 +1,364 @@
+#!/usr/bin/env python
+"""bench.py -- decode-step retrieve+attend latency and frame-ingest rate (BASELINE.json metric).
+
+Workload (config 2): LLaVA-OneVision-7B-shaped KV -- 28 layers x 4 KV heads =
+112 clustering domains, d = 128, bf16, a 128K-token stream (669 frames x 196 tokens = 131,124
+tokens per domain) held as 256 clusters per domain, top-16 cluster retrieval (k_v = 1) plus the
+4-frame local window. Synthetic data generated on the GPU (paper_2604_10060_b200/workload.py);
+the pre-clustered state is installed through the bulk add_cluster path, then `--frames` new
+frames are ingested online (timed: frames/s) and `--steps` decode steps are timed.
+
+One JSON line on rank 0. `value` = decode µs/step (lower is better) measured with CUDA events on
+the context stream, inputs resident in HBM; `e2e` = the same through the public API with host
+query / host output (H2D + D2H inside the timed region). Per-step working set (~530 MB of
+selected K/V) exceeds the 126 MB L2 and every step uses a different query (different clusters),
+so no L2 flush is needed ("inputs larger than L2").
+
+--gpus N (torchrun): the 112 domains are sharded across ranks by (layer, KV head); each step ends
+with an NCCL all-gather of the per-domain outputs; time = max over ranks (strong scaling).
+--impl reference: the reference's own CPU path (oracle/_ref, compiled from the unmodified
+reference sources) on the host cores, on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "decode-step retrieve+attend µs @128K-token KV; frame ingest frames/s"
+D_TOTAL, HEAD_DIM, N_TOK, N_CLUST, T_FRAME, TOP_K, WINDOW = 112, 128, 669 * 196, 256, 196, 16, 4
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--frames", type=int, default=0, help="timed ingest frames (default = steps)")
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--domains", type=int, default=D_TOTAL)
+    return p.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            m = json.load(f)
+        return float(m["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampler for the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=6)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 5 + i and r[5 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def traffic_from_profiles():
+    """dram bytes per attention launch from the committed ncu --set full summary, if any."""
+    path = os.path.join(ROOT, "profiles", "ncu_attend_summary.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+# --------------------------------------------------------------------------- reference arm
+
+def run_reference(args, rank: int):
+    if rank != 0:
+        return
+    from oracle import pyoracle as po
+
+    if po.reference() is None:
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libkvclust_ref.so not built"}))
+        return
+    threads = os.cpu_count() or 1
+    dom_sample = 2  # domains per reference instance (each instance ~300 MB of KVEntry)
+    st = _host_sample(dom_sample)
+    q = _host_queries(st, args.warmup + args.steps)
+    us, mean = po.time_reference(0, threads, st["keys"], st["values"], st["assign"], N_CLUST,
+                                 args.warmup, args.steps, TOP_K, WINDOW * T_FRAME, queries=q)
+    # `threads` instances ran concurrently, each over dom_sample domains
+    scale = D_TOTAL / (dom_sample * threads)
+    per_step = us * scale
+    sample = (f"{threads} concurrent reference instances x {dom_sample} domains (N={N_TOK}, C={N_CLUST}, "
+              f"top-{TOP_K} + {WINDOW}-frame window): retrieve() + fp64 attention over the attended set; "
+              f"wall us/step scaled by {D_TOTAL}/({dom_sample}x{threads})")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(per_step, 3), "unit": "us/step",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_step / 1e3,
+        "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": _config(args, 1),
+        "cpu_baseline": {"value": round(per_step, 3), "unit": "us/step", "cores": threads,
+                         "kind": "reference", "sample": sample},
+        "e2e": {"value": round(per_step, 3), "unit": "us/step", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def _host_sample(dom: int, seed: int = 42):
+    """A bounded host copy of the workload: `dom` domains of the config-2 state (f32)."""
+    import torch
+    from paper_2604_10060_b200 import workload
+
+    dev = "cuda" if torch.cuda.is_available() else "cpu"
+    st = workload.clustered_state(dom, N_TOK, N_CLUST, HEAD_DIM, T_FRAME, seed=seed, device=dev)
+    return {"keys": st.keys.float().cpu().numpy(), "values": st.values.float().cpu().numpy(),
+            "assign": st.assign, "state": st}
+
+
+def _host_queries(h, n):
+    from paper_2604_10060_b200 import workload
+
+    return workload.queries_near(h["state"], n).cpu().numpy()
+
+
+def _config(args, world):
+    return {"workload": "config2: LLaVA-OV-7B KV (28 layers x 4 KV heads = 112 domains), d=128, bf16, "
+                        "131,124-token stream/domain, 256 clusters/domain, top-16 + 4-frame window",
+            "domains": D_TOTAL, "tokens_per_domain": N_TOK, "clusters_per_domain": N_CLUST,
+            "top_k": TOP_K, "window_frames": WINDOW, "head_dim": HEAD_DIM, "kv_dtype": "bf16",
+            "parallelism": f"domain-shard{world}" if world > 1 else "single",
+            "l2": "per-step working set > L2 (no flush)"}
+
+
+# --------------------------------------------------------------------------- our arm
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2604_10060_b200 import ClusterKVCache, Config, DTYPE_BF16, workload
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    D = args.domains // world  # strong scaling over (layer, head) domains
+    frames_t = args.frames or args.steps
+
+    cfg = Config.make(kv_dtype=DTYPE_BF16, k_v=1, k_s=TOP_K, window_frames=WINDOW, build_batch_frames=1,
+                      offload_horizon_frames=1 << 30, device_capacity_entries=1 << 40,
+                      pool_bytes=int(1.25 * D * (N_TOK + 64 * N_CLUST + 400 * T_FRAME) * HEAD_DIM * 4),
+                      max_slots=max(4096, 4 * D * N_CLUST), max_cluster_pages=512, max_tokens=T_FRAME)
+    kv = ClusterKVCache(cfg, HEAD_DIM, D)
+    st = workload.clustered_state(D, N_TOK, N_CLUST, HEAD_DIM, T_FRAME, seed=42 + rank)
+    t0 = time.time()
+    kv.bulk_load(st.visual, st.keys, st.values, st.assign, st.frame_ids, st.token_ids, N_CLUST)
+    load_s = time.time() - t0
+    del st.keys, st.values
+    torch.cuda.empty_cache()
+    stream = torch.cuda.ExternalStream(kv.stream)
+
+    # ------------------------------------------------------------------ ingest (frames/s)
+    nf = args.warmup + frames_t
+    fk, fv, fvis, fids = workload.frames_near(st, nf, N_TOK // T_FRAME + 1)
+    fk_h = fk[args.warmup:].cpu().pin_memory()
+    fv_h = fv[args.warmup:].cpu().pin_memory()
+    for i in range(args.warmup):
+        kv.process_frame(int(fids[i]), fvis[i], fk[i], fv[i])
+    splits0 = kv.maint_stats()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = kv.launch_count()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    with Clocks(local) as clk_ingest:
+        ev0.record(stream)
+        for i in range(args.warmup, nf):
+            kv.process_frame(int(fids[i]), fvis[i], fk[i], fv[i], want_assigned=False)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    ingest_ms = ev0.elapsed_time(ev1)
+    ingest_launches = kv.launch_count() - launches0
+    splits = (kv.maint_stats() - splits0).tolist()
+    # e2e ingest: frames from pinned host memory through the public API
+    more_k, more_v, more_vis, more_ids = workload.frames_near(st, frames_t, int(fids[-1]) + 1, seed=99)
+    mk_h = more_k.cpu().pin_memory().numpy().view(np.int16)
+    mv_h = more_v.cpu().pin_memory().numpy().view(np.int16)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for i in range(frames_t):
+        kv.process_frame(int(more_ids[i]), more_vis[i], mk_h[i], mv_h[i], want_assigned=False)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ingest_e2e_ms = e0.elapsed_time(e1)
+    del fk, fv, fk_h, fv_h, more_k, more_v
+
+    # ------------------------------------------------------------------ decode (us/step)
+    nq = args.warmup + args.steps
+    q_dev = workload.queries_near(st, nq, seed=11 + rank)
+    out_dev = torch.zeros(D, HEAD_DIM, device="cuda")
+    gathered = torch.zeros(world * D, HEAD_DIM, device="cuda") if world > 1 else None
+    for i in range(args.warmup):
+        kv.query(i, q_dev[i], out=out_dev)
+    kv.set_timing(True)
+    att_us, k4_us, att_bytes_l = [], [], []
+    launches0 = kv.launch_count()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    with Clocks(local) as clk:
+        with torch.cuda.stream(stream):
+            ev0.record(stream)
+            for i in range(args.warmup, nq):
+                kv.query(i, q_dev[i], out=out_dev)
+                tm = kv.step_timing()
+                k4_us.append(tm[0])
+                att_us.append(tm[1])
+                att_bytes_l.append(tm[4])
+                if world > 1:
+                    dist.all_gather_into_tensor(gathered, out_dev)
+            ev1.record(stream)
+        torch.cuda.synchronize()
+    decode_ms = ev0.elapsed_time(ev1)
+    decode_launches = kv.launch_count() - launches0
+    kv.set_timing(False)
+    # e2e decode: host query in, host output out, through the public API
+    q_host = q_dev.cpu().numpy()
+    out_host = np.zeros((D, HEAD_DIM), np.float32)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for i in range(args.warmup, nq):
+        kv.query(i, q_host[i], out=out_host)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    decode_e2e_ms = e0.elapsed_time(e1)
+
+    # max over ranks
+    vals = torch.tensor([decode_ms, decode_e2e_ms, ingest_ms, ingest_e2e_ms], device="cuda", dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(vals, op=dist.ReduceOp.MAX)
+    decode_ms, decode_e2e_ms, ingest_ms, ingest_e2e_ms = vals.tolist()
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    us_step = decode_ms * 1e3 / args.steps
+    hbm, src = peaks()
+    # algorithmic bytes of the attention launch: attended tokens x (K + V) x bf16
+    att_bytes = float(np.mean(att_bytes_l))
+    att_time = float(np.mean(att_us)) * 1e-6
+    achieved = att_bytes / att_time / 1e9
+    step_bytes = att_bytes + D * N_CLUST * HEAD_DIM * 8 + D * HEAD_DIM * 8  # + fp64 centroids + q/out
+    line = {
+        "metric": METRIC, "value": round(us_step, 3), "unit": "us/step", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": us_step / 1e3,
+        "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (GPU generator, reference distributions)", "config": _config(args, world),
+        "e2e": {"value": round(decode_e2e_ms * 1e3 / args.steps, 3), "unit": "us/step",
+                "h2d_bytes_per_step": D * world * HEAD_DIM * 4, "d2h_bytes_per_step": D * world * HEAD_DIM * 4},
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
+                     "frac": round(achieved / hbm, 4), "traffic": traffic_from_profiles(),
+                     "kernel": "k_attend (split-KV attention over selected clusters + window)",
+                     "peak_source": src, "algorithmic_bytes_per_launch": att_bytes,
+                     "kernel_us": round(att_time * 1e6, 2),
+                     "step_bytes": step_bytes, "step_frac": round(step_bytes / (us_step * 1e-6) / 1e9 / hbm, 4),
+                     "score_select_us": round(float(np.mean(k4_us)), 2)},
+        "gpu_launches": int(decode_launches),
+        "clocks": clk.summary(),
+        "ingest": {"value": round(frames_t / (ingest_ms * 1e-3), 1), "unit": "frames/s",
+                   "frames": frames_t, "domains_per_frame": D * world, "tokens_per_frame": T_FRAME,
+                   "e2e": {"value": round(frames_t / (ingest_e2e_ms * 1e-3), 1), "unit": "frames/s",
+                           "h2d_bytes_per_step": D * T_FRAME * HEAD_DIM * 2 * 2, "d2h_bytes_per_step": 0},
+                   "gpu_launches": int(ingest_launches),
+                   "maint_delta": dict(zip(["inserts", "absorbed", "immediate_splits", "deferred_marks",
+                                            "settled_splits", "split_ops", "host_over", "maint_fetches",
+                                            "partitions_opened"], splits)),
+                   "clocks": clk_ingest.summary()},
+        "bulk_load_s": round(load_s, 2),
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(args)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def cpu_baseline(args):
+    """The reference hot path on the host, single thread, bounded sample (1 domain)."""
+    try:
+        from oracle import pyoracle as po
+
+        if po.reference() is None:
+            return {"value": None, "unit": "us/step", "cores": 0, "kind": "reference",
+                    "sample": "oracle/_ref not built"}
+        dom = 1
+        h = _host_sample(dom, seed=7)
+        q = _host_queries(h, 3)
+        us, _ = po.time_reference(0, 1, h["keys"], h["values"], h["assign"], N_CLUST, 1, 2, TOP_K,
+                                  WINDOW * T_FRAME, queries=q)
+        return {"value": round(us * D_TOTAL / dom, 1), "unit": "us/step", "cores": 1, "kind": "reference",
+                "sample": f"1 domain (N={N_TOK}, C={N_CLUST}, top-{TOP_K}+window), 2 timed steps of retrieve() + "
+                          f"fp64 attention, single thread, scaled x{D_TOTAL}"}
+    except Exception as e:  # the baseline must not break the GPU line
+        return {"value": None, "unit": "us/step", "cores": 0, "kind": "reference", "sample": f"failed: {e}"}
+
+
+if __name__ == "__main__":
+    main()

@@ -141,6 +141,9 @@ def reference():
                                         C.c_uint64, i32p, f64p, C.POINTER(C.c_int)]
         lib.ref_time_decode.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, f32p, f32p, i32p, f32p,
                                         C.c_int, C.c_int, C.c_int, f64p]
+        lib.ref_time_mt.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, f32p, f32p,
+                                    i32p, f32p, C.c_int, C.c_int, C.c_int, C.c_int, f32p, f32p,
+                                    f32p, C.c_int, f64p]
         _ref = lib
     return _ref
 
@@ -466,3 +469,28 @@ def attended_digest(per_layer):
             h = fnv(h, f)
             h = fnv(h, t)
     return h
+
+
+def time_reference(mode: int, threads: int, keys: np.ndarray, values: np.ndarray, assign: np.ndarray,
+                   C_: int, warmup: int, steps: int, k_s: int = 16, window_tokens: int = 784,
+                   queries: np.ndarray | None = None, fvis=None, fkeys=None, fvals=None):
+    """CPU timing of the reference hot path (ref_shim.cpp ref_time_mt). keys/values [L, N, d] f32.
+    Returns (max-over-threads us/step, mean us/step)."""
+    lib = reference()
+    assert lib is not None
+    L, N, d = keys.shape
+    k = np.ascontiguousarray(keys, np.float32)
+    v = np.ascontiguousarray(values, np.float32)
+    a = np.ascontiguousarray(assign, np.int32)
+    q = np.ascontiguousarray(queries if queries is not None else np.zeros((warmup + steps, L, d)), np.float32)
+    T = 0 if fkeys is None else fkeys.shape[2]
+    fv_ = np.ascontiguousarray(fvis if fvis is not None else np.zeros((1, d)), np.float32)
+    fk = np.ascontiguousarray(fkeys if fkeys is not None else np.zeros((1, d)), np.float32)
+    fvv = np.ascontiguousarray(fvals if fvals is not None else np.zeros((1, d)), np.float32)
+    out = np.zeros(2)
+    rc = lib.ref_time_mt(mode, threads, d, L, N, C_, _p(k, f32p), _p(v, f32p), _p(a, i32p), _p(q, f32p),
+                         warmup, steps, k_s, window_tokens, _p(fv_, f32p), _p(fk, f32p), _p(fvv, f32p), T,
+                         _p(out, f64p))
+    if rc != 0:
+        raise RuntimeError(lib.ref_last_error().decode())
+    return float(out[0]), float(out[1])

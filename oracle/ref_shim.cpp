@@ -31,6 +31,7 @@
 #include <optional>
 #include <set>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "kvclust/clustering.hpp"
@@ -972,6 +973,145 @@ int ref_time_decode(int d, int L, int N, int C, const float* keys, const float* 
   t[0] = t_ret / steps;
   t[1] = t_att / steps;
   t[2] = sink;
+  GUARD_END
+}
+
+// Multi-threaded CPU baseline: `threads` independent reference instances,
+// each over the same `L`-domain sample (state built with add_cluster as in ref_time_decode),
+// run concurrently. mode 0: `steps` retrieve() + fp64 attention per instance (queries
+// [steps][L][d]); mode 1: place_frame + on_insert for `steps` frames per instance (frames:
+// visual [steps][d], keys/values [steps][L][T][d]). out[0] = wall microseconds per step
+// (max over threads), out[1] = mean per-thread microseconds per step.
+int ref_time_mt(int mode, int threads, int d, int L, int N, int C, const float* keys,
+                const float* values, const std::int32_t* assign, const float* queries, int warmup,
+                int steps, int k_s, int window_tokens, const float* fvis, const float* fkeys,
+                const float* fvals, int T, double* out) {
+  GUARD_BEGIN
+  std::vector<double> per(static_cast<std::size_t>(threads), 0.0);
+  std::vector<std::string> errs(static_cast<std::size_t>(threads));
+  auto worker = [&](int ti) {
+    try {
+      HierIndex index(d, L);
+      Embedding vis(static_cast<std::size_t>(d), 0.0f);
+      if (fvis) vis.assign(fvis, fvis + d); else vis[0] = 1.0f;
+      std::int64_t pid = index.add_partition(0, vis);
+      const int TT = 196;
+      for (int l = 0; l < L; ++l) {
+        std::vector<std::vector<KVEntry>> groups(static_cast<std::size_t>(C));
+        for (int i = 0; i < N; ++i) {
+          KVEntry e;
+          std::size_t off = (static_cast<std::size_t>(l) * N + i) * d;
+          e.key.assign(keys + off, keys + off + d);
+          e.value.assign(values + off, values + off + d);
+          e.frame_id = i / TT;
+          e.layer_id = l;
+          e.token_id = i % TT;
+          groups[static_cast<std::size_t>(assign[static_cast<std::size_t>(l) * N + i])].push_back(std::move(e));
+        }
+        for (auto& g : groups) {
+          if (g.empty()) continue;
+          ClusterRecord rec;
+          rec.layer_id = l;
+          rec.visual_parent = pid;
+          rec.rep = compute_representative(g);
+          rec.variance = compute_variance(g, rec.rep);
+          rec.stat_count = static_cast<std::int64_t>(g.size());
+          rec.members = std::move(g);
+          index.add_cluster(std::move(rec));
+        }
+      }
+      CostModel cost;
+      cost.device_capacity_entries = static_cast<std::int64_t>(L) * (N + (warmup + steps) * T + 1) + 1;
+      TieredStore store(index, cost);
+      MaintainerConfig mc;
+      Maintainer maint(index, store, mc);
+      RetrievalConfig rc;
+      rc.k_v = 1;
+      rc.k_s = k_s;
+      std::vector<KVEntry> window;
+      for (int l = 0; l < L; ++l)
+        for (int i = N - window_tokens; i < N; ++i) {
+          KVEntry e;
+          std::size_t off = (static_cast<std::size_t>(l) * N + i) * d;
+          e.key.assign(keys + off, keys + off + d);
+          e.value.assign(values + off, values + off + d);
+          e.frame_id = i / TT;
+          e.layer_id = l;
+          e.token_id = i % TT;
+          window.push_back(std::move(e));
+        }
+      double sink = 0.0;
+      auto t0 = std::chrono::steady_clock::now();
+      for (int s = 0; s < warmup + steps; ++s) {
+        if (s == warmup) t0 = std::chrono::steady_clock::now();
+        if (mode == 0) {
+          QueryBundle b;
+          for (int l = 0; l < L; ++l) {
+            const float* q = queries + (static_cast<std::size_t>(s) * L + l) * d;
+            b.q.emplace_back(q, q + d);
+          }
+          RetrievalResult r = retrieve(b, rc, index, store, maint, window);
+          for (int l = 0; l < L; ++l) {  // fp64 attention restatement over the attended set
+            const auto& att = r.layers[static_cast<std::size_t>(l)].attended_tokens;
+            const float* q = queries + (static_cast<std::size_t>(s) * L + l) * d;
+            const double scale = 1.0 / std::sqrt(static_cast<double>(d));
+            std::vector<double> sc(att.size());
+            double mx = -1e300;
+            for (std::size_t j = 0; j < att.size(); ++j) {
+              std::size_t i = static_cast<std::size_t>(att[j].first) * TT + static_cast<std::size_t>(att[j].second);
+              const float* k = keys + (static_cast<std::size_t>(l) * N + i) * d;
+              double acc = 0.0;
+              for (int c = 0; c < d; ++c) acc += static_cast<double>(q[c]) * k[c];
+              sc[j] = acc * scale;
+              mx = std::max(mx, sc[j]);
+            }
+            std::vector<double> o(static_cast<std::size_t>(d), 0.0);
+            double den = 0.0;
+            for (std::size_t j = 0; j < att.size(); ++j) {
+              std::size_t i = static_cast<std::size_t>(att[j].first) * TT + static_cast<std::size_t>(att[j].second);
+              const float* v = values + (static_cast<std::size_t>(l) * N + i) * d;
+              double w = std::exp(sc[j] - mx);
+              den += w;
+              for (int c = 0; c < d; ++c) o[static_cast<std::size_t>(c)] += w * v[c];
+            }
+            sink += o[0] / den;
+          }
+        } else {
+          const std::int64_t fid = 1000000 + s;
+          Embedding fv(fvis + static_cast<std::size_t>(s) * d, fvis + static_cast<std::size_t>(s + 1) * d);
+          std::int64_t p = maint.place_frame(fid, fv);
+          for (int l = 0; l < L; ++l)
+            for (int t = 0; t < T; ++t) {
+              KVEntry e;
+              std::size_t off = ((static_cast<std::size_t>(s) * L + l) * T + t) * d;
+              e.key.assign(fkeys + off, fkeys + off + d);
+              e.value.assign(fvals + off, fvals + off + d);
+              e.frame_id = fid;
+              e.layer_id = l;
+              e.token_id = t;
+              maint.on_insert(p, e);
+            }
+        }
+      }
+      auto t1 = std::chrono::steady_clock::now();
+      per[static_cast<std::size_t>(ti)] = std::chrono::duration<double, std::micro>(t1 - t0).count() / steps;
+      if (sink == 12345.678) per[static_cast<std::size_t>(ti)] += 0.0;
+    } catch (const std::exception& e) {
+      errs[static_cast<std::size_t>(ti)] = e.what();
+    }
+  };
+  std::vector<std::thread> pool;
+  for (int i = 0; i < threads; ++i) pool.emplace_back(worker, i);
+  for (auto& th : pool) th.join();
+  for (const auto& e : errs)
+    if (!e.empty()) throw Error(e);
+  double mx = 0.0, mean = 0.0;
+  for (double v : per) {
+    mx = std::max(mx, v);
+    mean += v / threads;
+  }
+  out[0] = mx;
+  out[1] = mean;
   GUARD_END
 }
 

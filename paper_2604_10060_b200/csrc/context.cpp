@@ -97,6 +97,14 @@ void* Context::dalloc(std::size_t bytes) {
   return p;
 }
 
+void* Context::dalloc_scratch(std::size_t bytes) {
+  if (bytes > scratch_cap_) {
+    scratch_cap_ = std::max(bytes, scratch_cap_ * 2);
+    scratch_ = dalloc(scratch_cap_);
+  }
+  return scratch_;
+}
+
 void* Context::halloc(std::size_t bytes) {
   void* p = nullptr;
   KVC_CUDA(cudaMallocHost(&p, std::max<std::size_t>(bytes, 16)));

@@ -122,6 +122,9 @@ class Context {
   std::vector<void*> dev_allocs_;
   void* dalloc(std::size_t bytes);
   void* halloc(std::size_t bytes);  // pinned
+  void* dalloc_scratch(std::size_t bytes);  // reusable device scratch (grows)
+  void* scratch_ = nullptr;
+  std::size_t scratch_cap_ = 0;
   std::vector<void*> host_allocs_;
   // frame input + staging
   void* d_fk_ = nullptr;

@@ -79,6 +79,11 @@ void Context::decode_step(std::int64_t qid, const float* q, int q_mem, float* ou
   const auto* h_nc = reinterpret_cast<const std::int32_t*>(hp(da_.n_cand));
   (void)h_parts;
   (void)h_nps;
+  {  // algorithmic bytes of the attention launch: attended tokens x (K + V)
+    std::int64_t tok = 0;
+    for (int l = 0; l < L_; ++l) tok += h_att[l];
+    step_t_[4] = static_cast<double>(tok) * 2.0 * d_ * es_;
+  }
 
   // Translate every layer's slots to ids before any settle frees / reuses a slot.
   std::vector<std::vector<std::pair<std::int64_t, int>>> ranked(static_cast<std::size_t>(L_)), pf(static_cast<std::size_t>(L_));
@@ -247,19 +252,15 @@ std::int64_t Context::bulk_load(const float* visual, const void* keys, const voi
       cids.push_back(id);
       new_ids.push_back(id);
     }
-    // headers (counts / ids / residence); statistics are computed exactly on the device
-    for (std::size_t i = 0; i < slots.size(); ++i) {
-      const Cluster& cl = C(cids[i]);
-      const std::int64_t n = static_cast<std::int64_t>(cl.members.size());
-      const std::int64_t s = slots[i];
-      std::int32_t zero = 0;
-      std::uint8_t z8 = 0;
-      KVC_CUDA(cudaMemcpyAsync(t_.stat + s, &n, 8, cudaMemcpyHostToDevice, st_));
-      KVC_CUDA(cudaMemcpyAsync(t_.nmem + s, &n, 8, cudaMemcpyHostToDevice, st_));
-      KVC_CUDA(cudaMemcpyAsync(t_.cid + s, &cids[i], 8, cudaMemcpyHostToDevice, st_));
-      KVC_CUDA(cudaMemcpyAsync(t_.nbuf + s, &zero, 4, cudaMemcpyHostToDevice, st_));
-      KVC_CUDA(cudaMemcpyAsync(t_.lazy + s, &z8, 1, cudaMemcpyHostToDevice, st_));
-      KVC_CUDA(cudaMemcpyAsync(t_.resid + s, &z8, 1, cudaMemcpyHostToDevice, st_));
+    // headers (counts / ids / residence) in one batch; statistics are computed exactly on the
+    // device from the staged rows
+    {
+      std::vector<SlotHeader> hd(slots.size());
+      for (std::size_t i = 0; i < slots.size(); ++i)
+        hd[i] = SlotHeader{slots[i], 0, cids[i], static_cast<std::int64_t>(C(cids[i]).members.size())};
+      auto* dh = static_cast<SlotHeader*>(dalloc_scratch(hd.size() * sizeof(SlotHeader)));
+      KVC_CUDA(cudaMemcpyAsync(dh, hd.data(), hd.size() * sizeof(SlotHeader), cudaMemcpyHostToDevice, st_));
+      launches_ += launch_slot_headers(t_, dh, static_cast<std::int32_t>(hd.size()), st_);
       sync();
     }
     ensure_idx(N, static_cast<std::int64_t>(runs.size()));

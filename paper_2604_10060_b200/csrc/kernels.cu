@@ -590,6 +590,18 @@ __global__ void k_exact_stats(DevTables t, const AppendRun* runs, int n_runs, co
   }
 }
 
+__global__ void k_slot_headers(DevTables t, const SlotHeader* h, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const SlotHeader x = h[i];
+  t.stat[x.slot] = x.n;
+  t.nmem[x.slot] = x.n;
+  t.cid[x.slot] = x.cid;
+  t.nbuf[x.slot] = 0;
+  t.lazy[x.slot] = 0;
+  t.resid[x.slot] = 0;
+}
+
 __global__ void k_to_f32(const void* src, float* dst, int64_t n, int bf16) {
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x)
@@ -1251,6 +1263,12 @@ int launch_exact_stats(const DevTables& t, const AppendRun* runs, int32_t n_runs
   const int threads = 128;
   const size_t smem = static_cast<size_t>(t.d + threads) * 8;
   k_exact_stats<<<n_runs, threads, smem, st>>>(t, runs, n_runs, idx, sk);
+  return 1;
+}
+
+int launch_slot_headers(const DevTables& t, const SlotHeader* h, int32_t n, cudaStream_t st) {
+  if (n <= 0) return 0;
+  k_slot_headers<<<(n + 127) / 128, 128, 0, st>>>(t, h, n);
   return 1;
 }
 

@@ -199,6 +199,13 @@ int launch_flat_topk(const DevTables& t, const float* q, const int32_t* slots,
                      const uint8_t* bufs, int32_t n, int32_t k, int32_t* out_idx,
                      cudaStream_t st);
 
+// Fresh-slot headers for a batch of clusters: counts, ids, Device residence, no buffer.
+struct SlotHeader {
+  int32_t slot, pad;
+  int64_t cid, n;
+};
+int launch_slot_headers(const DevTables& t, const SlotHeader* h, int32_t n, cudaStream_t st);
+
 // Converts staged kv-dtype rows to fp32 (for host read-back).
 int launch_to_f32(const DevTables& t, const void* src, float* dst, int64_t n_elems,
                   cudaStream_t st);
