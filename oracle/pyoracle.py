@@ -484,12 +484,12 @@ def time_reference(mode: int, threads: int, keys: np.ndarray, values: np.ndarray
     a = np.ascontiguousarray(assign, np.int32)
     q = np.ascontiguousarray(queries if queries is not None else np.zeros((warmup + steps, L, d)), np.float32)
     T = 0 if fkeys is None else fkeys.shape[2]
-    fv_ = np.ascontiguousarray(fvis if fvis is not None else np.zeros((1, d)), np.float32)
+    fv_ = np.ascontiguousarray(fvis, np.float32) if fvis is not None else None
     fk = np.ascontiguousarray(fkeys if fkeys is not None else np.zeros((1, d)), np.float32)
     fvv = np.ascontiguousarray(fvals if fvals is not None else np.zeros((1, d)), np.float32)
     out = np.zeros(2)
     rc = lib.ref_time_mt(mode, threads, d, L, N, C_, _p(k, f32p), _p(v, f32p), _p(a, i32p), _p(q, f32p),
-                         warmup, steps, k_s, window_tokens, _p(fv_, f32p), _p(fk, f32p), _p(fvv, f32p), T,
+                         warmup, steps, k_s, window_tokens, _p(fv_, f32p) if fv_ is not None else None, _p(fk, f32p), _p(fvv, f32p), T,
                          _p(out, f64p))
     if rc != 0:
         raise RuntimeError(lib.ref_last_error().decode())

@@ -220,8 +220,9 @@ void Context::alloc_device() {
 
   // decode result block
   const int kv = cfg_.k_v, ks = cfg_.k_s, kp = cfg_.prefetch_k;
-  da_.max_items = 512;
-  da_.chunk_pages = 4;
+  da_.chunk_pages = 8;
+  da_.max_desc = 4096;
+  da_.max_items = da_.max_desc / da_.chunk_pages;
   std::size_t off = 0;
   auto carve = [&](std::size_t bytes) {
     std::size_t o = off;
@@ -248,7 +249,8 @@ void Context::alloc_device() {
   da_.n_ver = reinterpret_cast<std::int32_t*>(base + o_nv);
   da_.attended = reinterpret_cast<std::int64_t*>(base + o_att);
   da_.n_cand = reinterpret_cast<std::int32_t*>(base + o_nc);
-  da_.items = static_cast<int4*>(dalloc(L * da_.max_items * sizeof(int4)));
+  da_.desc = static_cast<int4*>(dalloc(L * da_.max_desc * sizeof(int4)));
+  da_.n_desc = static_cast<std::int32_t*>(dalloc(L * 4));
   da_.n_items = static_cast<std::int32_t*>(dalloc(L * 4));
   da_.part_ml = static_cast<float*>(dalloc(L * da_.max_items * 2 * 4));
   da_.part_o = static_cast<float*>(dalloc(L * da_.max_items * d * 4));

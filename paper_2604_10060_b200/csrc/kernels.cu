@@ -323,6 +323,7 @@ __global__ void __launch_bounds__(32) k_resolve(DevTables t, IngestArgs a) {
       const double* rp = (ib ? t.brep64 : t.rep64) + static_cast<int64_t>(s) * d;
       const double nr = ib ? t.bnorm[s] : t.rnorm[s];
       double acc = 0.0;
+#pragma unroll 16
       for (int i = 0; i < d; ++i) acc = dadd(acc, dmul(static_cast<double>(keyf[i]), rp[i]));
       const double cs = clamp1(ddiv(acc, dmul(nkt, nr)));
       relsim[r] = cs;
@@ -656,6 +657,7 @@ __device__ __forceinline__ double exact_cos(const float* q, double nq, const dou
     return -2.0;
   }
   double acc = 0.0;
+#pragma unroll 16
   for (int i = 0; i < d; ++i) acc = dadd(acc, dmul(static_cast<double>(q[i]), row[i]));
   return clamp1(ddiv(acc, dmul(nq, nr)));
 }
@@ -802,7 +804,9 @@ __global__ void __launch_bounds__(256) k_score_select(DevTables t, DecodeArgs a,
   if (passes == 1 && threadIdx.x == 0) a.n_pf[l] = 0;
   if (degen && threadIdx.x == 0) set_err(t, DERR_DEGENERATE);
 
-  // ---- verified (dedup in rank order, retrieval.cpp:20-26) + attended count + work list
+  // ---- verified (dedup in rank order, retrieval.cpp:20-26), attended count, page descriptors
+  __shared__ int vnp[64], vnbp[64], voff[65];
+  __shared__ int ring_cnt[64], ring_off[65];
   if (threadIdx.x == 0) {
     int nv = 0;
     for (int i = 0; i < a.n_ranked[l]; ++i) {
@@ -812,30 +816,21 @@ __global__ void __launch_bounds__(256) k_score_select(DevTables t, DecodeArgs a,
       if (!dup) vers[nv++] = s;
     }
     nver_s = nv;
-    unsigned long long att = 0;
-    int ni = 0;
-    int4* items = a.items + static_cast<int64_t>(l) * a.max_items;
-    for (int j = 0; j < nv; ++j) {
-      const int s = vers[j];
-      a.ver_slot[l * a.k_s + j] = s;
-      att += static_cast<unsigned long long>(t.nmem[s] + t.nbuf[s]);
-      const int np = t.npages[s], nbp = t.nbpages[s];
-      for (int f = 0; f < np; f += a.chunk_pages)
-        if (ni < a.max_items) items[ni++] = make_int4(0, s, f, min(a.chunk_pages, np - f));
-      for (int f = 0; f < nbp; f += a.chunk_pages)
-        if (ni < a.max_items) items[ni++] = make_int4(1, s, f, min(a.chunk_pages, nbp - f));
-    }
     a.n_ver[l] = nv;
-    att_s = att;
-    red_i[0] = ni;
   }
   __syncthreads();
-  // window ring: unmasked tokens per (ring slot, page)
-  __shared__ int ring_cnt[64];
-  const int W = t.W, rpp = t.rpp;
-  for (int i = threadIdx.x; i < W * rpp && i < 64; i += blockDim.x) ring_cnt[i] = 0;
-  __syncthreads();
   const int nv = nver_s;
+  const int W = t.W, rpp = t.rpp;
+  if (threadIdx.x < nv) {  // per verified cluster: counts (parallel global loads)
+    const int s = vers[threadIdx.x];
+    a.ver_slot[l * a.k_s + threadIdx.x] = s;
+    vnp[threadIdx.x] = t.npages[s];
+    vnbp[threadIdx.x] = t.nbpages[s];
+    atomicAdd(&att_s, static_cast<unsigned long long>(t.nmem[s] + t.nbuf[s]));
+  }
+  if (threadIdx.x < 64) ring_cnt[threadIdx.x] = 0;
+  __syncthreads();
+  // window ring: tokens whose owner is not a verified cluster (retrieval.cpp:107-108 dedup)
   for (int i = threadIdx.x; i < W * t.tmax; i += blockDim.x) {
     const int rs = i / t.tmax, tt = i % t.tmax;
     if (tt >= t.ring_count[rs]) continue;
@@ -849,23 +844,47 @@ __global__ void __launch_bounds__(256) k_score_select(DevTables t, DecodeArgs a,
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    int ni = red_i[0];
-    int4* items = a.items + static_cast<int64_t>(l) * a.max_items;
-    for (int i = 0; i < W * rpp && i < 64; ++i)
-      if (ring_cnt[i] > 0) {
-        if (ni < a.max_items)
-          items[ni++] = make_int4(2, i / rpp, i % rpp, 1);
-        else
-          set_err(t, DERR_ITEMS);
-      }
-    a.n_items[l] = ni;
+    int o = 0;
+    for (int j = 0; j < nv; ++j) {
+      voff[j] = o;
+      o += vnp[j] + vnbp[j];
+    }
+    voff[nv] = o;
+    for (int i = 0; i < W * rpp && i < 64; ++i) {
+      ring_off[i] = o;
+      o += ring_cnt[i] > 0 ? 1 : 0;
+    }
+    ring_off[min(W * rpp, 64)] = o;
+    if (o > a.max_desc) {
+      set_err(t, DERR_ITEMS);
+      o = a.max_desc;
+    }
+    a.n_desc[l] = o;
+    a.n_items[l] = (o + a.chunk_pages - 1) / a.chunk_pages;
     a.attended[l] = static_cast<int64_t>(att_s);
   }
-  if (a.n_items != nullptr) {
-    __syncthreads();
-    if (a.n_items[l] == 0)  // nothing attended: output zeros
-      for (int i = threadIdx.x; i < d; i += blockDim.x) a.out[static_cast<int64_t>(l) * d + i] = 0.f;
+  __syncthreads();
+  int4* desc = a.desc + static_cast<int64_t>(l) * a.max_desc;
+  const int ndesc = voff[nv];
+  for (int i = threadIdx.x; i < ndesc && i < a.max_desc; i += blockDim.x) {
+    int j = 0;
+    while (j + 1 < nv && voff[j + 1] <= i) ++j;
+    const int s = vers[j];
+    const int k = i - voff[j];
+    const bool isb = k >= vnp[j];
+    const int page = isb ? t.bpages[static_cast<int64_t>(s) * t.maxbp + (k - vnp[j])]
+                         : t.pages[static_cast<int64_t>(s) * t.maxp + k];
+    desc[i] = make_int4(page, t.pg_fill[page], isb ? 1 : 0, 0);
   }
+  for (int i = threadIdx.x; i < W * rpp && i < 64; i += blockDim.x)
+    if (ring_cnt[i] > 0 && ring_off[i] < a.max_desc) {
+      const int rs = i / rpp, j = i % rpp;
+      const int page = t.ring_pages[(static_cast<int64_t>(l) * W + rs) * rpp + j];
+      desc[ring_off[i]] = make_int4(page, t.pg_fill[page], 2 | (rs << 8), j * t.P);
+    }
+  __syncthreads();
+  if (a.n_items[l] == 0)  // nothing attended: output zeros
+    for (int i = threadIdx.x; i < d; i += blockDim.x) a.out[static_cast<int64_t>(l) * d + i] = 0.f;
 }
 
 // ============================================================================ K6
@@ -920,70 +939,66 @@ __global__ void __launch_bounds__(128) k_attend(DevTables t, DecodeArgs a, int* 
   __shared__ int last_flag;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int L = t.L;
+  const int L = min(t.L, 1024);
+  for (int l = tid; l < L; l += blockDim.x) prefix[l + 1] = a.n_items[l];
   if (tid == 0) {
-    prefix[0] = 0;
-    for (int l = 0; l < L && l < 1024; ++l) prefix[l + 1] = prefix[l] + a.n_items[l];
     for (int s = 0; s < STAGES; ++s) mbar_init(&full[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  const int total = prefix[min(L, 1024)];
+  if (tid == 0) {
+    prefix[0] = 0;
+    for (int l = 0; l < L; ++l) prefix[l + 1] += prefix[l];
+  }
+  __syncthreads();
+  const int total = prefix[L];
 
-  // ---- producer state (thread 0 only)
-  int p_item = -1, p_dom = 0, p_j = 0, p_pg = 0;
-  int4 p_it = make_int4(0, 0, 0, 0);
+  // ---- producer state (thread 0 only): the current item's page descriptors in smem
+  __shared__ int4 pq[32];
+  int p_n = 0, p_k = 0, p_dom = 0, p_j = 0;
   bool p_done = false;
   auto produce = [&](int s) -> bool {  // thread 0: next page into stage s
     if (p_done) return false;
-    while (true) {
-      if (p_item < 0 || p_pg >= p_it.w) {
-        const int g = atomicAdd(work_ctr, 1);
-        if (g >= total) {
-          p_done = true;
-          return false;
-        }
-        int lo = 0, hi = L;  // prefix[lo] <= g < prefix[lo+1]
-        while (hi - lo > 1) {
-          const int mid = (lo + hi) / 2;
-          if (prefix[mid] <= g) lo = mid; else hi = mid;
-        }
-        p_dom = lo;
-        p_j = g - prefix[lo];
-        p_it = a.items[static_cast<int64_t>(p_dom) * a.max_items + p_j];
-        p_item = g;
-        p_pg = 0;
+    if (p_k >= p_n) {
+      const int g = atomicAdd(work_ctr, 1);
+      if (g >= total) {
+        p_done = true;
+        return false;
       }
-      StageMeta m;
-      m.dom = p_dom;
-      m.item = p_j;
-      m.kind = p_it.x;
-      m.flags = (p_pg == 0 ? 1 : 0) | (p_pg == p_it.w - 1 ? 2 : 0);
-      const int pidx = p_it.z + p_pg;
-      if (m.kind == 0) {
-        m.page = t.pages[static_cast<int64_t>(p_it.y) * t.maxp + pidx];
-        m.ring_slot = -1;
-        m.tok0 = 0;
-      } else if (m.kind == 1) {
-        m.page = t.bpages[static_cast<int64_t>(p_it.y) * t.maxbp + pidx];
-        m.ring_slot = -1;
-        m.tok0 = 0;
-      } else {
-        m.ring_slot = p_it.y;
-        m.page = t.ring_pages[(static_cast<int64_t>(p_dom) * t.W + p_it.y) * t.rpp + pidx];
-        m.tok0 = pidx * P;
+      int lo = 0, hi = L;  // prefix[lo] <= g < prefix[lo+1]
+      while (hi - lo > 1) {
+        const int mid = (lo + hi) / 2;
+        if (prefix[mid] <= g) lo = mid; else hi = mid;
       }
-      m.fill = t.pg_fill[m.page];
-      p_pg += 1;
-      meta[s] = m;
-      const uint32_t bytes = static_cast<uint32_t>(m.fill) * ROWB;
-      uint8_t* dst = stages + s * stage_bytes;
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      mbar_expect(&full[s], 2 * bytes);
-      bulk_g2s(dst, page_k(t, m.page), bytes, &full[s]);
-      bulk_g2s(dst + static_cast<int64_t>(P) * ROWB, page_v(t, m.page), bytes, &full[s]);
-      return true;
+      p_dom = lo;
+      p_j = g - prefix[lo];
+      const int first = p_j * a.chunk_pages;
+      p_n = min(a.chunk_pages, a.n_desc[p_dom] - first);
+      const int4* src = a.desc + static_cast<int64_t>(p_dom) * a.max_desc + first;
+#pragma unroll 8
+      for (int i = 0; i < 32; ++i)
+        if (i < p_n) pq[i] = src[i];  // independent loads, one latency per item
+      p_k = 0;
     }
+    const int4 dsc = pq[p_k];
+    StageMeta m;
+    m.dom = p_dom;
+    m.item = p_j;
+    m.page = dsc.x;
+    m.fill = dsc.y;
+    m.kind = dsc.z & 0xff;
+    m.ring_slot = dsc.z >> 8;
+    m.tok0 = dsc.w;
+    m.flags = (p_k == 0 ? 1 : 0) | (p_k == p_n - 1 ? 2 : 0);
+    p_k += 1;
+    meta[s] = m;
+    const uint32_t bytes = static_cast<uint32_t>(m.fill) * ROWB;
+    uint8_t* dst = stages + s * stage_bytes;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mbar_expect(&full[s], 2 * bytes);
+    bulk_g2s(dst, page_k(t, m.page), bytes, &full[s]);
+    bulk_g2s(dst + static_cast<int64_t>(P) * ROWB, page_v(t, m.page), bytes, &full[s]);
+    return true;
   };
   __shared__ int issued[STAGES];
   if (tid == 0)

@@ -148,10 +148,12 @@ struct DecodeArgs {
   int32_t* n_ver;          // [L]
   int64_t* attended;       // [L]        attended-set size (members+buffers of verified U window)
   int32_t* n_cand;         // [L]        candidates compared (count_candidates)
-  // attention work list: item = (domain, kind, ref, first page, n pages)
-  int4* items;             // [L][max_items]
-  int32_t* n_items;        // [L]
-  int32_t max_items, chunk_pages;
+  // attention work list: page descriptors per domain (x page, y fill, z kind | ring_slot << 8,
+  // w first token of the page within its frame); an item = chunk_pages consecutive descriptors
+  int4* desc;              // [L][max_desc]
+  int32_t* n_desc;         // [L]
+  int32_t* n_items;        // [L] = ceil(n_desc / chunk_pages)
+  int32_t max_desc, max_items, chunk_pages;
   // attention partials / output
   float* part_ml;          // [L][max_items][2]
   float* part_o;           // [L][max_items][d]
