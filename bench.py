@@ -254,7 +254,7 @@ def main():
     for i in range(args.warmup):
         kv.query(i, q_dev[i], out=out_dev)
     kv.set_timing(True)
-    att_us, k4_us, att_bytes_l = [], [], []
+    att_us, k4_us, att_bytes_l, host_ph = [], [], [], []
     launches0 = kv.launch_count()
     torch.cuda.synchronize()
     if world > 1:
@@ -268,6 +268,7 @@ def main():
                 k4_us.append(tm[0])
                 att_us.append(tm[1])
                 att_bytes_l.append(tm[4])
+                host_ph.append(tm[5:8].copy())
                 if world > 1:
                     dist.all_gather_into_tensor(gathered, out_dev)
             ev1.record(stream)
@@ -319,6 +320,10 @@ def main():
                      "step_bytes": step_bytes, "step_frac": round(step_bytes / (us_step * 1e-6) / 1e9 / hbm, 4),
                      "score_select_us": round(float(np.mean(k4_us)), 2)},
         "gpu_launches": int(decode_launches),
+        "phases_us": {"score_select": round(float(np.mean(k4_us)), 2), "attend": round(att_time * 1e6, 2),
+                      "host_wait_device": round(float(np.mean([h[0] for h in host_ph])), 2),
+                      "host_replay": round(float(np.mean([h[1] for h in host_ph])), 2),
+                      "host_repin": round(float(np.mean([h[2] for h in host_ph])), 2)},
         "clocks": clk.summary(),
         "ingest": {"value": round(frames_t / (ingest_ms * 1e-3), 1), "unit": "frames/s",
                    "frames": frames_t, "domains_per_frame": D * world, "tokens_per_frame": T_FRAME,

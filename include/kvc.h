@@ -199,9 +199,11 @@ KVC_API int kvc_fetch(kvc_ctx* ctx, int64_t id, int32_t cause, double* cost_us);
 /* ------------------------------------------------------------------ instrumentation */
 /* Kernel launches issued by this context since creation (for bench gpu_launches). */
 KVC_API int64_t kvc_launch_count(kvc_ctx* ctx);
-/* Timing of the last decode step's device phases in microseconds (CUDA events):
- * t[0]=score/select, t[1]=attention, t[2]=combine, t[3]=whole step; and the algorithmic
- * bytes of the attention launch (t[4]) */
+/* Timing of the last decode step (needs kvc_set_timing(1)), t[8]: device phases in
+ * microseconds from CUDA events -- t[0] score/select, t[1] attention (+ fused combine), t[2]
+ * unused, t[3] launch-to-end on the device; t[4] algorithmic bytes of the attention launch;
+ * host phases in microseconds -- t[5] wait for the device, t[6] retrieve bookkeeping replay,
+ * t[7] repin + checks. */
 KVC_API int kvc_last_step_timing(kvc_ctx* ctx, double* t);
 /* Enables per-phase CUDA-event timing (off by default: it adds event records). */
 KVC_API void kvc_set_timing(kvc_ctx* ctx, int32_t on);

@@ -384,6 +384,6 @@ class ClusterKVCache:
         lib().kvc_set_timing(self.h, 1 if on else 0)
 
     def step_timing(self):
-        t = np.zeros(5)
+        t = np.zeros(8)
         lib().kvc_last_step_timing(self.h, _p(t, f64p))
         return t

@@ -165,6 +165,7 @@ void Context::alloc_device() {
   t_.pl_pool_cap = S * 4 + 1024;
   t_.pl_pool = static_cast<std::int32_t*>(dalloc(t_.pl_pool_cap * 4));
   t_.err = static_cast<std::int32_t*>(dalloc(16));
+  h_err_ = static_cast<std::int32_t*>(halloc(16));
 
   // page stack: ring pages are [0, ring_pages); the stack holds the rest
   {
@@ -303,9 +304,13 @@ void Context::sync() { KVC_CUDA(cudaStreamSynchronize(st_)); }
 void Context::check_dev_err() {
   std::int32_t e = 0;
   KVC_CUDA(cudaMemcpy(&e, t_.err, 4, cudaMemcpyDeviceToHost));
+  check_err_word(e);
+}
+
+void Context::check_err_word(std::int32_t e) {
   if (!e) return;
-  std::int32_t z = 0;
-  KVC_CUDA(cudaMemcpy(t_.err, &z, 4, cudaMemcpyHostToDevice));
+  KVC_CUDA(cudaMemsetAsync(t_.err, 0, 4, st_));
+  sync();
   if (e & DERR_DEGENERATE) fail(-2, "cosine of zero vector");
   if (e & DERR_PAGES) fail(-21, "page pool exhausted (raise kvc_cfg.pool_bytes)");
   if (e & DERR_CLUSTER_PAGES) fail(-21, "cluster exceeds max_cluster_pages / max_buffer_pages");
@@ -748,8 +753,9 @@ void Context::run_inserts(std::int64_t frame_id, std::int64_t pid, int T, std::i
       KVC_CUDA(cudaMemcpyAsync(h_evk_, ia_.ev_kind, static_cast<std::size_t>(L_) * t_.tmax * 4, cudaMemcpyDeviceToHost, st_));
       KVC_CUDA(cudaMemcpyAsync(h_evs_, ia_.ev_slot, static_cast<std::size_t>(L_) * t_.tmax * 4, cudaMemcpyDeviceToHost, st_));
       KVC_CUDA(cudaMemcpyAsync(h_stop_, ia_.stop_t, static_cast<std::size_t>(L_) * 12, cudaMemcpyDeviceToHost, st_));
+      KVC_CUDA(cudaMemcpyAsync(h_err_, t_.err, 4, cudaMemcpyDeviceToHost, st_));
       sync();
-      check_dev_err();
+      check_err_word(*h_err_);
       launch = false;
     }
     const int l = frontier;

@@ -254,6 +254,8 @@ class Context {
   void ensure_idx(std::int64_t n, std::int64_t runs);
   void sync();
   void check_dev_err();
+  void check_err_word(std::int32_t e);  // inspects a copied DevTables::err word
+  std::int32_t* h_err_ = nullptr;       // pinned copy of DevTables::err
 };
 
 }  // namespace kvc

@@ -9,6 +9,7 @@
 //   engine.cpp:176-237    answer_query: repin + checks after the query
 //   index.cpp:263-343     check_invariants;  store.cpp:183-189 audit
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstring>
 #include <numeric>
@@ -50,8 +51,11 @@ void Context::decode_step(std::int64_t qid, const float* q, int q_mem, float* ou
   KVC_CUDA(cudaMemcpyAsync(h_dec_, d_dec_, dec_bytes_, cudaMemcpyDeviceToHost, st_));
   if (out && out_mem != KVC_MEM_DEVICE)
     KVC_CUDA(cudaMemcpyAsync(out, d_out_, static_cast<std::size_t>(L_) * d_ * 4, cudaMemcpyDeviceToHost, st_));
+  KVC_CUDA(cudaMemcpyAsync(h_err_, t_.err, 4, cudaMemcpyDeviceToHost, st_));
+  const auto th0 = std::chrono::steady_clock::now();
   sync();
-  check_dev_err();
+  const auto th1 = std::chrono::steady_clock::now();
+  check_err_word(*h_err_);
   if (timing_) {
     float ms = 0.f;
     for (int i = 0; i < 3; ++i) {
@@ -178,8 +182,14 @@ void Context::decode_step(std::int64_t qid, const float* q, int q_mem, float* ou
       }
     last_digest_ = h;
   }
+  const auto th2 = std::chrono::steady_clock::now();
   repin();  // engine.cpp:234
   if (cfg_.check_invariants) check();
+  const auto th3 = std::chrono::steady_clock::now();
+  // host-side phases (us): wait for the device, replay of the retrieve bookkeeping, repin/checks
+  step_t_[5] = std::chrono::duration<double, std::micro>(th1 - th0).count();
+  step_t_[6] = std::chrono::duration<double, std::micro>(th2 - th1).count();
+  step_t_[7] = std::chrono::duration<double, std::micro>(th3 - th2).count();
 }
 
 // ---------------------------------------------------------------------------- bulk load

@@ -662,48 +662,61 @@ __device__ __forceinline__ double exact_cos(const float* q, double nq, const dou
   return clamp1(ddiv(acc, dmul(nq, nr)));
 }
 
-struct K4Smem {
-  double* vsim;
-  long long* vkey;
-  uint8_t* vtaken;
-  double* csim;
-  long long* ckey;
-  uint8_t* ctaken;
-  int* cslot;
-  uint8_t* cbuf;
-};
+// Block-wide bitonic sort of n (power of two) entries "best first" by (sim desc, key asc);
+// `ord` carries the payload. Padding entries use sim = -inf, key = LLONG_MAX.
+__device__ void block_bitonic(double* sim, long long* key, int* ord, int n) {
+  for (int k = 2; k <= n; k <<= 1)
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const int p = i ^ j;
+        if (p > i) {
+          const bool up = (i & k) == 0;
+          const bool sw = up ? better(sim[p], key[p], sim[i], key[i]) : better(sim[i], key[i], sim[p], key[p]);
+          if (sw) {
+            const double ts = sim[i];
+            sim[i] = sim[p];
+            sim[p] = ts;
+            const long long tk = key[i];
+            key[i] = key[p];
+            key[p] = tk;
+            const int to = ord[i];
+            ord[i] = ord[p];
+            ord[p] = to;
+          }
+        }
+      }
+      __syncthreads();
+    }
+}
+
+__host__ __device__ inline int pow2_at_least(int n) {
+  int p = 1;
+  while (p < n) p <<= 1;
+  return p;
+}
 
 __global__ void __launch_bounds__(256) k_score_select(DevTables t, DecodeArgs a, int* work_ctr) {
   extern __shared__ uint8_t sm4[];
   const int l = blockIdx.x, d = t.d, L = t.L;
   const int P = *t.n_parts;
   const int cmax = t.cmax;
-  // carve
+  const int ns = pow2_at_least(max(t.max_parts, cmax));
   uint8_t* p = sm4;
   float* qf = reinterpret_cast<float*>(p);
   p += ((d * 4 + 15) / 16) * 16;
-  double* vsim = reinterpret_cast<double*>(p);
-  p += static_cast<size_t>(t.max_parts) * 8;
-  long long* vkey = reinterpret_cast<long long*>(p);
-  p += static_cast<size_t>(t.max_parts) * 8;
-  double* csim = reinterpret_cast<double*>(p);
-  p += static_cast<size_t>(cmax) * 8;
-  long long* ckey = reinterpret_cast<long long*>(p);
-  p += static_cast<size_t>(cmax) * 8;
+  double* sim = reinterpret_cast<double*>(p);
+  p += static_cast<size_t>(ns) * 8;
+  long long* key = reinterpret_cast<long long*>(p);
+  p += static_cast<size_t>(ns) * 8;
+  int* ord = reinterpret_cast<int*>(p);
+  p += static_cast<size_t>(ns) * 4;
   int* cslot = reinterpret_cast<int*>(p);
   p += static_cast<size_t>(cmax) * 4;
   uint8_t* cbuf = p;
-  p += cmax;
-  uint8_t* vtaken = p;
-  p += t.max_parts;
-  uint8_t* ctaken = p;
-  p += cmax;
-  __shared__ double red_s[32];
-  __shared__ long long red_k[32];
-  __shared__ int red_i[33];
   __shared__ double nq_s;
   __shared__ int ncand_s, chosen[64];
   __shared__ int vers[64], nver_s;
+  __shared__ int rank_slot[64], n_rank_s;
   __shared__ unsigned long long att_s;
   __shared__ bool degen;
 
@@ -723,24 +736,31 @@ __global__ void __launch_bounds__(256) k_score_select(DevTables t, DecodeArgs a,
   __syncthreads();
   const double nq = nq_s;
   bool dg = false;
-  // ---- stage 1: visual_topk (index.cpp:192-208)
-  for (int pp = threadIdx.x; pp < P; pp += blockDim.x) {
-    vsim[pp] = exact_cos(qf, nq, t.vrep + static_cast<int64_t>(pp) * d, t.vnorm[pp], d, dg);
-    vkey[pp] = pp;
-    vtaken[pp] = 0;
+  // ---- stage 1: visual_topk (index.cpp:192-208): exact cosines, sort (sim desc, id asc)
+  const int np2 = pow2_at_least(max(P, 1));
+  for (int pp = threadIdx.x; pp < np2; pp += blockDim.x) {
+    if (pp < P) {
+      sim[pp] = exact_cos(qf, nq, t.vrep + static_cast<int64_t>(pp) * d, t.vnorm[pp], d, dg);
+      key[pp] = pp;
+    } else {
+      sim[pp] = -INFINITY;
+      key[pp] = LLONG_MAX;
+    }
+    ord[pp] = pp;
   }
   if (dg) degen = true;
   __syncthreads();
+  block_bitonic(sim, key, ord, np2);
   const int kv = min(a.k_v, P);
-  for (int i = 0; i < kv; ++i) {
-    const int b = block_take_best(vsim, vkey, vtaken, P, red_s, red_k, red_i);
-    if (threadIdx.x == 0) chosen[i] = b;
+  if (threadIdx.x < kv) {
+    chosen[threadIdx.x] = ord[threadIdx.x];
+    a.parts[l * a.k_v + threadIdx.x] = ord[threadIdx.x];
   }
-  __syncthreads();
-  if (threadIdx.x < kv) a.parts[l * a.k_v + threadIdx.x] = chosen[threadIdx.x];
   if (threadIdx.x == 0) a.n_parts_sel[l] = kv;
+  __syncthreads();
 
-  // ---- stage 2 (and the prefetch ranking of layer l+1, retrieval.cpp:117-128)
+  // ---- stage 2: semantic_topk (index.cpp:210-240) and the prefetch ranking of layer l+1
+  // with this layer's query (retrieval.cpp:117-128)
   const int passes = (a.prefetch && l + 1 < L) ? 2 : 1;
   for (int pass = 0; pass < passes; ++pass) {
     const int layer = l + pass;
@@ -748,8 +768,8 @@ __global__ void __launch_bounds__(256) k_score_select(DevTables t, DecodeArgs a,
     if (threadIdx.x == 0) ncand_s = 0;
     __syncthreads();
     for (int i = 0; i < kv; ++i) {
-      const int64_t key = static_cast<int64_t>(chosen[i]) * L + layer;
-      const int off = t.pl_off[key], cnt = t.pl_cnt[key];
+      const int64_t pk = static_cast<int64_t>(chosen[i]) * L + layer;
+      const int off = t.pl_off[pk], cnt = t.pl_cnt[pk];
       for (int j = threadIdx.x; j < cnt; j += blockDim.x) {
         const int s = t.pl_pool[off + j];
         const int lz = t.lazy[s];
@@ -769,35 +789,43 @@ __global__ void __launch_bounds__(256) k_score_select(DevTables t, DecodeArgs a,
     __syncthreads();
     const int nc = min(ncand_s, cmax);
     if (pass == 0 && threadIdx.x == 0) a.n_cand[l] = nc;
+    const int nc2 = pow2_at_least(max(nc, 1));
     dg = false;
-    for (int c = threadIdx.x; c < nc; c += blockDim.x) {
-      const int s = cslot[c];
-      const bool ib = cbuf[c];
-      csim[c] = exact_cos(qf, nq, (ib ? t.brep64 : t.rep64) + static_cast<int64_t>(s) * d,
-                          ib ? t.bnorm[s] : t.rnorm[s], d, dg);
-      ckey[c] = 2LL * t.cid[s] + (ib ? 1 : 0);
-      ctaken[c] = 0;
+    for (int c = threadIdx.x; c < nc2; c += blockDim.x) {
+      if (c < nc) {
+        const int s = cslot[c];
+        const bool ib = cbuf[c];
+        sim[c] = exact_cos(qf, nq, (ib ? t.brep64 : t.rep64) + static_cast<int64_t>(s) * d,
+                           ib ? t.bnorm[s] : t.rnorm[s], d, dg);
+        key[c] = 2LL * t.cid[s] + (ib ? 1 : 0);
+      } else {
+        sim[c] = -INFINITY;
+        key[c] = LLONG_MAX;
+      }
+      ord[c] = c;
     }
     if (dg) degen = true;
     __syncthreads();
+    block_bitonic(sim, key, ord, nc2);
     const int take = min(ktake, nc);
-    for (int i = 0; i < take; ++i) {
-      const int b = block_take_best(csim, ckey, ctaken, nc, red_s, red_k, red_i);
-      if (threadIdx.x == 0) {
-        if (pass == 0) {
-          a.ranked_slot[l * a.k_s + i] = cslot[b];
-          a.ranked_buf[l * a.k_s + i] = cbuf[b];
-        } else {
-          a.pf_slot[l * a.prefetch_k + i] = cslot[b];
-          a.pf_buf[l * a.prefetch_k + i] = cbuf[b];
-        }
+    if (threadIdx.x < take) {
+      const int b = ord[threadIdx.x];
+      if (pass == 0) {
+        rank_slot[threadIdx.x] = cslot[b];
+        a.ranked_slot[l * a.k_s + threadIdx.x] = cslot[b];
+        a.ranked_buf[l * a.k_s + threadIdx.x] = cbuf[b];
+      } else {
+        a.pf_slot[l * a.prefetch_k + threadIdx.x] = cslot[b];
+        a.pf_buf[l * a.prefetch_k + threadIdx.x] = cbuf[b];
       }
     }
     if (threadIdx.x == 0) {
-      if (pass == 0)
+      if (pass == 0) {
         a.n_ranked[l] = take;
-      else
+        n_rank_s = take;
+      } else {
         a.n_pf[l] = take;
+      }
     }
     __syncthreads();
   }
@@ -809,8 +837,8 @@ __global__ void __launch_bounds__(256) k_score_select(DevTables t, DecodeArgs a,
   __shared__ int ring_cnt[64], ring_off[65];
   if (threadIdx.x == 0) {
     int nv = 0;
-    for (int i = 0; i < a.n_ranked[l]; ++i) {
-      const int s = a.ranked_slot[l * a.k_s + i];
+    for (int i = 0; i < n_rank_s; ++i) {
+      const int s = rank_slot[i];
       bool dup = false;
       for (int j = 0; j < nv; ++j) dup |= vers[j] == s;
       if (!dup) vers[nv++] = s;
@@ -920,10 +948,19 @@ struct StageMeta {
   int kind, ring_slot, tok0, flags;  // flags: 1 first page of item, 2 last page of item
 };
 
+// 8 warps; a 64-token sub-tile of a page is split 8 tokens per warp, 4 lanes per token
+// (D/4 dims each, two accumulators) for q.k; each lane owns D/32 output dims for p.v.
+constexpr int ATT_THREADS = 256;
+constexpr int ATT_WARPS = ATT_THREADS / 32;
+
 template <int D, bool BF16, int STAGES>
-__global__ void __launch_bounds__(128) k_attend(DevTables t, DecodeArgs a, int* work_ctr) {
+__global__ void __launch_bounds__(ATT_THREADS) k_attend(DevTables t, DecodeArgs a, int* work_ctr) {
   constexpr int ES = BF16 ? 2 : 4;
   constexpr int ROWB = D * ES;
+  constexpr int QB = ROWB / 4;  // bytes of a row handled by one lane for q.k
+  constexpr int CH = QB / 16;   // 16-byte chunks per lane
+  constexpr int EPC = 16 / ES;  // elements per chunk
+  constexpr int OPL = D / 32;   // output dims per lane
   extern __shared__ __align__(128) uint8_t sm6[];
   const int P = t.P;
   const int64_t stage_bytes = static_cast<int64_t>(2) * P * ROWB;
@@ -934,9 +971,11 @@ __global__ void __launch_bounds__(128) k_attend(DevTables t, DecodeArgs a, int* 
   __shared__ int vers_s[64];
   __shared__ int nver_sh;
   __shared__ int prefix[1025];
-  __shared__ float wm[4], wl[4];
-  __shared__ float wo[4][D];
+  __shared__ float wm[ATT_WARPS], wl[ATT_WARPS];
+  __shared__ float wo[ATT_WARPS][D];
   __shared__ int last_flag;
+  __shared__ int issued[STAGES];
+  __shared__ int4 pq[32];
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int L = min(t.L, 1024);
@@ -953,11 +992,10 @@ __global__ void __launch_bounds__(128) k_attend(DevTables t, DecodeArgs a, int* 
   __syncthreads();
   const int total = prefix[L];
 
-  // ---- producer state (thread 0 only): the current item's page descriptors in smem
-  __shared__ int4 pq[32];
+  // ---- producer (thread 0): the current item's page descriptors live in smem
   int p_n = 0, p_k = 0, p_dom = 0, p_j = 0;
   bool p_done = false;
-  auto produce = [&](int s) -> bool {  // thread 0: next page into stage s
+  auto produce = [&](int s) -> bool {
     if (p_done) return false;
     if (p_k >= p_n) {
       const int g = atomicAdd(work_ctr, 1);
@@ -965,7 +1003,7 @@ __global__ void __launch_bounds__(128) k_attend(DevTables t, DecodeArgs a, int* 
         p_done = true;
         return false;
       }
-      int lo = 0, hi = L;  // prefix[lo] <= g < prefix[lo+1]
+      int lo = 0, hi = L;
       while (hi - lo > 1) {
         const int mid = (lo + hi) / 2;
         if (prefix[mid] <= g) lo = mid; else hi = mid;
@@ -977,7 +1015,7 @@ __global__ void __launch_bounds__(128) k_attend(DevTables t, DecodeArgs a, int* 
       const int4* src = a.desc + static_cast<int64_t>(p_dom) * a.max_desc + first;
 #pragma unroll 8
       for (int i = 0; i < 32; ++i)
-        if (i < p_n) pq[i] = src[i];  // independent loads, one latency per item
+        if (i < p_n) pq[i] = src[i];
       p_k = 0;
     }
     const int4 dsc = pq[p_k];
@@ -1000,99 +1038,91 @@ __global__ void __launch_bounds__(128) k_attend(DevTables t, DecodeArgs a, int* 
     bulk_g2s(dst + static_cast<int64_t>(P) * ROWB, page_v(t, m.page), bytes, &full[s]);
     return true;
   };
-  __shared__ int issued[STAGES];
   if (tid == 0)
     for (int s = 0; s < STAGES; ++s) issued[s] = produce(s) ? 1 : 0;
   __syncthreads();
 
   float m_run = -INFINITY, l_run = 0.f;
-  constexpr int OPL = D / 32;  // output dims per lane
   float o_run[OPL];
 #pragma unroll
   for (int i = 0; i < OPL; ++i) o_run[i] = 0.f;
   int cur_dom = -1;
   uint32_t phase_bits = 0;
   const float sl2 = a.scale_log2;
+  const int sub = lane >> 2;   // token within the warp's 8
+  const int part = lane & 3;   // quarter of the row for q.k
 
   for (int s = 0;; s = (s + 1) % STAGES) {
     if (!issued[s]) break;
     mbar_wait(&full[s], (phase_bits >> s) & 1u);
     phase_bits ^= (1u << s);
     const StageMeta m = meta[s];
-    if (m.flags & 1) {  // new item: reset state, load the domain's query / verified list
-      m_run = -INFINITY;
-      l_run = 0.f;
-#pragma unroll
-      for (int i = 0; i < OPL; ++i) o_run[i] = 0.f;
-      if (m.dom != cur_dom) {
-        __syncthreads();
-        for (int i = tid; i < D; i += 128) qs[i] = a.q[static_cast<int64_t>(m.dom) * D + i];
-        if (tid == 0) nver_sh = a.n_ver[m.dom];
-        if (tid < 64) vers_s[tid] = tid < a.n_ver[m.dom] ? a.ver_slot[m.dom * a.k_s + tid] : -1;
-        __syncthreads();
-        cur_dom = m.dom;
-      }
+    if ((m.flags & 1) && m.dom != cur_dom) {  // load the domain's query and verified list
+      __syncthreads();
+      for (int i = tid; i < D; i += ATT_THREADS) qs[i] = a.q[static_cast<int64_t>(m.dom) * D + i];
+      if (tid == 0) nver_sh = a.n_ver[m.dom];
+      if (tid < 64) vers_s[tid] = tid < a.n_ver[m.dom] ? a.ver_slot[m.dom * a.k_s + tid] : -1;
+      __syncthreads();
+      cur_dom = m.dom;
     }
     const uint8_t* Ks = stages + s * stage_bytes;
     const uint8_t* Vs = Ks + static_cast<int64_t>(P) * ROWB;
-    // ---- scores: 2 threads per token, 16 tokens per warp per sub-tile of 64
-    for (int tb = 0; tb < P; tb += 64) {
-      const int tok = tb + (tid >> 1);
-      const int half = tid & 1;
-      float sc = -INFINITY;
+    for (int tb = 0; tb < m.fill; tb += 64) {
+      const int tok = tb + warp * 8 + sub;
       bool valid = tok < m.fill;
       if (valid && m.kind == 2) {
         const int own = t.ring_owner[(static_cast<int64_t>(m.dom) * t.W + m.ring_slot) * t.tmax + m.tok0 + tok];
         for (int j = 0; j < nver_sh; ++j) valid &= vers_s[j] != own;
       }
-      float acc = 0.f;
+      float acc0 = 0.f, acc1 = 0.f;
       if (tok < m.fill) {
-        constexpr int CH = ROWB / 32;  // 16-byte chunks per half row
-        const uint8_t* krow = Ks + static_cast<int64_t>(tok) * ROWB + half * (ROWB / 2);
+        const uint8_t* krow = Ks + static_cast<int64_t>(tok) * ROWB + part * QB;
+        const float* qq0 = qs + part * (D / 4);
 #pragma unroll
         for (int j = 0; j < CH; ++j) {
-          const int c = (j + tok) % CH;
+          const int c = (j + sub) % CH;  // rotate chunks across tokens: spreads smem banks
           const uint4 raw = *reinterpret_cast<const uint4*>(krow + c * 16);
+          const float* qq = qq0 + c * EPC;
           if (BF16) {
             const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
-            const float* qq = qs + half * (D / 2) + c * 8;
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
               const float2 f = __bfloat1622float2(h2[e]);
-              acc = fmaf(f.x, qq[2 * e], acc);
-              acc = fmaf(f.y, qq[2 * e + 1], acc);
+              acc0 = fmaf(f.x, qq[2 * e], acc0);
+              acc1 = fmaf(f.y, qq[2 * e + 1], acc1);
             }
           } else {
             const float* f = reinterpret_cast<const float*>(&raw);
-            const float* qq = qs + half * (D / 2) + c * 4;
-#pragma unroll
-            for (int e = 0; e < 4; ++e) acc = fmaf(f[e], qq[e], acc);
+            acc0 = fmaf(f[0], qq[0], acc0);
+            acc1 = fmaf(f[1], qq[1], acc1);
+            acc0 = fmaf(f[2], qq[2], acc0);
+            acc1 = fmaf(f[3], qq[3], acc1);
           }
         }
       }
+      float acc = acc0 + acc1;
       acc += __shfl_xor_sync(kFull, acc, 1);
-      if (valid) sc = acc * sl2;
-      // warp max over its 16 tokens
+      acc += __shfl_xor_sync(kFull, acc, 2);
+      const float sc = valid ? acc * sl2 : -INFINITY;
       float mx = sc;
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(kFull, mx, o));
+      for (int o = 16; o >= 4; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(kFull, mx, o));
       const float m_new = fmaxf(m_run, mx);
-      if (m_new == -INFINITY) continue;  // nothing valid yet in this warp
+      if (m_new == -INFINITY) continue;  // warp-uniform
       const float alpha = exp2f(m_run - m_new);
       const float pr = valid ? exp2f(sc - m_new) : 0.f;
-      float psum = half == 0 ? pr : 0.f;
+      float psum = part == 0 ? pr : 0.f;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) psum += __shfl_xor_sync(kFull, psum, o);
       l_run = l_run * alpha + psum;
 #pragma unroll
       for (int i = 0; i < OPL; ++i) o_run[i] *= alpha;
       m_run = m_new;
-      // P.V over the warp's 16 tokens; lane owns dims [lane*OPL, lane*OPL + OPL)
-#pragma unroll 4
-      for (int j = 0; j < 16; ++j) {
-        const float pj = __shfl_sync(kFull, pr, 2 * j);
-        const int tj = tb + warp * 16 + j;
-        if (tj >= m.fill || pj == 0.f) continue;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float pj = __shfl_sync(kFull, pr, 4 * j);
+        const int tj = tb + warp * 8 + j;
+        if (tj >= m.fill) break;
         const uint8_t* vrow = Vs + static_cast<int64_t>(tj) * ROWB + lane * OPL * ES;
         if (BF16) {
 #pragma unroll
@@ -1107,8 +1137,9 @@ __global__ void __launch_bounds__(128) k_attend(DevTables t, DecodeArgs a, int* 
         }
       }
     }
-    __syncthreads();  // stage s fully consumed
-    if (m.flags & 2) {  // item done: merge the 4 warps, write the partial
+    __syncthreads();  // stage s consumed
+    if (tid == 0) issued[s] = produce(s) ? 1 : 0;  // refill while the item epilogue runs
+    if (m.flags & 2) {  // item done: merge warps, write the partial, maybe combine the domain
       if (lane == 0) {
         wm[warp] = m_run;
         wl[warp] = l_run;
@@ -1116,17 +1147,18 @@ __global__ void __launch_bounds__(128) k_attend(DevTables t, DecodeArgs a, int* 
 #pragma unroll
       for (int i = 0; i < OPL; ++i) wo[warp][lane * OPL + i] = o_run[i];
       __syncthreads();
-      float M = fmaxf(fmaxf(wm[0], wm[1]), fmaxf(wm[2], wm[3]));
+      float M = -INFINITY;
+      for (int w = 0; w < ATT_WARPS; ++w) M = fmaxf(M, wm[w]);
       const int64_t pi = static_cast<int64_t>(m.dom) * a.max_items + m.item;
-      for (int c = tid; c < D; c += 128) {
+      for (int c = tid; c < D; c += ATT_THREADS) {
         float o = 0.f;
-        for (int w = 0; w < 4; ++w)
+        for (int w = 0; w < ATT_WARPS; ++w)
           if (wm[w] != -INFINITY) o += wo[w][c] * exp2f(wm[w] - M);
         a.part_o[pi * D + c] = o;
       }
       if (tid == 0) {
         float lsum = 0.f;
-        for (int w = 0; w < 4; ++w)
+        for (int w = 0; w < ATT_WARPS; ++w)
           if (wm[w] != -INFINITY) lsum += wl[w] * exp2f(wm[w] - M);
         a.part_ml[pi * 2] = M;
         a.part_ml[pi * 2 + 1] = lsum;
@@ -1135,13 +1167,13 @@ __global__ void __launch_bounds__(128) k_attend(DevTables t, DecodeArgs a, int* 
       __syncthreads();
       if (tid == 0) last_flag = (atomicAdd(&a.dom_done[m.dom], 1) + 1 == a.n_items[m.dom]);
       __syncthreads();
-      if (last_flag) {  // combine all partials of the domain (split-KV reduction)
+      if (last_flag) {  // split-KV combine of all partials of the domain
         __threadfence();
         const int ni = a.n_items[m.dom];
         const float* ml = a.part_ml + static_cast<int64_t>(m.dom) * a.max_items * 2;
         float MM = -INFINITY;
         for (int i = 0; i < ni; ++i) MM = fmaxf(MM, ml[2 * i]);
-        for (int c = tid; c < D; c += 128) {
+        for (int c = tid; c < D; c += ATT_THREADS) {
           float num = 0.f, den = 0.f;
           for (int i = 0; i < ni; ++i) {
             if (ml[2 * i] == -INFINITY) continue;
@@ -1157,9 +1189,7 @@ __global__ void __launch_bounds__(128) k_attend(DevTables t, DecodeArgs a, int* 
       l_run = 0.f;
 #pragma unroll
       for (int i = 0; i < OPL; ++i) o_run[i] = 0.f;
-      __syncthreads();
     }
-    if (tid == 0) issued[s] = produce(s) ? 1 : 0;
     __syncthreads();
   }
 }
@@ -1321,9 +1351,9 @@ int launch_attend_t(const DevTables& t, const DecodeArgs& a, cudaStream_t st) {
     attr = true;
   }
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_attend<D, BF16, STAGES>, 128, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_attend<D, BF16, STAGES>, ATT_THREADS, smem);
   per_sm = max(1, per_sm);
-  k_attend<D, BF16, STAGES><<<g_sms * per_sm, 128, smem, st>>>(t, a, g_ctr);
+  k_attend<D, BF16, STAGES><<<g_sms * per_sm, ATT_THREADS, smem, st>>>(t, a, g_ctr);
   return 1;
 }
 }  // namespace
@@ -1336,8 +1366,9 @@ int launch_decode(const DevTables& t, const DecodeArgs& a, cudaStream_t st, cuda
     cudaMalloc(&g_ctr, 64);
   }
   if (ev) cudaEventRecord(ev[0], st);
-  const size_t smem4 = ((t.d * 4 + 15) / 16) * 16 + static_cast<size_t>(t.max_parts) * 17 +
-                       static_cast<size_t>(t.cmax) * 22 + 64;
+  const int ns = pow2_at_least(t.max_parts > t.cmax ? t.max_parts : t.cmax);
+  const size_t smem4 = ((t.d * 4 + 15) / 16) * 16 + static_cast<size_t>(ns) * 20 +
+                       static_cast<size_t>(t.cmax) * 5 + 64;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_score_select, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
