@@ -206,6 +206,11 @@ void Context::alloc_device() {
   ia_.stop_kind = ia_.stop_t + L;
   ia_.stop_slot = ia_.stop_t + 2 * L;
   ia_.n_exact = static_cast<std::int32_t*>(dalloc(L * 4));
+  ia_.topm_idx = static_cast<std::int16_t*>(dalloc(L * t_.tmax * TOPM * 2));
+  ia_.topm_val = static_cast<float*>(dalloc(L * t_.tmax * TOPM * 4));
+  ia_.topm_next = static_cast<float*>(dalloc(L * t_.tmax * 4));
+  ia_.dom_pool = static_cast<std::int32_t*>(dalloc(L * POOL * 4));
+  ia_.dom_pool_n = static_cast<std::int32_t*>(dalloc(L * 4));
   d_active_ = static_cast<std::int32_t*>(dalloc(L * 4 * 2));
   d_cursor_ = d_active_ + L;
   h_active_ = static_cast<std::int32_t*>(halloc(L * 4 * 2));
@@ -749,6 +754,7 @@ void Context::run_inserts(std::int64_t frame_id, std::int64_t pid, int T, std::i
       KVC_CUDA(cudaMemcpyAsync(d_active_, h_active_, L_ * 8, cudaMemcpyHostToDevice, st_));
       launches_ += launch_build_cands(t_, ia_, st_);
       launches_ += launch_approx(t_, ia_, st_);
+      launches_ += launch_topm(t_, ia_, st_);
       launches_ += launch_resolve(t_, ia_, st_);
       KVC_CUDA(cudaMemcpyAsync(h_evk_, ia_.ev_kind, static_cast<std::size_t>(L_) * t_.tmax * 4, cudaMemcpyDeviceToHost, st_));
       KVC_CUDA(cudaMemcpyAsync(h_evs_, ia_.ev_slot, static_cast<std::size_t>(L_) * t_.tmax * 4, cudaMemcpyDeviceToHost, st_));

@@ -57,7 +57,7 @@ struct LedgerOp {  // TransferOp (store.hpp:35-42)
 };
 
 struct LayerOut {  // LayerResult (retrieval.hpp:49-59)
-  std::vector<std::pair<std::int64_t, int>> ranked;
+  std::vector<std::pair<std::int64_t, int>> ranked, pf;  // pf: device prefetch ranking (l+1)
   std::vector<std::int64_t> selected, predicted;
   std::int64_t prefetch_hits = 0, verified = 0, rep_count = 0, attended_count = 0;
   double lat[5] = {0, 0, 0, 0, 0};
@@ -203,6 +203,8 @@ class Context {
   std::vector<LayerOut> last_;
   double last_ttft_ = 0.0, last_recall_ = -1.0;
   std::uint64_t last_digest_ = 0;
+
+  std::vector<std::int64_t> verified_tmp_;
 
   // ---- helpers
   void alloc_device();

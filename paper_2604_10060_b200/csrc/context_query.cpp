@@ -90,12 +90,14 @@ void Context::decode_step(std::int64_t qid, const float* q, int q_mem, float* ou
   }
 
   // Translate every layer's slots to ids before any settle frees / reuses a slot.
-  std::vector<std::vector<std::pair<std::int64_t, int>>> ranked(static_cast<std::size_t>(L_)), pf(static_cast<std::size_t>(L_));
   for (int l = 0; l < L_; ++l) {
+    LayerOut& lo = last_[static_cast<std::size_t>(l)];
+    lo.ranked.clear();
+    lo.pf.clear();
     for (int i = 0; i < h_nr[l]; ++i)
-      ranked[static_cast<std::size_t>(l)].push_back({slot_id_[static_cast<std::size_t>(h_rs[l * da_.k_s + i])], h_rb[l * da_.k_s + i]});
+      lo.ranked.push_back({slot_id_[static_cast<std::size_t>(h_rs[l * da_.k_s + i])], h_rb[l * da_.k_s + i]});
     for (int i = 0; i < h_np[l]; ++i)
-      pf[static_cast<std::size_t>(l)].push_back({slot_id_[static_cast<std::size_t>(h_ps[l * da_.prefetch_k + i])], h_pb[l * da_.prefetch_k + i]});
+      lo.pf.push_back({slot_id_[static_cast<std::size_t>(h_ps[l * da_.prefetch_k + i])], h_pb[l * da_.prefetch_k + i]});
   }
 
   // retrieval.cpp:58-128, layer by layer
@@ -106,11 +108,15 @@ void Context::decode_step(std::int64_t qid, const float* q, int q_mem, float* ou
   last_ttft_ = 0.0;
   for (int l = 0; l < L_; ++l) {
     LayerOut& lo = last_[static_cast<std::size_t>(l)];
-    lo = LayerOut{};
+    lo.selected.clear();
+    lo.predicted.clear();
+    lo.attended.clear();
+    lo.prefetch_hits = lo.verified = lo.rep_count = lo.attended_count = 0;
+    for (double& x : lo.lat) x = 0.0;
     const std::int64_t compared = static_cast<std::int64_t>(parts_.size()) + h_nc[l];
     lo.lat[0] = cfg_.lookup_cost_per_candidate_us * static_cast<double>(compared);
-    lo.ranked = ranked[static_cast<std::size_t>(l)];
-    std::vector<std::int64_t> verified;
+    std::vector<std::int64_t>& verified = verified_tmp_;
+    verified.clear();
     for (const auto& r : lo.ranked)
       if (std::find(verified.begin(), verified.end(), r.first) == verified.end()) verified.push_back(r.first);
     lo.verified = static_cast<std::int64_t>(verified.size());
@@ -127,6 +133,10 @@ void Context::decode_step(std::int64_t qid, const float* q, int q_mem, float* ou
     predicted_next.clear();
     stall_next = 0.0;
     for (std::int64_t cid : verified) {
+      if (!C(cid).lazy) {  // materialize() is the identity for clusters without a pending split
+        lo.selected.push_back(cid);
+        continue;
+      }
       std::vector<std::int64_t> s = materialize(cid);
       lo.selected.insert(lo.selected.end(), s.begin(), s.end());
     }
@@ -154,7 +164,7 @@ void Context::decode_step(std::int64_t qid, const float* q, int q_mem, float* ou
     lo.rep_count = layer_live_count_[static_cast<std::size_t>(l)];
     lo.lat[4] = cfg_.compute_cost_per_token_us * static_cast<double>(lo.attended_count + lo.rep_count);
     if (cfg_.prefetch_enabled && l + 1 < L_) {
-      for (const auto& r : pf[static_cast<std::size_t>(l)])
+      for (const auto& r : lo.pf)
         if (std::find(predicted_next.begin(), predicted_next.end(), r.first) == predicted_next.end())
           predicted_next.push_back(r.first);
       double pf_cost = 0.0;

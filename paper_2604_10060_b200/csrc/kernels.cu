@@ -211,23 +211,213 @@ __global__ void __launch_bounds__(256) k_approx(DevTables t, IngestArgs a) {
   }
 }
 
+// ============================================================================ K1b
+// Per (domain, token): the TOPM best approximate candidates and the (TOPM+1)-th value, so the
+// sequential resolve reads a few values per token instead of a full row. One warp per token.
+__global__ void __launch_bounds__(256) k_topm(DevTables t, IngestArgs a) {
+  extern __shared__ float rowsm[];  // [8 warps][cmax]
+  const int dom = a.active[blockIdx.y];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tt = blockIdx.x * 8 + warp;
+  if (tt >= a.T) return;
+  const int n = a.cand_n[dom];
+  float* row = rowsm + warp * t.cmax;
+  const float* src = a.approx + (static_cast<int64_t>(dom) * t.tmax + tt) * t.cmax;
+  for (int c = lane; c < n; c += 32) row[c] = src[c];
+  __syncwarp();
+  const int64_t o = (static_cast<int64_t>(dom) * t.tmax + tt);
+  for (int r = 0; r <= TOPM; ++r) {
+    float bv = -INFINITY;
+    int bi = -1;
+    for (int c = lane; c < n; c += 32)
+      if (row[c] > bv || (row[c] == bv && bi >= 0 && c < bi)) {
+        bv = row[c];
+        bi = c;
+      }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const float ov = __shfl_xor_sync(kFull, bv, off);
+      const int oi = __shfl_xor_sync(kFull, bi, off);
+      if (ov > bv || (ov == bv && oi >= 0 && (bi < 0 || oi < bi))) {
+        bv = ov;
+        bi = oi;
+      }
+    }
+    if (lane == 0) {
+      if (r < TOPM) {
+        a.topm_idx[o * TOPM + r] = static_cast<int16_t>(bi);
+        a.topm_val[o * TOPM + r] = bi >= 0 ? bv : -INFINITY;
+      } else {
+        a.topm_next[o] = bi >= 0 ? bv : -INFINITY;
+      }
+    }
+    if (bi >= 0 && lane == (bi & 31)) row[bi] = -INFINITY;
+    __syncwarp();
+  }
+}
+
 // ============================================================================ K2
-// One warp per domain. Per token: exact fp64 cosines for (a) every candidate touched earlier in
-// this launch (its representative moved) and (b) every untouched candidate whose approximate
-// score is within 2*margin of the best untouched approximate score; arg-best with the
-// CandidateRef tie-break; then the maintainer branch.
+// One warp per domain: the sequential on_insert chain of the frame (maintainer.cpp:88-176),
+// exact in fp64. Per token t:
+//   argmax(t) over exact cosines computed in the previous chain phase,
+//   Eq. 3/4 update of the winner into pending buffers (elementwise),
+//   ONE chain phase where every lane runs a 128-long sequential fp64 sum: the sq_dist(k_t, r')
+//   (vecmath.hpp:42-51), |r'|, |buf'| for token t, and the exact dots of token t+1 against every
+//   candidate it could pick (touched clusters + untouched ones within 2*margin of the best
+//   untouched approximate score),
+//   Eq. 5 decision for t, commit.
+// Winner state is cached in shared memory (HOT entries), pages come from a per-domain pool.
+constexpr int HOT = 16;
+constexpr int RELMAX = 96;
+constexpr int SPECIAL_LANES = 3;
+
+struct ResolveShared {
+  // hot cluster state
+  int hslot[HOT];
+  double hrn[HOT], hbn[HOT], hvar[HOT];
+  long long hstat[HOT], hnmem[HOT], hcid[HOT];
+  int hnbuf[HOT], hnp[HOT], hlast[HOT], hfill[HOT], hbnp[HOT], hblast[HOT], hbfill[HOT];
+  uint8_t hlazy[HOT], hresid[HOT];
+  int nhot;
+  // relevant entries of the next token
+  const double* e_ptr[RELMAX];
+  double e_nr[RELMAX], e_dot[RELMAX];
+  long long e_key[RELMAX];
+  int e_cand[RELMAX];
+  uint8_t e_var[RELMAX];  // 0 current state, 1 pending (winner), 2 speculative fresh buffer
+  int ne;
+  int pool[POOL];
+  int npool;
+};
+
+__device__ void hot_writeback(const DevTables& t, ResolveShared& S, const double* hrep,
+                              const double* hbrep, int h) {
+  const int lane = threadIdx.x & 31, d = t.d;
+  const int64_t s = S.hslot[h];
+  for (int i = lane; i < d; i += 32) {
+    const double r = hrep[h * d + i];
+    t.rep64[s * d + i] = r;
+    t.rep32[s * d + i] = static_cast<float>(r);
+    if (S.hnbuf[h] > 0) {
+      const double b = hbrep[h * d + i];
+      t.brep64[s * d + i] = b;
+      t.brep32[s * d + i] = static_cast<float>(b);
+    }
+  }
+  if (lane == 0) {
+    t.rnorm[s] = S.hrn[h];
+    t.bnorm[s] = S.hbn[h];
+    t.var[s] = S.hvar[h];
+    t.stat[s] = S.hstat[h];
+    t.nmem[s] = S.hnmem[h];
+    t.nbuf[s] = S.hnbuf[h];
+    t.lazy[s] = S.hlazy[h];
+    t.npages[s] = S.hnp[h];
+    t.nbpages[s] = S.hbnp[h];
+    if (S.hlast[h] >= 0) t.pg_fill[S.hlast[h]] = S.hfill[h];
+    if (S.hblast[h] >= 0) t.pg_fill[S.hblast[h]] = S.hbfill[h];
+  }
+}
+
+__device__ int hot_load(const DevTables& t, ResolveShared& S, double* hrep, double* hbrep, int slot) {
+  const int lane = threadIdx.x & 31, d = t.d;
+  const int h = S.nhot;
+  __syncwarp();  // every lane has read nhot before lane 0 bumps it
+  for (int i = lane; i < d; i += 32) {
+    hrep[h * d + i] = t.rep64[static_cast<int64_t>(slot) * d + i];
+    hbrep[h * d + i] = t.brep64[static_cast<int64_t>(slot) * d + i];
+  }
+  if (lane == 0) {
+    S.hslot[h] = slot;
+    S.hrn[h] = t.rnorm[slot];
+    S.hbn[h] = t.bnorm[slot];
+    S.hvar[h] = t.var[slot];
+    S.hstat[h] = t.stat[slot];
+    S.hnmem[h] = t.nmem[slot];
+    S.hcid[h] = t.cid[slot];
+    S.hnbuf[h] = t.nbuf[slot];
+    S.hlazy[h] = t.lazy[slot];
+    S.hresid[h] = t.resid[slot];
+    const int np = t.npages[slot], nbp = t.nbpages[slot];
+    S.hnp[h] = np;
+    S.hlast[h] = np > 0 ? t.pages[static_cast<int64_t>(slot) * t.maxp + np - 1] : -1;
+    S.hfill[h] = S.hlast[h] >= 0 ? t.pg_fill[S.hlast[h]] : t.P;
+    S.hbnp[h] = nbp;
+    S.hblast[h] = nbp > 0 ? t.bpages[static_cast<int64_t>(slot) * t.maxbp + nbp - 1] : -1;
+    S.hbfill[h] = S.hblast[h] >= 0 ? t.pg_fill[S.hblast[h]] : t.P;
+    S.nhot = h + 1;
+  }
+  __syncwarp();
+  return h;
+}
+
+// append one K/V row to a hot slot's member (to_buf = 0) or buffer page list
+__device__ void hot_append(const DevTables& t, ResolveShared& S, int h, bool to_buf,
+                           const uint8_t* src_k, const uint8_t* src_v) {
+  const int lane = threadIdx.x & 31;
+  int page = -1, row = -1;
+  if (lane == 0) {
+    int& np = to_buf ? S.hbnp[h] : S.hnp[h];
+    int& last = to_buf ? S.hblast[h] : S.hlast[h];
+    int& fill = to_buf ? S.hbfill[h] : S.hfill[h];
+    if (fill >= t.P) {
+      const int cap = to_buf ? t.maxbp : t.maxp;
+      if (np >= cap) {
+        set_err(t, DERR_CLUSTER_PAGES);
+      } else {
+        if (S.npool == 0) {  // refill the domain's page pool from the shared free stack
+          const int top = atomicSub(t.free_top, POOL);
+          const int got = max(0, min(POOL, top));
+          if (got < POOL) atomicAdd(t.free_top, POOL - got);
+          for (int i = 0; i < got; ++i) S.pool[i] = t.free_stack[top - 1 - i];
+          S.npool = got;
+        }
+        if (S.npool == 0) {
+          set_err(t, DERR_PAGES);
+        } else {
+          const int pg = S.pool[--S.npool];
+          if (last >= 0) t.pg_fill[last] = t.P;
+          int* list = to_buf ? t.bpages + static_cast<int64_t>(S.hslot[h]) * t.maxbp
+                             : t.pages + static_cast<int64_t>(S.hslot[h]) * t.maxp;
+          list[np] = pg;
+          np += 1;
+          last = pg;
+          fill = 0;
+        }
+      }
+    }
+    if (fill < t.P && last >= 0) {
+      page = last;
+      row = fill++;
+    }
+  }
+  page = __shfl_sync(kFull, page, 0);
+  row = __shfl_sync(kFull, row, 0);
+  if (page < 0) return;
+  const int rb = t.d * t.es;
+  uint8_t* dk = page_k(t, page) + static_cast<int64_t>(row) * rb;
+  uint8_t* dv = page_v(t, page) + static_cast<int64_t>(row) * rb;
+  for (int o = lane * 16; o < rb; o += 32 * 16) {
+    *reinterpret_cast<uint4*>(dk + o) = *reinterpret_cast<const uint4*>(src_k + o);
+    *reinterpret_cast<uint4*>(dv + o) = *reinterpret_cast<const uint4*>(src_v + o);
+  }
+}
+
 __global__ void __launch_bounds__(32) k_resolve(DevTables t, IngestArgs a) {
-  extern __shared__ uint8_t smraw[];
+  extern __shared__ __align__(16) uint8_t smraw[];
+  __shared__ ResolveShared S;
   const int d = t.d, cmax = t.cmax, lane = threadIdx.x;
-  double* nk = reinterpret_cast<double*>(smraw);       // [tmax]
-  double* repn = nk + t.tmax;                           // [d]
-  double* bufn = repn + d;                              // [d]
-  double* relsim = bufn + d;                            // [cmax]
-  float* keyf = reinterpret_cast<float*>(relsim + cmax);  // [d]
-  int* cslot = reinterpret_cast<int*>(keyf + d);         // [cmax]
-  int* rel = cslot + cmax;                               // [cmax]
-  uint8_t* cbuf = reinterpret_cast<uint8_t*>(rel + cmax);  // [cmax]
-  uint8_t* touched = cbuf + cmax;                          // [cmax]
+  double* hrep = reinterpret_cast<double*>(smraw);  // [HOT][d]
+  double* hbrep = hrep + HOT * d;                    // [HOT][d]
+  double* kd = hbrep + HOT * d;                      // [2][d] keys of t and t+1 (as double)
+  double* nrep = kd + 2 * d;                         // [d] pending r'
+  double* nbrep = nrep + d;                          // [d] pending buffer mean
+  double* diff = nbrep + d;                          // [d] k_t - r'
+  double* nk = diff + d;                             // [tmax]
+  int* cslot = reinterpret_cast<int*>(nk + t.tmax);  // [cmax]
+  int8_t* chot = reinterpret_cast<int8_t*>(cslot + cmax);  // [cmax] hot index or -1
+  uint8_t* cbuf = reinterpret_cast<uint8_t*>(chot + cmax);  // [cmax]
+  uint8_t* touched = cbuf + cmax;                            // [cmax]
 
   const int dom = a.active[blockIdx.x];
   const int T = a.T;
@@ -237,15 +427,24 @@ __global__ void __launch_bounds__(32) k_resolve(DevTables t, IngestArgs a) {
     cslot[c] = a.cand_slot[static_cast<int64_t>(dom) * cmax + c];
     cbuf[c] = a.cand_buf[static_cast<int64_t>(dom) * cmax + c];
     touched[c] = 0;
+    chot[c] = -1;
   }
+  if (lane == 0) {
+    S.nhot = 0;
+    S.npool = a.dom_pool_n[dom];
+    a.stop_t[dom] = T;
+    a.stop_kind[dom] = EV_NONE;
+    a.stop_slot[dom] = -1;
+  }
+  if (lane < POOL) S.pool[lane] = a.dom_pool[dom * POOL + lane];
   const void* fk = a.fk;
   const uint8_t* fkb = static_cast<const uint8_t*>(a.fk);
   const uint8_t* fvb = static_cast<const uint8_t*>(a.fv);
   const int rb = d * t.es;
-  // |k_t| for every remaining token (vecmath.hpp:35-40), one sequential chain per lane
-  for (int tt = cur + lane; tt < T; tt += 32) {
+  for (int tt = cur + lane; tt < T; tt += 32) {  // |k_t| (vecmath.hpp:35-40)
     double s = 0.0;
     const int64_t base = (static_cast<int64_t>(dom) * t.tmax + tt) * d;
+#pragma unroll 8
     for (int i = 0; i < d; ++i) {
       const double x = static_cast<double>(ld_kv(fk, base + i, t.kv_bf16));
       s = dadd(s, dmul(x, x));
@@ -253,13 +452,18 @@ __global__ void __launch_bounds__(32) k_resolve(DevTables t, IngestArgs a) {
     nk[tt] = __dsqrt_rn(s);
   }
   __syncwarp();
-  if (lane == 0) {
-    a.stop_t[dom] = T;
-    a.stop_kind[dom] = EV_NONE;
-    a.stop_slot[dom] = -1;
+  int n_exact = 0;
+  bool stopped = false;
+  if (cur >= T) goto done;
+  if (n == 0) {  // maintainer.cpp:93-94: empty partition layer -> host seeds a cluster
+    if (lane == 0) {
+      a.stop_t[dom] = cur;
+      a.stop_kind[dom] = EV_SEED;
+    }
+    goto done;
   }
-  if (cur < T) {  // a degenerate representative throws at the first cosine (vecmath.hpp:59)
-    bool bad = false;
+  {
+    bool bad = false;  // a degenerate representative throws at its first cosine (vecmath.hpp:59)
     for (int c = lane; c < n; c += 32) {
       const int s = cslot[c];
       if ((cbuf[c] ? t.bnorm[s] : t.rnorm[s]) < 1e-12) bad = true;
@@ -269,187 +473,306 @@ __global__ void __launch_bounds__(32) k_resolve(DevTables t, IngestArgs a) {
         set_err(t, DERR_DEGENERATE);
         a.stop_t[dom] = cur;
       }
-      return;
+      goto done;
     }
   }
-  int n_exact = 0;
-  const float margin2 = 2.f * a.margin;
-  for (int tt = cur; tt < T; ++tt) {
-    const int64_t frow = static_cast<int64_t>(dom) * t.tmax + tt;
-    for (int i = lane; i < d; i += 32) keyf[i] = ld_kv(fk, frow * d + i, t.kv_bf16);
-    __syncwarp();
-    const double nkt = nk[tt];
-    if (n == 0) {  // maintainer.cpp:93-94
-      if (lane == 0) {
-        a.stop_t[dom] = tt;
-        a.stop_kind[dom] = EV_SEED;
-      }
-      break;
-    }
-    if (nkt < 1e-12) {
-      if (lane == 0) {
-        set_err(t, DERR_DEGENERATE);
-        a.stop_t[dom] = tt;
-      }
-      break;
-    }
-    // (1) best approximate score among untouched candidates
-    const float* ap = a.approx + frow * cmax;
-    float ba = -FLT_MAX;
-    for (int c = lane; c < n; c += 32)
-      if (!touched[c]) ba = fmaxf(ba, ap[c]);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) ba = fmaxf(ba, __shfl_xor_sync(kFull, ba, o));
-    const float thr = ba - margin2;
-    // (2) relevant candidates
-    int nrel = 0;
-    for (int c0 = 0; c0 < n; c0 += 32) {
-      const int c = c0 + lane;
-      const bool f = c < n && (touched[c] || ap[c] >= thr);
-      const unsigned m = __ballot_sync(kFull, f);
-      if (f) rel[nrel + __popc(m & ((1u << lane) - 1))] = c;
-      nrel += __popc(m);
-    }
-    __syncwarp();
-    n_exact += nrel;
-    // (3) exact cosines (vecmath.hpp:54-61), sequential sums
-    double bs = -3.0;
-    long long bk = LLONG_MAX;
-    int bp = -1;
-    for (int r = lane; r < nrel; r += 32) {
-      const int c = rel[r];
-      const int s = cslot[c];
-      const bool ib = cbuf[c];
-      const double* rp = (ib ? t.brep64 : t.rep64) + static_cast<int64_t>(s) * d;
-      const double nr = ib ? t.bnorm[s] : t.rnorm[s];
-      double acc = 0.0;
-#pragma unroll 16
-      for (int i = 0; i < d; ++i) acc = dadd(acc, dmul(static_cast<double>(keyf[i]), rp[i]));
-      const double cs = clamp1(ddiv(acc, dmul(nkt, nr)));
-      relsim[r] = cs;
-      const long long key = 2LL * t.cid[s] + (ib ? 1 : 0);
-      if (better(cs, key, bs, bk)) {
-        bs = cs;
-        bk = key;
-        bp = r;
-      }
-    }
-    warp_best(bs, bk, bp);
-    const int bc = rel[bp];
-    const int slot = cslot[bc];
-    const bool isbuf = cbuf[bc];
-    // (4) Eq. 3/4 update into repn (not yet committed): r' = (n r + k)/(n+1)
-    const double dn = static_cast<double>(t.stat[slot]);
-    const double* rp = t.rep64 + static_cast<int64_t>(slot) * d;
+  {
+    const float margin2 = 2.f * a.margin;
+    int kb = 0;  // kd[kb] holds the key of token t
     for (int i = lane; i < d; i += 32)
-      repn[i] = ddiv(dadd(dmul(dn, rp[i]), static_cast<double>(keyf[i])), dadd(dn, 1.0));
-    // buffer running mean if the entry parks in the buffer (index.cpp:181-188); computed for
-    // every branch (cheap) so BUFJOIN and DEFER -- including DEFER onto an already-lazy
-    // cluster, whose buffer is non-empty -- share it
-    const int nb = t.nbuf[slot];
-    {
-      const double dnb = static_cast<double>(nb);
-      const double* bp2 = t.brep64 + static_cast<int64_t>(slot) * d;
-      for (int i = lane; i < d; i += 32)
-        bufn[i] = nb == 0 ? static_cast<double>(keyf[i])
-                          : ddiv(dadd(dmul(dnb, bp2[i]), static_cast<double>(keyf[i])), dadd(dnb, 1.0));
-    }
+      kd[i] = static_cast<double>(ld_kv(fk, (static_cast<int64_t>(dom) * t.tmax + cur) * d + i, t.kv_bf16));
     __syncwarp();
-    // sequential chains: lane 0 sq_dist(k, r') (vecmath.hpp:42-51), lane 1 |r'|, lane 2 |buf'|
-    double chain = 0.0;
-    if (lane == 0) {
-      for (int i = 0; i < d; ++i) {
-        const double df = dsub(static_cast<double>(keyf[i]), repn[i]);
-        chain = dadd(chain, dmul(df, df));
-      }
-    } else if (lane == 1) {
-      for (int i = 0; i < d; ++i) chain = dadd(chain, dmul(repn[i], repn[i]));
-      chain = __dsqrt_rn(chain);
-    } else if (lane == 2) {
-      for (int i = 0; i < d; ++i) chain = dadd(chain, dmul(bufn[i], bufn[i]));
-      chain = __dsqrt_rn(chain);
-    }
-    const double sq = __shfl_sync(kFull, chain, 0);
-    const double rn = __shfl_sync(kFull, chain, 1);
-    const double bn = __shfl_sync(kFull, chain, 2);
-    const double varn = ddiv(dadd(dmul(dn, t.var[slot]), sq), dadd(dn, 1.0));
 
-    int kind;
-    if (isbuf) {
-      kind = EV_BUFJOIN;
-    } else {
-      const int64_t npre = t.nmem[slot];
-      const double tau = t.tau_tab[npre < t.tau_len ? npre : t.tau_len - 1];
-      if (varn <= tau)
-        kind = EV_ABSORB;
-      else if (t.resid[slot] == 0)
-        kind = EV_SPLIT;
-      else if (a.defer)
-        kind = EV_DEFER;
-      else
-        kind = EV_EAGER;
-    }
-    if (kind == EV_SPLIT || kind == EV_EAGER) {  // host slow path; nothing committed
-      if (lane == 0) {
-        a.stop_t[dom] = tt;
-        a.stop_kind[dom] = kind;
-        a.stop_slot[dom] = slot;
+    // Builds the entry list of token tn. The winner w of the previous token (or -1) may have a
+    // pending state; wlive/wbuf_pending/fresh describe which variants are needed.
+    auto build_entries = [&](int tn, int w_slot, bool w_isbuf, bool fresh_possible, int w_h) {
+      const int64_t o = static_cast<int64_t>(dom) * t.tmax + tn;
+      // best untouched approximate value among the top-M
+      float bu = -INFINITY;
+      bool found = false;
+      for (int r = 0; r < TOPM; ++r) {
+        const int c = a.topm_idx[o * TOPM + r];
+        if (c < 0) break;
+        if (!touched[c]) {
+          bu = a.topm_val[o * TOPM + r];
+          found = true;
+          break;
+        }
       }
-      break;
-    }
-    // commit statistics
-    double* rw = t.rep64 + static_cast<int64_t>(slot) * d;
-    float* rw32 = t.rep32 + static_cast<int64_t>(slot) * d;
-    for (int i = lane; i < d; i += 32) {
-      rw[i] = repn[i];
-      rw32[i] = static_cast<float>(repn[i]);
-    }
-    if (lane == 0) {
-      t.rnorm[slot] = rn;
-      t.var[slot] = varn;
-      t.stat[slot] += 1;
-    }
-    const uint8_t* srck = fkb + frow * rb;
-    const uint8_t* srcv = fvb + frow * rb;
-    if (kind == EV_ABSORB) {
-      warp_append(t, slot, false, srck, srcv);
-      if (lane == 0) t.nmem[slot] += 1;
-    } else {  // BUFJOIN / DEFER: entry parks in the buffer
-      double* bw = t.brep64 + static_cast<int64_t>(slot) * d;
-      float* bw32 = t.brep32 + static_cast<int64_t>(slot) * d;
+      const float thr = bu - margin2;
+      const bool complete = found && !(a.topm_next[o] >= thr);
+      if (lane == 0) S.ne = 0;
+      __syncwarp();
+      auto add = [&](int c, int var, const double* ptr, double nr, long long key) {
+        const int k = atomicAdd(&S.ne, 1);
+        if (k < RELMAX) {
+          S.e_cand[k] = c;
+          S.e_var[k] = static_cast<uint8_t>(var);
+          S.e_ptr[k] = ptr;
+          S.e_nr[k] = nr;
+          S.e_key[k] = key;
+        } else {
+          set_err(t, DERR_CANDIDATES);
+        }
+      };
+      for (int c = lane; c < n; c += 32) {
+        const int s = cslot[c];
+        const bool ib = cbuf[c];
+        const long long key = 2LL * t.cid[s] + (ib ? 1 : 0);
+        if (touched[c] || s == w_slot) {
+          const int h = chot[c];
+          if (s == w_slot) {
+            if (!ib) {
+              add(c, 1, nrep, 0.0, key);
+            } else if (w_isbuf) {
+              add(c, 1, nbrep, 0.0, key);
+            } else {  // live winner with a registered buffer: ABSORB keeps it, DEFER moves it
+              add(c, 0, hbrep + w_h * d, S.hbn[w_h], key);
+              add(c, 1, nbrep, 0.0, key);
+            }
+          } else if (h >= 0) {
+            add(c, 0, (ib ? hbrep : hrep) + h * d, ib ? S.hbn[h] : S.hrn[h], key);
+          } else {
+            add(c, 0, (ib ? t.brep64 : t.rep64) + static_cast<int64_t>(s) * d, ib ? t.bnorm[s] : t.rnorm[s], key);
+          }
+        } else {
+          const float v = a.approx[o * cmax + c];
+          if (!complete ? v >= thr || !found : false) {
+            add(c, 0, (ib ? t.brep64 : t.rep64) + static_cast<int64_t>(s) * d, ib ? t.bnorm[s] : t.rnorm[s], key);
+          }
+        }
+      }
+      if (complete) {  // the untouched relevant candidates are inside the top-M list
+        for (int r = lane; r < TOPM; r += 32) {
+          const int c = a.topm_idx[o * TOPM + r];
+          if (c < 0 || touched[c] || cslot[c] == w_slot) continue;
+          if (a.topm_val[o * TOPM + r] >= thr) {
+            const int s = cslot[c];
+            const bool ib = cbuf[c];
+            add(c, 0, (ib ? t.brep64 : t.rep64) + static_cast<int64_t>(s) * d, ib ? t.bnorm[s] : t.rnorm[s],
+                2LL * t.cid[s] + (ib ? 1 : 0));
+          }
+        }
+      }
+      if (fresh_possible && lane == 0)  // the buffer a DEFER would register (index.cpp:153-160)
+        add(-2, 2, nbrep, 0.0, 2LL * S.hcid[w_h] + 1);
+      __syncwarp();
+    };
+
+    // exact dots of the entries against the key in kd[kn]; with `with_specials` the top three
+    // lanes of the first pass run the token-t chains |buf'|^2, |r'|^2 and sq_dist(k_t, r')
+    auto chain_phase = [&](int kn, bool with_specials, double& sq, double& rn, double& bn) {
+      const int ne = min(S.ne, RELMAX);
+      const double* kq = kd + kn * d;
+      const int dot_lanes0 = with_specials ? 32 - SPECIAL_LANES : 32;
+      sq = rn = bn = 0.0;
+      int base = 0;
+      for (int pass = 0;; ++pass) {
+        const int lanes_here = pass == 0 ? dot_lanes0 : 32;
+        const bool specials = pass == 0 && with_specials;
+        if (base >= ne && !specials) break;
+        const double* A = nullptr;
+        const double* B = nullptr;
+        int e = -1;
+        if (lane < lanes_here && base + lane < ne) {
+          e = base + lane;
+          A = kq;
+          B = S.e_ptr[e];
+        } else if (specials && lane >= dot_lanes0) {
+          const int sp = lane - dot_lanes0;  // 0 buf', 1 r', 2 k - r'
+          A = sp == 0 ? nbrep : (sp == 1 ? nrep : diff);
+          B = A;
+        }
+        double acc = 0.0;
+        if (A) {
+#pragma unroll 16
+          for (int i = 0; i < d; ++i) acc = dadd(acc, dmul(A[i], B[i]));
+        }
+        if (e >= 0) S.e_dot[e] = acc;
+        if (specials) {
+          bn = __dsqrt_rn(__shfl_sync(kFull, acc, dot_lanes0));
+          rn = __dsqrt_rn(__shfl_sync(kFull, acc, dot_lanes0 + 1));
+          sq = __shfl_sync(kFull, acc, dot_lanes0 + 2);
+        }
+        base += lanes_here;
+        if (base >= ne) break;
+      }
+      __syncwarp();
+      n_exact += ne;
+    };
+
+    double sq = 0.0, rn = 0.0, bn = 0.0;
+    build_entries(cur, -1, false, false, 0);
+    chain_phase(kb, false, sq, rn, bn);
+    // entry validity / norms are resolved when the winner's branch is known
+    for (int tt = cur; tt < T; ++tt) {
+      const double nkt = nk[tt];
+      if (nkt < 1e-12) {
+        if (lane == 0) {
+          set_err(t, DERR_DEGENERATE);
+          a.stop_t[dom] = tt;
+        }
+        stopped = true;
+        break;
+      }
+      // ---- argmax(tt) over the entries (CandidateRef order tie-break)
+      double bs = -3.0;
+      long long bk = LLONG_MAX;
+      int bp = -1;
+      for (int e = lane; e < min(S.ne, RELMAX); e += 32) {
+        if (S.e_var[e] == 0xff) continue;  // invalidated variant
+        const double nr = S.e_nr[e];
+        if (nr < 1e-12) set_err(t, DERR_DEGENERATE);
+        const double cs = clamp1(ddiv(S.e_dot[e], dmul(nkt, nr)));
+        if (better(cs, S.e_key[e], bs, bk)) {
+          bs = cs;
+          bk = S.e_key[e];
+          bp = e;
+        }
+      }
+      warp_best(bs, bk, bp);
+      const int bc = S.e_cand[bp];
+      const int w = cslot[bc];
+      const bool isbuf = cbuf[bc];
+      // ---- winner state in the hot cache
+      int h = -1;
+      for (int i = 0; i < S.nhot; ++i)
+        if (S.hslot[i] == w) h = i;
+      if (h < 0) {
+        if (S.nhot == HOT) {  // flush: keep "touched" marks, drop the cache
+          for (int i = 0; i < HOT; ++i) hot_writeback(t, S, hrep, hbrep, i);
+          for (int c = lane; c < n; c += 32) chot[c] = -1;
+          if (lane == 0) S.nhot = 0;
+          __syncwarp();
+        }
+        h = hot_load(t, S, hrep, hbrep, w);
+      }
+      // ---- Eq. 3/4 into pending buffers (maintainer.cpp:16-25, index.cpp:181-188)
+      const double* kt = kd + kb * d;
+      const double dn = static_cast<double>(S.hstat[h]);
+      const int nb = S.hnbuf[h];
+      const double dnb = static_cast<double>(nb);
       for (int i = lane; i < d; i += 32) {
-        bw[i] = bufn[i];
-        bw32[i] = static_cast<float>(bufn[i]);
+        const double r = ddiv(dadd(dmul(dn, hrep[h * d + i]), kt[i]), dadd(dn, 1.0));
+        nrep[i] = r;
+        diff[i] = dsub(kt[i], r);
+        nbrep[i] = nb == 0 ? kt[i] : ddiv(dadd(dmul(dnb, hbrep[h * d + i]), kt[i]), dadd(dnb, 1.0));
+      }
+      // mark the winner touched / hot before the next token's entries are chosen
+      for (int c = lane; c < n; c += 32)
+        if (cslot[c] == w) {
+          touched[c] = 1;
+          chot[c] = static_cast<int8_t>(h);
+        }
+      const bool has_next = tt + 1 < T;
+      const bool fresh_possible = !isbuf && S.hresid[h] != 0 && a.defer && nb == 0;
+      if (has_next) {
+        for (int i = lane; i < d; i += 32)
+          kd[(kb ^ 1) * d + i] =
+              static_cast<double>(ld_kv(fk, (static_cast<int64_t>(dom) * t.tmax + tt + 1) * d + i, t.kv_bf16));
+      }
+      __syncwarp();
+      if (has_next) {
+        build_entries(tt + 1, w, isbuf, fresh_possible, h);
+      } else if (lane == 0) {
+        S.ne = 0;
+      }
+      __syncwarp();
+      chain_phase(kb ^ 1, true, sq, rn, bn);
+      const double varn = ddiv(dadd(dmul(dn, S.hvar[h]), sq), dadd(dn, 1.0));
+      int kind;
+      if (isbuf) {
+        kind = EV_BUFJOIN;
+      } else {
+        const int64_t npre = S.hnmem[h];
+        const double tau = t.tau_tab[npre < t.tau_len ? npre : t.tau_len - 1];
+        if (varn <= tau)
+          kind = EV_ABSORB;
+        else if (S.hresid[h] == 0)
+          kind = EV_SPLIT;
+        else if (a.defer)
+          kind = EV_DEFER;
+        else
+          kind = EV_EAGER;
+      }
+      if (kind == EV_SPLIT || kind == EV_EAGER) {  // host slow path; nothing committed
+        if (lane == 0) {
+          a.stop_t[dom] = tt;
+          a.stop_kind[dom] = kind;
+          a.stop_slot[dom] = w;
+        }
+        stopped = true;
+        break;
+      }
+      // ---- resolve the pending variants of the next token's entries
+      const bool buf_moved = kind == EV_BUFJOIN || kind == EV_DEFER;
+      for (int e = lane; e < min(S.ne, RELMAX); e += 32) {
+        if (S.e_var[e] == 1) {
+          const bool ib = S.e_cand[e] >= 0 && cbuf[S.e_cand[e]];
+          if (ib && !buf_moved) {
+            S.e_var[e] = 0xff;
+          } else {
+            S.e_nr[e] = ib ? bn : rn;
+          }
+        } else if (S.e_var[e] == 0 && S.e_cand[e] >= 0 && cslot[S.e_cand[e]] == w && cbuf[S.e_cand[e]] && buf_moved) {
+          S.e_var[e] = 0xff;  // old buffer state superseded
+        } else if (S.e_var[e] == 2) {
+          if (kind == EV_DEFER && nb == 0) {
+            S.e_cand[e] = n;  // the new candidate index (registered below)
+            S.e_nr[e] = bn;
+          } else {
+            S.e_var[e] = 0xff;
+          }
+        }
+      }
+      // ---- commit
+      for (int i = lane; i < d; i += 32) {
+        hrep[h * d + i] = nrep[i];
+        if (buf_moved) hbrep[h * d + i] = nbrep[i];
       }
       if (lane == 0) {
-        t.bnorm[slot] = bn;
-        if (kind == EV_DEFER) t.lazy[slot] = 1;
+        S.hrn[h] = rn;
+        S.hvar[h] = varn;
+        S.hstat[h] += 1;
+        if (kind == EV_ABSORB) S.hnmem[h] += 1;
+        if (buf_moved) {
+          S.hbn[h] = bn;
+          S.hnbuf[h] = nb + 1;
+        }
+        if (kind == EV_DEFER) S.hlazy[h] = 1;
+        const int64_t frow = static_cast<int64_t>(dom) * t.tmax + tt;
+        a.ev_kind[frow] = kind;
+        a.ev_slot[frow] = w;
+        t.ring_owner[(static_cast<int64_t>(dom) * t.W + a.ring_slot) * t.tmax + tt] = w;
       }
-      warp_append(t, slot, true, srck, srcv);
-      if (lane == 0) t.nbuf[slot] = nb + 1;
-    }
-    if (lane == 0) {
-      a.ev_kind[frow] = kind;
-      a.ev_slot[frow] = slot;
-      t.ring_owner[(static_cast<int64_t>(dom) * t.W + a.ring_slot) * t.tmax + tt] = slot;
-    }
-    // the winner's representative moved: every candidate of this slot is now "touched"
-    for (int c = lane; c < n; c += 32)
-      if (cslot[c] == slot) touched[c] = 1;
-    const bool fresh_buffer = kind == EV_DEFER && nb == 0;
-    if (fresh_buffer && lane == 0) {  // register the new buffer candidate (index.cpp:153-160)
-      if (n < cmax) {
-        cslot[n] = slot;
-        cbuf[n] = 1;
-        touched[n] = 1;
-      } else {
-        set_err(t, DERR_CANDIDATES);
+      {
+        const int64_t frow = static_cast<int64_t>(dom) * t.tmax + tt;
+        hot_append(t, S, h, buf_moved, fkb + frow * rb, fvb + frow * rb);
       }
+      if (kind == EV_DEFER && nb == 0 && lane == 0) {  // register the new buffer candidate
+        if (n < cmax) {
+          cslot[n] = w;
+          cbuf[n] = 1;
+          touched[n] = 1;
+          chot[n] = static_cast<int8_t>(h);
+        } else {
+          set_err(t, DERR_CANDIDATES);
+        }
+      }
+      if (kind == EV_DEFER && nb == 0) n = min(n + 1, cmax);
+      kb ^= 1;
+      __syncwarp();
     }
-    if (fresh_buffer) n = min(n + 1, cmax);
-    __syncwarp();
   }
-  if (lane == 0) a.n_exact[dom] = n_exact;
+done:
+  __syncwarp();
+  for (int i = 0; i < S.nhot; ++i) hot_writeback(t, S, hrep, hbrep, i);
+  if (lane < POOL) a.dom_pool[dom * POOL + lane] = S.pool[lane];
+  if (lane == 0) {
+    a.dom_pool_n[dom] = S.npool;
+    a.n_exact[dom] = n_exact;
+  }
+  (void)stopped;
 }
 
 // ============================================================================ ring write
@@ -1256,14 +1579,25 @@ int launch_approx(const DevTables& t, const IngestArgs& a, cudaStream_t st) {
 }
 
 int launch_resolve(const DevTables& t, const IngestArgs& a, cudaStream_t st) {
-  const size_t smem = static_cast<size_t>(t.tmax) * 8 + 2 * t.d * 8 + static_cast<size_t>(t.cmax) * 8 +
-                      t.d * 4 + static_cast<size_t>(t.cmax) * 4 * 2 + static_cast<size_t>(t.cmax) * 2 + 64;
+  const size_t smem = static_cast<size_t>(HOT) * 2 * t.d * 8 + static_cast<size_t>(5) * t.d * 8 +
+                      static_cast<size_t>(t.tmax) * 8 + static_cast<size_t>(t.cmax) * (4 + 3) + 64;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_resolve, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
   k_resolve<<<a.n_active, 32, smem, st>>>(t, a);
+  return 1;
+}
+
+int launch_topm(const DevTables& t, const IngestArgs& a, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_topm, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  dim3 g((a.T + 7) / 8, a.n_active);
+  k_topm<<<g, 256, static_cast<size_t>(8) * t.cmax * 4, st>>>(t, a);
   return 1;
 }
 

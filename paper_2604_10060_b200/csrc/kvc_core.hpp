@@ -128,7 +128,17 @@ struct IngestArgs {
   int32_t* stop_kind;      // [L]
   int32_t* stop_slot;      // [L]
   int32_t* n_exact;        // [L] exact re-scores performed (instrumentation)
+  // per-token approximate top-M (K1b): candidate index, value, and the (M+1)-th value
+  int16_t* topm_idx;       // [L][tmax][TOPM]
+  float* topm_val;         // [L][tmax][TOPM]
+  float* topm_next;        // [L][tmax]
+  // per-domain reserve of free pages carried between resolve launches (no pushes to the
+  // shared free stack while pops may run concurrently)
+  int32_t* dom_pool;       // [L][POOL]
+  int32_t* dom_pool_n;     // [L]
 };
+constexpr int TOPM = 8;
+constexpr int POOL = 16;
 
 // ----------------------------------------------------------------------------- decode
 struct DecodeArgs {
@@ -167,6 +177,7 @@ struct DecodeArgs {
 int launch_build_cands(const DevTables& t, const IngestArgs& a, cudaStream_t st);
 int launch_approx(const DevTables& t, const IngestArgs& a, cudaStream_t st);
 int launch_resolve(const DevTables& t, const IngestArgs& a, cudaStream_t st);
+int launch_topm(const DevTables& t, const IngestArgs& a, cudaStream_t st);
 int launch_ring_write(const DevTables& t, const void* fk, const void* fv, int32_t T,
                       int32_t ring_slot, cudaStream_t st);
 int launch_decode(const DevTables& t, const DecodeArgs& a, cudaStream_t st, cudaEvent_t* ev);
