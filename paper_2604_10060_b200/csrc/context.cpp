@@ -209,6 +209,9 @@ void Context::alloc_device() {
   ia_.topm_idx = static_cast<std::int16_t*>(dalloc(L * t_.tmax * TOPM * 2));
   ia_.topm_val = static_cast<float*>(dalloc(L * t_.tmax * TOPM * 4));
   ia_.topm_next = static_cast<float*>(dalloc(L * t_.tmax * 4));
+  ia_.topm_exact = static_cast<double*>(dalloc(L * t_.tmax * TOPM * 8));
+  ia_.ev_page = static_cast<std::int32_t*>(dalloc(L * t_.tmax * 4));
+  ia_.ev_row = static_cast<std::int32_t*>(dalloc(L * t_.tmax * 4));
   ia_.dom_pool = static_cast<std::int32_t*>(dalloc(L * POOL * 4));
   ia_.dom_pool_n = static_cast<std::int32_t*>(dalloc(L * 4));
   d_active_ = static_cast<std::int32_t*>(dalloc(L * 4 * 2));
@@ -756,6 +759,7 @@ void Context::run_inserts(std::int64_t frame_id, std::int64_t pid, int T, std::i
       launches_ += launch_approx(t_, ia_, st_);
       launches_ += launch_topm(t_, ia_, st_);
       launches_ += launch_resolve(t_, ia_, st_);
+      launches_ += launch_store_rows(t_, ia_, st_);
       KVC_CUDA(cudaMemcpyAsync(h_evk_, ia_.ev_kind, static_cast<std::size_t>(L_) * t_.tmax * 4, cudaMemcpyDeviceToHost, st_));
       KVC_CUDA(cudaMemcpyAsync(h_evs_, ia_.ev_slot, static_cast<std::size_t>(L_) * t_.tmax * 4, cudaMemcpyDeviceToHost, st_));
       KVC_CUDA(cudaMemcpyAsync(h_stop_, ia_.stop_t, static_cast<std::size_t>(L_) * 12, cudaMemcpyDeviceToHost, st_));
@@ -769,21 +773,26 @@ void Context::run_inserts(std::int64_t frame_id, std::int64_t pid, int T, std::i
     const std::int32_t* evk = h_evk_ + static_cast<std::size_t>(l) * t_.tmax;
     const std::int32_t* evs = h_evs_ + static_cast<std::size_t>(l) * t_.tmax;
     std::int32_t* owner = &ring_owner_h_[(static_cast<std::size_t>(l) * t_.W + ring_slot) * t_.tmax];
+    std::int64_t last_cid = -1;
     for (int t = replayed[static_cast<std::size_t>(l)]; t < stop; ++t) {
       const std::int32_t slot = evs[t];
       const std::int64_t cid = slot_id_[static_cast<std::size_t>(slot)];
-      Cluster& c = C(cid);
+      Cluster& c = *clusters_[static_cast<std::size_t>(cid)];
       mstats_[0] += 1;  // inserts
       c.stat_count += 1;
       c.last_touch = std::max(c.last_touch, frame_id);
-      frame_add(frame_id, cid);
+      if (cid != last_cid) {  // consecutive tokens mostly share a cluster
+        frame_add(frame_id, cid);
+        last_cid = cid;
+      }
       owner[t] = slot;
       switch (evk[t]) {
         case EV_ABSORB:  // add_member + note_device_append (index.cpp:170-175, store.cpp:132-137)
           c.members.push_back({frame_id, t});
           if (c.host) c.device_tail += 1;
           device_entries_ += 1;
-          touch(cid);
+          c.tracked = true;  // touch (store.cpp:139-141)
+          c.last_use = tick_++;
           mstats_[1] += 1;
           break;
         case EV_BUFJOIN:  // add_to_buffer + note_device_buffer_append

@@ -212,20 +212,24 @@ __global__ void __launch_bounds__(256) k_approx(DevTables t, IngestArgs a) {
 }
 
 // ============================================================================ K1b
-// Per (domain, token): the TOPM best approximate candidates and the (TOPM+1)-th value, so the
-// sequential resolve reads a few values per token instead of a full row. One warp per token.
+// Per (domain, token): the TOPM best approximate candidates, the (TOPM+1)-th value, and the
+// EXACT cosine of each of those TOPM candidates against the launch-time representative -- valid
+// for as long as the candidate stays untouched, so the sequential resolve rarely needs a
+// global-memory chain. One warp per token.
 __global__ void __launch_bounds__(256) k_topm(DevTables t, IngestArgs a) {
   extern __shared__ float rowsm[];  // [8 warps][cmax]
   const int dom = a.active[blockIdx.y];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tt = blockIdx.x * 8 + warp;
-  if (tt >= a.T) return;
+  if (tt >= a.T || tt < a.cursor[dom]) return;
   const int n = a.cand_n[dom];
+  const int d = t.d;
   float* row = rowsm + warp * t.cmax;
   const float* src = a.approx + (static_cast<int64_t>(dom) * t.tmax + tt) * t.cmax;
   for (int c = lane; c < n; c += 32) row[c] = src[c];
   __syncwarp();
   const int64_t o = (static_cast<int64_t>(dom) * t.tmax + tt);
+  int my_c = -1;  // lane r < TOPM keeps the r-th candidate
   for (int r = 0; r <= TOPM; ++r) {
     float bv = -INFINITY;
     int bi = -1;
@@ -243,6 +247,7 @@ __global__ void __launch_bounds__(256) k_topm(DevTables t, IngestArgs a) {
         bi = oi;
       }
     }
+    if (lane == r) my_c = bi;
     if (lane == 0) {
       if (r < TOPM) {
         a.topm_idx[o * TOPM + r] = static_cast<int16_t>(bi);
@@ -254,37 +259,60 @@ __global__ void __launch_bounds__(256) k_topm(DevTables t, IngestArgs a) {
     if (bi >= 0 && lane == (bi & 31)) row[bi] = -INFINITY;
     __syncwarp();
   }
+  // exact cosines: lanes 0..TOPM-1 one candidate each, lane TOPM the key norm
+  const int64_t kbase = o * d;
+  double acc = 0.0, nr = 1.0;
+  if (lane < TOPM && my_c >= 0) {
+    const int s = a.cand_slot[static_cast<int64_t>(dom) * t.cmax + my_c];
+    const bool ib = a.cand_buf[static_cast<int64_t>(dom) * t.cmax + my_c];
+    const double* rp = (ib ? t.brep64 : t.rep64) + static_cast<int64_t>(s) * d;
+    nr = ib ? t.bnorm[s] : t.rnorm[s];
+#pragma unroll 16
+    for (int i = 0; i < d; ++i) acc = dadd(acc, dmul(static_cast<double>(ld_kv(a.fk, kbase + i, t.kv_bf16)), rp[i]));
+  } else if (lane == TOPM) {
+#pragma unroll 16
+    for (int i = 0; i < d; ++i) {
+      const double x = static_cast<double>(ld_kv(a.fk, kbase + i, t.kv_bf16));
+      acc = dadd(acc, dmul(x, x));
+    }
+    acc = __dsqrt_rn(acc);
+  }
+  const double nk = __shfl_sync(kFull, acc, TOPM);
+  if (lane < TOPM) a.topm_exact[o * TOPM + lane] = my_c >= 0 ? clamp1(ddiv(acc, dmul(nk, nr))) : -3.0;
 }
 
 // ============================================================================ K2
 // One warp per domain: the sequential on_insert chain of the frame (maintainer.cpp:88-176),
 // exact in fp64. Per token t:
-//   argmax(t) over exact cosines computed in the previous chain phase,
-//   Eq. 3/4 update of the winner into pending buffers (elementwise),
-//   ONE chain phase where every lane runs a 128-long sequential fp64 sum: the sq_dist(k_t, r')
-//   (vecmath.hpp:42-51), |r'|, |buf'| for token t, and the exact dots of token t+1 against every
-//   candidate it could pick (touched clusters + untouched ones within 2*margin of the best
-//   untouched approximate score),
-//   Eq. 5 decision for t, commit.
-// Winner state is cached in shared memory (HOT entries), pages come from a per-domain pool.
-constexpr int HOT = 16;
+//   argmax(t) over exact cosines (precomputed for untouched top-M candidates by K1b, computed
+//   in the previous chain phase for clusters touched earlier in this launch),
+//   Eq. 3/4 update of the winner into pending shared buffers (elementwise),
+//   ONE chain phase in which each lane runs a d-long sequential fp64 sum out of shared memory:
+//   sq_dist(k_t, r') (vecmath.hpp:42-51), |r'|, |buf'| for token t and the exact dots of token
+//   t+1 against every touched candidate (with the winner's pending state),
+//   Eq. 5 decision for t and commit; K/V rows are copied later by K3 (off the chain).
+// Winner state lives in shared memory (HOT entries); pages come from a per-domain pool.
+constexpr int HOT = 32;
 constexpr int RELMAX = 96;
+constexpr int TLMAX = 96;
 constexpr int SPECIAL_LANES = 3;
+constexpr uint8_t EV_CHAIN = 0, EV_PEND = 1, EV_FRESH = 2, EV_PRE = 3, EV_SLOW = 4, EV_DEAD = 0xff;
 
 struct ResolveShared {
-  // hot cluster state
-  int hslot[HOT];
+  int hslot[HOT], hcl[HOT], hcb[HOT];  // slot, its live / buffer candidate index (-1 none)
   double hrn[HOT], hbn[HOT], hvar[HOT];
-  long long hstat[HOT], hnmem[HOT], hcid[HOT];
+  long long hstat[HOT], hnmem[HOT];
   int hnbuf[HOT], hnp[HOT], hlast[HOT], hfill[HOT], hbnp[HOT], hblast[HOT], hbfill[HOT];
-  uint8_t hlazy[HOT], hresid[HOT];
+  uint8_t hlazy[HOT], hresid[HOT], hdirty[HOT];
   int nhot;
-  // relevant entries of the next token
-  const double* e_ptr[RELMAX];
+  int tl[TLMAX];  // touched candidate indices
+  int ntl;
+  int e_a[RELMAX], e_b[RELMAX];  // chain operands as offsets (doubles) into the shared block
+  const double* e_gptr[RELMAX];  // global representative (EV_SLOW)
   double e_nr[RELMAX], e_dot[RELMAX];
   long long e_key[RELMAX];
   int e_cand[RELMAX];
-  uint8_t e_var[RELMAX];  // 0 current state, 1 pending (winner), 2 speculative fresh buffer
+  uint8_t e_var[RELMAX];
   int ne;
   int pool[POOL];
   int npool;
@@ -292,6 +320,7 @@ struct ResolveShared {
 
 __device__ void hot_writeback(const DevTables& t, ResolveShared& S, const double* hrep,
                               const double* hbrep, int h) {
+  if (!S.hdirty[h]) return;
   const int lane = threadIdx.x & 31, d = t.d;
   const int64_t s = S.hslot[h];
   for (int i = lane; i < d; i += 32) {
@@ -319,25 +348,29 @@ __device__ void hot_writeback(const DevTables& t, ResolveShared& S, const double
   }
 }
 
-__device__ int hot_load(const DevTables& t, ResolveShared& S, double* hrep, double* hbrep, int slot) {
+// Loads a slot into the next hot entry (caller guarantees room). cl/cb: its candidate indices.
+__device__ int hot_load(const DevTables& t, ResolveShared& S, double* hrep, double* hbrep, int slot,
+                        int cl, int cb) {
   const int lane = threadIdx.x & 31, d = t.d;
   const int h = S.nhot;
-  __syncwarp();  // every lane has read nhot before lane 0 bumps it
+  __syncwarp();
   for (int i = lane; i < d; i += 32) {
     hrep[h * d + i] = t.rep64[static_cast<int64_t>(slot) * d + i];
     hbrep[h * d + i] = t.brep64[static_cast<int64_t>(slot) * d + i];
   }
   if (lane == 0) {
     S.hslot[h] = slot;
+    S.hcl[h] = cl;
+    S.hcb[h] = cb;
     S.hrn[h] = t.rnorm[slot];
     S.hbn[h] = t.bnorm[slot];
     S.hvar[h] = t.var[slot];
     S.hstat[h] = t.stat[slot];
     S.hnmem[h] = t.nmem[slot];
-    S.hcid[h] = t.cid[slot];
     S.hnbuf[h] = t.nbuf[slot];
     S.hlazy[h] = t.lazy[slot];
     S.hresid[h] = t.resid[slot];
+    S.hdirty[h] = 0;
     const int np = t.npages[slot], nbp = t.nbpages[slot];
     S.hnp[h] = np;
     S.hlast[h] = np > 0 ? t.pages[static_cast<int64_t>(slot) * t.maxp + np - 1] : -1;
@@ -351,111 +384,101 @@ __device__ int hot_load(const DevTables& t, ResolveShared& S, double* hrep, doub
   return h;
 }
 
-// append one K/V row to a hot slot's member (to_buf = 0) or buffer page list
-__device__ void hot_append(const DevTables& t, ResolveShared& S, int h, bool to_buf,
-                           const uint8_t* src_k, const uint8_t* src_v) {
-  const int lane = threadIdx.x & 31;
-  int page = -1, row = -1;
-  if (lane == 0) {
-    int& np = to_buf ? S.hbnp[h] : S.hnp[h];
-    int& last = to_buf ? S.hblast[h] : S.hlast[h];
-    int& fill = to_buf ? S.hbfill[h] : S.hfill[h];
-    if (fill >= t.P) {
-      const int cap = to_buf ? t.maxbp : t.maxp;
-      if (np >= cap) {
-        set_err(t, DERR_CLUSTER_PAGES);
-      } else {
-        if (S.npool == 0) {  // refill the domain's page pool from the shared free stack
-          const int top = atomicSub(t.free_top, POOL);
-          const int got = max(0, min(POOL, top));
-          if (got < POOL) atomicAdd(t.free_top, POOL - got);
-          for (int i = 0; i < got; ++i) S.pool[i] = t.free_stack[top - 1 - i];
-          S.npool = got;
-        }
-        if (S.npool == 0) {
-          set_err(t, DERR_PAGES);
-        } else {
-          const int pg = S.pool[--S.npool];
-          if (last >= 0) t.pg_fill[last] = t.P;
-          int* list = to_buf ? t.bpages + static_cast<int64_t>(S.hslot[h]) * t.maxbp
-                             : t.pages + static_cast<int64_t>(S.hslot[h]) * t.maxp;
-          list[np] = pg;
-          np += 1;
-          last = pg;
-          fill = 0;
-        }
-      }
+// Reserves the next row of a hot slot's member / buffer page list (lane 0 only).
+__device__ void hot_reserve_row(const DevTables& t, ResolveShared& S, int h, bool to_buf, int& page,
+                                int& row) {
+  page = -1;
+  row = -1;
+  int& np = to_buf ? S.hbnp[h] : S.hnp[h];
+  int& last = to_buf ? S.hblast[h] : S.hlast[h];
+  int& fill = to_buf ? S.hbfill[h] : S.hfill[h];
+  if (fill >= t.P || last < 0) {
+    const int cap = to_buf ? t.maxbp : t.maxp;
+    if (np >= cap) {
+      set_err(t, DERR_CLUSTER_PAGES);
+      return;
     }
-    if (fill < t.P && last >= 0) {
-      page = last;
-      row = fill++;
+    if (S.npool == 0) {  // refill from the shared free stack (pops only during resolve)
+      const int top = atomicSub(t.free_top, POOL);
+      const int got = max(0, min(POOL, top));
+      if (got < POOL) atomicAdd(t.free_top, POOL - got);
+      for (int i = 0; i < got; ++i) S.pool[i] = t.free_stack[top - 1 - i];
+      S.npool = got;
     }
+    if (S.npool == 0) {
+      set_err(t, DERR_PAGES);
+      return;
+    }
+    const int pg = S.pool[--S.npool];
+    if (last >= 0) t.pg_fill[last] = t.P;
+    int* list = to_buf ? t.bpages + static_cast<int64_t>(S.hslot[h]) * t.maxbp
+                       : t.pages + static_cast<int64_t>(S.hslot[h]) * t.maxp;
+    list[np] = pg;
+    np += 1;
+    last = pg;
+    fill = 0;
   }
-  page = __shfl_sync(kFull, page, 0);
-  row = __shfl_sync(kFull, row, 0);
-  if (page < 0) return;
-  const int rb = t.d * t.es;
-  uint8_t* dk = page_k(t, page) + static_cast<int64_t>(row) * rb;
-  uint8_t* dv = page_v(t, page) + static_cast<int64_t>(row) * rb;
-  for (int o = lane * 16; o < rb; o += 32 * 16) {
-    *reinterpret_cast<uint4*>(dk + o) = *reinterpret_cast<const uint4*>(src_k + o);
-    *reinterpret_cast<uint4*>(dv + o) = *reinterpret_cast<const uint4*>(src_v + o);
-  }
+  page = last;
+  row = fill++;
 }
 
 __global__ void __launch_bounds__(32) k_resolve(DevTables t, IngestArgs a) {
   extern __shared__ __align__(16) uint8_t smraw[];
   __shared__ ResolveShared S;
   const int d = t.d, cmax = t.cmax, lane = threadIdx.x;
-  double* hrep = reinterpret_cast<double*>(smraw);  // [HOT][d]
-  double* hbrep = hrep + HOT * d;                    // [HOT][d]
-  double* kd = hbrep + HOT * d;                      // [2][d] keys of t and t+1 (as double)
-  double* nrep = kd + 2 * d;                         // [d] pending r'
-  double* nbrep = nrep + d;                          // [d] pending buffer mean
-  double* diff = nbrep + d;                          // [d] k_t - r'
-  double* nk = diff + d;                             // [tmax]
-  int* cslot = reinterpret_cast<int*>(nk + t.tmax);  // [cmax]
-  int8_t* chot = reinterpret_cast<int8_t*>(cslot + cmax);  // [cmax] hot index or -1
-  uint8_t* cbuf = reinterpret_cast<uint8_t*>(chot + cmax);  // [cmax]
-  uint8_t* touched = cbuf + cmax;                            // [cmax]
+  double* sd = reinterpret_cast<double*>(smraw);
+  double* hrep = sd;                     // [HOT][d]
+  double* hbrep = hrep + HOT * d;        // [HOT][d]
+  double* kd = hbrep + HOT * d;          // [2][d] keys of t and t+1
+  double* nrep = kd + 2 * d;             // [d] pending r'
+  double* nbrep = nrep + d;              // [d] pending buffer mean
+  double* diff = nbrep + d;              // [d] k_t - r'
+  double* nk = diff + d;                 // [tmax]
+  long long* ckey = reinterpret_cast<long long*>(nk + t.tmax);  // [cmax] CandidateRef order key
+  int* cslot = reinterpret_cast<int*>(ckey + cmax);              // [cmax]
+  int8_t* chot = reinterpret_cast<int8_t*>(cslot + cmax);        // [cmax] hot index or -1
+  uint8_t* cbuf = reinterpret_cast<uint8_t*>(chot + cmax);       // [cmax]
+  uint8_t* touched = cbuf + cmax;                                  // [cmax]
+  const int OFF_HREP = 0, OFF_HBREP = HOT * d, OFF_KD = 2 * HOT * d, OFF_NREP = OFF_KD + 2 * d,
+            OFF_NBREP = OFF_NREP + d, OFF_DIFF = OFF_NBREP + d;
 
   const int dom = a.active[blockIdx.x];
   const int T = a.T;
   const int cur = a.cursor[dom];
   int n = a.cand_n[dom];
   for (int c = lane; c < n; c += 32) {
-    cslot[c] = a.cand_slot[static_cast<int64_t>(dom) * cmax + c];
-    cbuf[c] = a.cand_buf[static_cast<int64_t>(dom) * cmax + c];
+    const int s = a.cand_slot[static_cast<int64_t>(dom) * cmax + c];
+    const uint8_t b = a.cand_buf[static_cast<int64_t>(dom) * cmax + c];
+    cslot[c] = s;
+    cbuf[c] = b;
+    ckey[c] = 2LL * t.cid[s] + b;
     touched[c] = 0;
     chot[c] = -1;
   }
   if (lane == 0) {
     S.nhot = 0;
+    S.ntl = 0;
     S.npool = a.dom_pool_n[dom];
     a.stop_t[dom] = T;
     a.stop_kind[dom] = EV_NONE;
     a.stop_slot[dom] = -1;
   }
   if (lane < POOL) S.pool[lane] = a.dom_pool[dom * POOL + lane];
-  const void* fk = a.fk;
-  const uint8_t* fkb = static_cast<const uint8_t*>(a.fk);
-  const uint8_t* fvb = static_cast<const uint8_t*>(a.fv);
-  const int rb = d * t.es;
   for (int tt = cur + lane; tt < T; tt += 32) {  // |k_t| (vecmath.hpp:35-40)
     double s = 0.0;
     const int64_t base = (static_cast<int64_t>(dom) * t.tmax + tt) * d;
 #pragma unroll 8
     for (int i = 0; i < d; ++i) {
-      const double x = static_cast<double>(ld_kv(fk, base + i, t.kv_bf16));
+      const double x = static_cast<double>(ld_kv(a.fk, base + i, t.kv_bf16));
       s = dadd(s, dmul(x, x));
     }
     nk[tt] = __dsqrt_rn(s);
+    a.ev_page[static_cast<int64_t>(dom) * t.tmax + tt] = -1;
   }
   __syncwarp();
   int n_exact = 0;
-  bool stopped = false;
   if (cur >= T) goto done;
-  if (n == 0) {  // maintainer.cpp:93-94: empty partition layer -> host seeds a cluster
+  if (n == 0) {  // maintainer.cpp:93-94: empty partition layer -> the host seeds a cluster
     if (lane == 0) {
       a.stop_t[dom] = cur;
       a.stop_kind[dom] = EV_SEED;
@@ -480,122 +503,151 @@ __global__ void __launch_bounds__(32) k_resolve(DevTables t, IngestArgs a) {
     const float margin2 = 2.f * a.margin;
     int kb = 0;  // kd[kb] holds the key of token t
     for (int i = lane; i < d; i += 32)
-      kd[i] = static_cast<double>(ld_kv(fk, (static_cast<int64_t>(dom) * t.tmax + cur) * d + i, t.kv_bf16));
+      kd[i] = static_cast<double>(ld_kv(a.fk, (static_cast<int64_t>(dom) * t.tmax + cur) * d + i, t.kv_bf16));
+    if (lane == 0) S.ne = 0;
     __syncwarp();
 
-    // Builds the entry list of token tn. The winner w of the previous token (or -1) may have a
-    // pending state; wlive/wbuf_pending/fresh describe which variants are needed.
-    auto build_entries = [&](int tn, int w_slot, bool w_isbuf, bool fresh_possible, int w_h) {
-      const int64_t o = static_cast<int64_t>(dom) * t.tmax + tn;
-      // best untouched approximate value among the top-M
-      float bu = -INFINITY;
-      bool found = false;
-      for (int r = 0; r < TOPM; ++r) {
-        const int c = a.topm_idx[o * TOPM + r];
-        if (c < 0) break;
-        if (!touched[c]) {
-          bu = a.topm_val[o * TOPM + r];
-          found = true;
-          break;
-        }
+    auto add = [&](int c, uint8_t var, int oa, int ob, const double* g, double nr, long long key, double dot) {
+      const int k = atomicAdd(&S.ne, 1);
+      if (k < RELMAX) {
+        S.e_cand[k] = c;
+        S.e_var[k] = var;
+        S.e_a[k] = oa;
+        S.e_b[k] = ob;
+        S.e_gptr[k] = g;
+        S.e_nr[k] = nr;
+        S.e_key[k] = key;
+        S.e_dot[k] = dot;
+      } else {
+        set_err(t, DERR_CANDIDATES);
       }
-      const float thr = bu - margin2;
-      const bool complete = found && !(a.topm_next[o] >= thr);
-      if (lane == 0) S.ne = 0;
+    };
+    auto flush_hot = [&]() {
+      for (int i = 0; i < S.nhot; ++i) hot_writeback(t, S, hrep, hbrep, i);
+      for (int c = lane; c < n; c += 32) chot[c] = -1;
       __syncwarp();
-      auto add = [&](int c, int var, const double* ptr, double nr, long long key) {
-        const int k = atomicAdd(&S.ne, 1);
-        if (k < RELMAX) {
-          S.e_cand[k] = c;
-          S.e_var[k] = static_cast<uint8_t>(var);
-          S.e_ptr[k] = ptr;
-          S.e_nr[k] = nr;
-          S.e_key[k] = key;
-        } else {
-          set_err(t, DERR_CANDIDATES);
-        }
-      };
-      for (int c = lane; c < n; c += 32) {
-        const int s = cslot[c];
-        const bool ib = cbuf[c];
-        const long long key = 2LL * t.cid[s] + (ib ? 1 : 0);
-        if (touched[c] || s == w_slot) {
-          const int h = chot[c];
-          if (s == w_slot) {
-            if (!ib) {
-              add(c, 1, nrep, 0.0, key);
-            } else if (w_isbuf) {
-              add(c, 1, nbrep, 0.0, key);
-            } else {  // live winner with a registered buffer: ABSORB keeps it, DEFER moves it
-              add(c, 0, hbrep + w_h * d, S.hbn[w_h], key);
-              add(c, 1, nbrep, 0.0, key);
-            }
-          } else if (h >= 0) {
-            add(c, 0, (ib ? hbrep : hrep) + h * d, ib ? S.hbn[h] : S.hrn[h], key);
-          } else {
-            add(c, 0, (ib ? t.brep64 : t.rep64) + static_cast<int64_t>(s) * d, ib ? t.bnorm[s] : t.rnorm[s], key);
-          }
-        } else {
-          const float v = a.approx[o * cmax + c];
-          if (!complete ? v >= thr || !found : false) {
-            add(c, 0, (ib ? t.brep64 : t.rep64) + static_cast<int64_t>(s) * d, ib ? t.bnorm[s] : t.rnorm[s], key);
-          }
-        }
-      }
-      if (complete) {  // the untouched relevant candidates are inside the top-M list
-        for (int r = lane; r < TOPM; r += 32) {
-          const int c = a.topm_idx[o * TOPM + r];
-          if (c < 0 || touched[c] || cslot[c] == w_slot) continue;
-          if (a.topm_val[o * TOPM + r] >= thr) {
-            const int s = cslot[c];
-            const bool ib = cbuf[c];
-            add(c, 0, (ib ? t.brep64 : t.rep64) + static_cast<int64_t>(s) * d, ib ? t.bnorm[s] : t.rnorm[s],
-                2LL * t.cid[s] + (ib ? 1 : 0));
-          }
-        }
-      }
-      if (fresh_possible && lane == 0)  // the buffer a DEFER would register (index.cpp:153-160)
-        add(-2, 2, nbrep, 0.0, 2LL * S.hcid[w_h] + 1);
+      if (lane == 0) S.nhot = 0;
       __syncwarp();
     };
 
-    // exact dots of the entries against the key in kd[kn]; with `with_specials` the top three
-    // lanes of the first pass run the token-t chains |buf'|^2, |r'|^2 and sq_dist(k_t, r')
-    auto chain_phase = [&](int kn, bool with_specials, double& sq, double& rn, double& bn) {
+    // Entries of token tn. w: the winner of tn-1 (slot, hot index) whose statistics are pending.
+    auto build_entries = [&](int tn, int w_slot, bool w_isbuf, bool fresh_possible, int w_h) {
+      const int64_t o = static_cast<int64_t>(dom) * t.tmax + tn;
+      if (lane == 0) S.ne = 0;
+      __syncwarp();
+      // (a) touched candidates: exact chain on their current (hot or pending) state
+      for (int i = lane; i < S.ntl; i += 32) {
+        const int c = S.tl[i];
+        const int s = cslot[c];
+        const bool ib = cbuf[c];
+        const int h = chot[c];
+        if (s == w_slot) {
+          if (!ib) {
+            add(c, EV_PEND, 0, OFF_NREP, nullptr, 0.0, ckey[c], 0.0);
+          } else if (w_isbuf) {
+            add(c, EV_PEND, 0, OFF_NBREP, nullptr, 0.0, ckey[c], 0.0);
+          } else {  // live winner with a registered buffer: ABSORB keeps it, DEFER moves it
+            add(c, EV_CHAIN, 0, OFF_HBREP + w_h * d, nullptr, S.hbn[w_h], ckey[c], 0.0);
+            add(c, EV_PEND, 0, OFF_NBREP, nullptr, 0.0, ckey[c], 0.0);
+          }
+        } else if (h >= 0) {
+          add(c, EV_CHAIN, 0, (ib ? OFF_HBREP : OFF_HREP) + h * d, nullptr, ib ? S.hbn[h] : S.hrn[h], ckey[c], 0.0);
+        } else {  // touched earlier, flushed out of the cache: global state (written back)
+          add(c, EV_SLOW, 0, 0, (ib ? t.brep64 : t.rep64) + static_cast<int64_t>(s) * d,
+              ib ? t.bnorm[s] : t.rnorm[s], ckey[c], 0.0);
+        }
+      }
+      if (fresh_possible && lane == 0)  // the buffer a DEFER would register (index.cpp:153-160)
+        add(-2, EV_FRESH, 0, OFF_NBREP, nullptr, 0.0, 2LL * t.cid[w_slot] + 1, 0.0);
+      // (b) untouched candidates within 2*margin of the best untouched approximate score
+      int first_untouched = -1;
+      for (int r = 0; r < TOPM; ++r) {
+        const int c = a.topm_idx[o * TOPM + r];
+        if (c < 0) break;
+        if (!touched[c] && cslot[c] != w_slot) {
+          first_untouched = r;
+          break;
+        }
+      }
+      const float bu = first_untouched >= 0 ? a.topm_val[o * TOPM + first_untouched] : -INFINITY;
+      const float thr = bu - margin2;
+      const bool complete = first_untouched >= 0 && !(a.topm_next[o] >= thr);
+      if (complete) {
+        if (lane < TOPM) {
+          const int c = a.topm_idx[o * TOPM + lane];
+          if (c >= 0 && !touched[c] && cslot[c] != w_slot && a.topm_val[o * TOPM + lane] >= thr)
+            add(c, EV_PRE, 0, 0, nullptr, 0.0, ckey[c], a.topm_exact[o * TOPM + lane]);
+        }
+      } else {  // rare: scan the whole approximate row
+        for (int c = lane; c < n; c += 32) {
+          if (touched[c] || cslot[c] == w_slot) continue;
+          const float v = a.approx[o * cmax + c];
+          if (first_untouched < 0 || v >= thr) {
+            const int s = cslot[c];
+            const bool ib = cbuf[c];
+            add(c, EV_SLOW, 0, 0, (ib ? t.brep64 : t.rep64) + static_cast<int64_t>(s) * d,
+                ib ? t.bnorm[s] : t.rnorm[s], ckey[c], 0.0);
+          }
+        }
+      }
+      __syncwarp();
+    };
+
+    // exact dots of the chain entries against the key at offset `koff`; with `specials` the
+    // top three lanes of the first pass run |buf'|^2, |r'|^2 and sq_dist(k_t, r') for token t
+    auto chain_phase = [&](int koff, const double* kq, bool specials, double& sq, double& rn, double& bn) {
       const int ne = min(S.ne, RELMAX);
-      const double* kq = kd + kn * d;
-      const int dot_lanes0 = with_specials ? 32 - SPECIAL_LANES : 32;
+      // slow entries (global representatives): one lane each, before the shared chain
+      for (int e = lane; e < ne; e += 32)
+        if (S.e_var[e] == EV_SLOW) {
+          const double* g = S.e_gptr[e];
+          double acc = 0.0;
+#pragma unroll 16
+          for (int i = 0; i < d; ++i) acc = dadd(acc, dmul(kq[i], g[i]));
+          S.e_dot[e] = acc;
+        }
+      // compact the shared-chain entries in order
+      const int dot_lanes0 = specials ? 32 - SPECIAL_LANES : 32;
       sq = rn = bn = 0.0;
-      int base = 0;
+      int pos = 0;  // next entry to consider
       for (int pass = 0;; ++pass) {
         const int lanes_here = pass == 0 ? dot_lanes0 : 32;
-        const bool specials = pass == 0 && with_specials;
-        if (base >= ne && !specials) break;
-        const double* A = nullptr;
-        const double* B = nullptr;
-        int e = -1;
-        if (lane < lanes_here && base + lane < ne) {
-          e = base + lane;
-          A = kq;
-          B = S.e_ptr[e];
-        } else if (specials && lane >= dot_lanes0) {
-          const int sp = lane - dot_lanes0;  // 0 buf', 1 r', 2 k - r'
-          A = sp == 0 ? nbrep : (sp == 1 ? nrep : diff);
-          B = A;
+        const bool sp_pass = pass == 0 && specials;
+        // find this lane's entry: the (lane)-th chain entry at or after pos
+        int mine = -1, taken = 0, p = pos;
+        while (p < ne && taken < lanes_here) {
+          const uint8_t v = S.e_var[p];
+          if (v == EV_CHAIN || v == EV_PEND || v == EV_FRESH) {
+            if (taken == lane) mine = p;
+            ++taken;
+          }
+          ++p;
+        }
+        if (taken == 0 && !sp_pass) break;
+        int oa = -1, ob = -1;
+        if (mine >= 0) {
+          oa = koff;
+          ob = S.e_b[mine];
+        } else if (sp_pass && lane >= dot_lanes0) {
+          const int spc = lane - dot_lanes0;  // 0 buf', 1 r', 2 k - r'
+          oa = spc == 0 ? OFF_NBREP : (spc == 1 ? OFF_NREP : OFF_DIFF);
+          ob = oa;
         }
         double acc = 0.0;
-        if (A) {
+        if (oa >= 0) {
+          const double* A = sd + oa;
+          const double* B = sd + ob;
 #pragma unroll 16
           for (int i = 0; i < d; ++i) acc = dadd(acc, dmul(A[i], B[i]));
         }
-        if (e >= 0) S.e_dot[e] = acc;
-        if (specials) {
+        if (mine >= 0) S.e_dot[mine] = acc;
+        if (sp_pass) {
           bn = __dsqrt_rn(__shfl_sync(kFull, acc, dot_lanes0));
           rn = __dsqrt_rn(__shfl_sync(kFull, acc, dot_lanes0 + 1));
           sq = __shfl_sync(kFull, acc, dot_lanes0 + 2);
         }
-        base += lanes_here;
-        if (base >= ne) break;
+        pos = p;
+        if (pos >= ne) break;
       }
       __syncwarp();
       n_exact += ne;
@@ -603,8 +655,7 @@ __global__ void __launch_bounds__(32) k_resolve(DevTables t, IngestArgs a) {
 
     double sq = 0.0, rn = 0.0, bn = 0.0;
     build_entries(cur, -1, false, false, 0);
-    chain_phase(kb, false, sq, rn, bn);
-    // entry validity / norms are resolved when the winner's branch is known
+    chain_phase(OFF_KD, kd, false, sq, rn, bn);
     for (int tt = cur; tt < T; ++tt) {
       const double nkt = nk[tt];
       if (nkt < 1e-12) {
@@ -612,18 +663,23 @@ __global__ void __launch_bounds__(32) k_resolve(DevTables t, IngestArgs a) {
           set_err(t, DERR_DEGENERATE);
           a.stop_t[dom] = tt;
         }
-        stopped = true;
         break;
       }
-      // ---- argmax(tt) over the entries (CandidateRef order tie-break)
+      // ---- argmax(tt) (CandidateRef order tie-break)
       double bs = -3.0;
       long long bk = LLONG_MAX;
       int bp = -1;
       for (int e = lane; e < min(S.ne, RELMAX); e += 32) {
-        if (S.e_var[e] == 0xff) continue;  // invalidated variant
-        const double nr = S.e_nr[e];
-        if (nr < 1e-12) set_err(t, DERR_DEGENERATE);
-        const double cs = clamp1(ddiv(S.e_dot[e], dmul(nkt, nr)));
+        const uint8_t v = S.e_var[e];
+        if (v == EV_DEAD) continue;
+        double cs;
+        if (v == EV_PRE) {
+          cs = S.e_dot[e];
+        } else {
+          const double nr = S.e_nr[e];
+          if (nr < 1e-12) set_err(t, DERR_DEGENERATE);
+          cs = clamp1(ddiv(S.e_dot[e], dmul(nkt, nr)));
+        }
         if (better(cs, S.e_key[e], bs, bk)) {
           bs = cs;
           bk = S.e_key[e];
@@ -634,18 +690,36 @@ __global__ void __launch_bounds__(32) k_resolve(DevTables t, IngestArgs a) {
       const int bc = S.e_cand[bp];
       const int w = cslot[bc];
       const bool isbuf = cbuf[bc];
-      // ---- winner state in the hot cache
-      int h = -1;
-      for (int i = 0; i < S.nhot; ++i)
-        if (S.hslot[i] == w) h = i;
+      // ---- winner into the hot cache
+      int h = chot[bc];
       if (h < 0) {
-        if (S.nhot == HOT) {  // flush: keep "touched" marks, drop the cache
-          for (int i = 0; i < HOT; ++i) hot_writeback(t, S, hrep, hbrep, i);
-          for (int c = lane; c < n; c += 32) chot[c] = -1;
-          if (lane == 0) S.nhot = 0;
-          __syncwarp();
+        if (S.nhot >= HOT) flush_hot();
+        // candidate indices of the slot (live / buffer)
+        int cl = -1, cb = -1;
+        for (int c = lane; c < n; c += 32)
+          if (cslot[c] == w) {
+            if (cbuf[c]) cb = c; else cl = c;
+          }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+          cl = max(cl, __shfl_xor_sync(kFull, cl, off));
+          cb = max(cb, __shfl_xor_sync(kFull, cb, off));
         }
-        h = hot_load(t, S, hrep, hbrep, w);
+        h = hot_load(t, S, hrep, hbrep, w, cl, cb);
+        if (cl >= 0 && lane == 0) chot[cl] = static_cast<int8_t>(h);
+        if (cb >= 0 && lane == 0) chot[cb] = static_cast<int8_t>(h);
+      }
+      // mark the winner's candidates touched (they enter the touched list once)
+      if (lane == 0) {
+        const int cl = S.hcl[h], cb = S.hcb[h];
+        if (cl >= 0 && !touched[cl]) {
+          touched[cl] = 1;
+          if (S.ntl < TLMAX) S.tl[S.ntl++] = cl; else set_err(t, DERR_CANDIDATES);
+        }
+        if (cb >= 0 && !touched[cb]) {
+          touched[cb] = 1;
+          if (S.ntl < TLMAX) S.tl[S.ntl++] = cb; else set_err(t, DERR_CANDIDATES);
+        }
       }
       // ---- Eq. 3/4 into pending buffers (maintainer.cpp:16-25, index.cpp:181-188)
       const double* kt = kd + kb * d;
@@ -658,27 +732,20 @@ __global__ void __launch_bounds__(32) k_resolve(DevTables t, IngestArgs a) {
         diff[i] = dsub(kt[i], r);
         nbrep[i] = nb == 0 ? kt[i] : ddiv(dadd(dmul(dnb, hbrep[h * d + i]), kt[i]), dadd(dnb, 1.0));
       }
-      // mark the winner touched / hot before the next token's entries are chosen
-      for (int c = lane; c < n; c += 32)
-        if (cslot[c] == w) {
-          touched[c] = 1;
-          chot[c] = static_cast<int8_t>(h);
-        }
       const bool has_next = tt + 1 < T;
       const bool fresh_possible = !isbuf && S.hresid[h] != 0 && a.defer && nb == 0;
-      if (has_next) {
+      if (has_next)
         for (int i = lane; i < d; i += 32)
           kd[(kb ^ 1) * d + i] =
-              static_cast<double>(ld_kv(fk, (static_cast<int64_t>(dom) * t.tmax + tt + 1) * d + i, t.kv_bf16));
-      }
+              static_cast<double>(ld_kv(a.fk, (static_cast<int64_t>(dom) * t.tmax + tt + 1) * d + i, t.kv_bf16));
       __syncwarp();
       if (has_next) {
         build_entries(tt + 1, w, isbuf, fresh_possible, h);
-      } else if (lane == 0) {
-        S.ne = 0;
+      } else {
+        if (lane == 0) S.ne = 0;
+        __syncwarp();
       }
-      __syncwarp();
-      chain_phase(kb ^ 1, true, sq, rn, bn);
+      chain_phase(OFF_KD + (kb ^ 1) * d, kd + (kb ^ 1) * d, true, sq, rn, bn);
       const double varn = ddiv(dadd(dmul(dn, S.hvar[h]), sq), dadd(dn, 1.0));
       int kind;
       if (isbuf) {
@@ -701,27 +768,29 @@ __global__ void __launch_bounds__(32) k_resolve(DevTables t, IngestArgs a) {
           a.stop_kind[dom] = kind;
           a.stop_slot[dom] = w;
         }
-        stopped = true;
         break;
       }
       // ---- resolve the pending variants of the next token's entries
       const bool buf_moved = kind == EV_BUFJOIN || kind == EV_DEFER;
       for (int e = lane; e < min(S.ne, RELMAX); e += 32) {
-        if (S.e_var[e] == 1) {
-          const bool ib = S.e_cand[e] >= 0 && cbuf[S.e_cand[e]];
+        const uint8_t v = S.e_var[e];
+        const int c = S.e_cand[e];
+        if (v == EV_PEND) {
+          const bool ib = cbuf[c];
           if (ib && !buf_moved) {
-            S.e_var[e] = 0xff;
+            S.e_var[e] = EV_DEAD;
           } else {
             S.e_nr[e] = ib ? bn : rn;
           }
-        } else if (S.e_var[e] == 0 && S.e_cand[e] >= 0 && cslot[S.e_cand[e]] == w && cbuf[S.e_cand[e]] && buf_moved) {
-          S.e_var[e] = 0xff;  // old buffer state superseded
-        } else if (S.e_var[e] == 2) {
+        } else if (v == EV_CHAIN && c >= 0 && cslot[c] == w && cbuf[c] && buf_moved) {
+          S.e_var[e] = EV_DEAD;  // old buffer state superseded
+        } else if (v == EV_FRESH) {
           if (kind == EV_DEFER && nb == 0) {
             S.e_cand[e] = n;  // the new candidate index (registered below)
             S.e_nr[e] = bn;
+            S.e_var[e] = EV_PEND;
           } else {
-            S.e_var[e] = 0xff;
+            S.e_var[e] = EV_DEAD;
           }
         }
       }
@@ -731,6 +800,7 @@ __global__ void __launch_bounds__(32) k_resolve(DevTables t, IngestArgs a) {
         if (buf_moved) hbrep[h * d + i] = nbrep[i];
       }
       if (lane == 0) {
+        S.hdirty[h] = 1;
         S.hrn[h] = rn;
         S.hvar[h] = varn;
         S.hstat[h] += 1;
@@ -741,22 +811,25 @@ __global__ void __launch_bounds__(32) k_resolve(DevTables t, IngestArgs a) {
         }
         if (kind == EV_DEFER) S.hlazy[h] = 1;
         const int64_t frow = static_cast<int64_t>(dom) * t.tmax + tt;
+        int page, row;
+        hot_reserve_row(t, S, h, buf_moved, page, row);
+        a.ev_page[frow] = page;
+        a.ev_row[frow] = row;
         a.ev_kind[frow] = kind;
         a.ev_slot[frow] = w;
         t.ring_owner[(static_cast<int64_t>(dom) * t.W + a.ring_slot) * t.tmax + tt] = w;
-      }
-      {
-        const int64_t frow = static_cast<int64_t>(dom) * t.tmax + tt;
-        hot_append(t, S, h, buf_moved, fkb + frow * rb, fvb + frow * rb);
-      }
-      if (kind == EV_DEFER && nb == 0 && lane == 0) {  // register the new buffer candidate
-        if (n < cmax) {
-          cslot[n] = w;
-          cbuf[n] = 1;
-          touched[n] = 1;
-          chot[n] = static_cast<int8_t>(h);
-        } else {
-          set_err(t, DERR_CANDIDATES);
+        if (kind == EV_DEFER && nb == 0) {  // register the new buffer candidate
+          if (n < cmax) {
+            cslot[n] = w;
+            cbuf[n] = 1;
+            ckey[n] = 2LL * t.cid[w] + 1;
+            touched[n] = 1;
+            chot[n] = static_cast<int8_t>(h);
+            S.hcb[h] = n;
+            if (S.ntl < TLMAX) S.tl[S.ntl++] = n; else set_err(t, DERR_CANDIDATES);
+          } else {
+            set_err(t, DERR_CANDIDATES);
+          }
         }
       }
       if (kind == EV_DEFER && nb == 0) n = min(n + 1, cmax);
@@ -772,7 +845,29 @@ done:
     a.dom_pool_n[dom] = S.npool;
     a.n_exact[dom] = n_exact;
   }
-  (void)stopped;
+}
+
+// ============================================================================ K3
+// Copies every committed row of the launch to the (page, row) K2 reserved for it.
+__global__ void k_store_rows(DevTables t, IngestArgs a) {
+  const int dom = a.active[blockIdx.y];
+  const int rb = t.d * t.es;
+  const int warps = blockDim.x / 32, warp = threadIdx.x / 32, lane = threadIdx.x & 31;
+  const int cur = a.cursor[dom];
+  for (int tt = cur + blockIdx.x * warps + warp; tt < a.T; tt += gridDim.x * warps) {
+    const int64_t frow = static_cast<int64_t>(dom) * t.tmax + tt;
+    const int page = a.ev_page[frow];
+    if (page < 0) continue;
+    const int row = a.ev_row[frow];
+    const uint8_t* sk = static_cast<const uint8_t*>(a.fk) + frow * rb;
+    const uint8_t* sv = static_cast<const uint8_t*>(a.fv) + frow * rb;
+    uint8_t* dk = page_k(t, page) + static_cast<int64_t>(row) * rb;
+    uint8_t* dv = page_v(t, page) + static_cast<int64_t>(row) * rb;
+    for (int o = lane * 16; o < rb; o += 32 * 16) {
+      *reinterpret_cast<uint4*>(dk + o) = *reinterpret_cast<const uint4*>(sk + o);
+      *reinterpret_cast<uint4*>(dv + o) = *reinterpret_cast<const uint4*>(sv + o);
+    }
+  }
 }
 
 // ============================================================================ ring write
@@ -1580,13 +1675,19 @@ int launch_approx(const DevTables& t, const IngestArgs& a, cudaStream_t st) {
 
 int launch_resolve(const DevTables& t, const IngestArgs& a, cudaStream_t st) {
   const size_t smem = static_cast<size_t>(HOT) * 2 * t.d * 8 + static_cast<size_t>(5) * t.d * 8 +
-                      static_cast<size_t>(t.tmax) * 8 + static_cast<size_t>(t.cmax) * (4 + 3) + 64;
+                      static_cast<size_t>(t.tmax) * 8 + static_cast<size_t>(t.cmax) * (8 + 4 + 3) + 64;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_resolve, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
   k_resolve<<<a.n_active, 32, smem, st>>>(t, a);
+  return 1;
+}
+
+int launch_store_rows(const DevTables& t, const IngestArgs& a, cudaStream_t st) {
+  dim3 g((a.T + 31) / 32, a.n_active);
+  k_store_rows<<<g, 256, 0, st>>>(t, a);
   return 1;
 }
 

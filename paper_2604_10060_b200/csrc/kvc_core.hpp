@@ -132,6 +132,10 @@ struct IngestArgs {
   int16_t* topm_idx;       // [L][tmax][TOPM]
   float* topm_val;         // [L][tmax][TOPM]
   float* topm_next;        // [L][tmax]
+  double* topm_exact;      // [L][tmax][TOPM] exact cosine vs the launch-time representative (K1c)
+  // destination of each committed row (page, row) for the parallel store pass (K3)
+  int32_t* ev_page;        // [L][tmax]
+  int32_t* ev_row;         // [L][tmax]
   // per-domain reserve of free pages carried between resolve launches (no pushes to the
   // shared free stack while pops may run concurrently)
   int32_t* dom_pool;       // [L][POOL]
@@ -178,6 +182,7 @@ int launch_build_cands(const DevTables& t, const IngestArgs& a, cudaStream_t st)
 int launch_approx(const DevTables& t, const IngestArgs& a, cudaStream_t st);
 int launch_resolve(const DevTables& t, const IngestArgs& a, cudaStream_t st);
 int launch_topm(const DevTables& t, const IngestArgs& a, cudaStream_t st);
+int launch_store_rows(const DevTables& t, const IngestArgs& a, cudaStream_t st);
 int launch_ring_write(const DevTables& t, const void* fk, const void* fv, int32_t T,
                       int32_t ring_slot, cudaStream_t st);
 int launch_decode(const DevTables& t, const DecodeArgs& a, cudaStream_t st, cudaEvent_t* ev);
