@@ -228,11 +228,21 @@ def main():
             kv.process_frame(int(fids[i]), fvis[i], fk[i], fv[i], want_assigned=False)
         ev1.record(stream)
         torch.cuda.synchronize()
+    # phase breakdown on a few extra frames (CUDA events add records; kept out of the timed loop)
+    kv.set_timing(True)
+    ph = []
+    xk, xv, xvis, xids = workload.frames_near(st, 3, int(fids[-1]) + 10000, seed=123)
+    for i in range(3):
+        kv.process_frame(int(xids[i]), xvis[i], xk[i], xv[i], want_assigned=False)
+        ph.append(kv.ingest_timing())
+    kv.set_timing(False)
+    ingest_phases = dict(zip(["cands", "approx", "topm_exact", "resolve", "store_rows", "host_wait",
+                              "host_other", "host_events"], np.mean(ph, axis=0).round(2).tolist()))
     ingest_ms = ev0.elapsed_time(ev1)
     ingest_launches = kv.launch_count() - launches0
     splits = (kv.maint_stats() - splits0).tolist()
     # e2e ingest: frames from pinned host memory through the public API
-    more_k, more_v, more_vis, more_ids = workload.frames_near(st, frames_t, int(fids[-1]) + 1, seed=99)
+    more_k, more_v, more_vis, more_ids = workload.frames_near(st, frames_t, int(fids[-1]) + 20000, seed=99)
     mk_t = more_k.view(torch.int16).cpu().pin_memory()
     mv_t = more_v.view(torch.int16).cpu().pin_memory()
     mk_h, mv_h = mk_t.numpy(), mv_t.numpy()
@@ -330,6 +340,7 @@ def main():
                    "e2e": {"value": round(frames_t / (ingest_e2e_ms * 1e-3), 1), "unit": "frames/s",
                            "h2d_bytes_per_step": D * T_FRAME * HEAD_DIM * 2 * 2, "d2h_bytes_per_step": 0},
                    "gpu_launches": int(ingest_launches),
+                   "phases_us": ingest_phases,
                    "maint_delta": dict(zip(["inserts", "absorbed", "immediate_splits", "deferred_marks",
                                             "settled_splits", "split_ops", "host_over", "maint_fetches",
                                             "partitions_opened"], splits)),

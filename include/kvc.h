@@ -205,6 +205,12 @@ KVC_API int64_t kvc_launch_count(kvc_ctx* ctx);
  * host phases in microseconds -- t[5] wait for the device, t[6] retrieve bookkeeping replay,
  * t[7] repin + checks. */
 KVC_API int kvc_last_step_timing(kvc_ctx* ctx, double* t);
+/* Timing of the last ingested frame (needs kvc_set_timing(1)), t[8]: device microseconds of
+ * the candidate lists, approximate tile, top-M + exact pre-scores, sequential resolve and row
+ * store kernels (t[0..4], summed over launches); host microseconds waiting for the device (t[5])
+ * and of everything else in the on_insert loop incl. replay and host events (t[6]); t[7] the
+ * number of host events (seeds / splits) the frame needed. */
+KVC_API int kvc_last_ingest_timing(kvc_ctx* ctx, double* t);
 /* Enables per-phase CUDA-event timing (off by default: it adds event records). */
 KVC_API void kvc_set_timing(kvc_ctx* ctx, int32_t on);
 

@@ -143,6 +143,7 @@ def lib():
         L.kvc_launch_count.restype = C.c_int64
         L.kvc_last_step_timing.argtypes = [vp, f64p]
         L.kvc_set_timing.argtypes = [vp, C.c_int32]
+        L.kvc_last_ingest_timing.argtypes = [vp, f64p]
         _lib = L
     return _lib
 
@@ -155,7 +156,7 @@ EXPORTED = [
     "kvc_cluster", "kvc_cluster_entries", "kvc_cluster_payload", "kvc_n_partitions",
     "kvc_partition", "kvc_partition_layer", "kvc_maint_stats", "kvc_ledger",
     "kvc_ledger_log_size", "kvc_ledger_op", "kvc_check", "kvc_offload", "kvc_fetch",
-    "kvc_launch_count", "kvc_last_step_timing", "kvc_set_timing",
+    "kvc_launch_count", "kvc_last_step_timing", "kvc_set_timing", "kvc_last_ingest_timing",
 ]
 
 
@@ -382,6 +383,11 @@ class ClusterKVCache:
 
     def set_timing(self, on: bool):
         lib().kvc_set_timing(self.h, 1 if on else 0)
+
+    def ingest_timing(self):
+        t = np.zeros(8)
+        lib().kvc_last_ingest_timing(self.h, _p(t, f64p))
+        return t
 
     def step_timing(self):
         t = np.zeros(8)

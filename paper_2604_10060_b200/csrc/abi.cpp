@@ -323,4 +323,10 @@ int kvc_last_step_timing(kvc_ctx* ctx, double* t) {
 
 void kvc_set_timing(kvc_ctx* ctx, int32_t on) { ctx->impl->set_timing(on != 0); }
 
+int kvc_last_ingest_timing(kvc_ctx* ctx, double* t) {
+  const double* s = ctx->impl->ingest_timing();
+  for (int i = 0; i < 8; ++i) t[i] = s[i];
+  return KVC_OK;
+}
+
 }  // extern "C"

@@ -11,6 +11,7 @@
 #include "context.hpp"
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstring>
 #include <numeric>
@@ -746,6 +747,9 @@ void Context::run_inserts(std::int64_t frame_id, std::int64_t pid, int T, std::i
   ia_.pid = static_cast<std::int32_t>(pid);
   ia_.ring_slot = ring_slot;
   ia_.margin = 1e-4f;
+  double t_wait = 0.0;
+  for (double& x : ingest_t_) x = 0.0;
+  const auto r0 = std::chrono::steady_clock::now();
   while (frontier < L_) {
     if (launch) {
       flush_resid();
@@ -755,17 +759,32 @@ void Context::run_inserts(std::int64_t frame_id, std::int64_t pid, int T, std::i
       }
       for (int l = 0; l < L_; ++l) h_cursor_[l] = cursor[static_cast<std::size_t>(l)];
       KVC_CUDA(cudaMemcpyAsync(d_active_, h_active_, L_ * 8, cudaMemcpyHostToDevice, st_));
+      if (timing_) KVC_CUDA(cudaEventRecord(ev_[0], st_));
       launches_ += launch_build_cands(t_, ia_, st_);
+      if (timing_) KVC_CUDA(cudaEventRecord(ev_[1], st_));
       launches_ += launch_approx(t_, ia_, st_);
+      if (timing_) KVC_CUDA(cudaEventRecord(ev_[2], st_));
       launches_ += launch_topm(t_, ia_, st_);
+      if (timing_) KVC_CUDA(cudaEventRecord(ev_[3], st_));
       launches_ += launch_resolve(t_, ia_, st_);
+      if (timing_) KVC_CUDA(cudaEventRecord(ev_[4], st_));
       launches_ += launch_store_rows(t_, ia_, st_);
+      if (timing_) KVC_CUDA(cudaEventRecord(ev_[5], st_));
       KVC_CUDA(cudaMemcpyAsync(h_evk_, ia_.ev_kind, static_cast<std::size_t>(L_) * t_.tmax * 4, cudaMemcpyDeviceToHost, st_));
       KVC_CUDA(cudaMemcpyAsync(h_evs_, ia_.ev_slot, static_cast<std::size_t>(L_) * t_.tmax * 4, cudaMemcpyDeviceToHost, st_));
       KVC_CUDA(cudaMemcpyAsync(h_stop_, ia_.stop_t, static_cast<std::size_t>(L_) * 12, cudaMemcpyDeviceToHost, st_));
       KVC_CUDA(cudaMemcpyAsync(h_err_, t_.err, 4, cudaMemcpyDeviceToHost, st_));
+      const auto w0 = std::chrono::steady_clock::now();
       sync();
+      t_wait += std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - w0).count();
       check_err_word(*h_err_);
+      if (timing_) {
+        float ms = 0.f;
+        for (int i = 0; i < 5; ++i) {
+          KVC_CUDA(cudaEventElapsedTime(&ms, ev_[i], ev_[i + 1]));
+          ingest_t_[i] += ms * 1e3;
+        }
+      }
       launch = false;
     }
     const int l = frontier;
@@ -824,6 +843,7 @@ void Context::run_inserts(std::int64_t frame_id, std::int64_t pid, int T, std::i
       continue;
     }
     const std::int64_t id = handle_host_event(frame_id, pid, l, stop, h_stop_[L_ + l], h_stop_[2 * L_ + l]);
+    ingest_t_[7] += 1.0;  // host events this frame
     if (assigned) assigned[static_cast<std::size_t>(l) * T + stop] = id;
     cursor[static_cast<std::size_t>(l)] = stop + 1;
     replayed[static_cast<std::size_t>(l)] = stop + 1;
@@ -838,6 +858,8 @@ void Context::run_inserts(std::int64_t frame_id, std::int64_t pid, int T, std::i
       }
     }
   }
+  ingest_t_[5] = t_wait;
+  ingest_t_[6] = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - r0).count() - t_wait;
 }
 
 // ============================================================================ slow path

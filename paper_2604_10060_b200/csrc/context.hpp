@@ -111,6 +111,7 @@ class Context {
   std::int64_t launches() const { return launches_; }
   void set_timing(bool on) { timing_ = on; }
   const double* step_timing() const { return step_t_; }
+  const double* ingest_timing() const { return ingest_t_; }
 
  private:
   // ---- configuration
@@ -160,6 +161,7 @@ class Context {
   cudaEvent_t ev_[8];
   bool timing_ = false;
   double step_t_[8] = {0};
+  double ingest_t_[8] = {0};  // last frame: device us (cands, approx, topm, resolve, store), host us (wait, replay, rest)
   std::int64_t launches_ = 0;
 
   // ---- host control plane

@@ -429,17 +429,22 @@ __global__ void __launch_bounds__(32) k_resolve(DevTables t, IngestArgs a) {
   double* sd = reinterpret_cast<double*>(smraw);
   double* hrep = sd;                     // [HOT][d]
   double* hbrep = hrep + HOT * d;        // [HOT][d]
-  double* kd = hbrep + HOT * d;          // [2][d] keys of t and t+1
-  double* nrep = kd + 2 * d;             // [d] pending r'
+  double* kd = hbrep + HOT * d;          // [3][d] key ring: rows t, t+1, t+2 (slot = t % 3)
+  double* nrep = kd + 3 * d;             // [d] pending r'
   double* nbrep = nrep + d;              // [d] pending buffer mean
   double* diff = nbrep + d;              // [d] k_t - r'
   double* nk = diff + d;                 // [tmax]
-  long long* ckey = reinterpret_cast<long long*>(nk + t.tmax);  // [cmax] CandidateRef order key
+  double* tm_exact = nk + t.tmax;        // [tmax][TOPM] staged K1b outputs
+  float* tm_val = reinterpret_cast<float*>(tm_exact + static_cast<int64_t>(t.tmax) * TOPM);  // [tmax][TOPM]
+  float* tm_next = tm_val + t.tmax * TOPM;                                                    // [tmax]
+  int16_t* tm_idx = reinterpret_cast<int16_t*>(tm_next + t.tmax);                            // [tmax][TOPM]
+  long long* ckey = reinterpret_cast<long long*>(  // [cmax] CandidateRef order key
+      (reinterpret_cast<uintptr_t>(tm_idx + t.tmax * TOPM) + 15) & ~static_cast<uintptr_t>(15));
   int* cslot = reinterpret_cast<int*>(ckey + cmax);              // [cmax]
   int8_t* chot = reinterpret_cast<int8_t*>(cslot + cmax);        // [cmax] hot index or -1
   uint8_t* cbuf = reinterpret_cast<uint8_t*>(chot + cmax);       // [cmax]
   uint8_t* touched = cbuf + cmax;                                  // [cmax]
-  const int OFF_HREP = 0, OFF_HBREP = HOT * d, OFF_KD = 2 * HOT * d, OFF_NREP = OFF_KD + 2 * d,
+  const int OFF_HREP = 0, OFF_HBREP = HOT * d, OFF_KD = 2 * HOT * d, OFF_NREP = OFF_KD + 3 * d,
             OFF_NBREP = OFF_NREP + d, OFF_DIFF = OFF_NBREP + d;
 
   const int dom = a.active[blockIdx.x];
@@ -475,6 +480,16 @@ __global__ void __launch_bounds__(32) k_resolve(DevTables t, IngestArgs a) {
     nk[tt] = __dsqrt_rn(s);
     a.ev_page[static_cast<int64_t>(dom) * t.tmax + tt] = -1;
   }
+  {  // stage the per-token top-M lists of this launch's tokens (one latency instead of per token)
+    const int64_t o0 = (static_cast<int64_t>(dom) * t.tmax + cur) * TOPM;
+    const int cnt = (T - cur) * TOPM;
+    for (int i = lane; i < cnt; i += 32) {
+      tm_idx[cur * TOPM + i] = a.topm_idx[o0 + i];
+      tm_val[cur * TOPM + i] = a.topm_val[o0 + i];
+      tm_exact[cur * TOPM + i] = a.topm_exact[o0 + i];
+    }
+    for (int tt = cur + lane; tt < T; tt += 32) tm_next[tt] = a.topm_next[static_cast<int64_t>(dom) * t.tmax + tt];
+  }
   __syncwarp();
   int n_exact = 0;
   if (cur >= T) goto done;
@@ -501,9 +516,11 @@ __global__ void __launch_bounds__(32) k_resolve(DevTables t, IngestArgs a) {
   }
   {
     const float margin2 = 2.f * a.margin;
-    int kb = 0;  // kd[kb] holds the key of token t
-    for (int i = lane; i < d; i += 32)
-      kd[i] = static_cast<double>(ld_kv(a.fk, (static_cast<int64_t>(dom) * t.tmax + cur) * d + i, t.kv_bf16));
+    // key ring: kd[(t % 3) * d] holds token t; rows cur and cur+1 now, t+2 prefetched in iteration t
+    for (int r = 0; r < 2 && cur + r < T; ++r)
+      for (int i = lane; i < d; i += 32)
+        kd[((cur + r) % 3) * d + i] =
+            static_cast<double>(ld_kv(a.fk, (static_cast<int64_t>(dom) * t.tmax + cur + r) * d + i, t.kv_bf16));
     if (lane == 0) S.ne = 0;
     __syncwarp();
 
@@ -560,23 +577,24 @@ __global__ void __launch_bounds__(32) k_resolve(DevTables t, IngestArgs a) {
       if (fresh_possible && lane == 0)  // the buffer a DEFER would register (index.cpp:153-160)
         add(-2, EV_FRESH, 0, OFF_NBREP, nullptr, 0.0, 2LL * t.cid[w_slot] + 1, 0.0);
       // (b) untouched candidates within 2*margin of the best untouched approximate score
+      const int16_t* ti = tm_idx + tn * TOPM;
       int first_untouched = -1;
       for (int r = 0; r < TOPM; ++r) {
-        const int c = a.topm_idx[o * TOPM + r];
+        const int c = ti[r];
         if (c < 0) break;
         if (!touched[c] && cslot[c] != w_slot) {
           first_untouched = r;
           break;
         }
       }
-      const float bu = first_untouched >= 0 ? a.topm_val[o * TOPM + first_untouched] : -INFINITY;
+      const float bu = first_untouched >= 0 ? tm_val[tn * TOPM + first_untouched] : -INFINITY;
       const float thr = bu - margin2;
-      const bool complete = first_untouched >= 0 && !(a.topm_next[o] >= thr);
+      const bool complete = first_untouched >= 0 && !(tm_next[tn] >= thr);
       if (complete) {
         if (lane < TOPM) {
-          const int c = a.topm_idx[o * TOPM + lane];
-          if (c >= 0 && !touched[c] && cslot[c] != w_slot && a.topm_val[o * TOPM + lane] >= thr)
-            add(c, EV_PRE, 0, 0, nullptr, 0.0, ckey[c], a.topm_exact[o * TOPM + lane]);
+          const int c = ti[lane];
+          if (c >= 0 && !touched[c] && cslot[c] != w_slot && tm_val[tn * TOPM + lane] >= thr)
+            add(c, EV_PRE, 0, 0, nullptr, 0.0, ckey[c], tm_exact[tn * TOPM + lane]);
         }
       } else {  // rare: scan the whole approximate row
         for (int c = lane; c < n; c += 32) {
@@ -655,8 +673,16 @@ __global__ void __launch_bounds__(32) k_resolve(DevTables t, IngestArgs a) {
 
     double sq = 0.0, rn = 0.0, bn = 0.0;
     build_entries(cur, -1, false, false, 0);
-    chain_phase(OFF_KD, kd, false, sq, rn, bn);
+    chain_phase(OFF_KD + (cur % 3) * d, kd + (cur % 3) * d, false, sq, rn, bn);
+    constexpr int KPL = 8;  // key elements per lane held in flight (d <= 256)
     for (int tt = cur; tt < T; ++tt) {
+      // prefetch the key of tt + 2 into registers; stored into the ring at the end of the iteration
+      float kpre[KPL];
+#pragma unroll
+      for (int j = 0; j < KPL; ++j) {
+        const int i = lane + 32 * j;
+        kpre[j] = (tt + 2 < T && i < d) ? ld_kv(a.fk, (static_cast<int64_t>(dom) * t.tmax + tt + 2) * d + i, t.kv_bf16) : 0.f;
+      }
       const double nkt = nk[tt];
       if (nkt < 1e-12) {
         if (lane == 0) {
@@ -721,7 +747,11 @@ __global__ void __launch_bounds__(32) k_resolve(DevTables t, IngestArgs a) {
           if (S.ntl < TLMAX) S.tl[S.ntl++] = cb; else set_err(t, DERR_CANDIDATES);
         }
       }
+      // Eq. 5 threshold of the winner, loaded early so its latency hides behind the chain phase
+      const int64_t npre_w = S.hnmem[h];
+      const double tau_w = __ldg(&t.tau_tab[npre_w < t.tau_len ? npre_w : t.tau_len - 1]);
       // ---- Eq. 3/4 into pending buffers (maintainer.cpp:16-25, index.cpp:181-188)
+      const int kb = tt % 3, kn = (tt + 1) % 3;
       const double* kt = kd + kb * d;
       const double dn = static_cast<double>(S.hstat[h]);
       const int nb = S.hnbuf[h];
@@ -734,10 +764,6 @@ __global__ void __launch_bounds__(32) k_resolve(DevTables t, IngestArgs a) {
       }
       const bool has_next = tt + 1 < T;
       const bool fresh_possible = !isbuf && S.hresid[h] != 0 && a.defer && nb == 0;
-      if (has_next)
-        for (int i = lane; i < d; i += 32)
-          kd[(kb ^ 1) * d + i] =
-              static_cast<double>(ld_kv(a.fk, (static_cast<int64_t>(dom) * t.tmax + tt + 1) * d + i, t.kv_bf16));
       __syncwarp();
       if (has_next) {
         build_entries(tt + 1, w, isbuf, fresh_possible, h);
@@ -745,15 +771,13 @@ __global__ void __launch_bounds__(32) k_resolve(DevTables t, IngestArgs a) {
         if (lane == 0) S.ne = 0;
         __syncwarp();
       }
-      chain_phase(OFF_KD + (kb ^ 1) * d, kd + (kb ^ 1) * d, true, sq, rn, bn);
+      chain_phase(OFF_KD + kn * d, kd + kn * d, true, sq, rn, bn);
       const double varn = ddiv(dadd(dmul(dn, S.hvar[h]), sq), dadd(dn, 1.0));
       int kind;
       if (isbuf) {
         kind = EV_BUFJOIN;
       } else {
-        const int64_t npre = S.hnmem[h];
-        const double tau = t.tau_tab[npre < t.tau_len ? npre : t.tau_len - 1];
-        if (varn <= tau)
+        if (varn <= tau_w)
           kind = EV_ABSORB;
         else if (S.hresid[h] == 0)
           kind = EV_SPLIT;
@@ -833,7 +857,13 @@ __global__ void __launch_bounds__(32) k_resolve(DevTables t, IngestArgs a) {
         }
       }
       if (kind == EV_DEFER && nb == 0) n = min(n + 1, cmax);
-      kb ^= 1;
+      if (tt + 2 < T) {
+#pragma unroll
+        for (int j = 0; j < KPL; ++j) {
+          const int i = lane + 32 * j;
+          if (i < d) kd[((tt + 2) % 3) * d + i] = static_cast<double>(kpre[j]);
+        }
+      }
       __syncwarp();
     }
   }
@@ -1674,8 +1704,9 @@ int launch_approx(const DevTables& t, const IngestArgs& a, cudaStream_t st) {
 }
 
 int launch_resolve(const DevTables& t, const IngestArgs& a, cudaStream_t st) {
-  const size_t smem = static_cast<size_t>(HOT) * 2 * t.d * 8 + static_cast<size_t>(5) * t.d * 8 +
-                      static_cast<size_t>(t.tmax) * 8 + static_cast<size_t>(t.cmax) * (8 + 4 + 3) + 64;
+  const size_t smem = static_cast<size_t>(HOT) * 2 * t.d * 8 + static_cast<size_t>(6) * t.d * 8 +
+                      static_cast<size_t>(t.tmax) * (8 + TOPM * (8 + 4 + 2) + 4) + 16 +
+                      static_cast<size_t>(t.cmax) * (8 + 4 + 3) + 64;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_resolve, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
