@@ -235,6 +235,7 @@ def main():
     for i in range(3):
         kv.process_frame(int(xids[i]), xvis[i], xk[i], xv[i], want_assigned=False)
         ph.append(kv.ingest_timing())
+    prof_cycles = kv.resolve_profile()
     kv.set_timing(False)
     ingest_phases = dict(zip(["cands", "approx", "topm_exact", "resolve", "store_rows", "host_wait",
                               "host_other", "host_events"], np.mean(ph, axis=0).round(2).tolist()))
@@ -341,6 +342,8 @@ def main():
                            "h2d_bytes_per_step": D * T_FRAME * HEAD_DIM * 2 * 2, "d2h_bytes_per_step": 0},
                    "gpu_launches": int(ingest_launches),
                    "phases_us": ingest_phases,
+                   "resolve_cycles_per_frame": dict(zip(["argmax", "hot", "update", "build", "chain", "decide",
+                                                         "commit", "keyring"], prof_cycles.round(0).tolist())),
                    "maint_delta": dict(zip(["inserts", "absorbed", "immediate_splits", "deferred_marks",
                                             "settled_splits", "split_ops", "host_over", "maint_fetches",
                                             "partitions_opened"], splits)),

@@ -211,6 +211,8 @@ KVC_API int kvc_last_step_timing(kvc_ctx* ctx, double* t);
  * and of everything else in the on_insert loop incl. replay and host events (t[6]); t[7] the
  * number of host events (seeds / splits) the frame needed. */
 KVC_API int kvc_last_ingest_timing(kvc_ctx* ctx, double* t);
+/* Instrumentation: mean clock64 cycles per phase of the last resolve launch (out[8]). */
+KVC_API int kvc_debug_resolve_profile(kvc_ctx* ctx, double* out);
 /* Enables per-phase CUDA-event timing (off by default: it adds event records). */
 KVC_API void kvc_set_timing(kvc_ctx* ctx, int32_t on);
 

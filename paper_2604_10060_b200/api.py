@@ -144,6 +144,7 @@ def lib():
         L.kvc_last_step_timing.argtypes = [vp, f64p]
         L.kvc_set_timing.argtypes = [vp, C.c_int32]
         L.kvc_last_ingest_timing.argtypes = [vp, f64p]
+        L.kvc_debug_resolve_profile.argtypes = [vp, f64p]
         _lib = L
     return _lib
 
@@ -157,6 +158,7 @@ EXPORTED = [
     "kvc_partition", "kvc_partition_layer", "kvc_maint_stats", "kvc_ledger",
     "kvc_ledger_log_size", "kvc_ledger_op", "kvc_check", "kvc_offload", "kvc_fetch",
     "kvc_launch_count", "kvc_last_step_timing", "kvc_set_timing", "kvc_last_ingest_timing",
+    "kvc_debug_resolve_profile",
 ]
 
 
@@ -383,6 +385,11 @@ class ClusterKVCache:
 
     def set_timing(self, on: bool):
         lib().kvc_set_timing(self.h, 1 if on else 0)
+
+    def resolve_profile(self):
+        t = np.zeros(8)
+        lib().kvc_debug_resolve_profile(self.h, _p(t, f64p))
+        return t
 
     def ingest_timing(self):
         t = np.zeros(8)

@@ -323,6 +323,11 @@ int kvc_last_step_timing(kvc_ctx* ctx, double* t) {
 
 void kvc_set_timing(kvc_ctx* ctx, int32_t on) { ctx->impl->set_timing(on != 0); }
 
+int kvc_debug_resolve_profile(kvc_ctx* ctx, double* out) {
+  ctx->impl->resolve_profile(out);
+  return KVC_OK;
+}
+
 int kvc_last_ingest_timing(kvc_ctx* ctx, double* t) {
   const double* s = ctx->impl->ingest_timing();
   for (int i = 0; i < 8; ++i) t[i] = s[i];

@@ -214,6 +214,7 @@ void Context::alloc_device() {
   ia_.ev_page = static_cast<std::int32_t*>(dalloc(L * t_.tmax * 4));
   ia_.ev_row = static_cast<std::int32_t*>(dalloc(L * t_.tmax * 4));
   ia_.dom_pool = static_cast<std::int32_t*>(dalloc(L * POOL * 4));
+  ia_.prof = static_cast<long long*>(dalloc(L * 8 * 8));
   ia_.dom_pool_n = static_cast<std::int32_t*>(dalloc(L * 4));
   d_active_ = static_cast<std::int32_t*>(dalloc(L * 4 * 2));
   d_cursor_ = d_active_ + L;
@@ -305,6 +306,16 @@ void Context::ensure_idx(std::int64_t n, std::int64_t runs) {
     runs_cap_ = std::max(runs, runs_cap_ * 2);
     d_runs_ = static_cast<AppendRun*>(dalloc(runs_cap_ * sizeof(AppendRun)));
     h_runs_ = static_cast<AppendRun*>(halloc(runs_cap_ * sizeof(AppendRun)));
+  }
+}
+
+void Context::resolve_profile(double* out) {
+  std::vector<long long> p(static_cast<std::size_t>(L_) * 8);
+  KVC_CUDA(cudaMemcpy(p.data(), ia_.prof, p.size() * 8, cudaMemcpyDeviceToHost));
+  for (int k = 0; k < 8; ++k) {
+    double s = 0.0;
+    for (int l = 0; l < L_; ++l) s += static_cast<double>(p[static_cast<std::size_t>(l) * 8 + k]);
+    out[k] = s / L_;
   }
 }
 

@@ -112,6 +112,7 @@ class Context {
   void set_timing(bool on) { timing_ = on; }
   const double* step_timing() const { return step_t_; }
   const double* ingest_timing() const { return ingest_t_; }
+  void resolve_profile(double* out);  // mean clock64 cycles per resolve phase over domains
 
  private:
   // ---- configuration

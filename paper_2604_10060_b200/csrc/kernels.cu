@@ -318,17 +318,21 @@ struct ResolveShared {
   int npool;
 };
 
+// Shared row arrays use a padded stride so rows of different arrays start in different banks
+// (lanes of one chain phase read several arrays at the same index).
+__host__ __device__ inline int padded(int d) { return d + 2; }
+
 __device__ void hot_writeback(const DevTables& t, ResolveShared& S, const double* hrep,
                               const double* hbrep, int h) {
   if (!S.hdirty[h]) return;
-  const int lane = threadIdx.x & 31, d = t.d;
+  const int lane = threadIdx.x & 31, d = t.d, DS = padded(d);
   const int64_t s = S.hslot[h];
   for (int i = lane; i < d; i += 32) {
-    const double r = hrep[h * d + i];
+    const double r = hrep[h * DS + i];
     t.rep64[s * d + i] = r;
     t.rep32[s * d + i] = static_cast<float>(r);
     if (S.hnbuf[h] > 0) {
-      const double b = hbrep[h * d + i];
+      const double b = hbrep[h * DS + i];
       t.brep64[s * d + i] = b;
       t.brep32[s * d + i] = static_cast<float>(b);
     }
@@ -351,12 +355,12 @@ __device__ void hot_writeback(const DevTables& t, ResolveShared& S, const double
 // Loads a slot into the next hot entry (caller guarantees room). cl/cb: its candidate indices.
 __device__ int hot_load(const DevTables& t, ResolveShared& S, double* hrep, double* hbrep, int slot,
                         int cl, int cb) {
-  const int lane = threadIdx.x & 31, d = t.d;
+  const int lane = threadIdx.x & 31, d = t.d, DS = padded(d);
   const int h = S.nhot;
   __syncwarp();
   for (int i = lane; i < d; i += 32) {
-    hrep[h * d + i] = t.rep64[static_cast<int64_t>(slot) * d + i];
-    hbrep[h * d + i] = t.brep64[static_cast<int64_t>(slot) * d + i];
+    hrep[h * DS + i] = t.rep64[static_cast<int64_t>(slot) * d + i];
+    hbrep[h * DS + i] = t.brep64[static_cast<int64_t>(slot) * d + i];
   }
   if (lane == 0) {
     S.hslot[h] = slot;
@@ -426,14 +430,15 @@ __global__ void __launch_bounds__(32) k_resolve(DevTables t, IngestArgs a) {
   extern __shared__ __align__(16) uint8_t smraw[];
   __shared__ ResolveShared S;
   const int d = t.d, cmax = t.cmax, lane = threadIdx.x;
+  const int DS = padded(d);               // padded row stride (doubles)
   double* sd = reinterpret_cast<double*>(smraw);
-  double* hrep = sd;                     // [HOT][d]
-  double* hbrep = hrep + HOT * d;        // [HOT][d]
-  double* kd = hbrep + HOT * d;          // [3][d] key ring: rows t, t+1, t+2 (slot = t % 3)
-  double* nrep = kd + 3 * d;             // [d] pending r'
-  double* nbrep = nrep + d;              // [d] pending buffer mean
-  double* diff = nbrep + d;              // [d] k_t - r'
-  double* nk = diff + d;                 // [tmax]
+  double* hrep = sd;                     // [HOT][DS]
+  double* hbrep = hrep + HOT * DS;       // [HOT][DS]
+  double* kd = hbrep + HOT * DS;         // [3][DS] key ring: rows t, t+1, t+2 (slot = t % 3)
+  double* nrep = kd + 3 * DS;            // [DS] pending r'
+  double* nbrep = nrep + DS;             // [DS] pending buffer mean
+  double* diff = nbrep + DS;             // [DS] k_t - r'
+  double* nk = diff + DS;                // [tmax]
   double* tm_exact = nk + t.tmax;        // [tmax][TOPM] staged K1b outputs
   float* tm_val = reinterpret_cast<float*>(tm_exact + static_cast<int64_t>(t.tmax) * TOPM);  // [tmax][TOPM]
   float* tm_next = tm_val + t.tmax * TOPM;                                                    // [tmax]
@@ -444,8 +449,8 @@ __global__ void __launch_bounds__(32) k_resolve(DevTables t, IngestArgs a) {
   int8_t* chot = reinterpret_cast<int8_t*>(cslot + cmax);        // [cmax] hot index or -1
   uint8_t* cbuf = reinterpret_cast<uint8_t*>(chot + cmax);       // [cmax]
   uint8_t* touched = cbuf + cmax;                                  // [cmax]
-  const int OFF_HREP = 0, OFF_HBREP = HOT * d, OFF_KD = 2 * HOT * d, OFF_NREP = OFF_KD + 3 * d,
-            OFF_NBREP = OFF_NREP + d, OFF_DIFF = OFF_NBREP + d;
+  const int OFF_HREP = 0, OFF_HBREP = HOT * DS, OFF_KD = 2 * HOT * DS, OFF_NREP = OFF_KD + 3 * DS,
+            OFF_NBREP = OFF_NREP + DS, OFF_DIFF = OFF_NBREP + DS;
 
   const int dom = a.active[blockIdx.x];
   const int T = a.T;
@@ -519,7 +524,7 @@ __global__ void __launch_bounds__(32) k_resolve(DevTables t, IngestArgs a) {
     // key ring: kd[(t % 3) * d] holds token t; rows cur and cur+1 now, t+2 prefetched in iteration t
     for (int r = 0; r < 2 && cur + r < T; ++r)
       for (int i = lane; i < d; i += 32)
-        kd[((cur + r) % 3) * d + i] =
+        kd[((cur + r) % 3) * DS + i] =
             static_cast<double>(ld_kv(a.fk, (static_cast<int64_t>(dom) * t.tmax + cur + r) * d + i, t.kv_bf16));
     if (lane == 0) S.ne = 0;
     __syncwarp();
@@ -564,11 +569,11 @@ __global__ void __launch_bounds__(32) k_resolve(DevTables t, IngestArgs a) {
           } else if (w_isbuf) {
             add(c, EV_PEND, 0, OFF_NBREP, nullptr, 0.0, ckey[c], 0.0);
           } else {  // live winner with a registered buffer: ABSORB keeps it, DEFER moves it
-            add(c, EV_CHAIN, 0, OFF_HBREP + w_h * d, nullptr, S.hbn[w_h], ckey[c], 0.0);
+            add(c, EV_CHAIN, 0, OFF_HBREP + w_h * DS, nullptr, S.hbn[w_h], ckey[c], 0.0);
             add(c, EV_PEND, 0, OFF_NBREP, nullptr, 0.0, ckey[c], 0.0);
           }
         } else if (h >= 0) {
-          add(c, EV_CHAIN, 0, (ib ? OFF_HBREP : OFF_HREP) + h * d, nullptr, ib ? S.hbn[h] : S.hrn[h], ckey[c], 0.0);
+          add(c, EV_CHAIN, 0, (ib ? OFF_HBREP : OFF_HREP) + h * DS, nullptr, ib ? S.hbn[h] : S.hrn[h], ckey[c], 0.0);
         } else {  // touched earlier, flushed out of the cache: global state (written back)
           add(c, EV_SLOW, 0, 0, (ib ? t.brep64 : t.rep64) + static_cast<int64_t>(s) * d,
               ib ? t.bnorm[s] : t.rnorm[s], ckey[c], 0.0);
@@ -578,14 +583,19 @@ __global__ void __launch_bounds__(32) k_resolve(DevTables t, IngestArgs a) {
         add(-2, EV_FRESH, 0, OFF_NBREP, nullptr, 0.0, 2LL * t.cid[w_slot] + 1, 0.0);
       // (b) untouched candidates within 2*margin of the best untouched approximate score
       const int16_t* ti = tm_idx + tn * TOPM;
-      int first_untouched = -1;
-      for (int r = 0; r < TOPM; ++r) {
-        const int c = ti[r];
-        if (c < 0) break;
-        if (!touched[c] && cslot[c] != w_slot) {
-          first_untouched = r;
-          break;
+      int first_untouched;
+      {
+        bool u = false, stop = false;
+        if (lane < TOPM) {
+          const int c = ti[lane];
+          stop = c < 0;
+          u = !stop && !touched[c] && cslot[c] != w_slot;
         }
+        const unsigned um = __ballot_sync(kFull, u), sm = __ballot_sync(kFull, stop);
+        // the lists are dense: -1 entries only trail; first untouched before the first -1
+        const int fu = um ? __ffs(um) - 1 : -1;
+        const int fs = sm ? __ffs(sm) - 1 : 32;
+        first_untouched = (fu >= 0 && fu < fs) ? fu : -1;
       }
       const float bu = first_untouched >= 0 ? tm_val[tn * TOPM + first_untouched] : -INFINITY;
       const float thr = bu - margin2;
@@ -673,15 +683,21 @@ __global__ void __launch_bounds__(32) k_resolve(DevTables t, IngestArgs a) {
 
     double sq = 0.0, rn = 0.0, bn = 0.0;
     build_entries(cur, -1, false, false, 0);
-    chain_phase(OFF_KD + (cur % 3) * d, kd + (cur % 3) * d, false, sq, rn, bn);
+    chain_phase(OFF_KD + (cur % 3) * DS, kd + (cur % 3) * DS, false, sq, rn, bn);
     constexpr int KPL = 8;  // key elements per lane held in flight (d <= 256)
+    long long pr[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    long long c0 = clock64(), c1;
+#define PROF(k) c1 = clock64(); pr[k] += c1 - c0; c0 = c1;
     for (int tt = cur; tt < T; ++tt) {
-      // prefetch the key of tt + 2 into registers; stored into the ring at the end of the iteration
-      float kpre[KPL];
+      // prefetch the key of tt + 2 as raw 32-bit words (converted only at the end of the iteration,
+      // so no instruction here waits for the load)
+      uint32_t kpre[KPL];
+      const int words = t.kv_bf16 ? d / 2 : d;
+      const uint32_t* krow = reinterpret_cast<const uint32_t*>(a.fk) + (static_cast<int64_t>(dom) * t.tmax + tt + 2) * words;
 #pragma unroll
       for (int j = 0; j < KPL; ++j) {
-        const int i = lane + 32 * j;
-        kpre[j] = (tt + 2 < T && i < d) ? ld_kv(a.fk, (static_cast<int64_t>(dom) * t.tmax + tt + 2) * d + i, t.kv_bf16) : 0.f;
+        const int w = lane + 32 * j;
+        kpre[j] = (tt + 2 < T && w < words) ? krow[w] : 0u;
       }
       const double nkt = nk[tt];
       if (nkt < 1e-12) {
@@ -716,6 +732,7 @@ __global__ void __launch_bounds__(32) k_resolve(DevTables t, IngestArgs a) {
       const int bc = S.e_cand[bp];
       const int w = cslot[bc];
       const bool isbuf = cbuf[bc];
+      PROF(0)
       // ---- winner into the hot cache
       int h = chot[bc];
       if (h < 0) {
@@ -747,31 +764,38 @@ __global__ void __launch_bounds__(32) k_resolve(DevTables t, IngestArgs a) {
           if (S.ntl < TLMAX) S.tl[S.ntl++] = cb; else set_err(t, DERR_CANDIDATES);
         }
       }
+      PROF(1)
       // Eq. 5 threshold of the winner, loaded early so its latency hides behind the chain phase
       const int64_t npre_w = S.hnmem[h];
       const double tau_w = __ldg(&t.tau_tab[npre_w < t.tau_len ? npre_w : t.tau_len - 1]);
       // ---- Eq. 3/4 into pending buffers (maintainer.cpp:16-25, index.cpp:181-188)
       const int kb = tt % 3, kn = (tt + 1) % 3;
-      const double* kt = kd + kb * d;
+      const double* kt = kd + kb * DS;
       const double dn = static_cast<double>(S.hstat[h]);
       const int nb = S.hnbuf[h];
       const double dnb = static_cast<double>(nb);
+      // the buffer mean can only move on BUFJOIN or DEFER (a Host cluster under the deferred policy)
+      const bool buf_may_move = isbuf || (S.hresid[h] != 0 && a.defer);
       for (int i = lane; i < d; i += 32) {
-        const double r = ddiv(dadd(dmul(dn, hrep[h * d + i]), kt[i]), dadd(dn, 1.0));
+        const double r = ddiv(dadd(dmul(dn, hrep[h * DS + i]), kt[i]), dadd(dn, 1.0));
         nrep[i] = r;
         diff[i] = dsub(kt[i], r);
-        nbrep[i] = nb == 0 ? kt[i] : ddiv(dadd(dmul(dnb, hbrep[h * d + i]), kt[i]), dadd(dnb, 1.0));
+        if (buf_may_move)
+          nbrep[i] = nb == 0 ? kt[i] : ddiv(dadd(dmul(dnb, hbrep[h * DS + i]), kt[i]), dadd(dnb, 1.0));
       }
       const bool has_next = tt + 1 < T;
       const bool fresh_possible = !isbuf && S.hresid[h] != 0 && a.defer && nb == 0;
       __syncwarp();
+      PROF(2)
       if (has_next) {
         build_entries(tt + 1, w, isbuf, fresh_possible, h);
       } else {
         if (lane == 0) S.ne = 0;
         __syncwarp();
       }
-      chain_phase(OFF_KD + kn * d, kd + kn * d, true, sq, rn, bn);
+      PROF(3)
+      chain_phase(OFF_KD + kn * DS, kd + kn * DS, true, sq, rn, bn);
+      PROF(4)
       const double varn = ddiv(dadd(dmul(dn, S.hvar[h]), sq), dadd(dn, 1.0));
       int kind;
       if (isbuf) {
@@ -818,10 +842,11 @@ __global__ void __launch_bounds__(32) k_resolve(DevTables t, IngestArgs a) {
           }
         }
       }
+      PROF(5)
       // ---- commit
       for (int i = lane; i < d; i += 32) {
-        hrep[h * d + i] = nrep[i];
-        if (buf_moved) hbrep[h * d + i] = nbrep[i];
+        hrep[h * DS + i] = nrep[i];
+        if (buf_moved) hbrep[h * DS + i] = nbrep[i];
       }
       if (lane == 0) {
         S.hdirty[h] = 1;
@@ -857,15 +882,28 @@ __global__ void __launch_bounds__(32) k_resolve(DevTables t, IngestArgs a) {
         }
       }
       if (kind == EV_DEFER && nb == 0) n = min(n + 1, cmax);
+      PROF(6)
       if (tt + 2 < T) {
+        double* kr = kd + ((tt + 2) % 3) * DS;
 #pragma unroll
         for (int j = 0; j < KPL; ++j) {
-          const int i = lane + 32 * j;
-          if (i < d) kd[((tt + 2) % 3) * d + i] = static_cast<double>(kpre[j]);
+          const int w = lane + 32 * j;
+          if (w < words) {
+            if (t.kv_bf16) {
+              kr[2 * w] = static_cast<double>(__uint_as_float(kpre[j] << 16));
+              kr[2 * w + 1] = static_cast<double>(__uint_as_float(kpre[j] & 0xffff0000u));
+            } else {
+              kr[w] = static_cast<double>(__uint_as_float(kpre[j]));
+            }
+          }
         }
       }
       __syncwarp();
+      PROF(7)
     }
+#undef PROF
+    if (lane == 0)
+      for (int k = 0; k < 8; ++k) a.prof[dom * 8 + k] = pr[k];
   }
 done:
   __syncwarp();
@@ -1704,7 +1742,7 @@ int launch_approx(const DevTables& t, const IngestArgs& a, cudaStream_t st) {
 }
 
 int launch_resolve(const DevTables& t, const IngestArgs& a, cudaStream_t st) {
-  const size_t smem = static_cast<size_t>(HOT) * 2 * t.d * 8 + static_cast<size_t>(6) * t.d * 8 +
+  const size_t smem = static_cast<size_t>(HOT) * 2 * padded(t.d) * 8 + static_cast<size_t>(6) * padded(t.d) * 8 +
                       static_cast<size_t>(t.tmax) * (8 + TOPM * (8 + 4 + 2) + 4) + 16 +
                       static_cast<size_t>(t.cmax) * (8 + 4 + 3) + 64;
   static bool attr = false;

@@ -138,6 +138,7 @@ struct IngestArgs {
   int32_t* ev_row;         // [L][tmax]
   // per-domain reserve of free pages carried between resolve launches (no pushes to the
   // shared free stack while pops may run concurrently)
+  long long* prof;         // [L][8] clock64 cycles per resolve phase (instrumentation)
   int32_t* dom_pool;       // [L][POOL]
   int32_t* dom_pool_n;     // [L]
 };
