@@ -285,6 +285,7 @@ def main():
             ev1.record(stream)
         torch.cuda.synchronize()
     decode_ms = ev0.elapsed_time(ev1)
+    k4_cycles = kv.resolve_profile(decode=True)
     decode_launches = kv.launch_count() - launches0
     kv.set_timing(False)
     # e2e decode: host query in, host output out, through the public API
@@ -334,7 +335,9 @@ def main():
         "phases_us": {"score_select": round(float(np.mean(k4_us)), 2), "attend": round(att_time * 1e6, 2),
                       "host_wait_device": round(float(np.mean([h[0] for h in host_ph])), 2),
                       "host_replay": round(float(np.mean([h[1] for h in host_ph])), 2),
-                      "host_repin": round(float(np.mean([h[2] for h in host_ph])), 2)},
+                      "host_repin": round(float(np.mean([h[2] for h in host_ph])), 2),
+                      "k4_cycles": dict(zip(["qnorm", "visual", "cand_score", "sort", "tail1", "ring", "desc", "-"],
+                                            k4_cycles.round(0).tolist()))},
         "clocks": clk.summary(),
         "ingest": {"value": round(frames_t / (ingest_ms * 1e-3), 1), "unit": "frames/s",
                    "frames": frames_t, "domains_per_frame": D * world, "tokens_per_frame": T_FRAME,

@@ -386,8 +386,10 @@ class ClusterKVCache:
     def set_timing(self, on: bool):
         lib().kvc_set_timing(self.h, 1 if on else 0)
 
-    def resolve_profile(self):
+    def resolve_profile(self, decode=False):
         t = np.zeros(8)
+        if decode:
+            t[0] = -1.0
         lib().kvc_debug_resolve_profile(self.h, _p(t, f64p))
         return t
 

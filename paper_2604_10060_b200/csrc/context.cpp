@@ -266,6 +266,7 @@ void Context::alloc_device() {
   da_.part_ml = static_cast<float*>(dalloc(L * da_.max_items * 2 * 4));
   da_.part_o = static_cast<float*>(dalloc(L * da_.max_items * d * 4));
   da_.dom_done = static_cast<std::int32_t*>(dalloc(L * 4));
+  da_.k4prof = static_cast<long long*>(dalloc(L * 8 * 8));
   da_.k_v = kv;
   da_.k_s = ks;
   da_.prefetch_k = kp;
@@ -311,7 +312,7 @@ void Context::ensure_idx(std::int64_t n, std::int64_t runs) {
 
 void Context::resolve_profile(double* out) {
   std::vector<long long> p(static_cast<std::size_t>(L_) * 8);
-  KVC_CUDA(cudaMemcpy(p.data(), ia_.prof, p.size() * 8, cudaMemcpyDeviceToHost));
+  KVC_CUDA(cudaMemcpy(p.data(), out[0] < 0 ? da_.k4prof : ia_.prof, p.size() * 8, cudaMemcpyDeviceToHost));
   for (int k = 0; k < 8; ++k) {
     double s = 0.0;
     for (int l = 0; l < L_; ++l) s += static_cast<double>(p[static_cast<std::size_t>(l) * 8 + k]);

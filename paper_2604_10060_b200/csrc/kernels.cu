@@ -1181,34 +1181,63 @@ __host__ __device__ inline int pow2_at_least(int n) {
   return p;
 }
 
+// Exact top-`take` selection by rank counting: rank(i) = #entries better than i under
+// (sim desc, key asc); keys are unique so ranks are a permutation. O(n^2 / threads) broadcast
+// shared reads, no sorting network and only one barrier.
+__device__ void block_rank_select(const double* sim, const long long* key, int n, int take, int* order) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const double si = sim[i];
+    const long long ki = key[i];
+    int r = 0;
+    for (int j = 0; j < n; ++j) r += better(sim[j], key[j], si, ki) ? 1 : 0;
+    if (r < take) order[r] = i;
+  }
+  __syncthreads();
+}
+
+constexpr int K4_ROWS = 128;  // representative rows staged per chunk
+
+__host__ __device__ inline size_t k4_smem_bytes(int d, int cmax, int parts, int W, int tmax) {
+  const int nsel = cmax > parts ? cmax : parts;
+  return static_cast<size_t>(d + 1) * 8 + static_cast<size_t>(nsel) * 16 + static_cast<size_t>(cmax) * 5 +
+         static_cast<size_t>(K4_ROWS) * (d + 1) * 8 + static_cast<size_t>(W) * tmax * 4 + 256;
+}
+
 __global__ void __launch_bounds__(256) k_score_select(DevTables t, DecodeArgs a, int* work_ctr) {
-  extern __shared__ uint8_t sm4[];
-  const int l = blockIdx.x, d = t.d, L = t.L;
-  const int P = *t.n_parts;
+  extern __shared__ __align__(16) uint8_t sm4[];
+  const int l = blockIdx.x, d = t.d, L = t.L, DS = d + 1;
+  const int P = a.n_parts_host;
   const int cmax = t.cmax;
-  const int ns = pow2_at_least(max(t.max_parts, cmax));
+  const int nsel = cmax > P ? cmax : P;
   uint8_t* p = sm4;
-  float* qf = reinterpret_cast<float*>(p);
-  p += ((d * 4 + 15) / 16) * 16;
+  double* qd = reinterpret_cast<double*>(p);  // query as double (exact conversion)
+  p += static_cast<size_t>(d + 1) * 8;
   double* sim = reinterpret_cast<double*>(p);
-  p += static_cast<size_t>(ns) * 8;
+  p += static_cast<size_t>(nsel) * 8;
   long long* key = reinterpret_cast<long long*>(p);
-  p += static_cast<size_t>(ns) * 8;
-  int* ord = reinterpret_cast<int*>(p);
-  p += static_cast<size_t>(ns) * 4;
+  p += static_cast<size_t>(nsel) * 8;
+  double* stage = reinterpret_cast<double*>(p);  // [K4_ROWS][d+1]
+  p += static_cast<size_t>(K4_ROWS) * DS * 8;
+  int* owners = reinterpret_cast<int*>(p);  // [W][tmax] ring owners of this domain
+  p += static_cast<size_t>(t.W) * t.tmax * 4;
   int* cslot = reinterpret_cast<int*>(p);
   p += static_cast<size_t>(cmax) * 4;
   uint8_t* cbuf = p;
   __shared__ double nq_s;
   __shared__ int ncand_s, chosen[64];
   __shared__ int vers[64], nver_s;
-  __shared__ int rank_slot[64], n_rank_s;
+  __shared__ int rank_slot[64], n_rank_s, order[64];
   __shared__ unsigned long long att_s;
   __shared__ bool degen;
 
+  long long kc0 = clock64();
+#define K4MARK(k) if (a.k4prof && threadIdx.x == 0) { const long long kc1 = clock64(); a.k4prof[l * 8 + (k)] = kc1 - kc0; kc0 = kc1; }
   if (l == 0 && threadIdx.x == 0) *work_ctr = 0;
   const float* q = a.q + static_cast<int64_t>(l) * d;
-  for (int i = threadIdx.x; i < d; i += blockDim.x) qf[i] = q[i];
+  for (int i = threadIdx.x; i < d; i += blockDim.x) qd[i] = static_cast<double>(q[i]);
+  // the window ring owners are needed after ranking; fetch them now
+  for (int i = threadIdx.x; i < t.W * t.tmax; i += blockDim.x)
+    owners[i] = t.ring_owner[static_cast<int64_t>(l) * t.W * t.tmax + i];
   if (threadIdx.x == 0) {
     degen = false;
     att_s = 0;
@@ -1216,34 +1245,31 @@ __global__ void __launch_bounds__(256) k_score_select(DevTables t, DecodeArgs a,
   __syncthreads();
   if (threadIdx.x == 0) {
     double s = 0.0;
-    for (int i = 0; i < d; ++i) s = dadd(s, dmul(static_cast<double>(qf[i]), static_cast<double>(qf[i])));
+#pragma unroll 16
+    for (int i = 0; i < d; ++i) s = dadd(s, dmul(qd[i], qd[i]));
     nq_s = __dsqrt_rn(s);
   }
   __syncthreads();
   const double nq = nq_s;
-  bool dg = false;
-  // ---- stage 1: visual_topk (index.cpp:192-208): exact cosines, sort (sim desc, id asc)
-  const int np2 = pow2_at_least(max(P, 1));
-  for (int pp = threadIdx.x; pp < np2; pp += blockDim.x) {
-    if (pp < P) {
-      sim[pp] = exact_cos(qf, nq, t.vrep + static_cast<int64_t>(pp) * d, t.vnorm[pp], d, dg);
-      key[pp] = pp;
-    } else {
-      sim[pp] = -INFINITY;
-      key[pp] = LLONG_MAX;
-    }
-    ord[pp] = pp;
+  if (nq < 1e-12 && threadIdx.x == 0) degen = true;
+  K4MARK(0)
+  // ---- stage 1: visual_topk (index.cpp:192-208): exact cosines, order (sim desc, id asc)
+  for (int pp = threadIdx.x; pp < P; pp += blockDim.x) {
+    const double* row = t.vrep + static_cast<int64_t>(pp) * d;
+    double acc = 0.0;
+#pragma unroll 16
+    for (int i = 0; i < d; ++i) acc = dadd(acc, dmul(qd[i], row[i]));
+    const double nr = t.vnorm[pp];
+    if (nr < 1e-12) degen = true;
+    sim[pp] = clamp1(ddiv(acc, dmul(nq, nr)));
+    key[pp] = pp;
   }
-  if (dg) degen = true;
   __syncthreads();
-  block_bitonic(sim, key, ord, np2);
   const int kv = min(a.k_v, P);
-  if (threadIdx.x < kv) {
-    chosen[threadIdx.x] = ord[threadIdx.x];
-    a.parts[l * a.k_v + threadIdx.x] = ord[threadIdx.x];
-  }
+  block_rank_select(sim, key, P, kv, chosen);
+  if (threadIdx.x < kv) a.parts[l * a.k_v + threadIdx.x] = chosen[threadIdx.x];
   if (threadIdx.x == 0) a.n_parts_sel[l] = kv;
-  __syncthreads();
+  K4MARK(1)
 
   // ---- stage 2: semantic_topk (index.cpp:210-240) and the prefetch ranking of layer l+1
   // with this layer's query (retrieval.cpp:117-128)
@@ -1275,27 +1301,37 @@ __global__ void __launch_bounds__(256) k_score_select(DevTables t, DecodeArgs a,
     __syncthreads();
     const int nc = min(ncand_s, cmax);
     if (pass == 0 && threadIdx.x == 0) a.n_cand[l] = nc;
-    const int nc2 = pow2_at_least(max(nc, 1));
-    dg = false;
-    for (int c = threadIdx.x; c < nc2; c += blockDim.x) {
-      if (c < nc) {
+    // exact cosines: rows staged through shared memory with coalesced loads, one sequential
+    // fp64 chain per candidate (vecmath.hpp:27-61)
+    for (int c0 = 0; c0 < nc; c0 += K4_ROWS) {
+      const int rows = min(K4_ROWS, nc - c0);
+      for (int idx = threadIdx.x; idx < rows * d; idx += blockDim.x) {
+        const int r = idx / d, i = idx - r * d;
+        const int s = cslot[c0 + r];
+        stage[r * DS + i] = (cbuf[c0 + r] ? t.brep64 : t.rep64)[static_cast<int64_t>(s) * d + i];
+      }
+      __syncthreads();
+      for (int r = threadIdx.x; r < rows; r += blockDim.x) {
+        const int c = c0 + r;
         const int s = cslot[c];
         const bool ib = cbuf[c];
-        sim[c] = exact_cos(qf, nq, (ib ? t.brep64 : t.rep64) + static_cast<int64_t>(s) * d,
-                           ib ? t.bnorm[s] : t.rnorm[s], d, dg);
+        const double* row = stage + r * DS;
+        double acc = 0.0;
+#pragma unroll 16
+        for (int i = 0; i < d; ++i) acc = dadd(acc, dmul(qd[i], row[i]));
+        const double nr = ib ? t.bnorm[s] : t.rnorm[s];
+        if (nr < 1e-12) degen = true;
+        sim[c] = clamp1(ddiv(acc, dmul(nq, nr)));
         key[c] = 2LL * t.cid[s] + (ib ? 1 : 0);
-      } else {
-        sim[c] = -INFINITY;
-        key[c] = LLONG_MAX;
       }
-      ord[c] = c;
+      __syncthreads();
     }
-    if (dg) degen = true;
-    __syncthreads();
-    block_bitonic(sim, key, ord, nc2);
+    K4MARK(2)
     const int take = min(ktake, nc);
+    block_rank_select(sim, key, nc, take, order);
+    K4MARK(3)
     if (threadIdx.x < take) {
-      const int b = ord[threadIdx.x];
+      const int b = order[threadIdx.x];
       if (pass == 0) {
         rank_slot[threadIdx.x] = cslot[b];
         a.ranked_slot[l * a.k_s + threadIdx.x] = cslot[b];
@@ -1344,11 +1380,12 @@ __global__ void __launch_bounds__(256) k_score_select(DevTables t, DecodeArgs a,
   }
   if (threadIdx.x < 64) ring_cnt[threadIdx.x] = 0;
   __syncthreads();
+  K4MARK(4)
   // window ring: tokens whose owner is not a verified cluster (retrieval.cpp:107-108 dedup)
   for (int i = threadIdx.x; i < W * t.tmax; i += blockDim.x) {
     const int rs = i / t.tmax, tt = i % t.tmax;
     if (tt >= t.ring_count[rs]) continue;
-    const int own = t.ring_owner[(static_cast<int64_t>(l) * W + rs) * t.tmax + tt];
+    const int own = owners[rs * t.tmax + tt];
     bool m = false;
     for (int j = 0; j < nv; ++j) m |= vers[j] == own;
     if (!m) {
@@ -1378,6 +1415,7 @@ __global__ void __launch_bounds__(256) k_score_select(DevTables t, DecodeArgs a,
     a.attended[l] = static_cast<int64_t>(att_s);
   }
   __syncthreads();
+  K4MARK(5)
   int4* desc = a.desc + static_cast<int64_t>(l) * a.max_desc;
   const int ndesc = voff[nv];
   for (int i = threadIdx.x; i < ndesc && i < a.max_desc; i += blockDim.x) {
@@ -1397,6 +1435,8 @@ __global__ void __launch_bounds__(256) k_score_select(DevTables t, DecodeArgs a,
       desc[ring_off[i]] = make_int4(page, t.pg_fill[page], 2 | (rs << 8), j * t.P);
     }
   __syncthreads();
+  K4MARK(6)
+#undef K4MARK
   if (a.n_items[l] == 0)  // nothing attended: output zeros
     for (int i = threadIdx.x; i < d; i += blockDim.x) a.out[static_cast<int64_t>(l) * d + i] = 0.f;
 }
@@ -1431,16 +1471,44 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 
 struct StageMeta {
   int dom, item, page, fill;
-  int kind, ring_slot, tok0, flags;  // flags: 1 first page of item, 2 last page of item
+  int kind, ring_slot, tok0, flags;  // flags: 1 first page of item, 2 last page, 4 end of work
+  int nver;
+  int ver[64];                        // verified slots of the domain (ring-page masking)
 };
 
-// 8 warps; a 64-token sub-tile of a page is split 8 tokens per warp, 4 lanes per token
-// (D/4 dims each, two accumulators) for q.k; each lane owns D/32 output dims for p.v.
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                              uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void named_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+// Warp-specialised split-KV attention. Warp ATT_WARPS (the producer) walks the page descriptors
+// of claimed items and issues TMA bulk copies (K rows, V rows and the domain's query) into a ring
+// of STAGES shared-memory stages, with L2 evict-first hints so the streamed K/V do not evict the
+// cluster representatives K4 re-reads every step; "full" mbarriers carry the transaction bytes.
+// The ATT_WARPS consumer warps process a 64-token sub-tile 8 tokens per warp, 4 lanes per token
+// (D/4 dims, two accumulators), keep a per-warp online softmax, and release each stage through
+// an "empty" mbarrier (no CTA-wide barrier per page). At the end of an item the consumers merge
+// their states (named barrier) into a partial; the last CTA to finish a domain combines them.
 constexpr int ATT_THREADS = 256;
 constexpr int ATT_WARPS = ATT_THREADS / 32;
 
 template <int D, bool BF16, int STAGES>
-__global__ void __launch_bounds__(ATT_THREADS) k_attend(DevTables t, DecodeArgs a, int* work_ctr) {
+__global__ void __launch_bounds__(ATT_THREADS + 32) k_attend(DevTables t, DecodeArgs a, int* work_ctr) {
   constexpr int ES = BF16 ? 2 : 4;
   constexpr int ROWB = D * ES;
   constexpr int QB = ROWB / 4;  // bytes of a row handled by one lane for q.k
@@ -1449,25 +1517,26 @@ __global__ void __launch_bounds__(ATT_THREADS) k_attend(DevTables t, DecodeArgs 
   constexpr int OPL = D / 32;   // output dims per lane
   extern __shared__ __align__(128) uint8_t sm6[];
   const int P = t.P;
-  const int64_t stage_bytes = static_cast<int64_t>(2) * P * ROWB;
+  const int64_t kv_bytes = static_cast<int64_t>(2) * P * ROWB;
+  const int64_t stage_bytes = kv_bytes + D * 4;  // K rows, V rows, query (fp32)
   uint8_t* stages = sm6;
-  __shared__ __align__(8) uint64_t full[STAGES];
+  __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
   __shared__ StageMeta meta[STAGES];
-  __shared__ float qs[D];
-  __shared__ int vers_s[64];
-  __shared__ int nver_sh;
   __shared__ int prefix[1025];
   __shared__ float wm[ATT_WARPS], wl[ATT_WARPS];
   __shared__ float wo[ATT_WARPS][D];
   __shared__ int last_flag;
-  __shared__ int issued[STAGES];
-  __shared__ int4 pq[32];
+  __shared__ int4 pq_s[32];
+  __shared__ int pver_s[64];
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int L = min(t.L, 1024);
   for (int l = tid; l < L; l += blockDim.x) prefix[l + 1] = a.n_items[l];
   if (tid == 0) {
-    for (int s = 0; s < STAGES; ++s) mbar_init(&full[s], 1);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], ATT_WARPS);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -1478,90 +1547,98 @@ __global__ void __launch_bounds__(ATT_THREADS) k_attend(DevTables t, DecodeArgs 
   __syncthreads();
   const int total = prefix[L];
 
-  // ---- producer (thread 0): the current item's page descriptors live in smem
-  int p_n = 0, p_k = 0, p_dom = 0, p_j = 0;
-  bool p_done = false;
-  auto produce = [&](int s) -> bool {
-    if (p_done) return false;
-    if (p_k >= p_n) {
-      const int g = atomicAdd(work_ctr, 1);
-      if (g >= total) {
-        p_done = true;
-        return false;
+  if (warp == ATT_WARPS) {
+    // ================================================================ producer warp
+    if (lane != 0) return;
+    const uint64_t pol = policy_evict_first();
+    int p_n = 0, p_k = 0, p_dom = 0, p_j = 0, p_nver = 0;
+    int4* pq = pq_s;     // the claimed item's page descriptors
+    int* pver = pver_s;  // the domain's verified slots
+    for (int it = 0;; ++it) {
+      const int s = it % STAGES;
+      if (it >= STAGES) mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
+      StageMeta& m = meta[s];
+      if (p_k >= p_n) {  // claim the next item
+        const int g = atomicAdd(work_ctr, 1);
+        if (g >= total) {
+          m.flags = 4;
+          mbar_arrive(&full[s]);
+          break;
+        }
+        int lo = 0, hi = L;
+        while (hi - lo > 1) {
+          const int mid = (lo + hi) / 2;
+          if (prefix[mid] <= g) lo = mid; else hi = mid;
+        }
+        const bool new_dom = lo != p_dom || it == 0;
+        p_dom = lo;
+        p_j = g - prefix[lo];
+        const int first = p_j * a.chunk_pages;
+        p_n = min(a.chunk_pages, a.n_desc[p_dom] - first);
+        const int4* src = a.desc + static_cast<int64_t>(p_dom) * a.max_desc + first;
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          if (i < p_n) pq[i] = src[i];
+        if (new_dom) {
+          p_nver = a.n_ver[p_dom];
+          for (int i = 0; i < 64; ++i)
+            if (i < p_nver) pver[i] = a.ver_slot[p_dom * a.k_s + i];
+        }
+        p_k = 0;
       }
-      int lo = 0, hi = L;
-      while (hi - lo > 1) {
-        const int mid = (lo + hi) / 2;
-        if (prefix[mid] <= g) lo = mid; else hi = mid;
+      const int4 dsc = pq[p_k];
+      m.dom = p_dom;
+      m.item = p_j;
+      m.page = dsc.x;
+      m.fill = dsc.y;
+      m.kind = dsc.z & 0xff;
+      m.ring_slot = dsc.z >> 8;
+      m.tok0 = dsc.w;
+      m.flags = (p_k == 0 ? 1 : 0) | (p_k == p_n - 1 ? 2 : 0);
+      if (m.kind == 2) {
+        m.nver = p_nver;
+        for (int i = 0; i < p_nver; ++i) m.ver[i] = pver[i];
       }
-      p_dom = lo;
-      p_j = g - prefix[lo];
-      const int first = p_j * a.chunk_pages;
-      p_n = min(a.chunk_pages, a.n_desc[p_dom] - first);
-      const int4* src = a.desc + static_cast<int64_t>(p_dom) * a.max_desc + first;
-#pragma unroll 8
-      for (int i = 0; i < 32; ++i)
-        if (i < p_n) pq[i] = src[i];
-      p_k = 0;
+      p_k += 1;
+      const uint32_t bytes = static_cast<uint32_t>(m.fill) * ROWB;
+      uint8_t* dst = stages + s * stage_bytes;
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_expect(&full[s], 2 * bytes + D * 4);
+      bulk_g2s_hint(dst, page_k(t, m.page), bytes, &full[s], pol);
+      bulk_g2s_hint(dst + static_cast<int64_t>(P) * ROWB, page_v(t, m.page), bytes, &full[s], pol);
+      bulk_g2s(dst + kv_bytes, a.q + static_cast<int64_t>(m.dom) * D, D * 4, &full[s]);
     }
-    const int4 dsc = pq[p_k];
-    StageMeta m;
-    m.dom = p_dom;
-    m.item = p_j;
-    m.page = dsc.x;
-    m.fill = dsc.y;
-    m.kind = dsc.z & 0xff;
-    m.ring_slot = dsc.z >> 8;
-    m.tok0 = dsc.w;
-    m.flags = (p_k == 0 ? 1 : 0) | (p_k == p_n - 1 ? 2 : 0);
-    p_k += 1;
-    meta[s] = m;
-    const uint32_t bytes = static_cast<uint32_t>(m.fill) * ROWB;
-    uint8_t* dst = stages + s * stage_bytes;
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    mbar_expect(&full[s], 2 * bytes);
-    bulk_g2s(dst, page_k(t, m.page), bytes, &full[s]);
-    bulk_g2s(dst + static_cast<int64_t>(P) * ROWB, page_v(t, m.page), bytes, &full[s]);
-    return true;
-  };
-  if (tid == 0)
-    for (int s = 0; s < STAGES; ++s) issued[s] = produce(s) ? 1 : 0;
-  __syncthreads();
+    return;
+  }
 
+  // ================================================================== consumer warps
   float m_run = -INFINITY, l_run = 0.f;
   float o_run[OPL];
 #pragma unroll
   for (int i = 0; i < OPL; ++i) o_run[i] = 0.f;
-  int cur_dom = -1;
-  uint32_t phase_bits = 0;
   const float sl2 = a.scale_log2;
   const int sub = lane >> 2;   // token within the warp's 8
   const int part = lane & 3;   // quarter of the row for q.k
 
-  for (int s = 0;; s = (s + 1) % STAGES) {
-    if (!issued[s]) break;
-    mbar_wait(&full[s], (phase_bits >> s) & 1u);
-    phase_bits ^= (1u << s);
-    const StageMeta m = meta[s];
-    if ((m.flags & 1) && m.dom != cur_dom) {  // load the domain's query and verified list
-      __syncthreads();
-      for (int i = tid; i < D; i += ATT_THREADS) qs[i] = a.q[static_cast<int64_t>(m.dom) * D + i];
-      if (tid == 0) nver_sh = a.n_ver[m.dom];
-      if (tid < 64) vers_s[tid] = tid < a.n_ver[m.dom] ? a.ver_slot[m.dom * a.k_s + tid] : -1;
-      __syncthreads();
-      cur_dom = m.dom;
-    }
+  for (int it = 0;; ++it) {
+    const int s = it % STAGES;
+    mbar_wait(&full[s], (it / STAGES) & 1);
+    const StageMeta& m = meta[s];
+    const int flags = m.flags;
+    if (flags & 4) break;
+    const int fill = m.fill, kind = m.kind;
     const uint8_t* Ks = stages + s * stage_bytes;
     const uint8_t* Vs = Ks + static_cast<int64_t>(P) * ROWB;
-    for (int tb = 0; tb < m.fill; tb += 64) {
+    const float* qs = reinterpret_cast<const float*>(Ks + kv_bytes);
+    for (int tb = 0; tb < fill; tb += 64) {
       const int tok = tb + warp * 8 + sub;
-      bool valid = tok < m.fill;
-      if (valid && m.kind == 2) {
+      bool valid = tok < fill;
+      if (valid && kind == 2) {
         const int own = t.ring_owner[(static_cast<int64_t>(m.dom) * t.W + m.ring_slot) * t.tmax + m.tok0 + tok];
-        for (int j = 0; j < nver_sh; ++j) valid &= vers_s[j] != own;
+        for (int j = 0; j < m.nver; ++j) valid &= m.ver[j] != own;
       }
       float acc0 = 0.f, acc1 = 0.f;
-      if (tok < m.fill) {
+      if (tok < fill) {
         const uint8_t* krow = Ks + static_cast<int64_t>(tok) * ROWB + part * QB;
         const float* qq0 = qs + part * (D / 4);
 #pragma unroll
@@ -1608,7 +1685,7 @@ __global__ void __launch_bounds__(ATT_THREADS) k_attend(DevTables t, DecodeArgs 
       for (int j = 0; j < 8; ++j) {
         const float pj = __shfl_sync(kFull, pr, 4 * j);
         const int tj = tb + warp * 8 + j;
-        if (tj >= m.fill) break;
+        if (tj >= fill) break;
         const uint8_t* vrow = Vs + static_cast<int64_t>(tj) * ROWB + lane * OPL * ES;
         if (BF16) {
 #pragma unroll
@@ -1623,19 +1700,20 @@ __global__ void __launch_bounds__(ATT_THREADS) k_attend(DevTables t, DecodeArgs 
         }
       }
     }
-    __syncthreads();  // stage s consumed
-    if (tid == 0) issued[s] = produce(s) ? 1 : 0;  // refill while the item epilogue runs
-    if (m.flags & 2) {  // item done: merge warps, write the partial, maybe combine the domain
+    const int dom = m.dom, item = m.item;
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);  // stage s released by this warp
+    if (flags & 2) {  // item done: merge the warps, write the partial, maybe combine the domain
       if (lane == 0) {
         wm[warp] = m_run;
         wl[warp] = l_run;
       }
 #pragma unroll
       for (int i = 0; i < OPL; ++i) wo[warp][lane * OPL + i] = o_run[i];
-      __syncthreads();
+      named_sync(1, ATT_THREADS);
       float M = -INFINITY;
       for (int w = 0; w < ATT_WARPS; ++w) M = fmaxf(M, wm[w]);
-      const int64_t pi = static_cast<int64_t>(m.dom) * a.max_items + m.item;
+      const int64_t pi = static_cast<int64_t>(dom) * a.max_items + item;
       for (int c = tid; c < D; c += ATT_THREADS) {
         float o = 0.f;
         for (int w = 0; w < ATT_WARPS; ++w)
@@ -1650,13 +1728,13 @@ __global__ void __launch_bounds__(ATT_THREADS) k_attend(DevTables t, DecodeArgs 
         a.part_ml[pi * 2 + 1] = lsum;
       }
       __threadfence();
-      __syncthreads();
-      if (tid == 0) last_flag = (atomicAdd(&a.dom_done[m.dom], 1) + 1 == a.n_items[m.dom]);
-      __syncthreads();
+      named_sync(1, ATT_THREADS);
+      if (tid == 0) last_flag = (atomicAdd(&a.dom_done[dom], 1) + 1 == a.n_items[dom]);
+      named_sync(1, ATT_THREADS);
       if (last_flag) {  // split-KV combine of all partials of the domain
         __threadfence();
-        const int ni = a.n_items[m.dom];
-        const float* ml = a.part_ml + static_cast<int64_t>(m.dom) * a.max_items * 2;
+        const int ni = a.n_items[dom];
+        const float* ml = a.part_ml + static_cast<int64_t>(dom) * a.max_items * 2;
         float MM = -INFINITY;
         for (int i = 0; i < ni; ++i) MM = fmaxf(MM, ml[2 * i]);
         for (int c = tid; c < D; c += ATT_THREADS) {
@@ -1664,19 +1742,19 @@ __global__ void __launch_bounds__(ATT_THREADS) k_attend(DevTables t, DecodeArgs 
           for (int i = 0; i < ni; ++i) {
             if (ml[2 * i] == -INFINITY) continue;
             const float w = exp2f(ml[2 * i] - MM);
-            num += w * a.part_o[(static_cast<int64_t>(m.dom) * a.max_items + i) * D + c];
+            num += w * a.part_o[(static_cast<int64_t>(dom) * a.max_items + i) * D + c];
             den += w * ml[2 * i + 1];
           }
-          a.out[static_cast<int64_t>(m.dom) * D + c] = den > 0.f ? num / den : 0.f;
+          a.out[static_cast<int64_t>(dom) * D + c] = den > 0.f ? num / den : 0.f;
         }
-        if (tid == 0) a.dom_done[m.dom] = 0;
+        if (tid == 0) a.dom_done[dom] = 0;
       }
       m_run = -INFINITY;
       l_run = 0.f;
 #pragma unroll
       for (int i = 0; i < OPL; ++i) o_run[i] = 0.f;
+      named_sync(1, ATT_THREADS);  // wo / last_flag reuse
     }
-    __syncthreads();
   }
 }
 
@@ -1847,7 +1925,7 @@ int* g_ctr = nullptr;
 template <int D, bool BF16>
 int launch_attend_t(const DevTables& t, const DecodeArgs& a, cudaStream_t st) {
   constexpr int STAGES = BF16 ? 3 : 2;
-  const size_t smem = static_cast<size_t>(STAGES) * 2 * t.P * D * (BF16 ? 2 : 4);
+  const size_t smem = static_cast<size_t>(STAGES) * (2 * t.P * D * (BF16 ? 2 : 4) + D * 4);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_attend<D, BF16, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1855,9 +1933,9 @@ int launch_attend_t(const DevTables& t, const DecodeArgs& a, cudaStream_t st) {
     attr = true;
   }
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_attend<D, BF16, STAGES>, ATT_THREADS, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_attend<D, BF16, STAGES>, ATT_THREADS + 32, smem);
   per_sm = max(1, per_sm);
-  k_attend<D, BF16, STAGES><<<g_sms * per_sm, ATT_THREADS, smem, st>>>(t, a, g_ctr);
+  k_attend<D, BF16, STAGES><<<g_sms * per_sm, ATT_THREADS + 32, smem, st>>>(t, a, g_ctr);
   return 1;
 }
 }  // namespace
@@ -1870,12 +1948,10 @@ int launch_decode(const DevTables& t, const DecodeArgs& a, cudaStream_t st, cuda
     cudaMalloc(&g_ctr, 64);
   }
   if (ev) cudaEventRecord(ev[0], st);
-  const int ns = pow2_at_least(t.max_parts > t.cmax ? t.max_parts : t.cmax);
-  const size_t smem4 = ((t.d * 4 + 15) / 16) * 16 + static_cast<size_t>(ns) * 20 +
-                       static_cast<size_t>(t.cmax) * 5 + 64;
+  const size_t smem4 = k4_smem_bytes(t.d, t.cmax, a.n_parts_host, t.W, t.tmax);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_score_select, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_score_select, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     attr = true;
   }
   k_score_select<<<t.L, 256, smem4, st>>>(t, a, g_ctr);

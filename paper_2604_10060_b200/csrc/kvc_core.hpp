@@ -175,6 +175,7 @@ struct DecodeArgs {
   int32_t* dom_done;       // [L] completion counters (reset by the combine)
   float* out;              // [L][d]
   float scale_log2;        // log2(e) / sqrt(d)
+  long long* k4prof;       // [L][8] clock64 phase cycles (instrumentation; may be null)
 };
 
 // ----------------------------------------------------------------------------- launchers
