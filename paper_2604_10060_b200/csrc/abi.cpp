@@ -34,6 +34,16 @@ int guard(F&& f) {
   }
 }
 
+// Host-state readers first complete the deferred bookkeeping of the last decode step.
+Context& F(kvc_ctx* c) {
+  try {
+    c->impl->flush_pending();
+  } catch (const std::exception& e) {
+    g_err = e.what();
+  }
+  return *c->impl;
+}
+
 template <class T>
 int copy_out(const std::vector<T>& v, T* dst, int cap) {
   const int n = static_cast<int>(v.size());
@@ -115,7 +125,7 @@ void* kvc_stream(kvc_ctx* ctx) { return ctx ? static_cast<void*>(ctx->impl->stre
 int kvc_ingest_frame(kvc_ctx* ctx, int64_t frame_id, const float* visual, const void* keys,
                      const void* values, int32_t T, int32_t mem, int64_t* assigned,
                      int64_t* partition) {
-  return guard([&] { ctx->impl->ingest_frame(frame_id, visual, keys, values, T, mem, assigned, partition); });
+  return guard([&] { F(ctx).ingest_frame(frame_id, visual, keys, values, T, mem, assigned, partition); });
 }
 
 int kvc_decode_step(kvc_ctx* ctx, int64_t query_id, const float* q, int32_t q_mem, float* out,
@@ -124,7 +134,7 @@ int kvc_decode_step(kvc_ctx* ctx, int64_t query_id, const float* q, int32_t q_me
 }
 
 int kvc_last_ranked(kvc_ctx* ctx, int32_t layer, int64_t* ids, int32_t* is_buffer, int32_t cap) {
-  const auto& ls = ctx->impl->last_layers();
+  const auto& ls = F(ctx).last_layers();
   if (layer < 0 || layer >= static_cast<int>(ls.size())) return KVC_E_BAD_LAYER;
   const auto& r = ls[static_cast<std::size_t>(layer)].ranked;
   for (int i = 0; i < static_cast<int>(r.size()) && i < cap; ++i) {
@@ -135,13 +145,13 @@ int kvc_last_ranked(kvc_ctx* ctx, int32_t layer, int64_t* ids, int32_t* is_buffe
 }
 
 int kvc_last_selected(kvc_ctx* ctx, int32_t layer, int64_t* ids, int32_t cap) {
-  const auto& ls = ctx->impl->last_layers();
+  const auto& ls = F(ctx).last_layers();
   if (layer < 0 || layer >= static_cast<int>(ls.size())) return KVC_E_BAD_LAYER;
   return copy_out(ls[static_cast<std::size_t>(layer)].selected, ids, cap);
 }
 
 int kvc_last_attended(kvc_ctx* ctx, int32_t layer, int64_t* frames, int32_t* tokens, int32_t cap) {
-  const auto& ls = ctx->impl->last_layers();
+  const auto& ls = F(ctx).last_layers();
   if (layer < 0 || layer >= static_cast<int>(ls.size())) return KVC_E_BAD_LAYER;
   const auto& a = ls[static_cast<std::size_t>(layer)].attended;
   for (int i = 0; i < static_cast<int>(a.size()) && i < cap; ++i) {
@@ -152,7 +162,7 @@ int kvc_last_attended(kvc_ctx* ctx, int32_t layer, int64_t* frames, int32_t* tok
 }
 
 int kvc_last_layer_meta(kvc_ctx* ctx, int32_t layer, double* lat, int64_t* ints) {
-  const auto& ls = ctx->impl->last_layers();
+  const auto& ls = F(ctx).last_layers();
   if (layer < 0 || layer >= static_cast<int>(ls.size())) return KVC_E_BAD_LAYER;
   const auto& lo = ls[static_cast<std::size_t>(layer)];
   for (int i = 0; i < 5; ++i) lat[i] = lo.lat[i];
@@ -165,18 +175,18 @@ int kvc_last_layer_meta(kvc_ctx* ctx, int32_t layer, double* lat, int64_t* ints)
 }
 
 int kvc_last_query_meta(kvc_ctx* ctx, double* dd) {
-  dd[0] = ctx->impl->last_ttft();
-  dd[1] = ctx->impl->last_recall();
+  dd[0] = F(ctx).last_ttft();
+  dd[1] = F(ctx).last_recall();
   return KVC_OK;
 }
 
-uint64_t kvc_last_digest(kvc_ctx* ctx) { return ctx->impl->last_digest(); }
+uint64_t kvc_last_digest(kvc_ctx* ctx) { return F(ctx).last_digest(); }
 
 int kvc_flat_topk(kvc_ctx* ctx, const float* q, int32_t layer, int32_t k, int64_t* ids,
                   int32_t* is_buffer) {
   int n = 0;
   const int rc = guard([&] {
-    auto r = ctx->impl->flat_topk(q, layer, k);
+    auto r = F(ctx).flat_topk(q, layer, k);
     n = static_cast<int>(r.size());
     for (int i = 0; i < n; ++i) {
       ids[i] = r[static_cast<std::size_t>(i)].first;
@@ -187,28 +197,28 @@ int kvc_flat_topk(kvc_ctx* ctx, const float* q, int32_t layer, int32_t k, int64_
 }
 
 int kvc_build_now(kvc_ctx* ctx) {
-  return guard([&] { ctx->impl->build_now(); });
+  return guard([&] { F(ctx).build_now(); });
 }
 
 int kvc_bulk_load(kvc_ctx* ctx, const float* visual, const void* keys, const void* values,
                   int32_t N, int32_t C, const int32_t* assign, const int64_t* frame_ids,
                   const int32_t* token_ids, int32_t mem, int64_t* partition) {
   return guard([&] {
-    const int64_t p = ctx->impl->bulk_load(visual, keys, values, N, C, assign, frame_ids, token_ids, mem);
+    const int64_t p = F(ctx).bulk_load(visual, keys, values, N, C, assign, frame_ids, token_ids, mem);
     if (partition) *partition = p;
   });
 }
 
-int kvc_n_clusters(kvc_ctx* ctx) { return static_cast<int>(ctx->impl->cluster_ids().size()); }
+int kvc_n_clusters(kvc_ctx* ctx) { return static_cast<int>(F(ctx).cluster_ids().size()); }
 
 int kvc_cluster_ids(kvc_ctx* ctx, int64_t* ids, int32_t cap) {
-  return copy_out(ctx->impl->cluster_ids(), ids, cap);
+  return copy_out(F(ctx).cluster_ids(), ids, cap);
 }
 
 int kvc_cluster(kvc_ctx* ctx, int64_t id, int64_t* info, double* var, double* rep,
                 double* buffer_rep) {
   return guard([&] {
-    const kvc::Cluster* c = ctx->impl->cluster(id);
+    const kvc::Cluster* c = F(ctx).cluster(id);
     if (!c) kvc::fail(KVC_E_UNKNOWN_CLUSTER, "unknown cluster id: " + std::to_string(id));
     info[0] = c->layer;
     info[1] = c->parent;
@@ -221,14 +231,14 @@ int kvc_cluster(kvc_ctx* ctx, int64_t id, int64_t* info, double* var, double* re
     info[8] = c->first_frame;
     info[9] = c->last_touch;
     double v = 0.0;
-    ctx->impl->cluster_stats(id, &v, rep, buffer_rep);
+    F(ctx).cluster_stats(id, &v, rep, buffer_rep);
     if (var) *var = v;
   });
 }
 
 int kvc_cluster_entries(kvc_ctx* ctx, int64_t id, int32_t which, int64_t* frames, int32_t* tokens,
                         int32_t cap) {
-  const kvc::Cluster* c = ctx->impl->cluster(id);
+  const kvc::Cluster* c = F(ctx).cluster(id);
   if (!c) return KVC_E_UNKNOWN_CLUSTER;
   const auto& v = which == 0 ? c->members : c->buffer;
   for (int i = 0; i < static_cast<int>(v.size()) && i < cap; ++i) {
@@ -241,14 +251,14 @@ int kvc_cluster_entries(kvc_ctx* ctx, int64_t id, int32_t which, int64_t* frames
 int kvc_cluster_payload(kvc_ctx* ctx, int64_t id, int32_t which, float* keys, float* values,
                         int32_t cap) {
   int n = 0;
-  const int rc = guard([&] { n = ctx->impl->cluster_payload(id, which, keys, values, cap); });
+  const int rc = guard([&] { n = F(ctx).cluster_payload(id, which, keys, values, cap); });
   return rc != KVC_OK ? rc : n;
 }
 
-int kvc_n_partitions(kvc_ctx* ctx) { return static_cast<int>(ctx->impl->partitions().size()); }
+int kvc_n_partitions(kvc_ctx* ctx) { return static_cast<int>(F(ctx).partitions().size()); }
 
 int kvc_partition(kvc_ctx* ctx, int32_t p, double* visual_rep, int64_t* frames, int32_t cap) {
-  const auto& ps = ctx->impl->partitions();
+  const auto& ps = F(ctx).partitions();
   if (p < 0 || p >= static_cast<int>(ps.size())) return KVC_E_UNKNOWN_CLUSTER;
   const auto& part = ps[static_cast<std::size_t>(p)];
   if (visual_rep) std::memcpy(visual_rep, part.vrep.data(), part.vrep.size() * sizeof(double));
@@ -256,14 +266,14 @@ int kvc_partition(kvc_ctx* ctx, int32_t p, double* visual_rep, int64_t* frames, 
 }
 
 int kvc_partition_layer(kvc_ctx* ctx, int32_t p, int32_t layer, int64_t* ids, int32_t cap) {
-  const auto& ps = ctx->impl->partitions();
+  const auto& ps = F(ctx).partitions();
   if (p < 0 || p >= static_cast<int>(ps.size())) return KVC_E_UNKNOWN_CLUSTER;
-  if (layer < 0 || layer >= ctx->impl->L()) return KVC_E_BAD_LAYER;
+  if (layer < 0 || layer >= F(ctx).L()) return KVC_E_BAD_LAYER;
   return copy_out(ps[static_cast<std::size_t>(p)].per_layer[static_cast<std::size_t>(layer)], ids, cap);
 }
 
 int kvc_maint_stats(kvc_ctx* ctx, int64_t* out) {
-  std::memcpy(out, ctx->impl->maint_stats(), 9 * sizeof(int64_t));
+  std::memcpy(out, F(ctx).maint_stats(), 9 * sizeof(int64_t));
   return KVC_OK;
 }
 
@@ -273,18 +283,18 @@ int64_t kvc_ledger(kvc_ctx* ctx, int64_t* ops, int64_t* bytes, double* cost_us) 
     bytes[i] = 0;
     cost_us[i] = 0.0;
   }
-  for (const auto& op : ctx->impl->ledger()) {  // TransferLedger::record (store.cpp:21-27)
+  for (const auto& op : F(ctx).ledger()) {  // TransferLedger::record (store.cpp:21-27)
     ops[op.cause] += op.n_ops;
     bytes[op.cause] += op.bytes;
     cost_us[op.cause] += op.cost_us;
   }
-  return ctx->impl->device_entries();
+  return F(ctx).device_entries();
 }
 
-int kvc_ledger_log_size(kvc_ctx* ctx) { return static_cast<int>(ctx->impl->ledger().size()); }
+int kvc_ledger_log_size(kvc_ctx* ctx) { return static_cast<int>(F(ctx).ledger().size()); }
 
 int kvc_ledger_op(kvc_ctx* ctx, int32_t i, int64_t* ints) {
-  const auto& lg = ctx->impl->ledger();
+  const auto& lg = F(ctx).ledger();
   if (i < 0 || i >= static_cast<int>(lg.size())) return KVC_E_CONFIG;
   const auto& op = lg[static_cast<std::size_t>(i)];
   ints[0] = op.cause;
@@ -295,12 +305,12 @@ int kvc_ledger_op(kvc_ctx* ctx, int32_t i, int64_t* ints) {
 }
 
 int kvc_check(kvc_ctx* ctx) {
-  return guard([&] { ctx->impl->check(); });
+  return guard([&] { F(ctx).check(); });
 }
 
 int kvc_offload(kvc_ctx* ctx, int64_t id, double* cost_us) {
   return guard([&] {
-    const double c = ctx->impl->offload(id);
+    const double c = F(ctx).offload(id);
     if (cost_us) *cost_us = c;
   });
 }
@@ -308,7 +318,7 @@ int kvc_offload(kvc_ctx* ctx, int64_t id, double* cost_us) {
 int kvc_fetch(kvc_ctx* ctx, int64_t id, int32_t cause, double* cost_us) {
   return guard([&] {
     if (cause < 0 || cause > 4) kvc::fail(KVC_E_CONFIG, "unknown transfer cause");
-    const double c = ctx->impl->fetch(id, cause);
+    const double c = F(ctx).fetch(id, cause);
     if (cost_us) *cost_us = c;
   });
 }

@@ -243,10 +243,11 @@ void Context::alloc_device() {
   const std::size_t o_parts = carve(L * kv * 4), o_nps = carve(L * 4), o_rs = carve(L * ks * 4),
                     o_rb = carve(L * ks), o_nr = carve(L * 4), o_ps = carve(L * kp * 4),
                     o_pb = carve(L * kp), o_np = carve(L * 4), o_vs = carve(L * ks * 4),
-                    o_nv = carve(L * 4), o_att = carve(L * 8), o_nc = carve(L * 4);
+                    o_nv = carve(L * 4), o_att = carve(L * 8), o_nc = carve(L * 4), o_fl = carve(16);
   dec_bytes_ = off;
   d_dec_ = dalloc(dec_bytes_);
   h_dec_ = halloc(dec_bytes_);
+  h_dec2_ = halloc(dec_bytes_);
   auto* base = static_cast<std::uint8_t*>(d_dec_);
   da_.parts = reinterpret_cast<std::int32_t*>(base + o_parts);
   da_.n_parts_sel = reinterpret_cast<std::int32_t*>(base + o_nps);
@@ -260,6 +261,7 @@ void Context::alloc_device() {
   da_.n_ver = reinterpret_cast<std::int32_t*>(base + o_nv);
   da_.attended = reinterpret_cast<std::int64_t*>(base + o_att);
   da_.n_cand = reinterpret_cast<std::int32_t*>(base + o_nc);
+  da_.flags = reinterpret_cast<std::int32_t*>(base + o_fl);
   da_.desc = static_cast<int4*>(dalloc(L * da_.max_desc * sizeof(int4)));
   da_.n_desc = static_cast<std::int32_t*>(dalloc(L * 4));
   da_.n_items = static_cast<std::int32_t*>(dalloc(L * 4));

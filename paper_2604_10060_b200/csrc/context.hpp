@@ -105,6 +105,9 @@ class Context {
   const std::vector<LedgerOp>& ledger() const { return ledger_; }
   std::int64_t device_entries() const { return device_entries_; }
   void check();
+  // Completes the deferred host bookkeeping of the last decode step (every host-state reader
+  // calls this first; decode_step overlaps it with the next step's GPU work).
+  void flush_pending();
   double offload(std::int64_t id);
   double fetch(std::int64_t id, int cause);
   cudaStream_t stream() const { return st_; }
@@ -156,6 +159,10 @@ class Context {
   DecodeArgs da_{};
   void* d_dec_ = nullptr;  // packed result block
   void* h_dec_ = nullptr;
+  void* h_dec2_ = nullptr;  // second host copy: the pending (deferred) replay reads one, the next step fills the other
+  bool pending_ = false;    // a decode step's host bookkeeping has not been replayed yet
+  std::vector<std::int64_t> pending_gt_;
+  void replay_decode(const void* hblock, const std::int64_t* gt, int n_gt);
   std::size_t dec_bytes_ = 0;
   float* d_q_ = nullptr;
   float* d_out_ = nullptr;

@@ -35,10 +35,17 @@ std::uint64_t fnv1a(std::uint64_t h, std::uint64_t x) {  // engine.cpp:18-24
 void Context::decode_step(std::int64_t qid, const float* q, int q_mem, float* out, int out_mem,
                           const std::int64_t* gt, int n_gt) {
   (void)qid;
-  if (!built_) build_now();  // engine.cpp:202
+  if (!built_) {
+    flush_pending();
+    build_now();  // engine.cpp:202
+  }
   if (parts_.empty()) fail(-9, "retrieve before any index was built");
   if (!q) fail(-10, "null query");
-  flush_resid();
+  // A pending replay that settles a split changes the device index: finish it before launching.
+  if (pending_ && (reinterpret_cast<const std::int32_t*>(
+                       static_cast<const std::uint8_t*>(h_dec2_) +
+                       (reinterpret_cast<const std::uint8_t*>(da_.flags) - static_cast<const std::uint8_t*>(d_dec_)))[0] & 1))
+    flush_pending();
   const float* dq = q;
   if (q_mem != KVC_MEM_DEVICE) {
     KVC_CUDA(cudaMemcpyAsync(d_q_, q, static_cast<std::size_t>(L_) * d_ * 4, cudaMemcpyHostToDevice, st_));
@@ -47,11 +54,15 @@ void Context::decode_step(std::int64_t qid, const float* q, int q_mem, float* ou
   da_.q = dq;
   da_.out = (out && out_mem == KVC_MEM_DEVICE) ? out : d_out_;
   da_.n_parts_host = static_cast<std::int32_t>(parts_.size());
+  KVC_CUDA(cudaMemsetAsync(da_.flags, 0, 4, st_));
   launches_ += launch_decode(t_, da_, st_, timing_ ? ev_ : nullptr);
   KVC_CUDA(cudaMemcpyAsync(h_dec_, d_dec_, dec_bytes_, cudaMemcpyDeviceToHost, st_));
   if (out && out_mem != KVC_MEM_DEVICE)
     KVC_CUDA(cudaMemcpyAsync(out, d_out_, static_cast<std::size_t>(L_) * d_ * 4, cudaMemcpyDeviceToHost, st_));
   KVC_CUDA(cudaMemcpyAsync(h_err_, t_.err, 4, cudaMemcpyDeviceToHost, st_));
+  // the previous step's bookkeeping runs on the host while this step runs on the GPU
+  const auto tr0 = std::chrono::steady_clock::now();
+  flush_pending();
   const auto th0 = std::chrono::steady_clock::now();
   sync();
   const auto th1 = std::chrono::steady_clock::now();
@@ -65,10 +76,33 @@ void Context::decode_step(std::int64_t qid, const float* q, int q_mem, float* ou
     KVC_CUDA(cudaEventElapsedTime(&ms, ev_[0], ev_[3]));
     step_t_[3] = ms * 1e3;
   }
+  step_t_[5] = std::chrono::duration<double, std::micro>(th1 - th0).count();
+  step_t_[6] = std::chrono::duration<double, std::micro>(th0 - tr0).count();
+  std::swap(h_dec_, h_dec2_);  // h_dec2_ now holds this step's results
+  pending_ = true;
+  pending_gt_.assign(gt ? gt : nullptr, gt ? gt + (n_gt > 0 ? n_gt : 0) : nullptr);
+  // parity / recall / self-check callers need the bookkeeping now
+  if (cfg_.parity_mode || cfg_.check_invariants || (gt && n_gt > 0)) flush_pending();
+}
 
+void Context::flush_pending() {
+  if (!pending_) return;
+  pending_ = false;
+  replay_decode(h_dec2_, pending_gt_.empty() ? nullptr : pending_gt_.data(), static_cast<int>(pending_gt_.size()));
+}
+
+void Context::replay_decode(const void* hblock, const std::int64_t* gt, int n_gt) {
+  {  // algorithmic bytes of the attention launch: attended tokens x (K + V)
+    const auto* ha = reinterpret_cast<const std::int64_t*>(
+        static_cast<const std::uint8_t*>(hblock) +
+        (reinterpret_cast<const std::uint8_t*>(da_.attended) - static_cast<const std::uint8_t*>(d_dec_)));
+    std::int64_t tok = 0;
+    for (int l = 0; l < L_; ++l) tok += ha[l];
+    step_t_[4] = static_cast<double>(tok) * 2.0 * d_ * es_;
+  }
   // host copies of the device rankings (same carve offsets as alloc_device)
   auto hp = [&](const void* dptr) {
-    return static_cast<const std::uint8_t*>(h_dec_) +
+    return static_cast<const std::uint8_t*>(hblock) +
            (static_cast<const std::uint8_t*>(dptr) - static_cast<const std::uint8_t*>(d_dec_));
   };
   const auto* h_parts = reinterpret_cast<const std::int32_t*>(hp(da_.parts));
@@ -83,13 +117,14 @@ void Context::decode_step(std::int64_t qid, const float* q, int q_mem, float* ou
   const auto* h_nc = reinterpret_cast<const std::int32_t*>(hp(da_.n_cand));
   (void)h_parts;
   (void)h_nps;
-  {  // algorithmic bytes of the attention launch: attended tokens x (K + V)
-    std::int64_t tok = 0;
-    for (int l = 0; l < L_; ++l) tok += h_att[l];
-    step_t_[4] = static_cast<double>(tok) * 2.0 * d_ * es_;
-  }
 
-  // Translate every layer's slots to ids before any settle frees / reuses a slot.
+  // Translate every layer's slots to ids before any settle frees / reuses a slot; prefetch the
+  // host records the replay is about to touch (they are scattered across the heap).
+  for (int l = 0; l < L_; ++l)
+    for (int i = 0; i < h_nr[l]; ++i) {
+      const std::int64_t id = slot_id_[static_cast<std::size_t>(h_rs[l * da_.k_s + i])];
+      if (id >= 0) __builtin_prefetch(clusters_[static_cast<std::size_t>(id)].get(), 1, 1);
+    }
   for (int l = 0; l < L_; ++l) {
     LayerOut& lo = last_[static_cast<std::size_t>(l)];
     lo.ranked.clear();
@@ -195,11 +230,7 @@ void Context::decode_step(std::int64_t qid, const float* q, int q_mem, float* ou
   const auto th2 = std::chrono::steady_clock::now();
   repin();  // engine.cpp:234
   if (cfg_.check_invariants) check();
-  const auto th3 = std::chrono::steady_clock::now();
-  // host-side phases (us): wait for the device, replay of the retrieve bookkeeping, repin/checks
-  step_t_[5] = std::chrono::duration<double, std::micro>(th1 - th0).count();
-  step_t_[6] = std::chrono::duration<double, std::micro>(th2 - th1).count();
-  step_t_[7] = std::chrono::duration<double, std::micro>(th3 - th2).count();
+  step_t_[7] = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - th2).count();
 }
 
 // ---------------------------------------------------------------------------- bulk load

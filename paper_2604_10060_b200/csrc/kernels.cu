@@ -31,6 +31,10 @@ namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
 
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
 __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
@@ -1195,11 +1199,66 @@ __device__ void block_rank_select(const double* sim, const long long* key, int n
   __syncthreads();
 }
 
+// Top-`take` (take <= 64) of n <= 1024 entries, best first under (sim desc, key asc). Each warp
+// sorts 32-entry chunks in registers with a shuffle bitonic network (no block barriers), then
+// warp 0 merges the sorted chunks by repeatedly taking the best chunk head. `pay` is scratch
+// for the payload indices; order[r] receives the index of the r-th best entry.
+__device__ void block_topk(double* sim, long long* key, int* pay, int n, int take, int* order) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int nch = (n + 31) / 32;
+  for (int c = warp; c < nch; c += nw) {
+    const int i = c * 32 + lane;
+    double s = i < n ? sim[i] : -INFINITY;
+    long long k = i < n ? key[i] : LLONG_MAX;
+    int p = i < n ? i : -1;
+    for (int size = 2; size <= 32; size <<= 1)
+      for (int stride = size >> 1; stride > 0; stride >>= 1) {
+        const double ps = __shfl_xor_sync(kFull, s, stride);
+        const long long pk = __shfl_xor_sync(kFull, k, stride);
+        const int pp = __shfl_xor_sync(kFull, p, stride);
+        const bool up = (lane & size) == 0 || size == 32;
+        const bool lower = (lane & stride) == 0;
+        const bool pb = better(ps, pk, s, k);
+        if ((lower == up) ? pb : !pb) {
+          s = ps;
+          k = pk;
+          p = pp;
+        }
+      }
+    sim[c * 32 + lane] = s;
+    key[c * 32 + lane] = k;
+    pay[c * 32 + lane] = p;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    int head = 0;  // lane j walks chunk j
+    for (int r = 0; r < take; ++r) {
+      double bs = -INFINITY;
+      long long bk = LLONG_MAX;
+      int bl = -1;
+      if (lane < nch && head < 32) {
+        const int i = lane * 32 + head;
+        bs = sim[i];
+        bk = key[i];
+        if (pay[i] >= 0) bl = lane;
+      }
+      int src = bl;
+      warp_best(bs, bk, src);
+      if (src < 0) break;
+      if (lane == src) {
+        order[r] = pay[lane * 32 + head];
+        head += 1;
+      }
+    }
+  }
+  __syncthreads();
+}
+
 constexpr int K4_ROWS = 128;  // representative rows staged per chunk
 
 __host__ __device__ inline size_t k4_smem_bytes(int d, int cmax, int parts, int W, int tmax) {
   const int nsel = cmax > parts ? cmax : parts;
-  return static_cast<size_t>(d + 1) * 8 + static_cast<size_t>(nsel) * 16 + static_cast<size_t>(cmax) * 5 +
+  return static_cast<size_t>(d + 1) * 8 + static_cast<size_t>(nsel) * 20 + static_cast<size_t>(cmax) * 5 +
          static_cast<size_t>(K4_ROWS) * (d + 1) * 8 + static_cast<size_t>(W) * tmax * 4 + 256;
 }
 
@@ -1216,6 +1275,8 @@ __global__ void __launch_bounds__(256) k_score_select(DevTables t, DecodeArgs a,
   p += static_cast<size_t>(nsel) * 8;
   long long* key = reinterpret_cast<long long*>(p);
   p += static_cast<size_t>(nsel) * 8;
+  int* pay = reinterpret_cast<int*>(p);  // top-k payload scratch
+  p += static_cast<size_t>(nsel) * 4;
   double* stage = reinterpret_cast<double*>(p);  // [K4_ROWS][d+1]
   p += static_cast<size_t>(K4_ROWS) * DS * 8;
   int* owners = reinterpret_cast<int*>(p);  // [W][tmax] ring owners of this domain
@@ -1236,8 +1297,22 @@ __global__ void __launch_bounds__(256) k_score_select(DevTables t, DecodeArgs a,
   const float* q = a.q + static_cast<int64_t>(l) * d;
   for (int i = threadIdx.x; i < d; i += blockDim.x) qd[i] = static_cast<double>(q[i]);
   // the window ring owners are needed after ranking; fetch them now
-  for (int i = threadIdx.x; i < t.W * t.tmax; i += blockDim.x)
-    owners[i] = t.ring_owner[static_cast<int64_t>(l) * t.W * t.tmax + i];
+  {
+    const int n_own = t.W * t.tmax;
+    const int* src = t.ring_owner + static_cast<int64_t>(l) * n_own;
+    int v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int i = threadIdx.x + 256 * j;
+      v[j] = i < n_own ? src[i] : -1;
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int i = threadIdx.x + 256 * j;
+      if (i < n_own) owners[i] = v[j];
+    }
+    for (int i = threadIdx.x + 256 * 8; i < n_own; i += blockDim.x) owners[i] = src[i];
+  }
   if (threadIdx.x == 0) {
     degen = false;
     att_s = 0;
@@ -1254,19 +1329,33 @@ __global__ void __launch_bounds__(256) k_score_select(DevTables t, DecodeArgs a,
   if (nq < 1e-12 && threadIdx.x == 0) degen = true;
   K4MARK(0)
   // ---- stage 1: visual_topk (index.cpp:192-208): exact cosines, order (sim desc, id asc)
-  for (int pp = threadIdx.x; pp < P; pp += blockDim.x) {
-    const double* row = t.vrep + static_cast<int64_t>(pp) * d;
-    double acc = 0.0;
+  for (int p0 = 0; p0 < P; p0 += K4_ROWS) {
+    const int rows = min(K4_ROWS, P - p0);
+    for (int r = threadIdx.x >> 5; r < rows; r += blockDim.x >> 5) {
+      const double* src = t.vrep + static_cast<int64_t>(p0 + r) * d;
+      for (int i = threadIdx.x & 31; i < d; i += 32)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(stage + r * DS + i)), "l"(src + i)
+                     : "memory");
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();
+    for (int r = threadIdx.x; r < rows; r += blockDim.x) {
+      const double* row = stage + r * DS;
+      double acc = 0.0;
 #pragma unroll 16
-    for (int i = 0; i < d; ++i) acc = dadd(acc, dmul(qd[i], row[i]));
-    const double nr = t.vnorm[pp];
-    if (nr < 1e-12) degen = true;
-    sim[pp] = clamp1(ddiv(acc, dmul(nq, nr)));
-    key[pp] = pp;
+      for (int i = 0; i < d; ++i) acc = dadd(acc, dmul(qd[i], row[i]));
+      const double nr = t.vnorm[p0 + r];
+      if (nr < 1e-12) degen = true;
+      sim[p0 + r] = clamp1(ddiv(acc, dmul(nq, nr)));
+      key[p0 + r] = p0 + r;
+    }
+    __syncthreads();
   }
-  __syncthreads();
   const int kv = min(a.k_v, P);
-  block_rank_select(sim, key, P, kv, chosen);
+  if (P <= 1024)
+    block_topk(sim, key, pay, P, kv, chosen);
+  else
+    block_rank_select(sim, key, P, kv, chosen);
   if (threadIdx.x < kv) a.parts[l * a.k_v + threadIdx.x] = chosen[threadIdx.x];
   if (threadIdx.x == 0) a.n_parts_sel[l] = kv;
   K4MARK(1)
@@ -1305,11 +1394,15 @@ __global__ void __launch_bounds__(256) k_score_select(DevTables t, DecodeArgs a,
     // fp64 chain per candidate (vecmath.hpp:27-61)
     for (int c0 = 0; c0 < nc; c0 += K4_ROWS) {
       const int rows = min(K4_ROWS, nc - c0);
-      for (int idx = threadIdx.x; idx < rows * d; idx += blockDim.x) {
-        const int r = idx / d, i = idx - r * d;
+      // asynchronous 8-byte copies (LDGSTS): every row in flight at once, one latency per chunk
+      for (int r = threadIdx.x >> 5; r < rows; r += blockDim.x >> 5) {
         const int s = cslot[c0 + r];
-        stage[r * DS + i] = (cbuf[c0 + r] ? t.brep64 : t.rep64)[static_cast<int64_t>(s) * d + i];
+        const double* src = (cbuf[c0 + r] ? t.brep64 : t.rep64) + static_cast<int64_t>(s) * d;
+        for (int i = threadIdx.x & 31; i < d; i += 32)
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(stage + r * DS + i)), "l"(src + i)
+                       : "memory");
       }
+      asm volatile("cp.async.wait_all;" ::: "memory");
       __syncthreads();
       for (int r = threadIdx.x; r < rows; r += blockDim.x) {
         const int c = c0 + r;
@@ -1328,7 +1421,7 @@ __global__ void __launch_bounds__(256) k_score_select(DevTables t, DecodeArgs a,
     }
     K4MARK(2)
     const int take = min(ktake, nc);
-    block_rank_select(sim, key, nc, take, order);
+    block_topk(sim, key, pay, nc, take, order);
     K4MARK(3)
     if (threadIdx.x < take) {
       const int b = order[threadIdx.x];
@@ -1367,6 +1460,9 @@ __global__ void __launch_bounds__(256) k_score_select(DevTables t, DecodeArgs a,
     }
     nver_s = nv;
     a.n_ver[l] = nv;
+    bool lz = false;
+    for (int j = 0; j < nv; ++j) lz |= t.lazy[vers[j]] != 0;
+    if (lz) atomicOr(a.flags, 1);
   }
   __syncthreads();
   const int nv = nver_s;
@@ -1382,16 +1478,29 @@ __global__ void __launch_bounds__(256) k_score_select(DevTables t, DecodeArgs a,
   __syncthreads();
   K4MARK(4)
   // window ring: tokens whose owner is not a verified cluster (retrieval.cpp:107-108 dedup)
-  for (int i = threadIdx.x; i < W * t.tmax; i += blockDim.x) {
-    const int rs = i / t.tmax, tt = i % t.tmax;
-    if (tt >= t.ring_count[rs]) continue;
-    const int own = owners[rs * t.tmax + tt];
-    bool m = false;
-    for (int j = 0; j < nv; ++j) m |= vers[j] == own;
-    if (!m) {
-      atomicAdd(&att_s, 1ull);
-      if (rs * rpp + tt / t.P < 64) atomicAdd(&ring_cnt[rs * rpp + tt / t.P], 1);
+  {
+    unsigned long long mine = 0;
+    const int n_ring = W * t.tmax;
+    const int n_pad = (n_ring + blockDim.x - 1) / blockDim.x * blockDim.x;  // warp-uniform trip count
+    for (int i = threadIdx.x; i < n_pad; i += blockDim.x) {
+      const int rs = i / t.tmax, tt = i - rs * t.tmax;
+      bool keep = i < n_ring && tt < t.ring_count[rs];
+      if (keep) {
+        const int own = owners[i];
+        for (int j = 0; j < nv; ++j) keep &= vers[j] != own;
+      }
+      // page-level counts: lanes of a warp mostly share a page -> one atomic per (warp, page)
+      const int pg = keep ? rs * rpp + tt / t.P : -1;
+      const unsigned km = __ballot_sync(kFull, keep);
+      mine += keep ? 1 : 0;
+      if (km) {
+        const unsigned same = __match_any_sync(kFull, pg);
+        if (keep && pg < 64 && (threadIdx.x & 31) == __ffs(same) - 1) atomicAdd(&ring_cnt[pg], __popc(same));
+      }
     }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(kFull, mine, o);
+    if ((threadIdx.x & 31) == 0) atomicAdd(&att_s, mine);
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -1442,9 +1551,6 @@ __global__ void __launch_bounds__(256) k_score_select(DevTables t, DecodeArgs a,
 }
 
 // ============================================================================ K6
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
 __device__ __forceinline__ void mbar_init(uint64_t* bar, int cnt) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(cnt));
 }

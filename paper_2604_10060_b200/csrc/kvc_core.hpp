@@ -163,6 +163,7 @@ struct DecodeArgs {
   int32_t* n_ver;          // [L]
   int64_t* attended;       // [L]        attended-set size (members+buffers of verified U window)
   int32_t* n_cand;         // [L]        candidates compared (count_candidates)
+  int32_t* flags;          // [1] bit 0: a verified cluster has a pending split (needs a host settle)
   // attention work list: page descriptors per domain (x page, y fill, z kind | ring_slot << 8,
   // w first token of the page within its frame); an item = chunk_pages consecutive descriptors
   int4* desc;              // [L][max_desc]
