@@ -160,7 +160,7 @@ class Context {
   void* d_dec_ = nullptr;  // packed result block
   void* h_dec_ = nullptr;
   void* h_dec2_ = nullptr;  // second host copy: the pending (deferred) replay reads one, the next step fills the other
-  bool pending_ = false;    // a decode step's host bookkeeping has not been replayed yet
+  bool replay_pending_ = false;  // a decode step's host bookkeeping has not been replayed yet
   std::vector<std::int64_t> pending_gt_;
   void replay_decode(const void* hblock, const std::int64_t* gt, int n_gt);
   std::size_t dec_bytes_ = 0;

@@ -42,7 +42,7 @@ void Context::decode_step(std::int64_t qid, const float* q, int q_mem, float* ou
   if (parts_.empty()) fail(-9, "retrieve before any index was built");
   if (!q) fail(-10, "null query");
   // A pending replay that settles a split changes the device index: finish it before launching.
-  if (pending_ && (reinterpret_cast<const std::int32_t*>(
+  if (replay_pending_ && (reinterpret_cast<const std::int32_t*>(
                        static_cast<const std::uint8_t*>(h_dec2_) +
                        (reinterpret_cast<const std::uint8_t*>(da_.flags) - static_cast<const std::uint8_t*>(d_dec_)))[0] & 1))
     flush_pending();
@@ -79,15 +79,15 @@ void Context::decode_step(std::int64_t qid, const float* q, int q_mem, float* ou
   step_t_[5] = std::chrono::duration<double, std::micro>(th1 - th0).count();
   step_t_[6] = std::chrono::duration<double, std::micro>(th0 - tr0).count();
   std::swap(h_dec_, h_dec2_);  // h_dec2_ now holds this step's results
-  pending_ = true;
+  replay_pending_ = true;
   pending_gt_.assign(gt ? gt : nullptr, gt ? gt + (n_gt > 0 ? n_gt : 0) : nullptr);
   // parity / recall / self-check callers need the bookkeeping now
   if (cfg_.parity_mode || cfg_.check_invariants || (gt && n_gt > 0)) flush_pending();
 }
 
 void Context::flush_pending() {
-  if (!pending_) return;
-  pending_ = false;
+  if (!replay_pending_) return;
+  replay_pending_ = false;
   replay_decode(h_dec2_, pending_gt_.empty() ? nullptr : pending_gt_.data(), static_cast<int>(pending_gt_.size()));
 }
 
