@@ -289,8 +289,9 @@ def main():
     decode_launches = kv.launch_count() - launches0
     kv.set_timing(False)
     # e2e decode: host query in, host output out, through the public API
-    q_host = q_dev.cpu().numpy()
-    out_host = np.zeros((D, HEAD_DIM), np.float32)
+    q_pin = q_dev.cpu().pin_memory()  # pinned host buffers: the contract's e2e copies
+    out_pin = torch.zeros(D, HEAD_DIM, dtype=torch.float32).pin_memory()
+    q_host, out_host = q_pin.numpy(), out_pin.numpy()
     torch.cuda.synchronize()
     e0.record(stream)
     for i in range(args.warmup, nq):

@@ -1617,9 +1617,6 @@ template <int D, bool BF16, int STAGES>
 __global__ void __launch_bounds__(ATT_THREADS + 32) k_attend(DevTables t, DecodeArgs a, int* work_ctr) {
   constexpr int ES = BF16 ? 2 : 4;
   constexpr int ROWB = D * ES;
-  constexpr int QB = ROWB / 4;  // bytes of a row handled by one lane for q.k
-  constexpr int CH = QB / 16;   // 16-byte chunks per lane
-  constexpr int EPC = 16 / ES;  // elements per chunk
   constexpr int OPL = D / 32;   // output dims per lane
   extern __shared__ __align__(128) uint8_t sm6[];
   const int P = t.P;
@@ -1718,13 +1715,18 @@ __global__ void __launch_bounds__(ATT_THREADS + 32) k_attend(DevTables t, Decode
   }
 
   // ================================================================== consumer warps
+  // Lane l owns head dims [l*OPL, l*OPL + OPL) for both q.k (query in registers) and p.v. A warp
+  // takes 8 tokens of a 64-token sub-tile: each lane forms 8 partial dots over its dims, a
+  // transpose-reduce (7 shuffles) + 2 butterfly steps leaves token j's full score in the lanes
+  // whose bits 4,3,2 encode j; softmax statistics then need 3 shuffles each.
   float m_run = -INFINITY, l_run = 0.f;
   float o_run[OPL];
+  float qr[OPL];
 #pragma unroll
-  for (int i = 0; i < OPL; ++i) o_run[i] = 0.f;
+  for (int i = 0; i < OPL; ++i) o_run[i] = qr[i] = 0.f;
+  int cur_dom = -1;
   const float sl2 = a.scale_log2;
-  const int sub = lane >> 2;   // token within the warp's 8
-  const int part = lane & 3;   // quarter of the row for q.k
+  const int my_tok = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
 
   for (int it = 0;; ++it) {
     const int s = it % STAGES;
@@ -1735,64 +1737,90 @@ __global__ void __launch_bounds__(ATT_THREADS + 32) k_attend(DevTables t, Decode
     const int fill = m.fill, kind = m.kind;
     const uint8_t* Ks = stages + s * stage_bytes;
     const uint8_t* Vs = Ks + static_cast<int64_t>(P) * ROWB;
-    const float* qs = reinterpret_cast<const float*>(Ks + kv_bytes);
+    if (m.dom != cur_dom) {  // the domain's query (carried by every stage)
+      const float* qs = reinterpret_cast<const float*>(Ks + kv_bytes);
+#pragma unroll
+      for (int i = 0; i < OPL; ++i) qr[i] = qs[lane * OPL + i];
+      cur_dom = m.dom;
+    }
     for (int tb = 0; tb < fill; tb += 64) {
-      const int tok = tb + warp * 8 + sub;
+      const int t0 = tb + warp * 8;  // this warp's first token
+      if (t0 >= fill) continue;      // warp-uniform
+      // ---- partial dots: 8 tokens x OPL dims per lane
+      float v[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        float acc = 0.f;
+        if (t0 + j < fill) {
+          const uint8_t* krow = Ks + static_cast<int64_t>(t0 + j) * ROWB + lane * OPL * ES;
+          if (BF16) {
+#pragma unroll
+            for (int i = 0; i < OPL; i += 2) {
+              const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(krow + i * 2));
+              acc = fmaf(f.x, qr[i], acc);
+              if (i + 1 < OPL) acc = fmaf(f.y, qr[i + 1], acc);
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < OPL; ++i) acc = fmaf(reinterpret_cast<const float*>(krow)[i], qr[i], acc);
+          }
+        }
+        v[j] = acc;
+      }
+      // ---- transpose-reduce: xor 16 (8 -> 4 values), xor 8 (4 -> 2), xor 4 (2 -> 1)
+      float w4[4], w2[2];
+      const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float send = b4 ? v[i] : v[i + 4];
+        const float keep = b4 ? v[i + 4] : v[i];
+        w4[i] = keep + __shfl_xor_sync(kFull, send, 16);
+      }
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const float send = b3 ? w4[i] : w4[i + 2];
+        const float keep = b3 ? w4[i + 2] : w4[i];
+        w2[i] = keep + __shfl_xor_sync(kFull, send, 8);
+      }
+      float dot;
+      {
+        const float send = b2 ? w2[0] : w2[1];
+        const float keep = b2 ? w2[1] : w2[0];
+        dot = keep + __shfl_xor_sync(kFull, send, 4);
+      }
+      dot += __shfl_xor_sync(kFull, dot, 1);
+      dot += __shfl_xor_sync(kFull, dot, 2);
+      // lane holds token my_tok = (b4,b3,b2) of this warp's 8
+      const int tok = t0 + my_tok;
       bool valid = tok < fill;
       if (valid && kind == 2) {
         const int own = t.ring_owner[(static_cast<int64_t>(m.dom) * t.W + m.ring_slot) * t.tmax + m.tok0 + tok];
         for (int j = 0; j < m.nver; ++j) valid &= m.ver[j] != own;
       }
-      float acc0 = 0.f, acc1 = 0.f;
-      if (tok < fill) {
-        const uint8_t* krow = Ks + static_cast<int64_t>(tok) * ROWB + part * QB;
-        const float* qq0 = qs + part * (D / 4);
-#pragma unroll
-        for (int j = 0; j < CH; ++j) {
-          const int c = (j + sub) % CH;  // rotate chunks across tokens: spreads smem banks
-          const uint4 raw = *reinterpret_cast<const uint4*>(krow + c * 16);
-          const float* qq = qq0 + c * EPC;
-          if (BF16) {
-            const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const float2 f = __bfloat1622float2(h2[e]);
-              acc0 = fmaf(f.x, qq[2 * e], acc0);
-              acc1 = fmaf(f.y, qq[2 * e + 1], acc1);
-            }
-          } else {
-            const float* f = reinterpret_cast<const float*>(&raw);
-            acc0 = fmaf(f[0], qq[0], acc0);
-            acc1 = fmaf(f[1], qq[1], acc1);
-            acc0 = fmaf(f[2], qq[2], acc0);
-            acc1 = fmaf(f[3], qq[3], acc1);
-          }
-        }
-      }
-      float acc = acc0 + acc1;
-      acc += __shfl_xor_sync(kFull, acc, 1);
-      acc += __shfl_xor_sync(kFull, acc, 2);
-      const float sc = valid ? acc * sl2 : -INFINITY;
+      const float sc = valid ? dot * sl2 : -INFINITY;
       float mx = sc;
-#pragma unroll
-      for (int o = 16; o >= 4; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(kFull, mx, o));
+      mx = fmaxf(mx, __shfl_xor_sync(kFull, mx, 4));
+      mx = fmaxf(mx, __shfl_xor_sync(kFull, mx, 8));
+      mx = fmaxf(mx, __shfl_xor_sync(kFull, mx, 16));
       const float m_new = fmaxf(m_run, mx);
       if (m_new == -INFINITY) continue;  // warp-uniform
       const float alpha = exp2f(m_run - m_new);
       const float pr = valid ? exp2f(sc - m_new) : 0.f;
-      float psum = part == 0 ? pr : 0.f;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) psum += __shfl_xor_sync(kFull, psum, o);
+      float psum = (lane & 3) == 0 ? pr : 0.f;
+      psum += __shfl_xor_sync(kFull, psum, 4);
+      psum += __shfl_xor_sync(kFull, psum, 8);
+      psum += __shfl_xor_sync(kFull, psum, 16);
       l_run = l_run * alpha + psum;
 #pragma unroll
       for (int i = 0; i < OPL; ++i) o_run[i] *= alpha;
       m_run = m_new;
+      // ---- p.v: token j's probability lives in lane (j>>2&1)*16 + (j>>1&1)*8 + (j&1)*4
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        const float pj = __shfl_sync(kFull, pr, 4 * j);
-        const int tj = tb + warp * 8 + j;
-        if (tj >= fill) break;
-        const uint8_t* vrow = Vs + static_cast<int64_t>(tj) * ROWB + lane * OPL * ES;
+        const int src = ((j >> 2) & 1) * 16 + ((j >> 1) & 1) * 8 + (j & 1) * 4;
+        const float pj = __shfl_sync(kFull, pr, src);
+        if (t0 + j >= fill) break;
+        const uint8_t* vrow = Vs + static_cast<int64_t>(t0 + j) * ROWB + lane * OPL * ES;
         if (BF16) {
 #pragma unroll
           for (int i = 0; i < OPL; i += 2) {
