@@ -1255,10 +1255,11 @@ __device__ void block_topk(double* sim, long long* key, int* pay, int n, int tak
 }
 
 constexpr int K4_ROWS = 128;  // representative rows staged per chunk
+constexpr float kScoreMargin = 1e-4f;  // bound on |fp32 mirror cosine - exact fp64 cosine|
 
 __host__ __device__ inline size_t k4_smem_bytes(int d, int cmax, int parts, int W, int tmax) {
   const int nsel = cmax > parts ? cmax : parts;
-  return static_cast<size_t>(d + 1) * 8 + static_cast<size_t>(nsel) * 20 + static_cast<size_t>(cmax) * 5 +
+  return static_cast<size_t>(d + 1) * 8 + static_cast<size_t>(nsel) * 24 + static_cast<size_t>(cmax) * 5 +
          static_cast<size_t>(K4_ROWS) * (d + 1) * 8 + static_cast<size_t>(W) * tmax * 4 + 256;
 }
 
@@ -1277,6 +1278,8 @@ __global__ void __launch_bounds__(256) k_score_select(DevTables t, DecodeArgs a,
   p += static_cast<size_t>(nsel) * 8;
   int* pay = reinterpret_cast<int*>(p);  // top-k payload scratch
   p += static_cast<size_t>(nsel) * 4;
+  float* approx = reinterpret_cast<float*>(p);  // approximate candidate scores
+  p += static_cast<size_t>(nsel) * 4;
   double* stage = reinterpret_cast<double*>(p);  // [K4_ROWS][d+1]
   p += static_cast<size_t>(K4_ROWS) * DS * 8;
   int* owners = reinterpret_cast<int*>(p);  // [W][tmax] ring owners of this domain
@@ -1290,6 +1293,10 @@ __global__ void __launch_bounds__(256) k_score_select(DevTables t, DecodeArgs a,
   __shared__ int rank_slot[64], n_rank_s, order[64];
   __shared__ unsigned long long att_s;
   __shared__ bool degen;
+  __shared__ int ring_count_s[64];
+  __shared__ int sset[K4_ROWS], n_s;
+  __shared__ double ssim[K4_ROWS];
+  __shared__ long long skey[K4_ROWS];
 
   long long kc0 = clock64();
 #define K4MARK(k) if (a.k4prof && threadIdx.x == 0) { const long long kc1 = clock64(); a.k4prof[l * 8 + (k)] = kc1 - kc0; kc0 = kc1; }
@@ -1317,6 +1324,7 @@ __global__ void __launch_bounds__(256) k_score_select(DevTables t, DecodeArgs a,
     degen = false;
     att_s = 0;
   }
+  if (threadIdx.x < t.W && threadIdx.x < 64) ring_count_s[threadIdx.x] = t.ring_count[threadIdx.x];
   __syncthreads();
   if (threadIdx.x == 0) {
     double s = 0.0;
@@ -1390,38 +1398,95 @@ __global__ void __launch_bounds__(256) k_score_select(DevTables t, DecodeArgs a,
     __syncthreads();
     const int nc = min(ncand_s, cmax);
     if (pass == 0 && threadIdx.x == 0) a.n_cand[l] = nc;
-    // exact cosines: rows staged through shared memory with coalesced loads, one sequential
-    // fp64 chain per candidate (vecmath.hpp:27-61)
-    for (int c0 = 0; c0 < nc; c0 += K4_ROWS) {
-      const int rows = min(K4_ROWS, nc - c0);
-      // asynchronous 8-byte copies (LDGSTS): every row in flight at once, one latency per chunk
+    const int take = min(ktake, nc);
+    // (A) approximate cosines from the fp32 mirrors: rows staged with 16-byte async copies, one
+    //     thread per candidate reading its row in a rotated order (conflict-free banks)
+    float* st32 = reinterpret_cast<float*>(stage);  // [rows][d + 4]
+    const int DS32 = d + 4;
+    const int rows32 = min(nc, (2 * K4_ROWS * DS) / DS32);  // what the fp64 stage buffer holds
+    for (int c0 = 0; c0 < nc; c0 += rows32) {
+      const int rows = min(rows32, nc - c0);
       for (int r = threadIdx.x >> 5; r < rows; r += blockDim.x >> 5) {
         const int s = cslot[c0 + r];
-        const double* src = (cbuf[c0 + r] ? t.brep64 : t.rep64) + static_cast<int64_t>(s) * d;
-        for (int i = threadIdx.x & 31; i < d; i += 32)
-          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(stage + r * DS + i)), "l"(src + i)
+        const float* src = (cbuf[c0 + r] ? t.brep32 : t.rep32) + static_cast<int64_t>(s) * d;
+        for (int i = (threadIdx.x & 31) * 4; i < d; i += 128)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(st32 + r * DS32 + i)), "l"(src + i)
                        : "memory");
       }
       asm volatile("cp.async.wait_all;" ::: "memory");
       __syncthreads();
       for (int r = threadIdx.x; r < rows; r += blockDim.x) {
         const int c = c0 + r;
+        const float* row = st32 + r * DS32;
+        float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+        // element order rotated by the row index: banks (4r + r + i) mod 32 are distinct per lane
+        for (int i0 = 0; i0 < d; i0 += 4) {
+          const int j0 = (i0 + r) % d, j1 = (i0 + 1 + r) % d, j2 = (i0 + 2 + r) % d, j3 = (i0 + 3 + r) % d;
+          a0 = fmaf(static_cast<float>(qd[j0]), row[j0], a0);
+          a1 = fmaf(static_cast<float>(qd[j1]), row[j1], a1);
+          a2 = fmaf(static_cast<float>(qd[j2]), row[j2], a2);
+          a3 = fmaf(static_cast<float>(qd[j3]), row[j3], a3);
+        }
         const int s = cslot[c];
         const bool ib = cbuf[c];
-        const double* row = stage + r * DS;
-        double acc = 0.0;
-#pragma unroll 16
-        for (int i = 0; i < d; ++i) acc = dadd(acc, dmul(qd[i], row[i]));
         const double nr = ib ? t.bnorm[s] : t.rnorm[s];
         if (nr < 1e-12) degen = true;
-        sim[c] = clamp1(ddiv(acc, dmul(nq, nr)));
+        const float sa = ((a0 + a1) + (a2 + a3)) / static_cast<float>(nq * nr);
+        approx[c] = sa;
+        sim[c] = static_cast<double>(sa);
         key[c] = 2LL * t.cid[s] + (ib ? 1 : 0);
       }
       __syncthreads();
     }
     K4MARK(2)
-    const int take = min(ktake, nc);
-    block_topk(sim, key, pay, nc, take, order);
+    // (B) the set S of candidates that can reach the exact top-`take`: approximate score within
+    //     2*margin of the take-th best approximate score (|approx - exact| <= margin)
+    if (threadIdx.x == 0) n_s = 0;
+    if (take > 0 && take < nc) {
+      block_topk(sim, key, pay, nc, take, order);
+      const float thr = approx[order[take - 1]] - 2.f * kScoreMargin;
+      for (int c = threadIdx.x; c < nc; c += blockDim.x)
+        if (approx[c] >= thr) {
+          const int k = atomicAdd(&n_s, 1);
+          if (k < K4_ROWS) sset[k] = c;
+          else set_err(t, DERR_CANDIDATES);
+        }
+    } else {
+      for (int c = threadIdx.x; c < nc; c += blockDim.x) {
+        const int k = atomicAdd(&n_s, 1);
+        if (k < K4_ROWS) sset[k] = c;
+        else set_err(t, DERR_CANDIDATES);
+      }
+    }
+    __syncthreads();
+    const int ns_ = min(n_s, K4_ROWS);
+    // (C) exact cosines (vecmath.hpp:54-61) for S: fp64 rows staged with 8-byte async copies,
+    //     one sequential chain per candidate; exact top-`take` of S by rank counting
+    for (int r = threadIdx.x >> 5; r < ns_; r += blockDim.x >> 5) {
+      const int c = sset[r];
+      const double* src = (cbuf[c] ? t.brep64 : t.rep64) + static_cast<int64_t>(cslot[c]) * d;
+      for (int i = threadIdx.x & 31; i < d; i += 32)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(stage + r * DS + i)), "l"(src + i)
+                     : "memory");
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();
+    for (int r = threadIdx.x; r < ns_; r += blockDim.x) {
+      const int c = sset[r];
+      const int s = cslot[c];
+      const bool ib = cbuf[c];
+      const double* row = stage + r * DS;
+      double acc = 0.0;
+#pragma unroll 16
+      for (int i = 0; i < d; ++i) acc = dadd(acc, dmul(qd[i], row[i]));
+      const double nr = ib ? t.bnorm[s] : t.rnorm[s];
+      ssim[r] = clamp1(ddiv(acc, dmul(nq, nr)));
+      skey[r] = 2LL * t.cid[s] + (ib ? 1 : 0);
+    }
+    __syncthreads();
+    block_rank_select(ssim, skey, ns_, take, order);
+    if (threadIdx.x < take) order[threadIdx.x] = sset[order[threadIdx.x]];
+    __syncthreads();
     K4MARK(3)
     if (threadIdx.x < take) {
       const int b = order[threadIdx.x];
@@ -1460,9 +1525,6 @@ __global__ void __launch_bounds__(256) k_score_select(DevTables t, DecodeArgs a,
     }
     nver_s = nv;
     a.n_ver[l] = nv;
-    bool lz = false;
-    for (int j = 0; j < nv; ++j) lz |= t.lazy[vers[j]] != 0;
-    if (lz) atomicOr(a.flags, 1);
   }
   __syncthreads();
   const int nv = nver_s;
@@ -1473,6 +1535,7 @@ __global__ void __launch_bounds__(256) k_score_select(DevTables t, DecodeArgs a,
     vnp[threadIdx.x] = t.npages[s];
     vnbp[threadIdx.x] = t.nbpages[s];
     atomicAdd(&att_s, static_cast<unsigned long long>(t.nmem[s] + t.nbuf[s]));
+    if (t.lazy[s]) atomicOr(a.flags, 1);  // a pending split: the host must settle before the next step
   }
   if (threadIdx.x < 64) ring_cnt[threadIdx.x] = 0;
   __syncthreads();
@@ -1484,7 +1547,7 @@ __global__ void __launch_bounds__(256) k_score_select(DevTables t, DecodeArgs a,
     const int n_pad = (n_ring + blockDim.x - 1) / blockDim.x * blockDim.x;  // warp-uniform trip count
     for (int i = threadIdx.x; i < n_pad; i += blockDim.x) {
       const int rs = i / t.tmax, tt = i - rs * t.tmax;
-      bool keep = i < n_ring && tt < t.ring_count[rs];
+      bool keep = i < n_ring && tt < ring_count_s[rs];
       if (keep) {
         const int own = owners[i];
         for (int j = 0; j < nv; ++j) keep &= vers[j] != own;
