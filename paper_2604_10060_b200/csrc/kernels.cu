@@ -1280,7 +1280,8 @@ __global__ void __launch_bounds__(256) k_score_select(DevTables t, DecodeArgs a,
   p += static_cast<size_t>(nsel) * 4;
   float* approx = reinterpret_cast<float*>(p);  // approximate candidate scores
   p += static_cast<size_t>(nsel) * 4;
-  double* stage = reinterpret_cast<double*>(p);  // [K4_ROWS][d+1]
+  p = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 15) & ~static_cast<uintptr_t>(15));
+  double* stage = reinterpret_cast<double*>(p);  // [K4_ROWS][d+1] (16-byte aligned for cp.async)
   p += static_cast<size_t>(K4_ROWS) * DS * 8;
   int* owners = reinterpret_cast<int*>(p);  // [W][tmax] ring owners of this domain
   p += static_cast<size_t>(t.W) * t.tmax * 4;
