@@ -1296,6 +1296,7 @@ __global__ void __launch_bounds__(256) k_score_select(DevTables t, DecodeArgs a,
   __shared__ bool degen;
   __shared__ int ring_count_s[64];
   __shared__ int sset[K4_ROWS], n_s;
+  __shared__ float qf32[256];
   __shared__ double ssim[K4_ROWS];
   __shared__ long long skey[K4_ROWS];
 
@@ -1303,7 +1304,10 @@ __global__ void __launch_bounds__(256) k_score_select(DevTables t, DecodeArgs a,
 #define K4MARK(k) if (a.k4prof && threadIdx.x == 0) { const long long kc1 = clock64(); a.k4prof[l * 8 + (k)] = kc1 - kc0; kc0 = kc1; }
   if (l == 0 && threadIdx.x == 0) *work_ctr = 0;
   const float* q = a.q + static_cast<int64_t>(l) * d;
-  for (int i = threadIdx.x; i < d; i += blockDim.x) qd[i] = static_cast<double>(q[i]);
+  for (int i = threadIdx.x; i < d; i += blockDim.x) {
+    qd[i] = static_cast<double>(q[i]);
+    qf32[i] = q[i];
+  }
   // the window ring owners are needed after ranking; fetch them now
   {
     const int n_own = t.W * t.tmax;
@@ -1421,12 +1425,16 @@ __global__ void __launch_bounds__(256) k_score_select(DevTables t, DecodeArgs a,
         const float* row = st32 + r * DS32;
         float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
         // element order rotated by the row index: banks (4r + r + i) mod 32 are distinct per lane
+        int j = r & 31;
         for (int i0 = 0; i0 < d; i0 += 4) {
-          const int j0 = (i0 + r) % d, j1 = (i0 + 1 + r) % d, j2 = (i0 + 2 + r) % d, j3 = (i0 + 3 + r) % d;
-          a0 = fmaf(static_cast<float>(qd[j0]), row[j0], a0);
-          a1 = fmaf(static_cast<float>(qd[j1]), row[j1], a1);
-          a2 = fmaf(static_cast<float>(qd[j2]), row[j2], a2);
-          a3 = fmaf(static_cast<float>(qd[j3]), row[j3], a3);
+          a0 = fmaf(qf32[j], row[j], a0);
+          j = j + 1 == d ? 0 : j + 1;
+          a1 = fmaf(qf32[j], row[j], a1);
+          j = j + 1 == d ? 0 : j + 1;
+          a2 = fmaf(qf32[j], row[j], a2);
+          j = j + 1 == d ? 0 : j + 1;
+          a3 = fmaf(qf32[j], row[j], a3);
+          j = j + 1 == d ? 0 : j + 1;
         }
         const int s = cslot[c];
         const bool ib = cbuf[c];
