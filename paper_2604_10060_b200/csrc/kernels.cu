@@ -2138,9 +2138,11 @@ int launch_attend_t(const DevTables& t, const DecodeArgs& a, cudaStream_t st) {
                          static_cast<int>(smem));
     attr = true;
   }
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_attend<D, BF16, STAGES>, ATT_THREADS + 32, smem);
-  per_sm = max(1, per_sm);
+  static int per_sm = 0;  // occupancy is a property of the kernel: query once
+  if (!per_sm) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_attend<D, BF16, STAGES>, ATT_THREADS + 32, smem);
+    per_sm = max(1, per_sm);
+  }
   k_attend<D, BF16, STAGES><<<g_sms * per_sm, ATT_THREADS + 32, smem, st>>>(t, a, g_ctr);
   return 1;
 }
