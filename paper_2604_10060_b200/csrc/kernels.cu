@@ -1707,6 +1707,9 @@ __global__ void __launch_bounds__(ATT_THREADS + 32) k_attend(DevTables t, Decode
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int L = min(t.L, 1024);
   for (int l = tid; l < L; l += blockDim.x) prefix[l + 1] = a.n_items[l];
+  // stale rows past a page's fill are read unmasked (and weighted by p = 0): keep them finite
+  for (int64_t i = tid; i < STAGES * stage_bytes / 16; i += blockDim.x)
+    reinterpret_cast<uint4*>(stages)[i] = make_uint4(0, 0, 0, 0);
   if (tid == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
@@ -1818,24 +1821,24 @@ __global__ void __launch_bounds__(ATT_THREADS + 32) k_attend(DevTables t, Decode
     for (int tb = 0; tb < fill; tb += 64) {
       const int t0 = tb + warp * 8;  // this warp's first token
       if (t0 >= fill) continue;      // warp-uniform
-      // ---- partial dots: 8 tokens x OPL dims per lane
+      // ---- partial dots: 8 tokens x OPL dims per lane. Rows at or past `fill` hold finite stale
+      // data (stages are zeroed at start), so no per-token bounds tests: they are masked below.
       float v[8];
+      const uint8_t* kbase = Ks + static_cast<int64_t>(t0) * ROWB + lane * OPL * ES;
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         float acc = 0.f;
-        if (t0 + j < fill) {
-          const uint8_t* krow = Ks + static_cast<int64_t>(t0 + j) * ROWB + lane * OPL * ES;
-          if (BF16) {
+        const uint8_t* krow = kbase + j * ROWB;
+        if (BF16) {
 #pragma unroll
-            for (int i = 0; i < OPL; i += 2) {
-              const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(krow + i * 2));
-              acc = fmaf(f.x, qr[i], acc);
-              if (i + 1 < OPL) acc = fmaf(f.y, qr[i + 1], acc);
-            }
-          } else {
-#pragma unroll
-            for (int i = 0; i < OPL; ++i) acc = fmaf(reinterpret_cast<const float*>(krow)[i], qr[i], acc);
+          for (int i = 0; i < OPL; i += 2) {
+            const uint32_t w = *reinterpret_cast<const uint32_t*>(krow + i * 2);
+            acc = fmaf(__uint_as_float(w << 16), qr[i], acc);
+            if (i + 1 < OPL) acc = fmaf(__uint_as_float(w & 0xffff0000u), qr[i + 1], acc);
           }
+        } else {
+#pragma unroll
+          for (int i = 0; i < OPL; ++i) acc = fmaf(reinterpret_cast<const float*>(krow)[i], qr[i], acc);
         }
         v[j] = acc;
       }
@@ -1887,18 +1890,18 @@ __global__ void __launch_bounds__(ATT_THREADS + 32) k_attend(DevTables t, Decode
       for (int i = 0; i < OPL; ++i) o_run[i] *= alpha;
       m_run = m_new;
       // ---- p.v: token j's probability lives in lane (j>>2&1)*16 + (j>>1&1)*8 + (j&1)*4
+      const uint8_t* vbase = Vs + static_cast<int64_t>(t0) * ROWB + lane * OPL * ES;
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         const int src = ((j >> 2) & 1) * 16 + ((j >> 1) & 1) * 8 + (j & 1) * 4;
-        const float pj = __shfl_sync(kFull, pr, src);
-        if (t0 + j >= fill) break;
-        const uint8_t* vrow = Vs + static_cast<int64_t>(t0 + j) * ROWB + lane * OPL * ES;
+        const float pj = __shfl_sync(kFull, pr, src);  // 0 for masked / past-fill tokens
+        const uint8_t* vrow = vbase + j * ROWB;
         if (BF16) {
 #pragma unroll
           for (int i = 0; i < OPL; i += 2) {
-            const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(vrow + i * 2));
-            o_run[i] = fmaf(pj, f.x, o_run[i]);
-            if (i + 1 < OPL) o_run[i + 1] = fmaf(pj, f.y, o_run[i + 1]);
+            const uint32_t w = *reinterpret_cast<const uint32_t*>(vrow + i * 2);
+            o_run[i] = fmaf(pj, __uint_as_float(w << 16), o_run[i]);
+            if (i + 1 < OPL) o_run[i + 1] = fmaf(pj, __uint_as_float(w & 0xffff0000u), o_run[i + 1]);
           }
         } else {
 #pragma unroll
