@@ -225,8 +225,8 @@ int kvc_cluster(kvc_ctx* ctx, int64_t id, int64_t* info, double* var, double* re
     info[2] = static_cast<int64_t>(c->members.size());
     info[3] = static_cast<int64_t>(c->buffer.size());
     info[4] = c->stat_count;
-    info[5] = c->lazy ? 1 : 0;
-    info[6] = c->host ? 1 : 0;
+    info[5] = F(ctx).is_lazy(id) ? 1 : 0;
+    info[6] = F(ctx).is_host(id) ? 1 : 0;
     info[7] = c->device_tail;
     info[8] = c->first_frame;
     info[9] = c->last_touch;

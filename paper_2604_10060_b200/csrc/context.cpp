@@ -396,7 +396,6 @@ std::int64_t Context::new_cluster(std::int32_t layer, std::int64_t parent,
   c->parent = parent;
   c->members = std::move(members);
   c->stat_count = static_cast<std::int64_t>(c->members.size());
-  c->host = host;
   c->first_frame = c->members.front().frame;
   c->last_touch = c->members.front().frame;
   for (const Member& m : c->members) {
@@ -404,6 +403,8 @@ std::int64_t Context::new_cluster(std::int32_t layer, std::int64_t parent,
     c->last_touch = std::max(c->last_touch, m.frame);
     frame_add(m.frame, c->id);
   }
+  cflags_.push_back(host ? CF_HOST : 0);
+  last_use_.push_back(0);
   c->slot = take_slot();
   slot_id_[static_cast<std::size_t>(c->slot)] = c->id;
   resid_h_[static_cast<std::size_t>(c->slot)] = host ? 1 : 0;
@@ -499,7 +500,7 @@ std::int64_t Context::entry_bytes() const {  // CostModel::entry_bytes (store.hp
 
 std::int64_t Context::side_entries(const Cluster& c) const {  // store.cpp:76-80
   const std::int64_t buffered = static_cast<std::int64_t>(c.buffer.size());
-  if (!c.host) return static_cast<std::int64_t>(c.members.size()) + buffered;
+  if (!is_host(c.id)) return static_cast<std::int64_t>(c.members.size()) + buffered;
   return c.device_tail + buffered;
 }
 
@@ -507,26 +508,25 @@ void Context::adopt(std::int64_t id) {  // store.cpp:82-86
   Cluster& c = C(id);
   device_entries_ += side_entries(c);
   std::int64_t tk = tick_++;
-  if (!c.tracked) {
-    c.tracked = true;
-    c.last_use = tk;
+  if (!flag(id, CF_TRACKED)) {
+    set_flag(id, CF_TRACKED, true);
+    last_use_[static_cast<std::size_t>(id)] = tk;
   }
 }
 
 void Context::forget(std::int64_t id) {  // store.cpp:88-93
   Cluster& c = C(id);
   device_entries_ -= side_entries(c);
-  c.tracked = false;
-  if (c.pinned) {
-    c.pinned = false;
+  set_flag(id, CF_TRACKED, false);
+  if (flag(id, CF_PINNED)) {
+    set_flag(id, CF_PINNED, false);
     pinned_ids_.erase(std::remove(pinned_ids_.begin(), pinned_ids_.end(), id), pinned_ids_.end());
   }
 }
 
 void Context::touch(std::int64_t id) {  // store.cpp:139-141
-  Cluster& c = C(id);
-  c.tracked = true;
-  c.last_use = tick_++;
+  set_flag(id, CF_TRACKED, true);
+  last_use_[static_cast<std::size_t>(id)] = tick_++;
 }
 
 void Context::record(int cause, bool to_dev, std::int64_t id, std::int64_t bytes) {
@@ -536,9 +536,11 @@ void Context::record(int cause, bool to_dev, std::int64_t id, std::int64_t bytes
 }
 
 double Context::fetch(std::int64_t id, int cause) {  // store.cpp:95-113
-  Cluster& c = C(id);
+  if (id < 0 || id >= static_cast<std::int64_t>(clusters_.size()) || !clusters_[static_cast<std::size_t>(id)])
+    fail(-8, "unknown cluster id: " + std::to_string(id));
   touch(id);
-  if (!c.host) return 0.0;
+  if (!is_host(id)) return 0.0;  // resident: only the LRU tick moves (no object access)
+  Cluster& c = C(id);
   const std::int64_t moved = static_cast<std::int64_t>(c.members.size()) - c.device_tail;
   if (moved < 0) fail(-11, "device tail exceeds member count");
   double paid = 0.0;
@@ -548,7 +550,7 @@ double Context::fetch(std::int64_t id, int cause) {  // store.cpp:95-113
     paid = ledger_.back().cost_us;
     device_entries_ += moved;
   }
-  c.host = false;
+  set_flag(id, CF_HOST, false);
   c.device_tail = 0;
   resid_h_[static_cast<std::size_t>(c.slot)] = 0;
   resid_dirty_ = true;
@@ -558,7 +560,7 @@ double Context::fetch(std::int64_t id, int cause) {  // store.cpp:95-113
 
 double Context::offload(std::int64_t id) {  // store.cpp:115-130
   Cluster& c = C(id);
-  const std::int64_t moved = !c.host ? static_cast<std::int64_t>(c.members.size()) : c.device_tail;
+  const std::int64_t moved = !is_host(id) ? static_cast<std::int64_t>(c.members.size()) : c.device_tail;
   double paid = 0.0;
   if (moved > 0) {
     const std::int64_t bytes = moved * entry_bytes();
@@ -566,7 +568,7 @@ double Context::offload(std::int64_t id) {  // store.cpp:115-130
     paid = ledger_.back().cost_us;
     device_entries_ -= moved;
   }
-  c.host = true;
+  set_flag(id, CF_HOST, true);
   c.device_tail = 0;
   resid_h_[static_cast<std::size_t>(c.slot)] = 1;
   resid_dirty_ = true;
@@ -586,12 +588,15 @@ double Context::enforce_capacity() {  // store.cpp:156-164
 double Context::evict_one() {  // store.cpp:166-181
   std::int64_t victim = -1, vt = 0;
   for (const auto& up : clusters_) {
-    if (!up || !up->tracked || up->pinned) continue;
+    if (!up) continue;
+    const std::uint8_t f = cflags_[static_cast<std::size_t>(up->id)];
+    if (!(f & CF_TRACKED) || (f & CF_PINNED)) continue;
     if (side_entries(*up) == 0) continue;
     if (!up->buffer.empty()) continue;
-    if (victim < 0 || up->last_use < vt) {
+    const std::int64_t lu = last_use_[static_cast<std::size_t>(up->id)];
+    if (victim < 0 || lu < vt) {
       victim = up->id;
-      vt = up->last_use;
+      vt = lu;
     }
   }
   if (victim < 0) return -1.0;
@@ -619,9 +624,9 @@ std::vector<std::int64_t> Context::window_owner_ids() const {
 
 void Context::repin() {  // engine.cpp:67-75 + TieredStore::pin (store.cpp:143-145)
   for (std::int64_t id : pinned_ids_)
-    if (auto* c = clusters_[static_cast<std::size_t>(id)].get()) c->pinned = false;
+    if (clusters_[static_cast<std::size_t>(id)]) set_flag(id, CF_PINNED, false);
   pinned_ids_ = window_owner_ids();
-  for (std::int64_t id : pinned_ids_) C(id).pinned = true;
+  for (std::int64_t id : pinned_ids_) set_flag(id, CF_PINNED, true);
 }
 
 void Context::apply_cadence(std::int64_t frame_id, std::int64_t pid) {  // engine.cpp:95-132
@@ -631,7 +636,7 @@ void Context::apply_cadence(std::int64_t frame_id, std::int64_t pid) {  // engin
     for (const auto& list : closed.per_layer) ids.insert(ids.end(), list.begin(), list.end());
     for (std::int64_t cid : ids) {
       const Cluster& c = C(cid);
-      if (!c.host && !c.lazy) {
+      if (!is_host(cid) && !is_lazy(cid)) {
         const auto owners = window_owner_ids();
         if (!std::binary_search(owners.begin(), owners.end(), cid)) offload(cid);
       }
@@ -640,7 +645,8 @@ void Context::apply_cadence(std::int64_t frame_id, std::int64_t pid) {  // engin
   if (pid >= 0) last_partition_ = pid;
   std::vector<std::int64_t> stale;
   for (const auto& up : clusters_)
-    if (up && !up->host && !up->lazy && up->last_touch + cfg_.offload_horizon_frames < frame_id)
+    if (up && !(cflags_[static_cast<std::size_t>(up->id)] & (CF_HOST | CF_LAZY)) &&
+        up->last_touch + cfg_.offload_horizon_frames < frame_id)
       stale.push_back(up->id);
   if (!stale.empty()) {
     const auto owners = window_owner_ids();
@@ -822,10 +828,10 @@ void Context::run_inserts(std::int64_t frame_id, std::int64_t pid, int T, std::i
       switch (evk[t]) {
         case EV_ABSORB:  // add_member + note_device_append (index.cpp:170-175, store.cpp:132-137)
           c.members.push_back({frame_id, t});
-          if (c.host) c.device_tail += 1;
+          if (is_host(cid)) c.device_tail += 1;
           device_entries_ += 1;
-          c.tracked = true;  // touch (store.cpp:139-141)
-          c.last_use = tick_++;
+          set_flag(cid, CF_TRACKED, true);  // touch (store.cpp:139-141)
+          last_use_[static_cast<std::size_t>(cid)] = tick_++;
           mstats_[1] += 1;
           break;
         case EV_BUFJOIN:  // add_to_buffer + note_device_buffer_append
@@ -836,7 +842,7 @@ void Context::run_inserts(std::int64_t frame_id, std::int64_t pid, int T, std::i
           break;
         case EV_DEFER:  // lazy mark + buffer + register (maintainer.cpp:170-175)
           mstats_[6] += 1;
-          c.lazy = true;
+          set_flag(cid, CF_LAZY, true);
           c.buffer.push_back({frame_id, t});
           device_entries_ += 1;
           touch(cid);
@@ -1094,15 +1100,15 @@ std::int64_t Context::handle_host_event(std::int64_t frame_id, std::int64_t pid,
 
 std::vector<std::int64_t> Context::materialize(std::int64_t id) {  // maintainer.cpp:178-193
   Cluster& c = C(id);
-  if (!c.lazy) return {id};
-  if (c.host) fail(-11, "pending split settled without fetching the payload first");
+  if (!is_lazy(id)) return {id};
+  if (is_host(id)) fail(-11, "pending split settled without fetching the payload first");
   mstats_[4] += 1;  // settled_splits
   const std::int64_t rows = stage_cluster(c.slot, true);
   std::vector<Member> ids = c.members;
   ids.insert(ids.end(), c.buffer.begin(), c.buffer.end());
   const std::int64_t pid = c.parent;
   const int layer = c.layer;
-  const bool host = c.host;
+  const bool host = is_host(id);
   forget(id);
   drop_cluster(id);
   return split_pool(pid, layer, host, std::move(ids), rows, 0);

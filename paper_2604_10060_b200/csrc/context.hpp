@@ -31,15 +31,13 @@ struct Cluster {  // ClusterRecord (index.hpp:29-50) minus payload and statistic
   std::int32_t slot = -1;
   std::vector<Member> members, buffer;
   std::int64_t stat_count = 0;
-  bool lazy = false;
-  bool host = false;  // Residence::Host
   std::int64_t device_tail = 0;
   std::int64_t first_frame = 0, last_touch = 0;
-  // TieredStore::last_use_ entry (store.hpp:118)
-  bool tracked = false;
-  std::int64_t last_use = 0;
-  bool pinned = false;
+  // lazy_split, residence, the TieredStore LRU entry and the pin live in compact per-id arrays of
+  // the Context (cflags_ / last_use_) so the per-step bookkeeping stays cache resident
 };
+
+enum ClusterFlag : std::uint8_t { CF_HOST = 1, CF_LAZY = 2, CF_TRACKED = 4, CF_PINNED = 8 };
 
 struct Partition {  // VisualPartition (index.hpp:52-58)
   std::vector<std::int64_t> frames;
@@ -93,6 +91,8 @@ class Context {
   int d() const { return d_; }
   int L() const { return L_; }
   const Cluster* cluster(std::int64_t id) const;
+  bool is_host(std::int64_t id) const { return cflags_[static_cast<std::size_t>(id)] & CF_HOST; }
+  bool is_lazy(std::int64_t id) const { return cflags_[static_cast<std::size_t>(id)] & CF_LAZY; }
   std::vector<std::int64_t> cluster_ids() const;
   void cluster_stats(std::int64_t id, double* var, double* rep, double* brep);
   int cluster_payload(std::int64_t id, int which, float* k, float* v, int cap);
@@ -174,6 +174,13 @@ class Context {
 
   // ---- host control plane
   std::vector<std::unique_ptr<Cluster>> clusters_;  // by id (dense, null when removed)
+  std::vector<std::uint8_t> cflags_;                 // by id: ClusterFlag bits
+  std::vector<std::int64_t> last_use_;               // by id: TieredStore::last_use_ tick
+  bool flag(std::int64_t id, std::uint8_t f) const { return cflags_[static_cast<std::size_t>(id)] & f; }
+  void set_flag(std::int64_t id, std::uint8_t f, bool v) {
+    std::uint8_t& x = cflags_[static_cast<std::size_t>(id)];
+    x = v ? static_cast<std::uint8_t>(x | f) : static_cast<std::uint8_t>(x & ~f);
+  }
   std::int64_t n_live_ = 0;
   std::vector<std::int64_t> slot_id_;               // slot -> cluster id (-1 free)
   std::vector<std::int32_t> free_slots_;

@@ -118,13 +118,7 @@ void Context::replay_decode(const void* hblock, const std::int64_t* gt, int n_gt
   (void)h_parts;
   (void)h_nps;
 
-  // Translate every layer's slots to ids before any settle frees / reuses a slot; prefetch the
-  // host records the replay is about to touch (they are scattered across the heap).
-  for (int l = 0; l < L_; ++l)
-    for (int i = 0; i < h_nr[l]; ++i) {
-      const std::int64_t id = slot_id_[static_cast<std::size_t>(h_rs[l * da_.k_s + i])];
-      if (id >= 0) __builtin_prefetch(clusters_[static_cast<std::size_t>(id)].get(), 1, 1);
-    }
+  // Translate every layer's slots to ids before any settle frees / reuses a slot.
   for (int l = 0; l < L_; ++l) {
     LayerOut& lo = last_[static_cast<std::size_t>(l)];
     lo.ranked.clear();
@@ -168,7 +162,7 @@ void Context::replay_decode(const void* hblock, const std::int64_t* gt, int n_gt
     predicted_next.clear();
     stall_next = 0.0;
     for (std::int64_t cid : verified) {
-      if (!C(cid).lazy) {  // materialize() is the identity for clusters without a pending split
+      if (!is_lazy(cid)) {  // materialize() is the identity for clusters without a pending split
         lo.selected.push_back(cid);
         continue;
       }
@@ -340,7 +334,7 @@ std::vector<std::pair<std::int64_t, int>> Context::flat_topk(const float* q, int
     if (!up || up->layer != layer) continue;
     slots.push_back(up->slot);
     bufs.push_back(0);
-    if (up->lazy) {
+    if (is_lazy(up->id)) {
       slots.push_back(up->slot);
       bufs.push_back(1);
     }
@@ -437,12 +431,12 @@ void Context::check() {
     if (c.members.empty()) bad("cluster with no members");
     if (c.stat_count != static_cast<std::int64_t>(c.members.size() + c.buffer.size()))
       bad("statistics count out of step with held entries");
-    if (c.lazy != !c.buffer.empty()) bad("deferred-split flag out of step with buffer");
-    if (!c.host && c.device_tail != 0) bad("device-resident cluster with a device tail");
+    if (is_lazy(c.id) != !c.buffer.empty()) bad("deferred-split flag out of step with buffer");
+    if (!is_host(c.id) && c.device_tail != 0) bad("device-resident cluster with a device tail");
     if (c.device_tail < 0 || c.device_tail > static_cast<std::int64_t>(c.members.size()))
       bad("device tail outside the member count");
     if (dstat[s] != c.stat_count || dnmem[s] != static_cast<std::int64_t>(c.members.size()) ||
-        dnbuf[s] != static_cast<std::int32_t>(c.buffer.size()) || (dlazy[s] != 0) != c.lazy)
+        dnbuf[s] != static_cast<std::int32_t>(c.buffer.size()) || (dlazy[s] != 0) != is_lazy(c.id))
       bad("device cluster table out of step with the host control plane");
     std::int64_t first = c.members.front().frame;
     for (const Member& m : c.members) {
