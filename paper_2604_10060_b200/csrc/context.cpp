@@ -405,6 +405,7 @@ std::int64_t Context::new_cluster(std::int32_t layer, std::int64_t parent,
   }
   cflags_.push_back(host ? CF_HOST : 0);
   last_use_.push_back(0);
+  if (!host) min_lt_ = std::min(min_lt_, c->last_touch);
   c->slot = take_slot();
   slot_id_[static_cast<std::size_t>(c->slot)] = c->id;
   resid_h_[static_cast<std::size_t>(c->slot)] = host ? 1 : 0;
@@ -474,14 +475,20 @@ void Context::pl_upload(std::int64_t pid, int layer) {
   KVC_CUDA(cudaStreamSynchronize(st_));
 }
 
+// Partition representative -> device without a host sync: the values go through a pinned ring
+// (the stream is synchronised at least once per ingested frame, long before a slot is reused).
 void Context::upload_partition(std::int64_t pid) {
   const Partition& p = parts_[static_cast<std::size_t>(pid)];
-  double nrm = norm_d(p.vrep.data(), d_);
-  KVC_CUDA(cudaMemcpyAsync(t_.vrep + pid * d_, p.vrep.data(), d_ * 8, cudaMemcpyHostToDevice, st_));
-  KVC_CUDA(cudaMemcpyAsync(t_.vnorm + pid, &nrm, 8, cudaMemcpyHostToDevice, st_));
+  constexpr int kRing = 64;
+  if (!h_part_ring_) h_part_ring_ = static_cast<double*>(halloc(static_cast<std::size_t>(kRing) * (d_ + 2) * 8));
+  double* slot = h_part_ring_ + static_cast<std::size_t>(part_ring_pos_++ % kRing) * (d_ + 2);
+  std::memcpy(slot, p.vrep.data(), d_ * 8);
+  slot[d_] = norm_d(p.vrep.data(), d_);
   std::int32_t np = static_cast<std::int32_t>(parts_.size());
-  KVC_CUDA(cudaMemcpyAsync(t_.n_parts, &np, 4, cudaMemcpyHostToDevice, st_));
-  KVC_CUDA(cudaStreamSynchronize(st_));
+  std::memcpy(&slot[d_ + 1], &np, 4);
+  KVC_CUDA(cudaMemcpyAsync(t_.vrep + pid * d_, slot, d_ * 8, cudaMemcpyHostToDevice, st_));
+  KVC_CUDA(cudaMemcpyAsync(t_.vnorm + pid, &slot[d_], 8, cudaMemcpyHostToDevice, st_));
+  KVC_CUDA(cudaMemcpyAsync(t_.n_parts, &slot[d_ + 1], 4, cudaMemcpyHostToDevice, st_));
 }
 
 void Context::flush_resid() {
@@ -552,6 +559,7 @@ double Context::fetch(std::int64_t id, int cause) {  // store.cpp:95-113
   }
   set_flag(id, CF_HOST, false);
   c.device_tail = 0;
+  min_lt_ = std::min(min_lt_, c.last_touch);
   resid_h_[static_cast<std::size_t>(c.slot)] = 0;
   resid_dirty_ = true;
   paid += enforce_capacity();
@@ -643,7 +651,16 @@ void Context::apply_cadence(std::int64_t frame_id, std::int64_t pid) {  // engin
     }
   }
   if (pid >= 0) last_partition_ = pid;
+  // no Device, non-lazy cluster can be stale while the lower bound on their last_touch is recent
+  if (min_lt_ == INT64_MAX || min_lt_ + cfg_.offload_horizon_frames >= frame_id) {
+    enforce_capacity();
+    return;
+  }
   std::vector<std::int64_t> stale;
+  std::int64_t lo = INT64_MAX;
+  for (const auto& up : clusters_)
+    if (up && !(cflags_[static_cast<std::size_t>(up->id)] & (CF_HOST | CF_LAZY))) lo = std::min(lo, up->last_touch);
+  min_lt_ = lo;
   for (const auto& up : clusters_)
     if (up && !(cflags_[static_cast<std::size_t>(up->id)] & (CF_HOST | CF_LAZY)) &&
         up->last_touch + cfg_.offload_horizon_frames < frame_id)
@@ -813,45 +830,48 @@ void Context::run_inserts(std::int64_t frame_id, std::int64_t pid, int T, std::i
     const std::int32_t* evs = h_evs_ + static_cast<std::size_t>(l) * t_.tmax;
     std::int32_t* owner = &ring_owner_h_[(static_cast<std::size_t>(l) * t_.W + ring_slot) * t_.tmax];
     std::int64_t last_cid = -1;
-    for (int t = replayed[static_cast<std::size_t>(l)]; t < stop; ++t) {
+    // replay in runs of equal (cluster, outcome): ticks are consecutive within a run, so the run
+    // moves the LRU tick once (store.cpp:139-141) and appends its members in one go
+    for (int t = replayed[static_cast<std::size_t>(l)]; t < stop;) {
       const std::int32_t slot = evs[t];
+      const std::int32_t kind = evk[t];
+      int u = t + 1;
+      while (u < stop && evs[u] == slot && evk[u] == kind && kind != EV_DEFER) ++u;
+      const int n = u - t;
       const std::int64_t cid = slot_id_[static_cast<std::size_t>(slot)];
       Cluster& c = *clusters_[static_cast<std::size_t>(cid)];
-      mstats_[0] += 1;  // inserts
-      c.stat_count += 1;
+      mstats_[0] += n;  // inserts
+      c.stat_count += n;
       c.last_touch = std::max(c.last_touch, frame_id);
-      if (cid != last_cid) {  // consecutive tokens mostly share a cluster
+      if (cid != last_cid) {
         frame_add(frame_id, cid);
         last_cid = cid;
       }
-      owner[t] = slot;
-      switch (evk[t]) {
+      std::fill(owner + t, owner + u, slot);
+      std::vector<Member>& dst = kind == EV_ABSORB ? c.members : c.buffer;
+      for (int k = t; k < u; ++k) dst.push_back({frame_id, k});
+      device_entries_ += n;
+      set_flag(cid, CF_TRACKED, true);
+      tick_ += n;
+      last_use_[static_cast<std::size_t>(cid)] = tick_ - 1;
+      switch (kind) {
         case EV_ABSORB:  // add_member + note_device_append (index.cpp:170-175, store.cpp:132-137)
-          c.members.push_back({frame_id, t});
-          if (is_host(cid)) c.device_tail += 1;
-          device_entries_ += 1;
-          set_flag(cid, CF_TRACKED, true);  // touch (store.cpp:139-141)
-          last_use_[static_cast<std::size_t>(cid)] = tick_++;
-          mstats_[1] += 1;
+          if (is_host(cid)) c.device_tail += n;
+          mstats_[1] += n;
           break;
         case EV_BUFJOIN:  // add_to_buffer + note_device_buffer_append
-          c.buffer.push_back({frame_id, t});
-          device_entries_ += 1;
-          touch(cid);
-          mstats_[3] += 1;
+          mstats_[3] += n;
           break;
         case EV_DEFER:  // lazy mark + buffer + register (maintainer.cpp:170-175)
-          mstats_[6] += 1;
+          mstats_[6] += n;
           set_flag(cid, CF_LAZY, true);
-          c.buffer.push_back({frame_id, t});
-          device_entries_ += 1;
-          touch(cid);
-          mstats_[3] += 1;
+          mstats_[3] += n;
           break;
         default:
           fail(-11, "unexpected device event kind");
       }
-      if (assigned) assigned[static_cast<std::size_t>(l) * T + t] = cid;
+      if (assigned) std::fill(assigned + static_cast<std::size_t>(l) * T + t, assigned + static_cast<std::size_t>(l) * T + u, cid);
+      t = u;
     }
     replayed[static_cast<std::size_t>(l)] = stop;
     if (stop >= T) {

@@ -8,6 +8,7 @@
 // the split slow path or through debug accessors.
 #pragma once
 
+#include <climits>
 #include <cstdint>
 #include <deque>
 #include <memory>
@@ -190,6 +191,9 @@ class Context {
   std::vector<std::uint8_t> resid_h_;               // device residence mirror
   bool resid_dirty_ = false;
   std::int64_t pl_bump_ = 0;
+  std::int64_t min_lt_ = INT64_MAX;  // lower bound of last_touch over Device, non-lazy clusters
+  double* h_part_ring_ = nullptr;
+  std::int64_t part_ring_pos_ = 0;
   // store
   std::int64_t device_entries_ = 0, tick_ = 0;
   std::vector<std::int64_t> pinned_ids_;
