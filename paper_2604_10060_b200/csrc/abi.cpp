@@ -241,9 +241,12 @@ int kvc_cluster_entries(kvc_ctx* ctx, int64_t id, int32_t which, int64_t* frames
   const kvc::Cluster* c = F(ctx).cluster(id);
   if (!c) return KVC_E_UNKNOWN_CLUSTER;
   const auto& v = which == 0 ? c->members : c->buffer;
-  for (int i = 0; i < static_cast<int>(v.size()) && i < cap; ++i) {
-    frames[i] = v[static_cast<std::size_t>(i)].frame;
-    tokens[i] = v[static_cast<std::size_t>(i)].token;
+  int i = 0;
+  for (const kvc::Member& m : v) {
+    if (i >= cap) break;
+    frames[i] = m.frame;
+    tokens[i] = m.token;
+    ++i;
   }
   return static_cast<int>(v.size());
 }

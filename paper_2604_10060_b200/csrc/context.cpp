@@ -394,14 +394,14 @@ std::int64_t Context::new_cluster(std::int32_t layer, std::int64_t parent,
   c->id = static_cast<std::int64_t>(clusters_.size());
   c->layer = layer;
   c->parent = parent;
-  c->members = std::move(members);
+  c->members = MemberList(members);
   c->stat_count = static_cast<std::int64_t>(c->members.size());
   c->first_frame = c->members.front().frame;
   c->last_touch = c->members.front().frame;
-  for (const Member& m : c->members) {
-    c->first_frame = std::min(c->first_frame, m.frame);
-    c->last_touch = std::max(c->last_touch, m.frame);
-    frame_add(m.frame, c->id);
+  for (const MemberList::Run& r : c->members.runs()) {
+    c->first_frame = std::min(c->first_frame, r.frame);
+    c->last_touch = std::max(c->last_touch, r.frame);
+    frame_add(r.frame, c->id);
   }
   cflags_.push_back(host ? CF_HOST : 0);
   last_use_.push_back(0);
@@ -422,8 +422,8 @@ void Context::drop_cluster(std::int64_t id) {
   Cluster& c = C(id);
   auto& sib = parts_[static_cast<std::size_t>(c.parent)].per_layer[static_cast<std::size_t>(c.layer)];
   sib.erase(std::remove(sib.begin(), sib.end(), id), sib.end());
-  for (const Member& m : c.members) frame_del(m.frame, id);
-  for (const Member& m : c.buffer) frame_del(m.frame, id);
+  for (const MemberList::Run& r : c.members.runs()) frame_del(r.frame, id);
+  for (const MemberList::Run& r : c.buffer.runs()) frame_del(r.frame, id);
   layer_live_count_[static_cast<std::size_t>(c.layer)] -= 1;
   n_live_ -= 1;
   std::int32_t s = c.slot;
@@ -784,7 +784,7 @@ void Context::run_inserts(std::int64_t frame_id, std::int64_t pid, int T, std::i
   ia_.pid = static_cast<std::int32_t>(pid);
   ia_.ring_slot = ring_slot;
   ia_.margin = 1e-4f;
-  double t_wait = 0.0;
+  double t_wait = 0.0, t_replay = 0.0, t_launch = 0.0;
   for (double& x : ingest_t_) x = 0.0;
   const auto r0 = std::chrono::steady_clock::now();
   while (frontier < L_) {
@@ -796,6 +796,7 @@ void Context::run_inserts(std::int64_t frame_id, std::int64_t pid, int T, std::i
       }
       for (int l = 0; l < L_; ++l) h_cursor_[l] = cursor[static_cast<std::size_t>(l)];
       KVC_CUDA(cudaMemcpyAsync(d_active_, h_active_, L_ * 8, cudaMemcpyHostToDevice, st_));
+      const auto lc0 = std::chrono::steady_clock::now();
       if (timing_) KVC_CUDA(cudaEventRecord(ev_[0], st_));
       launches_ += launch_build_cands(t_, ia_, st_);
       if (timing_) KVC_CUDA(cudaEventRecord(ev_[1], st_));
@@ -812,6 +813,7 @@ void Context::run_inserts(std::int64_t frame_id, std::int64_t pid, int T, std::i
       KVC_CUDA(cudaMemcpyAsync(h_stop_, ia_.stop_t, static_cast<std::size_t>(L_) * 12, cudaMemcpyDeviceToHost, st_));
       KVC_CUDA(cudaMemcpyAsync(h_err_, t_.err, 4, cudaMemcpyDeviceToHost, st_));
       const auto w0 = std::chrono::steady_clock::now();
+      t_launch += std::chrono::duration<double, std::micro>(w0 - lc0).count();
       sync();
       t_wait += std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - w0).count();
       check_err_word(*h_err_);
@@ -830,6 +832,7 @@ void Context::run_inserts(std::int64_t frame_id, std::int64_t pid, int T, std::i
     const std::int32_t* evs = h_evs_ + static_cast<std::size_t>(l) * t_.tmax;
     std::int32_t* owner = &ring_owner_h_[(static_cast<std::size_t>(l) * t_.W + ring_slot) * t_.tmax];
     std::int64_t last_cid = -1;
+    const auto rp0 = std::chrono::steady_clock::now();
     // replay in runs of equal (cluster, outcome): ticks are consecutive within a run, so the run
     // moves the LRU tick once (store.cpp:139-141) and appends its members in one go
     for (int t = replayed[static_cast<std::size_t>(l)]; t < stop;) {
@@ -848,8 +851,7 @@ void Context::run_inserts(std::int64_t frame_id, std::int64_t pid, int T, std::i
         last_cid = cid;
       }
       std::fill(owner + t, owner + u, slot);
-      std::vector<Member>& dst = kind == EV_ABSORB ? c.members : c.buffer;
-      for (int k = t; k < u; ++k) dst.push_back({frame_id, k});
+      (kind == EV_ABSORB ? c.members : c.buffer).push_run(frame_id, t, n);
       device_entries_ += n;
       set_flag(cid, CF_TRACKED, true);
       tick_ += n;
@@ -873,6 +875,7 @@ void Context::run_inserts(std::int64_t frame_id, std::int64_t pid, int T, std::i
       if (assigned) std::fill(assigned + static_cast<std::size_t>(l) * T + t, assigned + static_cast<std::size_t>(l) * T + u, cid);
       t = u;
     }
+    t_replay += std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - rp0).count();
     replayed[static_cast<std::size_t>(l)] = stop;
     if (stop >= T) {
       frontier += 1;
@@ -899,6 +902,8 @@ void Context::run_inserts(std::int64_t frame_id, std::int64_t pid, int T, std::i
     }
   }
   ingest_t_[5] = t_wait;
+  ingest_t_[7] = t_replay;  // (instrumentation) replay loop; launches in ingest_t_[6] below
+  ingest_t_[4] = t_launch;
   ingest_t_[6] = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - r0).count() - t_wait;
 }
 
@@ -1107,7 +1112,7 @@ std::int64_t Context::handle_host_event(std::int64_t frame_id, std::int64_t pid,
   KVC_CUDA(cudaMemcpyAsync(static_cast<std::uint8_t*>(d_stage_v_) + rows * rb,
                            static_cast<std::uint8_t*>(d_fv_) + frow * rb, rb, cudaMemcpyDeviceToDevice, st_));
   std::vector<Member> ids = c.members;
-  ids.insert(ids.end(), c.buffer.begin(), c.buffer.end());
+  for (const Member& m : c.buffer) ids.push_back(m);
   ids.push_back({frame_id, tok});
   forget(cid);
   drop_cluster(cid);
@@ -1125,7 +1130,7 @@ std::vector<std::int64_t> Context::materialize(std::int64_t id) {  // maintainer
   mstats_[4] += 1;  // settled_splits
   const std::int64_t rows = stage_cluster(c.slot, true);
   std::vector<Member> ids = c.members;
-  ids.insert(ids.end(), c.buffer.begin(), c.buffer.end());
+  for (const Member& m : c.buffer) ids.push_back(m);
   const std::int64_t pid = c.parent;
   const int layer = c.layer;
   const bool host = is_host(id);

@@ -10,7 +10,9 @@
 
 #include <climits>
 #include <cstdint>
+#include <cstddef>
 #include <deque>
+#include <iterator>
 #include <memory>
 #include <unordered_map>
 #include <vector>
@@ -25,12 +27,75 @@ struct Member {
   std::int32_t token;
 };
 
+// Member identities of a cluster in stored order, run-length encoded: a frame's tokens are
+// appended in runs (one run per frame and cluster on the ingest path), so a 512-member cluster is
+// a handful of runs and appends never reallocate a long vector.
+class MemberList {
+ public:
+  struct Run {
+    std::int64_t frame;
+    std::int32_t tok0, count;
+  };
+  class iterator {
+   public:
+    using iterator_category = std::forward_iterator_tag;
+    using value_type = Member;
+    using difference_type = std::ptrdiff_t;
+    using pointer = const Member*;
+    using reference = Member;
+    iterator(const Run* r, std::int32_t k) : r_(r), k_(k) {}
+    Member operator*() const { return {r_->frame, r_->tok0 + k_}; }
+    iterator& operator++() {
+      if (++k_ == r_->count) {
+        ++r_;
+        k_ = 0;
+      }
+      return *this;
+    }
+    iterator operator++(int) {
+      iterator x = *this;
+      ++*this;
+      return x;
+    }
+    bool operator==(const iterator& o) const { return r_ == o.r_ && k_ == o.k_; }
+    bool operator!=(const iterator& o) const { return !(*this == o); }
+
+   private:
+    const Run* r_;
+    std::int32_t k_;
+  };
+  MemberList() = default;
+  MemberList(const std::vector<Member>& v) {
+    for (const Member& m : v) push_back(m);
+  }
+  void push_back(const Member& m) { push_run(m.frame, m.token, 1); }
+  void push_run(std::int64_t frame, std::int32_t tok0, std::int32_t count) {
+    if (count <= 0) return;
+    if (!runs_.empty() && runs_.back().frame == frame && runs_.back().tok0 + runs_.back().count == tok0)
+      runs_.back().count += count;
+    else
+      runs_.push_back({frame, tok0, count});
+    n_ += count;
+  }
+  std::size_t size() const { return static_cast<std::size_t>(n_); }
+  bool empty() const { return n_ == 0; }
+  Member front() const { return {runs_.front().frame, runs_.front().tok0}; }
+  iterator begin() const { return iterator(runs_.data(), 0); }
+  iterator end() const { return iterator(runs_.data() + runs_.size(), 0); }
+  const std::vector<Run>& runs() const { return runs_; }
+  operator std::vector<Member>() const { return std::vector<Member>(begin(), end()); }
+
+ private:
+  std::vector<Run> runs_;
+  std::int64_t n_ = 0;
+};
+
 struct Cluster {  // ClusterRecord (index.hpp:29-50) minus payload and statistics
   std::int64_t id = 0;
   std::int32_t layer = 0;
   std::int64_t parent = 0;
   std::int32_t slot = -1;
-  std::vector<Member> members, buffer;
+  MemberList members, buffer;
   std::int64_t stat_count = 0;
   std::int64_t device_tail = 0;
   std::int64_t first_frame = 0, last_touch = 0;
