@@ -195,7 +195,10 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    D = args.domains // world  # strong scaling over (layer, head) domains
+    from paper_2604_10060_b200.sharding import gather_domain_outputs, shard_domains
+
+    d0, d1 = shard_domains(args.domains, world, rank)  # strong scaling over (layer, head) domains
+    D = d1 - d0
     frames_t = args.frames or args.steps
 
     cfg = Config.make(kv_dtype=DTYPE_BF16, k_v=1, k_s=TOP_K, window_frames=WINDOW, build_batch_frames=1,
@@ -261,7 +264,6 @@ def main():
     nq = args.warmup + args.steps
     q_dev = workload.queries_near(st, nq, seed=11 + rank)
     out_dev = torch.zeros(D, HEAD_DIM, device="cuda")
-    gathered = torch.zeros(world * D, HEAD_DIM, device="cuda") if world > 1 else None
     for i in range(args.warmup):
         kv.query(i, q_dev[i], out=out_dev)
     kv.set_timing(True)
@@ -280,8 +282,8 @@ def main():
                 att_us.append(tm[1])
                 att_bytes_l.append(tm[4])
                 host_ph.append(tm[5:8].copy())
-                if world > 1:
-                    dist.all_gather_into_tensor(gathered, out_dev)
+                if world > 1:  # per-domain outputs to every rank (NCCL over NVLink)
+                    gather_domain_outputs(out_dev, args.domains)
             ev1.record(stream)
         torch.cuda.synchronize()
     decode_ms = ev0.elapsed_time(ev1)

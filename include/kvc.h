@@ -211,6 +211,19 @@ KVC_API int kvc_last_step_timing(kvc_ctx* ctx, double* t);
  * and of everything else in the on_insert loop incl. replay and host events (t[6]); t[7] the
  * number of host events (seeds / splits) the frame needed. */
 KVC_API int kvc_last_ingest_timing(kvc_ctx* ctx, double* t);
+/* Host slow-path primitives (no GPU needed), exported so the split / batch-build arithmetic can
+ * be checked bit-for-bit against the reference on CPU:
+ * split_two (clustering.cpp:180-208) and spherical_kmeans (clustering.cpp:80-178) over
+ * pts[n][d] f32; assign[n] receives the dense cluster index. Return the live cluster count
+ * (split_two: 2; *degenerate set for the (n-1, 1) rule) or a negative KVC_E_* code. tau
+ * (maintainer.cpp:11-14) and mix_seed (rng.hpp:47-52) as used by the device threshold table and
+ * the split seed sequence. */
+KVC_API int kvc_host_split_two(const float* pts, int32_t n, int32_t d, uint64_t seed, int32_t* assign,
+                               int32_t* degenerate);
+KVC_API int kvc_host_kmeans(const float* pts, int32_t n, int32_t d, int32_t k, int32_t max_iters, double tol,
+                            uint64_t seed, int32_t* assign, double* objective, int32_t* iterations);
+KVC_API double kvc_host_tau(int64_t n, double tau_min, double tau_max, double n0);
+KVC_API uint64_t kvc_host_mix_seed(uint64_t a, uint64_t b);
 /* Instrumentation: mean clock64 cycles per phase of the last resolve launch (out[8]). */
 KVC_API int kvc_debug_resolve_profile(kvc_ctx* ctx, double* out);
 /* Enables per-phase CUDA-event timing (off by default: it adds event records). */

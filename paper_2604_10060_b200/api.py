@@ -145,6 +145,13 @@ def lib():
         L.kvc_set_timing.argtypes = [vp, C.c_int32]
         L.kvc_last_ingest_timing.argtypes = [vp, f64p]
         L.kvc_debug_resolve_profile.argtypes = [vp, f64p]
+        L.kvc_host_split_two.argtypes = [f32p, C.c_int32, C.c_int32, C.c_uint64, i32p, i32p]
+        L.kvc_host_kmeans.argtypes = [f32p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_double,
+                                      C.c_uint64, i32p, f64p, i32p]
+        L.kvc_host_tau.restype = C.c_double
+        L.kvc_host_tau.argtypes = [C.c_int64, C.c_double, C.c_double, C.c_double]
+        L.kvc_host_mix_seed.restype = C.c_uint64
+        L.kvc_host_mix_seed.argtypes = [C.c_uint64, C.c_uint64]
         _lib = L
     return _lib
 
@@ -158,7 +165,8 @@ EXPORTED = [
     "kvc_partition", "kvc_partition_layer", "kvc_maint_stats", "kvc_ledger",
     "kvc_ledger_log_size", "kvc_ledger_op", "kvc_check", "kvc_offload", "kvc_fetch",
     "kvc_launch_count", "kvc_last_step_timing", "kvc_set_timing", "kvc_last_ingest_timing",
-    "kvc_debug_resolve_profile",
+    "kvc_debug_resolve_profile", "kvc_host_split_two", "kvc_host_kmeans", "kvc_host_tau",
+    "kvc_host_mix_seed",
 ]
 
 
@@ -402,3 +410,26 @@ class ClusterKVCache:
         t = np.zeros(8)
         lib().kvc_last_step_timing(self.h, _p(t, f64p))
         return t
+
+
+# ----------------------------------------------------------------------------- host slow path
+def host_split_two(pts: np.ndarray, seed: int):
+    """split_two (clustering.cpp:180-208) as run by the split slow path: (assign, degenerate)."""
+    p = np.ascontiguousarray(pts, np.float32)
+    n, d = p.shape
+    a = np.zeros(n, np.int32)
+    deg = C.c_int32()
+    _check(lib().kvc_host_split_two(_p(p, f32p), n, d, seed, _p(a, i32p), C.byref(deg)))
+    return a, bool(deg.value)
+
+
+def host_kmeans(pts: np.ndarray, k: int, max_iters: int = 50, tol: float = 1e-6, seed: int = 0):
+    """spherical_kmeans (clustering.cpp:80-178): (assign, k_live, objective, iterations)."""
+    p = np.ascontiguousarray(pts, np.float32)
+    n, d = p.shape
+    a = np.zeros(n, np.int32)
+    obj = C.c_double()
+    it = C.c_int32()
+    live = _check(lib().kvc_host_kmeans(_p(p, f32p), n, d, k, max_iters, tol, seed, _p(a, i32p),
+                                        C.byref(obj), C.byref(it)))
+    return a, live, obj.value, it.value

@@ -1,11 +1,13 @@
 // abi.cpp -- the extern "C" boundary (include/kvc.h). Every entry point catches kvc::Error and
 // returns its code; no exception crosses the ABI (SURVEY.md §8(b) "Errors").
+#include <cmath>
 #include <cstring>
 #include <memory>
 #include <string>
 
 #include "../../include/kvc.h"
 #include "context.hpp"
+#include "kmeans.hpp"
 
 using kvc::Context;
 
@@ -346,5 +348,36 @@ int kvc_last_ingest_timing(kvc_ctx* ctx, double* t) {
   for (int i = 0; i < 8; ++i) t[i] = s[i];
   return KVC_OK;
 }
+
+int kvc_host_split_two(const float* pts, int32_t n, int32_t d, uint64_t seed, int32_t* assign,
+                       int32_t* degenerate) {
+  int live = 0;
+  const int rc = guard([&] {
+    const kvc::KMeansOut o = kvc::split_two(pts, n, d, seed);
+    for (int i = 0; i < n; ++i) assign[i] = o.assign[static_cast<std::size_t>(i)];
+    if (degenerate) *degenerate = o.degenerate ? 1 : 0;
+    live = o.k_live;
+  });
+  return rc != KVC_OK ? rc : live;
+}
+
+int kvc_host_kmeans(const float* pts, int32_t n, int32_t d, int32_t k, int32_t max_iters, double tol,
+                    uint64_t seed, int32_t* assign, double* objective, int32_t* iterations) {
+  int live = 0;
+  const int rc = guard([&] {
+    const kvc::KMeansOut o = kvc::spherical_kmeans(pts, n, d, k, max_iters, tol, seed);
+    for (int i = 0; i < n; ++i) assign[i] = o.assign[static_cast<std::size_t>(i)];
+    if (objective) *objective = o.objective;
+    if (iterations) *iterations = o.iterations;
+    live = o.k_live;
+  });
+  return rc != KVC_OK ? rc : live;
+}
+
+double kvc_host_tau(int64_t n, double tau_min, double tau_max, double n0) {
+  return tau_min + (tau_max - tau_min) * std::exp(-static_cast<double>(n) / n0);  // maintainer.cpp:11-14
+}
+
+uint64_t kvc_host_mix_seed(uint64_t a, uint64_t b) { return kvc::mix_seed(a, b); }
 
 }  // extern "C"

@@ -1,0 +1,104 @@
+"""CPU tests of the product library without a GPU: the C-ABI loads and exports every entry point
+include/kvc.h declares, refuses to run without a device (no CPU fallback), and its host slow
+path (split / batch-build k-means, tau table, split seeds) is bit-exact with the reference."""
+import os
+import re
+
+import numpy as np
+import pytest
+
+from paper_2604_10060_b200 import api
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    with open(os.path.join(ROOT, "include", "kvc.h")) as f:
+        src = f.read()
+    return sorted(set(re.findall(r"KVC_API\s+[\w\s\*]+?\b(kvc_\w+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = api.lib()
+    syms = declared_symbols()
+    assert len(syms) >= 40
+    missing = [s for s in syms if not hasattr(lib, s)]
+    assert missing == []
+    assert sorted(api.EXPORTED) == syms
+
+
+def test_no_device_fails_loudly():
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    with pytest.raises(api.NoDevice):
+        api.ClusterKVCache(api.Config.make(), 32, 2)
+
+
+def test_config_defaults_match_reference_engine_config():
+    """kvc_cfg_default == EngineConfig{} field for field (engine.hpp:21-33)."""
+    from oracle import pyoracle as po
+
+    ref = po.EngineCfg.make()
+    mine = api.Config.make()
+    for name, _ in po.EngineCfg._fields_:
+        assert getattr(mine, name) == getattr(ref, name), name
+
+
+def test_unknown_config_key_rejected():
+    with pytest.raises(api.ConfigError):
+        api.Config.make(not_a_key=1)
+
+
+def test_host_tau_and_mix_seed_match_reference(ref_lib):
+    lib = api.lib()
+    for n in (0, 1, 7, 32, 100, 5000, 30000):
+        assert lib.kvc_host_tau(n, 0.05, 0.3, 32.0) == ref_lib.ref_prim_tau(n, 0.05, 0.3, 32.0)
+    for a, b in ((0, 2), (123, 0), (2**63 + 5, 77)):
+        assert lib.kvc_host_mix_seed(a, b) == ref_lib.ref_prim_mix_seed(a, b)
+
+
+@pytest.mark.parametrize("n,d,seed", [(2, 8, 1), (3, 16, 2), (50, 32, 3), (400, 128, 4), (1000, 64, 5)])
+def test_split_two_bit_exact(ref_lib, n, d, seed):
+    """The split slow path (maintainer.cpp:195-242 -> clustering.cpp:180-208)."""
+    from oracle import pyoracle as po
+
+    rng = np.random.default_rng(seed)
+    pts = rng.standard_normal((n, d)).astype(np.float32)
+    if seed == 2:  # all-identical points: the degenerate (n-1, 1) rule
+        pts[:] = pts[0]
+    a, deg = api.host_split_two(pts, seed * 7919)
+    ra = np.zeros(n, np.int32)
+    rdeg = ref_lib.ref_prim_split_two(po._p(pts, po.f32p), n, d, seed * 7919, po._p(ra, po.i32p))
+    assert np.array_equal(a, ra)
+    assert deg == bool(rdeg)
+
+
+@pytest.mark.parametrize("n,k,seed", [(64, 4, 1), (300, 16, 2), (196 * 4, 4, 3), (1000, 33, 4)])
+def test_spherical_kmeans_bit_exact(ref_lib, n, k, seed):
+    """Batch build (index.cpp:364-450 -> clustering.cpp:80-178)."""
+    import ctypes as C
+
+    from oracle import pyoracle as po
+
+    rng = np.random.default_rng(seed)
+    centers = rng.standard_normal((k, 48))
+    pts = (centers[rng.integers(0, k, n)] + 0.3 * rng.standard_normal((n, 48))).astype(np.float32)
+    a, live, obj, it = api.host_kmeans(pts, k, 50, 1e-6, seed)
+    ra = np.zeros(n, np.int32)
+    robj = C.c_double()
+    rit = C.c_int()
+    rlive = ref_lib.ref_prim_kmeans(po._p(pts, po.f32p), n, 48, k, 50, 1e-6, seed, po._p(ra, po.i32p),
+                                    C.byref(robj), C.byref(rit))
+    assert np.array_equal(a, ra) and live == rlive and obj == robj.value and it == rit.value
+
+
+def test_host_split_rejects_too_few_points():
+    with pytest.raises(api.TooFewPoints):
+        api.host_split_two(np.ones((1, 8), np.float32), 0)
+
+
+def test_host_split_rejects_zero_vector():
+    with pytest.raises(api.DegenerateVector):
+        api.host_split_two(np.zeros((3, 8), np.float32), 0)

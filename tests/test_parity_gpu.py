@@ -120,3 +120,39 @@ def test_deferred_and_prefetch_drift(ref_lib):
     st = r.kv.maint_stats()
     assert st[3] > 0, "stream must exercise the deferred path"
     assert r.att_err < ATT_TOL
+
+
+def test_config1_against_golden_fixture(stream1):
+    """Same stream, no reference library needed: the committed fixture (tests/golden, made by
+    tests/golden/make_golden.py from the reference) pins assignments, rankings and digests."""
+    import hashlib
+    import json
+    import os
+
+    from paper_2604_10060_b200 import ClusterKVCache
+    from tests.harness import product_config
+
+    with open(os.path.join(os.path.dirname(__file__), "golden", "config1_expect.json")) as f:
+        g = json.load(f)
+    s = stream1
+    kv = ClusterKVCache(product_config(po.config1_engine()), s.d, s.L)
+    fi = qi = 0
+    for kind, i in s.events():
+        if kind == "frame":
+            pid, asg = kv.process_frame(i, s.visual[i], s.keys[i], s.values[i])
+            exp = g["frames"][fi]
+            assert pid == exp["partition"]
+            assert hashlib.sha256(asg.astype(np.int64).tobytes()).hexdigest() == exp["assigned_sha256"], i
+            fi += 1
+        else:
+            kv.query(i, s.q[i], gt=s.gt[i])
+            exp = g["queries"][qi]
+            assert [kv.ranked(l) for l in range(s.L)] == [[tuple(x) for x in r] for r in exp["ranked"]]
+            assert [kv.selected(l) for l in range(s.L)] == exp["selected"]
+            assert str(kv.digest()) == exp["digest"]
+            assert kv.query_meta()[1] == exp["recall"]
+            qi += 1
+    assert kv.maint_stats().tolist() == g["maint_stats"]
+    ops, by, co, dev = kv.ledger()
+    assert ops.tolist() == g["ledger"]["ops"] and by.tolist() == g["ledger"]["bytes"]
+    assert dev == g["ledger"]["device_entries"]
