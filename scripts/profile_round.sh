@@ -1,0 +1,18 @@
+#!/bin/bash
+# Runs on a GPU box (via gpurun): tests, bench (both arms), the ncu launch list of a short bench and
+# one `ncu --set full` capture of the dominant kernels. Outputs land in gpurun_out/ (scratch);
+# summaries are copied into profiles/ by scripts/summarize_profiles.py on the build host.
+set -u
+OUT=gpurun_out/${1:-r1}
+mkdir -p "$OUT"
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,clocks.mem --format=csv > "$OUT/gpu.txt" 2>&1
+timeout 900 python -m pytest tests -m gpu -q > "$OUT/pytest_gpu.txt" 2>&1
+timeout 900 python bench.py > "$OUT/bench.json" 2> "$OUT/bench.err"
+timeout 900 python bench.py --impl reference > "$OUT/bench_reference.json" 2> "$OUT/bench_reference.err"
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none \
+  -k regex:"k_(attend|score_select|resolve|approx|topm|build_cands|store_rows|ring_write)" -c 600 --csv \
+  --log-file "$OUT/launches.csv" python bench.py --steps 5 --warmup 3 --frames 5 --no-cpu-baseline > "$OUT/ncu_launch.log" 2>&1
+timeout 1200 ncu --set full --clock-control none --import-source on \
+  -k regex:"k_(attend|score_select|resolve|approx|topm)" -s 25 -c 5 -o "$OUT/full" \
+  python bench.py --steps 5 --warmup 3 --frames 5 --no-cpu-baseline > "$OUT/ncu_full.log" 2>&1
+ls -la "$OUT"
