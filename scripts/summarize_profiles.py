@@ -1,0 +1,91 @@
+"""Summarises a profiling round (gpurun_out/<tag>/ from scripts/profile_round.sh) into profiles/.
+
+Writes profiles/<tag>_launches.csv (the ncu launch list), profiles/<tag>_summary.md (per-kernel
+share of the step, DRAM traffic, key counters) and profiles/ncu_attend_summary.json (DRAM bytes per
+attention launch, read by bench.py for roofline.traffic).
+"""
+import collections
+import csv
+import json
+import os
+import shutil
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+tag = sys.argv[1] if len(sys.argv) > 1 else "r1a"
+src = os.path.join(ROOT, "gpurun_out", tag)
+dst = os.path.join(ROOT, "profiles")
+os.makedirs(dst, exist_ok=True)
+shutil.copy(os.path.join(src, "launches.csv"), os.path.join(dst, f"{tag}_launches.csv"))
+
+rows = list(csv.reader(open(os.path.join(src, "launches.csv"))))
+hi = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
+h = rows[hi]
+ki, vi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
+agg = collections.defaultdict(list)
+for r in rows[hi + 1:]:
+    name = r[ki].split("(")[0].split("<")[0].split("::")[-1]
+    v = float(r[vi].replace(",", ""))
+    v = v / 1e3 if r[ui] in ("ns", "nsecond") else (v * 1e3 if r[ui] in ("ms", "msecond") else v)
+    agg[name].append(v)
+
+SCALE = {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3,
+         "byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3}
+
+
+def ncu_raw(kernel):
+    """Rows of the raw page for `kernel` across every full capture of the round, with durations
+    normalised to us and byte counts to MB."""
+    res = []
+    for rep in sorted(f for f in os.listdir(src) if f.endswith(".ncu-rep")):
+        out = subprocess.run(["ncu", "-i", os.path.join(src, rep), "--page", "raw", "--csv",
+                              "--kernel-name", f"regex:{kernel}"], capture_output=True, text=True).stdout
+        rr = list(csv.reader(out.splitlines()))
+        if len(rr) < 3:
+            continue
+        for x in rr[2:]:
+            m = dict(zip(rr[0], x))
+            units = dict(zip(rr[0], rr[1]))
+            for key in ("gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum"):
+                if key in m and units.get(key) in SCALE:
+                    m[key] = str(float(m[key].replace(",", "")) * SCALE[units[key]])
+            res.append(m)
+    return res
+
+def num(x):
+    try:
+        return float(str(x).replace(",", ""))
+    except Exception:
+        return None
+
+lines = [f"# Profiling round {tag}", "", "Source: `scripts/profile_round.sh` on one B200 (gpurun), read back with "
+         "`ncu -i`. Launch times are ncu's serialized, cold-cache `gpu__time_duration.sum` of a short bench "
+         "(5 decode steps, 5 ingested frames after 3 warm-up): compare SHARES, not absolutes.", "",
+         "| kernel | launches | mean us | total us |", "|---|---|---|---|"]
+tot = sum(sum(v) for v in agg.values())
+for k, v in sorted(agg.items(), key=lambda x: -sum(x[1])):
+    lines.append(f"| {k} | {len(v)} | {sum(v)/len(v):.1f} | {sum(v):.1f} ({100*sum(v)/tot:.0f}%) |")
+lines += ["", "## `ncu --set full` captures", "",
+          "| kernel | duration us | DRAM read MB | DRAM write MB | DRAM % peak | SM % | achieved occupancy | regs |",
+          "|---|---|---|---|---|---|---|---|"]
+att = {}
+for kname in ("k_attend", "k_score_select", "k_resolve", "k_approx", "k_topm"):
+    for m in ncu_raw(kname)[:1]:
+        dur = num(m.get("gpu__time_duration.sum"))
+        rd = num(m.get("dram__bytes_read.sum"))
+        wr = num(m.get("dram__bytes_write.sum"))
+        lines.append(f"| {kname} | {dur} | {rd} | {wr} | {m.get('gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed')} | "
+                     f"{m.get('sm__throughput.avg.pct_of_peak_sustained_elapsed')} | "
+                     f"{m.get('sm__warps_active.avg.pct_of_peak_sustained_active')} | {m.get('launch__registers_per_thread')} |")
+        if kname == "k_attend" and rd is not None:
+            # ncu reports MB (1e6) in this section
+            att = {"kernel": "k_attend", "dram_bytes_per_launch": int(((rd or 0) + (wr or 0)) * 1e6),
+                   "duration_us_ncu": dur, "source": f"profiles/{tag}_summary.md"}
+lines.append("")
+with open(os.path.join(dst, f"{tag}_summary.md"), "w") as f:
+    f.write("\n".join(lines) + "\n")
+if att:
+    with open(os.path.join(dst, "ncu_attend_summary.json"), "w") as f:
+        json.dump(att, f, indent=1)
+print("\n".join(lines))
