@@ -39,6 +39,13 @@ METRIC = "decode-step retrieve+attend µs @128K-token KV; frame ingest frames/s"
 D_TOTAL, HEAD_DIM, N_TOK, N_CLUST, T_FRAME, TOP_K, WINDOW = 112, 128, 669 * 196, 256, 196, 16, 4
 
 
+RESOLVE_KERNEL = "seq" if os.environ.get("KVC_RESOLVE") == "seq" else "spec"
+RESOLVE_PHASES = {  # clock64 phases of the resolve kernel (kvc_debug_resolve_profile), domain mean
+    "seq": ["argmax", "hot", "update", "build", "chain", "decide", "commit", "keyring"],
+    "spec": ["setup", "slot_table", "rep_chains", "exact_sums", "bound_max", "var_chain", "decisions",
+             "buffers", "verify", "commit", "rounds", "setup_keys", "setup_topm"],
+}
+
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
@@ -348,8 +355,8 @@ def main():
                            "h2d_bytes_per_step": D * T_FRAME * HEAD_DIM * 2 * 2, "d2h_bytes_per_step": 0},
                    "gpu_launches": int(ingest_launches),
                    "phases_us": ingest_phases,
-                   "resolve_cycles_per_frame": dict(zip(["argmax", "hot", "update", "build", "chain", "decide",
-                                                         "commit", "keyring"], prof_cycles.round(0).tolist())),
+                   "resolve_kernel": RESOLVE_KERNEL,
+                   "resolve_cycles_per_frame": dict(zip(RESOLVE_PHASES[RESOLVE_KERNEL], prof_cycles.round(1).tolist())),
                    "maint_delta": dict(zip(["inserts", "absorbed", "immediate_splits", "deferred_marks",
                                             "settled_splits", "split_ops", "host_over", "maint_fetches",
                                             "partitions_opened"], splits)),

@@ -224,7 +224,12 @@ KVC_API int kvc_host_kmeans(const float* pts, int32_t n, int32_t d, int32_t k, i
                             uint64_t seed, int32_t* assign, double* objective, int32_t* iterations);
 KVC_API double kvc_host_tau(int64_t n, double tau_min, double tau_max, double n0);
 KVC_API uint64_t kvc_host_mix_seed(uint64_t a, uint64_t b);
-/* Instrumentation: mean clock64 cycles per phase of the last resolve launch (out[8]). */
+/* Instrumentation: mean clock64 cycles per phase of the last resolve launch (out[16]; with
+ * out[0] < 0 on entry: of the last decode's score/select kernel, first 8 entries). */
+/* Device self-check of the reciprocal-based correctly rounded division used on the resolve
+ * chains against __ddiv_rn: n random (a, b) pairs, integer b in [1, max_den]; *mismatches
+ * receives the count of differing results. */
+KVC_API int kvc_debug_div_check(uint64_t n, uint64_t seed, int32_t max_den, uint64_t* mismatches);
 KVC_API int kvc_debug_resolve_profile(kvc_ctx* ctx, double* out);
 /* Enables per-phase CUDA-event timing (off by default: it adds event records). */
 KVC_API void kvc_set_timing(kvc_ctx* ctx, int32_t on);

@@ -145,6 +145,7 @@ def lib():
         L.kvc_set_timing.argtypes = [vp, C.c_int32]
         L.kvc_last_ingest_timing.argtypes = [vp, f64p]
         L.kvc_debug_resolve_profile.argtypes = [vp, f64p]
+        L.kvc_debug_div_check.argtypes = [C.c_uint64, C.c_uint64, C.c_int32, C.POINTER(C.c_uint64)]
         L.kvc_host_split_two.argtypes = [f32p, C.c_int32, C.c_int32, C.c_uint64, i32p, i32p]
         L.kvc_host_kmeans.argtypes = [f32p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_double,
                                       C.c_uint64, i32p, f64p, i32p]
@@ -166,7 +167,7 @@ EXPORTED = [
     "kvc_ledger_log_size", "kvc_ledger_op", "kvc_check", "kvc_offload", "kvc_fetch",
     "kvc_launch_count", "kvc_last_step_timing", "kvc_set_timing", "kvc_last_ingest_timing",
     "kvc_debug_resolve_profile", "kvc_host_split_two", "kvc_host_kmeans", "kvc_host_tau",
-    "kvc_host_mix_seed",
+    "kvc_host_mix_seed", "kvc_debug_div_check",
 ]
 
 
@@ -395,7 +396,7 @@ class ClusterKVCache:
         lib().kvc_set_timing(self.h, 1 if on else 0)
 
     def resolve_profile(self, decode=False):
-        t = np.zeros(8)
+        t = np.zeros(16)
         if decode:
             t[0] = -1.0
         lib().kvc_debug_resolve_profile(self.h, _p(t, f64p))
@@ -410,6 +411,14 @@ class ClusterKVCache:
         t = np.zeros(8)
         lib().kvc_last_step_timing(self.h, _p(t, f64p))
         return t
+
+
+# ----------------------------------------------------------------------------- device self-checks
+def debug_div_check(n: int, seed: int = 1, max_den: int = 1 << 20) -> int:
+    """Mismatches of the resolve chains' reciprocal division against __ddiv_rn (device)."""
+    m = C.c_uint64()
+    _check(lib().kvc_debug_div_check(n, seed, max_den, C.byref(m)))
+    return int(m.value)
 
 
 # ----------------------------------------------------------------------------- host slow path

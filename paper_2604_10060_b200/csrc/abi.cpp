@@ -338,6 +338,13 @@ int kvc_last_step_timing(kvc_ctx* ctx, double* t) {
 
 void kvc_set_timing(kvc_ctx* ctx, int32_t on) { ctx->impl->set_timing(on != 0); }
 
+int kvc_debug_div_check(uint64_t n, uint64_t seed, int32_t max_den, uint64_t* mismatches) {
+  int dev = 0;
+  if (cudaGetDeviceCount(&dev) != cudaSuccess || dev == 0) return KVC_E_NO_DEVICE;
+  *mismatches = kvc::debug_div_check(n, seed, max_den);
+  return *mismatches == ~0ull ? KVC_E_CUDA : KVC_OK;
+}
+
 int kvc_debug_resolve_profile(kvc_ctx* ctx, double* out) {
   ctx->impl->resolve_profile(out);
   return KVC_OK;

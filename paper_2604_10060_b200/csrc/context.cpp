@@ -10,6 +10,8 @@
 //   index.cpp:97-190      cluster registration, frame -> cluster map, buffers
 #include "context.hpp"
 
+#include <cstdlib>
+
 #include <algorithm>
 #include <chrono>
 #include <cmath>
@@ -214,8 +216,14 @@ void Context::alloc_device() {
   ia_.ev_page = static_cast<std::int32_t*>(dalloc(L * t_.tmax * 4));
   ia_.ev_row = static_cast<std::int32_t*>(dalloc(L * t_.tmax * 4));
   ia_.dom_pool = static_cast<std::int32_t*>(dalloc(L * POOL * 4));
-  ia_.prof = static_cast<long long*>(dalloc(L * 8 * 8));
+  ia_.prof = static_cast<long long*>(dalloc(L * 16 * 8));
   ia_.dom_pool_n = static_cast<std::int32_t*>(dalloc(L * 4));
+  ia_.rsnap = static_cast<double*>(dalloc(static_cast<std::int64_t>(L) * d * t_.tmax * 8));
+  ia_.bsnap = static_cast<double*>(dalloc(static_cast<std::int64_t>(L) * d * t_.tmax * 8));
+  {
+    const char* e = std::getenv("KVC_RESOLVE");  // "seq": the sequential resolve kernel
+    resolve_seq_ = e && std::string(e) == "seq";
+  }
   d_active_ = static_cast<std::int32_t*>(dalloc(L * 4 * 2));
   d_cursor_ = d_active_ + L;
   h_active_ = static_cast<std::int32_t*>(halloc(L * 4 * 2));
@@ -313,11 +321,14 @@ void Context::ensure_idx(std::int64_t n, std::int64_t runs) {
 }
 
 void Context::resolve_profile(double* out) {
-  std::vector<long long> p(static_cast<std::size_t>(L_) * 8);
-  KVC_CUDA(cudaMemcpy(p.data(), out[0] < 0 ? da_.k4prof : ia_.prof, p.size() * 8, cudaMemcpyDeviceToHost));
-  for (int k = 0; k < 8; ++k) {
+  const bool dec = out[0] < 0;
+  const int W = dec ? 8 : 16;  // K4: [L][8]; resolve: [L][16]
+  std::vector<long long> p(static_cast<std::size_t>(L_) * W);
+  KVC_CUDA(cudaMemcpy(p.data(), dec ? da_.k4prof : ia_.prof, p.size() * 8, cudaMemcpyDeviceToHost));
+  for (int k = 0; k < 16; ++k) {
     double s = 0.0;
-    for (int l = 0; l < L_; ++l) s += static_cast<double>(p[static_cast<std::size_t>(l) * 8 + k]);
+    if (k < W)
+      for (int l = 0; l < L_; ++l) s += static_cast<double>(p[static_cast<std::size_t>(l) * W + k]);
     out[k] = s / L_;
   }
 }
@@ -804,7 +815,10 @@ void Context::run_inserts(std::int64_t frame_id, std::int64_t pid, int T, std::i
       if (timing_) KVC_CUDA(cudaEventRecord(ev_[2], st_));
       launches_ += launch_topm(t_, ia_, st_);
       if (timing_) KVC_CUDA(cudaEventRecord(ev_[3], st_));
-      launches_ += launch_resolve(t_, ia_, st_);
+      {
+        const int n = resolve_seq_ ? 0 : launch_resolve_spec(t_, ia_, st_);
+        launches_ += n ? n : launch_resolve(t_, ia_, st_);
+      }
       if (timing_) KVC_CUDA(cudaEventRecord(ev_[4], st_));
       launches_ += launch_store_rows(t_, ia_, st_);
       if (timing_) KVC_CUDA(cudaEventRecord(ev_[5], st_));

@@ -234,6 +234,7 @@ class Context {
   float* d_out_ = nullptr;
   cudaEvent_t ev_[8];
   bool timing_ = false;
+  bool resolve_seq_ = false;  // KVC_RESOLVE=seq selects the sequential resolve kernel
   double step_t_[8] = {0};
   double ingest_t_[8] = {0};  // last frame: device us (cands, approx, topm, resolve, store), host us (wait, replay, rest)
   std::int64_t launches_ = 0;

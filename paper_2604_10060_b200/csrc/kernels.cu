@@ -907,7 +907,7 @@ __global__ void __launch_bounds__(32) k_resolve(DevTables t, IngestArgs a) {
     }
 #undef PROF
     if (lane == 0)
-      for (int k = 0; k < 8; ++k) a.prof[dom * 8 + k] = pr[k];
+      for (int k = 0; k < 8; ++k) a.prof[dom * 16 + k] = pr[k];
   }
 done:
   __syncwarp();

@@ -138,9 +138,13 @@ struct IngestArgs {
   int32_t* ev_row;         // [L][tmax]
   // per-domain reserve of free pages carried between resolve launches (no pushes to the
   // shared free stack while pops may run concurrently)
-  long long* prof;         // [L][8] clock64 cycles per resolve phase (instrumentation)
+  long long* prof;         // [L][16] clock64 cycles per resolve phase (instrumentation)
   int32_t* dom_pool;       // [L][POOL]
   int32_t* dom_pool_n;     // [L]
+  // speculative resolve (resolve_spec.cu): per-token state snapshots, column-major so that
+  // one thread per token reads them coalesced
+  double* rsnap;           // [L][d][tmax] representative after each token's insert
+  double* bsnap;           // [L][d][tmax] buffer mean after each buffer-moving insert
 };
 constexpr int TOPM = 8;
 constexpr int POOL = 16;
@@ -184,6 +188,11 @@ struct DecodeArgs {
 int launch_build_cands(const DevTables& t, const IngestArgs& a, cudaStream_t st);
 int launch_approx(const DevTables& t, const IngestArgs& a, cudaStream_t st);
 int launch_resolve(const DevTables& t, const IngestArgs& a, cudaStream_t st);
+// Speculate-and-verify resolve (resolve_spec.cu). Returns 0 (nothing launched) when the
+// shape does not fit its shared-memory plan; the caller then uses launch_resolve.
+int launch_resolve_spec(const DevTables& t, const IngestArgs& a, cudaStream_t st);
+// Counts div_rcp != __ddiv_rn over n random operands on the device (~0 on CUDA failure).
+uint64_t debug_div_check(uint64_t n, uint64_t seed, int max_den);
 int launch_topm(const DevTables& t, const IngestArgs& a, cudaStream_t st);
 int launch_store_rows(const DevTables& t, const IngestArgs& a, cudaStream_t st);
 int launch_ring_write(const DevTables& t, const void* fk, const void* fv, int32_t T,

@@ -15,6 +15,16 @@ pytestmark = pytest.mark.gpu
 ATT_TOL = 1e-3
 
 
+@pytest.fixture(params=["spec", "seq"])
+def resolve_mode(request, monkeypatch):
+    """Both device resolve kernels: speculate-and-verify (default) and the sequential one."""
+    if request.param == "seq":
+        monkeypatch.setenv("KVC_RESOLVE", "seq")
+    else:
+        monkeypatch.delenv("KVC_RESOLVE", raising=False)
+    return request.param
+
+
 @pytest.fixture(scope="module")
 def stream1():
     return po.gen_stream_restated(po.config1_stream())
@@ -27,7 +37,7 @@ def _run(stream, ecfg, ref_lib_present=True, dev_kw=None, check_attention=True, 
     return r
 
 
-def test_config1_full_stream(stream1, ref_lib):
+def test_config1_full_stream(stream1, ref_lib, resolve_mode):
     """64 frames (16 build + 48 online with ~360 splits) and 32 queries, top-4."""
     r = _run(stream1, po.config1_engine())
     assert r.mismatches == [], r.mismatches[:5]
@@ -98,7 +108,7 @@ def test_flat_topk_matches_reference(stream1, ref_lib):
     assert r.mismatches == []
 
 
-def test_eager_policy(ref_lib):
+def test_eager_policy(ref_lib, resolve_mode):
     """defer_host_splits = false: eager fetch + split, domains resolved one at a time."""
     s = po.gen_stream_restated(po.StreamCfg.make(n_scenes=3, frames_per_scene=12, tokens_per_frame=32,
                                                  d=32, L=3, n_queries=6, semantic_noise=0.05, seed=5))
@@ -108,7 +118,7 @@ def test_eager_policy(ref_lib):
     assert r.att_err < ATT_TOL
 
 
-def test_deferred_and_prefetch_drift(ref_lib):
+def test_deferred_and_prefetch_drift(ref_lib, resolve_mode):
     """Drift preset (workload.cpp:337-346) scaled down: deferred splits, buffers, settles, prefetch."""
     s = po.gen_stream_restated(po.StreamCfg.make(n_scenes=6, frames_per_scene=16, tokens_per_frame=16,
                                                  d=32, L=4, scene_cycle=2, drift_rate=0.06,
