@@ -229,6 +229,14 @@ KVC_API uint64_t kvc_host_mix_seed(uint64_t a, uint64_t b);
 /* Device self-check of the reciprocal-based correctly rounded division used on the resolve
  * chains against __ddiv_rn: n random (a, b) pairs, integer b in [1, max_den]; *mismatches
  * receives the count of differing results. */
+/* Device self-check of the frame-ingest distance tile: runs the candidate build and the distance
+ * tile (tensor-core or SIMT, whichever the context uses) + top-M for a frame keys[L][T][d] (kv
+ * dtype, host or device) against `partition` without inserting anything, then compares every
+ * (token, candidate) approximate cosine with the exact fp64 cosine. out4: max |approx - exact|,
+ * candidates outside a top-M list scoring above its (M+1)-th value, top-M exact values that differ
+ * from a fresh exact cosine, and the margin the resolve kernels certify with. */
+KVC_API int kvc_debug_assign_check(kvc_ctx* ctx, const void* keys, int32_t T, int64_t partition, int32_t mem,
+                                   double* out4);
 KVC_API int kvc_debug_div_check(uint64_t n, uint64_t seed, int32_t max_den, uint64_t* mismatches);
 KVC_API int kvc_debug_resolve_profile(kvc_ctx* ctx, double* out);
 /* Enables per-phase CUDA-event timing (off by default: it adds event records). */

@@ -145,6 +145,7 @@ def lib():
         L.kvc_set_timing.argtypes = [vp, C.c_int32]
         L.kvc_last_ingest_timing.argtypes = [vp, f64p]
         L.kvc_debug_resolve_profile.argtypes = [vp, f64p]
+        L.kvc_debug_assign_check.argtypes = [vp, vp, C.c_int32, C.c_int64, C.c_int32, f64p]
         L.kvc_debug_div_check.argtypes = [C.c_uint64, C.c_uint64, C.c_int32, C.POINTER(C.c_uint64)]
         L.kvc_host_split_two.argtypes = [f32p, C.c_int32, C.c_int32, C.c_uint64, i32p, i32p]
         L.kvc_host_kmeans.argtypes = [f32p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_double,
@@ -167,7 +168,7 @@ EXPORTED = [
     "kvc_ledger_log_size", "kvc_ledger_op", "kvc_check", "kvc_offload", "kvc_fetch",
     "kvc_launch_count", "kvc_last_step_timing", "kvc_set_timing", "kvc_last_ingest_timing",
     "kvc_debug_resolve_profile", "kvc_host_split_two", "kvc_host_kmeans", "kvc_host_tau",
-    "kvc_host_mix_seed", "kvc_debug_div_check",
+    "kvc_host_mix_seed", "kvc_debug_div_check", "kvc_debug_assign_check",
 ]
 
 
@@ -401,6 +402,14 @@ class ClusterKVCache:
             t[0] = -1.0
         lib().kvc_debug_resolve_profile(self.h, _p(t, f64p))
         return t
+
+    def assign_check(self, keys, partition: int = 0):
+        """Distance-tile self-check on a frame keys [L, T, d] (see kvc_debug_assign_check):
+        (max |approx - exact|, top-M violations, top-M exact mismatches, certified margin)."""
+        kp, mem = _ptr(keys)
+        out = np.zeros(4)
+        _check(lib().kvc_debug_assign_check(self.h, kp, int(keys.shape[1]), partition, mem, _p(out, f64p)))
+        return float(out[0]), int(out[1]), int(out[2]), float(out[3])
 
     def ingest_timing(self):
         t = np.zeros(8)

@@ -338,6 +338,11 @@ int kvc_last_step_timing(kvc_ctx* ctx, double* t) {
 
 void kvc_set_timing(kvc_ctx* ctx, int32_t on) { ctx->impl->set_timing(on != 0); }
 
+int kvc_debug_assign_check(kvc_ctx* ctx, const void* keys, int32_t T, int64_t partition, int32_t mem,
+                           double* out4) {
+  return guard([&] { F(ctx).debug_assign_check(keys, T, partition, mem, out4); });
+}
+
 int kvc_debug_div_check(uint64_t n, uint64_t seed, int32_t max_den, uint64_t* mismatches) {
   int dev = 0;
   if (cudaGetDeviceCount(&dev) != cudaSuccess || dev == 0) return KVC_E_NO_DEVICE;

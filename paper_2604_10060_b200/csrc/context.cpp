@@ -223,6 +223,9 @@ void Context::alloc_device() {
   {
     const char* e = std::getenv("KVC_RESOLVE");  // "seq": the sequential resolve kernel
     resolve_seq_ = e && std::string(e) == "seq";
+    const char* g = std::getenv("KVC_ASSIGN");  // "simt": the fp32 CUDA-core tile
+    assign_tc_ = !(g && std::string(g) == "simt") && assign_tc_supported(t_) &&
+                 make_key_tensor_map(key_map_, d_fk_, d, t_.tmax, L);
   }
   d_active_ = static_cast<std::int32_t*>(dalloc(L * 4 * 2));
   d_cursor_ = d_active_ + L;
@@ -318,6 +321,48 @@ void Context::ensure_idx(std::int64_t n, std::int64_t runs) {
     d_runs_ = static_cast<AppendRun*>(dalloc(runs_cap_ * sizeof(AppendRun)));
     h_runs_ = static_cast<AppendRun*>(halloc(runs_cap_ * sizeof(AppendRun)));
   }
+}
+
+void Context::debug_assign_check(const void* keys, int T, std::int64_t pid, int mem, double* out) {
+  if (T < 1 || T > t_.tmax) fail(-10, "tokens per frame outside [1, max_tokens]");
+  if (pid < 0 || pid >= static_cast<std::int64_t>(parts_.size())) fail(-3, "unknown partition");
+  flush_pending();
+  const std::size_t row = static_cast<std::size_t>(T) * d_ * es_;
+  const std::size_t pitch = static_cast<std::size_t>(t_.tmax) * d_ * es_;
+  const cudaMemcpyKind kind = mem == KVC_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  KVC_CUDA(cudaMemcpy2DAsync(d_fk_, pitch, keys, row, row, L_, kind, st_));
+  flush_resid();
+  ia_.T = T;
+  ia_.pid = static_cast<std::int32_t>(pid);
+  ia_.n_active = L_;
+  for (int l = 0; l < L_; ++l) {
+    h_active_[l] = l;
+    h_cursor_[l] = 0;
+  }
+  KVC_CUDA(cudaMemcpyAsync(d_active_, h_active_, L_ * 8, cudaMemcpyHostToDevice, st_));
+  launches_ += launch_build_cands(t_, ia_, st_);
+  if (assign_tc_) {
+    ia_.margin = kTcMargin;
+    launches_ += launch_assign_tc(t_, ia_, key_map_, st_);
+  } else {
+    ia_.margin = kSimtMargin;
+    launches_ += launch_approx(t_, ia_, st_);
+    launches_ += launch_topm(t_, ia_, st_);
+  }
+  if (!d_check_) d_check_ = dalloc(64);
+  unsigned long long* dres = static_cast<unsigned long long*>(d_check_);
+  KVC_CUDA(cudaMemsetAsync(dres, 0, 24, st_));
+  launches_ += launch_assign_err(t_, ia_, dres, st_);
+  unsigned long long h[3];
+  KVC_CUDA(cudaMemcpyAsync(h, dres, 24, cudaMemcpyDeviceToHost, st_));
+  sync();
+  check_dev_err();
+  double e;
+  std::memcpy(&e, &h[0], 8);
+  out[0] = e;
+  out[1] = static_cast<double>(h[1]);
+  out[2] = static_cast<double>(h[2]);
+  out[3] = ia_.margin;
 }
 
 void Context::resolve_profile(double* out) {
@@ -794,7 +839,6 @@ void Context::run_inserts(std::int64_t frame_id, std::int64_t pid, int T, std::i
   ia_.T = T;
   ia_.pid = static_cast<std::int32_t>(pid);
   ia_.ring_slot = ring_slot;
-  ia_.margin = 1e-4f;
   double t_wait = 0.0, t_replay = 0.0, t_launch = 0.0;
   for (double& x : ingest_t_) x = 0.0;
   const auto r0 = std::chrono::steady_clock::now();
@@ -811,9 +855,16 @@ void Context::run_inserts(std::int64_t frame_id, std::int64_t pid, int T, std::i
       if (timing_) KVC_CUDA(cudaEventRecord(ev_[0], st_));
       launches_ += launch_build_cands(t_, ia_, st_);
       if (timing_) KVC_CUDA(cudaEventRecord(ev_[1], st_));
-      launches_ += launch_approx(t_, ia_, st_);
-      if (timing_) KVC_CUDA(cudaEventRecord(ev_[2], st_));
-      launches_ += launch_topm(t_, ia_, st_);
+      if (assign_tc_) {
+        ia_.margin = kTcMargin;
+        launches_ += launch_assign_tc(t_, ia_, key_map_, st_);
+        if (timing_) KVC_CUDA(cudaEventRecord(ev_[2], st_));
+      } else {
+        ia_.margin = kSimtMargin;
+        launches_ += launch_approx(t_, ia_, st_);
+        if (timing_) KVC_CUDA(cudaEventRecord(ev_[2], st_));
+        launches_ += launch_topm(t_, ia_, st_);
+      }
       if (timing_) KVC_CUDA(cudaEventRecord(ev_[3], st_));
       {
         const int n = resolve_seq_ ? 0 : launch_resolve_spec(t_, ia_, st_);

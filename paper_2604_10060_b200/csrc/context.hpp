@@ -181,6 +181,10 @@ class Context {
   void set_timing(bool on) { timing_ = on; }
   const double* step_timing() const { return step_t_; }
   const double* ingest_timing() const { return ingest_t_; }
+  // Runs the candidate build + distance tile (+ top-M) on a frame for partition `pid` without
+  // resolving, then checks it against exact cosines. out: max |approx - exact|, top-M
+  // violations, exact mismatches, the margin the resolve kernels assume.
+  void debug_assign_check(const void* keys, int T, std::int64_t pid, int mem, double* out);
   void resolve_profile(double* out);  // mean clock64 cycles per resolve phase over domains
 
  private:
@@ -235,6 +239,9 @@ class Context {
   cudaEvent_t ev_[8];
   bool timing_ = false;
   bool resolve_seq_ = false;  // KVC_RESOLVE=seq selects the sequential resolve kernel
+  bool assign_tc_ = false;    // tensor-core distance tile (KVC_ASSIGN=simt disables)
+  alignas(64) unsigned char key_map_[128];  // CUtensorMap over the frame keys
+  void* d_check_ = nullptr;                 // debug_assign_check result words
   double step_t_[8] = {0};
   double ingest_t_[8] = {0};  // last frame: device us (cands, approx, topm, resolve, store), host us (wait, replay, rest)
   std::int64_t launches_ = 0;

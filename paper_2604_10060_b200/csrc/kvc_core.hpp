@@ -191,6 +191,15 @@ int launch_resolve(const DevTables& t, const IngestArgs& a, cudaStream_t st);
 // Speculate-and-verify resolve (resolve_spec.cu). Returns 0 (nothing launched) when the
 // shape does not fit its shared-memory plan; the caller then uses launch_resolve.
 int launch_resolve_spec(const DevTables& t, const IngestArgs& a, cudaStream_t st);
+// Tensor-core distance tile + top-M (assign_tc.cu) for bf16 frames with d in {64, 128}: replaces
+// launch_approx + launch_topm. key_map: a CUtensorMap over the frame keys [L][tmax][d] made by
+// make_key_tensor_map (128-byte swizzle, 64 x 128 boxes).
+bool assign_tc_supported(const DevTables& t);
+bool make_key_tensor_map(void* map, const void* keys, int d, int tmax, int L);
+int launch_assign_tc(const DevTables& t, const IngestArgs& a, const void* key_map, cudaStream_t st);
+int launch_assign_err(const DevTables& t, const IngestArgs& a, unsigned long long* out, cudaStream_t st);
+constexpr float kSimtMargin = 1e-4f;  // |approx - exact| bound of the fp32 SIMT tile
+constexpr float kTcMargin = 2e-4f;    // ... of the bf16 hi/lo tensor-core tile
 // Counts div_rcp != __ddiv_rn over n random operands on the device (~0 on CUDA failure).
 uint64_t debug_div_check(uint64_t n, uint64_t seed, int max_den);
 int launch_topm(const DevTables& t, const IngestArgs& a, cudaStream_t st);
