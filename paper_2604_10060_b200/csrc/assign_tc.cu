@@ -90,10 +90,27 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
   for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
 }
 
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&v)[8]) {
+  uint32_t r[8];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int j = 0; j < 8; ++j) v[j] = __uint_as_float(r[j]);
+}
+
 __host__ __device__ inline size_t tc_smem_bytes(int d) {
   const size_t kh = static_cast<size_t>(d / KB);
   return 1024 /*align slack*/ + 2 * kh * 128 * 128 /*A*/ + 2 * kh * NCH * 128 /*B hi, lo*/ +
-         NCH * 4 /*inv norms*/ + 64 /*barriers*/;
+         NCH * 4 /*inv norms*/ + NCH * 8 /*candidate rows*/ + 64 /*barriers*/;
+}
+
+// Element i of token row r of a swizzled [128 rows][128 B] key tile (kh = i / 64 selects the tile).
+__device__ __forceinline__ uint32_t a_word(const uint8_t* tile0, int KH, int r, int i) {
+  const int kh = i / KB, byte = (i % KB) * 2;
+  const uint8_t* p = tile0 + kh * 128 * 128 + r * 128 + ((((byte >> 4) ^ (r & 7)) << 4) | (byte & 15));
+  return *reinterpret_cast<const uint32_t*>(p);  // elements i, i+1 (i even)
 }
 
 __global__ void __launch_bounds__(AS_THREADS, 1) k_assign_tc(DevTables t, IngestArgs a,
@@ -105,7 +122,8 @@ __global__ void __launch_bounds__(AS_THREADS, 1) k_assign_tc(DevTables t, Ingest
   uint8_t* sBh = sA + 2 * KH * 128 * 128;           // [KH][NCH rows][128 B]
   uint8_t* sBl = sBh + KH * NCH * 128;
   float* inr = reinterpret_cast<float*>(sBl + KH * NCH * 128);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(inr + NCH);  // [0] keys loaded, [1] mma done
+  const float** crow = reinterpret_cast<const float**>(inr + NCH);  // candidate fp32 rows of the chunk
+  uint64_t* bars = reinterpret_cast<uint64_t*>(crow + NCH);  // [0] keys loaded, [1] mma done
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -133,26 +151,13 @@ __global__ void __launch_bounds__(AS_THREADS, 1) k_assign_tc(DevTables t, Ingest
       for (int kh = 0; kh < KH; ++kh) tma_load_3d(sA + (mt * KH + kh) * 128 * 128, &tmk, kh * KB, mt * 128, dom, &bars[0]);
   }
 
-  // this thread's token and its approximate 1/|k| (fp32)
+  // this thread's token (row of the TMA-loaded key tile)
   const int mt = warp >> 2;
-  const int m = mt * 128 + (warp & 3) * 32 + lane;
+  const int mr = (warp & 3) * 32 + lane;
+  const int m = mt * 128 + mr;
   const bool tok_ok = m < T && mt < mtiles;
-  const uint16_t* krow = static_cast<const uint16_t*>(a.fk) + (static_cast<int64_t>(dom) * t.tmax + m) * d;
+  const uint8_t* atile = sA + mt * KH * 128 * 128;
   float ink = 0.f;
-  if (tok_ok) {
-    float s = 0.f;
-    for (int i = 0; i < d; i += 8) {
-      const uint4 w = *reinterpret_cast<const uint4*>(krow + i);
-      const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-      for (int h = 0; h < 4; ++h) {
-        const float lo = __uint_as_float(ww[h] << 16), hi = __uint_as_float(ww[h] & 0xffff0000u);
-        s = fmaf(lo, lo, s);
-        s = fmaf(hi, hi, s);
-      }
-    }
-    ink = s > 0.f ? rsqrtf(s) : 0.f;
-  }
   float tv[TOPM + 1];
   int ti[TOPM + 1];
 #pragma unroll
@@ -167,42 +172,68 @@ __global__ void __launch_bounds__(AS_THREADS, 1) k_assign_tc(DevTables t, Ingest
   uint32_t phase = 0;
   for (int c0 = 0; c0 < n; c0 += NCH) {
     const int nc = min(NCH, n - c0);
-    // B: representatives as bf16 hi / lo, swizzled K-major rows (zero rows past nc)
-    const int q4 = d / 4;
-    for (int idx = tid; idx < NCH * q4; idx += AS_THREADS) {
-      const int r = idx / q4, q = idx - r * q4;
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (r < nc) {
-        const int s = cs[c0 + r];
-        const float* src = (cbuf[c0 + r] ? t.brep32 : t.rep32) + static_cast<int64_t>(s) * d;
-        v = *reinterpret_cast<const float4*>(src + 4 * q);
-      }
-      const __nv_bfloat162 h01 = __floats2bfloat162_rn(v.x, v.y), h23 = __floats2bfloat162_rn(v.z, v.w);
-      const float2 f01 = __bfloat1622float2(h01), f23 = __bfloat1622float2(h23);
-      const __nv_bfloat162 l01 = __floats2bfloat162_rn(v.x - f01.x, v.y - f01.y);
-      const __nv_bfloat162 l23 = __floats2bfloat162_rn(v.z - f23.x, v.w - f23.y);
-      const int e = 4 * q, kh = e / KB, byte = (e % KB) * 2;
-      const int off = kh * NCH * 128 + r * 128 + ((((byte >> 4) ^ (r & 7)) << 4) | (byte & 15));
-      uint2 hv, lv;
-      hv.x = *reinterpret_cast<const uint32_t*>(&h01);
-      hv.y = *reinterpret_cast<const uint32_t*>(&h23);
-      lv.x = *reinterpret_cast<const uint32_t*>(&l01);
-      lv.y = *reinterpret_cast<const uint32_t*>(&l23);
-      *reinterpret_cast<uint2*>(sBh + off) = hv;
-      *reinterpret_cast<uint2*>(sBl + off) = lv;
-    }
+    // B: representatives as bf16 hi / lo, swizzled K-major rows (zero rows past nc). Row
+    // pointers first, then each warp streams whole rows (coalesced), RB rows in flight.
     for (int r = tid; r < NCH; r += AS_THREADS) {
       float nr = 0.f;
+      const float* src = nullptr;
       if (r < nc) {
         const int s = cs[c0 + r];
-        nr = static_cast<float>(cbuf[c0 + r] ? t.bnorm[s] : t.rnorm[s]);
+        const bool ib = cbuf[c0 + r];
+        src = (ib ? t.brep32 : t.rep32) + static_cast<int64_t>(s) * d;
+        nr = static_cast<float>(ib ? t.bnorm[s] : t.rnorm[s]);
       }
+      crow[r] = src;
       inr[r] = nr > 0.f ? 1.f / nr : 0.f;
+    }
+    __syncthreads();
+    {
+      constexpr int RB = 8;
+      const int q4 = d / 4;  // float4 per row (<= 32: one per lane)
+      for (int r0 = warp * RB; r0 < NCH; r0 += 8 * RB) {
+        float4 v[RB];
+#pragma unroll
+        for (int k = 0; k < RB; ++k) {
+          const float* src = crow[r0 + k];
+          v[k] = (src && lane < q4) ? __ldg(reinterpret_cast<const float4*>(src) + lane) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int k = 0; k < RB; ++k) {
+          if (lane < q4) {
+            const int r = r0 + k;
+            const __nv_bfloat162 h01 = __floats2bfloat162_rn(v[k].x, v[k].y), h23 = __floats2bfloat162_rn(v[k].z, v[k].w);
+            const float2 f01 = __bfloat1622float2(h01), f23 = __bfloat1622float2(h23);
+            const __nv_bfloat162 l01 = __floats2bfloat162_rn(v[k].x - f01.x, v[k].y - f01.y);
+            const __nv_bfloat162 l23 = __floats2bfloat162_rn(v[k].z - f23.x, v[k].w - f23.y);
+            const int e = 4 * lane, kh = e / KB, byte = (e % KB) * 2;
+            const int off = kh * NCH * 128 + r * 128 + ((((byte >> 4) ^ (r & 7)) << 4) | (byte & 15));
+            uint2 hv, lv;
+            hv.x = *reinterpret_cast<const uint32_t*>(&h01);
+            hv.y = *reinterpret_cast<const uint32_t*>(&h23);
+            lv.x = *reinterpret_cast<const uint32_t*>(&l01);
+            lv.y = *reinterpret_cast<const uint32_t*>(&l23);
+            *reinterpret_cast<uint2*>(sBh + off) = hv;
+            *reinterpret_cast<uint2*>(sBl + off) = lv;
+          }
+        }
+      }
+    }
+    if (c0 == 0) {  // 1/|k| (fp32) from the TMA-loaded key tile
+      mbar_wait(&bars[0], 0);
+      if (tok_ok) {
+        float s2 = 0.f;
+        for (int i = 0; i < d; i += 2) {
+          const uint32_t w = a_word(atile, KH, mr, i);
+          const float lo = __uint_as_float(w << 16), hi = __uint_as_float(w & 0xffff0000u);
+          s2 = fmaf(lo, lo, s2);
+          s2 = fmaf(hi, hi, s2);
+        }
+        ink = s2 > 0.f ? rsqrtf(s2) : 0.f;
+      }
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();
     if (tid == 0) {
-      if (c0 == 0) mbar_wait(&bars[0], 0);
       tc_fence_after();
       for (int t2 = 0; t2 < mtiles; ++t2) {
         const uint32_t dcol = tmem + static_cast<uint32_t>(t2 * NCH);
@@ -225,29 +256,35 @@ __global__ void __launch_bounds__(AS_THREADS, 1) k_assign_tc(DevTables t, Ingest
     tc_fence_after();
     if (mt < mtiles) {
       const uint32_t tbase = tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16) + static_cast<uint32_t>(mt * NCH);
-      for (int cb = 0; cb < nc; cb += 32) {
-        float v[32];
-        tmem_ld32(tbase + static_cast<uint32_t>(cb), v);  // warp-collective
+#pragma unroll 1
+      for (int cb = 0; cb < nc; cb += 8) {  // 8 columns per tcgen05.ld keeps the loop body small
+        float v[8];
+        tmem_ld8(tbase + static_cast<uint32_t>(cb), v);  // warp-collective
         if (tok_ok) {
+          const float sc = ink;
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const int c = c0 + cb + j;
-            if (cb + j < nc) {
-              const float x = v[j] * ink * inr[cb + j];
-              arow[c] = x;
-              if (x > tv[TOPM]) {  // insertion keeps (value desc, index asc)
-                tv[TOPM] = x;
-                ti[TOPM] = c;
+          for (int j = 0; j < 8; ++j) v[j] *= sc * inr[cb + j];
+          if (cb + 8 <= nc) {
+            *reinterpret_cast<float4*>(arow + c0 + cb) = make_float4(v[0], v[1], v[2], v[3]);
+            *reinterpret_cast<float4*>(arow + c0 + cb + 4) = make_float4(v[4], v[5], v[6], v[7]);
+          } else {
+            for (int j = 0; j < nc - cb; ++j) arow[c0 + cb + j] = v[j];
+          }
 #pragma unroll
-                for (int k = TOPM; k > 0; --k)
-                  if (tv[k] > tv[k - 1]) {
-                    const float fv = tv[k];
-                    tv[k] = tv[k - 1];
-                    tv[k - 1] = fv;
-                    const int fi = ti[k];
-                    ti[k] = ti[k - 1];
-                    ti[k - 1] = fi;
-                  }
+          for (int j = 0; j < 8; ++j) {
+            const float x = v[j];
+            if (cb + j < nc && x > tv[TOPM]) {  // insertion keeps (value desc, index asc)
+              tv[TOPM] = x;
+              ti[TOPM] = c0 + cb + j;
+#pragma unroll
+              for (int k = TOPM; k > 0; --k) {
+                const bool sw = tv[k] > tv[k - 1];
+                const float fa = tv[k], fb = tv[k - 1];
+                const int ia = ti[k], ib = ti[k - 1];
+                tv[k] = sw ? fb : fa;
+                tv[k - 1] = sw ? fa : fb;
+                ti[k] = sw ? ib : ia;
+                ti[k - 1] = sw ? ia : ib;
               }
             }
           }
@@ -258,46 +295,51 @@ __global__ void __launch_bounds__(AS_THREADS, 1) k_assign_tc(DevTables t, Ingest
     __syncthreads();
   }
 
-  // exact fp64 cosines of the top-M against the launch-time representatives + |k|
+  // Exact fp64 cosines (vecmath.hpp:53-63) of the top-M entries that can decide the token's
+  // arg-best: those within 2 margins of the best approximate score (the others are NaN = "not
+  // computed"; the resolve kernels bound them by approx + margin instead). Keys come from the
+  // key tile in shared memory.
   if (tok_ok) {
     const int64_t o = static_cast<int64_t>(dom) * t.tmax + m;
+    const float cut = tv[0] - 2.f * a.margin;
     const double* rp[TOPM];
     double nr[TOPM];
 #pragma unroll
     for (int k = 0; k < TOPM; ++k) {
       const int c = ti[k];
-      if (c >= 0) {
+      rp[k] = nullptr;
+      nr[k] = 1.0;
+      if (c >= 0 && tv[k] >= cut) {
         const int s = cs[c];
         const bool ib = cbuf[c];
         rp[k] = (ib ? t.brep64 : t.rep64) + static_cast<int64_t>(s) * d;
         nr[k] = ib ? t.bnorm[s] : t.rnorm[s];
-      } else {
-        rp[k] = nullptr;
-        nr[k] = 1.0;
       }
     }
     double acc[TOPM];
 #pragma unroll
     for (int k = 0; k < TOPM; ++k) acc[k] = 0.0;
     double sk = 0.0;
-    for (int i = 0; i < d; i += 8) {
-      const uint4 w = *reinterpret_cast<const uint4*>(krow + i);
-      const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+    for (int i = 0; i < d; i += 2) {
+      const uint32_t w = a_word(atile, KH, mr, i);
+      const double x0 = static_cast<double>(__uint_as_float(w << 16));
+      const double x1 = static_cast<double>(__uint_as_float(w & 0xffff0000u));
+      sk = dadd(sk, dmul(x0, x0));
+      sk = dadd(sk, dmul(x1, x1));
 #pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        const double x = static_cast<double>(__uint_as_float((e & 1) ? (ww[e >> 1] & 0xffff0000u) : (ww[e >> 1] << 16)));
-        sk = dadd(sk, dmul(x, x));
-#pragma unroll
-        for (int k = 0; k < TOPM; ++k)
-          if (rp[k]) acc[k] = dadd(acc[k], dmul(x, __ldg(rp[k] + i + e)));
-      }
+      for (int k = 0; k < TOPM; ++k)
+        if (rp[k]) {
+          const double2 r2 = __ldg(reinterpret_cast<const double2*>(rp[k] + i));
+          acc[k] = dadd(acc[k], dmul(x0, r2.x));
+          acc[k] = dadd(acc[k], dmul(x1, r2.y));
+        }
     }
     const double nk = __dsqrt_rn(sk);
 #pragma unroll
     for (int k = 0; k < TOPM; ++k) {
       a.topm_idx[o * TOPM + k] = static_cast<int16_t>(ti[k]);
       a.topm_val[o * TOPM + k] = ti[k] >= 0 ? tv[k] : -INFINITY;
-      a.topm_exact[o * TOPM + k] = ti[k] >= 0 ? clamp1(ddiv(acc[k], dmul(nk, nr[k]))) : -3.0;
+      a.topm_exact[o * TOPM + k] = ti[k] < 0 ? -3.0 : (rp[k] ? clamp1(ddiv(acc[k], dmul(nk, nr[k]))) : NAN);
     }
     a.topm_next[o] = ti[TOPM] >= 0 ? tv[TOPM] : -INFINITY;
   }
@@ -337,7 +379,9 @@ __global__ void k_assign_err(DevTables t, IngestArgs a, unsigned long long* out)
       for (int j = 0; j < TOPM; ++j)
         if (a.topm_idx[o * TOPM + j] == c) k = j;
       if (k < 0 && ap > tnext) atomicAdd(&out[1], 1ull);
-      if (k >= 0 && a.topm_exact[o * TOPM + k] != ex) atomicAdd(&out[2], 1ull);
+      const double tx = k >= 0 ? a.topm_exact[o * TOPM + k] : 0.0;  // NaN: not computed (far below the best)
+      if (k >= 0 && !isnan(tx) && tx != ex) atomicAdd(&out[2], 1ull);
+      if (k >= 0 && isnan(tx) && ap >= a.topm_val[o * TOPM] - 2.0 * a.margin) atomicAdd(&out[2], 1ull);
     }
   }
 }

@@ -607,8 +607,17 @@ __global__ void __launch_bounds__(32) k_resolve(DevTables t, IngestArgs a) {
       if (complete) {
         if (lane < TOPM) {
           const int c = ti[lane];
-          if (c >= 0 && !touched[c] && cslot[c] != w_slot && tm_val[tn * TOPM + lane] >= thr)
-            add(c, EV_PRE, 0, 0, nullptr, 0.0, ckey[c], tm_exact[tn * TOPM + lane]);
+          if (c >= 0 && !touched[c] && cslot[c] != w_slot && tm_val[tn * TOPM + lane] >= thr) {
+            const double ex = tm_exact[tn * TOPM + lane];
+            if (isnan(ex)) {  // not computed by the tile kernel: exact from the representative
+              const int s = cslot[c];
+              const bool ib = cbuf[c];
+              add(c, EV_SLOW, 0, 0, (ib ? t.brep64 : t.rep64) + static_cast<int64_t>(s) * d,
+                  ib ? t.bnorm[s] : t.rnorm[s], ckey[c], 0.0);
+            } else {
+              add(c, EV_PRE, 0, 0, nullptr, 0.0, ckey[c], ex);
+            }
+          }
         }
       } else {  // rare: scan the whole approximate row
         for (int c = lane; c < n; c += 32) {

@@ -861,7 +861,8 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve_spec(DevTables t, Ing
         const bool w_alive = alive(w, u);
         const bool w_touched = w_alive && first_change(w) < u;
         double exw = 0.0;
-        const bool inw = w < nl && in_topm(w, exw);
+        // top-M entries far below the best carry NaN (exact not computed by the tile kernel)
+        const bool inw = w < nl && in_topm(w, exw) && !isnan(exw);
         bool wknown = w_alive && !w_touched && inw;
         double lowW;
         if (!w_alive) {
@@ -896,7 +897,7 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve_spec(DevTables t, Ing
           bool have = false;
           if (c < nl) {
             double ex;
-            const bool in = in_topm(c, ex);
+            const bool in = in_topm(c, ex) && !isnan(ex);
             if (!touched && in) {  // untouched, exact launch-time value known
               if (ex < lowW) return;
               v = ex;
