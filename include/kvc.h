@@ -125,7 +125,11 @@ KVC_API int kvc_ingest_frame(kvc_ctx* ctx, int64_t frame_id, const float* visual
  * selected clusters U the local window; no reference counterpart):
  * out[l] = sum_t softmax(q_l . k_t / sqrt(d)) v_t, fp32.
  * q: [L][d] f32 (`q_mem`); out: [L][d] f32 (`out_mem`), may be NULL. gt: ground-truth frames
- * for recall (host, may be NULL). */
+ * for recall (host, may be NULL).
+ * Asynchronous with device buffers: the call returns once the step is enqueued on kvc_stream();
+ * a device `out` is valid in that stream's order and a device `q` must stay valid until then.
+ * Host `out` is complete on return. The step's bookkeeping (the views below, ledger, stats) is
+ * replayed while the next step runs, or on first read. */
 KVC_API int kvc_decode_step(kvc_ctx* ctx, int64_t query_id, const float* q, int32_t q_mem, float* out,
                     int32_t out_mem, const int64_t* gt, int32_t n_gt);
 

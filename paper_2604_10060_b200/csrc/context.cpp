@@ -89,6 +89,11 @@ Context::~Context() {
   for (void* p : dev_allocs_) cudaFree(p);
   for (void* p : host_allocs_) cudaFreeHost(p);
   for (auto& e : ev_) cudaEventDestroy(e);
+  for (auto& e : ev_step_)
+    if (e) cudaEventDestroy(e);
+  for (auto& row : evb_)
+    for (auto& e : row)
+      if (e) cudaEventDestroy(e);
   if (st_) cudaStreamDestroy(st_);
 }
 
@@ -257,8 +262,12 @@ void Context::alloc_device() {
                     o_nv = carve(L * 4), o_att = carve(L * 8), o_nc = carve(L * 4), o_fl = carve(16);
   dec_bytes_ = off;
   d_dec_ = dalloc(dec_bytes_);
-  h_dec_ = halloc(dec_bytes_);
-  h_dec2_ = halloc(dec_bytes_);
+  for (int b = 0; b < 2; ++b) {
+    h_blk_[b] = halloc(dec_bytes_);
+    h_blk_err_[b] = static_cast<std::int32_t*>(halloc(16));
+    KVC_CUDA(cudaEventCreateWithFlags(&ev_step_[b], cudaEventDisableTiming));
+    for (auto& e : evb_[b]) KVC_CUDA(cudaEventCreate(&e));
+  }
   auto* base = static_cast<std::uint8_t*>(d_dec_);
   da_.parts = reinterpret_cast<std::int32_t*>(base + o_parts);
   da_.n_parts_sel = reinterpret_cast<std::int32_t*>(base + o_nps);
@@ -280,6 +289,7 @@ void Context::alloc_device() {
   da_.part_o = static_cast<float*>(dalloc(L * da_.max_items * d * 4));
   da_.dom_done = static_cast<std::int32_t*>(dalloc(L * 4));
   da_.k4prof = static_cast<long long*>(dalloc(L * 8 * 8));
+  da_.work_ctr = static_cast<std::int32_t*>(dalloc(64));
   da_.k_v = kv;
   da_.k_s = ks;
   da_.prefetch_k = kp;

@@ -228,10 +228,18 @@ class Context {
   // decode buffers
   DecodeArgs da_{};
   void* d_dec_ = nullptr;  // packed result block
-  void* h_dec_ = nullptr;
-  void* h_dec2_ = nullptr;  // second host copy: the pending (deferred) replay reads one, the next step fills the other
-  bool replay_pending_ = false;  // a decode step's host bookkeeping has not been replayed yet
-  std::vector<std::int64_t> pending_gt_;
+  // two host copies of the decode result block: step i fills one while step i-1's bookkeeping
+  // is replayed from the other
+  void* h_blk_[2] = {nullptr, nullptr};
+  std::int32_t* h_blk_err_[2] = {nullptr, nullptr};
+  cudaEvent_t ev_step_[2] = {nullptr, nullptr};
+  cudaEvent_t evb_[2][4] = {{nullptr, nullptr, nullptr, nullptr}, {nullptr, nullptr, nullptr, nullptr}};
+  bool step_timed_[2] = {false, false};
+  int cur_ = 0;           // buffer of the most recently launched step
+  bool inflight_ = false;  // that step's bookkeeping has not been replayed yet
+  std::vector<std::int64_t> step_gt_[2];
+  void launch_step(int b, const float* q, int q_mem, float* out, int out_mem);
+  bool finish_step(int b);
   void replay_decode(const void* hblock, const std::int64_t* gt, int n_gt);
   std::size_t dec_bytes_ = 0;
   float* d_q_ = nullptr;

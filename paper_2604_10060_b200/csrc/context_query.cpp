@@ -32,20 +32,15 @@ std::uint64_t fnv1a(std::uint64_t h, std::uint64_t x) {  // engine.cpp:18-24
 
 }  // namespace
 
-void Context::decode_step(std::int64_t qid, const float* q, int q_mem, float* out, int out_mem,
-                          const std::int64_t* gt, int n_gt) {
-  (void)qid;
-  if (!built_) {
-    flush_pending();
-    build_now();  // engine.cpp:202
-  }
-  if (parts_.empty()) fail(-9, "retrieve before any index was built");
-  if (!q) fail(-10, "null query");
-  // A pending replay that settles a split changes the device index: finish it before launching.
-  if (replay_pending_ && (reinterpret_cast<const std::int32_t*>(
-                       static_cast<const std::uint8_t*>(h_dec2_) +
-                       (reinterpret_cast<const std::uint8_t*>(da_.flags) - static_cast<const std::uint8_t*>(d_dec_)))[0] & 1))
-    flush_pending();
+// Asynchronous step pipeline. decode_step(i) enqueues the scoring/selection and attention
+// kernels of step i and the device->host copy of its result block, THEN replays the host
+// bookkeeping of step i-1 (fetch / touch / materialize / latency model, retrieval.cpp:58-128)
+// while the GPU runs step i, and returns without waiting for step i (outputs in device memory
+// follow stream order on kvc_stream()). Step i's kernels read only the device index, which the
+// bookkeeping of step i-1 changes only when it settles a pending split (the K4 flag): then step i
+// is relaunched after the settle. Host outputs, parity / check / recall modes and per-step timing
+// complete the step before returning.
+void Context::launch_step(int b, const float* q, int q_mem, float* out, int out_mem) {
   const float* dq = q;
   if (q_mem != KVC_MEM_DEVICE) {
     KVC_CUDA(cudaMemcpyAsync(d_q_, q, static_cast<std::size_t>(L_) * d_ * 4, cudaMemcpyHostToDevice, st_));
@@ -55,40 +50,79 @@ void Context::decode_step(std::int64_t qid, const float* q, int q_mem, float* ou
   da_.out = (out && out_mem == KVC_MEM_DEVICE) ? out : d_out_;
   da_.n_parts_host = static_cast<std::int32_t>(parts_.size());
   KVC_CUDA(cudaMemsetAsync(da_.flags, 0, 4, st_));
-  launches_ += launch_decode(t_, da_, st_, timing_ ? ev_ : nullptr);
-  KVC_CUDA(cudaMemcpyAsync(h_dec_, d_dec_, dec_bytes_, cudaMemcpyDeviceToHost, st_));
+  launches_ += launch_decode(t_, da_, st_, timing_ ? evb_[b] : nullptr);
+  KVC_CUDA(cudaMemcpyAsync(h_blk_[b], d_dec_, dec_bytes_, cudaMemcpyDeviceToHost, st_));
   if (out && out_mem != KVC_MEM_DEVICE)
     KVC_CUDA(cudaMemcpyAsync(out, d_out_, static_cast<std::size_t>(L_) * d_ * 4, cudaMemcpyDeviceToHost, st_));
-  KVC_CUDA(cudaMemcpyAsync(h_err_, t_.err, 4, cudaMemcpyDeviceToHost, st_));
-  // the previous step's bookkeeping runs on the host while this step runs on the GPU
-  const auto tr0 = std::chrono::steady_clock::now();
-  flush_pending();
-  const auto th0 = std::chrono::steady_clock::now();
-  sync();
-  const auto th1 = std::chrono::steady_clock::now();
-  check_err_word(*h_err_);
-  if (timing_) {
+  KVC_CUDA(cudaMemcpyAsync(h_blk_err_[b], t_.err, 4, cudaMemcpyDeviceToHost, st_));
+  KVC_CUDA(cudaEventRecord(ev_step_[b], st_));
+  step_timed_[b] = timing_;
+}
+
+// Waits for step buffer b and replays its bookkeeping. Returns the step's settle flag.
+bool Context::finish_step(int b) {
+  const auto w0 = std::chrono::steady_clock::now();
+  KVC_CUDA(cudaEventSynchronize(ev_step_[b]));
+  const auto w1 = std::chrono::steady_clock::now();
+  check_err_word(*h_blk_err_[b]);
+  if (step_timed_[b]) {  // per-kernel events of this step (recorded when it was launched)
     float ms = 0.f;
     for (int i = 0; i < 3; ++i) {
-      KVC_CUDA(cudaEventElapsedTime(&ms, ev_[i], ev_[i + 1]));
+      KVC_CUDA(cudaEventElapsedTime(&ms, evb_[b][i], evb_[b][i + 1]));
       step_t_[i] = ms * 1e3;
     }
-    KVC_CUDA(cudaEventElapsedTime(&ms, ev_[0], ev_[3]));
+    KVC_CUDA(cudaEventElapsedTime(&ms, evb_[b][0], evb_[b][3]));
     step_t_[3] = ms * 1e3;
   }
-  step_t_[5] = std::chrono::duration<double, std::micro>(th1 - th0).count();
-  step_t_[6] = std::chrono::duration<double, std::micro>(th0 - tr0).count();
-  std::swap(h_dec_, h_dec2_);  // h_dec2_ now holds this step's results
-  replay_pending_ = true;
-  pending_gt_.assign(gt ? gt : nullptr, gt ? gt + (n_gt > 0 ? n_gt : 0) : nullptr);
-  // parity / recall / self-check callers need the bookkeeping now
-  if (cfg_.parity_mode || cfg_.check_invariants || (gt && n_gt > 0)) flush_pending();
+  const bool settle =
+      (reinterpret_cast<const std::int32_t*>(static_cast<const std::uint8_t*>(h_blk_[b]) +
+                                             (reinterpret_cast<const std::uint8_t*>(da_.flags) -
+                                              static_cast<const std::uint8_t*>(d_dec_)))[0] &
+       1) != 0;
+  std::vector<std::int64_t> gt;
+  gt.swap(step_gt_[b]);
+  replay_decode(h_blk_[b], gt.empty() ? nullptr : gt.data(), static_cast<int>(gt.size()));
+  step_t_[5] = std::chrono::duration<double, std::micro>(w1 - w0).count();
+  step_t_[6] = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - w1).count();
+  return settle;
+}
+
+void Context::decode_step(std::int64_t qid, const float* q, int q_mem, float* out, int out_mem,
+                          const std::int64_t* gt, int n_gt) {
+  (void)qid;
+  if (!built_) {
+    flush_pending();
+    build_now();  // engine.cpp:202
+  }
+  if (parts_.empty()) fail(-9, "retrieve before any index was built");
+  if (!q) fail(-10, "null query");
+  const bool overlap = inflight_;
+  const int pb = cur_;
+  if (overlap) cur_ ^= 1;
+  launch_step(cur_, q, q_mem, out, out_mem);
+  step_gt_[cur_].assign(gt ? gt : nullptr, gt ? gt + (n_gt > 0 ? n_gt : 0) : nullptr);
+  inflight_ = true;
+  if (overlap) {
+    // the previous step's bookkeeping runs on the host while this step runs on the GPU
+    if (finish_step(pb)) {  // it settled a split: this step saw the pre-settle index
+      KVC_CUDA(cudaStreamSynchronize(st_));
+      launch_step(cur_, q, q_mem, out, out_mem);
+    }
+  }
+  // parity / recall / self-check callers need the bookkeeping now; a host output only needs the
+  // step's data (its bookkeeping still overlaps the next step)
+  if (cfg_.parity_mode || cfg_.check_invariants || (gt && n_gt > 0))
+    flush_pending();
+  else if (out && out_mem != KVC_MEM_DEVICE)
+    KVC_CUDA(cudaEventSynchronize(ev_step_[cur_]));
 }
 
 void Context::flush_pending() {
-  if (!replay_pending_) return;
-  replay_pending_ = false;
-  replay_decode(h_dec2_, pending_gt_.empty() ? nullptr : pending_gt_.data(), static_cast<int>(pending_gt_.size()));
+  if (!inflight_) return;
+  inflight_ = false;
+  if (finish_step(cur_)) {
+    // nothing launched after it: the settle is already reflected in the device index
+  }
 }
 
 void Context::replay_decode(const void* hblock, const std::int64_t* gt, int n_gt) {

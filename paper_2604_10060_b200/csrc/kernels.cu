@@ -2138,7 +2138,6 @@ int launch_flat_topk(const DevTables& t, const float* q, const int32_t* slots, c
 
 namespace {
 int g_sms = 0;
-int* g_ctr = nullptr;
 
 template <int D, bool BF16>
 int launch_attend_t(const DevTables& t, const DecodeArgs& a, cudaStream_t st) {
@@ -2155,7 +2154,7 @@ int launch_attend_t(const DevTables& t, const DecodeArgs& a, cudaStream_t st) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_attend<D, BF16, STAGES>, ATT_THREADS + 32, smem);
     per_sm = max(1, per_sm);
   }
-  k_attend<D, BF16, STAGES><<<g_sms * per_sm, ATT_THREADS + 32, smem, st>>>(t, a, g_ctr);
+  k_attend<D, BF16, STAGES><<<g_sms * per_sm, ATT_THREADS + 32, smem, st>>>(t, a, a.work_ctr);
   return 1;
 }
 }  // namespace
@@ -2165,7 +2164,6 @@ int launch_decode(const DevTables& t, const DecodeArgs& a, cudaStream_t st, cuda
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaMalloc(&g_ctr, 64);
   }
   if (ev) cudaEventRecord(ev[0], st);
   const size_t smem4 = k4_smem_bytes(t.d, t.cmax, a.n_parts_host, t.W, t.tmax);
@@ -2174,7 +2172,7 @@ int launch_decode(const DevTables& t, const DecodeArgs& a, cudaStream_t st, cuda
     cudaFuncSetAttribute(k_score_select, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     attr = true;
   }
-  k_score_select<<<t.L, 256, smem4, st>>>(t, a, g_ctr);
+  k_score_select<<<t.L, 256, smem4, st>>>(t, a, a.work_ctr);
   if (ev) cudaEventRecord(ev[1], st);
   int n = 1;
   switch (t.d * 2 + t.kv_bf16) {

@@ -181,6 +181,7 @@ struct DecodeArgs {
   float* out;              // [L][d]
   float scale_log2;        // log2(e) / sqrt(d)
   long long* k4prof;       // [L][8] clock64 phase cycles (instrumentation; may be null)
+  int32_t* work_ctr;       // attention work-claim counter (per context: contexts may run concurrently)
 };
 
 // ----------------------------------------------------------------------------- launchers
