@@ -882,6 +882,7 @@ void Context::run_inserts(std::int64_t frame_id, std::int64_t pid, int T, std::i
       }
       if (timing_) KVC_CUDA(cudaEventRecord(ev_[4], st_));
       launches_ += launch_store_rows(t_, ia_, st_);
+      KVC_CUDA(cudaGetLastError());
       if (timing_) KVC_CUDA(cudaEventRecord(ev_[5], st_));
       KVC_CUDA(cudaMemcpyAsync(h_evk_, ia_.ev_kind, static_cast<std::size_t>(L_) * t_.tmax * 4, cudaMemcpyDeviceToHost, st_));
       KVC_CUDA(cudaMemcpyAsync(h_evs_, ia_.ev_slot, static_cast<std::size_t>(L_) * t_.tmax * 4, cudaMemcpyDeviceToHost, st_));

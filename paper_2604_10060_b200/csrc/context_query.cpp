@@ -51,6 +51,7 @@ void Context::launch_step(int b, const float* q, int q_mem, float* out, int out_
   da_.n_parts_host = static_cast<std::int32_t>(parts_.size());
   KVC_CUDA(cudaMemsetAsync(da_.flags, 0, 4, st_));
   launches_ += launch_decode(t_, da_, st_, timing_ ? evb_[b] : nullptr);
+  KVC_CUDA(cudaGetLastError());  // launch-configuration failures surface here, not as empty results
   KVC_CUDA(cudaMemcpyAsync(h_blk_[b], d_dec_, dec_bytes_, cudaMemcpyDeviceToHost, st_));
   if (out && out_mem != KVC_MEM_DEVICE)
     KVC_CUDA(cudaMemcpyAsync(out, d_out_, static_cast<std::size_t>(L_) * d_ * 4, cudaMemcpyDeviceToHost, st_));
