@@ -274,7 +274,7 @@ def main():
     for i in range(args.warmup):
         kv.query(i, q_dev[i], out=out_dev)
     kv.set_timing(True)
-    att_us, k4_us, att_bytes_l, host_ph = [], [], [], []
+    att_us, k4_us, att_bytes_l, host_ph, span_us = [], [], [], [], []
     launches0 = kv.launch_count()
     torch.cuda.synchronize()
     if world > 1:
@@ -286,9 +286,10 @@ def main():
                 kv.query(i, q_dev[i], out=out_dev)
                 tm = kv.step_timing()
                 k4_us.append(tm[0])
+                span_us.append(tm[3])
                 att_us.append(tm[1])
                 att_bytes_l.append(tm[4])
-                host_ph.append(tm[5:8].copy())
+                host_ph.append(tm[5:9].copy())
                 if world > 1:  # per-domain outputs to every rank (NCCL over NVLink)
                     gather_domain_outputs(out_dev, args.domains)
             ev1.record(stream)
@@ -346,6 +347,8 @@ def main():
                       "host_wait_device": round(float(np.mean([h[0] for h in host_ph])), 2),
                       "host_replay": round(float(np.mean([h[1] for h in host_ph])), 2),
                       "host_repin": round(float(np.mean([h[2] for h in host_ph])), 2),
+                      "device_span": round(float(np.mean(span_us)), 2),
+                      "host_layer_loop": round(float(np.mean([h[3] for h in host_ph])), 2),
                       "k4_cycles": dict(zip(["qnorm", "visual", "cand_score", "sort", "tail1", "ring", "desc", "-"],
                                             k4_cycles.round(0).tolist()))},
         "clocks": clk.summary(),

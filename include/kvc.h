@@ -207,7 +207,7 @@ KVC_API int64_t kvc_launch_count(kvc_ctx* ctx);
  * microseconds from CUDA events -- t[0] score/select, t[1] attention (+ fused combine), t[2]
  * unused, t[3] launch-to-end on the device; t[4] algorithmic bytes of the attention launch;
  * host phases in microseconds -- t[5] wait for the device, t[6] retrieve bookkeeping replay,
- * t[7] repin + checks. */
+ * t[7] repin + checks; t[8], t[9] unused. t has 10 entries. */
 KVC_API int kvc_last_step_timing(kvc_ctx* ctx, double* t);
 /* Timing of the last ingested frame (needs kvc_set_timing(1)), t[8]: device microseconds of
  * the candidate lists, approximate tile, top-M + exact pre-scores, sequential resolve and row

@@ -417,7 +417,7 @@ class ClusterKVCache:
         return t
 
     def step_timing(self):
-        t = np.zeros(8)
+        t = np.zeros(10)
         lib().kvc_last_step_timing(self.h, _p(t, f64p))
         return t
 

@@ -332,7 +332,7 @@ int64_t kvc_launch_count(kvc_ctx* ctx) { return ctx->impl->launches(); }
 
 int kvc_last_step_timing(kvc_ctx* ctx, double* t) {
   const double* s = ctx->impl->step_timing();
-  for (int i = 0; i < 8; ++i) t[i] = s[i];
+  for (int i = 0; i < 10; ++i) t[i] = s[i];
   return KVC_OK;
 }
 

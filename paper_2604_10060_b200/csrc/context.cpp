@@ -91,6 +91,11 @@ Context::~Context() {
   for (auto& e : ev_) cudaEventDestroy(e);
   for (auto& e : ev_step_)
     if (e) cudaEventDestroy(e);
+  for (auto& e : ev_k4_)
+    if (e) cudaEventDestroy(e);
+  for (auto& e : ev_out_)
+    if (e) cudaEventDestroy(e);
+  if (cs_) cudaStreamDestroy(cs_);
   for (auto& row : evb_)
     for (auto& e : row)
       if (e) cudaEventDestroy(e);
@@ -172,7 +177,6 @@ void Context::alloc_device() {
   t_.pl_cnt = static_cast<std::int32_t*>(dalloc(static_cast<std::int64_t>(t_.max_parts) * L * 4));
   t_.pl_pool_cap = S * 4 + 1024;
   t_.pl_pool = static_cast<std::int32_t*>(dalloc(t_.pl_pool_cap * 4));
-  t_.err = static_cast<std::int32_t*>(dalloc(16));
   h_err_ = static_cast<std::int32_t*>(halloc(16));
 
   // page stack: ring pages are [0, ring_pages); the stack holds the rest
@@ -259,29 +263,20 @@ void Context::alloc_device() {
   const std::size_t o_parts = carve(L * kv * 4), o_nps = carve(L * 4), o_rs = carve(L * ks * 4),
                     o_rb = carve(L * ks), o_nr = carve(L * 4), o_ps = carve(L * kp * 4),
                     o_pb = carve(L * kp), o_np = carve(L * 4), o_vs = carve(L * ks * 4),
-                    o_nv = carve(L * 4), o_att = carve(L * 8), o_nc = carve(L * 4), o_fl = carve(16);
+                    o_nv = carve(L * 4), o_att = carve(L * 8), o_nc = carve(L * 4), o_fl = carve(L * 4), o_ew = carve(L * 4);
   dec_bytes_ = off;
-  d_dec_ = dalloc(dec_bytes_);
+  res_off_ = {o_parts, o_nps, o_rs, o_rb, o_nr, o_ps, o_pb, o_np, o_vs, o_nv, o_att, o_nc, o_fl, o_ew};
+  t_.err = static_cast<std::int32_t*>(dalloc(16));
+  KVC_CUDA(cudaStreamCreateWithFlags(&cs_, cudaStreamNonBlocking));
   for (int b = 0; b < 2; ++b) {
+    d_blk_[b] = dalloc(dec_bytes_);
     h_blk_[b] = halloc(dec_bytes_);
-    h_blk_err_[b] = static_cast<std::int32_t*>(halloc(16));
+    KVC_CUDA(cudaEventCreateWithFlags(&ev_k4_[b], cudaEventDisableTiming));
+    KVC_CUDA(cudaEventCreateWithFlags(&ev_out_[b], cudaEventDisableTiming));
     KVC_CUDA(cudaEventCreateWithFlags(&ev_step_[b], cudaEventDisableTiming));
     for (auto& e : evb_[b]) KVC_CUDA(cudaEventCreate(&e));
   }
-  auto* base = static_cast<std::uint8_t*>(d_dec_);
-  da_.parts = reinterpret_cast<std::int32_t*>(base + o_parts);
-  da_.n_parts_sel = reinterpret_cast<std::int32_t*>(base + o_nps);
-  da_.ranked_slot = reinterpret_cast<std::int32_t*>(base + o_rs);
-  da_.ranked_buf = base + o_rb;
-  da_.n_ranked = reinterpret_cast<std::int32_t*>(base + o_nr);
-  da_.pf_slot = reinterpret_cast<std::int32_t*>(base + o_ps);
-  da_.pf_buf = base + o_pb;
-  da_.n_pf = reinterpret_cast<std::int32_t*>(base + o_np);
-  da_.ver_slot = reinterpret_cast<std::int32_t*>(base + o_vs);
-  da_.n_ver = reinterpret_cast<std::int32_t*>(base + o_nv);
-  da_.attended = reinterpret_cast<std::int64_t*>(base + o_att);
-  da_.n_cand = reinterpret_cast<std::int32_t*>(base + o_nc);
-  da_.flags = reinterpret_cast<std::int32_t*>(base + o_fl);
+  set_result_block(0);
   da_.desc = static_cast<int4*>(dalloc(L * da_.max_desc * sizeof(int4)));
   da_.n_desc = static_cast<std::int32_t*>(dalloc(L * 4));
   da_.n_items = static_cast<std::int32_t*>(dalloc(L * 4));
@@ -373,6 +368,28 @@ void Context::debug_assign_check(const void* keys, int T, std::int64_t pid, int 
   out[1] = static_cast<double>(h[1]);
   out[2] = static_cast<double>(h[2]);
   out[3] = ia_.margin;
+}
+
+// Points the decode arguments' result fields at device result block b (two blocks: the kernels
+// of step i+1 write one while step i's block is copied to the host and replayed).
+void Context::set_result_block(int b) {
+  auto* base = static_cast<std::uint8_t*>(d_blk_[b]);
+  const ResultOffsets& o = res_off_;
+  da_.parts = reinterpret_cast<std::int32_t*>(base + o.parts);
+  da_.n_parts_sel = reinterpret_cast<std::int32_t*>(base + o.nps);
+  da_.ranked_slot = reinterpret_cast<std::int32_t*>(base + o.rs);
+  da_.ranked_buf = base + o.rb;
+  da_.n_ranked = reinterpret_cast<std::int32_t*>(base + o.nr);
+  da_.pf_slot = reinterpret_cast<std::int32_t*>(base + o.ps);
+  da_.pf_buf = base + o.pb;
+  da_.n_pf = reinterpret_cast<std::int32_t*>(base + o.np);
+  da_.ver_slot = reinterpret_cast<std::int32_t*>(base + o.vs);
+  da_.n_ver = reinterpret_cast<std::int32_t*>(base + o.nv);
+  da_.attended = reinterpret_cast<std::int64_t*>(base + o.att);
+  da_.n_cand = reinterpret_cast<std::int32_t*>(base + o.nc);
+  da_.flags = reinterpret_cast<std::int32_t*>(base + o.fl);
+  da_.errw = reinterpret_cast<std::int32_t*>(base + o.ew);
+  d_dec_ = d_blk_[b];
 }
 
 void Context::resolve_profile(double* out) {

@@ -231,10 +231,18 @@ class Context {
   // two host copies of the decode result block: step i fills one while step i-1's bookkeeping
   // is replayed from the other
   void* h_blk_[2] = {nullptr, nullptr};
-  std::int32_t* h_blk_err_[2] = {nullptr, nullptr};
-  cudaEvent_t ev_step_[2] = {nullptr, nullptr};
+  cudaEvent_t ev_step_[2] = {nullptr, nullptr};  // result block b copied to the host (copy stream)
+  cudaEvent_t ev_k4_[2] = {nullptr, nullptr};    // K4 of the step in block b done (compute stream)
+  cudaEvent_t ev_out_[2] = {nullptr, nullptr};   // attention output of that step done
+  cudaStream_t cs_ = nullptr;                    // copy stream for the result blocks
+  void* d_blk_[2] = {nullptr, nullptr};
+  struct ResultOffsets {
+    std::size_t parts, nps, rs, rb, nr, ps, pb, np, vs, nv, att, nc, fl, ew;
+  } res_off_{};
+  void set_result_block(int b);
   cudaEvent_t evb_[2][4] = {{nullptr, nullptr, nullptr, nullptr}, {nullptr, nullptr, nullptr, nullptr}};
   bool step_timed_[2] = {false, false};
+  bool blk_used_[2] = {false, false};
   int cur_ = 0;           // buffer of the most recently launched step
   bool inflight_ = false;  // that step's bookkeeping has not been replayed yet
   std::vector<std::int64_t> step_gt_[2];
@@ -250,7 +258,7 @@ class Context {
   bool assign_tc_ = false;    // tensor-core distance tile (KVC_ASSIGN=simt disables)
   alignas(64) unsigned char key_map_[128];  // CUtensorMap over the frame keys
   void* d_check_ = nullptr;                 // debug_assign_check result words
-  double step_t_[8] = {0};
+  double step_t_[10] = {0};
   double ingest_t_[8] = {0};  // last frame: device us (cands, approx, topm, resolve, store), host us (wait, replay, rest)
   std::int64_t launches_ = 0;
 

@@ -41,6 +41,9 @@ std::uint64_t fnv1a(std::uint64_t h, std::uint64_t x) {  // engine.cpp:18-24
 // is relaunched after the settle. Host outputs, parity / check / recall modes and per-step timing
 // complete the step before returning.
 void Context::launch_step(int b, const float* q, int q_mem, float* out, int out_mem) {
+  if (blk_used_[b]) KVC_CUDA(cudaStreamWaitEvent(st_, ev_step_[b], 0));  // block b's last copy done
+  blk_used_[b] = true;
+  set_result_block(b);
   const float* dq = q;
   if (q_mem != KVC_MEM_DEVICE) {
     KVC_CUDA(cudaMemcpyAsync(d_q_, q, static_cast<std::size_t>(L_) * d_ * 4, cudaMemcpyHostToDevice, st_));
@@ -49,24 +52,40 @@ void Context::launch_step(int b, const float* q, int q_mem, float* out, int out_
   da_.q = dq;
   da_.out = (out && out_mem == KVC_MEM_DEVICE) ? out : d_out_;
   da_.n_parts_host = static_cast<std::int32_t>(parts_.size());
-  KVC_CUDA(cudaMemsetAsync(da_.flags, 0, 4, st_));
-  launches_ += launch_decode(t_, da_, st_, timing_ ? evb_[b] : nullptr);
+  launches_ += launch_decode(t_, da_, st_, timing_ ? evb_[b] : nullptr, ev_k4_[b]);
   KVC_CUDA(cudaGetLastError());  // launch-configuration failures surface here, not as empty results
-  KVC_CUDA(cudaMemcpyAsync(h_blk_[b], d_dec_, dec_bytes_, cudaMemcpyDeviceToHost, st_));
+  // the result block goes to the host on the copy stream as soon as K4 is done (overlaps K6)
+  KVC_CUDA(cudaStreamWaitEvent(cs_, ev_k4_[b], 0));
+  KVC_CUDA(cudaMemcpyAsync(h_blk_[b], d_blk_[b], dec_bytes_, cudaMemcpyDeviceToHost, cs_));
+  KVC_CUDA(cudaEventRecord(ev_step_[b], cs_));
   if (out && out_mem != KVC_MEM_DEVICE)
     KVC_CUDA(cudaMemcpyAsync(out, d_out_, static_cast<std::size_t>(L_) * d_ * 4, cudaMemcpyDeviceToHost, st_));
-  KVC_CUDA(cudaMemcpyAsync(h_blk_err_[b], t_.err, 4, cudaMemcpyDeviceToHost, st_));
-  KVC_CUDA(cudaEventRecord(ev_step_[b], st_));
+  KVC_CUDA(cudaEventRecord(ev_out_[b], st_));
   step_timed_[b] = timing_;
 }
 
-// Waits for step buffer b and replays its bookkeeping. Returns the step's settle flag.
+// Waits for step buffer b's result block and replays its bookkeeping. Returns the settle flag.
 bool Context::finish_step(int b) {
   const auto w0 = std::chrono::steady_clock::now();
   KVC_CUDA(cudaEventSynchronize(ev_step_[b]));
   const auto w1 = std::chrono::steady_clock::now();
-  check_err_word(*h_blk_err_[b]);
+  auto hoff = [&](const void* dptr) {
+    return static_cast<const std::uint8_t*>(h_blk_[b]) +
+           (static_cast<const std::uint8_t*>(dptr) - static_cast<const std::uint8_t*>(d_dec_));
+  };
+  std::int32_t err = 0;
+  bool settle = false;
+  {
+    const auto* hew = reinterpret_cast<const std::int32_t*>(hoff(da_.errw));
+    const auto* hfl = reinterpret_cast<const std::int32_t*>(hoff(da_.flags));
+    for (int l = 0; l < L_; ++l) {
+      err |= hew[l];
+      settle |= hfl[l] != 0;
+    }
+  }
+  check_err_word(err);
   if (step_timed_[b]) {  // per-kernel events of this step (recorded when it was launched)
+    KVC_CUDA(cudaEventSynchronize(evb_[b][3]));
     float ms = 0.f;
     for (int i = 0; i < 3; ++i) {
       KVC_CUDA(cudaEventElapsedTime(&ms, evb_[b][i], evb_[b][i + 1]));
@@ -75,11 +94,6 @@ bool Context::finish_step(int b) {
     KVC_CUDA(cudaEventElapsedTime(&ms, evb_[b][0], evb_[b][3]));
     step_t_[3] = ms * 1e3;
   }
-  const bool settle =
-      (reinterpret_cast<const std::int32_t*>(static_cast<const std::uint8_t*>(h_blk_[b]) +
-                                             (reinterpret_cast<const std::uint8_t*>(da_.flags) -
-                                              static_cast<const std::uint8_t*>(d_dec_)))[0] &
-       1) != 0;
   std::vector<std::int64_t> gt;
   gt.swap(step_gt_[b]);
   replay_decode(h_blk_[b], gt.empty() ? nullptr : gt.data(), static_cast<int>(gt.size()));
@@ -115,7 +129,7 @@ void Context::decode_step(std::int64_t qid, const float* q, int q_mem, float* ou
   if (cfg_.parity_mode || cfg_.check_invariants || (gt && n_gt > 0))
     flush_pending();
   else if (out && out_mem != KVC_MEM_DEVICE)
-    KVC_CUDA(cudaEventSynchronize(ev_step_[cur_]));
+    KVC_CUDA(cudaEventSynchronize(ev_out_[cur_]));
 }
 
 void Context::flush_pending() {
@@ -164,6 +178,7 @@ void Context::replay_decode(const void* hblock, const std::int64_t* gt, int n_gt
       lo.pf.push_back({slot_id_[static_cast<std::size_t>(h_ps[l * da_.prefetch_k + i])], h_pb[l * da_.prefetch_k + i]});
   }
 
+  const auto tl0 = std::chrono::steady_clock::now();
   // retrieval.cpp:58-128, layer by layer
   const bool parity = cfg_.parity_mode != 0 || (gt && n_gt > 0);
   std::vector<std::int64_t> predicted_next;
@@ -236,6 +251,7 @@ void Context::replay_decode(const void* hblock, const std::int64_t* gt, int n_gt
       stall_next = std::max(0.0, pf_cost - lo.lat[4]);
     }
   }
+  step_t_[8] = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - tl0).count();
   for (const LayerOut& lo : last_) last_ttft_ += lo.lat[0] + lo.lat[1] + lo.lat[2] + lo.lat[3] + lo.lat[4];
   last_recall_ = -1.0;
   if (parity) {

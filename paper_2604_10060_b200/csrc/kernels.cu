@@ -1303,6 +1303,7 @@ __global__ void __launch_bounds__(256) k_score_select(DevTables t, DecodeArgs a,
   __shared__ int vers[64], nver_s;
   __shared__ int rank_slot[64], n_rank_s, order[64];
   __shared__ unsigned long long att_s;
+  __shared__ int lazy_any;
   __shared__ bool degen;
   __shared__ int ring_count_s[64];
   __shared__ int sset[K4_ROWS], n_s;
@@ -1338,6 +1339,7 @@ __global__ void __launch_bounds__(256) k_score_select(DevTables t, DecodeArgs a,
   if (threadIdx.x == 0) {
     degen = false;
     att_s = 0;
+    lazy_any = 0;
   }
   if (threadIdx.x < t.W && threadIdx.x < 64) ring_count_s[threadIdx.x] = t.ring_count[threadIdx.x];
   __syncthreads();
@@ -1554,10 +1556,11 @@ __global__ void __launch_bounds__(256) k_score_select(DevTables t, DecodeArgs a,
     vnp[threadIdx.x] = t.npages[s];
     vnbp[threadIdx.x] = t.nbpages[s];
     atomicAdd(&att_s, static_cast<unsigned long long>(t.nmem[s] + t.nbuf[s]));
-    if (t.lazy[s]) atomicOr(a.flags, 1);  // a pending split: the host must settle before the next step
+    if (t.lazy[s]) lazy_any = 1;  // a pending split: the host must settle before the next step
   }
   if (threadIdx.x < 64) ring_cnt[threadIdx.x] = 0;
   __syncthreads();
+  if (threadIdx.x == 0) a.flags[l] = lazy_any;
   K4MARK(4)
   // window ring: tokens whose owner is not a verified cluster (retrieval.cpp:107-108 dedup)
   {
@@ -1628,6 +1631,10 @@ __global__ void __launch_bounds__(256) k_score_select(DevTables t, DecodeArgs a,
   __syncthreads();
   K4MARK(6)
 #undef K4MARK
+  if (threadIdx.x == 0) {  // errors raised so far (this block's own are ordered before the read)
+    __threadfence();
+    a.errw[l] = atomicOr(t.err, 0);
+  }
   if (a.n_items[l] == 0)  // nothing attended: output zeros
     for (int i = threadIdx.x; i < d; i += blockDim.x) a.out[static_cast<int64_t>(l) * d + i] = 0.f;
 }
@@ -1682,6 +1689,7 @@ __global__ void __launch_bounds__(K4T) k_score_select2(DevTables t, DecodeArgs a
   __shared__ int vers[64], nver_s;
   __shared__ int rank_slot[64], n_rank_s, order[64];
   __shared__ unsigned long long att_s;
+  __shared__ int lazy_any;
   __shared__ bool degen;
   __shared__ int ring_count_s[64];
   __shared__ int sset[K4_SMAX], n_s;
@@ -1720,6 +1728,7 @@ __global__ void __launch_bounds__(K4T) k_score_select2(DevTables t, DecodeArgs a
   if (tid == 0) {
     degen = false;
     att_s = 0;
+    lazy_any = 0;
   }
   if (tid < t.W && tid < 64) ring_count_s[tid] = t.ring_count[tid];
   if (tid < 128) vhash[tid] = -1;
@@ -1971,12 +1980,13 @@ __global__ void __launch_bounds__(K4T) k_score_select2(DevTables t, DecodeArgs a
     vnp[tid] = t.npages[s];
     vnbp[tid] = t.nbpages[s];
     atomicAdd(&att_s, static_cast<unsigned long long>(t.nmem[s] + t.nbuf[s]));
-    if (t.lazy[s]) atomicOr(a.flags, 1);  // a pending split: the host must settle before the next step
+    if (t.lazy[s]) lazy_any = 1;  // a pending split: the host must settle before the next step
     int h = (s * 0x9E3779B1u) >> 25;      // 128-entry open-addressing set
     while (atomicCAS(&vhash[h], -1, s) != -1) h = (h + 1) & 127;
   }
   if (tid < 64) ring_cnt[tid] = 0;
   __syncthreads();
+  if (threadIdx.x == 0) a.flags[l] = lazy_any;
   K4MARK(4)
   // window ring: tokens whose owner is not a verified cluster (retrieval.cpp:107-108 dedup)
   {
@@ -2076,6 +2086,10 @@ __global__ void __launch_bounds__(K4T) k_score_select2(DevTables t, DecodeArgs a
   __syncthreads();
   K4MARK(6)
 #undef K4MARK
+  if (threadIdx.x == 0) {  // errors raised so far (this block's own are ordered before the read)
+    __threadfence();
+    a.errw[l] = atomicOr(t.err, 0);
+  }
   if (a.n_items[l] == 0)  // nothing attended: output zeros
     for (int i = tid; i < d; i += K4T) a.out[static_cast<int64_t>(l) * d + i] = 0.f;
 }
@@ -2608,7 +2622,7 @@ int launch_attend_t(const DevTables& t, const DecodeArgs& a, cudaStream_t st) {
 }
 }  // namespace
 
-int launch_decode(const DevTables& t, const DecodeArgs& a, cudaStream_t st, cudaEvent_t* ev) {
+int launch_decode(const DevTables& t, const DecodeArgs& a, cudaStream_t st, cudaEvent_t* ev, cudaEvent_t k4_done) {
   if (!g_sms) {
     int dev = 0;
     cudaGetDevice(&dev);
@@ -2630,6 +2644,7 @@ int launch_decode(const DevTables& t, const DecodeArgs& a, cudaStream_t st, cuda
     k_score_select<<<t.L, 256, smem4, st>>>(t, a, a.work_ctr);
   }
   if (ev) cudaEventRecord(ev[1], st);
+  if (k4_done) cudaEventRecord(k4_done, st);
   int n = 1;
   switch (t.d * 2 + t.kv_bf16) {
     case 64: n += launch_attend_t<32, false>(t, a, st); break;

@@ -167,7 +167,8 @@ struct DecodeArgs {
   int32_t* n_ver;          // [L]
   int64_t* attended;       // [L]        attended-set size (members+buffers of verified U window)
   int32_t* n_cand;         // [L]        candidates compared (count_candidates)
-  int32_t* flags;          // [1] bit 0: a verified cluster has a pending split (needs a host settle)
+  int32_t* flags;          // [L] 1: a verified cluster of the domain has a pending split (host settle)
+  int32_t* errw;           // [L] the device error word as seen by the domain's K4 block at its end
   // attention work list: page descriptors per domain (x page, y fill, z kind | ring_slot << 8,
   // w first token of the page within its frame); an item = chunk_pages consecutive descriptors
   int4* desc;              // [L][max_desc]
@@ -207,7 +208,9 @@ int launch_topm(const DevTables& t, const IngestArgs& a, cudaStream_t st);
 int launch_store_rows(const DevTables& t, const IngestArgs& a, cudaStream_t st);
 int launch_ring_write(const DevTables& t, const void* fk, const void* fv, int32_t T,
                       int32_t ring_slot, cudaStream_t st);
-int launch_decode(const DevTables& t, const DecodeArgs& a, cudaStream_t st, cudaEvent_t* ev);
+// k4_done (may be null) is recorded between the score/select and attention kernels.
+int launch_decode(const DevTables& t, const DecodeArgs& a, cudaStream_t st, cudaEvent_t* ev,
+                  cudaEvent_t k4_done = nullptr);
 
 // Slot initialisation from host-computed exact statistics: rep64 rows (rep, norm, var,
 // counts) uploaded by the host; this kernel fills the fp32 mirrors.
