@@ -94,6 +94,8 @@ typedef struct {
   int32_t max_tokens;          /* tokens per frame, default 256 */
   int32_t parity_mode;         /* materialise attended (frame, token) sets on the host */
   int32_t check_invariants;    /* run the structural self-check after build/query (engine.cpp:91,235) */
+  int32_t tier_stage_pages;    /* HBM staging pages for in-flight host-tier migrations, default 2048 */
+  int64_t host_pool_bytes;     /* pinned host tier for Host-resident clusters, default 256 MiB */
 } kvc_cfg;
 
 KVC_API void kvc_cfg_default(kvc_cfg* cfg);
@@ -199,6 +201,25 @@ KVC_API int kvc_check(kvc_ctx* ctx);
  * in *cost_us (the reference's ledger arithmetic). */
 KVC_API int kvc_offload(kvc_ctx* ctx, int64_t id, double* cost_us);
 KVC_API int kvc_fetch(kvc_ctx* ctx, int64_t id, int32_t cause, double* cost_us);
+
+/* ------------------------------------------------------------------ physical host tier
+ * TieredStore's Host residence is physical: a Host cluster's member pages live in one contiguous
+ * extent of pinned host memory and every residence change is migrated by one cudaMemcpyAsync
+ * per cluster on a transfer stream (K5), asynchronously. Kernels address pages wherever they
+ * physically are, so results never depend on migration progress.
+ * kvc_tier_sync completes every queued / in-flight migration (physical == logical residence).
+ * kvc_tier_stats out[10]: host pages in use, host-tier capacity (pages), clusters with host pages,
+ * offloads committed, fetches committed, bytes device->host, bytes host->device, migrations
+ * queued, batches in flight, HBM staging pages in use. */
+KVC_API int kvc_tier_sync(kvc_ctx* ctx);
+KVC_API int kvc_tier_stats(kvc_ctx* ctx, int64_t* out);
+/* out[3]: first host page of the cluster's extent (-1 none), its length in pages, migration busy */
+KVC_API int kvc_cluster_tier(kvc_ctx* ctx, int64_t id, int64_t* out);
+/* Debug: every live page table against the host's view of the tiers (reads each list; small
+ * contexts). out[4]: host page ids outside their cluster's extent, Device clusters holding host
+ * pages, Host clusters with all member pages in HBM, clusters whose page fills disagree with the
+ * member count / logical device tail. All zero after kvc_tier_sync. */
+KVC_API int kvc_debug_tier_check(kvc_ctx* ctx, int64_t* out4);
 
 /* ------------------------------------------------------------------ instrumentation */
 /* Kernel launches issued by this context since creation (for bench gpu_launches). */

@@ -80,7 +80,8 @@ class Config(C.Structure):
         ("pool_bytes", C.c_int64), ("max_slots", C.c_int32), ("max_cluster_pages", C.c_int32),
         ("max_buffer_pages", C.c_int32), ("max_partitions", C.c_int32),
         ("max_candidates", C.c_int32), ("max_tokens", C.c_int32), ("parity_mode", C.c_int32),
-        ("check_invariants", C.c_int32),
+        ("check_invariants", C.c_int32), ("tier_stage_pages", C.c_int32),
+        ("host_pool_bytes", C.c_int64),
     ]
 
     @classmethod
@@ -139,6 +140,10 @@ def lib():
         L.kvc_check.argtypes = [vp]
         L.kvc_offload.argtypes = [vp, C.c_int64, f64p]
         L.kvc_fetch.argtypes = [vp, C.c_int64, C.c_int32, f64p]
+        L.kvc_tier_sync.argtypes = [vp]
+        L.kvc_tier_stats.argtypes = [vp, i64p]
+        L.kvc_cluster_tier.argtypes = [vp, C.c_int64, i64p]
+        L.kvc_debug_tier_check.argtypes = [vp, i64p]
         L.kvc_launch_count.argtypes = [vp]
         L.kvc_launch_count.restype = C.c_int64
         L.kvc_last_step_timing.argtypes = [vp, f64p]
@@ -168,7 +173,8 @@ EXPORTED = [
     "kvc_ledger_log_size", "kvc_ledger_op", "kvc_check", "kvc_offload", "kvc_fetch",
     "kvc_launch_count", "kvc_last_step_timing", "kvc_set_timing", "kvc_last_ingest_timing",
     "kvc_debug_resolve_profile", "kvc_host_split_two", "kvc_host_kmeans", "kvc_host_tau",
-    "kvc_host_mix_seed", "kvc_debug_div_check", "kvc_debug_assign_check",
+    "kvc_host_mix_seed", "kvc_debug_div_check", "kvc_debug_assign_check", "kvc_tier_sync",
+    "kvc_tier_stats", "kvc_cluster_tier", "kvc_debug_tier_check",
 ]
 
 
@@ -388,6 +394,32 @@ class ClusterKVCache:
         c = C.c_double()
         _check(lib().kvc_fetch(self.h, cid, cause, C.byref(c)))
         return c.value
+
+    # ------------------------------------------------------------------ physical host tier
+    TIER_KEYS = ("host_pages", "host_capacity_pages", "host_clusters", "offloads", "fetches",
+                 "bytes_d2h", "bytes_h2d", "queued", "in_flight", "stage_pages")
+
+    def tier_sync(self):
+        """Completes every queued / in-flight host-tier migration (kvc_tier_sync)."""
+        _check(lib().kvc_tier_sync(self.h))
+
+    def tier_stats(self) -> dict:
+        out = np.zeros(10, np.int64)
+        _check(lib().kvc_tier_stats(self.h, _p(out, i64p)))
+        return dict(zip(self.TIER_KEYS, (int(x) for x in out)))
+
+    def cluster_tier(self, cid: int):
+        """(first host page, host pages, migration busy) of a cluster's host-tier extent."""
+        out = np.zeros(3, np.int64)
+        _check(lib().kvc_cluster_tier(self.h, cid, _p(out, i64p)))
+        return int(out[0]), int(out[1]), bool(out[2])
+
+    def tier_check(self):
+        """(host ids outside extents, Device clusters with host pages, Host clusters fully in
+        HBM, fill / tail mismatches) -- all zero once tier_sync() returned."""
+        out = np.zeros(4, np.int64)
+        _check(lib().kvc_debug_tier_check(self.h, _p(out, i64p)))
+        return tuple(int(x) for x in out)
 
     # ------------------------------------------------------------------ instrumentation
     def launch_count(self) -> int:

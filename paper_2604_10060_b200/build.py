@@ -24,8 +24,9 @@ CXXFLAGS = ["-std=c++17", "-O3", "-fPIC", "-ffp-contract=off", "-fvisibility=hid
 NVFLAGS = ["-std=c++17", "-O3", "-lineinfo", "--fmad=false", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
            "-Xcompiler", "-ffp-contract=off", "-Xptxas", "-v"] + ARCH
 
-SOURCES = ["kmeans.cpp", "context.cpp", "context_query.cpp", "abi.cpp", "kernels.cu", "resolve_spec.cu", "assign_tc.cu"]
-HEADERS = ["kvc_core.hpp", "devmath.cuh", "kmeans.hpp", "context.hpp", os.path.join("..", "..", "include", "kvc.h")]
+SOURCES = ["kmeans.cpp", "context.cpp", "context_query.cpp", "context_tiers.cpp", "abi.cpp", "kernels.cu",
+           "resolve_spec.cu", "assign_tc.cu", "tiers.cu"]
+HEADERS = ["kvc_core.hpp", "devmath.cuh", "kmeans.hpp", "context.hpp", "extent_alloc.hpp", os.path.join("..", "..", "include", "kvc.h")]
 
 
 def _stale(obj: str, src: str) -> bool:

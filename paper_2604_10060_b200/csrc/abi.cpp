@@ -102,6 +102,8 @@ void kvc_cfg_default(kvc_cfg* c) {
   c->max_tokens = 256;
   c->parity_mode = 0;
   c->check_invariants = 0;
+  c->tier_stage_pages = 2048;
+  c->host_pool_bytes = 256LL << 20;
 }
 
 const char* kvc_last_error(void) { return g_err.c_str(); }
@@ -316,6 +318,7 @@ int kvc_check(kvc_ctx* ctx) {
 int kvc_offload(kvc_ctx* ctx, int64_t id, double* cost_us) {
   return guard([&] {
     const double c = F(ctx).offload(id);
+    F(ctx).tier_kick();
     if (cost_us) *cost_us = c;
   });
 }
@@ -324,8 +327,25 @@ int kvc_fetch(kvc_ctx* ctx, int64_t id, int32_t cause, double* cost_us) {
   return guard([&] {
     if (cause < 0 || cause > 4) kvc::fail(KVC_E_CONFIG, "unknown transfer cause");
     const double c = F(ctx).fetch(id, cause);
+    F(ctx).tier_kick();
     if (cost_us) *cost_us = c;
   });
+}
+
+int kvc_tier_sync(kvc_ctx* ctx) {
+  return guard([&] { F(ctx).tier_sync(); });
+}
+
+int kvc_tier_stats(kvc_ctx* ctx, int64_t* out) {
+  return guard([&] { F(ctx).tier_stats(out); });
+}
+
+int kvc_debug_tier_check(kvc_ctx* ctx, int64_t* out) {
+  return guard([&] { F(ctx).tier_check(out); });
+}
+
+int kvc_cluster_tier(kvc_ctx* ctx, int64_t id, int64_t* out) {
+  return guard([&] { F(ctx).cluster_tier(id, out); });
 }
 
 int64_t kvc_launch_count(kvc_ctx* ctx) { return ctx->impl->launches(); }

@@ -86,6 +86,13 @@ Context::Context(const kvc_cfg& cfg, int d, int L) : cfg_(cfg), d_(d), L_(L) {
 
 Context::~Context() {
   if (st_) cudaStreamSynchronize(st_);
+  if (xs_) {
+    cudaStreamSynchronize(xs_);
+    cudaStreamDestroy(xs_);
+  }
+  for (const TierBatch& b : tier_fl_)
+    if (b.ev) cudaEventDestroy(b.ev);
+  for (cudaEvent_t e : tier_ev_free_) cudaEventDestroy(e);
   for (void* p : dev_allocs_) cudaFree(p);
   for (void* p : host_allocs_) cudaFreeHost(p);
   for (auto& e : ev_) cudaEventDestroy(e);
@@ -145,6 +152,8 @@ void Context::alloc_device() {
   const std::int64_t ring_pages = L * t_.W * t_.rpp;
   t_.max_pages = cfg_.max_pages > 0 ? cfg_.max_pages : cfg_.pool_bytes / t_.page_bytes;
   if (t_.max_pages <= ring_pages + 16) fail(-21, "page pool too small for the window ring");
+  t_.max_hpages = cfg_.host_pool_bytes > 0 ? cfg_.host_pool_bytes / t_.page_bytes : 0;
+  if (t_.max_pages + t_.max_hpages >= (1LL << 31)) fail(-10, "page pool + host tier exceed 2^31 pages");
 
   t_.rep64 = static_cast<double*>(dalloc(S * d * 8));
   t_.rep32 = static_cast<float*>(dalloc(S * d * 4));
@@ -163,7 +172,7 @@ void Context::alloc_device() {
   t_.pages = static_cast<std::int32_t*>(dalloc(S * t_.maxp * 4));
   t_.nbpages = static_cast<std::int32_t*>(dalloc(S * 4));
   t_.bpages = static_cast<std::int32_t*>(dalloc(S * t_.maxbp * 4));
-  t_.pg_fill = static_cast<std::int32_t*>(dalloc(t_.max_pages * 4));
+  t_.pg_fill = static_cast<std::int32_t*>(dalloc((t_.max_pages + t_.max_hpages) * 4));
   t_.free_stack = static_cast<std::int32_t*>(dalloc(t_.max_pages * 4));
   t_.free_top = static_cast<std::int32_t*>(dalloc(16));
   t_.pool = static_cast<std::uint8_t*>(dalloc(static_cast<std::size_t>(t_.max_pages) * t_.page_bytes));
@@ -178,6 +187,7 @@ void Context::alloc_device() {
   t_.pl_pool_cap = S * 4 + 1024;
   t_.pl_pool = static_cast<std::int32_t*>(dalloc(t_.pl_pool_cap * 4));
   h_err_ = static_cast<std::int32_t*>(halloc(16));
+  tier_alloc();
 
   // page stack: ring pages are [0, ring_pages); the stack holds the rest
   {
@@ -330,6 +340,7 @@ void Context::ensure_idx(std::int64_t n, std::int64_t runs) {
 
 void Context::debug_assign_check(const void* keys, int T, std::int64_t pid, int mem, double* out) {
   if (T < 1 || T > t_.tmax) fail(-10, "tokens per frame outside [1, max_tokens]");
+  tier_kick();
   if (pid < 0 || pid >= static_cast<std::int64_t>(parts_.size())) fail(-3, "unknown partition");
   flush_pending();
   const std::size_t row = static_cast<std::size_t>(T) * d_ * es_;
@@ -422,6 +433,7 @@ void Context::check_err_word(std::int32_t e) {
   if (e & DERR_CLUSTER_PAGES) fail(-21, "cluster exceeds max_cluster_pages / max_buffer_pages");
   if (e & DERR_CANDIDATES) fail(-21, "more candidates than max_candidates");
   if (e & DERR_ITEMS) fail(-21, "attention work list overflow");
+  if (e & DERR_TIER) fail(-11, "host-tier page outside its cluster's extent");
   fail(-1, "device error");
 }
 
@@ -510,7 +522,8 @@ void Context::drop_cluster(std::int64_t id) {
   layer_live_count_[static_cast<std::size_t>(c.layer)] -= 1;
   n_live_ -= 1;
   std::int32_t s = c.slot;
-  launches_ += launch_free_slot_pages(t_, s, st_);
+  launches_ += launch_free_slot_pages(t_, s, st_);  // HBM pages only
+  tier_forget(id);                                  // the host-tier extent
   slot_id_[static_cast<std::size_t>(s)] = -1;
   free_slots_.push_back(s);
   clusters_[static_cast<std::size_t>(id)].reset();
@@ -641,6 +654,7 @@ double Context::fetch(std::int64_t id, int cause) {  // store.cpp:95-113
     device_entries_ += moved;
   }
   set_flag(id, CF_HOST, false);
+  tier_note(id, false);  // physical: the host extent comes back to HBM (context_tiers.cpp)
   c.device_tail = 0;
   min_lt_ = std::min(min_lt_, c.last_touch);
   resid_h_[static_cast<std::size_t>(c.slot)] = 0;
@@ -660,6 +674,7 @@ double Context::offload(std::int64_t id) {  // store.cpp:115-130
     device_entries_ -= moved;
   }
   set_flag(id, CF_HOST, true);
+  tier_note(id, true);  // physical: member pages move to the host tier (context_tiers.cpp)
   c.device_tail = 0;
   resid_h_[static_cast<std::size_t>(c.slot)] = 1;
   resid_dirty_ = true;
@@ -799,6 +814,7 @@ void Context::ingest_frame(std::int64_t frame_id, const float* visual, const voi
                            const void* values, int T, int mem, std::int64_t* assigned,
                            std::int64_t* partition) {
   if (T < 1 || T > t_.tmax) fail(-10, "tokens per frame outside [1, max_tokens]");
+  tier_kick();
   if (!visual || !keys || !values) fail(-10, "null frame buffer");
   if (assigned) std::fill(assigned, assigned + static_cast<std::int64_t>(L_) * T, -1);
   if (partition) *partition = -1;
@@ -846,6 +862,7 @@ void Context::ingest_frame(std::int64_t frame_id, const float* visual, const voi
   frames_seen_ += 1;
   repin();
   apply_cadence(frame_id, pid);
+  tier_kick();
 }
 
 // Runs on_insert for every (layer, token) of the frame in layer-major order
@@ -1335,6 +1352,7 @@ void Context::build_now() {  // engine.cpp:77-93 + build_index (index.cpp:364-45
   }
   repin();
   apply_cadence(last, -1);
+  tier_kick();
   if (cfg_.check_invariants) check();
 }
 

@@ -18,6 +18,7 @@
 #include <vector>
 
 #include "../../include/kvc.h"
+#include "extent_alloc.hpp"
 #include "kvc_core.hpp"
 
 namespace kvc {
@@ -186,6 +187,12 @@ class Context {
   // violations, exact mismatches, the margin the resolve kernels assume.
   void debug_assign_check(const void* keys, int T, std::int64_t pid, int mem, double* out);
   void resolve_profile(double* out);  // mean clock64 cycles per resolve phase over domains
+  // physical host tier (context_tiers.cpp): migrations follow the logical residence
+  void tier_kick();  // polls in-flight migrations, starts queued ones (never blocks)
+  void tier_sync();  // completes everything queued or in flight
+  void tier_stats(std::int64_t* out) const;
+  void cluster_tier(std::int64_t id, std::int64_t* out) const;
+  void tier_check(std::int64_t* out);
 
  private:
   // ---- configuration
@@ -261,6 +268,41 @@ class Context {
   double step_t_[10] = {0};
   double ingest_t_[8] = {0};  // last frame: device us (cands, approx, topm, resolve, store), host us (wait, replay, rest)
   std::int64_t launches_ = 0;
+
+  // ---- physical host tier (context_tiers.cpp)
+  struct Extent {
+    std::int64_t start = -1, n = 0;
+  };
+  struct TierBatch {
+    int kind = 0;   // 0 offload, 1 fetch
+    int phase = 0;  // offload: 0 count, 1 copy, 2 commit; fetch: 0 copy, 1 commit
+    int ring = 0;   // mapped argument slot
+    std::vector<std::int64_t> ids;
+    std::vector<Extent> ext, stage;  // new host extent (offload) / staging run per cluster
+    cudaEvent_t ev = nullptr;
+  };
+  static constexpr int kTierRing = 8, kTierMaxBatch = 2048;
+  ExtentAlloc hext_alloc_, stage_alloc_;
+  std::vector<Extent> hext_;              // by cluster id: extent referenced by its page list
+  std::vector<std::uint8_t> tier_busy_;   // by cluster id: in a batch
+  std::vector<std::int64_t> off_q_, fet_q_;
+  std::deque<TierBatch> tier_fl_;
+  std::vector<cudaEvent_t> tier_ev_free_;
+  bool tier_ring_used_[kTierRing] = {};
+  TierMove* tier_mv_ = nullptr;        // [kTierRing][kTierMaxBatch] pinned, mapped
+  std::int32_t* tier_cnt_ = nullptr;   // [kTierRing][kTierMaxBatch] pinned, mapped (slots / counts)
+  std::int32_t* tier_scratch_ = nullptr;  // [kTierMaxBatch][maxp] device (fetch commit)
+  std::uint8_t* tier_stage_ = nullptr;    // HBM staging pages
+  cudaStream_t xs_ = nullptr;             // transfer stream (copy engines)
+  std::int64_t tier_n_[6] = {0, 0, 0, 0, 0, 0};  // offloads, fetches, bytes d2h, bytes h2d, batches, -
+  void tier_alloc();
+  void tier_note(std::int64_t id, bool to_host);  // a logical residence change (offload / fetch)
+  void tier_forget(std::int64_t id);              // the cluster is being removed
+  void tier_ensure(std::int64_t id);
+  bool tier_start();                              // starts one batch from the queues
+  bool tier_advance(TierBatch& b, bool block);    // next phase; true when the batch finished
+  int tier_ring_take();
+  cudaEvent_t tier_event();
 
   // ---- host control plane
   std::vector<std::unique_ptr<Cluster>> clusters_;  // by id (dense, null when removed)

@@ -274,6 +274,7 @@ void Context::replay_decode(const void* hblock, const std::int64_t* gt, int n_gt
   }
   const auto th2 = std::chrono::steady_clock::now();
   repin();  // engine.cpp:234
+  tier_kick();  // migrations for this step's fetches / evictions (asynchronous)
   if (cfg_.check_invariants) check();
   step_t_[7] = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - th2).count();
 }

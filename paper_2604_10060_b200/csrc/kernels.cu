@@ -80,7 +80,7 @@ __device__ bool warp_append(const DevTables& t, int slot, bool to_buf, const uin
                        : t.pages + static_cast<int64_t>(slot) * t.maxp;
     const int cap = to_buf ? t.maxbp : t.maxp;
     const int n = *np;
-    page = n > 0 ? list[n - 1] : -1;
+    page = n > (to_buf ? 0 : t.seal[slot]) ? list[n - 1] : -1;  // sealed pages take no rows
     if (page < 0 || t.pg_fill[page] >= t.P) {
       if (n >= cap) {
         set_err(t, DERR_CLUSTER_PAGES);
@@ -382,7 +382,7 @@ __device__ int hot_load(const DevTables& t, ResolveShared& S, double* hrep, doub
     S.hdirty[h] = 0;
     const int np = t.npages[slot], nbp = t.nbpages[slot];
     S.hnp[h] = np;
-    S.hlast[h] = np > 0 ? t.pages[static_cast<int64_t>(slot) * t.maxp + np - 1] : -1;
+    S.hlast[h] = np > t.seal[slot] ? t.pages[static_cast<int64_t>(slot) * t.maxp + np - 1] : -1;
     S.hfill[h] = S.hlast[h] >= 0 ? t.pg_fill[S.hlast[h]] : t.P;
     S.hbnp[h] = nbp;
     S.hblast[h] = nbp > 0 ? t.bpages[static_cast<int64_t>(slot) * t.maxbp + nbp - 1] : -1;
@@ -1003,7 +1003,16 @@ __global__ void k_gather_cluster(DevTables t, int slot, int with_buf, uint8_t* s
   const int page = isb ? t.bpages[static_cast<int64_t>(slot) * t.maxbp + j]
                        : t.pages[static_cast<int64_t>(slot) * t.maxp + j];
   const int fill = t.pg_fill[page];
-  const int64_t first = row0 + (isb ? nmem : 0) + static_cast<int64_t>(j) * t.P;
+  // member pages may be partial mid-list (sealed by an offload): rows before page j = sum of fills
+  __shared__ int before;
+  if (threadIdx.x == 0) {
+    int r = 0;
+    const int* list = isb ? t.bpages + static_cast<int64_t>(slot) * t.maxbp : t.pages + static_cast<int64_t>(slot) * t.maxp;
+    for (int i = 0; i < j; ++i) r += t.pg_fill[list[i]];
+    before = r;
+  }
+  __syncthreads();
+  const int64_t first = row0 + (isb ? nmem : 0) + before;
   const int rb = t.d * t.es;
   const uint8_t* pk = page_k(t, page);
   const uint8_t* pv = page_v(t, page);
@@ -1014,16 +1023,26 @@ __global__ void k_gather_cluster(DevTables t, int slot, int with_buf, uint8_t* s
 }
 
 __global__ void k_free_slot(DevTables t, int slot) {
+  // HBM pages return to the free stack; host-tier pages belong to an extent the host frees
   const int np = t.npages[slot], nbp = t.nbpages[slot];
-  __shared__ int base;
-  if (threadIdx.x == 0) base = atomicAdd(t.free_top, np + nbp);
+  __shared__ int base, nh;
+  if (threadIdx.x == 0) {
+    int h = 0;
+    for (int i = 0; i < np; ++i) h += is_host_page(t, t.pages[static_cast<int64_t>(slot) * t.maxp + i]) ? 1 : 0;
+    nh = h;
+    base = atomicAdd(t.free_top, np - h + nbp);
+    int k = 0;
+    for (int i = 0; i < np; ++i) {
+      const int pg = t.pages[static_cast<int64_t>(slot) * t.maxp + i];
+      if (!is_host_page(t, pg)) t.free_stack[base + k++] = pg;
+    }
+  }
   __syncthreads();
-  for (int i = threadIdx.x; i < np; i += blockDim.x)
-    t.free_stack[base + i] = t.pages[static_cast<int64_t>(slot) * t.maxp + i];
   for (int i = threadIdx.x; i < nbp; i += blockDim.x)
-    t.free_stack[base + np + i] = t.bpages[static_cast<int64_t>(slot) * t.maxbp + i];
+    t.free_stack[base + np - nh + i] = t.bpages[static_cast<int64_t>(slot) * t.maxbp + i];
   __syncthreads();
   if (threadIdx.x == 0) {
+    t.seal[slot] = 0;
     t.npages[slot] = 0;
     t.nbpages[slot] = 0;
     t.nmem[slot] = 0;

@@ -45,6 +45,7 @@ enum DevErr : int32_t {
   DERR_CLUSTER_PAGES = 4,
   DERR_CANDIDATES = 8,  // more candidates than max_candidates
   DERR_ITEMS = 16,      // attention work list overflow
+  DERR_TIER = 32,       // a host-tier page outside its cluster's extent
 };
 
 // ----------------------------------------------------------------------------- device state
@@ -75,10 +76,18 @@ struct DevTables {
   int32_t* pages;  // [S][maxp]
   int32_t* nbpages;
   int32_t* bpages; // [S][maxbp]
-  int32_t* pg_fill;     // [max_pages] rows used in each page
+  int32_t* pg_fill;     // [max_pages + max_hpages] rows used in each page (HBM, then host tier)
   int32_t* free_stack;  // [max_pages]
   int32_t* free_top;    // [1]
-  uint8_t* pool;        // page pool
+  uint8_t* pool;        // page pool (HBM)
+  // host tier (TieredStore Host residence, store.cpp:95-130): pinned, mapped host pages in the
+  // same page format. Page ids >= max_pages name host page (id - max_pages); every kernel reaches
+  // them through page_k/page_v, so attention over a not-yet-fetched cluster reads host memory.
+  uint8_t* hpool;
+  int64_t max_hpages;
+  // [S] leading member pages that are sealed (moved to / copied for the host tier): appends
+  // never write into them, so an offload's snapshot stays valid while its copy is in flight
+  int32_t* seal;
   // window ring (engine.cpp:54-65): W frame slots per domain, each ceil(tmax/P) pages
   int32_t* ring_pages;  // [L][W][rpp]
   int32_t* ring_owner;  // [L][W][tmax] owning slot of each window token (-1 none)
@@ -99,12 +108,15 @@ struct DevTables {
   int32_t* err;  // [1] DevErr bits
 };
 
+inline __host__ __device__ bool is_host_page(const DevTables& t, int32_t page) {
+  return page >= t.max_pages;
+}
 inline __host__ __device__ uint8_t* page_k(const DevTables& t, int32_t page) {
-  return t.pool + static_cast<int64_t>(page) * t.page_bytes;
+  return page < t.max_pages ? t.pool + static_cast<int64_t>(page) * t.page_bytes
+                            : t.hpool + (static_cast<int64_t>(page) - t.max_pages) * t.page_bytes;
 }
 inline __host__ __device__ uint8_t* page_v(const DevTables& t, int32_t page) {
-  return t.pool + static_cast<int64_t>(page) * t.page_bytes +
-         static_cast<int64_t>(t.P) * t.d * t.es;
+  return page_k(t, page) + static_cast<int64_t>(t.P) * t.d * t.es;
 }
 
 // ----------------------------------------------------------------------------- ingest
@@ -225,6 +237,26 @@ struct AppendRun {
 int launch_append_runs(const DevTables& t, const AppendRun* runs, int32_t n_runs,
                        const int32_t* idx, const void* stage_k, const void* stage_v,
                        cudaStream_t st);
+
+// ---- host tier migrations (tiers.cu). One entry per cluster of a batch.
+struct TierMove {
+  int32_t slot, n_pages;  // pages [0, n_pages) of the member list move
+  int64_t stage0;         // first staging page of the cluster's contiguous copy
+  int64_t host0;          // first host page of the cluster's extent
+};
+// Offload, step 1: npages of each slot -> out[i] (for extent sizing).
+int launch_tier_count(const DevTables& t, const int32_t* slots, int32_t n, int32_t* out, cudaStream_t st);
+// Offload, step 2: pages [0, n_pages) of each slot (HBM or host) -> staging, seals them.
+int launch_tier_gather(const DevTables& t, const TierMove* mv, int32_t n, int32_t max_pages_per_cluster,
+                       uint8_t* stage, cudaStream_t st);
+// Offload, step 3 (after the staging -> host copies completed): member pages [0, n_pages) become
+// host pages host0 + i; their HBM pages return to the free stack.
+int launch_tier_commit_offload(const DevTables& t, const TierMove* mv, int32_t n, cudaStream_t st);
+// Fetch (after the host extent -> staging copies completed): every host page of the slot's member
+// list gets a fresh HBM page filled from staging page stage0 + (id - max_pages - host0).
+// scratch: [n][maxp] int32 (new page ids between the copy and the table pass).
+int launch_tier_commit_fetch(const DevTables& t, const TierMove* mv, int32_t n, int32_t max_pages_per_cluster,
+                             const uint8_t* stage, int32_t* scratch, cudaStream_t st);
 
 // Gathers a cluster's members (then its buffer) into staging rows [n][d] K and V.
 int launch_gather_cluster(const DevTables& t, int32_t slot, int32_t include_buffer,

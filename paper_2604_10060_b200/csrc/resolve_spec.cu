@@ -411,7 +411,7 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve_spec(DevTables t, Ing
       S.ts_dbmax[ts] = 0ull;
       S.ts_fb[ts] = INT_MAX;
       const int np = t.npages[s], nbp = t.nbpages[s];
-      const int last = np > 0 ? t.pages[static_cast<int64_t>(s) * t.maxp + np - 1] : -1;
+      const int last = np > t.seal[s] ? t.pages[static_cast<int64_t>(s) * t.maxp + np - 1] : -1;
       const int blast = nbp > 0 ? t.bpages[static_cast<int64_t>(s) * t.maxbp + nbp - 1] : -1;
       S.ts_np0[ts] = np;
       S.ts_nbp0[ts] = nbp;
