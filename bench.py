@@ -54,6 +54,7 @@ def parse():
     p.add_argument("--frames", type=int, default=0, help="timed ingest frames (default = steps)")
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-offload", action="store_true", help="skip the config-3 host-tier measurement")
     p.add_argument("--domains", type=int, default=D_TOTAL)
     return p.parse_args()
 
@@ -368,10 +369,102 @@ def main():
     }
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args)
+    if world == 1 and not args.no_offload:
+        del kv, q_dev, out_dev
+        torch.cuda.empty_cache()
+        try:
+            line["offload"] = offload_phase(args)
+        except Exception as e:  # the host tier needs pinned host RAM; never lose the main line
+            line["offload"] = {"error": f"{type(e).__name__}: {e}"}
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def offload_phase(args):
+    """Config 3 per-GPU shard (14 of 112 domains, as one rank of 8 holds), 1-hour 1 fps stream:
+    705,600 tokens/domain in 1,378 clusters of 512, cold clusters offloaded to pinned host memory
+    by the reference cadence policy (engine.cpp:95-132; horizon 16 frames). Measures decode steps
+    whose selected clusters are cold (K6 attends them in the host tier through the mapping while
+    their fetches migrate on the copy engines), the same steps hot, and host-link GB/s of batched
+    per-cluster migrations (wall clock of kvc_tier_sync, host bookkeeping included)."""
+    import torch
+
+    from paper_2604_10060_b200 import ClusterKVCache, Config, DTYPE_BF16, workload
+
+    D3, N3, C3 = 14, 3600 * T_FRAME, 1378
+    kv_bytes = D3 * (N3 + 64 * C3) * HEAD_DIM * 2 * 2
+    cfg = Config.make(kv_dtype=DTYPE_BF16, k_v=1, k_s=TOP_K, window_frames=WINDOW, build_batch_frames=1,
+                      offload_horizon_frames=16, device_capacity_entries=1 << 40,
+                      pool_bytes=int(1.3 * kv_bytes), host_pool_bytes=int(1.1 * kv_bytes), tier_stage_pages=16384,
+                      max_slots=max(4096, 4 * D3 * C3), max_cluster_pages=512, max_tokens=T_FRAME,
+                      max_candidates=2048)
+    t0 = time.time()
+    kv = ClusterKVCache(cfg, HEAD_DIM, D3)
+    st = workload.clustered_state(D3, N3, C3, HEAD_DIM, T_FRAME, seed=4242)
+    kv.bulk_load(st.visual, st.keys, st.values, st.assign, st.frame_ids, st.token_ids, C3)
+    del st.keys, st.values
+    torch.cuda.empty_cache()
+    setup_s = time.time() - t0
+    # a new frame far past the loaded ones: the cadence offloads every stale cluster
+    fk, fv, fvis, fids = workload.frames_near(st, 1, N3 // T_FRAME + 100)
+    t0 = time.time()
+    kv.process_frame(int(fids[0]), fvis[0], fk[0], fv[0], want_assigned=False)
+    kv.tier_sync()
+    offload_s = time.time() - t0
+    s0 = kv.tier_stats()
+    stream = torch.cuda.ExternalStream(kv.stream)
+    nq = args.warmup + args.steps
+    q_dev = workload.queries_near(st, nq, seed=77)
+    out_dev = torch.zeros(D3, HEAD_DIM, device="cuda")
+
+    def timed():
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for i in range(args.warmup, nq):
+            kv.query(i, q_dev[i], out=out_dev)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        return ev0.elapsed_time(ev1) * 1e3 / args.steps
+
+    for i in range(args.warmup):  # warm-up queries (their clusters become hot; not re-timed cold)
+        kv.query(i, q_dev[i], out=out_dev)
+    kv.tier_sync()
+    s1 = kv.tier_stats()
+    cold_us = timed()
+    s2 = kv.tier_stats()
+    kv.tier_sync()
+    s3 = kv.tier_stats()
+    hot_us = timed()  # the same queries: their clusters now sit in HBM
+    # host-link bandwidth of batched migrations: the clusters the timed steps fetched go out and back
+    ids = kv.cluster_ids()
+    moved = [c for c in ids if kv.cluster(c)[0][6] == 0][:2048]
+    t0 = time.time()
+    for c in moved:
+        kv.offload(c)
+    kv.tier_sync()
+    d2h_s = time.time() - t0
+    s4 = kv.tier_stats()
+    t0 = time.time()
+    for c in moved:
+        kv.fetch(c, 1)
+    kv.tier_sync()
+    h2d_s = time.time() - t0
+    s5 = kv.tier_stats()
+    return {
+        "workload": "config3 per-GPU shard: 14 domains x 705,600 tokens (3600 frames x 196), 1,378 clusters/domain, "
+                    "top-16 + 4-frame window, bf16; cold clusters in pinned host memory (cadence horizon 16)",
+        "cold_us_per_step": round(cold_us, 2), "hot_us_per_step": round(hot_us, 2),
+        "cold_fetches_per_step": round((s3["fetches"] - s1["fetches"]) / args.steps, 1),
+        "host_pages_after_cadence": s0["host_pages"], "host_bytes_after_cadence": s0["host_pages"] * 2 * 64 * HEAD_DIM * 2,
+        "offload_wall_s": round(offload_s, 3), "setup_s": round(setup_s, 2),
+        "d2h_gbs_wall": round((s4["bytes_d2h"] - s3["bytes_d2h"]) / max(d2h_s, 1e-9) / 1e9, 2),
+        "h2d_gbs_wall": round((s5["bytes_h2d"] - s4["bytes_h2d"]) / max(h2d_s, 1e-9) / 1e9, 2),
+        "migrated_clusters": len(moved), "in_flight_at_end_of_cold_steps": s2["in_flight"] + s2["queued"],
+        "dma_copies": {"offload_batch": s4["copies"] - s3["copies"], "fetch_batch": s5["copies"] - s4["copies"]},
+    }
 
 
 def cpu_baseline(args):

@@ -208,9 +208,10 @@ KVC_API int kvc_fetch(kvc_ctx* ctx, int64_t id, int32_t cause, double* cost_us);
  * per cluster on a transfer stream (K5), asynchronously. Kernels address pages wherever they
  * physically are, so results never depend on migration progress.
  * kvc_tier_sync completes every queued / in-flight migration (physical == logical residence).
- * kvc_tier_stats out[10]: host pages in use, host-tier capacity (pages), clusters with host pages,
+ * kvc_tier_stats out[12]: host pages in use, host-tier capacity (pages), clusters with host pages,
  * offloads committed, fetches committed, bytes device->host, bytes host->device, migrations
- * queued, batches in flight, HBM staging pages in use. */
+ * queued, batches in flight, HBM staging pages in use, batches started, DMA copies issued
+ * (per-cluster copies merged when both sides are contiguous). */
 KVC_API int kvc_tier_sync(kvc_ctx* ctx);
 KVC_API int kvc_tier_stats(kvc_ctx* ctx, int64_t* out);
 /* out[3]: first host page of the cluster's extent (-1 none), its length in pages, migration busy */

@@ -294,7 +294,7 @@ class Context {
   std::int32_t* tier_scratch_ = nullptr;  // [kTierMaxBatch][maxp] device (fetch commit)
   std::uint8_t* tier_stage_ = nullptr;    // HBM staging pages
   cudaStream_t xs_ = nullptr;             // transfer stream (copy engines)
-  std::int64_t tier_n_[6] = {0, 0, 0, 0, 0, 0};  // offloads, fetches, bytes d2h, bytes h2d, batches, -
+  std::int64_t tier_n_[6] = {0, 0, 0, 0, 0, 0};  // offloads, fetches, bytes d2h, bytes h2d, batches, copies
   void tier_alloc();
   void tier_note(std::int64_t id, bool to_host);  // a logical residence change (offload / fetch)
   void tier_forget(std::int64_t id);              // the cluster is being removed

@@ -28,6 +28,51 @@
 
 namespace kvc {
 
+namespace {
+
+// One copy per cluster, merged with its predecessor when both its staging run and its host extent
+// continue the previous cluster's (first-fit over a quiet allocator hands out consecutive runs), so
+// a batch usually crosses the host link in a few large DMA transfers.
+struct CopyRun {
+  std::int64_t dev, host, n;
+};
+
+void add_run(std::vector<CopyRun>& runs, std::int64_t dev, std::int64_t host, std::int64_t n) {
+  if (!runs.empty() && runs.back().dev + runs.back().n == dev && runs.back().host + runs.back().n == host)
+    runs.back().n += n;
+  else
+    runs.push_back({dev, host, n});
+}
+
+// Submits the runs as one cudaMemcpyBatchAsync (one driver call for the batch; the copy engines
+// pick them up back to back), falling back to one cudaMemcpyAsync per run where unsupported.
+void submit_runs(const std::vector<CopyRun>& runs, std::uint8_t* dev_base, std::uint8_t* host_base,
+                 std::int64_t page_bytes, bool to_host, cudaStream_t st) {
+  if (runs.empty()) return;
+  std::vector<void*> dst(runs.size()), src(runs.size());
+  std::vector<std::size_t> sz(runs.size());
+  for (std::size_t i = 0; i < runs.size(); ++i) {
+    std::uint8_t* d = dev_base + runs[i].dev * page_bytes;
+    std::uint8_t* h = host_base + runs[i].host * page_bytes;
+    dst[i] = to_host ? h : d;
+    src[i] = to_host ? d : h;
+    sz[i] = static_cast<std::size_t>(runs[i].n * page_bytes);
+  }
+  cudaMemcpyAttributes attr{};
+  attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+  attr.flags = cudaMemcpyFlagPreferOverlapWithCompute;
+  std::size_t idx0 = 0, fail_idx = 0;
+  if (runs.size() > 1 &&
+      cudaMemcpyBatchAsync(dst.data(), src.data(), sz.data(), runs.size(), &attr, &idx0, 1, &fail_idx, st) ==
+          cudaSuccess)
+    return;
+  cudaGetLastError();  // clear a not-supported status
+  for (std::size_t i = 0; i < runs.size(); ++i)
+    KVC_CUDA(cudaMemcpyAsync(dst[i], src[i], sz[i], to_host ? cudaMemcpyDeviceToHost : cudaMemcpyHostToDevice, st));
+}
+
+}  // namespace
+
 void Context::tier_alloc() {
   KVC_CUDA(cudaStreamCreateWithFlags(&xs_, cudaStreamNonBlocking));
   t_.seal = static_cast<std::int32_t*>(dalloc(static_cast<std::size_t>(cfg_.max_slots) * 4));
@@ -116,6 +161,10 @@ bool Context::tier_start() {
     b.ring = ring;
     std::vector<std::int64_t> keep;
     const std::uint8_t qbit = kind == 0 ? 2 : 4;
+    if (kind == 1)  // in host-address order: neighbouring extents merge into one DMA transfer
+      std::sort(q.begin(), q.end(), [&](std::int64_t x, std::int64_t y) {
+        return hext_[static_cast<std::size_t>(x)].start < hext_[static_cast<std::size_t>(y)].start;
+      });
     for (std::int64_t id : q) {
       if (!alive(id)) continue;  // removed: its extent was released with it
       std::uint8_t& bz = tier_busy_[static_cast<std::size_t>(id)];
@@ -155,13 +204,15 @@ bool Context::tier_start() {
       launches_ += launch_tier_count(t_, cnt, n, cnt, st_);
       KVC_CUDA(cudaEventRecord(b.ev, st_));
     } else {
+      std::vector<CopyRun> runs;
       for (std::int32_t i = 0; i < n; ++i) {
         const Extent& e = b.ext[static_cast<std::size_t>(i)];
         const Extent& s = b.stage[static_cast<std::size_t>(i)];
         mv[i] = TierMove{C(b.ids[static_cast<std::size_t>(i)]).slot, static_cast<std::int32_t>(e.n), s.start, e.start};
-        KVC_CUDA(cudaMemcpyAsync(tier_stage_ + s.start * t_.page_bytes, t_.hpool + e.start * t_.page_bytes,
-                                 static_cast<std::size_t>(e.n) * t_.page_bytes, cudaMemcpyHostToDevice, xs_));
+        add_run(runs, s.start, e.start, e.n);
       }
+      submit_runs(runs, tier_stage_, t_.hpool, t_.page_bytes, false, xs_);
+      tier_n_[5] += static_cast<std::int64_t>(runs.size());
       KVC_CUDA(cudaEventRecord(b.ev, xs_));
     }
     tier_n_[4] += 1;
@@ -198,13 +249,34 @@ bool Context::tier_advance(TierBatch& b, bool block) {
     b.stage.assign(static_cast<std::size_t>(n), Extent{});
     int moves = 0, failed = 0;
     std::int32_t maxnp = 1;
+    // the batch's extents and staging runs are carved from one run each when the allocators have
+    // room, so the whole batch crosses the link as one DMA transfer
+    std::int64_t total = 0;
+    for (std::int32_t i = 0; i < n; ++i) {
+      const std::int64_t id = b.ids[static_cast<std::size_t>(i)];
+      if (alive(id) && is_host(id) && cnt[i] > 0 && cnt[i] != hext_[static_cast<std::size_t>(id)].n) total += cnt[i];
+    }
+    std::int64_t hbig = total > 0 ? hext_alloc_.alloc(total) : -1;
+    std::int64_t sbig = hbig >= 0 ? stage_alloc_.alloc(total) : -1;
+    if (sbig < 0 && hbig >= 0) {
+      hext_alloc_.release(hbig, total);
+      hbig = -1;
+    }
     for (std::int32_t i = 0; i < n; ++i) {
       const std::int64_t id = b.ids[static_cast<std::size_t>(i)];
       const std::int32_t np = cnt[i];
       mv[i] = TierMove{-1, 0, 0, 0};
       if (!alive(id) || !is_host(id) || np <= 0 || np == hext_[static_cast<std::size_t>(id)].n) continue;
-      const std::int64_t h0 = hext_alloc_.alloc(np);
-      const std::int64_t s0 = h0 >= 0 ? stage_alloc_.alloc(np) : -1;
+      std::int64_t h0, s0;
+      if (hbig >= 0) {
+        h0 = hbig;
+        s0 = sbig;
+        hbig += np;
+        sbig += np;
+      } else {
+        h0 = hext_alloc_.alloc(np);
+        s0 = h0 >= 0 ? stage_alloc_.alloc(np) : -1;
+      }
       if (s0 < 0) {  // tier or staging full: retry after in-flight batches release space
         if (h0 >= 0) hext_alloc_.release(h0, np);
         tier_note(id, true);
@@ -223,13 +295,14 @@ bool Context::tier_advance(TierBatch& b, bool block) {
     launches_ += launch_tier_gather(t_, mv, n, maxnp, tier_stage_, st_);
     KVC_CUDA(cudaEventRecord(b.ev, st_));
     KVC_CUDA(cudaStreamWaitEvent(xs_, b.ev, 0));
+    std::vector<CopyRun> runs;
     for (std::int32_t i = 0; i < n; ++i) {
       if (mv[i].slot < 0) continue;
-      const Extent& e = b.ext[static_cast<std::size_t>(i)];
-      const Extent& s = b.stage[static_cast<std::size_t>(i)];
-      KVC_CUDA(cudaMemcpyAsync(t_.hpool + e.start * pb, tier_stage_ + s.start * pb,
-                               static_cast<std::size_t>(e.n) * pb, cudaMemcpyDeviceToHost, xs_));
+      add_run(runs, b.stage[static_cast<std::size_t>(i)].start, b.ext[static_cast<std::size_t>(i)].start,
+              b.ext[static_cast<std::size_t>(i)].n);
     }
+    submit_runs(runs, tier_stage_, t_.hpool, pb, true, xs_);
+    tier_n_[5] += static_cast<std::int64_t>(runs.size());
     KVC_CUDA(cudaEventRecord(b.ev, xs_));
     b.phase = 1;
     return false;
@@ -328,6 +401,8 @@ void Context::tier_stats(std::int64_t* out) const {
   out[7] = static_cast<std::int64_t>(off_q_.size() + fet_q_.size());
   out[8] = static_cast<std::int64_t>(tier_fl_.size());
   out[9] = stage_alloc_.used();
+  out[10] = tier_n_[4];
+  out[11] = tier_n_[5];
 }
 
 void Context::cluster_tier(std::int64_t id, std::int64_t* out) const {
