@@ -70,7 +70,8 @@ Context::Context(const kvc_cfg& cfg, int d, int L) : cfg_(cfg), d_(d), L_(L) {
   if (cfg_.visual_floor < -1.0 || cfg_.visual_floor > 1.0) fail(-10, "visual floor must be a cosine value");
   if (cfg_.token_mode) fail(-10, "token-baseline mode is served by the token ablation entry points");
   if (cfg_.kv_dtype != KVC_DTYPE_F32 && cfg_.kv_dtype != KVC_DTYPE_BF16) fail(-10, "kv_dtype");
-  if (cfg_.page_tokens < 8 || cfg_.page_tokens > 256 || cfg_.page_tokens % 8) fail(-10, "page_tokens");
+  // (<= 64: a window page's dedup mask is one 64-bit word of its attention descriptor)
+  if (cfg_.page_tokens < 8 || cfg_.page_tokens > 64 || cfg_.page_tokens % 8) fail(-10, "page_tokens must be 8..64, a multiple of 8");
   if (d % 8 != 0 || d > 256) fail(-10, "the device path supports d % 8 == 0 and d <= 256");
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
@@ -293,13 +294,17 @@ void Context::alloc_device() {
   da_.part_ml = static_cast<float*>(dalloc(L * da_.max_items * 2 * 4));
   da_.part_o = static_cast<float*>(dalloc(L * da_.max_items * d * 4));
   da_.dom_done = static_cast<std::int32_t*>(dalloc(L * 4));
-  da_.k4prof = static_cast<long long*>(dalloc(L * 8 * 8));
+  da_.k4prof = static_cast<long long*>(dalloc(L * 16 * 8));
   da_.work_ctr = static_cast<std::int32_t*>(dalloc(64));
   da_.k_v = kv;
   da_.k_s = ks;
   da_.prefetch_k = kp;
   da_.prefetch = cfg_.prefetch_enabled;
   da_.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(d)));
+  {
+    const char* e = std::getenv("KVC_ATT_DEBUG");  // bit 0: attention consumers skip the math
+    da_.debug_flags = e ? std::atoi(e) : 0;
+  }
   d_q_ = static_cast<float*>(dalloc(L * d * 4));
   d_out_ = static_cast<float*>(dalloc(L * d * 4));
   KVC_CUDA(cudaStreamSynchronize(st_));
@@ -405,7 +410,7 @@ void Context::set_result_block(int b) {
 
 void Context::resolve_profile(double* out) {
   const bool dec = out[0] < 0;
-  const int W = dec ? 8 : 16;  // K4: [L][8]; resolve: [L][16]
+  const int W = 16;  // K4 and resolve: [L][16]
   std::vector<long long> p(static_cast<std::size_t>(L_) * W);
   KVC_CUDA(cudaMemcpy(p.data(), dec ? da_.k4prof : ia_.prof, p.size() * 8, cudaMemcpyDeviceToHost));
   for (int k = 0; k < 16; ++k) {

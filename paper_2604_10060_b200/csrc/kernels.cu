@@ -1331,7 +1331,7 @@ __global__ void __launch_bounds__(256) k_score_select(DevTables t, DecodeArgs a,
   __shared__ long long skey[K4_ROWS];
 
   long long kc0 = clock64();
-#define K4MARK(k) if (a.k4prof && threadIdx.x == 0) { const long long kc1 = clock64(); a.k4prof[l * 8 + (k)] = kc1 - kc0; kc0 = kc1; }
+#define K4MARK(k) if (a.k4prof && threadIdx.x == 0) { const long long kc1 = clock64(); a.k4prof[l * 16 + (k)] = kc1 - kc0; kc0 = kc1; }
   if (l == 0 && threadIdx.x == 0) *work_ctr = 0;
   const float* q = a.q + static_cast<int64_t>(l) * d;
   for (int i = threadIdx.x; i < d; i += blockDim.x) {
@@ -1555,6 +1555,7 @@ __global__ void __launch_bounds__(256) k_score_select(DevTables t, DecodeArgs a,
   // ---- verified (dedup in rank order, retrieval.cpp:20-26), attended count, page descriptors
   __shared__ int vnp[64], vnbp[64], voff[65];
   __shared__ int ring_cnt[64], ring_off[65];
+  __shared__ unsigned long long ring_mask[64];
   if (threadIdx.x == 0) {
     int nv = 0;
     for (int i = 0; i < n_rank_s; ++i) {
@@ -1577,7 +1578,10 @@ __global__ void __launch_bounds__(256) k_score_select(DevTables t, DecodeArgs a,
     atomicAdd(&att_s, static_cast<unsigned long long>(t.nmem[s] + t.nbuf[s]));
     if (t.lazy[s]) lazy_any = 1;  // a pending split: the host must settle before the next step
   }
-  if (threadIdx.x < 64) ring_cnt[threadIdx.x] = 0;
+  if (threadIdx.x < 64) {
+    ring_cnt[threadIdx.x] = 0;
+    ring_mask[threadIdx.x] = 0ull;
+  }
   __syncthreads();
   if (threadIdx.x == 0) a.flags[l] = lazy_any;
   K4MARK(4)
@@ -1600,6 +1604,11 @@ __global__ void __launch_bounds__(256) k_score_select(DevTables t, DecodeArgs a,
       if (km) {
         const unsigned same = __match_any_sync(kFull, pg);
         if (keep && pg < 64 && (threadIdx.x & 31) == __ffs(same) - 1) atomicAdd(&ring_cnt[pg], __popc(same));
+        const unsigned long long bit = keep ? 1ull << (tt % t.P) : 0ull;  // one shared atomic per (warp, page)
+        const unsigned blo = __reduce_or_sync(same, static_cast<unsigned>(bit));
+        const unsigned bhi = __reduce_or_sync(same, static_cast<unsigned>(bit >> 32));
+        if (keep && pg < 64 && (threadIdx.x & 31) == __ffs(same) - 1)
+          atomicOr(&ring_mask[pg], (static_cast<unsigned long long>(bhi) << 32) | blo);
       }
     }
 #pragma unroll
@@ -1639,13 +1648,14 @@ __global__ void __launch_bounds__(256) k_score_select(DevTables t, DecodeArgs a,
     const bool isb = k >= vnp[j];
     const int page = isb ? t.bpages[static_cast<int64_t>(s) * t.maxbp + (k - vnp[j])]
                          : t.pages[static_cast<int64_t>(s) * t.maxp + k];
-    desc[i] = make_int4(page, t.pg_fill[page], isb ? 1 : 0, 0);
+    desc[i] = make_int4(page, t.pg_fill[page] | ((isb ? 1 : 0) << 16), -1, -1);
   }
   for (int i = threadIdx.x; i < W * rpp && i < 64; i += blockDim.x)
     if (ring_cnt[i] > 0 && ring_off[i] < a.max_desc) {
       const int rs = i / rpp, j = i % rpp;
       const int page = t.ring_pages[(static_cast<int64_t>(l) * W + rs) * rpp + j];
-      desc[ring_off[i]] = make_int4(page, t.pg_fill[page], 2 | (rs << 8), j * t.P);
+      desc[ring_off[i]] = make_int4(page, t.pg_fill[page] | (2 << 16), static_cast<int>(ring_mask[i] & 0xffffffffu),
+                                    static_cast<int>(ring_mask[i] >> 32));
     }
   __syncthreads();
   K4MARK(6)
@@ -1656,6 +1666,60 @@ __global__ void __launch_bounds__(256) k_score_select(DevTables t, DecodeArgs a,
   }
   if (a.n_items[l] == 0)  // nothing attended: output zeros
     for (int i = threadIdx.x; i < d; i += blockDim.x) a.out[static_cast<int64_t>(l) * d + i] = 0.f;
+}
+
+// Block-wide exclusive scan of one int per thread (blockDim.x a multiple of 32, <= 1024);
+// `tot` (>= 32 ints of shared scratch) receives the warp totals. Returns the thread's prefix;
+// *total gets the block sum. Two barriers.
+__device__ __forceinline__ int block_excl_scan(int v, int* tot, int* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(kFull, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) tot[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    int w = lane < nw ? tot[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(kFull, w, o);
+      if (lane >= o) w += y;
+    }
+    if (lane < nw) tot[lane] = w;  // inclusive warp prefix
+  }
+  __syncthreads();
+  const int before = warp > 0 ? tot[warp - 1] : 0;
+  *total = tot[nw - 1];
+  return before + x - v;
+}
+
+// The value of the entry of rank `kth` under (v desc, key asc) among n float entries (keys unique):
+// rank counting with `sp` threads per entry (partial counts combined by shuffles), so n = 256
+// candidates cost 256 / sp broadcast shared reads per thread. Writes *out; ends with a barrier.
+__device__ void block_kth_value(const float* v, const long long* key, int n, int kth, float* out) {
+  int sp = 1;
+  while (sp < 32 && n * sp * 2 <= static_cast<int>(blockDim.x)) sp <<= 1;
+  const int groups = blockDim.x / sp;
+  const int part = threadIdx.x & (sp - 1);
+  for (int base = 0; base < n; base += groups) {
+    const int i = base + static_cast<int>(threadIdx.x) / sp;
+    int r = 0;
+    float vi = 0.f;
+    if (i < n) {
+      vi = v[i];
+      const long long ki = key[i];
+      for (int j = part; j < n; j += sp) {
+        const float vj = v[j];
+        r += (vj > vi || (vj == vi && key[j] < ki)) ? 1 : 0;
+      }
+    }
+    for (int o = sp >> 1; o > 0; o >>= 1) r += __shfl_xor_sync(kFull, r, o);
+    if (i < n && part == 0 && r == kth) *out = vi;
+  }
+  __syncthreads();
 }
 
 // ============================================================================ K4 (v2)
@@ -1716,9 +1780,11 @@ __global__ void __launch_bounds__(K4T) k_score_select2(DevTables t, DecodeArgs a
   __shared__ long long skey[K4_SMAX];
   __shared__ int vhash[128];
   __shared__ float red32[K4W];
+  __shared__ int red_i[32];
+  __shared__ float kth_s;
 
   long long kc0 = clock64();
-#define K4MARK(k) if (a.k4prof && tid == 0) { const long long kc1 = clock64(); a.k4prof[l * 8 + (k)] = kc1 - kc0; kc0 = kc1; }
+#define K4MARK(k) if (a.k4prof && tid == 0) { const long long kc1 = clock64(); a.k4prof[l * 16 + (k)] = kc1 - kc0; kc0 = kc1; }
   if (l == 0 && tid == 0) *work_ctr = 0;
   const float* q = a.q + static_cast<int64_t>(l) * d;
   float qsq = 0.f;
@@ -1801,10 +1867,10 @@ __global__ void __launch_bounds__(K4T) k_score_select2(DevTables t, DecodeArgs a
   }
   __syncthreads();
   const int kv = min(a.k_v, P);
-  if (P <= 1024)
-    block_topk(sim, key, pay, P, kv, chosen);
-  else
+  if (P <= 256 || P > 1024)  // rank counting: one barrier, P^2 / 512 broadcast reads per thread
     block_rank_select(sim, key, P, kv, chosen);
+  else
+    block_topk(sim, key, pay, P, kv, chosen);
   if (tid < kv) a.parts[l * a.k_v + tid] = chosen[tid];
   if (tid == 0) a.n_parts_sel[l] = kv;
   K4MARK(1)
@@ -1814,29 +1880,36 @@ __global__ void __launch_bounds__(K4T) k_score_select2(DevTables t, DecodeArgs a
   for (int pass = 0; pass < passes; ++pass) {
     const int layer = l + pass;
     const int ktake = pass == 0 ? a.k_s : a.prefetch_k;
-    if (tid == 0) ncand_s = 0;
-    __syncthreads();
+    // candidate list in per_layer_clusters order (live entry, then its registered buffer):
+    // compacted with a block scan (no per-candidate shared atomics)
+    int ncand = 0;
     for (int i = 0; i < kv; ++i) {
       const int64_t pk = static_cast<int64_t>(chosen[i]) * L + layer;
       const int off = t.pl_off[pk], cnt = t.pl_cnt[pk];
-      for (int j = tid; j < cnt; j += K4T) {
-        const int s = t.pl_pool[off + j];
-        const int lz = t.lazy[s];
-        const int k = atomicAdd(&ncand_s, lz ? 2 : 1);
-        if (k + (lz ? 2 : 1) > cmax) {
-          set_err(t, DERR_CANDIDATES);
-          continue;
+      for (int j0 = 0; j0 < cnt; j0 += K4T) {
+        const int j = j0 + tid;
+        const int s = j < cnt ? t.pl_pool[off + j] : -1;
+        const int lz = s >= 0 ? t.lazy[s] : 0;
+        int tot;
+        const int k = ncand + block_excl_scan(s >= 0 ? (lz ? 2 : 1) : 0, red_i, &tot);
+        if (s >= 0) {
+          if (k + (lz ? 2 : 1) > cmax) {
+            set_err(t, DERR_CANDIDATES);
+          } else {
+            cslot[k] = s;
+            cbuf[k] = 0;
+            if (lz) {
+              cslot[k + 1] = s;
+              cbuf[k + 1] = 1;
+            }
+          }
         }
-        cslot[k] = s;
-        cbuf[k] = 0;
-        if (lz) {
-          cslot[k + 1] = s;
-          cbuf[k + 1] = 1;
-        }
+        ncand += tot;
+        __syncthreads();  // red_i reuse
       }
     }
     __syncthreads();
-    const int nc = min(ncand_s, cmax);
+    const int nc = min(ncand, cmax);
     if (pass == 0 && tid == 0) a.n_cand[l] = nc;
     const int take = min(ktake, nc);
     // (A) approximate cosines: warp dot products over coalesced fp32 mirror rows, CB rows of a
@@ -1904,9 +1977,11 @@ __global__ void __launch_bounds__(K4T) k_score_select2(DevTables t, DecodeArgs a
     //     2*margin of the take-th best approximate score (|approx - exact| <= margin)
     if (tid == 0) n_s = 0;
     __syncthreads();
+    if (pass == 0) K4MARK(8)
     if (take > 0 && take < nc) {
-      block_topk(sim, key, pay, nc, take, order);
-      const float thr = approx[order[take - 1]] - 2.f * kScoreMargin;
+      block_kth_value(approx, key, nc, take - 1, &kth_s);
+      if (pass == 0) K4MARK(9)
+      const float thr = kth_s - 2.f * kScoreMargin;
       for (int c = tid; c < nc; c += K4T)
         if (approx[c] >= thr) {
           const int k = atomicAdd(&n_s, 1);
@@ -1922,6 +1997,8 @@ __global__ void __launch_bounds__(K4T) k_score_select2(DevTables t, DecodeArgs a
     }
     __syncthreads();
     const int ns_ = min(n_s, K4_SMAX);
+    if (a.k4prof && tid == 0 && pass == 0) a.k4prof[l * 16 + 7] = ns_;  // boundary-set size (instrumentation)
+    if (pass == 0) K4MARK(10)
     // (C) exact cosines (vecmath.hpp:54-61) of S; exact top-`take` of S by rank counting
     for (int r0 = 0; r0 < ns_; r0 += K4_SROWS) {
       const int rows = min(K4_SROWS, ns_ - r0);
@@ -1941,6 +2018,7 @@ __global__ void __launch_bounds__(K4T) k_score_select2(DevTables t, DecodeArgs a
       }
     }
     __syncthreads();
+    if (pass == 0) K4MARK(11)
     block_rank_select(ssim, skey, ns_, take, order);
     if (tid < take) order[tid] = sset[order[tid]];
     __syncthreads();
@@ -1972,6 +2050,7 @@ __global__ void __launch_bounds__(K4T) k_score_select2(DevTables t, DecodeArgs a
   // ---- verified (dedup in rank order, retrieval.cpp:20-26), attended count, page descriptors
   __shared__ int vnp[64], vnbp[64], voff[65];
   __shared__ int ring_cnt[64], ring_off[65];
+  __shared__ unsigned long long ring_mask[64];
   if (warp == 0) {  // dedup: lane i keeps rank i unless an earlier rank has the same slot
     const int nr_ = n_rank_s;
     int s0 = lane < nr_ ? rank_slot[lane] : -1, s1 = lane + 32 < nr_ ? rank_slot[lane + 32] : -1;
@@ -2003,7 +2082,10 @@ __global__ void __launch_bounds__(K4T) k_score_select2(DevTables t, DecodeArgs a
     int h = (s * 0x9E3779B1u) >> 25;      // 128-entry open-addressing set
     while (atomicCAS(&vhash[h], -1, s) != -1) h = (h + 1) & 127;
   }
-  if (tid < 64) ring_cnt[tid] = 0;
+  if (tid < 64) {
+    ring_cnt[tid] = 0;
+    ring_mask[tid] = 0ull;
+  }
   __syncthreads();
   if (threadIdx.x == 0) a.flags[l] = lazy_any;
   K4MARK(4)
@@ -2036,6 +2118,11 @@ __global__ void __launch_bounds__(K4T) k_score_select2(DevTables t, DecodeArgs a
       if (km) {
         const unsigned same = __match_any_sync(kFull, pg);
         if (keep && pg < 64 && lane == __ffs(same) - 1) atomicAdd(&ring_cnt[pg], __popc(same));
+        const unsigned long long bit = keep ? 1ull << (tt % t.P) : 0ull;  // one shared atomic per (warp, page)
+        const unsigned blo = __reduce_or_sync(same, static_cast<unsigned>(bit));
+        const unsigned bhi = __reduce_or_sync(same, static_cast<unsigned>(bit >> 32));
+        if (keep && pg < 64 && (threadIdx.x & 31) == __ffs(same) - 1)
+          atomicOr(&ring_mask[pg], (static_cast<unsigned long long>(bhi) << 32) | blo);
       }
     }
 #pragma unroll
@@ -2094,13 +2181,14 @@ __global__ void __launch_bounds__(K4T) k_score_select2(DevTables t, DecodeArgs a
     const bool isb = k >= vnp[j];
     const int page = isb ? t.bpages[static_cast<int64_t>(s) * t.maxbp + (k - vnp[j])]
                          : t.pages[static_cast<int64_t>(s) * t.maxp + k];
-    desc[i] = make_int4(page, t.pg_fill[page], isb ? 1 : 0, 0);
+    desc[i] = make_int4(page, t.pg_fill[page] | ((isb ? 1 : 0) << 16), -1, -1);
   }
   for (int i = tid; i < W * rpp && i < 64; i += K4T)
     if (ring_cnt[i] > 0 && ring_off[i] < a.max_desc) {
       const int rs = i / rpp, j = i % rpp;
       const int page = t.ring_pages[(static_cast<int64_t>(l) * W + rs) * rpp + j];
-      desc[ring_off[i]] = make_int4(page, t.pg_fill[page], 2 | (rs << 8), j * t.P);
+      desc[ring_off[i]] = make_int4(page, t.pg_fill[page] | (2 << 16), static_cast<int>(ring_mask[i] & 0xffffffffu),
+                                    static_cast<int>(ring_mask[i] >> 32));
     }
   __syncthreads();
   K4MARK(6)
@@ -2140,9 +2228,8 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 
 struct StageMeta {
   int dom, item, page, fill;
-  int kind, ring_slot, tok0, flags;  // flags: 1 first page of item, 2 last page, 4 end of work
-  int nver;
-  int ver[64];                        // verified slots of the domain (ring-page masking)
+  int kind, flags;                 // flags: 1 first page of item, 2 last page, 4 end of work
+  unsigned long long mask;         // tokens of the page to attend (window pages: K4's dedup)
 };
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
@@ -2174,6 +2261,7 @@ __device__ __forceinline__ void named_sync(int id, int n) {
 // an "empty" mbarrier (no CTA-wide barrier per page). At the end of an item the consumers merge
 // their states (named barrier) into a partial; the last CTA to finish a domain combines them.
 constexpr int ATT_THREADS = 256;
+constexpr int ATT_CHUNK = 8;  // pages per attention work item (DecodeArgs::chunk_pages)
 constexpr int ATT_WARPS = ATT_THREADS / 32;
 
 template <int D, bool BF16, int STAGES>
@@ -2192,12 +2280,10 @@ __global__ void __launch_bounds__(ATT_THREADS + 32) k_attend(DevTables t, Decode
   __shared__ float wm[ATT_WARPS], wl[ATT_WARPS];
   __shared__ float wo[ATT_WARPS][D];
   __shared__ int last_flag;
-  __shared__ int4 pq_s[32];
-  __shared__ int pver_s[64];
+  __shared__ __align__(16) int4 pqd[2][ATT_CHUNK];
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int L = min(t.L, 1024);
-  for (int l = tid; l < L; l += blockDim.x) prefix[l + 1] = a.n_items[l];
   // stale rows past a page's fill are read unmasked (and weighted by p = 0): keep them finite
   for (int64_t i = tid; i < STAGES * stage_bytes / 16; i += blockDim.x)
     reinterpret_cast<uint4*>(stages)[i] = make_uint4(0, 0, 0, 0);
@@ -2208,6 +2294,10 @@ __global__ void __launch_bounds__(ATT_THREADS + 32) k_attend(DevTables t, Decode
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  // launched as a programmatic dependent of K4: everything above overlapped K4's tail; the work
+  // list is read only after K4 completed and flushed (a no-op without the launch attribute)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  for (int l = tid; l < L; l += blockDim.x) prefix[l + 1] = a.n_items[l];
   __syncthreads();
   if (tid == 0) {
     prefix[0] = 0;
@@ -2220,16 +2310,16 @@ __global__ void __launch_bounds__(ATT_THREADS + 32) k_attend(DevTables t, Decode
     // ================================================================ producer warp
     if (lane != 0) return;
     const uint64_t pol = policy_evict_first();
-    int p_n = 0, p_k = 0, p_dom = 0, p_j = 0, p_nver = 0;
-    int4* pq = pq_s;     // the claimed item's page descriptors
-    int* pver = pver_s;  // the domain's verified slots
+    // Items are claimed on demand (claiming ahead parks the last items behind busy CTAs and
+    // lengthens the tail); the claimed item's descriptors arrive by cp.async into shared memory.
+    int cb = 0, g_cur = 0, c_dom = 0, c_j = 0, c_n = 0, p_k = 0;
     for (int it = 0;; ++it) {
       const int s = it % STAGES;
       if (it >= STAGES) mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
       StageMeta& m = meta[s];
-      if (p_k >= p_n) {  // claim the next item
-        const int g = atomicAdd(work_ctr, 1);
-        if (g >= total) {
+      if (p_k >= c_n) {  // claim the next item
+        g_cur = atomicAdd(work_ctr, 1);
+        if (g_cur >= total) {
           m.flags = 4;
           mbar_arrive(&full[s]);
           break;
@@ -2237,38 +2327,26 @@ __global__ void __launch_bounds__(ATT_THREADS + 32) k_attend(DevTables t, Decode
         int lo = 0, hi = L;
         while (hi - lo > 1) {
           const int mid = (lo + hi) / 2;
-          if (prefix[mid] <= g) lo = mid; else hi = mid;
+          if (prefix[mid] <= g_cur) lo = mid; else hi = mid;
         }
-        const bool new_dom = lo != p_dom || it == 0;
-        p_dom = lo;
-        p_j = g - prefix[lo];
-        const int first = p_j * a.chunk_pages;
-        p_n = min(a.chunk_pages, a.n_desc[p_dom] - first);
-        const int4* src = a.desc + static_cast<int64_t>(p_dom) * a.max_desc + first;
-#pragma unroll
-        for (int i = 0; i < 32; ++i)
-          if (i < p_n) pq[i] = src[i];
-        if (new_dom) {
-          p_nver = a.n_ver[p_dom];
-          for (int i = 0; i < 64; ++i)
-            if (i < p_nver) pver[i] = a.ver_slot[p_dom * a.k_s + i];
-        }
+        c_dom = lo;
+        c_j = g_cur - prefix[lo];
+        c_n = min(a.chunk_pages, a.n_desc[c_dom] - c_j * a.chunk_pages);
+        const int4* src = a.desc + static_cast<int64_t>(c_dom) * a.max_desc + c_j * a.chunk_pages;
+        for (int i = 0; i < c_n; ++i)
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(smem_u32(&pqd[cb][i])), "l"(src + i) : "memory");
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        asm volatile("cp.async.wait_all;" ::: "memory");
         p_k = 0;
       }
-      const int4 dsc = pq[p_k];
-      m.dom = p_dom;
-      m.item = p_j;
+      const int4 dsc = pqd[cb][p_k];
+      m.dom = c_dom;
+      m.item = c_j;
       m.page = dsc.x;
-      m.fill = dsc.y;
-      m.kind = dsc.z & 0xff;
-      m.ring_slot = dsc.z >> 8;
-      m.tok0 = dsc.w;
-      m.flags = (p_k == 0 ? 1 : 0) | (p_k == p_n - 1 ? 2 : 0);
-      if (m.kind == 2) {
-        m.nver = p_nver;
-        for (int i = 0; i < p_nver; ++i) m.ver[i] = pver[i];
-      }
-      p_k += 1;
+      m.fill = dsc.y & 0xffff;
+      m.kind = dsc.y >> 16;
+      m.mask = (static_cast<unsigned long long>(static_cast<uint32_t>(dsc.w)) << 32) | static_cast<uint32_t>(dsc.z);
+      m.flags = (p_k == 0 ? 1 : 0) | (p_k == c_n - 1 ? 2 : 0);
       const uint32_t bytes = static_cast<uint32_t>(m.fill) * ROWB;
       uint8_t* dst = stages + s * stage_bytes;
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -2276,6 +2354,7 @@ __global__ void __launch_bounds__(ATT_THREADS + 32) k_attend(DevTables t, Decode
       bulk_g2s_hint(dst, page_k(t, m.page), bytes, &full[s], pol);
       bulk_g2s_hint(dst + static_cast<int64_t>(P) * ROWB, page_v(t, m.page), bytes, &full[s], pol);
       bulk_g2s(dst + kv_bytes, a.q + static_cast<int64_t>(m.dom) * D, D * 4, &full[s]);
+      p_k += 1;
     }
     return;
   }
@@ -2300,7 +2379,7 @@ __global__ void __launch_bounds__(ATT_THREADS + 32) k_attend(DevTables t, Decode
     const StageMeta& m = meta[s];
     const int flags = m.flags;
     if (flags & 4) break;
-    const int fill = m.fill, kind = m.kind;
+    const int fill = m.fill;
     const uint8_t* Ks = stages + s * stage_bytes;
     const uint8_t* Vs = Ks + static_cast<int64_t>(P) * ROWB;
     if (m.dom != cur_dom) {  // the domain's query (carried by every stage)
@@ -2309,7 +2388,7 @@ __global__ void __launch_bounds__(ATT_THREADS + 32) k_attend(DevTables t, Decode
       for (int i = 0; i < OPL; ++i) qr[i] = qs[lane * OPL + i];
       cur_dom = m.dom;
     }
-    for (int tb = 0; tb < fill; tb += 64) {
+    for (int tb = 0; tb < ((a.debug_flags & 1) ? 0 : fill); tb += 64) {
       const int t0 = tb + warp * 8;  // this warp's first token
       if (t0 >= fill) continue;      // warp-uniform
       // ---- partial dots: 8 tokens x OPL dims per lane. Rows at or past `fill` hold finite stale
@@ -2358,11 +2437,7 @@ __global__ void __launch_bounds__(ATT_THREADS + 32) k_attend(DevTables t, Decode
       dot += __shfl_xor_sync(kFull, dot, 2);
       // lane holds token my_tok = (b4,b3,b2) of this warp's 8
       const int tok = t0 + my_tok;
-      bool valid = tok < fill;
-      if (valid && kind == 2) {
-        const int own = t.ring_owner[(static_cast<int64_t>(m.dom) * t.W + m.ring_slot) * t.tmax + m.tok0 + tok];
-        for (int j = 0; j < m.nver; ++j) valid &= m.ver[j] != own;
-      }
+      const bool valid = tok < fill && ((m.mask >> tok) & 1ull);  // window pages: K4's dedup mask
       const float sc = valid ? dot * sl2 : -INFINITY;
       float mx = sc;
       mx = fmaxf(mx, __shfl_xor_sync(kFull, mx, 4));
@@ -2621,9 +2696,8 @@ int launch_flat_topk(const DevTables& t, const float* q, const int32_t* slots, c
 namespace {
 int g_sms = 0;
 
-template <int D, bool BF16>
-int launch_attend_t(const DevTables& t, const DecodeArgs& a, cudaStream_t st) {
-  constexpr int STAGES = BF16 ? 3 : 2;
+template <int D, bool BF16, int STAGES>
+int launch_attend_s(const DevTables& t, const DecodeArgs& a, cudaStream_t st, bool pdl) {
   const size_t smem = static_cast<size_t>(STAGES) * (2 * t.P * D * (BF16 ? 2 : 4) + D * 4);
   static bool attr = false;
   if (!attr) {
@@ -2636,8 +2710,33 @@ int launch_attend_t(const DevTables& t, const DecodeArgs& a, cudaStream_t st) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_attend<D, BF16, STAGES>, ATT_THREADS + 32, smem);
     per_sm = max(1, per_sm);
   }
-  k_attend<D, BF16, STAGES><<<g_sms * per_sm, ATT_THREADS + 32, smem, st>>>(t, a, a.work_ctr);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(g_sms * per_sm));
+  cfg.blockDim = dim3(ATT_THREADS + 32);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr_pdl[1];
+  attr_pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr_pdl[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+  cfg.attrs = attr_pdl;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k_attend<D, BF16, STAGES>, t, a, a.work_ctr);
   return 1;
+}
+
+// Pipeline depth: KVC_ATT_STAGES (2..4) overrides the default of 2 (measured on B200: 2 stages x 3
+// CTAs per SM beat 3 stages x 2 CTAs, 97 vs 104 us for config 2).
+template <int D, bool BF16>
+int launch_attend_t(const DevTables& t, const DecodeArgs& a, cudaStream_t st, bool pdl) {
+  static int stages = -1;
+  if (stages < 0) {
+    const char* e = getenv("KVC_ATT_STAGES");
+    stages = e ? atoi(e) : 2;  // 2 stages -> 3 CTAs per SM (latency-bound consumers need the warps)
+    if (stages < 2 || stages > 4) stages = 2;
+  }
+  if (stages == 2) return launch_attend_s<D, BF16, 2>(t, a, st, pdl);
+  if (stages == 4) return launch_attend_s<D, BF16, 4>(t, a, st, pdl);
+  return launch_attend_s<D, BF16, 3>(t, a, st, pdl);
 }
 }  // namespace
 
@@ -2650,32 +2749,44 @@ int launch_decode(const DevTables& t, const DecodeArgs& a, cudaStream_t st, cuda
   if (ev) cudaEventRecord(ev[0], st);
   static int k4v = -1;
   if (k4v < 0) {
-    const char* e = getenv("KVC_K4");  // "v1": the 256-thread staged variant
-    k4v = (e && e[0] == 'v' && e[1] == '1') ? 1 : 2;
+    const char* e = getenv("KVC_K4");  // "v1": the 256-thread staged variant, "v2": select2
+    k4v = (e && e[0] == 'v' && e[1] == '1') ? 1 : (e && e[0] == 'v' && e[1] == '2') ? 2 : 3;
     cudaFuncSetAttribute(k_score_select, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     cudaFuncSetAttribute(k_score_select2, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   }
   const size_t smem4v2 = k4v2_smem_bytes(t.d, t.cmax, a.n_parts_host, t.W, t.tmax);
-  if (k4v == 2 && t.d % 4 == 0 && t.d <= 128 && t.W <= 64 && smem4v2 <= 200 * 1024) {
+  bool used3 = false;
+  if (k4v == 3 && launch_select3(t, a, st)) {
+    used3 = true;  // K4 v3 (select.cu)
+  } else if (k4v >= 2 && t.d % 4 == 0 && t.d <= 128 && t.W <= 64 && smem4v2 <= 200 * 1024) {
     k_score_select2<<<t.L, K4T, smem4v2, st>>>(t, a, a.work_ctr);
   } else {
     const size_t smem4 = k4_smem_bytes(t.d, t.cmax, a.n_parts_host, t.W, t.tmax);
     k_score_select<<<t.L, 256, smem4, st>>>(t, a, a.work_ctr);
   }
+  // K6 is a programmatic dependent of K4 (PDL: its launch and prologue overlap K4) unless an event
+  // has to be recorded between them (timing mode); k4_done then follows K6
+  static int pdl_env = -1;
+  if (pdl_env < 0) {
+    const char* e = getenv("KVC_PDL");
+    pdl_env = (e && e[0] == '0') ? 0 : 1;
+  }
+  const bool pdl = pdl_env && !ev && used3;
   if (ev) cudaEventRecord(ev[1], st);
-  if (k4_done) cudaEventRecord(k4_done, st);
+  if (k4_done && !pdl) cudaEventRecord(k4_done, st);
   int n = 1;
   switch (t.d * 2 + t.kv_bf16) {
-    case 64: n += launch_attend_t<32, false>(t, a, st); break;
-    case 65: n += launch_attend_t<32, true>(t, a, st); break;
-    case 128: n += launch_attend_t<64, false>(t, a, st); break;
-    case 129: n += launch_attend_t<64, true>(t, a, st); break;
-    case 256: n += launch_attend_t<128, false>(t, a, st); break;
-    case 257: n += launch_attend_t<128, true>(t, a, st); break;
-    case 512: n += launch_attend_t<256, false>(t, a, st); break;
-    case 513: n += launch_attend_t<256, true>(t, a, st); break;
+    case 64: n += launch_attend_t<32, false>(t, a, st, pdl); break;
+    case 65: n += launch_attend_t<32, true>(t, a, st, pdl); break;
+    case 128: n += launch_attend_t<64, false>(t, a, st, pdl); break;
+    case 129: n += launch_attend_t<64, true>(t, a, st, pdl); break;
+    case 256: n += launch_attend_t<128, false>(t, a, st, pdl); break;
+    case 257: n += launch_attend_t<128, true>(t, a, st, pdl); break;
+    case 512: n += launch_attend_t<256, false>(t, a, st, pdl); break;
+    case 513: n += launch_attend_t<256, true>(t, a, st, pdl); break;
     default: break;
   }
+  if (k4_done && pdl) cudaEventRecord(k4_done, st);
   if (ev) {
     cudaEventRecord(ev[2], st);
     cudaEventRecord(ev[3], st);

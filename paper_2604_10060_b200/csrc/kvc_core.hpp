@@ -195,6 +195,7 @@ struct DecodeArgs {
   float scale_log2;        // log2(e) / sqrt(d)
   long long* k4prof;       // [L][8] clock64 phase cycles (instrumentation; may be null)
   int32_t* work_ctr;       // attention work-claim counter (per context: contexts may run concurrently)
+  int32_t debug_flags;     // instrumentation experiments only (KVC_ATT_DEBUG); 0 in production
 };
 
 // ----------------------------------------------------------------------------- launchers
@@ -220,6 +221,8 @@ int launch_topm(const DevTables& t, const IngestArgs& a, cudaStream_t st);
 int launch_store_rows(const DevTables& t, const IngestArgs& a, cudaStream_t st);
 int launch_ring_write(const DevTables& t, const void* fk, const void* fv, int32_t T,
                       int32_t ring_slot, cudaStream_t st);
+// K4 v3 (select.cu); false when the shape does not fit it.
+bool launch_select3(const DevTables& t, const DecodeArgs& a, cudaStream_t st);
 // k4_done (may be null) is recorded between the score/select and attention kernels.
 int launch_decode(const DevTables& t, const DecodeArgs& a, cudaStream_t st, cudaEvent_t* ev,
                   cudaEvent_t k4_done = nullptr);

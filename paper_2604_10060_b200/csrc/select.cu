@@ -1,0 +1,607 @@
+// select.cu -- K4 v3: cluster scoring and selection for one decode step, one CTA per domain.
+//
+// Same contract as k_score_select2 (kernels.cu): visual_topk (index.cpp:192-208), semantic_topk
+// over the chosen partitions' clusters + registered buffers (index.cpp:210-240), the optional
+// prefetch ranking of layer l+1 (retrieval.cpp:117-128), the verified list (retrieval.cpp:20-26),
+// the attended-set size, and the attention work list (page descriptors) for K6.
+//
+// The CTA is latency bound: every phase is one round of independent global loads followed by
+// shared-memory work. The schedule is built around keeping that round count minimal:
+//   R1  query, window-ring owners, visual representatives (+ norms)
+//   R2  chosen partitions' list offsets
+//   R3  the candidate slots
+//   R4  per candidate: lazy flag, norm, id, and (warp-cooperative) the fp32 mirror row
+//   R5  boundary set S: fp64 masters (warp-cooperative) + page counts / member counts
+//   R6  verified clusters' page ids, R7 their fills
+// Exactness: the boundary set S = {c : #{j : approx_j > approx_c + 2m} < take} (m bounds
+// |fp32 mirror cosine - exact cosine|) contains every candidate that can reach the exact top-take;
+// S is re-scored with the reference's sequential fp64 cosine (vecmath.hpp:54-61) and ranked by
+// (sim desc, cluster id asc, live before buffer), so selections are bit-exact.
+#include "devmath.cuh"
+
+namespace kvc {
+
+namespace {
+
+using namespace dm;
+
+constexpr int K5T = 512;
+constexpr int K5W = K5T / 32;
+constexpr int K5_SROWS = 32;   // fp64 rows staged per exact re-score chunk
+constexpr int K5_SMAX = 256;   // boundary-set capacity
+constexpr int K5_CB = 16;      // mirror rows per warp in flight
+constexpr float kMargin3 = 1e-4f;  // |fp32 mirror cosine - exact cosine| bound (as kScoreMargin)
+
+// rank(i) = #entries better than i under (sim desc, key asc) -> order[rank] = i for rank < take
+__device__ void rank_select(const double* sim, const long long* key, int n, int take, int* order) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const double si = sim[i];
+    const long long ki = key[i];
+    int r = 0;
+    for (int j = 0; j < n; ++j) r += better(sim[j], key[j], si, ki) ? 1 : 0;
+    if (r < take) order[r] = i;
+  }
+  __syncthreads();
+}
+
+struct Sel3Smem {
+  // static part; the dynamic part holds stage / candidate arrays / owners
+  double nq;
+  float nq32;
+  int nc, nb, ns, nver, degen, lazy_any;
+  unsigned long long att;
+  int chosen[64];
+  int plo[64], plc[64], plpre[65];
+  int sset[K5_SMAX];
+  double ssim[K5_SMAX];
+  long long skey[K5_SMAX];
+  int snp[K5_SMAX], snbp[K5_SMAX];
+  long long snm[K5_SMAX];
+  int snb[K5_SMAX];
+  unsigned char slz[K5_SMAX];
+  int order[64];
+  int rank_si[64];  // rank -> S index
+  int vers[64], vsi[64];
+  int voff[65], ring_cnt[64], ring_off[65], ring_count[64];
+  unsigned long long ring_mask[64];  // per window page: tokens K6 attends (not owned by a verified cluster)
+  int vhash[128];
+  float red[K5W];
+  int redi[32];
+};
+
+__host__ __device__ inline size_t sel3_dyn_bytes(int d, int cmax, int parts, int W, int tmax) {
+  const int nsel = ((cmax > parts ? cmax : parts) + 1) & ~1;  // even: keeps the float4 arrays aligned
+  const int c4 = (cmax + 3) & ~3;
+  return static_cast<size_t>(K5_SROWS) * (d + 1) * 8  // stage
+         + static_cast<size_t>(d) * 8 + static_cast<size_t>(d) * 4  // qd, qf
+         + static_cast<size_t>(nsel) * 8 * 2                         // sim / ckey
+         + static_cast<size_t>(nsel) * 8                             // cnr (norms)
+         + static_cast<size_t>(c4) * 4                               // approx (float4-padded)
+         + static_cast<size_t>(cmax) * 4 + static_cast<size_t>(cmax) // cslot, cbuf
+         + static_cast<size_t>(W) * tmax * 4 + 64;                   // owners
+}
+
+__global__ void __launch_bounds__(K5T) k_select3(DevTables t, DecodeArgs a, int* work_ctr) {
+  extern __shared__ __align__(16) uint8_t dyn[];
+  __shared__ Sel3Smem S;
+  const int l = blockIdx.x, d = t.d, L = t.L, DS = d + 1;
+  const int P = a.n_parts_host;
+  const int cmax = t.cmax;
+  const int nsel = ((cmax > P ? cmax : P) + 1) & ~1;
+  const int c4 = (cmax + 3) & ~3;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int W = t.W, rpp = t.rpp;
+  uint8_t* p = dyn;
+  double* stage = reinterpret_cast<double*>(p);
+  p += static_cast<size_t>(K5_SROWS) * DS * 8;
+  double* qd = reinterpret_cast<double*>(p);
+  p += static_cast<size_t>(d) * 8;
+  double* sim = reinterpret_cast<double*>(p);
+  p += static_cast<size_t>(nsel) * 8;
+  long long* ckey = reinterpret_cast<long long*>(p);
+  p += static_cast<size_t>(nsel) * 8;
+  double* cnr = reinterpret_cast<double*>(p);
+  p += static_cast<size_t>(nsel) * 8;
+  float* approx = reinterpret_cast<float*>(p);
+  p += static_cast<size_t>(c4) * 4;
+  float* qf = reinterpret_cast<float*>(p);
+  p += static_cast<size_t>(d) * 4;
+  int* cslot = reinterpret_cast<int*>(p);
+  p += static_cast<size_t>(cmax) * 4;
+  int* owners = reinterpret_cast<int*>(p);
+  p += static_cast<size_t>(W) * t.tmax * 4;
+  uint8_t* cbuf = p;
+
+  // K6 (the attention kernel) may launch now: its prologue overlaps this kernel, and it waits for
+  // this grid's completion (griddepcontrol.wait) before reading the work list
+  asm volatile("griddepcontrol.launch_dependents;");
+  long long kc0 = clock64();
+#define K5MARK(k) if (a.k4prof && tid == 0) { const long long kc1 = clock64(); a.k4prof[l * 16 + (k)] = kc1 - kc0; kc0 = kc1; }
+  if (l == 0 && tid == 0) *work_ctr = 0;
+
+  // ------------------------------------------------------------------ R1
+  const float* q = a.q + static_cast<int64_t>(l) * d;
+  float qx = 0.f;
+  if (tid < d) {
+    qx = q[tid];
+    qd[tid] = static_cast<double>(qx);
+    qf[tid] = qx;
+  }
+  {
+    const int n_own = W * t.tmax;
+    const int* src = t.ring_owner + static_cast<int64_t>(l) * n_own;
+    int v[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int i = tid + K5T * j;
+      v[j] = i < n_own ? src[i] : -1;
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int i = tid + K5T * j;
+      if (i < n_own) owners[i] = v[j];
+    }
+    for (int i = tid + K5T * 4; i < n_own; i += K5T) owners[i] = src[i];
+  }
+  if (tid < W && tid < 64) S.ring_count[tid] = t.ring_count[tid];
+  if (tid < 128) S.vhash[tid] = -1;
+  if (tid < 64) {
+    S.ring_cnt[tid] = 0;
+    S.ring_mask[tid] = 0ull;
+  }
+  if (tid == 0) {
+    S.degen = 0;
+    S.att = 0;
+    S.lazy_any = 0;
+  }
+  // first chunk of visual representatives (P <= 32 in one chunk) staged with the query loads
+  const int p0rows = min(P, K5_SROWS);
+  for (int r = warp; r < p0rows; r += K5W) {
+    const double* src = t.vrep + static_cast<int64_t>(r) * d;
+    for (int i = lane; i < d; i += 32) stage[r * DS + i] = __ldg(src + i);
+  }
+  {
+    float sq = qx * qx;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(kFull, sq, o);
+    if (lane == 0) S.red[warp] = sq;
+  }
+  __syncthreads();
+  // exact |q| (vecmath.hpp:35-40) by the last thread while the visual chains run
+  if (tid == K5T - 1) {
+    double s = 0.0;
+#pragma unroll 16
+    for (int i = 0; i < d; ++i) s = dadd(s, dmul(qd[i], qd[i]));
+    S.nq = __dsqrt_rn(s);
+    float s32 = 0.f;
+    for (int w = 0; w < K5W; ++w) s32 += S.red[w];
+    S.nq32 = sqrtf(s32);
+  }
+  // ---- visual_topk: exact cosines (sim desc, partition id asc)
+  double vdot = 0.0, vnr = 1.0;
+  if (tid < p0rows) {
+    const double* row = stage + tid * DS;
+#pragma unroll 16
+    for (int i = 0; i < d; ++i) vdot = dadd(vdot, dmul(qd[i], row[i]));
+    vnr = t.vnorm[tid];
+  }
+  __syncthreads();
+  const double nq = S.nq;
+  const float nq32 = S.nq32;
+  if (tid == 0 && nq < 1e-12) S.degen = 1;
+  if (tid < p0rows) {
+    if (vnr < 1e-12) S.degen = 1;
+    sim[tid] = clamp1(ddiv(vdot, dmul(nq, vnr)));
+    ckey[tid] = tid;
+  }
+  for (int p0 = K5_SROWS; p0 < P; p0 += K5_SROWS) {  // more partitions: further chunks
+    const int rows = min(K5_SROWS, P - p0);
+    __syncthreads();
+    for (int r = warp; r < rows; r += K5W) {
+      const double* src = t.vrep + static_cast<int64_t>(p0 + r) * d;
+      for (int i = lane; i < d; i += 32) stage[r * DS + i] = __ldg(src + i);
+    }
+    __syncthreads();
+    if (tid < rows) {
+      double acc = 0.0;
+      const double* row = stage + tid * DS;
+#pragma unroll 16
+      for (int i = 0; i < d; ++i) acc = dadd(acc, dmul(qd[i], row[i]));
+      const double nr = t.vnorm[p0 + tid];
+      if (nr < 1e-12) S.degen = 1;
+      sim[p0 + tid] = clamp1(ddiv(acc, dmul(nq, nr)));
+      ckey[p0 + tid] = p0 + tid;
+    }
+  }
+  __syncthreads();
+  const int kv = min(a.k_v, P);
+  rank_select(sim, ckey, P, kv, S.chosen);
+  if (tid < kv) a.parts[l * a.k_v + tid] = S.chosen[tid];
+  if (tid == 0) a.n_parts_sel[l] = kv;
+  K5MARK(0)
+
+  // ------------------------------------------------------------------ semantic_topk (+ prefetch)
+  const int passes = (a.prefetch && l + 1 < L) ? 2 : 1;
+  for (int pass = 0; pass < passes; ++pass) {
+    const int layer = l + pass;
+    const int ktake = pass == 0 ? a.k_s : a.prefetch_k;
+    // R2: list offsets of the chosen partitions at `layer`
+    if (tid < kv) {
+      const int64_t pk = static_cast<int64_t>(S.chosen[tid]) * L + layer;
+      S.plo[tid] = t.pl_off[pk];
+      S.plc[tid] = t.pl_cnt[pk];
+    }
+    __syncthreads();
+    if (tid == 0) {
+      int acc = 0;
+      for (int i = 0; i < kv; ++i) {
+        S.plpre[i] = acc;
+        acc += S.plc[i];
+      }
+      S.plpre[kv] = acc;
+    }
+    __syncthreads();
+    const int nlive = S.plpre[kv];
+    // R3 + R4: candidate slots, then per candidate lazy / norm / id. Live entries take
+    // indices [0, nlive); registered buffers are appended after them (ranking is by key, so the
+    // list order only has to be deterministic).
+    int nb_total = 0;
+    for (int j0 = 0; j0 < nlive; j0 += K5T) {
+      const int j = j0 + tid;
+      int s = -1;
+      if (j < nlive) {
+        int i = 0;
+        while (i + 1 < kv && S.plpre[i + 1] <= j) ++i;
+        s = t.pl_pool[S.plo[i] + (j - S.plpre[i])];
+      }
+      int lz = 0;
+      if (s >= 0) {
+        lz = t.lazy[s];
+        const double nr = t.rnorm[s];
+        const long long cid = t.cid[s];
+        if (j < cmax) {
+          cslot[j] = s;
+          cbuf[j] = 0;
+          cnr[j] = nr;
+          ckey[j] = 2LL * cid;
+        }
+      }
+      const int nlz = __syncthreads_count(lz);
+      if (nlz > 0) {  // rare: registered buffers of pending splits get positions by a block scan
+        int x = lz;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(kFull, x, o);
+          if (lane >= o) x += y;
+        }
+        if (lane == 31) S.redi[warp] = x;
+        __syncthreads();
+        int before = 0;
+        for (int w = 0; w < warp; ++w) before += S.redi[w];
+        if (lz) {
+          const int k = nlive + nb_total + before + x - 1;
+          if (k < cmax) {
+            cslot[k] = s;
+            cbuf[k] = 1;
+            cnr[k] = t.bnorm[s];
+            ckey[k] = 2LL * t.cid[s] + 1;
+          }
+        }
+        __syncthreads();
+      }
+      nb_total += nlz;
+    }
+    const int nc_all = nlive + nb_total;
+    if (nc_all > cmax && tid == 0) set_err(t, DERR_CANDIDATES);
+    const int nc = min(nc_all, cmax);
+    if (pass == 0 && tid == 0) a.n_cand[l] = nc;
+    const int take = min(ktake, nc);
+    __syncthreads();
+    if (pass == 0) K5MARK(1)
+    // approximate cosines over the fp32 mirrors: K5_CB rows per warp, one 16-byte load per lane
+    // per row, all in flight together
+    {
+      const int nv4 = d >> 2;
+      const float4 qv = lane < nv4 ? reinterpret_cast<const float4*>(qf)[lane] : make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int c0 = warp * K5_CB; c0 < nc; c0 += K5W * K5_CB) {
+        float4 rv[K5_CB];
+#pragma unroll
+        for (int b = 0; b < K5_CB; ++b) {
+          const int c = c0 + b;
+          rv[b] = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (c < nc && lane < nv4) {
+            const float* base = cbuf[c] ? t.brep32 : t.rep32;
+            rv[b] = __ldg(reinterpret_cast<const float4*>(base + static_cast<int64_t>(cslot[c]) * d) + lane);
+          }
+        }
+        float acc[K5_CB];
+#pragma unroll
+        for (int b = 0; b < K5_CB; ++b) {
+          acc[b] = qv.x * rv[b].x;
+          acc[b] = fmaf(qv.y, rv[b].y, acc[b]);
+          acc[b] = fmaf(qv.z, rv[b].z, acc[b]);
+          acc[b] = fmaf(qv.w, rv[b].w, acc[b]);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+          for (int b = 0; b < K5_CB; ++b) acc[b] += __shfl_xor_sync(kFull, acc[b], o);
+        float mine = acc[0];
+#pragma unroll
+        for (int b = 1; b < K5_CB; ++b)
+          if (lane == b) mine = acc[b];
+        const int c = c0 + lane;
+        if (lane < K5_CB && c < nc) {
+          const double mnr = cnr[c];
+          if (mnr < 1e-12) S.degen = 1;
+          approx[c] = mine / (nq32 * static_cast<float>(mnr));
+        }
+      }
+      for (int c = nc + tid; c < c4; c += K5T) approx[c] = -INFINITY;
+    }
+    if (tid == 0) S.ns = 0;
+    __syncthreads();
+    if (pass == 0) K5MARK(2)
+    // boundary set S: candidates fewer than `take` of which beat approx_c by more than 2m
+    {
+      const int n4 = (nc + 3) >> 2;
+      for (int c = tid; c < nc; c += K5T) {
+        bool in = true;
+        if (take < nc) {
+          const float thr = approx[c] + 2.f * kMargin3 + 1e-6f;
+          int cnt = 0;
+          const float4* a4 = reinterpret_cast<const float4*>(approx);
+          int j = 0;
+          for (; j + 4 <= n4 && cnt < take; j += 4) {
+            const float4 x0 = a4[j], x1 = a4[j + 1], x2 = a4[j + 2], x3 = a4[j + 3];
+            cnt += (x0.x > thr) + (x0.y > thr) + (x0.z > thr) + (x0.w > thr);
+            cnt += (x1.x > thr) + (x1.y > thr) + (x1.z > thr) + (x1.w > thr);
+            cnt += (x2.x > thr) + (x2.y > thr) + (x2.z > thr) + (x2.w > thr);
+            cnt += (x3.x > thr) + (x3.y > thr) + (x3.z > thr) + (x3.w > thr);
+          }
+          for (; j < n4 && cnt < take; ++j) {
+            const float4 x = a4[j];
+            cnt += (x.x > thr) + (x.y > thr) + (x.z > thr) + (x.w > thr);
+          }
+          in = cnt < take;
+        }
+        if (in) {
+          const int k = atomicAdd(&S.ns, 1);
+          if (k < K5_SMAX) S.sset[k] = c;
+          else set_err(t, DERR_CANDIDATES);
+        }
+      }
+    }
+    __syncthreads();
+    const int ns = min(S.ns, K5_SMAX);
+    if (pass == 0 && a.k4prof && tid == 0) a.k4prof[l * 16 + 7] = ns;
+    // R5: exact cosines of S (fp64 masters staged warp-cooperatively) + counts for the tail
+    for (int r0 = 0; r0 < ns; r0 += K5_SROWS) {
+      const int rows = min(K5_SROWS, ns - r0);
+      for (int r = warp; r < rows; r += K5W) {
+        const int c = S.sset[r0 + r];
+        const double* src = (cbuf[c] ? t.brep64 : t.rep64) + static_cast<int64_t>(cslot[c]) * d;
+        for (int i = lane; i < d; i += 32) stage[r * DS + i] = __ldg(src + i);
+      }
+      if (pass == 0 && tid >= K5T - 32) {  // last warp: counts of this chunk's members
+        const int r = tid - (K5T - 32);
+        if (r < rows) {
+          const int s = cslot[S.sset[r0 + r]];
+          S.snp[r0 + r] = t.npages[s];
+          S.snbp[r0 + r] = t.nbpages[s];
+          S.snm[r0 + r] = t.nmem[s];
+          S.snb[r0 + r] = t.nbuf[s];
+          S.slz[r0 + r] = t.lazy[s];
+        }
+      }
+      __syncthreads();
+      if (tid < rows) {
+        const int c = S.sset[r0 + tid];
+        const double* row = stage + tid * DS;
+        double acc = 0.0;
+#pragma unroll 16
+        for (int i = 0; i < d; ++i) acc = dadd(acc, dmul(qd[i], row[i]));  // exact_cos order
+        S.ssim[r0 + tid] = clamp1(ddiv(acc, dmul(nq, cnr[c])));
+        S.skey[r0 + tid] = ckey[c];
+      }
+      __syncthreads();
+    }
+    if (pass == 0) K5MARK(3)
+    rank_select(S.ssim, S.skey, ns, take, S.order);
+    if (tid < take) {
+      const int si = S.order[tid];
+      const int c = S.sset[si];
+      if (pass == 0) {
+        S.rank_si[tid] = si;
+        a.ranked_slot[l * a.k_s + tid] = cslot[c];
+        a.ranked_buf[l * a.k_s + tid] = cbuf[c];
+      } else {
+        a.pf_slot[l * a.prefetch_k + tid] = cslot[c];
+        a.pf_buf[l * a.prefetch_k + tid] = cbuf[c];
+      }
+    }
+    if (tid == 0) {
+      if (pass == 0) a.n_ranked[l] = take;
+      else a.n_pf[l] = take;
+    }
+    if (pass == 0) {  // verified: rank order, first occurrence of each slot (retrieval.cpp:20-26)
+      __syncthreads();
+      if (warp == 0) {
+        const int s0 = lane < take ? cslot[S.sset[S.rank_si[lane]]] : -1;
+        const int s1 = lane + 32 < take ? cslot[S.sset[S.rank_si[lane + 32]]] : -1;
+        bool k0 = s0 >= 0, k1 = s1 >= 0;
+        for (int j = 0; j < take; ++j) {
+          const int sj = cslot[S.sset[S.rank_si[j]]];
+          if (j < lane && sj == s0) k0 = false;
+          if (j < lane + 32 && sj == s1) k1 = false;
+        }
+        const unsigned m0 = __ballot_sync(kFull, k0), m1 = __ballot_sync(kFull, k1);
+        const unsigned lt = (1u << lane) - 1u;
+        if (k0) {
+          S.vers[__popc(m0 & lt)] = s0;
+          S.vsi[__popc(m0 & lt)] = S.rank_si[lane];
+        }
+        if (k1) {
+          S.vers[__popc(m0) + __popc(m1 & lt)] = s1;
+          S.vsi[__popc(m0) + __popc(m1 & lt)] = S.rank_si[lane + 32];
+        }
+        if (lane == 0) {
+          S.nver = __popc(m0) + __popc(m1);
+          a.n_ver[l] = S.nver;
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (passes == 1 && tid == 0) a.n_pf[l] = 0;
+  if (S.degen && tid == 0) set_err(t, DERR_DEGENERATE);
+
+  // ------------------------------------------------------------------ attended set + work list
+  const int nv = S.nver;
+  if (tid < nv) {
+    const int s = S.vers[tid];
+    const int si = S.vsi[tid];
+    a.ver_slot[l * a.k_s + tid] = s;
+    atomicAdd(&S.att, static_cast<unsigned long long>(S.snm[si] + S.snb[si]));
+    if (S.slz[si]) S.lazy_any = 1;  // a pending split: the host settles it before the next step
+    int h = (s * 0x9E3779B1u) >> 25;
+    while (atomicCAS(&S.vhash[h], -1, s) != -1) h = (h + 1) & 127;
+  }
+  __syncthreads();
+  if (tid == 0) a.flags[l] = S.lazy_any;
+  K5MARK(4)
+  {  // window ring tokens whose owner is not a verified cluster (retrieval.cpp:107-108)
+    unsigned long long mine = 0;
+    const int n_ring = W * t.tmax;
+    const int n_pad = (n_ring + K5T - 1) / K5T * K5T;
+    for (int i = tid; i < n_pad; i += K5T) {
+      const int rs = i / t.tmax, tt = i - rs * t.tmax;
+      bool keep = i < n_ring && tt < S.ring_count[rs];
+      if (keep) {
+        const int own = owners[i];
+        if (own >= 0) {
+          int h = (own * 0x9E3779B1u) >> 25;
+          for (;;) {
+            const int v = S.vhash[h];
+            if (v == own) {
+              keep = false;
+              break;
+            }
+            if (v < 0) break;
+            h = (h + 1) & 127;
+          }
+        }
+      }
+      const int pg = keep ? rs * rpp + tt / t.P : -1;
+      const unsigned km = __ballot_sync(kFull, keep);
+      mine += keep ? 1 : 0;
+      if (km) {
+        const unsigned same = __match_any_sync(kFull, pg);
+        if (keep && pg < 64 && lane == __ffs(same) - 1) atomicAdd(&S.ring_cnt[pg], __popc(same));
+        const unsigned long long bit = keep ? 1ull << (tt % t.P) : 0ull;  // one shared atomic per (warp, page)
+        const unsigned blo = __reduce_or_sync(same, static_cast<unsigned>(bit));
+        const unsigned bhi = __reduce_or_sync(same, static_cast<unsigned>(bit >> 32));
+        if (keep && pg < 64 && (threadIdx.x & 31) == __ffs(same) - 1)
+          atomicOr(&S.ring_mask[pg], (static_cast<unsigned long long>(bhi) << 32) | blo);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(kFull, mine, o);
+    if (lane == 0) atomicAdd(&S.att, mine);
+  }
+  __syncthreads();
+  if (warp == 0) {  // descriptor offsets: verified clusters' pages, then non-empty ring pages
+    const int cnt0 = lane < nv ? S.snp[S.vsi[lane]] + S.snbp[S.vsi[lane]] : 0;
+    const int cnt1 = lane + 32 < nv ? S.snp[S.vsi[lane + 32]] + S.snbp[S.vsi[lane + 32]] : 0;
+    int x0 = cnt0, x1 = cnt1;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y0 = __shfl_up_sync(kFull, x0, o), y1 = __shfl_up_sync(kFull, x1, o);
+      if (lane >= o) {
+        x0 += y0;
+        x1 += y1;
+      }
+    }
+    const int tot0 = __shfl_sync(kFull, x0, 31);
+    if (lane < nv) S.voff[lane] = x0 - cnt0;
+    if (lane + 32 < nv) S.voff[lane + 32] = tot0 + x1 - cnt1;
+    const int vtot = tot0 + __shfl_sync(kFull, x1, 31);
+    if (lane == 0) S.voff[nv] = vtot;
+    const int nrp = min(W * rpp, 64);
+    const int r0 = lane < nrp && S.ring_cnt[lane] > 0 ? 1 : 0, r1 = lane + 32 < nrp && S.ring_cnt[lane + 32] > 0 ? 1 : 0;
+    const unsigned rm0 = __ballot_sync(kFull, r0), rm1 = __ballot_sync(kFull, r1);
+    const unsigned lt = (1u << lane) - 1u;
+    if (lane < nrp) S.ring_off[lane] = vtot + __popc(rm0 & lt);
+    if (lane + 32 < nrp) S.ring_off[lane + 32] = vtot + __popc(rm0) + __popc(rm1 & lt);
+    int o = vtot + __popc(rm0) + __popc(rm1);
+    if (lane == 0) {
+      S.ring_off[nrp] = o;
+      if (o > a.max_desc) {
+        set_err(t, DERR_ITEMS);
+        o = a.max_desc;
+      }
+      a.n_desc[l] = o;
+      a.n_items[l] = (o + a.chunk_pages - 1) / a.chunk_pages;
+      a.attended[l] = static_cast<int64_t>(S.att);
+    }
+  }
+  __syncthreads();
+  K5MARK(5)
+  // R6 + R7: page ids, then fills
+  int4* desc = a.desc + static_cast<int64_t>(l) * a.max_desc;
+  const int ndesc = min(S.voff[nv], a.max_desc);
+  for (int i0 = 0; i0 < ndesc; i0 += K5T) {
+    const int i = i0 + tid;
+    int page = -1, isb = 0;
+    if (i < ndesc) {
+      int lo = 0, hi = nv - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (S.voff[mid] <= i) lo = mid; else hi = mid - 1;
+      }
+      const int s = S.vers[lo];
+      const int k = i - S.voff[lo];
+      const int np = S.snp[S.vsi[lo]];
+      isb = k >= np;
+      page = isb ? t.bpages[static_cast<int64_t>(s) * t.maxbp + (k - np)] : t.pages[static_cast<int64_t>(s) * t.maxp + k];
+    }
+    if (page >= 0) desc[i] = make_int4(page, t.pg_fill[page] | (isb << 16), -1, -1);
+  }
+  for (int i = tid; i < W * rpp && i < 64; i += K5T)
+    if (S.ring_cnt[i] > 0 && S.ring_off[i] < a.max_desc) {
+      const int rs = i / rpp, j = i % rpp;
+      const int page = t.ring_pages[(static_cast<int64_t>(l) * W + rs) * rpp + j];
+      desc[S.ring_off[i]] = make_int4(page, t.pg_fill[page] | (2 << 16), static_cast<int>(S.ring_mask[i] & 0xffffffffu),
+                                      static_cast<int>(S.ring_mask[i] >> 32));
+    }
+  __syncthreads();
+  K5MARK(6)
+#undef K5MARK
+  if (tid == 0) {
+    __threadfence();
+    a.errw[l] = atomicOr(t.err, 0);
+  }
+  if (a.n_items[l] == 0)
+    for (int i = tid; i < d; i += K5T) a.out[static_cast<int64_t>(l) * d + i] = 0.f;
+}
+
+}  // namespace
+
+// Launches K4 v3 when the shape fits (d % 4 == 0, d <= 128, take lists <= 64, W * rpp <= 64);
+// returns false otherwise (the caller uses k_score_select2).
+bool launch_select3(const DevTables& t, const DecodeArgs& a, cudaStream_t st) {
+  if (t.d % 4 != 0 || t.d > 128 || t.W > 64 || t.W * t.rpp > 64 || a.k_s > 64 || a.prefetch_k > 64 || a.k_v > 64)
+    return false;
+  const size_t smem = sel3_dyn_bytes(t.d, t.cmax, a.n_parts_host, t.W, t.tmax);
+  if (smem + sizeof(Sel3Smem) > 220 * 1024) return false;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_select3, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  if (smem > 200 * 1024) return false;
+  k_select3<<<t.L, K5T, smem, st>>>(t, a, a.work_ctr);
+  return true;
+}
+
+}  // namespace kvc

@@ -77,7 +77,7 @@ lines += ["", "## `ncu --set full` captures", "",
           "| kernel | duration us | DRAM read MB | DRAM write MB | DRAM % peak | SM % | achieved occupancy | regs |",
           "|---|---|---|---|---|---|---|---|"]
 att = {}
-for kname in ("k_attend", "k_score_select2", "k_resolve_spec", "k_assign_tc", "k_approx", "k_topm"):
+for kname in ("k_attend", "k_select3", "k_score_select2", "k_resolve_spec", "k_assign_tc", "k_approx", "k_topm"):
     for m in ncu_raw(kname)[:1]:
         dur = num(m.get("gpu__time_duration.sum"))
         rd = num(m.get("dram__bytes_read.sum"))
