@@ -49,7 +49,7 @@ RESOLVE_PHASES = {  # clock64 phases of the resolve kernel (kvc_debug_resolve_pr
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--steps", type=int, default=50)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--frames", type=int, default=0, help="timed ingest frames (default = steps)")
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -283,14 +283,19 @@ def main():
         with torch.cuda.stream(stream):
             ev0.record(stream)
             h0 = time.perf_counter()
+            step_ev = []
             for i in range(args.warmup, nq):
                 kv.query(i, q_dev[i], out=out_dev)
                 if world > 1:  # per-domain outputs to every rank (NCCL over NVLink)
                     gather_domain_outputs(out_dev, args.domains)
+                e = torch.cuda.Event(enable_timing=True)  # step boundary (after K6, before the next K4)
+                e.record(stream)
+                step_ev.append(e)
             host_issue_us = (time.perf_counter() - h0) * 1e6 / args.steps
             ev1.record(stream)
         torch.cuda.synchronize()
     decode_ms = ev0.elapsed_time(ev1)
+    periods = [step_ev[i].elapsed_time(step_ev[i + 1]) * 1e3 for i in range(len(step_ev) - 1)]
     decode_launches = kv.launch_count() - launches0
     # instrumented pass over the same queries: per-kernel CUDA events on the context stream
     # (K4 and K6 durations, attended bytes per K6 launch) and host phases
@@ -355,13 +360,17 @@ def main():
         "gpu_launches": int(decode_launches),
         "phases_us": {"score_select": round(float(np.mean(k4_us)), 2), "attend": round(att_time * 1e6, 2),
                       "host_issue_per_step": round(host_issue_us, 2),
+                      "step_period_us": {"min": round(min(periods), 2) if periods else None,
+                                         "median": round(float(np.median(periods)), 2) if periods else None,
+                                         "max": round(max(periods), 2) if periods else None},
                       "host_wait_device": round(float(np.mean([h[0] for h in host_ph])), 2),
                       "host_replay": round(float(np.mean([h[1] for h in host_ph])), 2),
                       "host_repin": round(float(np.mean([h[2] for h in host_ph])), 2),
                       "device_span": round(float(np.mean(span_us)), 2),
                       "host_layer_loop": round(float(np.mean([h[3] for h in host_ph])), 2),
-                      "k4_cycles": dict(zip(["qnorm", "visual", "cand_score", "rank_select", "tail1", "ring", "desc", "boundary_set",
-                                             "pre_kth", "kth", "boundary_filter", "exact_rescore"],
+                      "k4_cycles": dict(zip(["query_visual", "candidates", "approx", "boundary_exact", "verified", "ring",
+                                             "descriptors", "boundary_set", "-", "-", "-", "-", "tail_after_marks",
+                                             "block_start_skew_ns", "span_ns", "mean_block_ns"],
                                             k4_cycles.round(0).tolist()))},
         "clocks": clk.summary(),
         "ingest": {"value": round(frames_t / (ingest_ms * 1e-3), 1), "unit": "frames/s",

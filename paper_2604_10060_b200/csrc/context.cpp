@@ -419,6 +419,20 @@ void Context::resolve_profile(double* out) {
       for (int l = 0; l < L_; ++l) s += static_cast<double>(p[static_cast<std::size_t>(l) * W + k]);
     out[k] = s / L_;
   }
+  if (dec) {  // K4 v3 global-timer stamps: block-start skew, span, mean block duration (ns)
+    long long s0 = LLONG_MAX, s1 = LLONG_MIN, e1 = LLONG_MIN;
+    double dur = 0.0;
+    for (int l = 0; l < L_; ++l) {
+      const long long a0 = p[static_cast<std::size_t>(l) * W + 13], a1 = p[static_cast<std::size_t>(l) * W + 14];
+      s0 = std::min(s0, a0);
+      s1 = std::max(s1, a0);
+      e1 = std::max(e1, a1);
+      dur += static_cast<double>(a1 - a0);
+    }
+    out[13] = static_cast<double>(s1 - s0);
+    out[14] = static_cast<double>(e1 - s0);
+    out[15] = dur / L_;
+  }
 }
 
 void Context::sync() { KVC_CUDA(cudaStreamSynchronize(st_)); }

@@ -9,6 +9,7 @@
 //   engine.cpp:176-237    answer_query: repin + checks after the query
 //   index.cpp:263-343     check_invariants;  store.cpp:183-189 audit
 #include <algorithm>
+#include <cstdlib>
 #include <chrono>
 #include <cmath>
 #include <cstring>
@@ -148,6 +149,12 @@ void Context::replay_decode(const void* hblock, const std::int64_t* gt, int n_gt
     std::int64_t tok = 0;
     for (int l = 0; l < L_; ++l) tok += ha[l];
     step_t_[4] = static_cast<double>(tok) * 2.0 * d_ * es_;
+    // L2 prefetch budget for the next steps: the first domains K6 will stream (KVC_L2PF_MB, default 0 = off: measured no net gain, the per-SM prefetch issue delays K4 as much as it saves in K6)
+    static const double budget = [] {
+      const char* e = std::getenv("KVC_L2PF_MB");
+      return (e ? std::atof(e) : 0.0) * 1048576.0;
+    }();
+    da_.l2pf_pages = static_cast<std::int32_t>(budget / (static_cast<double>(std::max(1, L_)) * t_.page_bytes));
   }
   // host copies of the device rankings (same carve offsets as alloc_device)
   auto hp = [&](const void* dptr) {

@@ -196,6 +196,7 @@ struct DecodeArgs {
   long long* k4prof;       // [L][8] clock64 phase cycles (instrumentation; may be null)
   int32_t* work_ctr;       // attention work-claim counter (per context: contexts may run concurrently)
   int32_t debug_flags;     // instrumentation experiments only (KVC_ATT_DEBUG); 0 in production
+  int32_t l2pf_pages;      // pages per domain K4 prefetches into L2 while it is latency bound
 };
 
 // ----------------------------------------------------------------------------- launchers

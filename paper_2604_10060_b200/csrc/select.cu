@@ -52,6 +52,7 @@ struct Sel3Smem {
   unsigned long long att;
   int chosen[64];
   int plo[64], plc[64], plpre[65];
+  int spo[64], spc[64];  // pl_off / pl_cnt of partitions 0..63 at layer l (R1, speculative)
   int sset[K5_SMAX];
   double ssim[K5_SMAX];
   long long skey[K5_SMAX];
@@ -62,8 +63,9 @@ struct Sel3Smem {
   int order[64];
   int rank_si[64];  // rank -> S index
   int vers[64], vsi[64];
-  int voff[65], ring_cnt[64], ring_off[65], ring_count[64];
+  int voff[65], ring_off[65], ring_count[64];
   unsigned long long ring_mask[64];  // per window page: tokens K6 attends (not owned by a verified cluster)
+  unsigned ring_half[128];           // the same, 32 tokens per word as the ring pass writes them
   int vhash[128];
   float red[K5W];
   int redi[32];
@@ -116,6 +118,11 @@ __global__ void __launch_bounds__(K5T) k_select3(DevTables t, DecodeArgs a, int*
   // this grid's completion (griddepcontrol.wait) before reading the work list
   asm volatile("griddepcontrol.launch_dependents;");
   long long kc0 = clock64();
+  if (a.k4prof && threadIdx.x == 0) {  // block start on the global timer (launch skew, instrumentation)
+    unsigned long long gt;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+    a.k4prof[l * 16 + 13] = static_cast<long long>(gt);
+  }
 #define K5MARK(k) if (a.k4prof && tid == 0) { const long long kc1 = clock64(); a.k4prof[l * 16 + (k)] = kc1 - kc0; kc0 = kc1; }
   if (l == 0 && tid == 0) *work_ctr = 0;
 
@@ -144,11 +151,12 @@ __global__ void __launch_bounds__(K5T) k_select3(DevTables t, DecodeArgs a, int*
     for (int i = tid + K5T * 4; i < n_own; i += K5T) owners[i] = src[i];
   }
   if (tid < W && tid < 64) S.ring_count[tid] = t.ring_count[tid];
-  if (tid < 128) S.vhash[tid] = -1;
-  if (tid < 64) {
-    S.ring_cnt[tid] = 0;
-    S.ring_mask[tid] = 0ull;
+  if (tid < P && tid < 64) {  // partition list offsets at layer l for the (likely few) partitions
+    S.spo[tid] = t.pl_off[static_cast<int64_t>(tid) * L + l];
+    S.spc[tid] = t.pl_cnt[static_cast<int64_t>(tid) * L + l];
   }
+  if (tid < 128) S.vhash[tid] = -1;
+  if (tid < 128) S.ring_half[tid] = 0u;
   if (tid == 0) {
     S.degen = 0;
     S.att = 0;
@@ -225,11 +233,18 @@ __global__ void __launch_bounds__(K5T) k_select3(DevTables t, DecodeArgs a, int*
   for (int pass = 0; pass < passes; ++pass) {
     const int layer = l + pass;
     const int ktake = pass == 0 ? a.k_s : a.prefetch_k;
-    // R2: list offsets of the chosen partitions at `layer`
+    if (tid == 0) S.nb = 0;
+    // R2: list offsets of the chosen partitions at `layer` (pass 0: loaded speculatively in R1)
     if (tid < kv) {
-      const int64_t pk = static_cast<int64_t>(S.chosen[tid]) * L + layer;
-      S.plo[tid] = t.pl_off[pk];
-      S.plc[tid] = t.pl_cnt[pk];
+      const int cp = S.chosen[tid];
+      if (pass == 0 && cp < 64) {
+        S.plo[tid] = S.spo[cp];
+        S.plc[tid] = S.spc[cp];
+      } else {
+        const int64_t pk = static_cast<int64_t>(cp) * L + layer;
+        S.plo[tid] = t.pl_off[pk];
+        S.plc[tid] = t.pl_cnt[pk];
+      }
     }
     __syncthreads();
     if (tid == 0) {
@@ -241,33 +256,77 @@ __global__ void __launch_bounds__(K5T) k_select3(DevTables t, DecodeArgs a, int*
       S.plpre[kv] = acc;
     }
     __syncthreads();
-    const int nlive = S.plpre[kv];
-    // R3 + R4: candidate slots, then per candidate lazy / norm / id. Live entries take
-    // indices [0, nlive); registered buffers are appended after them (ranking is by key, so the
-    // list order only has to be deterministic).
-    int nb_total = 0;
-    for (int j0 = 0; j0 < nlive; j0 += K5T) {
-      const int j = j0 + tid;
-      int s = -1;
-      if (j < nlive) {
+    const int nlive = min(S.plpre[kv], cmax);
+    if (S.plpre[kv] > cmax && tid == 0) set_err(t, DERR_CANDIDATES);
+    if (pass == 0) K5MARK(1)
+    // R3 + R4 fused per warp: a warp owns 16 candidates per round; lanes 0-15 load their slots,
+    // then (in the same round) the slots' lazy flags / norms / ids and, warp-cooperatively, their
+    // fp32 mirror rows; approximate cosines follow without a block barrier. Live entries take
+    // indices [0, nlive); registered buffers of pending splits are appended after them (ranking
+    // is by key, so the list order only has to be deterministic).
+    const int nv4 = d >> 2;
+    const float4 qv = lane < nv4 ? reinterpret_cast<const float4*>(qf)[lane] : make_float4(0.f, 0.f, 0.f, 0.f);
+    auto score16 = [&](int c0, int cend, int my_slot, bool my_buf) {
+      float4 rv[K5_CB];
+#pragma unroll
+      for (int b = 0; b < K5_CB; ++b) {
+        const int sb = __shfl_sync(kFull, my_slot, b);
+        const bool bb = __shfl_sync(kFull, my_buf ? 1 : 0, b) != 0;
+        rv[b] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (c0 + b < cend && lane < nv4)
+          rv[b] = __ldg(reinterpret_cast<const float4*>((bb ? t.brep32 : t.rep32) + static_cast<int64_t>(sb) * d) + lane);
+      }
+      float acc[K5_CB];
+#pragma unroll
+      for (int b = 0; b < K5_CB; ++b) {
+        acc[b] = qv.x * rv[b].x;
+        acc[b] = fmaf(qv.y, rv[b].y, acc[b]);
+        acc[b] = fmaf(qv.z, rv[b].z, acc[b]);
+        acc[b] = fmaf(qv.w, rv[b].w, acc[b]);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int b = 0; b < K5_CB; ++b) acc[b] += __shfl_xor_sync(kFull, acc[b], o);
+      float mine = acc[0];
+#pragma unroll
+      for (int b = 1; b < K5_CB; ++b)
+        if (lane == b) mine = acc[b];
+      return mine;
+    };
+    int my_lz = 0;
+    for (int r0 = 0; r0 < nlive; r0 += K5W * K5_CB) {
+      const int c0 = r0 + warp * K5_CB;
+      const int j = c0 + lane;
+      int s = 0;
+      double nr = 1.0;
+      if (lane < K5_CB && j < nlive) {
         int i = 0;
         while (i + 1 < kv && S.plpre[i + 1] <= j) ++i;
         s = t.pl_pool[S.plo[i] + (j - S.plpre[i])];
-      }
-      int lz = 0;
-      if (s >= 0) {
-        lz = t.lazy[s];
-        const double nr = t.rnorm[s];
+        const int lz = t.lazy[s];
+        nr = t.rnorm[s];
         const long long cid = t.cid[s];
-        if (j < cmax) {
-          cslot[j] = s;
-          cbuf[j] = 0;
-          cnr[j] = nr;
-          ckey[j] = 2LL * cid;
+        cslot[j] = s;
+        cbuf[j] = 0;
+        cnr[j] = nr;
+        ckey[j] = 2LL * cid;
+        my_lz += lz;
+      }
+      if (c0 < nlive) {  // warp-uniform
+        const float sc = score16(c0, nlive, s, false);
+        if (lane < K5_CB && j < nlive) {
+          if (nr < 1e-12) S.degen = 1;
+          approx[j] = sc / (nq32 * static_cast<float>(nr));
         }
       }
-      const int nlz = __syncthreads_count(lz);
-      if (nlz > 0) {  // rare: registered buffers of pending splits get positions by a block scan
+    }
+    int nb_total = 0;
+    if (__syncthreads_or(my_lz)) {  // registered buffers of pending splits (rare)
+      // buffer entries: positions by a block scan over the live list (order: live index)
+      for (int j0 = 0; j0 < nlive; j0 += K5T) {
+        const int j = j0 + tid;
+        const int lz = j < nlive ? t.lazy[cslot[j]] : 0;
         int x = lz;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -276,69 +335,44 @@ __global__ void __launch_bounds__(K5T) k_select3(DevTables t, DecodeArgs a, int*
         }
         if (lane == 31) S.redi[warp] = x;
         __syncthreads();
-        int before = 0;
-        for (int w = 0; w < warp; ++w) before += S.redi[w];
+        int before = 0, chunk = 0;
+        for (int w = 0; w < K5W; ++w) {
+          if (w < warp) before += S.redi[w];
+          chunk += S.redi[w];
+        }
         if (lz) {
-          const int k = nlive + nb_total + before + x - 1;
+          const int k = nlive + S.nb + before + x - 1;
+          const int sl = cslot[j];
           if (k < cmax) {
-            cslot[k] = s;
+            cslot[k] = sl;
             cbuf[k] = 1;
-            cnr[k] = t.bnorm[s];
-            ckey[k] = 2LL * t.cid[s] + 1;
+            cnr[k] = t.bnorm[sl];
+            ckey[k] = 2LL * t.cid[sl] + 1;
           }
         }
         __syncthreads();
+        if (tid == 0) S.nb += chunk;
+        __syncthreads();
       }
-      nb_total += nlz;
+      nb_total = S.nb;
+      const int nce = min(nlive + nb_total, cmax);
+      for (int c0 = nlive + warp * K5_CB; c0 < nce; c0 += K5W * K5_CB) {
+        const int j = c0 + lane;
+        const int sl = (lane < K5_CB && j < nce) ? cslot[j] : 0;
+        const float sc = score16(c0, nce, sl, true);
+        if (lane < K5_CB && j < nce) {
+          const double nr = cnr[j];
+          if (nr < 1e-12) S.degen = 1;
+          approx[j] = sc / (nq32 * static_cast<float>(nr));
+        }
+      }
     }
     const int nc_all = nlive + nb_total;
     if (nc_all > cmax && tid == 0) set_err(t, DERR_CANDIDATES);
     const int nc = min(nc_all, cmax);
     if (pass == 0 && tid == 0) a.n_cand[l] = nc;
     const int take = min(ktake, nc);
-    __syncthreads();
-    if (pass == 0) K5MARK(1)
-    // approximate cosines over the fp32 mirrors: K5_CB rows per warp, one 16-byte load per lane
-    // per row, all in flight together
-    {
-      const int nv4 = d >> 2;
-      const float4 qv = lane < nv4 ? reinterpret_cast<const float4*>(qf)[lane] : make_float4(0.f, 0.f, 0.f, 0.f);
-      for (int c0 = warp * K5_CB; c0 < nc; c0 += K5W * K5_CB) {
-        float4 rv[K5_CB];
-#pragma unroll
-        for (int b = 0; b < K5_CB; ++b) {
-          const int c = c0 + b;
-          rv[b] = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (c < nc && lane < nv4) {
-            const float* base = cbuf[c] ? t.brep32 : t.rep32;
-            rv[b] = __ldg(reinterpret_cast<const float4*>(base + static_cast<int64_t>(cslot[c]) * d) + lane);
-          }
-        }
-        float acc[K5_CB];
-#pragma unroll
-        for (int b = 0; b < K5_CB; ++b) {
-          acc[b] = qv.x * rv[b].x;
-          acc[b] = fmaf(qv.y, rv[b].y, acc[b]);
-          acc[b] = fmaf(qv.z, rv[b].z, acc[b]);
-          acc[b] = fmaf(qv.w, rv[b].w, acc[b]);
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-          for (int b = 0; b < K5_CB; ++b) acc[b] += __shfl_xor_sync(kFull, acc[b], o);
-        float mine = acc[0];
-#pragma unroll
-        for (int b = 1; b < K5_CB; ++b)
-          if (lane == b) mine = acc[b];
-        const int c = c0 + lane;
-        if (lane < K5_CB && c < nc) {
-          const double mnr = cnr[c];
-          if (mnr < 1e-12) S.degen = 1;
-          approx[c] = mine / (nq32 * static_cast<float>(mnr));
-        }
-      }
-      for (int c = nc + tid; c < c4; c += K5T) approx[c] = -INFINITY;
-    }
+    for (int c = nc + tid; c < c4; c += K5T) approx[c] = -INFINITY;
     if (tid == 0) S.ns = 0;
     __syncthreads();
     if (pass == 0) K5MARK(2)
@@ -392,6 +426,21 @@ __global__ void __launch_bounds__(K5T) k_select3(DevTables t, DecodeArgs a, int*
           S.snm[r0 + r] = t.nmem[s];
           S.snb[r0 + r] = t.nbuf[s];
           S.slz[r0 + r] = t.lazy[s];
+        }
+      }
+      if (pass == 0 && r0 == 0 && a.l2pf_pages > 0 && warp == 8 && ns > 0) {
+        // HBM is idle while this CTA is latency bound: pull the first pages of the likely
+        // selection (S contains every cluster that can be ranked) into L2 for K6; a small
+        // per-domain budget keeps the per-SM TMA issue short
+        const int per = min(16, (a.l2pf_pages + ns - 1) / ns);
+        for (int w = lane; w < ns * per; w += 32) {
+          const int s = cslot[S.sset[w / per]];
+          const int j = w % per;
+          const int np = t.npages[s];
+          const int pg = t.pages[static_cast<int64_t>(s) * t.maxp + j];
+          if (j < np && pg >= 0 && pg < t.max_pages)
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(page_k(t, pg)),
+                         "r"(static_cast<uint32_t>(t.page_bytes)) : "memory");
         }
       }
       __syncthreads();
@@ -470,43 +519,38 @@ __global__ void __launch_bounds__(K5T) k_select3(DevTables t, DecodeArgs a, int*
   __syncthreads();
   if (tid == 0) a.flags[l] = S.lazy_any;
   K5MARK(4)
-  {  // window ring tokens whose owner is not a verified cluster (retrieval.cpp:107-108)
+  {  // window ring tokens whose owner is not a verified cluster (retrieval.cpp:107-108), page-major:
+     // warp-sized runs of one ring page, so each warp's ballot IS 32 bits of that page's mask
     unsigned long long mine = 0;
-    const int n_ring = W * t.tmax;
-    const int n_pad = (n_ring + K5T - 1) / K5T * K5T;
-    for (int i = tid; i < n_pad; i += K5T) {
-      const int rs = i / t.tmax, tt = i - rs * t.tmax;
-      bool keep = i < n_ring && tt < S.ring_count[rs];
-      if (keep) {
-        const int own = owners[i];
-        if (own >= 0) {
-          int h = (own * 0x9E3779B1u) >> 25;
-          for (;;) {
-            const int v = S.vhash[h];
-            if (v == own) {
-              keep = false;
-              break;
+    const int P = t.P;
+    const int nv_tok = W * rpp * P;  // (P % 32 == 0: launch_select3)
+    for (int v0 = 0; v0 < nv_tok; v0 += K5T) {
+      const int v = v0 + tid;
+      bool keep = false;
+      if (v < nv_tok) {
+        const int pg = v / P, k = v - pg * P;
+        const int rs = pg / rpp, tt = (pg - rs * rpp) * P + k;
+        if (tt < S.ring_count[rs]) {
+          keep = true;
+          const int own = owners[rs * t.tmax + tt];
+          if (own >= 0) {
+            int h = (own * 0x9E3779B1u) >> 25;
+            for (;;) {
+              const int x = S.vhash[h];
+              if (x == own) {
+                keep = false;
+                break;
+              }
+              if (x < 0) break;
+              h = (h + 1) & 127;
             }
-            if (v < 0) break;
-            h = (h + 1) & 127;
           }
         }
       }
-      const int pg = keep ? rs * rpp + tt / t.P : -1;
-      const unsigned km = __ballot_sync(kFull, keep);
-      mine += keep ? 1 : 0;
-      if (km) {
-        const unsigned same = __match_any_sync(kFull, pg);
-        if (keep && pg < 64 && lane == __ffs(same) - 1) atomicAdd(&S.ring_cnt[pg], __popc(same));
-        const unsigned long long bit = keep ? 1ull << (tt % t.P) : 0ull;  // one shared atomic per (warp, page)
-        const unsigned blo = __reduce_or_sync(same, static_cast<unsigned>(bit));
-        const unsigned bhi = __reduce_or_sync(same, static_cast<unsigned>(bit >> 32));
-        if (keep && pg < 64 && (threadIdx.x & 31) == __ffs(same) - 1)
-          atomicOr(&S.ring_mask[pg], (static_cast<unsigned long long>(bhi) << 32) | blo);
-      }
+      const unsigned b = __ballot_sync(kFull, keep);
+      if (lane == 0 && v < nv_tok) S.ring_half[v >> 5] = b;
+      mine += lane == 0 ? __popc(b) : 0;
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(kFull, mine, o);
     if (lane == 0) atomicAdd(&S.att, mine);
   }
   __syncthreads();
@@ -528,7 +572,15 @@ __global__ void __launch_bounds__(K5T) k_select3(DevTables t, DecodeArgs a, int*
     const int vtot = tot0 + __shfl_sync(kFull, x1, 31);
     if (lane == 0) S.voff[nv] = vtot;
     const int nrp = min(W * rpp, 64);
-    const int r0 = lane < nrp && S.ring_cnt[lane] > 0 ? 1 : 0, r1 = lane + 32 < nrp && S.ring_cnt[lane + 32] > 0 ? 1 : 0;
+    const int hp = t.P / 32;  // 32-bit halves per page
+    auto page_mask = [&](int pg) -> unsigned long long {
+      return hp == 2 ? (static_cast<unsigned long long>(S.ring_half[2 * pg + 1]) << 32) | S.ring_half[2 * pg]
+                     : static_cast<unsigned long long>(S.ring_half[pg]);
+    };
+    if (lane < nrp) S.ring_mask[lane] = page_mask(lane);
+    if (lane + 32 < nrp) S.ring_mask[lane + 32] = page_mask(lane + 32);
+    const int r0 = lane < nrp && page_mask(lane) != 0ull ? 1 : 0;
+    const int r1 = lane + 32 < nrp && page_mask(lane + 32) != 0ull ? 1 : 0;
     const unsigned rm0 = __ballot_sync(kFull, r0), rm1 = __ballot_sync(kFull, r1);
     const unsigned lt = (1u << lane) - 1u;
     if (lane < nrp) S.ring_off[lane] = vtot + __popc(rm0 & lt);
@@ -568,7 +620,7 @@ __global__ void __launch_bounds__(K5T) k_select3(DevTables t, DecodeArgs a, int*
     if (page >= 0) desc[i] = make_int4(page, t.pg_fill[page] | (isb << 16), -1, -1);
   }
   for (int i = tid; i < W * rpp && i < 64; i += K5T)
-    if (S.ring_cnt[i] > 0 && S.ring_off[i] < a.max_desc) {
+    if (S.ring_mask[i] != 0ull && S.ring_off[i] < a.max_desc) {
       const int rs = i / rpp, j = i % rpp;
       const int page = t.ring_pages[(static_cast<int64_t>(l) * W + rs) * rpp + j];
       desc[S.ring_off[i]] = make_int4(page, t.pg_fill[page] | (2 << 16), static_cast<int>(S.ring_mask[i] & 0xffffffffu),
@@ -583,6 +635,12 @@ __global__ void __launch_bounds__(K5T) k_select3(DevTables t, DecodeArgs a, int*
   }
   if (a.n_items[l] == 0)
     for (int i = tid; i < d; i += K5T) a.out[static_cast<int64_t>(l) * d + i] = 0.f;
+  if (a.k4prof && threadIdx.x == 0) {
+    a.k4prof[l * 16 + 12] = clock64() - kc0;  // the tail after the last phase mark
+    unsigned long long gt;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+    a.k4prof[l * 16 + 14] = static_cast<long long>(gt);
+  }
 }
 
 }  // namespace
@@ -590,7 +648,8 @@ __global__ void __launch_bounds__(K5T) k_select3(DevTables t, DecodeArgs a, int*
 // Launches K4 v3 when the shape fits (d % 4 == 0, d <= 128, take lists <= 64, W * rpp <= 64);
 // returns false otherwise (the caller uses k_score_select2).
 bool launch_select3(const DevTables& t, const DecodeArgs& a, cudaStream_t st) {
-  if (t.d % 4 != 0 || t.d > 128 || t.W > 64 || t.W * t.rpp > 64 || a.k_s > 64 || a.prefetch_k > 64 || a.k_v > 64)
+  if (t.d % 4 != 0 || t.d > 128 || t.W > 64 || t.W * t.rpp > 64 || a.k_s > 64 || a.prefetch_k > 64 || a.k_v > 64 ||
+      t.P % 32 != 0)
     return false;
   const size_t smem = sel3_dyn_bytes(t.d, t.cmax, a.n_parts_host, t.W, t.tmax);
   if (smem + sizeof(Sel3Smem) > 220 * 1024) return false;
