@@ -325,6 +325,10 @@ struct Driver {
   std::int64_t last_partition = -1;
   bool check = true;  // run check_invariants / audit like engine.cpp:91-92,234-236
 
+  // token-baseline mode (engine.cpp:153-158, 179-203)
+  std::vector<std::vector<KVEntry>> pools;
+  TransferLedger baseline_ledger;
+
   std::vector<std::int64_t> last_assign;  // [L*T] routed cluster ids of the last frame
   std::int64_t last_pid = -1;
   RetrievalResult last_rr;
@@ -411,6 +415,13 @@ struct Driver {
   void frame(FrameInput&& f) {  // engine.cpp:134-174 (cluster mode)
     last_assign.assign(static_cast<std::size_t>(L) * f.layers[0].size(), -1);
     last_pid = -1;
+    if (cfg.retrieval.mode == RetrievalMode::TokenBaseline) {  // engine.cpp:153-158
+      pools.resize(static_cast<std::size_t>(L));
+      for (std::size_t l = 0; l < f.layers.size(); ++l)
+        for (const KVEntry& e : f.layers[l]) pools[l].push_back(e);
+      push_window(f);
+      return;
+    }
     if (!built) {
       pending.push_back(f);
       push_window(f);
@@ -429,6 +440,13 @@ struct Driver {
   }
 
   void query(const QueryBundle& b) {  // engine.cpp:176-237 (cluster mode)
+    if (cfg.retrieval.mode == RetrievalMode::TokenBaseline) {  // engine.cpp:179-203
+      std::set<std::int64_t> window_frames;
+      for (const FrameInput& f : window) window_frames.insert(f.frame_id);
+      pools.resize(static_cast<std::size_t>(L));
+      last_rr = retrieve_token_baseline(b, cfg.retrieval, pools, window_frames, cfg.cost, baseline_ledger);
+      return;
+    }
     if (!built) build_now();
     last_rr = retrieve(b, cfg.retrieval, *index, *store, *maint, window_entries());
     repin();
@@ -579,17 +597,19 @@ void ref_drv_maint_stats(void* h, std::int64_t* o) {
 // ops[5], bytes[5], cost[5]; returns device_entries
 std::int64_t ref_drv_ledger(void* h, std::int64_t* ops, std::int64_t* bytes, double* cost) {
   auto* drv = static_cast<Driver*>(h);
-  if (!drv->store) return 0;
+  const bool tok = drv->cfg.retrieval.mode == RetrievalMode::TokenBaseline;
+  if (!drv->store && !tok) return 0;
+  const TransferLedger& lg = tok ? drv->baseline_ledger : drv->store->ledger();
   const TransferCause causes[5] = {TransferCause::Retrieval, TransferCause::Maintenance,
                                    TransferCause::Prefetch, TransferCause::Completion,
                                    TransferCause::Offload};
   for (int i = 0; i < 5; ++i) {
-    CauseTotals t = drv->store->ledger().cause(causes[i]);
+    CauseTotals t = lg.cause(causes[i]);
     ops[i] = t.n_ops;
     bytes[i] = t.bytes;
     cost[i] = t.cost_us;
   }
-  return drv->store->device_entries();
+  return tok ? 0 : drv->store->device_entries();
 }
 
 int ref_drv_ledger_log_size(void* h) {

@@ -8,11 +8,16 @@
 #include "../../include/kvc.h"
 #include "context.hpp"
 #include "kmeans.hpp"
+#include "token.hpp"
 
 using kvc::Context;
+using kvc::TokenContext;
 
+// One of the two is set: the cluster path (Context) or the token-level baseline
+// (TokenContext, cfg.token_mode -- RetrievalMode::TokenBaseline, engine.cpp:153-158,179-203).
 struct kvc_ctx {
   std::unique_ptr<Context> impl;
+  std::unique_ptr<TokenContext> tok;
 };
 
 namespace {
@@ -36,8 +41,10 @@ int guard(F&& f) {
   }
 }
 
-// Host-state readers first complete the deferred bookkeeping of the last decode step.
+// Host-state readers first complete the deferred bookkeeping of the last decode step. Only call
+// inside guard(): a token-baseline context has no cluster index.
 Context& F(kvc_ctx* c) {
+  if (!c->impl) kvc::fail(KVC_E_CONFIG, "not available in token-baseline mode (cfg.token_mode)");
   try {
     c->impl->flush_pending();
   } catch (const std::exception& e) {
@@ -45,6 +52,15 @@ Context& F(kvc_ctx* c) {
   }
   return *c->impl;
 }
+
+// Entry points that return a count (not wrapped in guard): the cluster path only.
+#define KVC_CLUSTER_ONLY(ctx)                                                   \
+  do {                                                                          \
+    if (!(ctx)->impl) {                                                         \
+      g_err = "not available in token-baseline mode (cfg.token_mode)";          \
+      return KVC_E_CONFIG;                                                      \
+    }                                                                           \
+  } while (0)
 
 template <class T>
 int copy_out(const std::vector<T>& v, T* dst, int cap) {
@@ -113,7 +129,10 @@ int kvc_create(const kvc_cfg* cfg, int32_t d, int32_t L, kvc_ctx** out) {
     if (!cfg || !out) kvc::fail(KVC_E_CONFIG, "null argument");
     auto* h = new kvc_ctx;
     try {
-      h->impl = std::make_unique<Context>(*cfg, d, L);
+      if (cfg->token_mode)
+        h->tok = std::make_unique<TokenContext>(*cfg, d, L);
+      else
+        h->impl = std::make_unique<Context>(*cfg, d, L);
     } catch (...) {
       delete h;
       throw;
@@ -124,20 +143,37 @@ int kvc_create(const kvc_cfg* cfg, int32_t d, int32_t L, kvc_ctx** out) {
 
 void kvc_destroy(kvc_ctx* ctx) { delete ctx; }
 
-void* kvc_stream(kvc_ctx* ctx) { return ctx ? static_cast<void*>(ctx->impl->stream()) : nullptr; }
+void* kvc_stream(kvc_ctx* ctx) {
+  if (!ctx) return nullptr;
+  return ctx->tok ? static_cast<void*>(ctx->tok->stream()) : static_cast<void*>(ctx->impl->stream());
+}
 
 int kvc_ingest_frame(kvc_ctx* ctx, int64_t frame_id, const float* visual, const void* keys,
                      const void* values, int32_t T, int32_t mem, int64_t* assigned,
                      int64_t* partition) {
-  return guard([&] { F(ctx).ingest_frame(frame_id, visual, keys, values, T, mem, assigned, partition); });
+  return guard([&] {
+    if (ctx->tok) {  // engine.cpp:153-158: the entries join the pools
+      if (assigned) std::fill(assigned, assigned + static_cast<int64_t>(ctx->tok->L()) * (T > 0 ? T : 0), -1);
+      if (partition) *partition = -1;
+      ctx->tok->ingest_frame(frame_id, keys, values, T, mem);
+      return;
+    }
+    F(ctx).ingest_frame(frame_id, visual, keys, values, T, mem, assigned, partition);
+  });
 }
 
 int kvc_decode_step(kvc_ctx* ctx, int64_t query_id, const float* q, int32_t q_mem, float* out,
                     int32_t out_mem, const int64_t* gt, int32_t n_gt) {
-  return guard([&] { ctx->impl->decode_step(query_id, q, q_mem, out, out_mem, gt, n_gt); });
+  return guard([&] {
+    if (ctx->tok)
+      ctx->tok->decode_step(query_id, q, q_mem, out, out_mem, gt, n_gt);
+    else
+      ctx->impl->decode_step(query_id, q, q_mem, out, out_mem, gt, n_gt);
+  });
 }
 
 int kvc_last_ranked(kvc_ctx* ctx, int32_t layer, int64_t* ids, int32_t* is_buffer, int32_t cap) {
+  if (ctx->tok) return 0;  // no cluster ranking in the token baseline
   const auto& ls = F(ctx).last_layers();
   if (layer < 0 || layer >= static_cast<int>(ls.size())) return KVC_E_BAD_LAYER;
   const auto& r = ls[static_cast<std::size_t>(layer)].ranked;
@@ -149,12 +185,18 @@ int kvc_last_ranked(kvc_ctx* ctx, int32_t layer, int64_t* ids, int32_t* is_buffe
 }
 
 int kvc_last_selected(kvc_ctx* ctx, int32_t layer, int64_t* ids, int32_t cap) {
+  if (ctx->tok) return 0;
   const auto& ls = F(ctx).last_layers();
   if (layer < 0 || layer >= static_cast<int>(ls.size())) return KVC_E_BAD_LAYER;
   return copy_out(ls[static_cast<std::size_t>(layer)].selected, ids, cap);
 }
 
 int kvc_last_attended(kvc_ctx* ctx, int32_t layer, int64_t* frames, int32_t* tokens, int32_t cap) {
+  if (ctx->tok) {
+    int n = 0;
+    const int rc = guard([&] { n = ctx->tok->attended(layer, frames, tokens, cap); });
+    return rc != KVC_OK ? rc : n;
+  }
   const auto& ls = F(ctx).last_layers();
   if (layer < 0 || layer >= static_cast<int>(ls.size())) return KVC_E_BAD_LAYER;
   const auto& a = ls[static_cast<std::size_t>(layer)].attended;
@@ -166,6 +208,7 @@ int kvc_last_attended(kvc_ctx* ctx, int32_t layer, int64_t* frames, int32_t* tok
 }
 
 int kvc_last_layer_meta(kvc_ctx* ctx, int32_t layer, double* lat, int64_t* ints) {
+  if (ctx->tok) return guard([&] { ctx->tok->layer_meta(layer, lat, ints); });
   const auto& ls = F(ctx).last_layers();
   if (layer < 0 || layer >= static_cast<int>(ls.size())) return KVC_E_BAD_LAYER;
   const auto& lo = ls[static_cast<std::size_t>(layer)];
@@ -179,12 +222,17 @@ int kvc_last_layer_meta(kvc_ctx* ctx, int32_t layer, double* lat, int64_t* ints)
 }
 
 int kvc_last_query_meta(kvc_ctx* ctx, double* dd) {
+  if (ctx->tok) {
+    dd[0] = ctx->tok->ttft();
+    dd[1] = ctx->tok->recall();
+    return KVC_OK;
+  }
   dd[0] = F(ctx).last_ttft();
   dd[1] = F(ctx).last_recall();
   return KVC_OK;
 }
 
-uint64_t kvc_last_digest(kvc_ctx* ctx) { return F(ctx).last_digest(); }
+uint64_t kvc_last_digest(kvc_ctx* ctx) { return ctx->tok ? ctx->tok->digest() : F(ctx).last_digest(); }
 
 int kvc_flat_topk(kvc_ctx* ctx, const float* q, int32_t layer, int32_t k, int64_t* ids,
                   int32_t* is_buffer) {
@@ -213,9 +261,13 @@ int kvc_bulk_load(kvc_ctx* ctx, const float* visual, const void* keys, const voi
   });
 }
 
-int kvc_n_clusters(kvc_ctx* ctx) { return static_cast<int>(F(ctx).cluster_ids().size()); }
+int kvc_n_clusters(kvc_ctx* ctx) {
+  if (ctx->tok) return 0;
+  return static_cast<int>(F(ctx).cluster_ids().size());
+}
 
 int kvc_cluster_ids(kvc_ctx* ctx, int64_t* ids, int32_t cap) {
+  if (ctx->tok) return 0;
   return copy_out(F(ctx).cluster_ids(), ids, cap);
 }
 
@@ -242,6 +294,7 @@ int kvc_cluster(kvc_ctx* ctx, int64_t id, int64_t* info, double* var, double* re
 
 int kvc_cluster_entries(kvc_ctx* ctx, int64_t id, int32_t which, int64_t* frames, int32_t* tokens,
                         int32_t cap) {
+  KVC_CLUSTER_ONLY(ctx);
   const kvc::Cluster* c = F(ctx).cluster(id);
   if (!c) return KVC_E_UNKNOWN_CLUSTER;
   const auto& v = which == 0 ? c->members : c->buffer;
@@ -262,9 +315,13 @@ int kvc_cluster_payload(kvc_ctx* ctx, int64_t id, int32_t which, float* keys, fl
   return rc != KVC_OK ? rc : n;
 }
 
-int kvc_n_partitions(kvc_ctx* ctx) { return static_cast<int>(F(ctx).partitions().size()); }
+int kvc_n_partitions(kvc_ctx* ctx) {
+  if (ctx->tok) return 0;
+  return static_cast<int>(F(ctx).partitions().size());
+}
 
 int kvc_partition(kvc_ctx* ctx, int32_t p, double* visual_rep, int64_t* frames, int32_t cap) {
+  KVC_CLUSTER_ONLY(ctx);
   const auto& ps = F(ctx).partitions();
   if (p < 0 || p >= static_cast<int>(ps.size())) return KVC_E_UNKNOWN_CLUSTER;
   const auto& part = ps[static_cast<std::size_t>(p)];
@@ -273,6 +330,7 @@ int kvc_partition(kvc_ctx* ctx, int32_t p, double* visual_rep, int64_t* frames, 
 }
 
 int kvc_partition_layer(kvc_ctx* ctx, int32_t p, int32_t layer, int64_t* ids, int32_t cap) {
+  KVC_CLUSTER_ONLY(ctx);
   const auto& ps = F(ctx).partitions();
   if (p < 0 || p >= static_cast<int>(ps.size())) return KVC_E_UNKNOWN_CLUSTER;
   if (layer < 0 || layer >= F(ctx).L()) return KVC_E_BAD_LAYER;
@@ -280,11 +338,16 @@ int kvc_partition_layer(kvc_ctx* ctx, int32_t p, int32_t layer, int64_t* ids, in
 }
 
 int kvc_maint_stats(kvc_ctx* ctx, int64_t* out) {
+  if (ctx->tok) {  // the baseline never runs the maintainer
+    std::memset(out, 0, 9 * sizeof(int64_t));
+    return KVC_OK;
+  }
   std::memcpy(out, F(ctx).maint_stats(), 9 * sizeof(int64_t));
   return KVC_OK;
 }
 
 int64_t kvc_ledger(kvc_ctx* ctx, int64_t* ops, int64_t* bytes, double* cost_us) {
+  if (ctx->tok) return ctx->tok->ledger(ops, bytes, cost_us);  // the baseline ledger (engine.cpp:184)
   for (int i = 0; i < 5; ++i) {
     ops[i] = 0;
     bytes[i] = 0;
@@ -298,9 +361,11 @@ int64_t kvc_ledger(kvc_ctx* ctx, int64_t* ops, int64_t* bytes, double* cost_us) 
   return F(ctx).device_entries();
 }
 
-int kvc_ledger_log_size(kvc_ctx* ctx) { return static_cast<int>(F(ctx).ledger().size()); }
+// (token baseline: totals only -- one op per coalesced run would be thousands per query)
+int kvc_ledger_log_size(kvc_ctx* ctx) { return ctx->tok ? 0 : static_cast<int>(F(ctx).ledger().size()); }
 
 int kvc_ledger_op(kvc_ctx* ctx, int32_t i, int64_t* ints) {
+  KVC_CLUSTER_ONLY(ctx);
   const auto& lg = F(ctx).ledger();
   if (i < 0 || i >= static_cast<int>(lg.size())) return KVC_E_CONFIG;
   const auto& op = lg[static_cast<std::size_t>(i)];
@@ -348,15 +413,20 @@ int kvc_cluster_tier(kvc_ctx* ctx, int64_t id, int64_t* out) {
   return guard([&] { F(ctx).cluster_tier(id, out); });
 }
 
-int64_t kvc_launch_count(kvc_ctx* ctx) { return ctx->impl->launches(); }
+int64_t kvc_launch_count(kvc_ctx* ctx) { return ctx->tok ? ctx->tok->launches() : ctx->impl->launches(); }
 
 int kvc_last_step_timing(kvc_ctx* ctx, double* t) {
-  const double* s = ctx->impl->step_timing();
+  const double* s = ctx->tok ? ctx->tok->step_timing() : ctx->impl->step_timing();
   for (int i = 0; i < 10; ++i) t[i] = s[i];
   return KVC_OK;
 }
 
-void kvc_set_timing(kvc_ctx* ctx, int32_t on) { ctx->impl->set_timing(on != 0); }
+void kvc_set_timing(kvc_ctx* ctx, int32_t on) {
+  if (ctx->tok)
+    ctx->tok->set_timing(on != 0);
+  else
+    ctx->impl->set_timing(on != 0);
+}
 
 int kvc_debug_assign_check(kvc_ctx* ctx, const void* keys, int32_t T, int64_t partition, int32_t mem,
                            double* out4) {
@@ -371,11 +441,13 @@ int kvc_debug_div_check(uint64_t n, uint64_t seed, int32_t max_den, uint64_t* mi
 }
 
 int kvc_debug_resolve_profile(kvc_ctx* ctx, double* out) {
+  KVC_CLUSTER_ONLY(ctx);
   ctx->impl->resolve_profile(out);
   return KVC_OK;
 }
 
 int kvc_last_ingest_timing(kvc_ctx* ctx, double* t) {
+  KVC_CLUSTER_ONLY(ctx);
   const double* s = ctx->impl->ingest_timing();
   for (int i = 0; i < 8; ++i) t[i] = s[i];
   return KVC_OK;

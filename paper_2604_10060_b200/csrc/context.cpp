@@ -68,7 +68,7 @@ Context::Context(const kvc_cfg& cfg, int d, int L) : cfg_(cfg), d_(d), L_(L) {
   if (cfg_.n0 <= 0.0) fail(-10, "threshold horizon must be positive");
   if (cfg_.max_split_depth < 1) fail(-10, "split depth must be at least 1");
   if (cfg_.visual_floor < -1.0 || cfg_.visual_floor > 1.0) fail(-10, "visual floor must be a cosine value");
-  if (cfg_.token_mode) fail(-10, "token-baseline mode is served by the token ablation entry points");
+  if (cfg_.token_mode) fail(-10, "token-baseline mode is served by TokenContext (kvc_create dispatches on cfg.token_mode)");
   if (cfg_.kv_dtype != KVC_DTYPE_F32 && cfg_.kv_dtype != KVC_DTYPE_BF16) fail(-10, "kv_dtype");
   // (<= 64: a window page's dedup mask is one 64-bit word of its attention descriptor)
   if (cfg_.page_tokens < 8 || cfg_.page_tokens > 64 || cfg_.page_tokens % 8) fail(-10, "page_tokens must be 8..64, a multiple of 8");

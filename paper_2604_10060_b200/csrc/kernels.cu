@@ -2740,6 +2740,25 @@ int launch_attend_t(const DevTables& t, const DecodeArgs& a, cudaStream_t st, bo
 }
 }  // namespace
 
+int launch_attend(const DevTables& t, const DecodeArgs& a, cudaStream_t st) {
+  if (!g_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  switch (t.d * 2 + t.kv_bf16) {
+    case 64: return launch_attend_t<32, false>(t, a, st, false);
+    case 65: return launch_attend_t<32, true>(t, a, st, false);
+    case 128: return launch_attend_t<64, false>(t, a, st, false);
+    case 129: return launch_attend_t<64, true>(t, a, st, false);
+    case 256: return launch_attend_t<128, false>(t, a, st, false);
+    case 257: return launch_attend_t<128, true>(t, a, st, false);
+    case 512: return launch_attend_t<256, false>(t, a, st, false);
+    case 513: return launch_attend_t<256, true>(t, a, st, false);
+    default: return 0;
+  }
+}
+
 int launch_decode(const DevTables& t, const DecodeArgs& a, cudaStream_t st, cudaEvent_t* ev, cudaEvent_t k4_done) {
   if (!g_sms) {
     int dev = 0;

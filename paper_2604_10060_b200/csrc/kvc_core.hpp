@@ -222,6 +222,10 @@ int launch_topm(const DevTables& t, const IngestArgs& a, cudaStream_t st);
 int launch_store_rows(const DevTables& t, const IngestArgs& a, cudaStream_t st);
 int launch_ring_write(const DevTables& t, const void* fk, const void* fv, int32_t T,
                       int32_t ring_slot, cudaStream_t st);
+// K6 alone over a prepared work list (desc / n_desc / n_items / partials / out of `a`; the work
+// counter a.work_ctr must be zero). Used by the token-level baseline.
+int launch_attend(const DevTables& t, const DecodeArgs& a, cudaStream_t st);
+
 // K4 v3 (select.cu); false when the shape does not fit it.
 bool launch_select3(const DevTables& t, const DecodeArgs& a, cudaStream_t st);
 // k4_done (may be null) is recorded between the score/select and attention kernels.
