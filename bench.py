@@ -55,6 +55,7 @@ def parse():
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-offload", action="store_true", help="skip the config-3 host-tier measurement")
+    p.add_argument("--no-streams", action="store_true", help="skip the config-5 streams + token-ablation measurement")
     p.add_argument("--domains", type=int, default=D_TOTAL)
     return p.parse_args()
 
@@ -389,6 +390,11 @@ def main():
     }
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args)
+    if world == 1 and not args.no_streams:
+        try:
+            line["streams"] = streams_phase(args)
+        except Exception as e:
+            line["streams"] = {"error": f"{type(e).__name__}: {e}"}
     if world == 1 and not args.no_offload:
         del kv, q_dev, out_dev
         torch.cuda.empty_cache()
@@ -484,6 +490,74 @@ def offload_phase(args):
         "h2d_gbs_wall": round((s5["bytes_h2d"] - s4["bytes_h2d"]) / max(h2d_s, 1e-9) / 1e9, 2),
         "migrated_clusters": len(moved), "in_flight_at_end_of_cold_steps": s2["in_flight"] + s2["queued"],
         "dma_copies": {"offload_batch": s4["copies"] - s3["copies"], "fetch_batch": s5["copies"] - s4["copies"]},
+    }
+
+
+def streams_phase(args):
+    """Config 5 per-GPU share: 4 of 32 independent streams (32 streams partitioned by stream over 8
+    GPUs, no collective), each LLaVA-shaped (112 domains) with 65,464 tokens (334 frames x 196) in
+    128 clusters of ~512, top-16 + 4-frame window; all 4 contexts decode concurrently (one CUDA
+    stream each). Ablation: the token-level top-k baseline (retrieval.cpp:166-254) on the same rows
+    at the same budget (16 x 512 tokens), also 4 concurrent contexts."""
+    import torch
+
+    from paper_2604_10060_b200 import ClusterKVCache, Config, DTYPE_BF16, workload
+
+    S_, D5, T5 = 4, D_TOTAL, T_FRAME
+    NF = 334
+    N5, C5, BUDGET = NF * T5, 128, 16 * 512
+    clu, tok, qs = [], [], []
+    t0 = time.time()
+    for si in range(S_):
+        st = workload.clustered_state(D5, N5, C5, HEAD_DIM, T5, seed=500 + si)
+        kv_bytes = D5 * (N5 + 64 * C5 + WINDOW * T5) * HEAD_DIM * 2 * 2
+        ccfg = Config.make(kv_dtype=DTYPE_BF16, k_v=1, k_s=TOP_K, window_frames=WINDOW, build_batch_frames=1,
+                           offload_horizon_frames=1 << 30, device_capacity_entries=1 << 40,
+                           pool_bytes=int(1.3 * kv_bytes), max_slots=max(4096, 4 * D5 * C5), max_cluster_pages=512,
+                           max_tokens=T5, host_pool_bytes=0)
+        kc = ClusterKVCache(ccfg, HEAD_DIM, D5)
+        kc.bulk_load(st.visual, st.keys, st.values, st.assign, st.frame_ids, st.token_ids, C5)
+        tcfg = Config.make(kv_dtype=DTYPE_BF16, token_mode=1, token_budget=BUDGET, window_frames=WINDOW,
+                           pool_bytes=D5 * N5 * HEAD_DIM * 2 * 2, max_tokens=T5)
+        kt = ClusterKVCache(tcfg, HEAD_DIM, D5)
+        for f in range(NF):  # the same rows, frame by frame, from HBM
+            kt.process_frame(f, st.visual, st.keys[:, f * T5:(f + 1) * T5].contiguous(),
+                             st.values[:, f * T5:(f + 1) * T5].contiguous(), want_assigned=False)
+        qs.append(workload.queries_near(st, args.warmup + args.steps, seed=900 + si))
+        del st
+        clu.append(kc)
+        tok.append(kt)
+    torch.cuda.synchronize()
+    setup_s = time.time() - t0
+    outs = [torch.zeros(D5, HEAD_DIM, device="cuda") for _ in range(S_)]
+
+    def run(ctxs, host_sync):
+        for i in range(args.warmup):
+            for s_, c in enumerate(ctxs):
+                c.query(i, qs[s_][i], out=outs[s_])
+        torch.cuda.synchronize()
+        h0 = time.perf_counter()
+        for i in range(args.warmup, args.warmup + args.steps):
+            for s_, c in enumerate(ctxs):
+                c.query(i, qs[s_][i], out=outs[s_])
+        torch.cuda.synchronize()
+        return (time.perf_counter() - h0) * 1e6 / args.steps
+
+    clu_us = run(clu, False)
+    tok_us = run(tok, True)
+    att_c = float(np.mean([clu[0].layer_meta(l).attended_count for l in range(D5)]))
+    att_t = float(np.mean([tok[0].layer_meta(l).attended_count for l in range(D5)]))
+    return {
+        "workload": "config5 per-GPU share: 4 of 32 streams, each 112 domains x 65,464 tokens (334 frames x 196), "
+                    "128 clusters/domain, top-16 + 4-frame window, bf16; token ablation at budget 8,192",
+        "cluster_us_per_step_all_streams": round(clu_us, 1),
+        "cluster_stream_steps_per_s": round(S_ * 1e6 / clu_us, 1),
+        "token_us_per_step_all_streams": round(tok_us, 1),
+        "token_stream_steps_per_s": round(S_ * 1e6 / tok_us, 1),
+        "token_over_cluster_time": round(tok_us / clu_us, 2),
+        "attended_per_domain": {"cluster": round(att_c, 1), "token": round(att_t, 1)},
+        "timing": "wall clock over all streams' steps (host bookkeeping included), torch.cuda.synchronize on both sides",
+        "setup_s": round(setup_s, 1),
     }
 
 

@@ -441,7 +441,7 @@ int kvc_debug_div_check(uint64_t n, uint64_t seed, int32_t max_den, uint64_t* mi
 }
 
 int kvc_debug_resolve_profile(kvc_ctx* ctx, double* out) {
-  KVC_CLUSTER_ONLY(ctx);
+  if (ctx->tok) return guard([&] { ctx->tok->profile(out); });  // token-baseline select phases
   ctx->impl->resolve_profile(out);
   return KVC_OK;
 }

@@ -24,6 +24,9 @@ struct TokArgs {
   uint32_t* pick;             // [L][wcap] picked rows (top token_budget)
   uint32_t* attw;             // [L][wcap] attended rows (picked | window)
   int32_t* att_idx;           // [L][max_att] attended rows in order
+  int32_t* bidx;              // [L][cap] boundary rows (scratch)
+  double* bsim;               // [L][cap] their exact cosines (scratch)
+  long long* btie;            // [L][cap] their (frame id << 24 | token) tie-break keys (scratch)
   int32_t max_att, pages_per_dom;
   const int32_t* fidx;        // [cap] frame ordinal of each pool row (same for every domain)
   const int64_t* fid;         // [frames] frame id of each ordinal
@@ -32,7 +35,8 @@ struct TokArgs {
   int32_t* stats;             // [L][4] attended rows, host-side runs, host-side rows, boundary size
   const float* q;             // [L][d] current query
   int32_t* work_ctr;          // K6 work counter (reset by the select kernel)
-  int32_t* err;               // error bits (1: degenerate vector, 64: boundary overflow)
+  long long* prof;            // [L][8] clock64 cycles per select phase (instrumentation)
+  int32_t* err;               // error bits (1: degenerate vector, 64: > 1024 rows tie at the boundary value)
 };
 
 int launch_tok_append(const TokArgs& a, const void* fk, const void* fv, int T, int tmax, int64_t n0, cudaStream_t st);
@@ -59,6 +63,7 @@ class TokenContext {
   std::int64_t launches() const { return launches_; }
   void set_timing(bool on) { timing_ = on; }
   const double* step_timing() const { return step_t_; }
+  void profile(double* out);  // mean select-phase cycles over domains (out[8])
 
  private:
   kvc_cfg cfg_;
@@ -88,7 +93,7 @@ class TokenContext {
   // last query
   std::vector<std::vector<std::pair<std::int64_t, std::int32_t>>> att_;
   std::vector<double> lat_;  // [L][5]
-  std::vector<std::int64_t> attc_;
+  std::vector<std::int64_t> attc_, bnd_;
   double ttft_ = 0.0, recall_ = -1.0;
   std::uint64_t digest_ = 0;
   // baseline ledger totals (cause Retrieval, retrieval.cpp:224-229)

@@ -45,6 +45,7 @@ TokenContext::TokenContext(const kvc_cfg& cfg, int d, int L) : cfg_(cfg), d_(d),
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
     fail(-22, "no CUDA device: the B200 path has no CPU fallback");
   es_ = cfg_.kv_dtype == KVC_DTYPE_BF16 ? 2 : 4;
+  if (d * es_ > 512) fail(-10, "token baseline rows are at most 512 bytes (fp32 d <= 128, bf16 d <= 256)");
   KVC_CUDA(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
   for (auto& e : ev_) KVC_CUDA(cudaEventCreate(&e));
   const std::int64_t rb = static_cast<std::int64_t>(d) * es_;
@@ -67,6 +68,9 @@ TokenContext::TokenContext(const kvc_cfg& cfg, int d, int L) : cfg_(cfg), d_(d),
   const std::int64_t max_att = std::min<std::int64_t>(cap, cfg_.token_budget + static_cast<std::int64_t>(cfg_.window_frames) * tmax_);
   ta_.max_att = static_cast<std::int32_t>(max_att);
   ta_.att_idx = static_cast<std::int32_t*>(dalloc(static_cast<std::size_t>(L) * max_att * 4));
+  ta_.bidx = static_cast<std::int32_t*>(dalloc(static_cast<std::size_t>(L) * cap * 4));
+  ta_.bsim = static_cast<double*>(dalloc(static_cast<std::size_t>(L) * cap * 8));
+  ta_.btie = static_cast<long long*>(dalloc(static_cast<std::size_t>(L) * cap * 8));
   d_fidx_ = static_cast<std::int32_t*>(dalloc(static_cast<std::size_t>(cap) * 4));
   d_fid_ = static_cast<std::int64_t*>(dalloc(static_cast<std::size_t>(max_frames_) * 8));
   d_fstart_ = static_cast<std::int64_t*>(dalloc(static_cast<std::size_t>(max_frames_) * 8));
@@ -76,6 +80,7 @@ TokenContext::TokenContext(const kvc_cfg& cfg, int d, int L) : cfg_(cfg), d_(d),
   ta_.frame_hit = static_cast<std::uint8_t*>(dalloc(static_cast<std::size_t>(max_frames_)));
   ta_.stats = static_cast<std::int32_t*>(dalloc(static_cast<std::size_t>(L) * 16));
   ta_.err = static_cast<std::int32_t*>(dalloc(16));
+  ta_.prof = static_cast<long long*>(dalloc(static_cast<std::size_t>(L) * 8 * 8));
   ta_.work_ctr = static_cast<std::int32_t*>(dalloc(64));
   d_q_ = static_cast<float*>(dalloc(static_cast<std::size_t>(L) * d * 4));
   d_out_ = static_cast<float*>(dalloc(static_cast<std::size_t>(L) * d * 4));
@@ -118,6 +123,7 @@ TokenContext::TokenContext(const kvc_cfg& cfg, int d, int L) : cfg_(cfg), d_(d),
   att_.resize(static_cast<std::size_t>(L));
   lat_.assign(static_cast<std::size_t>(L) * 5, 0.0);
   attc_.assign(static_cast<std::size_t>(L), 0);
+  bnd_.assign(static_cast<std::size_t>(L), 0);
   KVC_CUDA(cudaStreamSynchronize(st_));
 }
 
@@ -133,6 +139,7 @@ TokenContext::~TokenContext() {
 void TokenContext::ingest_frame(std::int64_t frame_id, const void* keys, const void* values, int T, int mem) {
   if (T < 1 || T > tmax_) fail(-10, "tokens per frame outside [1, max_tokens]");
   if (!keys || !values) fail(-10, "null frame buffer");
+  if (frame_id < 0 || frame_id >= (1LL << 39)) fail(-10, "token baseline frame ids must be in [0, 2^39)");
   if (n_ + T > ta_.cap) fail(-21, "token pool full (raise kvc_cfg.pool_bytes)");
   const std::size_t row = static_cast<std::size_t>(T) * d_ * es_;
   const std::size_t pitch = static_cast<std::size_t>(tmax_) * d_ * es_;
@@ -193,7 +200,7 @@ void TokenContext::decode_step(std::int64_t qid, const float* q, int q_mem, floa
     KVC_CUDA(cudaMemsetAsync(ta_.err, 0, 4, st_));
     KVC_CUDA(cudaStreamSynchronize(st_));
     if (e & 1) fail(-2, "cosine of zero vector");
-    if (e & 64) fail(-21, "token boundary set exceeds its capacity (near-threshold ties)");
+    if (e & 64) fail(-21, "more than 1024 rows share the exact boundary value");
     fail(-1, "device error");
   }
   // latency model and ledger (retrieval.cpp:185-242): one op per run of adjacent host-side tokens
@@ -210,6 +217,7 @@ void TokenContext::decode_step(std::int64_t qid, const float* q, int q_mem, floa
     lt[1] = static_cast<double>(ops) * cfg_.alpha_us + static_cast<double>(htok * eb) * cfg_.beta_us_per_byte;
     lt[4] = cfg_.compute_cost_per_token_us * static_cast<double>(h_stats_[l * 4 + 0]);
     attc_[static_cast<std::size_t>(l)] = h_stats_[l * 4 + 0];
+    bnd_[static_cast<std::size_t>(l)] = h_stats_[l * 4 + 3];
     led_ops_ += ops;
     led_bytes_ += htok * eb;
     led_cost_ += lt[1];
@@ -266,7 +274,8 @@ int TokenContext::attended(int layer, std::int64_t* frames, std::int32_t* tokens
 void TokenContext::layer_meta(int layer, double* lat, std::int64_t* ints) const {
   if (layer < 0 || layer >= L_) fail(-7, "layer out of range");
   for (int i = 0; i < 5; ++i) lat[i] = lat_[static_cast<std::size_t>(layer) * 5 + i];
-  ints[0] = ints[1] = ints[2] = ints[3] = 0;
+  ints[0] = ints[1] = ints[2] = 0;
+  ints[3] = bnd_[static_cast<std::size_t>(layer)];  // (token mode) rows re-scored exactly at the boundary
   ints[4] = attc_[static_cast<std::size_t>(layer)];
 }
 
@@ -280,6 +289,16 @@ std::int64_t TokenContext::ledger(std::int64_t* ops, std::int64_t* bytes, double
   bytes[0] = led_bytes_;
   cost[0] = led_cost_;
   return 0;
+}
+
+void TokenContext::profile(double* out) {
+  std::vector<long long> p(static_cast<std::size_t>(L_) * 8);
+  KVC_CUDA(cudaMemcpy(p.data(), ta_.prof, p.size() * 8, cudaMemcpyDeviceToHost));
+  for (int k = 0; k < 8; ++k) {
+    double s = 0.0;
+    for (int l = 0; l < L_; ++l) s += static_cast<double>(p[static_cast<std::size_t>(l) * 8 + k]);
+    out[k] = s / L_;
+  }
 }
 
 }  // namespace kvc

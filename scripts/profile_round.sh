@@ -11,12 +11,12 @@ timeout 900 python bench.py > "$OUT/bench.json" 2> "$OUT/bench.err"
 timeout 900 python bench.py --impl reference > "$OUT/bench_reference.json" 2> "$OUT/bench_reference.err"
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none \
   -k regex:"k_(attend|score_select|select3|resolve|approx|topm|assign|build_cands|store_rows|ring_write|append|tier)" -c 600 --csv \
-  --log-file "$OUT/launches.csv" python bench.py --steps 5 --warmup 3 --frames 5 --no-cpu-baseline --no-offload > "$OUT/ncu_launch.log" 2>&1
+  --log-file "$OUT/launches.csv" python bench.py --steps 5 --warmup 3 --frames 5 --no-cpu-baseline --no-offload --no-streams > "$OUT/ncu_launch.log" 2>&1
 # decode kernels (skip the warm-up launches), then ingest kernels
 timeout 1200 ncu --set full --clock-control none --import-source on \
   -k regex:"k_(attend|select3|score_select)" -s 6 -c 2 -o "$OUT/full_decode" \
-  python bench.py --steps 5 --warmup 3 --frames 5 --no-cpu-baseline --no-offload > "$OUT/ncu_full_decode.log" 2>&1
+  python bench.py --steps 5 --warmup 3 --frames 5 --no-cpu-baseline --no-offload --no-streams > "$OUT/ncu_full_decode.log" 2>&1
 timeout 1200 ncu --set full --clock-control none --import-source on \
   -k regex:"k_(resolve|assign|approx|topm)" -s 12 -c 3 -o "$OUT/full_ingest" \
-  python bench.py --steps 5 --warmup 3 --frames 5 --no-cpu-baseline --no-offload > "$OUT/ncu_full_ingest.log" 2>&1
+  python bench.py --steps 5 --warmup 3 --frames 5 --no-cpu-baseline --no-offload --no-streams > "$OUT/ncu_full_ingest.log" 2>&1
 ls -la "$OUT"
