@@ -10,7 +10,7 @@ timeout 900 python -m pytest tests -m gpu -q > "$OUT/pytest_gpu.txt" 2>&1
 timeout 900 python bench.py > "$OUT/bench.json" 2> "$OUT/bench.err"
 timeout 900 python bench.py --impl reference > "$OUT/bench_reference.json" 2> "$OUT/bench_reference.err"
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none \
-  -k regex:"k_(attend|score_select|select3|resolve|approx|topm|assign|build_cands|store_rows|ring_write|append|tier)" -c 600 --csv \
+  -k regex:"k_(attend|score_select|select3|resolve|approx|topm|assign|build_cands|store_rows|ring_write|append|tier|tok)" -c 600 --csv \
   --log-file "$OUT/launches.csv" python bench.py --steps 5 --warmup 3 --frames 5 --no-cpu-baseline --no-offload --no-streams > "$OUT/ncu_launch.log" 2>&1
 # decode kernels (skip the warm-up launches), then ingest kernels
 timeout 1200 ncu --set full --clock-control none --import-source on \
@@ -20,3 +20,6 @@ timeout 1200 ncu --set full --clock-control none --import-source on \
   -k regex:"k_(resolve|assign|approx|topm)" -s 12 -c 3 -o "$OUT/full_ingest" \
   python bench.py --steps 5 --warmup 3 --frames 5 --no-cpu-baseline --no-offload --no-streams > "$OUT/ncu_full_ingest.log" 2>&1
 ls -la "$OUT"
+# token-level baseline kernels (config-5 shape, one stream)
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"k_tok_(approx|select|gather)|k_attend" -c 40 --csv \
+  --log-file "$OUT/launches_token.csv" python scripts/kernel_times.py token 3 > "$OUT/ncu_launch_token.log" 2>&1

@@ -73,6 +73,28 @@ for k, v in sorted(agg.items(), key=lambda x: -sum(x[1])):
 setup = [f"{k} ({len(v)} launches, {sum(v)/1e3:.1f} ms)" for k, v in agg.items() if k in SETUP]
 if setup:
     lines += ["", "Setup (bulk load, outside every timed region; excluded from the shares): " + ", ".join(setup) + "."]
+tok_csv = os.path.join(src, "launches_token.csv")
+if os.path.exists(tok_csv):
+    shutil.copy(tok_csv, os.path.join(dst, f"{tag}_launches_token.csv"))
+    import re
+
+    trows = list(csv.reader(open(tok_csv)))
+    try:
+        thi = next(i for i, r in enumerate(trows) if "Kernel Name" in r)
+        th = trows[thi]
+        tk, tv, tu = th.index("Kernel Name"), th.index("Metric Value"), th.index("Metric Unit")
+        tagg = collections.defaultdict(list)
+        for r in trows[thi + 1:]:
+            m = re.search(r"\b(k_\w+)", r[tk])
+            v = float(r[tv].replace(",", ""))
+            v = v / 1e3 if r[tu] in ("ns", "nsecond") else v
+            tagg[m.group(1) if m else r[tk][:30]].append(v)
+        lines += ["", "## Token-level baseline (config-5 shape, one stream: 112 domains x 65,464 tokens, budget 8,192)", "",
+                  "| kernel | launches | mean us |", "|---|---|---|"]
+        for k, v in sorted(tagg.items(), key=lambda x: -sum(x[1])):
+            lines.append(f"| {k} | {len(v)} | {sum(v)/len(v):.1f} |")
+    except StopIteration:
+        pass
 lines += ["", "## `ncu --set full` captures", "",
           "| kernel | duration us | DRAM read MB | DRAM write MB | DRAM % peak | SM % | achieved occupancy | regs |",
           "|---|---|---|---|---|---|---|---|"]
