@@ -56,6 +56,7 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-offload", action="store_true", help="skip the config-3 host-tier measurement")
     p.add_argument("--no-streams", action="store_true", help="skip the config-5 streams + token-ablation measurement")
+    p.add_argument("--exchange", default="fused", choices=["fused", "nccl"], help="multi-GPU output exchange")
     p.add_argument("--domains", type=int, default=D_TOTAL)
     return p.parse_args()
 
@@ -204,7 +205,7 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    from paper_2604_10060_b200.sharding import gather_domain_outputs, shard_domains
+    from paper_2604_10060_b200.sharding import FusedExchange, gather_domain_outputs, shard_domains
 
     d0, d1 = shard_domains(args.domains, world, rank)  # strong scaling over (layer, head) domains
     D = d1 - d0
@@ -273,8 +274,28 @@ def main():
     nq = args.warmup + args.steps
     q_dev = workload.queries_near(st, nq, seed=11 + rank)
     out_dev = torch.zeros(D, HEAD_DIM, device="cuda")
+    # multi-GPU output exchange: fused into the attention kernel (peer-memory row stores through
+    # CUDA IPC mappings + a per-step signal/wait), or NCCL all-gather (--exchange nccl / fallback)
+    exchange = "none"
+    ex = None
+    full_out = torch.zeros(args.domains, HEAD_DIM, device="cuda")
+    if world > 1:
+        exchange = "nccl"
+        if args.exchange == "fused":
+            try:
+                ex = FusedExchange(kv, args.domains)
+                exchange = "fused"
+            except Exception as e:  # e.g. no peer access: the collective still works
+                print(f"fused exchange unavailable ({e}); using NCCL all-gather", file=sys.stderr)
+
+    def exchange_step():
+        if ex is not None:
+            ex.gathered(full_out)
+        elif world > 1:
+            gather_domain_outputs(out_dev, args.domains)
     for i in range(args.warmup):
         kv.query(i, q_dev[i], out=out_dev)
+        exchange_step()
     launches0 = kv.launch_count()
     torch.cuda.synchronize()
     if world > 1:
@@ -287,8 +308,7 @@ def main():
             step_ev = []
             for i in range(args.warmup, nq):
                 kv.query(i, q_dev[i], out=out_dev)
-                if world > 1:  # per-domain outputs to every rank (NCCL over NVLink)
-                    gather_domain_outputs(out_dev, args.domains)
+                exchange_step()  # per-domain outputs to every rank
                 e = torch.cuda.Event(enable_timing=True)  # step boundary (after K6, before the next K4)
                 e.record(stream)
                 step_ev.append(e)
@@ -388,6 +408,9 @@ def main():
                    "clocks": clk_ingest.summary()},
         "bulk_load_s": round(load_s, 2),
     }
+    if world > 1:
+        line["config"]["output_exchange"] = ("fused: K6 stores output rows into every rank's buffer over peer memory, "
+                                             "per-step signal/wait" if exchange == "fused" else "NCCL all-gather")
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args)
     if world == 1 and not args.no_streams:

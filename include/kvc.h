@@ -222,6 +222,24 @@ KVC_API int kvc_cluster_tier(kvc_ctx* ctx, int64_t id, int64_t* out);
  * member count / logical device tail. All zero after kvc_tier_sync. */
 KVC_API int kvc_debug_tier_check(kvc_ctx* ctx, int64_t* out4);
 
+/* ------------------------------------------------------------------ multi-GPU: fused output exchange
+ * Domains are sharded over ranks (one process per GPU). Instead of an all-gather pass after each
+ * decode step, the attention kernel's split-KV combine stores every finished output row directly
+ * into every rank's exchange buffer over peer memory (NVLink; CUDA IPC mappings), and a per-step
+ * signal/wait pair orders the ranks. Exchange buffer of a rank (kvc_ipc_alloc,
+ * kvc_exchange_bytes): [2 step parities][total_domains][d] f32 followed by n_ranks u64 flags,
+ * zero-initialised. Each rank passes the mapped buffers of all ranks (its own included), in rank
+ * order, to kvc_set_peers; every rank must then run the same number of decode steps.
+ * kvc_peer_output copies the last step's gathered [total_domains][d] outputs (stream order). */
+KVC_API size_t kvc_exchange_bytes(int32_t n_ranks, int32_t total_domains, int32_t d);
+KVC_API int kvc_ipc_alloc(size_t bytes, void** dptr, uint8_t* handle64);
+KVC_API int kvc_ipc_open(const uint8_t* handle64, void** dptr);
+KVC_API int kvc_ipc_close(void* dptr);
+KVC_API int kvc_ipc_free(void* dptr);
+KVC_API int kvc_set_peers(kvc_ctx* ctx, int32_t n_ranks, int32_t rank, int32_t dom_offset, int32_t total_domains,
+                          void* const* bufs);
+KVC_API int kvc_peer_output(kvc_ctx* ctx, float* out, int32_t mem);
+
 /* ------------------------------------------------------------------ instrumentation */
 /* Kernel launches issued by this context since creation (for bench gpu_launches). */
 KVC_API int64_t kvc_launch_count(kvc_ctx* ctx);

@@ -144,6 +144,14 @@ def lib():
         L.kvc_tier_stats.argtypes = [vp, i64p]
         L.kvc_cluster_tier.argtypes = [vp, C.c_int64, i64p]
         L.kvc_debug_tier_check.argtypes = [vp, i64p]
+        L.kvc_exchange_bytes.restype = C.c_size_t
+        L.kvc_exchange_bytes.argtypes = [C.c_int32, C.c_int32, C.c_int32]
+        L.kvc_ipc_alloc.argtypes = [C.c_size_t, C.POINTER(vp), C.c_void_p]
+        L.kvc_ipc_open.argtypes = [C.c_void_p, C.POINTER(vp)]
+        L.kvc_ipc_close.argtypes = [vp]
+        L.kvc_ipc_free.argtypes = [vp]
+        L.kvc_set_peers.argtypes = [vp, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.POINTER(vp)]
+        L.kvc_peer_output.argtypes = [vp, vp, C.c_int32]
         L.kvc_launch_count.argtypes = [vp]
         L.kvc_launch_count.restype = C.c_int64
         L.kvc_last_step_timing.argtypes = [vp, f64p]
@@ -174,7 +182,8 @@ EXPORTED = [
     "kvc_launch_count", "kvc_last_step_timing", "kvc_set_timing", "kvc_last_ingest_timing",
     "kvc_debug_resolve_profile", "kvc_host_split_two", "kvc_host_kmeans", "kvc_host_tau",
     "kvc_host_mix_seed", "kvc_debug_div_check", "kvc_debug_assign_check", "kvc_tier_sync",
-    "kvc_tier_stats", "kvc_cluster_tier", "kvc_debug_tier_check",
+    "kvc_tier_stats", "kvc_cluster_tier", "kvc_debug_tier_check", "kvc_exchange_bytes", "kvc_ipc_alloc",
+    "kvc_ipc_open", "kvc_ipc_close", "kvc_ipc_free", "kvc_set_peers", "kvc_peer_output",
 ]
 
 
@@ -421,6 +430,18 @@ class ClusterKVCache:
         _check(lib().kvc_debug_tier_check(self.h, _p(out, i64p)))
         return tuple(int(x) for x in out)
 
+    # ------------------------------------------------------------------ fused output exchange
+    def set_peers(self, n_ranks: int, rank: int, dom_offset: int, total_domains: int, bufs):
+        """kvc_set_peers: bufs = every rank's mapped exchange buffer (device pointers, rank order)."""
+        arr = (C.c_void_p * len(bufs))(*[C.c_void_p(int(b)) for b in bufs])
+        _check(lib().kvc_set_peers(self.h, n_ranks, rank, dom_offset, total_domains, arr))
+
+    def peer_output(self, out):
+        """The last step's gathered outputs [total_domains, d] (torch CUDA tensor or numpy)."""
+        p, mem = _ptr(out)
+        _check(lib().kvc_peer_output(self.h, p, mem))
+        return out
+
     # ------------------------------------------------------------------ instrumentation
     def launch_count(self) -> int:
         return int(lib().kvc_launch_count(self.h))
@@ -483,3 +504,18 @@ def host_kmeans(pts: np.ndarray, k: int, max_iters: int = 50, tol: float = 1e-6,
     live = _check(lib().kvc_host_kmeans(_p(p, f32p), n, d, k, max_iters, tol, seed, _p(a, i32p),
                                         C.byref(obj), C.byref(it)))
     return a, live, obj.value, it.value
+
+
+def ipc_alloc(nbytes: int):
+    """cudaMalloc + cudaIpcGetMemHandle: (device pointer, 64-byte handle)."""
+    ptr = C.c_void_p()
+    h = (C.c_uint8 * 64)()
+    _check(lib().kvc_ipc_alloc(nbytes, C.byref(ptr), h))
+    return ptr.value, bytes(h)
+
+
+def ipc_open(handle: bytes) -> int:
+    ptr = C.c_void_p()
+    hb = (C.c_uint8 * 64).from_buffer_copy(handle)
+    _check(lib().kvc_ipc_open(hb, C.byref(ptr)))
+    return ptr.value

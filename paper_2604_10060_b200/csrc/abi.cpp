@@ -405,6 +405,47 @@ int kvc_tier_stats(kvc_ctx* ctx, int64_t* out) {
   return guard([&] { F(ctx).tier_stats(out); });
 }
 
+size_t kvc_exchange_bytes(int32_t n_ranks, int32_t total_domains, int32_t d) {
+  return 2ull * static_cast<size_t>(total_domains) * static_cast<size_t>(d) * 4 + static_cast<size_t>(n_ranks) * 8;
+}
+
+int kvc_ipc_alloc(size_t bytes, void** dptr, uint8_t* handle64) {
+  return guard([&] {
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) kvc::fail(KVC_E_NO_DEVICE, "no CUDA device");
+    KVC_CUDA(cudaMalloc(dptr, bytes));
+    KVC_CUDA(cudaMemset(*dptr, 0, bytes));
+    cudaIpcMemHandle_t h;
+    KVC_CUDA(cudaIpcGetMemHandle(&h, *dptr));
+    std::memcpy(handle64, &h, sizeof(h));
+  });
+}
+
+int kvc_ipc_open(const uint8_t* handle64, void** dptr) {
+  return guard([&] {
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle64, sizeof(h));
+    KVC_CUDA(cudaIpcOpenMemHandle(dptr, h, cudaIpcMemLazyEnablePeerAccess));
+  });
+}
+
+int kvc_ipc_close(void* dptr) {
+  return guard([&] { KVC_CUDA(cudaIpcCloseMemHandle(dptr)); });
+}
+
+int kvc_ipc_free(void* dptr) {
+  return guard([&] { KVC_CUDA(cudaFree(dptr)); });
+}
+
+int kvc_set_peers(kvc_ctx* ctx, int32_t n_ranks, int32_t rank, int32_t dom_offset, int32_t total_domains,
+                  void* const* bufs) {
+  return guard([&] { F(ctx).set_peers(n_ranks, rank, dom_offset, total_domains, bufs); });
+}
+
+int kvc_peer_output(kvc_ctx* ctx, float* out, int32_t mem) {
+  return guard([&] { F(ctx).peer_output(out, mem); });
+}
+
 int kvc_debug_tier_check(kvc_ctx* ctx, int64_t* out) {
   return guard([&] { F(ctx).tier_check(out); });
 }

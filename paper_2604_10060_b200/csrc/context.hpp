@@ -193,6 +193,9 @@ class Context {
   void tier_stats(std::int64_t* out) const;
   void cluster_tier(std::int64_t id, std::int64_t* out) const;
   void tier_check(std::int64_t* out);
+  // fused output exchange across ranks (multi-GPU by domain; context_query.cpp)
+  void set_peers(int n, int rank, int dom_offset, int total_domains, void* const* bufs);
+  void peer_output(float* out, int mem);
 
  private:
   // ---- configuration
@@ -303,6 +306,12 @@ class Context {
   bool tier_advance(TierBatch& b, bool block);    // next phase; true when the batch finished
   int tier_ring_take();
   cudaEvent_t tier_event();
+
+  // ---- fused output exchange (set_peers)
+  int peer_n_ = 0, peer_rank_ = 0, peer_total_ = 0;
+  std::uint8_t* peer_buf_[kMaxPeers] = {};
+  unsigned long long peer_step_ = 0;
+  unsigned long long* peer_flag_ptr(int r) const;
 
   // ---- host control plane
   std::vector<std::unique_ptr<Cluster>> clusters_;  // by id (dense, null when removed)

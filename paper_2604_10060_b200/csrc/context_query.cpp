@@ -103,6 +103,34 @@ bool Context::finish_step(int b) {
   return settle;
 }
 
+// Exchange buffer of rank r: [2 step parities][total domains][d] f32, then n u64 arrival flags.
+unsigned long long* Context::peer_flag_ptr(int r) const {
+  return reinterpret_cast<unsigned long long*>(peer_buf_[r] + 2LL * peer_total_ * d_ * 4);
+}
+
+void Context::set_peers(int n, int rank, int dom_offset, int total_domains, void* const* bufs) {
+  flush_pending();
+  if (n < 0 || n > kMaxPeers) fail(-10, "at most 8 ranks in the fused output exchange");
+  if (n > 0 && (rank < 0 || rank >= n || dom_offset < 0 || dom_offset + L_ > total_domains || !bufs))
+    fail(-10, "bad peer configuration");
+  peer_n_ = n;
+  peer_rank_ = rank;
+  peer_total_ = total_domains;
+  peer_step_ = 0;
+  for (int r = 0; r < kMaxPeers; ++r) peer_buf_[r] = r < n ? static_cast<std::uint8_t*>(bufs[r]) : nullptr;
+  da_.peer.n = 0;
+  da_.peer.dom_offset = dom_offset;
+}
+
+void Context::peer_output(float* out, int mem) {
+  if (peer_n_ == 0) fail(-10, "no fused output exchange configured");
+  if (peer_step_ == 0) fail(-10, "no decode step yet");
+  const std::uint8_t* src = peer_buf_[peer_rank_] + static_cast<std::int64_t>(peer_step_ % 2) * peer_total_ * d_ * 4;
+  KVC_CUDA(cudaMemcpyAsync(out, src, static_cast<std::size_t>(peer_total_) * d_ * 4,
+                           mem == KVC_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st_));
+  if (mem != KVC_MEM_DEVICE) sync();
+}
+
 void Context::decode_step(std::int64_t qid, const float* q, int q_mem, float* out, int out_mem,
                           const std::int64_t* gt, int n_gt) {
   (void)qid;
@@ -115,6 +143,12 @@ void Context::decode_step(std::int64_t qid, const float* q, int q_mem, float* ou
   const bool overlap = inflight_;
   const int pb = cur_;
   if (overlap) cur_ ^= 1;
+  if (peer_n_ > 0) {  // this step's rows go to buffer parity (step % 2) of every rank
+    peer_step_ += 1;
+    da_.peer.n = peer_n_;
+    for (int r = 0; r < peer_n_; ++r)
+      da_.peer.out[r] = reinterpret_cast<float*>(peer_buf_[r] + static_cast<std::int64_t>(peer_step_ % 2) * peer_total_ * d_ * 4);
+  }
   launch_step(cur_, q, q_mem, out, out_mem);
   step_gt_[cur_].assign(gt ? gt : nullptr, gt ? gt + (n_gt > 0 ? n_gt : 0) : nullptr);
   inflight_ = true;
@@ -124,6 +158,15 @@ void Context::decode_step(std::int64_t qid, const float* q, int q_mem, float* ou
       KVC_CUDA(cudaStreamSynchronize(st_));
       launch_step(cur_, q, q_mem, out, out_mem);
     }
+  }
+  if (peer_n_ > 0) {
+    // the step's launch is final: publish it to every rank, then wait until every rank has
+    // published it (their rows are in this rank's buffer); the next step's writes into parity
+    // (step + 1) % 2 are ordered after this wait in every rank's stream
+    unsigned long long* flags[kMaxPeers];
+    for (int r = 0; r < peer_n_; ++r) flags[r] = peer_flag_ptr(r);
+    launches_ += launch_peer_signal(flags, peer_n_, peer_rank_, peer_step_, st_);
+    launches_ += launch_peer_wait(peer_flag_ptr(peer_rank_), peer_n_, peer_step_, st_);
   }
   // parity / recall / self-check callers need the bookkeeping now; a host output only needs the
   // step's data (its bookkeeping still overlaps the next step)

@@ -1665,7 +1665,10 @@ __global__ void __launch_bounds__(256) k_score_select(DevTables t, DecodeArgs a,
     a.errw[l] = atomicOr(t.err, 0);
   }
   if (a.n_items[l] == 0)  // nothing attended: output zeros
-    for (int i = threadIdx.x; i < d; i += blockDim.x) a.out[static_cast<int64_t>(l) * d + i] = 0.f;
+    for (int i = threadIdx.x; i < d; i += blockDim.x) {
+      a.out[static_cast<int64_t>(l) * d + i] = 0.f;
+      for (int r = 0; r < a.peer.n; ++r) a.peer.out[r][static_cast<int64_t>(a.peer.dom_offset + l) * d + i] = 0.f;
+    }
 }
 
 // Block-wide exclusive scan of one int per thread (blockDim.x a multiple of 32, <= 1024);
@@ -2198,7 +2201,10 @@ __global__ void __launch_bounds__(K4T) k_score_select2(DevTables t, DecodeArgs a
     a.errw[l] = atomicOr(t.err, 0);
   }
   if (a.n_items[l] == 0)  // nothing attended: output zeros
-    for (int i = tid; i < d; i += K4T) a.out[static_cast<int64_t>(l) * d + i] = 0.f;
+    for (int i = tid; i < d; i += K4T) {
+      a.out[static_cast<int64_t>(l) * d + i] = 0.f;
+      for (int r = 0; r < a.peer.n; ++r) a.peer.out[r][static_cast<int64_t>(a.peer.dom_offset + l) * d + i] = 0.f;
+    }
 }
 
 // ============================================================================ K6
@@ -2520,7 +2526,11 @@ __global__ void __launch_bounds__(ATT_THREADS + 32) k_attend(DevTables t, Decode
             num += w * a.part_o[(static_cast<int64_t>(dom) * a.max_items + i) * D + c];
             den += w * ml[2 * i + 1];
           }
-          a.out[static_cast<int64_t>(dom) * D + c] = den > 0.f ? num / den : 0.f;
+          const float v = den > 0.f ? num / den : 0.f;
+          a.out[static_cast<int64_t>(dom) * D + c] = v;
+          if (a.peer.n) {  // fused exchange: the row goes straight to every rank over peer memory
+            for (int r = 0; r < a.peer.n; ++r) a.peer.out[r][static_cast<int64_t>(a.peer.dom_offset + dom) * D + c] = v;
+          }
         }
         if (tid == 0) a.dom_done[dom] = 0;
       }
@@ -2739,6 +2749,42 @@ int launch_attend_t(const DevTables& t, const DecodeArgs& a, cudaStream_t st, bo
   return launch_attend_s<D, BF16, 3>(t, a, st, pdl);
 }
 }  // namespace
+
+namespace {
+__global__ void k_peer_signal(unsigned long long* f0, unsigned long long* f1, unsigned long long* f2,
+                              unsigned long long* f3, unsigned long long* f4, unsigned long long* f5,
+                              unsigned long long* f6, unsigned long long* f7, int n, int rank,
+                              unsigned long long step) {
+  unsigned long long* f[8] = {f0, f1, f2, f3, f4, f5, f6, f7};
+  const int r = threadIdx.x;
+  __threadfence_system();  // this rank's output stores (earlier kernels) before the flag
+  if (r < n) asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(f[r] + rank), "l"(step) : "memory");
+}
+
+__global__ void k_peer_wait(const unsigned long long* flags, int n, unsigned long long step) {
+  if (threadIdx.x != 0) return;
+  for (int q = 0; q < n; ++q) {
+    unsigned long long v;
+    for (;;) {
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flags + q) : "memory");
+      if (v >= step) break;
+      __nanosleep(200);
+    }
+  }
+}
+}  // namespace
+
+int launch_peer_signal(unsigned long long* const* flags, int n, int rank, unsigned long long step, cudaStream_t st) {
+  unsigned long long* f[8] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  for (int i = 0; i < n && i < 8; ++i) f[i] = flags[i];
+  k_peer_signal<<<1, 32, 0, st>>>(f[0], f[1], f[2], f[3], f[4], f[5], f[6], f[7], n, rank, step);
+  return 1;
+}
+
+int launch_peer_wait(const unsigned long long* my_flags, int n, unsigned long long step, cudaStream_t st) {
+  k_peer_wait<<<1, 32, 0, st>>>(my_flags, n, step);
+  return 1;
+}
 
 int launch_attend(const DevTables& t, const DecodeArgs& a, cudaStream_t st) {
   if (!g_sms) {

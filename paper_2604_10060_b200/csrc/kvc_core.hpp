@@ -162,6 +162,17 @@ constexpr int TOPM = 8;
 constexpr int POOL = 16;
 
 // ----------------------------------------------------------------------------- decode
+// Fused output exchange across ranks (multi-GPU by domain): K6's combine (and K4's path for a
+// domain with nothing attended) stores each finished output row straight into every rank's full
+// output buffer over peer memory (NVLink P2P stores; CUDA IPC mappings), instead of a separate
+// all-gather pass; a per-step signal/wait pair of tiny kernels orders the ranks.
+constexpr int kMaxPeers = 8;
+struct PeerOut {
+  int32_t n;           // ranks (0: no fused exchange)
+  int32_t dom_offset;  // this rank's first global domain
+  float* out[kMaxPeers];  // rank p's full output buffer [total domains][d] (mapped)
+};
+
 struct DecodeArgs {
   const float* q;          // [L][d]
   int32_t k_v, k_s, prefetch_k, prefetch;
@@ -197,6 +208,7 @@ struct DecodeArgs {
   int32_t* work_ctr;       // attention work-claim counter (per context: contexts may run concurrently)
   int32_t debug_flags;     // instrumentation experiments only (KVC_ATT_DEBUG); 0 in production
   int32_t l2pf_pages;      // pages per domain K4 prefetches into L2 while it is latency bound
+  PeerOut peer;            // fused output exchange (multi-GPU); peer.n == 0 when unused
 };
 
 // ----------------------------------------------------------------------------- launchers
@@ -225,6 +237,12 @@ int launch_ring_write(const DevTables& t, const void* fk, const void* fv, int32_
 // K6 alone over a prepared work list (desc / n_desc / n_items / partials / out of `a`; the work
 // counter a.work_ctr must be zero). Used by the token-level baseline.
 int launch_attend(const DevTables& t, const DecodeArgs& a, cudaStream_t st);
+
+// Fused exchange signalling: rank `rank` publishes `step` into slot `rank` of every rank's flag
+// array (after a system-scope fence, so its output stores are visible first); the wait kernel
+// blocks the stream until every slot of this rank's flag array has reached `step`.
+int launch_peer_signal(unsigned long long* const* flags, int n, int rank, unsigned long long step, cudaStream_t st);
+int launch_peer_wait(const unsigned long long* my_flags, int n, unsigned long long step, cudaStream_t st);
 
 // K4 v3 (select.cu); false when the shape does not fit it.
 bool launch_select3(const DevTables& t, const DecodeArgs& a, cudaStream_t st);

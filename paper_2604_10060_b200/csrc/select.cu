@@ -634,7 +634,10 @@ __global__ void __launch_bounds__(K5T) k_select3(DevTables t, DecodeArgs a, int*
     a.errw[l] = atomicOr(t.err, 0);
   }
   if (a.n_items[l] == 0)
-    for (int i = tid; i < d; i += K5T) a.out[static_cast<int64_t>(l) * d + i] = 0.f;
+    for (int i = tid; i < d; i += K5T) {
+      a.out[static_cast<int64_t>(l) * d + i] = 0.f;
+      for (int r = 0; r < a.peer.n; ++r) a.peer.out[r][static_cast<int64_t>(a.peer.dom_offset + l) * d + i] = 0.f;
+    }
   if (a.k4prof && threadIdx.x == 0) {
     a.k4prof[l * 16 + 12] = clock64() - kc0;  // the tail after the last phase mark
     unsigned long long gt;

@@ -43,3 +43,33 @@ def gather_domain_outputs(out_local, n_domains: int, group=None):
     parts = [torch.empty_like(pad) for _ in range(world)]
     dist.all_gather(parts, pad, group=group)
     return torch.cat([p[: b - a] for p, (a, b) in zip(parts, blocks)], dim=0)
+
+
+class FusedExchange:
+    """Fused output exchange (kvc_set_peers): the attention kernel writes every finished output row
+    into every rank's exchange buffer over peer memory (NVLink P2P stores through CUDA IPC
+    mappings), replacing the per-step all-gather; only the 64-byte IPC handles go through the
+    process group (once). After kv.query, `gathered(out)` yields all domains' outputs."""
+
+    def __init__(self, kv, n_domains: int, group=None):
+        import torch.distributed as dist
+
+        from .api import ipc_alloc, ipc_open, lib
+
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.kv = kv
+        self.n_domains = n_domains
+        a, b = shard_domains(n_domains, self.world, self.rank)
+        if b - a != kv.L:
+            raise ValueError("the context must hold exactly this rank's domain block")
+        nbytes = int(lib().kvc_exchange_bytes(self.world, n_domains, kv.d))
+        self.own, handle = ipc_alloc(nbytes)
+        handles = [None] * self.world
+        dist.all_gather_object(handles, handle, group=group)
+        self.bufs = [self.own if r == self.rank else ipc_open(handles[r]) for r in range(self.world)]
+        dist.barrier(group=group)
+        kv.set_peers(self.world, self.rank, a, n_domains, self.bufs)
+
+    def gathered(self, out):
+        return self.kv.peer_output(out)
