@@ -202,9 +202,15 @@ def main():
 
     from paper_2604_10060_b200 import ClusterKVCache, Config, DTYPE_BF16, workload
 
-    torch.cuda.set_device(local)
+    # KVC_BENCH_ONE_GPU=1 (development only): every rank on cuda:0 with gloo, to exercise the
+    # multi-rank path (sharding, fused exchange through CUDA IPC) on a single-GPU box
+    one_gpu = os.environ.get("KVC_BENCH_ONE_GPU") == "1"
+    torch.cuda.set_device(0 if one_gpu else local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2604_10060_b200.sharding import FusedExchange, gather_domain_outputs, shard_domains
 
     d0, d1 = shard_domains(args.domains, world, rank)  # strong scaling over (layer, head) domains
@@ -349,7 +355,12 @@ def main():
     # max over ranks
     vals = torch.tensor([decode_ms, decode_e2e_ms, ingest_ms, ingest_e2e_ms], device="cuda", dtype=torch.float64)
     if world > 1:
-        dist.all_reduce(vals, op=dist.ReduceOp.MAX)
+        if one_gpu:
+            vc = vals.cpu()
+            dist.all_reduce(vc, op=dist.ReduceOp.MAX)
+            vals = vc
+        else:
+            dist.all_reduce(vals, op=dist.ReduceOp.MAX)
     decode_ms, decode_e2e_ms, ingest_ms, ingest_e2e_ms = vals.tolist()
     if rank != 0:
         if world > 1:

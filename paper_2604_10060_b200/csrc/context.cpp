@@ -10,6 +10,7 @@
 //   index.cpp:97-190      cluster registration, frame -> cluster map, buffers
 #include "context.hpp"
 
+#include <cstdio>
 #include <cstdlib>
 
 #include <algorithm>
@@ -195,15 +196,18 @@ void Context::alloc_device() {
     std::vector<std::int32_t> stack(static_cast<std::size_t>(t_.max_pages - ring_pages));
     for (std::size_t i = 0; i < stack.size(); ++i)
       stack[i] = static_cast<std::int32_t>(t_.max_pages - 1 - static_cast<std::int64_t>(i));
-    KVC_CUDA(cudaMemcpy(t_.free_stack, stack.data(), stack.size() * 4, cudaMemcpyHostToDevice));
+    KVC_CUDA(cudaMemcpyAsync(t_.free_stack, stack.data(), stack.size() * 4, cudaMemcpyHostToDevice, st_));
     std::int32_t top = static_cast<std::int32_t>(stack.size());
-    KVC_CUDA(cudaMemcpy(t_.free_top, &top, 4, cudaMemcpyHostToDevice));
+    KVC_CUDA(cudaMemcpyAsync(t_.free_top, &top, 4, cudaMemcpyHostToDevice, st_));
     std::vector<std::int32_t> rp(static_cast<std::size_t>(ring_pages));
     std::iota(rp.begin(), rp.end(), 0);
-    KVC_CUDA(cudaMemcpy(t_.ring_pages, rp.data(), rp.size() * 4, cudaMemcpyHostToDevice));
+    KVC_CUDA(cudaMemcpyAsync(t_.ring_pages, rp.data(), rp.size() * 4, cudaMemcpyHostToDevice, st_));
     ring_owner_h_.assign(static_cast<std::size_t>(L * t_.W * t_.tmax), -1);
     ring_frame_.assign(static_cast<std::size_t>(t_.W), RingFrame{});
-    KVC_CUDA(cudaMemcpy(t_.ring_owner, ring_owner_h_.data(), ring_owner_h_.size() * 4, cudaMemcpyHostToDevice));
+    KVC_CUDA(cudaMemcpyAsync(t_.ring_owner, ring_owner_h_.data(), ring_owner_h_.size() * 4, cudaMemcpyHostToDevice, st_));
+    // dalloc zero-fills on st_ (a non-blocking stream): every initial upload goes on st_ too and
+    // completes before the pageable sources die
+    KVC_CUDA(cudaStreamSynchronize(st_));
   }
   slot_id_.assign(static_cast<std::size_t>(S), -1);
   free_slots_.resize(static_cast<std::size_t>(S));
@@ -316,7 +320,8 @@ void Context::upload_tau() {
   for (std::int64_t n = 0; n < len; ++n) tau_host_[static_cast<std::size_t>(n)] = tau_of(n, cfg_);
   t_.tau_tab = static_cast<double*>(dalloc(len * 8));
   t_.tau_len = static_cast<std::int32_t>(len);
-  KVC_CUDA(cudaMemcpy(t_.tau_tab, tau_host_.data(), len * 8, cudaMemcpyHostToDevice));
+  KVC_CUDA(cudaMemcpyAsync(t_.tau_tab, tau_host_.data(), len * 8, cudaMemcpyHostToDevice, st_));
+  KVC_CUDA(cudaStreamSynchronize(st_));
 }
 
 void Context::ensure_stage(std::int64_t rows) {
@@ -412,7 +417,8 @@ void Context::resolve_profile(double* out) {
   const bool dec = out[0] < 0;
   const int W = 16;  // K4 and resolve: [L][16]
   std::vector<long long> p(static_cast<std::size_t>(L_) * W);
-  KVC_CUDA(cudaMemcpy(p.data(), dec ? da_.k4prof : ia_.prof, p.size() * 8, cudaMemcpyDeviceToHost));
+  KVC_CUDA(cudaMemcpyAsync(p.data(), dec ? da_.k4prof : ia_.prof, p.size() * 8, cudaMemcpyDeviceToHost, st_));
+  sync();
   for (int k = 0; k < 16; ++k) {
     double s = 0.0;
     if (k < W)
@@ -439,7 +445,8 @@ void Context::sync() { KVC_CUDA(cudaStreamSynchronize(st_)); }
 
 void Context::check_dev_err() {
   std::int32_t e = 0;
-  KVC_CUDA(cudaMemcpy(&e, t_.err, 4, cudaMemcpyDeviceToHost));
+  KVC_CUDA(cudaMemcpyAsync(&e, t_.err, 4, cudaMemcpyDeviceToHost, st_));  // (st_ is non-blocking:
+  sync();                                                                 //  not the legacy stream)
   check_err_word(e);
 }
 

@@ -427,15 +427,20 @@ void Context::tier_check(std::int64_t* out) {
   sync();
   for (int i = 0; i < 4; ++i) out[i] = 0;
   std::vector<std::int32_t> fill(static_cast<std::size_t>(t_.max_pages + t_.max_hpages));
-  KVC_CUDA(cudaMemcpy(fill.data(), t_.pg_fill, fill.size() * 4, cudaMemcpyDeviceToHost));
+  KVC_CUDA(cudaMemcpyAsync(fill.data(), t_.pg_fill, fill.size() * 4, cudaMemcpyDeviceToHost, st_));
+  sync();
   std::vector<std::int32_t> list(static_cast<std::size_t>(t_.maxp));
   for (const auto& up : clusters_) {
     if (!up) continue;
     const Cluster& c = *up;
     std::int32_t np = 0;
-    KVC_CUDA(cudaMemcpy(&np, t_.npages + c.slot, 4, cudaMemcpyDeviceToHost));
-    if (np > 0)
-      KVC_CUDA(cudaMemcpy(list.data(), t_.pages + static_cast<std::int64_t>(c.slot) * t_.maxp, np * 4, cudaMemcpyDeviceToHost));
+    KVC_CUDA(cudaMemcpyAsync(&np, t_.npages + c.slot, 4, cudaMemcpyDeviceToHost, st_));
+    sync();
+    if (np > 0) {
+      KVC_CUDA(cudaMemcpyAsync(list.data(), t_.pages + static_cast<std::int64_t>(c.slot) * t_.maxp, np * 4,
+                               cudaMemcpyDeviceToHost, st_));
+      sync();
+    }
     const Extent e = static_cast<std::size_t>(c.id) < hext_.size() ? hext_[static_cast<std::size_t>(c.id)] : Extent{};
     std::int64_t rows = 0, tail_rows = 0, nhost = 0;
     for (std::int32_t p = 0; p < np; ++p) {

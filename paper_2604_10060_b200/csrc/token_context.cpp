@@ -238,7 +238,8 @@ void TokenContext::decode_step(std::int64_t qid, const float* q, int q_mem, floa
   }
   if (cfg_.parity_mode) {  // attended (frame, token) lists and the digest
     std::vector<std::uint32_t> w(static_cast<std::size_t>(L_) * ta_.wcap);
-    KVC_CUDA(cudaMemcpy(w.data(), ta_.attw, w.size() * 4, cudaMemcpyDeviceToHost));
+    KVC_CUDA(cudaMemcpyAsync(w.data(), ta_.attw, w.size() * 4, cudaMemcpyDeviceToHost, st_));
+    KVC_CUDA(cudaStreamSynchronize(st_));
     std::uint64_t h = 1469598103934665603ull;
     for (int l = 0; l < L_; ++l) {
       auto& a = att_[static_cast<std::size_t>(l)];
@@ -293,7 +294,8 @@ std::int64_t TokenContext::ledger(std::int64_t* ops, std::int64_t* bytes, double
 
 void TokenContext::profile(double* out) {
   std::vector<long long> p(static_cast<std::size_t>(L_) * 8);
-  KVC_CUDA(cudaMemcpy(p.data(), ta_.prof, p.size() * 8, cudaMemcpyDeviceToHost));
+  KVC_CUDA(cudaMemcpyAsync(p.data(), ta_.prof, p.size() * 8, cudaMemcpyDeviceToHost, st_));
+  KVC_CUDA(cudaStreamSynchronize(st_));
   for (int k = 0; k < 8; ++k) {
     double s = 0.0;
     for (int l = 0; l < L_; ++l) s += static_cast<double>(p[static_cast<std::size_t>(l) * 8 + k]);
