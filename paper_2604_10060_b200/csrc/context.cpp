@@ -857,6 +857,7 @@ void Context::ingest_frame(std::int64_t frame_id, const float* visual, const voi
   ring_frame_[static_cast<std::size_t>(ring_slot)] = RingFrame{frame_id, T};
 
   if (!built_) {  // engine.cpp:161-166
+    launches_ += launch_ring_rows(t_, d_fk_, d_fv_, T, ring_slot, st_);
     PendingFrame pf;
     pf.frame_id = frame_id;
     pf.visual.assign(visual, visual + d_);

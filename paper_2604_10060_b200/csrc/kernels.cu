@@ -930,45 +930,54 @@ done:
 }
 
 // ============================================================================ K3
-// Copies every committed row of the launch to the (page, row) K2 reserved for it.
+// One warp per frame row of the launch's token range: the row's K and V (16-byte lane chunks,
+// loaded once) go to the window ring page of the frame and, when the resolve kernel committed the
+// token, to the (page, row) it reserved in the cluster's page list.
 __global__ void k_store_rows(DevTables t, IngestArgs a) {
   const int dom = a.active[blockIdx.y];
   const int rb = t.d * t.es;
   const int warps = blockDim.x / 32, warp = threadIdx.x / 32, lane = threadIdx.x & 31;
   const int cur = a.cursor[dom];
+  const int half = lane >> 4, hl = lane & 15;  // lanes 0-15: K, lanes 16-31: V
   for (int tt = cur + blockIdx.x * warps + warp; tt < a.T; tt += gridDim.x * warps) {
     const int64_t frow = static_cast<int64_t>(dom) * t.tmax + tt;
     const int page = a.ev_page[frow];
-    if (page < 0) continue;
-    const int row = a.ev_row[frow];
-    const uint8_t* sk = static_cast<const uint8_t*>(a.fk) + frow * rb;
-    const uint8_t* sv = static_cast<const uint8_t*>(a.fv) + frow * rb;
-    uint8_t* dk = page_k(t, page) + static_cast<int64_t>(row) * rb;
-    uint8_t* dv = page_v(t, page) + static_cast<int64_t>(row) * rb;
-    for (int o = lane * 16; o < rb; o += 32 * 16) {
-      *reinterpret_cast<uint4*>(dk + o) = *reinterpret_cast<const uint4*>(sk + o);
-      *reinterpret_cast<uint4*>(dv + o) = *reinterpret_cast<const uint4*>(sv + o);
+    const int row = page >= 0 ? a.ev_row[frow] : 0;
+    const uint8_t* src = static_cast<const uint8_t*>(half ? a.fv : a.fk) + frow * rb;
+    const int rpage = t.ring_pages[(static_cast<int64_t>(dom) * t.W + a.ring_slot) * t.rpp + tt / t.P];
+    uint8_t* dring = (half ? page_v(t, rpage) : page_k(t, rpage)) + static_cast<int64_t>(tt % t.P) * rb;
+    uint8_t* dclu = page >= 0 ? (half ? page_v(t, page) : page_k(t, page)) + static_cast<int64_t>(row) * rb : nullptr;
+    for (int o = hl * 16; o < rb; o += 16 * 16) {
+      const uint4 v = *reinterpret_cast<const uint4*>(src + o);
+      *reinterpret_cast<uint4*>(dring + o) = v;
+      if (dclu) *reinterpret_cast<uint4*>(dclu + o) = v;
     }
   }
 }
 
-// ============================================================================ ring write
-__global__ void k_ring_write(DevTables t, const uint8_t* fk, const uint8_t* fv, int T, int rs) {
+// Window-ring rows only (frames buffered for the batch build, which routes nothing yet).
+__global__ void k_ring_rows(DevTables t, const uint8_t* fk, const uint8_t* fv, int T, int rs) {
   const int dom = blockIdx.y;
   const int rb = t.d * t.es;
-  for (int tt = blockIdx.x; tt < t.tmax; tt += gridDim.x) {
-    if (threadIdx.x == 0) t.ring_owner[(static_cast<int64_t>(dom) * t.W + rs) * t.tmax + tt] = -1;
-    if (tt >= T) continue;
-    const int page = t.ring_pages[(static_cast<int64_t>(dom) * t.W + rs) * t.rpp + tt / t.P];
-    const int row = tt % t.P;
-    const int64_t src = (static_cast<int64_t>(dom) * t.tmax + tt) * rb;
-    uint8_t* dk = page_k(t, page) + static_cast<int64_t>(row) * rb;
-    uint8_t* dv = page_v(t, page) + static_cast<int64_t>(row) * rb;
-    for (int o = threadIdx.x * 16; o < rb; o += blockDim.x * 16) {
-      *reinterpret_cast<uint4*>(dk + o) = *reinterpret_cast<const uint4*>(fk + src + o);
-      *reinterpret_cast<uint4*>(dv + o) = *reinterpret_cast<const uint4*>(fv + src + o);
-    }
+  const int warps = blockDim.x / 32, warp = threadIdx.x / 32, lane = threadIdx.x & 31;
+  const int half = lane >> 4, hl = lane & 15;
+  for (int tt = blockIdx.x * warps + warp; tt < T; tt += gridDim.x * warps) {
+    const int64_t frow = static_cast<int64_t>(dom) * t.tmax + tt;
+    const uint8_t* src = (half ? fv : fk) + frow * rb;
+    const int rpage = t.ring_pages[(static_cast<int64_t>(dom) * t.W + rs) * t.rpp + tt / t.P];
+    uint8_t* dring = (half ? page_v(t, rpage) : page_k(t, rpage)) + static_cast<int64_t>(tt % t.P) * rb;
+    for (int o = hl * 16; o < rb; o += 16 * 16) *reinterpret_cast<uint4*>(dring + o) = *reinterpret_cast<const uint4*>(src + o);
   }
+}
+
+// ============================================================================ ring write
+// Frame start: the ring slot's ownership entries are reset (the resolve kernel then records the
+// owner of every routed token) and its page fills / token count set; the rows themselves are
+// copied by K3 after the resolve, together with the cluster rows.
+__global__ void k_ring_write(DevTables t, const uint8_t* fk, const uint8_t* fv, int T, int rs) {
+  const int dom = blockIdx.y;
+  for (int tt = blockIdx.x * blockDim.x + threadIdx.x; tt < t.tmax; tt += gridDim.x * blockDim.x)
+    t.ring_owner[(static_cast<int64_t>(dom) * t.W + rs) * t.tmax + tt] = -1;
   if (blockIdx.x == 0 && threadIdx.x < t.rpp) {
     const int j = threadIdx.x;
     const int page = t.ring_pages[(static_cast<int64_t>(dom) * t.W + rs) * t.rpp + j];
@@ -2618,7 +2627,7 @@ int launch_resolve(const DevTables& t, const IngestArgs& a, cudaStream_t st) {
 }
 
 int launch_store_rows(const DevTables& t, const IngestArgs& a, cudaStream_t st) {
-  dim3 g((a.T + 31) / 32, a.n_active);
+  dim3 g((a.T + 7) / 8, a.n_active);  // one warp per row
   k_store_rows<<<g, 256, 0, st>>>(t, a);
   return 1;
 }
@@ -2636,8 +2645,14 @@ int launch_topm(const DevTables& t, const IngestArgs& a, cudaStream_t st) {
 
 int launch_ring_write(const DevTables& t, const void* fk, const void* fv, int32_t T, int32_t rs,
                       cudaStream_t st) {
-  dim3 g(min(t.tmax, 64), t.L);
-  k_ring_write<<<g, 128, 0, st>>>(t, static_cast<const uint8_t*>(fk), static_cast<const uint8_t*>(fv), T, rs);
+  dim3 g(1, t.L);
+  k_ring_write<<<g, 256, 0, st>>>(t, static_cast<const uint8_t*>(fk), static_cast<const uint8_t*>(fv), T, rs);
+  return 1;
+}
+
+int launch_ring_rows(const DevTables& t, const void* fk, const void* fv, int32_t T, int32_t rs, cudaStream_t st) {
+  dim3 g((T + 7) / 8, t.L);
+  k_ring_rows<<<g, 256, 0, st>>>(t, static_cast<const uint8_t*>(fk), static_cast<const uint8_t*>(fv), T, rs);
   return 1;
 }
 

@@ -231,7 +231,12 @@ constexpr float kTcMargin = 2e-4f;    // ... of the bf16 hi/lo tensor-core tile
 // Counts div_rcp != __ddiv_rn over n random operands on the device (~0 on CUDA failure).
 uint64_t debug_div_check(uint64_t n, uint64_t seed, int max_den);
 int launch_topm(const DevTables& t, const IngestArgs& a, cudaStream_t st);
+// The launch's frame rows [cursor, T) of every active domain -> window ring; committed ones also
+// -> the (page, row) the resolve kernel reserved.
 int launch_store_rows(const DevTables& t, const IngestArgs& a, cudaStream_t st);
+// Frame start: the ring slot's owner entries / page fills / token count. Its rows are written by
+// launch_store_rows (routed frames) or launch_ring_rows (frames pending the batch build).
+int launch_ring_rows(const DevTables& t, const void* fk, const void* fv, int32_t T, int32_t rs, cudaStream_t st);
 int launch_ring_write(const DevTables& t, const void* fk, const void* fv, int32_t T,
                       int32_t ring_slot, cudaStream_t st);
 // K6 alone over a prepared work list (desc / n_desc / n_items / partials / out of `a`; the work
