@@ -227,9 +227,10 @@ void Context::alloc_device() {
   ia_.cand_slot = static_cast<std::int32_t*>(dalloc(L * t_.cmax * 4));
   ia_.cand_buf = static_cast<std::uint8_t*>(dalloc(L * t_.cmax));
   ia_.approx = static_cast<float*>(dalloc(L * t_.tmax * t_.cmax * 4));
-  ia_.ev_kind = static_cast<std::int32_t*>(dalloc(L * t_.tmax * 4));
-  ia_.ev_slot = static_cast<std::int32_t*>(dalloc(L * t_.tmax * 4));
-  ia_.stop_t = static_cast<std::int32_t*>(dalloc(L * 4 * 3 + 16));
+  // outcome words in one block (ev_kind | ev_slot | stop_t | stop_kind | stop_slot): one D2H per launch
+  ia_.ev_kind = static_cast<std::int32_t*>(dalloc(L * t_.tmax * 4 * 2 + L * 4 * 3 + 16));
+  ia_.ev_slot = ia_.ev_kind + L * t_.tmax;
+  ia_.stop_t = ia_.ev_slot + L * t_.tmax;
   ia_.stop_kind = ia_.stop_t + L;
   ia_.stop_slot = ia_.stop_t + 2 * L;
   ia_.n_exact = static_cast<std::int32_t*>(dalloc(L * 4));
@@ -255,9 +256,9 @@ void Context::alloc_device() {
   d_cursor_ = d_active_ + L;
   h_active_ = static_cast<std::int32_t*>(halloc(L * 4 * 2));
   h_cursor_ = h_active_ + L;
-  h_evk_ = static_cast<std::int32_t*>(halloc(L * t_.tmax * 4 * 2));
+  h_evk_ = static_cast<std::int32_t*>(halloc(L * t_.tmax * 4 * 2 + L * 4 * 3 + 16));
   h_evs_ = h_evk_ + L * t_.tmax;
-  h_stop_ = static_cast<std::int32_t*>(halloc(L * 4 * 3 + 16));
+  h_stop_ = h_evs_ + L * t_.tmax;
   ia_.active = d_active_;
   ia_.cursor = d_cursor_;
   ia_.fk = d_fk_;
@@ -495,6 +496,23 @@ void Context::frame_add(std::int64_t frame, std::int64_t cid) {
   auto& v = frame_clusters_[frame];
   auto it = std::lower_bound(v.begin(), v.end(), cid);
   if (it == v.end() || *it != cid) v.insert(it, cid);
+}
+
+// The replay's frame -> cluster entries of one frame, merged in one sorted pass.
+void Context::frame_add_flush(std::int64_t frame) {
+  if (fc_pending_.empty()) return;
+  std::sort(fc_pending_.begin(), fc_pending_.end());
+  fc_pending_.erase(std::unique(fc_pending_.begin(), fc_pending_.end()), fc_pending_.end());
+  auto& v = frame_clusters_[frame];
+  if (v.empty()) {
+    v.swap(fc_pending_);
+  } else {
+    std::vector<std::int64_t> m;
+    m.reserve(v.size() + fc_pending_.size());
+    std::set_union(v.begin(), v.end(), fc_pending_.begin(), fc_pending_.end(), std::back_inserter(m));
+    v.swap(m);
+  }
+  fc_pending_.clear();
 }
 
 void Context::frame_del(std::int64_t frame, std::int64_t cid) {
@@ -945,9 +963,8 @@ void Context::run_inserts(std::int64_t frame_id, std::int64_t pid, int T, std::i
       launches_ += launch_store_rows(t_, ia_, st_);
       KVC_CUDA(cudaGetLastError());
       if (timing_) KVC_CUDA(cudaEventRecord(ev_[5], st_));
-      KVC_CUDA(cudaMemcpyAsync(h_evk_, ia_.ev_kind, static_cast<std::size_t>(L_) * t_.tmax * 4, cudaMemcpyDeviceToHost, st_));
-      KVC_CUDA(cudaMemcpyAsync(h_evs_, ia_.ev_slot, static_cast<std::size_t>(L_) * t_.tmax * 4, cudaMemcpyDeviceToHost, st_));
-      KVC_CUDA(cudaMemcpyAsync(h_stop_, ia_.stop_t, static_cast<std::size_t>(L_) * 12, cudaMemcpyDeviceToHost, st_));
+      KVC_CUDA(cudaMemcpyAsync(h_evk_, ia_.ev_kind, (static_cast<std::size_t>(L_) * t_.tmax * 2 + static_cast<std::size_t>(L_) * 3) * 4,
+                               cudaMemcpyDeviceToHost, st_));
       KVC_CUDA(cudaMemcpyAsync(h_err_, t_.err, 4, cudaMemcpyDeviceToHost, st_));
       const auto w0 = std::chrono::steady_clock::now();
       t_launch += std::chrono::duration<double, std::micro>(w0 - lc0).count();
@@ -984,7 +1001,7 @@ void Context::run_inserts(std::int64_t frame_id, std::int64_t pid, int T, std::i
       c.stat_count += n;
       c.last_touch = std::max(c.last_touch, frame_id);
       if (cid != last_cid) {
-        frame_add(frame_id, cid);
+        fc_pending_.push_back(cid);  // frame -> cluster map entries, merged once (frame_add_flush)
         last_cid = cid;
       }
       std::fill(owner + t, owner + u, slot);
@@ -1022,6 +1039,7 @@ void Context::run_inserts(std::int64_t frame_id, std::int64_t pid, int T, std::i
       }
       continue;
     }
+    frame_add_flush(frame_id);  // host events add / remove map entries themselves
     const std::int64_t id = handle_host_event(frame_id, pid, l, stop, h_stop_[L_ + l], h_stop_[2 * L_ + l]);
     ingest_t_[7] += 1.0;  // host events this frame
     if (assigned) assigned[static_cast<std::size_t>(l) * T + stop] = id;
@@ -1038,6 +1056,7 @@ void Context::run_inserts(std::int64_t frame_id, std::int64_t pid, int T, std::i
       }
     }
   }
+  frame_add_flush(frame_id);
   ingest_t_[5] = t_wait;
   ingest_t_[7] = t_replay;  // (instrumentation) replay loop; launches in ingest_t_[6] below
   ingest_t_[4] = t_launch;

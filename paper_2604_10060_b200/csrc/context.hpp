@@ -376,6 +376,8 @@ class Context {
                            bool host);
   void drop_cluster(std::int64_t id);  // HierIndex::remove_cluster (host side)
   void frame_add(std::int64_t frame, std::int64_t cid);
+  void frame_add_flush(std::int64_t frame);
+  std::vector<std::int64_t> fc_pending_;
   void frame_del(std::int64_t frame, std::int64_t cid);
   void pl_upload(std::int64_t pid, int layer);
   void upload_partition(std::int64_t pid);
