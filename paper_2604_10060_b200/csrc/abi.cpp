@@ -158,7 +158,9 @@ int kvc_ingest_frame(kvc_ctx* ctx, int64_t frame_id, const float* visual, const 
       ctx->tok->ingest_frame(frame_id, keys, values, T, mem);
       return;
     }
-    F(ctx).ingest_frame(frame_id, visual, keys, values, T, mem, assigned, partition);
+    if (!ctx->impl) kvc::fail(KVC_E_CONFIG, "no context");
+    ctx->impl->flush_decode();  // (not F: the previous frame's deferred replay overlaps this frame)
+    ctx->impl->ingest_frame(frame_id, visual, keys, values, T, mem, assigned, partition);
   });
 }
 

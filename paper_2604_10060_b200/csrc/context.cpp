@@ -217,8 +217,12 @@ void Context::alloc_device() {
 
   // frame input (kv dtype, [L][tmax][d])
   const std::size_t frame_bytes = static_cast<std::size_t>(L) * t_.tmax * d * es_;
-  d_fk_ = dalloc(frame_bytes);
-  d_fv_ = dalloc(frame_bytes);
+  for (int b = 0; b < 2; ++b) {  // double-buffered frame input (pipelined ingest)
+    fkbuf_[b] = dalloc(frame_bytes);
+    fvbuf_[b] = dalloc(frame_bytes);
+  }
+  d_fk_ = fkbuf_[0];
+  d_fv_ = fvbuf_[0];
   ensure_stage(static_cast<std::int64_t>(t_.maxp + t_.maxbp) * t_.P + 1);
   ensure_idx(1 << 16, 1 << 12);
 
@@ -250,13 +254,20 @@ void Context::alloc_device() {
     resolve_seq_ = e && std::string(e) == "seq";
     const char* g = std::getenv("KVC_ASSIGN");  // "simt": the fp32 CUDA-core tile
     assign_tc_ = !(g && std::string(g) == "simt") && assign_tc_supported(t_) &&
-                 make_key_tensor_map(key_map_, d_fk_, d, t_.tmax, L);
+                 make_key_tensor_map(key_maps_[0], fkbuf_[0], d, t_.tmax, L) &&
+                 make_key_tensor_map(key_maps_[1], fkbuf_[1], d, t_.tmax, L);
+    std::memcpy(key_map_, key_maps_[0], sizeof(key_map_));
   }
   d_active_ = static_cast<std::int32_t*>(dalloc(L * 4 * 2));
   d_cursor_ = d_active_ + L;
   h_active_ = static_cast<std::int32_t*>(halloc(L * 4 * 2));
   h_cursor_ = h_active_ + L;
-  h_evk_ = static_cast<std::int32_t*>(halloc(L * t_.tmax * 4 * 2 + L * 4 * 3 + 16));
+  for (int b = 0; b < 2; ++b) {
+    h_out_[b] = static_cast<std::int32_t*>(halloc(L * t_.tmax * 4 * 2 + L * 4 * 3 + 16));
+    h_errb_[b] = static_cast<std::int32_t*>(halloc(16));
+    KVC_CUDA(cudaEventCreateWithFlags(&ev_ing_[b], cudaEventDisableTiming));
+  }
+  h_evk_ = h_out_[0];
   h_evs_ = h_evk_ + L * t_.tmax;
   h_stop_ = h_evs_ + L * t_.tmax;
   ia_.active = d_active_;
@@ -755,8 +766,7 @@ double Context::evict_one() {  // store.cpp:166-181
 
 // ============================================================================ engine (host)
 
-void Context::push_window(std::int64_t frame_id, int T) {  // engine.cpp:54-57
-  const int slot = static_cast<int>(frames_seen_ % t_.W);
+void Context::push_window(std::int64_t frame_id, int T, int slot) {  // engine.cpp:54-57
   window_.push_back({frame_id, slot, T});
   while (static_cast<int>(window_.size()) > t_.W) window_.pop_front();
 }
@@ -854,6 +864,40 @@ std::int64_t Context::place_frame(std::int64_t frame_id, const float* visual) {
   return pid;
 }
 
+void Context::select_frame_buffer(int b) {
+  d_fk_ = fkbuf_[b];
+  d_fv_ = fvbuf_[b];
+  ia_.fk = d_fk_;
+  ia_.fv = d_fv_;
+  std::memcpy(key_map_, key_maps_[b], sizeof(key_map_));
+  h_evk_ = h_out_[b];
+  h_evs_ = h_evk_ + static_cast<std::size_t>(L_) * t_.tmax;
+  h_stop_ = h_evs_ + static_cast<std::size_t>(L_) * t_.tmax;
+  h_err_ = h_errb_[b];
+}
+
+// Replay (+ host events) of the pending frame, then window / repin / cadence (engine.cpp:168-173).
+void Context::finish_frame(std::int64_t* assigned) {
+  PendingIngest p = ping_;
+  ping_.active = false;
+  ping_wait_ = p.ev;
+  select_frame_buffer(p.buf);
+  ia_.T = p.T;
+  ia_.pid = static_cast<std::int32_t>(p.pid);
+  ia_.ring_slot = p.ring_slot;
+  run_inserts(p.frame_id, p.pid, p.T, assigned, true);
+  push_window(p.frame_id, p.T, p.ring_slot);
+  repin();
+  apply_cadence(p.frame_id, p.pid);
+  tier_kick();
+}
+
+void Context::flush_ingest() {
+  if (!ping_.active) return;
+  KVC_CUDA(cudaEventSynchronize(ping_.ev));
+  finish_frame(nullptr);
+}
+
 void Context::ingest_frame(std::int64_t frame_id, const float* visual, const void* keys,
                            const void* values, int T, int mem, std::int64_t* assigned,
                            std::int64_t* partition) {
@@ -862,6 +906,22 @@ void Context::ingest_frame(std::int64_t frame_id, const float* visual, const voi
   if (!visual || !keys || !values) fail(-10, "null frame buffer");
   if (assigned) std::fill(assigned, assigned + static_cast<std::int64_t>(L_) * T, -1);
   if (partition) *partition = -1;
+  // Pipelined ingest (no per-entry outputs requested): this frame is launched before the previous
+  // frame's host replay, which then overlaps this frame's kernels. A previous frame that needs
+  // host events (seeds / splits change the device index) is completed first.
+  static const bool force_sync = std::getenv("KVC_INGEST_SYNC") != nullptr;
+  const bool async_ok = !assigned && !cfg_.parity_mode && !cfg_.check_invariants && built_ && cfg_.defer_host_splits &&
+                        !timing_ && !force_sync;
+  if (ping_.active) {
+    KVC_CUDA(cudaEventSynchronize(ping_.ev));
+    bool events = false;
+    const std::int32_t* stp = h_out_[ping_.buf] + 2 * static_cast<std::size_t>(L_) * t_.tmax;
+    for (int l = 0; l < L_ && !events; ++l) events = stp[l] < ping_.T;
+    if (!async_ok || events || *h_errb_[ping_.buf]) finish_frame(nullptr);
+  }
+  const int b = ping_.active ? (ping_.buf ^ 1) : (ibuf_ ^ 1);
+  ibuf_ = b;
+  select_frame_buffer(b);
   // payload -> device frame buffer [L][tmax][d]
   const std::size_t row = static_cast<std::size_t>(T) * d_ * es_;
   const std::size_t pitch = static_cast<std::size_t>(t_.tmax) * d_ * es_;
@@ -894,7 +954,7 @@ void Context::ingest_frame(std::int64_t frame_id, const float* visual, const voi
     pf.keys_f32.resize(n);
     rows_to_f32(pf.keys_raw.data(), es_ == 2, n, pf.keys_f32.data());
     pending_.push_back(std::move(pf));
-    push_window(frame_id, T);
+    push_window(frame_id, T, ring_slot);
     frames_seen_ += 1;
     if (static_cast<int>(pending_.size()) >= cfg_.build_batch_frames) build_now();
     return;
@@ -902,20 +962,87 @@ void Context::ingest_frame(std::int64_t frame_id, const float* visual, const voi
 
   const std::int64_t pid = place_frame(frame_id, visual);
   if (partition) *partition = pid;
-  run_inserts(frame_id, pid, T, assigned);
-  push_window(frame_id, T);
   frames_seen_ += 1;
-  repin();
-  apply_cadence(frame_id, pid);
-  tier_kick();
+  if (!async_ok) {
+    ia_.T = T;
+    ia_.pid = static_cast<std::int32_t>(pid);
+    ia_.ring_slot = ring_slot;
+    run_inserts(frame_id, pid, T, assigned, false);
+    push_window(frame_id, T, ring_slot);
+    repin();
+    apply_cadence(frame_id, pid);
+    tier_kick();
+    return;
+  }
+  // launch this frame (all domains from token 0), its outcome block copied back on the stream
+  ia_.T = T;
+  ia_.pid = static_cast<std::int32_t>(pid);
+  ia_.ring_slot = ring_slot;
+  {
+    std::vector<int> active(static_cast<std::size_t>(L_)), cursor(static_cast<std::size_t>(L_), 0);
+    std::iota(active.begin(), active.end(), 0);
+    launch_round(active, cursor);
+  }
+  PendingIngest next;
+  next.active = true;
+  next.frame_id = frame_id;
+  next.pid = pid;
+  next.T = T;
+  next.ring_slot = ring_slot;
+  next.buf = b;
+  next.ev = ev_ing_[b];
+  KVC_CUDA(cudaEventRecord(next.ev, st_));
+  if (ping_.active) {  // the previous frame (no host events): its replay overlaps this frame's kernels
+    finish_frame(nullptr);
+    select_frame_buffer(b);
+  }
+  ping_ = next;
 }
 
 // Runs on_insert for every (layer, token) of the frame in layer-major order
 // (engine.cpp:169-170). The GPU resolves every domain in parallel until a host event; the
 // host replays the outcomes in reference order and settles host events domain by domain so
 // ids, split seeds and LRU ticks are assigned exactly as the sequential reference does.
-void Context::run_inserts(std::int64_t frame_id, std::int64_t pid, int T, std::int64_t* assigned) {
-  const int ring_slot = static_cast<int>(frames_seen_ % t_.W);
+// One resolve round for `active` domains from their cursors: candidates, distance tile, resolve,
+// row store, and the outcome block / error word copied back (not waited for).
+void Context::launch_round(const std::vector<int>& active, const std::vector<int>& cursor) {
+  flush_resid();
+  ia_.n_active = static_cast<std::int32_t>(active.size());
+  for (std::size_t i = 0; i < active.size(); ++i) h_active_[i] = active[i];
+  for (int l = 0; l < L_; ++l) h_cursor_[l] = cursor[static_cast<std::size_t>(l)];
+  KVC_CUDA(cudaMemcpyAsync(d_active_, h_active_, L_ * 8, cudaMemcpyHostToDevice, st_));
+  round_timed_ = timing_;
+  if (timing_) KVC_CUDA(cudaEventRecord(ev_[0], st_));
+  launches_ += launch_build_cands(t_, ia_, st_);
+  if (timing_) KVC_CUDA(cudaEventRecord(ev_[1], st_));
+  if (assign_tc_) {
+    ia_.margin = kTcMargin;
+    launches_ += launch_assign_tc(t_, ia_, key_map_, st_);
+    if (timing_) KVC_CUDA(cudaEventRecord(ev_[2], st_));
+  } else {
+    ia_.margin = kSimtMargin;
+    launches_ += launch_approx(t_, ia_, st_);
+    if (timing_) KVC_CUDA(cudaEventRecord(ev_[2], st_));
+    launches_ += launch_topm(t_, ia_, st_);
+  }
+  if (timing_) KVC_CUDA(cudaEventRecord(ev_[3], st_));
+  {
+    const int n = resolve_seq_ ? 0 : launch_resolve_spec(t_, ia_, st_);
+    launches_ += n ? n : launch_resolve(t_, ia_, st_);
+  }
+  if (timing_) KVC_CUDA(cudaEventRecord(ev_[4], st_));
+  launches_ += launch_store_rows(t_, ia_, st_);
+  KVC_CUDA(cudaGetLastError());
+  if (timing_) KVC_CUDA(cudaEventRecord(ev_[5], st_));
+  KVC_CUDA(cudaMemcpyAsync(h_evk_, ia_.ev_kind, (static_cast<std::size_t>(L_) * t_.tmax * 2 + static_cast<std::size_t>(L_) * 3) * 4,
+                           cudaMemcpyDeviceToHost, st_));
+  KVC_CUDA(cudaMemcpyAsync(h_err_, t_.err, 4, cudaMemcpyDeviceToHost, st_));
+}
+
+// launched: the first round (all domains from token 0) is already in flight with its outcome
+// block in h_evk_ (pipelined ingest); otherwise it is launched here.
+void Context::run_inserts(std::int64_t frame_id, std::int64_t pid, int T, std::int64_t* assigned, bool launched) {
+  const int ring_slot = ia_.ring_slot;
   const bool eager = !cfg_.defer_host_splits;
   std::vector<int> cursor(static_cast<std::size_t>(L_), 0), replayed(static_cast<std::size_t>(L_), 0);
   std::vector<int> active;
@@ -933,45 +1060,23 @@ void Context::run_inserts(std::int64_t frame_id, std::int64_t pid, int T, std::i
   const auto r0 = std::chrono::steady_clock::now();
   while (frontier < L_) {
     if (launch) {
-      flush_resid();
-      ia_.n_active = static_cast<std::int32_t>(active.size());
-      for (std::size_t i = 0; i < active.size(); ++i) {
-        h_active_[i] = active[i];
-      }
-      for (int l = 0; l < L_; ++l) h_cursor_[l] = cursor[static_cast<std::size_t>(l)];
-      KVC_CUDA(cudaMemcpyAsync(d_active_, h_active_, L_ * 8, cudaMemcpyHostToDevice, st_));
       const auto lc0 = std::chrono::steady_clock::now();
-      if (timing_) KVC_CUDA(cudaEventRecord(ev_[0], st_));
-      launches_ += launch_build_cands(t_, ia_, st_);
-      if (timing_) KVC_CUDA(cudaEventRecord(ev_[1], st_));
-      if (assign_tc_) {
-        ia_.margin = kTcMargin;
-        launches_ += launch_assign_tc(t_, ia_, key_map_, st_);
-        if (timing_) KVC_CUDA(cudaEventRecord(ev_[2], st_));
+      cudaEvent_t done = nullptr;
+      if (launched) {
+        launched = false;  // the first round was launched by ingest_frame: wait for its outcome
+        done = ping_wait_;  // block only (the next frame's kernels may already be queued behind it)
       } else {
-        ia_.margin = kSimtMargin;
-        launches_ += launch_approx(t_, ia_, st_);
-        if (timing_) KVC_CUDA(cudaEventRecord(ev_[2], st_));
-        launches_ += launch_topm(t_, ia_, st_);
+        launch_round(active, cursor);
       }
-      if (timing_) KVC_CUDA(cudaEventRecord(ev_[3], st_));
-      {
-        const int n = resolve_seq_ ? 0 : launch_resolve_spec(t_, ia_, st_);
-        launches_ += n ? n : launch_resolve(t_, ia_, st_);
-      }
-      if (timing_) KVC_CUDA(cudaEventRecord(ev_[4], st_));
-      launches_ += launch_store_rows(t_, ia_, st_);
-      KVC_CUDA(cudaGetLastError());
-      if (timing_) KVC_CUDA(cudaEventRecord(ev_[5], st_));
-      KVC_CUDA(cudaMemcpyAsync(h_evk_, ia_.ev_kind, (static_cast<std::size_t>(L_) * t_.tmax * 2 + static_cast<std::size_t>(L_) * 3) * 4,
-                               cudaMemcpyDeviceToHost, st_));
-      KVC_CUDA(cudaMemcpyAsync(h_err_, t_.err, 4, cudaMemcpyDeviceToHost, st_));
       const auto w0 = std::chrono::steady_clock::now();
       t_launch += std::chrono::duration<double, std::micro>(w0 - lc0).count();
-      sync();
+      if (done)
+        KVC_CUDA(cudaEventSynchronize(done));
+      else
+        sync();
       t_wait += std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - w0).count();
       check_err_word(*h_err_);
-      if (timing_) {
+      if (round_timed_) {  // (the round may have been launched before timing was switched on)
         float ms = 0.f;
         for (int i = 0; i < 5; ++i) {
           KVC_CUDA(cudaEventElapsedTime(&ms, ev_[i], ev_[i + 1]));
@@ -1040,6 +1145,15 @@ void Context::run_inserts(std::int64_t frame_id, std::int64_t pid, int T, std::i
       continue;
     }
     frame_add_flush(frame_id);  // host events add / remove map entries themselves
+    if (h_stop_[L_ + l] == EV_SPLIT && is_host(slot_id_[static_cast<std::size_t>(h_stop_[2 * L_ + l])])) {
+      // Pipelined ingest launched this frame before the previous frame's cadence offloaded the
+      // cluster (residence only turns Device -> Host between frames): the device decided with the
+      // old residence. Nothing of this token was committed; resolve the domain again from it.
+      cursor[static_cast<std::size_t>(l)] = stop;
+      active.assign(1, l);
+      launch = true;
+      continue;
+    }
     const std::int64_t id = handle_host_event(frame_id, pid, l, stop, h_stop_[L_ + l], h_stop_[2 * L_ + l]);
     ingest_t_[7] += 1.0;  // host events this frame
     if (assigned) assigned[static_cast<std::size_t>(l) * T + stop] = id;

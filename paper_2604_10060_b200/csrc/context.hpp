@@ -175,6 +175,7 @@ class Context {
   // Completes the deferred host bookkeeping of the last decode step (every host-state reader
   // calls this first; decode_step overlaps it with the next step's GPU work).
   void flush_pending();
+  void flush_decode();  // only the decode step's deferred bookkeeping (ingest keeps its pipeline)
   double offload(std::int64_t id);
   double fetch(std::int64_t id, int cause);
   cudaStream_t stream() const { return st_; }
@@ -212,8 +213,10 @@ class Context {
   std::size_t scratch_cap_ = 0;
   std::vector<void*> host_allocs_;
   // frame input + staging
-  void* d_fk_ = nullptr;
+  void* d_fk_ = nullptr;  // the current frame's input buffer (one of fkbuf_ / fvbuf_)
   void* d_fv_ = nullptr;
+  void* fkbuf_[2] = {nullptr, nullptr};
+  void* fvbuf_[2] = {nullptr, nullptr};
   void* d_stage_k_ = nullptr;
   void* d_stage_v_ = nullptr;
   float* d_stage_f32_ = nullptr;
@@ -232,9 +235,29 @@ class Context {
   // ingest buffers
   IngestArgs ia_{};
   std::int32_t *d_active_ = nullptr, *h_active_ = nullptr, *d_cursor_ = nullptr, *h_cursor_ = nullptr;
-  std::int32_t* h_evk_ = nullptr;
+  std::int32_t* h_evk_ = nullptr;  // the current frame's outcome block (one of h_out_)
   std::int32_t* h_evs_ = nullptr;
   std::int32_t* h_stop_ = nullptr;  // [3][L]: stop_t, stop_kind, stop_slot
+  std::int32_t* h_out_[2] = {nullptr, nullptr};
+  std::int32_t* h_errb_[2] = {nullptr, nullptr};
+  // Pipelined ingest: frame i's kernels are launched and its outcome block copied back, and its
+  // host replay is deferred until the next ingest call has launched frame i + 1 (when frame i
+  // needed no host event), or until any host-state reader flushes it.
+  struct PendingIngest {
+    bool active = false;
+    std::int64_t frame_id = 0, pid = 0;
+    int T = 0, ring_slot = 0, buf = 0;
+    cudaEvent_t ev = nullptr;  // outcome block of the first launch on the host
+  };
+  PendingIngest ping_;
+  cudaEvent_t ev_ing_[2] = {nullptr, nullptr};  // per frame buffer: its outcome block reached the host
+  int ibuf_ = 0;  // buffer of the most recently launched frame
+  bool round_timed_ = false;  // the last resolve round recorded its phase events
+  cudaEvent_t ping_wait_ = nullptr;  // outcome event of the frame being finished
+  void select_frame_buffer(int b);
+  void launch_round(const std::vector<int>& active, const std::vector<int>& cursor);
+  void finish_frame(std::int64_t* assigned);  // replay (+ host events) of ping_, then window/cadence
+  void flush_ingest();
   // decode buffers
   DecodeArgs da_{};
   void* d_dec_ = nullptr;  // packed result block
@@ -266,7 +289,8 @@ class Context {
   bool timing_ = false;
   bool resolve_seq_ = false;  // KVC_RESOLVE=seq selects the sequential resolve kernel
   bool assign_tc_ = false;    // tensor-core distance tile (KVC_ASSIGN=simt disables)
-  alignas(64) unsigned char key_map_[128];  // CUtensorMap over the frame keys
+  alignas(64) unsigned char key_map_[128];  // CUtensorMap over the current frame's keys
+  alignas(64) unsigned char key_maps_[2][128];
   void* d_check_ = nullptr;                 // debug_assign_check result words
   double step_t_[10] = {0};
   double ingest_t_[8] = {0};  // last frame: device us (cands, approx, topm, resolve, store), host us (wait, replay, rest)
@@ -392,12 +416,12 @@ class Context {
   void record(int cause, bool to_dev, std::int64_t id, std::int64_t bytes);
   std::int64_t entry_bytes() const;
   // engine (engine.cpp)
-  void push_window(std::int64_t frame_id, int T);
+  void push_window(std::int64_t frame_id, int T, int slot);
   void repin();
   std::vector<std::int64_t> window_owner_ids() const;
   void apply_cadence(std::int64_t frame_id, std::int64_t pid);
   std::int64_t place_frame(std::int64_t frame_id, const float* visual);
-  void run_inserts(std::int64_t frame_id, std::int64_t pid, int T, std::int64_t* assigned);
+  void run_inserts(std::int64_t frame_id, std::int64_t pid, int T, std::int64_t* assigned, bool launched);
   // split slow path
   std::vector<std::int64_t> split_pool(std::int64_t pid, int layer, bool host,
                                        std::vector<Member>&& ids, std::int64_t rows, int depth_unused);

@@ -134,6 +134,7 @@ void Context::peer_output(float* out, int mem) {
 void Context::decode_step(std::int64_t qid, const float* q, int q_mem, float* out, int out_mem,
                           const std::int64_t* gt, int n_gt) {
   (void)qid;
+  flush_ingest();  // a frame whose replay is still deferred (pipelined ingest)
   if (!built_) {
     flush_pending();
     build_now();  // engine.cpp:202
@@ -177,6 +178,11 @@ void Context::decode_step(std::int64_t qid, const float* q, int q_mem, float* ou
 }
 
 void Context::flush_pending() {
+  flush_ingest();
+  flush_decode();
+}
+
+void Context::flush_decode() {
   if (!inflight_) return;
   inflight_ = false;
   if (finish_step(cur_)) {
