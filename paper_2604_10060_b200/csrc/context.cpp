@@ -105,6 +105,13 @@ Context::~Context() {
   for (auto& e : ev_out_)
     if (e) cudaEventDestroy(e);
   if (cs_) cudaStreamDestroy(cs_);
+  if (in_st_) {
+    cudaStreamSynchronize(in_st_);
+    cudaStreamDestroy(in_st_);
+  }
+  for (int b = 0; b < 2; ++b)
+    for (cudaEvent_t e : {ev_ing_[b], ev_in_[b], ev_buf_[b]})
+      if (e) cudaEventDestroy(e);
   for (auto& row : evb_)
     for (auto& e : row)
       if (e) cudaEventDestroy(e);
@@ -266,6 +273,9 @@ void Context::alloc_device() {
     h_out_[b] = static_cast<std::int32_t*>(halloc(L * t_.tmax * 4 * 2 + L * 4 * 3 + 16));
     h_errb_[b] = static_cast<std::int32_t*>(halloc(16));
     KVC_CUDA(cudaEventCreateWithFlags(&ev_ing_[b], cudaEventDisableTiming));
+    KVC_CUDA(cudaEventCreateWithFlags(&ev_in_[b], cudaEventDisableTiming));
+    KVC_CUDA(cudaEventCreateWithFlags(&ev_buf_[b], cudaEventDisableTiming));
+    KVC_CUDA(cudaEventRecord(ev_buf_[b], st_));
   }
   h_evk_ = h_out_[0];
   h_evs_ = h_evk_ + L * t_.tmax;
@@ -295,6 +305,7 @@ void Context::alloc_device() {
   res_off_ = {o_parts, o_nps, o_rs, o_rb, o_nr, o_ps, o_pb, o_np, o_vs, o_nv, o_att, o_nc, o_fl, o_ew};
   t_.err = static_cast<std::int32_t*>(dalloc(16));
   KVC_CUDA(cudaStreamCreateWithFlags(&cs_, cudaStreamNonBlocking));
+  KVC_CUDA(cudaStreamCreateWithFlags(&in_st_, cudaStreamNonBlocking));
   for (int b = 0; b < 2; ++b) {
     d_blk_[b] = dalloc(dec_bytes_);
     h_blk_[b] = halloc(dec_bytes_);
@@ -885,7 +896,11 @@ void Context::finish_frame(std::int64_t* assigned) {
   ia_.T = p.T;
   ia_.pid = static_cast<std::int32_t>(p.pid);
   ia_.ring_slot = p.ring_slot;
+  const std::int64_t l0 = launches_;
   run_inserts(p.frame_id, p.pid, p.T, assigned, true);
+  // re-launches (host events) read the frame buffer again; they happen before any later frame is
+  // launched, so the buffer's release event can be moved after them
+  if (launches_ != l0) KVC_CUDA(cudaEventRecord(ev_buf_[p.buf], st_));
   push_window(p.frame_id, p.T, p.ring_slot);
   repin();
   apply_cadence(p.frame_id, p.pid);
@@ -912,6 +927,19 @@ void Context::ingest_frame(std::int64_t frame_id, const float* visual, const voi
   static const bool force_sync = std::getenv("KVC_INGEST_SYNC") != nullptr;
   const bool async_ok = !assigned && !cfg_.parity_mode && !cfg_.check_invariants && built_ && cfg_.defer_host_splits &&
                         !timing_ && !force_sync;
+  const int b = ping_.active ? (ping_.buf ^ 1) : (ibuf_ ^ 1);
+  ibuf_ = b;
+  // The payload crosses on the input stream first, overlapping the pending frame's kernels
+  // (buffer b's last reader, two frames back, is complete: ordered by ev_buf_[b]).
+  {
+    const std::size_t row = static_cast<std::size_t>(T) * d_ * es_;
+    const std::size_t pitch = static_cast<std::size_t>(t_.tmax) * d_ * es_;
+    const cudaMemcpyKind kind = mem == KVC_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    KVC_CUDA(cudaStreamWaitEvent(in_st_, ev_buf_[b], 0));
+    KVC_CUDA(cudaMemcpy2DAsync(fkbuf_[b], pitch, keys, row, row, L_, kind, in_st_));
+    KVC_CUDA(cudaMemcpy2DAsync(fvbuf_[b], pitch, values, row, row, L_, kind, in_st_));
+    KVC_CUDA(cudaEventRecord(ev_in_[b], in_st_));
+  }
   if (ping_.active) {
     KVC_CUDA(cudaEventSynchronize(ping_.ev));
     bool events = false;
@@ -919,15 +947,8 @@ void Context::ingest_frame(std::int64_t frame_id, const float* visual, const voi
     for (int l = 0; l < L_ && !events; ++l) events = stp[l] < ping_.T;
     if (!async_ok || events || *h_errb_[ping_.buf]) finish_frame(nullptr);
   }
-  const int b = ping_.active ? (ping_.buf ^ 1) : (ibuf_ ^ 1);
-  ibuf_ = b;
   select_frame_buffer(b);
-  // payload -> device frame buffer [L][tmax][d]
-  const std::size_t row = static_cast<std::size_t>(T) * d_ * es_;
-  const std::size_t pitch = static_cast<std::size_t>(t_.tmax) * d_ * es_;
-  const cudaMemcpyKind kind = mem == KVC_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
-  KVC_CUDA(cudaMemcpy2DAsync(d_fk_, pitch, keys, row, row, L_, kind, st_));
-  KVC_CUDA(cudaMemcpy2DAsync(d_fv_, pitch, values, row, row, L_, kind, st_));
+  KVC_CUDA(cudaStreamWaitEvent(st_, ev_in_[b], 0));
   const int ring_slot = static_cast<int>(frames_seen_ % t_.W);
   launches_ += launch_ring_write(t_, d_fk_, d_fv_, T, ring_slot, st_);
   for (int l = 0; l < L_; ++l)
@@ -954,6 +975,7 @@ void Context::ingest_frame(std::int64_t frame_id, const float* visual, const voi
     pf.keys_f32.resize(n);
     rows_to_f32(pf.keys_raw.data(), es_ == 2, n, pf.keys_f32.data());
     pending_.push_back(std::move(pf));
+    KVC_CUDA(cudaEventRecord(ev_buf_[b], st_));
     push_window(frame_id, T, ring_slot);
     frames_seen_ += 1;
     if (static_cast<int>(pending_.size()) >= cfg_.build_batch_frames) build_now();
@@ -968,6 +990,7 @@ void Context::ingest_frame(std::int64_t frame_id, const float* visual, const voi
     ia_.pid = static_cast<std::int32_t>(pid);
     ia_.ring_slot = ring_slot;
     run_inserts(frame_id, pid, T, assigned, false);
+    KVC_CUDA(cudaEventRecord(ev_buf_[b], st_));
     push_window(frame_id, T, ring_slot);
     repin();
     apply_cadence(frame_id, pid);
@@ -983,6 +1006,7 @@ void Context::ingest_frame(std::int64_t frame_id, const float* visual, const voi
     std::iota(active.begin(), active.end(), 0);
     launch_round(active, cursor);
   }
+  KVC_CUDA(cudaEventRecord(ev_buf_[b], st_));  // the frame buffer's readers are all launched
   PendingIngest next;
   next.active = true;
   next.frame_id = frame_id;

@@ -251,6 +251,9 @@ class Context {
   };
   PendingIngest ping_;
   cudaEvent_t ev_ing_[2] = {nullptr, nullptr};  // per frame buffer: its outcome block reached the host
+  cudaEvent_t ev_in_[2] = {nullptr, nullptr};   // per frame buffer: payload copied in (input stream)
+  cudaEvent_t ev_buf_[2] = {nullptr, nullptr};  // per frame buffer: last reader on the compute stream done
+  cudaStream_t in_st_ = nullptr;                // frame payload copies
   int ibuf_ = 0;  // buffer of the most recently launched frame
   bool round_timed_ = false;  // the last resolve round recorded its phase events
   cudaEvent_t ping_wait_ = nullptr;  // outcome event of the frame being finished
