@@ -221,6 +221,11 @@ KVC_API int kvc_cluster_tier(kvc_ctx* ctx, int64_t id, int64_t* out);
  * pages, Host clusters with all member pages in HBM, clusters whose page fills disagree with the
  * member count / logical device tail. All zero after kvc_tier_sync. */
 KVC_API int kvc_debug_tier_check(kvc_ctx* ctx, int64_t* out4);
+/* split_two (clustering.cpp:180-208) of n host points (the context's d) through the device split
+ * kernel the maintenance slow path uses (split.cu); meta3 = {k_live, iterations, degenerate}.
+ * Bit-identical to kvc_host_split_two / kvc_host_kmeans(k=2, 50, 1e-9). Returns k_live or < 0. */
+KVC_API int kvc_debug_split_two(kvc_ctx* ctx, const float* pts, int32_t n, uint64_t seed, int32_t* assign,
+                                int32_t* meta3, double* objective);
 
 /* ------------------------------------------------------------------ multi-GPU: fused output exchange
  * Domains are sharded over ranks (one process per GPU). Instead of an all-gather pass after each

@@ -144,6 +144,7 @@ def lib():
         L.kvc_tier_stats.argtypes = [vp, i64p]
         L.kvc_cluster_tier.argtypes = [vp, C.c_int64, i64p]
         L.kvc_debug_tier_check.argtypes = [vp, i64p]
+        L.kvc_debug_split_two.argtypes = [vp, f32p, C.c_int32, C.c_uint64, i32p, i32p, f64p]
         L.kvc_exchange_bytes.restype = C.c_size_t
         L.kvc_exchange_bytes.argtypes = [C.c_int32, C.c_int32, C.c_int32]
         L.kvc_ipc_alloc.argtypes = [C.c_size_t, C.POINTER(vp), C.c_void_p]
@@ -182,7 +183,7 @@ EXPORTED = [
     "kvc_launch_count", "kvc_last_step_timing", "kvc_set_timing", "kvc_last_ingest_timing",
     "kvc_debug_resolve_profile", "kvc_host_split_two", "kvc_host_kmeans", "kvc_host_tau",
     "kvc_host_mix_seed", "kvc_debug_div_check", "kvc_debug_assign_check", "kvc_tier_sync",
-    "kvc_tier_stats", "kvc_cluster_tier", "kvc_debug_tier_check", "kvc_exchange_bytes", "kvc_ipc_alloc",
+    "kvc_tier_stats", "kvc_cluster_tier", "kvc_debug_tier_check", "kvc_debug_split_two", "kvc_exchange_bytes", "kvc_ipc_alloc",
     "kvc_ipc_open", "kvc_ipc_close", "kvc_ipc_free", "kvc_set_peers", "kvc_peer_output",
 ]
 
@@ -429,6 +430,18 @@ class ClusterKVCache:
         out = np.zeros(4, np.int64)
         _check(lib().kvc_debug_tier_check(self.h, _p(out, i64p)))
         return tuple(int(x) for x in out)
+
+    def debug_split_two(self, pts, seed: int):
+        """split_two of host points [n, d] through the device split kernel (split.cu):
+        (assign, k_live, iterations, degenerate, objective)."""
+        pts = np.ascontiguousarray(pts, np.float32)
+        n = pts.shape[0]
+        assign = np.zeros(n, np.int32)
+        meta = np.zeros(3, np.int32)
+        obj = np.zeros(1, np.float64)
+        _check(lib().kvc_debug_split_two(self.h, _p(pts, f32p), n, seed, _p(assign, i32p), _p(meta, i32p),
+                                         _p(obj, f64p)))
+        return assign, int(meta[0]), int(meta[1]), bool(meta[2]), float(obj[0])
 
     # ------------------------------------------------------------------ fused output exchange
     def set_peers(self, n_ranks: int, rank: int, dom_offset: int, total_domains: int, bufs):

@@ -452,6 +452,23 @@ int kvc_debug_tier_check(kvc_ctx* ctx, int64_t* out) {
   return guard([&] { F(ctx).tier_check(out); });
 }
 
+int kvc_debug_split_two(kvc_ctx* ctx, const float* pts, int32_t n, uint64_t seed, int32_t* assign, int32_t* meta3,
+                        double* objective) {
+  int live = 0;
+  const int rc = guard([&] {
+    const kvc::KMeansOut o = F(ctx).debug_split_two_dev(pts, n, seed);
+    for (int i = 0; i < n; ++i) assign[i] = o.assign[static_cast<std::size_t>(i)];
+    if (meta3) {
+      meta3[0] = o.k_live;
+      meta3[1] = o.iterations;
+      meta3[2] = o.degenerate ? 1 : 0;
+    }
+    if (objective) *objective = o.objective;
+    live = o.k_live;
+  });
+  return rc != KVC_OK ? rc : live;
+}
+
 int kvc_cluster_tier(kvc_ctx* ctx, int64_t id, int64_t* out) {
   return guard([&] { F(ctx).cluster_tier(id, out); });
 }

@@ -264,6 +264,8 @@ void Context::alloc_device() {
                  make_key_tensor_map(key_maps_[0], fkbuf_[0], d, t_.tmax, L) &&
                  make_key_tensor_map(key_maps_[1], fkbuf_[1], d, t_.tmax, L);
     std::memcpy(key_map_, key_maps_[0], sizeof(key_map_));
+    const char* sm = std::getenv("KVC_SPLIT_DEV_MIN");  // smallest group split on the GPU (0: never)
+    if (sm) split_dev_min_ = std::atoi(sm);
   }
   d_active_ = static_cast<std::int32_t*>(dalloc(L * 4 * 2));
   d_cursor_ = d_active_ + L;
@@ -1325,8 +1327,6 @@ std::vector<std::int64_t> Context::split_pool(std::int64_t pid, int layer, bool 
     idx.insert(idx.end(), g.begin(), g.end());
   };
 
-  std::vector<double> tmp(static_cast<std::size_t>(d_));
-  std::vector<float> sub;
   auto rec = [&](auto&& self, std::vector<int> grp, int depth) -> void {
     if (grp.size() < 2) {
       std::vector<double> rep(static_cast<std::size_t>(d_));
@@ -1335,11 +1335,7 @@ std::vector<std::int64_t> Context::split_pool(std::int64_t pid, int layer, bool 
       emit(grp, std::move(rep), var);
       return;
     }
-    sub.resize(grp.size() * static_cast<std::size_t>(d_));
-    for (std::size_t i = 0; i < grp.size(); ++i)
-      std::memcpy(&sub[i * d_], keys + static_cast<std::size_t>(grp[i]) * d_, d_ * 4);
-    const KMeansOut halves = split_two(sub.data(), static_cast<int>(grp.size()), d_,
-                                       mix_seed(maint_seed_, static_cast<std::uint64_t>(split_counter_++)));
+    const KMeansOut halves = split_two_staged(grp, mix_seed(maint_seed_, static_cast<std::uint64_t>(split_counter_++)));
     mstats_[5] += 1;  // split_ops_total
     std::vector<int> g2[2];
     for (std::size_t i = 0; i < grp.size(); ++i) g2[halves.assign[i]].push_back(grp[i]);
@@ -1366,6 +1362,71 @@ std::vector<std::int64_t> Context::split_pool(std::int64_t pid, int layer, bool 
   for (std::size_t i = 0; i < out.size(); ++i) ring_owner_patch(layer, C(out[i]).members, slots[i]);
   ring_owner_upload(layer);
   return out;
+}
+
+// split_two (kmeans.cpp, clustering.cpp:180-208) of the staged rows grp[]: on the GPU (split.cu)
+// for groups of at least split_dev_min_ rows, else on the host. Both are bit-identical; the host
+// owns the generator, so the device gets the seeding's two draws (first index, uniform) in the
+// order plus_plus makes them.
+KMeansOut Context::split_two_staged(const std::vector<int>& grp, std::uint64_t seed) {
+  const int n = static_cast<int>(grp.size());
+  if (split_dev_min_ <= 0 || n < std::max(2, split_dev_min_) || d_ > 256) {
+    std::vector<float> sub(static_cast<std::size_t>(n) * d_);
+    for (int i = 0; i < n; ++i)
+      std::memcpy(&sub[static_cast<std::size_t>(i) * d_], h_stage_f32_ + static_cast<std::size_t>(grp[i]) * d_,
+                  static_cast<std::size_t>(d_) * 4);
+    return split_two(sub.data(), n, d_, seed);
+  }
+  Rng64 rng(seed);
+  const int first = static_cast<int>(rng.index(static_cast<std::size_t>(n)));
+  const double uni = rng.uniform();
+  const std::size_t dbl = (static_cast<std::size_t>(n) * (d_ + 1) + 1) * 8;
+  const std::size_t ints = (2 * static_cast<std::size_t>(n) + 4) * 4;
+  auto* base = static_cast<std::uint8_t*>(dalloc_scratch(dbl + ints));
+  auto* u = reinterpret_cast<double*>(base);
+  double* d_obj = u + static_cast<std::size_t>(n) * (d_ + 1);
+  auto* d_i = reinterpret_cast<std::int32_t*>(base + dbl);  // idx[n] | assign[n] | meta[4]
+  const std::size_t hobj = (ints + 7) & ~std::size_t{7};
+  if (static_cast<std::int64_t>(hobj + 8) > split_cap_) {
+    split_cap_ = static_cast<std::int64_t>(hobj + 8) * 2;
+    h_split_ = halloc(static_cast<std::size_t>(split_cap_));
+  }
+  auto* h_i = static_cast<std::int32_t*>(h_split_);
+  auto* h_obj = reinterpret_cast<double*>(static_cast<std::uint8_t*>(h_split_) + hobj);
+  std::memcpy(h_i, grp.data(), static_cast<std::size_t>(n) * 4);
+  KVC_CUDA(cudaMemcpyAsync(d_i, h_i, static_cast<std::size_t>(n) * 4, cudaMemcpyHostToDevice, st_));
+  launches_ += launch_split_two(d_stage_f32_, d_i, n, d_, first, uni, u, d_i + n, d_i + 2 * n, d_obj, st_);
+  KVC_CUDA(cudaMemcpyAsync(h_i + n, d_i + n, static_cast<std::size_t>(n + 4) * 4, cudaMemcpyDeviceToHost, st_));
+  KVC_CUDA(cudaMemcpyAsync(h_obj, d_obj, 8, cudaMemcpyDeviceToHost, st_));
+  sync();
+  const std::int32_t* meta = h_i + 2 * n;
+  if (meta[3] != 0) fail(-2, "normalize of zero vector");
+  KMeansOut o;
+  o.assign.assign(h_i + n, h_i + 2 * n);
+  o.k_live = meta[0];
+  o.iterations = meta[1];
+  o.degenerate = meta[2] != 0;
+  o.objective = *h_obj;
+  return o;
+}
+
+KMeansOut Context::debug_split_two_dev(const float* pts, int n, std::uint64_t seed) {
+  if (n < 2) fail(-6, "split_two: need at least 2 points");
+  ensure_stage(n + 1);
+  KVC_CUDA(cudaMemcpyAsync(d_stage_f32_, pts, static_cast<std::size_t>(n) * d_ * 4, cudaMemcpyHostToDevice, st_));
+  std::vector<int> grp(static_cast<std::size_t>(n));
+  std::iota(grp.begin(), grp.end(), 0);
+  const int keep = split_dev_min_;
+  split_dev_min_ = 2;
+  KMeansOut o;
+  try {
+    o = split_two_staged(grp, seed);
+  } catch (...) {
+    split_dev_min_ = keep;
+    throw;
+  }
+  split_dev_min_ = keep;
+  return o;
 }
 
 std::int64_t Context::handle_host_event(std::int64_t frame_id, std::int64_t pid, int layer, int tok,

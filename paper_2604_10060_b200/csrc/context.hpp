@@ -19,6 +19,7 @@
 
 #include "../../include/kvc.h"
 #include "extent_alloc.hpp"
+#include "kmeans.hpp"
 #include "kvc_core.hpp"
 
 namespace kvc {
@@ -429,6 +430,17 @@ class Context {
   std::vector<std::int64_t> split_pool(std::int64_t pid, int layer, bool host,
                                        std::vector<Member>&& ids, std::int64_t rows, int depth_unused);
   std::int64_t stage_cluster(std::int32_t slot, bool with_buffer);
+ public:
+  // split_two (kmeans.cpp) of staged rows grp[] on the GPU (split.cu), bit-identical to the host
+  // restatement; falls back to it for groups below split_dev_min_ rows or d > 256.
+  KMeansOut split_two_staged(const std::vector<int>& grp, std::uint64_t seed);
+  // debug: split_two of host points through the device path (stages them first)
+  KMeansOut debug_split_two_dev(const float* pts, int n, std::uint64_t seed);
+
+ private:
+  int split_dev_min_ = 64;
+  void* h_split_ = nullptr;  // pinned: idx[n] | assign[n] | meta[4] | objective
+  std::int64_t split_cap_ = 0;
   void stage_download(std::int64_t rows);
   void init_slots(const std::vector<std::int32_t>& slots, const std::vector<std::vector<double>>& reps,
                   const std::vector<double>& vars, const std::vector<std::int64_t>& stats,
