@@ -73,6 +73,8 @@ Context::Context(const kvc_cfg& cfg, int d, int L) : cfg_(cfg), d_(d), L_(L) {
   if (cfg_.kv_dtype != KVC_DTYPE_F32 && cfg_.kv_dtype != KVC_DTYPE_BF16) fail(-10, "kv_dtype");
   // (<= 64: a window page's dedup mask is one 64-bit word of its attention descriptor)
   if (cfg_.page_tokens < 8 || cfg_.page_tokens > 64 || cfg_.page_tokens % 8) fail(-10, "page_tokens must be 8..64, a multiple of 8");
+  if (cfg_.max_candidates < 1 || cfg_.max_candidates > 6144)
+    fail(-10, "max_candidates must be 1..6144 (the ingest top-M keeps 8 candidate rows in shared memory)");
   if (d % 8 != 0 || d > 256) fail(-10, "the device path supports d % 8 == 0 and d <= 256");
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
@@ -1380,11 +1382,11 @@ KMeansOut Context::split_two_staged(const std::vector<int>& grp, std::uint64_t s
   Rng64 rng(seed);
   const int first = static_cast<int>(rng.index(static_cast<std::size_t>(n)));
   const double uni = rng.uniform();
-  const std::size_t dbl = (static_cast<std::size_t>(n) * (d_ + 1) + 1) * 8;
+  const std::size_t dbl = (static_cast<std::size_t>(n) * (2 * d_ + 3) + 1) * 8;
   const std::size_t ints = (2 * static_cast<std::size_t>(n) + 4) * 4;
   auto* base = static_cast<std::uint8_t*>(dalloc_scratch(dbl + ints));
   auto* u = reinterpret_cast<double*>(base);
-  double* d_obj = u + static_cast<std::size_t>(n) * (d_ + 1);
+  double* d_obj = u + static_cast<std::size_t>(n) * (2 * d_ + 3);
   auto* d_i = reinterpret_cast<std::int32_t*>(base + dbl);  // idx[n] | assign[n] | meta[4]
   const std::size_t hobj = (ints + 7) & ~std::size_t{7};
   if (static_cast<std::int64_t>(hobj + 8) > split_cap_) {

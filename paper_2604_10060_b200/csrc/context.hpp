@@ -438,7 +438,7 @@ class Context {
   KMeansOut debug_split_two_dev(const float* pts, int n, std::uint64_t seed);
 
  private:
-  int split_dev_min_ = 64;
+  int split_dev_min_ = 128;
   void* h_split_ = nullptr;  // pinned: idx[n] | assign[n] | meta[4] | objective
   std::int64_t split_cap_ = 0;
   void stage_download(std::int64_t rows);

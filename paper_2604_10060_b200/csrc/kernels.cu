@@ -987,15 +987,65 @@ __global__ void k_ring_write(DevTables t, const uint8_t* fk, const uint8_t* fv, 
 }
 
 // ============================================================================ store maintenance
-__global__ void k_append_runs(DevTables t, const AppendRun* runs, int n_runs, const int32_t* idx,
-                              const uint8_t* sk, const uint8_t* sv) {
-  const int w = (blockIdx.x * blockDim.x + threadIdx.x) / 32;
-  if (w >= n_runs) return;
-  const AppendRun r = runs[w];
-  const int rb = t.d * t.es;
-  for (int j = 0; j < r.n_rows; ++j) {
+// One CTA per run: the run's pages are claimed at once (the free-stack pops in the order a
+// row-by-row warp_append would make them, so the layout is the same), then every thread copies
+// 16-byte pieces of the run's rows. Runs of one launch target distinct (slot, list) pairs.
+__global__ void __launch_bounds__(256) k_append_runs(DevTables t, const AppendRun* runs, int n_runs,
+                                                     const int32_t* idx, const uint8_t* sk, const uint8_t* sv) {
+  const AppendRun r = runs[blockIdx.x];
+  const bool to_buf = r.to_buffer != 0;
+  int* list = to_buf ? t.bpages + static_cast<int64_t>(r.slot) * t.maxbp : t.pages + static_cast<int64_t>(r.slot) * t.maxp;
+  __shared__ int s_page0, s_fill0, s_room, s_base_n, s_rows;
+  if (threadIdx.x == 0) {
+    int* np = to_buf ? &t.nbpages[r.slot] : &t.npages[r.slot];
+    const int cap = to_buf ? t.maxbp : t.maxp;
+    const int n = *np;
+    const int page = n > (to_buf ? 0 : t.seal[r.slot]) ? list[n - 1] : -1;  // sealed pages take no rows
+    const int fill0 = page >= 0 ? t.pg_fill[page] : t.P;
+    const int room = page >= 0 ? min(t.P - fill0, r.n_rows) : 0;
+    int rows = r.n_rows;
+    int k = (rows - room + t.P - 1) / t.P;  // fresh pages
+    if (n + k > cap) {
+      set_err(t, DERR_CLUSTER_PAGES);
+      k = cap - n;
+    }
+    int top = k > 0 ? atomicSub(t.free_top, k) - k : 0;
+    if (top < 0) {
+      atomicAdd(t.free_top, k);
+      set_err(t, DERR_PAGES);
+      k = 0;
+    }
+    rows = min(rows, room + k * t.P);
+    for (int i = 0; i < k; ++i) {
+      const int pg = t.free_stack[top + k - 1 - i];
+      list[n + i] = pg;
+      t.pg_fill[pg] = min(t.P, rows - room - i * t.P);
+    }
+    *np = n + k;
+    if (room > 0) t.pg_fill[page] = fill0 + room;
+    s_page0 = page;
+    s_fill0 = fill0;
+    s_room = room;
+    s_base_n = n;
+    s_rows = rows;
+  }
+  __syncthreads();
+  const int rb = t.d * t.es, pieces = rb / 16, rows = s_rows, room = s_room;
+  for (int64_t q = threadIdx.x; q < static_cast<int64_t>(rows) * pieces; q += blockDim.x) {
+    const int j = static_cast<int>(q / pieces), o = static_cast<int>(q - static_cast<int64_t>(j) * pieces) * 16;
+    int page, pos;
+    if (j < room) {
+      page = s_page0;
+      pos = s_fill0 + j;
+    } else {
+      page = list[s_base_n + (j - room) / t.P];
+      pos = (j - room) % t.P;
+    }
     const int64_t row = idx[r.first_row + j];
-    if (!warp_append(t, r.slot, r.to_buffer != 0, sk + row * rb, sv + row * rb)) break;
+    *reinterpret_cast<uint4*>(page_k(t, page) + static_cast<int64_t>(pos) * rb + o) =
+        *reinterpret_cast<const uint4*>(sk + row * rb + o);
+    *reinterpret_cast<uint4*>(page_v(t, page) + static_cast<int64_t>(pos) * rb + o) =
+        *reinterpret_cast<const uint4*>(sv + row * rb + o);
   }
 }
 
@@ -2659,9 +2709,8 @@ int launch_ring_rows(const DevTables& t, const void* fk, const void* fv, int32_t
 int launch_append_runs(const DevTables& t, const AppendRun* runs, int32_t n_runs, const int32_t* idx,
                        const void* sk, const void* sv, cudaStream_t st) {
   if (n_runs <= 0) return 0;
-  const int warps = 4;
-  k_append_runs<<<(n_runs + warps - 1) / warps, 32 * warps, 0, st>>>(
-      t, runs, n_runs, idx, static_cast<const uint8_t*>(sk), static_cast<const uint8_t*>(sv));
+  k_append_runs<<<n_runs, 256, 0, st>>>(t, runs, n_runs, idx, static_cast<const uint8_t*>(sk),
+                                       static_cast<const uint8_t*>(sv));
   return 1;
 }
 

@@ -313,7 +313,7 @@ struct SlotHeader {
 int launch_slot_headers(const DevTables& t, const SlotHeader* h, int32_t n, cudaStream_t st);
 
 // Converts staged kv-dtype rows to fp32 (for host read-back).
-// split.cu: split_two of rows[idx[i]] (i < n), one CTA; scratch n * (d + 1) doubles; returns 0
+// split.cu: split_two of rows[idx[i]] (i < n), one CTA; scratch n * (2d + 3) doubles; returns 0
 // (nothing launched) for n < 2 or d > 256.
 int launch_split_two(const float* rows, const int32_t* idx, int n, int d, int first, double uni, double* scratch,
                      int32_t* assign, int32_t* meta, double* objective, cudaStream_t st);

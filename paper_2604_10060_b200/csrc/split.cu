@@ -17,16 +17,32 @@ namespace {
 using namespace dm;
 
 constexpr int SPT = 512;
+constexpr int OBJ_CHUNK = 4096;  // 32 KB of the objective's terms per shared-memory pass
 
-__device__ __forceinline__ double dot_seq(const double* a, const double* b, int d) {
+// Sequential fp64 dot of point i (column-major unit rows ut[c * n + i]: coalesced across the
+// threads of a warp, which take consecutive points) with a shared-memory vector.
+__device__ __forceinline__ double dot_col(const double* __restrict__ ut, int n, int i, const double* v, int d) {
   double s = 0.0;
-  for (int c = 0; c < d; ++c) s = dadd(s, dmul(a[c], b[c]));
+  for (int c = 0; c < d; ++c) s = dadd(s, dmul(ut[static_cast<int64_t>(c) * n + i], v[c]));
   return s;
 }
 
-__device__ __forceinline__ double unit_cos(const double* p, const double* c, double nc, int d) {
+// Both centroids in one pass (two independent chains; each is the reference's sequential dot).
+__device__ __forceinline__ void dot2_col(const double* __restrict__ ut, int n, int i, const double* c0,
+                                         const double* c1, int d, double& s0, double& s1) {
+  double a = 0.0, b = 0.0;
+  for (int c = 0; c < d; ++c) {
+    const double x = ut[static_cast<int64_t>(c) * n + i];
+    a = dadd(a, dmul(x, c0[c]));
+    b = dadd(b, dmul(x, c1[c]));
+  }
+  s0 = a;
+  s1 = b;
+}
+
+__device__ __forceinline__ double cos_of(double dot, double nc) {
   if (nc < 1e-12) return -2.0;  // degenerate centroid (clustering.cpp:72-76)
-  return clamp1(ddiv(dot_seq(p, c, d), nc));
+  return clamp1(ddiv(dot, nc));
 }
 
 struct SplitSmem {
@@ -38,22 +54,80 @@ struct SplitSmem {
   double far_s;
 };
 
-// rows: staged f32 rows; idx[n]: the points of this split (rows idx[i]); u: scratch [n][d].
-// out: assign[n]; meta[4] = {k_live, iterations, degenerate, error}; obj[1].
+// Cosines of every point to both centroids (unit_cos, clustering.cpp:72-76) into sc[2][n]. The
+// reference recomputes them in the objective of one iteration and the assignment of the next,
+// with the same centroids: computing them once yields the identical values.
+__device__ __forceinline__ void cosines(const double* __restrict__ ut, int n, int d, SplitSmem& S, double* sc) {
+  // two points per thread (four independent chains) and the loads of 8 dimensions issued ahead
+  // of their arithmetic: the chains are latency-bound, so memory-level parallelism is the lever
+  for (int i0 = threadIdx.x; i0 < n; i0 += 2 * SPT) {
+    const int i1 = i0 + SPT;
+    const bool has1 = i1 < n;
+    const int j1 = has1 ? i1 : i0;
+    double a0 = 0.0, b0 = 0.0, a1 = 0.0, b1 = 0.0;
+    int c = 0;
+    for (; c + 8 <= d; c += 8) {
+      double x0[8], x1[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        x0[k] = ut[static_cast<int64_t>(c + k) * n + i0];
+        x1[k] = ut[static_cast<int64_t>(c + k) * n + j1];
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const double c0 = S.cent[0][c + k], c1 = S.cent[1][c + k];
+        a0 = dadd(a0, dmul(x0[k], c0));
+        b0 = dadd(b0, dmul(x0[k], c1));
+        a1 = dadd(a1, dmul(x1[k], c0));
+        b1 = dadd(b1, dmul(x1[k], c1));
+      }
+    }
+    for (; c < d; ++c) {
+      const double x0 = ut[static_cast<int64_t>(c) * n + i0], x1 = ut[static_cast<int64_t>(c) * n + j1];
+      a0 = dadd(a0, dmul(x0, S.cent[0][c]));
+      b0 = dadd(b0, dmul(x0, S.cent[1][c]));
+      a1 = dadd(a1, dmul(x1, S.cent[0][c]));
+      b1 = dadd(b1, dmul(x1, S.cent[1][c]));
+    }
+    sc[i0] = cos_of(a0, S.cn[0]);
+    sc[n + i0] = cos_of(b0, S.cn[1]);
+    if (has1) {
+      sc[i1] = cos_of(a1, S.cn[0]);
+      sc[n + i1] = cos_of(b1, S.cn[1]);
+    }
+  }
+}
+
+__device__ __forceinline__ void centroid_norms(SplitSmem& S, int d) {
+  if (threadIdx.x < 2) {
+    const double* c = S.cent[threadIdx.x];
+    double s = 0.0;
+    for (int k = 0; k < d; ++k) s = dadd(s, dmul(c[k], c[k]));
+    S.cn[threadIdx.x] = __dsqrt_rn(s);
+  }
+}
+
+// rows: staged f32 rows; idx[n]: the points of this split (rows idx[i]).
+// scratch (doubles): u[n][d] | ut[d][n] | sc[2][n] | nearv[n]
+// out: assign[n]; meta[4] = {k_live, iterations, degenerate, error}; objective[1].
 __global__ void __launch_bounds__(SPT) k_split_two(const float* rows, const int32_t* idx, int n, int d, int first,
-                                                    double uni, double* u, int32_t* assign, int32_t* meta,
+                                                    double uni, double* scratch, int32_t* assign, int32_t* meta,
                                                     double* objective) {
   __shared__ SplitSmem S;
+  __shared__ double S_ob[OBJ_CHUNK];
   const int tid = threadIdx.x;
+  double* u = scratch;
+  double* ut = u + static_cast<int64_t>(n) * d;
+  double* sc = ut + static_cast<int64_t>(n) * d;
+  double* nearv = sc + 2 * static_cast<int64_t>(n);
   if (tid == 0) {
     S.same = 1;
     S.degen = 0;
   }
   __syncthreads();
-  // unit rows (clustering.cpp:14-22): r / norm(r)
+  // unit rows (clustering.cpp:14-22): r / norm(r), stored row- and column-major
   for (int i = tid; i < n; i += SPT) {
     const float* p = rows + static_cast<int64_t>(idx[i]) * d;
-    double* r = u + static_cast<int64_t>(i) * d;
     double s = 0.0;
     for (int c = 0; c < d; ++c) {
       const double x = static_cast<double>(p[c]);
@@ -61,16 +135,22 @@ __global__ void __launch_bounds__(SPT) k_split_two(const float* rows, const int3
     }
     const double nr = __dsqrt_rn(s);
     if (nr < 1e-12) S.degen = 1;
-    for (int c = 0; c < d; ++c) r[c] = ddiv(static_cast<double>(p[c]), nr);
+    for (int c = 0; c < d; ++c) {
+      const double r = ddiv(static_cast<double>(p[c]), nr);
+      u[static_cast<int64_t>(i) * d + c] = r;
+      ut[static_cast<int64_t>(c) * n + i] = r;
+    }
   }
   __syncthreads();
   if (S.degen) {
     if (tid == 0) meta[3] = -2;  // zero vector (the host raises KVC_E_DEGENERATE)
     return;
   }
+  for (int c = tid; c < d; c += SPT) S.cent[0][c] = u[c];
+  __syncthreads();
   // all points equal (within 1e-12 of the first): the deterministic (n-1, 1) partition
   for (int i = 1 + tid; i < n; i += SPT)
-    if (dot_seq(u + static_cast<int64_t>(i) * d, u, d) < 1.0 - 1e-12) S.same = 0;
+    if (dot_col(ut, n, i, S.cent[0], d) < 1.0 - 1e-12) S.same = 0;
   __syncthreads();
   if (S.same) {
     for (int i = tid; i < n; i += SPT) assign[i] = i == n - 1 ? 1 : 0;
@@ -83,10 +163,11 @@ __global__ void __launch_bounds__(SPT) k_split_two(const float* rows, const int3
     }
     return;
   }
-  // k-means++ seeding with 1 - cosine weights, k = 2 (clustering.cpp:25-70). near[] -> assign
-  // (as doubles in u's tail would cost memory; the weights are recomputed by the sequential pass)
-  double* nearv = u + static_cast<int64_t>(n) * d;  // [n] (scratch sized n * (d + 1))
-  for (int i = tid; i < n; i += SPT) nearv[i] = dot_seq(u + static_cast<int64_t>(i) * d, u + static_cast<int64_t>(first) * d, d);
+  // k-means++ seeding with 1 - cosine weights, k = 2 (clustering.cpp:25-70)
+  __syncthreads();
+  for (int c = tid; c < d; c += SPT) S.cent[0][c] = u[static_cast<int64_t>(first) * d + c];
+  __syncthreads();
+  for (int i = tid; i < n; i += SPT) nearv[i] = dot_col(ut, n, i, S.cent[0], d);
   __syncthreads();
   if (tid == 0) {
     double mass = 0.0;
@@ -111,77 +192,88 @@ __global__ void __launch_bounds__(SPT) k_split_two(const float* rows, const int3
     S.stop = 0;
   }
   __syncthreads();
-  for (int c = tid; c < d; c += SPT) {
-    S.cent[0][c] = u[static_cast<int64_t>(first) * d + c];
-    S.cent[1][c] = u[static_cast<int64_t>(S.pick) * d + c];
-  }
+  for (int c = tid; c < d; c += SPT) S.cent[1][c] = u[static_cast<int64_t>(S.pick) * d + c];
   for (int i = tid; i < n; i += SPT) assign[i] = 0;
   __syncthreads();
+  centroid_norms(S, d);
+  __syncthreads();
+  cosines(ut, n, d, S, sc);
+  __syncthreads();
   for (int it = 0; it < 50; ++it) {
-    // centroid norms (unit_cos recomputes them per call: the same value each time)
-    if (tid < 2) {
-      double s = 0.0;
-      for (int c = 0; c < d; ++c) s = dadd(s, dmul(S.cent[tid][c], S.cent[tid][c]));
-      S.cn[tid] = __dsqrt_rn(s);
-    }
     if (tid == 0) {
       S.moved = 0;
       S.cnt[0] = 0;
       S.cnt[1] = 0;
     }
     __syncthreads();
-    // assignment, ties to the lower index (clustering.cpp:99-112)
+    // assignment, ties to the lower index (clustering.cpp:99-112), from the cached cosines
     int c0 = 0, c1 = 0, mv = 0;
     for (int i = tid; i < n; i += SPT) {
-      const double* p = u + static_cast<int64_t>(i) * d;
-      const double s0 = unit_cos(p, S.cent[0], S.cn[0], d);
-      const double s1 = unit_cos(p, S.cent[1], S.cn[1], d);
-      const int bj = s1 > s0 ? 1 : 0;
+      const int bj = sc[n + i] > sc[i] ? 1 : 0;
       if (assign[i] != bj) mv = 1;
       assign[i] = bj;
-      c0 += bj == 0;
-      c1 += bj == 1;
+      c0 += 1 - bj;
+      c1 += bj;
     }
-    if (mv) S.moved = 1;
-    atomicAdd(&S.cnt[0], c0);
-    atomicAdd(&S.cnt[1], c1);
+    if (__syncthreads_or(mv) && tid == 0) S.moved = 1;
+    if (c0) atomicAdd(&S.cnt[0], c0);
+    if (c1) atomicAdd(&S.cnt[1], c1);
     __syncthreads();
     // empty-cluster reseed (clustering.cpp:117-136): the point farthest from its centroid among
-    // clusters with more than one point (first minimum in index order)
+    // clusters with more than one point (first minimum in index order), with this iteration's
+    // centroids, i.e. the cached cosines
     for (int j = 0; j < 2; ++j) {
       if (S.cnt[j] != 0) continue;  // block-uniform
       if (tid == 0) {
-        S.far_i = n;
-        S.far_s = INFINITY;
-      }
-      __syncthreads();
-      if (tid == 0) {  // sequential scan: the strict < keeps the first minimum
+        int far = n;
+        double far_s = INFINITY;
         for (int i = 0; i < n; ++i) {
           const int ai = assign[i];
           if (S.cnt[ai] <= 1) continue;
-          const double s = unit_cos(u + static_cast<int64_t>(i) * d, S.cent[ai], S.cn[ai], d);
-          if (s < S.far_s) {
-            S.far_s = s;
-            S.far_i = i;
+          const double s = sc[static_cast<int64_t>(ai) * n + i];
+          if (s < far_s) {
+            far_s = s;
+            far = i;
           }
         }
-        if (S.far_i != n) {
-          S.cnt[assign[S.far_i]] -= 1;
-          assign[S.far_i] = j;
+        if (far != n) {
+          S.cnt[assign[far]] -= 1;
+          assign[far] = j;
           S.cnt[j] += 1;
           S.moved = 1;
         }
       }
       __syncthreads();
     }
-    // arithmetic means, sums in point order (clustering.cpp:138-150); one (cluster, dim) per thread
+    // arithmetic means, sums in point order (clustering.cpp:138-150); one (cluster, dim) per
+    // thread, rows read coalesced across the dimension. Adding +0.0 for non-members leaves the
+    // sum unchanged (it is never -0.0: it starts at +0.0 and exact cancellation rounds to +0.0).
     double newc = 0.0;
     int wj = -1, wc = 0;
     if (tid < 2 * d) {
       wj = tid / d;
       wc = tid - wj * d;
+      // software-pipelined: the next 16 rows' loads are in flight while this group is summed
       double acc = 0.0;
-      for (int i = 0; i < n; ++i)
+      const int n16 = n & ~15;
+      double x[16];
+      auto load16 = [&](int i) {
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          const double v = u[static_cast<int64_t>(i + k) * d + wc];
+          x[k] = assign[i + k] == wj ? v : 0.0;
+        }
+      };
+      if (n16) load16(0);
+      for (int i = 0; i < n16; i += 16) {
+        double y[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) y[k] = x[k];
+        if (i + 16 < n16) load16(i + 16);
+#pragma unroll
+        for (int k = 0; k < 16; ++k) acc = dadd(acc, y[k]);
+      }
+      for (int i = n16; i < n; ++i)
         if (assign[i] == wj) acc = dadd(acc, u[static_cast<int64_t>(i) * d + wc]);
       if (S.cnt[wj] != 0) newc = dmul(acc, ddiv(1.0, static_cast<double>(S.cnt[wj])));
       else wj = -1;  // an empty cluster keeps its centroid
@@ -189,21 +281,22 @@ __global__ void __launch_bounds__(SPT) k_split_two(const float* rows, const int3
     __syncthreads();
     if (wj >= 0) S.cent[wj][wc] = newc;
     __syncthreads();
-    if (tid < 2) {
-      double s2 = 0.0;
-      for (int c = 0; c < d; ++c) s2 = dadd(s2, dmul(S.cent[tid][c], S.cent[tid][c]));
-      S.cn[tid] = __dsqrt_rn(s2);
-    }
+    centroid_norms(S, d);
+    __syncthreads();
+    cosines(ut, n, d, S, sc);
     __syncthreads();
     // mean cosine to the own centroid, summed in point order (clustering.cpp:152-163)
-    for (int i = tid; i < n; i += SPT) {
-      const int ai = assign[i];
-      nearv[i] = unit_cos(u + static_cast<int64_t>(i) * d, S.cent[ai], S.cn[ai], d);
+    // staged through shared memory in chunks so the one summing thread reads at smem latency
+    double obj = 0.0;
+    for (int base = 0; base < n; base += OBJ_CHUNK) {
+      const int m = min(OBJ_CHUNK, n - base);
+      for (int k = tid; k < m; k += SPT) S_ob[k] = sc[static_cast<int64_t>(assign[base + k]) * n + base + k];
+      __syncthreads();
+      if (tid == 0)
+        for (int k = 0; k < m; ++k) obj = dadd(obj, S_ob[k]);
+      __syncthreads();
     }
-    __syncthreads();
     if (tid == 0) {
-      double obj = 0.0;
-      for (int i = 0; i < n; ++i) obj = dadd(obj, nearv[i]);
       obj = ddiv(obj, static_cast<double>(n));
       *objective = obj;
       meta[1] = it + 1;
