@@ -111,6 +111,7 @@ Context::~Context() {
     cudaStreamSynchronize(in_st_);
     cudaStreamDestroy(in_st_);
   }
+  if (ev_init_) cudaEventDestroy(ev_init_);
   for (int b = 0; b < 2; ++b)
     for (cudaEvent_t e : {ev_ing_[b], ev_in_[b], ev_buf_[b]})
       if (e) cudaEventDestroy(e);
@@ -277,6 +278,7 @@ void Context::alloc_device() {
     h_out_[b] = static_cast<std::int32_t*>(halloc(L * t_.tmax * 4 * 2 + L * 4 * 3 + 16));
     h_errb_[b] = static_cast<std::int32_t*>(halloc(16));
     KVC_CUDA(cudaEventCreateWithFlags(&ev_ing_[b], cudaEventDisableTiming));
+    if (b == 0) KVC_CUDA(cudaEventCreateWithFlags(&ev_init_, cudaEventDisableTiming));
     KVC_CUDA(cudaEventCreateWithFlags(&ev_in_[b], cudaEventDisableTiming));
     KVC_CUDA(cudaEventCreateWithFlags(&ev_buf_[b], cudaEventDisableTiming));
     KVC_CUDA(cudaEventRecord(ev_buf_[b], st_));
@@ -1227,40 +1229,46 @@ void Context::init_slots(const std::vector<std::int32_t>& slots,
                          const std::vector<std::int64_t>& nmem, const std::vector<std::int64_t>& cids,
                          const std::vector<std::uint8_t>& resid, const std::vector<std::int32_t>* nbuf,
                          const std::vector<std::vector<double>>* breps) {
-  // Host-computed exact statistics -> device tables. Few rows (split children / seeds):
-  // plain async copies from pinned staging, then the fp32 mirrors are refreshed on device.
+  // Host-computed exact statistics -> device tables: one packed record per slot in pinned
+  // staging, one copy, one scatter kernel; then the fp32 mirrors are refreshed on device.
   const std::size_t n = slots.size();
   if (n == 0) return;
-  for (std::size_t i = 0; i < n; ++i) {
-    const std::int64_t s = slots[i];
-    const double rn = norm_d(reps[i].data(), d_);
-    KVC_CUDA(cudaMemcpyAsync(t_.rep64 + s * d_, reps[i].data(), d_ * 8, cudaMemcpyHostToDevice, st_));
-    KVC_CUDA(cudaMemcpyAsync(t_.rnorm + s, &rn, 8, cudaMemcpyHostToDevice, st_));
-    KVC_CUDA(cudaMemcpyAsync(t_.var + s, &vars[i], 8, cudaMemcpyHostToDevice, st_));
-    KVC_CUDA(cudaMemcpyAsync(t_.stat + s, &stats[i], 8, cudaMemcpyHostToDevice, st_));
-    KVC_CUDA(cudaMemcpyAsync(t_.nmem + s, &nmem[i], 8, cudaMemcpyHostToDevice, st_));
-    KVC_CUDA(cudaMemcpyAsync(t_.cid + s, &cids[i], 8, cudaMemcpyHostToDevice, st_));
-    KVC_CUDA(cudaMemcpyAsync(t_.resid + s, &resid[i], 1, cudaMemcpyHostToDevice, st_));
-    const std::int32_t nb = nbuf ? (*nbuf)[i] : 0;
-    const std::uint8_t lz = nb > 0 ? 1 : 0;
-    KVC_CUDA(cudaMemcpyAsync(t_.nbuf + s, &nb, 4, cudaMemcpyHostToDevice, st_));
-    KVC_CUDA(cudaMemcpyAsync(t_.lazy + s, &lz, 1, cudaMemcpyHostToDevice, st_));
-    if (breps && nb > 0) {
-      const double bn = norm_d((*breps)[i].data(), d_);
-      KVC_CUDA(cudaMemcpyAsync(t_.brep64 + s * d_, (*breps)[i].data(), d_ * 8, cudaMemcpyHostToDevice, st_));
-      KVC_CUDA(cudaMemcpyAsync(t_.bnorm + s, &bn, 8, cudaMemcpyHostToDevice, st_));
-    }
-    // the pageable sources must stay alive until the copies complete
-    KVC_CUDA(cudaStreamSynchronize(st_));
+  const std::size_t rb = slot_init_bytes(d_), bytes = n * rb + n * 4;  // records | slot list
+  if (static_cast<std::int64_t>(bytes) > init_cap_) {
+    if (h_init_) KVC_CUDA(cudaStreamSynchronize(st_));
+    init_cap_ = static_cast<std::int64_t>(std::max(bytes, static_cast<std::size_t>(init_cap_) * 2));
+    h_init_ = halloc(static_cast<std::size_t>(init_cap_));
+    d_init_ = dalloc(static_cast<std::size_t>(init_cap_));
+  } else {
+    KVC_CUDA(cudaEventSynchronize(ev_init_));  // the previous batch's copy has left the staging
   }
-  std::vector<std::int32_t> sl(slots.begin(), slots.end());
-  ensure_idx(static_cast<std::int64_t>(n), 1);
-  std::memcpy(h_idx_, sl.data(), n * 4);
-  KVC_CUDA(cudaMemcpyAsync(d_idx_, h_idx_, n * 4, cudaMemcpyHostToDevice, st_));
-  launches_ += launch_refresh_mirror(t_, d_idx_, static_cast<std::int32_t>(n), st_);
+  auto* h = static_cast<std::uint8_t*>(h_init_);
+  for (std::size_t i = 0; i < n; ++i) {
+    auto* r = h + i * rb;
+    SlotInit x{};
+    x.slot = slots[i];
+    x.nb = nbuf ? (*nbuf)[i] : 0;
+    x.stat = stats[i];
+    x.nmem = nmem[i];
+    x.cid = cids[i];
+    x.resid = resid[i];
+    x.lazy = x.nb > 0 ? 1 : 0;
+    x.has_brep = (breps && x.nb > 0) ? 1 : 0;
+    x.rnorm = norm_d(reps[i].data(), d_);
+    x.var = vars[i];
+    x.bnorm = x.has_brep ? norm_d((*breps)[i].data(), d_) : 0.0;
+    std::memcpy(r, &x, sizeof(x));
+    std::memcpy(r + sizeof(SlotInit), reps[i].data(), static_cast<std::size_t>(d_) * 8);
+    if (x.has_brep) std::memcpy(r + sizeof(SlotInit) + static_cast<std::size_t>(d_) * 8, (*breps)[i].data(), static_cast<std::size_t>(d_) * 8);
+  }
+  std::memcpy(h + n * rb, slots.data(), n * 4);
+  KVC_CUDA(cudaMemcpyAsync(d_init_, h_init_, bytes, cudaMemcpyHostToDevice, st_));
+  KVC_CUDA(cudaEventRecord(ev_init_, st_));
+  launches_ += launch_init_slots(t_, d_init_, static_cast<std::int32_t>(n), st_);
+  launches_ += launch_refresh_mirror(
+      t_, reinterpret_cast<const std::int32_t*>(static_cast<std::uint8_t*>(d_init_) + n * rb), static_cast<std::int32_t>(n), st_);
 }
 
-// Appends staged rows idx[run.first .. run.first + run.n) to each run's slot, in order.
 void Context::append_runs_idx(const std::vector<AppendRun>& runs, const std::vector<std::int32_t>& idx,
                               const void* src_k, const void* src_v) {
   if (runs.empty()) return;

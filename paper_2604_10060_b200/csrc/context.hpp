@@ -233,6 +233,7 @@ class Context {
   void* d_init_ = nullptr;
   void* h_init_ = nullptr;
   std::int64_t init_cap_ = 0;
+  cudaEvent_t ev_init_ = nullptr;  // the last slot-init copy out of h_init_
   // ingest buffers
   IngestArgs ia_{};
   std::int32_t *d_active_ = nullptr, *h_active_ = nullptr, *d_cursor_ = nullptr, *h_cursor_ = nullptr;

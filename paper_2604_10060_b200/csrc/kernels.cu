@@ -1181,6 +1181,28 @@ __global__ void k_slot_headers(DevTables t, const SlotHeader* h, int n) {
   t.resid[x.slot] = 0;
 }
 
+__global__ void k_init_slots(DevTables t, const uint8_t* recs, int n) {
+  const uint8_t* r = recs + static_cast<int64_t>(blockIdx.x) * slot_init_bytes(t.d);
+  const SlotInit& x = *reinterpret_cast<const SlotInit*>(r);
+  const double* rep = reinterpret_cast<const double*>(r + sizeof(SlotInit));
+  const int64_t s = x.slot;
+  for (int c = threadIdx.x; c < t.d; c += blockDim.x) {
+    t.rep64[s * t.d + c] = rep[c];
+    if (x.has_brep) t.brep64[s * t.d + c] = rep[t.d + c];
+  }
+  if (threadIdx.x == 0) {
+    t.rnorm[s] = x.rnorm;
+    t.var[s] = x.var;
+    t.stat[s] = x.stat;
+    t.nmem[s] = x.nmem;
+    t.cid[s] = x.cid;
+    t.resid[s] = x.resid;
+    t.nbuf[s] = x.nb;
+    t.lazy[s] = x.lazy;
+    if (x.has_brep) t.bnorm[s] = x.bnorm;
+  }
+}
+
 __global__ void k_to_f32(const void* src, float* dst, int64_t n, int bf16) {
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x)
@@ -2745,6 +2767,12 @@ int launch_exact_stats(const DevTables& t, const AppendRun* runs, int32_t n_runs
 int launch_slot_headers(const DevTables& t, const SlotHeader* h, int32_t n, cudaStream_t st) {
   if (n <= 0) return 0;
   k_slot_headers<<<(n + 127) / 128, 128, 0, st>>>(t, h, n);
+  return 1;
+}
+
+int launch_init_slots(const DevTables& t, const void* recs, int32_t n, cudaStream_t st) {
+  if (n <= 0) return 0;
+  k_init_slots<<<n, 128, 0, st>>>(t, static_cast<const uint8_t*>(recs), n);
   return 1;
 }
 

@@ -311,6 +311,16 @@ struct SlotHeader {
   int64_t cid, n;
 };
 int launch_slot_headers(const DevTables& t, const SlotHeader* h, int32_t n, cudaStream_t st);
+// Exact statistics of host-built slots (split children, seeds, batch build): one packed record
+// per slot, SlotInit followed by rep[d] and brep[d] doubles (slot_init_bytes(d) apart).
+struct SlotInit {
+  int32_t slot, nb;
+  int64_t stat, nmem, cid;
+  uint8_t resid, lazy, has_brep, pad[5];
+  double rnorm, var, bnorm;
+};
+inline __host__ __device__ size_t slot_init_bytes(int d) { return sizeof(SlotInit) + 2 * static_cast<size_t>(d) * 8; }
+int launch_init_slots(const DevTables& t, const void* recs, int32_t n, cudaStream_t st);
 
 // Converts staged kv-dtype rows to fp32 (for host read-back).
 // split.cu: split_two of rows[idx[i]] (i < n), one CTA; scratch n * (2d + 3) doubles; returns 0
