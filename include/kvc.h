@@ -224,6 +224,12 @@ KVC_API int kvc_debug_tier_check(kvc_ctx* ctx, int64_t* out4);
 /* split_two (clustering.cpp:180-208) of n host points (the context's d) through the device split
  * kernel the maintenance slow path uses (split.cu); meta3 = {k_live, iterations, degenerate}.
  * Bit-identical to kvc_host_split_two / kvc_host_kmeans(k=2, 50, 1e-9). Returns k_live or < 0. */
+/* spherical_kmeans (clustering.cpp:80-178) of n_sets host point sets (rows concatenated, the
+ * context's d) through the batch-build device kernel (kmeans_dev.cu), as the index build runs it;
+ * meta2[2i] = k_live, meta2[2i+1] = iterations. Bit-identical to kvc_host_kmeans. */
+KVC_API int kvc_debug_kmeans(kvc_ctx* ctx, const float* pts, int32_t n_sets, const int32_t* n, const int32_t* k,
+                             int32_t max_iters, double tol, const uint64_t* seeds, int32_t* assign, int32_t* meta2,
+                             double* objective);
 KVC_API int kvc_debug_split_two(kvc_ctx* ctx, const float* pts, int32_t n, uint64_t seed, int32_t* assign,
                                 int32_t* meta3, double* objective);
 

@@ -145,6 +145,8 @@ def lib():
         L.kvc_cluster_tier.argtypes = [vp, C.c_int64, i64p]
         L.kvc_debug_tier_check.argtypes = [vp, i64p]
         L.kvc_debug_split_two.argtypes = [vp, f32p, C.c_int32, C.c_uint64, i32p, i32p, f64p]
+        L.kvc_debug_kmeans.argtypes = [vp, f32p, C.c_int32, i32p, i32p, C.c_int32, C.c_double,
+                                       C.POINTER(C.c_uint64), i32p, i32p, f64p]
         L.kvc_exchange_bytes.restype = C.c_size_t
         L.kvc_exchange_bytes.argtypes = [C.c_int32, C.c_int32, C.c_int32]
         L.kvc_ipc_alloc.argtypes = [C.c_size_t, C.POINTER(vp), C.c_void_p]
@@ -183,7 +185,7 @@ EXPORTED = [
     "kvc_launch_count", "kvc_last_step_timing", "kvc_set_timing", "kvc_last_ingest_timing",
     "kvc_debug_resolve_profile", "kvc_host_split_two", "kvc_host_kmeans", "kvc_host_tau",
     "kvc_host_mix_seed", "kvc_debug_div_check", "kvc_debug_assign_check", "kvc_tier_sync",
-    "kvc_tier_stats", "kvc_cluster_tier", "kvc_debug_tier_check", "kvc_debug_split_two", "kvc_exchange_bytes", "kvc_ipc_alloc",
+    "kvc_tier_stats", "kvc_cluster_tier", "kvc_debug_tier_check", "kvc_debug_split_two", "kvc_debug_kmeans", "kvc_exchange_bytes", "kvc_ipc_alloc",
     "kvc_ipc_open", "kvc_ipc_close", "kvc_ipc_free", "kvc_set_peers", "kvc_peer_output",
 ]
 
@@ -442,6 +444,26 @@ class ClusterKVCache:
         _check(lib().kvc_debug_split_two(self.h, _p(pts, f32p), n, seed, _p(assign, i32p), _p(meta, i32p),
                                          _p(obj, f64p)))
         return assign, int(meta[0]), int(meta[1]), bool(meta[2]), float(obj[0])
+
+    def debug_kmeans(self, sets, ks, seeds, max_iters: int = 50, tol: float = 1e-6):
+        """spherical_kmeans of several point sets [n_i, d] in one batch-build launch
+        (kmeans_dev.cu): [(assign, k_live, iterations, objective)] per set."""
+        sets = [np.ascontiguousarray(x, np.float32) for x in sets]
+        pts = np.ascontiguousarray(np.concatenate(sets, 0))
+        n = np.array([x.shape[0] for x in sets], np.int32)
+        k = np.array(ks, np.int32)
+        sd = np.array(seeds, np.uint64)
+        assign = np.zeros(int(n.sum()), np.int32)
+        meta = np.zeros(2 * len(sets), np.int32)
+        obj = np.zeros(len(sets), np.float64)
+        _check(lib().kvc_debug_kmeans(self.h, _p(pts, f32p), len(sets), _p(n, i32p), _p(k, i32p), max_iters, tol,
+                                      sd.ctypes.data_as(C.POINTER(C.c_uint64)), _p(assign, i32p), _p(meta, i32p),
+                                      _p(obj, f64p)))
+        out, o = [], 0
+        for i, x in enumerate(sets):
+            out.append((assign[o:o + len(x)].copy(), int(meta[2 * i]), int(meta[2 * i + 1]), float(obj[i])))
+            o += len(x)
+        return out
 
     # ------------------------------------------------------------------ fused output exchange
     def set_peers(self, n_ranks: int, rank: int, dom_offset: int, total_domains: int, bufs):

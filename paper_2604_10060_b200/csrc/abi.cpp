@@ -469,6 +469,35 @@ int kvc_debug_split_two(kvc_ctx* ctx, const float* pts, int32_t n, uint64_t seed
   return rc != KVC_OK ? rc : live;
 }
 
+int kvc_debug_kmeans(kvc_ctx* ctx, const float* pts, int32_t n_sets, const int32_t* n, const int32_t* k,
+                     int32_t max_iters, double tol, const uint64_t* seeds, int32_t* assign, int32_t* meta2,
+                     double* objective) {
+  int rc = guard([&] {
+    std::vector<const float*> ptr;
+    std::vector<int> nn, kk;
+    std::vector<std::uint64_t> ss;
+    std::size_t off = 0;
+    const int d = F(ctx).d();
+    for (int i = 0; i < n_sets; ++i) {
+      ptr.push_back(pts + off * d);
+      nn.push_back(n[i]);
+      kk.push_back(k[i]);
+      ss.push_back(seeds[i]);
+      off += static_cast<std::size_t>(n[i]);
+    }
+    const std::vector<kvc::KMeansOut> o = F(ctx).kmeans_pools(ptr, nn, kk, ss, max_iters, tol);
+    off = 0;
+    for (int i = 0; i < n_sets; ++i) {
+      for (int t = 0; t < n[i]; ++t) assign[off + t] = o[static_cast<std::size_t>(i)].assign[static_cast<std::size_t>(t)];
+      off += static_cast<std::size_t>(n[i]);
+      meta2[2 * i] = o[static_cast<std::size_t>(i)].k_live;
+      meta2[2 * i + 1] = o[static_cast<std::size_t>(i)].iterations;
+      objective[i] = o[static_cast<std::size_t>(i)].objective;
+    }
+  });
+  return rc;
+}
+
 int kvc_cluster_tier(kvc_ctx* ctx, int64_t id, int64_t* out) {
   return guard([&] { F(ctx).cluster_tier(id, out); });
 }

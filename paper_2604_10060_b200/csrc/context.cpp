@@ -1506,6 +1506,125 @@ std::vector<std::int64_t> Context::materialize(std::int64_t id) {  // maintainer
 
 // ============================================================================ build
 
+// Batch spherical k-means of host point sets on the GPU (the index build's per-(partition, layer)
+// pools, index.cpp:405-425): one CTA per set, all sets of a chunk in one launch.
+std::vector<KMeansOut> Context::kmeans_pools(const std::vector<const float*>& pts, const std::vector<int>& n,
+                                             const std::vector<int>& k_req, const std::vector<std::uint64_t>& seeds,
+                                             int max_iters, double tol, bool stats) {
+  const std::size_t np = pts.size();
+  std::vector<KMeansOut> out(np);
+  const bool host_only = std::getenv("KVC_BUILD_HOST") != nullptr;  // ablation: host k-means
+  std::vector<std::size_t> dev;
+  for (std::size_t i = 0; i < np; ++i) {
+    const int k = std::max(1, std::min(k_req[i], n[i]));
+    if (!host_only && n[i] >= 1 && kmeans_smem_bytes(k, d_) <= 200 * 1024)
+      dev.push_back(i);
+    else
+      out[i] = spherical_kmeans(pts[i], n[i], d_, k_req[i], max_iters, tol, seeds[i]);
+  }
+  const std::size_t budget = std::size_t{3} << 30;  // scratch bytes per launch
+  for (std::size_t b = 0; b < dev.size();) {
+    std::size_t e = b, rows = 0, scr = 0, unis = 0;
+    int kmax = 1;
+    while (e < dev.size()) {
+      const std::size_t i = dev[e];
+      const std::size_t s = kmeans_scratch_doubles(n[i], d_) * 8;
+      if (e > b && scr + s > budget) break;
+      const int k = std::max(1, std::min(k_req[i], n[i]));
+      rows += static_cast<std::size_t>(n[i]);
+      scr += s;
+      unis += static_cast<std::size_t>(k);
+      kmax = std::max(kmax, k);
+      ++e;
+    }
+    const std::size_t nj = e - b;
+    // device: rows f32 | uniforms | jobs | assign (padded) | meta[4] | objective | reps | vars | scratch
+    std::size_t kd = 0, ksum = 0;
+    for (std::size_t q = 0; q < nj; ++q) {
+      const std::size_t i = dev[b + q];
+      const std::size_t k = static_cast<std::size_t>(std::max(1, std::min(k_req[i], n[i])));
+      ksum += k;
+      kd += k * d_;
+    }
+    const std::size_t rows_pad = (rows + 1) & ~std::size_t{1};
+    const std::size_t rows_b = rows * d_ * 4, uni_b = unis * 8, job_b = nj * sizeof(KmJob);
+    const std::size_t out_b = rows_pad * 4 + nj * 16 + nj * 8 + (stats ? (kd + ksum) * 8 : 0);
+    const std::size_t in_b = rows_b + uni_b + job_b;
+    void* dp = nullptr;
+    struct Free {
+      void*& d;
+      ~Free() {
+        if (d) cudaFree(d);
+      }
+    } guard{dp};
+    KVC_CUDA(cudaMalloc(&dp, in_b + out_b + scr));
+    auto* d8 = static_cast<std::uint8_t*>(dp);
+    std::vector<double> huni(unis);
+    std::vector<KmJob> hjob(nj);
+    std::size_t r0 = 0, s0 = 0, u0 = 0, k0 = 0;
+    for (std::size_t q = 0; q < nj; ++q) {
+      const std::size_t i = dev[b + q];
+      const int k = std::max(1, std::min(k_req[i], n[i]));
+      KVC_CUDA(cudaMemcpyAsync(d8 + r0 * d_ * 4, pts[i], static_cast<std::size_t>(n[i]) * d_ * 4,
+                               cudaMemcpyHostToDevice, st_));
+      Rng64 rng(seeds[i]);  // plus_plus's draws in order: the first index, then one uniform per pick
+      KmJob j{};
+      j.row0 = static_cast<std::int64_t>(r0);
+      j.scratch0 = static_cast<std::int64_t>(s0);
+      j.rep0 = stats ? static_cast<std::int64_t>(k0 * d_) : -1;
+      j.var0 = static_cast<std::int32_t>(k0);
+      j.n = n[i];
+      j.k = k;
+      j.first = static_cast<std::int32_t>(rng.index(static_cast<std::size_t>(n[i])));
+      j.out0 = static_cast<std::int32_t>(r0);
+      j.uni0 = static_cast<std::int32_t>(u0);
+      for (int t = 0; t + 1 < k; ++t) huni[u0 + t] = rng.uniform();
+      hjob[q] = j;
+      r0 += static_cast<std::size_t>(n[i]);
+      s0 += kmeans_scratch_doubles(n[i], d_);
+      u0 += static_cast<std::size_t>(k);
+      k0 += static_cast<std::size_t>(k);
+    }
+    KVC_CUDA(cudaMemcpyAsync(d8 + rows_b, huni.data(), uni_b, cudaMemcpyHostToDevice, st_));
+    KVC_CUDA(cudaMemcpyAsync(d8 + rows_b + uni_b, hjob.data(), job_b, cudaMemcpyHostToDevice, st_));
+    auto* d_assign = reinterpret_cast<std::int32_t*>(d8 + in_b);
+    auto* d_meta = d_assign + rows_pad;
+    auto* d_obj = reinterpret_cast<double*>(d_meta + nj * 4);
+    auto* d_reps = d_obj + nj;
+    auto* d_vars = d_reps + kd;
+    auto* d_scr = reinterpret_cast<double*>(d8 + in_b + out_b);
+    KVC_CUDA(cudaMemsetAsync(d_meta, 0, nj * 16, st_));
+    launches_ += launch_kmeans(reinterpret_cast<const float*>(d8), reinterpret_cast<const KmJob*>(d8 + rows_b + uni_b),
+                               static_cast<int>(nj), reinterpret_cast<const double*>(d8 + rows_b), d_scr, d_assign,
+                               d_meta, d_obj, d_reps, d_vars, d_, kmax, max_iters, tol, st_);
+    KVC_CUDA(cudaGetLastError());
+    std::vector<std::uint8_t> hout(out_b);
+    KVC_CUDA(cudaMemcpyAsync(hout.data(), d_assign, out_b, cudaMemcpyDeviceToHost, st_));
+    sync();
+    const auto* ha = reinterpret_cast<const std::int32_t*>(hout.data());
+    const auto* hm = ha + rows_pad;
+    const auto* ho = reinterpret_cast<const double*>(hm + nj * 4);
+    const double* hr = ho + nj;
+    const double* hv = hr + kd;
+    for (std::size_t q = 0; q < nj; ++q) {
+      const std::size_t i = dev[b + q];
+      if (hm[q * 4 + 3] != 0) fail(-2, "normalize of zero vector");
+      KMeansOut& o = out[i];
+      const KmJob& j = hjob[q];
+      o.assign.assign(ha + j.out0, ha + j.out0 + n[i]);
+      o.k_live = hm[q * 4 + 0];
+      o.iterations = hm[q * 4 + 1];
+      o.objective = ho[q];
+      if (stats) {
+        o.reps.assign(hr + j.rep0, hr + j.rep0 + static_cast<std::size_t>(o.k_live) * d_);
+        o.vars.assign(hv + j.var0, hv + j.var0 + o.k_live);
+      }
+    }
+    b = e;
+  }
+  return out;
+}
+
 void Context::build_now() {  // engine.cpp:77-93 + build_index (index.cpp:364-450)
   if (built_) return;
   if (pending_.empty()) fail(-9, "no frames available to build from");
@@ -1537,21 +1656,64 @@ void Context::build_now() {  // engine.cpp:77-93 + build_index (index.cpp:364-45
     upload_partition(static_cast<std::int64_t>(parts_.size()) - 1);
   }
   const std::size_t rb = static_cast<std::size_t>(d_) * es_;
-  for (std::size_t p = 0; p < pf.size(); ++p) {
+  // every (partition, layer) pool's semantic k-means at once on the GPU (index.cpp:405-425)
+  std::vector<std::vector<float>> pool_keys;
+  std::vector<const float*> pool_ptr;
+  std::vector<int> pool_n, pool_k;
+  std::vector<std::uint64_t> pool_seed;
+  for (std::size_t p = 0; p < pf.size(); ++p)
     for (int layer = 0; layer < L_; ++layer) {
-      // pool = frames of the partition in order, tokens in order (index.cpp:405-409)
-      std::vector<Member> ids;
       std::int64_t rows = 0;
       for (int fi : pf[p]) rows += pending_[static_cast<std::size_t>(fi)].T;
-      if (rows == 0) continue;
-      ensure_stage(rows + 1);
       std::vector<float> keys(static_cast<std::size_t>(rows) * d_);
-      std::vector<std::uint8_t> kraw(static_cast<std::size_t>(rows) * rb), vraw(static_cast<std::size_t>(rows) * rb);
       std::int64_t r = 0;
       for (int fi : pf[p]) {
         const PendingFrame& f = pending_[static_cast<std::size_t>(fi)];
         const std::size_t base = static_cast<std::size_t>(layer) * f.T;
         std::memcpy(&keys[static_cast<std::size_t>(r) * d_], &f.keys_f32[base * d_], static_cast<std::size_t>(f.T) * d_ * 4);
+        r += f.T;
+      }
+      pool_n.push_back(static_cast<int>(rows));
+      pool_k.push_back(static_cast<int>((rows + cfg_.target_semantic_cluster_size - 1) / cfg_.target_semantic_cluster_size));
+      pool_seed.push_back(mix_seed(bseed, (static_cast<std::uint64_t>(p) << 8) | static_cast<std::uint64_t>(layer) | 0x100u));
+      pool_keys.push_back(std::move(keys));
+      pool_ptr.push_back(pool_keys.back().data());
+    }
+  const auto bt0 = std::chrono::steady_clock::now();
+  std::vector<KMeansOut> pool_km;
+  {
+    std::vector<const float*> ptr;
+    std::vector<int> nn, kk;
+    std::vector<std::uint64_t> ss;
+    std::vector<std::size_t> which;
+    for (std::size_t i = 0; i < pool_n.size(); ++i)
+      if (pool_n[i] > 0) {
+        ptr.push_back(pool_keys[i].data());
+        nn.push_back(pool_n[i]);
+        kk.push_back(pool_k[i]);
+        ss.push_back(pool_seed[i]);
+        which.push_back(i);
+      }
+    std::vector<KMeansOut> r = kmeans_pools(ptr, nn, kk, ss, cfg_.kmeans_max_iters, cfg_.kmeans_tol, true);
+    pool_km.resize(pool_n.size());
+    for (std::size_t q = 0; q < which.size(); ++q) pool_km[which[q]] = std::move(r[q]);
+  }
+  const auto bt1 = std::chrono::steady_clock::now();
+  double t_repvar = 0.0, t_dev = 0.0;
+  for (std::size_t p = 0; p < pf.size(); ++p) {
+    for (int layer = 0; layer < L_; ++layer) {
+      // pool = frames of the partition in order, tokens in order (index.cpp:405-409)
+      const std::size_t pool = p * static_cast<std::size_t>(L_) + static_cast<std::size_t>(layer);
+      std::vector<Member> ids;
+      const std::int64_t rows = pool_n[pool];
+      if (rows == 0) continue;
+      ensure_stage(rows + 1);
+      const std::vector<float>& keys = pool_keys[pool];
+      std::vector<std::uint8_t> kraw(static_cast<std::size_t>(rows) * rb), vraw(static_cast<std::size_t>(rows) * rb);
+      std::int64_t r = 0;
+      for (int fi : pf[p]) {
+        const PendingFrame& f = pending_[static_cast<std::size_t>(fi)];
+        const std::size_t base = static_cast<std::size_t>(layer) * f.T;
         std::memcpy(&kraw[static_cast<std::size_t>(r) * rb], &f.keys_raw[base * rb], static_cast<std::size_t>(f.T) * rb);
         std::memcpy(&vraw[static_cast<std::size_t>(r) * rb], &f.vals_raw[base * rb], static_cast<std::size_t>(f.T) * rb);
         for (int t = 0; t < f.T; ++t) ids.push_back({f.frame_id, t});
@@ -1559,9 +1721,7 @@ void Context::build_now() {  // engine.cpp:77-93 + build_index (index.cpp:364-45
       }
       KVC_CUDA(cudaMemcpyAsync(d_stage_k_, kraw.data(), kraw.size(), cudaMemcpyHostToDevice, st_));
       KVC_CUDA(cudaMemcpyAsync(d_stage_v_, vraw.data(), vraw.size(), cudaMemcpyHostToDevice, st_));
-      const int ks = static_cast<int>((rows + cfg_.target_semantic_cluster_size - 1) / cfg_.target_semantic_cluster_size);
-      const std::uint64_t sseed = mix_seed(bseed, (static_cast<std::uint64_t>(p) << 8) | static_cast<std::uint64_t>(layer) | 0x100u);
-      const KMeansOut sk = spherical_kmeans(keys.data(), static_cast<int>(rows), d_, ks, cfg_.kmeans_max_iters, cfg_.kmeans_tol, sseed);
+      const KMeansOut& sk = pool_km[pool];
       std::vector<std::vector<int>> groups(static_cast<std::size_t>(sk.k_live));
       for (std::int64_t i = 0; i < rows; ++i) groups[static_cast<std::size_t>(sk.assign[static_cast<std::size_t>(i)])].push_back(static_cast<int>(i));
       std::vector<std::int32_t> slots;
@@ -1572,9 +1732,18 @@ void Context::build_now() {  // engine.cpp:77-93 + build_index (index.cpp:364-45
       std::vector<AppendRun> runs;
       std::vector<std::int32_t> idx;
       for (auto& g : groups) {
+        const auto rv0 = std::chrono::steady_clock::now();
+        const std::size_t gi = static_cast<std::size_t>(&g - groups.data());
         std::vector<double> rep(static_cast<std::size_t>(d_));
-        representative(keys.data(), g.data(), static_cast<int>(g.size()), d_, rep.data());
-        const double var = variance(keys.data(), g.data(), static_cast<int>(g.size()), d_, rep.data());
+        double var;
+        if (!sk.vars.empty()) {  // computed by the device build with the k-means
+          std::copy_n(&sk.reps[gi * d_], d_, rep.begin());
+          var = sk.vars[gi];
+        } else {
+          representative(keys.data(), g.data(), static_cast<int>(g.size()), d_, rep.data());
+          var = variance(keys.data(), g.data(), static_cast<int>(g.size()), d_, rep.data());
+        }
+        t_repvar += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - rv0).count();
         std::vector<Member> m;
         for (int i : g) m.push_back(ids[static_cast<std::size_t>(i)]);
         const std::int64_t id = new_cluster(layer, static_cast<std::int64_t>(p), std::move(m), false);
@@ -1589,14 +1758,22 @@ void Context::build_now() {  // engine.cpp:77-93 + build_index (index.cpp:364-45
         runs.push_back({c.slot, static_cast<std::int32_t>(idx.size()), static_cast<std::int32_t>(g.size()), 0});
         idx.insert(idx.end(), g.begin(), g.end());
       }
+      const auto dv0 = std::chrono::steady_clock::now();
       init_slots(slots, reps, vars, stats, nmem, cids, res, nullptr, nullptr);
       append_runs_idx(runs, idx);
       pl_upload(static_cast<std::int64_t>(p), layer);
+      t_dev += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - dv0).count();
     }
   }
+  const auto bt2 = std::chrono::steady_clock::now();
+  if (std::getenv("KVC_BUILD_TIMING"))
+    std::fprintf(stderr, "build: kmeans %.1f ms, pools %.1f ms (rep/var %.1f, device %.1f)\n",
+                 std::chrono::duration<double, std::milli>(bt1 - bt0).count(),
+                 std::chrono::duration<double, std::milli>(bt2 - bt1).count(), t_repvar, t_dev);
   // TieredStore(index, cost) adopts every cluster in id order (store.cpp:67-74)
   for (std::int64_t id : cluster_ids()) adopt(id);
   built_ = true;
+  const auto bt3 = std::chrono::steady_clock::now();
   const std::int64_t last = pending_.back().frame_id;
   pending_.clear();
   // ring owners of the window frames
@@ -1608,6 +1785,10 @@ void Context::build_now() {  // engine.cpp:77-93 + build_index (index.cpp:364-45
   repin();
   apply_cadence(last, -1);
   tier_kick();
+  if (std::getenv("KVC_BUILD_TIMING"))
+    std::fprintf(stderr, "build: adopt %.1f ms, ring/repin/cadence %.1f ms\n",
+                 std::chrono::duration<double, std::milli>(bt3 - bt2).count(),
+                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - bt3).count());
   if (cfg_.check_invariants) check();
 }
 

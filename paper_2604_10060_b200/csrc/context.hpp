@@ -435,6 +435,11 @@ class Context {
   // split_two (kmeans.cpp) of staged rows grp[] on the GPU (split.cu), bit-identical to the host
   // restatement; falls back to it for groups below split_dev_min_ rows or d > 256.
   KMeansOut split_two_staged(const std::vector<int>& grp, std::uint64_t seed);
+  // spherical_kmeans (kmeans.cpp) of several host point sets at once on the GPU (kmeans_dev.cu),
+  // bit-identical to the host restatement; sets that do not fit a CTA run on the host.
+  std::vector<KMeansOut> kmeans_pools(const std::vector<const float*>& pts, const std::vector<int>& n,
+                                      const std::vector<int>& k_req, const std::vector<std::uint64_t>& seeds,
+                                      int max_iters, double tol, bool stats = false);
   // debug: split_two of host points through the device path (stages them first)
   KMeansOut debug_split_two_dev(const float* pts, int n, std::uint64_t seed);
 

@@ -45,6 +45,9 @@ struct KMeansOut {
   double objective = 0.0;
   int iterations = 0;
   bool degenerate = false;
+  // (device batch build only) Eq. 1 representative [k_live][d] and Eq. 2 variance [k_live] of
+  // each output cluster, computed exactly as representative() / variance() below
+  std::vector<double> reps, vars;
 };
 
 KMeansOut spherical_kmeans(const float* pts, int n, int d, int k, int max_iters, double tol,

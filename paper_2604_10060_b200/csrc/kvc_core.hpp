@@ -321,6 +321,17 @@ struct SlotInit {
 };
 inline __host__ __device__ size_t slot_init_bytes(int d) { return sizeof(SlotInit) + 2 * static_cast<size_t>(d) * 8; }
 int launch_init_slots(const DevTables& t, const void* recs, int32_t n, cudaStream_t st);
+// kmeans_dev.cu: batch spherical k-means, one CTA per pool (rows [row0, row0 + n) of `rows`,
+// final k = max(1, min(k_req, n)), the host's draws: first index + k - 1 uniforms at uni0).
+struct KmJob {
+  int64_t row0, scratch0, rep0;  // rep0: k x d doubles of Eq. 1 representatives (-1: not wanted)
+  int32_t n, k, first, out0, uni0, var0;  // var0: k doubles of Eq. 2 variances
+};
+size_t kmeans_smem_bytes(int k, int d);
+size_t kmeans_scratch_doubles(int n, int d);
+int launch_kmeans(const float* rows, const KmJob* jobs, int n_jobs, const double* uniforms, double* scratch,
+                  int32_t* assign, int32_t* meta, double* objective, double* reps, double* vars, int d, int k_max,
+                  int max_iters, double tol, cudaStream_t st);
 
 // Converts staged kv-dtype rows to fp32 (for host read-back).
 // split.cu: split_two of rows[idx[i]] (i < n), one CTA; scratch n * (2d + 3) doubles; returns 0
