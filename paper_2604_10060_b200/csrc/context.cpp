@@ -913,7 +913,18 @@ void Context::finish_frame(std::int64_t* assigned) {
   tier_kick();
 }
 
+// Replays the frame held in pong_ (its kernels are complete and it had no host events).
+void Context::finish_pong() {
+  if (!pong_.active) return;
+  const PendingIngest keep = ping_;
+  ping_ = pong_;
+  pong_.active = false;
+  finish_frame(nullptr);
+  ping_ = keep;
+}
+
 void Context::flush_ingest() {
+  finish_pong();
   if (!ping_.active) return;
   KVC_CUDA(cudaEventSynchronize(ping_.ev));
   finish_frame(nullptr);
@@ -942,10 +953,18 @@ void Context::ingest_frame(std::int64_t frame_id, const float* visual, const voi
     const std::size_t pitch = static_cast<std::size_t>(t_.tmax) * d_ * es_;
     const cudaMemcpyKind kind = mem == KVC_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
     KVC_CUDA(cudaStreamWaitEvent(in_st_, ev_buf_[b], 0));
-    KVC_CUDA(cudaMemcpy2DAsync(fkbuf_[b], pitch, keys, row, row, L_, kind, in_st_));
-    KVC_CUDA(cudaMemcpy2DAsync(fvbuf_[b], pitch, values, row, row, L_, kind, in_st_));
+    if (pitch == row) {  // frames of max_tokens tokens: one linear copy each
+      KVC_CUDA(cudaMemcpyAsync(fkbuf_[b], keys, row * L_, kind, in_st_));
+      KVC_CUDA(cudaMemcpyAsync(fvbuf_[b], values, row * L_, kind, in_st_));
+    } else {
+      KVC_CUDA(cudaMemcpy2DAsync(fkbuf_[b], pitch, keys, row, row, L_, kind, in_st_));
+      KVC_CUDA(cudaMemcpy2DAsync(fvbuf_[b], pitch, values, row, row, L_, kind, in_st_));
+    }
     KVC_CUDA(cudaEventRecord(ev_in_[b], in_st_));
   }
+  // the frame before the previous one is replayed now, after this frame's payload copy was queued
+  // (so the copies run back to back while the host replays)
+  finish_pong();
   if (ping_.active) {
     KVC_CUDA(cudaEventSynchronize(ping_.ev));
     bool events = false;
@@ -1022,10 +1041,9 @@ void Context::ingest_frame(std::int64_t frame_id, const float* visual, const voi
   next.buf = b;
   next.ev = ev_ing_[b];
   KVC_CUDA(cudaEventRecord(next.ev, st_));
-  if (ping_.active) {  // the previous frame (no host events): its replay overlaps this frame's kernels
-    finish_frame(nullptr);
-    select_frame_buffer(b);
-  }
+  // the previous frame (no host events, kernels complete) is replayed at the start of the next
+  // call (or by any reader of host state: flush_ingest), overlapping this frame's kernels
+  if (ping_.active) pong_ = ping_;
   ping_ = next;
 }
 

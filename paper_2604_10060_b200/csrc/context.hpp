@@ -251,7 +251,9 @@ class Context {
     int T = 0, ring_slot = 0, buf = 0;
     cudaEvent_t ev = nullptr;  // outcome block of the first launch on the host
   };
-  PendingIngest ping_;
+  PendingIngest ping_;  // launched, outcome not yet inspected
+  PendingIngest pong_;  // the frame before: kernels complete, no host events, replay pending
+  void finish_pong();
   cudaEvent_t ev_ing_[2] = {nullptr, nullptr};  // per frame buffer: its outcome block reached the host
   cudaEvent_t ev_in_[2] = {nullptr, nullptr};   // per frame buffer: payload copied in (input stream)
   cudaEvent_t ev_buf_[2] = {nullptr, nullptr};  // per frame buffer: last reader on the compute stream done
