@@ -8,6 +8,7 @@
 // the split slow path or through debug accessors.
 #pragma once
 
+#include <array>
 #include <climits>
 #include <cstdint>
 #include <cstddef>
@@ -251,6 +252,7 @@ class Context {
     int T = 0, ring_slot = 0, buf = 0;
     cudaEvent_t ev = nullptr;  // outcome block of the first launch on the host
   };
+  const void* mapped_host(const void* p);
   PendingIngest ping_;  // launched, outcome not yet inspected
   PendingIngest pong_;  // the frame before: kernels complete, no host events, replay pending
   void finish_pong();

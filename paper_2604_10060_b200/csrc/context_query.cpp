@@ -41,17 +41,40 @@ std::uint64_t fnv1a(std::uint64_t h, std::uint64_t x) {  // engine.cpp:18-24
 // bookkeeping of step i-1 changes only when it settles a pending split (the K4 flag): then step i
 // is relaunched after the settle. Host outputs, parity / check / recall modes and per-step timing
 // complete the step before returning.
+// Device address of pinned (page-locked, mapped) host memory, or nullptr for pageable memory.
+// Asked every step (a buffer may be freed and its address reused by pageable memory).
+const void* Context::mapped_host(const void* p) {
+  if (!p) return nullptr;
+  static const bool off = std::getenv("KVC_NO_ZERO_COPY") != nullptr;
+  if (off) return nullptr;
+  cudaPointerAttributes at{};
+  const void* dp = nullptr;
+  if (cudaPointerGetAttributes(&at, p) == cudaSuccess && at.type == cudaMemoryTypeHost && at.devicePointer)
+    dp = at.devicePointer;
+  cudaGetLastError();  // (pageable pointers are not an error worth keeping)
+  return dp;
+}
+
 void Context::launch_step(int b, const float* q, int q_mem, float* out, int out_mem) {
   if (blk_used_[b]) KVC_CUDA(cudaStreamWaitEvent(st_, ev_step_[b], 0));  // block b's last copy done
   blk_used_[b] = true;
   set_result_block(b);
+  // Host query / output in pinned memory are used in place (zero-copy): K4 reads the query over
+  // the link and leaves the device copy for K6, K6's combine writes the rows to the host; no
+  // separate copies (and their launch latencies) on the critical path of an end-to-end step.
   const float* dq = q;
-  if (q_mem != KVC_MEM_DEVICE) {
+  da_.q_src = nullptr;
+  const float* q_map = q_mem != KVC_MEM_DEVICE ? static_cast<const float*>(mapped_host(q)) : nullptr;
+  float* out_map = (out && out_mem != KVC_MEM_DEVICE) ? static_cast<float*>(const_cast<void*>(mapped_host(out))) : nullptr;
+  if (q_map) {
+    da_.q_src = q_map;
+    dq = d_q_;
+  } else if (q_mem != KVC_MEM_DEVICE) {
     KVC_CUDA(cudaMemcpyAsync(d_q_, q, static_cast<std::size_t>(L_) * d_ * 4, cudaMemcpyHostToDevice, st_));
     dq = d_q_;
   }
   da_.q = dq;
-  da_.out = (out && out_mem == KVC_MEM_DEVICE) ? out : d_out_;
+  da_.out = (out && out_mem == KVC_MEM_DEVICE) ? out : (out_map ? out_map : d_out_);
   da_.n_parts_host = static_cast<std::int32_t>(parts_.size());
   launches_ += launch_decode(t_, da_, st_, timing_ ? evb_[b] : nullptr, ev_k4_[b]);
   KVC_CUDA(cudaGetLastError());  // launch-configuration failures surface here, not as empty results
@@ -59,7 +82,7 @@ void Context::launch_step(int b, const float* q, int q_mem, float* out, int out_
   KVC_CUDA(cudaStreamWaitEvent(cs_, ev_k4_[b], 0));
   KVC_CUDA(cudaMemcpyAsync(h_blk_[b], d_blk_[b], dec_bytes_, cudaMemcpyDeviceToHost, cs_));
   KVC_CUDA(cudaEventRecord(ev_step_[b], cs_));
-  if (out && out_mem != KVC_MEM_DEVICE)
+  if (out && out_mem != KVC_MEM_DEVICE && !out_map)
     KVC_CUDA(cudaMemcpyAsync(out, d_out_, static_cast<std::size_t>(L_) * d_ * 4, cudaMemcpyDeviceToHost, st_));
   KVC_CUDA(cudaEventRecord(ev_out_[b], st_));
   step_timed_[b] = timing_;

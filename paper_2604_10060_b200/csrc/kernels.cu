@@ -1414,10 +1414,12 @@ __global__ void __launch_bounds__(256) k_score_select(DevTables t, DecodeArgs a,
   long long kc0 = clock64();
 #define K4MARK(k) if (a.k4prof && threadIdx.x == 0) { const long long kc1 = clock64(); a.k4prof[l * 16 + (k)] = kc1 - kc0; kc0 = kc1; }
   if (l == 0 && threadIdx.x == 0) *work_ctr = 0;
-  const float* q = a.q + static_cast<int64_t>(l) * d;
+  const float* q = (a.q_src ? a.q_src : a.q) + static_cast<int64_t>(l) * d;
   for (int i = threadIdx.x; i < d; i += blockDim.x) {
-    qd[i] = static_cast<double>(q[i]);
-    qf32[i] = q[i];
+    const float x = q[i];
+    if (a.q_src) const_cast<float*>(a.q)[static_cast<int64_t>(l) * d + i] = x;
+    qd[i] = static_cast<double>(x);
+    qf32[i] = x;
   }
   // the window ring owners are needed after ranking; fetch them now
   {
@@ -1870,10 +1872,11 @@ __global__ void __launch_bounds__(K4T) k_score_select2(DevTables t, DecodeArgs a
   long long kc0 = clock64();
 #define K4MARK(k) if (a.k4prof && tid == 0) { const long long kc1 = clock64(); a.k4prof[l * 16 + (k)] = kc1 - kc0; kc0 = kc1; }
   if (l == 0 && tid == 0) *work_ctr = 0;
-  const float* q = a.q + static_cast<int64_t>(l) * d;
+  const float* q = (a.q_src ? a.q_src : a.q) + static_cast<int64_t>(l) * d;
   float qsq = 0.f;
   for (int i = tid; i < d; i += K4T) {
     const float x = q[i];
+    if (a.q_src) const_cast<float*>(a.q)[static_cast<int64_t>(l) * d + i] = x;
     qd[i] = static_cast<double>(x);
     qf[i] = x;
     qsq += x * x;

@@ -174,7 +174,9 @@ struct PeerOut {
 };
 
 struct DecodeArgs {
-  const float* q;          // [L][d]
+  const float* q;          // [L][d] (device)
+  const float* q_src;      // non-null: the query lives in pinned host memory; K4 reads it from
+                           // there (zero-copy) and writes the device copy q for K6
   int32_t k_v, k_s, prefetch_k, prefetch;
   int32_t n_parts_host;    // partitions known to the host (== device count)
   // outputs (device)

@@ -127,10 +127,11 @@ __global__ void __launch_bounds__(K5T) k_select3(DevTables t, DecodeArgs a, int*
   if (l == 0 && tid == 0) *work_ctr = 0;
 
   // ------------------------------------------------------------------ R1
-  const float* q = a.q + static_cast<int64_t>(l) * d;
+  const float* q = (a.q_src ? a.q_src : a.q) + static_cast<int64_t>(l) * d;
   float qx = 0.f;
   if (tid < d) {
     qx = q[tid];
+    if (a.q_src) const_cast<float*>(a.q)[static_cast<int64_t>(l) * d + tid] = qx;
     qd[tid] = static_cast<double>(qx);
     qf[tid] = qx;
   }

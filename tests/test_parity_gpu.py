@@ -207,3 +207,34 @@ def test_async_decode_pipeline_matches_sync():
     st = kv_a.maint_stats()
     print("deferred marks", st[3], "settled splits", st[4])
     assert st[3] > 0 and st[4] > 0  # deferred splits were settled on the async path
+
+
+def test_pinned_host_buffers_zero_copy(stream1):
+    """A query and output in pinned host memory are used in place (K4 reads the query over the
+    link, K6 writes the rows to the host): outputs equal the pageable (copied) path bitwise, and
+    the pinned output is complete when query() returns."""
+    import torch
+
+    from paper_2604_10060_b200 import ClusterKVCache
+    from tests.harness import product_config
+
+    s = stream1
+    ecfg = po.config1_engine()
+    kv_p = ClusterKVCache(product_config(ecfg, parity_mode=0, check_invariants=0), s.d, s.L)
+    kv_c = ClusterKVCache(product_config(ecfg, parity_mode=0, check_invariants=0), s.d, s.L)
+    q_pin = torch.zeros(s.L, s.d).pin_memory()
+    o_pin = torch.zeros(s.L, s.d).pin_memory()
+    n = 0
+    for kind, i in s.events():
+        if kind == "frame":
+            kv_p.process_frame(i, s.visual[i], s.keys[i], s.values[i])
+            kv_c.process_frame(i, s.visual[i], s.keys[i], s.values[i])
+            continue
+        q_pin.copy_(torch.from_numpy(np.ascontiguousarray(s.q[i], np.float32)))
+        o_pin.fill_(float("nan"))
+        kv_p.query(i, q_pin.numpy(), out=o_pin.numpy())
+        ref = kv_c.query(i, np.ascontiguousarray(s.q[i], np.float32).copy())
+        assert np.array_equal(o_pin.numpy(), ref), i
+        assert kv_p.digest() == kv_c.digest()
+        n += 1
+    assert n > 0
