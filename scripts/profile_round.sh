@@ -23,3 +23,11 @@ ls -la "$OUT"
 # token-level baseline kernels (config-5 shape, one stream)
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"k_tok_(approx|select|gather)|k_attend" -c 40 --csv \
   --log-file "$OUT/launches_token.csv" python scripts/kernel_times.py token 3 > "$OUT/ncu_launch_token.log" 2>&1
+# maintenance / build slow paths on the GPU: split k-means, drift ingest, batch build
+timeout 600 python scripts/split_time.py > "$OUT/split_time.txt" 2>&1
+timeout 900 python scripts/drift_ingest.py 0.05 10 16 > "$OUT/drift_ingest.json" 2> "$OUT/drift_ingest.err"
+KVC_BUILD_TIMING=1 BUILD_HOST_TOO=1 timeout 900 python scripts/build_time.py 16 32 > "$OUT/build_time.txt" 2>&1
+KVC_BUILD_TIMING=1 timeout 900 python scripts/build_time.py 112 32 >> "$OUT/build_time.txt" 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_kmeans" -c 1 -o "$OUT/full_kmeans" \
+  python scripts/build_time.py 16 32 > "$OUT/ncu_full_kmeans.log" 2>&1
+ls -la "$OUT"

@@ -1,3 +1,11 @@
+"""GPU split_two (split.cu) vs the host restatement, d = 128 (development measurement).
+
+    python scripts/split_time.py
+"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import time, numpy as np
 from oracle import pyoracle as po
 from paper_2604_10060_b200 import api, ClusterKVCache

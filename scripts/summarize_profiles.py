@@ -99,7 +99,8 @@ lines += ["", "## `ncu --set full` captures", "",
           "| kernel | duration us | DRAM read MB | DRAM write MB | DRAM % peak | SM % | achieved occupancy | regs |",
           "|---|---|---|---|---|---|---|---|"]
 att = {}
-for kname in ("k_attend", "k_select3", "k_score_select2", "k_resolve_spec", "k_assign_tc", "k_approx", "k_topm"):
+for kname in ("k_attend", "k_select3", "k_score_select2", "k_resolve_spec", "k_assign_tc", "k_approx", "k_topm",
+              "k_kmeans"):
     for m in ncu_raw(kname)[:1]:
         dur = num(m.get("gpu__time_duration.sum"))
         rd = num(m.get("dram__bytes_read.sum"))
@@ -111,6 +112,18 @@ for kname in ("k_attend", "k_select3", "k_score_select2", "k_resolve_spec", "k_a
             # ncu reports MB (1e6) in this section
             att = {"kernel": "k_attend", "dram_bytes_per_launch": int(((rd or 0) + (wr or 0)) * 1e6),
                    "duration_us_ncu": dur, "source": f"profiles/{tag}_summary.md"}
+# maintenance / build slow paths (scripts/split_time.py, drift_ingest.py, build_time.py)
+slow = []
+for fn, title in (("split_time.txt", "GPU split k-means vs host (n, d, iterations, times)"),
+                  ("build_time.txt", "Batch index build: device vs host k-means"),
+                  ("drift_ingest.json", "Drift ingest (16 domains, noise 0.05): host split vs GPU split")):
+    pth = os.path.join(src, fn)
+    if os.path.exists(pth):
+        body = [x for x in open(pth).read().splitlines() if x.strip() and "warn" not in x.lower()]
+        slow += ["", f"### {title}", "", "```"] + body[-12:] + ["```"]
+        shutil.copy(pth, os.path.join(dst, f"{tag}_{fn}"))
+if slow:
+    lines += ["", "## Maintenance and build slow paths on the GPU"] + slow
 lines.append("")
 with open(os.path.join(dst, f"{tag}_summary.md"), "w") as f:
     f.write("\n".join(lines) + "\n")
