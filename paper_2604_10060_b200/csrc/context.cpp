@@ -1535,7 +1535,7 @@ std::vector<KMeansOut> Context::kmeans_pools(const std::vector<const float*>& pt
   std::vector<std::size_t> dev;
   for (std::size_t i = 0; i < np; ++i) {
     const int k = std::max(1, std::min(k_req[i], n[i]));
-    if (!host_only && n[i] >= 1 && kmeans_smem_bytes(k, d_) <= 200 * 1024)
+    if (!host_only && n[i] >= 1 && kmeans_smem_bytes(k, d_) <= 227 * 1024)
       dev.push_back(i);
     else
       out[i] = spherical_kmeans(pts[i], n[i], d_, k_req[i], max_iters, tol, seeds[i]);
