@@ -346,8 +346,10 @@ def main():
     q_host, out_host = q_pin.numpy(), out_pin.numpy()
     torch.cuda.synchronize()
     e0.record(stream)
+    h0 = time.perf_counter()
     for i in range(args.warmup, nq):
         kv.query(i, q_host[i], out=out_host)
+    e2e_host_us = (time.perf_counter() - h0) * 1e6 / args.steps
     e1.record(stream)
     torch.cuda.synchronize()
     decode_e2e_ms = e0.elapsed_time(e1)
@@ -392,6 +394,7 @@ def main():
         "gpu_launches": int(decode_launches),
         "phases_us": {"score_select": round(float(np.mean(k4_us)), 2), "attend": round(att_time * 1e6, 2),
                       "host_issue_per_step": round(host_issue_us, 2),
+                      "e2e_host_per_step": round(e2e_host_us, 2),
                       "step_period_us": {"min": round(min(periods), 2) if periods else None,
                                          "median": round(float(np.median(periods)), 2) if periods else None,
                                          "max": round(max(periods), 2) if periods else None},

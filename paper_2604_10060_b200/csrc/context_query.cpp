@@ -120,9 +120,10 @@ bool Context::finish_step(int b) {
   }
   std::vector<std::int64_t> gt;
   gt.swap(step_gt_[b]);
+  const auto w2 = std::chrono::steady_clock::now();  // (after the instrumentation's event wait)
   replay_decode(h_blk_[b], gt.empty() ? nullptr : gt.data(), static_cast<int>(gt.size()));
   step_t_[5] = std::chrono::duration<double, std::micro>(w1 - w0).count();
-  step_t_[6] = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - w1).count();
+  step_t_[6] = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - w2).count();
   return settle;
 }
 
