@@ -112,6 +112,8 @@ Context::~Context() {
     cudaStreamDestroy(in_st_);
   }
   if (ev_init_) cudaEventDestroy(ev_init_);
+  for (cudaEvent_t e : ev_act_)
+    if (e) cudaEventDestroy(e);
   for (int b = 0; b < 2; ++b)
     for (cudaEvent_t e : {ev_ing_[b], ev_in_[b], ev_buf_[b]})
       if (e) cudaEventDestroy(e);
@@ -267,13 +269,16 @@ void Context::alloc_device() {
                  make_key_tensor_map(key_maps_[0], fkbuf_[0], d, t_.tmax, L) &&
                  make_key_tensor_map(key_maps_[1], fkbuf_[1], d, t_.tmax, L);
     std::memcpy(key_map_, key_maps_[0], sizeof(key_map_));
+    const char* sp = std::getenv("KVC_INGEST_SPEC");  // 0: no speculative next-frame round
+    spec_ingest_ = !(sp && std::string(sp) == "0");
     const char* sm = std::getenv("KVC_SPLIT_DEV_MIN");  // smallest group split on the GPU (0: never)
     if (sm) split_dev_min_ = std::atoi(sm);
   }
   d_active_ = static_cast<std::int32_t*>(dalloc(L * 4 * 2));
   d_cursor_ = d_active_ + L;
-  h_active_ = static_cast<std::int32_t*>(halloc(L * 4 * 2));
+  h_active_ = static_cast<std::int32_t*>(halloc(L * 4 * 2 * kActSlots));  // kActSlots staging slots
   h_cursor_ = h_active_ + L;
+  d_evflags_ = static_cast<std::int32_t*>(dalloc(16));  // per frame buffer: first round stopped
   for (int b = 0; b < 2; ++b) {
     h_out_[b] = static_cast<std::int32_t*>(halloc(L * t_.tmax * 4 * 2 + L * 4 * 3 + 16));
     h_errb_[b] = static_cast<std::int32_t*>(halloc(16));
@@ -902,6 +907,8 @@ void Context::finish_frame(std::int64_t* assigned) {
   ia_.T = p.T;
   ia_.pid = static_cast<std::int32_t>(p.pid);
   ia_.ring_slot = p.ring_slot;
+  ia_.my_events = d_evflags_ + p.buf;
+  ia_.prev_events = nullptr;
   const std::int64_t l0 = launches_;
   run_inserts(p.frame_id, p.pid, p.T, assigned, true);
   // re-launches (host events) read the frame buffer again; they happen before any later frame is
@@ -965,7 +972,11 @@ void Context::ingest_frame(std::int64_t frame_id, const float* visual, const voi
   // the frame before the previous one is replayed now, after this frame's payload copy was queued
   // (so the copies run back to back while the host replays)
   finish_pong();
-  if (ping_.active) {
+  // Speculation: this frame's first round is queued behind the pending frame's before that
+  // frame's outcome is known (no device idle while the host waits and launches). It commits
+  // nothing if the pending frame stopped for host events; this frame is then launched again.
+  const bool spec = ping_.active && async_ok && spec_ingest_;
+  if (ping_.active && !spec) {
     KVC_CUDA(cudaEventSynchronize(ping_.ev));
     bool events = false;
     const std::int32_t* stp = h_out_[ping_.buf] + 2 * static_cast<std::size_t>(L_) * t_.tmax;
@@ -1026,11 +1037,12 @@ void Context::ingest_frame(std::int64_t frame_id, const float* visual, const voi
   ia_.T = T;
   ia_.pid = static_cast<std::int32_t>(pid);
   ia_.ring_slot = ring_slot;
-  {
-    std::vector<int> active(static_cast<std::size_t>(L_)), cursor(static_cast<std::size_t>(L_), 0);
-    std::iota(active.begin(), active.end(), 0);
-    launch_round(active, cursor);
-  }
+  std::vector<int> all_doms(static_cast<std::size_t>(L_)), zero_cursor(static_cast<std::size_t>(L_), 0);
+  std::iota(all_doms.begin(), all_doms.end(), 0);
+  ia_.my_events = d_evflags_ + b;
+  ia_.prev_events = spec ? d_evflags_ + ping_.buf : nullptr;
+  launch_round(all_doms, zero_cursor);
+  ia_.prev_events = nullptr;
   KVC_CUDA(cudaEventRecord(ev_buf_[b], st_));  // the frame buffer's readers are all launched
   PendingIngest next;
   next.active = true;
@@ -1041,6 +1053,27 @@ void Context::ingest_frame(std::int64_t frame_id, const float* visual, const voi
   next.buf = b;
   next.ev = ev_ing_[b];
   KVC_CUDA(cudaEventRecord(next.ev, st_));
+  if (spec) {  // now the pending frame's outcome
+    KVC_CUDA(cudaEventSynchronize(ping_.ev));
+    bool events = false;
+    const std::int32_t* stp = h_out_[ping_.buf] + 2 * static_cast<std::size_t>(L_) * t_.tmax;
+    for (int l = 0; l < L_ && !events; ++l) events = stp[l] < ping_.T;
+    if (events || *h_errb_[ping_.buf]) {
+      // host events: settle the pending frame (its relaunches queue behind the skipped round),
+      // then launch this frame again on the settled index
+      finish_frame(nullptr);
+      select_frame_buffer(b);
+      ia_.T = T;
+      ia_.pid = static_cast<std::int32_t>(pid);
+      ia_.ring_slot = ring_slot;
+      ia_.my_events = d_evflags_ + b;
+      launch_round(all_doms, zero_cursor);
+      KVC_CUDA(cudaEventRecord(ev_buf_[b], st_));
+      KVC_CUDA(cudaEventRecord(next.ev, st_));
+      ping_ = next;
+      return;
+    }
+  }
   // the previous frame (no host events, kernels complete) is replayed at the start of the next
   // call (or by any reader of host state: flush_ingest), overlapping this frame's kernels
   if (ping_.active) pong_ = ping_;
@@ -1056,9 +1089,17 @@ void Context::ingest_frame(std::int64_t frame_id, const float* visual, const voi
 void Context::launch_round(const std::vector<int>& active, const std::vector<int>& cursor) {
   flush_resid();
   ia_.n_active = static_cast<std::int32_t>(active.size());
-  for (std::size_t i = 0; i < active.size(); ++i) h_active_[i] = active[i];
-  for (int l = 0; l < L_; ++l) h_cursor_[l] = cursor[static_cast<std::size_t>(l)];
-  KVC_CUDA(cudaMemcpyAsync(d_active_, h_active_, L_ * 8, cudaMemcpyHostToDevice, st_));
+  // rotating pinned staging: a round may be queued behind another whose copy has not run yet
+  // (speculative next frame), so consecutive rounds never share a staging slot
+  const int slot = act_next_;
+  act_next_ = (act_next_ + 1) % kActSlots;
+  if (ev_act_[slot]) KVC_CUDA(cudaEventSynchronize(ev_act_[slot]));
+  std::int32_t* ha = h_active_ + static_cast<std::size_t>(slot) * 2 * L_;
+  for (std::size_t i = 0; i < active.size(); ++i) ha[i] = active[i];
+  for (int l = 0; l < L_; ++l) ha[L_ + l] = cursor[static_cast<std::size_t>(l)];
+  KVC_CUDA(cudaMemcpyAsync(d_active_, ha, L_ * 8, cudaMemcpyHostToDevice, st_));
+  if (!ev_act_[slot]) KVC_CUDA(cudaEventCreateWithFlags(&ev_act_[slot], cudaEventDisableTiming));
+  KVC_CUDA(cudaEventRecord(ev_act_[slot], st_));
   round_timed_ = timing_;
   if (timing_) KVC_CUDA(cudaEventRecord(ev_[0], st_));
   launches_ += launch_build_cands(t_, ia_, st_);

@@ -253,6 +253,11 @@ class Context {
     cudaEvent_t ev = nullptr;  // outcome block of the first launch on the host
   };
   const void* mapped_host(const void* p);
+  static constexpr int kActSlots = 4;
+  int act_next_ = 0;
+  cudaEvent_t ev_act_[kActSlots] = {nullptr, nullptr, nullptr, nullptr};
+  std::int32_t* d_evflags_ = nullptr;  // [2] per frame buffer: its first round stopped a domain
+  bool spec_ingest_ = true;            // KVC_INGEST_SPEC=0: wait for the previous outcome first
   PendingIngest ping_;  // launched, outcome not yet inspected
   PendingIngest pong_;  // the frame before: kernels complete, no host events, replay pending
   void finish_pong();

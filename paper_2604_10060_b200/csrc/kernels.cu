@@ -117,6 +117,7 @@ __device__ bool warp_append(const DevTables& t, int slot, bool to_buf, const uin
 // ============================================================================ K0
 __global__ void k_build_cands(DevTables t, IngestArgs a) {
   const int dom = a.active[blockIdx.x];
+  if (a.my_events && blockIdx.x == 0 && threadIdx.x == 0) *a.my_events = 0;
   __shared__ int cnt_s;
   if (threadIdx.x == 0) cnt_s = 0;
   __syncthreads();
@@ -460,6 +461,7 @@ __global__ void __launch_bounds__(32) k_resolve(DevTables t, IngestArgs a) {
   const int dom = a.active[blockIdx.x];
   const int T = a.T;
   const int cur = a.cursor[dom];
+  if (a.prev_events && *a.prev_events) return;  // skipped speculative round: no writes
   int n = a.cand_n[dom];
   for (int c = lane; c < n; c += 32) {
     const int s = a.cand_slot[static_cast<int64_t>(dom) * cmax + c];
@@ -935,6 +937,8 @@ done:
 // token, to the (page, row) it reserved in the cluster's page list.
 __global__ void k_store_rows(DevTables t, IngestArgs a) {
   const int dom = a.active[blockIdx.y];
+  if (a.prev_events && *a.prev_events) return;  // skipped speculative round: no writes
+  if (a.my_events && blockIdx.x == 0 && threadIdx.x == 0 && a.stop_t[dom] < a.T) atomicOr(a.my_events, 1);
   const int rb = t.d * t.es;
   const int warps = blockDim.x / 32, warp = threadIdx.x / 32, lane = threadIdx.x & 31;
   const int cur = a.cursor[dom];

@@ -155,6 +155,10 @@ struct IngestArgs {
   int32_t* dom_pool_n;     // [L]
   // speculative resolve (resolve_spec.cu): per-token state snapshots, column-major so that
   // one thread per token reads them coalesced
+  // speculative next frame: a round launched behind the previous frame's first round before
+  // its outcome is known; it commits nothing if that round stopped any domain (*prev_events)
+  const int32_t* prev_events;  // null: not speculative
+  int32_t* my_events;          // this frame's first-round flag: some domain stopped early
   double* rsnap;           // [L][d][tmax] representative after each token's insert
   double* bsnap;           // [L][d][tmax] buffer mean after each buffer-moving insert
 };

@@ -238,6 +238,9 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve_spec(DevTables t, Ing
     }
   };
 
+  // speculative round after a frame that stopped for host events: write nothing at all (the
+  // outcome arrays still hold that frame's first round, which its relaunches copy back whole)
+  if (a.prev_events && *a.prev_events) return;
   if (tid < 16) sh_prof[tid] = 0;
   if (tid == 0) {
     a.stop_t[dom] = T;
