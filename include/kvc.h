@@ -263,8 +263,9 @@ KVC_API int kvc_last_step_timing(kvc_ctx* ctx, double* t);
 /* Timing of the last ingested frame (needs kvc_set_timing(1)), t[8]: device microseconds of
  * the candidate lists, approximate tile, top-M + exact pre-scores, sequential resolve and row
  * store kernels (t[0..4], summed over launches); host microseconds waiting for the device (t[5])
- * and of everything else in the on_insert loop incl. replay and host events (t[6]); t[7] the
- * number of host events (seeds / splits) the frame needed. */
+ * and of everything else in the on_insert loop incl. replay and host events (t[6]), of which the
+ * outcome replay loop (t[7]) and relaunch issue (t[8]); t[9] the number of host events (seeds /
+ * splits) the frame needed. t must hold 10 doubles. */
 KVC_API int kvc_last_ingest_timing(kvc_ctx* ctx, double* t);
 /* Host slow-path primitives (no GPU needed), exported so the split / batch-build arithmetic can
  * be checked bit-for-bit against the reference on CPU:

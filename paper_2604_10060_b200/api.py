@@ -500,7 +500,7 @@ class ClusterKVCache:
         return float(out[0]), int(out[1]), int(out[2]), float(out[3])
 
     def ingest_timing(self):
-        t = np.zeros(8)
+        t = np.zeros(10)
         lib().kvc_last_ingest_timing(self.h, _p(t, f64p))
         return t
 

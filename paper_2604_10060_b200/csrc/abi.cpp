@@ -538,7 +538,7 @@ int kvc_debug_resolve_profile(kvc_ctx* ctx, double* out) {
 int kvc_last_ingest_timing(kvc_ctx* ctx, double* t) {
   KVC_CLUSTER_ONLY(ctx);
   const double* s = ctx->impl->ingest_timing();
-  for (int i = 0; i < 8; ++i) t[i] = s[i];
+  for (int i = 0; i < 10; ++i) t[i] = s[i];
   return KVC_OK;
 }
 

@@ -1244,7 +1244,7 @@ void Context::run_inserts(std::int64_t frame_id, std::int64_t pid, int T, std::i
       continue;
     }
     const std::int64_t id = handle_host_event(frame_id, pid, l, stop, h_stop_[L_ + l], h_stop_[2 * L_ + l]);
-    ingest_t_[7] += 1.0;  // host events this frame
+    ingest_t_[9] += 1.0;  // host events this frame
     if (assigned) assigned[static_cast<std::size_t>(l) * T + stop] = id;
     cursor[static_cast<std::size_t>(l)] = stop + 1;
     replayed[static_cast<std::size_t>(l)] = stop + 1;
@@ -1261,9 +1261,9 @@ void Context::run_inserts(std::int64_t frame_id, std::int64_t pid, int T, std::i
   }
   frame_add_flush(frame_id);
   ingest_t_[5] = t_wait;
-  ingest_t_[7] = t_replay;  // (instrumentation) replay loop; launches in ingest_t_[6] below
-  ingest_t_[4] = t_launch;
   ingest_t_[6] = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - r0).count() - t_wait;
+  ingest_t_[7] = t_replay;  // (part of [6]) the outcome replay loop
+  ingest_t_[8] = t_launch;  // (part of [6]) relaunch issue
 }
 
 // ============================================================================ slow path

@@ -307,7 +307,9 @@ class Context {
   alignas(64) unsigned char key_maps_[2][128];
   void* d_check_ = nullptr;                 // debug_assign_check result words
   double step_t_[10] = {0};
-  double ingest_t_[8] = {0};  // last frame: device us (cands, approx, topm, resolve, store), host us (wait, replay, rest)
+  // last frame: device us (cands, assign, topm, resolve, store), host us (wait, on_insert loop,
+  // of which replay and relaunch issue), host events
+  double ingest_t_[10] = {0};
   std::int64_t launches_ = 0;
 
   // ---- physical host tier (context_tiers.cpp)
