@@ -115,7 +115,7 @@ __global__ void __launch_bounds__(SPT) k_split_two(const float* rows, const int3
                                                     double* objective) {
   __shared__ SplitSmem S;
   __shared__ double S_ob[OBJ_CHUNK];
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   double* u = scratch;
   double* ut = u + static_cast<int64_t>(n) * d;
   double* sc = ut + static_cast<int64_t>(n) * d;
@@ -245,36 +245,46 @@ __global__ void __launch_bounds__(SPT) k_split_two(const float* rows, const int3
       }
       __syncthreads();
     }
-    // arithmetic means, sums in point order (clustering.cpp:138-150); one (cluster, dim) per
-    // thread, rows read coalesced across the dimension. Adding +0.0 for non-members leaves the
-    // sum unchanged (it is never -0.0: it starts at +0.0 and exact cancellation rounds to +0.0).
+    // member lists in point order (warp j scans cluster j with ballots), in the k-means++ scratch
+    // (nearv is dead after seeding): memb[0, cnt0) = cluster 0, memb[cnt0, n) = cluster 1
+    int* memb = reinterpret_cast<int*>(nearv);
+    if (warp < 2) {
+      int w = warp == 0 ? 0 : S.cnt[0];
+      for (int base = 0; base < n; base += 32) {
+        const int i = base + lane;
+        const bool m = i < n && assign[i] == warp;
+        const unsigned bal = __ballot_sync(0xffffffffu, m);
+        if (m) memb[w + __popc(bal & ((1u << lane) - 1u))] = i;
+        w += __popc(bal);
+      }
+    }
+    __syncthreads();
+    // arithmetic means, sums in member (= point) order (clustering.cpp:138-150); one (cluster,
+    // dim) chain per thread over that cluster's members only, rows read coalesced across the
+    // dimension, the next 16 members' loads in flight while a group is summed
     double newc = 0.0;
     int wj = -1, wc = 0;
     if (tid < 2 * d) {
       wj = tid / d;
       wc = tid - wj * d;
-      // software-pipelined: the next 16 rows' loads are in flight while this group is summed
+      const int mb = wj == 0 ? 0 : S.cnt[0], me = wj == 0 ? S.cnt[0] : n;
       double acc = 0.0;
-      const int n16 = n & ~15;
+      const int m16 = mb + ((me - mb) & ~15);
       double x[16];
-      auto load16 = [&](int i) {
+      auto load16 = [&](int m) {
 #pragma unroll
-        for (int k = 0; k < 16; ++k) {
-          const double v = u[static_cast<int64_t>(i + k) * d + wc];
-          x[k] = assign[i + k] == wj ? v : 0.0;
-        }
+        for (int k = 0; k < 16; ++k) x[k] = u[static_cast<int64_t>(memb[m + k]) * d + wc];
       };
-      if (n16) load16(0);
-      for (int i = 0; i < n16; i += 16) {
+      if (m16 > mb) load16(mb);
+      for (int m = mb; m < m16; m += 16) {
         double y[16];
 #pragma unroll
         for (int k = 0; k < 16; ++k) y[k] = x[k];
-        if (i + 16 < n16) load16(i + 16);
+        if (m + 16 < m16) load16(m + 16);
 #pragma unroll
         for (int k = 0; k < 16; ++k) acc = dadd(acc, y[k]);
       }
-      for (int i = n16; i < n; ++i)
-        if (assign[i] == wj) acc = dadd(acc, u[static_cast<int64_t>(i) * d + wc]);
+      for (int m = m16; m < me; ++m) acc = dadd(acc, u[static_cast<int64_t>(memb[m]) * d + wc]);
       if (S.cnt[wj] != 0) newc = dmul(acc, ddiv(1.0, static_cast<double>(S.cnt[wj])));
       else wj = -1;  // an empty cluster keeps its centroid
     }
