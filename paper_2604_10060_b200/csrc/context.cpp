@@ -293,6 +293,15 @@ void Context::alloc_device() {
   h_stop_ = h_evs_ + L * t_.tmax;
   ia_.active = d_active_;
   ia_.cursor = d_cursor_;
+  ia_.err_copy = ia_.ev_kind + 2 * static_cast<std::int64_t>(L) * t_.tmax + 3 * L;
+  // every domain from token 0 (a frame's first round): constant device arrays, no staging copy
+  d_all_active_ = static_cast<std::int32_t*>(dalloc(L * 4 * 2));
+  {
+    std::vector<std::int32_t> h(static_cast<std::size_t>(2 * L), 0);
+    for (int l = 0; l < L; ++l) h[static_cast<std::size_t>(l)] = l;
+    KVC_CUDA(cudaMemcpyAsync(d_all_active_, h.data(), h.size() * 4, cudaMemcpyHostToDevice, st_));
+    KVC_CUDA(cudaStreamSynchronize(st_));
+  }
   ia_.fk = d_fk_;
   ia_.fv = d_fv_;
   ia_.defer = cfg_.defer_host_splits;
@@ -395,6 +404,9 @@ void Context::debug_assign_check(const void* keys, int T, std::int64_t pid, int 
   ia_.T = T;
   ia_.pid = static_cast<std::int32_t>(pid);
   ia_.n_active = L_;
+  ia_.active = d_active_;
+  ia_.cursor = d_cursor_;
+  ia_.my_events = nullptr;
   for (int l = 0; l < L_; ++l) {
     h_active_[l] = l;
     h_cursor_[l] = 0;
@@ -895,7 +907,7 @@ void Context::select_frame_buffer(int b) {
   h_evk_ = h_out_[b];
   h_evs_ = h_evk_ + static_cast<std::size_t>(L_) * t_.tmax;
   h_stop_ = h_evs_ + static_cast<std::size_t>(L_) * t_.tmax;
-  h_err_ = h_errb_[b];
+  h_err_ = h_out_[b] + 2 * static_cast<std::size_t>(L_) * t_.tmax + 3 * static_cast<std::size_t>(L_);
 }
 
 // Replay (+ host events) of the pending frame, then window / repin / cadence (engine.cpp:168-173).
@@ -981,7 +993,7 @@ void Context::ingest_frame(std::int64_t frame_id, const float* visual, const voi
     bool events = false;
     const std::int32_t* stp = h_out_[ping_.buf] + 2 * static_cast<std::size_t>(L_) * t_.tmax;
     for (int l = 0; l < L_ && !events; ++l) events = stp[l] < ping_.T;
-    if (!async_ok || events || *h_errb_[ping_.buf]) finish_frame(nullptr);
+    if (!async_ok || events || stp[3 * L_]) finish_frame(nullptr);
   }
   select_frame_buffer(b);
   KVC_CUDA(cudaStreamWaitEvent(st_, ev_in_[b], 0));
@@ -1058,7 +1070,7 @@ void Context::ingest_frame(std::int64_t frame_id, const float* visual, const voi
     bool events = false;
     const std::int32_t* stp = h_out_[ping_.buf] + 2 * static_cast<std::size_t>(L_) * t_.tmax;
     for (int l = 0; l < L_ && !events; ++l) events = stp[l] < ping_.T;
-    if (events || *h_errb_[ping_.buf]) {
+    if (events || stp[3 * L_]) {
       // host events: settle the pending frame (its relaunches queue behind the skipped round),
       // then launch this frame again on the settled index
       finish_frame(nullptr);
@@ -1089,6 +1101,15 @@ void Context::ingest_frame(std::int64_t frame_id, const float* visual, const voi
 void Context::launch_round(const std::vector<int>& active, const std::vector<int>& cursor) {
   flush_resid();
   ia_.n_active = static_cast<std::int32_t>(active.size());
+  bool first = static_cast<int>(active.size()) == L_;
+  for (int l = 0; l < L_ && first; ++l) first = active[static_cast<std::size_t>(l)] == l && cursor[static_cast<std::size_t>(l)] == 0;
+  if (first) {  // a frame's first round: the constant arrays
+    ia_.active = d_all_active_;
+    ia_.cursor = d_all_active_ + L_;
+  } else {
+    ia_.active = d_active_;
+    ia_.cursor = d_cursor_;
+  }
   // rotating pinned staging: a round may be queued behind another whose copy has not run yet
   // (speculative next frame), so consecutive rounds never share a staging slot
   const int slot = act_next_;
@@ -1097,9 +1118,11 @@ void Context::launch_round(const std::vector<int>& active, const std::vector<int
   std::int32_t* ha = h_active_ + static_cast<std::size_t>(slot) * 2 * L_;
   for (std::size_t i = 0; i < active.size(); ++i) ha[i] = active[i];
   for (int l = 0; l < L_; ++l) ha[L_ + l] = cursor[static_cast<std::size_t>(l)];
-  KVC_CUDA(cudaMemcpyAsync(d_active_, ha, L_ * 8, cudaMemcpyHostToDevice, st_));
-  if (!ev_act_[slot]) KVC_CUDA(cudaEventCreateWithFlags(&ev_act_[slot], cudaEventDisableTiming));
-  KVC_CUDA(cudaEventRecord(ev_act_[slot], st_));
+  if (!first) {
+    KVC_CUDA(cudaMemcpyAsync(d_active_, ha, L_ * 8, cudaMemcpyHostToDevice, st_));
+    if (!ev_act_[slot]) KVC_CUDA(cudaEventCreateWithFlags(&ev_act_[slot], cudaEventDisableTiming));
+    KVC_CUDA(cudaEventRecord(ev_act_[slot], st_));
+  }
   round_timed_ = timing_;
   if (timing_) KVC_CUDA(cudaEventRecord(ev_[0], st_));
   launches_ += launch_build_cands(t_, ia_, st_);
@@ -1123,9 +1146,9 @@ void Context::launch_round(const std::vector<int>& active, const std::vector<int
   launches_ += launch_store_rows(t_, ia_, st_);
   KVC_CUDA(cudaGetLastError());
   if (timing_) KVC_CUDA(cudaEventRecord(ev_[5], st_));
-  KVC_CUDA(cudaMemcpyAsync(h_evk_, ia_.ev_kind, (static_cast<std::size_t>(L_) * t_.tmax * 2 + static_cast<std::size_t>(L_) * 3) * 4,
+  // outcome block + the error word K3 copied after it, in one copy
+  KVC_CUDA(cudaMemcpyAsync(h_evk_, ia_.ev_kind, (static_cast<std::size_t>(L_) * t_.tmax * 2 + static_cast<std::size_t>(L_) * 3 + 1) * 4,
                            cudaMemcpyDeviceToHost, st_));
-  KVC_CUDA(cudaMemcpyAsync(h_err_, t_.err, 4, cudaMemcpyDeviceToHost, st_));
 }
 
 // launched: the first round (all domains from token 0) is already in flight with its outcome

@@ -257,6 +257,7 @@ class Context {
   int act_next_ = 0;
   cudaEvent_t ev_act_[kActSlots] = {nullptr, nullptr, nullptr, nullptr};
   std::int32_t* d_evflags_ = nullptr;  // [2] per frame buffer: its first round stopped a domain
+  std::int32_t* d_all_active_ = nullptr;  // [0..L) then L zeros: a first round's active / cursor
   bool spec_ingest_ = true;            // KVC_INGEST_SPEC=0: wait for the previous outcome first
   PendingIngest ping_;  // launched, outcome not yet inspected
   PendingIngest pong_;  // the frame before: kernels complete, no host events, replay pending

@@ -937,6 +937,7 @@ done:
 // token, to the (page, row) it reserved in the cluster's page list.
 __global__ void k_store_rows(DevTables t, IngestArgs a) {
   const int dom = a.active[blockIdx.y];
+  if (a.err_copy && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) *a.err_copy = *t.err;
   if (a.prev_events && *a.prev_events) return;  // skipped speculative round: no writes
   if (a.my_events && blockIdx.x == 0 && threadIdx.x == 0 && a.stop_t[dom] < a.T) atomicOr(a.my_events, 1);
   const int rb = t.d * t.es;

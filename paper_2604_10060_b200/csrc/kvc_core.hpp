@@ -157,6 +157,7 @@ struct IngestArgs {
   // one thread per token reads them coalesced
   // speculative next frame: a round launched behind the previous frame's first round before
   // its outcome is known; it commits nothing if that round stopped any domain (*prev_events)
+  int32_t* err_copy;            // the error word, copied by K3 into the outcome block (one D2H)
   const int32_t* prev_events;  // null: not speculative
   int32_t* my_events;          // this frame's first-round flag: some domain stopped early
   double* rsnap;           // [L][d][tmax] representative after each token's insert
