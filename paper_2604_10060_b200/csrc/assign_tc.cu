@@ -115,6 +115,7 @@ __device__ __forceinline__ uint32_t a_word(const uint8_t* tile0, int KH, int r, 
 
 __global__ void __launch_bounds__(AS_THREADS, 1) k_assign_tc(DevTables t, IngestArgs a,
                                                              const __grid_constant__ CUtensorMap tmk) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // (launched as a dependent of K0)
   extern __shared__ uint8_t smraw[];
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
   const int d = t.d, KH = d / KB;
@@ -429,7 +430,7 @@ int launch_assign_tc(const DevTables& t, const IngestArgs& a, const void* key_ma
                          static_cast<int>(tc_smem_bytes(128)));
     attr = true;
   }
-  k_assign_tc<<<a.n_active, AS_THREADS, smem, st>>>(t, a, *static_cast<const CUtensorMap*>(key_map));
+  launch_pdl(k_assign_tc, dim3(a.n_active), dim3(AS_THREADS), smem, st, t, a, *static_cast<const CUtensorMap*>(key_map));
   return 1;
 }
 

@@ -936,6 +936,7 @@ done:
 // loaded once) go to the window ring page of the frame and, when the resolve kernel committed the
 // token, to the (page, row) it reserved in the cluster's page list.
 __global__ void k_store_rows(DevTables t, IngestArgs a) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // (launched as a dependent of K2)
   const int dom = a.active[blockIdx.y];
   if (a.err_copy && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) *a.err_copy = *t.err;
   if (a.prev_events && *a.prev_events) return;  // skipped speculative round: no writes
@@ -2708,7 +2709,7 @@ int launch_resolve(const DevTables& t, const IngestArgs& a, cudaStream_t st) {
 
 int launch_store_rows(const DevTables& t, const IngestArgs& a, cudaStream_t st) {
   dim3 g((a.T + 7) / 8, a.n_active);  // one warp per row
-  k_store_rows<<<g, 256, 0, st>>>(t, a);
+  launch_pdl(k_store_rows, g, dim3(256), 0, st, t, a);
   return 1;
 }
 

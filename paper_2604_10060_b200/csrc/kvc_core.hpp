@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
 
@@ -347,5 +348,32 @@ int launch_split_two(const float* rows, const int32_t* idx, int n, int d, int fi
                      int32_t* assign, int32_t* meta, double* objective, cudaStream_t st);
 int launch_to_f32(const DevTables& t, const void* src, float* dst, int64_t n_elems,
                   cudaStream_t st);
+
+#ifdef __CUDACC__
+// Launch as a programmatic dependent of the previous kernel on the stream (its launch and block
+// scheduling overlap the predecessor's tail; the kernel must execute griddepcontrol.wait before
+// touching global memory). KVC_INGEST_PDL=0 launches normally.
+inline bool ingest_pdl_enabled() {
+  static const int on = [] {
+    const char* e = std::getenv("KVC_INGEST_PDL");
+    return e ? std::atoi(e) : 1;
+  }();
+  return on != 0;
+}
+template <class K, class... A>
+inline void launch_pdl(K kernel, dim3 g, dim3 b, size_t smem, cudaStream_t st, A... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = g;
+  cfg.blockDim = b;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = ingest_pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+#endif
 
 }  // namespace kvc

@@ -212,6 +212,7 @@ __device__ int warp0_exscan(const int32_t* in_a, const int32_t* in_b, int32_t* o
 }
 
 __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve_spec(DevTables t, IngestArgs a) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // (launched as a dependent of K1)
   extern __shared__ __align__(16) uint8_t smraw[];
   SpecSmem S;
   spec_carve(smraw, &S, t.d, t.es, a.T, t.tmax, t.cmax);
@@ -1175,7 +1176,7 @@ int launch_resolve_spec(const DevTables& t, const IngestArgs& a, cudaStream_t st
     cudaFuncSetAttribute(k_resolve_spec, cudaFuncAttributeMaxDynamicSharedMemorySize, max_optin - 1024);
   }
   if (smem > static_cast<size_t>(max_optin - 1024)) return 0;
-  k_resolve_spec<<<a.n_active, RS_THREADS, smem, st>>>(t, a);
+  launch_pdl(k_resolve_spec, dim3(a.n_active), dim3(RS_THREADS), smem, st, t, a);
   return 1;
 }
 
