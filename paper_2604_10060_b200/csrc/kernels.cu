@@ -116,6 +116,7 @@ __device__ bool warp_append(const DevTables& t, int slot, bool to_buf, const uin
 
 // ============================================================================ K0
 __global__ void k_build_cands(DevTables t, IngestArgs a) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // (a dependent of the ring write)
   const int dom = a.active[blockIdx.x];
   if (a.my_events && blockIdx.x == 0 && threadIdx.x == 0) *a.my_events = 0;
   __shared__ int cnt_s;
@@ -2677,7 +2678,7 @@ __global__ void __launch_bounds__(256) k_flat_topk(DevTables t, const float* q, 
 // ============================================================================ launchers
 
 int launch_build_cands(const DevTables& t, const IngestArgs& a, cudaStream_t st) {
-  k_build_cands<<<a.n_active, 256, 0, st>>>(t, a);
+  launch_pdl(k_build_cands, dim3(a.n_active), dim3(256), 0, st, t, a);
   return 1;
 }
 
