@@ -49,9 +49,11 @@ const void* Context::mapped_host(const void* p) {
   if (off) return nullptr;
   cudaPointerAttributes at{};
   const void* dp = nullptr;
-  if (cudaPointerGetAttributes(&at, p) == cudaSuccess && at.type == cudaMemoryTypeHost && at.devicePointer)
+  const cudaError_t e = cudaPointerGetAttributes(&at, p);
+  if (e == cudaSuccess && at.type == cudaMemoryTypeHost && at.devicePointer)
     dp = at.devicePointer;
-  cudaGetLastError();  // (pageable pointers are not an error worth keeping)
+  else if (e != cudaSuccess)
+    cudaGetLastError();  // clear only this query's own error (an unknown pointer is pageable memory)
   return dp;
 }
 
