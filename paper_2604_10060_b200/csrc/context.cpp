@@ -1153,6 +1153,22 @@ void Context::launch_round(const std::vector<int>& active, const std::vector<int
 
 // launched: the first round (all domains from token 0) is already in flight with its outcome
 // block in h_evk_ (pipelined ingest); otherwise it is launched here.
+namespace {
+// First index in [u, stop) whose (slot, kind) differs from the run's: blocks of 8 compared without
+// branches (vectorised), then the differing block scanned.
+inline int run_end(const std::int32_t* evs, const std::int32_t* evk, int u, int stop, std::int32_t slot,
+                   std::int32_t kind) {
+  while (u + 8 <= stop) {
+    int diff = 0;
+    for (int j = 0; j < 8; ++j) diff |= (evs[u + j] != slot) | (evk[u + j] != kind);
+    if (diff) break;
+    u += 8;
+  }
+  while (u < stop && evs[u] == slot && evk[u] == kind) ++u;
+  return u;
+}
+}  // namespace
+
 void Context::run_inserts(std::int64_t frame_id, std::int64_t pid, int T, std::int64_t* assigned, bool launched) {
   const int ring_slot = ia_.ring_slot;
   const bool eager = !cfg_.defer_host_splits;
@@ -1196,6 +1212,25 @@ void Context::run_inserts(std::int64_t frame_id, std::int64_t pid, int T, std::i
         }
       }
       launch = false;
+      // the replay below is bound by cache misses on scattered per-cluster state: touch every
+      // pending domain's first cluster now, with the loads independent of each other
+      for (int pass = 0; pass < 2; ++pass)
+        for (int l = frontier; l < L_; ++l) {
+          const int t0 = replayed[static_cast<std::size_t>(l)];
+          if (t0 >= h_stop_[l]) continue;
+          const std::int32_t sl = h_evs_[static_cast<std::size_t>(l) * t_.tmax + t0];
+          if (sl < 0 || static_cast<std::size_t>(sl) >= slot_id_.size()) continue;
+          const std::int64_t cid = slot_id_[static_cast<std::size_t>(sl)];
+          if (cid < 0 || static_cast<std::size_t>(cid) >= clusters_.size() || !clusters_[static_cast<std::size_t>(cid)]) continue;
+          const Cluster* cp = clusters_[static_cast<std::size_t>(cid)].get();
+          if (pass == 0) {
+            __builtin_prefetch(cp);
+            __builtin_prefetch(&last_use_[static_cast<std::size_t>(cid)], 1);
+            __builtin_prefetch(&cflags_[static_cast<std::size_t>(cid)], 1);
+          } else if (!cp->members.runs().empty()) {
+            __builtin_prefetch(&cp->members.runs().back(), 1);
+          }
+        }
     }
     const int l = frontier;
     const int stop = h_stop_[l];
@@ -1210,7 +1245,7 @@ void Context::run_inserts(std::int64_t frame_id, std::int64_t pid, int T, std::i
       const std::int32_t slot = evs[t];
       const std::int32_t kind = evk[t];
       int u = t + 1;
-      while (u < stop && evs[u] == slot && evk[u] == kind && kind != EV_DEFER) ++u;
+      if (kind != EV_DEFER) u = run_end(evs, evk, u, stop, slot, kind);
       const int n = u - t;
       const std::int64_t cid = slot_id_[static_cast<std::size_t>(slot)];
       Cluster& c = *clusters_[static_cast<std::size_t>(cid)];
