@@ -196,25 +196,55 @@ __global__ void __launch_bounds__(TT) k_tok_select(TokArgs a, int64_t n, int bud
     S.nq = __dsqrt_rn(s);
     if (S.nq < 1e-12) S.degen = 1;
   }
-  // ---- radix select: the k-th largest key (3 digits: 11, 11, 10 bits)
+  // ---- radix select: the k-th largest key, 4 digits of 8 bits. Each warp counts into its own
+  // shared sub-histogram (match_any aggregates a warp's equal bins; the leader adds without an
+  // atomic), so clustered keys do not serialise every warp on one hot bin; the 32 sub-histograms
+  // are then summed per bin.
+  __shared__ uint16_t whist[TT / 32][256];
   uint32_t vk = 0;
   if (k > 0) {
-    const int shifts[3] = {21, 10, 0};
-    const int widths[3] = {11, 11, 10};
-    for (int p = 0; p < 3; ++p) {
-      const int nbins = 1 << widths[p];
-      for (int i = tid; i < nbins; i += TT) S.hist[i] = 0;
-      __syncthreads();
+    for (int p = 0; p < 4; ++p) {
+      const int shift = 24 - 8 * p;
+      constexpr int nbins = 256;
       const uint32_t pre = S.prefix, pm = S.pmask;
-      // warp-aggregated increments: clustered keys put many rows in the same few bins
       const int64_t npad = (n + TT - 1) / TT * TT;
-      for (int64_t i = tid; i < npad; i += TT) {
-        const uint32_t key = i < n ? fkey(ap[i]) : 0u;
-        const int bin = (i < n && (key & pm) == pre) ? static_cast<int>((key >> shifts[p]) & (nbins - 1)) : -1;
-        const unsigned same = __match_any_sync(kFull, bin);
-        if (bin >= 0 && lane == __ffs(same) - 1) atomicAdd(&S.hist[bin], static_cast<unsigned>(__popc(same)));
+      // chunks of 2047 keys per thread keep a warp's 16-bit counts below 65535
+      constexpr int64_t kChunk = static_cast<int64_t>(2047) * TT;
+      for (int b = tid; b < nbins; b += TT) S.hist[b] = 0;
+      for (int64_t c0 = 0; c0 < npad; c0 += kChunk) {
+        for (int i = lane; i < nbins; i += 32) whist[warp][i] = 0;
+        __syncwarp();
+        const int64_t c1 = min(npad, c0 + kChunk);
+        // eight keys per thread are loaded before any is counted: the warp-synchronous counting
+        // would otherwise expose one memory latency per key
+        constexpr int KB = 8;
+        for (int64_t i0 = c0 + tid; i0 < c1; i0 += KB * TT) {
+          int bins[KB];
+#pragma unroll
+          for (int j = 0; j < KB; ++j) {
+            const int64_t i = i0 + static_cast<int64_t>(j) * TT;
+            const bool in = i < c1 && i < n;
+            const uint32_t key = in ? fkey(ap[i]) : 0u;
+            bins[j] = (in && (key & pm) == pre) ? static_cast<int>((key >> shift) & (nbins - 1)) : -1;
+          }
+#pragma unroll
+          for (int j = 0; j < KB; ++j) {
+            if (i0 + static_cast<int64_t>(j) * TT - lane >= c1) break;  // warp-uniform (c1 is a multiple of 32)
+            const int bin = bins[j];
+            const unsigned same = __match_any_sync(kFull, bin);
+            if (bin >= 0 && lane == __ffs(same) - 1) whist[warp][bin] = static_cast<uint16_t>(whist[warp][bin] + __popc(same));
+            __syncwarp();
+          }
+        }
+        __syncthreads();
+        for (int b = tid; b < nbins; b += TT) {
+          uint32_t c = 0;
+#pragma unroll 8
+          for (int w = 0; w < TT / 32; ++w) c += whist[w][b];
+          S.hist[b] += c;
+        }
+        __syncthreads();
       }
-      __syncthreads();
       if (warp == 0) {  // find the bin holding the kk-th largest (scan from the top)
         const int per = nbins / 32;
         int cnt = 0;
@@ -238,8 +268,8 @@ __global__ void __launch_bounds__(TT) k_tok_select(TokArgs a, int64_t n, int bud
             acc += c;
           }
           const uint32_t bin = static_cast<uint32_t>(hi - b);
-          S.prefix = pre | (bin << shifts[p]);
-          S.pmask = pm | (static_cast<uint32_t>(nbins - 1) << shifts[p]);
+          S.prefix = pre | (bin << shift);
+          S.pmask = pm | (static_cast<uint32_t>(nbins - 1) << shift);
           S.kk = kk - acc;
           S.ncnt = S.hist[bin];  // after the last digit: rows whose key equals v_k
         }
