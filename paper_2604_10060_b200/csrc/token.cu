@@ -290,25 +290,37 @@ __global__ void __launch_bounds__(TT) k_tok_select(TokArgs a, int64_t n, int bud
   const float hi_t = vkf + 2.f * kTokMargin + 1e-6f, lo_t = vkf - 2.f * kTokMargin - 1e-6f;
   const int64_t nw = (n + 31) / 32;
   // word-aligned passes: warp w handles words w, w + 32, ...; lane = bit
-  for (int64_t w0 = 0; w0 < nw; w0 += TT / 32) {
-    const int64_t w = w0 + warp;
-    const int64_t i = w * 32 + lane;
-    bool in = false, bd = false;
-    if (w < nw && i < n && k > 0) {
-      const float x = ap[i];
-      if (x >= hi_t) in = true;
-      else if (x >= lo_t) bd = true;
+  // (eight words per warp are loaded before any is classified: one memory latency per batch)
+  constexpr int WB = 8;
+  for (int64_t wb = 0; wb < nw; wb += WB * (TT / 32)) {
+    float xs[WB];
+#pragma unroll
+    for (int j = 0; j < WB; ++j) {
+      const int64_t w = wb + static_cast<int64_t>(j) * (TT / 32) + warp;
+      const int64_t i = w * 32 + lane;
+      xs[j] = (w < nw && i < n && k > 0) ? ap[i] : -INFINITY;
     }
-    const unsigned bin = __ballot_sync(kFull, in);
-    const unsigned bbd = __ballot_sync(kFull, bd);
-    if (w < nw) {
-      if (lane == 0) pick[w] = bin;
-      if (lane == 0 && bin) atomicAdd(&S.nu, __popc(bin));
-      if (bbd) {
-        int base = 0;
-        if (lane == 0) base = atomicAdd(&S.nb, __popc(bbd));
-        base = __shfl_sync(kFull, base, 0);
-        if (bd) a.bidx[static_cast<int64_t>(l) * a.cap + base + __popc(bbd & ((1u << lane) - 1u))] = static_cast<int>(i);
+#pragma unroll
+    for (int j = 0; j < WB; ++j) {
+      const int64_t w = wb + static_cast<int64_t>(j) * (TT / 32) + warp;
+      const int64_t i = w * 32 + lane;
+      bool in = false, bd = false;
+      if (w < nw && i < n && k > 0) {
+        const float x = xs[j];
+        if (x >= hi_t) in = true;
+        else if (x >= lo_t) bd = true;
+      }
+      const unsigned bin = __ballot_sync(kFull, in);
+      const unsigned bbd = __ballot_sync(kFull, bd);
+      if (w < nw) {
+        if (lane == 0) pick[w] = bin;
+        if (lane == 0 && bin) atomicAdd(&S.nu, __popc(bin));
+        if (bbd) {
+          int base = 0;
+          if (lane == 0) base = atomicAdd(&S.nb, __popc(bbd));
+          base = __shfl_sync(kFull, base, 0);
+          if (bd) a.bidx[static_cast<int64_t>(l) * a.cap + base + __popc(bbd & ((1u << lane) - 1u))] = static_cast<int>(i);
+        }
       }
     }
   }
