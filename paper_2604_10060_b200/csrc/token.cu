@@ -32,6 +32,7 @@ constexpr int TB_EQ = 1024;      // rows sharing the boundary's exact r-th value
 // covers the sum with margin. Clustered keys put many rows near the threshold, so the margin is
 // kept tight and the boundary is ranked exactly by a radix select, not by pairwise counting.
 constexpr float kTokMargin = 4e-5f;
+constexpr int kTokRowsPerBlock = 1024;  // KT2 (bf16, d = 128): rows per block
 
 __device__ __forceinline__ float ldf(const uint8_t* row, int i, int bf16) {
   return bf16 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(row)[i]) : reinterpret_cast<const float*>(row)[i];
@@ -92,10 +93,14 @@ __global__ void __launch_bounds__(256) k_tok_approx(TokArgs a, int64_t n) {
   const float* knp = a.kn32 + static_cast<int64_t>(l) * a.cap;
   if (rb == 256 && a.es == 2) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, half = lane >> 4, hl = lane & 15;
-    const int64_t r0 = static_cast<int64_t>(blockIdx.x) * 256 + warp * 32;  // this warp's 32 rows
     float qv[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u) qv[u] = qs[hl * 8 + u];
+    // a block walks TOK_ROWS_PER_BLOCK / 256 tiles of 256 rows (amortises the query prologue)
+    for (int64_t tile = static_cast<int64_t>(blockIdx.x) * (kTokRowsPerBlock / 256);
+         tile < static_cast<int64_t>(blockIdx.x + 1) * (kTokRowsPerBlock / 256); ++tile) {
+    const int64_t r0 = tile * 256 + warp * 32;  // this warp's 32 rows
+    if (r0 >= n) break;  // warp-uniform
 #pragma unroll
     for (int g = 0; g < 2; ++g) {  // two groups of 16 rows
       uint4 w[8];
@@ -118,6 +123,7 @@ __global__ void __launch_bounds__(256) k_tok_approx(TokArgs a, int64_t n) {
         const int64_t i = r0 + g * 16 + p * 2 + half;
         if (hl == 0 && i < n) outp[i] = acc / (nq32 * knp[i]);
       }
+    }
     }
     return;
   }
@@ -608,7 +614,8 @@ int launch_tok_append(const TokArgs& a, const void* fk, const void* fv, int T, i
 int launch_tok_decode(const TokArgs& a, const DevTables& stage, const DecodeArgs& da, int64_t n, int budget,
                       int64_t win_lo, cudaStream_t st) {
   if (n <= 0) return 0;
-  k_tok_approx<<<dim3(static_cast<unsigned>((n + 255) / 256), a.L), 256, a.d * 4, st>>>(a, n);
+  const int64_t per_block = (a.d * a.es == 256 && a.es == 2) ? kTokRowsPerBlock : 256;
+  k_tok_approx<<<dim3(static_cast<unsigned>((n + per_block - 1) / per_block), a.L), 256, a.d * 4, st>>>(a, n);
   k_tok_select<<<a.L, TT, 0, st>>>(a, n, budget, win_lo);
   k_tok_gather<<<dim3(static_cast<unsigned>(max(1, (a.max_att + 63) / 64)), a.L), 256, 0, st>>>(a, stage, da);
   // (rows of more than 512 bytes -- d > 128 in fp32 -- are outside the gather's two 16-byte chunks per lane)
