@@ -52,3 +52,26 @@ def test_async_ingest_equals_sync(cfg):
     assert st_s[3] == st_a[3]
     st = kv_s.maint_stats()
     assert st[2] + st[3] > 0, "stream must exercise splits"
+
+
+def test_async_ingest_gpu_splits_equal_sync_host_splits(monkeypatch):
+    """Every split of >= 2 rows on the GPU (split.cu) in the pipelined, speculative path leaves the
+    state of the synchronous path with host splits."""
+    from paper_2604_10060_b200 import ClusterKVCache
+
+    s = po.gen_stream_restated(po.StreamCfg.make(n_scenes=4, frames_per_scene=12, tokens_per_frame=48, d=64, L=3,
+                                                 n_queries=8, queries_at_end=0, semantic_noise=0.08, seed=23))
+    ecfg = po.EngineCfg.make(build_batch_frames=6, offload_horizon_frames=3, device_capacity_entries=1200)
+    monkeypatch.setenv("KVC_SPLIT_DEV_MIN", "0")
+    kv_s = ClusterKVCache(product_config(ecfg, parity_mode=0, check_invariants=0), s.d, s.L)
+    monkeypatch.setenv("KVC_SPLIT_DEV_MIN", "2")
+    kv_a = ClusterKVCache(product_config(ecfg, parity_mode=0, check_invariants=0), s.d, s.L)
+    for kind, i in s.events():
+        if kind == "frame":
+            kv_s.process_frame(i, s.visual[i], s.keys[i], s.values[i], want_assigned=True)
+            kv_a.process_frame(i, s.visual[i], s.keys[i], s.values[i], want_assigned=False)
+        else:
+            np.testing.assert_allclose(kv_s.query(i, s.q[i]), kv_a.query(i, s.q[i]), rtol=0, atol=1e-6)
+    st_s, st_a = _state(kv_s), _state(kv_a)
+    assert st_s == st_a
+    assert kv_s.maint_stats()[5] > 0, "stream must exercise split_two"
