@@ -83,7 +83,8 @@ typedef struct {
   uint64_t seed;
   /* ---- device data plane ---- */
   int32_t kv_dtype;            /* KVC_DTYPE_F32 (bit-exact fp32 keys) or KVC_DTYPE_BF16 */
-  int32_t page_tokens;         /* tokens per K/V page (cluster-contiguous store), default 64 */
+  int32_t page_tokens;         /* tokens per K/V page (cluster-contiguous store); 0 (default) = auto:
+                                  64, halved while the attention kernel's page ring does not fit */
   int64_t max_pages;           /* page-pool size (0 = derive from pool_bytes) */
   int64_t pool_bytes;          /* page-pool bytes when max_pages == 0, default 1 GiB */
   int32_t max_slots;           /* live-cluster table capacity, default 65536 */

@@ -94,6 +94,7 @@ def reference():
         lib.ref_drv_set_checks.argtypes = [vp, C.c_int]
         lib.ref_drv_frame.argtypes = [vp, C.c_int64, f32p, f32p, f32p, C.c_int, i64p, i64p]
         lib.ref_drv_build_now.argtypes = [vp]
+        lib.ref_drv_bulk_load.argtypes = [vp, f32p, f32p, f32p, C.c_int, C.c_int, i32p, i64p, i32p, i64p]
         lib.ref_drv_query.argtypes = [vp, C.c_int64, f32p, i64p, C.c_int]
         lib.ref_drv_q_ranked.argtypes = [vp, C.c_int, i64p, i32p, C.c_int]
         lib.ref_drv_q_selected.argtypes = [vp, C.c_int, i64p, C.c_int]
@@ -350,6 +351,20 @@ class RefDriver:
 
     def build_now(self):
         self._chk(self.lib.ref_drv_build_now(self.h))
+
+    def bulk_load(self, visual, keys, values, assign, frame_ids, token_ids, n_clusters):
+        """The checker side of kvc_bulk_load (ref_shim.cpp ref_drv_bulk_load): keys/values
+        [L, N, d] f32, assign [L, N]; returns the partition id."""
+        k = np.ascontiguousarray(keys, np.float32)
+        v = np.ascontiguousarray(values, np.float32)
+        a = np.ascontiguousarray(assign, np.int32)
+        fr = np.ascontiguousarray(frame_ids, np.int64)
+        tk = np.ascontiguousarray(token_ids, np.int32)
+        pid = C.c_int64(-1)
+        self._chk(self.lib.ref_drv_bulk_load(self.h, _p(np.ascontiguousarray(visual, np.float32), f32p),
+                                             _p(k, f32p), _p(v, f32p), k.shape[1], n_clusters, _p(a, i32p),
+                                             _p(fr, i64p), _p(tk, i32p), C.byref(pid)))
+        return pid.value
 
     def query(self, qid, q, gt=None):
         gt = np.zeros(0, np.int64) if gt is None else np.ascontiguousarray(gt, np.int64)

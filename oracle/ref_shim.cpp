@@ -22,6 +22,7 @@
 // Errors: every entry point catches kvclust::Error and returns a negative code
 // (see kvc.h's KVC_E_* values, which mirror error.hpp:9-82).
 
+#include <algorithm>
 #include <chrono>
 #include <cmath>
 #include <cstdint>
@@ -887,23 +888,32 @@ int ref_prim_kmeans(const float* pts, int n, int d, int k, int max_iters, double
   }
 }
 
-// ---------------------------------------------------------------- CPU baseline timers
 
-// Builds a reference HierIndex directly from a synthetic clustered state (one partition,
-// L layers, C clusters/layer, members given as keys/values [L][N][d] with assignment
-// [L][N]); then times `steps` retrieve() calls (retrieval.cpp:45-143) plus the fp64
-// attention restatement over each layer's attended set. Returns microseconds per step
-// for retrieve (t[0]) and attention (t[1]).
-int ref_time_decode(int d, int L, int N, int C, const float* keys, const float* values,
-                    const std::int32_t* assign, const float* queries /*[steps][L][d]*/,
-                    int steps, int k_s, int window_tokens, double* t) {
-  GUARD_BEGIN
-  HierIndex index(d, L);
+// Installs one partition's pre-clustered state through the public HierIndex API, the way
+// kvc_bulk_load documents it (include/kvc.h): add_partition (index.cpp:59-69) for the
+// visual, the partition's frame list set to the members' distinct frames (the product records
+// every loaded frame with visual_stat_count = #frames), then per layer, per cluster index
+// ascending, add_cluster (index.cpp:97-120) with the exact Eq. 1/2 statistics
+// (compute_representative / compute_variance, index.cpp:345-362). Members keep row order.
+// keys/values [L][N][d]; assign [L][N]; frame_ids / token_ids [N] (NULL: i / 196, i % 196).
+static std::int64_t install_clusters(HierIndex& index, int d, int L, int N, int C, const float* keys,
+                                     const float* values, const std::int32_t* assign, const float* visual,
+                                     const std::int64_t* frame_ids, const std::int32_t* token_ids,
+                                     bool full_partition) {
   Embedding vis(static_cast<std::size_t>(d), 0.0f);
-  vis[0] = 1.0f;
-  std::int64_t pid = index.add_partition(0, vis);
-  // value lookup by (layer, frame, token); token id = position in the layer
-  const int T = 196;
+  if (visual) vis.assign(visual, visual + d); else vis[0] = 1.0f;
+  auto fid = [&](int i) -> std::int64_t { return frame_ids ? frame_ids[i] : i / 196; };
+  auto tid = [&](int i) -> std::int32_t { return token_ids ? token_ids[i] : i % 196; };
+  std::vector<std::int64_t> fr;
+  for (int i = 0; i < N; ++i) fr.push_back(fid(i));
+  std::sort(fr.begin(), fr.end());
+  fr.erase(std::unique(fr.begin(), fr.end()), fr.end());
+  const std::int64_t pid = index.add_partition(fr.empty() ? 0 : fr.front(), vis);
+  if (full_partition) {
+    VisualPartition& p = index.partition(pid);
+    p.frame_ids = fr;
+    p.visual_stat_count = static_cast<std::int64_t>(fr.size());
+  }
   for (int l = 0; l < L; ++l) {
     std::vector<std::vector<KVEntry>> groups(static_cast<std::size_t>(C));
     for (int i = 0; i < N; ++i) {
@@ -911,10 +921,12 @@ int ref_time_decode(int d, int L, int N, int C, const float* keys, const float* 
       std::size_t off = (static_cast<std::size_t>(l) * N + i) * d;
       e.key.assign(keys + off, keys + off + d);
       e.value.assign(values + off, values + off + d);
-      e.frame_id = i / T;
+      e.frame_id = fid(i);
       e.layer_id = l;
-      e.token_id = i % T;
-      groups[static_cast<std::size_t>(assign[static_cast<std::size_t>(l) * N + i])].push_back(std::move(e));
+      e.token_id = tid(i);
+      const std::int32_t a = assign[static_cast<std::size_t>(l) * N + i];
+      if (a < 0 || a >= C) throw ConfigError("cluster index out of range");
+      groups[static_cast<std::size_t>(a)].push_back(std::move(e));
     }
     for (auto& g : groups) {
       if (g.empty()) continue;
@@ -928,6 +940,43 @@ int ref_time_decode(int d, int L, int N, int C, const float* keys, const float* 
       index.add_cluster(std::move(rec));
     }
   }
+  return pid;
+}
+
+// Bulk construction on the driver (the checker side of kvc_bulk_load): the index is built by
+// install_clusters, then the store adopts every cluster in id order (store.cpp:67-74) and the
+// maintainer is created with the engine's seed (engine.cpp:84), as after StreamEngine's build.
+int ref_drv_bulk_load(void* h, const float* visual, const float* keys, const float* values, int N, int C,
+                      const std::int32_t* assign, const std::int64_t* frame_ids, const std::int32_t* token_ids,
+                      std::int64_t* partition) {
+  GUARD_BEGIN
+  auto* drv = static_cast<Driver*>(h);
+  if (drv->built || !drv->pending.empty()) throw ConfigError("bulk load needs a fresh driver");
+  drv->index.emplace(drv->d, drv->L);
+  *partition = install_clusters(*drv->index, drv->d, drv->L, N, C, keys, values, assign, visual, frame_ids,
+                                token_ids, true);
+  drv->store.emplace(*drv->index, drv->cfg.cost);
+  MaintainerConfig m = drv->cfg.maintainer;
+  m.seed = mix_seed(drv->cfg.seed, 2);
+  drv->maint.emplace(*drv->index, *drv->store, m);
+  drv->built = true;
+  GUARD_END
+}
+
+// ---------------------------------------------------------------- CPU baseline timers
+
+// Builds a reference HierIndex directly from a synthetic clustered state (one partition,
+// L layers, C clusters/layer, members given as keys/values [L][N][d] with assignment
+// [L][N]); then times `steps` retrieve() calls (retrieval.cpp:45-143) plus the fp64
+// attention restatement over each layer's attended set. Returns microseconds per step
+// for retrieve (t[0]) and attention (t[1]).
+int ref_time_decode(int d, int L, int N, int C, const float* keys, const float* values,
+                    const std::int32_t* assign, const float* queries /*[steps][L][d]*/,
+                    int steps, int k_s, int window_tokens, double* t) {
+  GUARD_BEGIN
+  HierIndex index(d, L);
+  install_clusters(index, d, L, N, C, keys, values, assign, nullptr, nullptr, nullptr, false);
+  const int T = 196;
   CostModel cost;
   cost.device_capacity_entries = static_cast<std::int64_t>(L) * N + 1;
   TieredStore store(index, cost);
@@ -1012,34 +1061,8 @@ int ref_time_mt(int mode, int threads, int d, int L, int N, int C, const float* 
   auto worker = [&](int ti) {
     try {
       HierIndex index(d, L);
-      Embedding vis(static_cast<std::size_t>(d), 0.0f);
-      if (fvis) vis.assign(fvis, fvis + d); else vis[0] = 1.0f;
-      std::int64_t pid = index.add_partition(0, vis);
+      install_clusters(index, d, L, N, C, keys, values, assign, fvis, nullptr, nullptr, false);
       const int TT = 196;
-      for (int l = 0; l < L; ++l) {
-        std::vector<std::vector<KVEntry>> groups(static_cast<std::size_t>(C));
-        for (int i = 0; i < N; ++i) {
-          KVEntry e;
-          std::size_t off = (static_cast<std::size_t>(l) * N + i) * d;
-          e.key.assign(keys + off, keys + off + d);
-          e.value.assign(values + off, values + off + d);
-          e.frame_id = i / TT;
-          e.layer_id = l;
-          e.token_id = i % TT;
-          groups[static_cast<std::size_t>(assign[static_cast<std::size_t>(l) * N + i])].push_back(std::move(e));
-        }
-        for (auto& g : groups) {
-          if (g.empty()) continue;
-          ClusterRecord rec;
-          rec.layer_id = l;
-          rec.visual_parent = pid;
-          rec.rep = compute_representative(g);
-          rec.variance = compute_variance(g, rec.rep);
-          rec.stat_count = static_cast<std::int64_t>(g.size());
-          rec.members = std::move(g);
-          index.add_cluster(std::move(rec));
-        }
-      }
       CostModel cost;
       cost.device_capacity_entries = static_cast<std::int64_t>(L) * (N + (warmup + steps) * T + 1) + 1;
       TieredStore store(index, cost);

@@ -42,14 +42,11 @@ int guard(F&& f) {
 }
 
 // Host-state readers first complete the deferred bookkeeping of the last decode step. Only call
-// inside guard(): a token-baseline context has no cluster index.
+// inside guard(): it throws (a failed replay must surface as the reader's status, never leave
+// stale views behind a success count) and a token-baseline context has no cluster index.
 Context& F(kvc_ctx* c) {
   if (!c->impl) kvc::fail(KVC_E_CONFIG, "not available in token-baseline mode (cfg.token_mode)");
-  try {
-    c->impl->flush_pending();
-  } catch (const std::exception& e) {
-    g_err = e.what();
-  }
+  c->impl->flush_pending();
   return *c->impl;
 }
 
@@ -61,6 +58,18 @@ Context& F(kvc_ctx* c) {
       return KVC_E_CONFIG;                                                      \
     }                                                                           \
   } while (0)
+
+// Readers that return a count (not wrapped in guard): the cluster path, with the deferred
+// decode bookkeeping completed first; a replay failure is returned as the reader's status.
+#define KVC_READER(ctx)                                                         \
+  do {                                                                          \
+    KVC_CLUSTER_ONLY(ctx);                                                      \
+    const int rc_ = guard([&] { (ctx)->impl->flush_pending(); });               \
+    if (rc_ != KVC_OK) return rc_;                                              \
+  } while (0)
+
+// After KVC_READER: the flushed context.
+inline Context& R(kvc_ctx* c) { return *c->impl; }
 
 template <class T>
 int copy_out(const std::vector<T>& v, T* dst, int cap) {
@@ -107,7 +116,7 @@ void kvc_cfg_default(kvc_cfg* c) {
   c->seed = 0;
   // device data plane
   c->kv_dtype = KVC_DTYPE_F32;
-  c->page_tokens = 64;
+  c->page_tokens = 0;  // auto: 64, halved while the attention kernel's page ring does not fit
   c->max_pages = 0;
   c->pool_bytes = 1LL << 30;
   c->max_slots = 65536;
@@ -176,7 +185,8 @@ int kvc_decode_step(kvc_ctx* ctx, int64_t query_id, const float* q, int32_t q_me
 
 int kvc_last_ranked(kvc_ctx* ctx, int32_t layer, int64_t* ids, int32_t* is_buffer, int32_t cap) {
   if (ctx->tok) return 0;  // no cluster ranking in the token baseline
-  const auto& ls = F(ctx).last_layers();
+  KVC_READER(ctx);
+  const auto& ls = R(ctx).last_layers();
   if (layer < 0 || layer >= static_cast<int>(ls.size())) return KVC_E_BAD_LAYER;
   const auto& r = ls[static_cast<std::size_t>(layer)].ranked;
   for (int i = 0; i < static_cast<int>(r.size()) && i < cap; ++i) {
@@ -188,7 +198,8 @@ int kvc_last_ranked(kvc_ctx* ctx, int32_t layer, int64_t* ids, int32_t* is_buffe
 
 int kvc_last_selected(kvc_ctx* ctx, int32_t layer, int64_t* ids, int32_t cap) {
   if (ctx->tok) return 0;
-  const auto& ls = F(ctx).last_layers();
+  KVC_READER(ctx);
+  const auto& ls = R(ctx).last_layers();
   if (layer < 0 || layer >= static_cast<int>(ls.size())) return KVC_E_BAD_LAYER;
   return copy_out(ls[static_cast<std::size_t>(layer)].selected, ids, cap);
 }
@@ -199,7 +210,8 @@ int kvc_last_attended(kvc_ctx* ctx, int32_t layer, int64_t* frames, int32_t* tok
     const int rc = guard([&] { n = ctx->tok->attended(layer, frames, tokens, cap); });
     return rc != KVC_OK ? rc : n;
   }
-  const auto& ls = F(ctx).last_layers();
+  KVC_READER(ctx);
+  const auto& ls = R(ctx).last_layers();
   if (layer < 0 || layer >= static_cast<int>(ls.size())) return KVC_E_BAD_LAYER;
   const auto& a = ls[static_cast<std::size_t>(layer)].attended;
   for (int i = 0; i < static_cast<int>(a.size()) && i < cap; ++i) {
@@ -211,7 +223,8 @@ int kvc_last_attended(kvc_ctx* ctx, int32_t layer, int64_t* frames, int32_t* tok
 
 int kvc_last_layer_meta(kvc_ctx* ctx, int32_t layer, double* lat, int64_t* ints) {
   if (ctx->tok) return guard([&] { ctx->tok->layer_meta(layer, lat, ints); });
-  const auto& ls = F(ctx).last_layers();
+  KVC_READER(ctx);
+  const auto& ls = R(ctx).last_layers();
   if (layer < 0 || layer >= static_cast<int>(ls.size())) return KVC_E_BAD_LAYER;
   const auto& lo = ls[static_cast<std::size_t>(layer)];
   for (int i = 0; i < 5; ++i) lat[i] = lo.lat[i];
@@ -229,12 +242,19 @@ int kvc_last_query_meta(kvc_ctx* ctx, double* dd) {
     dd[1] = ctx->tok->recall();
     return KVC_OK;
   }
-  dd[0] = F(ctx).last_ttft();
-  dd[1] = F(ctx).last_recall();
+  KVC_READER(ctx);
+  dd[0] = R(ctx).last_ttft();
+  dd[1] = R(ctx).last_recall();
   return KVC_OK;
 }
 
-uint64_t kvc_last_digest(kvc_ctx* ctx) { return ctx->tok ? ctx->tok->digest() : F(ctx).last_digest(); }
+// 0 (with kvc_last_error set) when the deferred bookkeeping of the step failed
+uint64_t kvc_last_digest(kvc_ctx* ctx) {
+  if (ctx->tok) return ctx->tok->digest();
+  uint64_t h = 0;
+  const int rc = guard([&] { h = F(ctx).last_digest(); });
+  return rc == KVC_OK ? h : 0;
+}
 
 int kvc_flat_topk(kvc_ctx* ctx, const float* q, int32_t layer, int32_t k, int64_t* ids,
                   int32_t* is_buffer) {
@@ -265,12 +285,14 @@ int kvc_bulk_load(kvc_ctx* ctx, const float* visual, const void* keys, const voi
 
 int kvc_n_clusters(kvc_ctx* ctx) {
   if (ctx->tok) return 0;
-  return static_cast<int>(F(ctx).cluster_ids().size());
+  KVC_READER(ctx);
+  return static_cast<int>(R(ctx).cluster_ids().size());
 }
 
 int kvc_cluster_ids(kvc_ctx* ctx, int64_t* ids, int32_t cap) {
   if (ctx->tok) return 0;
-  return copy_out(F(ctx).cluster_ids(), ids, cap);
+  KVC_READER(ctx);
+  return copy_out(R(ctx).cluster_ids(), ids, cap);
 }
 
 int kvc_cluster(kvc_ctx* ctx, int64_t id, int64_t* info, double* var, double* rep,
@@ -296,8 +318,8 @@ int kvc_cluster(kvc_ctx* ctx, int64_t id, int64_t* info, double* var, double* re
 
 int kvc_cluster_entries(kvc_ctx* ctx, int64_t id, int32_t which, int64_t* frames, int32_t* tokens,
                         int32_t cap) {
-  KVC_CLUSTER_ONLY(ctx);
-  const kvc::Cluster* c = F(ctx).cluster(id);
+  KVC_READER(ctx);
+  const kvc::Cluster* c = R(ctx).cluster(id);
   if (!c) return KVC_E_UNKNOWN_CLUSTER;
   const auto& v = which == 0 ? c->members : c->buffer;
   int i = 0;
@@ -319,12 +341,13 @@ int kvc_cluster_payload(kvc_ctx* ctx, int64_t id, int32_t which, float* keys, fl
 
 int kvc_n_partitions(kvc_ctx* ctx) {
   if (ctx->tok) return 0;
-  return static_cast<int>(F(ctx).partitions().size());
+  KVC_READER(ctx);
+  return static_cast<int>(R(ctx).partitions().size());
 }
 
 int kvc_partition(kvc_ctx* ctx, int32_t p, double* visual_rep, int64_t* frames, int32_t cap) {
-  KVC_CLUSTER_ONLY(ctx);
-  const auto& ps = F(ctx).partitions();
+  KVC_READER(ctx);
+  const auto& ps = R(ctx).partitions();
   if (p < 0 || p >= static_cast<int>(ps.size())) return KVC_E_UNKNOWN_CLUSTER;
   const auto& part = ps[static_cast<std::size_t>(p)];
   if (visual_rep) std::memcpy(visual_rep, part.vrep.data(), part.vrep.size() * sizeof(double));
@@ -332,10 +355,10 @@ int kvc_partition(kvc_ctx* ctx, int32_t p, double* visual_rep, int64_t* frames, 
 }
 
 int kvc_partition_layer(kvc_ctx* ctx, int32_t p, int32_t layer, int64_t* ids, int32_t cap) {
-  KVC_CLUSTER_ONLY(ctx);
-  const auto& ps = F(ctx).partitions();
+  KVC_READER(ctx);
+  const auto& ps = R(ctx).partitions();
   if (p < 0 || p >= static_cast<int>(ps.size())) return KVC_E_UNKNOWN_CLUSTER;
-  if (layer < 0 || layer >= F(ctx).L()) return KVC_E_BAD_LAYER;
+  if (layer < 0 || layer >= R(ctx).L()) return KVC_E_BAD_LAYER;
   return copy_out(ps[static_cast<std::size_t>(p)].per_layer[static_cast<std::size_t>(layer)], ids, cap);
 }
 
@@ -344,31 +367,37 @@ int kvc_maint_stats(kvc_ctx* ctx, int64_t* out) {
     std::memset(out, 0, 9 * sizeof(int64_t));
     return KVC_OK;
   }
-  std::memcpy(out, F(ctx).maint_stats(), 9 * sizeof(int64_t));
+  KVC_READER(ctx);
+  std::memcpy(out, R(ctx).maint_stats(), 9 * sizeof(int64_t));
   return KVC_OK;
 }
 
 int64_t kvc_ledger(kvc_ctx* ctx, int64_t* ops, int64_t* bytes, double* cost_us) {
   if (ctx->tok) return ctx->tok->ledger(ops, bytes, cost_us);  // the baseline ledger (engine.cpp:184)
+  KVC_READER(ctx);
   for (int i = 0; i < 5; ++i) {
     ops[i] = 0;
     bytes[i] = 0;
     cost_us[i] = 0.0;
   }
-  for (const auto& op : F(ctx).ledger()) {  // TransferLedger::record (store.cpp:21-27)
+  for (const auto& op : R(ctx).ledger()) {  // TransferLedger::record (store.cpp:21-27)
     ops[op.cause] += op.n_ops;
     bytes[op.cause] += op.bytes;
     cost_us[op.cause] += op.cost_us;
   }
-  return F(ctx).device_entries();
+  return R(ctx).device_entries();
 }
 
 // (token baseline: totals only -- one op per coalesced run would be thousands per query)
-int kvc_ledger_log_size(kvc_ctx* ctx) { return ctx->tok ? 0 : static_cast<int>(F(ctx).ledger().size()); }
+int kvc_ledger_log_size(kvc_ctx* ctx) {
+  if (ctx->tok) return 0;
+  KVC_READER(ctx);
+  return static_cast<int>(R(ctx).ledger().size());
+}
 
 int kvc_ledger_op(kvc_ctx* ctx, int32_t i, int64_t* ints) {
-  KVC_CLUSTER_ONLY(ctx);
-  const auto& lg = F(ctx).ledger();
+  KVC_READER(ctx);
+  const auto& lg = R(ctx).ledger();
   if (i < 0 || i >= static_cast<int>(lg.size())) return KVC_E_CONFIG;
   const auto& op = lg[static_cast<std::size_t>(i)];
   ints[0] = op.cause;

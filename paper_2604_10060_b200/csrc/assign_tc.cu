@@ -424,12 +424,7 @@ int launch_assign_err(const DevTables& t, const IngestArgs& a, unsigned long lon
 
 int launch_assign_tc(const DevTables& t, const IngestArgs& a, const void* key_map, cudaStream_t st) {
   const size_t smem = tc_smem_bytes(t.d);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_assign_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(tc_smem_bytes(128)));
-    attr = true;
-  }
+  if (!smem_optin(reinterpret_cast<const void*>(k_assign_tc), smem)) return 0;
   launch_pdl(k_assign_tc, dim3(a.n_active), dim3(AS_THREADS), smem, st, t, a, *static_cast<const CUtensorMap*>(key_map));
   return 1;
 }

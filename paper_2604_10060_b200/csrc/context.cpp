@@ -72,7 +72,8 @@ Context::Context(const kvc_cfg& cfg, int d, int L) : cfg_(cfg), d_(d), L_(L) {
   if (cfg_.token_mode) fail(-10, "token-baseline mode is served by TokenContext (kvc_create dispatches on cfg.token_mode)");
   if (cfg_.kv_dtype != KVC_DTYPE_F32 && cfg_.kv_dtype != KVC_DTYPE_BF16) fail(-10, "kv_dtype");
   // (<= 64: a window page's dedup mask is one 64-bit word of its attention descriptor)
-  if (cfg_.page_tokens < 8 || cfg_.page_tokens > 64 || cfg_.page_tokens % 8) fail(-10, "page_tokens must be 8..64, a multiple of 8");
+  if (cfg_.page_tokens != 0 && (cfg_.page_tokens < 8 || cfg_.page_tokens > 64 || cfg_.page_tokens % 8))
+    fail(-10, "page_tokens must be 0 (auto) or 8..64, a multiple of 8");
   if (cfg_.max_candidates < 1 || cfg_.max_candidates > 6144)
     fail(-10, "max_candidates must be 1..6144 (the ingest top-M keeps 8 candidate rows in shared memory)");
   if (d % 8 != 0 || d > 256) fail(-10, "the device path supports d % 8 == 0 and d <= 256");
@@ -80,6 +81,16 @@ Context::Context(const kvc_cfg& cfg, int d, int L) : cfg_(cfg), d_(d), L_(L) {
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
     fail(-22, "no CUDA device: the B200 path has no CPU fallback");
   es_ = cfg_.kv_dtype == KVC_DTYPE_BF16 ? 2 : 4;
+  if (cfg_.page_tokens == 0) cfg_.page_tokens = auto_page_tokens(d, cfg_.kv_dtype == KVC_DTYPE_BF16);
+  if (d == 32 || d == 64 || d == 128 || d == 256) {
+    // K6 stages whole pages (K + V) in shared memory: e.g. fp32, d = 256, 64-token pages needs
+    // 2 x 128 KB, more than a CTA can have -- reject here instead of failing every decode step
+    const std::size_t att = attend_smem_bytes(d, cfg_.page_tokens, cfg_.kv_dtype == KVC_DTYPE_BF16);
+    if (att > static_cast<std::size_t>(device_smem_optin()))
+      fail(-10, "page_tokens * d * sizeof(kv) too large for the attention kernel's shared-memory ring (" +
+                    std::to_string(att) + " B > " + std::to_string(device_smem_optin()) +
+                    " B per CTA): use a smaller page_tokens");
+  }
   KVC_CUDA(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
   for (auto& e : ev_) KVC_CUDA(cudaEventCreate(&e));
   alloc_device();
@@ -506,6 +517,8 @@ void Context::check_err_word(std::int32_t e) {
   if (e & DERR_CANDIDATES) fail(-21, "more candidates than max_candidates");
   if (e & DERR_ITEMS) fail(-21, "attention work list overflow");
   if (e & DERR_TIER) fail(-11, "host-tier page outside its cluster's extent");
+  if (e & DERR_TAKE)
+    fail(-21, "more than 64 ranked clusters per domain (min(k_s, candidates) and min(prefetch_k, candidates) must be <= 64)");
   fail(-1, "device error");
 }
 

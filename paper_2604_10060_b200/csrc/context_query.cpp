@@ -78,7 +78,11 @@ void Context::launch_step(int b, const float* q, int q_mem, float* out, int out_
   da_.q = dq;
   da_.out = (out && out_mem == KVC_MEM_DEVICE) ? out : (out_map ? out_map : d_out_);
   da_.n_parts_host = static_cast<std::int32_t>(parts_.size());
-  launches_ += launch_decode(t_, da_, st_, timing_ ? evb_[b] : nullptr, ev_k4_[b]);
+  const int nl = launch_decode(t_, da_, st_, timing_ ? evb_[b] : nullptr, ev_k4_[b]);
+  if (nl < 2)
+    fail(-20, "decode kernels could not be launched for d = " + std::to_string(d_) +
+                  " (attention is instantiated for d in {32, 64, 128, 256}; or a shared-memory opt-in was refused)");
+  launches_ += nl;
   KVC_CUDA(cudaGetLastError());  // launch-configuration failures surface here, not as empty results
   // the result block goes to the host on the copy stream as soon as K4 is done (overlaps K6)
   KVC_CUDA(cudaStreamWaitEvent(cs_, ev_k4_[b], 0));
@@ -483,7 +487,11 @@ std::vector<std::pair<std::int64_t, int>> Context::flat_topk(const float* q, int
   KVC_CUDA(cudaMemcpyAsync(d_idx_, h_idx_, static_cast<std::size_t>(n) * 8, cudaMemcpyHostToDevice, st_));
   KVC_CUDA(cudaMemcpyAsync(d_q_, q, d_ * 4, cudaMemcpyHostToDevice, st_));
   std::int32_t* d_out = d_idx_ + 2 * n;
-  launches_ += launch_flat_topk(t_, d_q_, d_idx_, reinterpret_cast<std::uint8_t*>(d_idx_ + n), n, k, d_out, st_);
+  auto* gs = static_cast<std::uint8_t*>(dalloc_scratch(static_cast<std::size_t>(n) * 17 + 16));
+  const int nl = launch_flat_topk(t_, d_q_, d_idx_, reinterpret_cast<std::uint8_t*>(d_idx_ + n), n, k, d_out, gs, st_);
+  if (nl == 0) fail(-20, "flat top-k kernel could not be launched");
+  launches_ += nl;
+  KVC_CUDA(cudaGetLastError());
   const int take = std::min(n, k);
   std::vector<std::int32_t> order(static_cast<std::size_t>(take));
   KVC_CUDA(cudaMemcpyAsync(order.data(), d_out, take * 4, cudaMemcpyDeviceToHost, st_));

@@ -1371,13 +1371,15 @@ __device__ void block_topk(double* sim, long long* key, int* pay, int n, int tak
   __syncthreads();
 }
 
-constexpr int K4_ROWS = 128;  // representative rows staged per chunk
+constexpr int K4_ROWS = 128;  // representative rows staged per chunk (d <= 128)
+// fp64 rows the stage buffer holds: 128 up to d = 128, 48 for wider rows (d = 256: 98 KB)
+__host__ __device__ inline int k4_stage_rows(int d) { return d <= 128 ? K4_ROWS : 48; }
 constexpr float kScoreMargin = 1e-4f;  // bound on |fp32 mirror cosine - exact fp64 cosine|
 
 __host__ __device__ inline size_t k4_smem_bytes(int d, int cmax, int parts, int W, int tmax) {
   const int nsel = cmax > parts ? cmax : parts;
   return static_cast<size_t>(d + 1) * 8 + static_cast<size_t>(nsel) * 24 + static_cast<size_t>(cmax) * 5 +
-         static_cast<size_t>(K4_ROWS) * (d + 1) * 8 + static_cast<size_t>(W) * tmax * 4 + 256;
+         static_cast<size_t>(k4_stage_rows(d)) * (d + 1) * 8 + static_cast<size_t>(W) * tmax * 4 + 256;
 }
 
 __global__ void __launch_bounds__(256) k_score_select(DevTables t, DecodeArgs a, int* work_ctr) {
@@ -1398,8 +1400,9 @@ __global__ void __launch_bounds__(256) k_score_select(DevTables t, DecodeArgs a,
   float* approx = reinterpret_cast<float*>(p);  // approximate candidate scores
   p += static_cast<size_t>(nsel) * 4;
   p = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 15) & ~static_cast<uintptr_t>(15));
-  double* stage = reinterpret_cast<double*>(p);  // [K4_ROWS][d+1] (16-byte aligned for cp.async)
-  p += static_cast<size_t>(K4_ROWS) * DS * 8;
+  const int SR = k4_stage_rows(d);
+  double* stage = reinterpret_cast<double*>(p);  // [SR][d+1] (16-byte aligned for cp.async)
+  p += static_cast<size_t>(SR) * DS * 8;
   int* owners = reinterpret_cast<int*>(p);  // [W][tmax] ring owners of this domain
   p += static_cast<size_t>(t.W) * t.tmax * 4;
   int* cslot = reinterpret_cast<int*>(p);
@@ -1463,8 +1466,8 @@ __global__ void __launch_bounds__(256) k_score_select(DevTables t, DecodeArgs a,
   if (nq < 1e-12 && threadIdx.x == 0) degen = true;
   K4MARK(0)
   // ---- stage 1: visual_topk (index.cpp:192-208): exact cosines, order (sim desc, id asc)
-  for (int p0 = 0; p0 < P; p0 += K4_ROWS) {
-    const int rows = min(K4_ROWS, P - p0);
+  for (int p0 = 0; p0 < P; p0 += SR) {
+    const int rows = min(SR, P - p0);
     for (int r = threadIdx.x >> 5; r < rows; r += blockDim.x >> 5) {
       const double* src = t.vrep + static_cast<int64_t>(p0 + r) * d;
       for (int i = threadIdx.x & 31; i < d; i += 32)
@@ -1524,12 +1527,16 @@ __global__ void __launch_bounds__(256) k_score_select(DevTables t, DecodeArgs a,
     __syncthreads();
     const int nc = min(ncand_s, cmax);
     if (pass == 0 && threadIdx.x == 0) a.n_cand[l] = nc;
-    const int take = min(ktake, nc);
+    int take = min(ktake, nc);
+    if (take > 64) {  // ranked lists live in 64-entry shared arrays
+      if (threadIdx.x == 0) set_err(t, DERR_TAKE);
+      take = 64;
+    }
     // (A) approximate cosines from the fp32 mirrors: rows staged with 16-byte async copies, one
     //     thread per candidate reading its row in a rotated order (conflict-free banks)
     float* st32 = reinterpret_cast<float*>(stage);  // [rows][d + 4]
     const int DS32 = d + 4;
-    const int rows32 = min(nc, (2 * K4_ROWS * DS) / DS32);  // what the fp64 stage buffer holds
+    const int rows32 = min(nc, (2 * SR * DS) / DS32);  // what the fp64 stage buffer holds
     for (int c0 = 0; c0 < nc; c0 += rows32) {
       const int rows = min(rows32, nc - c0);
       for (int r = threadIdx.x >> 5; r < rows; r += blockDim.x >> 5) {
@@ -1578,18 +1585,46 @@ __global__ void __launch_bounds__(256) k_score_select(DevTables t, DecodeArgs a,
       for (int c = threadIdx.x; c < nc; c += blockDim.x)
         if (approx[c] >= thr) {
           const int k = atomicAdd(&n_s, 1);
-          if (k < K4_ROWS) sset[k] = c;
-          else set_err(t, DERR_CANDIDATES);
+          if (k < SR) sset[k] = c;
         }
     } else {
       for (int c = threadIdx.x; c < nc; c += blockDim.x) {
         const int k = atomicAdd(&n_s, 1);
-        if (k < K4_ROWS) sset[k] = c;
-        else set_err(t, DERR_CANDIDATES);
+        if (k < SR) sset[k] = c;
       }
     }
     __syncthreads();
-    const int ns_ = min(n_s, K4_ROWS);
+    if (n_s > SR) {
+      // Near-tie-heavy query (rare): S exceeds the stage. Exact cosines of EVERY candidate, SR rows
+      // at a time, into sim[] (free after the threshold pass), then the exact top-`take` over all
+      // of them -- the reference ranks any number of ties (index.cpp:210-240).
+      for (int c0 = 0; c0 < nc; c0 += SR) {
+        const int rows = min(SR, nc - c0);
+        for (int r = threadIdx.x >> 5; r < rows; r += blockDim.x >> 5) {
+          const double* src = (cbuf[c0 + r] ? t.brep64 : t.rep64) + static_cast<int64_t>(cslot[c0 + r]) * d;
+          for (int i = threadIdx.x & 31; i < d; i += 32)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(stage + r * DS + i)), "l"(src + i)
+                         : "memory");
+        }
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        __syncthreads();
+        for (int r = threadIdx.x; r < rows; r += blockDim.x) {
+          const int c = c0 + r;
+          const int s = cslot[c];
+          const bool ib = cbuf[c];
+          const double* row = stage + r * DS;
+          double acc = 0.0;
+#pragma unroll 16
+          for (int i = 0; i < d; ++i) acc = dadd(acc, dmul(qd[i], row[i]));
+          sim[c] = clamp1(ddiv(acc, dmul(nq, ib ? t.bnorm[s] : t.rnorm[s])));
+          key[c] = 2LL * t.cid[s] + (ib ? 1 : 0);
+        }
+        __syncthreads();
+      }
+      block_rank_select(sim, key, nc, take, order);  // order[] = candidate indices
+      __syncthreads();
+    } else {
+    const int ns_ = n_s;
     // (C) exact cosines (vecmath.hpp:54-61) for S: fp64 rows staged with 8-byte async copies,
     //     one sequential chain per candidate; exact top-`take` of S by rank counting
     for (int r = threadIdx.x >> 5; r < ns_; r += blockDim.x >> 5) {
@@ -1617,6 +1652,7 @@ __global__ void __launch_bounds__(256) k_score_select(DevTables t, DecodeArgs a,
     block_rank_select(ssim, skey, ns_, take, order);
     if (threadIdx.x < take) order[threadIdx.x] = sset[order[threadIdx.x]];
     __syncthreads();
+    }
     K4MARK(3)
     if (threadIdx.x < take) {
       const int b = order[threadIdx.x];
@@ -1813,489 +1849,6 @@ __device__ void block_kth_value(const float* v, const long long* key, int n, int
     if (i < n && part == 0 && r == kth) *out = vi;
   }
   __syncthreads();
-}
-
-// ============================================================================ K4 (v2)
-// Same contract as k_score_select with the latency structure of a 512-thread block: every phase
-// issues its global loads in register batches (no staging of the whole candidate set), the
-// approximate scores are warp dot products over coalesced fp32 mirror rows, exact fp64 re-scores
-// run one sequential chain per boundary candidate over warp-staged rows, and the window dedup
-// uses a shared hash set of the verified slots.
-constexpr int K4T = 512;
-constexpr int K4W = K4T / 32;
-constexpr int K4_SROWS = 32;  // fp64 rows staged per exact-rescore chunk
-constexpr int K4_SMAX = 256;  // boundary-set capacity
-
-__host__ __device__ inline size_t k4v2_smem_bytes(int d, int cmax, int parts, int W, int tmax) {
-  const int nsel = cmax > parts ? cmax : parts;
-  return static_cast<size_t>(d) * 12 + static_cast<size_t>(nsel) * 24 + static_cast<size_t>(cmax) * 5 +
-         static_cast<size_t>(K4_SROWS) * (d + 1) * 8 + static_cast<size_t>(W) * tmax * 4 + 256;
-}
-
-__global__ void __launch_bounds__(K4T) k_score_select2(DevTables t, DecodeArgs a, int* work_ctr) {
-  extern __shared__ __align__(16) uint8_t sm4[];
-  const int l = blockIdx.x, d = t.d, L = t.L, DS = d + 1;
-  const int P = a.n_parts_host;
-  const int cmax = t.cmax;
-  const int nsel = cmax > P ? cmax : P;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  uint8_t* p = sm4;
-  double* stage = reinterpret_cast<double*>(p);  // [K4_SROWS][d+1]
-  p += static_cast<size_t>(K4_SROWS) * DS * 8;
-  double* qd = reinterpret_cast<double*>(p);
-  p += static_cast<size_t>(d) * 8;
-  double* sim = reinterpret_cast<double*>(p);
-  p += static_cast<size_t>(nsel) * 8;
-  long long* key = reinterpret_cast<long long*>(p);
-  p += static_cast<size_t>(nsel) * 8;
-  float* qf = reinterpret_cast<float*>(p);
-  p += static_cast<size_t>(d) * 4;
-  int* pay = reinterpret_cast<int*>(p);
-  p += static_cast<size_t>(nsel) * 4;
-  float* approx = reinterpret_cast<float*>(p);
-  p += static_cast<size_t>(nsel) * 4;
-  int* owners = reinterpret_cast<int*>(p);  // [W][tmax]
-  p += static_cast<size_t>(t.W) * t.tmax * 4;
-  int* cslot = reinterpret_cast<int*>(p);
-  p += static_cast<size_t>(cmax) * 4;
-  uint8_t* cbuf = p;
-  __shared__ double nq_s;
-  __shared__ float nq32_s;
-  __shared__ int ncand_s, chosen[64];
-  __shared__ int vers[64], nver_s;
-  __shared__ int rank_slot[64], n_rank_s, order[64];
-  __shared__ unsigned long long att_s;
-  __shared__ int lazy_any;
-  __shared__ bool degen;
-  __shared__ int ring_count_s[64];
-  __shared__ int sset[K4_SMAX], n_s;
-  __shared__ double ssim[K4_SMAX];
-  __shared__ long long skey[K4_SMAX];
-  __shared__ int vhash[128];
-  __shared__ float red32[K4W];
-  __shared__ int red_i[32];
-  __shared__ float kth_s;
-
-  long long kc0 = clock64();
-#define K4MARK(k) if (a.k4prof && tid == 0) { const long long kc1 = clock64(); a.k4prof[l * 16 + (k)] = kc1 - kc0; kc0 = kc1; }
-  if (l == 0 && tid == 0) *work_ctr = 0;
-  const float* q = (a.q_src ? a.q_src : a.q) + static_cast<int64_t>(l) * d;
-  float qsq = 0.f;
-  for (int i = tid; i < d; i += K4T) {
-    const float x = q[i];
-    if (a.q_src) const_cast<float*>(a.q)[static_cast<int64_t>(l) * d + i] = x;
-    qd[i] = static_cast<double>(x);
-    qf[i] = x;
-    qsq += x * x;
-  }
-  {  // window ring owners of this domain (needed after ranking), all loads in flight together
-    const int n_own = t.W * t.tmax;
-    const int* src = t.ring_owner + static_cast<int64_t>(l) * n_own;
-    int v[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int i = tid + K4T * j;
-      v[j] = i < n_own ? src[i] : -1;
-    }
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int i = tid + K4T * j;
-      if (i < n_own) owners[i] = v[j];
-    }
-    for (int i = tid + K4T * 4; i < n_own; i += K4T) owners[i] = src[i];
-  }
-  if (tid == 0) {
-    degen = false;
-    att_s = 0;
-    lazy_any = 0;
-  }
-  if (tid < t.W && tid < 64) ring_count_s[tid] = t.ring_count[tid];
-  if (tid < 128) vhash[tid] = -1;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) qsq += __shfl_xor_sync(kFull, qsq, o);
-  if (lane == 0) red32[warp] = qsq;
-  __syncthreads();
-  if (warp == 0) {  // exact |q| (vecmath.hpp:35-40) by lane 0; fp32 |q| for the approximate scale
-    float s32 = lane < K4W ? red32[lane] : 0.f;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s32 += __shfl_xor_sync(kFull, s32, o);
-    if (lane == 0) {
-      double s = 0.0;
-#pragma unroll 16
-      for (int i = 0; i < d; ++i) s = dadd(s, dmul(qd[i], qd[i]));
-      nq_s = __dsqrt_rn(s);
-      nq32_s = sqrtf(s32);
-    }
-  }
-  __syncthreads();
-  const double nq = nq_s;
-  const float nq32 = nq32_s;
-  if (nq < 1e-12 && tid == 0) degen = true;
-  K4MARK(0)
-
-  // exact cosines of q with up to K4_SROWS fp64 rows (warp-staged), one chain per row
-  auto exact_rows = [&](auto row_ptr, auto row_norm, int rows, double* out_sim) {
-    for (int r = warp; r < rows; r += K4W) {
-      const double* src = row_ptr(r);
-      for (int i = lane; i < d; i += 32) stage[r * DS + i] = __ldg(src + i);
-    }
-    __syncthreads();
-    for (int r = tid; r < rows; r += K4T) {
-      const double* row = stage + r * DS;
-      double acc = 0.0;
-#pragma unroll 16
-      for (int i = 0; i < d; ++i) acc = dadd(acc, dmul(qd[i], row[i]));  // exact_cos order
-      const double nr = row_norm(r);
-      if (nr < 1e-12) degen = true;
-      out_sim[r] = clamp1(ddiv(acc, dmul(nq, nr)));
-    }
-    __syncthreads();
-  };
-
-  // ---- stage 1: visual_topk (index.cpp:192-208): exact cosines, order (sim desc, id asc)
-  for (int p0 = 0; p0 < P; p0 += K4_SROWS) {
-    const int rows = min(K4_SROWS, P - p0);
-    exact_rows([&](int r) { return t.vrep + static_cast<int64_t>(p0 + r) * d; },
-               [&](int r) { return t.vnorm[p0 + r]; }, rows, sim + p0);
-    for (int r = tid; r < rows; r += K4T) key[p0 + r] = p0 + r;
-  }
-  __syncthreads();
-  const int kv = min(a.k_v, P);
-  if (P <= 256 || P > 1024)  // rank counting: one barrier, P^2 / 512 broadcast reads per thread
-    block_rank_select(sim, key, P, kv, chosen);
-  else
-    block_topk(sim, key, pay, P, kv, chosen);
-  if (tid < kv) a.parts[l * a.k_v + tid] = chosen[tid];
-  if (tid == 0) a.n_parts_sel[l] = kv;
-  K4MARK(1)
-
-  // ---- stage 2: semantic_topk (index.cpp:210-240) and the prefetch ranking of layer l+1
-  const int passes = (a.prefetch && l + 1 < L) ? 2 : 1;
-  for (int pass = 0; pass < passes; ++pass) {
-    const int layer = l + pass;
-    const int ktake = pass == 0 ? a.k_s : a.prefetch_k;
-    // candidate list in per_layer_clusters order (live entry, then its registered buffer):
-    // compacted with a block scan (no per-candidate shared atomics)
-    int ncand = 0;
-    for (int i = 0; i < kv; ++i) {
-      const int64_t pk = static_cast<int64_t>(chosen[i]) * L + layer;
-      const int off = t.pl_off[pk], cnt = t.pl_cnt[pk];
-      for (int j0 = 0; j0 < cnt; j0 += K4T) {
-        const int j = j0 + tid;
-        const int s = j < cnt ? t.pl_pool[off + j] : -1;
-        const int lz = s >= 0 ? t.lazy[s] : 0;
-        int tot;
-        const int k = ncand + block_excl_scan(s >= 0 ? (lz ? 2 : 1) : 0, red_i, &tot);
-        if (s >= 0) {
-          if (k + (lz ? 2 : 1) > cmax) {
-            set_err(t, DERR_CANDIDATES);
-          } else {
-            cslot[k] = s;
-            cbuf[k] = 0;
-            if (lz) {
-              cslot[k + 1] = s;
-              cbuf[k + 1] = 1;
-            }
-          }
-        }
-        ncand += tot;
-        __syncthreads();  // red_i reuse
-      }
-    }
-    __syncthreads();
-    const int nc = min(ncand, cmax);
-    if (pass == 0 && tid == 0) a.n_cand[l] = nc;
-    const int take = min(ktake, nc);
-    // (A) approximate cosines: warp dot products over coalesced fp32 mirror rows, CB rows of a
-    //     warp in flight together
-    {
-      constexpr int CB = 8;
-      const int nv4 = d >> 2;  // float4 per row (<= 32: d <= 128)
-      const float4 qv = lane < nv4 ? reinterpret_cast<const float4*>(qf)[lane] : make_float4(0.f, 0.f, 0.f, 0.f);
-      for (int c0 = warp * CB; c0 < nc; c0 += K4W * CB) {
-        float4 rv[CB];
-        double nr[CB];
-        long long cid[CB];
-#pragma unroll
-        for (int b = 0; b < CB; ++b) {
-          const int c = c0 + b;
-          nr[b] = 1.0;
-          cid[b] = 0;
-          rv[b] = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (c < nc) {
-            const int s = cslot[c];
-            const bool ib = cbuf[c];
-            const float4* src = reinterpret_cast<const float4*>((ib ? t.brep32 : t.rep32) + static_cast<int64_t>(s) * d);
-            if (lane < nv4) rv[b] = __ldg(src + lane);
-            nr[b] = ib ? t.bnorm[s] : t.rnorm[s];
-            cid[b] = t.cid[s];
-          }
-        }
-        float acc[CB];
-#pragma unroll
-        for (int b = 0; b < CB; ++b) {
-          acc[b] = qv.x * rv[b].x;
-          acc[b] = fmaf(qv.y, rv[b].y, acc[b]);
-          acc[b] = fmaf(qv.z, rv[b].z, acc[b]);
-          acc[b] = fmaf(qv.w, rv[b].w, acc[b]);
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-          for (int b = 0; b < CB; ++b) acc[b] += __shfl_xor_sync(kFull, acc[b], o);
-        if (lane < CB) {
-          float mine = acc[0];
-          double mnr = nr[0];
-          long long mcid = cid[0];
-#pragma unroll
-          for (int b = 1; b < CB; ++b)
-            if (lane == b) {
-              mine = acc[b];
-              mnr = nr[b];
-              mcid = cid[b];
-            }
-          const int c = c0 + lane;
-          if (c < nc) {
-            if (mnr < 1e-12) degen = true;
-            const float sa = mine / (nq32 * static_cast<float>(mnr));
-            approx[c] = sa;
-            sim[c] = static_cast<double>(sa);
-            key[c] = 2LL * mcid + (cbuf[c] ? 1 : 0);
-          }
-        }
-      }
-    }
-    __syncthreads();
-    K4MARK(2)
-    // (B) the set S of candidates that can reach the exact top-`take`: approximate score within
-    //     2*margin of the take-th best approximate score (|approx - exact| <= margin)
-    if (tid == 0) n_s = 0;
-    __syncthreads();
-    if (pass == 0) K4MARK(8)
-    if (take > 0 && take < nc) {
-      block_kth_value(approx, key, nc, take - 1, &kth_s);
-      if (pass == 0) K4MARK(9)
-      const float thr = kth_s - 2.f * kScoreMargin;
-      for (int c = tid; c < nc; c += K4T)
-        if (approx[c] >= thr) {
-          const int k = atomicAdd(&n_s, 1);
-          if (k < K4_SMAX) sset[k] = c;
-          else set_err(t, DERR_CANDIDATES);
-        }
-    } else {
-      for (int c = tid; c < nc; c += K4T) {
-        const int k = atomicAdd(&n_s, 1);
-        if (k < K4_SMAX) sset[k] = c;
-        else set_err(t, DERR_CANDIDATES);
-      }
-    }
-    __syncthreads();
-    const int ns_ = min(n_s, K4_SMAX);
-    if (a.k4prof && tid == 0 && pass == 0) a.k4prof[l * 16 + 7] = ns_;  // boundary-set size (instrumentation)
-    if (pass == 0) K4MARK(10)
-    // (C) exact cosines (vecmath.hpp:54-61) of S; exact top-`take` of S by rank counting
-    for (int r0 = 0; r0 < ns_; r0 += K4_SROWS) {
-      const int rows = min(K4_SROWS, ns_ - r0);
-      exact_rows(
-          [&](int r) {
-            const int c = sset[r0 + r];
-            return (cbuf[c] ? t.brep64 : t.rep64) + static_cast<int64_t>(cslot[c]) * d;
-          },
-          [&](int r) {
-            const int c = sset[r0 + r];
-            return cbuf[c] ? t.bnorm[cslot[c]] : t.rnorm[cslot[c]];
-          },
-          rows, ssim + r0);
-      for (int r = tid; r < rows; r += K4T) {
-        const int c = sset[r0 + r];
-        skey[r0 + r] = key[c];
-      }
-    }
-    __syncthreads();
-    if (pass == 0) K4MARK(11)
-    block_rank_select(ssim, skey, ns_, take, order);
-    if (tid < take) order[tid] = sset[order[tid]];
-    __syncthreads();
-    K4MARK(3)
-    if (tid < take) {
-      const int b = order[tid];
-      if (pass == 0) {
-        rank_slot[tid] = cslot[b];
-        a.ranked_slot[l * a.k_s + tid] = cslot[b];
-        a.ranked_buf[l * a.k_s + tid] = cbuf[b];
-      } else {
-        a.pf_slot[l * a.prefetch_k + tid] = cslot[b];
-        a.pf_buf[l * a.prefetch_k + tid] = cbuf[b];
-      }
-    }
-    if (tid == 0) {
-      if (pass == 0) {
-        a.n_ranked[l] = take;
-        n_rank_s = take;
-      } else {
-        a.n_pf[l] = take;
-      }
-    }
-    __syncthreads();
-  }
-  if (passes == 1 && tid == 0) a.n_pf[l] = 0;
-  if (degen && tid == 0) set_err(t, DERR_DEGENERATE);
-
-  // ---- verified (dedup in rank order, retrieval.cpp:20-26), attended count, page descriptors
-  __shared__ int vnp[64], vnbp[64], voff[65];
-  __shared__ int ring_cnt[64], ring_off[65];
-  __shared__ unsigned long long ring_mask[64];
-  if (warp == 0) {  // dedup: lane i keeps rank i unless an earlier rank has the same slot
-    const int nr_ = n_rank_s;
-    int s0 = lane < nr_ ? rank_slot[lane] : -1, s1 = lane + 32 < nr_ ? rank_slot[lane + 32] : -1;
-    bool k0 = s0 >= 0, k1 = s1 >= 0;
-    for (int j = 0; j < nr_; ++j) {
-      const int sj = rank_slot[j];
-      if (j < lane && sj == s0) k0 = false;
-      if (j < lane + 32 && sj == s1) k1 = false;
-    }
-    const unsigned m0 = __ballot_sync(kFull, k0), m1 = __ballot_sync(kFull, k1);
-    const unsigned lt = (1u << lane) - 1u;
-    if (k0) vers[__popc(m0 & lt)] = s0;
-    if (k1) vers[__popc(m0) + __popc(m1 & lt)] = s1;
-    if (lane == 0) {
-      nver_s = __popc(m0) + __popc(m1);
-      a.n_ver[l] = nver_s;
-    }
-  }
-  __syncthreads();
-  const int nv = nver_s;
-  const int W = t.W, rpp = t.rpp;
-  if (tid < nv) {  // per verified cluster: counts (parallel global loads), hash-set entry
-    const int s = vers[tid];
-    a.ver_slot[l * a.k_s + tid] = s;
-    vnp[tid] = t.npages[s];
-    vnbp[tid] = t.nbpages[s];
-    atomicAdd(&att_s, static_cast<unsigned long long>(t.nmem[s] + t.nbuf[s]));
-    if (t.lazy[s]) lazy_any = 1;  // a pending split: the host must settle before the next step
-    int h = (s * 0x9E3779B1u) >> 25;      // 128-entry open-addressing set
-    while (atomicCAS(&vhash[h], -1, s) != -1) h = (h + 1) & 127;
-  }
-  if (tid < 64) {
-    ring_cnt[tid] = 0;
-    ring_mask[tid] = 0ull;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) a.flags[l] = lazy_any;
-  K4MARK(4)
-  // window ring: tokens whose owner is not a verified cluster (retrieval.cpp:107-108 dedup)
-  {
-    unsigned long long mine = 0;
-    const int n_ring = W * t.tmax;
-    const int n_pad = (n_ring + K4T - 1) / K4T * K4T;  // warp-uniform trip count
-    for (int i = tid; i < n_pad; i += K4T) {
-      const int rs = i / t.tmax, tt = i - rs * t.tmax;
-      bool keep = i < n_ring && tt < ring_count_s[rs];
-      if (keep) {
-        const int own = owners[i];
-        if (own >= 0) {
-          int h = (own * 0x9E3779B1u) >> 25;
-          for (;;) {
-            const int v = vhash[h];
-            if (v == own) {
-              keep = false;
-              break;
-            }
-            if (v < 0) break;
-            h = (h + 1) & 127;
-          }
-        }
-      }
-      const int pg = keep ? rs * rpp + tt / t.P : -1;
-      const unsigned km = __ballot_sync(kFull, keep);
-      mine += keep ? 1 : 0;
-      if (km) {
-        const unsigned same = __match_any_sync(kFull, pg);
-        if (keep && pg < 64 && lane == __ffs(same) - 1) atomicAdd(&ring_cnt[pg], __popc(same));
-        const unsigned long long bit = keep ? 1ull << (tt % t.P) : 0ull;  // one shared atomic per (warp, page)
-        const unsigned blo = __reduce_or_sync(same, static_cast<unsigned>(bit));
-        const unsigned bhi = __reduce_or_sync(same, static_cast<unsigned>(bit >> 32));
-        if (keep && pg < 64 && (threadIdx.x & 31) == __ffs(same) - 1)
-          atomicOr(&ring_mask[pg], (static_cast<unsigned long long>(bhi) << 32) | blo);
-      }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(kFull, mine, o);
-    if (lane == 0) atomicAdd(&att_s, mine);
-  }
-  __syncthreads();
-  if (warp == 0) {  // descriptor offsets: verified clusters' pages, then non-empty ring pages
-    const int cnt0 = lane < nv ? vnp[lane] + vnbp[lane] : 0;
-    const int cnt1 = lane + 32 < nv ? vnp[lane + 32] + vnbp[lane + 32] : 0;
-    int x0 = cnt0, x1 = cnt1;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y0 = __shfl_up_sync(kFull, x0, o), y1 = __shfl_up_sync(kFull, x1, o);
-      if (lane >= o) {
-        x0 += y0;
-        x1 += y1;
-      }
-    }
-    const int tot0 = __shfl_sync(kFull, x0, 31);
-    if (lane < nv) voff[lane] = x0 - cnt0;
-    if (lane + 32 < nv) voff[lane + 32] = tot0 + x1 - cnt1;
-    const int vtot = tot0 + __shfl_sync(kFull, x1, 31);
-    if (lane == 0) voff[nv] = vtot;
-    const int nrp = min(W * rpp, 64);
-    const int r0 = lane < nrp && ring_cnt[lane] > 0 ? 1 : 0, r1 = lane + 32 < nrp && ring_cnt[lane + 32] > 0 ? 1 : 0;
-    const unsigned rm0 = __ballot_sync(kFull, r0), rm1 = __ballot_sync(kFull, r1);
-    const unsigned lt = (1u << lane) - 1u;
-    if (lane < nrp) ring_off[lane] = vtot + __popc(rm0 & lt);
-    if (lane + 32 < nrp) ring_off[lane + 32] = vtot + __popc(rm0) + __popc(rm1 & lt);
-    int o = vtot + __popc(rm0) + __popc(rm1);
-    if (lane == 0) {
-      ring_off[nrp] = o;
-      if (o > a.max_desc) {
-        set_err(t, DERR_ITEMS);
-        o = a.max_desc;
-      }
-      a.n_desc[l] = o;
-      a.n_items[l] = (o + a.chunk_pages - 1) / a.chunk_pages;
-      a.attended[l] = static_cast<int64_t>(att_s);
-    }
-  }
-  __syncthreads();
-  K4MARK(5)
-  int4* desc = a.desc + static_cast<int64_t>(l) * a.max_desc;
-  const int ndesc = voff[nv];
-  for (int i = tid; i < ndesc && i < a.max_desc; i += K4T) {
-    int lo = 0, hi = nv - 1;  // the verified cluster whose page range holds i
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (voff[mid] <= i) lo = mid; else hi = mid - 1;
-    }
-    const int j = lo;
-    const int s = vers[j];
-    const int k = i - voff[j];
-    const bool isb = k >= vnp[j];
-    const int page = isb ? t.bpages[static_cast<int64_t>(s) * t.maxbp + (k - vnp[j])]
-                         : t.pages[static_cast<int64_t>(s) * t.maxp + k];
-    desc[i] = make_int4(page, t.pg_fill[page] | ((isb ? 1 : 0) << 16), -1, -1);
-  }
-  for (int i = tid; i < W * rpp && i < 64; i += K4T)
-    if (ring_cnt[i] > 0 && ring_off[i] < a.max_desc) {
-      const int rs = i / rpp, j = i % rpp;
-      const int page = t.ring_pages[(static_cast<int64_t>(l) * W + rs) * rpp + j];
-      desc[ring_off[i]] = make_int4(page, t.pg_fill[page] | (2 << 16), static_cast<int>(ring_mask[i] & 0xffffffffu),
-                                    static_cast<int>(ring_mask[i] >> 32));
-    }
-  __syncthreads();
-  K4MARK(6)
-#undef K4MARK
-  if (threadIdx.x == 0) {  // errors raised so far (this block's own are ordered before the read)
-    __threadfence();
-    a.errw[l] = atomicOr(t.err, 0);
-  }
-  if (a.n_items[l] == 0)  // nothing attended: output zeros
-    for (int i = tid; i < d; i += K4T) {
-      a.out[static_cast<int64_t>(l) * d + i] = 0.f;
-      for (int r = 0; r < a.peer.n; ++r) a.peer.out[r][static_cast<int64_t>(a.peer.dom_offset + l) * d + i] = 0.f;
-    }
 }
 
 // ============================================================================ K6
@@ -2634,11 +2187,13 @@ __global__ void __launch_bounds__(ATT_THREADS + 32) k_attend(DevTables t, Decode
   }
 }
 
-// flat top-k over an explicit candidate list (one CTA)
+// flat top-k over an explicit candidate list (one CTA). The (sim, key, taken) arrays live in
+// shared memory when they fit, else in the caller's global scratch (`gscratch`, n * 17 bytes).
 __global__ void __launch_bounds__(256) k_flat_topk(DevTables t, const float* q, const int32_t* slots,
-                                                   const uint8_t* bufs, int n, int k, int32_t* out) {
+                                                   const uint8_t* bufs, int n, int k, int32_t* out,
+                                                   uint8_t* gscratch) {
   extern __shared__ uint8_t smf[];
-  double* sim = reinterpret_cast<double*>(smf);
+  double* sim = reinterpret_cast<double*>(gscratch ? gscratch : smf);
   long long* key = reinterpret_cast<long long*>(sim + n);
   uint8_t* taken = reinterpret_cast<uint8_t*>(key + n);
   __shared__ double red_s[32];
@@ -2685,11 +2240,7 @@ int launch_build_cands(const DevTables& t, const IngestArgs& a, cudaStream_t st)
 int launch_approx(const DevTables& t, const IngestArgs& a, cudaStream_t st) {
   const int dp = t.d + 1;
   const size_t smem = static_cast<size_t>(AT * dp + AC * dp + AT + AC) * 4;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_approx, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
-  }
+  if (!smem_optin(reinterpret_cast<const void*>(k_approx), smem)) return 0;
   dim3 g((a.T + AT - 1) / AT, a.n_active);
   k_approx<<<g, 256, smem, st>>>(t, a);
   return 1;
@@ -2699,11 +2250,7 @@ int launch_resolve(const DevTables& t, const IngestArgs& a, cudaStream_t st) {
   const size_t smem = static_cast<size_t>(HOT) * 2 * padded(t.d) * 8 + static_cast<size_t>(6) * padded(t.d) * 8 +
                       static_cast<size_t>(t.tmax) * (8 + TOPM * (8 + 4 + 2) + 4) + 16 +
                       static_cast<size_t>(t.cmax) * (8 + 4 + 3) + 64;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_resolve, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
-  }
+  if (!smem_optin(reinterpret_cast<const void*>(k_resolve), smem)) return 0;
   k_resolve<<<a.n_active, 32, smem, st>>>(t, a);
   return 1;
 }
@@ -2715,13 +2262,10 @@ int launch_store_rows(const DevTables& t, const IngestArgs& a, cudaStream_t st) 
 }
 
 int launch_topm(const DevTables& t, const IngestArgs& a, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_topm, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
-  }
+  const size_t smem = static_cast<size_t>(8) * t.cmax * 4;
+  if (!smem_optin(reinterpret_cast<const void*>(k_topm), smem)) return 0;
   dim3 g((a.T + 7) / 8, a.n_active);
-  k_topm<<<g, 256, static_cast<size_t>(8) * t.cmax * 4, st>>>(t, a);
+  k_topm<<<g, 256, smem, st>>>(t, a);
   return 1;
 }
 
@@ -2794,36 +2338,33 @@ int launch_to_f32(const DevTables& t, const void* src, float* dst, int64_t n, cu
 }
 
 int launch_flat_topk(const DevTables& t, const float* q, const int32_t* slots, const uint8_t* bufs,
-                     int32_t n, int32_t k, int32_t* out, cudaStream_t st) {
-  const size_t smem = static_cast<size_t>(n) * 17 + 16;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_flat_topk, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
-  }
-  k_flat_topk<<<1, 256, smem, st>>>(t, q, slots, bufs, n, k, out);
+                     int32_t n, int32_t k, int32_t* out, uint8_t* gscratch, cudaStream_t st) {
+  const size_t bytes = static_cast<size_t>(n) * 17 + 16;
+  const bool in_smem = bytes + 2048 <= static_cast<size_t>(device_smem_optin()) &&
+                       smem_optin(reinterpret_cast<const void*>(k_flat_topk), bytes);
+  if (!in_smem && !gscratch) return 0;
+  k_flat_topk<<<1, 256, in_smem ? bytes : 0, st>>>(t, q, slots, bufs, n, k, out, in_smem ? nullptr : gscratch);
   return 1;
 }
 
 namespace {
-int g_sms = 0;
+int att_stages() {
+  static const int stages = [] {
+    const char* e = getenv("KVC_ATT_STAGES");
+    const int s = e ? atoi(e) : 2;  // 2 stages -> 3 CTAs per SM (latency-bound consumers need the warps)
+    return (s < 2 || s > 4) ? 2 : s;
+  }();
+  return stages;
+}
 
 template <int D, bool BF16, int STAGES>
 int launch_attend_s(const DevTables& t, const DecodeArgs& a, cudaStream_t st, bool pdl) {
   const size_t smem = static_cast<size_t>(STAGES) * (2 * t.P * D * (BF16 ? 2 : 4) + D * 4);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_attend<D, BF16, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(smem));
-    attr = true;
-  }
-  static int per_sm = 0;  // occupancy is a property of the kernel: query once
-  if (!per_sm) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_attend<D, BF16, STAGES>, ATT_THREADS + 32, smem);
-    per_sm = max(1, per_sm);
-  }
+  const void* fn = reinterpret_cast<const void*>(k_attend<D, BF16, STAGES>);
+  if (!smem_optin(fn, smem)) return 0;  // the context constructor rejects such shapes
+  const int per_sm = occupancy(fn, ATT_THREADS + 32, smem);
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(static_cast<unsigned>(g_sms * per_sm));
+  cfg.gridDim = dim3(static_cast<unsigned>(device_sms() * per_sm));
   cfg.blockDim = dim3(ATT_THREADS + 32);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
@@ -2840,12 +2381,7 @@ int launch_attend_s(const DevTables& t, const DecodeArgs& a, cudaStream_t st, bo
 // CTAs per SM beat 3 stages x 2 CTAs, 97 vs 104 us for config 2).
 template <int D, bool BF16>
 int launch_attend_t(const DevTables& t, const DecodeArgs& a, cudaStream_t st, bool pdl) {
-  static int stages = -1;
-  if (stages < 0) {
-    const char* e = getenv("KVC_ATT_STAGES");
-    stages = e ? atoi(e) : 2;  // 2 stages -> 3 CTAs per SM (latency-bound consumers need the warps)
-    if (stages < 2 || stages > 4) stages = 2;
-  }
+  const int stages = att_stages();
   if (stages == 2) return launch_attend_s<D, BF16, 2>(t, a, st, pdl);
   if (stages == 4) return launch_attend_s<D, BF16, 4>(t, a, st, pdl);
   return launch_attend_s<D, BF16, 3>(t, a, st, pdl);
@@ -2888,12 +2424,11 @@ int launch_peer_wait(const unsigned long long* my_flags, int n, unsigned long lo
   return 1;
 }
 
+size_t attend_smem_bytes(int d, int page_tokens, bool bf16) {
+  return static_cast<size_t>(att_stages()) * (2 * static_cast<size_t>(page_tokens) * d * (bf16 ? 2 : 4) + d * 4);
+}
+
 int launch_attend(const DevTables& t, const DecodeArgs& a, cudaStream_t st) {
-  if (!g_sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
-  }
   switch (t.d * 2 + t.kv_bf16) {
     case 64: return launch_attend_t<32, false>(t, a, st, false);
     case 65: return launch_attend_t<32, true>(t, a, st, false);
@@ -2908,27 +2443,18 @@ int launch_attend(const DevTables& t, const DecodeArgs& a, cudaStream_t st) {
 }
 
 int launch_decode(const DevTables& t, const DecodeArgs& a, cudaStream_t st, cudaEvent_t* ev, cudaEvent_t k4_done) {
-  if (!g_sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
-  }
   if (ev) cudaEventRecord(ev[0], st);
-  static int k4v = -1;
-  if (k4v < 0) {
-    const char* e = getenv("KVC_K4");  // "v1": the 256-thread staged variant, "v2": select2
-    k4v = (e && e[0] == 'v' && e[1] == '1') ? 1 : (e && e[0] == 'v' && e[1] == '2') ? 2 : 3;
-    cudaFuncSetAttribute(k_score_select, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-    cudaFuncSetAttribute(k_score_select2, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  }
-  const size_t smem4v2 = k4v2_smem_bytes(t.d, t.cmax, a.n_parts_host, t.W, t.tmax);
+  // K4 v3 (select.cu) whenever the shape fits it (d <= 128, d % 4 == 0, page_tokens % 32 == 0,
+  // lists <= 64); otherwise, or with KVC_K4=v1 (read per step), the general staged variant
+  // k_score_select (any d <= 256, any page size)
+  const char* kv_env = getenv("KVC_K4");
+  const bool force_v1 = kv_env && kv_env[0] == 'v' && kv_env[1] == '1';
   bool used3 = false;
-  if (k4v == 3 && launch_select3(t, a, st)) {
-    used3 = true;  // K4 v3 (select.cu)
-  } else if (k4v >= 2 && t.d % 4 == 0 && t.d <= 128 && t.W <= 64 && smem4v2 <= 200 * 1024) {
-    k_score_select2<<<t.L, K4T, smem4v2, st>>>(t, a, a.work_ctr);
+  if (!force_v1 && launch_select3(t, a, st)) {
+    used3 = true;
   } else {
     const size_t smem4 = k4_smem_bytes(t.d, t.cmax, a.n_parts_host, t.W, t.tmax);
+    if (!smem_optin(reinterpret_cast<const void*>(k_score_select), smem4)) return 0;
     k_score_select<<<t.L, 256, smem4, st>>>(t, a, a.work_ctr);
   }
   // K6 is a programmatic dependent of K4 (PDL: its launch and prologue overlap K4) unless an event

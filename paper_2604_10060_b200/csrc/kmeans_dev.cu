@@ -475,11 +475,7 @@ int launch_kmeans(const float* rows, const KmJob* jobs, int n_jobs, const double
                   int max_iters, double tol, cudaStream_t st) {
   if (n_jobs <= 0) return 0;
   const size_t smem = kmeans_smem_bytes(k_max, d);
-  static size_t set = 0;
-  if (smem > 48 * 1024 && smem > set) {
-    cudaFuncSetAttribute(k_kmeans, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    set = smem;
-  }
+  if (!smem_optin(reinterpret_cast<const void*>(k_kmeans), smem)) return 0;
   k_kmeans<<<n_jobs, KT, smem, st>>>(rows, jobs, uniforms, scratch, assign, meta, objective, reps, vars, d,
                                      max_iters, tol);
   return 1;

@@ -47,6 +47,7 @@ enum DevErr : int32_t {
   DERR_CANDIDATES = 8,  // more candidates than max_candidates
   DERR_ITEMS = 16,      // attention work list overflow
   DERR_TIER = 32,       // a host-tier page outside its cluster's extent
+  DERR_TAKE = 64,       // more than 64 ranked candidates per domain (k_s / prefetch_k x candidates)
 };
 
 // ----------------------------------------------------------------------------- device state
@@ -309,9 +310,10 @@ int launch_exact_stats(const DevTables& t, const AppendRun* runs, int32_t n_runs
                        const int32_t* idx, const void* stage_k, cudaStream_t st);
 
 // Flat top-k (oracle_flat_topk) of one query over an explicit candidate list.
+// gscratch: n * 17 + 16 bytes of global scratch, used when the arrays exceed shared memory
 int launch_flat_topk(const DevTables& t, const float* q, const int32_t* slots,
                      const uint8_t* bufs, int32_t n, int32_t k, int32_t* out_idx,
-                     cudaStream_t st);
+                     uint8_t* gscratch, cudaStream_t st);
 
 // Fresh-slot headers for a batch of clusters: counts, ids, Device residence, no buffer.
 struct SlotHeader {
@@ -348,6 +350,20 @@ int launch_split_two(const float* rows, const int32_t* idx, int n, int d, int fi
                      int32_t* assign, int32_t* meta, double* objective, cudaStream_t st);
 int launch_to_f32(const DevTables& t, const void* src, float* dst, int64_t n_elems,
                   cudaStream_t st);
+
+// launch_util.cu: per-device launch state. smem_optin raises a kernel's dynamic shared-memory
+// attribute on the current device when `bytes` exceeds what was set there (false: the device's
+// opt-in limit is smaller); occupancy is cached per (kernel, device, block, smem).
+int current_device();
+int device_sms();
+int device_smem_optin();
+bool smem_optin(const void* fn, size_t bytes);
+int occupancy(const void* fn, int threads, size_t smem);
+// K6 dynamic shared memory for a context's shape (kernels.cu); kvc::Context rejects shapes whose
+// K6 ring does not fit the device.
+size_t attend_smem_bytes(int d, int page_tokens, bool bf16);
+// kvc_cfg.page_tokens == 0: 64 tokens per page, halved (down to 8) while K6's ring does not fit
+int auto_page_tokens(int d, bool bf16);
 
 #ifdef __CUDACC__
 // Launch as a programmatic dependent of the previous kernel on the stream (its launch and block

@@ -1168,14 +1168,8 @@ int launch_resolve_spec(const DevTables& t, const IngestArgs& a, cudaStream_t st
   if (t.d % 4 != 0 || t.d > 256 || t.tmax > 32767 || t.cmax > 32767) return 0;
   SpecSmem s;
   const size_t smem = spec_carve(nullptr, &s, t.d, t.es, a.T, t.tmax, t.cmax);
-  static int max_optin = 0;
-  if (!max_optin) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    cudaFuncSetAttribute(k_resolve_spec, cudaFuncAttributeMaxDynamicSharedMemorySize, max_optin - 1024);
-  }
-  if (smem > static_cast<size_t>(max_optin - 1024)) return 0;
+  if (smem > static_cast<size_t>(device_smem_optin() - 1024)) return 0;
+  if (!smem_optin(reinterpret_cast<const void*>(k_resolve_spec), smem)) return 0;
   launch_pdl(k_resolve_spec, dim3(a.n_active), dim3(RS_THREADS), smem, st, t, a);
   return 1;
 }

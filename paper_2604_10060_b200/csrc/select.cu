@@ -378,41 +378,39 @@ __global__ void __launch_bounds__(K5T) k_select3(DevTables t, DecodeArgs a, int*
     __syncthreads();
     if (pass == 0) K5MARK(2)
     // boundary set S: candidates fewer than `take` of which beat approx_c by more than 2m
-    {
+    auto in_boundary = [&](int c) -> bool {
+      if (take >= nc) return true;
+      const float thr = approx[c] + 2.f * kMargin3 + 1e-6f;
       const int n4 = (nc + 3) >> 2;
-      for (int c = tid; c < nc; c += K5T) {
-        bool in = true;
-        if (take < nc) {
-          const float thr = approx[c] + 2.f * kMargin3 + 1e-6f;
-          int cnt = 0;
-          const float4* a4 = reinterpret_cast<const float4*>(approx);
-          int j = 0;
-          for (; j + 4 <= n4 && cnt < take; j += 4) {
-            const float4 x0 = a4[j], x1 = a4[j + 1], x2 = a4[j + 2], x3 = a4[j + 3];
-            cnt += (x0.x > thr) + (x0.y > thr) + (x0.z > thr) + (x0.w > thr);
-            cnt += (x1.x > thr) + (x1.y > thr) + (x1.z > thr) + (x1.w > thr);
-            cnt += (x2.x > thr) + (x2.y > thr) + (x2.z > thr) + (x2.w > thr);
-            cnt += (x3.x > thr) + (x3.y > thr) + (x3.z > thr) + (x3.w > thr);
-          }
-          for (; j < n4 && cnt < take; ++j) {
-            const float4 x = a4[j];
-            cnt += (x.x > thr) + (x.y > thr) + (x.z > thr) + (x.w > thr);
-          }
-          in = cnt < take;
-        }
-        if (in) {
-          const int k = atomicAdd(&S.ns, 1);
-          if (k < K5_SMAX) S.sset[k] = c;
-          else set_err(t, DERR_CANDIDATES);
-        }
+      int cnt = 0;
+      const float4* a4 = reinterpret_cast<const float4*>(approx);
+      int j = 0;
+      for (; j + 4 <= n4 && cnt < take; j += 4) {
+        const float4 x0 = a4[j], x1 = a4[j + 1], x2 = a4[j + 2], x3 = a4[j + 3];
+        cnt += (x0.x > thr) + (x0.y > thr) + (x0.z > thr) + (x0.w > thr);
+        cnt += (x1.x > thr) + (x1.y > thr) + (x1.z > thr) + (x1.w > thr);
+        cnt += (x2.x > thr) + (x2.y > thr) + (x2.z > thr) + (x2.w > thr);
+        cnt += (x3.x > thr) + (x3.y > thr) + (x3.z > thr) + (x3.w > thr);
       }
-    }
+      for (; j < n4 && cnt < take; ++j) {
+        const float4 x = a4[j];
+        cnt += (x.x > thr) + (x.y > thr) + (x.z > thr) + (x.w > thr);
+      }
+      return cnt < take;
+    };
+    for (int c = tid; c < nc; c += K5T)
+      if (in_boundary(c)) {
+        const int k = atomicAdd(&S.ns, 1);
+        if (k < K5_SMAX) S.sset[k] = c;
+      }
     __syncthreads();
-    const int ns = min(S.ns, K5_SMAX);
-    if (pass == 0 && a.k4prof && tid == 0) a.k4prof[l * 16 + 7] = ns;
-    // R5: exact cosines of S (fp64 masters staged warp-cooperatively) + counts for the tail
-    for (int r0 = 0; r0 < ns; r0 += K5_SROWS) {
-      const int rows = min(K5_SROWS, ns - r0);
+    const int ns_all = S.ns;
+    if (pass == 0 && a.k4prof && tid == 0) a.k4prof[l * 16 + 7] = ns_all;
+    // R5: exact cosines of S entries [lo, hi) (fp64 masters staged warp-cooperatively) + counts
+    // for the tail
+    auto rescore = [&](int lo, int hi) {
+    for (int r0 = lo; r0 < hi; r0 += K5_SROWS) {
+      const int rows = min(K5_SROWS, hi - r0);
       for (int r = warp; r < rows; r += K5W) {
         const int c = S.sset[r0 + r];
         const double* src = (cbuf[c] ? t.brep64 : t.rep64) + static_cast<int64_t>(cslot[c]) * d;
@@ -429,12 +427,12 @@ __global__ void __launch_bounds__(K5T) k_select3(DevTables t, DecodeArgs a, int*
           S.slz[r0 + r] = t.lazy[s];
         }
       }
-      if (pass == 0 && r0 == 0 && a.l2pf_pages > 0 && warp == 8 && ns > 0) {
+      if (pass == 0 && r0 == 0 && a.l2pf_pages > 0 && warp == 8 && hi > 0) {
         // HBM is idle while this CTA is latency bound: pull the first pages of the likely
         // selection (S contains every cluster that can be ranked) into L2 for K6; a small
         // per-domain budget keeps the per-SM TMA issue short
-        const int per = min(16, (a.l2pf_pages + ns - 1) / ns);
-        for (int w = lane; w < ns * per; w += 32) {
+        const int per = min(16, (a.l2pf_pages + hi - 1) / hi);
+        for (int w = lane; w < hi * per; w += 32) {
           const int s = cslot[S.sset[w / per]];
           const int j = w % per;
           const int np = t.npages[s];
@@ -455,6 +453,50 @@ __global__ void __launch_bounds__(K5T) k_select3(DevTables t, DecodeArgs a, int*
         S.skey[r0 + tid] = ckey[c];
       }
       __syncthreads();
+    }
+    };
+    int ns = min(ns_all, K5_SMAX);
+    if (ns_all <= K5_SMAX) {
+      rescore(0, ns);
+    } else {
+      // Near-tie-heavy query (rare): S exceeds its shared-memory capacity. Exact chunked
+      // tournament instead of a failure -- the reference ranks any number of ties
+      // (index.cpp:210-240): keep the exact top-`take` of the S members seen so far in entries
+      // [0, kept), append the next chunk of S members (candidate order) after them, re-score the
+      // chunk, rank the union and compact its top-`take` back to the front. The final ranking
+      // below then sees exactly the top-`take` of all of S.
+      int kept = 0;
+      const int room = K5_SMAX - take;  // take <= 64
+      for (int cb = 0; cb < nc; cb += room) {
+        __syncthreads();
+        if (tid == 0) S.ns = kept;
+        __syncthreads();
+        for (int c = cb + tid; c < min(cb + room, nc); c += K5T)
+          if (in_boundary(c)) S.sset[atomicAdd(&S.ns, 1)] = c;
+        __syncthreads();
+        const int hi = S.ns;
+        if (hi == kept) continue;
+        rescore(kept, hi);
+        rank_select(S.ssim, S.skey, hi, take, S.order);
+        const int keep = min(take, hi);
+        int csset = 0, csnp = 0, csnbp = 0, csnb = 0;
+        double cssim = 0.0;
+        long long cskey = 0, csnm = 0;
+        unsigned char cslz = 0;
+        if (tid < keep) {
+          const int si = S.order[tid];
+          csset = S.sset[si]; cssim = S.ssim[si]; cskey = S.skey[si];
+          csnp = S.snp[si]; csnbp = S.snbp[si]; csnm = S.snm[si]; csnb = S.snb[si]; cslz = S.slz[si];
+        }
+        __syncthreads();
+        if (tid < keep) {
+          S.sset[tid] = csset; S.ssim[tid] = cssim; S.skey[tid] = cskey;
+          S.snp[tid] = csnp; S.snbp[tid] = csnbp; S.snm[tid] = csnm; S.snb[tid] = csnb; S.slz[tid] = cslz;
+        }
+        kept = keep;
+      }
+      __syncthreads();
+      ns = kept;
     }
     if (pass == 0) K5MARK(3)
     rank_select(S.ssim, S.skey, ns, take, S.order);
@@ -656,13 +698,8 @@ bool launch_select3(const DevTables& t, const DecodeArgs& a, cudaStream_t st) {
       t.P % 32 != 0)
     return false;
   const size_t smem = sel3_dyn_bytes(t.d, t.cmax, a.n_parts_host, t.W, t.tmax);
-  if (smem + sizeof(Sel3Smem) > 220 * 1024) return false;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_select3, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
-  }
-  if (smem > 200 * 1024) return false;
+  if (smem + sizeof(Sel3Smem) > static_cast<size_t>(device_smem_optin())) return false;
+  if (!smem_optin(reinterpret_cast<const void*>(k_select3), smem)) return false;
   k_select3<<<t.L, K5T, smem, st>>>(t, a, a.work_ctr);
   return true;
 }

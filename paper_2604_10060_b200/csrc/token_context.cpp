@@ -39,12 +39,13 @@ TokenContext::TokenContext(const kvc_cfg& cfg, int d, int L) : cfg_(cfg), d_(d),
     fail(-10, "cost constants must be non-negative");
   if (cfg_.kv_dtype != KVC_DTYPE_F32 && cfg_.kv_dtype != KVC_DTYPE_BF16) fail(-10, "kv_dtype");
   if (d < 1 || L < 1 || d % 8 != 0 || d > 256) fail(-10, "the device path supports d % 8 == 0 and d <= 256");
-  if (cfg_.page_tokens < 8 || cfg_.page_tokens > 64 || cfg_.page_tokens % 8)
-    fail(-10, "page_tokens must be 8..64, a multiple of 8");
+  if (cfg_.page_tokens != 0 && (cfg_.page_tokens < 8 || cfg_.page_tokens > 64 || cfg_.page_tokens % 8))
+    fail(-10, "page_tokens must be 0 (auto) or 8..64, a multiple of 8");
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
     fail(-22, "no CUDA device: the B200 path has no CPU fallback");
   es_ = cfg_.kv_dtype == KVC_DTYPE_BF16 ? 2 : 4;
+  if (cfg_.page_tokens == 0) cfg_.page_tokens = auto_page_tokens(d, cfg_.kv_dtype == KVC_DTYPE_BF16);
   if (d * es_ > 512) fail(-10, "token baseline rows are at most 512 bytes (fp32 d <= 128, bf16 d <= 256)");
   KVC_CUDA(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
   for (auto& e : ev_) KVC_CUDA(cudaEventCreate(&e));

@@ -86,3 +86,32 @@ def queries_near(state: ClusteredState, n_steps: int, noise: float = 0.05, seed:
     cl = torch.randint(0, C, (n_steps, L), generator=g, device=dev)
     base = state.centers[torch.arange(L, device=dev)[None, :], cl]
     return _unit(base + noise * torch.randn(n_steps, L, d, generator=g, device=dev)).float().contiguous()
+
+
+def frames_drift(state: ClusteredState, n_frames: int, first_frame: int, noise: float = 0.02,
+                 drift: float = 0.01, visual_noise: float = 0.05, seed: int = 17, dtype=torch.bfloat16):
+    """New frames [n, L, T, d] with gen_stream's scene dynamics (workload.cpp:110-135): each
+    domain's center starts at one existing cluster center and drifts by perturb(center, drift)
+    every frame after the first; keys = normalize(center + noise * N(0, I)) (semantic_noise 0.02,
+    drift_rate 0.01 as SURVEY §8(d) config 2 states), values N(0, 1), visual = perturb(visual
+    center, visual_noise). At d = 128 a key's squared distance to its center is about noise^2 * d
+    = 0.051 > tau_min = 0.05, so clusters of ~512 members are over the Eq. 5 threshold and the
+    stream splits them: the maintenance regime, unlike `frames_near`'s absorb-only one."""
+    dev = state.centers.device
+    g = torch.Generator(device=dev)
+    g.manual_seed(seed)
+    L, T, d, C = state.L, state.T, state.d, state.C
+    cl = torch.randint(0, C, (L,), generator=g, device=dev)
+    center = state.centers[torch.arange(L, device=dev), cl].clone()  # [L, d]
+    ks, vs = [], []
+    vis = torch.from_numpy(state.visual).to(dev)
+    visual = []
+    for f in range(n_frames):
+        if f > 0:
+            center = _unit(center + drift * torch.randn(L, d, generator=g, device=dev))
+        visual.append(_unit(vis + visual_noise * torch.randn(d, generator=g, device=dev)))
+        ks.append(_unit(center[:, None, :] + noise * torch.randn(L, T, d, generator=g, device=dev)).to(dtype))
+        vs.append(torch.randn(L, T, d, generator=g, device=dev).to(dtype))
+    return (torch.stack(ks).contiguous(), torch.stack(vs).contiguous(),
+            torch.stack(visual).float().cpu().numpy(),
+            np.arange(first_frame, first_frame + n_frames, dtype=np.int64))

@@ -32,16 +32,27 @@ __global__ void k(double* out, long long* cyc, double x, int n) {
   float f = (float)x;
   for (int i = 0; i < n; ++i) f = __shfl_xor_sync(0xffffffff, f, 1) + 1.0f;
   long long t6 = clock64();
-  out[threadIdx.x] = a + acc + acc2 + acc3 + f + c0 + c1 + c2 + c3 + c4 + c5 + c6 + c7;
-  if (threadIdx.x == 0) { cyc[0] = t1 - t0; cyc[1] = t2 - t1; cyc[2] = t3 - t2; cyc[3] = t4 - t3; cyc[4] = t5 - t4; cyc[5] = t6 - t5; }
+  // the Eq. 3/4 element chain of one cluster (maintainer.cpp:16-25): r' = (n r + k) / (n + 1),
+  // each insert depending on the previous r (correctly rounded division, as the device chains)
+  double r = x, nn = 3.0;
+  for (int i = 0; i < n; ++i) { r = __ddiv_rn(__dadd_rn(__dmul_rn(nn, r), b), __dadd_rn(nn, 1.0)); nn = __dadd_rn(nn, 1.0); }
+  long long t7 = clock64();
+  double dv = x;
+  for (int i = 0; i < n; ++i) dv = __ddiv_rn(dv, 1.0000001);
+  long long t8 = clock64();
+  out[threadIdx.x] = a + acc + acc2 + acc3 + f + c0 + c1 + c2 + c3 + c4 + c5 + c6 + c7 + r + dv;
+  if (threadIdx.x == 0) { cyc[0] = t1 - t0; cyc[1] = t2 - t1; cyc[2] = t3 - t2; cyc[3] = t4 - t3; cyc[4] = t5 - t4; cyc[5] = t6 - t5; cyc[6] = t7 - t6; cyc[7] = t8 - t7; }
 }
 int main() {
   double* o; long long* c; cudaMalloc(&o, 1024 * 8); cudaMalloc(&c, 64);
   const int n = 1024;
   k<<<1, 32>>>(o, c, 1.5, n); cudaDeviceSynchronize();
   k<<<1, 32>>>(o, c, 1.5, n); cudaDeviceSynchronize();
-  long long h[6]; cudaMemcpy(h, c, 48, cudaMemcpyDeviceToHost);
-  printf("cycles: dadd-chain %.1f/op | 8 indep dadd %.2f/op | lds dot %.1f/elem | f32lds dot %.1f/elem | reg dot %.1f/elem | shfl %.1f\n",
-         h[0] / (double)n, h[1] / (8.0 * n), h[2] / 1024.0, h[3] / 1024.0, h[4] / (double)n, h[5] / (double)n);
+  long long h[8]; cudaMemcpy(h, c, 64, cudaMemcpyDeviceToHost);
+  printf("{\"dadd_chain_cycles\": %.2f, \"dadd_indep_cycles\": %.3f, \"lds_dot_cycles_per_elem\": %.2f, "
+         "\"f32lds_dot_cycles_per_elem\": %.2f, \"reg_dot_cycles_per_elem\": %.2f, \"shfl_cycles\": %.2f, "
+         "\"eq34_element_chain_cycles\": %.2f, \"ddiv_chain_cycles\": %.2f}\n",
+         h[0] / (double)n, h[1] / (8.0 * n), h[2] / 1024.0, h[3] / 1024.0, h[4] / (double)n, h[5] / (double)n,
+         h[6] / (double)n, h[7] / (double)n);
   return 0;
 }

@@ -111,5 +111,34 @@ class Replay:
         ro, rb, rc, rd = self.ref.ledger()
         if not (np.array_equal(ko, ro) and np.array_equal(kb, rb) and np.allclose(kc, rc, rtol=0, atol=1e-6) and kd == rd):
             self.mismatches.append(("ledger", ko.tolist(), ro.tolist(), kd, rd))
-        if self.kv.cluster_ids() != self.ref.cluster_ids():
-            self.mismatches.append(("cluster_ids",))
+        self.mismatches.extend(compare_state(self.kv, self.ref))
+
+
+def compare_state(kv, ref, members=True, limit=20):
+    """Every cluster of the product against the checker (index.hpp:29-50 ClusterRecord): the ten
+    integer fields, the fp64 Eq. 3/4 state (`variance`, `rep`, and `buffer_rep` while a buffer is
+    held) BITWISE, and the member / buffer (frame, token) lists in stored order."""
+    out = []
+    ids = kv.cluster_ids()
+    if ids != ref.cluster_ids():
+        return [("cluster_ids", len(ids), len(ref.cluster_ids()))]
+    for cid in ids:
+        ki, kvar, krep, kbrep = kv.cluster(cid)
+        ri, rvar, rrep, rbrep = ref.cluster(cid)
+        if not np.array_equal(ki, ri):
+            out.append(("cluster_info", cid, ki.tolist(), ri.tolist()))
+        elif np.float64(kvar).tobytes() != np.float64(rvar).tobytes():
+            out.append(("cluster_variance", cid, kvar, rvar))
+        elif krep.tobytes() != rrep.tobytes():
+            out.append(("cluster_rep", cid, int(np.argmax(krep != rrep))))
+        elif ri[3] > 0 and kbrep.tobytes() != rbrep.tobytes():
+            out.append(("cluster_buffer_rep", cid))
+        elif members:
+            for which in (0, 1):
+                kf, kt = kv.cluster_entries(cid, which)
+                rf, rt = ref.cluster_entries(cid, which)
+                if not (np.array_equal(kf, rf) and np.array_equal(kt, rt)):
+                    out.append(("cluster_entries", cid, which))
+        if len(out) >= limit:
+            break
+    return out

@@ -8,7 +8,7 @@ import numpy as np
 import pytest
 
 from oracle import pyoracle as po
-from tests.harness import Replay
+from tests.harness import Replay, attention_oracle, compare_state, rel_err
 
 pytestmark = pytest.mark.gpu
 
@@ -62,6 +62,7 @@ def test_config1_bf16(stream1, ref_lib):
     kbf = torch.from_numpy(s.keys).bfloat16()
     vbf = torch.from_numpy(s.values).bfloat16()
     mism = []
+    att_err = 0.0
     for kind, i in s.events():
         if kind == "frame":
             kk = kbf[i].contiguous().view(torch.int16).numpy()
@@ -71,13 +72,19 @@ def test_config1_bf16(stream1, ref_lib):
             if pid != rpid or not np.array_equal(asg, rasg):
                 mism.append(("frame", i))
         else:
-            kv.query(i, s.q[i], gt=s.gt[i])
+            out = kv.query(i, s.q[i], gt=s.gt[i])
             ref.query(i, s.q[i], s.gt[i])
             for l in range(s.L):
                 if kv.ranked(l) != ref.ranked(l) or kv.selected(l) != ref.selected(l):
                     mism.append(("query", i, l))
+                # K6's bf16 instantiation against the fp64 restatement over the reference's set
+                fr, tk = ref.attended(l)
+                att_err = max(att_err, rel_err(out[l], attention_oracle(s, fr, tk, l, s.q[i, l])))
             if kv.digest() != ref.digest():
                 mism.append(("digest", i))
+    assert mism == [], mism[:5]
+    assert att_err < ATT_TOL, att_err
+    mism = compare_state(kv, ref)
     assert mism == [], mism[:5]
 
 
