@@ -252,6 +252,53 @@ KVC_API int kvc_set_peers(kvc_ctx* ctx, int32_t n_ranks, int32_t rank, int32_t d
                           void* const* bufs);
 KVC_API int kvc_peer_output(kvc_ctx* ctx, float* out, int32_t mem);
 
+/* ------------------------------------------------------------------ component-level API
+ * The reference's HierIndex / TieredStore / Maintainer / retrieve calls one at a time (the C++
+ * drop-in include/kvclust_b200.hpp is built on these; engine-level callers use the hot path
+ * above). Payloads are f32 (kv_dtype f32 contexts). */
+/* HierIndex::add_partition (index.cpp:59-69) / append_frame (index.cpp:71-79) */
+KVC_API int kvc_add_partition(kvc_ctx* ctx, int64_t first_frame, const float* visual, int64_t* partition);
+KVC_API int kvc_append_frame(kvc_ctx* ctx, int64_t partition, int64_t frame_id, const float* visual);
+/* HierIndex::add_cluster (index.cpp:97-120) + TieredStore::adopt (store.cpp:82-86) when `adopt`:
+ * n members keys/values [n][d] f32 host with their (frame, token) ids; representative and variance
+ * are the exact Eq. 1/2 statistics (compute_representative / compute_variance), computed on the
+ * device; residence 0 Device / 1 Host. *id receives the new cluster id. */
+KVC_API int kvc_add_cluster(kvc_ctx* ctx, int32_t layer, int64_t partition, int32_t n, const float* keys,
+                            const float* values, const int64_t* frames, const int32_t* tokens, int32_t residence,
+                            int32_t adopt, int64_t* id);
+KVC_API int kvc_adopt(kvc_ctx* ctx, int64_t id);
+/* retrieve()'s explicit local window (retrieval.hpp:73-75) empty: no window entries attended */
+KVC_API int kvc_reset_window(kvc_ctx* ctx);
+/* Per-call RetrievalConfig (retrieval.hpp:20-32): k_v, k_s, prefetch_k, prefetch_enabled and the
+ * lookup / compute cost constants are taken from cfg (other fields ignored). */
+KVC_API int kvc_set_retrieval(kvc_ctx* ctx, const kvc_cfg* cfg);
+/* Re-configures a live context from cfg, `what` bits: 1 the RetrievalConfig fields (as
+ * kvc_set_retrieval), 2 the CostModel (TieredStore(index, cost), store.hpp:17-31: alpha_us,
+ * beta_us_per_byte, bytes_per_entry, device_capacity_entries), 4 the MaintainerConfig
+ * (Maintainer(index, store, cfg), maintainer.hpp:28-34: tau_min / tau_max / n0, defer_host_splits,
+ * max_split_depth, visual_floor; cfg.seed is taken as MaintainerConfig::seed itself). */
+KVC_API int kvc_reconfigure(kvc_ctx* ctx, const kvc_cfg* cfg, int32_t what);
+/* Maintainer::place_frame (maintainer.cpp:37-53) / on_insert (maintainer.cpp:88-176): one entry of
+ * one domain resolved on the device (no window row); *cluster receives the routed id. */
+KVC_API int kvc_place_frame(kvc_ctx* ctx, int64_t frame_id, const float* visual, int64_t* partition);
+KVC_API int kvc_insert(kvc_ctx* ctx, int64_t partition, int32_t layer, int32_t token, int64_t frame_id,
+                       const float* key, const float* value, int64_t* cluster);
+/* Maintainer::materialize (maintainer.cpp:178-193): returns the count of replacement ids */
+KVC_API int kvc_materialize(kvc_ctx* ctx, int64_t id, int64_t* ids, int32_t cap);
+/* TieredStore::touch / pin (replaces the pinned set) / enforce_capacity (store.cpp:139-164) */
+KVC_API int kvc_touch(kvc_ctx* ctx, int64_t id);
+KVC_API int kvc_pin(kvc_ctx* ctx, const int64_t* ids, int32_t n);
+KVC_API int kvc_enforce_capacity(kvc_ctx* ctx, double* cost_us);
+/* visual_topk (index.cpp:192-208) / semantic_topk (index.cpp:210-240) on the device; return counts */
+KVC_API int kvc_visual_topk(kvc_ctx* ctx, const float* q, int32_t k, int64_t* ids);
+KVC_API int kvc_semantic_topk(kvc_ctx* ctx, const float* q, int32_t layer, const int64_t* partitions, int32_t n_parts,
+                              int32_t k, int64_t* ids, int32_t* is_buffer);
+/* RetrievalResult fetched_frames (which = 0) / context_frames (which = 1) of the last decode step
+ * (retrieval.cpp:99-110; needs cfg.parity_mode or ground truth). Returns the count. */
+KVC_API int kvc_last_frames(kvc_ctx* ctx, int32_t which, int64_t* frames, int32_t cap);
+/* LayerResult::predicted of the last decode step (clusters prefetched for this layer) */
+KVC_API int kvc_last_predicted(kvc_ctx* ctx, int32_t layer, int64_t* ids, int32_t cap);
+
 /* ------------------------------------------------------------------ instrumentation */
 /* Kernel launches issued by this context since creation (for bench gpu_launches). */
 KVC_API int64_t kvc_launch_count(kvc_ctx* ctx);
@@ -296,6 +343,11 @@ KVC_API int kvc_debug_assign_check(kvc_ctx* ctx, const void* keys, int32_t T, in
                                    double* out4);
 KVC_API int kvc_debug_div_check(uint64_t n, uint64_t seed, int32_t max_den, uint64_t* mismatches);
 KVC_API int kvc_debug_resolve_profile(kvc_ctx* ctx, double* out);
+/* Host-event slow path profile (cumulative since creation / the last reset), out8: microseconds in
+ * host events (split / seed) total, of which staging + download of the cluster rows, split k-means
+ * (split_two calls), host Eq. 1/2 statistics of the children, slot / page / list uploads; then the
+ * relaunch-and-wait of a domain after an event; the number of host events and of split_two calls. */
+KVC_API int kvc_debug_event_profile(kvc_ctx* ctx, double* out8, int32_t reset);
 /* Enables per-phase CUDA-event timing (off by default: it adds event records). */
 KVC_API void kvc_set_timing(kvc_ctx* ctx, int32_t on);
 

@@ -558,6 +558,130 @@ int kvc_debug_div_check(uint64_t n, uint64_t seed, int32_t max_den, uint64_t* mi
   return *mismatches == ~0ull ? KVC_E_CUDA : KVC_OK;
 }
 
+// ------------------------------------------------------------------ component-level API
+int kvc_add_partition(kvc_ctx* ctx, int64_t first_frame, const float* visual, int64_t* partition) {
+  return guard([&] {
+    const int64_t p = F(ctx).api_add_partition(first_frame, visual);
+    if (partition) *partition = p;
+  });
+}
+
+int kvc_append_frame(kvc_ctx* ctx, int64_t partition, int64_t frame_id, const float* visual) {
+  return guard([&] { F(ctx).api_append_frame(partition, frame_id, visual); });
+}
+
+int kvc_add_cluster(kvc_ctx* ctx, int32_t layer, int64_t partition, int32_t n, const float* keys,
+                    const float* values, const int64_t* frames, const int32_t* tokens, int32_t residence,
+                    int32_t adopt, int64_t* id) {
+  return guard([&] {
+    const int64_t c = F(ctx).api_add_cluster(layer, partition, n, keys, values, frames, tokens, residence != 0, adopt != 0);
+    if (id) *id = c;
+  });
+}
+
+int kvc_adopt(kvc_ctx* ctx, int64_t id) {
+  return guard([&] { F(ctx).api_adopt(id); });
+}
+
+int kvc_reset_window(kvc_ctx* ctx) {
+  return guard([&] {
+    if (ctx->tok)
+      ctx->tok->reset_window();
+    else
+      F(ctx).api_reset_window();
+  });
+}
+
+int kvc_set_retrieval(kvc_ctx* ctx, const kvc_cfg* cfg) {
+  return guard([&] {
+    if (!cfg) kvc::fail(KVC_E_CONFIG, "null config");
+    if (ctx->tok) kvc::fail(KVC_E_CONFIG, "token-baseline contexts take their budget at creation");
+    F(ctx).api_set_retrieval(*cfg);
+  });
+}
+
+int kvc_reconfigure(kvc_ctx* ctx, const kvc_cfg* cfg, int32_t what) {
+  return guard([&] {
+    if (!cfg) kvc::fail(KVC_E_CONFIG, "null config");
+    F(ctx).api_reconfigure(*cfg, what);
+  });
+}
+
+int kvc_place_frame(kvc_ctx* ctx, int64_t frame_id, const float* visual, int64_t* partition) {
+  return guard([&] {
+    const int64_t p = F(ctx).api_place_frame(frame_id, visual);
+    if (partition) *partition = p;
+  });
+}
+
+int kvc_insert(kvc_ctx* ctx, int64_t partition, int32_t layer, int32_t token, int64_t frame_id, const float* key,
+               const float* value, int64_t* cluster) {
+  return guard([&] {
+    const int64_t c = F(ctx).api_insert(partition, layer, token, frame_id, key, value);
+    if (cluster) *cluster = c;
+  });
+}
+
+int kvc_materialize(kvc_ctx* ctx, int64_t id, int64_t* ids, int32_t cap) {
+  std::vector<int64_t> r;
+  const int rc = guard([&] { r = F(ctx).api_materialize(id); });
+  return rc != KVC_OK ? rc : copy_out(r, ids, cap);
+}
+
+int kvc_touch(kvc_ctx* ctx, int64_t id) {
+  return guard([&] { F(ctx).api_touch(id); });
+}
+
+int kvc_pin(kvc_ctx* ctx, const int64_t* ids, int32_t n) {
+  return guard([&] { F(ctx).api_pin(std::vector<int64_t>(ids, ids + (n > 0 ? n : 0))); });
+}
+
+int kvc_enforce_capacity(kvc_ctx* ctx, double* cost_us) {
+  return guard([&] {
+    const double c = F(ctx).api_enforce_capacity();
+    if (cost_us) *cost_us = c;
+  });
+}
+
+int kvc_visual_topk(kvc_ctx* ctx, const float* q, int32_t k, int64_t* ids) {
+  std::vector<int64_t> r;
+  const int rc = guard([&] { r = F(ctx).api_visual_topk(q, k); });
+  return rc != KVC_OK ? rc : copy_out(r, ids, k);
+}
+
+int kvc_semantic_topk(kvc_ctx* ctx, const float* q, int32_t layer, const int64_t* partitions, int32_t n_parts,
+                      int32_t k, int64_t* ids, int32_t* is_buffer) {
+  int n = 0;
+  const int rc = guard([&] {
+    auto r = F(ctx).api_semantic_topk(q, layer, std::vector<int64_t>(partitions, partitions + (n_parts > 0 ? n_parts : 0)), k);
+    n = static_cast<int>(r.size());
+    for (int i = 0; i < n; ++i) {
+      ids[i] = r[static_cast<std::size_t>(i)].first;
+      is_buffer[i] = r[static_cast<std::size_t>(i)].second;
+    }
+  });
+  return rc != KVC_OK ? rc : n;
+}
+
+int kvc_last_frames(kvc_ctx* ctx, int32_t which, int64_t* frames, int32_t cap) {
+  if (which != 0 && which != 1) return KVC_E_CONFIG;
+  if (ctx->tok) return copy_out(ctx->tok->last_frames(which), frames, cap);
+  KVC_READER(ctx);
+  return copy_out(which == 0 ? R(ctx).last_fetched_frames() : R(ctx).last_context_frames(), frames, cap);
+}
+
+int kvc_last_predicted(kvc_ctx* ctx, int32_t layer, int64_t* ids, int32_t cap) {
+  if (ctx->tok) return 0;
+  KVC_READER(ctx);
+  const auto& ls = R(ctx).last_layers();
+  if (layer < 0 || layer >= static_cast<int>(ls.size())) return KVC_E_BAD_LAYER;
+  return copy_out(ls[static_cast<std::size_t>(layer)].predicted, ids, cap);
+}
+
+int kvc_debug_event_profile(kvc_ctx* ctx, double* out8, int32_t reset) {
+  return guard([&] { F(ctx).event_profile(out8, reset != 0); });
+}
+
 int kvc_debug_resolve_profile(kvc_ctx* ctx, double* out) {
   if (ctx->tok) return guard([&] { ctx->tok->profile(out); });  // token-baseline select phases
   ctx->impl->resolve_profile(out);

@@ -275,6 +275,8 @@ void Context::alloc_device() {
   {
     const char* e = std::getenv("KVC_RESOLVE");  // "seq": the sequential resolve kernel
     resolve_seq_ = e && std::string(e) == "seq";
+    const char* rl = std::getenv("KVC_RELAUNCH");  // "spec": speculative kernel for relaunches too
+    relaunch_seq_ = !(rl && std::string(rl) == "spec");
     const char* g = std::getenv("KVC_ASSIGN");  // "simt": the fp32 CUDA-core tile
     assign_tc_ = !(g && std::string(g) == "simt") && assign_tc_supported(t_) &&
                  make_key_tensor_map(key_maps_[0], fkbuf_[0], d, t_.tmax, L) &&
@@ -318,28 +320,18 @@ void Context::alloc_device() {
   ia_.defer = cfg_.defer_host_splits;
 
   // decode result block
-  const int kv = cfg_.k_v, ks = cfg_.k_s, kp = cfg_.prefetch_k;
+  // ranked lists never exceed the candidate count (take = min(k, candidates)), so the result
+  // blocks are sized by the clamped budgets (k_s = 10^6 "exhaustive" budgets stay small)
+  const std::int32_t kv = std::min(cfg_.k_v, t_.max_parts), ks = std::min(cfg_.k_s, t_.cmax),
+                     kp = std::min(cfg_.prefetch_k, t_.cmax);
   da_.chunk_pages = 8;
   da_.max_desc = 4096;
   da_.max_items = da_.max_desc / da_.chunk_pages;
-  std::size_t off = 0;
-  auto carve = [&](std::size_t bytes) {
-    std::size_t o = off;
-    off += (bytes + 15) & ~std::size_t(15);
-    return o;
-  };
-  const std::size_t o_parts = carve(L * kv * 4), o_nps = carve(L * 4), o_rs = carve(L * ks * 4),
-                    o_rb = carve(L * ks), o_nr = carve(L * 4), o_ps = carve(L * kp * 4),
-                    o_pb = carve(L * kp), o_np = carve(L * 4), o_vs = carve(L * ks * 4),
-                    o_nv = carve(L * 4), o_att = carve(L * 8), o_nc = carve(L * 4), o_fl = carve(L * 4), o_ew = carve(L * 4);
-  dec_bytes_ = off;
-  res_off_ = {o_parts, o_nps, o_rs, o_rb, o_nr, o_ps, o_pb, o_np, o_vs, o_nv, o_att, o_nc, o_fl, o_ew};
   t_.err = static_cast<std::int32_t*>(dalloc(16));
   KVC_CUDA(cudaStreamCreateWithFlags(&cs_, cudaStreamNonBlocking));
   KVC_CUDA(cudaStreamCreateWithFlags(&in_st_, cudaStreamNonBlocking));
+  alloc_result_blocks(kv, ks, kp);
   for (int b = 0; b < 2; ++b) {
-    d_blk_[b] = dalloc(dec_bytes_);
-    h_blk_[b] = halloc(dec_bytes_);
     KVC_CUDA(cudaEventCreateWithFlags(&ev_k4_[b], cudaEventDisableTiming));
     KVC_CUDA(cudaEventCreateWithFlags(&ev_out_[b], cudaEventDisableTiming));
     KVC_CUDA(cudaEventCreateWithFlags(&ev_step_[b], cudaEventDisableTiming));
@@ -450,6 +442,32 @@ void Context::debug_assign_check(const void* keys, int T, std::int64_t pid, int 
 
 // Points the decode arguments' result fields at device result block b (two blocks: the kernels
 // of step i+1 write one while step i's block is copied to the host and replayed).
+// Decode result blocks (device + pinned host, double-buffered): the step's ranked / prefetch /
+// verified lists and counters, carved for budgets kv / ks / kp per domain.
+void Context::alloc_result_blocks(std::int32_t kv, std::int32_t ks, std::int32_t kp) {
+  const std::size_t L = static_cast<std::size_t>(L_);
+  std::size_t off = 0;
+  auto carve = [&](std::size_t bytes) {
+    std::size_t o = off;
+    off += (bytes + 15) & ~std::size_t(15);
+    return o;
+  };
+  const std::size_t o_parts = carve(L * kv * 4), o_nps = carve(L * 4), o_rs = carve(L * ks * 4),
+                    o_rb = carve(L * ks), o_nr = carve(L * 4), o_ps = carve(L * kp * 4),
+                    o_pb = carve(L * kp), o_np = carve(L * 4), o_vs = carve(L * ks * 4),
+                    o_nv = carve(L * 4), o_att = carve(L * 8), o_nc = carve(L * 4), o_fl = carve(L * 4), o_ew = carve(L * 4);
+  dec_bytes_ = off;
+  res_off_ = {o_parts, o_nps, o_rs, o_rb, o_nr, o_ps, o_pb, o_np, o_vs, o_nv, o_att, o_nc, o_fl, o_ew};
+  for (int b = 0; b < 2; ++b) {
+    d_blk_[b] = dalloc(dec_bytes_);
+    h_blk_[b] = halloc(dec_bytes_);
+  }
+  kv_cap_ = kv;
+  ks_cap_ = ks;
+  kp_cap_ = kp;
+  set_result_block(cur_);
+}
+
 void Context::set_result_block(int b) {
   auto* base = static_cast<std::uint8_t*>(d_blk_[b]);
   const ResultOffsets& o = res_off_;
@@ -1152,7 +1170,8 @@ void Context::launch_round(const std::vector<int>& active, const std::vector<int
   }
   if (timing_) KVC_CUDA(cudaEventRecord(ev_[3], st_));
   {
-    const int n = resolve_seq_ ? 0 : launch_resolve_spec(t_, ia_, st_);
+    const bool seq = resolve_seq_ || (round_after_event_ && relaunch_seq_);
+    const int n = seq ? 0 : launch_resolve_spec(t_, ia_, st_);
     launches_ += n ? n : launch_resolve(t_, ia_, st_);
   }
   if (timing_) KVC_CUDA(cudaEventRecord(ev_[4], st_));
@@ -1182,24 +1201,28 @@ inline int run_end(const std::int32_t* evs, const std::int32_t* evk, int u, int 
 }
 }  // namespace
 
-void Context::run_inserts(std::int64_t frame_id, std::int64_t pid, int T, std::int64_t* assigned, bool launched) {
+void Context::run_inserts(std::int64_t frame_id, std::int64_t pid, int T, std::int64_t* assigned, bool launched,
+                          int l_lo, int l_hi, int tok0) {
   const int ring_slot = ia_.ring_slot;
   const bool eager = !cfg_.defer_host_splits;
+  if (l_hi < 0) l_hi = L_;
   std::vector<int> cursor(static_cast<std::size_t>(L_), 0), replayed(static_cast<std::size_t>(L_), 0);
+  for (int l = l_lo; l < l_hi; ++l) cursor[static_cast<std::size_t>(l)] = replayed[static_cast<std::size_t>(l)] = tok0;
   std::vector<int> active;
   if (eager)
-    active.push_back(0);
+    active.push_back(l_lo);
   else
-    for (int l = 0; l < L_; ++l) active.push_back(l);
-  int frontier = 0;
+    for (int l = l_lo; l < l_hi; ++l) active.push_back(l);
+  int frontier = l_lo;
   bool launch = true;
+  bool relaunch_after_event = false;
   ia_.T = T;
   ia_.pid = static_cast<std::int32_t>(pid);
   ia_.ring_slot = ring_slot;
   double t_wait = 0.0, t_replay = 0.0, t_launch = 0.0;
   for (double& x : ingest_t_) x = 0.0;
   const auto r0 = std::chrono::steady_clock::now();
-  while (frontier < L_) {
+  while (frontier < l_hi) {
     if (launch) {
       const auto lc0 = std::chrono::steady_clock::now();
       cudaEvent_t done = nullptr;
@@ -1207,7 +1230,9 @@ void Context::run_inserts(std::int64_t frame_id, std::int64_t pid, int T, std::i
         launched = false;  // the first round was launched by ingest_frame: wait for its outcome
         done = ping_wait_;  // block only (the next frame's kernels may already be queued behind it)
       } else {
+        round_after_event_ = relaunch_after_event;
         launch_round(active, cursor);
+        round_after_event_ = false;
       }
       const auto w0 = std::chrono::steady_clock::now();
       t_launch += std::chrono::duration<double, std::micro>(w0 - lc0).count();
@@ -1216,6 +1241,8 @@ void Context::run_inserts(std::int64_t frame_id, std::int64_t pid, int T, std::i
       else
         sync();
       t_wait += std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - w0).count();
+      if (relaunch_after_event) evt_t_[5] += std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - lc0).count();
+      relaunch_after_event = false;
       check_err_word(*h_err_);
       if (round_timed_) {  // (the round may have been launched before timing was switched on)
         float ms = 0.f;
@@ -1228,7 +1255,7 @@ void Context::run_inserts(std::int64_t frame_id, std::int64_t pid, int T, std::i
       // the replay below is bound by cache misses on scattered per-cluster state: touch every
       // pending domain's first cluster now, with the loads independent of each other
       for (int pass = 0; pass < 2; ++pass)
-        for (int l = frontier; l < L_; ++l) {
+        for (int l = frontier; l < l_hi; ++l) {
           const int t0 = replayed[static_cast<std::size_t>(l)];
           if (t0 >= h_stop_[l]) continue;
           const std::int32_t sl = h_evs_[static_cast<std::size_t>(l) * t_.tmax + t0];
@@ -1249,7 +1276,7 @@ void Context::run_inserts(std::int64_t frame_id, std::int64_t pid, int T, std::i
     const int stop = h_stop_[l];
     const std::int32_t* evk = h_evk_ + static_cast<std::size_t>(l) * t_.tmax;
     const std::int32_t* evs = h_evs_ + static_cast<std::size_t>(l) * t_.tmax;
-    std::int32_t* owner = &ring_owner_h_[(static_cast<std::size_t>(l) * t_.W + ring_slot) * t_.tmax];
+    std::int32_t* owner = ring_slot >= 0 ? &ring_owner_h_[(static_cast<std::size_t>(l) * t_.W + ring_slot) * t_.tmax] : nullptr;
     std::int64_t last_cid = -1;
     const auto rp0 = std::chrono::steady_clock::now();
     // replay in runs of equal (cluster, outcome): ticks are consecutive within a run, so the run
@@ -1269,7 +1296,7 @@ void Context::run_inserts(std::int64_t frame_id, std::int64_t pid, int T, std::i
         fc_pending_.push_back(cid);  // frame -> cluster map entries, merged once (frame_add_flush)
         last_cid = cid;
       }
-      std::fill(owner + t, owner + u, slot);
+      if (owner) std::fill(owner + t, owner + u, slot);
       (kind == EV_ABSORB ? c.members : c.buffer).push_run(frame_id, t, n);
       device_entries_ += n;
       set_flag(cid, CF_TRACKED, true);
@@ -1298,7 +1325,7 @@ void Context::run_inserts(std::int64_t frame_id, std::int64_t pid, int T, std::i
     replayed[static_cast<std::size_t>(l)] = stop;
     if (stop >= T) {
       frontier += 1;
-      if (eager && frontier < L_) {
+      if (eager && frontier < l_hi) {
         active.assign(1, frontier);
         launch = true;
       }
@@ -1322,9 +1349,10 @@ void Context::run_inserts(std::int64_t frame_id, std::int64_t pid, int T, std::i
     if (stop + 1 < T) {
       active.assign(1, l);
       launch = true;
+      relaunch_after_event = true;
     } else {
       frontier += 1;
-      if (eager && frontier < L_) {
+      if (eager && frontier < l_hi) {
         active.assign(1, frontier);
         launch = true;
       }
@@ -1437,7 +1465,13 @@ void Context::ring_owner_upload(int layer) {
 std::vector<std::int64_t> Context::split_pool(std::int64_t pid, int layer, bool host,
                                               std::vector<Member>&& ids, std::int64_t rows, int) {
   if (static_cast<std::int64_t>(ids.size()) != rows) fail(-11, "pool size mismatch");
+  auto now = [] { return std::chrono::steady_clock::now(); };
+  auto us = [](std::chrono::steady_clock::time_point a, std::chrono::steady_clock::time_point b) {
+    return std::chrono::duration<double, std::micro>(b - a).count();
+  };
+  const auto sd0 = now();
   stage_download(rows);
+  evt_t_[1] += us(sd0, now());
   const float* keys = h_stage_f32_;
   std::vector<std::int64_t> out;
   std::vector<std::int32_t> slots;
@@ -1475,15 +1509,20 @@ std::vector<std::int64_t> Context::split_pool(std::int64_t pid, int layer, bool 
       emit(grp, std::move(rep), var);
       return;
     }
+    const auto k0 = now();
     const KMeansOut halves = split_two_staged(grp, mix_seed(maint_seed_, static_cast<std::uint64_t>(split_counter_++)));
+    evt_t_[2] += us(k0, now());
+    evt_t_[7] += 1.0;
     mstats_[5] += 1;  // split_ops_total
     std::vector<int> g2[2];
     for (std::size_t i = 0; i < grp.size(); ++i) g2[halves.assign[i]].push_back(grp[i]);
     for (auto& g : g2) {
       if (g.empty()) continue;
       std::vector<double> rep(static_cast<std::size_t>(d_));
+      const auto h0 = now();
       representative(keys, g.data(), static_cast<int>(g.size()), d_, rep.data());
       const double var = variance(keys, g.data(), static_cast<int>(g.size()), d_, rep.data());
+      evt_t_[3] += us(h0, now());
       if (depth + 1 < cfg_.max_split_depth && g.size() >= 2 &&
           var > tau_of(static_cast<std::int64_t>(g.size()), cfg_)) {
         self(self, std::move(g), depth + 1);
@@ -1496,11 +1535,13 @@ std::vector<std::int64_t> Context::split_pool(std::int64_t pid, int layer, bool 
   std::iota(all.begin(), all.end(), 0);
   rec(rec, std::move(all), 0);
 
+  const auto u0 = now();
   init_slots(slots, reps, vars, stats, nmem, cids, res, nullptr, nullptr);
   append_runs_idx(runs, idx);
   pl_upload(pid, layer);
   for (std::size_t i = 0; i < out.size(); ++i) ring_owner_patch(layer, C(out[i]).members, slots[i]);
   ring_owner_upload(layer);
+  evt_t_[4] += us(u0, now());
   return out;
 }
 
@@ -1571,6 +1612,12 @@ KMeansOut Context::debug_split_two_dev(const float* pts, int n, std::uint64_t se
 
 std::int64_t Context::handle_host_event(std::int64_t frame_id, std::int64_t pid, int layer, int tok,
                                         int kind, std::int32_t slot) {
+  struct Tm {
+    double* acc;
+    std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+    ~Tm() { *acc += std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count(); }
+  } tm{&evt_t_[0]};
+  evt_t_[6] += 1.0;
   mstats_[0] += 1;  // inserts (maintainer.cpp:89)
   const std::size_t frow = static_cast<std::size_t>(layer) * t_.tmax + tok;
   const std::size_t rb = static_cast<std::size_t>(d_) * es_;
@@ -1601,6 +1648,7 @@ std::int64_t Context::handle_host_event(std::int64_t frame_id, std::int64_t pid,
     fail(-11, "unknown host event");
   }
   mstats_[2] += 1;  // immediate_splits
+  const auto ts0 = std::chrono::steady_clock::now();
   const std::int64_t rows = stage_cluster(c.slot, true);
   KVC_CUDA(cudaMemcpyAsync(static_cast<std::uint8_t*>(d_stage_k_) + rows * rb,
                            static_cast<std::uint8_t*>(d_fk_) + frow * rb, rb, cudaMemcpyDeviceToDevice, st_));

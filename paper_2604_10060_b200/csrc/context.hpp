@@ -199,6 +199,30 @@ class Context {
   // fused output exchange across ranks (multi-GPU by domain; context_query.cpp)
   void set_peers(int n, int rank, int dom_offset, int total_domains, void* const* bufs);
   void peer_output(float* out, int mem);
+  // component-level API (context_api.cpp): the reference's HierIndex / TieredStore / Maintainer /
+  // retrieve calls one by one, for the C++ drop-in (include/kvclust_b200.hpp)
+  std::int64_t api_add_partition(std::int64_t first_frame, const float* visual);
+  void api_append_frame(std::int64_t pid, std::int64_t frame, const float* visual);
+  std::int64_t api_add_cluster(int layer, std::int64_t parent, int n, const float* keys, const float* values,
+                               const std::int64_t* frames, const std::int32_t* tokens, bool host, bool adopt_it);
+  void api_adopt(std::int64_t id);
+  void api_reset_window();
+  void api_set_retrieval(const kvc_cfg& c);
+  void api_reconfigure(const kvc_cfg& c, int what);  // bits: 1 retrieval, 2 cost model, 4 maintainer
+  std::int64_t api_place_frame(std::int64_t frame, const float* visual);
+  std::int64_t api_insert(std::int64_t pid, int layer, int token, std::int64_t frame, const float* key,
+                          const float* value);
+  std::vector<std::int64_t> api_materialize(std::int64_t id);
+  void api_touch(std::int64_t id);
+  void api_pin(const std::vector<std::int64_t>& ids);
+  double api_enforce_capacity();
+  std::vector<std::int64_t> api_visual_topk(const float* q, int k);
+  std::vector<std::pair<std::int64_t, int>> api_semantic_topk(const float* q, int layer,
+                                                              const std::vector<std::int64_t>& part_ids, int k);
+  // frames of the last step's selected clusters / attended entries (RetrievalResult
+  // fetched_frames / context_frames, retrieval.cpp:99-110; parity mode or ground truth given)
+  const std::vector<std::int64_t>& last_fetched_frames() const { return last_fetched_; }
+  const std::vector<std::int64_t>& last_context_frames() const { return last_context_; }
 
  private:
   // ---- configuration
@@ -298,11 +322,19 @@ class Context {
   bool finish_step(int b);
   void replay_decode(const void* hblock, const std::int64_t* gt, int n_gt);
   std::size_t dec_bytes_ = 0;
+  std::int32_t kv_cap_ = 0, ks_cap_ = 0, kp_cap_ = 0;  // budgets the result blocks are carved for
+  void alloc_result_blocks(std::int32_t kv, std::int32_t ks, std::int32_t kp);
   float* d_q_ = nullptr;
   float* d_out_ = nullptr;
   cudaEvent_t ev_[8];
   bool timing_ = false;
   bool resolve_seq_ = false;  // KVC_RESOLVE=seq selects the sequential resolve kernel
+  // A domain relaunched after a split (one domain, its state just changed under the remaining
+  // tokens) runs the sequential kernel: the speculation restarts at most tokens there (the two
+  // children compete for them), measured 2.4 ms vs 0.85 ms per relaunch on the drift stream.
+  // KVC_RELAUNCH=spec keeps the speculative kernel.
+  bool relaunch_seq_ = true;
+  bool round_after_event_ = false;
   bool assign_tc_ = false;    // tensor-core distance tile (KVC_ASSIGN=simt disables)
   alignas(64) unsigned char key_map_[128];  // CUtensorMap over the current frame's keys
   alignas(64) unsigned char key_maps_[2][128];
@@ -311,6 +343,18 @@ class Context {
   // last frame: device us (cands, assign, topm, resolve, store), host us (wait, on_insert loop,
   // of which replay and relaunch issue), host events
   double ingest_t_[10] = {0};
+  // host-event (split / seed) slow-path profile, cumulative: total, stage + download, split
+  // k-means, host Eq. 1/2 stats, slot/page uploads, relaunch after an event, #events, #split_two
+  double evt_t_[8] = {0};
+
+ public:
+  void event_profile(double* out, bool reset) {
+    for (int i = 0; i < 8; ++i) out[i] = evt_t_[i];
+    if (reset)
+      for (double& x : evt_t_) x = 0.0;
+  }
+
+ private:
   std::int64_t launches_ = 0;
 
   // ---- physical host tier (context_tiers.cpp)
@@ -404,6 +448,7 @@ class Context {
   // last query
   std::vector<LayerOut> last_;
   double last_ttft_ = 0.0, last_recall_ = -1.0;
+  std::vector<std::int64_t> last_fetched_, last_context_;
   std::uint64_t last_digest_ = 0;
 
   std::vector<std::int64_t> verified_tmp_;
@@ -438,7 +483,10 @@ class Context {
   std::vector<std::int64_t> window_owner_ids() const;
   void apply_cadence(std::int64_t frame_id, std::int64_t pid);
   std::int64_t place_frame(std::int64_t frame_id, const float* visual);
-  void run_inserts(std::int64_t frame_id, std::int64_t pid, int T, std::int64_t* assigned, bool launched);
+  // domains [l_lo, l_hi) (l_hi < 0: all) from token tok0 (Maintainer::on_insert uses one domain,
+  // one token, no window ring: ia_.ring_slot = -1)
+  void run_inserts(std::int64_t frame_id, std::int64_t pid, int T, std::int64_t* assigned, bool launched,
+                   int l_lo = 0, int l_hi = -1, int tok0 = 0);
   // split slow path
   std::vector<std::int64_t> split_pool(std::int64_t pid, int layer, bool host,
                                        std::vector<Member>&& ids, std::int64_t rows, int depth_unused);

@@ -269,7 +269,7 @@ void Context::replay_decode(const void* hblock, const std::int64_t* gt, int n_gt
   const bool parity = cfg_.parity_mode != 0 || (gt && n_gt > 0);
   std::vector<std::int64_t> predicted_next;
   double stall_next = 0.0;
-  std::vector<std::int64_t> context_frames;
+  std::vector<std::int64_t> context_frames, fetched_frames;
   last_ttft_ = 0.0;
   for (int l = 0; l < L_; ++l) {
     LayerOut& lo = last_[static_cast<std::size_t>(l)];
@@ -311,7 +311,10 @@ void Context::replay_decode(const void* hblock, const std::int64_t* gt, int n_gt
     if (parity) {
       auto& att = lo.attended;
       for (std::int64_t cid : lo.selected)
-        for (const Member& m : C(cid).members) att.push_back({m.frame, m.token});
+        for (const Member& m : C(cid).members) {
+          att.push_back({m.frame, m.token});
+          fetched_frames.push_back(m.frame);  // retrieval.cpp:101-105
+        }
       for (const WinFrame& w : window_)
         for (int t = 0; t < w.T; ++t) att.push_back({w.frame_id, t});
       std::sort(att.begin(), att.end());
@@ -340,9 +343,15 @@ void Context::replay_decode(const void* hblock, const std::int64_t* gt, int n_gt
   step_t_[8] = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - tl0).count();
   for (const LayerOut& lo : last_) last_ttft_ += lo.lat[0] + lo.lat[1] + lo.lat[2] + lo.lat[3] + lo.lat[4];
   last_recall_ = -1.0;
+  last_fetched_.clear();
+  last_context_.clear();
   if (parity) {
     std::sort(context_frames.begin(), context_frames.end());
     context_frames.erase(std::unique(context_frames.begin(), context_frames.end()), context_frames.end());
+    std::sort(fetched_frames.begin(), fetched_frames.end());
+    fetched_frames.erase(std::unique(fetched_frames.begin(), fetched_frames.end()), fetched_frames.end());
+    last_context_ = context_frames;
+    last_fetched_ = fetched_frames;
     if (gt && n_gt > 0) {
       std::int64_t hit = 0;
       for (int i = 0; i < n_gt; ++i)

@@ -883,7 +883,7 @@ __global__ void __launch_bounds__(32) k_resolve(DevTables t, IngestArgs a) {
         a.ev_row[frow] = row;
         a.ev_kind[frow] = kind;
         a.ev_slot[frow] = w;
-        t.ring_owner[(static_cast<int64_t>(dom) * t.W + a.ring_slot) * t.tmax + tt] = w;
+        if (a.ring_slot >= 0) t.ring_owner[(static_cast<int64_t>(dom) * t.W + a.ring_slot) * t.tmax + tt] = w;
         if (kind == EV_DEFER && nb == 0) {  // register the new buffer candidate
           if (n < cmax) {
             cslot[n] = w;
@@ -951,12 +951,16 @@ __global__ void k_store_rows(DevTables t, IngestArgs a) {
     const int page = a.ev_page[frow];
     const int row = page >= 0 ? a.ev_row[frow] : 0;
     const uint8_t* src = static_cast<const uint8_t*>(half ? a.fv : a.fk) + frow * rb;
-    const int rpage = t.ring_pages[(static_cast<int64_t>(dom) * t.W + a.ring_slot) * t.rpp + tt / t.P];
-    uint8_t* dring = (half ? page_v(t, rpage) : page_k(t, rpage)) + static_cast<int64_t>(tt % t.P) * rb;
+    // ring_slot < 0: entries inserted outside a frame (Maintainer::on_insert), no window row
+    uint8_t* dring = nullptr;
+    if (a.ring_slot >= 0) {
+      const int rpage = t.ring_pages[(static_cast<int64_t>(dom) * t.W + a.ring_slot) * t.rpp + tt / t.P];
+      dring = (half ? page_v(t, rpage) : page_k(t, rpage)) + static_cast<int64_t>(tt % t.P) * rb;
+    }
     uint8_t* dclu = page >= 0 ? (half ? page_v(t, page) : page_k(t, page)) + static_cast<int64_t>(row) * rb : nullptr;
     for (int o = hl * 16; o < rb; o += 16 * 16) {
       const uint4 v = *reinterpret_cast<const uint4*>(src + o);
-      *reinterpret_cast<uint4*>(dring + o) = v;
+      if (dring) *reinterpret_cast<uint4*>(dring + o) = v;
       if (dclu) *reinterpret_cast<uint4*>(dclu + o) = v;
     }
   }
@@ -2212,11 +2216,16 @@ __global__ void __launch_bounds__(256) k_flat_topk(DevTables t, const float* q, 
   __syncthreads();
   bool dg = false;
   for (int c = threadIdx.x; c < n; c += blockDim.x) {
-    const int s = slots[c];
-    const bool ib = bufs[c];
-    sim[c] = exact_cos(qf, nq, (ib ? t.brep64 : t.rep64) + static_cast<int64_t>(s) * d,
-                       ib ? t.bnorm[s] : t.rnorm[s], d, dg);
-    key[c] = 2LL * t.cid[s] + (ib ? 1 : 0);
+    if (!slots) {  // visual_topk (index.cpp:192-208): partitions 0..n-1, ties to the lower id
+      sim[c] = exact_cos(qf, nq, t.vrep + static_cast<int64_t>(c) * d, t.vnorm[c], d, dg);
+      key[c] = c;
+    } else {
+      const int s = slots[c];
+      const bool ib = bufs[c];
+      sim[c] = exact_cos(qf, nq, (ib ? t.brep64 : t.rep64) + static_cast<int64_t>(s) * d,
+                         ib ? t.bnorm[s] : t.rnorm[s], d, dg);
+      key[c] = 2LL * t.cid[s] + (ib ? 1 : 0);
+    }
     taken[c] = 0;
   }
   if (dg) set_err(t, DERR_DEGENERATE);

@@ -310,7 +310,8 @@ int launch_exact_stats(const DevTables& t, const AppendRun* runs, int32_t n_runs
                        const int32_t* idx, const void* stage_k, cudaStream_t st);
 
 // Flat top-k (oracle_flat_topk) of one query over an explicit candidate list.
-// gscratch: n * 17 + 16 bytes of global scratch, used when the arrays exceed shared memory
+// gscratch: n * 17 + 16 bytes of global scratch, used when the arrays exceed shared memory;
+// slots == nullptr ranks the visual partitions 0..n-1 instead (visual_topk)
 int launch_flat_topk(const DevTables& t, const float* q, const int32_t* slots,
                      const uint8_t* bufs, int32_t n, int32_t k, int32_t* out_idx,
                      uint8_t* gscratch, cudaStream_t st);

@@ -989,7 +989,7 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve_spec(DevTables t, Ing
     const int s = S.cslot[S.win[u]];
     a.ev_kind[orow0 + u] = S.kind[u];
     a.ev_slot[orow0 + u] = s;
-    t.ring_owner[(static_cast<int64_t>(dom) * t.W + a.ring_slot) * tmax + cur + u] = s;
+    if (a.ring_slot >= 0) t.ring_owner[(static_cast<int64_t>(dom) * t.W + a.ring_slot) * tmax + cur + u] = s;
   }
   // rank of each committed token among its slot's member / buffer rows (warp per slot)
   for (int ts = warp; ts < nts; ts += RS_WARPS) {

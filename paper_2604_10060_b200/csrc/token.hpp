@@ -64,6 +64,11 @@ class TokenContext {
   void set_timing(bool on) { timing_ = on; }
   const double* step_timing() const { return step_t_; }
   void profile(double* out);  // mean select-phase cycles over domains (out[8])
+  // the baseline's window_frames argument (retrieval.cpp:166-254) empty: nothing attended without
+  // a fetch (the component-level retrieve_token_baseline call)
+  void reset_window() { window_.clear(); }
+  // RetrievalResult fetched_frames / context_frames of the last query (parity mode)
+  const std::vector<std::int64_t>& last_frames(int which) const { return which == 0 ? fetched_ : context_; }
 
  private:
   kvc_cfg cfg_;
@@ -96,6 +101,7 @@ class TokenContext {
   std::vector<std::int64_t> attc_, bnd_;
   double ttft_ = 0.0, recall_ = -1.0;
   std::uint64_t digest_ = 0;
+  std::vector<std::int64_t> fetched_, context_;
   // baseline ledger totals (cause Retrieval, retrieval.cpp:224-229)
   std::int64_t led_ops_ = 0, led_bytes_ = 0;
   double led_cost_ = 0.0;

@@ -237,10 +237,25 @@ void TokenContext::decode_step(std::int64_t qid, const float* q, int q_mem, floa
       if (std::binary_search(ctx.begin(), ctx.end(), gt[i])) hit += 1;
     recall_ = static_cast<double>(hit) / static_cast<double>(n_gt);
   }
+  fetched_.clear();
+  context_.clear();
   if (cfg_.parity_mode) {  // attended (frame, token) lists and the digest
-    std::vector<std::uint32_t> w(static_cast<std::size_t>(L_) * ta_.wcap);
+    std::vector<std::uint32_t> w(static_cast<std::size_t>(L_) * ta_.wcap), pk(static_cast<std::size_t>(L_) * ta_.wcap);
     KVC_CUDA(cudaMemcpyAsync(w.data(), ta_.attw, w.size() * 4, cudaMemcpyDeviceToHost, st_));
+    KVC_CUDA(cudaMemcpyAsync(pk.data(), ta_.pick, pk.size() * 4, cudaMemcpyDeviceToHost, st_));
     KVC_CUDA(cudaStreamSynchronize(st_));
+    // fetched_frames: frames of the picked tokens (retrieval.cpp:210-213); context_frames: frames
+    // with attended entries
+    for (std::size_t o = 0; o < fid_.size(); ++o) {
+      if (h_hit_[o]) context_.push_back(fid_[o]);
+      bool picked = false;
+      for (int l = 0; l < L_ && !picked; ++l)
+        for (std::int64_t i = fstart_[o]; i < fstart_[o] + ft_[o] && !picked; ++i)
+          picked = (pk[static_cast<std::size_t>(l) * ta_.wcap + i / 32] >> (i % 32)) & 1u;
+      if (picked) fetched_.push_back(fid_[o]);
+    }
+    std::sort(context_.begin(), context_.end());
+    std::sort(fetched_.begin(), fetched_.end());
     std::uint64_t h = 1469598103934665603ull;
     for (int l = 0; l < L_; ++l) {
       auto& a = att_[static_cast<std::size_t>(l)];
