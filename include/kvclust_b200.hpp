@@ -112,8 +112,8 @@ struct BuildConfig {
 
 class HierIndex {
  public:
-  HierIndex() = default;
-  HierIndex(std::int32_t dim, std::int32_t layers) : dim_(dim), layers_(layers) {}
+  HierIndex();
+  HierIndex(std::int32_t dim, std::int32_t layers);
   HierIndex(HierIndex&&) noexcept;
   HierIndex& operator=(HierIndex&&) noexcept;
   HierIndex(const HierIndex&) = delete;  // the state is a device context
@@ -173,6 +173,8 @@ class HierIndex {
   // host-assembled state not yet installed on the device (add_partition / add_cluster before the
   // first device operation)
   std::vector<VisualPartition> pending_parts_;
+  std::vector<Embedding> pending_first_visual_;                                   // per pending partition
+  std::vector<std::vector<std::pair<std::int64_t, Embedding>>> pending_appends_;  // append_frame calls
   std::vector<ClusterRecord> pending_clusters_;
   std::vector<std::uint8_t> pending_adopted_;
   mutable std::unique_ptr<View> view_;
@@ -180,6 +182,7 @@ class HierIndex {
   const View& view() const;
   void install_pending() const;
   friend class TieredStore;
+  friend class StreamEngine;
 };
 
 DVec compute_representative(const std::vector<KVEntry>& members);

@@ -70,5 +70,30 @@ def build(verbose: bool = False) -> str:
     return LIB
 
 
+REF_INC = os.environ.get("KVCLUST_REF_INCLUDE", "/root/reference/proj/core/include")
+JSON_INC = "/opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty"
+DROPIN_SRC = os.path.join(HERE, "dropin", "kvclust_b200.cpp")
+DROPIN_LIB = os.path.join(OUT, "libkvclust_b200.so")
+
+
+def build_dropin() -> str | None:
+    """The C++ drop-in (include/kvclust_b200*.hpp): libkvclust_b200.so over libkvc.so. It keeps the
+    reference's header-only utilities (vecmath / error / rng / clustering / workload headers), so
+    it is built where those headers are (the reference install a drop-in user has); elsewhere the
+    prebuilt library is kept."""
+    if not os.path.exists(os.path.join(REF_INC, "kvclust", "vecmath.hpp")):
+        return DROPIN_LIB if os.path.exists(DROPIN_LIB) else None
+    deps = [DROPIN_SRC, LIB, os.path.join(ROOT, "include", "kvclust_b200.hpp"),
+            os.path.join(ROOT, "include", "kvclust_b200_engine.hpp"), os.path.join(ROOT, "include", "kvc.h")]
+    if os.path.exists(DROPIN_LIB) and all(os.path.getmtime(p) <= os.path.getmtime(DROPIN_LIB) for p in deps):
+        return DROPIN_LIB
+    cmd = ["g++", "-std=c++20", "-O2", "-fPIC", "-shared", "-Wall", "-Wextra", "-Wno-unused-parameter",
+           "-ffp-contract=off", "-I", os.path.join(ROOT, "include"), "-I", os.path.join(ROOT, "include", "kvclust_dropin"),
+           "-I", REF_INC, "-I", JSON_INC, DROPIN_SRC, "-o", DROPIN_LIB, "-L" + OUT, "-lkvc", "-Wl,-rpath,$ORIGIN"]
+    subprocess.run(cmd, check=True)
+    return DROPIN_LIB
+
+
 if __name__ == "__main__":
     print(build(verbose="-v" in sys.argv))
+    print(build_dropin())

@@ -2156,9 +2156,14 @@ __global__ void __launch_bounds__(ATT_THREADS + 32) k_attend(DevTables t, Decode
         a.part_ml[pi * 2] = M;
         a.part_ml[pi * 2 + 1] = lsum;
       }
-      __threadfence();
+      // the consumers' partial writes are ordered before the barrier; ONE gpu-scope fence by the
+      // signalling thread after it is cumulative over them (as a grid barrier's release), so the
+      // other 255 threads no longer stall on a membar per item
       named_sync(1, ATT_THREADS);
-      if (tid == 0) last_flag = (atomicAdd(&a.dom_done[dom], 1) + 1 == a.n_items[dom]);
+      if (tid == 0) {
+        __threadfence();
+        last_flag = (atomicAdd(&a.dom_done[dom], 1) + 1 == a.n_items[dom]);
+      }
       named_sync(1, ATT_THREADS);
       if (last_flag) {  // split-KV combine of all partials of the domain
         __threadfence();
@@ -2188,6 +2193,82 @@ __global__ void __launch_bounds__(ATT_THREADS + 32) k_attend(DevTables t, Decode
       for (int i = 0; i < OPL; ++i) o_run[i] = 0.f;
       named_sync(1, ATT_THREADS);  // wo / last_flag reuse
     }
+  }
+}
+
+// Attention for head widths without a K6 instantiation (d not in {32, 64, 128, 256}; the
+// reference's own tests use d = 8, 16, ...): one CTA per domain walks the domain's page
+// descriptors (the same work list K6 reads), a warp per token with lanes over the dims
+// (warp-reduced q.k), online softmax in exp2 space per warp, warps merged at the end. Not a
+// bandwidth path -- the headline shapes take K6.
+constexpr int AG_WARPS = 8;
+constexpr int AG_MAXD = 256;
+__global__ void __launch_bounds__(AG_WARPS * 32) k_attend_generic(DevTables t, DecodeArgs a) {
+  const int l = blockIdx.x, d = t.d, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __shared__ float qs[AG_MAXD];
+  __shared__ float wm[AG_WARPS], wl[AG_WARPS];
+  __shared__ float wo[AG_WARPS][AG_MAXD];
+  if (a.n_items[l] == 0) return;  // K4 wrote the zero row
+  for (int i = threadIdx.x; i < d; i += blockDim.x) qs[i] = a.q[static_cast<int64_t>(l) * d + i];
+  __syncthreads();
+  float m = -INFINITY, lsum = 0.f, o[AG_MAXD / 32];
+#pragma unroll
+  for (int k = 0; k < AG_MAXD / 32; ++k) o[k] = 0.f;
+  const int nd = a.n_desc[l];
+  int tok = 0;  // running token index over the domain's attended pages
+  for (int di = 0; di < nd; ++di) {
+    const int4 dsc = a.desc[static_cast<int64_t>(l) * a.max_desc + di];
+    const int fill = dsc.y & 0xffff;
+    const unsigned long long mask =
+        (static_cast<unsigned long long>(static_cast<uint32_t>(dsc.w)) << 32) | static_cast<uint32_t>(dsc.z);
+    const uint8_t* kp = page_k(t, dsc.x);
+    const uint8_t* vp = page_v(t, dsc.x);
+    for (int r = 0; r < fill; ++r, ++tok) {
+      if (((mask >> r) & 1ull) == 0 || tok % AG_WARPS != warp) continue;
+      float dot = 0.f;
+      for (int i = lane; i < d; i += 32) {
+        const float kv = t.kv_bf16 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(kp)[static_cast<int64_t>(r) * d + i])
+                                   : reinterpret_cast<const float*>(kp)[static_cast<int64_t>(r) * d + i];
+        dot = fmaf(qs[i], kv, dot);
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, off);
+      const float s2 = dot * a.scale_log2;
+      const float mn = fmaxf(m, s2);
+      const float corr = exp2f(m - mn), p = exp2f(s2 - mn);
+      lsum = lsum * corr + p;
+#pragma unroll
+      for (int k = 0; k < AG_MAXD / 32; ++k) {
+        const int i = lane + 32 * k;
+        if (i < d) {
+          const float vv = t.kv_bf16 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(vp)[static_cast<int64_t>(r) * d + i])
+                                     : reinterpret_cast<const float*>(vp)[static_cast<int64_t>(r) * d + i];
+          o[k] = o[k] * corr + p * vv;
+        }
+      }
+      m = mn;
+    }
+  }
+  if (lane == 0) {
+    wm[warp] = m;
+    wl[warp] = lsum;
+  }
+#pragma unroll
+  for (int k = 0; k < AG_MAXD / 32; ++k)
+    if (lane + 32 * k < d) wo[warp][lane + 32 * k] = o[k];
+  __syncthreads();
+  float M = -INFINITY;
+  for (int w = 0; w < AG_WARPS; ++w) M = fmaxf(M, wm[w]);
+  float den = 0.f;
+  for (int w = 0; w < AG_WARPS; ++w)
+    if (wm[w] != -INFINITY) den += wl[w] * exp2f(wm[w] - M);
+  for (int i = threadIdx.x; i < d; i += blockDim.x) {
+    float num = 0.f;
+    for (int w = 0; w < AG_WARPS; ++w)
+      if (wm[w] != -INFINITY) num += wo[w][i] * exp2f(wm[w] - M);
+    const float v = den > 0.f ? num / den : 0.f;
+    a.out[static_cast<int64_t>(l) * d + i] = v;
+    for (int r = 0; r < a.peer.n; ++r) a.peer.out[r][static_cast<int64_t>(a.peer.dom_offset + l) * d + i] = v;
   }
 }
 
@@ -2447,7 +2528,10 @@ int launch_attend(const DevTables& t, const DecodeArgs& a, cudaStream_t st) {
     case 257: return launch_attend_t<128, true>(t, a, st, false);
     case 512: return launch_attend_t<256, false>(t, a, st, false);
     case 513: return launch_attend_t<256, true>(t, a, st, false);
-    default: return 0;
+    default:
+      if (t.d > AG_MAXD) return 0;
+      k_attend_generic<<<t.L, AG_WARPS * 32, 0, st>>>(t, a);
+      return 1;
   }
 }
 
@@ -2486,7 +2570,12 @@ int launch_decode(const DevTables& t, const DecodeArgs& a, cudaStream_t st, cuda
     case 257: n += launch_attend_t<128, true>(t, a, st, pdl); break;
     case 512: n += launch_attend_t<256, false>(t, a, st, pdl); break;
     case 513: n += launch_attend_t<256, true>(t, a, st, pdl); break;
-    default: break;
+    default:
+      if (t.d <= AG_MAXD) {  // head widths K6 is not instantiated for
+        k_attend_generic<<<t.L, AG_WARPS * 32, 0, st>>>(t, a);
+        n += 1;
+      }
+      break;
   }
   if (k4_done && pdl) cudaEventRecord(k4_done, st);
   if (ev) {

@@ -102,3 +102,22 @@ def test_host_split_rejects_too_few_points():
 def test_host_split_rejects_zero_vector():
     with pytest.raises(api.DegenerateVector):
         api.host_split_two(np.zeros((3, 8), np.float32), 0)
+
+
+def test_cpp_dropin_library_exports_the_reference_api():
+    """libkvclust_b200.so (the C++ drop-in) defines the reference's hot-path API in namespace
+    kvclust: StreamEngine / run_stream (engine.hpp), HierIndex / build_index (index.hpp),
+    TieredStore (store.hpp), Maintainer / updated_stats / tau (maintainer.hpp), retrieve /
+    oracle_flat_topk / retrieve_token_baseline (retrieval.hpp)."""
+    import subprocess
+
+    lib = os.path.join(ROOT, "paper_2604_10060_b200", "_lib", "libkvclust_b200.so")
+    if not os.path.exists(lib):
+        pytest.skip("drop-in not built (needs the reference headers at build time)")
+    out = subprocess.run(["nm", "-DC", "--defined-only", lib], capture_output=True, text=True, check=True).stdout
+    for sym in ["kvclust::run_stream(", "kvclust::StreamEngine::process(", "kvclust::StreamEngine::finish()",
+                "kvclust::build_index(", "kvclust::HierIndex::semantic_topk(", "kvclust::HierIndex::visual_topk(",
+                "kvclust::TieredStore::fetch(", "kvclust::Maintainer::on_insert(", "kvclust::Maintainer::place_frame(",
+                "kvclust::Maintainer::materialize(", "kvclust::retrieve(", "kvclust::oracle_flat_topk(",
+                "kvclust::retrieve_token_baseline(", "kvclust::updated_stats(", "kvclust::tau("]:
+        assert sym in out, sym

@@ -111,3 +111,16 @@ def test_flat_topk_beyond_shared_memory(ref_lib):
         assert kv.flat_topk(q, 0, k) == ref.flat_topk(q, 0, k)
     q = keys[0, 0].copy()  # the tied direction: 50 exact ties broken by id
     assert kv.flat_topk(q, 0, 60) == ref.flat_topk(q, 0, 60)
+
+
+@pytest.mark.parametrize("d", [8, 16, 48])
+def test_head_widths_without_a_k6_instantiation(ref_lib, d):
+    """d outside {32, 64, 128, 256} (the reference's own unit tests use d = 8 / 16): selection and
+    bookkeeping bit-exact, attention through the generic kernel within 1e-3 of the fp64 oracle."""
+    s = po.gen_stream_restated(po.StreamCfg.make(n_scenes=3, frames_per_scene=8, tokens_per_frame=12, d=d,
+                                                 L=3, n_queries=8, semantic_noise=0.05, seed=13))
+    ecfg = po.EngineCfg.make(build_batch_frames=6, k_v=2, k_s=3)
+    r = Replay(s, ecfg, po.RefDriver(ecfg, s.d, s.L, checks=False)).run()
+    r.final_compare()
+    assert r.mismatches == [], r.mismatches[:5]
+    assert r.att_err < 1e-3
