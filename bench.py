@@ -118,13 +118,17 @@ class Clocks:
 
 
 def traffic_from_profiles():
-    """dram bytes per attention launch from the committed ncu --set full summary, if any."""
+    """dram bytes per attention launch from the committed `ncu --set full` capture
+    (profiles/ncu_attend_summary.json, written by scripts/summarize_profiles.py) and where it came
+    from: the profile round, the commit it was captured at, the command. ncu cannot run inside the
+    timed bench, so the number is stamped rather than silently reused."""
     path = os.path.join(ROOT, "profiles", "ncu_attend_summary.json")
     try:
         with open(path) as f:
-            return json.load(f).get("dram_bytes_per_launch")
+            j = json.load(f)
+        return j.get("dram_bytes_per_launch"), {k: j.get(k) for k in ("round", "head", "captured", "command", "source")}
     except Exception:
-        return None
+        return None, None
 
 
 # --------------------------------------------------------------------------- reference arm
@@ -398,6 +402,7 @@ def main():
     att_time = float(np.mean(att_us)) * 1e-6
     achieved = att_bytes / att_time / 1e9
     step_bytes = att_bytes + D * N_CLUST * HEAD_DIM * 8 + D * HEAD_DIM * 8  # + fp64 centroids + q/out
+    traffic, traffic_src = traffic_from_profiles()
     line = {
         "metric": METRIC, "value": round(us_step, 3), "unit": "us/step", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": us_step / 1e3,
@@ -406,7 +411,8 @@ def main():
         "e2e": {"value": round(decode_e2e_ms * 1e3 / args.steps, 3), "unit": "us/step",
                 "h2d_bytes_per_step": D * world * HEAD_DIM * 4, "d2h_bytes_per_step": D * world * HEAD_DIM * 4},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
-                     "frac": round(achieved / hbm, 4), "traffic": traffic_from_profiles(),
+                     "frac": round(achieved / hbm, 4), "traffic": traffic,
+                     "traffic_source": traffic_src,
                      "kernel": "k_attend (split-KV attention over selected clusters + window)",
                      "peak_source": src, "algorithmic_bytes_per_launch": att_bytes,
                      "kernel_us": round(att_time * 1e6, 2),

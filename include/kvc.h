@@ -343,11 +343,13 @@ KVC_API int kvc_debug_assign_check(kvc_ctx* ctx, const void* keys, int32_t T, in
                                    double* out4);
 KVC_API int kvc_debug_div_check(uint64_t n, uint64_t seed, int32_t max_den, uint64_t* mismatches);
 KVC_API int kvc_debug_resolve_profile(kvc_ctx* ctx, double* out);
-/* Host-event slow path profile (cumulative since creation / the last reset), out8: microseconds in
+/* Host-event slow path profile (cumulative since creation / the last reset), out10: microseconds in
  * host events (split / seed) total, of which staging + download of the cluster rows, split k-means
  * (split_two calls), host Eq. 1/2 statistics of the children, slot / page / list uploads; then the
- * relaunch-and-wait of a domain after an event; the number of host events and of split_two calls. */
-KVC_API int kvc_debug_event_profile(kvc_ctx* ctx, double* out8, int32_t reset);
+ * relaunch-and-wait of a domain after an event; the number of host events and of split_two calls;
+ * speculative split k-means launched / consumed (the next domain's split 2-means'd on a side
+ * stream during a relaunch). */
+KVC_API int kvc_debug_event_profile(kvc_ctx* ctx, double* out10, int32_t reset);
 /* Enables per-phase CUDA-event timing (off by default: it adds event records). */
 KVC_API void kvc_set_timing(kvc_ctx* ctx, int32_t on);
 

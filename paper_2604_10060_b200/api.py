@@ -497,11 +497,11 @@ class ClusterKVCache:
         return t
 
     EVENT_KEYS = ("events_us", "stage_us", "kmeans_us", "host_stats_us", "upload_us", "relaunch_us", "events",
-                  "split_two_calls")
+                  "split_two_calls", "spec_splits", "spec_hits")
 
     def event_profile(self, reset: bool = False) -> dict:
         """Host-event slow-path profile (kvc_debug_event_profile), cumulative."""
-        t = np.zeros(8)
+        t = np.zeros(10)
         _check(lib().kvc_debug_event_profile(self.h, _p(t, f64p), 1 if reset else 0))
         return dict(zip(self.EVENT_KEYS, t.round(1).tolist()))
 

@@ -678,8 +678,8 @@ int kvc_last_predicted(kvc_ctx* ctx, int32_t layer, int64_t* ids, int32_t cap) {
   return copy_out(ls[static_cast<std::size_t>(layer)].predicted, ids, cap);
 }
 
-int kvc_debug_event_profile(kvc_ctx* ctx, double* out8, int32_t reset) {
-  return guard([&] { F(ctx).event_profile(out8, reset != 0); });
+int kvc_debug_event_profile(kvc_ctx* ctx, double* out10, int32_t reset) {
+  return guard([&] { F(ctx).event_profile(out10, reset != 0); });
 }
 
 int kvc_debug_resolve_profile(kvc_ctx* ctx, double* out) {

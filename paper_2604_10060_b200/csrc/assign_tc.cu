@@ -310,7 +310,7 @@ __global__ void __launch_bounds__(AS_THREADS, 1) k_assign_tc(DevTables t, Ingest
       const int c = ti[k];
       rp[k] = nullptr;
       nr[k] = 1.0;
-      if (c >= 0 && tv[k] >= cut) {
+      if (c >= 0 && (a.exact_all || tv[k] >= cut)) {
         const int s = cs[c];
         const bool ib = cbuf[c];
         rp[k] = (ib ? t.brep64 : t.rep64) + static_cast<int64_t>(s) * d;

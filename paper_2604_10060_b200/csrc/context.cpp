@@ -101,6 +101,11 @@ Context::Context(const kvc_cfg& cfg, int d, int L) : cfg_(cfg), d_(d), L_(L) {
 
 Context::~Context() {
   if (st_) cudaStreamSynchronize(st_);
+  if (spec_st_) {
+    cudaStreamSynchronize(spec_st_);
+    cudaStreamDestroy(spec_st_);
+  }
+  if (spec_.ev) cudaEventDestroy(spec_.ev);
   if (xs_) {
     cudaStreamSynchronize(xs_);
     cudaStreamDestroy(xs_);
@@ -277,6 +282,8 @@ void Context::alloc_device() {
     resolve_seq_ = e && std::string(e) == "seq";
     const char* rl = std::getenv("KVC_RELAUNCH");  // "spec": speculative kernel for relaunches too
     relaunch_seq_ = !(rl && std::string(rl) == "spec");
+    const char* ss = std::getenv("KVC_SPEC_SPLIT");  // 0: no speculative split k-means
+    spec_split_ = !(ss && std::string(ss) == "0");
     const char* g = std::getenv("KVC_ASSIGN");  // "simt": the fp32 CUDA-core tile
     assign_tc_ = !(g && std::string(g) == "simt") && assign_tc_supported(t_) &&
                  make_key_tensor_map(key_maps_[0], fkbuf_[0], d, t_.tmax, L) &&
@@ -1155,6 +1162,7 @@ void Context::launch_round(const std::vector<int>& active, const std::vector<int
     KVC_CUDA(cudaEventRecord(ev_act_[slot], st_));
   }
   round_timed_ = timing_;
+  ia_.exact_all = round_after_event_ ? 1 : 0;
   if (timing_) KVC_CUDA(cudaEventRecord(ev_[0], st_));
   launches_ += launch_build_cands(t_, ia_, st_);
   if (timing_) KVC_CUDA(cudaEventRecord(ev_[1], st_));
@@ -1206,6 +1214,10 @@ void Context::run_inserts(std::int64_t frame_id, std::int64_t pid, int T, std::i
   const int ring_slot = ia_.ring_slot;
   const bool eager = !cfg_.defer_host_splits;
   if (l_hi < 0) l_hi = L_;
+  if (spec_.active) {  // a speculation of an earlier frame is never consumed
+    KVC_CUDA(cudaEventSynchronize(spec_.ev));
+    spec_.active = false;
+  }
   std::vector<int> cursor(static_cast<std::size_t>(L_), 0), replayed(static_cast<std::size_t>(L_), 0);
   for (int l = l_lo; l < l_hi; ++l) cursor[static_cast<std::size_t>(l)] = replayed[static_cast<std::size_t>(l)] = tok0;
   std::vector<int> active;
@@ -1343,6 +1355,8 @@ void Context::run_inserts(std::int64_t frame_id, std::int64_t pid, int T, std::i
     }
     const std::int64_t id = handle_host_event(frame_id, pid, l, stop, h_stop_[L_ + l], h_stop_[2 * L_ + l]);
     ingest_t_[9] += 1.0;  // host events this frame
+    // the next domain's pending split, 2-means'd on the side while this domain is relaunched
+    if (spec_split_ && l + 1 < l_hi && split_dev_min_ > 0) spec_split_launch(l + 1, T);
     if (assigned) assigned[static_cast<std::size_t>(l) * T + stop] = id;
     cursor[static_cast<std::size_t>(l)] = stop + 1;
     replayed[static_cast<std::size_t>(l)] = stop + 1;
@@ -1510,7 +1524,10 @@ std::vector<std::int64_t> Context::split_pool(std::int64_t pid, int layer, bool 
       return;
     }
     const auto k0 = now();
-    const KMeansOut halves = split_two_staged(grp, mix_seed(maint_seed_, static_cast<std::uint64_t>(split_counter_++)));
+    KMeansOut halves;
+    const std::uint64_t ctr = static_cast<std::uint64_t>(split_counter_++);
+    if (!(depth == 0 && static_cast<std::int64_t>(grp.size()) == rows && spec_split_take(spec_slot_hint_, static_cast<int>(grp.size()), ctr, halves)))
+      halves = split_two_staged(grp, mix_seed(maint_seed_, ctr));
     evt_t_[2] += us(k0, now());
     evt_t_[7] += 1.0;
     mstats_[5] += 1;  // split_ops_total
@@ -1591,6 +1608,93 @@ KMeansOut Context::split_two_staged(const std::vector<int>& grp, std::uint64_t s
   return o;
 }
 
+// Stage + 2-means of the first pending split of domains [from_layer, L) on the side stream, with
+// the seed of the current split counter (see SpecSplit in context.hpp).
+void Context::spec_split_launch(int from_layer, int T) {
+  int l = -1;
+  for (int x = from_layer; x < L_; ++x)
+    if (h_stop_[x] < T) {
+      l = x;
+      break;
+    }
+  if (l < 0) return;
+  const int kind = h_stop_[L_ + l];
+  if (kind != EV_SPLIT && kind != EV_EAGER) return;  // seeds need no k-means
+  const std::int32_t slot = h_stop_[2 * L_ + l];
+  const int tok = h_stop_[l];
+  if (slot < 0 || static_cast<std::size_t>(slot) >= slot_id_.size() || slot_id_[static_cast<std::size_t>(slot)] < 0) return;
+  const std::int64_t cid = slot_id_[static_cast<std::size_t>(slot)];
+  if (is_host(cid)) return;  // the settle re-resolves such a token (residence changed between frames)
+  const Cluster& c = C(cid);
+  // rows at the event = the cluster's rows before this frame + this domain's tokens routed to it
+  // before the stop (committed on the device by the first round, replayed on the host later)
+  std::int64_t n = static_cast<std::int64_t>(c.members.size() + c.buffer.size()) + 1;
+  const std::int32_t* evs = h_evs_ + static_cast<std::size_t>(l) * t_.tmax;
+  for (int t = 0; t < tok; ++t) n += evs[t] == slot ? 1 : 0;
+  if (n < std::max(2, split_dev_min_) || d_ > 256) return;
+  if (!spec_st_) {
+    KVC_CUDA(cudaStreamCreateWithFlags(&spec_st_, cudaStreamNonBlocking));
+    KVC_CUDA(cudaEventCreateWithFlags(&spec_.ev, cudaEventDisableTiming));
+  }
+  if (spec_.active) KVC_CUDA(cudaEventSynchronize(spec_.ev));  // its buffers are about to be reused
+  if (n + 1 > spec_.cap) {
+    spec_.cap = std::max<std::int64_t>(n + 1, spec_.cap * 2);
+    const std::size_t rb = static_cast<std::size_t>(d_) * es_;
+    spec_.dk = dalloc(static_cast<std::size_t>(spec_.cap) * rb);
+    spec_.dv = dalloc(static_cast<std::size_t>(spec_.cap) * rb);
+    spec_.df32 = static_cast<float*>(dalloc(static_cast<std::size_t>(spec_.cap) * d_ * 4));
+    spec_.scratch = static_cast<double*>(dalloc((static_cast<std::size_t>(spec_.cap) * (2 * d_ + 3) + 1) * 8));
+    spec_.d_i = static_cast<std::int32_t*>(dalloc((2 * static_cast<std::size_t>(spec_.cap) + 4) * 4));
+    spec_.d_obj = static_cast<double*>(dalloc(8));
+    spec_.h_i = static_cast<std::int32_t*>(halloc((2 * static_cast<std::size_t>(spec_.cap) + 4) * 4));
+    spec_.h_obj = static_cast<double*>(halloc(8));
+  }
+  const std::uint64_t counter = static_cast<std::uint64_t>(split_counter_);
+  Rng64 rng(mix_seed(maint_seed_, counter));
+  const int first = static_cast<int>(rng.index(static_cast<std::size_t>(n)));
+  const double uni = rng.uniform();
+  // the side stream starts after everything queued so far (the first round's commits)
+  KVC_CUDA(cudaEventRecord(spec_.ev, st_));
+  KVC_CUDA(cudaStreamWaitEvent(spec_st_, spec_.ev, 0));
+  const std::size_t rb = static_cast<std::size_t>(d_) * es_;
+  launches_ += launch_gather_cluster(t_, slot, 1, spec_.dk, spec_.dv, 0, spec_st_);
+  const std::size_t frow = static_cast<std::size_t>(l) * t_.tmax + tok;
+  KVC_CUDA(cudaMemcpyAsync(static_cast<std::uint8_t*>(spec_.dk) + static_cast<std::size_t>(n - 1) * rb,
+                           static_cast<std::uint8_t*>(d_fk_) + frow * rb, rb, cudaMemcpyDeviceToDevice, spec_st_));
+  launches_ += launch_to_f32(t_, spec_.dk, spec_.df32, n * d_, spec_st_);
+  for (std::int64_t i = 0; i < n; ++i) spec_.h_i[i] = static_cast<std::int32_t>(i);
+  KVC_CUDA(cudaMemcpyAsync(spec_.d_i, spec_.h_i, static_cast<std::size_t>(n) * 4, cudaMemcpyHostToDevice, spec_st_));
+  launches_ += launch_split_two(spec_.df32, spec_.d_i, static_cast<int>(n), d_, first, uni, spec_.scratch, spec_.d_i + n,
+                                spec_.d_i + 2 * n, spec_.d_obj, spec_st_);
+  KVC_CUDA(cudaMemcpyAsync(spec_.h_i + n, spec_.d_i + n, static_cast<std::size_t>(n + 4) * 4, cudaMemcpyDeviceToHost, spec_st_));
+  KVC_CUDA(cudaMemcpyAsync(spec_.h_obj, spec_.d_obj, 8, cudaMemcpyDeviceToHost, spec_st_));
+  KVC_CUDA(cudaEventRecord(spec_.ev, spec_st_));
+  spec_.active = true;
+  spec_.layer = l;
+  spec_.tok = tok;
+  spec_.slot = slot;
+  spec_.rows = n;
+  spec_.counter = counter;
+  spec_tries_ += 1;
+}
+
+bool Context::spec_split_take(std::int32_t slot, int n, std::uint64_t counter, KMeansOut& out) {
+  if (!spec_.active || slot < 0) return false;
+  const bool hit = spec_.slot == slot && spec_.rows == n && spec_.counter == counter;
+  if (!hit) return false;
+  KVC_CUDA(cudaEventSynchronize(spec_.ev));
+  spec_.active = false;
+  const std::int32_t* meta = spec_.h_i + 2 * static_cast<std::size_t>(n);
+  if (meta[3] != 0) return false;  // a degenerate row: the normal path raises it
+  out.assign.assign(spec_.h_i + n, spec_.h_i + 2 * static_cast<std::size_t>(n));
+  out.k_live = meta[0];
+  out.iterations = meta[1];
+  out.degenerate = meta[2] != 0;
+  out.objective = *spec_.h_obj;
+  spec_hits_ += 1;
+  return true;
+}
+
 KMeansOut Context::debug_split_two_dev(const float* pts, int n, std::uint64_t seed) {
   if (n < 2) fail(-6, "split_two: need at least 2 points");
   ensure_stage(n + 1);
@@ -1659,7 +1763,9 @@ std::int64_t Context::handle_host_event(std::int64_t frame_id, std::int64_t pid,
   ids.push_back({frame_id, tok});
   forget(cid);
   drop_cluster(cid);
+  spec_slot_hint_ = slot;
   const std::vector<std::int64_t> kids = split_pool(pid, layer, false, std::move(ids), rows + 1, 0);
+  spec_slot_hint_ = -1;
   for (std::int64_t k : kids)  // home_of (maintainer.cpp:62-70)
     for (const Member& m : C(k).members)
       if (m.frame == frame_id && m.token == tok) return k;

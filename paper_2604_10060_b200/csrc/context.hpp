@@ -346,12 +346,44 @@ class Context {
   // host-event (split / seed) slow-path profile, cumulative: total, stage + download, split
   // k-means, host Eq. 1/2 stats, slot/page uploads, relaunch after an event, #events, #split_two
   double evt_t_[8] = {0};
+  // Speculative split k-means (host-event pipelining): while a domain is relaunched after its
+  // split, the NEXT domain's pending split (its first event of the frame, known from the first
+  // round) is already staged and 2-means'd on a side stream with the seed the global split
+  // counter will give it if the relaunched domain splits no more (maintainer.cpp:222). The
+  // settle takes the result when counter, cluster and row count match, else computes it anew --
+  // nothing is committed speculatively, so a misprediction costs only the side work.
+  struct SpecSplit {
+    bool active = false;
+    int layer = -1, tok = -1;
+    std::int32_t slot = -1;
+    std::int64_t rows = 0;  // staged rows incl. the triggering token
+    std::uint64_t counter = 0;
+    cudaEvent_t ev = nullptr;
+    void *dk = nullptr, *dv = nullptr;
+    float* df32 = nullptr;
+    std::int64_t cap = 0;  // rows the staging holds
+    double* scratch = nullptr;
+    std::int32_t* d_i = nullptr;  // idx[n] | assign[n] | meta[4]
+    double* d_obj = nullptr;
+    std::int32_t* h_i = nullptr;
+    double* h_obj = nullptr;
+  } spec_;
+  cudaStream_t spec_st_ = nullptr;
+  std::int32_t spec_slot_hint_ = -1;  // slot of the cluster an immediate split is settling
+  bool spec_split_ = true;  // KVC_SPEC_SPLIT=0 disables
+  std::int64_t spec_tries_ = 0, spec_hits_ = 0;
+  void spec_split_launch(int from_layer, int T);
+  bool spec_split_take(std::int32_t slot, int n, std::uint64_t counter, KMeansOut& out);
 
  public:
   void event_profile(double* out, bool reset) {
     for (int i = 0; i < 8; ++i) out[i] = evt_t_[i];
-    if (reset)
+    out[8] = static_cast<double>(spec_tries_);
+    out[9] = static_cast<double>(spec_hits_);
+    if (reset) {
       for (double& x : evt_t_) x = 0.0;
+      spec_tries_ = spec_hits_ = 0;
+    }
   }
 
  private:

@@ -135,6 +135,10 @@ struct IngestArgs {
   float* approx;           // [L][tmax][cmax] approximate cosines (K1)
   float margin;            // certified bound on |approx - exact| (cosine units)
   int32_t defer;           // MaintainerConfig::defer_host_splits
+  // the tile's epilogue computes the exact cosine of every top-M candidate, not only those within
+  // 2 margins of the best (a relaunch after a split: the new children take the best tokens, so
+  // the resolve would otherwise re-score the runner-up candidates from global memory per token)
+  int32_t exact_all;
   // outputs
   int32_t* ev_kind;        // [L][tmax]
   int32_t* ev_slot;        // [L][tmax]

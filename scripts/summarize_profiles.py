@@ -96,22 +96,30 @@ if os.path.exists(tok_csv):
     except StopIteration:
         pass
 lines += ["", "## `ncu --set full` captures", "",
-          "| kernel | duration us | DRAM read MB | DRAM write MB | DRAM % peak | SM % | achieved occupancy | regs |",
-          "|---|---|---|---|---|---|---|---|"]
+          "| kernel | duration us | DRAM read MB | DRAM write MB | DRAM % peak | SM % | tensor pipe % | achieved occupancy | regs |",
+          "|---|---|---|---|---|---|---|---|---|"]
 att = {}
-for kname in ("k_attend", "k_select3", "k_score_select2", "k_resolve_spec", "k_assign_tc", "k_approx", "k_topm",
-              "k_kmeans"):
+for kname in ("k_attend", "k_select3", "k_score_select", "k_resolve_spec", "k_resolve", "k_assign_tc", "k_approx",
+              "k_topm", "k_split_two", "k_kmeans"):
     for m in ncu_raw(kname)[:1]:
         dur = num(m.get("gpu__time_duration.sum"))
         rd = num(m.get("dram__bytes_read.sum"))
         wr = num(m.get("dram__bytes_write.sum"))
         lines.append(f"| {kname} | {dur} | {rd} | {wr} | {m.get('gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed')} | "
                      f"{m.get('sm__throughput.avg.pct_of_peak_sustained_elapsed')} | "
+                     f"{m.get('sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed')} | "
                      f"{m.get('sm__warps_active.avg.pct_of_peak_sustained_active')} | {m.get('launch__registers_per_thread')} |")
         if kname == "k_attend" and rd is not None:
             # ncu reports MB (1e6) in this section
+            import datetime
+
+            head = subprocess.run(["git", "-C", ROOT, "rev-parse", "--short", "HEAD"], capture_output=True,
+                                  text=True).stdout.strip()
             att = {"kernel": "k_attend", "dram_bytes_per_launch": int(((rd or 0) + (wr or 0)) * 1e6),
-                   "duration_us_ncu": dur, "source": f"profiles/{tag}_summary.md"}
+                   "duration_us_ncu": dur, "source": f"profiles/{tag}_summary.md", "round": tag, "head": head,
+                   "captured": datetime.datetime.utcnow().strftime("%Y-%m-%dT%H:%MZ"),
+                   "command": "ncu --set full --clock-control none -k regex:k_(attend|select3|score_select) -s 6 -c 2 "
+                              "python bench.py --steps 5 --warmup 3 --frames 5 (scripts/profile_round.sh)"}
 # maintenance / build slow paths (scripts/split_time.py, drift_ingest.py, build_time.py)
 slow = []
 for fn, title in (("split_time.txt", "GPU split k-means vs host (n, d, iterations, times)"),
