@@ -39,6 +39,18 @@ __device__ __forceinline__ bool better(double sa, long long ka, double sb, long 
   return sa > sb || (sa == sb && ka < kb);
 }
 
+// RN(a / b) for b > 0 given y = RN(1 / b): q1 = RN(a y) is within 2 ulps, one remainder
+// correction makes it faithful, the second is Markstein's correctly rounded step -- bit-identical
+// to __ddiv_rn (checked on the device by kvc_debug_div_check). One reciprocal serves every
+// element of an Eq. 3/4 update (they share the divisor n + 1).
+__device__ __forceinline__ double div_rcp(double a, double b, double y) {
+  const double q1 = __dmul_rn(a, y);
+  const double r1 = __fma_rn(-q1, b, a);
+  const double q2 = __fma_rn(r1, y, q1);
+  const double r2 = __fma_rn(-q2, b, a);
+  return __fma_rn(r2, y, q2);
+}
+
 // Warp arg-best over (sim, key, payload).
 __device__ __forceinline__ void warp_best(double& s, long long& k, int& p) {
 #pragma unroll

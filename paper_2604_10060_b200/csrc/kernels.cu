@@ -40,6 +40,15 @@ __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a,
 __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
 __device__ __forceinline__ double ddiv(double a, double b) { return __ddiv_rn(a, b); }
+// RN(a / b) for b > 0 given y = RN(1 / b): a faithful quotient + Markstein's correctly rounded
+// step, bit-identical to __ddiv_rn (devmath.cuh dm::div_rcp; kvc_debug_div_check)
+__device__ __forceinline__ double div_rcp(double a, double b, double y) {
+  const double q1 = __dmul_rn(a, y);
+  const double r1 = __fma_rn(-q1, b, a);
+  const double q2 = __fma_rn(r1, y, q1);
+  const double r2 = __fma_rn(-q2, b, a);
+  return __fma_rn(r2, y, q2);
+}
 __device__ __forceinline__ double clamp1(double x) { return x < -1.0 ? -1.0 : (x > 1.0 ? 1.0 : x); }
 
 __device__ __forceinline__ float ld_kv(const void* base, int64_t i, int bf16) {
@@ -321,6 +330,7 @@ struct ResolveShared {
   int e_cand[RELMAX];
   uint8_t e_var[RELMAX];
   int ne;
+  int sel[32];  // chain phase: entry index per lane
   int pool[POOL];
   int npool;
 };
@@ -658,16 +668,30 @@ __global__ void __launch_bounds__(32) k_resolve(DevTables t, IngestArgs a) {
       for (int pass = 0;; ++pass) {
         const int lanes_here = pass == 0 ? dot_lanes0 : 32;
         const bool sp_pass = pass == 0 && specials;
-        // find this lane's entry: the (lane)-th chain entry at or after pos
-        int mine = -1, taken = 0, p = pos;
+        // find this lane's entry: the (lane)-th chain entry at or after pos (ballots over windows
+        // of 32 entries instead of a per-lane serial scan)
+        int taken = 0, p = pos;
         while (p < ne && taken < lanes_here) {
-          const uint8_t v = S.e_var[p];
-          if (v == EV_CHAIN || v == EV_PEND || v == EV_FRESH) {
-            if (taken == lane) mine = p;
-            ++taken;
+          const int e = p + lane;
+          uint8_t v = EV_DEAD;
+          if (e < ne) v = S.e_var[e];
+          const bool isc = v == EV_CHAIN || v == EV_PEND || v == EV_FRESH;
+          unsigned m = __ballot_sync(kFull, isc);
+          const int need = lanes_here - taken;
+          int span = min(32, ne - p);
+          if (__popc(m) > need) {  // keep the lowest `need` chain entries; the window ends after them
+            unsigned rest = m;
+            for (int i = 0; i < need; ++i) rest &= rest - 1;
+            m ^= rest;
+            span = 32 - __clz(m);
           }
-          ++p;
+          if ((m >> lane) & 1u) S.sel[taken + __popc(m & ((1u << lane) - 1u))] = e;
+          taken += __popc(m);
+          p += span;
         }
+        __syncwarp();
+        const int mine = lane < taken ? S.sel[lane] : -1;
+        __syncwarp();  // S.sel is rewritten by the next pass
         if (taken == 0 && !sp_pass) break;
         int oa = -1, ob = -1;
         if (mine >= 0) {
@@ -702,7 +726,7 @@ __global__ void __launch_bounds__(32) k_resolve(DevTables t, IngestArgs a) {
     build_entries(cur, -1, false, false, 0);
     chain_phase(OFF_KD + (cur % 3) * DS, kd + (cur % 3) * DS, false, sq, rn, bn);
     constexpr int KPL = 8;  // key elements per lane held in flight (d <= 256)
-    long long pr[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    long long pr[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};  // phase cycles | slow, scans, tokens, entries
     long long c0 = clock64(), c1;
 #define PROF(k) c1 = clock64(); pr[k] += c1 - c0; c0 = c1;
     for (int tt = cur; tt < T; ++tt) {
@@ -793,12 +817,15 @@ __global__ void __launch_bounds__(32) k_resolve(DevTables t, IngestArgs a) {
       const double dnb = static_cast<double>(nb);
       // the buffer mean can only move on BUFJOIN or DEFER (a Host cluster under the deferred policy)
       const bool buf_may_move = isbuf || (S.hresid[h] != 0 && a.defer);
-      for (int i = lane; i < d; i += 32) {
-        const double r = ddiv(dadd(dmul(dn, hrep[h * DS + i]), kt[i]), dadd(dn, 1.0));
-        nrep[i] = r;
-        diff[i] = dsub(kt[i], r);
-        if (buf_may_move)
-          nbrep[i] = nb == 0 ? kt[i] : ddiv(dadd(dmul(dnb, hbrep[h * DS + i]), kt[i]), dadd(dnb, 1.0));
+      {  // every element shares the divisor n + 1: one correctly rounded reciprocal + Markstein
+        const double b1 = dadd(dn, 1.0), y1 = ddiv(1.0, b1);
+        const double bb = dadd(dnb, 1.0), yb = ddiv(1.0, bb);
+        for (int i = lane; i < d; i += 32) {
+          const double r = div_rcp(dadd(dmul(dn, hrep[h * DS + i]), kt[i]), b1, y1);
+          nrep[i] = r;
+          diff[i] = dsub(kt[i], r);
+          if (buf_may_move) nbrep[i] = nb == 0 ? kt[i] : div_rcp(dadd(dmul(dnb, hbrep[h * DS + i]), kt[i]), bb, yb);
+        }
       }
       const bool has_next = tt + 1 < T;
       const bool fresh_possible = !isbuf && S.hresid[h] != 0 && a.defer && nb == 0;
@@ -811,6 +838,14 @@ __global__ void __launch_bounds__(32) k_resolve(DevTables t, IngestArgs a) {
         __syncwarp();
       }
       PROF(3)
+      if (lane == 0) {
+        int ns = 0;
+        for (int e = 0; e < min(S.ne, RELMAX); ++e) ns += S.e_var[e] == EV_SLOW;
+        pr[8] += ns;
+        pr[10] += 1;
+        pr[11] += min(S.ne, RELMAX);
+      }
+      c0 = clock64();
       chain_phase(OFF_KD + kn * DS, kd + kn * DS, true, sq, rn, bn);
       PROF(4)
       const double varn = ddiv(dadd(dmul(dn, S.hvar[h]), sq), dadd(dn, 1.0));
@@ -920,7 +955,7 @@ __global__ void __launch_bounds__(32) k_resolve(DevTables t, IngestArgs a) {
     }
 #undef PROF
     if (lane == 0)
-      for (int k = 0; k < 8; ++k) a.prof[dom * 16 + k] = pr[k];
+      for (int k = 0; k < 12; ++k) a.prof[dom * 16 + k] = pr[k];
   }
 done:
   __syncwarp();

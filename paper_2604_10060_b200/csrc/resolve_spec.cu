@@ -43,15 +43,6 @@ constexpr int RS_WARPS = RS_THREADS / 32;
 constexpr int FRESH_MAX = 64;  // buffers registered (DEFER onto an empty buffer) per launch
 constexpr double kSlack = 1e-12;
 
-// RN(a / b) for b > 0 given y = RN(1 / b): q1 = RN(a y) is within 2 ulps, one remainder
-// correction makes it faithful, the second is Markstein's correctly rounded step.
-__device__ __forceinline__ double div_rcp(double a, double b, double y) {
-  const double q1 = __dmul_rn(a, y);
-  const double r1 = __fma_rn(-q1, b, a);
-  const double q2 = __fma_rn(r1, y, q1);
-  const double r2 = __fma_rn(-q2, b, a);
-  return __fma_rn(r2, y, q2);
-}
 
 struct SpecSmem {
   uint32_t* keys;

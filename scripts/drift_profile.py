@@ -52,7 +52,7 @@ for i in range(F):
     m = kv.maint_stats() - m0
     rows.append({"frame": i, "ms": round(dt, 2), "splits": int(m[2]), "split_ops": int(m[5])})
     if TIMED:
-        kts.append(np.round(kv.ingest_timing(), 1).tolist() + ["seq_last_launch_cycles"] + np.round(kv.resolve_profile()[:8], 0).tolist())
+        kts.append(np.round(kv.ingest_timing(), 1).tolist() + ["seq_last_launch_cycles"] + np.round(kv.resolve_profile()[:12], 0).tolist())
 kv.maint_stats()  # completes the last frame's deferred replay
 torch.cuda.synchronize()
 wall = (time.perf_counter() - T0) * 1e3
