@@ -267,6 +267,32 @@ KVC_API int kvc_add_cluster(kvc_ctx* ctx, int32_t layer, int64_t partition, int3
                             const float* values, const int64_t* frames, const int32_t* tokens, int32_t residence,
                             int32_t adopt, int64_t* id);
 KVC_API int kvc_adopt(kvc_ctx* ctx, int64_t id);
+/* Verbatim installs (a parsed or host-assembled index, index.hpp:29-58): a VisualPartition with its
+ * frame list, fp64 visual_rep and visual_stat_count; a ClusterRecord with members AND pending-split
+ * buffer entries and the caller's rep / variance / stat_count / buffer_rep / lazy flag / residence /
+ * device tail (not recomputed). want_id >= the next id keeps the record's id (ids are never reused,
+ * index.cpp:105); -1 assigns the next one. */
+typedef struct {
+  int32_t layer;
+  int64_t partition;
+  int32_t n_members;
+  const float *member_keys, *member_values; /* [n_members][d] f32 */
+  const int64_t* member_frames;
+  const int32_t* member_tokens;
+  int32_t n_buffer;
+  const float *buffer_keys, *buffer_values; /* [n_buffer][d] f32 */
+  const int64_t* buffer_frames;
+  const int32_t* buffer_tokens;
+  const double* rep;        /* [d] */
+  double variance;
+  int64_t stat_count;
+  const double* buffer_rep; /* [d] or NULL */
+  int32_t lazy_split, residence, adopt;
+  int64_t device_tail, want_id;
+} kvc_cluster_record;
+KVC_API int kvc_add_partition_ex(kvc_ctx* ctx, const int64_t* frames, int32_t n_frames, const double* visual_rep,
+                                 int64_t visual_stat_count, int64_t* partition);
+KVC_API int kvc_add_cluster_ex(kvc_ctx* ctx, const kvc_cluster_record* record, int64_t* id);
 /* retrieve()'s explicit local window (retrieval.hpp:73-75) empty: no window entries attended */
 KVC_API int kvc_reset_window(kvc_ctx* ctx);
 /* Per-call RetrievalConfig (retrieval.hpp:20-32): k_v, k_s, prefetch_k, prefetch_enabled and the
@@ -276,7 +302,9 @@ KVC_API int kvc_set_retrieval(kvc_ctx* ctx, const kvc_cfg* cfg);
  * kvc_set_retrieval), 2 the CostModel (TieredStore(index, cost), store.hpp:17-31: alpha_us,
  * beta_us_per_byte, bytes_per_entry, device_capacity_entries), 4 the MaintainerConfig
  * (Maintainer(index, store, cfg), maintainer.hpp:28-34: tau_min / tau_max / n0, defer_host_splits,
- * max_split_depth, visual_floor; cfg.seed is taken as MaintainerConfig::seed itself). */
+ * max_split_depth, visual_floor; cfg.seed is taken as MaintainerConfig::seed itself), 8 the
+ * BuildConfig of a direct build_index call (index.hpp:76-82: target sizes, k-means iterations /
+ * tolerance; cfg.seed is taken as BuildConfig::seed itself). */
 KVC_API int kvc_reconfigure(kvc_ctx* ctx, const kvc_cfg* cfg, int32_t what);
 /* Maintainer::place_frame (maintainer.cpp:37-53) / on_insert (maintainer.cpp:88-176): one entry of
  * one domain resolved on the device (no window row); *cluster receives the routed id. */

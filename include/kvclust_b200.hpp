@@ -108,6 +108,7 @@ struct BuildConfig {
   int target_semantic_cluster_size = 32;
   int kmeans_max_iters = 50;
   double kmeans_tol = 1e-6;
+  std::uint64_t seed = 0;
 };
 
 class HierIndex {
@@ -157,6 +158,11 @@ class HierIndex {
   std::int64_t total_member_entries() const;
   void check_invariants() const;
 
+  // The reference's index.v1 JSON (index.cpp:452-592): partitions, clusters with members, buffers
+  // and statistics. A parsed index is host-assembled and installed on first device use.
+  std::string to_json_string() const;
+  static HierIndex from_json_string(const std::string& text);
+
   // The device context behind this index (created on first use from the host-assembled
   // state; kvclust_b200.cpp). Not part of the reference's surface.
   b200::Device& device() const;
@@ -177,6 +183,7 @@ class HierIndex {
   std::vector<std::vector<std::pair<std::int64_t, Embedding>>> pending_appends_;  // append_frame calls
   std::vector<ClusterRecord> pending_clusters_;
   std::vector<std::uint8_t> pending_adopted_;
+  std::set<std::int64_t> pending_registered_;
   mutable std::unique_ptr<View> view_;
 
   const View& view() const;

@@ -12,8 +12,10 @@ importing without the built library raises ImportError.
 """
 from __future__ import annotations
 
+import atexit
 import ctypes as C
 import os
+import weakref
 from dataclasses import dataclass
 
 import numpy as np
@@ -191,7 +193,7 @@ EXPORTED = [
     "kvc_debug_event_profile", "kvc_add_partition", "kvc_append_frame", "kvc_add_cluster", "kvc_adopt",
     "kvc_reset_window", "kvc_set_retrieval", "kvc_place_frame", "kvc_insert", "kvc_materialize", "kvc_touch",
     "kvc_pin", "kvc_enforce_capacity", "kvc_visual_topk", "kvc_semantic_topk", "kvc_last_frames",
-    "kvc_last_predicted", "kvc_reconfigure",
+    "kvc_last_predicted", "kvc_reconfigure", "kvc_add_partition_ex", "kvc_add_cluster_ex",
 ]
 
 
@@ -231,6 +233,20 @@ class LayerMeta:
     attended_count: int
 
 
+_LIVE = weakref.WeakSet()
+
+
+@atexit.register
+def _close_all():
+    """Destroys every live context at interpreter exit (device memory is released explicitly, so
+    compute-sanitizer's leak check reports only real leaks)."""
+    for kv in list(_LIVE):
+        try:
+            kv.close()
+        except Exception:
+            pass
+
+
 class ClusterKVCache:
     """One stream's cluster-level KV cache on the current CUDA device (kvc_create)."""
 
@@ -239,6 +255,7 @@ class ClusterKVCache:
         self.h = vp()
         _check(lib().kvc_create(C.byref(cfg), d, L, C.byref(self.h)))
         self.es = 2 if cfg.kv_dtype == DTYPE_BF16 else 4
+        _LIVE.add(self)
 
     def close(self):
         if self.h:

@@ -579,6 +579,25 @@ int kvc_add_cluster(kvc_ctx* ctx, int32_t layer, int64_t partition, int32_t n, c
   });
 }
 
+int kvc_add_partition_ex(kvc_ctx* ctx, const int64_t* frames, int32_t n_frames, const double* visual_rep,
+                         int64_t visual_stat_count, int64_t* partition) {
+  return guard([&] {
+    const int64_t p = F(ctx).api_add_partition_ex(frames, n_frames, visual_rep, visual_stat_count);
+    if (partition) *partition = p;
+  });
+}
+
+int kvc_add_cluster_ex(kvc_ctx* ctx, const kvc_cluster_record* r, int64_t* id) {
+  return guard([&] {
+    if (!r) kvc::fail(KVC_E_CONFIG, "null record");
+    const int64_t c = F(ctx).api_add_cluster_ex(
+        r->layer, r->partition, r->n_members, r->member_keys, r->member_values, r->member_frames, r->member_tokens,
+        r->n_buffer, r->buffer_keys, r->buffer_values, r->buffer_frames, r->buffer_tokens, r->rep, r->variance,
+        r->stat_count, r->buffer_rep, r->lazy_split != 0, r->residence != 0, r->device_tail, r->adopt != 0, r->want_id);
+    if (id) *id = c;
+  });
+}
+
 int kvc_adopt(kvc_ctx* ctx, int64_t id) {
   return guard([&] { F(ctx).api_adopt(id); });
 }

@@ -91,15 +91,22 @@ Context::Context(const kvc_cfg& cfg, int d, int L) : cfg_(cfg), d_(d), L_(L) {
                     std::to_string(att) + " B > " + std::to_string(device_smem_optin()) +
                     " B per CTA): use a smaller page_tokens");
   }
-  KVC_CUDA(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
-  for (auto& e : ev_) KVC_CUDA(cudaEventCreate(&e));
-  alloc_device();
-  upload_tau();
+  try {
+    KVC_CUDA(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
+    for (auto& e : ev_) KVC_CUDA(cudaEventCreate(&e));
+    alloc_device();
+    upload_tau();
+  } catch (...) {  // a failed construction (e.g. the pool does not fit) releases what it took
+    release();
+    throw;
+  }
   mstats_[0] = 0;
   last_.resize(static_cast<std::size_t>(L_));
 }
 
-Context::~Context() {
+Context::~Context() { release(); }
+
+void Context::release() {
   if (st_) cudaStreamSynchronize(st_);
   if (spec_st_) {
     cudaStreamSynchronize(spec_st_);
@@ -115,7 +122,8 @@ Context::~Context() {
   for (cudaEvent_t e : tier_ev_free_) cudaEventDestroy(e);
   for (void* p : dev_allocs_) cudaFree(p);
   for (void* p : host_allocs_) cudaFreeHost(p);
-  for (auto& e : ev_) cudaEventDestroy(e);
+  for (auto& e : ev_)
+    if (e) cudaEventDestroy(e);
   for (auto& e : ev_step_)
     if (e) cudaEventDestroy(e);
   for (auto& e : ev_k4_)
@@ -137,6 +145,7 @@ Context::~Context() {
     for (auto& e : row)
       if (e) cudaEventDestroy(e);
   if (st_) cudaStreamDestroy(st_);
+  cudaGetLastError();  // nothing of a released context may surface in a later launch check
 }
 
 void* Context::dalloc(std::size_t bytes) {
@@ -1912,7 +1921,9 @@ std::vector<KMeansOut> Context::kmeans_pools(const std::vector<const float*>& pt
 void Context::build_now() {  // engine.cpp:77-93 + build_index (index.cpp:364-450)
   if (built_) return;
   if (pending_.empty()) fail(-9, "no frames available to build from");
-  const std::uint64_t bseed = mix_seed(cfg_.seed, 1);
+  // engine.cpp:79: BuildConfig::seed = mix_seed(engine seed, 1); a direct build_index call passes
+  // its BuildConfig's seed verbatim (kvc_reconfigure bit 8)
+  const std::uint64_t bseed = build_seed_set_ ? build_seed_ : mix_seed(cfg_.seed, 1);
   maint_seed_ = mix_seed(cfg_.seed, 2);
   const int n = static_cast<int>(pending_.size());
   std::vector<float> vis(static_cast<std::size_t>(n) * d_);

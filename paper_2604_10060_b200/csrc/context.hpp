@@ -143,6 +143,7 @@ class Context {
  public:
   Context(const kvc_cfg& cfg, int d, int L);
   ~Context();
+  void release();  // every device / host allocation, stream and event (destructor, failed ctor)
 
   void ingest_frame(std::int64_t frame_id, const float* visual, const void* keys,
                     const void* values, int T, int mem, std::int64_t* assigned,
@@ -206,6 +207,12 @@ class Context {
   std::int64_t api_add_cluster(int layer, std::int64_t parent, int n, const float* keys, const float* values,
                                const std::int64_t* frames, const std::int32_t* tokens, bool host, bool adopt_it);
   void api_adopt(std::int64_t id);
+  std::int64_t api_add_partition_ex(const std::int64_t* frames, int n_frames, const double* visual_rep, std::int64_t stat);
+  std::int64_t api_add_cluster_ex(int layer, std::int64_t parent, int n_mem, const float* mk, const float* mv,
+                                  const std::int64_t* mf, const std::int32_t* mt, int n_buf, const float* bk,
+                                  const float* bv, const std::int64_t* bf, const std::int32_t* bt, const double* rep,
+                                  double var, std::int64_t stat, const double* brep, bool lazy, bool host,
+                                  std::int64_t device_tail, bool adopt_it, std::int64_t want_id);
   void api_reset_window();
   void api_set_retrieval(const kvc_cfg& c);
   void api_reconfigure(const kvc_cfg& c, int what);  // bits: 1 retrieval, 2 cost model, 4 maintainer
@@ -326,7 +333,7 @@ class Context {
   void alloc_result_blocks(std::int32_t kv, std::int32_t ks, std::int32_t kp);
   float* d_q_ = nullptr;
   float* d_out_ = nullptr;
-  cudaEvent_t ev_[8];
+  cudaEvent_t ev_[8] = {};
   bool timing_ = false;
   bool resolve_seq_ = false;  // KVC_RESOLVE=seq selects the sequential resolve kernel
   // A domain relaunched after a split (one domain, its state just changed under the remaining
@@ -370,6 +377,8 @@ class Context {
   } spec_;
   cudaStream_t spec_st_ = nullptr;
   std::int32_t spec_slot_hint_ = -1;  // slot of the cluster an immediate split is settling
+  bool build_seed_set_ = false;  // build_index(frames, BuildConfig) called directly: its seed
+  std::uint64_t build_seed_ = 0;
   bool spec_split_ = true;  // KVC_SPEC_SPLIT=0 disables
   std::int64_t spec_tries_ = 0, spec_hits_ = 0;
   void spec_split_launch(int from_layer, int T);

@@ -92,6 +92,87 @@ std::int64_t Context::api_add_cluster(int layer, std::int64_t parent, int n, con
   return id;
 }
 
+// A VisualPartition installed verbatim (frames, fp64 visual_rep, visual_stat_count): a parsed
+// index (HierIndex::from_json_string) or a host-assembled one whose frames were appended.
+std::int64_t Context::api_add_partition_ex(const std::int64_t* frames, int n_frames, const double* visual_rep,
+                                           std::int64_t stat) {
+  flush_pending();
+  if (n_frames < 1) fail(-10, "a partition needs at least one frame");
+  const std::int64_t pid = api_add_partition(frames[0], std::vector<float>(static_cast<std::size_t>(d_), 0.f).data());
+  Partition& p = parts_[static_cast<std::size_t>(pid)];
+  p.frames.assign(frames, frames + n_frames);
+  p.vrep.assign(visual_rep, visual_rep + d_);
+  p.stat = stat;
+  upload_partition(pid);
+  sync();
+  return pid;
+}
+
+// A ClusterRecord installed verbatim (index.hpp:29-50): members and pending-split buffer entries
+// (f32 payloads), rep / variance / stat_count / buffer_rep as given (the caller's statistics,
+// not recomputed), lazy flag (= registered buffer), residence, device tail. want_id >= the next
+// id keeps the caller's id (ids are never reused: index.cpp:105).
+std::int64_t Context::api_add_cluster_ex(int layer, std::int64_t parent, int n_mem, const float* mk, const float* mv,
+                                         const std::int64_t* mf, const std::int32_t* mt, int n_buf, const float* bk,
+                                         const float* bv, const std::int64_t* bf, const std::int32_t* bt, const double* rep,
+                                         double var, std::int64_t stat, const double* brep, bool lazy, bool host,
+                                         std::int64_t device_tail, bool adopt_it, std::int64_t want_id) {
+  flush_pending();
+  if (n_mem < 1) fail(-5, "cluster with no members");
+  if (layer < 0 || layer >= L_) fail(-7, "layer out of range: " + std::to_string(layer));
+  if (parent < 0 || parent >= static_cast<std::int64_t>(parts_.size())) fail(-8, "unknown partition id");
+  if (cfg_.kv_dtype != KVC_DTYPE_F32) fail(-10, "add_cluster takes f32 payloads (kv_dtype f32 contexts)");
+  if (want_id >= 0) {
+    if (want_id < static_cast<std::int64_t>(clusters_.size())) fail(-10, "cluster ids are never reused");
+    while (static_cast<std::int64_t>(clusters_.size()) < want_id) {  // skipped ids stay dead
+      clusters_.push_back(nullptr);
+      cflags_.push_back(0);
+      last_use_.push_back(0);
+    }
+  }
+  std::vector<Member> m(static_cast<std::size_t>(n_mem));
+  for (int i = 0; i < n_mem; ++i) m[static_cast<std::size_t>(i)] = {mf[i], mt[i]};
+  const std::int64_t id = new_cluster(layer, parent, std::move(m), host);
+  Cluster& c = C(id);
+  if (n_buf > 0) {
+    std::vector<Member> b(static_cast<std::size_t>(n_buf));
+    for (int i = 0; i < n_buf; ++i) b[static_cast<std::size_t>(i)] = {bf[i], bt[i]};
+    c.buffer = MemberList(b);
+    for (const MemberList::Run& r : c.buffer.runs()) frame_add(r.frame, id);
+  }
+  c.stat_count = stat;
+  c.device_tail = device_tail;
+  if (lazy) set_flag(id, CF_LAZY, true);
+  const std::size_t rb = static_cast<std::size_t>(d_) * es_;
+  ensure_stage(n_mem + n_buf + 1);
+  KVC_CUDA(cudaMemcpyAsync(d_stage_k_, mk, static_cast<std::size_t>(n_mem) * rb, cudaMemcpyHostToDevice, st_));
+  KVC_CUDA(cudaMemcpyAsync(d_stage_v_, mv, static_cast<std::size_t>(n_mem) * rb, cudaMemcpyHostToDevice, st_));
+  if (n_buf > 0) {
+    KVC_CUDA(cudaMemcpyAsync(static_cast<std::uint8_t*>(d_stage_k_) + static_cast<std::size_t>(n_mem) * rb, bk,
+                             static_cast<std::size_t>(n_buf) * rb, cudaMemcpyHostToDevice, st_));
+    KVC_CUDA(cudaMemcpyAsync(static_cast<std::uint8_t*>(d_stage_v_) + static_cast<std::size_t>(n_mem) * rb, bv,
+                             static_cast<std::size_t>(n_buf) * rb, cudaMemcpyHostToDevice, st_));
+  }
+  std::vector<double> r(rep, rep + d_), b(static_cast<std::size_t>(d_), 0.0);
+  if (brep) b.assign(brep, brep + d_);
+  const std::vector<std::int32_t> nb{n_buf};
+  const std::vector<std::vector<double>> breps{b};
+  init_slots({c.slot}, {r}, {var}, {stat}, {static_cast<std::int64_t>(n_mem)}, {id}, {static_cast<std::uint8_t>(host ? 1 : 0)},
+             &nb, &breps);
+  std::vector<AppendRun> runs{{c.slot, 0, n_mem, 0}};
+  if (n_buf > 0) runs.push_back({c.slot, n_mem, n_buf, 1});
+  std::vector<std::int32_t> idx(static_cast<std::size_t>(n_mem + n_buf));
+  std::iota(idx.begin(), idx.end(), 0);
+  append_runs_idx(runs, idx);
+  check_dev_err();
+  resid_h_[static_cast<std::size_t>(c.slot)] = host ? 1 : 0;
+  resid_dirty_ = true;
+  flush_resid();
+  pl_upload(parent, layer);
+  if (adopt_it) adopt(id);
+  return id;
+}
+
 void Context::api_adopt(std::int64_t id) {
   flush_pending();
   C(id);
@@ -144,6 +225,16 @@ void Context::api_reconfigure(const kvc_cfg& c, int what) {
     cfg_.beta_us_per_byte = c.beta_us_per_byte;
     cfg_.bytes_per_entry = c.bytes_per_entry;
     cfg_.device_capacity_entries = c.device_capacity_entries;
+  }
+  if (what & 8) {  // BuildConfig of a direct build_index call (index.hpp:76-82), seed verbatim
+    if (c.target_visual_cluster_size < 1 || c.target_semantic_cluster_size < 1)
+      fail(-10, "target cluster sizes must be positive");
+    cfg_.target_visual_cluster_size = c.target_visual_cluster_size;
+    cfg_.target_semantic_cluster_size = c.target_semantic_cluster_size;
+    cfg_.kmeans_max_iters = c.kmeans_max_iters;
+    cfg_.kmeans_tol = c.kmeans_tol;
+    build_seed_set_ = true;
+    build_seed_ = c.seed;
   }
   if (what & 4) {
     if (c.tau_min < 0.0 || c.tau_max < c.tau_min) fail(-10, "variance thresholds must satisfy 0 <= tau_min <= tau_max");

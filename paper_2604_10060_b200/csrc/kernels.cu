@@ -900,6 +900,7 @@ __global__ void __launch_bounds__(32) k_resolve(DevTables t, IngestArgs a) {
         hrep[h * DS + i] = nrep[i];
         if (buf_moved) hbrep[h * DS + i] = nbrep[i];
       }
+      __syncwarp();  // every lane read S.hvar[h] / the pending entries above (racecheck: WAR)
       if (lane == 0) {
         S.hdirty[h] = 1;
         S.hrn[h] = rn;

@@ -465,6 +465,9 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve_spec(DevTables t, Ing
         S.tauw[i] = __ldg(&t.tau_tab[n < t.tau_len ? n : t.tau_len - 1]);
       }
     }
+    // the chains below read other threads' reciprocals (S.rcp) and thresholds (S.tauw)
+    // (compute-sanitizer racecheck: RAW hazard without this barrier)
+    __syncthreads();
     prof(1);
     // ---------------------------------------------------------------- C: representative chains
     // one thread per (slot, element): r_i <- (n r_i + k_i) / (n + 1) over the slot's tokens

@@ -11,6 +11,8 @@
 #include <string>
 #include <vector>
 
+#include <nlohmann/json.hpp>
+
 #include "kvc.h"
 #include "kvclust_b200.hpp"
 #include "kvclust_b200_engine.hpp"
@@ -342,6 +344,14 @@ void TransferLedger::clear() {
 
 // =============================================================================== HierIndex
 
+namespace {
+ClusterRecord* pending_cluster(std::vector<ClusterRecord>& cs, std::int64_t id) {
+  for (ClusterRecord& r : cs)
+    if (r.cluster_id == id) return &r;
+  throw UnknownCluster(id);
+}
+}  // namespace
+
 struct HierIndex::View {
   std::vector<VisualPartition> parts;
   std::map<std::int64_t, ClusterRecord> clusters;
@@ -380,33 +390,66 @@ b200::Device& HierIndex::device() const {
 void HierIndex::install_pending() const {
   if (pending_parts_.empty() && pending_clusters_.empty()) return;
   auto* self = const_cast<HierIndex*>(this);
-  for (std::size_t i = 0; i < pending_parts_.size(); ++i) {
+  for (const VisualPartition& p : pending_parts_) {  // verbatim: frames, fp64 visual_rep, count
     std::int64_t pid = -1;
-    check(kvc_add_partition(dev_->ctx, pending_parts_[i].frame_ids.front(), pending_first_visual_[i].data(), &pid));
-    for (const auto& [frame, vis] : pending_appends_[i]) check(kvc_append_frame(dev_->ctx, pid, frame, vis.data()));
+    check(kvc_add_partition_ex(dev_->ctx, p.frame_ids.data(), static_cast<int>(p.frame_ids.size()), p.visual_rep.data(),
+                               p.visual_stat_count, &pid));
   }
-  for (std::size_t i = 0; i < pending_clusters_.size(); ++i) {
-    const ClusterRecord& rec = pending_clusters_[i];
-    const int n = static_cast<int>(rec.members.size());
-    std::vector<float> k(static_cast<std::size_t>(n) * dim_), v(k.size());
-    std::vector<std::int64_t> fr(static_cast<std::size_t>(n));
-    std::vector<std::int32_t> tk(static_cast<std::size_t>(n));
-    for (int j = 0; j < n; ++j) {
-      const KVEntry& e = rec.members[static_cast<std::size_t>(j)];
-      std::memcpy(&k[static_cast<std::size_t>(j) * dim_], e.key.data(), static_cast<std::size_t>(dim_) * 4);
-      std::memcpy(&v[static_cast<std::size_t>(j) * dim_], e.value.data(), static_cast<std::size_t>(dim_) * 4);
-      fr[static_cast<std::size_t>(j)] = e.frame_id;
-      tk[static_cast<std::size_t>(j)] = e.token_id;
+  auto rows = [&](const std::vector<KVEntry>& es, std::vector<float>& k, std::vector<float>& v,
+                  std::vector<std::int64_t>& fr, std::vector<std::int32_t>& tk) {
+    const std::size_t n = es.size();
+    k.assign(n * static_cast<std::size_t>(dim_), 0.f);
+    v.assign(k.size(), 0.f);
+    fr.resize(n);
+    tk.resize(n);
+    for (std::size_t j = 0; j < n; ++j) {
+      if (static_cast<int>(es[j].key.size()) != dim_ || static_cast<int>(es[j].value.size()) != dim_)
+        throw DimMismatch(es[j].key.size(), static_cast<std::size_t>(dim_));
+      std::memcpy(&k[j * dim_], es[j].key.data(), static_cast<std::size_t>(dim_) * 4);
+      std::memcpy(&v[j * dim_], es[j].value.data(), static_cast<std::size_t>(dim_) * 4);
+      fr[j] = es[j].frame_id;
+      tk[j] = es[j].token_id;
     }
+  };
+  for (std::size_t i = 0; i < pending_clusters_.size(); ++i) {  // verbatim records, ids kept
+    const ClusterRecord& rec = pending_clusters_[i];
+    std::vector<float> mk, mv, bk, bv;
+    std::vector<std::int64_t> mf, bf;
+    std::vector<std::int32_t> mt, bt;
+    rows(rec.members, mk, mv, mf, mt);
+    rows(rec.buffer, bk, bv, bf, bt);
+    if (static_cast<int>(rec.rep.size()) != dim_) throw DimMismatch(rec.rep.size(), static_cast<std::size_t>(dim_));
+    kvc_cluster_record r{};
+    r.layer = rec.layer_id;
+    r.partition = rec.visual_parent;
+    r.n_members = static_cast<int>(rec.members.size());
+    r.member_keys = mk.data();
+    r.member_values = mv.data();
+    r.member_frames = mf.data();
+    r.member_tokens = mt.data();
+    r.n_buffer = static_cast<int>(rec.buffer.size());
+    r.buffer_keys = bk.data();
+    r.buffer_values = bv.data();
+    r.buffer_frames = bf.data();
+    r.buffer_tokens = bt.data();
+    r.rep = rec.rep.data();
+    r.variance = rec.variance;
+    r.stat_count = rec.stat_count;
+    r.buffer_rep = rec.buffer_rep.size() == static_cast<std::size_t>(dim_) ? rec.buffer_rep.data() : nullptr;
+    r.lazy_split = (rec.lazy_split || pending_registered_.count(rec.cluster_id)) ? 1 : 0;
+    r.residence = rec.residence == Residence::Host ? 1 : 0;
+    r.adopt = pending_adopted_[i];
+    r.device_tail = rec.device_tail;
+    r.want_id = rec.cluster_id;
     std::int64_t id = -1;
-    check(kvc_add_cluster(dev_->ctx, rec.layer_id, rec.visual_parent, n, k.data(), v.data(), fr.data(), tk.data(),
-                          rec.residence == Residence::Host ? 1 : 0, pending_adopted_[i], &id));
+    check(kvc_add_cluster_ex(dev_->ctx, &r, &id));
   }
   self->pending_parts_.clear();
   self->pending_first_visual_.clear();
   self->pending_appends_.clear();
   self->pending_clusters_.clear();
   self->pending_adopted_.clear();
+  self->pending_registered_.clear();
   mark_device_changed();
 }
 
@@ -420,6 +463,7 @@ const HierIndex::View& HierIndex::view() const {
   if (!dev_) {  // host-assembled, not yet installed
     v->parts = pending_parts_;
     for (const ClusterRecord& r : pending_clusters_) v->clusters.emplace(r.cluster_id, r);
+    v->registered = pending_registered_;
   } else {
     install_pending();
     kvc_ctx* c = dev_->ctx;
@@ -489,7 +533,7 @@ const HierIndex::View& HierIndex::view() const {
   // rep_set: live clusters in id order, then the registered buffers (index.cpp:97-168)
   for (const auto& [id, r] : v->clusters) v->rep_set[static_cast<std::size_t>(r.layer_id)].push_back({id, false});
   for (const auto& [id, r] : v->clusters)
-    if (r.lazy_split) {
+    if (dev_ ? r.lazy_split : v->registered.count(id) != 0) {
       v->rep_set[static_cast<std::size_t>(r.layer_id)].push_back({id, true});
       v->registered.insert(id);
     }
@@ -508,6 +552,11 @@ const HierIndex::View& HierIndex::view() const {
 const std::vector<VisualPartition>& HierIndex::partitions() const { return view().parts; }
 
 VisualPartition& HierIndex::partition(std::int64_t id) {
+  if (!dev_) {
+    if (id < 0 || id >= static_cast<std::int64_t>(pending_parts_.size())) throw UnknownCluster(id);
+    mark_device_changed();
+    return pending_parts_[static_cast<std::size_t>(id)];
+  }
   auto& ps = const_cast<View&>(view()).parts;
   if (id < 0 || id >= static_cast<std::int64_t>(ps.size())) throw UnknownCluster(id);
   return ps[static_cast<std::size_t>(id)];
@@ -519,6 +568,10 @@ const VisualPartition& HierIndex::partition(std::int64_t id) const {
 const std::map<std::int64_t, ClusterRecord>& HierIndex::clusters() const { return view().clusters; }
 
 ClusterRecord& HierIndex::cluster(std::int64_t id) {
+  if (!dev_) {  // host-assembled: the caller edits the pending record itself
+    mark_device_changed();
+    return *pending_cluster(pending_clusters_, id);
+  }
   auto& cs = const_cast<View&>(view()).clusters;
   auto it = cs.find(id);
   if (it == cs.end()) throw UnknownCluster(id);
@@ -625,12 +678,170 @@ namespace {
 }
 }  // namespace
 
-void HierIndex::remove_cluster(std::int64_t) { maintainer_only("remove_cluster"); }
-void HierIndex::register_buffer(std::int64_t) { maintainer_only("register_buffer"); }
-void HierIndex::deregister_buffer(std::int64_t) { maintainer_only("deregister_buffer"); }
-bool HierIndex::buffer_registered(std::int64_t cluster_id) const { return view().registered.count(cluster_id) != 0; }
-void HierIndex::add_member(std::int64_t, KVEntry) { maintainer_only("add_member"); }
-void HierIndex::add_to_buffer(std::int64_t, KVEntry) { maintainer_only("add_to_buffer"); }
+// Low-level mutators (index.cpp:122-190). On a host-assembled index (before any device operation)
+// they edit the pending state; once the index lives on the device, the maintainer owns it.
+void HierIndex::remove_cluster(std::int64_t id) {
+  if (dev_) maintainer_only("remove_cluster");
+  ClusterRecord* r = pending_cluster(pending_clusters_, id);
+  auto& sib = pending_parts_[static_cast<std::size_t>(r->visual_parent)].per_layer_clusters[r->layer_id];
+  sib.erase(std::remove(sib.begin(), sib.end(), id), sib.end());
+  const std::size_t i = static_cast<std::size_t>(r - pending_clusters_.data());
+  pending_clusters_.erase(pending_clusters_.begin() + static_cast<std::ptrdiff_t>(i));
+  pending_adopted_.erase(pending_adopted_.begin() + static_cast<std::ptrdiff_t>(i));
+  pending_registered_.erase(id);
+  mark_device_changed();
+}
+void HierIndex::register_buffer(std::int64_t cluster_id) {
+  if (dev_) maintainer_only("register_buffer");
+  pending_cluster(pending_clusters_, cluster_id);
+  pending_registered_.insert(cluster_id);
+  mark_device_changed();
+}
+void HierIndex::deregister_buffer(std::int64_t cluster_id) {
+  if (dev_) maintainer_only("deregister_buffer");
+  pending_registered_.erase(cluster_id);
+  mark_device_changed();
+}
+bool HierIndex::buffer_registered(std::int64_t cluster_id) const {
+  if (!dev_) return pending_registered_.count(cluster_id) != 0;
+  return view().registered.count(cluster_id) != 0;
+}
+void HierIndex::add_member(std::int64_t cluster_id, KVEntry entry) {
+  if (dev_) maintainer_only("add_member");
+  ClusterRecord* r = pending_cluster(pending_clusters_, cluster_id);
+  r->last_touch_frame = std::max(r->last_touch_frame, entry.frame_id);
+  r->members.push_back(std::move(entry));
+  mark_device_changed();
+}
+void HierIndex::add_to_buffer(std::int64_t cluster_id, KVEntry entry) {
+  if (dev_) maintainer_only("add_to_buffer");
+  ClusterRecord* r = pending_cluster(pending_clusters_, cluster_id);
+  // running mean of the buffered keys (index.cpp:177-190)
+  if (r->buffer_rep.empty()) r->buffer_rep.assign(entry.key.size(), 0.0);
+  const double n = static_cast<double>(r->buffer.size());
+  for (std::size_t i = 0; i < r->buffer_rep.size(); ++i)
+    r->buffer_rep[i] = (n * r->buffer_rep[i] + static_cast<double>(entry.key[i])) / (n + 1.0);
+  r->buffer.push_back(std::move(entry));
+  mark_device_changed();
+}
+
+// index.v1 JSON (the reference's schema, index.cpp:452-592)
+namespace {
+using json = nlohmann::json;
+json emb_json(const Embedding& v) {
+  json a = json::array();
+  for (float x : v) a.push_back(static_cast<double>(x));
+  return a;
+}
+Embedding emb_from(const json& a) {
+  Embedding v;
+  for (const auto& x : a) v.push_back(static_cast<float>(x.get<double>()));
+  return v;
+}
+json entry_json(const KVEntry& e) {
+  return json{{"key", emb_json(e.key)}, {"value", emb_json(e.value)}, {"frame", e.frame_id},
+              {"layer", e.layer_id}, {"token", e.token_id}};
+}
+KVEntry entry_from(const json& j) {
+  KVEntry e;
+  e.key = emb_from(j.at("key"));
+  e.value = emb_from(j.at("value"));
+  e.frame_id = j.at("frame").get<std::int64_t>();
+  e.layer_id = j.at("layer").get<std::int32_t>();
+  e.token_id = j.at("token").get<std::int32_t>();
+  return e;
+}
+}  // namespace
+
+std::string HierIndex::to_json_string() const {
+  json root;
+  root["format"] = "kvclust.index.v1";
+  root["dim"] = dim_;
+  root["layers"] = layers_;
+  std::int64_t next = 0;
+  for (const auto& [id, r] : clusters()) next = std::max(next, id + 1);
+  root["next_cluster_id"] = next;
+  json parts = json::array();
+  for (const VisualPartition& p : partitions()) {
+    json jp;
+    jp["id"] = p.partition_id;
+    jp["frames"] = p.frame_ids;
+    jp["visual_rep"] = p.visual_rep;
+    jp["visual_stat_count"] = p.visual_stat_count;
+    json lm = json::object();
+    for (const auto& [layer, ids] : p.per_layer_clusters) lm[std::to_string(layer)] = ids;
+    jp["clusters"] = std::move(lm);
+    parts.push_back(std::move(jp));
+  }
+  root["partitions"] = std::move(parts);
+  json cs = json::array();
+  for (const auto& [id, r] : clusters()) {
+    json jc;
+    jc["id"] = id;
+    jc["layer"] = r.layer_id;
+    jc["parent"] = r.visual_parent;
+    jc["rep"] = r.rep;
+    jc["variance"] = r.variance;
+    jc["stat_count"] = r.stat_count;
+    jc["lazy_split"] = r.lazy_split;
+    jc["residence"] = r.residence == Residence::Device ? "device" : "host";
+    jc["device_tail"] = r.device_tail;
+    jc["first_frame"] = r.first_frame_id;
+    jc["last_touch"] = r.last_touch_frame;
+    json m = json::array(), b = json::array();
+    for (const KVEntry& e : r.members) m.push_back(entry_json(e));
+    for (const KVEntry& e : r.buffer) b.push_back(entry_json(e));
+    jc["members"] = std::move(m);
+    jc["buffer"] = std::move(b);
+    jc["buffer_rep"] = r.buffer_rep;
+    cs.push_back(std::move(jc));
+  }
+  root["clusters"] = std::move(cs);
+  return root.dump(2);
+}
+
+HierIndex HierIndex::from_json_string(const std::string& text) {
+  json root;
+  try {
+    root = json::parse(text);
+  } catch (const json::parse_error& e) {
+    throw ParseError(0, std::string("bad index json: ") + e.what());
+  }
+  if (root.value("format", "") != "kvclust.index.v1") throw ParseError(0, "unrecognized index format");
+  HierIndex idx(root.at("dim").get<std::int32_t>(), root.at("layers").get<std::int32_t>());
+  for (const json& jp : root.at("partitions")) {
+    VisualPartition p;
+    p.partition_id = jp.at("id").get<std::int64_t>();
+    p.frame_ids = jp.at("frames").get<std::vector<std::int64_t>>();
+    p.visual_rep = jp.at("visual_rep").get<DVec>();
+    p.visual_stat_count = jp.at("visual_stat_count").get<std::int64_t>();
+    for (const auto& [ls, ids] : jp.at("clusters").items()) p.per_layer_clusters[std::stoi(ls)] = ids.get<std::vector<std::int64_t>>();
+    idx.pending_first_visual_.push_back(Embedding(p.visual_rep.begin(), p.visual_rep.end()));
+    idx.pending_appends_.emplace_back();
+    idx.pending_parts_.push_back(std::move(p));
+  }
+  for (const json& jc : root.at("clusters")) {
+    ClusterRecord r;
+    r.cluster_id = jc.at("id").get<std::int64_t>();
+    r.layer_id = jc.at("layer").get<std::int32_t>();
+    r.visual_parent = jc.at("parent").get<std::int64_t>();
+    r.rep = jc.at("rep").get<DVec>();
+    r.variance = jc.at("variance").get<double>();
+    r.stat_count = jc.at("stat_count").get<std::int64_t>();
+    r.lazy_split = jc.at("lazy_split").get<bool>();
+    r.residence = jc.at("residence").get<std::string>() == "device" ? Residence::Device : Residence::Host;
+    r.device_tail = jc.at("device_tail").get<std::int64_t>();
+    r.first_frame_id = jc.at("first_frame").get<std::int64_t>();
+    r.last_touch_frame = jc.at("last_touch").get<std::int64_t>();
+    for (const json& je : jc.at("members")) r.members.push_back(entry_from(je));
+    for (const json& je : jc.at("buffer")) r.buffer.push_back(entry_from(je));
+    r.buffer_rep = jc.at("buffer_rep").get<DVec>();
+    if (r.lazy_split) idx.pending_registered_.insert(r.cluster_id);
+    idx.pending_clusters_.push_back(std::move(r));
+    idx.pending_adopted_.push_back(0);
+  }
+  return idx;
+}
 
 std::vector<std::int64_t> HierIndex::visual_topk(const Embedding& query, int k_v) const {
   if (static_cast<std::int32_t>(query.size()) != dim_) throw DimMismatch(query.size(), static_cast<std::size_t>(dim_));
@@ -699,6 +910,11 @@ HierIndex build_index(const std::vector<FrameInput>& frames, const BuildConfig& 
   c.build_batch_frames = static_cast<int>(frames.size());
   c.device_capacity_entries = std::int64_t(1) << 40;
   idx.dev_ = std::make_shared<b200::Device>(c, d, L);
+  {
+    kvc_cfg bc = c;
+    bc.seed = cfg.seed;  // BuildConfig::seed, verbatim
+    check(kvc_reconfigure(idx.dev_->ctx, &bc, 8));
+  }
   std::vector<float> k, v;
   for (const FrameInput& f : frames) {
     int T = 0;

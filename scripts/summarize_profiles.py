@@ -99,7 +99,7 @@ lines += ["", "## `ncu --set full` captures", "",
           "| kernel | duration us | DRAM read MB | DRAM write MB | DRAM % peak | SM % | tensor pipe % | achieved occupancy | regs |",
           "|---|---|---|---|---|---|---|---|---|"]
 att = {}
-for kname in ("k_attend", "k_select3", "k_score_select", "k_resolve_spec", "k_resolve", "k_assign_tc", "k_approx",
+for kname in ("k_attend", "k_select3", "k_score_select", "k_resolve_spec", "k_assign_tc", "k_approx",
               "k_topm", "k_split_two", "k_kmeans"):
     for m in ncu_raw(kname)[:1]:
         dur = num(m.get("gpu__time_duration.sum"))
