@@ -44,31 +44,18 @@ void add_run(std::vector<CopyRun>& runs, std::int64_t dev, std::int64_t host, st
     runs.push_back({dev, host, n});
 }
 
-// Submits the runs as one cudaMemcpyBatchAsync (one driver call for the batch; the copy engines
-// pick them up back to back), falling back to one cudaMemcpyAsync per run where unsupported.
+// Submits the runs as one cudaMemcpyAsync each on the transfer stream (runs are already merged, so
+// a batch usually crosses the host link in a few large transfers).
 void submit_runs(const std::vector<CopyRun>& runs, std::uint8_t* dev_base, std::uint8_t* host_base,
                  std::int64_t page_bytes, bool to_host, cudaStream_t st) {
-  if (runs.empty()) return;
-  std::vector<void*> dst(runs.size()), src(runs.size());
-  std::vector<std::size_t> sz(runs.size());
-  for (std::size_t i = 0; i < runs.size(); ++i) {
-    std::uint8_t* d = dev_base + runs[i].dev * page_bytes;
-    std::uint8_t* h = host_base + runs[i].host * page_bytes;
-    dst[i] = to_host ? h : d;
-    src[i] = to_host ? d : h;
-    sz[i] = static_cast<std::size_t>(runs[i].n * page_bytes);
+  for (const CopyRun& r : runs) {
+    std::uint8_t* d = dev_base + r.dev * page_bytes;
+    std::uint8_t* h = host_base + r.host * page_bytes;
+    KVC_CUDA(cudaMemcpyAsync(to_host ? static_cast<void*>(h) : static_cast<void*>(d),
+                             to_host ? static_cast<const void*>(d) : static_cast<const void*>(h),
+                             static_cast<std::size_t>(r.n * page_bytes),
+                             to_host ? cudaMemcpyDeviceToHost : cudaMemcpyHostToDevice, st));
   }
-  cudaMemcpyAttributes attr{};
-  attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-  attr.flags = cudaMemcpyFlagPreferOverlapWithCompute;
-  std::size_t idx0 = 0, fail_idx = 0;
-  if (runs.size() > 1 &&
-      cudaMemcpyBatchAsync(dst.data(), src.data(), sz.data(), runs.size(), &attr, &idx0, 1, &fail_idx, st) ==
-          cudaSuccess)
-    return;
-  cudaGetLastError();  // clear a not-supported status
-  for (std::size_t i = 0; i < runs.size(); ++i)
-    KVC_CUDA(cudaMemcpyAsync(dst[i], src[i], sz[i], to_host ? cudaMemcpyDeviceToHost : cudaMemcpyHostToDevice, st));
 }
 
 }  // namespace
