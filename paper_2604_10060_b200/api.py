@@ -164,6 +164,7 @@ def lib():
         L.kvc_last_ingest_timing.argtypes = [vp, f64p]
         L.kvc_debug_resolve_profile.argtypes = [vp, f64p]
         L.kvc_debug_event_profile.argtypes = [vp, f64p, C.c_int32]
+        L.kvc_debug_wave_profile.argtypes = [vp, f64p, C.c_int32]
         L.kvc_debug_assign_check.argtypes = [vp, vp, C.c_int32, C.c_int64, C.c_int32, f64p]
         L.kvc_debug_div_check.argtypes = [C.c_uint64, C.c_uint64, C.c_int32, C.POINTER(C.c_uint64)]
         L.kvc_host_split_two.argtypes = [f32p, C.c_int32, C.c_int32, C.c_uint64, i32p, i32p]
@@ -190,7 +191,7 @@ EXPORTED = [
     "kvc_host_mix_seed", "kvc_debug_div_check", "kvc_debug_assign_check", "kvc_tier_sync",
     "kvc_tier_stats", "kvc_cluster_tier", "kvc_debug_tier_check", "kvc_debug_split_two", "kvc_debug_kmeans", "kvc_exchange_bytes", "kvc_ipc_alloc",
     "kvc_ipc_open", "kvc_ipc_close", "kvc_ipc_free", "kvc_set_peers", "kvc_peer_output",
-    "kvc_debug_event_profile", "kvc_add_partition", "kvc_append_frame", "kvc_add_cluster", "kvc_adopt",
+    "kvc_debug_event_profile", "kvc_debug_wave_profile", "kvc_add_partition", "kvc_append_frame", "kvc_add_cluster", "kvc_adopt",
     "kvc_reset_window", "kvc_set_retrieval", "kvc_place_frame", "kvc_insert", "kvc_materialize", "kvc_touch",
     "kvc_pin", "kvc_enforce_capacity", "kvc_visual_topk", "kvc_semantic_topk", "kvc_last_frames",
     "kvc_last_predicted", "kvc_reconfigure", "kvc_add_partition_ex", "kvc_add_cluster_ex",
@@ -521,6 +522,15 @@ class ClusterKVCache:
         t = np.zeros(10)
         _check(lib().kvc_debug_event_profile(self.h, _p(t, f64p), 1 if reset else 0))
         return dict(zip(self.EVENT_KEYS, t.round(1).tolist()))
+
+    WAVE_KEYS = ("frames_with_events", "waves", "passes", "rolled_back_domains", "verify_kmeans", "events",
+                 "stage_us", "kmeans_jobs", "kmeans_us", "install_us", "relaunch_us", "verify_commit_us")
+
+    def wave_profile(self, reset: bool = False) -> dict:
+        """Wave-engine profile (kvc_debug_wave_profile), cumulative."""
+        t = np.zeros(12)
+        _check(lib().kvc_debug_wave_profile(self.h, _p(t, f64p), 1 if reset else 0))
+        return dict(zip(self.WAVE_KEYS, t.round(1).tolist()))
 
     def assign_check(self, keys, partition: int = 0):
         """Distance-tile self-check on a frame keys [L, T, d] (see kvc_debug_assign_check):

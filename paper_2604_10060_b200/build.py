@@ -25,7 +25,7 @@ NVFLAGS = ["-std=c++17", "-O3", "-lineinfo", "--fmad=false", "-Xcompiler", "-fPI
            "-Xcompiler", "-ffp-contract=off", "-Xptxas", "-v"] + ARCH
 
 SOURCES = ["kmeans.cpp", "context.cpp", "context_query.cpp", "context_tiers.cpp", "abi.cpp", "kernels.cu",
-           "resolve_spec.cu", "assign_tc.cu", "tiers.cu", "select.cu", "split.cu", "kmeans_dev.cu", "token.cu", "token_context.cpp", "launch_util.cu", "context_api.cpp"]
+           "resolve_spec.cu", "assign_tc.cu", "tiers.cu", "select.cu", "split.cu", "kmeans_dev.cu", "token.cu", "token_context.cpp", "launch_util.cu", "context_api.cpp", "waves.cu", "context_waves.cpp"]
 HEADERS = ["kvc_core.hpp", "devmath.cuh", "kmeans.hpp", "context.hpp", "extent_alloc.hpp", "token.hpp", os.path.join("..", "..", "include", "kvc.h")]
 
 

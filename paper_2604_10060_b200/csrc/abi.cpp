@@ -701,6 +701,11 @@ int kvc_debug_event_profile(kvc_ctx* ctx, double* out10, int32_t reset) {
   return guard([&] { F(ctx).event_profile(out10, reset != 0); });
 }
 
+int kvc_debug_wave_profile(kvc_ctx* ctx, double* out12, int32_t reset) {
+  KVC_CLUSTER_ONLY(ctx);
+  return guard([&] { ctx->impl->wave_profile(out12, reset != 0); });
+}
+
 int kvc_debug_resolve_profile(kvc_ctx* ctx, double* out) {
   if (ctx->tok) return guard([&] { ctx->tok->profile(out); });  // token-baseline select phases
   ctx->impl->resolve_profile(out);

@@ -108,6 +108,7 @@ Context::~Context() { release(); }
 
 void Context::release() {
   if (st_) cudaStreamSynchronize(st_);
+  waves_free();
   if (spec_st_) {
     cudaStreamSynchronize(spec_st_);
     cudaStreamDestroy(spec_st_);
@@ -291,6 +292,10 @@ void Context::alloc_device() {
     resolve_seq_ = e && std::string(e) == "seq";
     const char* rl = std::getenv("KVC_RELAUNCH");  // "spec": speculative kernel for relaunches too
     relaunch_seq_ = !(rl && std::string(rl) == "spec");
+    const char* wv = std::getenv("KVC_WAVES");  // 0: settle host events one domain at a time
+    waves_ = !(wv && std::string(wv) == "0");
+    const char* wp = std::getenv("KVC_WAVES_PERTURB");
+    waves_perturb_ = wp && std::string(wp) == "1";
     const char* ss = std::getenv("KVC_SPEC_SPLIT");  // 0: no speculative split k-means
     spec_split_ = !(ss && std::string(ss) == "0");
     const char* g = std::getenv("KVC_ASSIGN");  // "simt": the fp32 CUDA-core tile
@@ -620,6 +625,12 @@ void Context::frame_del(std::int64_t frame, std::int64_t cid) {
 std::int64_t Context::new_cluster(std::int32_t layer, std::int64_t parent,
                                   std::vector<Member>&& members, bool host) {
   if (members.empty()) fail(-5, "cluster with no members");
+  return new_cluster_at(take_slot(), layer, parent, std::move(members), host);
+}
+
+std::int64_t Context::new_cluster_at(std::int32_t slot, std::int32_t layer, std::int64_t parent,
+                                     std::vector<Member>&& members, bool host) {
+  if (members.empty()) fail(-5, "cluster with no members");
   if (layer < 0 || layer >= L_) fail(-7, "layer out of range: " + std::to_string(layer));
   auto c = std::make_unique<Cluster>();
   c->id = static_cast<std::int64_t>(clusters_.size());
@@ -637,7 +648,7 @@ std::int64_t Context::new_cluster(std::int32_t layer, std::int64_t parent,
   cflags_.push_back(host ? CF_HOST : 0);
   last_use_.push_back(0);
   if (!host) min_lt_ = std::min(min_lt_, c->last_touch);
-  c->slot = take_slot();
+  c->slot = slot;
   slot_id_[static_cast<std::size_t>(c->slot)] = c->id;
   resid_h_[static_cast<std::size_t>(c->slot)] = host ? 1 : 0;
   parts_[static_cast<std::size_t>(parent)].per_layer[static_cast<std::size_t>(layer)].push_back(c->id);
@@ -650,6 +661,13 @@ std::int64_t Context::new_cluster(std::int32_t layer, std::int64_t parent,
 
 // HierIndex::remove_cluster (index.cpp:122-145); device pages are released by the caller.
 void Context::drop_cluster(std::int64_t id) {
+  const std::int32_t s = C(id).slot;
+  launches_ += launch_free_slot_pages(t_, s, st_);  // HBM pages only
+  drop_cluster_host(id);
+  free_slots_.push_back(s);
+}
+
+void Context::drop_cluster_host(std::int64_t id) {
   Cluster& c = C(id);
   auto& sib = parts_[static_cast<std::size_t>(c.parent)].per_layer[static_cast<std::size_t>(c.layer)];
   sib.erase(std::remove(sib.begin(), sib.end(), id), sib.end());
@@ -657,11 +675,9 @@ void Context::drop_cluster(std::int64_t id) {
   for (const MemberList::Run& r : c.buffer.runs()) frame_del(r.frame, id);
   layer_live_count_[static_cast<std::size_t>(c.layer)] -= 1;
   n_live_ -= 1;
-  std::int32_t s = c.slot;
-  launches_ += launch_free_slot_pages(t_, s, st_);  // HBM pages only
-  tier_forget(id);                                  // the host-tier extent
+  const std::int32_t s = c.slot;
+  tier_forget(id);  // the host-tier extent
   slot_id_[static_cast<std::size_t>(s)] = -1;
-  free_slots_.push_back(s);
   clusters_[static_cast<std::size_t>(id)].reset();
 }
 
@@ -670,6 +686,20 @@ void Context::pl_upload(std::int64_t pid, int layer) {
   Partition& p = parts_[static_cast<std::size_t>(pid)];
   const auto& ids = p.per_layer[static_cast<std::size_t>(layer)];
   const std::int32_t n = static_cast<std::int32_t>(ids.size());
+  pl_reserve(pid, layer, n);
+  const std::int32_t off = p.dev_off[static_cast<std::size_t>(layer)];
+  std::vector<std::int32_t> tmp(static_cast<std::size_t>(n));
+  for (std::int32_t i = 0; i < n; ++i) tmp[static_cast<std::size_t>(i)] = C(ids[static_cast<std::size_t>(i)]).slot;
+  // the stream is synchronised below, so pageable sources may be locals
+  if (n > 0) KVC_CUDA(cudaMemcpyAsync(t_.pl_pool + off, tmp.data(), n * 4, cudaMemcpyHostToDevice, st_));
+  const std::int64_t k = pid * L_ + layer;
+  KVC_CUDA(cudaMemcpyAsync(t_.pl_off + k, &off, 4, cudaMemcpyHostToDevice, st_));
+  KVC_CUDA(cudaMemcpyAsync(t_.pl_cnt + k, &n, 4, cudaMemcpyHostToDevice, st_));
+  KVC_CUDA(cudaStreamSynchronize(st_));
+}
+
+void Context::pl_reserve(std::int64_t pid, int layer, std::int32_t n) {
+  Partition& p = parts_[static_cast<std::size_t>(pid)];
   std::int32_t& off = p.dev_off[static_cast<std::size_t>(layer)];
   std::int32_t& cap = p.dev_cap[static_cast<std::size_t>(layer)];
   if (n > cap) {
@@ -684,7 +714,9 @@ void Context::pl_upload(std::int64_t pid, int layer) {
       for (std::size_t q = 0; q < parts_.size(); ++q)
         for (int l = 0; l < L_; ++l) {
           const std::int32_t m = static_cast<std::int32_t>(parts_[q].per_layer[static_cast<std::size_t>(l)].size());
-          const std::int32_t c2 = (static_cast<std::int64_t>(q) == pid && l == layer) ? ncap : m;
+          std::int32_t c2 = (static_cast<std::int64_t>(q) == pid && l == layer) ? ncap : m;
+          const std::size_t fk = q * static_cast<std::size_t>(L_) + static_cast<std::size_t>(l);
+          if (fk < pl_floor_.size()) c2 = std::max(c2, pl_floor_[fk]);  // lists the wave engine holds
           if (pl_bump_ + c2 > t_.pl_pool_cap) fail(-21, "partition-list pool full");
           parts_[q].dev_off[static_cast<std::size_t>(l)] = static_cast<std::int32_t>(pl_bump_);
           parts_[q].dev_cap[static_cast<std::size_t>(l)] = c2;
@@ -697,14 +729,6 @@ void Context::pl_upload(std::int64_t pid, int layer) {
       pl_bump_ += ncap;
     }
   }
-  std::vector<std::int32_t> tmp(static_cast<std::size_t>(n));
-  for (std::int32_t i = 0; i < n; ++i) tmp[static_cast<std::size_t>(i)] = C(ids[static_cast<std::size_t>(i)]).slot;
-  // the stream is synchronised below, so pageable sources may be locals
-  if (n > 0) KVC_CUDA(cudaMemcpyAsync(t_.pl_pool + off, tmp.data(), n * 4, cudaMemcpyHostToDevice, st_));
-  const std::int64_t k = pid * L_ + layer;
-  KVC_CUDA(cudaMemcpyAsync(t_.pl_off + k, &off, 4, cudaMemcpyHostToDevice, st_));
-  KVC_CUDA(cudaMemcpyAsync(t_.pl_cnt + k, &n, 4, cudaMemcpyHostToDevice, st_));
-  KVC_CUDA(cudaStreamSynchronize(st_));
 }
 
 // Partition representative -> device without a host sync: the values go through a pinned ring
@@ -1223,6 +1247,10 @@ void Context::run_inserts(std::int64_t frame_id, std::int64_t pid, int T, std::i
   const int ring_slot = ia_.ring_slot;
   const bool eager = !cfg_.defer_host_splits;
   if (l_hi < 0) l_hi = L_;
+  if (waves_ && !eager && l_lo == 0 && l_hi == L_ && tok0 == 0) {
+    run_inserts_waves(frame_id, pid, T, assigned, launched);
+    return;
+  }
   if (spec_.active) {  // a speculation of an earlier frame is never consumed
     KVC_CUDA(cudaEventSynchronize(spec_.ev));
     spec_.active = false;

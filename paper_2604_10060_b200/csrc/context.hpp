@@ -501,12 +501,21 @@ class Context {
   std::int32_t take_slot();
   std::int64_t new_cluster(std::int32_t layer, std::int64_t parent, std::vector<Member>&& members,
                            bool host);
+  // new_cluster on a slot the caller already holds (the wave engine installs children first)
+  std::int64_t new_cluster_at(std::int32_t slot, std::int32_t layer, std::int64_t parent, std::vector<Member>&& members,
+                              bool host);
   void drop_cluster(std::int64_t id);  // HierIndex::remove_cluster (host side)
+  // drop_cluster without releasing the slot: its pages are freed and the slot returned by the caller
+  void drop_cluster_host(std::int64_t id);
   void frame_add(std::int64_t frame, std::int64_t cid);
   void frame_add_flush(std::int64_t frame);
   std::vector<std::int64_t> fc_pending_;
   void frame_del(std::int64_t frame, std::int64_t cid);
   void pl_upload(std::int64_t pid, int layer);
+  // capacity of the device slot list of (pid, layer) for n entries (may re-lay every list, which
+  // rewrites the device lists from the host ones)
+  void pl_reserve(std::int64_t pid, int layer, std::int32_t n);
+  std::vector<std::int32_t> pl_floor_;  // [pid * L + layer] capacity a compaction keeps (wave engine)
   void upload_partition(std::int64_t pid);
   void flush_resid();
   // store (store.cpp:67-189)
@@ -528,6 +537,21 @@ class Context {
   // one token, no window ring: ia_.ring_slot = -1)
   void run_inserts(std::int64_t frame_id, std::int64_t pid, int T, std::int64_t* assigned, bool launched,
                    int l_lo = 0, int l_hi = -1, int tok0 = 0);
+  // Parallel settle of a frame's host events across domains (context_waves.cpp; deferred mode,
+  // whole frames). KVC_WAVES=0 keeps the one-domain-at-a-time loop of run_inserts.
+  struct Waves;
+  Waves* wv_ = nullptr;
+  bool waves_ = true;
+  bool waves_perturb_ = false;  // KVC_WAVES_PERTURB=1: first-pass counter predictions made wrong (tests)
+  void run_inserts_waves(std::int64_t frame_id, std::int64_t pid, int T, std::int64_t* assigned, bool launched);
+  void replay_runs(int l, std::int64_t frame_id, int T, int t0, int t1, std::int64_t* assigned);
+  void waves_free();
+ public:
+  // frames with events, waves, passes, rolled-back domains, verification k-means, events, stage us,
+  // k-means jobs, k-means us, stats + install us, relaunch us, verify + commit us (cumulative)
+  void wave_profile(double* out12, bool reset);
+
+ private:
   // split slow path
   std::vector<std::int64_t> split_pool(std::int64_t pid, int layer, bool host,
                                        std::vector<Member>&& ids, std::int64_t rows, int depth_unused);

@@ -1,0 +1,1012 @@
+// context_waves.cpp -- parallel settle of a frame's host events (seeds / immediate splits) in
+// deferred mode, bit-identical to the reference's sequential order.
+//
+// The reference inserts a frame layer by layer, token by token (engine.cpp:169-170 ->
+// Maintainer::on_insert, maintainer.cpp:88-176). An immediate split (maintainer.cpp:139-149)
+// draws its k-means seed from ONE global counter, mix_seed(seed, split_counter_++)
+// (maintainer.cpp:222), and its children take the next global cluster ids (index.cpp:105); both
+// are numbered in that layer-major order. Everything else a split touches belongs to its own
+// domain: the parent, its siblings of the same (partition, layer) list, the tokens after it.
+// Residence does not change inside a frame in deferred mode (fetch / enforce_capacity run only on
+// the eager path), so domains are independent apart from the two counters.
+//
+// The engine therefore settles the pending events of ALL domains at once, in waves:
+//   wave: stage every pending event's pool (parent members, buffer, token) in one launch ->
+//         split_two of every pool in one launch (counter PREDICTED from the other domains' event
+//         counts) -> exact children statistics in one launch -> recursion (Eq. 5 on a child,
+//         maintainer.cpp:232-236) as further sub-waves -> children installed (provisional ids
+//         above every existing id, in creation order: the same order relations as the final ids)
+//         -> one relaunch round of every such domain from its next token.
+//   verify: when no domain has events left, the exact counter of every split_two follows from
+//         the final event counts; a split whose predicted counter differs is recomputed with the
+//         exact seed (one launch) and compared. If any assignment differs, that domain is rolled
+//         back to the snapshot taken at its first event (device statistics, page counts and tail
+//         fills of its (partition, layer) clusters; its speculative children freed) and settled
+//         again with the corrected counts. The lowest failing domain is always exact on its next
+//         pass, so the loop terminates.
+//   commit: the host replays every domain in reference order -- outcome runs, events, final ids,
+//         counters, LRU ticks (store.cpp:82-86, 139-141) -- exactly as the sequential path does,
+//         then uploads the final cluster ids, partition lists and window-ring owners.
+// The host state (Cluster objects, ticks, counters) is only touched at commit, so a rollback is a
+// device-side restore plus a reset of the domain's wave record.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+
+#include "context.hpp"
+#include "kmeans.hpp"
+
+namespace kvc {
+
+namespace {
+
+inline double tau_at(std::int64_t n, const kvc_cfg& c) {  // maintainer.cpp:11-14 (as context.cpp tau_of)
+  return c.tau_min + (c.tau_max - c.tau_min) * std::exp(-static_cast<double>(n) / c.n0);
+}
+
+struct DBuf {  // growable device buffer
+  void* p = nullptr;
+  std::size_t cap = 0;
+  // keep: the first `keep` bytes survive a growth (copied on the stream, which is synchronised)
+  void ensure(std::size_t bytes, cudaStream_t st, std::size_t keep = 0) {
+    if (bytes <= cap) return;
+    std::size_t n = std::max<std::size_t>(bytes, cap * 2);
+    n = std::max<std::size_t>(n, 1 << 16);
+    void* q = nullptr;
+    KVC_CUDA(cudaMalloc(&q, n));
+    if (p) {
+      if (keep) KVC_CUDA(cudaMemcpyAsync(q, p, std::min(keep, cap), cudaMemcpyDeviceToDevice, st));
+      KVC_CUDA(cudaStreamSynchronize(st));
+      KVC_CUDA(cudaFree(p));
+    }
+    p = q;
+    cap = n;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+  template <class T>
+  T* as(std::size_t byte_off = 0) const {
+    return reinterpret_cast<T*>(static_cast<std::uint8_t*>(p) + byte_off);
+  }
+};
+
+struct HBuf {  // growable pinned host buffer (contents not kept)
+  void* p = nullptr;
+  std::size_t cap = 0;
+  void ensure(std::size_t bytes, cudaStream_t st) {
+    if (bytes <= cap) return;
+    const std::size_t n = std::max<std::size_t>({bytes, cap * 2, std::size_t{1} << 16});
+    if (p) {
+      KVC_CUDA(cudaStreamSynchronize(st));
+      KVC_CUDA(cudaFreeHost(p));
+    }
+    KVC_CUDA(cudaHostAlloc(&p, n, cudaHostAllocDefault));
+    cap = n;
+  }
+  void release() {
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    cap = 0;
+  }
+  template <class T>
+  T* as(std::size_t byte_off = 0) const {
+    return reinterpret_cast<T*>(static_cast<std::uint8_t*>(p) + byte_off);
+  }
+};
+
+// Packs several arrays into one pinned buffer and moves them in one H2D copy.
+struct Upload {
+  HBuf h;
+  DBuf d;
+  std::size_t used = 0;
+  std::vector<std::pair<const void*, std::size_t>> parts;
+  void reset() {
+    used = 0;
+    parts.clear();
+  }
+  std::size_t add(const void* src, std::size_t bytes) {
+    const std::size_t off = (used + 15) & ~std::size_t{15};
+    parts.emplace_back(src, bytes);
+    used = off + bytes;
+    return off;
+  }
+  // copies the parts (in add order) into the pinned buffer and sends them; returns device base
+  std::uint8_t* send(cudaStream_t st) {
+    h.ensure(used, st);
+    d.ensure(used, st);
+    std::size_t off = 0;
+    for (auto& pr : parts) {
+      off = (off + 15) & ~std::size_t{15};
+      if (pr.second) std::memcpy(h.as<std::uint8_t>(off), pr.first, pr.second);
+      off += pr.second;
+    }
+    if (used) KVC_CUDA(cudaMemcpyAsync(d.p, h.p, used, cudaMemcpyHostToDevice, st));
+    return static_cast<std::uint8_t*>(d.p);
+  }
+};
+
+constexpr int kNoKid = -1;
+inline int leaf_code(int i) { return -2 - i; }
+inline bool is_leaf_code(int k) { return k <= -2; }
+inline int leaf_of(int k) { return -2 - k; }
+
+}  // namespace
+
+struct Context::Waves {
+  struct Op {  // one split_two call
+    int ev = -1, depth = 0;
+    std::vector<int> rows;  // pool rows (relative to the event's staged pool)
+    std::uint64_t ctr = 0;  // the counter its k-means used
+    std::int64_t ok_ctr = -1;  // a counter its result was verified for
+    std::vector<std::int32_t> assign;
+    int kids[2] = {kNoKid, kNoKid};  // op index, leaf_code(leaf), or kNoKid (empty group)
+  };
+  struct Leaf {
+    std::vector<int> rows;
+    std::int32_t slot = -1;
+  };
+  struct Event {
+    int layer = 0, tok = 0, kind = 0;
+    std::int32_t parent_slot = -1;
+    std::int64_t row0 = 0;  // staged pool rows [row0, row0 + n)
+    int n = 0;
+    int root = -1;              // root op (splits) or leaf (seeds: leaf_code)
+    std::vector<int> ops;       // DFS preorder = counter order
+    std::vector<int> stack;     // ops still to run (top = next in preorder)
+    std::vector<int> emitted;   // leaves in emission order (filled at the end of the event)
+    std::uint64_t ctr0 = 0;     // predicted counter of the first op
+  };
+  struct Dom {
+    bool active = false;  // has events this frame (snapshot taken)
+    bool done = true;
+    int cur = 0;          // next token to resolve
+    int pend_tok = -1, pend_kind = 0;
+    std::int32_t pend_slot = -1;
+    bool pend_valid = false;  // a pending event not yet turned into an Event
+    bool retry = false;   // relaunch from pend_tok without an event (stale residence)
+    bool first_retry = false;
+    int cur_ev = -1;      // the event being settled (its ops still to run count in predictions)
+    int first_tok = -1, first_kind = 0;
+    std::int32_t first_slot = -1;
+    int snap0 = 0, snap_n = 0;
+    std::vector<int> events;
+    std::vector<std::int32_t> pl;     // speculative (partition, layer) slot list
+    std::vector<std::int32_t> taken;  // leaf slots created by this pass
+    int ops = 0, prev_ops = -1;
+    std::uint64_t epoch = 0;
+  };
+  std::vector<Op> ops;
+  std::vector<Leaf> leaves;
+  std::vector<Event> evs;
+  std::vector<Dom> dom;
+  // per-slot pool sizes during speculation (valid when stamp == the owning domain's epoch)
+  std::vector<std::int64_t> sz;
+  std::vector<std::uint64_t> sz_stamp;
+  std::uint64_t epoch_next = 1;
+  // device
+  DBuf stage_k, stage_v, stage_f32;  // staged pools (kv dtype, f32), append-only within a frame
+  std::int64_t rows_used = 0;
+  DBuf snap;                          // slot snapshots
+  std::int64_t snap_used = 0;
+  DBuf km_scratch, km_out;            // k-means scratch / assign | meta | counts
+  HBuf h_out;
+  Upload up;
+  std::int64_t prov_next = 0;
+  // stats (cumulative; kvc_debug_wave_profile)
+  double st[12] = {0};
+};
+
+void Context::waves_free() {
+  if (!wv_) return;
+  wv_->stage_k.release();
+  wv_->stage_v.release();
+  wv_->stage_f32.release();
+  wv_->snap.release();
+  wv_->km_scratch.release();
+  wv_->km_out.release();
+  wv_->h_out.release();
+  wv_->up.h.release();
+  wv_->up.d.release();
+  delete wv_;
+  wv_ = nullptr;
+}
+
+void Context::wave_profile(double* out, bool reset) {
+  for (int i = 0; i < 12; ++i) out[i] = wv_ ? wv_->st[i] : 0.0;
+  if (reset && wv_)
+    for (double& x : wv_->st) x = 0.0;
+}
+
+// Replays device outcomes of domain l, tokens [t0, t1) (the outcome runs of run_inserts).
+void Context::replay_runs(int l, std::int64_t frame_id, int T, int t0, int t1, std::int64_t* assigned) {
+  const int ring_slot = ia_.ring_slot;
+  const std::int32_t* evk = h_evk_ + static_cast<std::size_t>(l) * t_.tmax;
+  const std::int32_t* evs = h_evs_ + static_cast<std::size_t>(l) * t_.tmax;
+  std::int32_t* owner = ring_slot >= 0 ? &ring_owner_h_[(static_cast<std::size_t>(l) * t_.W + ring_slot) * t_.tmax] : nullptr;
+  std::int64_t last_cid = -1;
+  for (int t = t0; t < t1;) {
+    const std::int32_t slot = evs[t];
+    const std::int32_t kind = evk[t];
+    int u = t + 1;
+    if (kind != EV_DEFER)
+      while (u < t1 && evs[u] == slot && evk[u] == kind) ++u;
+    const int n = u - t;
+    if (slot < 0 || static_cast<std::size_t>(slot) >= slot_id_.size() || slot_id_[static_cast<std::size_t>(slot)] < 0) {
+      std::string m = "wave replay: outcome names an unknown slot: domain " + std::to_string(l) + " token " +
+                      std::to_string(t) + " of [" + std::to_string(t0) + "," + std::to_string(t1) + ") slot " +
+                      std::to_string(slot) + " kind " + std::to_string(kind);
+      if (wv_ && static_cast<std::size_t>(l) < wv_->dom.size()) {
+        const Waves::Dom& D = wv_->dom[static_cast<std::size_t>(l)];
+        m += "; first event " + std::to_string(D.first_tok) + " kind " + std::to_string(D.first_kind) + " events:";
+        for (int ei : D.events) {
+          const Waves::Event& e = wv_->evs[static_cast<std::size_t>(ei)];
+          m += " (tok " + std::to_string(e.tok) + " kind " + std::to_string(e.kind) + " parent " + std::to_string(e.parent_slot) + " leaves";
+          for (int li : e.emitted) m += " " + std::to_string(wv_->leaves[static_cast<std::size_t>(li)].slot);
+          m += ")";
+        }
+        m += " pl:";
+        for (std::int32_t x : D.pl) m += " " + std::to_string(x);
+      }
+      fail(-11, m);
+    }
+    const std::int64_t cid = slot_id_[static_cast<std::size_t>(slot)];
+    Cluster& c = *clusters_[static_cast<std::size_t>(cid)];
+    mstats_[0] += n;
+    c.stat_count += n;
+    c.last_touch = std::max(c.last_touch, frame_id);
+    if (cid != last_cid) {
+      fc_pending_.push_back(cid);
+      last_cid = cid;
+    }
+    if (owner) std::fill(owner + t, owner + u, slot);
+    (kind == EV_ABSORB ? c.members : c.buffer).push_run(frame_id, t, n);
+    device_entries_ += n;
+    set_flag(cid, CF_TRACKED, true);
+    tick_ += n;
+    last_use_[static_cast<std::size_t>(cid)] = tick_ - 1;
+    switch (kind) {
+      case EV_ABSORB:
+        if (is_host(cid)) c.device_tail += n;
+        mstats_[1] += n;
+        break;
+      case EV_BUFJOIN:
+        mstats_[3] += n;
+        break;
+      case EV_DEFER:
+        mstats_[6] += n;
+        set_flag(cid, CF_LAZY, true);
+        mstats_[3] += n;
+        break;
+      default:
+        fail(-11, "unexpected device event kind");
+    }
+    if (assigned) std::fill(assigned + static_cast<std::size_t>(l) * T + t, assigned + static_cast<std::size_t>(l) * T + u, cid);
+    t = u;
+  }
+}
+
+void Context::run_inserts_waves(std::int64_t frame_id, std::int64_t pid, int T, std::int64_t* assigned, bool launched) {
+  using clk = std::chrono::steady_clock;
+  auto us = [](clk::time_point a, clk::time_point b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
+  const auto t_start = clk::now();
+  if (!wv_) wv_ = new Waves();
+  Waves& W = *wv_;
+  if (spec_.active) {
+    KVC_CUDA(cudaEventSynchronize(spec_.ev));
+    spec_.active = false;
+  }
+  ia_.T = T;
+  ia_.pid = static_cast<std::int32_t>(pid);
+  const int ring_slot = ia_.ring_slot;
+  for (double& x : ingest_t_) x = 0.0;
+  double t_wait = 0.0;
+
+  // ---- the first round (all domains from token 0)
+  if (launched) {
+    KVC_CUDA(cudaEventSynchronize(ping_wait_));
+  } else {
+    std::vector<int> all(static_cast<std::size_t>(L_)), zero(static_cast<std::size_t>(L_), 0);
+    std::iota(all.begin(), all.end(), 0);
+    launch_round(all, zero);
+    const auto w0 = clk::now();
+    sync();
+    t_wait += us(w0, clk::now());
+  }
+  check_err_word(*h_err_);
+  if (round_timed_) {
+    float ms = 0.f;
+    for (int i = 0; i < 5; ++i) {
+      KVC_CUDA(cudaEventElapsedTime(&ms, ev_[i], ev_[i + 1]));
+      ingest_t_[i] += ms * 1e3;
+    }
+  }
+
+  W.ops.clear();
+  W.leaves.clear();
+  W.evs.clear();
+  W.dom.assign(static_cast<std::size_t>(L_), Waves::Dom{});
+  W.rows_used = 0;
+  W.snap_used = 0;
+  if (W.sz.size() < slot_id_.size()) {
+    W.sz.resize(slot_id_.size(), 0);
+    W.sz_stamp.resize(slot_id_.size(), 0);
+  }
+  const std::uint64_t ctr_base = static_cast<std::uint64_t>(split_counter_);
+  W.prov_next = std::int64_t{1} << 40;
+
+  auto size_of = [&](std::int32_t slot, Waves::Dom& D) -> std::int64_t& {
+    const std::size_t s = static_cast<std::size_t>(slot);
+    if (W.sz_stamp[s] != D.epoch) {
+      W.sz_stamp[s] = D.epoch;
+      const std::int64_t cid = slot_id_[s];
+      W.sz[s] = cid >= 0 && clusters_[static_cast<std::size_t>(cid)]
+                    ? static_cast<std::int64_t>(clusters_[static_cast<std::size_t>(cid)]->members.size() +
+                                                clusters_[static_cast<std::size_t>(cid)]->buffer.size())
+                    : 0;
+    }
+    return W.sz[s];
+  };
+  // counts the outcome of tokens [a, b) of domain l into the pool sizes
+  auto count_outcome = [&](int l, int a, int b) {
+    Waves::Dom& D = W.dom[static_cast<std::size_t>(l)];
+    const std::int32_t* evs = h_evs_ + static_cast<std::size_t>(l) * t_.tmax;
+    for (int t = a; t < b; ++t) size_of(evs[t], D) += 1;
+  };
+  auto host_slots = [&](int l) {
+    std::vector<std::int32_t> v;
+    const auto& ids = parts_[static_cast<std::size_t>(pid)].per_layer[static_cast<std::size_t>(l)];
+    v.reserve(ids.size());
+    for (std::int64_t id : ids) v.push_back(C(id).slot);
+    return v;
+  };
+  // a stop reported by a round for domain l
+  auto take_stop = [&](int l) {
+    Waves::Dom& D = W.dom[static_cast<std::size_t>(l)];
+    const int stop = h_stop_[l];
+    count_outcome(l, D.cur, std::min(stop, T));
+    if (stop >= T) {
+      D.done = true;
+      D.cur = T;
+      return;
+    }
+    D.done = false;
+    D.cur = stop;
+    D.pend_tok = stop;
+    D.pend_kind = h_stop_[L_ + l];
+    D.pend_slot = h_stop_[2 * L_ + l];
+    D.retry = false;
+    D.pend_valid = true;
+    if (D.pend_kind == EV_EAGER) fail(-11, "wave engine: eager event in deferred mode");
+    if (D.pend_kind == EV_SPLIT && is_host(slot_id_[static_cast<std::size_t>(D.pend_slot)])) {
+      // the pipelined launch decided with the residence before the previous frame's cadence
+      // offloaded the cluster (residence only turns Device -> Host between frames): nothing of
+      // this token was committed; resolve the domain again from it
+      D.retry = true;
+      D.pend_valid = false;
+    }
+    if (D.pend_kind != EV_SEED && D.pend_kind != EV_SPLIT) fail(-11, "wave engine: unexpected host event");
+  };
+
+  // ---- domains with events after the first round: snapshot their (partition, layer) clusters
+  std::vector<std::int32_t> snap_slots;
+  bool any_events = false;
+  for (int l = 0; l < L_; ++l) {
+    Waves::Dom& D = W.dom[static_cast<std::size_t>(l)];
+    D.epoch = W.epoch_next++;
+    D.cur = 0;
+    take_stop(l);
+    if (D.done) continue;
+    D.active = true;
+    any_events = true;
+    D.first_tok = D.pend_tok;
+    D.first_kind = D.pend_kind;
+    D.first_slot = D.pend_slot;
+    D.first_retry = D.retry;
+    D.pl = host_slots(l);
+    D.snap0 = static_cast<int>(snap_slots.size());
+    D.snap_n = static_cast<int>(D.pl.size());
+    snap_slots.insert(snap_slots.end(), D.pl.begin(), D.pl.end());
+  }
+  if (!any_events) {  // no host events: plain replay
+    for (int l = 0; l < L_; ++l) replay_runs(l, frame_id, T, 0, T, assigned);
+    frame_add_flush(frame_id);
+    ingest_t_[5] = t_wait;
+    ingest_t_[6] = us(t_start, clk::now()) - t_wait;
+    return;
+  }
+  const std::size_t snap_rb = slot_snap_bytes(d_);
+  W.snap.ensure(snap_slots.size() * snap_rb, st_);
+  if (!snap_slots.empty()) {
+    W.up.reset();
+    const std::size_t o = W.up.add(snap_slots.data(), snap_slots.size() * 4);
+    std::uint8_t* db = W.up.send(st_);
+    launches_ += launch_snap_slots(t_, reinterpret_cast<const std::int32_t*>(db + o), static_cast<std::int32_t>(snap_slots.size()),
+                                   W.snap.p, st_);
+  }
+  W.st[0] += 1;  // frames with events
+
+  const std::size_t rb = static_cast<std::size_t>(d_) * es_;
+  const std::int64_t frame_rows = static_cast<std::int64_t>(L_) * t_.tmax;
+  double t_stage = 0, t_km = 0, t_stats = 0, t_inst = 0, t_relaunch = 0, t_verify = 0;
+
+  int passes = 0;
+  // predicted counter of the next op of domain l
+  auto predict = [&](int l) -> std::uint64_t {
+    std::uint64_t c = ctr_base;
+    for (int k = 0; k < l; ++k) {
+      const Waves::Dom& E = W.dom[static_cast<std::size_t>(k)];
+      if (!E.active) continue;
+      std::int64_t est = E.ops;
+      if (!E.done) {
+        std::int64_t left = E.pend_valid && E.pend_kind == EV_SPLIT ? 1 : 0;
+        if (E.cur_ev >= 0) left += static_cast<std::int64_t>(W.evs[static_cast<std::size_t>(E.cur_ev)].stack.size());
+        est = std::max<std::int64_t>(E.ops + left, E.prev_ops);
+      }
+      c += static_cast<std::uint64_t>(est);
+    }
+    // test hook (KVC_WAVES_PERTURB=1): every first-pass prediction is wrong, so every split is
+    // re-verified and (almost) every domain with events is rolled back and settled again
+    if (waves_perturb_ && passes == 1) c += 7;
+    return c + static_cast<std::uint64_t>(W.dom[static_cast<std::size_t>(l)].ops);
+  };
+
+  // k-means of a batch of ops with the given counters -> assignments (host) ; returns false on
+  // a degenerate row
+  auto run_kmeans = [&](const std::vector<int>& opl, const std::vector<std::uint64_t>& ctrs,
+                        std::vector<std::vector<std::int32_t>>& out) {
+    const auto k0 = clk::now();
+    const std::size_t nj = opl.size();
+    std::vector<std::int32_t> idx;
+    std::vector<std::size_t> idx_off(nj), scr_off(nj), out_off(nj);
+    std::size_t scr = 0, outw = 0;
+    for (std::size_t j = 0; j < nj; ++j) {
+      const Waves::Op& o = W.ops[static_cast<std::size_t>(opl[j])];
+      const Waves::Event& e = W.evs[static_cast<std::size_t>(o.ev)];
+      idx_off[j] = idx.size();
+      for (int r : o.rows) idx.push_back(static_cast<std::int32_t>(e.row0 + r));
+      scr_off[j] = scr;
+      scr += (o.rows.size() * (2 * static_cast<std::size_t>(d_) + 3) + 1) * 8;
+      out_off[j] = outw;
+      outw += o.rows.size() + 4;
+    }
+    W.km_scratch.ensure(scr, st_);
+    W.km_out.ensure(outw * 4 + nj * 8 + 64, st_);
+    std::vector<SplitJob> jobs(nj);
+    std::int32_t* dout = W.km_out.as<std::int32_t>();
+    double* dobj = reinterpret_cast<double*>(W.km_out.as<std::uint8_t>((outw * 4 + 7) & ~std::size_t{7}));
+    W.up.reset();
+    const std::size_t o_idx = W.up.add(idx.data(), idx.size() * 4);
+    const std::size_t o_jobs = W.up.add(jobs.data(), nj * sizeof(SplitJob));  // filled below
+    // the jobs point into the uploaded index array: size the device side first, then fill them
+    W.up.h.ensure(W.up.used, st_);
+    W.up.d.ensure(W.up.used, st_);
+    std::uint8_t* dbase = static_cast<std::uint8_t*>(W.up.d.p);
+    for (std::size_t j = 0; j < nj; ++j) {
+      const Waves::Op& o = W.ops[static_cast<std::size_t>(opl[j])];
+      Rng64 rng(mix_seed(maint_seed_, ctrs[j]));
+      const int n = static_cast<int>(o.rows.size());
+      SplitJob& J = jobs[j];
+      J.rows = W.stage_f32.as<float>();
+      J.idx = reinterpret_cast<const std::int32_t*>(dbase + o_idx) + idx_off[j];
+      J.scratch = W.km_scratch.as<double>(scr_off[j]);
+      J.assign = dout + out_off[j];
+      J.meta = dout + out_off[j] + n;
+      J.objective = dobj + j;
+      J.first = static_cast<std::int32_t>(rng.index(static_cast<std::size_t>(n)));
+      J.uni = rng.uniform();
+      J.n = n;
+    }
+    std::uint8_t* db = W.up.send(st_);
+    launches_ += launch_split_two_batch(reinterpret_cast<const SplitJob*>(db + o_jobs), static_cast<int>(nj), d_, st_);
+    W.h_out.ensure(outw * 4, st_);
+    KVC_CUDA(cudaMemcpyAsync(W.h_out.p, dout, outw * 4, cudaMemcpyDeviceToHost, st_));
+    sync();
+    out.resize(nj);
+    for (std::size_t j = 0; j < nj; ++j) {
+      const Waves::Op& o = W.ops[static_cast<std::size_t>(opl[j])];
+      const std::int32_t* a = W.h_out.as<std::int32_t>() + out_off[j];
+      const std::int32_t* meta = a + o.rows.size();
+      if (meta[3] != 0) fail(-2, "normalize of zero vector");
+      out[j].assign(a, a + o.rows.size());
+    }
+    W.st[7] += static_cast<double>(nj);  // k-means jobs
+    return us(k0, clk::now());
+  };
+
+  // ---------------------------------------------------------------- the wave / pass loop
+  for (;;) {
+    passes += 1;
+    // waves until no domain has a pending event
+    for (;;) {
+      std::vector<int> E;  // domains with a pending event (not retries)
+      std::vector<int> relaunch, rcur;
+      for (int l = 0; l < L_; ++l) {
+        Waves::Dom& D = W.dom[static_cast<std::size_t>(l)];
+        if (!D.active || D.done) continue;
+        if (D.retry) {
+          relaunch.push_back(l);
+          rcur.push_back(D.pend_tok);
+          D.cur = D.pend_tok;
+          D.retry = false;
+          continue;
+        }
+        E.push_back(l);
+      }
+      if (E.empty() && relaunch.empty()) break;
+      W.st[1] += 1;  // waves
+      const auto s0 = clk::now();
+      // ---- events: stage pools
+      std::vector<GatherJob> gj;
+      std::vector<int> new_evs;
+      std::int64_t rows_need = W.rows_used;
+      for (int l : E) {
+        Waves::Dom& D = W.dom[static_cast<std::size_t>(l)];
+        Waves::Event e;
+        e.layer = l;
+        e.tok = D.pend_tok;
+        e.kind = D.pend_kind;
+        e.parent_slot = D.pend_kind == EV_SPLIT ? D.pend_slot : -1;
+        e.n = e.kind == EV_SPLIT ? static_cast<int>(size_of(e.parent_slot, D)) + 1 : 1;
+        e.row0 = rows_need;
+        rows_need += e.n;
+        new_evs.push_back(static_cast<int>(W.evs.size()));
+        D.cur_ev = static_cast<int>(W.evs.size());
+        D.pend_valid = false;
+        D.events.push_back(static_cast<int>(W.evs.size()));
+        W.evs.push_back(std::move(e));
+      }
+      const std::int64_t keep_rows = W.rows_used;
+      W.stage_k.ensure(static_cast<std::size_t>(rows_need) * rb, st_, static_cast<std::size_t>(keep_rows) * rb);
+      W.stage_v.ensure(static_cast<std::size_t>(rows_need) * rb, st_, static_cast<std::size_t>(keep_rows) * rb);
+      W.stage_f32.ensure(static_cast<std::size_t>(rows_need) * d_ * 4, st_, static_cast<std::size_t>(keep_rows) * d_ * 4);
+      W.rows_used = rows_need;
+      W.km_out.ensure(new_evs.size() * 4 + 64, st_);
+      for (std::size_t i = 0; i < new_evs.size(); ++i) {
+        const Waves::Event& e = W.evs[static_cast<std::size_t>(new_evs[i])];
+        GatherJob g{};
+        g.slot = e.parent_slot;
+        g.with_buf = 1;
+        g.row0 = e.row0;
+        g.frame_row = static_cast<std::int64_t>(e.layer) * t_.tmax + e.tok;
+        g.count_out = W.km_out.as<std::int32_t>() + i;
+        gj.push_back(g);
+      }
+      if (!gj.empty()) {
+        W.up.reset();
+        const std::size_t o = W.up.add(gj.data(), gj.size() * sizeof(GatherJob));
+        std::uint8_t* db = W.up.send(st_);
+        launches_ += launch_gather_batch(t_, reinterpret_cast<const GatherJob*>(db + o), static_cast<std::int32_t>(gj.size()),
+                                         d_fk_, d_fv_, W.stage_k.p, W.stage_v.p, st_);
+        launches_ += launch_to_f32(t_, W.stage_k.as<std::uint8_t>(static_cast<std::size_t>(keep_rows) * rb),
+                                   W.stage_f32.as<float>(static_cast<std::size_t>(keep_rows) * d_ * 4),
+                                   (rows_need - keep_rows) * d_, st_);
+        W.h_out.ensure(gj.size() * 4, st_);
+        KVC_CUDA(cudaMemcpyAsync(W.h_out.p, W.km_out.p, gj.size() * 4, cudaMemcpyDeviceToHost, st_));
+        sync();
+        for (std::size_t i = 0; i < new_evs.size(); ++i)
+          if (W.h_out.as<std::int32_t>()[i] != W.evs[static_cast<std::size_t>(new_evs[i])].n)
+            fail(-11, "wave engine: staged pool size differs from the host's count");
+      }
+      t_stage += us(s0, clk::now());
+      // ---- root ops / seed leaves
+      for (int ei : new_evs) {
+        Waves::Event& e = W.evs[static_cast<std::size_t>(ei)];
+        if (e.kind == EV_SEED) {
+          Waves::Leaf lf;
+          lf.rows = {0};
+          W.leaves.push_back(std::move(lf));
+          e.root = leaf_code(static_cast<int>(W.leaves.size()) - 1);
+        } else {
+          Waves::Op o;
+          o.ev = ei;
+          o.depth = 0;
+          o.rows.resize(static_cast<std::size_t>(e.n));
+          std::iota(o.rows.begin(), o.rows.end(), 0);
+          W.ops.push_back(std::move(o));
+          e.root = static_cast<int>(W.ops.size()) - 1;
+          e.stack.push_back(e.root);
+        }
+      }
+      // ---- sub-waves: one op per event at a time, in DFS preorder (its counter order)
+      std::vector<std::pair<int, int>> pending_stats;  // (leaf, event) needing stats + var
+      for (int ei : new_evs) {
+        const Waves::Event& e = W.evs[static_cast<std::size_t>(ei)];
+        if (is_leaf_code(e.root)) pending_stats.emplace_back(leaf_of(e.root), ei);
+      }
+      bool first_sub = true;
+      for (;;) {
+        std::vector<int> opl;
+        std::vector<std::uint64_t> ctrs;
+        for (int ei : new_evs) {
+          Waves::Event& e = W.evs[static_cast<std::size_t>(ei)];
+          if (e.stack.empty()) continue;
+          const int oi = e.stack.back();
+          e.stack.pop_back();
+          Waves::Dom& D = W.dom[static_cast<std::size_t>(e.layer)];
+          Waves::Op& o = W.ops[static_cast<std::size_t>(oi)];
+          o.ctr = predict(e.layer);
+          D.ops += 1;
+          e.ops.push_back(oi);
+          opl.push_back(oi);
+          ctrs.push_back(o.ctr);
+        }
+        if (opl.empty() && !(first_sub && !pending_stats.empty())) break;
+        first_sub = false;
+        // k-means
+        std::vector<std::vector<std::int32_t>> res;
+        if (!opl.empty()) t_km += run_kmeans(opl, ctrs, res);
+        const auto st0 = clk::now();
+        // groups -> exact statistics in fresh slots
+        struct G {
+          int op, g;
+          std::vector<int> rows;
+          std::int32_t slot;
+        };
+        std::vector<G> groups;
+        for (std::size_t j = 0; j < opl.size(); ++j) {
+          Waves::Op& o = W.ops[static_cast<std::size_t>(opl[j])];
+          o.assign = std::move(res[j]);
+          std::vector<int> g2[2];
+          for (std::size_t i = 0; i < o.rows.size(); ++i) g2[o.assign[i]].push_back(o.rows[i]);
+          for (int g = 0; g < 2; ++g)
+            if (!g2[g].empty()) groups.push_back({opl[j], g, std::move(g2[g]), take_slot()});
+        }
+        std::vector<AppendRun> runs;
+        std::vector<std::int32_t> idx, slots;
+        for (const G& g : groups) {
+          const Waves::Event& e = W.evs[static_cast<std::size_t>(W.ops[static_cast<std::size_t>(g.op)].ev)];
+          runs.push_back({g.slot, static_cast<std::int32_t>(idx.size()), static_cast<std::int32_t>(g.rows.size()), 0});
+          for (int r : g.rows) idx.push_back(static_cast<std::int32_t>(e.row0 + r));
+          slots.push_back(g.slot);
+        }
+        for (auto& ps : pending_stats) {  // seeds
+          Waves::Leaf& lf = W.leaves[static_cast<std::size_t>(ps.first)];
+          const Waves::Event& e = W.evs[static_cast<std::size_t>(ps.second)];
+          lf.slot = take_slot();
+          runs.push_back({lf.slot, static_cast<std::int32_t>(idx.size()), 1, 0});
+          idx.push_back(static_cast<std::int32_t>(e.row0));
+          slots.push_back(lf.slot);
+          W.dom[static_cast<std::size_t>(e.layer)].taken.push_back(lf.slot);
+        }
+        pending_stats.clear();
+        std::vector<double> vars(runs.size());
+        if (!runs.empty()) {
+          W.up.reset();
+          const std::size_t o_r = W.up.add(runs.data(), runs.size() * sizeof(AppendRun));
+          const std::size_t o_i = W.up.add(idx.data(), idx.size() * 4);
+          const std::size_t o_s = W.up.add(slots.data(), slots.size() * 4);
+          std::uint8_t* db = W.up.send(st_);
+          launches_ += launch_exact_stats(t_, reinterpret_cast<const AppendRun*>(db + o_r), static_cast<std::int32_t>(runs.size()),
+                                          reinterpret_cast<const std::int32_t*>(db + o_i), W.stage_k.p, st_);
+          W.km_out.ensure(runs.size() * 8 + 64, st_);
+          launches_ += launch_read_vars(t_, reinterpret_cast<const std::int32_t*>(db + o_s), static_cast<std::int32_t>(slots.size()),
+                                        W.km_out.as<double>(), st_);
+          W.h_out.ensure(runs.size() * 8, st_);
+          KVC_CUDA(cudaMemcpyAsync(W.h_out.p, W.km_out.p, runs.size() * 8, cudaMemcpyDeviceToHost, st_));
+          sync();
+          std::memcpy(vars.data(), W.h_out.p, runs.size() * 8);
+        }
+        // recursion decisions (maintainer.cpp:228-238), in group order per op
+        for (std::size_t gi = 0; gi < groups.size(); ++gi) {
+          G& g = groups[gi];
+          const int o_ev = W.ops[static_cast<std::size_t>(g.op)].ev, o_depth = W.ops[static_cast<std::size_t>(g.op)].depth;
+          const Waves::Event& e = W.evs[static_cast<std::size_t>(o_ev)];
+          const std::int64_t sz = static_cast<std::int64_t>(g.rows.size());
+          if (o_depth + 1 < cfg_.max_split_depth && sz >= 2 && vars[gi] > tau_at(sz, cfg_)) {
+            free_slots_.push_back(g.slot);  // no pages were attached
+            Waves::Op c;
+            c.ev = o_ev;
+            c.depth = o_depth + 1;
+            c.rows = std::move(g.rows);
+            W.ops.push_back(std::move(c));
+            W.ops[static_cast<std::size_t>(g.op)].kids[g.g] = static_cast<int>(W.ops.size()) - 1;
+          } else {
+            Waves::Leaf lf;
+            lf.rows = std::move(g.rows);
+            lf.slot = g.slot;
+            W.leaves.push_back(std::move(lf));
+            W.ops[static_cast<std::size_t>(g.op)].kids[g.g] = leaf_code(static_cast<int>(W.leaves.size()) - 1);
+            W.dom[static_cast<std::size_t>(e.layer)].taken.push_back(g.slot);
+          }
+        }
+        // children to run: push kid 1 first so kid 0 (its subtree) runs first (preorder)
+        for (int oi : opl) {
+          const Waves::Op& o = W.ops[static_cast<std::size_t>(oi)];
+          Waves::Event& e = W.evs[static_cast<std::size_t>(o.ev)];
+          for (int g = 1; g >= 0; --g)
+            if (o.kids[g] >= 0) e.stack.push_back(o.kids[g]);
+        }
+        t_stats += us(st0, clk::now());
+      }
+      // ---- install children: headers, pages, partition lists; relaunch the domains
+      const auto i0 = clk::now();
+      std::vector<SlotHeader> hd;
+      std::vector<AppendRun> runs;
+      std::vector<std::int32_t> idx;
+      for (int ei : new_evs) {
+        Waves::Event& e = W.evs[static_cast<std::size_t>(ei)];
+        Waves::Dom& D = W.dom[static_cast<std::size_t>(e.layer)];
+        // emission order: in-order over the split tree (maintainer.cpp:224-238)
+        if (is_leaf_code(e.root)) {
+          e.emitted.push_back(leaf_of(e.root));
+        } else {
+          auto walk = [&](auto&& self, int oi) -> void {
+            const Waves::Op& o = W.ops[static_cast<std::size_t>(oi)];
+            for (int g = 0; g < 2; ++g) {
+              if (o.kids[g] == kNoKid) continue;
+              if (is_leaf_code(o.kids[g]))
+                e.emitted.push_back(leaf_of(o.kids[g]));
+              else
+                self(self, o.kids[g]);
+            }
+          };
+          walk(walk, e.root);
+        }
+        if (e.kind == EV_SPLIT) D.pl.erase(std::remove(D.pl.begin(), D.pl.end(), e.parent_slot), D.pl.end());
+        for (int li : e.emitted) {
+          const Waves::Leaf& lf = W.leaves[static_cast<std::size_t>(li)];
+          const std::int64_t n = static_cast<std::int64_t>(lf.rows.size());
+          hd.push_back({lf.slot, 0, W.prov_next++, n});
+          runs.push_back({lf.slot, static_cast<std::int32_t>(idx.size()), static_cast<std::int32_t>(n), 0});
+          for (int r : lf.rows) idx.push_back(static_cast<std::int32_t>(e.row0 + r));
+          D.pl.push_back(lf.slot);
+          W.sz_stamp[static_cast<std::size_t>(lf.slot)] = D.epoch;
+          W.sz[static_cast<std::size_t>(lf.slot)] = n;
+        }
+        D.cur = e.tok + 1;
+        D.cur_ev = -1;
+        if (D.cur >= T) {
+          D.done = true;
+        } else {
+          relaunch.push_back(e.layer);
+          rcur.push_back(D.cur);
+        }
+      }
+      // partition lists of every domain in speculation (capacity first: a compaction rewrites
+      // the device lists from the host ones)
+      std::vector<std::int32_t> plrec, ploff;
+      pl_floor_.assign(parts_.size() * static_cast<std::size_t>(L_), 0);
+      for (int l = 0; l < L_; ++l)
+        if (W.dom[static_cast<std::size_t>(l)].active)
+          pl_floor_[static_cast<std::size_t>(pid) * L_ + l] = static_cast<std::int32_t>(W.dom[static_cast<std::size_t>(l)].pl.size());
+      for (int ei : new_evs) {
+        const int l = W.evs[static_cast<std::size_t>(ei)].layer;
+        pl_reserve(pid, l, static_cast<std::int32_t>(W.dom[static_cast<std::size_t>(l)].pl.size()));
+      }
+      pl_floor_.clear();
+      for (int l = 0; l < L_; ++l) {
+        const Waves::Dom& D = W.dom[static_cast<std::size_t>(l)];
+        if (!D.active) continue;
+        ploff.push_back(static_cast<std::int32_t>(plrec.size()));
+        plrec.push_back(static_cast<std::int32_t>(pid * L_ + l));
+        plrec.push_back(parts_[static_cast<std::size_t>(pid)].dev_off[static_cast<std::size_t>(l)]);
+        plrec.push_back(static_cast<std::int32_t>(D.pl.size()));
+        plrec.insert(plrec.end(), D.pl.begin(), D.pl.end());
+      }
+      W.up.reset();
+      const std::size_t o_h = W.up.add(hd.data(), hd.size() * sizeof(SlotHeader));
+      const std::size_t o_r = W.up.add(runs.data(), runs.size() * sizeof(AppendRun));
+      const std::size_t o_i = W.up.add(idx.data(), idx.size() * 4);
+      const std::size_t o_p = W.up.add(plrec.data(), plrec.size() * 4);
+      const std::size_t o_q = W.up.add(ploff.data(), ploff.size() * 4);
+      std::uint8_t* db = W.up.send(st_);
+      launches_ += launch_slot_headers(t_, reinterpret_cast<const SlotHeader*>(db + o_h), static_cast<std::int32_t>(hd.size()), st_);
+      launches_ += launch_append_runs(t_, reinterpret_cast<const AppendRun*>(db + o_r), static_cast<std::int32_t>(runs.size()),
+                                      reinterpret_cast<const std::int32_t*>(db + o_i), W.stage_k.p, W.stage_v.p, st_);
+      launches_ += launch_pl_scatter(t_, reinterpret_cast<const std::int32_t*>(db + o_p), reinterpret_cast<const std::int32_t*>(db + o_q),
+                                     static_cast<std::int32_t>(ploff.size()), st_);
+      t_inst += us(i0, clk::now());
+      // ---- relaunch
+      if (!relaunch.empty()) {
+        const auto r0 = clk::now();
+        std::vector<int> cursor(static_cast<std::size_t>(L_), 0);
+        for (std::size_t i = 0; i < relaunch.size(); ++i) cursor[static_cast<std::size_t>(relaunch[i])] = rcur[i];
+        round_after_event_ = true;
+        launch_round(relaunch, cursor);
+        round_after_event_ = false;
+        sync();
+        check_err_word(*h_err_);
+        for (int l : relaunch) take_stop(l);
+        t_relaunch += us(r0, clk::now());
+      } else {
+        sync();
+      }
+    }
+    // ---- verify the predicted counters
+    const auto v0 = clk::now();
+    std::vector<int> chk;
+    std::vector<std::uint64_t> chk_ctr;
+    {
+      std::uint64_t c = ctr_base;
+      for (int l = 0; l < L_; ++l) {
+        const Waves::Dom& D = W.dom[static_cast<std::size_t>(l)];
+        if (!D.active) continue;
+        for (int ei : D.events)
+          for (int oi : W.evs[static_cast<std::size_t>(ei)].ops) {
+            const Waves::Op& o = W.ops[static_cast<std::size_t>(oi)];
+            if (o.ctr != c && o.ok_ctr != static_cast<std::int64_t>(c)) {
+              chk.push_back(oi);
+              chk_ctr.push_back(c);
+            }
+            ++c;
+          }
+      }
+    }
+    std::vector<int> bad_dom;
+    if (!chk.empty()) {
+      std::vector<std::vector<std::int32_t>> res;
+      run_kmeans(chk, chk_ctr, res);
+      W.st[4] += static_cast<double>(chk.size());
+      for (std::size_t j = 0; j < chk.size(); ++j) {
+        Waves::Op& o = W.ops[static_cast<std::size_t>(chk[j])];
+        if (res[j] == o.assign) {
+          o.ok_ctr = static_cast<std::int64_t>(chk_ctr[j]);
+        } else {
+          const int l = W.evs[static_cast<std::size_t>(o.ev)].layer;
+          if (bad_dom.empty() || bad_dom.back() != l) bad_dom.push_back(l);
+        }
+      }
+    }
+    t_verify += us(v0, clk::now());
+    if (bad_dom.empty()) break;
+    // ---- roll the failing domains back to their first event
+    W.st[3] += static_cast<double>(bad_dom.size());
+    std::vector<std::int32_t> ridx, fslots;
+    for (int l : bad_dom) {
+      Waves::Dom& D = W.dom[static_cast<std::size_t>(l)];
+      for (int i = 0; i < D.snap_n; ++i) ridx.push_back(D.snap0 + i);
+      fslots.insert(fslots.end(), D.taken.begin(), D.taken.end());
+    }
+    W.up.reset();
+    const std::size_t o_f = W.up.add(fslots.data(), fslots.size() * 4);
+    const std::size_t o_x = W.up.add(ridx.data(), ridx.size() * 4);
+    std::uint8_t* db = W.up.send(st_);
+    launches_ += launch_free_slots(t_, reinterpret_cast<const std::int32_t*>(db + o_f), static_cast<std::int32_t>(fslots.size()), st_);
+    launches_ += launch_restore_slots(t_, reinterpret_cast<const std::int32_t*>(db + o_x), static_cast<std::int32_t>(ridx.size()),
+                                      W.snap.p, st_);
+    for (std::int32_t s : fslots) free_slots_.push_back(s);
+    std::vector<std::int32_t> plrec, ploff;
+    for (int l : bad_dom) {
+      Waves::Dom& D = W.dom[static_cast<std::size_t>(l)];
+      D.prev_ops = D.ops;
+      D.ops = 0;
+      D.events.clear();
+      D.taken.clear();
+      D.pl = host_slots(l);
+      D.epoch = W.epoch_next++;
+      D.cur = D.first_tok;
+      D.done = false;
+      D.pend_tok = D.first_tok;
+      D.pend_kind = D.first_kind;
+      D.pend_slot = D.first_slot;
+      D.retry = D.first_retry;
+      D.pend_valid = !D.retry;
+      D.cur_ev = -1;
+      count_outcome(l, 0, D.first_tok);
+      ploff.push_back(static_cast<std::int32_t>(plrec.size()));
+      plrec.push_back(static_cast<std::int32_t>(pid * L_ + l));
+      plrec.push_back(parts_[static_cast<std::size_t>(pid)].dev_off[static_cast<std::size_t>(l)]);
+      plrec.push_back(static_cast<std::int32_t>(D.pl.size()));
+      plrec.insert(plrec.end(), D.pl.begin(), D.pl.end());
+    }
+    W.up.reset();
+    const std::size_t o_p = W.up.add(plrec.data(), plrec.size() * 4);
+    const std::size_t o_q = W.up.add(ploff.data(), ploff.size() * 4);
+    db = W.up.send(st_);
+    launches_ += launch_pl_scatter(t_, reinterpret_cast<const std::int32_t*>(db + o_p), reinterpret_cast<const std::int32_t*>(db + o_q),
+                                   static_cast<std::int32_t>(ploff.size()), st_);
+    sync();
+  }
+  W.st[2] += passes;
+
+  // ---------------------------------------------------------------- commit in reference order
+  const auto c0 = clk::now();
+  std::vector<SlotCid> cids;
+  std::vector<std::int32_t> parents;
+  for (int l = 0; l < L_; ++l) {
+    Waves::Dom& D = W.dom[static_cast<std::size_t>(l)];
+    int t = 0;
+    for (int ei : D.events) {
+      const Waves::Event& e = W.evs[static_cast<std::size_t>(ei)];
+      replay_runs(l, frame_id, T, t, e.tok, assigned);
+      frame_add_flush(frame_id);  // host events add / remove map entries themselves
+      mstats_[0] += 1;            // inserts (maintainer.cpp:89)
+      evt_t_[6] += 1.0;
+      W.st[5] += 1;
+      std::vector<Member> ids;
+      if (e.kind == EV_SPLIT) {
+        const std::int64_t cid = slot_id_[static_cast<std::size_t>(e.parent_slot)];
+        Cluster& c = C(cid);
+        mstats_[2] += 1;  // immediate_splits
+        ids.reserve(static_cast<std::size_t>(e.n));
+        for (const Member& m : c.members) ids.push_back(m);
+        for (const Member& m : c.buffer) ids.push_back(m);
+        ids.push_back({frame_id, e.tok});
+        if (static_cast<int>(ids.size()) != e.n) fail(-11, "wave commit: pool size mismatch");
+        forget(cid);
+        drop_cluster_host(cid);
+        parents.push_back(e.parent_slot);
+        for (int oi : e.ops) {
+          const Waves::Op& o = W.ops[static_cast<std::size_t>(oi)];
+          const std::uint64_t ctr = static_cast<std::uint64_t>(split_counter_++);
+          if (o.ctr != ctr && o.ok_ctr != static_cast<std::int64_t>(ctr)) fail(-11, "wave commit: unverified split counter");
+          mstats_[5] += 1;  // split_ops_total
+          evt_t_[7] += 1.0;
+        }
+      } else {
+        ids.push_back({frame_id, e.tok});
+      }
+      std::int64_t home = -1;
+      for (int li : e.emitted) {
+        const Waves::Leaf& lf = W.leaves[static_cast<std::size_t>(li)];
+        std::vector<Member> m;
+        m.reserve(lf.rows.size());
+        bool has_tok = false;
+        for (int r : lf.rows) {
+          m.push_back(ids[static_cast<std::size_t>(r)]);
+          has_tok |= r == e.n - 1;
+        }
+        const std::int64_t id = new_cluster_at(lf.slot, l, pid, std::move(m), false);
+        adopt(id);
+        ring_owner_patch(l, C(id).members, lf.slot);
+        cids.push_back({id, lf.slot, 0});
+        if (has_tok && home < 0) home = id;  // home_of (maintainer.cpp:62-70)
+      }
+      if (home < 0) home = slot_id_[static_cast<std::size_t>(W.leaves[static_cast<std::size_t>(e.emitted.front())].slot)];
+      if (assigned) assigned[static_cast<std::size_t>(l) * T + e.tok] = home;
+      t = e.tok + 1;
+    }
+    replay_runs(l, frame_id, T, t, T, assigned);
+  }
+  frame_add_flush(frame_id);
+  // device: final ids, released parents, final partition lists, window-ring owners
+  std::vector<std::int32_t> plrec, ploff;
+  for (int l = 0; l < L_; ++l) {
+    const Waves::Dom& D = W.dom[static_cast<std::size_t>(l)];
+    if (!D.active) continue;
+    const auto& ids = parts_[static_cast<std::size_t>(pid)].per_layer[static_cast<std::size_t>(l)];
+    pl_reserve(pid, l, static_cast<std::int32_t>(ids.size()));
+    ploff.push_back(static_cast<std::int32_t>(plrec.size()));
+    plrec.push_back(static_cast<std::int32_t>(pid * L_ + l));
+    plrec.push_back(parts_[static_cast<std::size_t>(pid)].dev_off[static_cast<std::size_t>(l)]);
+    plrec.push_back(static_cast<std::int32_t>(ids.size()));
+    for (std::int64_t id : ids) plrec.push_back(C(id).slot);
+  }
+  W.up.reset();
+  const std::size_t o_c = W.up.add(cids.data(), cids.size() * sizeof(SlotCid));
+  const std::size_t o_f = W.up.add(parents.data(), parents.size() * 4);
+  const std::size_t o_p = W.up.add(plrec.data(), plrec.size() * 4);
+  const std::size_t o_q = W.up.add(ploff.data(), ploff.size() * 4);
+  const std::size_t o_o = W.up.add(ring_owner_h_.data(), ring_owner_h_.size() * 4);
+  std::uint8_t* db = W.up.send(st_);
+  launches_ += launch_set_cids(t_, reinterpret_cast<const SlotCid*>(db + o_c), static_cast<std::int32_t>(cids.size()), st_);
+  launches_ += launch_free_slots(t_, reinterpret_cast<const std::int32_t*>(db + o_f), static_cast<std::int32_t>(parents.size()), st_);
+  launches_ += launch_pl_scatter(t_, reinterpret_cast<const std::int32_t*>(db + o_p), reinterpret_cast<const std::int32_t*>(db + o_q),
+                                 static_cast<std::int32_t>(ploff.size()), st_);
+  KVC_CUDA(cudaMemcpyAsync(t_.ring_owner, db + o_o, ring_owner_h_.size() * 4, cudaMemcpyDeviceToDevice, st_));
+  for (std::int32_t s : parents) free_slots_.push_back(s);
+  sync();  // the upload staging is reused by the next frame
+  (void)ring_slot;
+  const double t_commit = us(c0, clk::now());
+  W.st[6] += t_stage;
+  W.st[8] += t_km;
+  W.st[9] += t_stats + t_inst;
+  W.st[10] += t_relaunch;
+  W.st[11] += t_verify + t_commit;
+  evt_t_[0] += us(t_start, clk::now());
+  evt_t_[1] += t_stage;
+  evt_t_[2] += t_km;
+  evt_t_[3] += t_stats;
+  evt_t_[4] += t_inst + t_commit;
+  evt_t_[5] += t_relaunch;
+  ingest_t_[5] = t_wait;
+  ingest_t_[6] = us(t_start, clk::now()) - t_wait;
+  ingest_t_[9] = W.st[5];
+}
+
+}  // namespace kvc

@@ -355,6 +355,49 @@ int launch_split_two(const float* rows, const int32_t* idx, int n, int d, int fi
                      int32_t* assign, int32_t* meta, double* objective, cudaStream_t st);
 int launch_to_f32(const DevTables& t, const void* src, float* dst, int64_t n_elems,
                   cudaStream_t st);
+// split_two for many independent point sets in one launch (one CTA per job).
+struct SplitJob {
+  const float* rows;
+  const int32_t* idx;
+  double* scratch;  // n * (2d + 3) doubles
+  int32_t* assign;  // [n]
+  int32_t* meta;    // [4]
+  double* objective;
+  double uni;
+  int32_t n, first;
+};
+int launch_split_two_batch(const SplitJob* jobs, int n_jobs, int d, cudaStream_t st);
+
+// ---- ingest wave engine (waves.cu, context_waves.cpp)
+// Staging of a slot's members (then its buffer when with_buf) and/or one frame row at row0.
+struct GatherJob {
+  int32_t slot, with_buf;  // slot -1: no cluster rows
+  int64_t row0;
+  int64_t frame_row;  // row of the frame buffer [L][tmax] appended after the cluster's rows (-1 none)
+  int32_t* count_out;  // rows staged (checked by the host against its own count; may be null)
+};
+int launch_gather_batch(const DevTables& t, const GatherJob* jobs, int32_t n, const void* fk, const void* fv,
+                        void* sk, void* sv, cudaStream_t st);
+int launch_free_slots(const DevTables& t, const int32_t* slots, int32_t n, cudaStream_t st);
+// Snapshot of a slot's ingest-mutable state: header, then rep64[d], brep64[d], rep32[d], brep32[d].
+struct SlotSnap {
+  int32_t slot, npages, nbpages, nbuf;
+  int64_t stat, nmem, cid;
+  int32_t fill_m, fill_b;
+  uint8_t lazy, resid, pad[6];
+  double var, rnorm, bnorm;
+};
+inline __host__ __device__ size_t slot_snap_bytes(int d) { return sizeof(SlotSnap) + static_cast<size_t>(d) * 24; }
+int launch_snap_slots(const DevTables& t, const int32_t* slots, int32_t n, void* arena, cudaStream_t st);
+int launch_restore_slots(const DevTables& t, const int32_t* idx, int32_t n, const void* arena, cudaStream_t st);
+// Partition lists from packed records {pid * L + layer, pool offset, n, slots[n]} at rec_off[i].
+int launch_pl_scatter(const DevTables& t, const int32_t* recs, const int32_t* rec_off, int32_t n, cudaStream_t st);
+struct SlotCid {
+  int64_t cid;
+  int32_t slot, pad;
+};
+int launch_set_cids(const DevTables& t, const SlotCid* x, int32_t n, cudaStream_t st);
+int launch_read_vars(const DevTables& t, const int32_t* slots, int32_t n, double* out, cudaStream_t st);
 
 // launch_util.cu: per-device launch state. smem_optin raises a kernel's dynamic shared-memory
 // attribute on the current device when `bytes` exceeds what was set there (false: the device's

@@ -110,9 +110,9 @@ __device__ __forceinline__ void centroid_norms(SplitSmem& S, int d) {
 // rows: staged f32 rows; idx[n]: the points of this split (rows idx[i]).
 // scratch (doubles): u[n][d] | ut[d][n] | sc[2][n] | nearv[n]
 // out: assign[n]; meta[4] = {k_live, iterations, degenerate, error}; objective[1].
-__global__ void __launch_bounds__(SPT) k_split_two(const float* rows, const int32_t* idx, int n, int d, int first,
-                                                    double uni, double* scratch, int32_t* assign, int32_t* meta,
-                                                    double* objective) {
+__device__ __forceinline__ void split_two_body(const float* rows, const int32_t* idx, int n, int d, int first,
+                                               double uni, double* scratch, int32_t* assign, int32_t* meta,
+                                               double* objective) {
   __shared__ SplitSmem S;
   __shared__ double S_ob[OBJ_CHUNK];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -334,7 +334,26 @@ __global__ void __launch_bounds__(SPT) k_split_two(const float* rows, const int3
   }
 }
 
+__global__ void __launch_bounds__(SPT) k_split_two(const float* rows, const int32_t* idx, int n, int d, int first,
+                                                    double uni, double* scratch, int32_t* assign, int32_t* meta,
+                                                    double* objective) {
+  split_two_body(rows, idx, n, d, first, uni, scratch, assign, meta, objective);
+}
+
+// Independent splits in one launch (one CTA each): the ingest wave engine settles the split
+// events of many domains at once (context_waves.cpp).
+__global__ void __launch_bounds__(SPT) k_split_two_batch(const SplitJob* jobs, int d) {
+  const SplitJob j = jobs[blockIdx.x];
+  split_two_body(j.rows, j.idx, j.n, d, j.first, j.uni, j.scratch, j.assign, j.meta, j.objective);
+}
+
 }  // namespace
+
+int launch_split_two_batch(const SplitJob* jobs, int n_jobs, int d, cudaStream_t st) {
+  if (n_jobs <= 0 || d > 256) return 0;
+  k_split_two_batch<<<n_jobs, SPT, 0, st>>>(jobs, d);
+  return 1;
+}
 
 int launch_split_two(const float* rows, const int32_t* idx, int n, int d, int first, double uni, double* scratch,
                      int32_t* assign, int32_t* meta, double* objective, cudaStream_t st) {

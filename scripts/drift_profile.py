@@ -36,6 +36,7 @@ if PRE:
 fk, fv, fvis, fids = workload.frames_drift(st, F, N // T + 1 + 100000, seed=7)
 rows = []
 kv.event_profile(reset=True)
+kv.wave_profile(reset=True)
 TIMED = os.environ.get("DRIFT_TIMING") == "1"
 kv.set_timing(TIMED)
 kts = []
@@ -66,7 +67,8 @@ for i in range(3):
                         "host_replay", "host_relaunch_issue", "host_events"], np.round(kv.ingest_timing(), 1).tolist())))
 kv.set_timing(False)
 prof = kv.event_profile()
+wprof = kv.wave_profile()
 tot = wall
-print(json.dumps({"domains": D, "frames": F, "ms_per_frame": round(tot / F, 2), "rows": rows, "event_profile": prof,
+print(json.dumps({"domains": D, "frames": F, "ms_per_frame": round(tot / F, 2), "rows": rows, "event_profile": prof, "wave_profile": wprof,
                   "per_event_us": {k: round(v / max(prof["events"], 1), 1) for k, v in prof.items() if k.endswith("_us")},
                   "timed_frames": kt, "all_frames_timing": kts}))
