@@ -115,8 +115,12 @@ struct Upload {
     used = off + bytes;
     return off;
   }
-  // copies the parts (in add order) into the pinned buffer and sends them; returns device base
+  cudaEvent_t copied = nullptr;  // the last H2D out of the pinned buffer
+  // copies the parts (in add order) into the pinned buffer and sends them; returns device base.
+  // The device copy is only read by kernels queued before the next send (stream order); the
+  // pinned side must wait until the previous copy has left it.
   std::uint8_t* send(cudaStream_t st) {
+    if (copied) KVC_CUDA(cudaEventSynchronize(copied));
     h.ensure(used, st);
     d.ensure(used, st);
     std::size_t off = 0;
@@ -126,6 +130,8 @@ struct Upload {
       off += pr.second;
     }
     if (used) KVC_CUDA(cudaMemcpyAsync(d.p, h.p, used, cudaMemcpyHostToDevice, st));
+    if (!copied) KVC_CUDA(cudaEventCreateWithFlags(&copied, cudaEventDisableTiming));
+    KVC_CUDA(cudaEventRecord(copied, st));
     return static_cast<std::uint8_t*>(d.p);
   }
 };
@@ -212,6 +218,7 @@ void Context::waves_free() {
   wv_->h_out.release();
   wv_->up.h.release();
   wv_->up.d.release();
+  if (wv_->up.copied) cudaEventDestroy(wv_->up.copied);
   delete wv_;
   wv_ = nullptr;
 }
