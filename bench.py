@@ -487,6 +487,7 @@ def ingest_regime(kv, stream, args, world, local, frames_t, gen, first, name):
     for i in range(args.warmup):
         kv.process_frame(int(fids[i]), fvis[i], fk[i], fv[i], want_assigned=False)
     s0 = kv.maint_stats()
+    kv.wave_profile(reset=True)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     launches0 = kv.launch_count()
     torch.cuda.synchronize()
@@ -503,6 +504,7 @@ def ingest_regime(kv, stream, args, world, local, frames_t, gen, first, name):
     ms = ev0.elapsed_time(ev1)
     launches = kv.launch_count() - launches0
     maint = (kv.maint_stats() - s0).tolist()
+    waves = kv.wave_profile(reset=True)
     n_clusters = len(kv.cluster_ids())
     # instrumented pass (outside the timed region): kernel phases and touched clusters |U|
     kv.set_timing(True)
@@ -534,7 +536,7 @@ def ingest_regime(kv, stream, args, world, local, frames_t, gen, first, name):
     frames_f32 = (fvis[args.warmup:], fk[args.warmup:, :nd].float().cpu().numpy(),
                   fv[args.warmup:, :nd].float().cpu().numpy())
     return {"_ms": ms, "_e2e_ms": e2e_ms, "_launches": launches, "_clocks": clk, "_frames_f32": frames_f32,
-            "phases_us": phases, "maint_delta": dict(zip(MAINT_KEYS, maint)),
+            "phases_us": phases, "maint_delta": dict(zip(MAINT_KEYS, maint)), "wave_engine": waves,
             "resolve_cycles_per_frame": dict(zip(RESOLVE_PHASES[RESOLVE_KERNEL], prof.round(1).tolist())),
             "touched_clusters_per_domain_frame": round(float(np.mean(touched)), 2),
             "clusters_per_domain": round(n_clusters / kv.L, 1)}

@@ -378,11 +378,12 @@ KVC_API int kvc_debug_resolve_profile(kvc_ctx* ctx, double* out);
  * speculative split k-means launched / consumed (the next domain's split 2-means'd on a side
  * stream during a relaunch). */
 KVC_API int kvc_debug_event_profile(kvc_ctx* ctx, double* out10, int32_t reset);
-/* Wave engine profile (parallel settle of a frame's host events across domains; cumulative), out12:
+/* Wave engine profile (parallel settle of a frame's host events across domains; cumulative), out13:
  * frames with events, waves, verification passes, rolled-back domains, verification k-means jobs,
  * host events, then microseconds in pool staging, k-means jobs (count), k-means, children
- * statistics + install, relaunch rounds, verification + commit. */
-KVC_API int kvc_debug_wave_profile(kvc_ctx* ctx, double* out12, int32_t reset);
+ * statistics + install, relaunch rounds, verification + commit; splits verified as the same
+ * partition with exchanged labels. */
+KVC_API int kvc_debug_wave_profile(kvc_ctx* ctx, double* out13, int32_t reset);
 /* Enables per-phase CUDA-event timing (off by default: it adds event records). */
 KVC_API void kvc_set_timing(kvc_ctx* ctx, int32_t on);
 

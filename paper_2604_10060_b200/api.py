@@ -524,11 +524,12 @@ class ClusterKVCache:
         return dict(zip(self.EVENT_KEYS, t.round(1).tolist()))
 
     WAVE_KEYS = ("frames_with_events", "waves", "passes", "rolled_back_domains", "verify_kmeans", "events",
-                 "stage_us", "kmeans_jobs", "kmeans_us", "install_us", "relaunch_us", "verify_commit_us")
+                 "stage_us", "kmeans_jobs", "kmeans_us", "install_us", "relaunch_us", "verify_commit_us",
+                 "verified_swapped")
 
     def wave_profile(self, reset: bool = False) -> dict:
         """Wave-engine profile (kvc_debug_wave_profile), cumulative."""
-        t = np.zeros(12)
+        t = np.zeros(13)
         _check(lib().kvc_debug_wave_profile(self.h, _p(t, f64p), 1 if reset else 0))
         return dict(zip(self.WAVE_KEYS, t.round(1).tolist()))
 

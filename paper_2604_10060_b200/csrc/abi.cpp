@@ -701,9 +701,9 @@ int kvc_debug_event_profile(kvc_ctx* ctx, double* out10, int32_t reset) {
   return guard([&] { F(ctx).event_profile(out10, reset != 0); });
 }
 
-int kvc_debug_wave_profile(kvc_ctx* ctx, double* out12, int32_t reset) {
+int kvc_debug_wave_profile(kvc_ctx* ctx, double* out13, int32_t reset) {
   KVC_CLUSTER_ONLY(ctx);
-  return guard([&] { ctx->impl->wave_profile(out12, reset != 0); });
+  return guard([&] { ctx->impl->wave_profile(out13, reset != 0); });
 }
 
 int kvc_debug_resolve_profile(kvc_ctx* ctx, double* out) {

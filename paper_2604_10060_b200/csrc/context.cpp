@@ -270,7 +270,8 @@ void Context::alloc_device() {
   ia_.cand_buf = static_cast<std::uint8_t*>(dalloc(L * t_.cmax));
   ia_.approx = static_cast<float*>(dalloc(L * t_.tmax * t_.cmax * 4));
   // outcome words in one block (ev_kind | ev_slot | stop_t | stop_kind | stop_slot): one D2H per launch
-  ia_.ev_kind = static_cast<std::int32_t*>(dalloc(L * t_.tmax * 4 * 2 + L * 4 * 3 + 16));
+  // ... | error word | tie flags [L] (k_resolve)
+  ia_.ev_kind = static_cast<std::int32_t*>(dalloc(L * t_.tmax * 4 * 2 + L * 4 * 4 + 16));
   ia_.ev_slot = ia_.ev_kind + L * t_.tmax;
   ia_.stop_t = ia_.ev_slot + L * t_.tmax;
   ia_.stop_kind = ia_.stop_t + L;
@@ -296,6 +297,8 @@ void Context::alloc_device() {
     waves_ = !(wv && std::string(wv) == "0");
     const char* wp = std::getenv("KVC_WAVES_PERTURB");
     waves_perturb_ = wp && std::string(wp) == "1";
+    const char* wl = std::getenv("KVC_WAVES_LOG");
+    waves_log_ = wl && std::string(wl) == "1";
     const char* ss = std::getenv("KVC_SPEC_SPLIT");  // 0: no speculative split k-means
     spec_split_ = !(ss && std::string(ss) == "0");
     const char* g = std::getenv("KVC_ASSIGN");  // "simt": the fp32 CUDA-core tile
@@ -314,7 +317,7 @@ void Context::alloc_device() {
   h_cursor_ = h_active_ + L;
   d_evflags_ = static_cast<std::int32_t*>(dalloc(16));  // per frame buffer: first round stopped
   for (int b = 0; b < 2; ++b) {
-    h_out_[b] = static_cast<std::int32_t*>(halloc(L * t_.tmax * 4 * 2 + L * 4 * 3 + 16));
+    h_out_[b] = static_cast<std::int32_t*>(halloc(L * t_.tmax * 4 * 2 + L * 4 * 4 + 16));
     h_errb_[b] = static_cast<std::int32_t*>(halloc(16));
     KVC_CUDA(cudaEventCreateWithFlags(&ev_ing_[b], cudaEventDisableTiming));
     if (b == 0) KVC_CUDA(cudaEventCreateWithFlags(&ev_init_, cudaEventDisableTiming));
@@ -328,6 +331,7 @@ void Context::alloc_device() {
   ia_.active = d_active_;
   ia_.cursor = d_cursor_;
   ia_.err_copy = ia_.ev_kind + 2 * static_cast<std::int64_t>(L) * t_.tmax + 3 * L;
+  ia_.tie = ia_.err_copy + 1;
   // every domain from token 0 (a frame's first round): constant device arrays, no staging copy
   d_all_active_ = static_cast<std::int32_t*>(dalloc(L * 4 * 2));
   {
@@ -1220,7 +1224,7 @@ void Context::launch_round(const std::vector<int>& active, const std::vector<int
   KVC_CUDA(cudaGetLastError());
   if (timing_) KVC_CUDA(cudaEventRecord(ev_[5], st_));
   // outcome block + the error word K3 copied after it, in one copy
-  KVC_CUDA(cudaMemcpyAsync(h_evk_, ia_.ev_kind, (static_cast<std::size_t>(L_) * t_.tmax * 2 + static_cast<std::size_t>(L_) * 3 + 1) * 4,
+  KVC_CUDA(cudaMemcpyAsync(h_evk_, ia_.ev_kind, (static_cast<std::size_t>(L_) * t_.tmax * 2 + static_cast<std::size_t>(L_) * 4 + 1) * 4,
                            cudaMemcpyDeviceToHost, st_));
 }
 

@@ -542,14 +542,16 @@ class Context {
   struct Waves;
   Waves* wv_ = nullptr;
   bool waves_ = true;
-  bool waves_perturb_ = false;  // KVC_WAVES_PERTURB=1: first-pass counter predictions made wrong (tests)
+  bool waves_perturb_ = false;
+  bool waves_log_ = false;  // KVC_WAVES_LOG=1: per-frame pass / rollback lines on stderr  // KVC_WAVES_PERTURB=1: first-pass counter predictions made wrong (tests)
   void run_inserts_waves(std::int64_t frame_id, std::int64_t pid, int T, std::int64_t* assigned, bool launched);
   void replay_runs(int l, std::int64_t frame_id, int T, int t0, int t1, std::int64_t* assigned);
   void waves_free();
  public:
   // frames with events, waves, passes, rolled-back domains, verification k-means, events, stage us,
-  // k-means jobs, k-means us, stats + install us, relaunch us, verify + commit us (cumulative)
-  void wave_profile(double* out12, bool reset);
+  // k-means jobs, k-means us, stats + install us, relaunch us, verify + commit us, splits verified
+  // with exchanged labels (cumulative)
+  void wave_profile(double* out13, bool reset);
 
  private:
   // split slow path

@@ -31,6 +31,7 @@
 // device-side restore plus a reset of the domain's wave record.
 #include <algorithm>
 #include <chrono>
+#include <cstdio>
 #include <cmath>
 #include <cstring>
 #include <numeric>
@@ -149,6 +150,7 @@ struct Context::Waves {
     std::vector<int> rows;  // pool rows (relative to the event's staged pool)
     std::uint64_t ctr = 0;  // the counter its k-means used
     std::int64_t ok_ctr = -1;  // a counter its result was verified for
+    bool ok_swap = false;      // ... as the same partition with the two labels exchanged
     std::vector<std::int32_t> assign;
     int kids[2] = {kNoKid, kNoKid};  // op index, leaf_code(leaf), or kNoKid (empty group)
   };
@@ -185,6 +187,7 @@ struct Context::Waves {
     std::vector<std::int32_t> taken;  // leaf slots created by this pass
     int ops = 0, prev_ops = -1;
     std::uint64_t epoch = 0;
+    bool tie = false;  // a relaunch decision of this pass was an exact tie broken by the id key
   };
   std::vector<Op> ops;
   std::vector<Leaf> leaves;
@@ -204,7 +207,7 @@ struct Context::Waves {
   Upload up;
   std::int64_t prov_next = 0;
   // stats (cumulative; kvc_debug_wave_profile)
-  double st[12] = {0};
+  double st[16] = {0};
 };
 
 void Context::waves_free() {
@@ -224,7 +227,7 @@ void Context::waves_free() {
 }
 
 void Context::wave_profile(double* out, bool reset) {
-  for (int i = 0; i < 12; ++i) out[i] = wv_ ? wv_->st[i] : 0.0;
+  for (int i = 0; i < 13; ++i) out[i] = wv_ ? wv_->st[i] : 0.0;
   if (reset && wv_)
     for (double& x : wv_->st) x = 0.0;
 }
@@ -441,7 +444,7 @@ void Context::run_inserts_waves(std::int64_t frame_id, std::int64_t pid, int T, 
   const std::int64_t frame_rows = static_cast<std::int64_t>(L_) * t_.tmax;
   double t_stage = 0, t_km = 0, t_stats = 0, t_inst = 0, t_relaunch = 0, t_verify = 0;
 
-  int passes = 0;
+  int passes = 1;  // 1 + waves whose validation rolled domains back
   // predicted counter of the next op of domain l
   auto predict = [&](int l) -> std::uint64_t {
     std::uint64_t c = ctr_base;
@@ -458,7 +461,7 @@ void Context::run_inserts_waves(std::int64_t frame_id, std::int64_t pid, int T, 
     }
     // test hook (KVC_WAVES_PERTURB=1): every first-pass prediction is wrong, so every split is
     // re-verified and (almost) every domain with events is rolled back and settled again
-    if (waves_perturb_ && passes == 1) c += 7;
+    if (waves_perturb_ && W.dom[static_cast<std::size_t>(l)].prev_ops < 0) c += 7;
     return c + static_cast<std::uint64_t>(W.dom[static_cast<std::size_t>(l)].ops);
   };
 
@@ -525,346 +528,63 @@ void Context::run_inserts_waves(std::int64_t frame_id, std::int64_t pid, int T, 
     return us(k0, clk::now());
   };
 
-  // ---------------------------------------------------------------- the wave / pass loop
-  for (;;) {
-    passes += 1;
-    // waves until no domain has a pending event
-    for (;;) {
-      std::vector<int> E;  // domains with a pending event (not retries)
-      std::vector<int> relaunch, rcur;
-      for (int l = 0; l < L_; ++l) {
-        Waves::Dom& D = W.dom[static_cast<std::size_t>(l)];
-        if (!D.active || D.done) continue;
-        if (D.retry) {
-          relaunch.push_back(l);
-          rcur.push_back(D.pend_tok);
-          D.cur = D.pend_tok;
-          D.retry = false;
-          continue;
-        }
-        E.push_back(l);
-      }
-      if (E.empty() && relaunch.empty()) break;
-      W.st[1] += 1;  // waves
-      const auto s0 = clk::now();
-      // ---- events: stage pools
-      std::vector<GatherJob> gj;
-      std::vector<int> new_evs;
-      std::int64_t rows_need = W.rows_used;
-      for (int l : E) {
-        Waves::Dom& D = W.dom[static_cast<std::size_t>(l)];
-        Waves::Event e;
-        e.layer = l;
-        e.tok = D.pend_tok;
-        e.kind = D.pend_kind;
-        e.parent_slot = D.pend_kind == EV_SPLIT ? D.pend_slot : -1;
-        e.n = e.kind == EV_SPLIT ? static_cast<int>(size_of(e.parent_slot, D)) + 1 : 1;
-        e.row0 = rows_need;
-        rows_need += e.n;
-        new_evs.push_back(static_cast<int>(W.evs.size()));
-        D.cur_ev = static_cast<int>(W.evs.size());
-        D.pend_valid = false;
-        D.events.push_back(static_cast<int>(W.evs.size()));
-        W.evs.push_back(std::move(e));
-      }
-      const std::int64_t keep_rows = W.rows_used;
-      W.stage_k.ensure(static_cast<std::size_t>(rows_need) * rb, st_, static_cast<std::size_t>(keep_rows) * rb);
-      W.stage_v.ensure(static_cast<std::size_t>(rows_need) * rb, st_, static_cast<std::size_t>(keep_rows) * rb);
-      W.stage_f32.ensure(static_cast<std::size_t>(rows_need) * d_ * 4, st_, static_cast<std::size_t>(keep_rows) * d_ * 4);
-      W.rows_used = rows_need;
-      W.km_out.ensure(new_evs.size() * 4 + 64, st_);
-      for (std::size_t i = 0; i < new_evs.size(); ++i) {
-        const Waves::Event& e = W.evs[static_cast<std::size_t>(new_evs[i])];
-        GatherJob g{};
-        g.slot = e.parent_slot;
-        g.with_buf = 1;
-        g.row0 = e.row0;
-        g.frame_row = static_cast<std::int64_t>(e.layer) * t_.tmax + e.tok;
-        g.count_out = W.km_out.as<std::int32_t>() + i;
-        gj.push_back(g);
-      }
-      if (!gj.empty()) {
-        W.up.reset();
-        const std::size_t o = W.up.add(gj.data(), gj.size() * sizeof(GatherJob));
-        std::uint8_t* db = W.up.send(st_);
-        launches_ += launch_gather_batch(t_, reinterpret_cast<const GatherJob*>(db + o), static_cast<std::int32_t>(gj.size()),
-                                         d_fk_, d_fv_, W.stage_k.p, W.stage_v.p, st_);
-        launches_ += launch_to_f32(t_, W.stage_k.as<std::uint8_t>(static_cast<std::size_t>(keep_rows) * rb),
-                                   W.stage_f32.as<float>(static_cast<std::size_t>(keep_rows) * d_ * 4),
-                                   (rows_need - keep_rows) * d_, st_);
-        W.h_out.ensure(gj.size() * 4, st_);
-        KVC_CUDA(cudaMemcpyAsync(W.h_out.p, W.km_out.p, gj.size() * 4, cudaMemcpyDeviceToHost, st_));
-        sync();
-        for (std::size_t i = 0; i < new_evs.size(); ++i)
-          if (W.h_out.as<std::int32_t>()[i] != W.evs[static_cast<std::size_t>(new_evs[i])].n)
-            fail(-11, "wave engine: staged pool size differs from the host's count");
-      }
-      t_stage += us(s0, clk::now());
-      // ---- root ops / seed leaves
-      for (int ei : new_evs) {
-        Waves::Event& e = W.evs[static_cast<std::size_t>(ei)];
-        if (e.kind == EV_SEED) {
-          Waves::Leaf lf;
-          lf.rows = {0};
-          W.leaves.push_back(std::move(lf));
-          e.root = leaf_code(static_cast<int>(W.leaves.size()) - 1);
-        } else {
-          Waves::Op o;
-          o.ev = ei;
-          o.depth = 0;
-          o.rows.resize(static_cast<std::size_t>(e.n));
-          std::iota(o.rows.begin(), o.rows.end(), 0);
-          W.ops.push_back(std::move(o));
-          e.root = static_cast<int>(W.ops.size()) - 1;
-          e.stack.push_back(e.root);
-        }
-      }
-      // ---- sub-waves: one op per event at a time, in DFS preorder (its counter order)
-      std::vector<std::pair<int, int>> pending_stats;  // (leaf, event) needing stats + var
-      for (int ei : new_evs) {
-        const Waves::Event& e = W.evs[static_cast<std::size_t>(ei)];
-        if (is_leaf_code(e.root)) pending_stats.emplace_back(leaf_of(e.root), ei);
-      }
-      bool first_sub = true;
-      for (;;) {
-        std::vector<int> opl;
-        std::vector<std::uint64_t> ctrs;
-        for (int ei : new_evs) {
-          Waves::Event& e = W.evs[static_cast<std::size_t>(ei)];
-          if (e.stack.empty()) continue;
-          const int oi = e.stack.back();
-          e.stack.pop_back();
-          Waves::Dom& D = W.dom[static_cast<std::size_t>(e.layer)];
-          Waves::Op& o = W.ops[static_cast<std::size_t>(oi)];
-          o.ctr = predict(e.layer);
-          D.ops += 1;
-          e.ops.push_back(oi);
-          opl.push_back(oi);
-          ctrs.push_back(o.ctr);
-        }
-        if (opl.empty() && !(first_sub && !pending_stats.empty())) break;
-        first_sub = false;
-        // k-means
-        std::vector<std::vector<std::int32_t>> res;
-        if (!opl.empty()) t_km += run_kmeans(opl, ctrs, res);
-        const auto st0 = clk::now();
-        // groups -> exact statistics in fresh slots
-        struct G {
-          int op, g;
-          std::vector<int> rows;
-          std::int32_t slot;
-        };
-        std::vector<G> groups;
-        for (std::size_t j = 0; j < opl.size(); ++j) {
-          Waves::Op& o = W.ops[static_cast<std::size_t>(opl[j])];
-          o.assign = std::move(res[j]);
-          std::vector<int> g2[2];
-          for (std::size_t i = 0; i < o.rows.size(); ++i) g2[o.assign[i]].push_back(o.rows[i]);
-          for (int g = 0; g < 2; ++g)
-            if (!g2[g].empty()) groups.push_back({opl[j], g, std::move(g2[g]), take_slot()});
-        }
-        std::vector<AppendRun> runs;
-        std::vector<std::int32_t> idx, slots;
-        for (const G& g : groups) {
-          const Waves::Event& e = W.evs[static_cast<std::size_t>(W.ops[static_cast<std::size_t>(g.op)].ev)];
-          runs.push_back({g.slot, static_cast<std::int32_t>(idx.size()), static_cast<std::int32_t>(g.rows.size()), 0});
-          for (int r : g.rows) idx.push_back(static_cast<std::int32_t>(e.row0 + r));
-          slots.push_back(g.slot);
-        }
-        for (auto& ps : pending_stats) {  // seeds
-          Waves::Leaf& lf = W.leaves[static_cast<std::size_t>(ps.first)];
-          const Waves::Event& e = W.evs[static_cast<std::size_t>(ps.second)];
-          lf.slot = take_slot();
-          runs.push_back({lf.slot, static_cast<std::int32_t>(idx.size()), 1, 0});
-          idx.push_back(static_cast<std::int32_t>(e.row0));
-          slots.push_back(lf.slot);
-          W.dom[static_cast<std::size_t>(e.layer)].taken.push_back(lf.slot);
-        }
-        pending_stats.clear();
-        std::vector<double> vars(runs.size());
-        if (!runs.empty()) {
-          W.up.reset();
-          const std::size_t o_r = W.up.add(runs.data(), runs.size() * sizeof(AppendRun));
-          const std::size_t o_i = W.up.add(idx.data(), idx.size() * 4);
-          const std::size_t o_s = W.up.add(slots.data(), slots.size() * 4);
-          std::uint8_t* db = W.up.send(st_);
-          launches_ += launch_exact_stats(t_, reinterpret_cast<const AppendRun*>(db + o_r), static_cast<std::int32_t>(runs.size()),
-                                          reinterpret_cast<const std::int32_t*>(db + o_i), W.stage_k.p, st_);
-          W.km_out.ensure(runs.size() * 8 + 64, st_);
-          launches_ += launch_read_vars(t_, reinterpret_cast<const std::int32_t*>(db + o_s), static_cast<std::int32_t>(slots.size()),
-                                        W.km_out.as<double>(), st_);
-          W.h_out.ensure(runs.size() * 8, st_);
-          KVC_CUDA(cudaMemcpyAsync(W.h_out.p, W.km_out.p, runs.size() * 8, cudaMemcpyDeviceToHost, st_));
-          sync();
-          std::memcpy(vars.data(), W.h_out.p, runs.size() * 8);
-        }
-        // recursion decisions (maintainer.cpp:228-238), in group order per op
-        for (std::size_t gi = 0; gi < groups.size(); ++gi) {
-          G& g = groups[gi];
-          const int o_ev = W.ops[static_cast<std::size_t>(g.op)].ev, o_depth = W.ops[static_cast<std::size_t>(g.op)].depth;
-          const Waves::Event& e = W.evs[static_cast<std::size_t>(o_ev)];
-          const std::int64_t sz = static_cast<std::int64_t>(g.rows.size());
-          if (o_depth + 1 < cfg_.max_split_depth && sz >= 2 && vars[gi] > tau_at(sz, cfg_)) {
-            free_slots_.push_back(g.slot);  // no pages were attached
-            Waves::Op c;
-            c.ev = o_ev;
-            c.depth = o_depth + 1;
-            c.rows = std::move(g.rows);
-            W.ops.push_back(std::move(c));
-            W.ops[static_cast<std::size_t>(g.op)].kids[g.g] = static_cast<int>(W.ops.size()) - 1;
-          } else {
-            Waves::Leaf lf;
-            lf.rows = std::move(g.rows);
-            lf.slot = g.slot;
-            W.leaves.push_back(std::move(lf));
-            W.ops[static_cast<std::size_t>(g.op)].kids[g.g] = leaf_code(static_cast<int>(W.leaves.size()) - 1);
-            W.dom[static_cast<std::size_t>(e.layer)].taken.push_back(g.slot);
-          }
-        }
-        // children to run: push kid 1 first so kid 0 (its subtree) runs first (preorder)
-        for (int oi : opl) {
-          const Waves::Op& o = W.ops[static_cast<std::size_t>(oi)];
-          Waves::Event& e = W.evs[static_cast<std::size_t>(o.ev)];
-          for (int g = 1; g >= 0; --g)
-            if (o.kids[g] >= 0) e.stack.push_back(o.kids[g]);
-        }
-        t_stats += us(st0, clk::now());
-      }
-      // ---- install children: headers, pages, partition lists; relaunch the domains
-      const auto i0 = clk::now();
-      std::vector<SlotHeader> hd;
-      std::vector<AppendRun> runs;
-      std::vector<std::int32_t> idx;
-      for (int ei : new_evs) {
-        Waves::Event& e = W.evs[static_cast<std::size_t>(ei)];
-        Waves::Dom& D = W.dom[static_cast<std::size_t>(e.layer)];
-        // emission order: in-order over the split tree (maintainer.cpp:224-238)
-        if (is_leaf_code(e.root)) {
-          e.emitted.push_back(leaf_of(e.root));
-        } else {
-          auto walk = [&](auto&& self, int oi) -> void {
-            const Waves::Op& o = W.ops[static_cast<std::size_t>(oi)];
-            for (int g = 0; g < 2; ++g) {
-              if (o.kids[g] == kNoKid) continue;
-              if (is_leaf_code(o.kids[g]))
-                e.emitted.push_back(leaf_of(o.kids[g]));
-              else
-                self(self, o.kids[g]);
-            }
-          };
-          walk(walk, e.root);
-        }
-        if (e.kind == EV_SPLIT) D.pl.erase(std::remove(D.pl.begin(), D.pl.end(), e.parent_slot), D.pl.end());
-        for (int li : e.emitted) {
-          const Waves::Leaf& lf = W.leaves[static_cast<std::size_t>(li)];
-          const std::int64_t n = static_cast<std::int64_t>(lf.rows.size());
-          hd.push_back({lf.slot, 0, W.prov_next++, n});
-          runs.push_back({lf.slot, static_cast<std::int32_t>(idx.size()), static_cast<std::int32_t>(n), 0});
-          for (int r : lf.rows) idx.push_back(static_cast<std::int32_t>(e.row0 + r));
-          D.pl.push_back(lf.slot);
-          W.sz_stamp[static_cast<std::size_t>(lf.slot)] = D.epoch;
-          W.sz[static_cast<std::size_t>(lf.slot)] = n;
-        }
-        D.cur = e.tok + 1;
-        D.cur_ev = -1;
-        if (D.cur >= T) {
-          D.done = true;
-        } else {
-          relaunch.push_back(e.layer);
-          rcur.push_back(D.cur);
-        }
-      }
-      // partition lists of every domain in speculation (capacity first: a compaction rewrites
-      // the device lists from the host ones)
-      std::vector<std::int32_t> plrec, ploff;
-      pl_floor_.assign(parts_.size() * static_cast<std::size_t>(L_), 0);
-      for (int l = 0; l < L_; ++l)
-        if (W.dom[static_cast<std::size_t>(l)].active)
-          pl_floor_[static_cast<std::size_t>(pid) * L_ + l] = static_cast<std::int32_t>(W.dom[static_cast<std::size_t>(l)].pl.size());
-      for (int ei : new_evs) {
-        const int l = W.evs[static_cast<std::size_t>(ei)].layer;
-        pl_reserve(pid, l, static_cast<std::int32_t>(W.dom[static_cast<std::size_t>(l)].pl.size()));
-      }
-      pl_floor_.clear();
-      for (int l = 0; l < L_; ++l) {
-        const Waves::Dom& D = W.dom[static_cast<std::size_t>(l)];
-        if (!D.active) continue;
-        ploff.push_back(static_cast<std::int32_t>(plrec.size()));
-        plrec.push_back(static_cast<std::int32_t>(pid * L_ + l));
-        plrec.push_back(parts_[static_cast<std::size_t>(pid)].dev_off[static_cast<std::size_t>(l)]);
-        plrec.push_back(static_cast<std::int32_t>(D.pl.size()));
-        plrec.insert(plrec.end(), D.pl.begin(), D.pl.end());
-      }
-      W.up.reset();
-      const std::size_t o_h = W.up.add(hd.data(), hd.size() * sizeof(SlotHeader));
-      const std::size_t o_r = W.up.add(runs.data(), runs.size() * sizeof(AppendRun));
-      const std::size_t o_i = W.up.add(idx.data(), idx.size() * 4);
-      const std::size_t o_p = W.up.add(plrec.data(), plrec.size() * 4);
-      const std::size_t o_q = W.up.add(ploff.data(), ploff.size() * 4);
-      std::uint8_t* db = W.up.send(st_);
-      launches_ += launch_slot_headers(t_, reinterpret_cast<const SlotHeader*>(db + o_h), static_cast<std::int32_t>(hd.size()), st_);
-      launches_ += launch_append_runs(t_, reinterpret_cast<const AppendRun*>(db + o_r), static_cast<std::int32_t>(runs.size()),
-                                      reinterpret_cast<const std::int32_t*>(db + o_i), W.stage_k.p, W.stage_v.p, st_);
-      launches_ += launch_pl_scatter(t_, reinterpret_cast<const std::int32_t*>(db + o_p), reinterpret_cast<const std::int32_t*>(db + o_q),
-                                     static_cast<std::int32_t>(ploff.size()), st_);
-      t_inst += us(i0, clk::now());
-      // ---- relaunch
-      if (!relaunch.empty()) {
-        const auto r0 = clk::now();
-        std::vector<int> cursor(static_cast<std::size_t>(L_), 0);
-        for (std::size_t i = 0; i < relaunch.size(); ++i) cursor[static_cast<std::size_t>(relaunch[i])] = rcur[i];
-        round_after_event_ = true;
-        launch_round(relaunch, cursor);
-        round_after_event_ = false;
-        sync();
-        check_err_word(*h_err_);
-        for (int l : relaunch) take_stop(l);
-        t_relaunch += us(r0, clk::now());
-      } else {
-        sync();
-      }
+  // ---------------------------------------------------------------- the wave loop
+  // Each iteration: (1) a validation sweep over the prefix of finished domains, where the split
+  // counters are exact: every split whose k-means ran with another counter is recomputed with the
+  // exact one (in the same launch as this wave's new splits); a domain whose result changes is
+  // rolled back to its first event and restarted in this same wave, its first split taking the
+  // exact result just computed. (2) The pending events of all unfinished domains are settled
+  // (staging, k-means, children statistics, recursion as sub-waves, install) and (3) their domains
+  // relaunched from the next token in one round.
+  std::vector<std::uint64_t> first_ctr(static_cast<std::size_t>(L_), 0);
+  // restart of a rolled-back domain: its first event again, with the staged pool of the previous
+  // attempt (the snapshot restores exactly the state it was staged from) and, for a split, the
+  // k-means result for the exact counter
+  struct Prefab {
+    bool on = false;
+    std::int64_t row0 = 0;
+    int n = 0;
+    std::uint64_t ctr = 0;
+    std::vector<std::int32_t> assign;
+  };
+  std::vector<Prefab> prefab(static_cast<std::size_t>(L_));
+  auto new_event = [&](int l) -> int {
+    Waves::Dom& D = W.dom[static_cast<std::size_t>(l)];
+    Waves::Event e;
+    e.layer = l;
+    e.tok = D.pend_tok;
+    e.kind = D.pend_kind;
+    e.parent_slot = D.pend_kind == EV_SPLIT ? D.pend_slot : -1;
+    e.n = e.kind == EV_SPLIT ? static_cast<int>(size_of(e.parent_slot, D)) + 1 : 1;
+    e.row0 = -1;
+    const int ei = static_cast<int>(W.evs.size());
+    D.cur_ev = ei;
+    D.pend_valid = false;
+    D.events.push_back(ei);
+    W.evs.push_back(std::move(e));
+    return ei;
+  };
+  auto root_op = [&](int ei) {
+    Waves::Event& e = W.evs[static_cast<std::size_t>(ei)];
+    if (e.kind == EV_SEED) {
+      Waves::Leaf lf;
+      lf.rows = {0};
+      W.leaves.push_back(std::move(lf));
+      e.root = leaf_code(static_cast<int>(W.leaves.size()) - 1);
+      return;
     }
-    // ---- verify the predicted counters
-    const auto v0 = clk::now();
-    std::vector<int> chk;
-    std::vector<std::uint64_t> chk_ctr;
-    {
-      std::uint64_t c = ctr_base;
-      for (int l = 0; l < L_; ++l) {
-        const Waves::Dom& D = W.dom[static_cast<std::size_t>(l)];
-        if (!D.active) continue;
-        for (int ei : D.events)
-          for (int oi : W.evs[static_cast<std::size_t>(ei)].ops) {
-            const Waves::Op& o = W.ops[static_cast<std::size_t>(oi)];
-            if (o.ctr != c && o.ok_ctr != static_cast<std::int64_t>(c)) {
-              chk.push_back(oi);
-              chk_ctr.push_back(c);
-            }
-            ++c;
-          }
-      }
-    }
-    std::vector<int> bad_dom;
-    if (!chk.empty()) {
-      std::vector<std::vector<std::int32_t>> res;
-      run_kmeans(chk, chk_ctr, res);
-      W.st[4] += static_cast<double>(chk.size());
-      for (std::size_t j = 0; j < chk.size(); ++j) {
-        Waves::Op& o = W.ops[static_cast<std::size_t>(chk[j])];
-        if (res[j] == o.assign) {
-          o.ok_ctr = static_cast<std::int64_t>(chk_ctr[j]);
-        } else {
-          const int l = W.evs[static_cast<std::size_t>(o.ev)].layer;
-          if (bad_dom.empty() || bad_dom.back() != l) bad_dom.push_back(l);
-        }
-      }
-    }
-    t_verify += us(v0, clk::now());
-    if (bad_dom.empty()) break;
-    // ---- roll the failing domains back to their first event
-    W.st[3] += static_cast<double>(bad_dom.size());
+    Waves::Op o;
+    o.ev = ei;
+    o.depth = 0;
+    o.rows.resize(static_cast<std::size_t>(e.n));
+    std::iota(o.rows.begin(), o.rows.end(), 0);
+    W.ops.push_back(std::move(o));
+    e.root = static_cast<int>(W.ops.size()) - 1;
+    e.stack.push_back(e.root);
+  };
+  auto rollback = [&](const std::vector<int>& doms) {
     std::vector<std::int32_t> ridx, fslots;
-    for (int l : bad_dom) {
+    for (int l : doms) {
       Waves::Dom& D = W.dom[static_cast<std::size_t>(l)];
       for (int i = 0; i < D.snap_n; ++i) ridx.push_back(D.snap0 + i);
       fslots.insert(fslots.end(), D.taken.begin(), D.taken.end());
@@ -876,14 +596,14 @@ void Context::run_inserts_waves(std::int64_t frame_id, std::int64_t pid, int T, 
     launches_ += launch_free_slots(t_, reinterpret_cast<const std::int32_t*>(db + o_f), static_cast<std::int32_t>(fslots.size()), st_);
     launches_ += launch_restore_slots(t_, reinterpret_cast<const std::int32_t*>(db + o_x), static_cast<std::int32_t>(ridx.size()),
                                       W.snap.p, st_);
-    for (std::int32_t s : fslots) free_slots_.push_back(s);
-    std::vector<std::int32_t> plrec, ploff;
-    for (int l : bad_dom) {
+    for (std::int32_t sl : fslots) free_slots_.push_back(sl);
+    for (int l : doms) {
       Waves::Dom& D = W.dom[static_cast<std::size_t>(l)];
       D.prev_ops = D.ops;
       D.ops = 0;
       D.events.clear();
       D.taken.clear();
+      D.tie = false;
       D.pl = host_slots(l);
       D.epoch = W.epoch_next++;
       D.cur = D.first_tok;
@@ -895,6 +615,380 @@ void Context::run_inserts_waves(std::int64_t frame_id, std::int64_t pid, int T, 
       D.pend_valid = !D.retry;
       D.cur_ev = -1;
       count_outcome(l, 0, D.first_tok);
+    }
+  };
+
+  for (;;) {
+    // ---- (1) validation sweep
+    const auto v0 = clk::now();
+    std::vector<int> chk;
+    std::vector<std::uint64_t> chk_ctr;
+    bool any_undone = false;
+    {
+      // exact over the prefix of finished domains; past the first unfinished one the counters are
+      // the current best prediction (an unfinished domain counts as predict() counts it), so a
+      // finished domain whose split ran with a counter that is now predicted wrong is corrected
+      // (recomputed and, if its result changes, restarted) without waiting for the domains before
+      // it to finish; the final sweep, with every domain finished, is exact
+      std::uint64_t c = ctr_base;
+      for (int l = 0; l < L_; ++l) {
+        const Waves::Dom& D = W.dom[static_cast<std::size_t>(l)];
+        if (!D.active) continue;
+        if (!D.done) {
+          any_undone = true;
+          std::int64_t left = D.pend_valid && D.pend_kind == EV_SPLIT ? 1 : 0;
+          if (D.cur_ev >= 0) left += static_cast<std::int64_t>(W.evs[static_cast<std::size_t>(D.cur_ev)].stack.size());
+          c += static_cast<std::uint64_t>(std::max<std::int64_t>(D.ops + left, D.prev_ops));
+          continue;
+        }
+        first_ctr[static_cast<std::size_t>(l)] = c;
+        for (int ei : D.events)
+          for (int oi : W.evs[static_cast<std::size_t>(ei)].ops) {
+            const Waves::Op& o = W.ops[static_cast<std::size_t>(oi)];
+            if (o.ctr != c && o.ok_ctr != static_cast<std::int64_t>(c)) {
+              chk.push_back(oi);
+              chk_ctr.push_back(c);
+            }
+            ++c;
+          }
+      }
+    }
+    t_verify += us(v0, clk::now());
+    if (!any_undone && chk.empty()) break;
+    // ---- (2) this wave's events
+    std::vector<int> relaunch, rcur, new_evs;
+    for (int l = 0; l < L_; ++l) {
+      Waves::Dom& D = W.dom[static_cast<std::size_t>(l)];
+      if (!D.active || D.done) continue;
+      if (D.retry) {
+        relaunch.push_back(l);
+        rcur.push_back(D.pend_tok);
+        D.cur = D.pend_tok;
+        D.retry = false;
+        continue;
+      }
+      if (D.pend_valid) new_evs.push_back(new_event(l));
+    }
+    W.st[1] += 1;  // waves
+    const auto s0 = clk::now();
+    // stage the new pools
+    auto stage = [&](const std::vector<int>& evl) {
+      std::vector<GatherJob> gj;
+      std::vector<int> staged;
+      std::int64_t rows_need = W.rows_used;
+      for (int ei : evl) {
+        Waves::Event& e = W.evs[static_cast<std::size_t>(ei)];
+        if (e.row0 >= 0) continue;  // reused
+        e.row0 = rows_need;
+        rows_need += e.n;
+        staged.push_back(ei);
+      }
+      if (staged.empty()) return;
+      const std::int64_t keep_rows = W.rows_used;
+      W.stage_k.ensure(static_cast<std::size_t>(rows_need) * rb, st_, static_cast<std::size_t>(keep_rows) * rb);
+      W.stage_v.ensure(static_cast<std::size_t>(rows_need) * rb, st_, static_cast<std::size_t>(keep_rows) * rb);
+      W.stage_f32.ensure(static_cast<std::size_t>(rows_need) * d_ * 4, st_, static_cast<std::size_t>(keep_rows) * d_ * 4);
+      W.rows_used = rows_need;
+      W.km_out.ensure(staged.size() * 4 + 64, st_);
+      for (std::size_t i = 0; i < staged.size(); ++i) {
+        const Waves::Event& e = W.evs[static_cast<std::size_t>(staged[i])];
+        GatherJob g{};
+        g.slot = e.parent_slot;
+        g.with_buf = 1;
+        g.row0 = e.row0;
+        g.frame_row = static_cast<std::int64_t>(e.layer) * t_.tmax + e.tok;
+        g.count_out = W.km_out.as<std::int32_t>() + i;
+        gj.push_back(g);
+      }
+      W.up.reset();
+      const std::size_t o = W.up.add(gj.data(), gj.size() * sizeof(GatherJob));
+      std::uint8_t* db = W.up.send(st_);
+      launches_ += launch_gather_batch(t_, reinterpret_cast<const GatherJob*>(db + o), static_cast<std::int32_t>(gj.size()),
+                                       d_fk_, d_fv_, W.stage_k.p, W.stage_v.p, st_);
+      launches_ += launch_to_f32(t_, W.stage_k.as<std::uint8_t>(static_cast<std::size_t>(keep_rows) * rb),
+                                 W.stage_f32.as<float>(static_cast<std::size_t>(keep_rows) * d_ * 4),
+                                 (rows_need - keep_rows) * d_, st_);
+      W.h_out.ensure(gj.size() * 4, st_);
+      KVC_CUDA(cudaMemcpyAsync(W.h_out.p, W.km_out.p, gj.size() * 4, cudaMemcpyDeviceToHost, st_));
+      sync();
+      for (std::size_t i = 0; i < staged.size(); ++i)
+        if (W.h_out.as<std::int32_t>()[i] != W.evs[static_cast<std::size_t>(staged[i])].n)
+          fail(-11, "wave engine: staged pool size differs from the host's count");
+    };
+    stage(new_evs);
+    t_stage += us(s0, clk::now());
+    for (int ei : new_evs) root_op(ei);
+    // ---- sub-waves: one op per event at a time, in DFS preorder (its counter order); the first
+    // also carries the validation sweep's recomputations
+    std::vector<std::pair<int, int>> pending_stats;  // (leaf, event) needing stats + var
+    for (int ei : new_evs) {
+      const Waves::Event& e = W.evs[static_cast<std::size_t>(ei)];
+      if (is_leaf_code(e.root)) pending_stats.emplace_back(leaf_of(e.root), ei);
+    }
+    bool first_sub = true;
+    for (;;) {
+      std::vector<int> opl;
+      std::vector<std::uint64_t> ctrs;
+      for (int ei : new_evs) {
+        Waves::Event& e = W.evs[static_cast<std::size_t>(ei)];
+        if (e.stack.empty()) continue;
+        const int oi = e.stack.back();
+        e.stack.pop_back();
+        Waves::Dom& D = W.dom[static_cast<std::size_t>(e.layer)];
+        Waves::Op& o = W.ops[static_cast<std::size_t>(oi)];
+        o.ctr = predict(e.layer);
+        D.ops += 1;
+        e.ops.push_back(oi);
+        opl.push_back(oi);
+        ctrs.push_back(o.ctr);
+      }
+      const std::size_t n_settle = opl.size();
+      if (first_sub) {
+        opl.insert(opl.end(), chk.begin(), chk.end());
+        ctrs.insert(ctrs.end(), chk_ctr.begin(), chk_ctr.end());
+      }
+      if (opl.empty() && !(first_sub && !pending_stats.empty())) break;
+      // k-means
+      std::vector<std::vector<std::int32_t>> res;
+      if (!opl.empty()) t_km += run_kmeans(opl, ctrs, res);
+      std::vector<int> settled(opl.begin(), opl.begin() + static_cast<std::ptrdiff_t>(n_settle));
+      for (std::size_t j = 0; j < n_settle; ++j) W.ops[static_cast<std::size_t>(opl[j])].assign = std::move(res[j]);
+      if (first_sub && !chk.empty()) {
+        // ---- validation results: failing domains are rolled back and restarted in this wave
+        const auto c0 = clk::now();
+        W.st[4] += static_cast<double>(chk.size());
+        std::vector<int> bad_dom;
+        std::vector<std::vector<std::int32_t>> exact_first(static_cast<std::size_t>(L_));
+        for (std::size_t j = 0; j < chk.size(); ++j) {
+          std::vector<std::int32_t>& r = res[n_settle + j];
+          Waves::Op& o = W.ops[static_cast<std::size_t>(chk[j])];
+          const int l = W.evs[static_cast<std::size_t>(o.ev)].layer;
+          const Waves::Dom& D = W.dom[static_cast<std::size_t>(l)];
+          const bool is_first = !D.events.empty() && W.evs[static_cast<std::size_t>(D.events.front())].root == chk[j];
+          // the same two groups with the labels exchanged: only the children's emission order (and
+          // so their ids) changes. Valid when neither group was split further (the sub-splits'
+          // counters would follow the other order) and no relaunch decision of the domain was a
+          // tie broken by the provisional ids (every other decision is order-independent).
+          bool swapped = !D.tie && is_leaf_code(o.kids[0]) && is_leaf_code(o.kids[1]) && r.size() == o.assign.size();
+          for (std::size_t i = 0; swapped && i < r.size(); ++i) swapped = r[i] == 1 - o.assign[i];
+          if (r == o.assign || swapped) {
+            o.ok_ctr = static_cast<std::int64_t>(chk_ctr[j]);
+            o.ok_swap = swapped;
+            W.st[12] += swapped ? 1 : 0;
+          } else if (bad_dom.empty() || bad_dom.back() != l) {
+            bad_dom.push_back(l);
+          }
+          if (is_first) exact_first[static_cast<std::size_t>(l)] = std::move(r);
+        }
+        if (!bad_dom.empty()) {
+          passes += 1;
+          W.st[3] += static_cast<double>(bad_dom.size());
+          if (waves_log_) {
+            std::string m = "[waves] frame " + std::to_string(frame_id) + " wave " + std::to_string(W.st[1]) + " checked " +
+                            std::to_string(chk.size()) + " failed domains " + std::to_string(bad_dom.size()) + ":";
+            for (int l : bad_dom) {
+              const Waves::Dom& D = W.dom[static_cast<std::size_t>(l)];
+              m += " " + std::to_string(l) + "(ops " + std::to_string(D.ops) + " prev " + std::to_string(D.prev_ops) + ")";
+            }
+            std::fprintf(stderr, "%s\n", m.c_str());
+          }
+          // the exact result of each failing domain's first split (for its restart)
+          for (int l : bad_dom) {
+            Waves::Dom& D = W.dom[static_cast<std::size_t>(l)];
+            Prefab& pf = prefab[static_cast<std::size_t>(l)];
+            pf = Prefab{};
+            const Waves::Event& e1 = W.evs[static_cast<std::size_t>(D.events.front())];
+            pf.row0 = e1.row0;
+            pf.n = e1.n;
+            if (e1.kind != EV_SPLIT) continue;
+            const Waves::Op& o1 = W.ops[static_cast<std::size_t>(e1.root)];
+            const std::uint64_t c1 = first_ctr[static_cast<std::size_t>(l)];
+            pf.on = true;
+            pf.ctr = c1;
+            if (!exact_first[static_cast<std::size_t>(l)].empty()) {
+              pf.assign = exact_first[static_cast<std::size_t>(l)];
+            } else {
+              pf.assign = o1.assign;
+              if (o1.ctr != c1 && o1.ok_swap)
+                for (std::int32_t& a : pf.assign) a = 1 - a;
+            }
+          }
+          rollback(bad_dom);
+          // restart: first event again (pool reused), its root split from the exact result
+          for (int l : bad_dom) {
+            Waves::Dom& D = W.dom[static_cast<std::size_t>(l)];
+            if (D.retry) {  // the first stop was a stale-residence retry: relaunch it
+              relaunch.push_back(l);
+              rcur.push_back(D.pend_tok);
+              D.cur = D.pend_tok;
+              D.retry = false;
+              continue;
+            }
+            const Prefab& pf = prefab[static_cast<std::size_t>(l)];
+            const int ei = new_event(l);
+            Waves::Event& e = W.evs[static_cast<std::size_t>(ei)];
+            if (e.n != pf.n) fail(-11, "wave engine: restarted pool size differs");
+            e.row0 = pf.row0;
+            root_op(ei);
+            new_evs.push_back(ei);
+            if (is_leaf_code(e.root)) {
+              pending_stats.emplace_back(leaf_of(e.root), ei);
+              continue;
+            }
+            Waves::Op& o = W.ops[static_cast<std::size_t>(e.root)];
+            e.stack.pop_back();
+            o.ctr = pf.ctr;
+            o.assign = pf.assign;
+            D.ops += 1;
+            e.ops.push_back(e.root);
+            settled.push_back(e.root);
+          }
+        }
+        t_verify += us(c0, clk::now());
+      }
+      first_sub = false;
+      const auto st0 = clk::now();
+      // groups -> exact statistics in fresh slots
+      struct G {
+        int op, g;
+        std::vector<int> rows;
+        std::int32_t slot;
+      };
+      std::vector<G> groups;
+      for (int oi : settled) {
+        const Waves::Op& o = W.ops[static_cast<std::size_t>(oi)];
+        std::vector<int> g2[2];
+        for (std::size_t i = 0; i < o.rows.size(); ++i) g2[o.assign[i]].push_back(o.rows[i]);
+        for (int g = 0; g < 2; ++g)
+          if (!g2[g].empty()) groups.push_back({oi, g, std::move(g2[g]), take_slot()});
+      }
+      std::vector<AppendRun> runs;
+      std::vector<std::int32_t> idx, slots;
+      for (const G& g : groups) {
+        const Waves::Event& e = W.evs[static_cast<std::size_t>(W.ops[static_cast<std::size_t>(g.op)].ev)];
+        runs.push_back({g.slot, static_cast<std::int32_t>(idx.size()), static_cast<std::int32_t>(g.rows.size()), 0});
+        for (int r : g.rows) idx.push_back(static_cast<std::int32_t>(e.row0 + r));
+        slots.push_back(g.slot);
+      }
+      for (auto& ps : pending_stats) {  // seeds
+        Waves::Leaf& lf = W.leaves[static_cast<std::size_t>(ps.first)];
+        const Waves::Event& e = W.evs[static_cast<std::size_t>(ps.second)];
+        lf.slot = take_slot();
+        runs.push_back({lf.slot, static_cast<std::int32_t>(idx.size()), 1, 0});
+        idx.push_back(static_cast<std::int32_t>(e.row0));
+        slots.push_back(lf.slot);
+        W.dom[static_cast<std::size_t>(e.layer)].taken.push_back(lf.slot);
+      }
+      pending_stats.clear();
+      std::vector<double> vars(runs.size());
+      if (!runs.empty()) {
+        W.up.reset();
+        const std::size_t o_r = W.up.add(runs.data(), runs.size() * sizeof(AppendRun));
+        const std::size_t o_i = W.up.add(idx.data(), idx.size() * 4);
+        const std::size_t o_s = W.up.add(slots.data(), slots.size() * 4);
+        std::uint8_t* db = W.up.send(st_);
+        launches_ += launch_exact_stats(t_, reinterpret_cast<const AppendRun*>(db + o_r), static_cast<std::int32_t>(runs.size()),
+                                        reinterpret_cast<const std::int32_t*>(db + o_i), W.stage_k.p, st_);
+        W.km_out.ensure(runs.size() * 8 + 64, st_);
+        launches_ += launch_read_vars(t_, reinterpret_cast<const std::int32_t*>(db + o_s), static_cast<std::int32_t>(slots.size()),
+                                      W.km_out.as<double>(), st_);
+        W.h_out.ensure(runs.size() * 8, st_);
+        KVC_CUDA(cudaMemcpyAsync(W.h_out.p, W.km_out.p, runs.size() * 8, cudaMemcpyDeviceToHost, st_));
+        sync();
+        std::memcpy(vars.data(), W.h_out.p, runs.size() * 8);
+      }
+      // recursion decisions (maintainer.cpp:228-238), in group order per op
+      for (std::size_t gi = 0; gi < groups.size(); ++gi) {
+        G& g = groups[gi];
+        const int o_ev = W.ops[static_cast<std::size_t>(g.op)].ev, o_depth = W.ops[static_cast<std::size_t>(g.op)].depth;
+        const Waves::Event& e = W.evs[static_cast<std::size_t>(o_ev)];
+        const std::int64_t sz = static_cast<std::int64_t>(g.rows.size());
+        if (o_depth + 1 < cfg_.max_split_depth && sz >= 2 && vars[gi] > tau_at(sz, cfg_)) {
+          free_slots_.push_back(g.slot);  // no pages were attached
+          Waves::Op c;
+          c.ev = o_ev;
+          c.depth = o_depth + 1;
+          c.rows = std::move(g.rows);
+          W.ops.push_back(std::move(c));
+          W.ops[static_cast<std::size_t>(g.op)].kids[g.g] = static_cast<int>(W.ops.size()) - 1;
+        } else {
+          Waves::Leaf lf;
+          lf.rows = std::move(g.rows);
+          lf.slot = g.slot;
+          W.leaves.push_back(std::move(lf));
+          W.ops[static_cast<std::size_t>(g.op)].kids[g.g] = leaf_code(static_cast<int>(W.leaves.size()) - 1);
+          W.dom[static_cast<std::size_t>(e.layer)].taken.push_back(g.slot);
+        }
+      }
+      // children to run: push kid 1 first so kid 0 (its subtree) runs first (preorder)
+      for (int oi : settled) {
+        const Waves::Op& o = W.ops[static_cast<std::size_t>(oi)];
+        Waves::Event& e = W.evs[static_cast<std::size_t>(o.ev)];
+        for (int g = 1; g >= 0; --g)
+          if (o.kids[g] >= 0) e.stack.push_back(o.kids[g]);
+      }
+      t_stats += us(st0, clk::now());
+    }
+    // ---- install children: headers, pages, partition lists; relaunch the domains
+    const auto i0 = clk::now();
+    std::vector<SlotHeader> hd;
+    std::vector<AppendRun> runs;
+    std::vector<std::int32_t> idx;
+    for (int ei : new_evs) {
+      Waves::Event& e = W.evs[static_cast<std::size_t>(ei)];
+      Waves::Dom& D = W.dom[static_cast<std::size_t>(e.layer)];
+      if (D.events.empty() || std::find(D.events.begin(), D.events.end(), ei) == D.events.end())
+        continue;  // an event of an attempt rolled back in this wave
+      // emission order: in-order over the split tree (maintainer.cpp:224-238)
+      if (is_leaf_code(e.root)) {
+        e.emitted.push_back(leaf_of(e.root));
+      } else {
+        auto walk = [&](auto&& self, int oi) -> void {
+          const Waves::Op& o = W.ops[static_cast<std::size_t>(oi)];
+          for (int g = 0; g < 2; ++g) {
+            if (o.kids[g] == kNoKid) continue;
+            if (is_leaf_code(o.kids[g]))
+              e.emitted.push_back(leaf_of(o.kids[g]));
+            else
+              self(self, o.kids[g]);
+          }
+        };
+        walk(walk, e.root);
+      }
+      if (e.kind == EV_SPLIT) D.pl.erase(std::remove(D.pl.begin(), D.pl.end(), e.parent_slot), D.pl.end());
+      for (int li : e.emitted) {
+        const Waves::Leaf& lf = W.leaves[static_cast<std::size_t>(li)];
+        const std::int64_t n = static_cast<std::int64_t>(lf.rows.size());
+        hd.push_back({lf.slot, 0, W.prov_next++, n});
+        runs.push_back({lf.slot, static_cast<std::int32_t>(idx.size()), static_cast<std::int32_t>(n), 0});
+        for (int r : lf.rows) idx.push_back(static_cast<std::int32_t>(e.row0 + r));
+        D.pl.push_back(lf.slot);
+        W.sz_stamp[static_cast<std::size_t>(lf.slot)] = D.epoch;
+        W.sz[static_cast<std::size_t>(lf.slot)] = n;
+      }
+      D.cur = e.tok + 1;
+      D.cur_ev = -1;
+      if (D.cur >= T) {
+        D.done = true;
+      } else {
+        relaunch.push_back(e.layer);
+        rcur.push_back(D.cur);
+      }
+    }
+    // partition lists of every domain in speculation (capacity first: a compaction rewrites
+    // the device lists from the host ones)
+    std::vector<std::int32_t> plrec, ploff;
+    pl_floor_.assign(parts_.size() * static_cast<std::size_t>(L_), 0);
+    for (int l = 0; l < L_; ++l)
+      if (W.dom[static_cast<std::size_t>(l)].active)
+        pl_floor_[static_cast<std::size_t>(pid) * L_ + l] = static_cast<std::int32_t>(W.dom[static_cast<std::size_t>(l)].pl.size());
+    for (int l = 0; l < L_; ++l)
+      if (W.dom[static_cast<std::size_t>(l)].active)
+        pl_reserve(pid, l, static_cast<std::int32_t>(W.dom[static_cast<std::size_t>(l)].pl.size()));
+    pl_floor_.clear();
+    for (int l = 0; l < L_; ++l) {
+      const Waves::Dom& D = W.dom[static_cast<std::size_t>(l)];
+      if (!D.active) continue;
       ploff.push_back(static_cast<std::int32_t>(plrec.size()));
       plrec.push_back(static_cast<std::int32_t>(pid * L_ + l));
       plrec.push_back(parts_[static_cast<std::size_t>(pid)].dev_off[static_cast<std::size_t>(l)]);
@@ -902,14 +996,49 @@ void Context::run_inserts_waves(std::int64_t frame_id, std::int64_t pid, int T, 
       plrec.insert(plrec.end(), D.pl.begin(), D.pl.end());
     }
     W.up.reset();
+    const std::size_t o_h = W.up.add(hd.data(), hd.size() * sizeof(SlotHeader));
+    const std::size_t o_r = W.up.add(runs.data(), runs.size() * sizeof(AppendRun));
+    const std::size_t o_i = W.up.add(idx.data(), idx.size() * 4);
     const std::size_t o_p = W.up.add(plrec.data(), plrec.size() * 4);
     const std::size_t o_q = W.up.add(ploff.data(), ploff.size() * 4);
-    db = W.up.send(st_);
+    std::uint8_t* db = W.up.send(st_);
+    launches_ += launch_slot_headers(t_, reinterpret_cast<const SlotHeader*>(db + o_h), static_cast<std::int32_t>(hd.size()), st_);
+    launches_ += launch_append_runs(t_, reinterpret_cast<const AppendRun*>(db + o_r), static_cast<std::int32_t>(runs.size()),
+                                    reinterpret_cast<const std::int32_t*>(db + o_i), W.stage_k.p, W.stage_v.p, st_);
     launches_ += launch_pl_scatter(t_, reinterpret_cast<const std::int32_t*>(db + o_p), reinterpret_cast<const std::int32_t*>(db + o_q),
                                    static_cast<std::int32_t>(ploff.size()), st_);
-    sync();
+    t_inst += us(i0, clk::now());
+    // ---- relaunch
+    if (!relaunch.empty()) {
+      const auto r0 = clk::now();
+      std::vector<int> cursor(static_cast<std::size_t>(L_), 0);
+      for (std::size_t i = 0; i < relaunch.size(); ++i) cursor[static_cast<std::size_t>(relaunch[i])] = rcur[i];
+      round_after_event_ = true;
+      launch_round(relaunch, cursor);
+      round_after_event_ = false;
+      sync();
+      check_err_word(*h_err_);
+      const bool tie_known = resolve_seq_ || relaunch_seq_;  // only k_resolve reports ties
+      for (int l : relaunch) {
+        W.dom[static_cast<std::size_t>(l)].tie |= !tie_known || h_err_[1 + l] != 0;
+        take_stop(l);
+      }
+      t_relaunch += us(r0, clk::now());
+    } else {
+      sync();
+    }
   }
   W.st[2] += passes;
+  if (waves_log_) {
+    int act = 0, ops = 0, multi = 0;
+    for (const Waves::Dom& D : W.dom) {
+      act += D.active ? 1 : 0;
+      ops += D.ops;
+      multi += D.ops > 1 ? 1 : 0;
+    }
+    std::fprintf(stderr, "[waves] frame %lld done: passes %d, domains with events %d, ops %d, domains with >1 op %d\n",
+                 static_cast<long long>(frame_id), passes, act, ops, multi);
+  }
 
   // ---------------------------------------------------------------- commit in reference order
   const auto c0 = clk::now();
@@ -939,17 +1068,35 @@ void Context::run_inserts_waves(std::int64_t frame_id, std::int64_t pid, int T, 
         drop_cluster_host(cid);
         parents.push_back(e.parent_slot);
         for (int oi : e.ops) {
-          const Waves::Op& o = W.ops[static_cast<std::size_t>(oi)];
+          Waves::Op& o = W.ops[static_cast<std::size_t>(oi)];
           const std::uint64_t ctr = static_cast<std::uint64_t>(split_counter_++);
-          if (o.ctr != ctr && o.ok_ctr != static_cast<std::int64_t>(ctr)) fail(-11, "wave commit: unverified split counter");
+          if (o.ctr == ctr) o.ok_swap = false;
+          else if (o.ok_ctr != static_cast<std::int64_t>(ctr)) fail(-11, "wave commit: unverified split counter");
           mstats_[5] += 1;  // split_ops_total
           evt_t_[7] += 1.0;
         }
       } else {
         ids.push_back({frame_id, e.tok});
       }
+      std::vector<int> emitted;  // the reference's emission order (labels as the exact seed gives them)
+      if (is_leaf_code(e.root)) {
+        emitted.push_back(leaf_of(e.root));
+      } else {
+        auto walk = [&](auto&& self, int oi) -> void {
+          const Waves::Op& o = W.ops[static_cast<std::size_t>(oi)];
+          for (int k = 0; k < 2; ++k) {
+            const int g = o.ok_swap ? 1 - k : k;
+            if (o.kids[g] == kNoKid) continue;
+            if (is_leaf_code(o.kids[g]))
+              emitted.push_back(leaf_of(o.kids[g]));
+            else
+              self(self, o.kids[g]);
+          }
+        };
+        walk(walk, e.root);
+      }
       std::int64_t home = -1;
-      for (int li : e.emitted) {
+      for (int li : emitted) {
         const Waves::Leaf& lf = W.leaves[static_cast<std::size_t>(li)];
         std::vector<Member> m;
         m.reserve(lf.rows.size());
@@ -964,7 +1111,7 @@ void Context::run_inserts_waves(std::int64_t frame_id, std::int64_t pid, int T, 
         cids.push_back({id, lf.slot, 0});
         if (has_tok && home < 0) home = id;  // home_of (maintainer.cpp:62-70)
       }
-      if (home < 0) home = slot_id_[static_cast<std::size_t>(W.leaves[static_cast<std::size_t>(e.emitted.front())].slot)];
+      if (home < 0) home = slot_id_[static_cast<std::size_t>(W.leaves[static_cast<std::size_t>(emitted.front())].slot)];
       if (assigned) assigned[static_cast<std::size_t>(l) * T + e.tok] = home;
       t = e.tok + 1;
     }

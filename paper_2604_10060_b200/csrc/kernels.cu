@@ -473,6 +473,9 @@ __global__ void __launch_bounds__(32) k_resolve(DevTables t, IngestArgs a) {
   const int T = a.T;
   const int cur = a.cursor[dom];
   if (a.prev_events && *a.prev_events) return;  // skipped speculative round: no writes
+  // some decision of this launch was decided by the CandidateRef key (an exact tie of the best
+  // fp64 cosines): the wave engine then requires its speculative children in their final order
+  bool any_tie = false;
   int n = a.cand_n[dom];
   for (int c = lane; c < n; c += 32) {
     const int s = a.cand_slot[static_cast<int64_t>(dom) * cmax + c];
@@ -752,6 +755,7 @@ __global__ void __launch_bounds__(32) k_resolve(DevTables t, IngestArgs a) {
       double bs = -3.0;
       long long bk = LLONG_MAX;
       int bp = -1;
+      bool ltie = false;
       for (int e = lane; e < min(S.ne, RELMAX); e += 32) {
         const uint8_t v = S.e_var[e];
         if (v == EV_DEAD) continue;
@@ -763,13 +767,20 @@ __global__ void __launch_bounds__(32) k_resolve(DevTables t, IngestArgs a) {
           if (nr < 1e-12) set_err(t, DERR_DEGENERATE);
           cs = clamp1(ddiv(S.e_dot[e], dmul(nkt, nr)));
         }
+        if (cs == bs) ltie = true;
+        else if (cs > bs) ltie = false;
         if (better(cs, S.e_key[e], bs, bk)) {
           bs = cs;
           bk = S.e_key[e];
           bp = e;
         }
       }
+      const double lbs = bs;
       warp_best(bs, bk, bp);
+      {
+        const bool has = lbs == bs;
+        if (__popc(__ballot_sync(kFull, has)) >= 2 || __any_sync(kFull, has && ltie)) any_tie = true;
+      }
       const int bc = S.e_cand[bp];
       const int w = cslot[bc];
       const bool isbuf = cbuf[bc];
@@ -965,6 +976,7 @@ done:
   if (lane == 0) {
     a.dom_pool_n[dom] = S.npool;
     a.n_exact[dom] = n_exact;
+    if (a.tie) a.tie[dom] = any_tie ? 1 : 0;
   }
 }
 

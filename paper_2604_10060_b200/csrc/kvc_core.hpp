@@ -146,6 +146,8 @@ struct IngestArgs {
   int32_t* stop_kind;      // [L]
   int32_t* stop_slot;      // [L]
   int32_t* n_exact;        // [L] exact re-scores performed (instrumentation)
+  int32_t* tie;            // [L] (k_resolve) 1: a decision of the launch was an exact cosine tie
+                           // broken by the cluster-id key (in the outcome block, after the error word)
   // per-token approximate top-M (K1b): candidate index, value, and the (M+1)-th value
   int16_t* topm_idx;       // [L][tmax][TOPM]
   float* topm_val;         // [L][tmax][TOPM]
