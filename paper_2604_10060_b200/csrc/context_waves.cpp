@@ -465,66 +465,97 @@ void Context::run_inserts_waves(std::int64_t frame_id, std::int64_t pid, int T, 
     return c + static_cast<std::uint64_t>(W.dom[static_cast<std::size_t>(l)].ops);
   };
 
-  // k-means of a batch of ops with the given counters -> assignments (host) ; returns false on
-  // a degenerate row
-  auto run_kmeans = [&](const std::vector<int>& opl, const std::vector<std::uint64_t>& ctrs,
-                        std::vector<std::vector<std::int32_t>>& out) {
+  // One launch of split jobs (k_split_two_batch): k-means of an op's pool rows with the seed of
+  // `ctr` (or the labels `given`), and, for jobs with slots, its two groups' Eq. 1/2 statistics
+  // installed into those slots with their variances returned.
+  struct Job {
+    int op = -1;                       // op whose rows are used (or -1: a seed's single row)
+    int ev = -1;                       // event (row base) when op < 0
+    std::uint64_t ctr = 0;
+    std::int32_t slot[2] = {-1, -1};
+    bool want_var = false;
+    const std::vector<std::int32_t>* given = nullptr;
+    // results
+    std::vector<std::int32_t> assign;
+    double var[2] = {0.0, 0.0};
+  };
+  const std::vector<int> one_row = {0};
+  const std::vector<std::int32_t> label0 = {0};
+  auto run_jobs = [&](std::vector<Job>& jobs) {
     const auto k0 = clk::now();
-    const std::size_t nj = opl.size();
-    std::vector<std::int32_t> idx;
-    std::vector<std::size_t> idx_off(nj), scr_off(nj), out_off(nj);
+    const std::size_t nj = jobs.size();
+    if (nj == 0) return 0.0;
+    std::vector<std::int32_t> idx, given;
+    std::vector<std::size_t> idx_off(nj), scr_off(nj), out_off(nj), giv_off(nj, 0);
     std::size_t scr = 0, outw = 0;
     for (std::size_t j = 0; j < nj; ++j) {
-      const Waves::Op& o = W.ops[static_cast<std::size_t>(opl[j])];
-      const Waves::Event& e = W.evs[static_cast<std::size_t>(o.ev)];
+      const Job& J = jobs[j];
+      const std::vector<int>& rows = J.op >= 0 ? W.ops[static_cast<std::size_t>(J.op)].rows : one_row;
+      const Waves::Event& e = W.evs[static_cast<std::size_t>(J.op >= 0 ? W.ops[static_cast<std::size_t>(J.op)].ev : J.ev)];
       idx_off[j] = idx.size();
-      for (int r : o.rows) idx.push_back(static_cast<std::int32_t>(e.row0 + r));
+      for (int r : rows) idx.push_back(static_cast<std::int32_t>(e.row0 + r));
       scr_off[j] = scr;
-      scr += (o.rows.size() * (2 * static_cast<std::size_t>(d_) + 3) + 1) * 8;
+      scr += (rows.size() * (2 * static_cast<std::size_t>(d_) + 3) + 2) * 8;
       out_off[j] = outw;
-      outw += o.rows.size() + 4;
+      outw += rows.size() + 4;
+      if (J.given) {
+        giv_off[j] = given.size();
+        given.insert(given.end(), J.given->begin(), J.given->end());
+      }
     }
     W.km_scratch.ensure(scr, st_);
-    W.km_out.ensure(outw * 4 + nj * 8 + 64, st_);
-    std::vector<SplitJob> jobs(nj);
+    const std::size_t var_off = (outw * 4 + 7) & ~std::size_t{7};
+    const std::size_t obj_off = var_off + nj * 16;
+    W.km_out.ensure(obj_off + nj * 8 + 64, st_);
+    std::vector<SplitJob> sj(nj);
     std::int32_t* dout = W.km_out.as<std::int32_t>();
-    double* dobj = reinterpret_cast<double*>(W.km_out.as<std::uint8_t>((outw * 4 + 7) & ~std::size_t{7}));
     W.up.reset();
     const std::size_t o_idx = W.up.add(idx.data(), idx.size() * 4);
-    const std::size_t o_jobs = W.up.add(jobs.data(), nj * sizeof(SplitJob));  // filled below
-    // the jobs point into the uploaded index array: size the device side first, then fill them
+    const std::size_t o_giv = W.up.add(given.data(), given.size() * 4);
+    const std::size_t o_jobs = W.up.add(sj.data(), nj * sizeof(SplitJob));  // filled below
+    // the jobs point into the uploaded arrays: size the device side first, then fill them
     W.up.h.ensure(W.up.used, st_);
     W.up.d.ensure(W.up.used, st_);
     std::uint8_t* dbase = static_cast<std::uint8_t*>(W.up.d.p);
     for (std::size_t j = 0; j < nj; ++j) {
-      const Waves::Op& o = W.ops[static_cast<std::size_t>(opl[j])];
-      Rng64 rng(mix_seed(maint_seed_, ctrs[j]));
-      const int n = static_cast<int>(o.rows.size());
-      SplitJob& J = jobs[j];
-      J.rows = W.stage_f32.as<float>();
-      J.idx = reinterpret_cast<const std::int32_t*>(dbase + o_idx) + idx_off[j];
-      J.scratch = W.km_scratch.as<double>(scr_off[j]);
-      J.assign = dout + out_off[j];
-      J.meta = dout + out_off[j] + n;
-      J.objective = dobj + j;
-      J.first = static_cast<std::int32_t>(rng.index(static_cast<std::size_t>(n)));
-      J.uni = rng.uniform();
-      J.n = n;
+      const Job& J = jobs[j];
+      const int n = static_cast<int>(J.op >= 0 ? W.ops[static_cast<std::size_t>(J.op)].rows.size() : 1);
+      SplitJob& X = sj[j];
+      X.rows = W.stage_f32.as<float>();
+      X.idx = reinterpret_cast<const std::int32_t*>(dbase + o_idx) + idx_off[j];
+      X.scratch = W.km_scratch.as<double>(scr_off[j]);
+      X.assign = dout + out_off[j];
+      X.meta = dout + out_off[j] + n;
+      X.objective = W.km_out.as<double>(obj_off) + j;
+      X.n = n;
+      X.slot[0] = J.slot[0];
+      X.slot[1] = J.slot[1];
+      X.var_out = (J.want_var || J.slot[0] >= 0 || J.slot[1] >= 0) ? W.km_out.as<double>(var_off) + 2 * j : nullptr;
+      X.assign_in = J.given ? reinterpret_cast<const std::int32_t*>(dbase + o_giv) + giv_off[j] : nullptr;
+      if (!J.given) {
+        Rng64 rng(mix_seed(maint_seed_, J.ctr));
+        X.first = static_cast<std::int32_t>(rng.index(static_cast<std::size_t>(n)));
+        X.uni = rng.uniform();
+      } else {
+        X.first = 0;
+        X.uni = 0.0;
+      }
     }
     std::uint8_t* db = W.up.send(st_);
-    launches_ += launch_split_two_batch(reinterpret_cast<const SplitJob*>(db + o_jobs), static_cast<int>(nj), d_, st_);
-    W.h_out.ensure(outw * 4, st_);
-    KVC_CUDA(cudaMemcpyAsync(W.h_out.p, dout, outw * 4, cudaMemcpyDeviceToHost, st_));
+    launches_ += launch_split_two_batch(t_, reinterpret_cast<const SplitJob*>(db + o_jobs), static_cast<int>(nj), d_, st_);
+    W.h_out.ensure(obj_off, st_);
+    KVC_CUDA(cudaMemcpyAsync(W.h_out.p, dout, obj_off, cudaMemcpyDeviceToHost, st_));
     sync();
-    out.resize(nj);
     for (std::size_t j = 0; j < nj; ++j) {
-      const Waves::Op& o = W.ops[static_cast<std::size_t>(opl[j])];
+      Job& J = jobs[j];
+      const std::size_t n = J.op >= 0 ? W.ops[static_cast<std::size_t>(J.op)].rows.size() : 1;
       const std::int32_t* a = W.h_out.as<std::int32_t>() + out_off[j];
-      const std::int32_t* meta = a + o.rows.size();
-      if (meta[3] != 0) fail(-2, "normalize of zero vector");
-      out[j].assign(a, a + o.rows.size());
+      if (a[n + 3] != 0) fail(-2, "normalize of zero vector");
+      J.assign.assign(a, a + n);
+      J.var[0] = W.h_out.as<double>(var_off)[2 * j];
+      J.var[1] = W.h_out.as<double>(var_off)[2 * j + 1];
+      if (!J.given) W.st[7] += 1;  // k-means jobs
     }
-    W.st[7] += static_cast<double>(nj);  // k-means jobs
     return us(k0, clk::now());
   };
 
@@ -719,16 +750,14 @@ void Context::run_inserts_waves(std::int64_t frame_id, std::int64_t pid, int T, 
     t_stage += us(s0, clk::now());
     for (int ei : new_evs) root_op(ei);
     // ---- sub-waves: one op per event at a time, in DFS preorder (its counter order); the first
-    // also carries the validation sweep's recomputations
-    std::vector<std::pair<int, int>> pending_stats;  // (leaf, event) needing stats + var
-    for (int ei : new_evs) {
-      const Waves::Event& e = W.evs[static_cast<std::size_t>(ei)];
-      if (is_leaf_code(e.root)) pending_stats.emplace_back(leaf_of(e.root), ei);
-    }
+    // also carries the validation sweep's recomputations and the seeds' statistics
+    std::vector<int> seed_evs;  // events whose root is a seed leaf
+    for (int ei : new_evs)
+      if (is_leaf_code(W.evs[static_cast<std::size_t>(ei)].root)) seed_evs.push_back(ei);
     bool first_sub = true;
     for (;;) {
-      std::vector<int> opl;
-      std::vector<std::uint64_t> ctrs;
+      std::vector<Job> jobs;
+      std::vector<int> settled;  // ops whose groups are decided this sub-wave (jobs[0 .. n_settle))
       for (int ei : new_evs) {
         Waves::Event& e = W.evs[static_cast<std::size_t>(ei)];
         if (e.stack.empty()) continue;
@@ -739,20 +768,42 @@ void Context::run_inserts_waves(std::int64_t frame_id, std::int64_t pid, int T, 
         o.ctr = predict(e.layer);
         D.ops += 1;
         e.ops.push_back(oi);
-        opl.push_back(oi);
-        ctrs.push_back(o.ctr);
+        settled.push_back(oi);
+        Job J;
+        J.op = oi;
+        J.ctr = o.ctr;
+        J.slot[0] = take_slot();
+        J.slot[1] = take_slot();
+        jobs.push_back(std::move(J));
       }
-      const std::size_t n_settle = opl.size();
+      const std::size_t n_settle = jobs.size();
+      auto add_seed_jobs = [&](const std::vector<int>& evl) {
+        for (int ei : evl) {
+          const Waves::Event& e = W.evs[static_cast<std::size_t>(ei)];
+          Waves::Leaf& lf = W.leaves[static_cast<std::size_t>(leaf_of(e.root))];
+          lf.slot = take_slot();
+          W.dom[static_cast<std::size_t>(e.layer)].taken.push_back(lf.slot);
+          Job J;
+          J.ev = ei;
+          J.slot[0] = lf.slot;
+          J.given = &label0;
+          jobs.push_back(std::move(J));
+        }
+      };
       if (first_sub) {
-        opl.insert(opl.end(), chk.begin(), chk.end());
-        ctrs.insert(ctrs.end(), chk_ctr.begin(), chk_ctr.end());
+        add_seed_jobs(seed_evs);
+        for (std::size_t j = 0; j < chk.size(); ++j) {
+          Job J;
+          J.op = chk[j];
+          J.ctr = chk_ctr[j];
+          jobs.push_back(std::move(J));
+        }
       }
-      if (opl.empty() && !(first_sub && !pending_stats.empty())) break;
-      // k-means
-      std::vector<std::vector<std::int32_t>> res;
-      if (!opl.empty()) t_km += run_kmeans(opl, ctrs, res);
-      std::vector<int> settled(opl.begin(), opl.begin() + static_cast<std::ptrdiff_t>(n_settle));
-      for (std::size_t j = 0; j < n_settle; ++j) W.ops[static_cast<std::size_t>(opl[j])].assign = std::move(res[j]);
+      if (jobs.empty()) break;
+      t_km += run_jobs(jobs);
+      const std::size_t chk0 = jobs.size() - (first_sub ? chk.size() : 0);
+      for (std::size_t j = 0; j < n_settle; ++j) W.ops[static_cast<std::size_t>(settled[j])].assign = jobs[j].assign;
+      std::vector<Job> done_jobs(jobs.begin(), jobs.begin() + static_cast<std::ptrdiff_t>(n_settle));
       if (first_sub && !chk.empty()) {
         // ---- validation results: failing domains are rolled back and restarted in this wave
         const auto c0 = clk::now();
@@ -760,7 +811,7 @@ void Context::run_inserts_waves(std::int64_t frame_id, std::int64_t pid, int T, 
         std::vector<int> bad_dom;
         std::vector<std::vector<std::int32_t>> exact_first(static_cast<std::size_t>(L_));
         for (std::size_t j = 0; j < chk.size(); ++j) {
-          std::vector<std::int32_t>& r = res[n_settle + j];
+          std::vector<std::int32_t>& r = jobs[chk0 + j].assign;
           Waves::Op& o = W.ops[static_cast<std::size_t>(chk[j])];
           const int l = W.evs[static_cast<std::size_t>(o.ev)].layer;
           const Waves::Dom& D = W.dom[static_cast<std::size_t>(l)];
@@ -814,7 +865,10 @@ void Context::run_inserts_waves(std::int64_t frame_id, std::int64_t pid, int T, 
             }
           }
           rollback(bad_dom);
-          // restart: first event again (pool reused), its root split from the exact result
+          // restart: first event again (pool reused), its root split from the exact result; the
+          // restarted splits' (and seeds') statistics in one more launch
+          std::vector<Job> rj;
+          std::vector<int> restart_seeds;
           for (int l : bad_dom) {
             Waves::Dom& D = W.dom[static_cast<std::size_t>(l)];
             if (D.retry) {  // the first stop was a stale-residence retry: relaunch it
@@ -832,7 +886,7 @@ void Context::run_inserts_waves(std::int64_t frame_id, std::int64_t pid, int T, 
             root_op(ei);
             new_evs.push_back(ei);
             if (is_leaf_code(e.root)) {
-              pending_stats.emplace_back(leaf_of(e.root), ei);
+              restart_seeds.push_back(ei);
               continue;
             }
             Waves::Op& o = W.ops[static_cast<std::size_t>(e.root)];
@@ -842,82 +896,57 @@ void Context::run_inserts_waves(std::int64_t frame_id, std::int64_t pid, int T, 
             D.ops += 1;
             e.ops.push_back(e.root);
             settled.push_back(e.root);
+            Job J;
+            J.op = e.root;
+            J.given = &prefab[static_cast<std::size_t>(l)].assign;
+            J.slot[0] = take_slot();
+            J.slot[1] = take_slot();
+            rj.push_back(std::move(J));
           }
+          const std::size_t n_rs = rj.size();
+          std::swap(jobs, rj);
+          add_seed_jobs(restart_seeds);
+          if (!jobs.empty()) t_km += run_jobs(jobs);
+          for (std::size_t j = 0; j < n_rs; ++j) done_jobs.push_back(std::move(jobs[j]));
         }
         t_verify += us(c0, clk::now());
       }
       first_sub = false;
       const auto st0 = clk::now();
-      // groups -> exact statistics in fresh slots
-      struct G {
-        int op, g;
-        std::vector<int> rows;
-        std::int32_t slot;
-      };
-      std::vector<G> groups;
-      for (int oi : settled) {
-        const Waves::Op& o = W.ops[static_cast<std::size_t>(oi)];
+      // groups (their statistics are installed in the jobs' slots) and the recursion decisions
+      // (maintainer.cpp:228-238)
+      for (std::size_t j = 0; j < settled.size(); ++j) {
+        const int oi = settled[j];
+        const Job& J = done_jobs[j];
+        const int o_ev = W.ops[static_cast<std::size_t>(oi)].ev, o_depth = W.ops[static_cast<std::size_t>(oi)].depth;
+        const int layer = W.evs[static_cast<std::size_t>(o_ev)].layer;
         std::vector<int> g2[2];
-        for (std::size_t i = 0; i < o.rows.size(); ++i) g2[o.assign[i]].push_back(o.rows[i]);
-        for (int g = 0; g < 2; ++g)
-          if (!g2[g].empty()) groups.push_back({oi, g, std::move(g2[g]), take_slot()});
-      }
-      std::vector<AppendRun> runs;
-      std::vector<std::int32_t> idx, slots;
-      for (const G& g : groups) {
-        const Waves::Event& e = W.evs[static_cast<std::size_t>(W.ops[static_cast<std::size_t>(g.op)].ev)];
-        runs.push_back({g.slot, static_cast<std::int32_t>(idx.size()), static_cast<std::int32_t>(g.rows.size()), 0});
-        for (int r : g.rows) idx.push_back(static_cast<std::int32_t>(e.row0 + r));
-        slots.push_back(g.slot);
-      }
-      for (auto& ps : pending_stats) {  // seeds
-        Waves::Leaf& lf = W.leaves[static_cast<std::size_t>(ps.first)];
-        const Waves::Event& e = W.evs[static_cast<std::size_t>(ps.second)];
-        lf.slot = take_slot();
-        runs.push_back({lf.slot, static_cast<std::int32_t>(idx.size()), 1, 0});
-        idx.push_back(static_cast<std::int32_t>(e.row0));
-        slots.push_back(lf.slot);
-        W.dom[static_cast<std::size_t>(e.layer)].taken.push_back(lf.slot);
-      }
-      pending_stats.clear();
-      std::vector<double> vars(runs.size());
-      if (!runs.empty()) {
-        W.up.reset();
-        const std::size_t o_r = W.up.add(runs.data(), runs.size() * sizeof(AppendRun));
-        const std::size_t o_i = W.up.add(idx.data(), idx.size() * 4);
-        const std::size_t o_s = W.up.add(slots.data(), slots.size() * 4);
-        std::uint8_t* db = W.up.send(st_);
-        launches_ += launch_exact_stats(t_, reinterpret_cast<const AppendRun*>(db + o_r), static_cast<std::int32_t>(runs.size()),
-                                        reinterpret_cast<const std::int32_t*>(db + o_i), W.stage_k.p, st_);
-        W.km_out.ensure(runs.size() * 8 + 64, st_);
-        launches_ += launch_read_vars(t_, reinterpret_cast<const std::int32_t*>(db + o_s), static_cast<std::int32_t>(slots.size()),
-                                      W.km_out.as<double>(), st_);
-        W.h_out.ensure(runs.size() * 8, st_);
-        KVC_CUDA(cudaMemcpyAsync(W.h_out.p, W.km_out.p, runs.size() * 8, cudaMemcpyDeviceToHost, st_));
-        sync();
-        std::memcpy(vars.data(), W.h_out.p, runs.size() * 8);
-      }
-      // recursion decisions (maintainer.cpp:228-238), in group order per op
-      for (std::size_t gi = 0; gi < groups.size(); ++gi) {
-        G& g = groups[gi];
-        const int o_ev = W.ops[static_cast<std::size_t>(g.op)].ev, o_depth = W.ops[static_cast<std::size_t>(g.op)].depth;
-        const Waves::Event& e = W.evs[static_cast<std::size_t>(o_ev)];
-        const std::int64_t sz = static_cast<std::int64_t>(g.rows.size());
-        if (o_depth + 1 < cfg_.max_split_depth && sz >= 2 && vars[gi] > tau_at(sz, cfg_)) {
-          free_slots_.push_back(g.slot);  // no pages were attached
-          Waves::Op c;
-          c.ev = o_ev;
-          c.depth = o_depth + 1;
-          c.rows = std::move(g.rows);
-          W.ops.push_back(std::move(c));
-          W.ops[static_cast<std::size_t>(g.op)].kids[g.g] = static_cast<int>(W.ops.size()) - 1;
-        } else {
-          Waves::Leaf lf;
-          lf.rows = std::move(g.rows);
-          lf.slot = g.slot;
-          W.leaves.push_back(std::move(lf));
-          W.ops[static_cast<std::size_t>(g.op)].kids[g.g] = leaf_code(static_cast<int>(W.leaves.size()) - 1);
-          W.dom[static_cast<std::size_t>(e.layer)].taken.push_back(g.slot);
+        {
+          const Waves::Op& o = W.ops[static_cast<std::size_t>(oi)];
+          for (std::size_t i = 0; i < o.rows.size(); ++i) g2[o.assign[i]].push_back(o.rows[i]);
+        }
+        for (int g = 0; g < 2; ++g) {
+          if (g2[g].empty()) {
+            free_slots_.push_back(J.slot[g]);
+            continue;
+          }
+          const std::int64_t sz = static_cast<std::int64_t>(g2[g].size());
+          if (o_depth + 1 < cfg_.max_split_depth && sz >= 2 && J.var[g] > tau_at(sz, cfg_)) {
+            free_slots_.push_back(J.slot[g]);  // no pages were attached
+            Waves::Op c;
+            c.ev = o_ev;
+            c.depth = o_depth + 1;
+            c.rows = std::move(g2[g]);
+            W.ops.push_back(std::move(c));
+            W.ops[static_cast<std::size_t>(oi)].kids[g] = static_cast<int>(W.ops.size()) - 1;
+          } else {
+            Waves::Leaf lf;
+            lf.rows = std::move(g2[g]);
+            lf.slot = J.slot[g];
+            W.leaves.push_back(std::move(lf));
+            W.ops[static_cast<std::size_t>(oi)].kids[g] = leaf_code(static_cast<int>(W.leaves.size()) - 1);
+            W.dom[static_cast<std::size_t>(layer)].taken.push_back(J.slot[g]);
+          }
         }
       }
       // children to run: push kid 1 first so kid 0 (its subtree) runs first (preorder)

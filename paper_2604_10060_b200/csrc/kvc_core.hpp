@@ -367,8 +367,13 @@ struct SplitJob {
   double* objective;
   double uni;
   int32_t n, first;
+  // wave engine: group g's Eq. 1/2 statistics installed into slot[g] (>= 0) and its variance
+  // written to var_out[g]; assign_in (non-null): no k-means, these labels
+  int32_t slot[2];
+  double* var_out;
+  const int32_t* assign_in;
 };
-int launch_split_two_batch(const SplitJob* jobs, int n_jobs, int d, cudaStream_t st);
+int launch_split_two_batch(const DevTables& t, const SplitJob* jobs, int n_jobs, int d, cudaStream_t st);
 
 // ---- ingest wave engine (waves.cu, context_waves.cpp)
 // Staging of a slot's members (then its buffer when with_buf) and/or one frame row at row0.

@@ -98,6 +98,20 @@ __device__ __forceinline__ void cosines(const double* __restrict__ ut, int n, in
   }
 }
 
+// Sequential sum s + x[0] + x[1] + ... (exact order) with the shared-memory loads issued 8 ahead.
+__device__ __forceinline__ double seq_sum8(double s, const double* x, int m) {
+  int k = 0;
+  for (; k + 8 <= m; k += 8) {
+    double v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = x[k + j];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) s = dadd(s, v[j]);
+  }
+  for (; k < m; ++k) s = dadd(s, x[k]);
+  return s;
+}
+
 __device__ __forceinline__ void centroid_norms(SplitSmem& S, int d) {
   if (threadIdx.x < 2) {
     const double* c = S.cent[threadIdx.x];
@@ -115,6 +129,7 @@ __device__ __forceinline__ void split_two_body(const float* rows, const int32_t*
                                                double* objective) {
   __shared__ SplitSmem S;
   __shared__ double S_ob[OBJ_CHUNK];
+  __shared__ double S_mass;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   double* u = scratch;
   double* ut = u + static_cast<int64_t>(n) * d;
@@ -169,28 +184,47 @@ __device__ __forceinline__ void split_two_body(const float* rows, const int32_t*
   __syncthreads();
   for (int i = tid; i < n; i += SPT) nearv[i] = dot_col(ut, n, i, S.cent[0], d);
   __syncthreads();
+  // The seeding's two sequential sums over the points (the mass, then the weighted scan) run on
+  // one thread; the weights are staged in shared memory (the chosen point's weight 0.0: adding
+  // +0.0 to a sum of non-negative terms is exact, the same as skipping it) and read 8 at a time
+  // ahead of the dependent adds.
+  double mass = 0.0;
+  for (int base = 0; base < n; base += OBJ_CHUNK) {
+    const int m = min(OBJ_CHUNK, n - base);
+    for (int k = tid; k < m; k += SPT) S_ob[k] = base + k == first ? 0.0 : fmax(0.0, dsub(1.0, nearv[base + k]));
+    __syncthreads();
+    if (tid == 0) mass = seq_sum8(mass, S_ob, m);
+    __syncthreads();
+  }
   if (tid == 0) {
-    double mass = 0.0;
-    for (int i = 0; i < n; ++i)
-      if (i != first) mass = dadd(mass, fmax(0.0, dsub(1.0, nearv[i])));
-    int pick = n;
-    if (mass > 1e-15) {
-      const double target = dmul(uni, mass);
-      double run = 0.0;
-      for (int i = 0; i < n; ++i) {
-        if (i == first) continue;
-        run = dadd(run, fmax(0.0, dsub(1.0, nearv[i])));
-        if (run >= target) {
-          pick = i;
-          break;
-        }
-      }
-    }
-    if (pick == n) pick = first == 0 ? 1 : 0;
-    S.pick = pick;
+    S.pick = n;
     S.prev = -INFINITY;
     S.stop = 0;
+    S_mass = mass;
   }
+  __syncthreads();
+  if (S_mass > 1e-15) {
+    const double target = dmul(uni, S_mass);
+    double run = 0.0;
+    for (int base = 0; base < n; base += OBJ_CHUNK) {
+      const int m = min(OBJ_CHUNK, n - base);
+      for (int k = tid; k < m; k += SPT) S_ob[k] = base + k == first ? 0.0 : fmax(0.0, dsub(1.0, nearv[base + k]));
+      __syncthreads();
+      if (tid == 0 && S.pick == n) {
+        for (int k = 0; k < m; ++k) {
+          if (base + k == first) continue;
+          run = dadd(run, S_ob[k]);
+          if (run >= target) {
+            S.pick = base + k;
+            break;
+          }
+        }
+      }
+      __syncthreads();
+      if (S.pick != n) break;
+    }
+  }
+  if (tid == 0 && S.pick == n) S.pick = first == 0 ? 1 : 0;
   __syncthreads();
   for (int c = tid; c < d; c += SPT) S.cent[1][c] = u[static_cast<int64_t>(S.pick) * d + c];
   for (int i = tid; i < n; i += SPT) assign[i] = 0;
@@ -302,8 +336,7 @@ __device__ __forceinline__ void split_two_body(const float* rows, const int32_t*
       const int m = min(OBJ_CHUNK, n - base);
       for (int k = tid; k < m; k += SPT) S_ob[k] = sc[static_cast<int64_t>(assign[base + k]) * n + base + k];
       __syncthreads();
-      if (tid == 0)
-        for (int k = 0; k < m; ++k) obj = dadd(obj, S_ob[k]);
+      if (tid == 0) obj = seq_sum8(obj, S_ob, m);
       __syncthreads();
     }
     if (tid == 0) {
@@ -318,11 +351,17 @@ __device__ __forceinline__ void split_two_body(const float* rows, const int32_t*
   }
   // compact ids (clustering.cpp:166-177)
   if (tid == 0) {
-    int c[2] = {0, 0};
-    for (int i = 0; i < n; ++i) c[assign[i]] += 1;
-    S.cnt[0] = c[0];
-    S.cnt[1] = c[1];
+    S.cnt[0] = 0;
+    S.cnt[1] = 0;
   }
+  __syncthreads();
+  {
+    int c1 = 0;
+    for (int i = tid; i < n; i += SPT) c1 += assign[i];
+    if (c1) atomicAdd(&S.cnt[1], c1);
+  }
+  __syncthreads();
+  if (tid == 0) S.cnt[0] = n - S.cnt[1];
   __syncthreads();
   const int live0 = S.cnt[0] != 0, live1 = S.cnt[1] != 0;
   if (!live0)
@@ -340,18 +379,132 @@ __global__ void __launch_bounds__(SPT) k_split_two(const float* rows, const int3
   split_two_body(rows, idx, n, d, first, uni, scratch, assign, meta, objective);
 }
 
+// Eq. 1 / Eq. 2 statistics of the two groups of a split (compute_representative /
+// compute_variance, index.cpp:345-362, exactly as k_exact_stats computes them: sums over the
+// group's rows in pool order, fp64, round-to-nearest, uncontracted) into slots slot[0] / slot[1]
+// (rep64, rep32, rnorm, var), and the variances to var_out (the host's Eq. 5 recursion test).
+// memb: n ints of scratch.
+__device__ void child_stats(const DevTables& t, const float* rows, const int32_t* idx, int n, const int32_t* assign,
+                            const int32_t slot[2], double* var_out, int* memb, double* sq) {
+  __shared__ double srep[2][256];
+  __shared__ int scnt[2];
+  __shared__ double sinv[2];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, d = t.d;
+  // member lists in pool order (warp g scans group g with ballots)
+  if (warp < 2) {
+    int w = 0;
+    if (warp == 1) {  // group 1 starts after group 0's count
+      for (int base = 0; base < n; base += 32) {
+        const int i = base + lane;
+        w += __popc(__ballot_sync(0xffffffffu, i < n && assign[i] == 0));
+      }
+    }
+    const int start = w;
+    for (int base = 0; base < n; base += 32) {
+      const int i = base + lane;
+      const bool m = i < n && assign[i] == warp;
+      const unsigned bal = __ballot_sync(0xffffffffu, m);
+      if (m) memb[w + __popc(bal & ((1u << lane) - 1u))] = i;
+      w += __popc(bal);
+    }
+    if (lane == 0) scnt[warp] = w - start;
+  }
+  __syncthreads();
+  const int c0 = scnt[0], c1 = scnt[1];
+  if (tid < 2) sinv[tid] = (tid == 0 ? c0 : c1) > 0 ? ddiv(1.0, static_cast<double>(tid == 0 ? c0 : c1)) : 0.0;
+  __syncthreads();
+  // representatives: one (group, dim) chain per thread over the group's rows, 16 loads ahead
+  if (tid < 2 * d) {
+    const int g = tid / d, c = tid - g * d;
+    const int mb = g == 0 ? 0 : c0, me = g == 0 ? c0 : c0 + c1;
+    double acc = 0.0;
+    const int m16 = mb + ((me - mb) & ~15);
+    float x[16];
+    auto load16 = [&](int m) {
+#pragma unroll
+      for (int k = 0; k < 16; ++k) x[k] = rows[static_cast<int64_t>(idx[memb[m + k]]) * d + c];
+    };
+    if (m16 > mb) load16(mb);
+    for (int m = mb; m < m16; m += 16) {
+      float y[16];
+#pragma unroll
+      for (int k = 0; k < 16; ++k) y[k] = x[k];
+      if (m + 16 < m16) load16(m + 16);
+#pragma unroll
+      for (int k = 0; k < 16; ++k) acc = dadd(acc, static_cast<double>(y[k]));
+    }
+    for (int m = m16; m < me; ++m) acc = dadd(acc, static_cast<double>(rows[static_cast<int64_t>(idx[memb[m]]) * d + c]));
+    const double r = dmul(acc, sinv[g]);
+    srep[g][c] = r;
+    if (me > mb && slot[g] >= 0) {
+      t.rep64[static_cast<int64_t>(slot[g]) * d + c] = r;
+      t.rep32[static_cast<int64_t>(slot[g]) * d + c] = static_cast<float>(r);
+    }
+  }
+  __syncthreads();
+  // squared distances per row (sequential over the dimension), in member order
+  for (int m = tid; m < c0 + c1; m += blockDim.x) {
+    const int g = m < c0 ? 0 : 1;
+    const float* p = rows + static_cast<int64_t>(idx[memb[m]]) * d;
+    double a = 0.0;
+    for (int c = 0; c < d; ++c) {
+      const double df = dsub(static_cast<double>(p[c]), srep[g][c]);
+      a = dadd(a, dmul(df, df));
+    }
+    sq[m] = a;
+  }
+  __syncthreads();
+  // sequential sums over the rows (one thread per group), the norm of the representative
+  if (tid == 0 || tid == 32) {
+    const int g = tid == 0 ? 0 : 1;
+    const int mb = g == 0 ? 0 : c0, me = g == 0 ? c0 : c0 + c1;
+    if (me > mb) {
+      double total = 0.0;
+      for (int m = mb; m < me; ++m) total = dadd(total, sq[m]);
+      const double var = ddiv(total, static_cast<double>(me - mb));
+      double nn = 0.0;
+      for (int c = 0; c < d; ++c) nn = dadd(nn, dmul(srep[g][c], srep[g][c]));
+      if (slot[g] >= 0) {
+        t.var[slot[g]] = var;
+        t.rnorm[slot[g]] = __dsqrt_rn(nn);
+      }
+      if (var_out) var_out[g] = var;
+    } else if (var_out) {
+      var_out[g] = 0.0;
+    }
+  }
+}
+
 // Independent splits in one launch (one CTA each): the ingest wave engine settles the split
-// events of many domains at once (context_waves.cpp).
-__global__ void __launch_bounds__(SPT) k_split_two_batch(const SplitJob* jobs, int d) {
+// events of many domains at once (context_waves.cpp). A job with slots also installs its two
+// groups' statistics; a job with assign_in skips the k-means (a result already known).
+__global__ void __launch_bounds__(SPT) k_split_two_batch(DevTables t, const SplitJob* jobs, int d) {
   const SplitJob j = jobs[blockIdx.x];
-  split_two_body(j.rows, j.idx, j.n, d, j.first, j.uni, j.scratch, j.assign, j.meta, j.objective);
+  if (j.assign_in) {
+    for (int i = threadIdx.x; i < j.n; i += SPT) j.assign[i] = j.assign_in[i];
+    if (threadIdx.x == 0) {
+      j.meta[0] = 2;
+      j.meta[1] = 0;
+      j.meta[2] = 0;
+      j.meta[3] = 0;
+    }
+    __syncthreads();
+  } else {
+    split_two_body(j.rows, j.idx, j.n, d, j.first, j.uni, j.scratch, j.assign, j.meta, j.objective);
+    __syncthreads();
+    if (j.meta[3] != 0) return;  // degenerate row: the host raises it
+  }
+  if (j.slot[0] < 0 && j.slot[1] < 0 && !j.var_out) return;
+  int* memb = reinterpret_cast<int*>(j.scratch);
+  double* sq = j.scratch + (static_cast<int64_t>(j.n) + 1) / 2 + 1;
+  child_stats(t, j.rows, j.idx, j.n, j.assign, j.slot, j.var_out, memb, sq);
 }
 
 }  // namespace
 
-int launch_split_two_batch(const SplitJob* jobs, int n_jobs, int d, cudaStream_t st) {
+int launch_split_two_batch(const DevTables& t, const SplitJob* jobs, int n_jobs, int d, cudaStream_t st) {
   if (n_jobs <= 0 || d > 256) return 0;
-  k_split_two_batch<<<n_jobs, SPT, 0, st>>>(jobs, d);
+  k_split_two_batch<<<n_jobs, SPT, 0, st>>>(t, jobs, d);
   return 1;
 }
 
