@@ -356,6 +356,9 @@ KVC_API int kvc_host_kmeans(const float* pts, int32_t n, int32_t d, int32_t k, i
                             uint64_t seed, int32_t* assign, double* objective, int32_t* iterations);
 KVC_API double kvc_host_tau(int64_t n, double tau_min, double tau_max, double n0);
 KVC_API uint64_t kvc_host_mix_seed(uint64_t a, uint64_t b);
+/* Test hook: the first two outputs of mt19937_64(seed) from the wave engine's shortcut (fast2)
+ * and from std::mt19937_64 (std2). */
+KVC_API void kvc_host_rng_first2(uint64_t seed, uint64_t* fast2, uint64_t* std2);
 /* Instrumentation: mean clock64 cycles per phase of the last resolve launch (out[16]; with
  * out[0] < 0 on entry: of the last decode's score/select kernel, first 8 entries). */
 /* Device self-check of the reciprocal-based correctly rounded division used on the resolve

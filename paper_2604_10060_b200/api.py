@@ -174,6 +174,8 @@ def lib():
         L.kvc_host_tau.argtypes = [C.c_int64, C.c_double, C.c_double, C.c_double]
         L.kvc_host_mix_seed.restype = C.c_uint64
         L.kvc_host_mix_seed.argtypes = [C.c_uint64, C.c_uint64]
+        L.kvc_host_rng_first2.argtypes = [C.c_uint64, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]
+        L.kvc_host_rng_first2.restype = None
         _lib = L
     return _lib
 
@@ -188,7 +190,7 @@ EXPORTED = [
     "kvc_ledger_log_size", "kvc_ledger_op", "kvc_check", "kvc_offload", "kvc_fetch",
     "kvc_launch_count", "kvc_last_step_timing", "kvc_set_timing", "kvc_last_ingest_timing",
     "kvc_debug_resolve_profile", "kvc_host_split_two", "kvc_host_kmeans", "kvc_host_tau",
-    "kvc_host_mix_seed", "kvc_debug_div_check", "kvc_debug_assign_check", "kvc_tier_sync",
+    "kvc_host_mix_seed", "kvc_host_rng_first2", "kvc_debug_div_check", "kvc_debug_assign_check", "kvc_tier_sync",
     "kvc_tier_stats", "kvc_cluster_tier", "kvc_debug_tier_check", "kvc_debug_split_two", "kvc_debug_kmeans", "kvc_exchange_bytes", "kvc_ipc_alloc",
     "kvc_ipc_open", "kvc_ipc_close", "kvc_ipc_free", "kvc_set_peers", "kvc_peer_output",
     "kvc_debug_event_profile", "kvc_debug_wave_profile", "kvc_add_partition", "kvc_append_frame", "kvc_add_cluster", "kvc_adopt",

@@ -750,4 +750,11 @@ double kvc_host_tau(int64_t n, double tau_min, double tau_max, double n0) {
 
 uint64_t kvc_host_mix_seed(uint64_t a, uint64_t b) { return kvc::mix_seed(a, b); }
 
+void kvc_host_rng_first2(uint64_t seed, uint64_t* fast2, uint64_t* std2) {
+  kvc::mt64_first2(seed, fast2);
+  kvc::Rng64 r(seed);
+  std2[0] = r.u64();
+  std2[1] = r.u64();
+}
+
 }  // extern "C"

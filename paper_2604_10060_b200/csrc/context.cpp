@@ -299,6 +299,8 @@ void Context::alloc_device() {
     waves_perturb_ = wp && std::string(wp) == "1";
     const char* wl = std::getenv("KVC_WAVES_LOG");
     waves_log_ = wl && std::string(wl) == "1";
+    const char* we = std::getenv("KVC_WAVES_EAGER");
+    waves_eager_ = we && std::string(we) == "1";
     const char* ss = std::getenv("KVC_SPEC_SPLIT");  // 0: no speculative split k-means
     spec_split_ = !(ss && std::string(ss) == "0");
     const char* g = std::getenv("KVC_ASSIGN");  // "simt": the fp32 CUDA-core tile

@@ -543,7 +543,8 @@ class Context {
   Waves* wv_ = nullptr;
   bool waves_ = true;
   bool waves_perturb_ = false;
-  bool waves_log_ = false;  // KVC_WAVES_LOG=1: per-frame pass / rollback lines on stderr  // KVC_WAVES_PERTURB=1: first-pass counter predictions made wrong (tests)
+  bool waves_log_ = false;
+  bool waves_eager_ = false;  // KVC_WAVES_EAGER=1: validation sweep predicts through restarted domains  // KVC_WAVES_LOG=1: per-frame pass / rollback lines on stderr  // KVC_WAVES_PERTURB=1: first-pass counter predictions made wrong (tests)
   void run_inserts_waves(std::int64_t frame_id, std::int64_t pid, int T, std::int64_t* assigned, bool launched);
   void replay_runs(int l, std::int64_t frame_id, int T, int t0, int t1, std::int64_t* assigned);
   void waves_free();

@@ -188,6 +188,7 @@ struct Context::Waves {
     int ops = 0, prev_ops = -1;
     std::uint64_t epoch = 0;
     bool tie = false;  // a relaunch decision of this pass was an exact tie broken by the id key
+    bool restarted = false;  // rolled back and not finished since (its event count is uncertain)
   };
   std::vector<Op> ops;
   std::vector<Leaf> leaves;
@@ -381,6 +382,7 @@ void Context::run_inserts_waves(std::int64_t frame_id, std::int64_t pid, int T, 
     count_outcome(l, D.cur, std::min(stop, T));
     if (stop >= T) {
       D.done = true;
+      D.restarted = false;
       D.cur = T;
       return;
     }
@@ -532,10 +534,11 @@ void Context::run_inserts_waves(std::int64_t frame_id, std::int64_t pid, int T, 
       X.slot[1] = J.slot[1];
       X.var_out = (J.want_var || J.slot[0] >= 0 || J.slot[1] >= 0) ? W.km_out.as<double>(var_off) + 2 * j : nullptr;
       X.assign_in = J.given ? reinterpret_cast<const std::int32_t*>(dbase + o_giv) + giv_off[j] : nullptr;
-      if (!J.given) {
-        Rng64 rng(mix_seed(maint_seed_, J.ctr));
-        X.first = static_cast<std::int32_t>(rng.index(static_cast<std::size_t>(n)));
-        X.uni = rng.uniform();
+      if (!J.given) {  // Rng64::index then Rng64::uniform (rng.hpp:14-44) from the first two draws
+        std::uint64_t r2[2];
+        mt64_first2(mix_seed(maint_seed_, J.ctr), r2);
+        X.first = static_cast<std::int32_t>(r2[0] % static_cast<std::uint64_t>(n));
+        X.uni = static_cast<double>(r2[1] >> 11) * 0x1.0p-53;
       } else {
         X.first = 0;
         X.uni = 0.0;
@@ -546,6 +549,18 @@ void Context::run_inserts_waves(std::int64_t frame_id, std::int64_t pid, int T, 
     W.h_out.ensure(obj_off, st_);
     KVC_CUDA(cudaMemcpyAsync(W.h_out.p, dout, obj_off, cudaMemcpyDeviceToHost, st_));
     sync();
+    if (waves_log_) {
+      std::size_t nmax = 0, nsum = 0;
+      int itmax = 0;
+      for (std::size_t j = 0; j < nj; ++j) {
+        const std::size_t n = jobs[j].op >= 0 ? W.ops[static_cast<std::size_t>(jobs[j].op)].rows.size() : 1;
+        nmax = std::max(nmax, n);
+        nsum += n;
+        itmax = std::max(itmax, W.h_out.as<std::int32_t>()[out_off[j] + n + 1]);
+      }
+      std::fprintf(stderr, "[waves] jobs %zu rows max %zu mean %.0f iters max %d: %.0f us\n", nj, nmax,
+                   static_cast<double>(nsum) / static_cast<double>(nj), itmax, us(k0, clk::now()));
+    }
     for (std::size_t j = 0; j < nj; ++j) {
       Job& J = jobs[j];
       const std::size_t n = J.op >= 0 ? W.ops[static_cast<std::size_t>(J.op)].rows.size() : 1;
@@ -635,6 +650,7 @@ void Context::run_inserts_waves(std::int64_t frame_id, std::int64_t pid, int T, 
       D.events.clear();
       D.taken.clear();
       D.tie = false;
+      D.restarted = true;
       D.pl = host_slots(l);
       D.epoch = W.epoch_next++;
       D.cur = D.first_tok;
@@ -662,16 +678,21 @@ void Context::run_inserts_waves(std::int64_t frame_id, std::int64_t pid, int T, 
       // (recomputed and, if its result changes, restarted) without waiting for the domains before
       // it to finish; the final sweep, with every domain finished, is exact
       std::uint64_t c = ctr_base;
+      bool uncertain = false;
       for (int l = 0; l < L_; ++l) {
         const Waves::Dom& D = W.dom[static_cast<std::size_t>(l)];
         if (!D.active) continue;
         if (!D.done) {
           any_undone = true;
+          // past a restarted domain the counters move with its new event count: wait for it
+          // (KVC_WAVES_EAGER=1 predicts through it as through any unfinished domain)
+          if (D.restarted && !waves_eager_) uncertain = true;
           std::int64_t left = D.pend_valid && D.pend_kind == EV_SPLIT ? 1 : 0;
           if (D.cur_ev >= 0) left += static_cast<std::int64_t>(W.evs[static_cast<std::size_t>(D.cur_ev)].stack.size());
           c += static_cast<std::uint64_t>(std::max<std::int64_t>(D.ops + left, D.prev_ops));
           continue;
         }
+        if (uncertain) continue;
         first_ctr[static_cast<std::size_t>(l)] = c;
         for (int ei : D.events)
           for (int oi : W.evs[static_cast<std::size_t>(ei)].ops) {
@@ -999,6 +1020,7 @@ void Context::run_inserts_waves(std::int64_t frame_id, std::int64_t pid, int T, 
       D.cur_ev = -1;
       if (D.cur >= T) {
         D.done = true;
+        D.restarted = false;
       } else {
         relaunch.push_back(e.layer);
         rcur.push_back(D.cur);

@@ -9,6 +9,23 @@
 
 namespace kvc {
 
+void mt64_first2(std::uint64_t seed, std::uint64_t out[2]) {
+  constexpr std::uint64_t kF = 6364136223846793005ULL, kA = 0xB5026F5AA96619E9ULL;
+  constexpr std::uint64_t kUpper = 0xFFFFFFFF80000000ULL, kLower = 0x7FFFFFFFULL;
+  std::uint64_t x[158];
+  x[0] = seed;
+  for (std::uint64_t i = 1; i < 158; ++i) x[i] = kF * (x[i - 1] ^ (x[i - 1] >> 62)) + i;
+  for (int i = 0; i < 2; ++i) {
+    const std::uint64_t y = (x[i] & kUpper) | (x[i + 1] & kLower);
+    std::uint64_t z = x[i + 156] ^ (y >> 1) ^ ((y & 1ULL) ? kA : 0ULL);
+    z ^= (z >> 29) & 0x5555555555555555ULL;
+    z ^= (z << 17) & 0x71D67FFFEDA60000ULL;
+    z ^= (z << 37) & 0xFFF7EEE000000000ULL;
+    z ^= z >> 43;
+    out[i] = z;
+  }
+}
+
 std::uint64_t mix_seed(std::uint64_t a, std::uint64_t b) {
   std::uint64_t z = a + 0x9e3779b97f4a7c15ULL * (b + 1);
   z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;

@@ -31,6 +31,13 @@ class Rng64 {  // rng.hpp:14-44 semantics
 
 std::uint64_t mix_seed(std::uint64_t a, std::uint64_t b);  // rng.hpp:47-52
 
+// The first two outputs of std::mt19937_64(seed) without building the whole 312-word state: the
+// first twist step of words 0 and 1 reads only words 0..2 and 156..157 of the seeded state. A
+// split's k-means++ makes exactly two draws (the first centre's index, then the uniform), so the
+// wave engine derives them from this (equal to Rng64's by construction; checked against
+// std::mt19937_64 in tests/test_host_abi.py through kvc_host_rng_first2).
+void mt64_first2(std::uint64_t seed, std::uint64_t out[2]);
+
 // fp64 sequential kernels (vecmath.hpp:27-51)
 double dot_fd(const float* a, const double* b, int d);
 double dot_dd(const double* a, const double* b, int d);

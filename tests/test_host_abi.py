@@ -59,6 +59,21 @@ def test_host_tau_and_mix_seed_match_reference(ref_lib):
         assert lib.kvc_host_mix_seed(a, b) == ref_lib.ref_prim_mix_seed(a, b)
 
 
+def test_mt64_first_two_draws_shortcut():
+    """The wave engine's k-means++ draws (kmeans.cpp mt64_first2) equal std::mt19937_64's first two
+    outputs for the seeds mix_seed produces."""
+    import ctypes as C
+
+    lib = api.lib()
+    rng = np.random.default_rng(5)
+    seeds = [0, 1, 5489, 2**64 - 1] + [int(x) for x in rng.integers(0, 2**63, 200, dtype=np.int64)]
+    seeds += [lib.kvc_host_mix_seed(42, c) for c in range(200)]
+    f, r = (C.c_uint64 * 2)(), (C.c_uint64 * 2)()
+    for sd in seeds:
+        lib.kvc_host_rng_first2(sd, f, r)
+        assert list(f) == list(r), sd
+
+
 @pytest.mark.parametrize("n,d,seed", [(2, 8, 1), (3, 16, 2), (50, 32, 3), (400, 128, 4), (1000, 64, 5)])
 def test_split_two_bit_exact(ref_lib, n, d, seed):
     """The split slow path (maintainer.cpp:195-242 -> clustering.cpp:180-208)."""
