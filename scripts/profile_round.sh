@@ -24,7 +24,7 @@ timeout 1200 ncu --set full --clock-control none --import-source on \
   -k regex:"k_(resolve_spec|assign_tc)" -s 12 -c 2 -o "$OUT/full_ingest" \
   python bench.py --steps 5 --warmup 3 --frames 5 --no-cpu-baseline --no-offload --no-streams --no-config4 > "$OUT/ncu_full_ingest.log" 2>&1
 timeout 1200 ncu --set full --clock-control none --import-source on \
-  -k regex:"k_(resolve|split_two)$" -s 30 -c 2 -o "$OUT/full_drift" \
+  -k regex:"k_(resolve|split_two_batch)$" -s 30 -c 3 -o "$OUT/full_drift" \
   python scripts/drift_profile.py 16 8 > "$OUT/ncu_full_drift.log" 2>&1
 DRIFT_TIMING=1 timeout 600 python scripts/drift_profile.py 112 12 > "$OUT/drift_profile.json" 2>&1
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"k_tok_(approx|select|gather)|k_attend" -c 40 --csv \

@@ -99,13 +99,13 @@ lines += ["", "## `ncu --set full` captures", "",
           "| kernel | duration us | DRAM read MB | DRAM write MB | DRAM % peak | SM % | tensor pipe % | achieved occupancy | regs |",
           "|---|---|---|---|---|---|---|---|---|"]
 att = {}
-for kname in ("k_attend", "k_select3", "k_score_select", "k_resolve_spec", "k_assign_tc", "k_approx",
-              "k_topm", "k_split_two", "k_kmeans"):
+for kname in ("k_attend", "k_select3", "k_score_select", "k_resolve_spec", "k_resolve\\(", "k_assign_tc", "k_approx",
+              "k_topm", "k_split_two_batch", "k_split_two\\(", "k_kmeans"):
     for m in ncu_raw(kname)[:1]:
         dur = num(m.get("gpu__time_duration.sum"))
         rd = num(m.get("dram__bytes_read.sum"))
         wr = num(m.get("dram__bytes_write.sum"))
-        lines.append(f"| {kname} | {dur} | {rd} | {wr} | {m.get('gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed')} | "
+        lines.append(f"| {kname.replace(chr(92), '').replace('(', '')} | {dur} | {rd} | {wr} | {m.get('gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed')} | "
                      f"{m.get('sm__throughput.avg.pct_of_peak_sustained_elapsed')} | "
                      f"{m.get('sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed')} | "
                      f"{m.get('sm__warps_active.avg.pct_of_peak_sustained_active')} | {m.get('launch__registers_per_thread')} |")
@@ -132,6 +132,38 @@ for fn, title in (("split_time.txt", "GPU split k-means vs host (n, d, iteration
         shutil.copy(pth, os.path.join(dst, f"{tag}_{fn}"))
 if slow:
     lines += ["", "## Maintenance and build slow paths on the GPU"] + slow
+# the round's bench lines, test logs and drift-regime wave-engine profile travel with the summary
+for fn in ("bench.json", "bench_reference.json", "pytest_gpu.txt", "smoke.txt", "drift_profile.json", "gpu.txt",
+           "cpu.txt"):
+    pth = os.path.join(src, fn)
+    if os.path.exists(pth):
+        shutil.copy(pth, os.path.join(dst, f"{tag}_{fn}"))
+dp = os.path.join(src, "drift_profile.json")
+if os.path.exists(dp):
+    try:
+        d = json.loads(open(dp).read().strip().splitlines()[-1])
+        wp = d.get("wave_profile", {})
+        fr = max(1.0, wp.get("frames_with_events", 1.0))
+        lines += ["", "## Drift-regime ingest (112 domains, scripts/drift_profile.py): wave engine", "",
+                  f"{d['frames']} frames, {d['ms_per_frame']} ms per frame (wall, incl. host replay).", "",
+                  "| per frame with events | value |", "|---|---|"]
+        for k in ("waves", "rolled_back_domains", "verify_kmeans", "events", "kmeans_jobs", "verified_swapped"):
+            if k in wp:
+                lines.append(f"| {k} | {wp[k] / fr:.1f} |")
+        for k in ("stage_us", "kmeans_us", "install_us", "relaunch_us", "verify_commit_us"):
+            if k in wp:
+                lines.append(f"| {k} | {wp[k] / fr:.0f} |")
+    except Exception as e:  # keep the summary even if the profile line is malformed
+        lines += ["", f"(drift profile unreadable: {e})"]
+san = os.path.join(ROOT, "gpurun_out", f"{tag}_san")
+if os.path.isdir(san):
+    sl = ["", "## compute-sanitizer (scripts/sanitize.sh)", "", "| run | summary |", "|---|---|"]
+    for fn in sorted(os.listdir(san)):
+        body = open(os.path.join(san, fn)).read().splitlines()
+        summ = [x.replace("========= ", "") for x in body if "SUMMARY" in x or x.startswith("racecheck") or
+                x.startswith("memcheck") or x.startswith("synccheck")]
+        sl.append(f"| {fn} | {'; '.join(summ)} |")
+    lines += sl
 lines.append("")
 with open(os.path.join(dst, f"{tag}_summary.md"), "w") as f:
     f.write("\n".join(lines) + "\n")
