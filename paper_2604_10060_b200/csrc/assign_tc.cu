@@ -299,10 +299,46 @@ __global__ void __launch_bounds__(AS_THREADS, 1) k_assign_tc(DevTables t, Ingest
   // Exact fp64 cosines (vecmath.hpp:53-63) of the top-M entries that can decide the token's
   // arg-best: those within 2 margins of the best approximate score (the others are NaN = "not
   // computed"; the resolve kernels bound them by approx + margin instead). Keys come from the
-  // key tile in shared memory.
+  // key tile in shared memory; the fp64 representatives of the union of every token's needed
+  // candidates (a frame's tokens share few clusters) are staged once into shared memory (the B
+  // tiles are free after the last MMA), so the sequential dot chains read at shared-memory
+  // latency instead of one L2 round trip per step. Same operands, same order: same bits.
+  const float cut = tv[0] - 2.f * a.margin;
+  __shared__ int s_nx;
+  int* mark = reinterpret_cast<int*>(sBh);  // [n] candidate -> staged row (or -1)
+  const int xs = d + 1;                     // odd row stride (doubles): rows spread over the banks
+  const int mark_bytes = (cmax * 4 + 15) & ~15;
+  double* xrows = reinterpret_cast<double*>(sBh + mark_bytes);
+  const int xcap = (2 * KH * NCH * 128 - mark_bytes) / (xs * 8);
+  for (int c = tid; c < n; c += AS_THREADS) mark[c] = 0;
+  __syncthreads();
+  if (tok_ok)
+#pragma unroll
+    for (int k = 0; k < TOPM; ++k)
+      if (ti[k] >= 0 && (a.exact_all || tv[k] >= cut)) mark[ti[k]] = 1;
+  __syncthreads();
+  if (warp == 0) {  // compact: staged row index in candidate order
+    int nb = 0;
+    for (int c0 = 0; c0 < n; c0 += 32) {
+      const int c = c0 + lane;
+      const bool mk = c < n && mark[c] != 0;
+      const unsigned bal = __ballot_sync(0xffffffffu, mk);
+      if (c < n) mark[c] = mk ? nb + __popc(bal & ((1u << lane) - 1u)) : -1;
+      nb += __popc(bal);
+    }
+    if (lane == 0) s_nx = nb;
+  }
+  __syncthreads();
+  for (int c = warp; c < n; c += AS_THREADS / 32) {  // one warp per staged row, lanes over dims
+    const int x = mark[c];
+    if (x < 0 || x >= xcap) continue;
+    const int s = cs[c];
+    const double* src = (cbuf[c] ? t.brep64 : t.rep64) + static_cast<int64_t>(s) * d;
+    for (int i = lane; i < d; i += 32) xrows[x * xs + i] = src[i];
+  }
+  __syncthreads();
   if (tok_ok) {
     const int64_t o = static_cast<int64_t>(dom) * t.tmax + m;
-    const float cut = tv[0] - 2.f * a.margin;
     const double* rp[TOPM];
     double nr[TOPM];
 #pragma unroll
@@ -313,7 +349,8 @@ __global__ void __launch_bounds__(AS_THREADS, 1) k_assign_tc(DevTables t, Ingest
       if (c >= 0 && (a.exact_all || tv[k] >= cut)) {
         const int s = cs[c];
         const bool ib = cbuf[c];
-        rp[k] = (ib ? t.brep64 : t.rep64) + static_cast<int64_t>(s) * d;
+        const int x = mark[c];
+        rp[k] = x < xcap ? xrows + x * xs : (ib ? t.brep64 : t.rep64) + static_cast<int64_t>(s) * d;
         nr[k] = ib ? t.bnorm[s] : t.rnorm[s];
       }
     }
@@ -330,9 +367,9 @@ __global__ void __launch_bounds__(AS_THREADS, 1) k_assign_tc(DevTables t, Ingest
 #pragma unroll
       for (int k = 0; k < TOPM; ++k)
         if (rp[k]) {
-          const double2 r2 = __ldg(reinterpret_cast<const double2*>(rp[k] + i));
-          acc[k] = dadd(acc[k], dmul(x0, r2.x));
-          acc[k] = dadd(acc[k], dmul(x1, r2.y));
+          const double r0 = rp[k][i], r1 = rp[k][i + 1];  // shared (staged) or global (overflow)
+          acc[k] = dadd(acc[k], dmul(x0, r0));
+          acc[k] = dadd(acc[k], dmul(x1, r1));
         }
     }
     const double nk = __dsqrt_rn(sk);

@@ -206,19 +206,21 @@ __device__ __forceinline__ void split_two_body(const float* rows, const int32_t*
   if (S_mass > 1e-15) {
     const double target = dmul(uni, S_mass);
     double run = 0.0;
+    int pick = n;  // thread 0's scan state; S.pick is written once, when the pick is found
     for (int base = 0; base < n; base += OBJ_CHUNK) {
       const int m = min(OBJ_CHUNK, n - base);
       for (int k = tid; k < m; k += SPT) S_ob[k] = base + k == first ? 0.0 : fmax(0.0, dsub(1.0, nearv[base + k]));
       __syncthreads();
-      if (tid == 0 && S.pick == n) {
+      if (tid == 0) {
         for (int k = 0; k < m; ++k) {
           if (base + k == first) continue;
           run = dadd(run, S_ob[k]);
           if (run >= target) {
-            S.pick = base + k;
+            pick = base + k;
             break;
           }
         }
+        if (pick != n) S.pick = pick;
       }
       __syncthreads();
       if (S.pick != n) break;

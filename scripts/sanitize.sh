@@ -16,7 +16,7 @@ timeout 1800 $CS --tool racecheck --racecheck-report all --print-limit 50 \
   python -c "import __graft_entry__ as g; g.smoke()" > "$OUT/racecheck.txt" 2>&1
 echo "racecheck rc=$?" >> "$OUT/racecheck.txt"
 # the same without K6 (its mbarrier stage hand-off is outside racecheck's model): any hazard left is real
-timeout 1800 $CS --tool racecheck --racecheck-report all --print-limit 50 --kernel-name-exclude regex:k_attend \
+timeout 1800 $CS --tool racecheck --racecheck-report all --print-limit 50 --kernel-name-exclude kns=k_attend \
   python -c "import __graft_entry__ as g; g.smoke()" > "$OUT/racecheck_no_k6.txt" 2>&1
 echo "racecheck (k_attend excluded) rc=$?" >> "$OUT/racecheck_no_k6.txt"
 timeout 1800 $CS --tool synccheck --print-limit 50 \
