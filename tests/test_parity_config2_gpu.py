@@ -17,6 +17,10 @@ decode steps. Compared:
     variance / buffer_rep BITWISE and member lists (tests/harness.py compare_state).
 The `tiered` variant uses the reference cadence (horizon 16): the first new frame offloads every
 stale cluster to the physical pinned host tier and the decode steps fetch them back.
+
+The same slice runs at the two other per-domain shapes the bench times: config 3 (1-hour stream,
+705,600 tokens and C = 1,378 clusters per domain, tiered: the bench's `offload` phase) and config 5
+(one stream of 65,464 tokens and C = 128 per domain: the bench's `streams` phase).
 """
 import numpy as np
 import pytest
@@ -27,7 +31,12 @@ from tests.harness import compare_state, rel_err
 pytestmark = pytest.mark.gpu
 
 ATT_TOL = 1e-3
-D, N, C, T, HD, TOPK, W = 4, 669 * 196, 256, 196, 128, 16, 4
+D, T, HD, TOPK, W = 4, 196, 128, 16, 4
+SHAPES = {  # per-domain stream length (tokens) and clusters
+    "config2": (669 * 196, 256),
+    "config3": (3600 * 196, 1378),
+    "config5": (334 * 196, 128),
+}
 
 
 def _attend_oracle(q, K, V):
@@ -43,9 +52,13 @@ def _attend_oracle(q, K, V):
     return out
 
 
-@pytest.mark.parametrize("tiered", [False, True], ids=["resident", "tiered"])
-def test_config2_slice_matches_reference(ref_lib, tiered):
+@pytest.mark.parametrize("shape,tiered", [("config2", False), ("config2", True), ("config3", True),
+                                          ("config5", False)],
+                         ids=["resident", "tiered", "config3-tiered", "config5"])
+def test_config2_slice_matches_reference(ref_lib, shape, tiered):
     import torch
+
+    N, C = SHAPES[shape]
 
     from paper_2604_10060_b200 import ClusterKVCache, workload
     from tests.harness import product_config
@@ -59,6 +72,7 @@ def test_config2_slice_matches_reference(ref_lib, tiered):
     kv_bytes = D * (N + 64 * C + 64 * T) * HD * 2 * 2
     kv = ClusterKVCache(product_config(ecfg, kv_dtype=1, check_invariants=0, pool_bytes=int(1.6 * kv_bytes),
                                        max_slots=8 * D * C, max_cluster_pages=512, max_tokens=T,
+                                       max_candidates=2048 if C > 1024 else 1024,
                                        host_pool_bytes=int(1.3 * kv_bytes) if tiered else 1 << 20,
                                        tier_stage_pages=8192),
                         HD, D)
