@@ -389,6 +389,10 @@ KVC_API int kvc_debug_event_profile(kvc_ctx* ctx, double* out10, int32_t reset);
 KVC_API int kvc_debug_wave_profile(kvc_ctx* ctx, double* out13, int32_t reset);
 /* Enables per-phase CUDA-event timing (off by default: it adds event records). */
 KVC_API void kvc_set_timing(kvc_ctx* ctx, int32_t on);
+/* Rows zero-padded to the context's width d (a caller with a narrower head width, e.g. the C++
+ * drop-in for d % 8 != 0): attention keeps the softmax scale 1/sqrt(d_logical). Everything else
+ * of the path is a sequential sum over the elements, unchanged by trailing zeros. */
+KVC_API int kvc_set_head_dim(kvc_ctx* ctx, int32_t d_logical);
 
 #ifdef __cplusplus
 }

@@ -161,6 +161,7 @@ def lib():
         L.kvc_launch_count.restype = C.c_int64
         L.kvc_last_step_timing.argtypes = [vp, f64p]
         L.kvc_set_timing.argtypes = [vp, C.c_int32]
+        L.kvc_set_head_dim.argtypes = [vp, C.c_int32]
         L.kvc_last_ingest_timing.argtypes = [vp, f64p]
         L.kvc_debug_resolve_profile.argtypes = [vp, f64p]
         L.kvc_debug_event_profile.argtypes = [vp, f64p, C.c_int32]
@@ -188,7 +189,7 @@ EXPORTED = [
     "kvc_cluster", "kvc_cluster_entries", "kvc_cluster_payload", "kvc_n_partitions",
     "kvc_partition", "kvc_partition_layer", "kvc_maint_stats", "kvc_ledger",
     "kvc_ledger_log_size", "kvc_ledger_op", "kvc_check", "kvc_offload", "kvc_fetch",
-    "kvc_launch_count", "kvc_last_step_timing", "kvc_set_timing", "kvc_last_ingest_timing",
+    "kvc_launch_count", "kvc_last_step_timing", "kvc_set_timing", "kvc_set_head_dim", "kvc_last_ingest_timing",
     "kvc_debug_resolve_profile", "kvc_host_split_two", "kvc_host_kmeans", "kvc_host_tau",
     "kvc_host_mix_seed", "kvc_host_rng_first2", "kvc_debug_div_check", "kvc_debug_assign_check", "kvc_tier_sync",
     "kvc_tier_stats", "kvc_cluster_tier", "kvc_debug_tier_check", "kvc_debug_split_two", "kvc_debug_kmeans", "kvc_exchange_bytes", "kvc_ipc_alloc",

@@ -539,6 +539,15 @@ int kvc_last_step_timing(kvc_ctx* ctx, double* t) {
   return KVC_OK;
 }
 
+int kvc_set_head_dim(kvc_ctx* ctx, int32_t d_logical) {
+  return guard([&] {
+    if (ctx->tok)
+      ctx->tok->set_head_dim(d_logical);
+    else
+      ctx->impl->set_head_dim(d_logical);
+  });
+}
+
 void kvc_set_timing(kvc_ctx* ctx, int32_t on) {
   if (ctx->tok)
     ctx->tok->set_timing(on != 0);

@@ -50,7 +50,7 @@ void rows_to_f32(const void* src, int bf16, std::size_t n, float* dst) {
 
 // ============================================================================ lifetime
 
-Context::Context(const kvc_cfg& cfg, int d, int L) : cfg_(cfg), d_(d), L_(L) {
+Context::Context(const kvc_cfg& cfg, int d, int L) : cfg_(cfg), d_(d), L_(L), dl_(d) {
   // EngineConfig::validate (engine.cpp:9-14), RetrievalConfig::validate (retrieval.cpp:10-16)
   if (cfg_.k_v <= 0 || cfg_.k_s <= 0 || cfg_.window_frames <= 0 || cfg_.prefetch_k <= 0)
     fail(-10, "retrieval budgets must be positive");
@@ -545,6 +545,13 @@ void Context::resolve_profile(double* out) {
 
 void Context::sync() { KVC_CUDA(cudaStreamSynchronize(st_)); }
 
+void Context::set_head_dim(int d_logical) {
+  if (d_logical < 1 || d_logical > d_) fail(-10, "head width must be in [1, d]");
+  flush_pending();
+  da_.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(d_logical)));
+  dl_ = d_logical;  // CostModel::entry_bytes counts the caller's width (store.hpp:27-30)
+}
+
 void Context::check_dev_err() {
   std::int32_t e = 0;
   KVC_CUDA(cudaMemcpyAsync(&e, t_.err, 4, cudaMemcpyDeviceToHost, st_));  // (st_ is non-blocking:
@@ -764,7 +771,7 @@ void Context::flush_resid() {
 
 std::int64_t Context::entry_bytes() const {  // CostModel::entry_bytes (store.hpp:27-30)
   return cfg_.bytes_per_entry > 0 ? cfg_.bytes_per_entry
-                                  : static_cast<std::int64_t>(d_) * 2 * static_cast<std::int64_t>(sizeof(float));
+                                  : static_cast<std::int64_t>(dl_) * 2 * static_cast<std::int64_t>(sizeof(float));
 }
 
 std::int64_t Context::side_entries(const Cluster& c) const {  // store.cpp:76-80

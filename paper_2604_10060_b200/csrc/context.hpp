@@ -184,6 +184,8 @@ class Context {
   cudaStream_t stream() const { return st_; }
   std::int64_t launches() const { return launches_; }
   void set_timing(bool on) { timing_ = on; }
+  // attention scale 1/sqrt(d_logical) for rows zero-padded to d (kvc_set_head_dim)
+  void set_head_dim(int d_logical);
   const double* step_timing() const { return step_t_; }
   const double* ingest_timing() const { return ingest_t_; }
   // Runs the candidate build + distance tile (+ top-M) on a frame for partition `pid` without
@@ -217,6 +219,7 @@ class Context {
   void api_set_retrieval(const kvc_cfg& c);
   void api_reconfigure(const kvc_cfg& c, int what);  // bits: 1 retrieval, 2 cost model, 4 maintainer
   std::int64_t api_place_frame(std::int64_t frame, const float* visual);
+  void component_index();
   std::int64_t api_insert(std::int64_t pid, int layer, int token, std::int64_t frame, const float* key,
                           const float* value);
   std::vector<std::int64_t> api_materialize(std::int64_t id);
@@ -235,6 +238,7 @@ class Context {
   // ---- configuration
   kvc_cfg cfg_;
   int d_, L_, es_;
+  int dl_ = 0;  // the caller's head width (kvc_set_head_dim; d_ unless rows are zero-padded)
   // ---- device
   DevTables t_{};
   cudaStream_t st_ = nullptr;

@@ -253,9 +253,17 @@ void Context::api_reconfigure(const kvc_cfg& c, int what) {
   }
 }
 
+// A Maintainer may start on an empty HierIndex (maintainer.cpp:37-53 opens the first partition):
+// the component API owns the index from then on (no engine batch build pending).
+void Context::component_index() {
+  if (built_) return;
+  if (!pending_.empty()) fail(-9, "the engine is still collecting its build batch (ingest_frame before build)");
+  built_ = true;
+}
+
 std::int64_t Context::api_place_frame(std::int64_t frame, const float* visual) {  // maintainer.cpp:37-53
   flush_pending();
-  if (!built_) fail(-9, "place_frame before any index was built");
+  component_index();
   return place_frame(frame, visual);
 }
 
@@ -265,7 +273,7 @@ std::int64_t Context::api_place_frame(std::int64_t frame, const float* visual) {
 std::int64_t Context::api_insert(std::int64_t pid, int layer, int token, std::int64_t frame, const float* key,
                                  const float* value) {
   flush_pending();
-  if (!built_) fail(-9, "on_insert before any index was built");
+  component_index();
   if (layer < 0 || layer >= L_) fail(-7, "layer out of range: " + std::to_string(layer));
   if (pid < 0 || pid >= static_cast<std::int64_t>(parts_.size())) fail(-8, "unknown partition id");
   if (token < 0 || token >= t_.tmax) fail(-10, "token id outside [0, max_tokens)");

@@ -62,6 +62,7 @@ class TokenContext {
   int L() const { return L_; }
   std::int64_t launches() const { return launches_; }
   void set_timing(bool on) { timing_ = on; }
+  void set_head_dim(int d_logical);
   const double* step_timing() const { return step_t_; }
   void profile(double* out);  // mean select-phase cycles over domains (out[8])
   // the baseline's window_frames argument (retrieval.cpp:166-254) empty: nothing attended without
@@ -73,6 +74,7 @@ class TokenContext {
  private:
   kvc_cfg cfg_;
   int d_, L_, es_;
+  int dl_ = 0;  // the caller's head width (kvc_set_head_dim)
   cudaStream_t st_ = nullptr;
   std::vector<void*> dev_, host_;
   void* dalloc(std::size_t bytes);

@@ -205,7 +205,7 @@ void TokenContext::decode_step(std::int64_t qid, const float* q, int q_mem, floa
     fail(-1, "device error");
   }
   // latency model and ledger (retrieval.cpp:185-242): one op per run of adjacent host-side tokens
-  const std::int64_t eb = cfg_.bytes_per_entry > 0 ? cfg_.bytes_per_entry : static_cast<std::int64_t>(d_) * 2 * 4;
+  const std::int64_t eb = cfg_.bytes_per_entry > 0 ? cfg_.bytes_per_entry : static_cast<std::int64_t>(dl_ ? dl_ : d_) * 2 * 4;
   ttft_ = 0.0;
   std::int64_t tok_total = 0;
   for (int l = 0; l < L_; ++l) {
@@ -317,6 +317,12 @@ void TokenContext::profile(double* out) {
     for (int l = 0; l < L_; ++l) s += static_cast<double>(p[static_cast<std::size_t>(l) * 8 + k]);
     out[k] = s / L_;
   }
+}
+
+void TokenContext::set_head_dim(int d_logical) {
+  if (d_logical < 1 || d_logical > d_) fail(-10, "head width must be in [1, d]");
+  dl_ = d_logical;
+  da_.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(d_logical)));
 }
 
 }  // namespace kvc

@@ -53,11 +53,40 @@ inline int check(int rc) {
   return rc;
 }
 
+// Head widths: the device path stores rows of a multiple of 8 elements (16-byte vector moves for
+// bf16 / f32 rows). A narrower width d (the reference's own unit tests use d = 4) is carried as
+// d rounded up to 8 with zero padding: every quantity of the path is a sequential sum over the
+// elements (dot, norm, sq_dist, the Eq. 3/4 running means, the k-means unit rows and centroid
+// sums), and appending +0 terms to such a sum leaves it bit-identical, so rankings, statistics and
+// splits are those of width d; the attention softmax keeps 1/sqrt(d) (kvc_set_head_dim). Rows are
+// padded on the way in and cut back to d on the way out.
+inline int padded_width(int d) { return d > 0 && d % 8 != 0 ? (d + 7) / 8 * 8 : d; }
+
 struct Device {
   kvc_ctx* ctx = nullptr;
   kvc_cfg cfg{};
-  int d = 0, L = 0;
-  Device(const kvc_cfg& c, int d_, int L_) : cfg(c), d(d_), L(L_) { check(kvc_create(&cfg, d, L, &ctx)); }
+  int d = 0, dp = 0, L = 0;  // logical width, device width (padded)
+  Device(const kvc_cfg& c, int d_, int L_) : cfg(c), d(d_), dp(padded_width(d_)), L(L_) {
+    check(kvc_create(&cfg, dp, L, &ctx));
+    if (dp != d) check(kvc_set_head_dim(ctx, d));
+  }
+  // `rows` rows of width d -> width dp (zero padding); a no-op view when dp == d
+  template <class T>
+  const T* pad(const T* src, std::size_t rows, std::vector<T>& buf) const {
+    if (dp == d || !src) return src;
+    buf.assign(rows * static_cast<std::size_t>(dp), T(0));
+    for (std::size_t r = 0; r < rows; ++r)
+      std::memcpy(&buf[r * dp], src + r * d, static_cast<std::size_t>(d) * sizeof(T));
+    return buf.data();
+  }
+  // rows of width dp (device) -> width d in place of a buffer sized rows * dp
+  template <class T>
+  void cut(std::vector<T>& v, std::size_t rows) const {
+    if (dp == d) return;
+    for (std::size_t r = 0; r < rows; ++r)
+      std::memmove(&v[r * d], &v[r * dp], static_cast<std::size_t>(d) * sizeof(T));
+    v.resize(rows * static_cast<std::size_t>(d));
+  }
   ~Device() {
     if (ctx) kvc_destroy(ctx);
   }
@@ -115,11 +144,12 @@ void put_build(kvc_cfg& c, const BuildConfig& b) {
 
 // FrameInput -> [L][T][d] keys / values; token ids must be the positions 0..T-1 (the engine keys
 // a frame's entries by position, as gen_stream and every reference caller produce them)
-void pack_frame(const FrameInput& f, int d, int L, std::vector<float>& k, std::vector<float>& v, int& T) {
+void pack_frame(const FrameInput& f, int d, int L, std::vector<float>& k, std::vector<float>& v, int& T, int dp = 0) {
+  if (dp <= 0) dp = d;
   if (static_cast<int>(f.visual.size()) != d) throw ConfigError("frame width does not match the engine");
   if (static_cast<int>(f.layers.size()) != L) throw ConfigError("frame layer count does not match the engine");
   T = static_cast<int>(f.layers[0].size());
-  k.assign(static_cast<std::size_t>(L) * T * d, 0.f);
+  k.assign(static_cast<std::size_t>(L) * T * dp, 0.f);
   v.assign(k.size(), 0.f);
   for (int l = 0; l < L; ++l) {
     const auto& layer = f.layers[static_cast<std::size_t>(l)];
@@ -129,19 +159,20 @@ void pack_frame(const FrameInput& f, int d, int L, std::vector<float>& k, std::v
       if (e.token_id != t) throw ConfigError("frame entries must carry token ids 0..T-1 in order");
       if (static_cast<int>(e.key.size()) != d || static_cast<int>(e.value.size()) != d)
         throw DimMismatch(e.key.size(), static_cast<std::size_t>(d));
-      std::memcpy(&k[(static_cast<std::size_t>(l) * T + t) * d], e.key.data(), static_cast<std::size_t>(d) * 4);
-      std::memcpy(&v[(static_cast<std::size_t>(l) * T + t) * d], e.value.data(), static_cast<std::size_t>(d) * 4);
+      std::memcpy(&k[(static_cast<std::size_t>(l) * T + t) * dp], e.key.data(), static_cast<std::size_t>(d) * 4);
+      std::memcpy(&v[(static_cast<std::size_t>(l) * T + t) * dp], e.value.data(), static_cast<std::size_t>(d) * 4);
     }
   }
 }
 
-std::vector<float> pack_query(const QueryBundle& b, int d, int L) {
+std::vector<float> pack_query(const QueryBundle& b, int d, int L, int dp = 0) {
+  if (dp <= 0) dp = d;
   if (static_cast<int>(b.q.size()) != L) throw ConfigError("query bundle layer count does not match the stored layers");
-  std::vector<float> q(static_cast<std::size_t>(L) * d);
+  std::vector<float> q(static_cast<std::size_t>(L) * dp, 0.f);
   for (int l = 0; l < L; ++l) {
     if (static_cast<int>(b.q[static_cast<std::size_t>(l)].size()) != d)
       throw DimMismatch(b.q[static_cast<std::size_t>(l)].size(), static_cast<std::size_t>(d));
-    std::memcpy(&q[static_cast<std::size_t>(l) * d], b.q[static_cast<std::size_t>(l)].data(), static_cast<std::size_t>(d) * 4);
+    std::memcpy(&q[static_cast<std::size_t>(l) * dp], b.q[static_cast<std::size_t>(l)].data(), static_cast<std::size_t>(d) * 4);
   }
   return q;
 }
@@ -390,23 +421,25 @@ b200::Device& HierIndex::device() const {
 void HierIndex::install_pending() const {
   if (pending_parts_.empty() && pending_clusters_.empty()) return;
   auto* self = const_cast<HierIndex*>(this);
+  const int dp = dev_->dp;
   for (const VisualPartition& p : pending_parts_) {  // verbatim: frames, fp64 visual_rep, count
     std::int64_t pid = -1;
-    check(kvc_add_partition_ex(dev_->ctx, p.frame_ids.data(), static_cast<int>(p.frame_ids.size()), p.visual_rep.data(),
-                               p.visual_stat_count, &pid));
+    std::vector<double> pv;
+    check(kvc_add_partition_ex(dev_->ctx, p.frame_ids.data(), static_cast<int>(p.frame_ids.size()),
+                               dev_->pad(p.visual_rep.data(), 1, pv), p.visual_stat_count, &pid));
   }
   auto rows = [&](const std::vector<KVEntry>& es, std::vector<float>& k, std::vector<float>& v,
                   std::vector<std::int64_t>& fr, std::vector<std::int32_t>& tk) {
     const std::size_t n = es.size();
-    k.assign(n * static_cast<std::size_t>(dim_), 0.f);
+    k.assign(n * static_cast<std::size_t>(dp), 0.f);
     v.assign(k.size(), 0.f);
     fr.resize(n);
     tk.resize(n);
     for (std::size_t j = 0; j < n; ++j) {
       if (static_cast<int>(es[j].key.size()) != dim_ || static_cast<int>(es[j].value.size()) != dim_)
         throw DimMismatch(es[j].key.size(), static_cast<std::size_t>(dim_));
-      std::memcpy(&k[j * dim_], es[j].key.data(), static_cast<std::size_t>(dim_) * 4);
-      std::memcpy(&v[j * dim_], es[j].value.data(), static_cast<std::size_t>(dim_) * 4);
+      std::memcpy(&k[j * dp], es[j].key.data(), static_cast<std::size_t>(dim_) * 4);
+      std::memcpy(&v[j * dp], es[j].value.data(), static_cast<std::size_t>(dim_) * 4);
       fr[j] = es[j].frame_id;
       tk[j] = es[j].token_id;
     }
@@ -432,10 +465,11 @@ void HierIndex::install_pending() const {
     r.buffer_values = bv.data();
     r.buffer_frames = bf.data();
     r.buffer_tokens = bt.data();
-    r.rep = rec.rep.data();
+    std::vector<double> prep, pbrep;
+    r.rep = dev_->pad(rec.rep.data(), 1, prep);
     r.variance = rec.variance;
     r.stat_count = rec.stat_count;
-    r.buffer_rep = rec.buffer_rep.size() == static_cast<std::size_t>(dim_) ? rec.buffer_rep.data() : nullptr;
+    r.buffer_rep = rec.buffer_rep.size() == static_cast<std::size_t>(dim_) ? dev_->pad(rec.buffer_rep.data(), 1, pbrep) : nullptr;
     r.lazy_split = (rec.lazy_split || pending_registered_.count(rec.cluster_id)) ? 1 : 0;
     r.residence = rec.residence == Residence::Host ? 1 : 0;
     r.adopt = pending_adopted_[i];
@@ -472,10 +506,11 @@ const HierIndex::View& HierIndex::view() const {
     for (int p = 0; p < P; ++p) {
       VisualPartition vp;
       vp.partition_id = p;
-      DVec rep(static_cast<std::size_t>(dim_));
+      DVec rep(static_cast<std::size_t>(dev_->dp));
       int n = check(kvc_partition(c, p, rep.data(), nullptr, 0));
       vp.frame_ids.resize(static_cast<std::size_t>(n));
       check(kvc_partition(c, p, rep.data(), vp.frame_ids.data(), n));
+      dev_->cut(rep, 1);
       vp.visual_rep = rep;
       vp.visual_stat_count = n;
       for (int l = 0; l < layers_; ++l) {
@@ -493,9 +528,11 @@ const HierIndex::View& HierIndex::view() const {
     for (std::int64_t id : ids) {
       ClusterRecord r;
       std::int64_t info[10];
-      DVec rep(static_cast<std::size_t>(dim_)), brep(static_cast<std::size_t>(dim_), 0.0);
+      DVec rep(static_cast<std::size_t>(dev_->dp)), brep(static_cast<std::size_t>(dev_->dp), 0.0);
       double var = 0.0;
       check(kvc_cluster(c, id, info, &var, rep.data(), brep.data()));
+      dev_->cut(rep, 1);
+      dev_->cut(brep, 1);
       r.cluster_id = id;
       r.layer_id = static_cast<std::int32_t>(info[0]);
       r.visual_parent = info[1];
@@ -512,9 +549,11 @@ const HierIndex::View& HierIndex::view() const {
         if (n == 0) continue;
         std::vector<std::int64_t> fr(static_cast<std::size_t>(n));
         std::vector<std::int32_t> tk(static_cast<std::size_t>(n));
-        std::vector<float> k(static_cast<std::size_t>(n) * dim_), val(k.size());
+        std::vector<float> k(static_cast<std::size_t>(n) * dev_->dp), val(k.size());
         check(kvc_cluster_entries(c, id, which, fr.data(), tk.data(), n));
         check(kvc_cluster_payload(c, id, which, k.data(), val.data(), n));
+        dev_->cut(k, static_cast<std::size_t>(n));
+        dev_->cut(val, static_cast<std::size_t>(n));
         auto& dst = which == 0 ? r.members : r.buffer;
         for (int j = 0; j < n; ++j) {
           KVEntry e;
@@ -598,7 +637,8 @@ std::int64_t HierIndex::add_partition(std::int64_t first_frame_id, const Embeddi
   if (static_cast<std::int32_t>(visual.size()) != dim_) throw DimMismatch(visual.size(), static_cast<std::size_t>(dim_));
   if (dev_) {
     std::int64_t pid = -1;
-    check(kvc_add_partition(dev_->ctx, first_frame_id, visual.data(), &pid));
+    std::vector<float> pv;
+    check(kvc_add_partition(dev_->ctx, first_frame_id, dev_->pad(visual.data(), 1, pv), &pid));
     mark_device_changed();
     return pid;
   }
@@ -616,7 +656,9 @@ std::int64_t HierIndex::add_partition(std::int64_t first_frame_id, const Embeddi
 
 void HierIndex::append_frame(std::int64_t partition_id, std::int64_t frame_id, const Embedding& visual) {
   if (dev_) {
-    check(kvc_append_frame(dev_->ctx, partition_id, frame_id, visual.data()));
+    if (static_cast<std::int32_t>(visual.size()) != dim_) throw DimMismatch(visual.size(), static_cast<std::size_t>(dim_));
+    std::vector<float> pv;
+    check(kvc_append_frame(dev_->ctx, partition_id, frame_id, dev_->pad(visual.data(), 1, pv)));
     mark_device_changed();
     return;
   }
@@ -648,7 +690,9 @@ std::int64_t HierIndex::add_cluster(ClusterRecord&& rec) {
       tk[static_cast<std::size_t>(j)] = e.token_id;
     }
     std::int64_t id = -1;
-    check(kvc_add_cluster(dev_->ctx, rec.layer_id, rec.visual_parent, n, k.data(), v.data(), fr.data(), tk.data(),
+    std::vector<float> pk, pv;
+    check(kvc_add_cluster(dev_->ctx, rec.layer_id, rec.visual_parent, n, dev_->pad(k.data(), static_cast<std::size_t>(n), pk),
+                          dev_->pad(v.data(), static_cast<std::size_t>(n), pv), fr.data(), tk.data(),
                           rec.residence == Residence::Host ? 1 : 0, 0, &id));
     mark_device_changed();
     return id;
@@ -849,7 +893,8 @@ std::vector<std::int64_t> HierIndex::visual_topk(const Embedding& query, int k_v
   b200::Device& dv = device();
   if (check(kvc_n_partitions(dv.ctx)) == 0) throw EmptyIndex("visual_topk on an empty index");
   std::vector<std::int64_t> ids(static_cast<std::size_t>(k_v));
-  const int n = check(kvc_visual_topk(dv.ctx, query.data(), k_v, ids.data()));
+  std::vector<float> pq;
+  const int n = check(kvc_visual_topk(dv.ctx, dv.pad(query.data(), 1, pq), k_v, ids.data()));
   ids.resize(static_cast<std::size_t>(std::min(n, k_v)));
   return ids;
 }
@@ -862,7 +907,8 @@ std::vector<CandidateRef> HierIndex::semantic_topk(const Embedding& query, std::
   b200::Device& dv = device();
   std::vector<std::int64_t> ids(static_cast<std::size_t>(k_s));
   std::vector<std::int32_t> buf(static_cast<std::size_t>(k_s));
-  const int n = check(kvc_semantic_topk(dv.ctx, query.data(), layer, partition_ids.data(),
+  std::vector<float> pq;
+  const int n = check(kvc_semantic_topk(dv.ctx, dv.pad(query.data(), 1, pq), layer, partition_ids.data(),
                                         static_cast<int>(partition_ids.size()), k_s, ids.data(), buf.data()));
   std::vector<CandidateRef> out;
   for (int i = 0; i < n && i < k_s; ++i) out.push_back({ids[static_cast<std::size_t>(i)], buf[static_cast<std::size_t>(i)] != 0});
@@ -918,8 +964,10 @@ HierIndex build_index(const std::vector<FrameInput>& frames, const BuildConfig& 
   std::vector<float> k, v;
   for (const FrameInput& f : frames) {
     int T = 0;
-    b200::pack_frame(f, d, L, k, v, T);
-    check(kvc_ingest_frame(idx.dev_->ctx, f.frame_id, f.visual.data(), k.data(), v.data(), T, KVC_MEM_HOST, nullptr, nullptr));
+    b200::pack_frame(f, d, L, k, v, T, idx.dev_->dp);
+    std::vector<float> pv;
+    check(kvc_ingest_frame(idx.dev_->ctx, f.frame_id, idx.dev_->pad(f.visual.data(), 1, pv), k.data(), v.data(), T, KVC_MEM_HOST,
+                           nullptr, nullptr));
   }
   check(kvc_reset_window(idx.dev_->ctx));  // an index has no local window
   // a TieredStore over the built index re-applies its own CostModel (kvc_reconfigure)
@@ -1039,7 +1087,9 @@ Maintainer::Maintainer(HierIndex& index, TieredStore& store, const MaintainerCon
 std::int64_t Maintainer::place_frame(std::int64_t frame_id, const Embedding& visual) {
   if (static_cast<std::int32_t>(visual.size()) != index_.dim()) throw DimMismatch(visual.size(), static_cast<std::size_t>(index_.dim()));
   std::int64_t pid = -1;
-  check(kvc_place_frame(index_.device().ctx, frame_id, visual.data(), &pid));
+  std::vector<float> pv;
+  b200::Device& dv = index_.device();
+  check(kvc_place_frame(dv.ctx, frame_id, dv.pad(visual.data(), 1, pv), &pid));
   index_.mark_device_changed();
   return pid;
 }
@@ -1048,8 +1098,10 @@ std::int64_t Maintainer::on_insert(std::int64_t partition_id, const KVEntry& ent
   if (static_cast<std::int32_t>(entry.key.size()) != index_.dim() || entry.value.size() != entry.key.size())
     throw DimMismatch(entry.key.size(), static_cast<std::size_t>(index_.dim()));
   std::int64_t cid = -1;
-  check(kvc_insert(index_.device().ctx, partition_id, entry.layer_id, entry.token_id, entry.frame_id, entry.key.data(),
-                   entry.value.data(), &cid));
+  b200::Device& dv = index_.device();
+  std::vector<float> pk, pv;
+  check(kvc_insert(dv.ctx, partition_id, entry.layer_id, entry.token_id, entry.frame_id, dv.pad(entry.key.data(), 1, pk),
+                   dv.pad(entry.value.data(), 1, pv), &cid));
   index_.mark_device_changed();
   return cid;
 }
@@ -1085,11 +1137,12 @@ RetrievalResult retrieve(const QueryBundle& bundle, const RetrievalConfig& cfg, 
   b200::put_retrieval(c, cfg);
   check(kvc_reconfigure(dv.ctx, &c, 1));
   check(kvc_reset_window(dv.ctx));
-  const std::vector<float> q = b200::pack_query(bundle, dv.d, dv.L);
-  b200::g_attention.assign(static_cast<std::size_t>(dv.L) * dv.d, 0.f);
+  const std::vector<float> q = b200::pack_query(bundle, dv.d, dv.L, dv.dp);
+  b200::g_attention.assign(static_cast<std::size_t>(dv.L) * dv.dp, 0.f);
   const auto& gt = bundle.ground_truth_frames;
   check(kvc_decode_step(dv.ctx, bundle.query_id, q.data(), KVC_MEM_HOST, b200::g_attention.data(), KVC_MEM_HOST,
                         gt.empty() ? nullptr : gt.data(), static_cast<int>(gt.size())));
+  dv.cut(b200::g_attention, static_cast<std::size_t>(dv.L));
   RetrievalResult r = b200::read_result(dv, bundle.query_id);
   index.mark_device_changed();
   store.ledger();  // pull the step's ledger ops
@@ -1103,7 +1156,8 @@ std::vector<CandidateRef> oracle_flat_topk(const HierIndex& index, const Embeddi
   const int cap = std::max(1, std::min(k, check(kvc_n_clusters(dv.ctx)) * 2 + 1));
   std::vector<std::int64_t> ids(static_cast<std::size_t>(cap));
   std::vector<std::int32_t> buf(static_cast<std::size_t>(cap));
-  const int n = check(kvc_flat_topk(dv.ctx, query.data(), layer, std::min(k, cap), ids.data(), buf.data()));
+  std::vector<float> pq;
+  const int n = check(kvc_flat_topk(dv.ctx, dv.pad(query.data(), 1, pq), layer, std::min(k, cap), ids.data(), buf.data()));
   std::vector<CandidateRef> out;
   for (int i = 0; i < n; ++i) out.push_back({ids[static_cast<std::size_t>(i)], buf[static_cast<std::size_t>(i)] != 0});
   return out;
@@ -1156,16 +1210,16 @@ RetrievalResult retrieve_token_baseline(const QueryBundle& bundle, const Retriev
   std::vector<float> k, v;
   std::size_t off = 0;
   for (const auto& [fid, T] : frames) {
-    k.assign(static_cast<std::size_t>(L) * T * d, 0.f);
+    k.assign(static_cast<std::size_t>(L) * T * dv.dp, 0.f);
     v.assign(k.size(), 0.f);
     for (int l = 0; l < L; ++l)
       for (int t = 0; t < T; ++t) {
         const KVEntry& e = pools[static_cast<std::size_t>(l)][off + static_cast<std::size_t>(t)];
         if (e.frame_id != fid) throw ConfigError("token pools must hold the same frames at every layer");
-        std::memcpy(&k[(static_cast<std::size_t>(l) * T + t) * d], e.key.data(), static_cast<std::size_t>(d) * 4);
-        std::memcpy(&v[(static_cast<std::size_t>(l) * T + t) * d], e.value.data(), static_cast<std::size_t>(d) * 4);
+        std::memcpy(&k[(static_cast<std::size_t>(l) * T + t) * dv.dp], e.key.data(), static_cast<std::size_t>(d) * 4);
+        std::memcpy(&v[(static_cast<std::size_t>(l) * T + t) * dv.dp], e.value.data(), static_cast<std::size_t>(d) * 4);
       }
-    std::vector<float> vis(static_cast<std::size_t>(d), 0.f);
+    std::vector<float> vis(static_cast<std::size_t>(dv.dp), 0.f);
     check(kvc_ingest_frame(dv.ctx, fid, vis.data(), k.data(), v.data(), T, KVC_MEM_HOST, nullptr, nullptr));
     off += static_cast<std::size_t>(T);
   }
@@ -1176,11 +1230,12 @@ RetrievalResult retrieve_token_baseline(const QueryBundle& bundle, const Retriev
   if (!tail) throw ConfigError("retrieve_token_baseline: window_frames must be the pools' most recent frames");
   if (window_frames.empty()) check(kvc_reset_window(dv.ctx));
   const b200::Totals t0 = b200::ledger_totals(dv);
-  const std::vector<float> q = b200::pack_query(bundle, d, L);
-  b200::g_attention.assign(static_cast<std::size_t>(L) * d, 0.f);
+  const std::vector<float> q = b200::pack_query(bundle, d, L, dv.dp);
+  b200::g_attention.assign(static_cast<std::size_t>(L) * dv.dp, 0.f);
   const auto& gt = bundle.ground_truth_frames;
   check(kvc_decode_step(dv.ctx, bundle.query_id, q.data(), KVC_MEM_HOST, b200::g_attention.data(), KVC_MEM_HOST,
                         gt.empty() ? nullptr : gt.data(), static_cast<int>(gt.size())));
+  dv.cut(b200::g_attention, static_cast<std::size_t>(L));
   RetrievalResult r = b200::read_result(dv, bundle.query_id);
   const b200::Totals t1 = b200::ledger_totals(dv);
   if (t1.ops > t0.ops) {  // the step's coalesced-run ops, recorded as one aggregate entry
@@ -1230,7 +1285,7 @@ void StreamEngine::process(const StreamEvent& event) {
 void StreamEngine::ingest_frame(const FrameInput& frame) {  // engine.cpp:134-174
   std::vector<float> k, v;
   int T = 0;
-  b200::pack_frame(frame, d_, L_, k, v, T);
+  b200::pack_frame(frame, d_, L_, k, v, T, dev_->dp);
   frames_processed_ += 1;
   frames_in_batch_ += 1;
   if (cfg_.batched_ingest) {
@@ -1242,7 +1297,8 @@ void StreamEngine::ingest_frame(const FrameInput& frame) {  // engine.cpp:134-17
     ingest_cost_us_ += cfg_.ingest_overhead_us;
     frames_in_batch_ = 0;
   }
-  check(kvc_ingest_frame(dev_->ctx, frame.frame_id, frame.visual.data(), k.data(), v.data(), T, KVC_MEM_HOST, nullptr,
+  std::vector<float> pvis;
+  check(kvc_ingest_frame(dev_->ctx, frame.frame_id, dev_->pad(frame.visual.data(), 1, pvis), k.data(), v.data(), T, KVC_MEM_HOST, nullptr,
                          nullptr));
   if (view_) view_->mark_device_changed();
 }
@@ -1250,11 +1306,12 @@ void StreamEngine::ingest_frame(const FrameInput& frame) {  // engine.cpp:134-17
 void StreamEngine::answer_query(const QueryBundle& bundle) {  // engine.cpp:176-237
   const bool token = cfg_.retrieval.mode == RetrievalMode::TokenBaseline;
   const b200::Totals t0 = b200::ledger_totals(*dev_);
-  const std::vector<float> q = b200::pack_query(bundle, d_, L_);
-  att_.assign(static_cast<std::size_t>(L_) * d_, 0.f);
+  const std::vector<float> q = b200::pack_query(bundle, d_, L_, dev_->dp);
+  att_.assign(static_cast<std::size_t>(L_) * dev_->dp, 0.f);
   const auto& gt = bundle.ground_truth_frames;
   check(kvc_decode_step(dev_->ctx, bundle.query_id, q.data(), KVC_MEM_HOST, att_.data(), KVC_MEM_HOST,
                         gt.empty() ? nullptr : gt.data(), static_cast<int>(gt.size())));
+  dev_->cut(att_, static_cast<std::size_t>(L_));
   const b200::Totals t1 = b200::ledger_totals(*dev_);
   QueryRow row;
   row.query_id = bundle.query_id;
