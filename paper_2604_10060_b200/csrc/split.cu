@@ -23,7 +23,15 @@ constexpr int OBJ_CHUNK = 4096;  // 32 KB of the objective's terms per shared-me
 // threads of a warp, which take consecutive points) with a shared-memory vector.
 __device__ __forceinline__ double dot_col(const double* __restrict__ ut, int n, int i, const double* v, int d) {
   double s = 0.0;
-  for (int c = 0; c < d; ++c) s = dadd(s, dmul(ut[static_cast<int64_t>(c) * n + i], v[c]));
+  int c = 0;
+  for (; c + 16 <= d; c += 16) {  // the loads of 16 dimensions in flight ahead of the chain
+    double x[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) x[k] = ut[static_cast<int64_t>(c + k) * n + i];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) s = dadd(s, dmul(x[k], v[c + k]));
+  }
+  for (; c < d; ++c) s = dadd(s, dmul(ut[static_cast<int64_t>(c) * n + i], v[c]));
   return s;
 }
 
@@ -58,6 +66,32 @@ struct SplitSmem {
 // reference recomputes them in the objective of one iteration and the assignment of the next,
 // with the same centroids: computing them once yields the identical values.
 __device__ __forceinline__ void cosines(const double* __restrict__ ut, int n, int d, SplitSmem& S, double* sc) {
+  if (n <= SPT) {
+    // one point per thread: the loads of 16 dimensions in flight ahead of the two chains
+    const int i0 = threadIdx.x;
+    if (i0 < n) {
+      double a0 = 0.0, b0 = 0.0;
+      int c = 0;
+      for (; c + 16 <= d; c += 16) {
+        double x0[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) x0[k] = ut[static_cast<int64_t>(c + k) * n + i0];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          a0 = dadd(a0, dmul(x0[k], S.cent[0][c + k]));
+          b0 = dadd(b0, dmul(x0[k], S.cent[1][c + k]));
+        }
+      }
+      for (; c < d; ++c) {
+        const double x0 = ut[static_cast<int64_t>(c) * n + i0];
+        a0 = dadd(a0, dmul(x0, S.cent[0][c]));
+        b0 = dadd(b0, dmul(x0, S.cent[1][c]));
+      }
+      sc[i0] = cos_of(a0, S.cn[0]);
+      sc[n + i0] = cos_of(b0, S.cn[1]);
+    }
+    return;
+  }
   // two points per thread (four independent chains) and the loads of 8 dimensions issued ahead
   // of their arithmetic: the chains are latency-bound, so memory-level parallelism is the lever
   for (int i0 = threadIdx.x; i0 < n; i0 += 2 * SPT) {
@@ -144,16 +178,27 @@ __device__ __forceinline__ void split_two_body(const float* rows, const int32_t*
   for (int i = tid; i < n; i += SPT) {
     const float* p = rows + static_cast<int64_t>(idx[i]) * d;
     double s = 0.0;
-    for (int c = 0; c < d; ++c) {
-      const double x = static_cast<double>(p[c]);
-      s = dadd(s, dmul(x, x));
+    for (int c0 = 0; c0 < d; c0 += 16) {  // 16 loads in flight ahead of the sequential sum
+      float x[16];
+#pragma unroll
+      for (int k = 0; k < 16; ++k) x[k] = c0 + k < d ? p[c0 + k] : 0.f;
+#pragma unroll
+      for (int k = 0; k < 16; ++k)
+        if (c0 + k < d) s = dadd(s, dmul(static_cast<double>(x[k]), static_cast<double>(x[k])));
     }
     const double nr = __dsqrt_rn(s);
     if (nr < 1e-12) S.degen = 1;
-    for (int c = 0; c < d; ++c) {
-      const double r = ddiv(static_cast<double>(p[c]), nr);
-      u[static_cast<int64_t>(i) * d + c] = r;
-      ut[static_cast<int64_t>(c) * n + i] = r;
+    for (int c0 = 0; c0 < d; c0 += 16) {
+      float x[16];
+#pragma unroll
+      for (int k = 0; k < 16; ++k) x[k] = c0 + k < d ? p[c0 + k] : 0.f;
+#pragma unroll
+      for (int k = 0; k < 16; ++k)
+        if (c0 + k < d) {
+          const double r = ddiv(static_cast<double>(x[k]), nr);
+          u[static_cast<int64_t>(i) * d + c0 + k] = r;
+          ut[static_cast<int64_t>(c0 + k) * n + i] = r;
+        }
     }
   }
   __syncthreads();
