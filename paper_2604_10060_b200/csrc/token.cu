@@ -26,7 +26,7 @@ namespace {
 using namespace dm;
 
 constexpr int TT = 1024;         // KT3 threads
-constexpr int TB_EQ = 1024;      // rows sharing the boundary's exact r-th value (ranked by frame, token)
+constexpr int TB_EQ = 1024;      // tie-group rows ranked in shared memory (more: a second radix select)
 // |fp32 scan cosine - exact cosine| bound for d <= 256: the fp32 dot of bf16/fp32 rows with an fp32
 // query errs by <= gamma_d * |q||k| (gamma_256 ~ 1.5e-5) and each fp32 norm by <= ~(d/2+2)u; 4e-5
 // covers the sum with margin. Clustered keys put many rows near the threshold, so the margin is
@@ -436,14 +436,75 @@ __global__ void __launch_bounds__(TT) k_tok_select(TokArgs a, int64_t n, int bud
       }
     }
     __syncthreads();
-    const int neq = min(S.neq, TB_EQ);
-    if (S.neq > TB_EQ && tid == 0) atomicOr(a.err, 1 << 6);
     const int need = S.kk;
-    for (int e = tid; e < neq; e += TT) {
-      int rank = 0;
-      for (int u = 0; u < neq; ++u)
-        rank += (S.efr[u] < S.efr[e] || (S.efr[u] == S.efr[e] && S.etk[u] < S.etk[e])) ? 1 : 0;
-      if (rank < need) atomicOr(&pick[S.esel[e] >> 5], 1u << (S.esel[e] & 31));
+    if (S.neq <= TB_EQ) {  // rank the tie group in shared memory by (frame, token)
+      const int neq = S.neq;
+      for (int e = tid; e < neq; e += TT) {
+        int rank = 0;
+        for (int u = 0; u < neq; ++u)
+          rank += (S.efr[u] < S.efr[e] || (S.efr[u] == S.efr[e] && S.etk[u] < S.etk[e])) ? 1 : 0;
+        if (rank < need) atomicOr(&pick[S.esel[e] >> 5], 1u << (S.esel[e] & 31));
+      }
+    } else {
+      // a larger tie group (repeated / static frames): the need-th smallest (frame, token) key of
+      // the tied rows by a second radix select (keys inverted so the smallest rank first); the
+      // keys are unique, so exactly the rows at or below it are taken
+      __syncthreads();
+      if (tid == 0) {
+        S.prefix64 = 0ull;
+        S.pmask64 = 0ull;
+        S.kk = need;
+      }
+      __syncthreads();
+      for (int p = 0; p < 6; ++p) {
+        const int sh = p < 5 ? 53 - 11 * p : 0;
+        const int width = p < 5 ? 11 : 9;
+        const int nbins = 1 << width;
+        for (int i = tid; i < nbins; i += TT) S.hist[i] = 0;
+        __syncthreads();
+        const unsigned long long pre = S.prefix64, pm = S.pmask64;
+        const int nbp = (nb + TT - 1) / TT * TT;
+        for (int j = tid; j < nbp; j += TT) {
+          const bool tied = j < nb && dkey(bsim[j]) == tau;
+          const unsigned long long key = tied ? ~static_cast<unsigned long long>(btie[j]) : 0ull;
+          const int bin = (tied && (key & pm) == pre) ? static_cast<int>((key >> sh) & static_cast<unsigned long long>(nbins - 1)) : -1;
+          const unsigned same = __match_any_sync(kFull, bin);
+          if (bin >= 0 && lane == __ffs(same) - 1) atomicAdd(&S.hist[bin], static_cast<unsigned>(__popc(same)));
+        }
+        __syncthreads();
+        if (warp == 0) {
+          const int per = nbins / 32;
+          int cnt = 0;
+          const int hi = nbins - 1 - lane * per;
+          for (int b = 0; b < per; ++b) cnt += S.hist[hi - b];
+          int incl = cnt;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(kFull, incl, o);
+            if (lane >= o) incl += y;
+          }
+          const int kk = S.kk;
+          const unsigned hit = __ballot_sync(kFull, incl >= kk);
+          const int src = __ffs(hit) - 1;
+          if (lane == src) {
+            int acc = incl - cnt;
+            int b = 0;
+            for (; b < per; ++b) {
+              const int c = S.hist[hi - b];
+              if (acc + c >= kk) break;
+              acc += c;
+            }
+            S.prefix64 = pre | (static_cast<unsigned long long>(hi - b) << sh);
+            S.pmask64 = pm | (static_cast<unsigned long long>(nbins - 1) << sh);
+            S.kk = kk - acc;
+          }
+        }
+        __syncthreads();
+      }
+      const unsigned long long tau2 = S.prefix64;
+      for (int j = tid; j < nb; j += TT)
+        if (dkey(bsim[j]) == tau && ~static_cast<unsigned long long>(btie[j]) >= tau2)
+          atomicOr(&pick[bidx[j] >> 5], 1u << (bidx[j] & 31));
     }
   }
   __syncthreads();

@@ -36,7 +36,7 @@ struct TokArgs {
   const float* q;             // [L][d] current query
   int32_t* work_ctr;          // K6 work counter (reset by the select kernel)
   long long* prof;            // [L][8] clock64 cycles per select phase (instrumentation)
-  int32_t* err;               // error bits (1: degenerate vector, 64: > 1024 rows tie at the boundary value)
+  int32_t* err;               // error bits (1: degenerate vector)
 };
 
 int launch_tok_append(const TokArgs& a, const void* fk, const void* fv, int T, int tmax, int64_t n0, cudaStream_t st);

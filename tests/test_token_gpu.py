@@ -109,3 +109,26 @@ def test_token_mode_rejects_cluster_views():
     assert kv.cluster_ids() == []
     with pytest.raises(ConfigError):
         kv.check()
+
+
+@pytest.mark.parametrize("budget", [3000, 7000])
+def test_token_baseline_large_exact_tie_group(ref_lib, budget):
+    """Static frames: every row of a domain holds the same key, so all 7,840 rows tie at the exact
+    boundary value (a boundary set above 4,096 rows takes the radix path, and the tie group is far
+    above the 1,024 rows ranked in shared memory): the reference ranks them by (frame, token)
+    (retrieval.cpp:198-204); the kernel's second radix select over the packed (frame, token) keys
+    must pick the same rows."""
+    rng = np.random.default_rng(3)
+    d, L, T, F = 64, 2, 196, 40
+    key = rng.standard_normal((L, d)).astype(np.float32)
+    keys = np.broadcast_to(key[None, :, None, :], (F, L, T, d)).copy()
+    values = rng.standard_normal((F, L, T, d)).astype(np.float32)
+    visual = np.broadcast_to(rng.standard_normal(d).astype(np.float32), (F, d)).copy()
+    q = rng.standard_normal((3, L, d)).astype(np.float32)
+    kinds = np.array([0] * F + [1] * 3, np.int32)
+    s = po.Stream(d, L, T, kinds, visual, keys, values, q, [[0, 1]] * 3)
+    ecfg = po.EngineCfg.make(token_mode=1, token_budget=budget, window_frames=2)
+    mism, att_err, nq = _run(s, ecfg)
+    assert nq == 3
+    assert mism == [], mism[:5]
+    assert att_err < 1e-3, att_err
