@@ -22,6 +22,7 @@ reference sources) on the host cores, on a bounded sample of the same workload.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -82,22 +83,53 @@ class Clocks:
     def __init__(self, index: int):
         self.index = index
         self.rows = []
+        self.sampler = "nvidia-smi"
         self._stop = threading.Event()
         self._t = None
 
+    def _nvml_row(self, h):
+        """The same fields as the nvidia-smi query, in process through NVML (no fork/exec of
+        nvidia-smi inside the timed region)."""
+        import pynvml as N
+
+        sm = N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)
+        mx = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
+        pw = N.nvmlDeviceGetPowerUsage(h) / 1000.0
+        r = N.nvmlDeviceGetCurrentClocksEventReasons(h)
+        act = lambda bit: "Active" if r & bit else "Not Active"
+        return [str(self.index), str(sm), str(mx), f"{pw:.1f}", hex(r), act(N.nvmlClocksEventReasonHwSlowdown),
+                act(N.nvmlClocksEventReasonHwThermalSlowdown), act(N.nvmlClocksEventReasonSwThermalSlowdown),
+                act(N.nvmlClocksEventReasonSwPowerCap)]
+
     def _run(self):
+        h = None
+        try:
+            import pynvml as N
+
+            N.nvmlInit()
+            h = N.nvmlDeviceGetHandleByIndex(self.index)
+            self.sampler = "nvml (in process; nvidia-smi's fields)"
+        except Exception:
+            h = None
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                     timeout=5).stdout.strip()
-                if out:
-                    self.rows.append([x.strip() for x in out.split(",")])
+                if h is not None:
+                    self.rows.append(self._nvml_row(h))
+                else:
+                    out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                         timeout=5).stdout.strip()
+                    if out:
+                        self.rows.append([x.strip() for x in out.split(",")])
             except Exception:
                 pass
             self._stop.wait(0.2)
 
     def __enter__(self):
+        # Python's cyclic garbage collector is paused inside timed regions (as timeit does): a
+        # collection pause of the harness would otherwise land on a random step
+        self._gc = gc.isenabled()
+        gc.disable()
         self._t = threading.Thread(target=self._run, daemon=True)
         self._t.start()
         return self
@@ -105,6 +137,8 @@ class Clocks:
     def __exit__(self, *a):
         self._stop.set()
         self._t.join(timeout=6)
+        if self._gc:
+            gc.enable()
 
     def summary(self):
         if not self.rows:
@@ -114,7 +148,7 @@ class Clocks:
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 5 + i and r[5 + i] == "Active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+                "reasons": reasons, "samples": len(self.rows), "sampler": self.sampler}
 
 
 def traffic_from_profiles():
