@@ -381,6 +381,8 @@ void Context::alloc_device() {
   {
     const char* e = std::getenv("KVC_ATT_DEBUG");  // bit 0: attention consumers skip the math
     da_.debug_flags = e ? std::atoi(e) : 0;
+    const char* pf = std::getenv("KVC_ATT_PF");  // K6: L2 prefetch distance in pages (0: off)
+    da_.att_pf = pf ? std::atoi(pf) : 0;
   }
   d_q_ = static_cast<float*>(dalloc(L * d * 4));
   d_out_ = static_cast<float*>(dalloc(L * d * 4));

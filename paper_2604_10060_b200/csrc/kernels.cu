@@ -2056,6 +2056,18 @@ __global__ void __launch_bounds__(ATT_THREADS + 32) k_attend(DevTables t, Decode
       bulk_g2s_hint(dst, page_k(t, m.page), bytes, &full[s], pol);
       bulk_g2s_hint(dst + static_cast<int64_t>(P) * ROWB, page_v(t, m.page), bytes, &full[s], pol);
       bulk_g2s(dst + kv_bytes, a.q + static_cast<int64_t>(m.dom) * D, D * 4, &full[s]);
+      // the item's page PF_AHEAD ahead goes DRAM -> L2 now (no shared memory held): more bytes in
+      // flight than the two shared-memory stages carry at loaded-DRAM latency
+      if (a.att_pf > 0 && p_k + a.att_pf < c_n) {
+        const int4 nd = pqd[cb][p_k + a.att_pf];
+        if (!is_host_page(t, nd.x)) {
+          const uint32_t nb = static_cast<uint32_t>(nd.y & 0xffff) * ROWB;
+          if (nb) {
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(page_k(t, nd.x)), "r"(nb) : "memory");
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(page_v(t, nd.x)), "r"(nb) : "memory");
+          }
+        }
+      }
       p_k += 1;
     }
     return;

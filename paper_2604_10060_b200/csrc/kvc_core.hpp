@@ -223,6 +223,7 @@ struct DecodeArgs {
   int32_t* work_ctr;       // attention work-claim counter (per context: contexts may run concurrently)
   int32_t debug_flags;     // instrumentation experiments only (KVC_ATT_DEBUG); 0 in production
   int32_t l2pf_pages;      // pages per domain K4 prefetches into L2 while it is latency bound
+  int32_t att_pf;          // K6 producer: the item's page this many pages ahead prefetched into L2 (0: off)
   PeerOut peer;            // fused output exchange (multi-GPU); peer.n == 0 when unused
 };
 

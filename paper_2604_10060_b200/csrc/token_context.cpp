@@ -110,6 +110,10 @@ TokenContext::TokenContext(const kvc_cfg& cfg, int d, int L) : cfg_(cfg), d_(d),
   da_.dom_done = static_cast<std::int32_t*>(dalloc(static_cast<std::size_t>(L) * 4));
   da_.work_ctr = ta_.work_ctr;
   da_.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(d)));
+  {
+    const char* pf = std::getenv("KVC_ATT_PF");  // K6: L2 prefetch distance in pages (0: off)
+    da_.att_pf = pf ? std::atoi(pf) : 0;
+  }
   da_.q = d_q_;
   ta_.q = d_q_;
   void* hs = nullptr;
