@@ -798,6 +798,36 @@ def offload_phase(args):
     kv.tier_sync()
     h2d_s = time.time() - t0
     s5 = kv.tier_stats()
+    # the reference's cross-layer prefetch (retrieval.cpp:117-128: layer l's query ranks layer
+    # l+1's clusters, which are fetched with cause Prefetch) turned on: its fetches are real H2D
+    # migrations on the transfer stream, issued after each step's replay while the next steps run.
+    # Measured on fresh cold queries with every resident cluster offloaded again first.
+    pf = {}
+    try:
+        kv.set_retrieval(prefetch_enabled=1, prefetch_k=TOP_K)
+        for c in [c for c in kv.cluster_ids() if kv.cluster(c)[0][6] == 0]:
+            kv.offload(c)
+        kv.tier_sync()
+        q2 = workload.queries_near(st, nq, seed=991)
+        l0, p0 = kv.ledger(), kv.tier_stats()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for i in range(nq):
+            kv.query(100000 + i, q2[i], out=out_dev)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        l1, p1 = kv.ledger(), kv.tier_stats()
+        causes = ("retrieval", "maintenance", "prefetch", "completion", "offload")
+        pf = {"cold_us_per_step_with_prefetch": round(ev0.elapsed_time(ev1) * 1e3 / nq, 2),
+              "ledger_h2d_bytes_per_step_by_cause": {causes[k]: int((l1[1][k] - l0[1][k]) / nq) for k in (0, 2, 3)},
+              "physical_h2d_bytes_per_step": int((p1["bytes_h2d"] - p0["bytes_h2d"]) / nq),
+              "migrations_in_flight_at_end": p1["in_flight"] + p1["queued"],
+              "note": "one step covers every layer at once, so a layer's prediction for layer l+1 is "
+                      "issued with (not ahead of) that layer's own selection: the side-stream fetches "
+                      "help the following steps only"}
+    except Exception as e:  # never lose the main line
+        pf = {"error": f"{type(e).__name__}: {e}"}
     return {
         "workload": "config3 per-GPU shard: 14 domains x 705,600 tokens (3600 frames x 196), 1,378 clusters/domain, "
                     "top-16 + 4-frame window, bf16; cold clusters in pinned host memory (cadence horizon 16)",
@@ -809,6 +839,7 @@ def offload_phase(args):
         "h2d_gbs_wall": round((s5["bytes_h2d"] - s4["bytes_h2d"]) / max(h2d_s, 1e-9) / 1e9, 2),
         "migrated_clusters": len(moved), "in_flight_at_end_of_cold_steps": s2["in_flight"] + s2["queued"],
         "dma_copies": {"offload_batch": s4["copies"] - s3["copies"], "fetch_batch": s5["copies"] - s4["copies"]},
+        "prefetch": pf,
     }
 
 

@@ -423,6 +423,17 @@ class ClusterKVCache:
     def check(self):
         _check(lib().kvc_check(self.h))
 
+    def set_retrieval(self, **fields):
+        """Per-call RetrievalConfig (kvc_set_retrieval): k_v, k_s, prefetch_k, prefetch_enabled,
+        lookup / compute cost constants; other fields keep the context's configuration."""
+        import copy
+
+        c = copy.copy(self.cfg)
+        for k, v in fields.items():
+            setattr(c, k, v)
+        _check(lib().kvc_set_retrieval(self.h, C.byref(c)))
+        self.cfg = c
+
     def offload(self, cid: int) -> float:
         c = C.c_double()
         _check(lib().kvc_offload(self.h, cid, C.byref(c)))
