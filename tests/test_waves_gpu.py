@@ -48,9 +48,10 @@ def _drift_pair(monkeypatch, perturb: bool, D=8, N=24_000, C=48, frames=6, pre=0
     return kvs, outs
 
 
-@pytest.mark.parametrize("perturb", [False, True])
-def test_waves_equal_sequential_drift(monkeypatch, perturb):
-    (seq, wav), outs = _drift_pair(monkeypatch, perturb)
+@pytest.mark.parametrize("perturb,D,frames", [(False, 8, 6), (True, 8, 6), (False, 32, 14)],
+                         ids=["8dom", "8dom-perturbed", "32dom-14frames"])
+def test_waves_equal_sequential_drift(monkeypatch, perturb, D, frames):
+    (seq, wav), outs = _drift_pair(monkeypatch, perturb, D=D, frames=frames)
     ms, mw = seq.maint_stats(), wav.maint_stats()
     assert ms.tolist() == mw.tolist()
     assert ms[2] >= 8, "the drift frames must split"
@@ -60,6 +61,8 @@ def test_waves_equal_sequential_drift(monkeypatch, perturb):
         np.testing.assert_array_equal(a, b)
     prof = wav.wave_profile()
     assert prof["events"] >= ms[2]
+    if D >= 32:  # enough domains that predictions go wrong and domains are rolled back on their own
+        assert prof["rolled_back_domains"] > 0
     if perturb:
         assert prof["rolled_back_domains"] > 0 and prof["passes"] > prof["frames_with_events"]
 
