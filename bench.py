@@ -833,6 +833,14 @@ def offload_phase(args):
                     "top-16 + 4-frame window, bf16; cold clusters in pinned host memory (cadence horizon 16)",
         "cold_us_per_step": round(cold_us, 2), "hot_us_per_step": round(hot_us, 2),
         "cold_fetches_per_step": round((s3["fetches"] - s1["fetches"]) / args.steps, 1),
+        # fetch-on-read: the step copies its selected Host clusters into HBM between K4 and K6
+        # (select.cu R6 + tiers.cu k_fetch_read) instead of K6 reading them in place and the queued
+        # fetch migration reading them again
+        "fetch_on_read": {
+            "clusters_per_step": round((s3["read_fetches"] - s1["read_fetches"]) / args.steps, 1),
+            "h2d_bytes_per_step": int((s3["read_fetch_bytes"] - s1["read_fetch_bytes"]) / args.steps),
+            "link_gbs_over_cold_step": round((s3["read_fetch_bytes"] - s1["read_fetch_bytes"]) / args.steps
+                                             / max(cold_us, 1e-9) / 1e3, 2)},
         "host_pages_after_cadence": s0["host_pages"], "host_bytes_after_cadence": s0["host_pages"] * 2 * 64 * HEAD_DIM * 2,
         "offload_wall_s": round(offload_s, 3), "setup_s": round(setup_s, 2),
         "d2h_gbs_wall": round((s4["bytes_d2h"] - s3["bytes_d2h"]) / max(d2h_s, 1e-9) / 1e9, 2),

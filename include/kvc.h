@@ -209,10 +209,14 @@ KVC_API int kvc_fetch(kvc_ctx* ctx, int64_t id, int32_t cause, double* cost_us);
  * per cluster on a transfer stream (K5), asynchronously. Kernels address pages wherever they
  * physically are, so results never depend on migration progress.
  * kvc_tier_sync completes every queued / in-flight migration (physical == logical residence).
- * kvc_tier_stats out[12]: host pages in use, host-tier capacity (pages), clusters with host pages,
+ * A decode step copies the host pages of the clusters it selected into HBM itself, between
+ * selection and attention (fetch-on-read: one crossing of the host link; KVC_FETCH_ON_READ=0
+ * leaves them to the queued fetch migrations while attention reads them in place).
+ * kvc_tier_stats out[14]: host pages in use, host-tier capacity (pages), clusters with host pages,
  * offloads committed, fetches committed, bytes device->host, bytes host->device, migrations
  * queued, batches in flight, HBM staging pages in use, batches started, DMA copies issued
- * (per-cluster copies merged when both sides are contiguous). */
+ * (per-cluster copies merged when both sides are contiguous), fetches done by fetch-on-read and
+ * their bytes (included in the fetch / host->device totals). */
 KVC_API int kvc_tier_sync(kvc_ctx* ctx);
 KVC_API int kvc_tier_stats(kvc_ctx* ctx, int64_t* out);
 /* out[3]: first host page of the cluster's extent (-1 none), its length in pages, migration busy */

@@ -446,14 +446,15 @@ class ClusterKVCache:
 
     # ------------------------------------------------------------------ physical host tier
     TIER_KEYS = ("host_pages", "host_capacity_pages", "host_clusters", "offloads", "fetches",
-                 "bytes_d2h", "bytes_h2d", "queued", "in_flight", "stage_pages", "batches", "copies")
+                 "bytes_d2h", "bytes_h2d", "queued", "in_flight", "stage_pages", "batches", "copies",
+                 "read_fetches", "read_fetch_bytes")
 
     def tier_sync(self):
         """Completes every queued / in-flight host-tier migration (kvc_tier_sync)."""
         _check(lib().kvc_tier_sync(self.h))
 
     def tier_stats(self) -> dict:
-        out = np.zeros(12, np.int64)
+        out = np.zeros(len(self.TIER_KEYS), np.int64)
         _check(lib().kvc_tier_stats(self.h, _p(out, i64p)))
         return dict(zip(self.TIER_KEYS, (int(x) for x in out)))
 

@@ -386,6 +386,15 @@ void Context::alloc_device() {
   }
   d_q_ = static_cast<float*>(dalloc(L * d * 4));
   d_out_ = static_cast<float*>(dalloc(L * d * 4));
+  if (t_.max_hpages > 0) {  // fetch-on-read (DecodeArgs::fr_*): copy lists, one per domain
+    const char* e = std::getenv("KVC_FETCH_ON_READ");
+    fr_enabled_ = !(e && e[0] == '0');
+    da_.fr_jobs = static_cast<int4*>(dalloc(L * da_.max_desc * sizeof(int4)));
+    da_.fr_nj = static_cast<std::int32_t*>(dalloc(L * 4));
+    da_.fr_reserve = static_cast<std::int32_t>(std::min<std::int64_t>(t_.max_pages / 16 + 2LL * t_.maxp, t_.max_pages));
+  } else {
+    fr_enabled_ = false;
+  }
   KVC_CUDA(cudaStreamSynchronize(st_));
 }
 
@@ -484,9 +493,12 @@ void Context::alloc_result_blocks(std::int32_t kv, std::int32_t ks, std::int32_t
   const std::size_t o_parts = carve(L * kv * 4), o_nps = carve(L * 4), o_rs = carve(L * ks * 4),
                     o_rb = carve(L * ks), o_nr = carve(L * 4), o_ps = carve(L * kp * 4),
                     o_pb = carve(L * kp), o_np = carve(L * 4), o_vs = carve(L * ks * 4),
-                    o_nv = carve(L * 4), o_att = carve(L * 8), o_nc = carve(L * 4), o_fl = carve(L * 4), o_ew = carve(L * 4);
+                    o_nv = carve(L * 4), o_att = carve(L * 8), o_nc = carve(L * 4), o_fl = carve(L * 4), o_ew = carve(L * 4),
+                    o_frn = carve(L * 4);
+  dec_lean_bytes_ = off;  // the fetch-on-read records go last: copied only by steps that use them
+  const std::size_t o_frr = carve(L * std::min<std::int32_t>(std::max<std::int32_t>(ks, 1), 64) * 16);
   dec_bytes_ = off;
-  res_off_ = {o_parts, o_nps, o_rs, o_rb, o_nr, o_ps, o_pb, o_np, o_vs, o_nv, o_att, o_nc, o_fl, o_ew};
+  res_off_ = {o_parts, o_nps, o_rs, o_rb, o_nr, o_ps, o_pb, o_np, o_vs, o_nv, o_att, o_nc, o_fl, o_ew, o_frn, o_frr};
   for (int b = 0; b < 2; ++b) {
     d_blk_[b] = dalloc(dec_bytes_);
     h_blk_[b] = halloc(dec_bytes_);
@@ -514,6 +526,9 @@ void Context::set_result_block(int b) {
   da_.n_cand = reinterpret_cast<std::int32_t*>(base + o.nc);
   da_.flags = reinterpret_cast<std::int32_t*>(base + o.fl);
   da_.errw = reinterpret_cast<std::int32_t*>(base + o.ew);
+  da_.fr_n = reinterpret_cast<std::int32_t*>(base + o.frn);
+  da_.fr_rec = reinterpret_cast<int4*>(base + o.frr);
+  da_.fr_max = std::min<std::int32_t>(std::max<std::int32_t>(ks_cap_, 1), 64);
   d_dec_ = d_blk_[b];
 }
 

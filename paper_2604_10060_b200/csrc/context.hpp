@@ -320,8 +320,12 @@ class Context {
   cudaStream_t cs_ = nullptr;                    // copy stream for the result blocks
   void* d_blk_[2] = {nullptr, nullptr};
   struct ResultOffsets {
-    std::size_t parts, nps, rs, rb, nr, ps, pb, np, vs, nv, att, nc, fl, ew;
+    std::size_t parts, nps, rs, rb, nr, ps, pb, np, vs, nv, att, nc, fl, ew, frn, frr;
   } res_off_{};
+  std::size_t dec_lean_bytes_ = 0;       // the block without the fetch-on-read records
+  bool blk_fr_[2] = {false, false};      // block b's step ran with fetch-on-read
+  bool fr_enabled_ = true;               // KVC_FETCH_ON_READ (default 1)
+  void fr_commit(int b);
   void set_result_block(int b);
   cudaEvent_t evb_[2][4] = {{nullptr, nullptr, nullptr, nullptr}, {nullptr, nullptr, nullptr, nullptr}};
   bool step_timed_[2] = {false, false};
@@ -427,7 +431,8 @@ class Context {
   std::int32_t* tier_scratch_ = nullptr;  // [kTierMaxBatch][maxp] device (fetch commit)
   std::uint8_t* tier_stage_ = nullptr;    // HBM staging pages
   cudaStream_t xs_ = nullptr;             // transfer stream (copy engines)
-  std::int64_t tier_n_[6] = {0, 0, 0, 0, 0, 0};  // offloads, fetches, bytes d2h, bytes h2d, batches, copies
+  // offloads, fetches, bytes d2h, bytes h2d, batches, copies, fetch-on-read clusters / bytes
+  std::int64_t tier_n_[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   void tier_alloc();
   void tier_note(std::int64_t id, bool to_host);  // a logical residence change (offload / fetch)
   void tier_forget(std::int64_t id);              // the cluster is being removed

@@ -78,6 +78,8 @@ void Context::launch_step(int b, const float* q, int q_mem, float* out, int out_
   da_.q = dq;
   da_.out = (out && out_mem == KVC_MEM_DEVICE) ? out : (out_map ? out_map : d_out_);
   da_.n_parts_host = static_cast<std::int32_t>(parts_.size());
+  da_.fr_on = fr_enabled_ && hext_alloc_.used() > 0 ? 1 : 0;  // some cluster has host pages
+  blk_fr_[b] = da_.fr_on != 0;
   const int nl = launch_decode(t_, da_, st_, timing_ ? evb_[b] : nullptr, ev_k4_[b]);
   if (nl < 2)
     fail(-20, "decode kernels could not be launched for d = " + std::to_string(d_) +
@@ -86,7 +88,7 @@ void Context::launch_step(int b, const float* q, int q_mem, float* out, int out_
   KVC_CUDA(cudaGetLastError());  // launch-configuration failures surface here, not as empty results
   // the result block goes to the host on the copy stream as soon as K4 is done (overlaps K6)
   KVC_CUDA(cudaStreamWaitEvent(cs_, ev_k4_[b], 0));
-  KVC_CUDA(cudaMemcpyAsync(h_blk_[b], d_blk_[b], dec_bytes_, cudaMemcpyDeviceToHost, cs_));
+  KVC_CUDA(cudaMemcpyAsync(h_blk_[b], d_blk_[b], da_.fr_on ? dec_bytes_ : dec_lean_bytes_, cudaMemcpyDeviceToHost, cs_));
   KVC_CUDA(cudaEventRecord(ev_step_[b], cs_));
   if (out && out_mem != KVC_MEM_DEVICE && !out_map)
     KVC_CUDA(cudaMemcpyAsync(out, d_out_, static_cast<std::size_t>(L_) * d_ * 4, cudaMemcpyDeviceToHost, st_));
@@ -124,6 +126,7 @@ bool Context::finish_step(int b) {
     KVC_CUDA(cudaEventElapsedTime(&ms, evb_[b][0], evb_[b][3]));
     step_t_[3] = ms * 1e3;
   }
+  fr_commit(b);
   std::vector<std::int64_t> gt;
   gt.swap(step_gt_[b]);
   const auto w2 = std::chrono::steady_clock::now();  // (after the instrumentation's event wait)
@@ -131,6 +134,35 @@ bool Context::finish_step(int b) {
   step_t_[5] = std::chrono::duration<double, std::micro>(w1 - w0).count();
   step_t_[6] = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - w2).count();
   return settle;
+}
+
+// Fetch-on-read bookkeeping of step buffer b (select.cu / tiers.cu k_fetch_read): each listed
+// cluster's host pages now have HBM copies the page table names, so its extent is released here
+// -- the physical side of the fetch the replay records for it (store.cpp:95-116). A record whose
+// extent is no longer the cluster's current one (re-offloaded meanwhile, or the cluster gone) is
+// skipped: the migration that replaced it already released the old extent.
+void Context::fr_commit(int b) {
+  if (!blk_fr_[b]) return;
+  blk_fr_[b] = false;
+  const auto* base = static_cast<const std::uint8_t*>(h_blk_[b]);
+  const auto* n = reinterpret_cast<const std::int32_t*>(base + res_off_.frn);
+  const auto* rec = reinterpret_cast<const std::int32_t*>(base + res_off_.frr);
+  for (int l = 0; l < L_; ++l)
+    for (int j = 0; j < n[l]; ++j) {
+      const std::int32_t* r = rec + (static_cast<std::int64_t>(l) * da_.fr_max + j) * 4;
+      const std::int64_t id = static_cast<std::int64_t>(static_cast<std::uint32_t>(r[0])) |
+                              (static_cast<std::int64_t>(r[1]) << 32);
+      if (id < 0 || id >= static_cast<std::int64_t>(clusters_.size()) || !clusters_[static_cast<std::size_t>(id)] ||
+          static_cast<std::size_t>(id) >= hext_.size())
+        continue;
+      const Extent e = hext_[static_cast<std::size_t>(id)];
+      if (e.n != r[3] || e.start != r[2]) continue;
+      tier_forget(id);
+      tier_n_[1] += 1;
+      tier_n_[3] += e.n * t_.page_bytes;
+      tier_n_[6] += 1;
+      tier_n_[7] += e.n * t_.page_bytes;
+    }
 }
 
 // Exchange buffer of rank r: [2 step parities][total domains][d] f32, then n u64 arrival flags.
@@ -187,6 +219,8 @@ void Context::decode_step(std::int64_t qid, const float* q, int q_mem, float* ou
     // the previous step's bookkeeping runs on the host while this step runs on the GPU
     if (finish_step(pb)) {  // it settled a split: this step saw the pre-settle index
       KVC_CUDA(cudaStreamSynchronize(st_));
+      KVC_CUDA(cudaEventSynchronize(ev_step_[cur_]));
+      fr_commit(cur_);  // the discarded launch's fetch-on-read copies did happen
       launch_step(cur_, q, q_mem, out, out_mem);
     }
   }

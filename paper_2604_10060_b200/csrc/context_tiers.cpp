@@ -8,6 +8,9 @@
 //   offload: count pages (K) -> gather pages to staging + seal them (K) -> D2H per cluster (xs_)
 //            -> commit: page ids become host ids, HBM pages return to the free stack (K)
 //   fetch:   H2D per cluster (xs_) -> commit: fresh HBM pages filled from staging, ids rewritten (K)
+//   fetch-on-read: a decode step's selected Host clusters are copied by the step itself (K4 takes
+//            the pages, k_fetch_read copies, tiers.cu); Context::fr_commit then drops the extent,
+//            so the queued fetch finds nothing left to move
 // Phases advance when their event has completed (tier_kick polls; nothing blocks the decode
 // pipeline). Until a migration commits, every kernel keeps addressing the pages where they are
 // (page_k/page_v resolve host ids through the mapping), so results never depend on migration
@@ -241,7 +244,7 @@ bool Context::tier_advance(TierBatch& b, bool block) {
     std::int64_t total = 0;
     for (std::int32_t i = 0; i < n; ++i) {
       const std::int64_t id = b.ids[static_cast<std::size_t>(i)];
-      if (alive(id) && is_host(id) && cnt[i] > 0 && cnt[i] != hext_[static_cast<std::size_t>(id)].n) total += cnt[i];
+      if (alive(id) && is_host(id) && cnt[i] > 0) total += cnt[i];
     }
     std::int64_t hbig = total > 0 ? hext_alloc_.alloc(total) : -1;
     std::int64_t sbig = hbig >= 0 ? stage_alloc_.alloc(total) : -1;
@@ -253,7 +256,7 @@ bool Context::tier_advance(TierBatch& b, bool block) {
       const std::int64_t id = b.ids[static_cast<std::size_t>(i)];
       const std::int32_t np = cnt[i];
       mv[i] = TierMove{-1, 0, 0, 0};
-      if (!alive(id) || !is_host(id) || np <= 0 || np == hext_[static_cast<std::size_t>(id)].n) continue;
+      if (!alive(id) || !is_host(id) || np <= 0) continue;  // np == 0: every page already in the host tier
       std::int64_t h0, s0;
       if (hbig >= 0) {
         h0 = hbig;
@@ -390,6 +393,8 @@ void Context::tier_stats(std::int64_t* out) const {
   out[9] = stage_alloc_.used();
   out[10] = tier_n_[4];
   out[11] = tier_n_[5];
+  out[12] = tier_n_[6];
+  out[13] = tier_n_[7];
 }
 
 void Context::cluster_tier(std::int64_t id, std::int64_t* out) const {

@@ -2608,6 +2608,7 @@ int launch_decode(const DevTables& t, const DecodeArgs& a, cudaStream_t st, cuda
   } else {
     const size_t smem4 = k4_smem_bytes(t.d, t.cmax, a.n_parts_host, t.W, t.tmax);
     if (!smem_optin(reinterpret_cast<const void*>(k_score_select), smem4)) return 0;
+    if (a.fr_on) cudaMemsetAsync(a.fr_n, 0, static_cast<size_t>(t.L) * 4, st);  // (fetch-on-read is K4 v3's)
     k_score_select<<<t.L, 256, smem4, st>>>(t, a, a.work_ctr);
   }
   // K6 is a programmatic dependent of K4 (PDL: its launch and prologue overlap K4) unless an event
@@ -2618,9 +2619,10 @@ int launch_decode(const DevTables& t, const DecodeArgs& a, cudaStream_t st, cuda
     pdl_env = (e && e[0] == '0') ? 0 : 1;
   }
   const bool pdl = pdl_env && !ev && used3;
+  int n = 1;
+  if (a.fr_on && used3) n += launch_fetch_read(t, a, st, pdl);  // K4 -> fetch-on-read copies -> K6
   if (ev) cudaEventRecord(ev[1], st);
   if (k4_done && !pdl) cudaEventRecord(k4_done, st);
-  int n = 1;
   switch (t.d * 2 + t.kv_bf16) {
     case 64: n += launch_attend_t<32, false>(t, a, st, pdl); break;
     case 65: n += launch_attend_t<32, true>(t, a, st, pdl); break;

@@ -225,6 +225,19 @@ struct DecodeArgs {
   int32_t l2pf_pages;      // pages per domain K4 prefetches into L2 while it is latency bound
   int32_t att_pf;          // K6 producer: the item's page this many pages ahead prefetched into L2 (0: off)
   PeerOut peer;            // fused output exchange (multi-GPU); peer.n == 0 when unused
+  // fetch-on-read (select.cu R6 + tiers.cu k_fetch_read): a verified cluster whose member pages
+  // are in the host tier gets fresh HBM pages in K4 (all of its host pages or none, never below
+  // fr_reserve free pages); K4 points the work list at them and lists the copies, which
+  // k_fetch_read performs between K4 and K6 (one crossing of the host link instead of K6 reading
+  // in place and the fetch migration reading again). The host drops the cluster's extent from
+  // fr_rec when it replays the step (the reference's fetch of that cluster, store.cpp:95-116).
+  int32_t fr_on;           // 0: off (no host pages, K4 v1/v2, KVC_FETCH_ON_READ=0)
+  int32_t fr_reserve;      // free HBM pages K4 leaves untouched
+  int32_t fr_max;          // records per domain in fr_rec (>= k_s)
+  int4* fr_jobs;           // [L][max_desc] {host page, HBM page, slot, page index}
+  int32_t* fr_nj;          // [L] copies listed by K4
+  int32_t* fr_n;           // [L] migrated clusters (result block; written by K4 in every mode)
+  int4* fr_rec;            // [L][fr_max] {cluster id lo, hi, extent's first host page, pages}
 };
 
 // ----------------------------------------------------------------------------- launchers
@@ -293,6 +306,9 @@ struct TierMove {
 };
 // Offload, step 1: npages of each slot -> out[i] (for extent sizing).
 int launch_tier_count(const DevTables& t, const int32_t* slots, int32_t n, int32_t* out, cudaStream_t st);
+// fetch-on-read copies listed by K4 (DecodeArgs::fr_jobs), launched between K4 and K6 as a
+// programmatic dependent of K4 (K6 then depends on it); pdl as for K6.
+int launch_fetch_read(const DevTables& t, const DecodeArgs& a, cudaStream_t st, bool pdl);
 // Offload, step 2: pages [0, n_pages) of each slot (HBM or host) -> staging, seals them.
 int launch_tier_gather(const DevTables& t, const TierMove* mv, int32_t n, int32_t max_pages_per_cluster,
                        uint8_t* stage, cudaStream_t st);

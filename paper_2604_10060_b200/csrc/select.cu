@@ -67,6 +67,8 @@ struct Sel3Smem {
   unsigned long long ring_mask[64];  // per window page: tokens K6 attends (not owned by a verified cluster)
   unsigned ring_half[128];           // the same, 32 tokens per word as the ring pass writes them
   int vhash[128];
+  int fr_base[64], fr_job[64];  // fetch-on-read: free-stack base / first copy of verified cluster v
+  int fr_cnt, fr_jn;
   float red[K5W];
   int redi[32];
 };
@@ -162,6 +164,8 @@ __global__ void __launch_bounds__(K5T) k_select3(DevTables t, DecodeArgs a, int*
     S.degen = 0;
     S.att = 0;
     S.lazy_any = 0;
+    S.fr_cnt = 0;
+    S.fr_jn = 0;
   }
   // first chunk of visual representatives (P <= 32 in one chunk) staged with the query loads
   const int p0rows = min(P, K5_SROWS);
@@ -642,6 +646,46 @@ __global__ void __launch_bounds__(K5T) k_select3(DevTables t, DecodeArgs a, int*
   }
   __syncthreads();
   K5MARK(5)
+  // fetch-on-read: a verified cluster whose member pages are in the host tier (its leading pages,
+  // store.cpp:95-130 / context_tiers.cpp) takes fresh HBM pages for all of them (CAS on the free
+  // stack, never below fr_reserve; none when that fails: K6 then reads them in place). The work
+  // list below names the new pages and k_fetch_read fills them before K6 runs.
+  if (a.fr_on) {
+    for (int v = warp; v < nv; v += K5W) {
+      const int s = S.vers[v];
+      const int np = S.snp[S.vsi[v]];
+      const int* list = t.pages + static_cast<int64_t>(s) * t.maxp;
+      int nh = 0, last = -1;
+      for (int k0 = 0; k0 < np; k0 += 32) {
+        const unsigned m = __ballot_sync(kFull, k0 + lane < np && is_host_page(t, list[k0 + lane]));
+        nh += __popc(m);
+        if (m) last = k0 + 31 - __clz(static_cast<int>(m));
+      }
+      if (lane == 0) {
+        int base = -1;
+        if (nh > 0 && last + 1 == nh) {
+          int top = *reinterpret_cast<volatile int*>(t.free_top);
+          while (top - nh >= a.fr_reserve) {
+            const int old = atomicCAS(t.free_top, top, top - nh);
+            if (old == top) {
+              base = top - nh;
+              break;
+            }
+            top = old;
+          }
+        }
+        if (base >= 0) {
+          const int j = atomicAdd(&S.fr_cnt, 1);
+          const long long cid = t.cid[s];
+          a.fr_rec[l * a.fr_max + j] = make_int4(static_cast<int>(cid & 0xffffffffll), static_cast<int>(cid >> 32),
+                                                 static_cast<int>(list[0] - t.max_pages), nh);
+          S.fr_job[v] = atomicAdd(&S.fr_jn, nh);
+        }
+        S.fr_base[v] = base;
+      }
+    }
+    __syncthreads();
+  }
   // R6 + R7: page ids, then fills
   int4* desc = a.desc + static_cast<int64_t>(l) * a.max_desc;
   const int ndesc = min(S.voff[nv], a.max_desc);
@@ -659,6 +703,12 @@ __global__ void __launch_bounds__(K5T) k_select3(DevTables t, DecodeArgs a, int*
       const int np = S.snp[S.vsi[lo]];
       isb = k >= np;
       page = isb ? t.bpages[static_cast<int64_t>(s) * t.maxbp + (k - np)] : t.pages[static_cast<int64_t>(s) * t.maxp + k];
+      if (a.fr_on && !isb && S.fr_base[lo] >= 0 && is_host_page(t, page)) {  // leading: k < its host page count
+        const int dst = t.free_stack[S.fr_base[lo] + k];
+        a.fr_jobs[static_cast<int64_t>(l) * a.max_desc + S.fr_job[lo] + k] = make_int4(page, dst, s, k);
+        desc[i] = make_int4(dst, t.pg_fill[page], -1, -1);
+        page = -1;
+      }
     }
     if (page >= 0) desc[i] = make_int4(page, t.pg_fill[page] | (isb << 16), -1, -1);
   }
@@ -673,6 +723,8 @@ __global__ void __launch_bounds__(K5T) k_select3(DevTables t, DecodeArgs a, int*
   K5MARK(6)
 #undef K5MARK
   if (tid == 0) {
+    a.fr_n[l] = a.fr_on ? S.fr_cnt : 0;
+    if (a.fr_on) a.fr_nj[l] = S.fr_jn;
     __threadfence();
     a.errw[l] = atomicOr(t.err, 0);
   }

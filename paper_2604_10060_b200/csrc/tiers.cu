@@ -5,8 +5,11 @@
 // contiguous extent of pinned, mapped host pages (the cluster's pages back to back), so a fetch
 // or an offload is one cudaMemcpyAsync per cluster on the transfer stream between that extent and
 // a contiguous staging run in HBM. The kernels below move pages between the (scattered) HBM page
-// pool and the staging run and rewrite the page tables; the bulk bytes cross the host link on the
-// copy engines, never through SM loads.
+// pool and the staging run and rewrite the page tables; the bulk bytes of queued migrations cross
+// the host link on the copy engines. The one exception is fetch-on-read (k_fetch_read): the pages
+// of host-resident clusters a decode step selected are copied by SM loads between K4 and K6,
+// because K6 needs them within the step anyway (the reference fetches every verified cluster,
+// retrieval.cpp:76-89); K6 then reads the fresh (L2-resident) HBM copies.
 #include "devmath.cuh"
 
 namespace kvc {
@@ -23,9 +26,54 @@ __device__ __forceinline__ void copy_page(uint8_t* dst, const uint8_t* src, int6
   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) d[i] = s[i];
 }
 
+// Member pages to move, 0 when every one is already in the host tier (nothing to offload).
 __global__ void k_tier_count(DevTables t, const int32_t* slots, int n, int32_t* out) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) out[i] = t.npages[slots[i]];
+  if (i >= n) return;
+  const int np = t.npages[slots[i]];
+  const int* list = t.pages + static_cast<int64_t>(slots[i]) * t.maxp;
+  int dev = 0;
+  for (int p = 0; p < np; ++p) dev += is_host_page(t, list[p]) ? 0 : 1;
+  out[i] = dev > 0 ? np : 0;
+}
+
+// Fetch-on-read copies (DecodeArgs::fr_jobs, listed by K4): one CTA per page, 8 x 16 B loads per
+// thread in flight (a 32 KB page in one round trip over the host link); then the page table
+// entry and the fill move to the HBM page. K6 (a programmatic dependent) waits for this grid.
+__global__ void __launch_bounds__(256) k_fetch_read(DevTables t, DecodeArgs a) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;");
+  int any = 0;
+  for (int l = threadIdx.x; l < t.L; l += blockDim.x) any |= a.fr_nj[l];
+  if (!__syncthreads_or(any)) return;  // a hot step: nothing to copy
+  const int64_t n16 = t.page_bytes / 16;
+  int base = 0, g = blockIdx.x;
+  for (int l = 0; l < t.L; ++l) {
+    const int nj = a.fr_nj[l];
+    for (; g < base + nj; g += gridDim.x) {
+      const int4 j = a.fr_jobs[static_cast<int64_t>(l) * a.max_desc + (g - base)];
+      const uint4* src = reinterpret_cast<const uint4*>(page_k(t, j.x));
+      uint4* dst = reinterpret_cast<uint4*>(page_k(t, j.y));
+      for (int64_t i0 = 0; i0 < n16; i0 += 8 * 256) {
+        uint4 r[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int64_t i = i0 + u * 256 + threadIdx.x;
+          if (i < n16) r[u] = src[i];
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int64_t i = i0 + u * 256 + threadIdx.x;
+          if (i < n16) dst[i] = r[u];
+        }
+      }
+      if (threadIdx.x == 0) {
+        t.pg_fill[j.y] = t.pg_fill[j.x];
+        t.pages[static_cast<int64_t>(j.z) * t.maxp + j.w] = j.y;
+      }
+    }
+    base += nj;
+  }
 }
 
 // grid (x: pages, y: clusters): member page p of cluster y -> staging page stage0 + p. Pages already
@@ -124,6 +172,20 @@ __global__ void k_tier_fetch_tables(DevTables t, const TierMove* mv, int n, cons
 int launch_tier_count(const DevTables& t, const int32_t* slots, int32_t n, int32_t* out, cudaStream_t st) {
   if (n <= 0) return 0;
   k_tier_count<<<(n + 255) / 256, 256, 0, st>>>(t, slots, n, out);
+  return 1;
+}
+
+int launch_fetch_read(const DevTables& t, const DecodeArgs& a, cudaStream_t st, bool pdl) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(2 * device_sms()));
+  cfg.blockDim = dim3(256);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k_fetch_read, t, a);
   return 1;
 }
 

@@ -116,3 +116,60 @@ def test_host_tier_full_fails_loudly():
             if kv.cluster(c)[0][6] == 0:
                 kv.offload(c)
         kv.tier_sync()
+
+
+def _offloaded_engine(monkeypatch, fr: bool):
+    """config-1 stream, 40 frames ingested, every Device cluster offloaded and synced."""
+    from paper_2604_10060_b200 import ClusterKVCache
+
+    monkeypatch.setenv("KVC_FETCH_ON_READ", "1" if fr else "0")
+    s = po.gen_stream_restated(po.config1_stream())
+    ecfg = po.config1_engine(offload_horizon_frames=1 << 20)
+    kv = ClusterKVCache(product_config(ecfg, check_invariants=0), s.d, s.L)
+    monkeypatch.delenv("KVC_FETCH_ON_READ")
+    n = 0
+    for kind, i in s.events():
+        if kind == "frame":
+            kv.process_frame(i, s.visual[i], s.keys[i], s.values[i])
+            n += 1
+            if n == 40:
+                break
+    kv.tier_sync()
+    for c in kv.cluster_ids():
+        if kv.cluster(c)[0][6] == 0:
+            kv.offload(c)
+    kv.tier_sync()
+    return s, kv
+
+
+def test_fetch_on_read(monkeypatch):
+    """A decode step copies its selected Host clusters into HBM between K4 and K6 (select.cu R6,
+    tiers.cu k_fetch_read): same outputs and the same logical ledger as the queued-fetch path,
+    extents released, page tables consistent, payloads bit for bit, nothing left to migrate."""
+    runs = [_offloaded_engine(monkeypatch, fr) for fr in (False, True)]
+    s = runs[0][0]
+    payload = {c: runs[0][1].cluster_payload(c) for c in runs[0][1].cluster_ids()}
+    outs = [[], []]
+    for j, (_, kv) in enumerate(runs):
+        for qi in range(6):
+            outs[j].append(kv.query(qi, s.q[qi % len(s.q)]).copy())
+    for a, b in zip(*outs):
+        np.testing.assert_array_equal(a, b)
+    (_, off), (_, on) = runs
+    lo, ln = off.ledger(), on.ledger()
+    assert np.array_equal(lo[0], ln[0]) and np.array_equal(lo[1], ln[1])
+    st = on.tier_stats()
+    assert st["read_fetches"] > 0 and st["read_fetch_bytes"] > 0, st
+    assert off.tier_stats()["read_fetches"] == 0
+    for kv in (off, on):
+        kv.tier_sync()
+        assert kv.tier_check() == (0, 0, 0, 0)
+    for c in on.cluster_ids():
+        k, v = on.cluster_payload(c)
+        assert np.array_equal(k, payload[c][0]) and np.array_equal(v, payload[c][1])
+        if on.cluster(c)[0][6] == 0:  # Device: no extent left behind
+            assert on.cluster_tier(c)[1] == 0
+    # the copies replaced the queued fetches' host-link traffic
+    st_on, st_off = on.tier_stats(), off.tier_stats()
+    assert st_on["bytes_h2d"] == st_off["bytes_h2d"], (st_on, st_off)
+    assert st_on["copies"] < st_off["copies"]
