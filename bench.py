@@ -828,6 +828,26 @@ def offload_phase(args):
                       "help the following steps only"}
     except Exception as e:  # never lose the main line
         pf = {"error": f"{type(e).__name__}: {e}"}
+    # the host link's own copy-engine bandwidth (pinned 256 MiB, best of 5): the roofline of a cold step
+    link = {}
+    try:
+        hb = torch.empty(256 << 20, dtype=torch.uint8, pin_memory=True)
+        db = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+        for name, (dst, src) in (("h2d", (db, hb)), ("d2h", (hb, db))):
+            best = 1e30
+            for _ in range(6):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                torch.cuda.synchronize()
+                e0.record()
+                dst.copy_(src, non_blocking=True)
+                e1.record()
+                torch.cuda.synchronize()
+                best = min(best, e0.elapsed_time(e1))
+            link[name + "_gbs"] = round(hb.numel() / (best * 1e-3) / 1e9, 2)
+        del hb, db
+    except Exception as e:
+        link = {"error": f"{type(e).__name__}: {e}"}
+    fr_bytes = (s3["read_fetch_bytes"] - s1["read_fetch_bytes"]) / args.steps
     return {
         "workload": "config3 per-GPU shard: 14 domains x 705,600 tokens (3600 frames x 196), 1,378 clusters/domain, "
                     "top-16 + 4-frame window, bf16; cold clusters in pinned host memory (cadence horizon 16)",
@@ -839,8 +859,12 @@ def offload_phase(args):
         "fetch_on_read": {
             "clusters_per_step": round((s3["read_fetches"] - s1["read_fetches"]) / args.steps, 1),
             "h2d_bytes_per_step": int((s3["read_fetch_bytes"] - s1["read_fetch_bytes"]) / args.steps),
-            "link_gbs_over_cold_step": round((s3["read_fetch_bytes"] - s1["read_fetch_bytes"]) / args.steps
-                                             / max(cold_us, 1e-9) / 1e3, 2)},
+            "link_gbs_over_cold_step": round(fr_bytes / max(cold_us, 1e-9) / 1e3, 2),
+            # the copies' share of the step: cold minus hot time (K4 / K6 / launches as in a hot step)
+            "link_gbs_over_copy_time": round(fr_bytes / max(cold_us - hot_us, 1e-9) / 1e3, 2),
+            "link_frac": round(fr_bytes / max(cold_us - hot_us, 1e-9) / 1e3 / link["h2d_gbs"], 3)
+            if "h2d_gbs" in link else None},
+        "host_link_copy_engine": dict(link, how="pinned 256 MiB tensor copy, best of 6, CUDA events"),
         "host_pages_after_cadence": s0["host_pages"], "host_bytes_after_cadence": s0["host_pages"] * 2 * 64 * HEAD_DIM * 2,
         "offload_wall_s": round(offload_s, 3), "setup_s": round(setup_s, 2),
         "d2h_gbs_wall": round((s4["bytes_d2h"] - s3["bytes_d2h"]) / max(d2h_s, 1e-9) / 1e9, 2),
