@@ -376,6 +376,9 @@ KVC_API void kvc_host_rng_first2(uint64_t seed, uint64_t* fast2, uint64_t* std2)
  * from a fresh exact cosine, and the margin the resolve kernels certify with. */
 KVC_API int kvc_debug_assign_check(kvc_ctx* ctx, const void* keys, int32_t T, int64_t partition, int32_t mem,
                                    double* out4);
+/* Debug: the kernels' reciprocal division (one RN(1/b) + two FMA corrections) against __ddiv_rn on
+ * n random operands: integer divisors in [1, max_den], or (max_den <= 0) real divisors in
+ * [2^-8, 2^8) with float numerators (the unit rows of the split k-means). */
 KVC_API int kvc_debug_div_check(uint64_t n, uint64_t seed, int32_t max_den, uint64_t* mismatches);
 KVC_API int kvc_debug_resolve_profile(kvc_ctx* ctx, double* out);
 /* Host-event slow path profile (cumulative since creation / the last reset), out10: microseconds in

@@ -1225,7 +1225,11 @@ void Context::launch_round(const std::vector<int>& active, const std::vector<int
     KVC_CUDA(cudaEventRecord(ev_act_[slot], st_));
   }
   round_timed_ = timing_;
-  ia_.exact_all = round_after_event_ ? 1 : 0;
+  static const bool exact_all_env = [] {  // KVC_EXACT_ALL=1: every round as a relaunch round (profiling)
+    const char* e = std::getenv("KVC_EXACT_ALL");
+    return e && e[0] == '1';
+  }();
+  ia_.exact_all = round_after_event_ || exact_all_env ? 1 : 0;
   if (timing_) KVC_CUDA(cudaEventRecord(ev_[0], st_));
   launches_ += launch_build_cands(t_, ia_, st_);
   if (timing_) KVC_CUDA(cudaEventRecord(ev_[1], st_));

@@ -497,7 +497,7 @@ void Context::run_inserts_waves(std::int64_t frame_id, std::int64_t pid, int T, 
       idx_off[j] = idx.size();
       for (int r : rows) idx.push_back(static_cast<std::int32_t>(e.row0 + r));
       scr_off[j] = scr;
-      scr += (rows.size() * (2 * static_cast<std::size_t>(d_) + 3) + 2) * 8;
+      scr += ((rows.size() * (2 * static_cast<std::size_t>(d_) + 3) + 2) * 8 + 15) & ~std::size_t{15};  // 16-byte rows
       out_off[j] = outw;
       outw += rows.size() + 4;
       if (J.given) {
@@ -545,10 +545,31 @@ void Context::run_inserts_waves(std::int64_t frame_id, std::int64_t pid, int T, 
       }
     }
     std::uint8_t* db = W.up.send(st_);
+    static long long* sprof = [] {  // KVC_SPLIT_PROF=1: per-job phase clocks (development)
+      const char* e = std::getenv("KVC_SPLIT_PROF");
+      long long* p = nullptr;
+      if (e && e[0] == '1') {
+        KVC_CUDA(cudaMalloc(&p, 8192 * 16 * 8));
+        split_prof_set(p);
+      }
+      return p;
+    }();
     launches_ += launch_split_two_batch(t_, reinterpret_cast<const SplitJob*>(db + o_jobs), static_cast<int>(nj), d_, st_);
     W.h_out.ensure(obj_off, st_);
     KVC_CUDA(cudaMemcpyAsync(W.h_out.p, dout, obj_off, cudaMemcpyDeviceToHost, st_));
     sync();
+    if (sprof && nj <= 8192) {
+      std::vector<long long> pr(nj * 16);
+      KVC_CUDA(cudaMemcpy(pr.data(), sprof, pr.size() * 8, cudaMemcpyDeviceToHost));
+      std::size_t jm = 0;
+      for (std::size_t j = 0; j < nj; ++j)
+        if (!jobs[j].given && (jobs[jm].given || pr[j * 16 + 11] > pr[jm * 16 + 11])) jm = j;
+      if (!jobs[jm].given) {
+        std::string m = "[split-prof] jobs " + std::to_string(nj) + " max-n job:";
+        for (int k = 0; k < 12; ++k) m += " " + std::to_string(pr[jm * 16 + k]);
+        std::fprintf(stderr, "%s\n", m.c_str());
+      }
+    }
     if (waves_log_) {
       std::size_t nmax = 0, nsum = 0;
       int itmax = 0;
@@ -1073,6 +1094,12 @@ void Context::run_inserts_waves(std::int64_t frame_id, std::int64_t pid, int T, 
       for (int l : relaunch) {
         W.dom[static_cast<std::size_t>(l)].tie |= !tie_known || h_err_[1 + l] != 0;
         take_stop(l);
+      }
+      if (waves_log_) {
+        int cmin = T;
+        for (int c : rcur) cmin = std::min(cmin, c);
+        std::fprintf(stderr, "[waves] relaunch %zu domains (first token %d, seq %d): %.0f us incl. install\n", relaunch.size(),
+                     cmin, relaunch_seq_ ? 1 : 0, us(i0, clk::now()));
       }
       t_relaunch += us(r0, clk::now());
     } else {

@@ -391,6 +391,7 @@ struct SplitJob {
   const int32_t* assign_in;
 };
 int launch_split_two_batch(const DevTables& t, const SplitJob* jobs, int n_jobs, int d, cudaStream_t st);
+void split_prof_set(long long* p);  // KVC_SPLIT_PROF: per-job phase clocks [job][16] (nullptr: off)
 
 // ---- ingest wave engine (waves.cu, context_waves.cpp)
 // Staging of a slot's members (then its buffer when with_buf) and/or one frame row at row0.

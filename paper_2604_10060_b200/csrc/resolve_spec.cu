@@ -1148,7 +1148,10 @@ __global__ void k_div_check(uint64_t n, uint64_t seed, int max_den, unsigned lon
     x ^= x << 13;
     x ^= x >> 7;
     x ^= x << 17;
-    const double b = static_cast<double>(1 + (x % static_cast<uint64_t>(max_den)));
+    // max_den > 0: integer divisors (counts); otherwise real divisors in [2^-8, 2^8) (norms)
+    const double b = max_den > 0 ? static_cast<double>(1 + (x % static_cast<uint64_t>(max_den)))
+                                 : ldexp(1.0 + static_cast<double>(x >> 12) * 0x1p-52, static_cast<int>((x >> 4) % 16) - 8);
+    if (max_den <= 0) a = static_cast<double>(static_cast<float>(a));  // unit rows: float numerators
     const double y = __ddiv_rn(1.0, b);
     const double q = div_rcp(a, b, y);
     if (__double_as_longlong(q) != __double_as_longlong(__ddiv_rn(a, b))) ++nb;

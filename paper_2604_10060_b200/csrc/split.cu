@@ -53,7 +53,14 @@ __device__ __forceinline__ double cos_of(double dot, double nc) {
   return clamp1(ddiv(dot, nc));
 }
 
+// Phase clocks of the batched kernel (KVC_SPLIT_PROF, development): per job, cycles of
+// [unit rows, same check, seeding, assign+reseed+lists, centroid update, norms, cosines,
+// objective, compaction, child stats] and [10] iterations, [11] n.
+__device__ long long* g_split_prof = nullptr;
+
 struct SplitSmem {
+  long long pc[12];
+  long long pc_t;
   double cent[2][256];
   double cn[2];
   double prev;
@@ -160,48 +167,95 @@ __device__ __forceinline__ void centroid_norms(SplitSmem& S, int d) {
 // out: assign[n]; meta[4] = {k_live, iterations, degenerate, error}; objective[1].
 __device__ __forceinline__ void split_two_body(const float* rows, const int32_t* idx, int n, int d, int first,
                                                double uni, double* scratch, int32_t* assign, int32_t* meta,
-                                               double* objective) {
+                                               double* objective, double* S_ob) {
   __shared__ SplitSmem S;
-  __shared__ double S_ob[OBJ_CHUNK];
   __shared__ double S_mass;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   double* u = scratch;
   double* ut = u + static_cast<int64_t>(n) * d;
   double* sc = ut + static_cast<int64_t>(n) * d;
   double* nearv = sc + 2 * static_cast<int64_t>(n);
+  const bool prof = g_split_prof != nullptr;
+#define SPROF(k)                                   \
+  if (prof && tid == 0) {                          \
+    const long long c_ = clock64();                \
+    S.pc[k] += c_ - S.pc_t;                        \
+    S.pc_t = c_;                                   \
+  }
   if (tid == 0) {
     S.same = 1;
     S.degen = 0;
+    for (int k = 0; k < 12; ++k) S.pc[k] = 0;
+    S.pc[11] = n;
+    S.pc_t = clock64();
   }
   __syncthreads();
-  // unit rows (clustering.cpp:14-22): r / norm(r), stored row- and column-major
+  // unit rows (clustering.cpp:14-22): r / norm(r), stored row- and column-major. One point per
+  // thread (the norm is the reference's sequential sum); rows are read 16 bytes per load and the
+  // row-major copy written 16 bytes per store (each warp instruction touches 32 rows: 4x fewer
+  // of them than element-wise accesses)
+  const bool vec = (d & 3) == 0;
   for (int i = tid; i < n; i += SPT) {
     const float* p = rows + static_cast<int64_t>(idx[i]) * d;
     double s = 0.0;
-    for (int c0 = 0; c0 < d; c0 += 16) {  // 16 loads in flight ahead of the sequential sum
+    for (int c0 = 0; c0 < d; c0 += 16) {  // 16 elements in flight ahead of the sequential sum
       float x[16];
+      if (vec && c0 + 16 <= d) {
 #pragma unroll
-      for (int k = 0; k < 16; ++k) x[k] = c0 + k < d ? p[c0 + k] : 0.f;
+        for (int k = 0; k < 16; k += 4) {
+          const float4 v = *reinterpret_cast<const float4*>(p + c0 + k);
+          x[k] = v.x;
+          x[k + 1] = v.y;
+          x[k + 2] = v.z;
+          x[k + 3] = v.w;
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < 16; ++k) x[k] = c0 + k < d ? p[c0 + k] : 0.f;
+      }
 #pragma unroll
       for (int k = 0; k < 16; ++k)
         if (c0 + k < d) s = dadd(s, dmul(static_cast<double>(x[k]), static_cast<double>(x[k])));
     }
     const double nr = __dsqrt_rn(s);
     if (nr < 1e-12) S.degen = 1;
+    // RN(x / nr) for every element from one reciprocal (div_rcp: Markstein's correctly rounded
+    // step, bit-identical to __ddiv_rn; tests/test_kernels_gpu.py checks it on real divisors)
+    const double y = ddiv(1.0, nr);
+    double* ur = u + static_cast<int64_t>(i) * d;
     for (int c0 = 0; c0 < d; c0 += 16) {
       float x[16];
+      if (vec && c0 + 16 <= d) {
 #pragma unroll
-      for (int k = 0; k < 16; ++k) x[k] = c0 + k < d ? p[c0 + k] : 0.f;
+        for (int k = 0; k < 16; k += 4) {
+          const float4 v = *reinterpret_cast<const float4*>(p + c0 + k);
+          x[k] = v.x;
+          x[k + 1] = v.y;
+          x[k + 2] = v.z;
+          x[k + 3] = v.w;
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < 16; ++k) x[k] = c0 + k < d ? p[c0 + k] : 0.f;
+      }
+      double r[16];
+#pragma unroll
+      for (int k = 0; k < 16; ++k) r[k] = nr < 1e-12 || c0 + k >= d ? 0.0 : div_rcp(static_cast<double>(x[k]), nr, y);
+      if (vec && c0 + 16 <= d) {
+#pragma unroll
+        for (int k = 0; k < 16; k += 2) *reinterpret_cast<double2*>(ur + c0 + k) = make_double2(r[k], r[k + 1]);
+      } else {
+#pragma unroll
+        for (int k = 0; k < 16; ++k)
+          if (c0 + k < d) ur[c0 + k] = r[k];
+      }
 #pragma unroll
       for (int k = 0; k < 16; ++k)
-        if (c0 + k < d) {
-          const double r = ddiv(static_cast<double>(x[k]), nr);
-          u[static_cast<int64_t>(i) * d + c0 + k] = r;
-          ut[static_cast<int64_t>(c0 + k) * n + i] = r;
-        }
+        if (c0 + k < d) ut[static_cast<int64_t>(c0 + k) * n + i] = r[k];
     }
   }
   __syncthreads();
+  SPROF(0)
   if (S.degen) {
     if (tid == 0) meta[3] = -2;  // zero vector (the host raises KVC_E_DEGENERATE)
     return;
@@ -225,6 +279,7 @@ __device__ __forceinline__ void split_two_body(const float* rows, const int32_t*
   }
   // k-means++ seeding with 1 - cosine weights, k = 2 (clustering.cpp:25-70)
   __syncthreads();
+  SPROF(1)
   for (int c = tid; c < d; c += SPT) S.cent[0][c] = u[static_cast<int64_t>(first) * d + c];
   __syncthreads();
   for (int i = tid; i < n; i += SPT) nearv[i] = dot_col(ut, n, i, S.cent[0], d);
@@ -280,6 +335,7 @@ __device__ __forceinline__ void split_two_body(const float* rows, const int32_t*
   __syncthreads();
   cosines(ut, n, d, S, sc);
   __syncthreads();
+  SPROF(2)
   for (int it = 0; it < 50; ++it) {
     if (tid == 0) {
       S.moved = 0;
@@ -328,7 +384,9 @@ __device__ __forceinline__ void split_two_body(const float* rows, const int32_t*
     }
     // member lists in point order (warp j scans cluster j with ballots), in the k-means++ scratch
     // (nearv is dead after seeding): memb[0, cnt0) = cluster 0, memb[cnt0, n) = cluster 1
-    int* memb = reinterpret_cast<int*>(nearv);
+    // (in shared memory -- the objective's staging area, free until the objective -- when they fit:
+    // the centroid sums below read them ahead of their dependent row loads)
+    int* memb = n <= 2 * OBJ_CHUNK ? reinterpret_cast<int*>(S_ob) : reinterpret_cast<int*>(nearv);
     if (warp < 2) {
       int w = warp == 0 ? 0 : S.cnt[0];
       for (int base = 0; base < n; base += 32) {
@@ -340,6 +398,7 @@ __device__ __forceinline__ void split_two_body(const float* rows, const int32_t*
       }
     }
     __syncthreads();
+    SPROF(3)
     // arithmetic means, sums in member (= point) order (clustering.cpp:138-150); one (cluster,
     // dim) chain per thread over that cluster's members only, rows read coalesced across the
     // dimension, the next 16 members' loads in flight while a group is summed
@@ -372,10 +431,13 @@ __device__ __forceinline__ void split_two_body(const float* rows, const int32_t*
     __syncthreads();
     if (wj >= 0) S.cent[wj][wc] = newc;
     __syncthreads();
+    SPROF(4)
     centroid_norms(S, d);
     __syncthreads();
+    SPROF(5)
     cosines(ut, n, d, S, sc);
     __syncthreads();
+    SPROF(6)
     // mean cosine to the own centroid, summed in point order (clustering.cpp:152-163)
     // staged through shared memory in chunks so the one summing thread reads at smem latency
     double obj = 0.0;
@@ -394,6 +456,8 @@ __device__ __forceinline__ void split_two_body(const float* rows, const int32_t*
       S.prev = obj;
     }
     __syncthreads();
+    SPROF(7)
+    if (prof && tid == 0) S.pc[10] = it + 1;
     if (S.stop) break;
   }
   // compact ids (clustering.cpp:166-177)
@@ -418,12 +482,17 @@ __device__ __forceinline__ void split_two_body(const float* rows, const int32_t*
     meta[2] = 0;
     meta[3] = 0;
   }
+  SPROF(8)
+  if (prof && tid == 0)
+    for (int k = 0; k < 12; ++k) g_split_prof[blockIdx.x * 16 + k] = S.pc[k];
+#undef SPROF
 }
 
 __global__ void __launch_bounds__(SPT) k_split_two(const float* rows, const int32_t* idx, int n, int d, int first,
                                                     double uni, double* scratch, int32_t* assign, int32_t* meta,
                                                     double* objective) {
-  split_two_body(rows, idx, n, d, first, uni, scratch, assign, meta, objective);
+  __shared__ double S_ob[OBJ_CHUNK];
+  split_two_body(rows, idx, n, d, first, uni, scratch, assign, meta, objective, S_ob);
 }
 
 // Eq. 1 / Eq. 2 statistics of the two groups of a split (compute_representative /
@@ -432,7 +501,7 @@ __global__ void __launch_bounds__(SPT) k_split_two(const float* rows, const int3
 // (rep64, rep32, rnorm, var), and the variances to var_out (the host's Eq. 5 recursion test).
 // memb: n ints of scratch.
 __device__ void child_stats(const DevTables& t, const float* rows, const int32_t* idx, int n, const int32_t* assign,
-                            const int32_t slot[2], double* var_out, int* memb, double* sq) {
+                            const int32_t slot[2], double* var_out, int* memb, double* sq, double* sbuf) {
   __shared__ double srep[2][256];
   __shared__ int scnt[2];
   __shared__ double sinv[2];
@@ -459,6 +528,11 @@ __device__ void child_stats(const DevTables& t, const float* rows, const int32_t
   __syncthreads();
   const int c0 = scnt[0], c1 = scnt[1];
   if (tid < 2) sinv[tid] = (tid == 0 ? c0 : c1) > 0 ? ddiv(1.0, static_cast<double>(tid == 0 ? c0 : c1)) : 0.0;
+  // the members' staged row indices (one dependent load less in the chains below), in shared
+  // memory when they fit beside the squared distances (n ints + n doubles in the staging area)
+  const bool in_smem = static_cast<int64_t>(n) * 12 <= static_cast<int64_t>(OBJ_CHUNK) * 8;
+  int* mrow = in_smem ? reinterpret_cast<int*>(sbuf + n) : memb;
+  for (int m = tid; m < n; m += blockDim.x) mrow[m] = idx[memb[m]];
   __syncthreads();
   // representatives: one (group, dim) chain per thread over the group's rows, 16 loads ahead
   if (tid < 2 * d) {
@@ -469,7 +543,7 @@ __device__ void child_stats(const DevTables& t, const float* rows, const int32_t
     float x[16];
     auto load16 = [&](int m) {
 #pragma unroll
-      for (int k = 0; k < 16; ++k) x[k] = rows[static_cast<int64_t>(idx[memb[m + k]]) * d + c];
+      for (int k = 0; k < 16; ++k) x[k] = rows[static_cast<int64_t>(mrow[m + k]) * d + c];
     };
     if (m16 > mb) load16(mb);
     for (int m = mb; m < m16; m += 16) {
@@ -480,7 +554,7 @@ __device__ void child_stats(const DevTables& t, const float* rows, const int32_t
 #pragma unroll
       for (int k = 0; k < 16; ++k) acc = dadd(acc, static_cast<double>(y[k]));
     }
-    for (int m = m16; m < me; ++m) acc = dadd(acc, static_cast<double>(rows[static_cast<int64_t>(idx[memb[m]]) * d + c]));
+    for (int m = m16; m < me; ++m) acc = dadd(acc, static_cast<double>(rows[static_cast<int64_t>(mrow[m]) * d + c]));
     const double r = dmul(acc, sinv[g]);
     srep[g][c] = r;
     if (me > mb && slot[g] >= 0) {
@@ -489,35 +563,60 @@ __device__ void child_stats(const DevTables& t, const float* rows, const int32_t
     }
   }
   __syncthreads();
-  // squared distances per row (sequential over the dimension), in member order
+  // squared distances per row (sequential over the dimension), in member order; rows read 16
+  // bytes per load (one row per thread)
+  double* sqs = in_smem ? sbuf : sq;
+  const bool vec = (d & 3) == 0;
   for (int m = tid; m < c0 + c1; m += blockDim.x) {
     const int g = m < c0 ? 0 : 1;
-    const float* p = rows + static_cast<int64_t>(idx[memb[m]]) * d;
+    const float* p = rows + static_cast<int64_t>(mrow[m]) * d;
     double a = 0.0;
-    for (int c = 0; c < d; ++c) {
-      const double df = dsub(static_cast<double>(p[c]), srep[g][c]);
-      a = dadd(a, dmul(df, df));
+    if (vec) {
+      for (int c = 0; c < d; c += 16) {
+        float4 v[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) v[k] = *reinterpret_cast<const float4*>(p + c + 4 * k);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float e[4] = {v[k].x, v[k].y, v[k].z, v[k].w};
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            if (c + 4 * k + q >= d) break;
+            const double df = dsub(static_cast<double>(e[q]), srep[g][c + 4 * k + q]);
+            a = dadd(a, dmul(df, df));
+          }
+        }
+      }
+    } else {
+      for (int c = 0; c < d; ++c) {
+        const double df = dsub(static_cast<double>(p[c]), srep[g][c]);
+        a = dadd(a, dmul(df, df));
+      }
     }
-    sq[m] = a;
+    sqs[m] = a;
   }
   __syncthreads();
-  // sequential sums over the rows (one thread per group), the norm of the representative
+  // sequential sums over the rows (one thread per group, staged reads 8 ahead), and the norms of
+  // the representatives on two other threads
   if (tid == 0 || tid == 32) {
     const int g = tid == 0 ? 0 : 1;
     const int mb = g == 0 ? 0 : c0, me = g == 0 ? c0 : c0 + c1;
     if (me > mb) {
-      double total = 0.0;
-      for (int m = mb; m < me; ++m) total = dadd(total, sq[m]);
+      const double total = seq_sum8(0.0, sqs + mb, me - mb);
       const double var = ddiv(total, static_cast<double>(me - mb));
-      double nn = 0.0;
-      for (int c = 0; c < d; ++c) nn = dadd(nn, dmul(srep[g][c], srep[g][c]));
-      if (slot[g] >= 0) {
-        t.var[slot[g]] = var;
-        t.rnorm[slot[g]] = __dsqrt_rn(nn);
-      }
+      if (slot[g] >= 0) t.var[slot[g]] = var;
       if (var_out) var_out[g] = var;
     } else if (var_out) {
       var_out[g] = 0.0;
+    }
+  }
+  if (tid == 64 || tid == 96) {
+    const int g = tid == 64 ? 0 : 1;
+    const int mb = g == 0 ? 0 : c0, me = g == 0 ? c0 : c0 + c1;
+    if (me > mb && slot[g] >= 0) {
+      double nn = 0.0;
+      for (int c = 0; c < d; ++c) nn = dadd(nn, dmul(srep[g][c], srep[g][c]));
+      t.rnorm[slot[g]] = __dsqrt_rn(nn);
     }
   }
 }
@@ -526,6 +625,7 @@ __device__ void child_stats(const DevTables& t, const float* rows, const int32_t
 // events of many domains at once (context_waves.cpp). A job with slots also installs its two
 // groups' statistics; a job with assign_in skips the k-means (a result already known).
 __global__ void __launch_bounds__(SPT) k_split_two_batch(DevTables t, const SplitJob* jobs, int d) {
+  __shared__ double S_ob[OBJ_CHUNK];  // staging shared by the k-means and the children statistics
   const SplitJob j = jobs[blockIdx.x];
   if (j.assign_in) {
     for (int i = threadIdx.x; i < j.n; i += SPT) j.assign[i] = j.assign_in[i];
@@ -537,17 +637,21 @@ __global__ void __launch_bounds__(SPT) k_split_two_batch(DevTables t, const Spli
     }
     __syncthreads();
   } else {
-    split_two_body(j.rows, j.idx, j.n, d, j.first, j.uni, j.scratch, j.assign, j.meta, j.objective);
+    split_two_body(j.rows, j.idx, j.n, d, j.first, j.uni, j.scratch, j.assign, j.meta, j.objective, S_ob);
     __syncthreads();
     if (j.meta[3] != 0) return;  // degenerate row: the host raises it
   }
   if (j.slot[0] < 0 && j.slot[1] < 0 && !j.var_out) return;
   int* memb = reinterpret_cast<int*>(j.scratch);
   double* sq = j.scratch + (static_cast<int64_t>(j.n) + 1) / 2 + 1;
-  child_stats(t, j.rows, j.idx, j.n, j.assign, j.slot, j.var_out, memb, sq);
+  const long long c0 = clock64();
+  child_stats(t, j.rows, j.idx, j.n, j.assign, j.slot, j.var_out, memb, sq, S_ob);
+  if (g_split_prof && threadIdx.x == 0) g_split_prof[blockIdx.x * 16 + 9] = clock64() - c0;
 }
 
 }  // namespace
+
+void split_prof_set(long long* p) { cudaMemcpyToSymbol(g_split_prof, &p, sizeof(p)); }
 
 int launch_split_two_batch(const DevTables& t, const SplitJob* jobs, int n_jobs, int d, cudaStream_t st) {
   if (n_jobs <= 0 || d > 256) return 0;
