@@ -1230,6 +1230,11 @@ void Context::launch_round(const std::vector<int>& active, const std::vector<int
     return e && e[0] == '1';
   }();
   ia_.exact_all = round_after_event_ || exact_all_env ? 1 : 0;
+  static const bool resolve_prof = [] {  // KVC_RESOLVE_PROF=1: the sequential resolve's phase clocks
+    const char* e = std::getenv("KVC_RESOLVE_PROF");
+    return e && e[0] == '1';
+  }();
+  ia_.prof_on = resolve_prof ? 1 : 0;
   if (timing_) KVC_CUDA(cudaEventRecord(ev_[0], st_));
   launches_ += launch_build_cands(t_, ia_, st_);
   if (timing_) KVC_CUDA(cudaEventRecord(ev_[1], st_));

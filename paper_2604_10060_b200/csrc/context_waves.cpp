@@ -53,7 +53,13 @@ struct DBuf {  // growable device buffer
   // keep: the first `keep` bytes survive a growth (copied on the stream, which is synchronised)
   void ensure(std::size_t bytes, cudaStream_t st, std::size_t keep = 0) {
     if (bytes <= cap) return;
-    std::size_t n = std::max<std::size_t>(bytes, cap * 2);
+    static const bool log = [] {
+      const char* e = std::getenv("KVC_WAVES_LOG");
+      return e && e[0] == '1';
+    }();
+    if (log) std::fprintf(stderr, "[waves] device buffer growth %zu -> %zu bytes\n", cap, bytes);
+    // 2x headroom: a growth (allocation + synchronisation) stays a rare event across frames
+    std::size_t n = std::max<std::size_t>(bytes * 2, cap * 2);
     n = std::max<std::size_t>(n, 1 << 16);
     void* q = nullptr;
     KVC_CUDA(cudaMalloc(&q, n));
@@ -81,7 +87,7 @@ struct HBuf {  // growable pinned host buffer (contents not kept)
   std::size_t cap = 0;
   void ensure(std::size_t bytes, cudaStream_t st) {
     if (bytes <= cap) return;
-    const std::size_t n = std::max<std::size_t>({bytes, cap * 2, std::size_t{1} << 16});
+    const std::size_t n = std::max<std::size_t>({bytes * 2, cap * 2, std::size_t{1} << 16});
     if (p) {
       KVC_CUDA(cudaStreamSynchronize(st));
       KVC_CUDA(cudaFreeHost(p));
@@ -305,7 +311,16 @@ void Context::run_inserts_waves(std::int64_t frame_id, std::int64_t pid, int T, 
   using clk = std::chrono::steady_clock;
   auto us = [](clk::time_point a, clk::time_point b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
   const auto t_start = clk::now();
-  if (!wv_) wv_ = new Waves();
+  if (!wv_) {
+    wv_ = new Waves();
+    // staging for a typical frame's pools up front (about one 1,000-member pool per domain)
+    const std::size_t rows0 = static_cast<std::size_t>(L_) * 3072;
+    const std::size_t rb0 = static_cast<std::size_t>(d_) * es_;
+    wv_->stage_k.ensure(rows0 * rb0 / 2, st_);  // (ensure doubles: rows0 rows)
+    wv_->stage_v.ensure(rows0 * rb0 / 2, st_);
+    wv_->stage_f32.ensure(rows0 * d_ * 2, st_);
+    wv_->km_scratch.ensure(rows0 * (2 * d_ + 3) * 4, st_);
+  }
   Waves& W = *wv_;
   if (spec_.active) {
     KVC_CUDA(cudaEventSynchronize(spec_.ev));

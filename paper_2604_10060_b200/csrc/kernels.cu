@@ -495,13 +495,34 @@ __global__ void __launch_bounds__(32) k_resolve(DevTables t, IngestArgs a) {
     a.stop_slot[dom] = -1;
   }
   if (lane < POOL) S.pool[lane] = a.dom_pool[dom * POOL + lane];
-  for (int tt = cur + lane; tt < T; tt += 32) {  // |k_t| (vecmath.hpp:35-40)
+  for (int tt = cur + lane; tt < T; tt += 32) {  // |k_t| (vecmath.hpp:35-40), 16-byte key loads
     double s = 0.0;
     const int64_t base = (static_cast<int64_t>(dom) * t.tmax + tt) * d;
+    if (t.kv_bf16 && (d & 7) == 0) {
+      const uint4* row = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(a.fk) + base);
+      for (int i = 0; i < d / 8; i += 4) {
+        uint4 w[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) w[k] = i + k < d / 8 ? row[i + k] : make_uint4(0, 0, 0, 0);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          if (i + k >= d / 8) break;
+          const uint32_t u4[4] = {w[k].x, w[k].y, w[k].z, w[k].w};
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const double lo = static_cast<double>(__uint_as_float(u4[q] << 16));
+            const double hi = static_cast<double>(__uint_as_float(u4[q] & 0xffff0000u));
+            s = dadd(s, dmul(lo, lo));
+            s = dadd(s, dmul(hi, hi));
+          }
+        }
+      }
+    } else {
 #pragma unroll 8
-    for (int i = 0; i < d; ++i) {
-      const double x = static_cast<double>(ld_kv(a.fk, base + i, t.kv_bf16));
-      s = dadd(s, dmul(x, x));
+      for (int i = 0; i < d; ++i) {
+        const double x = static_cast<double>(ld_kv(a.fk, base + i, t.kv_bf16));
+        s = dadd(s, dmul(x, x));
+      }
     }
     nk[tt] = __dsqrt_rn(s);
     a.ev_page[static_cast<int64_t>(dom) * t.tmax + tt] = -1;
@@ -713,10 +734,11 @@ __global__ void __launch_bounds__(32) k_resolve(DevTables t, IngestArgs a) {
           for (int i = 0; i < d; ++i) acc = dadd(acc, dmul(A[i], B[i]));
         }
         if (mine >= 0) S.e_dot[mine] = acc;
-        if (sp_pass) {
-          bn = __dsqrt_rn(__shfl_sync(kFull, acc, dot_lanes0));
-          rn = __dsqrt_rn(__shfl_sync(kFull, acc, dot_lanes0 + 1));
-          sq = __shfl_sync(kFull, acc, dot_lanes0 + 2);
+        if (sp_pass) {  // the two norms' square roots on their own lanes, in parallel
+          const double rt = lane == dot_lanes0 || lane == dot_lanes0 + 1 ? __dsqrt_rn(acc) : acc;
+          bn = __shfl_sync(kFull, rt, dot_lanes0);
+          rn = __shfl_sync(kFull, rt, dot_lanes0 + 1);
+          sq = __shfl_sync(kFull, rt, dot_lanes0 + 2);
         }
         pos = p;
         if (pos >= ne) break;
@@ -730,8 +752,9 @@ __global__ void __launch_bounds__(32) k_resolve(DevTables t, IngestArgs a) {
     chain_phase(OFF_KD + (cur % 3) * DS, kd + (cur % 3) * DS, false, sq, rn, bn);
     constexpr int KPL = 8;  // key elements per lane held in flight (d <= 256)
     long long pr[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};  // phase cycles | slow, scans, tokens, entries
-    long long c0 = clock64(), c1;
-#define PROF(k) c1 = clock64(); pr[k] += c1 - c0; c0 = c1;
+    const bool prof_on = a.prof_on != 0;
+    long long c0 = prof_on ? clock64() : 0, c1;
+#define PROF(k) if (prof_on) { c1 = clock64(); pr[k] += c1 - c0; c0 = c1; }
     for (int tt = cur; tt < T; ++tt) {
       // prefetch the key of tt + 2 as raw 32-bit words (converted only at the end of the iteration,
       // so no instruction here waits for the load)
@@ -849,14 +872,16 @@ __global__ void __launch_bounds__(32) k_resolve(DevTables t, IngestArgs a) {
         __syncwarp();
       }
       PROF(3)
-      if (lane == 0) {
-        int ns = 0;
-        for (int e = 0; e < min(S.ne, RELMAX); ++e) ns += S.e_var[e] == EV_SLOW;
-        pr[8] += ns;
-        pr[10] += 1;
-        pr[11] += min(S.ne, RELMAX);
+      if (prof_on) {
+        if (lane == 0) {
+          int ns = 0;
+          for (int e = 0; e < min(S.ne, RELMAX); ++e) ns += S.e_var[e] == EV_SLOW;
+          pr[8] += ns;
+          pr[10] += 1;
+          pr[11] += min(S.ne, RELMAX);
+        }
+        c0 = clock64();
       }
-      c0 = clock64();
       chain_phase(OFF_KD + kn * DS, kd + kn * DS, true, sq, rn, bn);
       PROF(4)
       const double varn = ddiv(dadd(dmul(dn, S.hvar[h]), sq), dadd(dn, 1.0));
@@ -966,7 +991,7 @@ __global__ void __launch_bounds__(32) k_resolve(DevTables t, IngestArgs a) {
       PROF(7)
     }
 #undef PROF
-    if (lane == 0)
+    if (lane == 0 && prof_on)
       for (int k = 0; k < 12; ++k) a.prof[dom * 16 + k] = pr[k];
   }
 done:

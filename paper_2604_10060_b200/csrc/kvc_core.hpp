@@ -159,6 +159,7 @@ struct IngestArgs {
   // per-domain reserve of free pages carried between resolve launches (no pushes to the
   // shared free stack while pops may run concurrently)
   long long* prof;         // [L][16] clock64 cycles per resolve phase (instrumentation)
+  int32_t prof_on;         // the sequential resolve records its per-token phase clocks (timing mode)
   int32_t* dom_pool;       // [L][POOL]
   int32_t* dom_pool_n;     // [L]
   // speculative resolve (resolve_spec.cu): per-token state snapshots, column-major so that

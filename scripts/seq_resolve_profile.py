@@ -1,7 +1,7 @@
 """Per-token phase cycles of the sequential resolve kernel (k_resolve, kernels.cu) on full frames
 of the config-2 shape: KVC_RESOLVE=seq forces it for every round. Development measurement.
 
-    KVC_RESOLVE=seq python scripts/seq_resolve_profile.py [domains] [frames] [drift]
+    KVC_RESOLVE=seq [KVC_RESOLVE_PROF=1] python scripts/seq_resolve_profile.py [domains] [frames] [drift]
 """
 import json
 import os
@@ -38,7 +38,8 @@ for i in range(F):
     tm = kv.ingest_timing()
     p = kv.resolve_profile()
     tok = max(p[10], 1)
-    out.append({"resolve_us": round(float(tm[3]), 1), "tokens_per_domain": round(float(p[10]), 1),
+    out.append({"kernels_us": dict(zip(["cands", "assign", "topm", "resolve", "store_rows"], np.round(tm[:5], 1).tolist())),
+                "resolve_us": round(float(tm[3]), 1), "tokens_per_domain": round(float(p[10]), 1),
                 "cycles_per_token": {n: round(float(p[k]) / tok, 1) for k, n in enumerate(names)},
                 "slow_per_token": round(float(p[8]) / tok, 2), "entries_per_token": round(float(p[11]) / tok, 2)})
 kv.set_timing(False)
