@@ -1113,8 +1113,17 @@ void Context::run_inserts_waves(std::int64_t frame_id, std::int64_t pid, int T, 
       if (waves_log_) {
         int cmin = T;
         for (int c : rcur) cmin = std::min(cmin, c);
-        std::fprintf(stderr, "[waves] relaunch %zu domains (first token %d, seq %d): %.0f us incl. install\n", relaunch.size(),
-                     cmin, relaunch_seq_ ? 1 : 0, us(i0, clk::now()));
+        std::string kt;
+        if (round_timed_) {  // (timing mode) the round's kernels: cands, tile, top-M, resolve, store
+          for (int i = 0; i < 5; ++i) {
+            float ms = 0.f;
+            KVC_CUDA(cudaEventElapsedTime(&ms, ev_[i], ev_[i + 1]));
+            kt += " " + std::to_string(static_cast<int>(ms * 1e3));
+          }
+          kt = "; kernels us" + kt;
+        }
+        std::fprintf(stderr, "[waves] relaunch %zu domains (first token %d, seq %d): %.0f us incl. install (install %.0f)%s\n",
+                     relaunch.size(), cmin, relaunch_seq_ ? 1 : 0, us(i0, clk::now()), us(i0, r0), kt.c_str());
       }
       t_relaunch += us(r0, clk::now());
     } else {
