@@ -380,6 +380,9 @@ KVC_API int kvc_debug_assign_check(kvc_ctx* ctx, const void* keys, int32_t T, in
  * n random operands: integer divisors in [1, max_den], or (max_den <= 0) real divisors in
  * [2^-8, 2^8) with float numerators (the unit rows of the split k-means). */
 KVC_API int kvc_debug_div_check(uint64_t n, uint64_t seed, int32_t max_den, uint64_t* mismatches);
+/* Debug: per-domain averages of the last resolve round's phase clocks, out16 (the speculative
+ * kernel always records them; the sequential kernel only with KVC_RESOLVE_PROF=1); out[0] < 0 on
+ * entry selects the decode step's K4 clocks instead. */
 KVC_API int kvc_debug_resolve_profile(kvc_ctx* ctx, double* out);
 /* Host-event slow path profile (cumulative since creation / the last reset), out10: microseconds in
  * host events (split / seed) total, of which staging + download of the cluster rows, split k-means
