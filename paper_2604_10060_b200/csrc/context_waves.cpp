@@ -1105,9 +1105,8 @@ void Context::run_inserts_waves(std::int64_t frame_id, std::int64_t pid, int T, 
       round_after_event_ = false;
       sync();
       check_err_word(*h_err_);
-      const bool tie_known = resolve_seq_ || relaunch_seq_;  // only k_resolve reports ties
-      for (int l : relaunch) {
-        W.dom[static_cast<std::size_t>(l)].tie |= !tie_known || h_err_[1 + l] != 0;
+      for (int l : relaunch) {  // (both resolve kernels report key-decided exact ties)
+        W.dom[static_cast<std::size_t>(l)].tie |= h_err_[1 + l] != 0;
         take_stop(l);
       }
       if (waves_log_) {

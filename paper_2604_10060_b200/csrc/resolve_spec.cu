@@ -202,12 +202,110 @@ __device__ int warp0_exscan(const int32_t* in_a, const int32_t* in_b, int32_t* o
   return run;
 }
 
+// fp32 routing simulation for relaunch rounds (see the kernel): up to SIM_SLOTS touched candidates
+// cached in the per-token scratch arrays a_var .. db (free until the first round's phase B).
+constexpr int SIM_SLOTS = 12;
+__device__ void simulate_routing(const DevTables& t, SpecSmem& S, const IngestArgs& a, int dom, int Tl, int nl,
+                                 bool bf16, int lane) {
+  const int d = t.d, q = d / 32;  // dimensions per lane (d % 32 == 0 here; else only partially)
+  if (d % 32 != 0) return;
+  const size_t room = 5 * static_cast<size_t>(t.tmax) * 8;
+  const size_t per = static_cast<size_t>(d) * 4 + 16;
+  const int slots = min(SIM_SLOTS, static_cast<int>(room / per));
+  if (slots < 2) return;
+  float* rep = reinterpret_cast<float*>(S.a_var);              // [slots][d]
+  float* rn = rep + static_cast<size_t>(slots) * d;           // [slots] |rep|
+  float* cnt = rn + slots;                                     // [slots] n
+  for (int c = lane; c < nl; c += 32) S.cts[c] = -1;           // candidate -> slot
+  __syncwarp();
+  int used = 0;
+  for (int u = 0; u < Tl; ++u) {
+    float x[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int i = lane + 32 * j;
+      x[j] = j < q ? static_cast<float>(keyd(S, u, i, bf16)) : 0.f;
+    }
+    const float nk = static_cast<float>(S.nk[u]);
+    float bs = -INFINITY;
+    long long bk = LLONG_MAX;
+    int bc = -1;
+    for (int k = 0; k < TOPM; ++k) {
+      const int c = S.tm_idx[u * TOPM + k];
+      if (c < 0) break;
+      const int sl = S.cts[c];
+      float v;
+      if (sl >= 0) {
+        float p = 0.f;
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if (j < q) p = fmaf(x[j], rep[sl * d + lane + 32 * j], p);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) p += __shfl_xor_sync(0xffffffffu, p, o);
+        v = p / (nk * rn[sl]);
+      } else {
+        const double e = S.tm_ex[u * TOPM + k];
+        v = isnan(e) ? -INFINITY : static_cast<float>(e);
+      }
+      const long long key = S.ckey[c];
+      if (v > bs || (v == bs && key < bk)) {
+        bs = v;
+        bk = key;
+        bc = c;
+      }
+    }
+    if (bc < 0) return;  // no proposal past here: the launch-time speculation stays
+    if (lane == 0) S.win[u] = static_cast<int16_t>(bc);
+    int sl = S.cts[bc];
+    if (sl < 0 && used < slots) {  // the winner's launch-time state into a slot
+      sl = used++;
+      const int64_t sg = S.cslot[bc];
+      const float* src = (S.cbuf[bc] ? t.brep32 : t.rep32) + sg * d;
+      float ss = 0.f;
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (j < q) {
+          const float r = src[lane + 32 * j];
+          rep[sl * d + lane + 32 * j] = r;
+          ss = fmaf(r, r, ss);
+        }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+      if (lane == 0) {
+        rn[sl] = sqrtf(ss);
+        cnt[sl] = static_cast<float>(S.cbuf[bc] ? t.nbuf[sg] : t.stat[sg]);
+        S.cts[bc] = static_cast<int16_t>(sl);
+      }
+    }
+    __syncwarp();
+    if (sl >= 0) {  // Eq. 3 in fp32: r' = (n r + k) / (n + 1)
+      const float n = cnt[sl], inv = 1.f / (n + 1.f);
+      float ss = 0.f;
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (j < q) {
+          const int i = lane + 32 * j;
+          const float r = (n * rep[sl * d + i] + x[j]) * inv;
+          rep[sl * d + i] = r;
+          ss = fmaf(r, r, ss);
+        }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+      if (lane == 0) {
+        rn[sl] = sqrtf(ss);
+        cnt[sl] = n + 1.f;
+      }
+    }
+    __syncwarp();
+  }
+}
+
 __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve_spec(DevTables t, IngestArgs a) {
   asm volatile("griddepcontrol.wait;" ::: "memory");  // (launched as a dependent of K1)
   extern __shared__ __align__(16) uint8_t smraw[];
   SpecSmem S;
   spec_carve(smraw, &S, t.d, t.es, a.T, t.tmax, t.cmax);
-  __shared__ int sh_nts, sh_te, sh_tfail, sh_nreq, sh_bad, sh_ntot, sh_nfresh, sh_ptotal, sh_nexact;
+  __shared__ int sh_nts, sh_te, sh_tfail, sh_nreq, sh_bad, sh_ntot, sh_nfresh, sh_ptotal, sh_nexact, sh_tie;
   __shared__ long long sh_prof[16];
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -234,12 +332,14 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve_spec(DevTables t, Ing
   // outcome arrays still hold that frame's first round, which its relaunches copy back whole)
   if (a.prev_events && *a.prev_events) return;
   if (tid < 16) sh_prof[tid] = 0;
+  if (tid == 0 && a.tie) a.tie[dom] = 0;  // (early returns below decide nothing)
   if (tid == 0) {
     a.stop_t[dom] = T;
     a.stop_kind[dom] = EV_NONE;
     a.stop_slot[dom] = -1;
     sh_bad = INT_MAX;
     sh_nexact = 0;
+    sh_tie = 0;
   }
   for (int u = tid; u < Tl; u += RS_THREADS) a.ev_page[orow0 + u] = -1;
   if (Tl <= 0) return;
@@ -346,6 +446,15 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve_spec(DevTables t, Ing
     sh_ntot = nl;
     sh_nfresh = 0;
   }
+  // Relaunch rounds (after a split: the fresh children absorb most of the remaining tokens and
+  // move by ~1/n per absorb, so the launch-time speculation above fails at almost every token):
+  // warp 0 simulates the routing sequentially in fp32 -- touched candidates' states updated by
+  // Eq. 3 in fp32, their cosines re-evaluated per token, untouched ones from K1b's exact
+  // launch-time values -- and speculates its winners instead. The simulation only proposes;
+  // every decision is still verified exactly below, so a wrong proposal costs a round, never
+  // exactness.
+  if (a.exact_all && warp == 0 && d <= 256) simulate_routing(t, S, a, dom, Tl, nl, bf16, lane);
+  __syncthreads();
   prof(0);
 
   int t0 = 0;
@@ -889,6 +998,7 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve_spec(DevTables t, Ing
           bp = w;
         }
         bool amb = false;
+        bool ltie = false;  // this lane's best value was reached by two of its candidates
         // c != w, alive at u; touched: its state changed before u
         auto consider = [&](int c, bool touched) {
           double v = 0.0;
@@ -910,6 +1020,8 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve_spec(DevTables t, Ing
             v = exact_at(c, u, touched ? last_change(c, u) : -1);
             ++n_ex;
           }
+          if (v == bs) ltie = true;
+          else if (v > bs) ltie = false;
           if (better(v, S.ckey[c], bs, bk)) {
             bs = v;
             bk = S.ckey[c];
@@ -937,13 +1049,20 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve_spec(DevTables t, Ing
         if (any && !wknown && w_alive && lane == 0) {
           const double v = exact_at(w, u, w_touched ? last_change(w, u) : -1);
           ++n_ex;
+          if (v == bs) ltie = true;
+          else if (v > bs) ltie = false;
           if (better(v, S.ckey[w], bs, bk)) {
             bs = v;
             bk = S.ckey[w];
             bp = w;
           }
         }
+        const double lbs = bs;
         warp_best(bs, bk, bp);
+        if (any) {  // an exact tie of the best fp64 cosines decided by the key (IngestArgs::tie)
+          const bool has = lbs == bs;
+          if ((__popc(__ballot_sync(kFull, has)) >= 2 || __any_sync(kFull, has && ltie)) && lane == 0) sh_tie = 1;
+        }
         const int vw = any ? bp : w;
         if (lane == 0) {
           S.vwin[u] = static_cast<int16_t>(vw);
@@ -1127,6 +1246,7 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve_spec(DevTables t, Ing
   prof(9);
   if (tid == 0) {
     a.n_exact[dom] = sh_nexact;
+    if (a.tie) a.tie[dom] = sh_tie;
     for (int k = 0; k < 10; ++k) a.prof[dom * 16 + k] = sh_prof[k];
     a.prof[dom * 16 + 10] = iters;
   }
