@@ -291,8 +291,8 @@ void Context::alloc_device() {
   {
     const char* e = std::getenv("KVC_RESOLVE");  // "seq": the sequential resolve kernel
     resolve_seq_ = e && std::string(e) == "seq";
-    const char* rl = std::getenv("KVC_RELAUNCH");  // "spec": speculative kernel for relaunches too
-    relaunch_seq_ = !(rl && std::string(rl) == "spec");
+    const char* rl = std::getenv("KVC_RELAUNCH");  // "seq": the sequential kernel for relaunches
+    relaunch_seq_ = rl && std::string(rl) == "seq";
     const char* wv = std::getenv("KVC_WAVES");  // 0: settle host events one domain at a time
     waves_ = !(wv && std::string(wv) == "0");
     const char* wp = std::getenv("KVC_WAVES_PERTURB");

@@ -344,11 +344,10 @@ class Context {
   cudaEvent_t ev_[8] = {};
   bool timing_ = false;
   bool resolve_seq_ = false;  // KVC_RESOLVE=seq selects the sequential resolve kernel
-  // A domain relaunched after a split (one domain, its state just changed under the remaining
-  // tokens) runs the sequential kernel: the speculation restarts at most tokens there (the two
-  // children compete for them), measured 2.4 ms vs 0.85 ms per relaunch on the drift stream.
-  // KVC_RELAUNCH=spec keeps the speculative kernel.
-  bool relaunch_seq_ = true;
+  // A domain relaunched after a split runs the speculative kernel seeded by the fp32 routing
+  // simulation, its fresh children settled by warp-parallel cosine bounds (resolve_spec.cu):
+  // ≈ 0.35 ms vs ≈ 1 ms per relaunch round for the sequential kernel (KVC_RELAUNCH=seq).
+  bool relaunch_seq_ = false;
   bool round_after_event_ = false;
   bool assign_tc_ = false;    // tensor-core distance tile (KVC_ASSIGN=simt disables)
   alignas(64) unsigned char key_map_[128];  // CUtensorMap over the current frame's keys

@@ -88,6 +88,11 @@ struct HBuf {  // growable pinned host buffer (contents not kept)
   void ensure(std::size_t bytes, cudaStream_t st) {
     if (bytes <= cap) return;
     const std::size_t n = std::max<std::size_t>({bytes * 2, cap * 2, std::size_t{1} << 16});
+    static const bool log = [] {
+      const char* e = std::getenv("KVC_WAVES_LOG");
+      return e && e[0] == '1';
+    }();
+    if (log) std::fprintf(stderr, "[waves] pinned buffer growth %zu -> %zu bytes\n", cap, bytes);
     if (p) {
       KVC_CUDA(cudaStreamSynchronize(st));
       KVC_CUDA(cudaFreeHost(p));
@@ -320,6 +325,12 @@ void Context::run_inserts_waves(std::int64_t frame_id, std::int64_t pid, int T, 
     wv_->stage_v.ensure(rows0 * rb0 / 2, st_);
     wv_->stage_f32.ensure(rows0 * d_ * 2, st_);
     wv_->km_scratch.ensure(rows0 * (2 * d_ + 3) * 4, st_);
+    // snapshots of every domain's (partition, layer) clusters, the packed uploads and results
+    wv_->snap.ensure(static_cast<std::size_t>(L_) * 192 * slot_snap_bytes(d_), st_);
+    wv_->up.h.ensure(std::size_t{2} << 20, st_);
+    wv_->up.d.ensure(std::size_t{2} << 20, st_);
+    wv_->km_out.ensure(std::size_t{2} << 20, st_);
+    wv_->h_out.ensure(std::size_t{2} << 20, st_);
   }
   Waves& W = *wv_;
   if (spec_.active) {
@@ -1120,6 +1131,28 @@ void Context::run_inserts_waves(std::int64_t frame_id, std::int64_t pid, int T, 
             kt += " " + std::to_string(static_cast<int>(ms * 1e3));
           }
           kt = "; kernels us" + kt;
+        }
+        if (!relaunch_seq_) {  // the speculative kernel's rounds (prof[10]) over the relaunched domains
+          std::vector<long long> pr(static_cast<std::size_t>(L_) * 16);
+          KVC_CUDA(cudaMemcpy(pr.data(), ia_.prof, pr.size() * 8, cudaMemcpyDeviceToHost));
+          long long mx = 0, sm = 0;
+          for (int l : relaunch) {
+            mx = std::max(mx, pr[static_cast<std::size_t>(l) * 16 + 10]);
+            sm += pr[static_cast<std::size_t>(l) * 16 + 10];
+          }
+          kt += "; spec rounds max " + std::to_string(mx) + " mean " + std::to_string(sm / std::max<long long>(1, static_cast<long long>(relaunch.size())));
+          long long best = -1;
+          int bl = relaunch[0];
+          for (int l : relaunch) {
+            long long tot = 0;
+            for (int k = 0; k < 10; ++k) tot += pr[static_cast<std::size_t>(l) * 16 + k];
+            if (tot > best) {
+              best = tot;
+              bl = l;
+            }
+          }
+          kt += "; slowest domain phases";
+          for (int k = 0; k < 10; ++k) kt += " " + std::to_string(pr[static_cast<std::size_t>(bl) * 16 + k]);
         }
         std::fprintf(stderr, "[waves] relaunch %zu domains (first token %d, seq %d): %.0f us incl. install (install %.0f)%s\n",
                      relaunch.size(), cmin, relaunch_seq_ ? 1 : 0, us(i0, clk::now()), us(i0, r0), kt.c_str());

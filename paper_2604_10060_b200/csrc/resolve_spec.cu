@@ -42,6 +42,8 @@ constexpr int RS_THREADS = 512;
 constexpr int RS_WARPS = RS_THREADS / 32;
 constexpr int FRESH_MAX = 64;  // buffers registered (DEFER onto an empty buffer) per launch
 constexpr double kSlack = 1e-12;
+constexpr double kApproxEps = 1e-11;  // |warp-parallel fp64 cosine - sequential cosine| bound (d <= 256)
+constexpr double kMoveApprox = 1e-3;  // movement bound past which a touched candidate is settled by it
 
 
 struct SpecSmem {
@@ -944,7 +946,31 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve_spec(DevTables t, Ing
         }
         return clamp1(ddiv(acc, dmul(S.nk[u], nr)));  // cosine_sim (vecmath.hpp:53-63)
       };
+      // The same cosine from a warp-parallel fp64 sum (every lane calls it with the same c): the
+      // lanes' partial sums and the tree differ from the sequential order only by rounding, so
+      // |approx - exact| <= 2 gamma_d + O(u) < kApproxEps in cosine units -- tight enough that
+      // only near-ties still need the sequential value. NaN: degenerate (the exact path raises it).
+      auto approx_at = [&](int c, int u, int st) -> double {
+        const bool isb = S.cbuf[c];
+        double part = 0.0, nr;
+        if (st >= 0) {
+          const double* p = (isb ? bsnap : rsnap) + static_cast<int64_t>(st) * 4;
+          nr = isb ? S.a_bn[st] : S.a_rn[st];
+          for (int i = lane; i < d; i += 32) part += keyd(S, u, i, bf16) * p[static_cast<int64_t>(i >> 2) * tmax * 4 + (i & 3)];
+        } else {
+          const double* p = (isb ? t.brep64 : t.rep64) + static_cast<int64_t>(S.cslot[c]) * d;
+          nr = S.cnorm[c];
+          for (int i = lane; i < d; i += 32) part += keyd(S, u, i, bf16) * p[i];
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(kFull, part, o);
+        return nr < 1e-12 ? NAN : part / (S.nk[u] * nr);
+      };
       int n_ex = 0;
+      // relaunch rounds (fresh children) use the warp-parallel cosine for any sizeable movement;
+      // first rounds keep the movement bound (their clusters barely move, and the sequential
+      // values of the few ambiguous candidates run on parallel lanes)
+      const double move_approx = a.exact_all ? kMoveApprox : 3.0 * kMoveApprox;
       for (int u = t0 + warp; u <= uend; u += RS_WARPS) {
         const int64_t orow = orow0 + u;
         const int w = S.win[u];
@@ -985,6 +1011,11 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve_spec(DevTables t, Ing
           lowW = exw;
         } else if (wknown) {
           lowW = exw;
+        } else if (w_touched && delta_max(w) > move_approx) {
+          // its state moved far (a fresh child after a split): the warp-parallel value less its
+          // bound, instead of the movement bound
+          const double ap = approx_at(w, u, last_change(w, u));
+          lowW = isnan(ap) ? -INFINITY : ap - kApproxEps;
         } else {
           const double base = inw ? exw : static_cast<double>(arow[w]) - margin;
           lowW = base - (w_touched ? delta_max(w) : 0.0);
@@ -999,11 +1030,14 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve_spec(DevTables t, Ing
         }
         bool amb = false;
         bool ltie = false;  // this lane's best value was reached by two of its candidates
+        // far-moved touched candidates the movement bound could not exclude, settled below by the
+        // warp-parallel cosine (two per lane; a third goes to the sequential value at once)
+        int pend0 = -1, pend1 = -1;
         // c != w, alive at u; touched: its state changed before u
-        auto consider = [&](int c, bool touched) {
+        auto consider = [&](int c, bool touched, bool deferred) {
           double v = 0.0;
           bool have = false;
-          if (c < nl) {
+          if (c < nl && !deferred) {
             double ex;
             const bool in = in_topm(c, ex) && !isnan(ex);
             if (!touched && in) {  // untouched, exact launch-time value known
@@ -1011,8 +1045,19 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve_spec(DevTables t, Ing
               v = ex;
               have = true;
             } else {
+              const double dm = touched ? delta_max(c) : 0.0;
               const double base = in ? ex : static_cast<double>(arow[c]) + margin;
-              if (base + (touched ? delta_max(c) : 0.0) < lowW) return;
+              if (base + dm < lowW) return;
+              if (dm > move_approx) {
+                if (pend0 < 0) {
+                  pend0 = c;
+                  return;
+                }
+                if (pend1 < 0) {
+                  pend1 = c;
+                  return;
+                }
+              }
             }
           }
           amb = true;
@@ -1033,17 +1078,28 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve_spec(DevTables t, Ing
           // untouched candidates outside the top-M list are bounded by tnext + margin
           if (lane < TOPM) {
             const int c = my_ti;
-            if (c >= 0 && c != w && first_change(c) >= u) consider(c, false);
+            if (c >= 0 && c != w && first_change(c) >= u) consider(c, false, false);
           }
           for (int ts = lane; ts < nts; ts += 32) {
             const int lc = S.ts_lc[ts];
-            if (lc != w && S.ctok[S.ts_off[ts]] < u) consider(lc, true);
+            if (lc != w && S.ctok[S.ts_off[ts]] < u) consider(lc, true, false);
             const int cb = S.ts_cb[ts];
-            if (cb >= 0 && cb != w && alive(cb, u) && S.ts_fb[ts] < u) consider(cb, true);
+            if (cb >= 0 && cb != w && alive(cb, u) && S.ts_fb[ts] < u) consider(cb, true, false);
           }
         } else {
           for (int c = lane; c < ntot2; c += 32)
-            if (c != w && alive(c, u)) consider(c, first_change(c) < u);
+            if (c != w && alive(c, u)) consider(c, first_change(c) < u, false);
+        }
+        for (int r = 0; r < 2; ++r) {
+          const int mine = r == 0 ? pend0 : pend1;
+          unsigned m = __ballot_sync(kFull, mine >= 0);
+          while (m) {
+            const int src = __ffs(m) - 1;
+            m &= m - 1;
+            const int c = __shfl_sync(kFull, mine, src);
+            const double ap = approx_at(c, u, last_change(c, u));
+            if (lane == src && (isnan(ap) || ap + kApproxEps >= lowW)) consider(c, true, true);
+          }
         }
         const bool any = __any_sync(kFull, amb);
         if (any && !wknown && w_alive && lane == 0) {

@@ -48,9 +48,14 @@ def _drift_pair(monkeypatch, perturb: bool, D=8, N=24_000, C=48, frames=6, pre=0
     return kvs, outs
 
 
-@pytest.mark.parametrize("perturb,D,frames", [(False, 8, 6), (True, 8, 6), (False, 32, 14)],
-                         ids=["8dom", "8dom-perturbed", "32dom-14frames"])
-def test_waves_equal_sequential_drift(monkeypatch, perturb, D, frames):
+@pytest.mark.parametrize("perturb,D,frames,relaunch", [(False, 8, 6, "spec"), (True, 8, 6, "spec"), (False, 32, 14, "spec"),
+                                                        (False, 8, 6, "seq"), (True, 8, 6, "seq")],
+                         ids=["8dom", "8dom-perturbed", "32dom-14frames", "8dom-seq-relaunch", "8dom-perturbed-seq-relaunch"])
+def test_waves_equal_sequential_drift(monkeypatch, perturb, D, frames, relaunch):
+    """relaunch: the resolve kernel of the rounds after a split -- the speculative one seeded by
+    the fp32 routing simulation (default) or the sequential one (KVC_RELAUNCH=seq); ties are
+    reported by both, so the label exchange is exercised with either."""
+    monkeypatch.setenv("KVC_RELAUNCH", relaunch)
     (seq, wav), outs = _drift_pair(monkeypatch, perturb, D=D, frames=frames)
     ms, mw = seq.maint_stats(), wav.maint_stats()
     assert ms.tolist() == mw.tolist()
