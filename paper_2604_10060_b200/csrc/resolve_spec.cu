@@ -229,34 +229,46 @@ __device__ void simulate_routing(const DevTables& t, SpecSmem& S, const IngestAr
       x[j] = j < q ? static_cast<float>(keyd(S, u, i, bf16)) : 0.f;
     }
     const float nk = static_cast<float>(S.nk[u]);
-    float bs = -INFINITY;
-    long long bk = LLONG_MAX;
-    int bc = -1;
-    for (int k = 0; k < TOPM; ++k) {
-      const int c = S.tm_idx[u * TOPM + k];
-      if (c < 0) break;
-      const int sl = S.cts[c];
-      float v;
-      if (sl >= 0) {
-        float p = 0.f;
+    // lane k < TOPM holds top-M entry k: launch-time value when untouched; the touched ones get
+    // the simulated state's cosine, one warp-wide dot each
+    const int c = lane < TOPM ? S.tm_idx[u * TOPM + lane] : -1;
+    const int csl = c >= 0 ? S.cts[c] : -1;
+    float v = -INFINITY;
+    if (c >= 0 && csl < 0) {
+      const double e = S.tm_ex[u * TOPM + lane];
+      v = isnan(e) ? -INFINITY : static_cast<float>(e);
+    }
+    long long key = c >= 0 ? S.ckey[c] : LLONG_MAX;
+    unsigned tm = __ballot_sync(0xffffffffu, c >= 0 && csl >= 0);
+    while (tm) {
+      const int k = __ffs(tm) - 1;
+      tm &= tm - 1;
+      const int sl = __shfl_sync(0xffffffffu, csl, k);
+      float p = 0.f;
 #pragma unroll
-        for (int j = 0; j < 8; ++j)
-          if (j < q) p = fmaf(x[j], rep[sl * d + lane + 32 * j], p);
+      for (int j = 0; j < 8; ++j)
+        if (j < q) p = fmaf(x[j], rep[sl * d + lane + 32 * j], p);
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) p += __shfl_xor_sync(0xffffffffu, p, o);
-        v = p / (nk * rn[sl]);
-      } else {
-        const double e = S.tm_ex[u * TOPM + k];
-        v = isnan(e) ? -INFINITY : static_cast<float>(e);
-      }
-      const long long key = S.ckey[c];
-      if (v > bs || (v == bs && key < bk)) {
-        bs = v;
-        bk = key;
-        bc = c;
+      for (int o = 16; o > 0; o >>= 1) p += __shfl_xor_sync(0xffffffffu, p, o);
+      if (lane == k) v = p / (nk * rn[sl]);
+    }
+    // arg-best over the top-M lanes (value desc, key asc)
+    float bs = v;
+    long long bk = key;
+    int bc = c;
+#pragma unroll
+    for (int o = 4; o > 0; o >>= 1) {
+      const float so = __shfl_xor_sync(0xffffffffu, bs, o);
+      const long long ko = __shfl_xor_sync(0xffffffffu, bk, o);
+      const int co = __shfl_xor_sync(0xffffffffu, bc, o);
+      if (so > bs || (so == bs && ko < bk)) {
+        bs = so;
+        bk = ko;
+        bc = co;
       }
     }
-    if (bc < 0) return;  // no proposal past here: the launch-time speculation stays
+    bc = __shfl_sync(0xffffffffu, bc, 0);
+    if (bc < 0 || __shfl_sync(0xffffffffu, bs, 0) == -INFINITY) return;  // no proposal past here
     if (lane == 0) S.win[u] = static_cast<int16_t>(bc);
     int sl = S.cts[bc];
     if (sl < 0 && used < slots) {  // the winner's launch-time state into a slot
