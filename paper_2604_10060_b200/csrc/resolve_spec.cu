@@ -271,6 +271,7 @@ __device__ void simulate_routing(const DevTables& t, SpecSmem& S, const IngestAr
     if (bc < 0 || __shfl_sync(0xffffffffu, bs, 0) == -INFINITY) return;  // no proposal past here
     if (lane == 0) S.win[u] = static_cast<int16_t>(bc);
     int sl = S.cts[bc];
+    __syncwarp();  // every lane read the map before lane 0 may rewrite it (racecheck: WAR)
     if (sl < 0 && used < slots) {  // the winner's launch-time state into a slot
       sl = used++;
       const int64_t sg = S.cslot[bc];
@@ -305,6 +306,7 @@ __device__ void simulate_routing(const DevTables& t, SpecSmem& S, const IngestAr
         }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+      __syncwarp();  // (every lane read cnt[sl] above)
       if (lane == 0) {
         rn[sl] = sqrtf(ss);
         cnt[sl] = n + 1.f;
