@@ -1534,12 +1534,23 @@ void Context::append_runs_idx(const std::vector<AppendRun>& runs, const std::vec
 // device view (including a frame being ingested, whose slot already replaced the oldest window
 // frame), so lookups go through ring_frame_, not the reference-order window_.
 void Context::ring_owner_patch(int layer, const std::vector<Member>& ids, std::int32_t slot) {
-  for (const Member& m : ids)
+  // only members of the few window frames matter: one range test rejects the others
+  std::int64_t lo = INT64_MAX, hi = INT64_MIN;
+  for (int rs = 0; rs < t_.W; ++rs) {
+    const RingFrame& rf = ring_frame_[static_cast<std::size_t>(rs)];
+    if (rf.T <= 0) continue;
+    lo = std::min(lo, rf.frame_id);
+    hi = std::max(hi, rf.frame_id);
+  }
+  if (lo > hi) return;
+  for (const Member& m : ids) {
+    if (m.frame < lo || m.frame > hi) continue;
     for (int rs = 0; rs < t_.W; ++rs) {
       const RingFrame& rf = ring_frame_[static_cast<std::size_t>(rs)];
       if (rf.frame_id == m.frame && m.token < rf.T)
         ring_owner_h_[(static_cast<std::size_t>(layer) * t_.W + rs) * t_.tmax + m.token] = slot;
     }
+  }
 }
 
 void Context::ring_owner_upload(int layer) {

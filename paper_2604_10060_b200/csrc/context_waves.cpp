@@ -1252,6 +1252,7 @@ void Context::run_inserts_waves(std::int64_t frame_id, std::int64_t pid, int T, 
     replay_runs(l, frame_id, T, t, T, assigned);
   }
   frame_add_flush(frame_id);
+  const auto c1 = clk::now();
   // device: final ids, released parents, final partition lists, window-ring owners
   std::vector<std::int32_t> plrec, ploff;
   for (int l = 0; l < L_; ++l) {
@@ -1265,6 +1266,7 @@ void Context::run_inserts_waves(std::int64_t frame_id, std::int64_t pid, int T, 
     plrec.push_back(static_cast<std::int32_t>(ids.size()));
     for (std::int64_t id : ids) plrec.push_back(C(id).slot);
   }
+  const auto c2 = clk::now();
   W.up.reset();
   const std::size_t o_c = W.up.add(cids.data(), cids.size() * sizeof(SlotCid));
   const std::size_t o_f = W.up.add(parents.data(), parents.size() * 4);
@@ -1278,9 +1280,17 @@ void Context::run_inserts_waves(std::int64_t frame_id, std::int64_t pid, int T, 
                                  static_cast<std::int32_t>(ploff.size()), st_);
   KVC_CUDA(cudaMemcpyAsync(t_.ring_owner, db + o_o, ring_owner_h_.size() * 4, cudaMemcpyDeviceToDevice, st_));
   for (std::int32_t s : parents) free_slots_.push_back(s);
+  const auto c3 = clk::now();
   sync();  // the upload staging is reused by the next frame
   (void)ring_slot;
   const double t_commit = us(c0, clk::now());
+  if (waves_log_)
+    std::fprintf(stderr, "[waves] commit us: replay %.0f lists %.0f upload %.0f sync %.0f\n", us(c0, c1), us(c1, c2), us(c2, c3),
+                 us(c3, clk::now()));
+  if (waves_log_)
+    std::fprintf(stderr, "[waves] frame %lld times us: stage %.0f kmeans %.0f stats %.0f install %.0f relaunch %.0f verify %.0f commit %.0f total %.0f\n",
+                 static_cast<long long>(frame_id), t_stage, t_km, t_stats, t_inst, t_relaunch, t_verify, t_commit,
+                 us(t_start, clk::now()));
   W.st[6] += t_stage;
   W.st[8] += t_km;
   W.st[9] += t_stats + t_inst;
