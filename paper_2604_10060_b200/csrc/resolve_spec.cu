@@ -221,13 +221,17 @@ __device__ void simulate_routing(const DevTables& t, SpecSmem& S, const IngestAr
   for (int c = lane; c < nl; c += 32) S.cts[c] = -1;           // candidate -> slot
   __syncwarp();
   int used = 0;
-  for (int u = 0; u < Tl; ++u) {
-    float x[8];
+  // the winner's updated state against the NEXT token, reduced together with its norm (one
+  // butterfly instead of two when consecutive tokens meet the same cluster)
+  int pre_sl = -1;
+  float pre_dot = 0.f;
+  float x[8];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int i = lane + 32 * j;
-      x[j] = j < q ? static_cast<float>(keyd(S, u, i, bf16)) : 0.f;
-    }
+  for (int j = 0; j < 8; ++j) x[j] = j < q ? static_cast<float>(keyd(S, 0, lane + 32 * j, bf16)) : 0.f;
+  for (int u = 0; u < Tl; ++u) {
+    float xn[8];  // the next token's elements (for the fused reduction below)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) xn[j] = (j < q && u + 1 < Tl) ? static_cast<float>(keyd(S, u + 1, lane + 32 * j, bf16)) : 0.f;
     const float nk = static_cast<float>(S.nk[u]);
     // lane k < TOPM holds top-M entry k: launch-time value when untouched; the touched ones get
     // the simulated state's cosine, one warp-wide dot each
@@ -239,7 +243,8 @@ __device__ void simulate_routing(const DevTables& t, SpecSmem& S, const IngestAr
       v = isnan(e) ? -INFINITY : static_cast<float>(e);
     }
     long long key = c >= 0 ? S.ckey[c] : LLONG_MAX;
-    unsigned tm = __ballot_sync(0xffffffffu, c >= 0 && csl >= 0);
+    if (c >= 0 && csl >= 0 && csl == pre_sl) v = pre_dot / (nk * rn[csl]);
+    unsigned tm = __ballot_sync(0xffffffffu, c >= 0 && csl >= 0 && csl != pre_sl);
     while (tm) {
       const int k = __ffs(tm) - 1;
       tm &= tm - 1;
@@ -293,9 +298,10 @@ __device__ void simulate_routing(const DevTables& t, SpecSmem& S, const IngestAr
       }
     }
     __syncwarp();
+    pre_sl = -1;
     if (sl >= 0) {  // Eq. 3 in fp32: r' = (n r + k) / (n + 1)
       const float n = cnt[sl], inv = 1.f / (n + 1.f);
-      float ss = 0.f;
+      float ss = 0.f, pn = 0.f;
 #pragma unroll
       for (int j = 0; j < 8; ++j)
         if (j < q) {
@@ -303,16 +309,24 @@ __device__ void simulate_routing(const DevTables& t, SpecSmem& S, const IngestAr
           const float r = (n * rep[sl * d + i] + x[j]) * inv;
           rep[sl * d + i] = r;
           ss = fmaf(r, r, ss);
+          pn = fmaf(xn[j], r, pn);
         }
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+      for (int o = 16; o > 0; o >>= 1) {
+        ss += __shfl_xor_sync(0xffffffffu, ss, o);
+        pn += __shfl_xor_sync(0xffffffffu, pn, o);
+      }
       __syncwarp();  // (every lane read cnt[sl] above)
       if (lane == 0) {
         rn[sl] = sqrtf(ss);
         cnt[sl] = n + 1.f;
       }
+      pre_sl = sl;
+      pre_dot = pn;
     }
     __syncwarp();
+#pragma unroll
+    for (int j = 0; j < 8; ++j) x[j] = xn[j];
   }
 }
 
