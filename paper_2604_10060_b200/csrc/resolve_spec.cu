@@ -1039,9 +1039,12 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve_spec(DevTables t, Ing
           lowW = exw;
         } else if (wknown) {
           lowW = exw;
-        } else if (w_touched && delta_max(w) > move_approx) {
+        } else if (w_touched && delta_max(w) > move_approx &&
+                   (a.exact_all || !(static_cast<double>(S.tm_next[u]) + margin <
+                                     (inw ? exw : static_cast<double>(arow[w]) - margin) - delta_max(w)))) {
           // its state moved far (a fresh child after a split): the warp-parallel value less its
-          // bound, instead of the movement bound
+          // bound, instead of the movement bound (first rounds: only when the movement bound is
+          // too loose to confine the candidates to the top-M list)
           const double ap = approx_at(w, u, last_change(w, u));
           lowW = isnan(ap) ? -INFINITY : ap - kApproxEps;
         } else {
