@@ -432,10 +432,48 @@ __device__ __forceinline__ void split_two_body(const float* rows, const int32_t*
     if (wj >= 0) S.cent[wj][wc] = newc;
     __syncthreads();
     SPROF(4)
-    centroid_norms(S, d);
-    __syncthreads();
-    SPROF(5)
-    cosines(ut, n, d, S, sc);
+    if (n < SPT) {
+      // an idle thread forms both centroid norms (two interleaved sequential chains) while the
+      // point threads form their dots; the cosines divide once both are there
+      double a0 = 0.0, b0 = 0.0;
+      if (tid == SPT - 1) {
+        double s0 = 0.0, s1 = 0.0;
+        for (int k = 0; k < d; ++k) {
+          s0 = dadd(s0, dmul(S.cent[0][k], S.cent[0][k]));
+          s1 = dadd(s1, dmul(S.cent[1][k], S.cent[1][k]));
+        }
+        S.cn[0] = __dsqrt_rn(s0);
+        S.cn[1] = __dsqrt_rn(s1);
+      } else if (tid < n) {
+        int c = 0;
+        for (; c + 16 <= d; c += 16) {
+          double x0[16];
+#pragma unroll
+          for (int k = 0; k < 16; ++k) x0[k] = ut[static_cast<int64_t>(c + k) * n + tid];
+#pragma unroll
+          for (int k = 0; k < 16; ++k) {
+            a0 = dadd(a0, dmul(x0[k], S.cent[0][c + k]));
+            b0 = dadd(b0, dmul(x0[k], S.cent[1][c + k]));
+          }
+        }
+        for (; c < d; ++c) {
+          const double x0 = ut[static_cast<int64_t>(c) * n + tid];
+          a0 = dadd(a0, dmul(x0, S.cent[0][c]));
+          b0 = dadd(b0, dmul(x0, S.cent[1][c]));
+        }
+      }
+      __syncthreads();
+      SPROF(5)
+      if (tid < n) {
+        sc[tid] = cos_of(a0, S.cn[0]);
+        sc[n + tid] = cos_of(b0, S.cn[1]);
+      }
+    } else {
+      centroid_norms(S, d);
+      __syncthreads();
+      SPROF(5)
+      cosines(ut, n, d, S, sc);
+    }
     __syncthreads();
     SPROF(6)
     // mean cosine to the own centroid, summed in point order (clustering.cpp:152-163)
